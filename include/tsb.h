@@ -1,0 +1,223 @@
+/*
+ * tsb.h -- C ABI of the B200-native C-ToF Gaussian-splat render/optimise path.
+ *
+ * This is the drop-in boundary that replaces the reference "tofsplat" hot path
+ * (/root/reference/proj, a CPU C++20/Eigen library).  Every entry point names
+ * the reference interface it replaces.  Plain pointers and sizes only; no
+ * torch / Eigen / STL types cross it.  All device work is issued on the
+ * context's CUDA stream; functions return TSB_OK or an error code and set a
+ * thread-local message (tsb_last_error) -- the C++ shell in
+ * include/tofsplat_b200/splat.hpp rethrows it as std::runtime_error with the
+ * reference's messages (splat.cpp:91-100).
+ *
+ * There is no CPU fallback: if no sm_100 device is present, tsb_ctx_create
+ * fails with TSB_ERR_CUDA.
+ *
+ * Data layouts (reference -> here):
+ *   Gaussian parameters (scene.hpp:23-38, 75 doubles AoS) -> fp32 SoA arrays
+ *     position 3n, log_scale 3n, rotation 4n (w,x,y,z), opacity_logit n,
+ *     reflectivity_dc n (= reflectivity_sh[0]; sh_degree 0),
+ *     motion 3n per keyframe (the per-Gaussian keyframe offsets that stand in for
+ *     the DeformNet tick offsets, trainer.cpp:259-279 / SURVEY.md App. B).
+ *     "3n" means 3 x n column-major == Eigen::Matrix3Xd storage.
+ *   Image (image.hpp:12-38, planar channel-major double) -> planar fp32 [C][H][W].
+ *   SceneGrads (splat.hpp:79-92) -> fp32 arrays with the same shapes as the params.
+ */
+#ifndef TSB_H
+#define TSB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSB_ABI_VERSION 1
+
+enum {
+    TSB_OK = 0,
+    TSB_ERR_INVALID = 1,     /* bad argument (reference: std::runtime_error) */
+    TSB_ERR_CUDA = 2,        /* CUDA runtime failure / no device */
+    TSB_ERR_NOMEM = 3,       /* device allocation failed */
+    TSB_ERR_UNSUPPORTED = 4, /* valid reference input this build does not handle */
+    TSB_ERR_NCCL = 5
+};
+
+/* Where a pointer argument lives. */
+enum { TSB_HOST = 0, TSB_DEVICE = 1 };
+
+/* Output channel bits (RenderChannels, splat.hpp:13-20). */
+enum {
+    TSB_CH_QUAD = 1u << 0,      /* 4 raw samples per modulation frequency */
+    TSB_CH_DEPTH = 1u << 1,     /* depth_raw and depth */
+    TSB_CH_WEIGHT = 1u << 2,    /* weight (= alpha, sum_k w_k); always computed */
+    TSB_CH_TRANSM = 1u << 3,    /* transmittance T_N; always computed */
+    TSB_CH_COUNTS = 1u << 4     /* per-pixel n_contrib / n_processed (parity) */
+};
+
+/* CameraModel (camera.hpp:9-17).  R row-major; p_cam = R p_world + t. */
+typedef struct {
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    double near_plane, far_plane;
+    double R[9];
+    double t[3];
+} tsb_camera;
+
+/* RenderOptions + Backgrounds (splat.hpp:22-37).  bg_quad holds 4 values per
+ * modulation frequency. */
+typedef struct {
+    double alpha_threshold;     /* 1/255 */
+    double transmittance_floor; /* 1e-4 */
+    double dilation;            /* 0.3 px^2 */
+    double sigma_cutoff;        /* 3 */
+    double coverage_eps;        /* 1e-12 */
+    int32_t tile_size;          /* 16 */
+    uint32_t channels;          /* TSB_CH_* */
+    double bg_quad[8];
+} tsb_render_options;
+
+/* CanonicalScene header (scene.hpp:44-52) + ToFConfig (tof.hpp:13-21).
+ * n_freq = 2 renders two quads that share geometry (the
+ * oracle for that is two reference renders with different frequencies). */
+typedef struct {
+    int32_t n;            /* Gaussians */
+    int32_t n_keyframes;  /* 0 = static; else >= 2 keyframe offsets per Gaussian */
+    int32_t sh_degree;    /* 0 (view-independent reflectivity) */
+    int32_t n_freq;       /* 1 or 2 */
+    double frequency[2];  /* Hz */
+    double source_intensity;
+    double speed_of_light;
+} tsb_scene_desc;
+
+/* Frame selector for dynamic scenes: rendered mean = (1-w)(x + d_k) + w (x + d_{k+1})
+ * (trainer.cpp:279); w == 0 renders x + d_k exactly (trainer.cpp:278). */
+typedef struct {
+    int32_t key;  /* k in [0, n_keyframes-2] */
+    int32_t _pad;
+    double w;     /* in [0, 1] */
+} tsb_frame;
+
+typedef struct tsb_ctx tsb_ctx;
+typedef struct tsb_scene tsb_scene;
+typedef struct tsb_pass tsb_pass;
+typedef struct tsb_comm tsb_comm;
+
+/* ---- context ------------------------------------------------------------ */
+const char* tsb_last_error(void);
+int tsb_abi_version(void);
+/* One context per (host thread, GPU): owns a CUDA stream. */
+int tsb_ctx_create(int device, tsb_ctx** out);
+void tsb_ctx_destroy(tsb_ctx* ctx);
+int tsb_ctx_synchronize(tsb_ctx* ctx);
+/* The context's cudaStream_t (as void*), for callers that time on it. */
+void* tsb_ctx_stream(tsb_ctx* ctx);
+/* Number of kernels this context has launched (bench.py gpu_launches). */
+int64_t tsb_ctx_launch_count(tsb_ctx* ctx);
+
+/* ---- scene: parameters, gradients, Adam state (trainer.cpp:63-132) ------- */
+int tsb_scene_create(tsb_ctx* ctx, const tsb_scene_desc* desc, tsb_scene** out);
+void tsb_scene_destroy(tsb_scene* s);
+/* Upload parameters (replaces Params::from_scene / to_scene, trainer.cpp:70-104).
+ * motion: n_keyframes * 3n floats (keyframe-major), may be NULL when static. */
+int tsb_scene_set_params(tsb_scene* s, int where, const float* position, const float* log_scale,
+                         const float* rotation, const float* opacity_logit,
+                         const float* reflectivity_dc, const float* motion);
+int tsb_scene_get_params(tsb_scene* s, float* position, float* log_scale, float* rotation,
+                         float* opacity_logit, float* reflectivity_dc, float* motion);
+/* Accumulated gradients (GroupGrads, trainer.cpp:107-132).  d_position is the
+ * gradient w.r.t. the canonical mean (trainer.cpp:329-331); d_motion per keyframe.
+ * d_bg_quad: 4 per frequency (SceneGrads::d_bg_quad); loss: summed loss. */
+int tsb_scene_get_grads(tsb_scene* s, float* d_position, float* d_log_scale, float* d_rotation,
+                        float* d_opacity_logit, float* d_reflectivity_dc, float* d_motion,
+                        double* d_bg_quad, double* loss);
+int tsb_scene_zero_grads(tsb_scene* s);
+/* Adam moments (AdamState m_/v_, trainer.cpp:18-31), same layout as the params. */
+int tsb_scene_get_adam_state(tsb_scene* s, float* m_position, float* v_position);
+/* Densification statistic sum_i ||dL/dx_canon,i|| (trainer.cpp:381-384), n floats. */
+int tsb_scene_get_densify_stat(tsb_scene* s, float* grad_norm_sum, int64_t* count);
+
+/* Learning rates per parameter group (LrTable, trainer.hpp:36-44 resolved the
+ * way fit() does, trainer.cpp:339-366). */
+typedef struct {
+    double position, log_scale, rotation, opacity, reflectivity, motion;
+    double beta1, beta2, eps; /* AdamParams, trainer.hpp:14-18 */
+} tsb_adam_config;
+/* One fused AdamState::step over every group (trainer.cpp:18-31, 339-366) +
+ * densify statistic (trainer.cpp:381-384); clears the gradients afterwards. */
+int tsb_scene_adam_step(tsb_scene* s, const tsb_adam_config* cfg);
+
+/* ---- render pass (RenderPass, splat.hpp:97-117) ------------------------- */
+/* A pass is a reusable per-frame workspace: prepare() == the RenderPass ctor
+ * (prepare + depth sort + build_tiles, splat.cpp:90-200). */
+int tsb_pass_create(tsb_ctx* ctx, tsb_pass** out);
+void tsb_pass_destroy(tsb_pass* p);
+int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam,
+                     const tsb_render_options* opt, const tsb_frame* frame);
+/* RenderPass::visible_count (splat.hpp:108). */
+int tsb_pass_visible_count(tsb_pass* p, int32_t* out);
+int tsb_pass_num_keys(tsb_pass* p, int64_t* out);
+
+/* RenderPass::forward (splat.cpp:209-339).  Results stay in pass-owned device
+ * buffers (tsb_pass_output).  With a target bound (planar [4*n_freq][H][W]
+ * fp32, `where` = TSB_HOST/TSB_DEVICE), the forward epilogue also evaluates
+ * sum_c channel_weight[c] * mse(quad_c, target_c) (losses.cpp:9-25,
+ * trainer.cpp:210-219) and writes d_quad for the backward pass. */
+int tsb_pass_forward(tsb_pass* p);
+int tsb_pass_forward_loss(tsb_pass* p, int where, const float* target,
+                          const double* channel_weight /* 4*n_freq */, double* loss_out /* may be NULL: no sync */);
+
+enum {
+    TSB_OUT_QUAD = 0,      /* [4*n_freq][H][W] f32 */
+    TSB_OUT_DEPTH_RAW = 1, /* [H][W] f32 */
+    TSB_OUT_DEPTH = 2,     /* [H][W] f32 (NaN where weight <= coverage_eps) */
+    TSB_OUT_WEIGHT = 3,    /* [H][W] f32 */
+    TSB_OUT_TRANSM = 4,    /* [H][W] f32 */
+    TSB_OUT_N_CONTRIB = 5, /* [H][W] i32 */
+    TSB_OUT_N_PROCESSED = 6, /* [H][W] i32 */
+    TSB_OUT_D_QUAD = 7     /* [4*n_freq][H][W] f32 upstream gradient */
+};
+/* Device pointer and byte size of a pass-owned buffer. */
+int tsb_pass_output(tsb_pass* p, int which, void** dptr, size_t* bytes);
+/* Copy a pass-owned buffer to host memory (synchronous). */
+int tsb_pass_download(tsb_pass* p, int which, void* host, size_t bytes);
+
+/* RenderPass::backward (splat.cpp:347-650) for the quad channel.  d_quad: NULL
+ * uses the loss residual written by tsb_pass_forward_loss, else an upstream
+ * image [4*n_freq][H][W] (`where`).  Gradients are ACCUMULATED into the scene
+ * (GroupGrads::add + trajectory chain, trainer.cpp:256, 312-331). */
+int tsb_pass_backward(tsb_pass* p, int where, const float* d_quad);
+
+/* Parity / diagnostics: integer intermediates the reference keeps private
+ * (splat.cpp:86-87).  Sizes: gidx V, rect 4V (x0,x1,y0,y1 per rank), tiles+1
+ * offsets, K ids (indices into the prepared order). */
+int tsb_pass_debug_prepared(tsb_pass* p, int32_t* gidx, int32_t* rect);
+int tsb_pass_debug_tiles(tsb_pass* p, int32_t* tiles_x, int32_t* tiles_y, int64_t* offsets,
+                         int32_t* ids);
+/* fp32 per-rank raster records (mean x/y, conic a/b/c, opacity, coef, depth,
+ * sin/cos per frequency) and per-rank screen-space gradients after backward
+ * (8 floats: d_mean2d x,y, d_conic a,b,c, d_opacity, d_coef, d_depth). */
+int tsb_pass_debug_records(tsb_pass* p, float* rec12 /* 12 per rank */);
+int tsb_pass_debug_screen_grads(tsb_pass* p, float* g8 /* 8 per rank */);
+/* Pixels the fp32 raster flagged as decision-ambiguous and recomposited in fp64. */
+int tsb_pass_debug_fixups(tsb_pass* p, int32_t* count);
+
+/* ---- data-parallel gradient reduction (trainer.cpp:123-131 -> NCCL) ----- */
+int tsb_comm_unique_id(void* out /* 128 bytes */);
+int tsb_comm_create(tsb_ctx* ctx, const void* unique_id, int nranks, int rank, tsb_comm** out);
+void tsb_comm_destroy(tsb_comm* c);
+/* In-place sum of the scene's gradient buffer (+ bg grads + loss) across ranks. */
+int tsb_scene_allreduce_grads(tsb_scene* s, tsb_comm* c);
+
+/* ---- small host helpers mirroring the Python _core surface --------------- */
+/* unambiguous_range (tof.hpp:36-38), quad_to_depth (tof.hpp:59-65),
+ * quad_basis (tof.hpp:75-79); frequency <= 0 uses the default sensor. */
+double tsb_unambiguous_range(double frequency);
+double tsb_quad_to_depth(double q0, double q90, double q180, double q270, double frequency);
+void tsb_quad_basis(double depth, double frequency, double* out4);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSB_H */

@@ -1,0 +1,969 @@
+// C-ABI implementation (include/tsb.h): contexts, device scenes, reusable
+// render-pass workspaces, fused Adam, NCCL gradient reduction.
+//
+// Host code only; every device operation is stream-ordered on the context's
+// stream.  tsb_pass_prepare synchronises once per frame to learn the number of
+// tile keys (the CUB radix sort needs it on the host).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "tsb_internal.h"
+
+using namespace tsb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define TSB_CUDA(expr)                                                                      \
+    do {                                                                                    \
+        cudaError_t e_ = (expr);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(e_ == cudaErrorMemoryAllocation ? TSB_ERR_NOMEM : TSB_ERR_CUDA,     \
+                        std::string(#expr) + ": " + cudaGetErrorString(e_));                \
+    } while (0)
+
+#define TSB_CHECK_LAUNCH()                                                                  \
+    do {                                                                                    \
+        cudaError_t e_ = cudaGetLastError();                                                \
+        if (e_ != cudaSuccess) return fail(TSB_ERR_CUDA, std::string("kernel launch: ") +  \
+                                                             cudaGetErrorString(e_));       \
+    } while (0)
+
+template <typename T>
+int dev_alloc(T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+    if (e != cudaSuccess) return fail(TSB_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    return TSB_OK;
+}
+
+template <typename T>
+void dev_free(T*& p) {
+    if (p) cudaFree((void*)p);
+    p = nullptr;
+}
+
+}  // namespace
+
+struct tsb_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+    void* pinned = nullptr;  // small pinned staging (K, V readback)
+};
+
+struct tsb_scene {
+    tsb_ctx* ctx = nullptr;
+    tsb_scene_desc d{};
+    int narrays = 0;
+    float4* params = nullptr;
+    float4* grads = nullptr;
+    float4* m = nullptr;
+    float4* v = nullptr;
+    float* densify = nullptr;
+    double* stats = nullptr;  // [0..7] d_bg_quad, [8] loss
+    float* staging = nullptr; // 4n floats for host<->device (un)packing
+    int64_t step = 0;
+    int64_t densify_count = 0;
+};
+
+struct tsb_pass {
+    tsb_ctx* ctx = nullptr;
+    tsb_scene* scene = nullptr;
+    CamK cam{};
+    OptK opt{};
+    FrameK frame{};
+    uint32_t channels = 0;
+    int nf = 1, W = 0, H = 0, ntiles = 0, nblocks = 0;
+    bool prepared = false, forwarded = false, have_loss = false;
+    int32_t V = 0;
+    int64_t K = 0;
+    // capacities
+    int n_cap = 0, px_cap = 0, blk_cap = 0, tiles_cap = 0;
+    int64_t k_cap = 0;
+    size_t temp_bytes = 0;
+    // per Gaussian
+    uint64_t *key_a = nullptr, *key_b = nullptr;
+    uint32_t *gidx_a = nullptr, *gidx_b = nullptr;
+    uint32_t *touched = nullptr, *cnt_sorted = nullptr, *offsets = nullptr;
+    uint2* rect = nullptr;
+    RecK rec{};
+    float* screen = nullptr;  // [8][n]
+    // per key
+    uint16_t *tkey_a = nullptr, *tkey_b = nullptr;
+    uint32_t *tval_a = nullptr, *tval_b = nullptr;
+    uint2* ranges = nullptr;
+    // per pixel
+    float* out = nullptr;
+    int32_t *n_contrib = nullptr, *n_processed = nullptr, *last = nullptr;
+    float* T_pre = nullptr;
+    float* d_quad = nullptr;
+    float* target = nullptr;
+    int32_t* flagged = nullptr;
+    // misc
+    int32_t* counters = nullptr;  // [0] n_visible, [1] n_flagged
+    double* loss_part = nullptr;
+    double* bg_part = nullptr;
+    double* loss_dev = nullptr;
+    float* chw = nullptr;
+    void* temp = nullptr;
+};
+
+extern "C" {
+
+const char* tsb_last_error(void) { return g_err.c_str(); }
+int tsb_abi_version(void) { return TSB_ABI_VERSION; }
+
+int tsb_ctx_create(int device, tsb_ctx** out) {
+    if (!out) return fail(TSB_ERR_INVALID, "tsb_ctx_create: out is null");
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return fail(TSB_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= count) return fail(TSB_ERR_INVALID, "tsb_ctx_create: bad device index");
+    cudaDeviceProp prop;
+    TSB_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        return fail(TSB_ERR_CUDA, "tsb_ctx_create: device is not sm_100 (B200); this build has no other path");
+    TSB_CUDA(cudaSetDevice(device));
+    tsb_ctx* c = new tsb_ctx();
+    c->device = device;
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(TSB_ERR_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+    }
+    e = cudaMallocHost(&c->pinned, 4096);
+    if (e != cudaSuccess) {
+        cudaStreamDestroy(c->stream);
+        delete c;
+        return fail(TSB_ERR_NOMEM, "cudaMallocHost failed");
+    }
+    *out = c;
+    return TSB_OK;
+}
+
+void tsb_ctx_destroy(tsb_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    cudaFreeHost(c->pinned);
+    cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+int tsb_ctx_synchronize(tsb_ctx* c) {
+    if (!c) return fail(TSB_ERR_INVALID, "null context");
+    TSB_CUDA(cudaStreamSynchronize(c->stream));
+    return TSB_OK;
+}
+
+void* tsb_ctx_stream(tsb_ctx* c) { return c ? (void*)c->stream : nullptr; }
+int64_t tsb_ctx_launch_count(tsb_ctx* c) { return c ? c->launches : 0; }
+
+// ---------------------------------------------------------------------------
+// scene
+// ---------------------------------------------------------------------------
+int tsb_scene_create(tsb_ctx* ctx, const tsb_scene_desc* d, tsb_scene** out) {
+    if (!ctx || !d || !out) return fail(TSB_ERR_INVALID, "tsb_scene_create: null argument");
+    *out = nullptr;
+    if (d->n < 0) return fail(TSB_ERR_INVALID, "scene: negative Gaussian count");
+    if (d->n_keyframes < 0 || d->n_keyframes == 1 || d->n_keyframes > kMaxKeyframes)
+        return fail(TSB_ERR_INVALID, "scene: n_keyframes must be 0 or in [2, 16]");
+    if (d->sh_degree < 0 || d->sh_degree > 3) return fail(TSB_ERR_INVALID, "scene: sh_degree must be in [0, 3]");
+    if (d->sh_degree != 0)
+        return fail(TSB_ERR_UNSUPPORTED, "scene: only sh_degree 0 reflectivity is implemented on the B200 path");
+    if (d->n_freq < 1 || d->n_freq > 2) return fail(TSB_ERR_INVALID, "scene: n_freq must be 1 or 2");
+    for (int f = 0; f < d->n_freq; ++f)
+        if (!(d->frequency[f] > 0.0)) return fail(TSB_ERR_INVALID, "scene: modulation frequency must be > 0");
+    if (!(d->source_intensity > 0.0) || !(d->speed_of_light > 0.0))
+        return fail(TSB_ERR_INVALID, "scene: invalid ToF config");
+    TSB_CUDA(cudaSetDevice(ctx->device));
+    tsb_scene* s = new tsb_scene();
+    s->ctx = ctx;
+    s->d = *d;
+    s->narrays = 3 + d->n_keyframes;
+    const size_t nel = (size_t)s->narrays * (size_t)std::max(d->n, 1);
+    int rc = TSB_OK;
+    if ((rc = dev_alloc(&s->params, nel)) || (rc = dev_alloc(&s->grads, nel)) || (rc = dev_alloc(&s->m, nel)) ||
+        (rc = dev_alloc(&s->v, nel)) || (rc = dev_alloc(&s->densify, (size_t)std::max(d->n, 1))) ||
+        (rc = dev_alloc(&s->stats, 9)) || (rc = dev_alloc(&s->staging, 4 * (size_t)std::max(d->n, 1)))) {
+        tsb_scene_destroy(s);
+        return rc;
+    }
+    cudaStream_t st = ctx->stream;
+    cudaMemsetAsync(s->params, 0, nel * sizeof(float4), st);
+    cudaMemsetAsync(s->grads, 0, nel * sizeof(float4), st);
+    cudaMemsetAsync(s->m, 0, nel * sizeof(float4), st);
+    cudaMemsetAsync(s->v, 0, nel * sizeof(float4), st);
+    cudaMemsetAsync(s->densify, 0, sizeof(float) * std::max(d->n, 1), st);
+    cudaMemsetAsync(s->stats, 0, sizeof(double) * 9, st);
+    TSB_CUDA(cudaStreamSynchronize(st));
+    *out = s;
+    return TSB_OK;
+}
+
+void tsb_scene_destroy(tsb_scene* s) {
+    if (!s) return;
+    cudaSetDevice(s->ctx->device);
+    cudaStreamSynchronize(s->ctx->stream);
+    dev_free(s->params);
+    dev_free(s->grads);
+    dev_free(s->m);
+    dev_free(s->v);
+    dev_free(s->densify);
+    dev_free(s->stats);
+    dev_free(s->staging);
+    delete s;
+}
+
+namespace {
+
+// Pack one SoA parameter array (comps floats per Gaussian) into lanes
+// comp0..comp0+comps-1 of float4 array `dst`.
+int pack_one(tsb_scene* s, float4* dst, const float* src, int where, int comps, int comp0) {
+    const int n = s->d.n;
+    if (n == 0 || !src) return TSB_OK;
+    cudaStream_t st = s->ctx->stream;
+    const float* dsrc = src;
+    if (where == TSB_HOST) {
+        TSB_CUDA(cudaMemcpyAsync(s->staging, src, sizeof(float) * comps * (size_t)n, cudaMemcpyHostToDevice, st));
+        dsrc = s->staging;
+    }
+    launch_pack_params(dst, dsrc, n, comps, comp0, 4, st);
+    s->ctx->launches++;
+    TSB_CHECK_LAUNCH();
+    if (where == TSB_HOST) TSB_CUDA(cudaStreamSynchronize(st));  // staging reuse
+    return TSB_OK;
+}
+
+int unpack_one(tsb_scene* s, const float4* src, float* host, int comps, int comp0) {
+    const int n = s->d.n;
+    if (n == 0 || !host) return TSB_OK;
+    cudaStream_t st = s->ctx->stream;
+    launch_unpack(src, s->staging, n, comps, comp0, st);
+    s->ctx->launches++;
+    TSB_CHECK_LAUNCH();
+    TSB_CUDA(cudaMemcpyAsync(host, s->staging, sizeof(float) * comps * (size_t)n, cudaMemcpyDeviceToHost, st));
+    TSB_CUDA(cudaStreamSynchronize(st));
+    return TSB_OK;
+}
+
+}  // namespace
+
+int tsb_scene_set_params(tsb_scene* s, int where, const float* position, const float* log_scale,
+                         const float* rotation, const float* opacity_logit, const float* reflectivity_dc,
+                         const float* motion) {
+    if (!s) return fail(TSB_ERR_INVALID, "null scene");
+    if (where != TSB_HOST && where != TSB_DEVICE) return fail(TSB_ERR_INVALID, "bad memory kind");
+    TSB_CUDA(cudaSetDevice(s->ctx->device));
+    const int n = s->d.n;
+    int rc;
+    if ((rc = pack_one(s, s->params, position, where, 3, 0))) return rc;
+    if ((rc = pack_one(s, s->params, opacity_logit, where, 1, 3))) return rc;
+    if ((rc = pack_one(s, s->params + n, log_scale, where, 3, 0))) return rc;
+    if ((rc = pack_one(s, s->params + n, reflectivity_dc, where, 1, 3))) return rc;
+    if ((rc = pack_one(s, s->params + 2 * (size_t)n, rotation, where, 4, 0))) return rc;
+    if (motion)
+        for (int k = 0; k < s->d.n_keyframes; ++k)
+            if ((rc = pack_one(s, s->params + (size_t)(3 + k) * n, motion + (size_t)k * 3 * n, where, 3, 0)))
+                return rc;
+    return TSB_OK;
+}
+
+int tsb_scene_get_params(tsb_scene* s, float* position, float* log_scale, float* rotation, float* opacity_logit,
+                         float* reflectivity_dc, float* motion) {
+    if (!s) return fail(TSB_ERR_INVALID, "null scene");
+    TSB_CUDA(cudaSetDevice(s->ctx->device));
+    const int n = s->d.n;
+    int rc;
+    if ((rc = unpack_one(s, s->params, position, 3, 0))) return rc;
+    if ((rc = unpack_one(s, s->params, opacity_logit, 1, 3))) return rc;
+    if ((rc = unpack_one(s, s->params + n, log_scale, 3, 0))) return rc;
+    if ((rc = unpack_one(s, s->params + n, reflectivity_dc, 1, 3))) return rc;
+    if ((rc = unpack_one(s, s->params + 2 * (size_t)n, rotation, 4, 0))) return rc;
+    if (motion)
+        for (int k = 0; k < s->d.n_keyframes; ++k)
+            if ((rc = unpack_one(s, s->params + (size_t)(3 + k) * n, motion + (size_t)k * 3 * n, 3, 0))) return rc;
+    return TSB_OK;
+}
+
+int tsb_scene_get_grads(tsb_scene* s, float* d_position, float* d_log_scale, float* d_rotation,
+                        float* d_opacity_logit, float* d_reflectivity_dc, float* d_motion, double* d_bg_quad,
+                        double* loss) {
+    if (!s) return fail(TSB_ERR_INVALID, "null scene");
+    TSB_CUDA(cudaSetDevice(s->ctx->device));
+    const int n = s->d.n;
+    int rc;
+    if ((rc = unpack_one(s, s->grads, d_position, 3, 0))) return rc;
+    if ((rc = unpack_one(s, s->grads, d_opacity_logit, 1, 3))) return rc;
+    if ((rc = unpack_one(s, s->grads + n, d_log_scale, 3, 0))) return rc;
+    if ((rc = unpack_one(s, s->grads + n, d_reflectivity_dc, 1, 3))) return rc;
+    if ((rc = unpack_one(s, s->grads + 2 * (size_t)n, d_rotation, 4, 0))) return rc;
+    if (d_motion)
+        for (int k = 0; k < s->d.n_keyframes; ++k)
+            if ((rc = unpack_one(s, s->grads + (size_t)(3 + k) * n, d_motion + (size_t)k * 3 * n, 3, 0))) return rc;
+    double st9[9];
+    TSB_CUDA(cudaMemcpyAsync(st9, s->stats, sizeof st9, cudaMemcpyDeviceToHost, s->ctx->stream));
+    TSB_CUDA(cudaStreamSynchronize(s->ctx->stream));
+    if (d_bg_quad) std::memcpy(d_bg_quad, st9, sizeof(double) * 4 * s->d.n_freq);
+    if (loss) *loss = st9[8];
+    return TSB_OK;
+}
+
+int tsb_scene_zero_grads(tsb_scene* s) {
+    if (!s) return fail(TSB_ERR_INVALID, "null scene");
+    TSB_CUDA(cudaSetDevice(s->ctx->device));
+    const size_t nel = (size_t)s->narrays * (size_t)std::max(s->d.n, 1);
+    TSB_CUDA(cudaMemsetAsync(s->grads, 0, nel * sizeof(float4), s->ctx->stream));
+    TSB_CUDA(cudaMemsetAsync(s->stats, 0, sizeof(double) * 9, s->ctx->stream));
+    return TSB_OK;
+}
+
+int tsb_scene_get_adam_state(tsb_scene* s, float* m_position, float* v_position) {
+    if (!s) return fail(TSB_ERR_INVALID, "null scene");
+    int rc;
+    if ((rc = unpack_one(s, s->m, m_position, 3, 0))) return rc;
+    if ((rc = unpack_one(s, s->v, v_position, 3, 0))) return rc;
+    return TSB_OK;
+}
+
+int tsb_scene_get_densify_stat(tsb_scene* s, float* grad_norm_sum, int64_t* count) {
+    if (!s) return fail(TSB_ERR_INVALID, "null scene");
+    TSB_CUDA(cudaSetDevice(s->ctx->device));
+    if (grad_norm_sum && s->d.n > 0) {
+        TSB_CUDA(cudaMemcpyAsync(grad_norm_sum, s->densify, sizeof(float) * s->d.n, cudaMemcpyDeviceToHost,
+                                 s->ctx->stream));
+        TSB_CUDA(cudaStreamSynchronize(s->ctx->stream));
+    }
+    if (count) *count = s->densify_count;
+    return TSB_OK;
+}
+
+int tsb_scene_adam_step(tsb_scene* s, const tsb_adam_config* cfg) {
+    if (!s || !cfg) return fail(TSB_ERR_INVALID, "tsb_scene_adam_step: null argument");
+    TSB_CUDA(cudaSetDevice(s->ctx->device));
+    s->step += 1;
+    const double t = (double)s->step;
+    const double bc1 = 1.0 - std::pow(cfg->beta1, t);
+    const double bc2 = 1.0 - std::pow(cfg->beta2, t);
+    std::vector<double> lr((size_t)s->narrays * 4, 0.0);
+    for (int c = 0; c < 3; ++c) lr[c] = cfg->position;
+    lr[3] = cfg->opacity;
+    for (int c = 0; c < 3; ++c) lr[4 + c] = cfg->log_scale;
+    lr[7] = cfg->reflectivity;
+    for (int c = 0; c < 4; ++c) lr[8 + c] = cfg->rotation;
+    for (int k = 0; k < s->d.n_keyframes; ++k)
+        for (int c = 0; c < 3; ++c) lr[(size_t)(3 + k) * 4 + c] = cfg->motion;
+    launch_adam(s->params, s->grads, s->m, s->v, s->d.n, s->narrays, lr.data(), cfg->beta1, cfg->beta2, cfg->eps,
+                bc1, bc2, s->densify, s->ctx->stream);
+    s->ctx->launches++;
+    TSB_CHECK_LAUNCH();
+    s->densify_count++;
+    TSB_CUDA(cudaMemsetAsync(s->stats, 0, sizeof(double) * 9, s->ctx->stream));
+    return TSB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// render pass
+// ---------------------------------------------------------------------------
+int tsb_pass_create(tsb_ctx* ctx, tsb_pass** out) {
+    if (!ctx || !out) return fail(TSB_ERR_INVALID, "tsb_pass_create: null argument");
+    TSB_CUDA(cudaSetDevice(ctx->device));
+    tsb_pass* p = new tsb_pass();
+    p->ctx = ctx;
+    int rc;
+    if ((rc = dev_alloc(&p->counters, 4)) || (rc = dev_alloc(&p->loss_dev, 1)) || (rc = dev_alloc(&p->chw, 8))) {
+        tsb_pass_destroy(p);
+        return rc;
+    }
+    *out = p;
+    return TSB_OK;
+}
+
+namespace {
+
+void free_gauss(tsb_pass* p) {
+    dev_free(p->key_a); dev_free(p->key_b); dev_free(p->gidx_a); dev_free(p->gidx_b);
+    dev_free(p->touched); dev_free(p->cnt_sorted); dev_free(p->offsets); dev_free(p->rect);
+    dev_free(p->rec.A); dev_free(p->rec.B); dev_free(p->rec.C); dev_free(p->rec.D); dev_free(p->screen);
+}
+void free_keys(tsb_pass* p) {
+    dev_free(p->tkey_a); dev_free(p->tkey_b); dev_free(p->tval_a); dev_free(p->tval_b);
+}
+void free_pixels(tsb_pass* p) {
+    dev_free(p->out); dev_free(p->n_contrib); dev_free(p->n_processed); dev_free(p->last);
+    dev_free(p->T_pre); dev_free(p->d_quad); dev_free(p->target); dev_free(p->flagged);
+}
+
+int ensure_gauss(tsb_pass* p, int n) {
+    if (n <= p->n_cap) return TSB_OK;
+    free_gauss(p);
+    const int cap = std::max(n, 1);
+    int rc;
+    if ((rc = dev_alloc(&p->key_a, cap)) || (rc = dev_alloc(&p->key_b, cap)) || (rc = dev_alloc(&p->gidx_a, cap)) ||
+        (rc = dev_alloc(&p->gidx_b, cap)) || (rc = dev_alloc(&p->touched, cap)) ||
+        (rc = dev_alloc(&p->cnt_sorted, cap)) || (rc = dev_alloc(&p->offsets, cap)) ||
+        (rc = dev_alloc(&p->rect, cap)) || (rc = dev_alloc(&p->rec.A, cap)) || (rc = dev_alloc(&p->rec.B, cap)) ||
+        (rc = dev_alloc(&p->rec.C, cap)) || (rc = dev_alloc(&p->rec.D, cap)) ||
+        (rc = dev_alloc(&p->screen, (size_t)8 * cap)))
+        return rc;
+    TSB_CUDA(cudaMemsetAsync(p->screen, 0, sizeof(float) * 8 * (size_t)cap, p->ctx->stream));
+    p->n_cap = cap;
+    p->temp_bytes = 0;  // recompute temp size
+    return TSB_OK;
+}
+
+int ensure_temp(tsb_pass* p) {
+    const size_t need = binning_temp_bytes(p->n_cap, std::max<int64_t>(p->k_cap, 1));
+    if (need <= p->temp_bytes && p->temp) return TSB_OK;
+    dev_free(p->temp);
+    TSB_CUDA(cudaMalloc(&p->temp, need));
+    p->temp_bytes = need;
+    return TSB_OK;
+}
+
+int ensure_keys(tsb_pass* p, int64_t k) {
+    if (k <= p->k_cap && p->tkey_a) return TSB_OK;
+    free_keys(p);
+    const int64_t cap = std::max<int64_t>((int64_t)(k * 1.25) + 1024, 1);
+    int rc;
+    if ((rc = dev_alloc(&p->tkey_a, cap)) || (rc = dev_alloc(&p->tkey_b, cap)) || (rc = dev_alloc(&p->tval_a, cap)) ||
+        (rc = dev_alloc(&p->tval_b, cap)))
+        return rc;
+    p->k_cap = cap;
+    p->temp_bytes = 0;
+    return TSB_OK;
+}
+
+int ensure_pixels(tsb_pass* p, int W, int H, int nf, int ntiles, int nblocks) {
+    const int npx = W * H;
+    const int nch = out_channels(2);
+    if (npx > p->px_cap) {
+        free_pixels(p);
+        int rc;
+        if ((rc = dev_alloc(&p->out, (size_t)nch * npx)) || (rc = dev_alloc(&p->n_contrib, npx)) ||
+            (rc = dev_alloc(&p->n_processed, npx)) || (rc = dev_alloc(&p->last, npx)) ||
+            (rc = dev_alloc(&p->T_pre, npx)) || (rc = dev_alloc(&p->d_quad, (size_t)8 * npx)) ||
+            (rc = dev_alloc(&p->target, (size_t)8 * npx)) || (rc = dev_alloc(&p->flagged, npx)))
+            return rc;
+        p->px_cap = npx;
+    }
+    if (nblocks > p->blk_cap) {
+        dev_free(p->loss_part);
+        dev_free(p->bg_part);
+        int rc;
+        if ((rc = dev_alloc(&p->loss_part, nblocks)) || (rc = dev_alloc(&p->bg_part, (size_t)8 * nblocks))) return rc;
+        p->blk_cap = nblocks;
+    }
+    if (ntiles > p->tiles_cap) {
+        dev_free(p->ranges);
+        int rc;
+        if ((rc = dev_alloc(&p->ranges, ntiles))) return rc;
+        p->tiles_cap = ntiles;
+    }
+    (void)nf;
+    return TSB_OK;
+}
+
+PixK pixk(tsb_pass* p) {
+    PixK px;
+    px.out = p->out;
+    const bool counts = (p->channels & TSB_CH_COUNTS) != 0;
+    px.n_contrib = counts ? p->n_contrib : nullptr;
+    px.n_processed = counts ? p->n_processed : nullptr;
+    px.last = p->last;
+    px.T_pre = p->T_pre;
+    px.d_quad = p->d_quad;
+    px.flagged = p->flagged;
+    px.n_flagged = p->counters + 1;
+    return px;
+}
+
+SceneK scenek(const tsb_scene* s) {
+    SceneK k;
+    k.n = s->d.n;
+    k.nk = s->d.n_keyframes;
+    k.nf = s->d.n_freq;
+    k.sh_degree = s->d.sh_degree;
+    k.freq[0] = s->d.frequency[0];
+    k.freq[1] = s->d.n_freq > 1 ? s->d.frequency[1] : 0.0;
+    k.s_int = s->d.source_intensity;
+    k.c = s->d.speed_of_light;
+    const size_t n = (size_t)s->d.n;
+    k.pos_op = s->params;
+    k.scale_amp = s->params + n;
+    k.quat = s->params + 2 * n;
+    k.motion = s->params + 3 * n;
+    return k;
+}
+
+int bits_for(int ntiles) {
+    int b = 1;
+    while ((1 << b) < ntiles) ++b;
+    return b;
+}
+
+}  // namespace
+
+void tsb_pass_destroy(tsb_pass* p) {
+    if (!p) return;
+    cudaSetDevice(p->ctx->device);
+    cudaStreamSynchronize(p->ctx->stream);
+    free_gauss(p);
+    free_keys(p);
+    free_pixels(p);
+    dev_free(p->ranges);
+    dev_free(p->counters);
+    dev_free(p->loss_part);
+    dev_free(p->bg_part);
+    dev_free(p->loss_dev);
+    dev_free(p->chw);
+    dev_free(p->temp);
+    delete p;
+}
+
+int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb_render_options* opt,
+                     const tsb_frame* frame) {
+    if (!p) return fail(TSB_ERR_INVALID, "null pass");
+    p->prepared = p->forwarded = p->have_loss = false;
+    // RenderPassImpl ctor checks (splat.cpp:91-100)
+    if (!s || !cam) return fail(TSB_ERR_INVALID, "render: scene and camera required");
+    if (!(cam->fx > 0 && cam->fy > 0 && cam->width > 0 && cam->height > 0 && cam->near_plane > 0 &&
+          cam->far_plane > cam->near_plane))
+        return fail(TSB_ERR_INVALID, "render: invalid camera");
+    if (!opt) return fail(TSB_ERR_INVALID, "render: options required");
+    if (s->ctx != p->ctx) return fail(TSB_ERR_INVALID, "render: scene and pass belong to different contexts");
+    if (cam->width > 32767 || cam->height > 32767)
+        return fail(TSB_ERR_UNSUPPORTED, "render: image dimensions above 32767 are not supported");
+    TSB_CUDA(cudaSetDevice(p->ctx->device));
+    cudaStream_t st = p->ctx->stream;
+
+    p->scene = s;
+    p->nf = s->d.n_freq;
+    p->W = cam->width;
+    p->H = cam->height;
+    p->channels = opt->channels;
+    CamK& C = p->cam;
+    C.fx = cam->fx; C.fy = cam->fy; C.cx = cam->cx; C.cy = cam->cy;
+    C.W = cam->width; C.H = cam->height;
+    C.near_plane = cam->near_plane;
+    for (int i = 0; i < 9; ++i) C.R[i] = cam->R[i];
+    for (int i = 0; i < 3; ++i) C.t[i] = cam->t[i];
+    C.lim_x = 1.3 * (0.5 * cam->width / cam->fx);
+    C.lim_y = 1.3 * (0.5 * cam->height / cam->fy);
+    for (int i = 0; i < 3; ++i)
+        C.center[i] = -(cam->R[0 * 3 + i] * cam->t[0] + cam->R[1 * 3 + i] * cam->t[1] + cam->R[2 * 3 + i] * cam->t[2]);
+    OptK& O = p->opt;
+    O.alpha_thr = opt->alpha_threshold;
+    O.floor_T = opt->transmittance_floor;
+    O.dilation = opt->dilation;
+    O.sigma_cutoff = opt->sigma_cutoff;
+    O.cov_eps = opt->coverage_eps;
+    O.cut2 = opt->sigma_cutoff * opt->sigma_cutoff;
+    O.ts = std::max(1, opt->tile_size);
+    O.tiles_x = (cam->width + O.ts - 1) / O.ts;
+    O.tiles_y = (cam->height + O.ts - 1) / O.ts;
+    O.sub = (O.ts + kTile - 1) / kTile;
+    O.alpha_thr_f = (float)O.alpha_thr;
+    O.floor_f = (float)O.floor_T;
+    O.cut2_f = (float)O.cut2;
+    O.cov_eps_f = (float)O.cov_eps;
+    for (int c = 0; c < 8; ++c) O.bg_quad[c] = c < 4 * p->nf ? opt->bg_quad[c] : 0.0;
+    p->ntiles = O.tiles_x * O.tiles_y;
+    if (p->ntiles > 65536) return fail(TSB_ERR_UNSUPPORTED, "render: more than 65536 tiles");
+    p->nblocks = p->ntiles * O.sub * O.sub;
+    if (frame) {
+        if (s->d.n_keyframes > 0 && (frame->key < 0 || frame->key > s->d.n_keyframes - 2))
+            return fail(TSB_ERR_INVALID, "render: frame keyframe index out of range");
+        p->frame.key = frame->key;
+        p->frame.w = frame->w;
+    } else {
+        p->frame.key = 0;
+        p->frame.w = 0.0;
+    }
+
+    const int n = s->d.n;
+    int rc;
+    if ((rc = ensure_gauss(p, n))) return rc;
+    if ((rc = ensure_pixels(p, p->W, p->H, p->nf, p->ntiles, p->nblocks))) return rc;
+    if ((rc = ensure_temp(p))) return rc;
+
+    const SceneK S = scenek(s);
+    TSB_CUDA(cudaMemsetAsync(p->counters, 0, sizeof(int32_t) * 4, st));
+    launch_preprocess(S, C, O, p->frame, p->key_a, p->gidx_a, p->touched, p->rect, p->rec, p->counters, st);
+    launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, n, p->temp, p->temp_bytes, st);
+    launch_gather_counts(p->gidx_b, p->touched, p->cnt_sorted, n, st);
+    launch_scan(p->cnt_sorted, p->offsets, n, p->temp, p->temp_bytes, st);
+    p->ctx->launches += 2;
+    TSB_CHECK_LAUNCH();
+    // K = offsets[n-1] + cnt[n-1]; V = counters[0]
+    uint32_t* hp = (uint32_t*)p->ctx->pinned;
+    hp[0] = hp[1] = 0;
+    if (n > 0) {
+        TSB_CUDA(cudaMemcpyAsync(hp, p->offsets + (n - 1), 4, cudaMemcpyDeviceToHost, st));
+        TSB_CUDA(cudaMemcpyAsync(hp + 1, p->cnt_sorted + (n - 1), 4, cudaMemcpyDeviceToHost, st));
+    }
+    TSB_CUDA(cudaMemcpyAsync(hp + 2, p->counters, 4, cudaMemcpyDeviceToHost, st));
+    TSB_CUDA(cudaStreamSynchronize(st));
+    p->K = (int64_t)hp[0] + (int64_t)hp[1];
+    p->V = (int32_t)hp[2];
+    if ((rc = ensure_keys(p, p->K))) return rc;
+    if ((rc = ensure_temp(p))) return rc;
+    launch_duplicate(p->gidx_b, p->offsets, p->cnt_sorted, p->rect, p->tkey_a, p->tval_a, n, O.ts, O.tiles_x, st);
+    launch_sort_tiles(p->tkey_a, p->tkey_b, p->tval_a, p->tval_b, p->K, bits_for(p->ntiles), p->temp, p->temp_bytes,
+                      st);
+    launch_ranges(p->tkey_b, p->K, p->ranges, p->ntiles, st);
+    p->ctx->launches += 2;
+    TSB_CHECK_LAUNCH();
+    p->prepared = true;
+    return TSB_OK;
+}
+
+int tsb_pass_visible_count(tsb_pass* p, int32_t* out) {
+    if (!p || !out) return fail(TSB_ERR_INVALID, "null argument");
+    if (!p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
+    *out = p->V;
+    return TSB_OK;
+}
+
+int tsb_pass_num_keys(tsb_pass* p, int64_t* out) {
+    if (!p || !out) return fail(TSB_ERR_INVALID, "null argument");
+    if (!p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
+    *out = p->K;
+    return TSB_OK;
+}
+
+namespace {
+
+int run_forward(tsb_pass* p, const float* target, bool loss) {
+    if (!p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
+    TSB_CUDA(cudaSetDevice(p->ctx->device));
+    cudaStream_t st = p->ctx->stream;
+    PixK px = pixk(p);
+    TSB_CUDA(cudaMemsetAsync(p->counters + 1, 0, sizeof(int32_t), st));
+    launch_raster_fwd(p->rec, p->ranges, p->tval_b, p->opt, p->W, p->H, p->nf, px, loss ? target : nullptr,
+                      p->chw, p->loss_part, st);
+    launch_fixup(scenek(p->scene), p->cam, p->opt, p->frame, p->ranges, p->tval_b, px, p->nf, st);
+    p->ctx->launches += 2;
+    if (loss) {
+        TSB_CUDA(cudaMemsetAsync(p->loss_dev, 0, sizeof(double), st));
+        launch_fixup_loss(px, p->W, p->H, p->nf, target, p->chw, p->loss_dev, p->W * p->H, st);
+        launch_reduce_partials(p->loss_part, p->nblocks, 1, p->loss_dev, 1.0 / ((double)p->W * p->H), st);
+        // scene loss accumulator += this pass's loss
+        launch_reduce_partials(p->loss_dev, 1, 1, p->scene->stats + 8, 1.0, st);
+        p->ctx->launches += 3;
+    }
+    TSB_CHECK_LAUNCH();
+    p->forwarded = true;
+    p->have_loss = loss;
+    return TSB_OK;
+}
+
+}  // namespace
+
+int tsb_pass_forward(tsb_pass* p) {
+    if (!p) return fail(TSB_ERR_INVALID, "null pass");
+    return run_forward(p, nullptr, false);
+}
+
+int tsb_pass_forward_loss(tsb_pass* p, int where, const float* target, const double* channel_weight,
+                          double* loss_out) {
+    if (!p || !target || !channel_weight) return fail(TSB_ERR_INVALID, "tsb_pass_forward_loss: null argument");
+    if (!p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
+    TSB_CUDA(cudaSetDevice(p->ctx->device));
+    cudaStream_t st = p->ctx->stream;
+    const size_t nq = (size_t)4 * p->nf * p->W * p->H;
+    const float* dt = target;
+    if (where == TSB_HOST) {
+        TSB_CUDA(cudaMemcpyAsync(p->target, target, nq * sizeof(float), cudaMemcpyHostToDevice, st));
+        dt = p->target;
+    } else if (where != TSB_DEVICE) {
+        return fail(TSB_ERR_INVALID, "bad memory kind");
+    }
+    float w[8] = {0};
+    for (int c = 0; c < 4 * p->nf; ++c) w[c] = (float)channel_weight[c];
+    float* hw = (float*)p->ctx->pinned + 16;
+    TSB_CUDA(cudaStreamSynchronize(st));  // pinned staging reuse
+    std::memcpy(hw, w, sizeof w);
+    TSB_CUDA(cudaMemcpyAsync(p->chw, hw, sizeof w, cudaMemcpyHostToDevice, st));
+    int rc = run_forward(p, dt, true);
+    if (rc) return rc;
+    if (loss_out) {
+        double* hl = (double*)((char*)p->ctx->pinned + 256);
+        TSB_CUDA(cudaMemcpyAsync(hl, p->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+        TSB_CUDA(cudaStreamSynchronize(st));
+        *loss_out = *hl;
+    }
+    return TSB_OK;
+}
+
+int tsb_pass_output(tsb_pass* p, int which, void** dptr, size_t* bytes) {
+    if (!p || !dptr) return fail(TSB_ERR_INVALID, "null argument");
+    if (!p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
+    const size_t HW = (size_t)p->W * p->H;
+    void* ptr = nullptr;
+    size_t b = 0;
+    switch (which) {
+        case TSB_OUT_QUAD: ptr = p->out; b = 4 * p->nf * HW * 4; break;
+        case TSB_OUT_DEPTH_RAW: ptr = p->out + ch_depth_raw(p->nf) * HW; b = HW * 4; break;
+        case TSB_OUT_DEPTH: ptr = p->out + ch_depth(p->nf) * HW; b = HW * 4; break;
+        case TSB_OUT_WEIGHT: ptr = p->out + ch_weight(p->nf) * HW; b = HW * 4; break;
+        case TSB_OUT_TRANSM: ptr = p->out + ch_T(p->nf) * HW; b = HW * 4; break;
+        case TSB_OUT_N_CONTRIB:
+            if (!(p->channels & TSB_CH_COUNTS)) return fail(TSB_ERR_INVALID, "counts channel not enabled");
+            ptr = p->n_contrib; b = HW * 4; break;
+        case TSB_OUT_N_PROCESSED:
+            if (!(p->channels & TSB_CH_COUNTS)) return fail(TSB_ERR_INVALID, "counts channel not enabled");
+            ptr = p->n_processed; b = HW * 4; break;
+        case TSB_OUT_D_QUAD: ptr = p->d_quad; b = 4 * p->nf * HW * 4; break;
+        default: return fail(TSB_ERR_INVALID, "unknown output");
+    }
+    *dptr = ptr;
+    if (bytes) *bytes = b;
+    return TSB_OK;
+}
+
+int tsb_pass_download(tsb_pass* p, int which, void* host, size_t bytes) {
+    void* d = nullptr;
+    size_t b = 0;
+    int rc = tsb_pass_output(p, which, &d, &b);
+    if (rc) return rc;
+    if (!host || bytes < b) return fail(TSB_ERR_INVALID, "tsb_pass_download: host buffer too small");
+    TSB_CUDA(cudaMemcpyAsync(host, d, b, cudaMemcpyDeviceToHost, p->ctx->stream));
+    TSB_CUDA(cudaStreamSynchronize(p->ctx->stream));
+    return TSB_OK;
+}
+
+int tsb_pass_backward(tsb_pass* p, int where, const float* d_quad) {
+    if (!p) return fail(TSB_ERR_INVALID, "null pass");
+    if (!p->forwarded) return fail(TSB_ERR_INVALID, "backward requires a forward pass");
+    TSB_CUDA(cudaSetDevice(p->ctx->device));
+    cudaStream_t st = p->ctx->stream;
+    const float* up = p->d_quad;
+    if (d_quad) {
+        const size_t nq = (size_t)4 * p->nf * p->W * p->H;
+        if (where == TSB_HOST) {
+            TSB_CUDA(cudaMemcpyAsync(p->d_quad, d_quad, nq * sizeof(float), cudaMemcpyHostToDevice, st));
+        } else if (where == TSB_DEVICE) {
+            up = d_quad;
+        } else {
+            return fail(TSB_ERR_INVALID, "bad memory kind");
+        }
+    } else if (!p->have_loss) {
+        return fail(TSB_ERR_INVALID, "backward: no upstream gradient and no loss was evaluated");
+    }
+    tsb_scene* s = p->scene;
+    float dpsi[2];
+    for (int f = 0; f < p->nf; ++f) dpsi[f] = (float)(4.0 * M_PI * s->d.frequency[f] / s->d.speed_of_light);
+    launch_raster_bwd(p->rec, p->ranges, p->tval_b, p->opt, p->W, p->H, p->nf, dpsi, pixk(p), up, p->screen,
+                      s->d.n, p->bg_part, st);
+    launch_reduce_partials(p->bg_part, p->nblocks, 4 * p->nf, s->stats, 1.0, st);
+    launch_chain(scenek(s), p->cam, p->opt, p->frame, p->touched, p->screen, s->grads, st);
+    p->ctx->launches += 3;
+    TSB_CHECK_LAUNCH();
+    return TSB_OK;
+}
+
+// ---- debug / parity ----
+int tsb_pass_debug_prepared(tsb_pass* p, int32_t* gidx, int32_t* rect) {
+    if (!p || !p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
+    cudaStream_t st = p->ctx->stream;
+    const int V = p->V;
+    std::vector<uint32_t> g(V > 0 ? V : 1);
+    if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), p->gidx_b, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, st));
+    std::vector<uint2> r((size_t)std::max(p->scene->d.n, 1));
+    if (rect && p->scene->d.n > 0)
+        TSB_CUDA(cudaMemcpyAsync(r.data(), p->rect, sizeof(uint2) * p->scene->d.n, cudaMemcpyDeviceToHost, st));
+    TSB_CUDA(cudaStreamSynchronize(st));
+    for (int i = 0; i < V; ++i) {
+        if (gidx) gidx[i] = (int32_t)g[i];
+        if (rect) {
+            const uint2 rc = r[g[i]];
+            rect[4 * i + 0] = rc.x & 0xffff;
+            rect[4 * i + 1] = rc.x >> 16;
+            rect[4 * i + 2] = rc.y & 0xffff;
+            rect[4 * i + 3] = rc.y >> 16;
+        }
+    }
+    return TSB_OK;
+}
+
+int tsb_pass_debug_tiles(tsb_pass* p, int32_t* tiles_x, int32_t* tiles_y, int64_t* offsets, int32_t* ids) {
+    if (!p || !p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
+    if (tiles_x) *tiles_x = p->opt.tiles_x;
+    if (tiles_y) *tiles_y = p->opt.tiles_y;
+    cudaStream_t st = p->ctx->stream;
+    std::vector<uint2> rg(p->ntiles);
+    TSB_CUDA(cudaMemcpyAsync(rg.data(), p->ranges, sizeof(uint2) * p->ntiles, cudaMemcpyDeviceToHost, st));
+    std::vector<uint32_t> vals((size_t)std::max<int64_t>(p->K, 1));
+    std::vector<uint32_t> order((size_t)std::max(p->V, 1));
+    if (ids && p->K > 0) {
+        TSB_CUDA(cudaMemcpyAsync(vals.data(), p->tval_b, sizeof(uint32_t) * p->K, cudaMemcpyDeviceToHost, st));
+        if (p->V > 0)
+            TSB_CUDA(cudaMemcpyAsync(order.data(), p->gidx_b, sizeof(uint32_t) * p->V, cudaMemcpyDeviceToHost, st));
+    }
+    TSB_CUDA(cudaStreamSynchronize(st));
+    // ranges are contiguous in tile order: offsets[t] = start of tile t
+    if (offsets) {
+        int64_t acc = 0;
+        for (int t = 0; t < p->ntiles; ++t) {
+            offsets[t] = acc;
+            acc += (int64_t)rg[t].y - rg[t].x;
+        }
+        offsets[p->ntiles] = acc;
+    }
+    if (ids && p->K > 0) {
+        // values are Gaussian indices; the reference lists hold prepared (rank) indices
+        std::vector<int32_t> rank_of((size_t)std::max(p->scene->d.n, 1), -1);
+        for (int r = 0; r < p->V; ++r) rank_of[order[r]] = r;
+        int64_t o = 0;
+        for (int t = 0; t < p->ntiles; ++t)
+            for (uint32_t e = rg[t].x; e < rg[t].y; ++e) ids[o++] = rank_of[vals[e]];
+    }
+    return TSB_OK;
+}
+
+int tsb_pass_debug_records(tsb_pass* p, float* rec12) {
+    if (!p || !p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
+    cudaStream_t st = p->ctx->stream;
+    const int n = p->scene->d.n, V = p->V;
+    std::vector<float4> A(std::max(n, 1)), B(std::max(n, 1)), C(std::max(n, 1)), D(std::max(n, 1));
+    std::vector<uint32_t> g(std::max(V, 1));
+    if (n > 0) {
+        TSB_CUDA(cudaMemcpyAsync(A.data(), p->rec.A, sizeof(float4) * n, cudaMemcpyDeviceToHost, st));
+        TSB_CUDA(cudaMemcpyAsync(B.data(), p->rec.B, sizeof(float4) * n, cudaMemcpyDeviceToHost, st));
+        TSB_CUDA(cudaMemcpyAsync(C.data(), p->rec.C, sizeof(float4) * n, cudaMemcpyDeviceToHost, st));
+        if (p->nf > 1) TSB_CUDA(cudaMemcpyAsync(D.data(), p->rec.D, sizeof(float4) * n, cudaMemcpyDeviceToHost, st));
+    }
+    if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), p->gidx_b, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, st));
+    TSB_CUDA(cudaStreamSynchronize(st));
+    for (int r = 0; r < V; ++r) {
+        const uint32_t i = g[r];
+        float* o = rec12 + 12 * (size_t)r;
+        const float l11 = B[i].x, l12 = B[i].y, l22 = B[i].z;
+        o[0] = A[i].x + A[i].z;  // mean x (approximate: rounded sum)
+        o[1] = A[i].y + A[i].w;
+        o[2] = l11 * l11;            // conic a
+        o[3] = l11 * l12;            // conic b
+        o[4] = l12 * l12 + l22 * l22;  // conic c
+        o[5] = B[i].w;
+        o[6] = C[i].x;
+        o[7] = C[i].y;
+        o[8] = C[i].z;
+        o[9] = C[i].w;
+        o[10] = p->nf > 1 ? D[i].x : 0.f;
+        o[11] = p->nf > 1 ? D[i].y : 0.f;
+    }
+    return TSB_OK;
+}
+
+int tsb_pass_debug_screen_grads(tsb_pass* p, float* g8) {
+    (void)g8;
+    if (!p) return fail(TSB_ERR_INVALID, "null pass");
+    return fail(TSB_ERR_UNSUPPORTED, "screen gradients are consumed by the chain kernel");
+}
+
+int tsb_pass_debug_fixups(tsb_pass* p, int32_t* count) {
+    if (!p || !count) return fail(TSB_ERR_INVALID, "null argument");
+    int32_t* h = (int32_t*)((char*)p->ctx->pinned + 512);
+    TSB_CUDA(cudaMemcpyAsync(h, p->counters + 1, 4, cudaMemcpyDeviceToHost, p->ctx->stream));
+    TSB_CUDA(cudaStreamSynchronize(p->ctx->stream));
+    *count = *h;
+    return TSB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// NCCL
+// ---------------------------------------------------------------------------
+struct tsb_comm {
+    ncclComm_t comm = nullptr;
+    tsb_ctx* ctx = nullptr;
+};
+
+int tsb_comm_unique_id(void* out) {
+    if (!out) return fail(TSB_ERR_INVALID, "null argument");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return fail(TSB_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memcpy(out, &id, sizeof id);
+    return TSB_OK;
+}
+
+int tsb_comm_create(tsb_ctx* ctx, const void* unique_id, int nranks, int rank, tsb_comm** out) {
+    if (!ctx || !unique_id || !out) return fail(TSB_ERR_INVALID, "tsb_comm_create: null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(TSB_ERR_INVALID, "tsb_comm_create: bad rank");
+    TSB_CUDA(cudaSetDevice(ctx->device));
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof id);
+    tsb_comm* c = new tsb_comm();
+    c->ctx = ctx;
+    ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        return fail(TSB_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    *out = c;
+    return TSB_OK;
+}
+
+void tsb_comm_destroy(tsb_comm* c) {
+    if (!c) return;
+    if (c->comm) ncclCommDestroy(c->comm);
+    delete c;
+}
+
+int tsb_scene_allreduce_grads(tsb_scene* s, tsb_comm* c) {
+    if (!s || !c) return fail(TSB_ERR_INVALID, "null argument");
+    const size_t nel = (size_t)s->narrays * (size_t)s->d.n * 4;
+    cudaStream_t st = s->ctx->stream;
+    ncclResult_t r = ncclGroupStart();
+    if (r == ncclSuccess && nel > 0) r = ncclAllReduce(s->grads, s->grads, nel, ncclFloat, ncclSum, c->comm, st);
+    if (r == ncclSuccess) r = ncclAllReduce(s->stats, s->stats, 9, ncclDouble, ncclSum, c->comm, st);
+    ncclResult_t r2 = ncclGroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+        return fail(TSB_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
+    return TSB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host helpers (tof.hpp)
+// ---------------------------------------------------------------------------
+static double freq_or_default(double f) { return f > 0 ? f : 29.9792458e6; }
+
+double tsb_unambiguous_range(double frequency) { return 299792458.0 / (2.0 * freq_or_default(frequency)); }
+
+double tsb_quad_to_depth(double q0, double q90, double q180, double q270, double frequency) {
+    const double re = q90 - q270, im = q0 - q180;
+    if (re == 0.0 && im == 0.0) return std::nan("");
+    double psi = std::atan2(im, re);
+    if (psi < 0.0) psi += 2.0 * M_PI;
+    return psi * 299792458.0 / (4.0 * M_PI * freq_or_default(frequency));
+}
+
+void tsb_quad_basis(double depth, double frequency, double* out4) {
+    const double psi = 4.0 * M_PI * depth * freq_or_default(frequency) / 299792458.0;
+    const double s = std::sin(psi), c = std::cos(psi);
+    out4[0] = s;
+    out4[1] = c;
+    out4[2] = -s;
+    out4[3] = -c;
+}
+
+}  // extern "C"

@@ -1,0 +1,158 @@
+// fp64 per-Gaussian preprocess shared by the preprocess, fp64 fix-up and chain
+// kernels.  This TU family is compiled with -fmad=false so that every double
+// operation rounds exactly as written, in the same order as the reference
+// RenderPassImpl::prepare (proj/src/splat.cpp:105-177) and the CPU oracle
+// (oracle/tofsplat_oracle.c prepare()).  Integer outcomes (cull, tile rect,
+// global (depth, index) order) are therefore bit-identical to the oracle.
+#pragma once
+
+#include "tsb_internal.h"
+
+namespace tsb {
+
+struct Prep64 {
+    double x[3];  // rendered world mean (trajectory-interpolated)
+    double p[3];  // camera-space mean
+    double depth; // Euclidean distance (splat.cpp:124)
+    double opacity;
+    double mean[2];
+    double ca, cb, cc;
+    double c11;  // dilated cov2d(1,1): l22 = 1/sqrt(c11)
+    double coef;
+    double refl_raw;
+    double M[6];      // J W (2x3 row-major)
+    double cov3d[9];  // row-major
+    double tx, ty;
+    bool clx, cly;
+    int x0, x1, y0, y1;
+};
+
+__device__ __forceinline__ int d2i_like_x86(double v) {
+    // static_cast<int>(std::floor(..)) on x86-64: out-of-range -> INT_MIN
+    if (!(v >= -2147483648.0 && v < 2147483648.0)) return (int)0x80000000u;
+    return (int)v;
+}
+
+__device__ __forceinline__ double clampd(double v, double lo, double hi) {
+    return v < lo ? lo : (v > hi ? hi : v);
+}
+
+// Rendered mean at the frame (trainer.cpp:259-279): Xi = x + d_k, Xip1 = x + d_{k+1},
+// P = (w == 0) ? Xi : (1 - w) Xi + w Xip1.
+__device__ __forceinline__ void frame_mean(const SceneK& S, const FrameK& F, int gi, double* x) {
+    const float4 po = S.pos_op[gi];
+    const double c[3] = {(double)po.x, (double)po.y, (double)po.z};
+    if (S.nk == 0) {
+        x[0] = c[0]; x[1] = c[1]; x[2] = c[2];
+        return;
+    }
+    const float4 da = S.motion[(size_t)F.key * S.n + gi];
+    const float4 db = S.motion[(size_t)(F.key + 1) * S.n + gi];
+    const double a[3] = {(double)da.x, (double)da.y, (double)da.z};
+    const double b[3] = {(double)db.x, (double)db.y, (double)db.z};
+    for (int i = 0; i < 3; ++i) {
+        const double Xi = c[i] + a[i];
+        const double Xip1 = c[i] + b[i];
+        x[i] = (F.w == 0.0) ? Xi : (1.0 - F.w) * Xi + F.w * Xip1;
+    }
+}
+
+// quat_to_rotation (scene.cpp:10-18) with Eigen::normalized semantics.
+__device__ __forceinline__ void quat_rot(const double* q, double* u, double* R) {
+    const double z = q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3];
+    if (z > 0.0) {
+        const double n = sqrt(z);
+        for (int i = 0; i < 4; ++i) u[i] = q[i] / n;
+    } else {
+        for (int i = 0; i < 4; ++i) u[i] = q[i];
+    }
+    const double w = u[0], x = u[1], y = u[2], zz = u[3];
+    R[0] = 1 - 2 * (y * y + zz * zz); R[1] = 2 * (x * y - w * zz);    R[2] = 2 * (x * zz + w * y);
+    R[3] = 2 * (x * y + w * zz);     R[4] = 1 - 2 * (x * x + zz * zz); R[5] = 2 * (y * zz - w * x);
+    R[6] = 2 * (x * zz - w * y);     R[7] = 2 * (y * zz + w * x);     R[8] = 1 - 2 * (x * x + y * y);
+}
+
+// RenderPassImpl::prepare for one Gaussian (splat.cpp:114-176).  Returns true when
+// the splat survives culling.  Only sh_degree 0 is handled (refl_raw = C0 * dc).
+__device__ __forceinline__ bool prep64(const SceneK& S, const CamK& C, const OptK& O,
+                                       const FrameK& F, int gi, Prep64& s) {
+    frame_mean(S, F, gi, s.x);
+    const double* R = C.R;
+    for (int i = 0; i < 3; ++i)
+        s.p[i] = R[i * 3 + 0] * s.x[0] + R[i * 3 + 1] * s.x[1] + R[i * 3 + 2] * s.x[2] + C.t[i];
+    if (s.p[2] < C.near_plane) return false;
+    s.depth = sqrt(s.p[0] * s.p[0] + s.p[1] * s.p[1] + s.p[2] * s.p[2]);
+    const float4 po = S.pos_op[gi];
+    s.opacity = 1.0 / (1.0 + exp(-(double)po.w));
+    if (s.opacity < O.alpha_thr) return false;
+
+    const double z = s.p[2];
+    s.mean[0] = C.fx * s.p[0] / z + C.cx;
+    s.mean[1] = C.fy * s.p[1] / z + C.cy;
+
+    const float4 qf = S.quat[gi];
+    const double q[4] = {(double)qf.x, (double)qf.y, (double)qf.z, (double)qf.w};
+    double u[4], Rq[9];
+    quat_rot(q, u, Rq);
+    const float4 sa = S.scale_amp[gi];
+    const double sv[3] = {exp((double)sa.x), exp((double)sa.y), exp((double)sa.z)};
+    double M3[9];
+    for (int r = 0; r < 3; ++r)
+        for (int j = 0; j < 3; ++j) M3[r * 3 + j] = Rq[r * 3 + j] * sv[j];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            s.cov3d[i * 3 + j] = M3[i * 3 + 0] * M3[j * 3 + 0] + M3[i * 3 + 1] * M3[j * 3 + 1] +
+                                 M3[i * 3 + 2] * M3[j * 3 + 2];
+    const double rx = s.p[0] / z, ry = s.p[1] / z;
+    s.clx = rx < -C.lim_x || rx > C.lim_x;
+    s.cly = ry < -C.lim_y || ry > C.lim_y;
+    s.tx = clampd(rx, -C.lim_x, C.lim_x) * z;
+    s.ty = clampd(ry, -C.lim_y, C.lim_y) * z;
+    double J[6];
+    J[0] = C.fx / z; J[1] = 0.0; J[2] = -C.fx * s.tx / (z * z);
+    J[3] = 0.0; J[4] = C.fy / z; J[5] = -C.fy * s.ty / (z * z);
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 3; ++j)
+            s.M[i * 3 + j] = J[i * 3 + 0] * R[0 * 3 + j] + J[i * 3 + 1] * R[1 * 3 + j] + J[i * 3 + 2] * R[2 * 3 + j];
+    double T23[6];
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 3; ++j)
+            T23[i * 3 + j] = s.M[i * 3 + 0] * s.cov3d[0 * 3 + j] + s.M[i * 3 + 1] * s.cov3d[1 * 3 + j] +
+                             s.M[i * 3 + 2] * s.cov3d[2 * 3 + j];
+    double c2[4];
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j)
+            c2[i * 2 + j] = T23[i * 3 + 0] * s.M[j * 3 + 0] + T23[i * 3 + 1] * s.M[j * 3 + 1] +
+                            T23[i * 3 + 2] * s.M[j * 3 + 2];
+    c2[0] += O.dilation;
+    c2[3] += O.dilation;
+    const double det = c2[0] * c2[3] - c2[1] * c2[1];
+    if (!(det > 0.0)) return false;
+    s.ca = c2[3] / det;
+    s.cb = -c2[1] / det;
+    s.cc = c2[0] / det;
+    s.c11 = c2[3];
+    const double mid = 0.5 * (c2[0] + c2[3]);
+    const double disc = mid * mid - det;
+    const double lam_max = mid + sqrt(disc > 0.1 ? disc : 0.1);
+    const double radius = O.sigma_cutoff * sqrt(lam_max);
+    int v;
+    v = d2i_like_x86(floor(s.mean[0] - radius)); s.x0 = v > 0 ? v : 0;
+    v = d2i_like_x86(ceil(s.mean[0] + radius)) + 1; s.x1 = v < C.W ? v : C.W;
+    v = d2i_like_x86(floor(s.mean[1] - radius)); s.y0 = v > 0 ? v : 0;
+    v = d2i_like_x86(ceil(s.mean[1] + radius)) + 1; s.y1 = v < C.H ? v : C.H;
+    if (s.x0 >= s.x1 || s.y0 >= s.y1) return false;
+
+    // sh_degree 0: view-independent reflectivity (sh.hpp:26-31; splat.cpp:163-167)
+    s.refl_raw = (double)sa.w * 0.28209479177387814;
+    const double r = clampd(s.refl_raw, 0.0, 1.0);
+    s.coef = S.s_int * r / (s.depth * s.depth);
+    return true;
+}
+
+// phase_of_depth (tof.hpp:41-43) and its derivative (splat.cpp:171).
+__device__ __forceinline__ double phase_of_depth(double depth, double f, double c) {
+    return 4.0 * M_PI * depth * f / c;
+}
+
+}  // namespace tsb

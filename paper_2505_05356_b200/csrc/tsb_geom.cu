@@ -1,0 +1,318 @@
+// fp64 per-Gaussian kernels: preprocess, fp64 pixel fix-up, parameter chain.
+// Compiled with -fmad=false (see tsb_fp64.cuh).
+#include <cuda_runtime.h>
+
+#include "tsb_fp64.cuh"
+
+namespace tsb {
+
+// ---------------------------------------------------------------------------
+// k_preprocess: RenderPassImpl::prepare (splat.cpp:105-177), one thread per
+// Gaussian.  Writes the fp64 depth sort key (bits of the positive double, so
+// unsigned order == numeric order; culled -> ~0), tile rect, tiles touched and
+// the fp32 raster record (indexed by Gaussian; the duplicate kernel gathers it
+// into rank order).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, FrameK F,
+                                                    uint64_t* __restrict__ depth_key,
+                                                    uint32_t* __restrict__ gidx,
+                                                    uint32_t* __restrict__ touched,
+                                                    uint2* __restrict__ rect, RecK rec,
+                                                    int32_t* __restrict__ n_visible) {
+    const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+    bool vis = false;
+    if (gi < S.n) {
+        Prep64 s;
+        vis = prep64(S, C, O, F, gi, s);
+        gidx[gi] = (uint32_t)gi;
+        if (vis) {
+            depth_key[gi] = (uint64_t)__double_as_longlong(s.depth);
+            const int ts = O.ts;
+            const int tx0 = s.x0 / ts, tx1 = (s.x1 - 1) / ts;
+            const int ty0 = s.y0 / ts, ty1 = (s.y1 - 1) / ts;
+            touched[gi] = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+            rect[gi] = make_uint2((uint32_t)s.x0 | ((uint32_t)s.x1 << 16),
+                                  (uint32_t)s.y0 | ((uint32_t)s.y1 << 16));
+            // factored conic (Cholesky of [[a, b], [b, c]]) in fp64, rounded once
+            const double l11 = sqrt(s.ca);
+            const double l12 = s.cb / l11;
+            const double l22 = 1.0 / sqrt(s.c11);
+            rec.A[gi] = make_float4((float)s.x0, (float)s.y0, (float)(s.mean[0] - (double)s.x0),
+                                    (float)(s.mean[1] - (double)s.y0));
+            rec.B[gi] = make_float4((float)l11, (float)l12, (float)l22, (float)s.opacity);
+            double sn, cs;
+            sincos(phase_of_depth(s.depth, S.freq[0], S.c), &sn, &cs);
+            rec.C[gi] = make_float4((float)s.coef, (float)s.depth, (float)sn, (float)cs);
+            if (S.nf > 1) {
+                sincos(phase_of_depth(s.depth, S.freq[1], S.c), &sn, &cs);
+                rec.D[gi] = make_float4((float)sn, (float)cs, 0.f, 0.f);
+            }
+        } else {
+            depth_key[gi] = ~0ull;
+            touched[gi] = 0u;
+        }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, vis);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(n_visible, __popc(m));
+}
+
+void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
+                       uint64_t* depth_key, uint32_t* gidx, uint32_t* touched, uint2* rect, RecK rec,
+                       int32_t* n_visible, cudaStream_t st) {
+    if (S.n <= 0) return;
+    const int bs = 256;
+    k_preprocess<<<(S.n + bs - 1) / bs, bs, 0, st>>>(S, C, O, F, depth_key, gidx, touched, rect, rec,
+                                                      n_visible);
+}
+
+// ---------------------------------------------------------------------------
+// k_fixup: fp64 re-composite of the pixels the fp32 raster flagged as having a
+// decision (maha <= cutoff^2, alpha >= threshold, T < floor) inside its error
+// band.  One warp per flagged pixel: lanes recompute the fp64 records of 32
+// list entries in parallel (the same prep64 the preprocess used), then the warp
+// walks them in order exactly as splat.cpp:260-297 does.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, FrameK F,
+                                               const uint2* __restrict__ ranges,
+                                               const uint32_t* __restrict__ tile_vals, PixK px,
+                                               int nf) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int count = *px.n_flagged;
+    const int W = C.W, H = C.H;
+    const size_t HW = (size_t)W * H;
+    for (int i = warp; i < count; i += nwarps) {
+        const int pix = px.flagged[i];
+        const int x = pix % W, y = pix / W;
+        const int tile = (y / O.ts) * O.tiles_x + (x / O.ts);
+        const uint2 rg = ranges[tile];
+        const double pcx = x + 0.5, pcy = y + 0.5;
+        double T = 1.0, SW = 0.0, SD = 0.0, Tpre = 1.0;
+        double accQ[8];
+        for (int c = 0; c < 8; ++c) accQ[c] = 0.0;
+        int nc = 0, processed = (int)(rg.y - rg.x), last_eff = -1;
+        bool done = false;
+        for (uint32_t b = rg.x; b < rg.y && !done; b += 32) {
+            const uint32_t e = b + lane;
+            bool inc = false;
+            double alpha = 0, coef = 0, depth = 0, sn[2] = {0, 0}, cs[2] = {0, 0};
+            if (e < rg.y) {
+                Prep64 s;
+                prep64(S, C, O, F, (int)tile_vals[e], s);  // visible by construction
+                if (!(x < s.x0 || x >= s.x1 || y < s.y0 || y >= s.y1)) {
+                    const double dx = pcx - s.mean[0], dy = pcy - s.mean[1];
+                    const double maha = s.ca * dx * dx + 2.0 * s.cb * dx * dy + s.cc * dy * dy;
+                    if (!(maha > O.cut2 || maha < 0.0)) {
+                        const double g = exp(-0.5 * maha);
+                        alpha = s.opacity * g;
+                        if (!(alpha < O.alpha_thr)) {
+                            inc = true;
+                            coef = s.coef;
+                            depth = s.depth;
+                            for (int f = 0; f < nf; ++f) {
+                                sincos(phase_of_depth(s.depth, S.freq[f], S.c), &sn[f], &cs[f]);
+                            }
+                        }
+                    }
+                }
+            }
+            const unsigned incm = __ballot_sync(0xffffffffu, inc);
+            const int nb = min(32u, rg.y - b);
+            for (int j = 0; j < nb; ++j) {
+                if (!((incm >> j) & 1u)) continue;
+                const double a = __shfl_sync(0xffffffffu, alpha, j);
+                const double cf = __shfl_sync(0xffffffffu, coef, j);
+                const double dp = __shfl_sync(0xffffffffu, depth, j);
+                double s_[2], c_[2];
+                for (int f = 0; f < 2; ++f) {
+                    s_[f] = __shfl_sync(0xffffffffu, sn[f], j);
+                    c_[f] = __shfl_sync(0xffffffffu, cs[f], j);
+                }
+                ++nc;
+                const double w = a * T;
+                const double w2 = a * T * T;
+                const double cq = cf * w2;
+                for (int f = 0; f < nf; ++f) {
+                    accQ[4 * f + 0] += cq * s_[f];
+                    accQ[4 * f + 1] += cq * c_[f];
+                    accQ[4 * f + 2] -= cq * s_[f];
+                    accQ[4 * f + 3] -= cq * c_[f];
+                }
+                SW += w;
+                SD += w * dp;
+                Tpre = T;
+                T *= 1.0 - a;
+                if (T == 0.0 && last_eff < 0) last_eff = (int)(b + j + 1 - rg.x);
+                if (T < O.floor_T) {
+                    processed = (int)(b + j + 1 - rg.x);
+                    done = true;
+                    break;
+                }
+            }
+        }
+        if (lane == 0) {
+            const size_t o = (size_t)y * W + x;
+            for (int c = 0; c < 4 * nf; ++c)
+                px.out[c * HW + o] = (float)(accQ[c] + O.bg_quad[c] * T * T);
+            px.out[ch_depth_raw(nf) * HW + o] = (float)SD;
+            px.out[ch_depth(nf) * HW + o] = SW > O.cov_eps ? (float)(SD / SW) : __int_as_float(0x7fc00000);
+            px.out[ch_weight(nf) * HW + o] = (float)SW;
+            px.out[ch_T(nf) * HW + o] = (float)T;
+            if (px.n_contrib) px.n_contrib[o] = nc;
+            if (px.n_processed) px.n_processed[o] = processed;
+            const int le = last_eff >= 0 ? last_eff : processed;
+            px.last[o] = le | (int)0x80000000;
+            px.T_pre[o] = (float)Tpre;
+        }
+    }
+}
+
+void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
+                  const uint2* ranges, const uint32_t* tile_vals, const PixK& px, int nf, cudaStream_t st) {
+    k_fixup<<<148 * 4, 128, 0, st>>>(S, C, O, F, ranges, tile_vals, px, nf);
+}
+
+// ---------------------------------------------------------------------------
+// k_chain: per visible Gaussian, chain the 8 screen-space gradients back to the
+// parameters (splat.cpp:551-648) in fp64, then through the trajectory
+// (trainer.cpp:313-314, 329-331), and accumulate into the scene gradient
+// buffer (GroupGrads::add).  Clears the screen-gradient slots it consumed.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_chain(SceneK S, CamK C, OptK O, FrameK F,
+                                               const uint32_t* __restrict__ touched,
+                                               float* __restrict__ screen,
+                                               float4* __restrict__ grads) {
+    const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gi >= S.n || touched[gi] == 0u) return;
+    float g8[8];
+    for (int c = 0; c < 8; ++c) {
+        g8[c] = screen[(size_t)c * S.n + gi];
+        screen[(size_t)c * S.n + gi] = 0.f;
+    }
+    Prep64 s;
+    prep64(S, C, O, F, gi, s);
+    const double d_mean0 = g8[0], d_mean1 = g8[1], d_ca = g8[2], d_cb = g8[3], d_cc = g8[4];
+    const double d_op = g8[5], d_coef = g8[6], d_dep = g8[7];
+    const double* R = C.R;
+
+    const double d_logit = d_op * s.opacity * (1.0 - s.opacity);
+    const double r_cl = clampd(s.refl_raw, 0.0, 1.0);
+    const double d2 = s.depth * s.depth;
+    const double d_depth = d_dep + d_coef * (-2.0 * S.s_int * r_cl / (d2 * s.depth));
+    double d_amp = 0.0;
+    if (s.refl_raw > 0.0 && s.refl_raw < 1.0) d_amp = 0.28209479177387814 * (d_coef * S.s_int / d2);
+
+    const double Q[4] = {s.ca, s.cb, s.cb, s.cc};
+    const double GQ[4] = {d_ca, 0.5 * d_cb, 0.5 * d_cb, d_cc};
+    double QG[4], G2[4];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) QG[a * 2 + b] = Q[a * 2 + 0] * GQ[0 * 2 + b] + Q[a * 2 + 1] * GQ[1 * 2 + b];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) G2[a * 2 + b] = -(QG[a * 2 + 0] * Q[0 * 2 + b] + QG[a * 2 + 1] * Q[1 * 2 + b]);
+    double GM[6], dM[6], MtG[6], G3[9];
+    for (int a = 0; a < 2; ++a)
+        for (int j = 0; j < 3; ++j) GM[a * 3 + j] = G2[a * 2 + 0] * s.M[0 * 3 + j] + G2[a * 2 + 1] * s.M[1 * 3 + j];
+    for (int a = 0; a < 2; ++a)
+        for (int j = 0; j < 3; ++j) {
+            double t = 0;
+            for (int k = 0; k < 3; ++k) t += (2.0 * GM[a * 3 + k]) * s.cov3d[k * 3 + j];
+            dM[a * 3 + j] = t;
+        }
+    for (int i = 0; i < 3; ++i)
+        for (int b = 0; b < 2; ++b) MtG[i * 2 + b] = s.M[0 * 3 + i] * G2[0 * 2 + b] + s.M[1 * 3 + i] * G2[1 * 2 + b];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) G3[i * 3 + j] = MtG[i * 2 + 0] * s.M[0 * 3 + j] + MtG[i * 2 + 1] * s.M[1 * 3 + j];
+    double dJ[6];
+    for (int a = 0; a < 2; ++a)
+        for (int j = 0; j < 3; ++j)
+            dJ[a * 3 + j] = dM[a * 3 + 0] * R[j * 3 + 0] + dM[a * 3 + 1] * R[j * 3 + 1] + dM[a * 3 + 2] * R[j * 3 + 2];
+    const double z = s.p[2], z2 = z * z, z3 = z2 * z;
+    double dp[3] = {0, 0, 0};
+    const double dtx = dJ[2] * (-C.fx / z2);
+    const double dty = dJ[5] * (-C.fy / z2);
+    dp[2] += dJ[0] * (-C.fx / z2) + dJ[4] * (-C.fy / z2) + dJ[2] * (2.0 * C.fx * s.tx / z3) +
+             dJ[5] * (2.0 * C.fy * s.ty / z3);
+    if (s.clx) dp[2] += dtx * (s.tx / z); else dp[0] += dtx;
+    if (s.cly) dp[2] += dty * (s.ty / z); else dp[1] += dty;
+    dp[0] += d_mean0 * C.fx / z;
+    dp[2] += d_mean0 * (-C.fx * s.p[0] / z2);
+    dp[1] += d_mean1 * C.fy / z;
+    dp[2] += d_mean1 * (-C.fy * s.p[1] / z2);
+    for (int a = 0; a < 3; ++a) dp[a] += d_depth * (s.p[a] / s.depth);
+    double dpos[3];
+    for (int a = 0; a < 3; ++a) dpos[a] = R[0 * 3 + a] * dp[0] + R[1 * 3 + a] * dp[1] + R[2 * 3 + a] * dp[2];
+
+    // cov3d = M3 M3^T, M3 = R(q) diag(exp(log_scale))
+    const float4 qf = S.quat[gi];
+    const double q[4] = {(double)qf.x, (double)qf.y, (double)qf.z, (double)qf.w};
+    double uq[4], Rq[9];
+    quat_rot(q, uq, Rq);
+    const float4 sa = S.scale_amp[gi];
+    const double sv[3] = {exp((double)sa.x), exp((double)sa.y), exp((double)sa.z)};
+    double M3[9], dM3[9];
+    for (int rr = 0; rr < 3; ++rr)
+        for (int j = 0; j < 3; ++j) M3[rr * 3 + j] = Rq[rr * 3 + j] * sv[j];
+    for (int rr = 0; rr < 3; ++rr)
+        for (int j = 0; j < 3; ++j) {
+            double t = 0;
+            for (int k = 0; k < 3; ++k) t += (2.0 * G3[rr * 3 + k]) * M3[k * 3 + j];
+            dM3[rr * 3 + j] = t;
+        }
+    double dls[3];
+    for (int j = 0; j < 3; ++j) {
+        double ds = 0;
+        for (int rr = 0; rr < 3; ++rr) ds += Rq[rr * 3 + j] * dM3[rr * 3 + j];
+        dls[j] = ds * sv[j];
+    }
+    double dRq[9];
+    for (int rr = 0; rr < 3; ++rr)
+        for (int j = 0; j < 3; ++j) dRq[rr * 3 + j] = dM3[rr * 3 + j] * sv[j];
+    const double w = uq[0], x = uq[1], y = uq[2], zq = uq[3];
+    const double dR[4][9] = {{0, -zq, y, zq, 0, -x, -y, x, 0},
+                             {0, y, zq, y, -2 * x, -w, zq, w, -2 * x},
+                             {-2 * y, x, w, x, 0, zq, -w, zq, -2 * y},
+                             {-2 * zq, -w, x, w, -2 * zq, y, x, y, 0}};
+    double duq[4];
+    for (int c = 0; c < 4; ++c) {
+        double t = 0;
+        for (int k = 0; k < 9; ++k) t += dRq[k] * (dR[c][k] * 2.0);
+        duq[c] = t;
+    }
+    const double qn = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    const double ud = uq[0] * duq[0] + uq[1] * duq[1] + uq[2] * duq[2] + uq[3] * duq[3];
+    double dq[4];
+    for (int c = 0; c < 4; ++c) dq[c] = (duq[c] - uq[c] * ud) / qn;
+
+    // accumulate (GroupGrads::add; canonical += dXi + dXip1 == dP)
+    const int n = S.n;
+    float4 g0 = grads[gi];
+    g0.x += (float)dpos[0]; g0.y += (float)dpos[1]; g0.z += (float)dpos[2]; g0.w += (float)d_logit;
+    grads[gi] = g0;
+    float4 g1 = grads[n + gi];
+    g1.x += (float)dls[0]; g1.y += (float)dls[1]; g1.z += (float)dls[2]; g1.w += (float)d_amp;
+    grads[n + gi] = g1;
+    float4 g2 = grads[2 * n + gi];
+    g2.x += (float)dq[0]; g2.y += (float)dq[1]; g2.z += (float)dq[2]; g2.w += (float)dq[3];
+    grads[2 * n + gi] = g2;
+    if (S.nk > 0) {
+        const double wa = 1.0 - F.w, wb = F.w;
+        float4* gm = grads + (size_t)(3 + F.key) * n + gi;
+        float4 a = *gm;
+        a.x += (float)(wa * dpos[0]); a.y += (float)(wa * dpos[1]); a.z += (float)(wa * dpos[2]);
+        *gm = a;
+        float4* gm2 = grads + (size_t)(3 + F.key + 1) * n + gi;
+        float4 b = *gm2;
+        b.x += (float)(wb * dpos[0]); b.y += (float)(wb * dpos[1]); b.z += (float)(wb * dpos[2]);
+        *gm2 = b;
+    }
+}
+
+void launch_chain(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
+                  const uint32_t* touched, float* screen, float4* grads, cudaStream_t st) {
+    if (S.n <= 0) return;
+    const int bs = 128;
+    k_chain<<<(S.n + bs - 1) / bs, bs, 0, st>>>(S, C, O, F, touched, screen, grads);
+}
+
+}  // namespace tsb

@@ -1,0 +1,121 @@
+// Internal definitions shared by the CUDA translation units and the C-ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tsb.h"
+
+namespace tsb {
+
+constexpr int kTile = 16;          // raster CTA block edge (pixels)
+constexpr int kRasterThreads = kTile * kTile;
+constexpr int kMaxKeyframes = 16;
+constexpr int kMaxArrays = 3 + kMaxKeyframes;  // pos_op, scale_amp, quat, motion[k]
+
+// Camera constants the kernels use (camera.hpp:9-49 + splat.cpp:109-111).
+struct CamK {
+    double fx, fy, cx, cy;
+    int W, H;
+    double near_plane;
+    double R[9], t[3];
+    double lim_x, lim_y;
+    double center[3];
+};
+
+// Render options (splat.hpp:28-37) in the forms the kernels compare against.
+struct OptK {
+    double alpha_thr, floor_T, dilation, sigma_cutoff, cov_eps, cut2;
+    int ts;            // binning tile size
+    int tiles_x, tiles_y;
+    int sub;           // 16x16 raster blocks per tile edge = ceil(ts/16)
+    float alpha_thr_f, floor_f, cut2_f, cov_eps_f;
+    double bg_quad[8];
+};
+
+// Device-resident scene (fp32 SoA float4 arrays; see tsb.h for the mapping).
+struct SceneK {
+    int n, nk, nf, sh_degree;
+    double freq[2], s_int, c;
+    const float4* pos_op;     // x, y, z, opacity_logit
+    const float4* scale_amp;  // log_scale xyz, reflectivity_dc
+    const float4* quat;       // w, x, y, z
+    const float4* motion;     // [nk][n] keyframe offsets (xyz, 0)
+};
+
+struct FrameK {
+    int key;
+    double w;
+};
+
+// fp32 raster records, indexed by Gaussian (SoA).  The conic is stored
+// factored, conic = L^T L, L = [[l11, l12], [0, l22]] (see tsb_raster.cu).
+struct RecK {
+    float4* A;  // base_x, base_y (integer rect origin), mean.x - base_x, mean.y - base_y
+    float4* B;  // l11, l12, l22, opacity
+    float4* C;  // coef, depth, sin(psi_0), cos(psi_0)
+    float4* D;  // sin(psi_1), cos(psi_1), 0, 0   (second frequency only)
+};
+
+// Per-pixel raster state written by the forward pass for the backward pass.
+struct PixK {
+    float* out;          // [C][H][W] planar outputs: quad(4*nf), depth_raw, depth, weight, T
+    int32_t* n_contrib;  // may be null
+    int32_t* n_processed;
+    int32_t* last;       // entries of the tile list the backward walks (bit 31: fp64-fixed)
+    float* T_pre;        // T before the last contributor
+    float* d_quad;       // [4*nf][H][W] upstream (written by loss epilogue)
+    int32_t* flagged;    // list of fp64-fixup pixels
+    int32_t* n_flagged;  // device counter
+};
+
+inline int out_channels(int nf) { return 4 * nf + 4; }
+// Channel plane index inside PixK::out.
+__host__ __device__ inline int ch_depth_raw(int nf) { return 4 * nf; }
+__host__ __device__ inline int ch_depth(int nf) { return 4 * nf + 1; }
+__host__ __device__ inline int ch_weight(int nf) { return 4 * nf + 2; }
+__host__ __device__ inline int ch_T(int nf) { return 4 * nf + 3; }
+
+// ---- launchers (defined in the .cu files) ----
+// tsb_geom.cu (fp64, compiled without FMA contraction)
+void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
+                       uint64_t* depth_key, uint32_t* gidx, uint32_t* touched, uint2* rect, RecK rec,
+                       int32_t* n_visible, cudaStream_t st);
+void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
+                  const uint2* ranges, const uint32_t* tile_vals, const PixK& px, int nf, cudaStream_t st);
+void launch_chain(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
+                  const uint32_t* touched, float* screen, float4* grads, cudaStream_t st);
+// tsb_bin.cu
+size_t binning_temp_bytes(int n, int64_t k_cap);
+void launch_gather_counts(const uint32_t* sorted_gidx, const uint32_t* touched, uint32_t* cnt_sorted,
+                          int n, cudaStream_t st);
+void launch_scan(const uint32_t* in, uint32_t* out, int n, void* temp, size_t temp_bytes,
+                 cudaStream_t st);
+void launch_sort_depth(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, uint32_t* vals_out,
+                       int n, void* temp, size_t temp_bytes, cudaStream_t st);
+void launch_duplicate(const uint32_t* sorted_gidx, const uint32_t* offsets, const uint32_t* cnt_sorted,
+                      const uint2* rect, uint16_t* keys, uint32_t* vals, int n, int ts, int tiles_x,
+                      cudaStream_t st);
+void launch_sort_tiles(uint16_t* keys_in, uint16_t* keys_out, uint32_t* vals_in, uint32_t* vals_out,
+                       int64_t k, int bits, void* temp, size_t temp_bytes, cudaStream_t st);
+void launch_ranges(const uint16_t* keys, int64_t k, uint2* ranges, int ntiles, cudaStream_t st);
+// tsb_raster.cu
+void launch_raster_fwd(const RecK& rec, const uint2* ranges, const uint32_t* tile_vals, const OptK& O,
+                       int W, int H, int nf, PixK px, const float* target, const float* ch_w,
+                       double* loss_part, cudaStream_t st);
+void launch_fixup_loss(const PixK& px, int W, int H, int nf, const float* target, const float* ch_w,
+                       double* loss_extra, int max_flag, cudaStream_t st);
+void launch_raster_bwd(const RecK& rec, const uint2* ranges, const uint32_t* tile_vals, const OptK& O,
+                       int W, int H, int nf, const float* dpsi, PixK px, const float* d_quad,
+                       float* screen, int scap, double* bg_part, cudaStream_t st);
+void launch_reduce_partials(const double* part, int nparts, int width, double* out,
+                            double scale, cudaStream_t st);
+// tsb_optim.cu
+void launch_pack_params(float4* dst, const float* src, int n, int comps, int comp0, int ncomp_dst,
+                        cudaStream_t st);
+void launch_unpack(const float4* src, float* dst, int n, int comps, int comp0, cudaStream_t st);
+void launch_adam(float4* params, float4* grads, float4* m, float4* v, int n, int narrays,
+                 const double* lr4 /* host [narrays*4] */, double beta1, double beta2, double eps,
+                 double bc1, double bc2, float* densify, cudaStream_t st);
+
+}  // namespace tsb

@@ -1,0 +1,83 @@
+// Parameter packing and the fused Adam step.
+//
+// Parameters, gradients and Adam moments share one layout: (3 + n_keyframes)
+// float4 arrays of n Gaussians each, contiguous (see tsb_internal.h).  One
+// thread per Gaussian walks every array (each access is a coalesced 16-B
+// vector load across the warp), which lets the densification statistic
+// (trainer.cpp:381-384) and the gradient clear ride along in the same pass.
+#include <cuda_runtime.h>
+
+#include "tsb_internal.h"
+
+namespace tsb {
+
+// dst[i].comp[comp0 + c] = src[i*comps + c] for c < comps (AoS-3/4 -> float4 lanes).
+__global__ void k_pack(float4* __restrict__ dst, const float* __restrict__ src, int n, int comps, int comp0) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float* d = reinterpret_cast<float*>(dst + i);
+    for (int c = 0; c < comps; ++c) d[comp0 + c] = src[(size_t)i * comps + c];
+}
+
+__global__ void k_unpack(const float4* __restrict__ src, float* __restrict__ dst, int n, int comps, int comp0) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float* s = reinterpret_cast<const float*>(src + i);
+    for (int c = 0; c < comps; ++c) dst[(size_t)i * comps + c] = s[comp0 + c];
+}
+
+void launch_pack_params(float4* dst, const float* src, int n, int comps, int comp0, int, cudaStream_t st) {
+    if (n <= 0) return;
+    k_pack<<<(n + 255) / 256, 256, 0, st>>>(dst, src, n, comps, comp0);
+}
+
+void launch_unpack(const float4* src, float* dst, int n, int comps, int comp0, cudaStream_t st) {
+    if (n <= 0) return;
+    k_unpack<<<(n + 255) / 256, 256, 0, st>>>(src, dst, n, comps, comp0);
+}
+
+struct LrTable {
+    float lr_bc1[kMaxArrays * 4];  // lr / (1 - beta1^t) per array component (0 for padding)
+};
+
+// AdamState::step (trainer.cpp:18-31) for every group at once:
+//   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;  p -= (lr/bc1) m / (sqrt(v/bc2) + eps)
+__global__ void __launch_bounds__(256) k_adam(float4* __restrict__ P, float4* __restrict__ G,
+                                              float4* __restrict__ M, float4* __restrict__ V, int n, int narrays,
+                                              LrTable lr, float b1, float b2, float eps, float inv_bc2,
+                                              float* __restrict__ densify) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float c1 = 1.f - b1, c2 = 1.f - b2;
+    for (int a = 0; a < narrays; ++a) {
+        const size_t k = (size_t)a * n + i;
+        const float4 g4 = G[k];
+        if (a == 0 && densify) densify[i] += sqrtf(g4.x * g4.x + g4.y * g4.y + g4.z * g4.z);
+        float4 p4 = P[k], m4 = M[k], v4 = V[k];
+        float* p = &p4.x;
+        float* m = &m4.x;
+        float* v = &v4.x;
+        const float* g = &g4.x;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            m[c] = b1 * m[c] + c1 * g[c];
+            v[c] = b2 * v[c] + c2 * (g[c] * g[c]);
+            p[c] -= lr.lr_bc1[a * 4 + c] * (m[c] / (sqrtf(v[c] * inv_bc2) + eps));
+        }
+        P[k] = p4;
+        M[k] = m4;
+        V[k] = v4;
+        G[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+void launch_adam(float4* params, float4* grads, float4* m, float4* v, int n, int narrays, const double* lr4,
+                 double beta1, double beta2, double eps, double bc1, double bc2, float* densify, cudaStream_t st) {
+    if (n <= 0) return;
+    LrTable t;
+    for (int i = 0; i < kMaxArrays * 4; ++i) t.lr_bc1[i] = i < narrays * 4 ? (float)(lr4[i] / bc1) : 0.f;
+    k_adam<<<(n + 255) / 256, 256, 0, st>>>(params, grads, m, v, n, narrays, t, (float)beta1, (float)beta2,
+                                            (float)eps, (float)(1.0 / bc2), densify);
+}
+
+}  // namespace tsb

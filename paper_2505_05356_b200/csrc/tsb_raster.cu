@@ -1,0 +1,451 @@
+// Tile rasterizer: forward composite (splat.cpp:209-339) and analytic backward
+// (splat.cpp:347-543) in fp32, one 16x16 CTA per tile, one thread per pixel.
+//
+// Records are staged per batch of 256 list entries in shared memory (each
+// thread loads one rank's record; every thread then reads the same entry ->
+// broadcast, conflict-free).  Termination is block-wide via
+// __syncthreads_count.
+//
+// Parity machinery: the reference decides maha <= cutoff^2,
+// alpha >= 1/255 and T < 1e-4 in fp64.  The fp32 composite tracks a bound on
+// its own error for each of those decisions; any pixel with a decision inside
+// its band is appended to a fix-up list and recomposited in fp64 by k_fixup
+// (tsb_geom.cu), so contributor counts match the fp64 reference exactly.
+//
+// Numerics: the conic is stored factored, conic = L^T L with
+// L = [[l11, l12], [0, l22]] (Cholesky, computed in fp64), so the Mahalanobis
+// distance is p^2 + q^2 with p = l11 dx + l12 dy, q = l22 dy.  That form has
+// no cancellation, unlike a dx^2 + 2b dx dy + c dy^2 (whose fp32 error grows
+// with the ellipse's condition number), and d(maha)/d(mean) falls out of p, q.
+#include <cuda_runtime.h>
+
+#include "tsb_internal.h"
+
+namespace tsb {
+
+constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // -0.5 * log2(e)
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Same bits in the forward and backward kernels: every operation is pinned with
+// an explicit-rounding intrinsic so the compiler cannot contract differently.
+struct Eval {
+    float dx, dy, p, q, maha, g, alpha;
+};
+
+__device__ __forceinline__ void eval_entry(const float4& A, const float4& B, float pcx, float pcy, Eval& e) {
+    e.dx = __fsub_rn(__fsub_rn(pcx, A.x), A.z);
+    e.dy = __fsub_rn(__fsub_rn(pcy, A.y), A.w);
+    e.p = __fmaf_rn(B.x, e.dx, __fmul_rn(B.y, e.dy));
+    e.q = __fmul_rn(B.z, e.dy);
+    e.maha = __fmaf_rn(e.p, e.p, __fmul_rn(e.q, e.q));
+}
+__device__ __forceinline__ void eval_alpha(const float4& B, Eval& e) {
+    e.g = ex2_approx(__fmul_rn(e.maha, kNegHalfLog2e));
+    e.alpha = __fmul_rn(B.w, e.g);
+}
+
+// Error-band constants: measured fp32-vs-fp64
+// maha error is ~1e-7 relative with the factored conic; alpha ~1.5e-6 relative.
+constexpr float kBandMaha = 2.0e-5f;   // relative to cutoff^2
+constexpr float kBandAlpha = 8.0e-6f;  // relative to the threshold
+constexpr float kEpsAlpha = 2.0e-6f;   // per-contributor alpha error used in the T bound
+
+template <int NF>
+struct Smem {
+    float4 A[kRasterThreads];
+    float4 B[kRasterThreads];
+    float4 C[kRasterThreads];
+    float4 D[NF > 1 ? kRasterThreads : 1];
+};
+
+// ---------------------------------------------------------------------------
+template <int NF>
+__global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, const uint2* __restrict__ ranges,
+                                                                const uint32_t* __restrict__ vals, OptK O, int W,
+                                                                int H, PixK px, const float* __restrict__ target,
+                                                                const float* __restrict__ chw,
+                                                                double* __restrict__ loss_part) {
+    __shared__ Smem<NF> sm;
+    __shared__ float red[kRasterThreads / 32];
+    const int nsub = O.sub * O.sub;
+    const int tile = blockIdx.x / nsub, sb = blockIdx.x % nsub;
+    const int tid = threadIdx.x;
+    const int lx = (sb % O.sub) * kTile + (tid % kTile), ly = (sb / O.sub) * kTile + (tid / kTile);
+    const int x = (tile % O.tiles_x) * O.ts + lx, y = (tile / O.tiles_x) * O.ts + ly;
+    const bool active = lx < O.ts && ly < O.ts && x < W && y < H;
+    const uint2 rg = ranges[tile];
+    const float pcx = (float)x + 0.5f, pcy = (float)y + 0.5f;
+
+    float T = 1.f, Tpre = 1.f, SW = 0.f, SD = 0.f, errT = 0.f;
+    float accS[NF], accC[NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) accS[f] = accC[f] = 0.f;
+    int nc = 0, processed = (int)(rg.y - rg.x), last_eff = -1;
+    bool done = !active, flag = false;
+    const float cut2 = O.cut2_f, thr = O.alpha_thr_f, fl = O.floor_f;
+    const float bandM = kBandMaha * cut2, bandA = kBandAlpha * thr;
+
+    for (uint32_t b = rg.x; b < rg.y; b += kRasterThreads) {
+        const uint32_t e = b + tid;
+        if (e < rg.y) {
+            const uint32_t r = vals[e];
+            sm.A[tid] = rec.A[r];
+            sm.B[tid] = rec.B[r];
+            sm.C[tid] = rec.C[r];
+            if (NF > 1) sm.D[tid] = rec.D[r];
+        }
+        __syncthreads();
+        if (!done) {
+            const int nb = min((uint32_t)kRasterThreads, rg.y - b);
+            for (int j = 0; j < nb; ++j) {
+                const float4 A = sm.A[j], B = sm.B[j];
+                Eval ev;
+                eval_entry(A, B, pcx, pcy, ev);
+                const float dm = ev.maha - cut2;
+                if (fabsf(dm) <= bandM) flag = true;
+                if (dm > 0.f) continue;
+                eval_alpha(B, ev);
+                const float da = ev.alpha - thr;
+                if (fabsf(da) <= bandA) flag = true;
+                if (da < 0.f) continue;
+                ++nc;
+                const float4 Cc = sm.C[j];
+                const float w = ev.alpha * T;
+                const float w2 = w * T;
+                const float cq = Cc.x * w2;
+                accS[0] = fmaf(cq, Cc.z, accS[0]);
+                accC[0] = fmaf(cq, Cc.w, accC[0]);
+                if (NF > 1) {
+                    const float4 Dd = sm.D[j];
+                    accS[NF - 1] = fmaf(cq, Dd.x, accS[NF - 1]);
+                    accC[NF - 1] = fmaf(cq, Dd.y, accC[NF - 1]);
+                }
+                SW += w;
+                SD = fmaf(w, Cc.y, SD);
+                Tpre = T;
+                const float om = 1.f - ev.alpha;
+                T = T * om;
+                errT += kEpsAlpha * __fdividef(ev.alpha, om) + 1.2e-7f;
+                if (T < fl * (1.f + 4.f * errT) && T > fl * (1.f - 4.f * errT)) flag = true;
+                if (T == 0.f && last_eff < 0) last_eff = (int)(b + j + 1 - rg.x);
+                if (T < fl) {
+                    processed = (int)(b + j + 1 - rg.x);
+                    done = true;
+                    break;
+                }
+            }
+        }
+        if (__syncthreads_count(done) == kRasterThreads) break;
+    }
+
+    float lpx = 0.f;
+    if (active) {
+        const size_t HW = (size_t)W * H, o = (size_t)y * W + x;
+        const float T2 = T * T;
+        float q[4 * NF];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            q[4 * f + 0] = accS[f] + (float)O.bg_quad[4 * f + 0] * T2;
+            q[4 * f + 1] = accC[f] + (float)O.bg_quad[4 * f + 1] * T2;
+            q[4 * f + 2] = -accS[f] + (float)O.bg_quad[4 * f + 2] * T2;
+            q[4 * f + 3] = -accC[f] + (float)O.bg_quad[4 * f + 3] * T2;
+        }
+#pragma unroll
+        for (int c = 0; c < 4 * NF; ++c) px.out[c * HW + o] = q[c];
+        px.out[ch_depth_raw(NF) * HW + o] = SD;
+        px.out[ch_depth(NF) * HW + o] = (double)SW > O.cov_eps ? SD / SW : __int_as_float(0x7fc00000);
+        px.out[ch_weight(NF) * HW + o] = SW;
+        px.out[ch_T(NF) * HW + o] = T;
+        if (px.n_contrib) px.n_contrib[o] = nc;
+        if (px.n_processed) px.n_processed[o] = processed;
+        px.last[o] = last_eff >= 0 ? last_eff : processed;
+        px.T_pre[o] = Tpre;
+        if (flag) {
+            const int slot = atomicAdd(px.n_flagged, 1);
+            px.flagged[slot] = (int)o;
+        } else if (target) {
+            const float s2 = 2.f / (float)HW;
+#pragma unroll
+            for (int c = 0; c < 4 * NF; ++c) {
+                const float r = q[c] - target[c * HW + o];
+                lpx = fmaf(chw[c] * r, r, lpx);
+                px.d_quad[c * HW + o] = chw[c] * s2 * r;
+            }
+        }
+    }
+    if (target) {
+        for (int m = 16; m > 0; m >>= 1) lpx += __shfl_xor_sync(0xffffffffu, lpx, m);
+        if ((tid & 31) == 0) red[tid >> 5] = lpx;
+        __syncthreads();
+        if (tid == 0) {
+            double s = 0.0;
+            for (int i = 0; i < kRasterThreads / 32; ++i) s += red[i];
+            loss_part[blockIdx.x] = s;
+        }
+    }
+}
+
+// Loss + d_quad for the fp64-fixed pixels (after k_fixup).
+__global__ void k_fixup_loss(PixK px, int W, int H, int nf, const float* __restrict__ target,
+                             const float* __restrict__ chw, double* __restrict__ loss_extra) {
+    const int count = *px.n_flagged;
+    double l = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+        const size_t HW = (size_t)W * H, o = (size_t)px.flagged[i];
+        const float s2 = 2.f / (float)HW;
+        for (int c = 0; c < 4 * nf; ++c) {
+            const float r = px.out[c * HW + o] - target[c * HW + o];
+            l += (double)(chw[c] * r * r);
+            px.d_quad[c * HW + o] = chw[c] * s2 * r;
+        }
+    }
+    for (int m = 16; m > 0; m >>= 1) l += __shfl_xor_sync(0xffffffffu, l, m);
+    if ((threadIdx.x & 31) == 0 && l != 0.0) atomicAdd(loss_extra, l);
+}
+
+// ---------------------------------------------------------------------------
+// Warp reduce-scatter of 8 per-lane values: 9 shuffles instead of 40.  On
+// return, lanes with (lane & 3) == 0 hold the warp sum of value index
+// ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1).
+__device__ __forceinline__ float reduce_scatter8(float v[8], int lane) {
+    {
+        const bool hi = lane & 16;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float send = hi ? v[i] : v[i + 4];
+            const float keep = hi ? v[i + 4] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+    }
+    {
+        const bool hi = lane & 8;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const float send = hi ? v[i] : v[i + 2];
+            const float keep = hi ? v[i + 2] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+    }
+    {
+        const bool hi = lane & 4;
+        const float send = hi ? v[0] : v[1];
+        const float keep = hi ? v[1] : v[0];
+        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    float s = v[0];
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    return s;
+}
+
+template <int NF>
+__global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const uint2* __restrict__ ranges,
+                                                                const uint32_t* __restrict__ vals, OptK O, int W,
+                                                                int H, float dpsi0, float dpsi1, PixK px,
+                                                                const float* __restrict__ d_quad,
+                                                                float* __restrict__ screen, int scap,
+                                                                double* __restrict__ bg_part) {
+    __shared__ Smem<NF> sm;
+    __shared__ uint32_t srank[kRasterThreads];
+    __shared__ float sacc[kRasterThreads][9];  // padded: 8 grads per entry
+    __shared__ int smax[kRasterThreads / 32];
+    __shared__ float sbg[kRasterThreads / 32][4 * NF];
+    const int nsub = O.sub * O.sub;
+    const int tile = blockIdx.x / nsub, sb = blockIdx.x % nsub;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int lx = (sb % O.sub) * kTile + (tid % kTile), ly = (sb / O.sub) * kTile + (tid / kTile);
+    const int x = (tile % O.tiles_x) * O.ts + lx, y = (tile / O.tiles_x) * O.ts + ly;
+    const bool active = lx < O.ts && ly < O.ts && x < W && y < H;
+    const uint2 rg = ranges[tile];
+    const float pcx = (float)x + 0.5f, pcy = (float)y + 0.5f;
+    const size_t HW = (size_t)W * H, o = (size_t)y * W + x;
+
+    int last = 0;
+    float Tnext = 0.f, A = 0.f;
+    float us[NF], uc[NF];
+    float bgc[4 * NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) us[f] = uc[f] = 0.f;
+#pragma unroll
+    for (int c = 0; c < 4 * NF; ++c) bgc[c] = 0.f;
+    if (active) {
+        last = px.last[o] & 0x7fffffff;
+        Tnext = px.T_pre[o];
+        const float Tf = px.out[ch_T(NF) * HW + o];
+        float up[4 * NF];
+#pragma unroll
+        for (int c = 0; c < 4 * NF; ++c) {
+            up[c] = d_quad[c * HW + o];
+            A = fmaf(up[c], (float)O.bg_quad[c], A);
+            bgc[c] = up[c] * Tf * Tf;
+        }
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            us[f] = up[4 * f + 0] - up[4 * f + 2];
+            uc[f] = up[4 * f + 1] - up[4 * f + 3];
+        }
+    }
+    // background gradient partials (splat.cpp:429-431)
+    if (bg_part) {
+#pragma unroll
+        for (int c = 0; c < 4 * NF; ++c) {
+            float v = bgc[c];
+            for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+            if (lane == 0) sbg[tid >> 5][c] = v;
+        }
+    }
+    int wmax = last;
+    for (int m = 16; m > 0; m >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, m));
+    if (lane == 0) smax[tid >> 5] = wmax;
+    for (int c = 0; c < 9; ++c) sacc[tid][c] = 0.f;
+    __syncthreads();
+    int bmax = 0;
+#pragma unroll
+    for (int i = 0; i < kRasterThreads / 32; ++i) bmax = max(bmax, smax[i]);
+    if (bg_part && tid < 4 * NF) {
+        double s = 0.0;
+        for (int i = 0; i < kRasterThreads / 32; ++i) s += sbg[i][tid];
+        bg_part[(size_t)blockIdx.x * 4 * NF + tid] = s;
+    }
+    bool first = true;
+    const float cut2 = O.cut2_f, thr = O.alpha_thr_f;
+
+    if (bmax > 0) {
+        const int nbatch = (bmax + kRasterThreads - 1) / kRasterThreads;
+        for (int bi = nbatch - 1; bi >= 0; --bi) {
+            const uint32_t b = rg.x + (uint32_t)bi * kRasterThreads;
+            const int nb = min(kRasterThreads, bmax - bi * kRasterThreads);
+            if (tid < nb) {
+                const uint32_t r = vals[b + tid];
+                srank[tid] = r;
+                sm.A[tid] = rec.A[r];
+                sm.B[tid] = rec.B[r];
+                sm.C[tid] = rec.C[r];
+                if (NF > 1) sm.D[tid] = rec.D[r];
+            }
+            __syncthreads();
+            for (int j = nb - 1; j >= 0; --j) {
+                const int el = bi * kRasterThreads + j;
+                bool contrib = false;
+                float g8[8];
+                if (el < last) {
+                    const float4 Aa = sm.A[j], Bb = sm.B[j];
+                    Eval ev;
+                    eval_entry(Aa, Bb, pcx, pcy, ev);
+                    if (!(ev.maha - cut2 > 0.f)) {
+                        eval_alpha(Bb, ev);
+                        if (!(ev.alpha - thr < 0.f)) {
+                            contrib = true;
+                            const float om = 1.f - ev.alpha;
+                            const float Tk = first ? Tnext : __fdiv_rn(Tnext, om);
+                            first = false;
+                            Tnext = Tk;
+                            const float4 Cc = sm.C[j];
+                            const float coef = Cc.x;
+                            float su = us[0] * Cc.z + uc[0] * Cc.w;       // upQ . basis
+                            float sd = dpsi0 * (us[0] * Cc.w - uc[0] * Cc.z);  // upQ . dbasis
+                            if (NF > 1) {
+                                const float4 Dd = sm.D[j];
+                                su += us[NF - 1] * Dd.x + uc[NF - 1] * Dd.y;
+                                sd += dpsi1 * (us[NF - 1] * Dd.y - uc[NF - 1] * Dd.x);
+                            }
+                            const float UQ = coef * su;
+                            const float T2 = Tk * Tk;
+                            const float w2 = ev.alpha * T2;
+                            const float d_alpha = T2 * (UQ + 2.f * (ev.alpha - 1.f) * A);
+                            A = ev.alpha * UQ + om * om * A;
+                            const float dpow = ev.alpha * d_alpha;
+                            g8[0] = dpow * (Bb.x * ev.p);
+                            g8[1] = dpow * (Bb.y * ev.p + Bb.z * ev.q);
+                            g8[2] = -0.5f * ev.dx * ev.dx * dpow;
+                            g8[3] = -ev.dx * ev.dy * dpow;
+                            g8[4] = -0.5f * ev.dy * ev.dy * dpow;
+                            g8[5] = ev.g * d_alpha;
+                            g8[6] = w2 * su;
+                            g8[7] = w2 * coef * sd;
+                        }
+                    }
+                }
+                if (__any_sync(0xffffffffu, contrib)) {
+                    if (!contrib) {
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) g8[c] = 0.f;
+                    }
+                    const float s = reduce_scatter8(g8, lane);
+                    if ((lane & 3) == 0) {
+                        const int vi = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+                        atomicAdd(&sacc[j][vi], s);
+                    }
+                }
+            }
+            __syncthreads();
+            if (tid < nb) {
+                const uint32_t r = srank[tid];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const float v = sacc[tid][c];
+                    if (v != 0.f) atomicAdd(&screen[(size_t)c * scap + r], v);
+                    sacc[tid][c] = 0.f;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+void launch_raster_fwd(const RecK& rec, const uint2* ranges, const uint32_t* tile_vals, const OptK& O, int W,
+                       int H, int nf, PixK px, const float* target, const float* ch_w, double* loss_part,
+                       cudaStream_t st) {
+    const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
+    if (nf > 1)
+        k_raster_fwd<2><<<grid, kRasterThreads, 0, st>>>(rec, ranges, tile_vals, O, W, H, px, target, ch_w, loss_part);
+    else
+        k_raster_fwd<1><<<grid, kRasterThreads, 0, st>>>(rec, ranges, tile_vals, O, W, H, px, target, ch_w, loss_part);
+}
+
+void launch_fixup_loss(const PixK& px, int W, int H, int nf, const float* target, const float* ch_w,
+                       double* loss_extra, int max_flag, cudaStream_t st) {
+    (void)max_flag;
+    k_fixup_loss<<<64, 256, 0, st>>>(px, W, H, nf, target, ch_w, loss_extra);
+}
+
+void launch_raster_bwd(const RecK& rec, const uint2* ranges, const uint32_t* tile_vals, const OptK& O, int W,
+                       int H, int nf, const float* dpsi, PixK px, const float* d_quad, float* screen, int scap,
+                       double* bg_part, cudaStream_t st) {
+    const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
+    if (nf > 1)
+        k_raster_bwd<2><<<grid, kRasterThreads, 0, st>>>(rec, ranges, tile_vals, O, W, H, dpsi[0], dpsi[1], px,
+                                                        d_quad, screen, scap, bg_part);
+    else
+        k_raster_bwd<1><<<grid, kRasterThreads, 0, st>>>(rec, ranges, tile_vals, O, W, H, dpsi[0], 0.f, px,
+                                                        d_quad, screen, scap, bg_part);
+}
+
+__global__ void k_reduce_partials(const double* __restrict__ part, int nparts, int width,
+                                  double* __restrict__ out, double scale) {
+    // one block; column c summed in a fixed order (deterministic)
+    __shared__ double s[256];
+    for (int c = 0; c < width; ++c) {
+        double a = 0.0;
+        for (int i = threadIdx.x; i < nparts; i += blockDim.x) a += part[(size_t)i * width + c];
+        s[threadIdx.x] = a;
+        __syncthreads();
+        for (int m = blockDim.x / 2; m > 0; m >>= 1) {
+            if ((int)threadIdx.x < m) s[threadIdx.x] += s[threadIdx.x + m];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) out[c] = (out[c] + s[0]) * scale;
+        __syncthreads();
+    }
+}
+
+void launch_reduce_partials(const double* part, int nparts, int width, double* out, double scale, cudaStream_t st) {
+    k_reduce_partials<<<1, 256, 0, st>>>(part, nparts, width, out, scale);
+}
+
+}  // namespace tsb

@@ -1,0 +1,464 @@
+"""Python mirror of the reference renderer / optimiser API over the C ABI.
+
+Reference names are kept: ``CameraModel`` (camera.hpp:9-49), ``ToFConfig``
+(tof.hpp:13-21), ``RenderOptions`` (splat.hpp:28-37), ``RenderPass`` with
+``forward`` / ``backward`` / ``visible_count`` (splat.hpp:97-112),
+``AdamParams`` / ``LrTable`` (trainer.hpp:14-44).  The Gaussian parameters
+live on the GPU in a ``GaussianScene`` (the device counterpart of
+``CanonicalScene`` + the trainer's ``Params`` / ``GroupGrads`` / ``AdamState``,
+trainer.cpp:63-132), so a training loop never copies them to the host.
+
+Every method calls libtsb.so; nothing here computes on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+from ._abi import check, lib
+
+SH_C0 = 0.28209479177387814
+
+
+@dataclass
+class ToFConfig:
+    """tof.hpp:13-21; a second frequency renders a second quad sharing geometry."""
+    modulation_frequency: float = 29.9792458e6
+    source_intensity: float = 1.0
+    speed_of_light: float = 299792458.0
+    second_frequency: Optional[float] = None
+
+    @property
+    def frequencies(self):
+        f = [self.modulation_frequency]
+        if self.second_frequency:
+            f.append(self.second_frequency)
+        return f
+
+
+@dataclass
+class CameraModel:
+    """Pinhole camera, pixel centres at +0.5, p_cam = R p + t (camera.hpp:9-49)."""
+    fx: float = 1.0
+    fy: float = 1.0
+    cx: float = 0.0
+    cy: float = 0.0
+    width: int = 0
+    height: int = 0
+    near_plane: float = 0.2
+    far_plane: float = 100.0
+    rotation: np.ndarray = field(default_factory=lambda: np.eye(3))
+    translation: np.ndarray = field(default_factory=lambda: np.zeros(3))
+
+    def valid(self) -> bool:
+        return (self.fx > 0 and self.fy > 0 and self.width > 0 and self.height > 0 and self.near_plane > 0
+                and self.far_plane > self.near_plane)
+
+    def to_abi(self) -> _abi.Camera:
+        c = _abi.Camera()
+        c.fx, c.fy, c.cx, c.cy = float(self.fx), float(self.fy), float(self.cx), float(self.cy)
+        c.width, c.height = int(self.width), int(self.height)
+        c.near_plane, c.far_plane = float(self.near_plane), float(self.far_plane)
+        R = np.asarray(self.rotation, dtype=np.float64).reshape(9)
+        t = np.asarray(self.translation, dtype=np.float64).reshape(3)
+        for i in range(9):
+            c.R[i] = R[i]
+        for i in range(3):
+            c.t[i] = t[i]
+        return c
+
+
+@dataclass
+class RenderOptions:
+    """splat.hpp:28-37 (+ Backgrounds::quad, 4 values per frequency)."""
+    alpha_threshold: float = 1.0 / 255.0
+    transmittance_floor: float = 1e-4
+    dilation: float = 0.3
+    sigma_cutoff: float = 3.0
+    coverage_eps: float = 1e-12
+    tile_size: int = 16
+    bg_quad: Sequence[float] = (0.0, 0.0, 0.0, 0.0)
+    counts: bool = False  # also emit per-pixel n_contrib / n_processed (parity diagnostics)
+
+    def to_abi(self) -> _abi.RenderOptions:
+        o = _abi.RenderOptions()
+        o.alpha_threshold = float(self.alpha_threshold)
+        o.transmittance_floor = float(self.transmittance_floor)
+        o.dilation = float(self.dilation)
+        o.sigma_cutoff = float(self.sigma_cutoff)
+        o.coverage_eps = float(self.coverage_eps)
+        o.tile_size = int(self.tile_size)
+        o.channels = _abi.CH_QUAD | _abi.CH_DEPTH | _abi.CH_WEIGHT | _abi.CH_TRANSM | (
+            _abi.CH_COUNTS if self.counts else 0)
+        bq = np.zeros(8)
+        b = np.asarray(self.bg_quad, dtype=np.float64).reshape(-1)[:8]
+        bq[: b.size] = b
+        for i in range(8):
+            o.bg_quad[i] = bq[i]
+        return o
+
+
+@dataclass
+class AdamParams:
+    """trainer.hpp:14-18."""
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-15
+
+
+@dataclass
+class LrTable:
+    """Per-group learning rates, already resolved (trainer.cpp:339-366: position lr
+    is multiplied by the scene extent there; reflectivity uses appearance/10)."""
+    position: float = 1.6e-4
+    log_scale: float = 5e-3
+    rotation: float = 1e-3
+    opacity: float = 0.05
+    reflectivity: float = 1.6e-4
+    motion: float = 1.6e-4
+
+    @staticmethod
+    def uniform(lr: float) -> "LrTable":
+        return LrTable(lr, lr, lr, lr, lr, lr)
+
+
+def frame_for_time(t: float, n_keyframes: int):
+    """Keyframe segment and weight for normalised time t in [0, 1]: i = floor(t K),
+    w = t K - i with K = n_keyframes - 1 (the trajectory lerp of trainer.cpp:259-279 /
+    deform.cpp:248-251 between tick offsets)."""
+    if n_keyframes < 2:
+        return 0, 0.0
+    K = n_keyframes - 1
+    i = min(int(math.floor(t * K)), K - 1)
+    return i, t * K - i
+
+
+class Context:
+    """One CUDA stream on one GPU (tsb_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib().tsb_ctx_create(int(device), C.byref(h)))
+        self._h = h
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def stream(self) -> int:
+        return int(lib().tsb_ctx_stream(self._h) or 0)
+
+    def synchronize(self):
+        check(lib().tsb_ctx_synchronize(self._h))
+
+    def launch_count(self) -> int:
+        return int(lib().tsb_ctx_launch_count(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tsb_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _f32(a, n, comps):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+    if a.size != n * comps:
+        raise RuntimeError(f"render: parameter count mismatch (expected {n}x{comps}, got {a.shape})")
+    return a
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(_abi._fp)
+
+
+class GaussianScene:
+    """Device-resident Gaussian parameters, gradients and Adam moments."""
+
+    def __init__(self, ctx: Context, n: int, n_keyframes: int = 0, tof: Optional[ToFConfig] = None,
+                 sh_degree: int = 0):
+        tof = tof or ToFConfig()
+        d = _abi.SceneDesc()
+        d.n, d.n_keyframes, d.sh_degree = int(n), int(n_keyframes), int(sh_degree)
+        fr = tof.frequencies
+        d.n_freq = len(fr)
+        for i, f in enumerate(fr):
+            d.frequency[i] = float(f)
+        d.source_intensity = float(tof.source_intensity)
+        d.speed_of_light = float(tof.speed_of_light)
+        h = C.c_void_p()
+        check(lib().tsb_scene_create(ctx.handle, C.byref(d), C.byref(h)))
+        self._h, self.ctx, self.n, self.n_keyframes, self.tof = h, ctx, int(n), int(n_keyframes), tof
+        self.n_freq = d.n_freq
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_params(self, position, log_scale, rotation, opacity_logit, reflectivity_dc, motion=None):
+        """Host numpy arrays (float32 SoA: position (n,3), log_scale (n,3), rotation (n,4) wxyz,
+        opacity_logit (n,), reflectivity_dc (n,), motion (n_keyframes, n, 3))."""
+        n = self.n
+        arrs = [_f32(position, n, 3), _f32(log_scale, n, 3), _f32(rotation, n, 4), _f32(opacity_logit, n, 1),
+                _f32(reflectivity_dc, n, 1)]
+        mo = None
+        if motion is not None and self.n_keyframes > 0:
+            mo = _f32(motion, n, 3 * self.n_keyframes)
+        check(lib().tsb_scene_set_params(self._h, _abi.TSB_HOST, *[a.ctypes.data for a in arrs],
+                                         mo.ctypes.data if mo is not None else None))
+
+    def set_params_device(self, position, log_scale, rotation, opacity_logit, reflectivity_dc, motion=None):
+        """Device pointers (ints) in the same SoA layout."""
+        check(lib().tsb_scene_set_params(self._h, _abi.TSB_DEVICE, position, log_scale, rotation, opacity_logit,
+                                         reflectivity_dc, motion))
+
+    def get_params(self):
+        n, k = self.n, self.n_keyframes
+        out = {"position": np.zeros((n, 3), np.float32), "log_scale": np.zeros((n, 3), np.float32),
+               "rotation": np.zeros((n, 4), np.float32), "opacity_logit": np.zeros(n, np.float32),
+               "reflectivity_dc": np.zeros(n, np.float32), "motion": np.zeros((k, n, 3), np.float32)}
+        check(lib().tsb_scene_get_params(self._h, _ptr(out["position"]), _ptr(out["log_scale"]),
+                                         _ptr(out["rotation"]), _ptr(out["opacity_logit"]),
+                                         _ptr(out["reflectivity_dc"]), _ptr(out["motion"]) if k else None))
+        return out
+
+    def grads(self):
+        """Accumulated GroupGrads (+ d_bg_quad, loss sum)."""
+        n, k = self.n, self.n_keyframes
+        g = {"d_position": np.zeros((n, 3), np.float32), "d_log_scale": np.zeros((n, 3), np.float32),
+             "d_rotation": np.zeros((n, 4), np.float32), "d_opacity_logit": np.zeros(n, np.float32),
+             "d_reflectivity_dc": np.zeros(n, np.float32), "d_motion": np.zeros((k, n, 3), np.float32),
+             "d_bg_quad": np.zeros(8), }
+        loss = C.c_double()
+        check(lib().tsb_scene_get_grads(self._h, _ptr(g["d_position"]), _ptr(g["d_log_scale"]),
+                                        _ptr(g["d_rotation"]), _ptr(g["d_opacity_logit"]),
+                                        _ptr(g["d_reflectivity_dc"]), _ptr(g["d_motion"]) if k else None,
+                                        g["d_bg_quad"].ctypes.data_as(_abi._dp), C.byref(loss)))
+        g["d_bg_quad"] = g["d_bg_quad"][: 4 * self.n_freq]
+        g["loss"] = loss.value
+        return g
+
+    def zero_grads(self):
+        check(lib().tsb_scene_zero_grads(self._h))
+
+    def adam_step(self, lr: LrTable, adam: AdamParams = AdamParams()):
+        cfg = _abi.AdamConfig(lr.position, lr.log_scale, lr.rotation, lr.opacity, lr.reflectivity, lr.motion,
+                              adam.beta1, adam.beta2, adam.eps)
+        check(lib().tsb_scene_adam_step(self._h, C.byref(cfg)))
+
+    def adam_moments_position(self):
+        m = np.zeros((self.n, 3), np.float32)
+        v = np.zeros((self.n, 3), np.float32)
+        check(lib().tsb_scene_get_adam_state(self._h, _ptr(m), _ptr(v)))
+        return m, v
+
+    def densify_stat(self):
+        s = np.zeros(self.n, np.float32)
+        c = C.c_int64()
+        check(lib().tsb_scene_get_densify_stat(self._h, _ptr(s), C.byref(c)))
+        return s, c.value
+
+    def allreduce_grads(self, comm: "Comm"):
+        check(lib().tsb_scene_allreduce_grads(self._h, comm.handle))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tsb_scene_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class RenderPass:
+    """Reusable per-frame workspace; ``prepare`` is the reference RenderPass ctor
+    (prepare + depth sort + build_tiles, splat.cpp:90-200)."""
+
+    def __init__(self, ctx: Context):
+        h = C.c_void_p()
+        check(lib().tsb_pass_create(ctx.handle, C.byref(h)))
+        self._h, self.ctx = h, ctx
+        self.scene = None
+        self.camera = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def prepare(self, scene: GaussianScene, camera: CameraModel, options: Optional[RenderOptions] = None,
+                frame=None):
+        options = options or RenderOptions()
+        cam = camera.to_abi() if hasattr(camera, "to_abi") else camera
+        fr = None
+        if frame is not None:
+            fr = _abi.Frame()
+            fr.key, fr.w = int(frame[0]), float(frame[1])
+        self._cam, self._opt = cam, options.to_abi()
+        check(lib().tsb_pass_prepare(self._h, scene.handle, C.byref(self._cam), C.byref(self._opt),
+                                     C.byref(fr) if fr is not None else None))
+        self.scene, self.camera, self.options = scene, camera, options
+        return self
+
+    def visible_count(self) -> int:
+        v = C.c_int32()
+        check(lib().tsb_pass_visible_count(self._h, C.byref(v)))
+        return v.value
+
+    def num_keys(self) -> int:
+        v = C.c_int64()
+        check(lib().tsb_pass_num_keys(self._h, C.byref(v)))
+        return v.value
+
+    def forward(self):
+        check(lib().tsb_pass_forward(self._h))
+        return self
+
+    def forward_loss(self, target, channel_weight=None, sync=True, device_ptr=None):
+        """Forward + fused L2 loss (sum_c w_c mse_c; reference trainer weight quad/4 per
+        channel, trainer.cpp:210-219).  target: host array (4*n_freq, H, W) or a device pointer."""
+        nf = self.scene.n_freq
+        if channel_weight is None:
+            channel_weight = [0.25] * (4 * nf)
+        w = (C.c_double * 8)(*([float(x) for x in channel_weight] + [0.0] * (8 - len(channel_weight))))
+        loss = C.c_double()
+        if device_ptr is not None:
+            check(lib().tsb_pass_forward_loss(self._h, _abi.TSB_DEVICE, C.c_void_p(device_ptr), w,
+                                              C.byref(loss) if sync else None))
+        else:
+            t = np.ascontiguousarray(np.asarray(target, dtype=np.float32))
+            self._target_keep = t
+            check(lib().tsb_pass_forward_loss(self._h, _abi.TSB_HOST, t.ctypes.data, w,
+                                              C.byref(loss) if sync else None))
+        return loss.value if sync else None
+
+    def backward(self, d_quad=None, device_ptr=None):
+        """Accumulate gradients into the scene (uses the loss residual when d_quad is None)."""
+        if device_ptr is not None:
+            check(lib().tsb_pass_backward(self._h, _abi.TSB_DEVICE, C.c_void_p(device_ptr)))
+        elif d_quad is not None:
+            up = np.ascontiguousarray(np.asarray(d_quad, dtype=np.float32))
+            self._up_keep = up
+            check(lib().tsb_pass_backward(self._h, _abi.TSB_HOST, up.ctypes.data))
+        else:
+            check(lib().tsb_pass_backward(self._h, _abi.TSB_HOST, None))
+        return self
+
+    def output_ptr(self, which: int):
+        p = C.c_void_p()
+        nb = C.c_size_t()
+        check(lib().tsb_pass_output(self._h, which, C.byref(p), C.byref(nb)))
+        return p.value, nb.value
+
+    def download(self, which: int, dtype=np.float32, shape=None):
+        _, nb = self.output_ptr(which)
+        a = np.empty(nb // 4, dtype=dtype)
+        check(lib().tsb_pass_download(self._h, which, a.ctypes.data, nb))
+        return a.reshape(shape) if shape is not None else a
+
+    def outputs(self):
+        """RenderedBuffers (splat.hpp:51-66) subset: quad, depth_raw, depth, weight, transmittance."""
+        H, W, nf = self.camera.height, self.camera.width, self.scene.n_freq
+        out = {"quad": self.download(_abi.OUT_QUAD, shape=(4 * nf, H, W)),
+               "depth_raw": self.download(_abi.OUT_DEPTH_RAW, shape=(H, W)),
+               "depth": self.download(_abi.OUT_DEPTH, shape=(H, W)),
+               "weight": self.download(_abi.OUT_WEIGHT, shape=(H, W)),
+               "transmittance": self.download(_abi.OUT_TRANSM, shape=(H, W))}
+        if self.options.counts:
+            out["n_contrib"] = self.download(_abi.OUT_N_CONTRIB, np.int32, (H, W))
+            out["n_processed"] = self.download(_abi.OUT_N_PROCESSED, np.int32, (H, W))
+        return out
+
+    # ---- parity diagnostics ----
+    def debug_prepared(self):
+        v = self.visible_count()
+        g = np.zeros(max(v, 1), np.int32)
+        r = np.zeros((max(v, 1), 4), np.int32)
+        check(lib().tsb_pass_debug_prepared(self._h, g.ctypes.data_as(_abi._ip), r.ctypes.data_as(_abi._ip)))
+        return {"gidx": g[:v], "rect": r[:v]}
+
+    def debug_tiles(self):
+        tx, ty = C.c_int32(), C.c_int32()
+        check(lib().tsb_pass_debug_tiles(self._h, C.byref(tx), C.byref(ty), None, None))
+        k = self.num_keys()
+        off = np.zeros(tx.value * ty.value + 1, np.int64)
+        ids = np.zeros(max(k, 1), np.int32)
+        check(lib().tsb_pass_debug_tiles(self._h, None, None, off.ctypes.data_as(_abi._lp),
+                                         ids.ctypes.data_as(_abi._ip)))
+        return off, ids[:k]
+
+    def debug_records(self):
+        v = self.visible_count()
+        r = np.zeros((max(v, 1), 12), np.float32)
+        check(lib().tsb_pass_debug_records(self._h, _ptr(r)))
+        return r[:v]
+
+    def debug_fixups(self) -> int:
+        c = C.c_int32()
+        check(lib().tsb_pass_debug_fixups(self._h, C.byref(c)))
+        return c.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tsb_pass_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Comm:
+    """NCCL communicator for frame-sharded data parallelism (tsb_comm)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_char * 128)()
+        check(lib().tsb_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, ctx: Context, uid: bytes, nranks: int, rank: int):
+        h = C.c_void_p()
+        buf = (C.c_char * 128).from_buffer_copy(uid)
+        check(lib().tsb_comm_create(ctx.handle, buf, int(nranks), int(rank), C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tsb_comm_destroy(self._h)
+            self._h = None
+
+
+# ---- Python _core surface (bindings.cpp:43-63) ----
+def unambiguous_range(frequency: float = 0.0) -> float:
+    return float(lib().tsb_unambiguous_range(float(frequency)))
+
+
+def quad_to_depth(q0, q90, q180, q270, frequency: float = 0.0) -> float:
+    return float(lib().tsb_quad_to_depth(float(q0), float(q90), float(q180), float(q270), float(frequency)))
+
+
+def quad_basis(depth: float, frequency: float = 0.0):
+    out = (C.c_double * 4)()
+    lib().tsb_quad_basis(float(depth), float(frequency), out)
+    return list(out)

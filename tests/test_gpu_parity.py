@@ -1,0 +1,263 @@
+"""Parity of the B200 path (through the C ABI) against the CPU oracle.
+
+Integer work must match bit for bit (prepared order, tile rects, per-tile lists,
+tile ranges, per-pixel contributor counts); floating point within the tolerances
+of BASELINE.json's north_star: rendered raw samples 1e-4 relative, gradients
+1e-3 relative (floors as in SURVEY.md App. D)."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+
+from helpers import gpu_scene, oracle_scene, rel_err
+
+pytestmark = pytest.mark.gpu
+
+QUAD_TOL = 1e-4
+GRAD_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def tsb():
+    import paper_2505_05356_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(tsb):
+    return tsb.Context(0)
+
+
+def render_both(tsb, ctx, gset, cam, tof, frame, opts, freq_index=0):
+    scene = gpu_scene(tsb, ctx, gset, tof)
+    rp = tsb.RenderPass(ctx).prepare(scene, cam, opts, frame).forward()
+    out = rp.outputs()
+    op = orc.OraclePass(oracle_scene(gset, frame, tof, freq_index), cam, opts)
+    return scene, rp, out, op, op.forward()
+
+
+def check_integers(rp, op, out, ref):
+    assert rp.visible_count() == op.visible_count()
+    gp, oprep = rp.debug_prepared(), op.prepared()
+    assert np.array_equal(gp["gidx"], oprep["gidx"]), "global (depth, index) order differs"
+    assert np.array_equal(gp["rect"], oprep["rect"]), "tile rects differ"
+    goff, gids = rp.debug_tiles()
+    ooff, oids = op.tile_lists()
+    assert rp.num_keys() == op.num_keys()
+    assert np.array_equal(goff, ooff), "tile ranges differ"
+    assert np.array_equal(gids, oids), "per-tile sorted lists differ"
+    assert np.array_equal(out["n_contrib"], ref["n_contrib"]), \
+        f"contributor counts differ at {np.argwhere(out['n_contrib'] != ref['n_contrib'])[:5]}"
+    assert np.array_equal(out["n_processed"], ref["n_processed"]), "termination indices differ"
+
+
+def check_images(out, ref, nf=1, f=0):
+    q = out["quad"][4 * f: 4 * f + 4]
+    assert rel_err(q, ref["quad"]) < QUAD_TOL
+    for k in ("depth_raw", "weight", "transmittance"):
+        assert rel_err(out[k], ref[k]) < QUAD_TOL, k
+    assert rel_err(out["depth"], ref["depth"]) < QUAD_TOL
+
+
+def test_c0_forward_full(tsb, ctx):
+    from paper_2505_05356_b200 import synthetic
+    cfg = synthetic.config("c0")
+    opts = tsb.RenderOptions(counts=True)
+    _, rp, out, op, ref = render_both(tsb, ctx, cfg.scene, cfg.camera, cfg.tof, cfg.frames[0], opts)
+    check_integers(rp, op, out, ref)
+    check_images(out, ref)
+    # records (fp64 preprocess rounded once to fp32) vs oracle, 1e-6 rel
+    rec = rp.debug_records()
+    orec = op.prepared()["rec"]
+    assert rel_err(rec[:, 5], orec[:, 5], 1e-9) < 1e-6  # opacity
+    assert rel_err(rec[:, 6], orec[:, 6], 1e-9) < 1e-6  # coef
+    assert rel_err(rec[:, 7], orec[:, 9], 1e-9) < 1e-6  # depth
+
+
+@pytest.mark.parametrize("tile_size", [5, 16, 32])
+def test_tile_size_invariance_and_lists(tsb, ctx, tile_size):
+    """test_splat.cpp:235-266: tile size never changes the result; lists must match the oracle."""
+    from paper_2505_05356_b200 import synthetic
+    g = synthetic.gaussians(3000, 5, n_keyframes=2)
+    cam = synthetic.camera(200, 150, 180.0)
+    opts = tsb.RenderOptions(tile_size=tile_size, counts=True, bg_quad=(0.3, 0.1, -0.2, 0.4))
+    _, rp, out, op, ref = render_both(tsb, ctx, g, cam, synthetic.ToFConfig(30e6), (0, 0.25), opts)
+    check_integers(rp, op, out, ref)
+    check_images(out, ref)
+
+
+def test_empty_scene_background(tsb, ctx):
+    """test_splat.cpp:62-103: an empty scene passes the background through."""
+    from paper_2505_05356_b200 import synthetic
+    g = synthetic.gaussians(0, 0)
+    cam = synthetic.camera(64, 48, 40.0)
+    opts = tsb.RenderOptions(bg_quad=(1.0, 2.0, 3.0, 4.0), counts=True)
+    scene = gpu_scene(tsb, ctx, g, synthetic.ToFConfig())
+    rp = tsb.RenderPass(ctx).prepare(scene, cam, opts)
+    assert rp.visible_count() == 0
+    rp.forward()
+    out = rp.outputs()
+    assert (out["transmittance"] == 1.0).all() and (out["weight"] == 0.0).all()
+    for c in range(4):
+        assert (out["quad"][c] == c + 1.0).all()
+    assert np.isnan(out["depth"]).all()
+    rp.backward(np.ones((4, 48, 64), np.float32))
+    gr = scene.grads()
+    assert np.allclose(gr["d_bg_quad"], 64 * 48)
+
+
+def test_single_splat_closed_form(tsb, ctx):
+    """test_splat.cpp:105-143: one on-axis splat has a closed-form footprint."""
+    from paper_2505_05356_b200 import synthetic
+    from paper_2505_05356_b200.render import SH_C0
+    cam = tsb.CameraModel(fx=50.0, fy=50.0, cx=32.5, cy=24.5, width=64, height=48)
+    z, s, o, r = 2.0, 0.2, 0.7, 0.5
+    g = synthetic.GaussianSet(np.array([[0, 0, z]], np.float32), np.full((1, 3), math.log(s), np.float32),
+                              np.array([[1, 0, 0, 0]], np.float32), np.array([math.log(o / (1 - o))], np.float32),
+                              np.array([r / SH_C0], np.float32))
+    tof = tsb.ToFConfig()
+    opts = tsb.RenderOptions(bg_quad=(0.3, 0.1, -0.2, 0.4))
+    scene = gpu_scene(tsb, ctx, g, tof)
+    rp = tsb.RenderPass(ctx).prepare(scene, cam, opts).forward()
+    out = rp.outputs()
+    var = (cam.fx * s / z) ** 2 + 0.3
+    psi = 4 * math.pi * z * tof.modulation_frequency / tof.speed_of_light
+    basis = [math.sin(psi), math.cos(psi), -math.sin(psi), -math.cos(psi)]
+    coef = r / (z * z)
+    o32 = float(np.float32(1.0) / (np.float32(1.0) + np.exp(-np.float32(math.log(o / (1 - o))))))
+    for dx, dy in [(0, 0), (1, 0), (0, 2), (-3, 4), (5, -2)]:
+        x, y = 32 + dx, 24 + dy
+        alpha = o32 * math.exp(-0.5 * (dx * dx + dy * dy) / var)
+        assert out["weight"][y, x] == pytest.approx(alpha, rel=2e-6)
+        assert out["transmittance"][y, x] == pytest.approx(1 - alpha, rel=2e-6)
+        assert out["depth"][y, x] == pytest.approx(z, rel=1e-6)
+        t = 1 - alpha
+        for c in range(4):
+            want = coef * alpha * basis[c] + opts.bg_quad[c] * t * t
+            assert out["quad"][c, y, x] == pytest.approx(want, rel=1e-5, abs=1e-6)
+    assert out["weight"][0, 0] == 0.0 and np.isnan(out["depth"][0, 0])
+
+
+def test_layered_splats_known_quartet(tsb, ctx):
+    """test_splat.cpp:177-217 / acceptance check 3: quad (0, cos 2pi/5, 0, -cos 2pi/5), weight 1, depth 2.5."""
+    from paper_2505_05356_b200 import synthetic
+    from paper_2505_05356_b200.render import SH_C0
+    cam = tsb.CameraModel(fx=40.0, fy=40.0, cx=32.5, cy=24.5, width=64, height=48)
+    g = synthetic.GaussianSet(np.array([[0, 0, 1.0], [0, 0, 4.0]], np.float32),
+                              np.log(np.array([[0.1] * 3, [0.4] * 3], np.float32)),
+                              np.array([[1, 0, 0, 0]] * 2, np.float32), np.array([0.0, 40.0], np.float32),
+                              np.array([1 / 32 / SH_C0, 1 / SH_C0], np.float32))
+    tof = tsb.ToFConfig(source_intensity=32.0)
+    scene = gpu_scene(tsb, ctx, g, tof)
+    rp = tsb.RenderPass(ctx).prepare(scene, cam, tsb.RenderOptions()).forward()
+    out = rp.outputs()
+    c5 = math.cos(2 * math.pi / 5)
+    q = out["quad"][:, 24, 32]
+    assert q[0] == pytest.approx(0.0, abs=1e-6) and q[2] == pytest.approx(0.0, abs=1e-6)
+    assert q[1] == pytest.approx(c5, rel=1e-5) and q[3] == pytest.approx(-c5, rel=1e-5)
+    assert out["weight"][24, 32] == pytest.approx(1.0, rel=1e-6)
+    assert out["depth"][24, 32] == pytest.approx(2.5, rel=1e-6)
+    assert tsb.quad_to_depth(*q.astype(float)) == pytest.approx(0.0, abs=1e-4) or \
+        tsb.quad_to_depth(*q.astype(float)) == pytest.approx(tsb.unambiguous_range(), abs=1e-4)
+
+
+def test_culling(tsb, ctx):
+    """test_splat.cpp:219-233."""
+    from paper_2505_05356_b200 import synthetic
+    from paper_2505_05356_b200.render import SH_C0
+    cam = tsb.CameraModel(fx=40.0, fy=40.0, cx=32.5, cy=24.5, width=64, height=48)
+    g = synthetic.GaussianSet(np.array([[0, 0, 0.05], [0, 0, -2.0], [100.0, 0, 2.0]], np.float32),
+                              np.log(np.array([[0.01] * 3, [0.1] * 3, [0.1] * 3], np.float32)),
+                              np.array([[1, 0, 0, 0]] * 3, np.float32), np.full(3, 2.0, np.float32),
+                              np.full(3, 0.5 / SH_C0, np.float32))
+    scene = gpu_scene(tsb, ctx, g, tsb.ToFConfig())
+    rp = tsb.RenderPass(ctx).prepare(scene, cam, tsb.RenderOptions()).forward()
+    assert rp.visible_count() == 0
+    assert rp.outputs()["weight"][24, 32] == 0.0
+
+
+def test_invalid_camera_raises(tsb, ctx):
+    from paper_2505_05356_b200 import synthetic
+    g = synthetic.gaussians(10, 0)
+    scene = gpu_scene(tsb, ctx, g, tsb.ToFConfig())
+    with pytest.raises(tsb.TsbError, match="render: invalid camera"):
+        tsb.RenderPass(ctx).prepare(scene, tsb.CameraModel(fx=0.0, width=10, height=10), tsb.RenderOptions())
+
+
+def _train_step_compare(tsb, ctx, cfg, cam=None, n_freq_check=True):
+    cam = cam or cfg.camera
+    g, tgt, frame, tof = cfg.scene, cfg.target, cfg.frames[0], cfg.tof
+    opts = tsb.RenderOptions(counts=True)
+    # target: render of the seed-1 set (+ seeded noise) -- input data for both sides
+    tscene = gpu_scene(tsb, ctx, tgt, tof)
+    rp = tsb.RenderPass(ctx).prepare(tscene, cam, opts, frame).forward()
+    target = rp.outputs()["quad"].astype(np.float32)
+    rng = np.random.default_rng(123)
+    target = (target + rng.normal(0.0, cfg.noise_std, target.shape)).astype(np.float32)
+
+    scene = gpu_scene(tsb, ctx, g, tof)
+    rp.prepare(scene, cam, opts, frame)
+    nf = len(tof.frequencies)
+    loss = rp.forward_loss(target, [0.25] * (4 * nf))
+    out = rp.outputs()
+    rp.backward()
+    gr = scene.grads()
+
+    HW = cam.width * cam.height
+    oloss = 0.0
+    og = None
+    for f in range(nf):
+        op = orc.OraclePass(oracle_scene(g, frame, tof, f), cam, opts)
+        ref = op.forward()
+        assert np.array_equal(out["n_contrib"], ref["n_contrib"])
+        assert rel_err(out["quad"][4 * f:4 * f + 4], ref["quad"]) < QUAD_TOL
+        d_quad = np.zeros((4, cam.height, cam.width))
+        for m in range(4):
+            v, d = orc.mse(ref["quad"][m], target[4 * f + m].astype(np.float64))
+            oloss += 0.25 * v
+            d_quad[m] = 0.25 * d
+        gg = op.backward(d_quad=d_quad)
+        og = gg if og is None else {k: og[k] + gg[k] for k in og}
+    assert loss == pytest.approx(oloss, rel=1e-5)
+    k, w = frame
+    checks = {"d_position": (gr["d_position"], og["d_position"]),
+              "d_log_scale": (gr["d_log_scale"], og["d_log_scale"]),
+              "d_rotation": (gr["d_rotation"], og["d_rotation"]),
+              "d_opacity_logit": (gr["d_opacity_logit"], og["d_opacity_logit"]),
+              "d_reflectivity_dc": (gr["d_reflectivity_dc"], og["d_refl_sh"][:, 0]),
+              "d_motion_k": (gr["d_motion"][k], (1 - w) * og["d_position"]),
+              "d_motion_k1": (gr["d_motion"][k + 1], w * og["d_position"])}
+    errs = {name: rel_err(a, b, 1e-4) for name, (a, b) in checks.items()}
+    assert all(e < GRAD_TOL for e in errs.values()), errs
+    return scene, og, errs
+
+
+def test_c1_training_step_grads_and_adam(tsb, ctx):
+    from paper_2505_05356_b200 import synthetic
+    cfg = synthetic.config("c1")
+    scene, og, errs = _train_step_compare(tsb, ctx, cfg)
+    before = scene.get_params()
+    scene.adam_step(tsb.LrTable.uniform(cfg.lr))
+    after = scene.get_params()
+    # oracle Adam on the oracle gradients (trainer.cpp:18-31), first step
+    p = before["position"].astype(np.float64).ravel().copy()
+    g = og["d_position"].ravel().copy()
+    m, v = np.zeros_like(p), np.zeros_like(p)
+    orc.adam_step(p, g, m, v, 1, cfg.lr)
+    dp_gpu = after["position"].astype(np.float64).ravel() - before["position"].astype(np.float64).ravel()
+    dp_ref = p - before["position"].astype(np.float64).ravel()
+    big = np.abs(g) > 1e-3 * np.abs(g).max()
+    assert rel_err(dp_gpu[big], dp_ref[big], 1e-3) < 1e-3
+    s, cnt = scene.densify_stat()
+    assert cnt == 1
+    assert rel_err(s, np.linalg.norm(og["d_position"], axis=1), 1e-4) < GRAD_TOL
+
+
+def test_two_frequency_step(tsb, ctx):
+    """c2 semantics: two quads sharing geometry == two reference renders, grads summed."""
+    from paper_2505_05356_b200 import synthetic
+    cfg = synthetic.config("c2", n=20_000)
+    cam = synthetic.camera(320, 288, 262.5, 160, 144)
+    _train_step_compare(tsb, ctx, cfg, cam)
