@@ -1,0 +1,459 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 C-ToF splat path (contract in the task statement).
+
+Headline (`value`): ToF raw frames/s of the BASELINE c3 sweep -- 1,000,000
+dynamic Gaussians at 640x480, 30 MHz, 300 frames at t = i/299, forward
+(quad + depth + weight) -- the north_star's >=100 frames/s target.  Frames are
+split across ranks (strong scaling; no data-path collective).  The `train`
+object reports the c4 data-parallel training step (2M Gaussians, 1024^2,
+64 frames/iter split over ranks, NCCL allreduce of the 20-float/Gaussian
+gradient buffer, fused Adam) in train iters/s.
+
+`--impl reference` times the CPU oracle restatement of the reference hot path
+(oracle/, "port": the reference needs Eigen, absent on this image) on the same
+workload with all host threads, one frame per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+METRIC = "ToF raw frames/s (fwd)"
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return PEAKS_FALLBACK
+
+
+# ---------------------------------------------------------------------------
+# clocks (pynvml sampling during the timed region)
+class ClockSampler:
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                 "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+class Dist:
+    def __init__(self, n_gpus: int):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t)
+        return float(t.item())
+
+    def bcast_bytes(self, b: bytes) -> bytes:
+        if not self.pg:
+            return b
+        obj = [b]
+        self.pg.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+class StreamTimer:
+    """CUDA events recorded on the library's own stream (torch ExternalStream)."""
+
+    def __init__(self, ctx):
+        import torch
+        self.torch = torch
+        self.stream = torch.cuda.ExternalStream(ctx.stream)
+        self.a = torch.cuda.Event(enable_timing=True)
+        self.b = torch.cuda.Event(enable_timing=True)
+
+    def start(self):
+        self.a.record(self.stream)
+
+    def stop_ms(self) -> float:
+        self.b.record(self.stream)
+        self.b.synchronize()
+        return self.a.elapsed_time(self.b)
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes per launch
+def stage_bytes(stage, n, k, v, ntiles, n_keyframes, npx, nf=1):
+    params = 16 * (3 + min(n_keyframes, 2))  # float4 arrays read by preprocess (pos_op, scale_amp, quat, 2 keys)
+    if stage == "preprocess":
+        return n * (params + 8 + 4 + 4 + 8) + v * (16 * (3 + (nf > 1)))
+    if stage == "depth_sort":  # CUB onesweep over 64-bit keys + 32-bit values: 8 passes r+w of 12 B + upsweep
+        return n * (8 + 8 * 24)
+    if stage == "scan":
+        return n * (4 + 4 + 4 + 4)
+    if stage == "duplicate":
+        return n * (4 + 4 + 4) + v * 8 + k * 6
+    if stage == "tile_sort":  # 16-bit keys + 32-bit values, ceil(bits/8) passes of r+w 6 B, + upsweep 2 B
+        bits = max(1, math.ceil(math.log2(max(ntiles, 2))))
+        return k * (2 + 12 * math.ceil(bits / 8))
+    if stage == "ranges":
+        return k * 2 + ntiles * 8
+    return None
+
+
+def pick_roofline(st, shapes, peaks):
+    # dominant stage by measured time among the HBM-bound stages with byte accounting
+    total = sum(ms for ms, _ in st.values())
+    best = None
+    for name, (ms, calls) in st.items():
+        if calls == 0 or ms <= 0:
+            continue
+        if best is None or ms > st[best][0]:
+            best = name
+    out = {"dominant_stage": best, "stage_ms_per_step": {k: round(v[0], 4) for k, v in st.items() if v[1]}}
+    hbm_best = None
+    for name, (ms, calls) in st.items():
+        if calls and stage_bytes(name, **shapes) is not None and (hbm_best is None or ms > st[hbm_best][0]):
+            hbm_best = name
+    if hbm_best is None:
+        return out
+    ms, calls = st[hbm_best]
+    per_launch_ms = ms / calls
+    bytes_ = stage_bytes(hbm_best, **shapes)
+    achieved = bytes_ / (per_launch_ms * 1e-3) / 1e9
+    out.update({"bound": "hbm", "kernel": hbm_best, "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
+                "algorithmic_bytes_per_launch": int(bytes_), "avg_launch_ms": round(per_launch_ms, 5),
+                "share_of_step": round(ms / total, 4) if total else None, "peak_source": peaks["source"]})
+    return out
+
+
+# ---------------------------------------------------------------------------
+def bench_c3(args, dist, tsb, synthetic):
+    cfg = synthetic.config("c3")
+    g = cfg.scene
+    ctx = tsb.Context(dist.local)
+    scene = tsb.GaussianScene(ctx, g.n, g.n_keyframes, cfg.tof)
+    scene.set_params(g.position, g.log_scale, g.rotation, g.opacity_logit, g.reflectivity_dc, g.motion)
+    rp = tsb.RenderPass(ctx)
+    opts = tsb.RenderOptions()
+    my_frames = cfg.frames[dist.rank::dist.world]
+
+    def step():
+        for fr in my_frames:
+            rp.prepare(scene, cfg.camera, opts, fr)
+            rp.forward()
+
+    for _ in range(args.warmup):
+        step()
+    ctx.synchronize()
+    timer = StreamTimer(ctx)
+    ctx.stage_times()
+    ctx.set_profiling(True)
+    l0 = ctx.launch_count()
+    dist.barrier()
+    ctx.synchronize()
+    with ClockSampler(dist.local) as clk:
+        timer.start()
+        for _ in range(args.steps):
+            step()
+        ms = timer.stop_ms()
+    ctx.synchronize()
+    launches = ctx.launch_count() - l0
+    ctx.set_profiling(False)
+    st = ctx.stage_times()
+    v, k = rp.visible_count(), rp.num_keys()
+    fixups = rp.debug_fixups()
+    ms_max = dist.max(ms)
+    frames_total = len(cfg.frames) * args.steps
+    value = frames_total / (ms_max / 1e3)
+
+    # e2e through the public API with host buffers: H2D of the scene from pinned host memory
+    # every step, D2H of every rendered frame's quad/depth/weight into pinned host memory.
+    import torch
+    H, W = cfg.camera.height, cfg.camera.width
+    pin = {k_: torch.empty(sz, dtype=torch.float32, pin_memory=True).numpy() for k_, sz in
+           [("quad", 4 * H * W), ("depth", H * W), ("weight", H * W)]}
+    host = {k_: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy() for k_, a in
+            [("position", g.position), ("log_scale", g.log_scale), ("rotation", g.rotation),
+             ("opacity_logit", g.opacity_logit), ("reflectivity_dc", g.reflectivity_dc), ("motion", g.motion)]}
+    h2d = sum(a.nbytes for a in host.values())
+    d2h = len(my_frames) * sum(a.nbytes for a in pin.values())
+
+    def e2e_step():
+        scene.set_params(host["position"], host["log_scale"], host["rotation"], host["opacity_logit"],
+                         host["reflectivity_dc"], host["motion"])
+        for fr in my_frames:
+            rp.prepare(scene, cfg.camera, opts, fr)
+            rp.forward()
+            tsb._abi.check(tsb._abi.lib().tsb_pass_download(rp.handle, tsb._abi.OUT_QUAD, pin["quad"].ctypes.data,
+                                                            pin["quad"].nbytes))
+            tsb._abi.check(tsb._abi.lib().tsb_pass_download(rp.handle, tsb._abi.OUT_DEPTH,
+                                                            pin["depth"].ctypes.data, pin["depth"].nbytes))
+            tsb._abi.check(tsb._abi.lib().tsb_pass_download(rp.handle, tsb._abi.OUT_WEIGHT,
+                                                            pin["weight"].ctypes.data, pin["weight"].nbytes))
+
+    e2e_step()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    ctx.synchronize()
+    e2e_s = dist.max(time.perf_counter() - t0)
+    e2e = {"value": round(frames_total / e2e_s, 3), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(d2h), "timer": "host wall clock around synchronous API calls"}
+
+    shapes = dict(n=g.n, k=k, v=v, ntiles=((W + 15) // 16) * ((H + 15) // 16), n_keyframes=g.n_keyframes,
+                  npx=H * W)
+    stage_ms = {name: (t / args.steps, c // args.steps) for name, (t, c) in st.items()}
+    roof = pick_roofline(stage_ms, shapes, load_peaks())
+    info = {"visible": v, "keys_per_frame": k, "fixup_pixels_last_frame": fixups, "clock": clk.summary(),
+            "launches": launches}
+    return value, ms_max / args.steps, e2e, roof, info, ctx
+
+
+def bench_train_c4(args, dist, tsb, synthetic, ctx):
+    """c4: 64 frames/iter split over ranks, loss vs seeded target renders, allreduce, fused Adam."""
+    import torch
+    cfg = synthetic.config("c4", args.train_n)
+    g, tg = cfg.scene, cfg.target
+    cam, opts = cfg.camera, tsb.RenderOptions()
+    scene = tsb.GaussianScene(ctx, g.n, g.n_keyframes, cfg.tof)
+    scene.set_params(g.position, g.log_scale, g.rotation, g.opacity_logit, g.reflectivity_dc, g.motion)
+    tscene = tsb.GaussianScene(ctx, tg.n, tg.n_keyframes, cfg.tof)
+    tscene.set_params(tg.position, tg.log_scale, tg.rotation, tg.opacity_logit, tg.reflectivity_dc, tg.motion)
+    rp = tsb.RenderPass(ctx)
+    my_frames = cfg.frames[dist.rank::dist.world]
+    H, W = cam.height, cam.width
+    targets = torch.empty((len(my_frames), 4, H, W), dtype=torch.float32, device=f"cuda:{dist.local}")
+    for i, fr in enumerate(my_frames):
+        rp.prepare(tscene, cam, opts, fr).forward()
+        targets[i].copy_(torch.from_numpy(rp.download(tsb._abi.OUT_QUAD, shape=(4, H, W))))
+    tscene.close()
+    torch.cuda.synchronize()
+    comm = None
+    if dist.world > 1:
+        uid = dist.bcast_bytes(tsb.Comm.unique_id() if dist.rank == 0 else b"")
+        comm = tsb.Comm(ctx, uid, dist.world, dist.rank)
+    lr = tsb.LrTable.uniform(cfg.lr)
+    w = [0.25] * 4
+
+    def it():
+        for i, fr in enumerate(my_frames):
+            rp.prepare(scene, cam, opts, fr)
+            rp.forward_loss(None, w, sync=False, device_ptr=targets[i].data_ptr())
+            rp.backward()
+        if comm:
+            scene.allreduce_grads(comm)
+        scene.adam_step(lr)
+
+    for _ in range(max(1, args.warmup)):
+        it()
+    ctx.synchronize()
+    timer = StreamTimer(ctx)
+    ctx.stage_times()
+    ctx.set_profiling(True)
+    dist.barrier()
+    ctx.synchronize()
+    timer.start()
+    for _ in range(args.train_steps):
+        it()
+    ms = timer.stop_ms()
+    ctx.set_profiling(False)
+    st = ctx.stage_times()
+    ms_max = dist.max(ms)
+    res = {"config": "c4", "n_gaussians": g.n, "image": f"{W}x{H}", "frames_per_iter": len(cfg.frames),
+           "iters_per_s": round(args.train_steps / (ms_max / 1e3), 4),
+           "ms_per_iter": round(ms_max / args.train_steps, 3),
+           "stage_ms_per_iter": {k: round(v[0] / args.train_steps, 3) for k, v in st.items() if v[1]},
+           "keys_per_frame_last": rp.num_keys()}
+    if comm:
+        comm.close()
+    return res
+
+
+def cpu_baseline_c3(frames=1):
+    """Oracle (reference restatement) on the host cores: RenderPass ctor + forward per frame."""
+    from oracle import oracle as orc
+    from paper_2505_05356_b200 import synthetic
+    sys.path.insert(0, str(ROOT / "tests"))
+    cfg = synthetic.config("c3")
+    opts = type("O", (), {})()
+    g = cfg.scene
+    t_total = 0.0
+    for i in range(frames):
+        fr = cfg.frames[(i * 97) % len(cfg.frames)]
+        sc = orc.scene_from_dc(g.rendered_means(fr), g.log_scale, g.rotation, g.opacity_logit, g.reflectivity_dc,
+                               frequency=cfg.tof.modulation_frequency)
+        t0 = time.perf_counter()
+        op = orc.OraclePass(sc, cfg.camera, opts)
+        op.forward()
+        t_total += time.perf_counter() - t0
+        del op
+    return frames / t_total, orc.num_threads()
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, dist):
+    if dist.rank != 0:
+        return 0
+    from oracle import oracle as orc
+    from paper_2505_05356_b200 import synthetic
+    cfg = synthetic.config("c3")
+    g = cfg.scene
+    opts = type("O", (), {})()
+    times = []
+    for s in range(args.warmup + args.steps):
+        fr = cfg.frames[(s * 37) % len(cfg.frames)]
+        sc = orc.scene_from_dc(g.rendered_means(fr), g.log_scale, g.rotation, g.opacity_logit, g.reflectivity_dc,
+                               frequency=cfg.tof.modulation_frequency)
+        t0 = time.perf_counter()
+        op = orc.OraclePass(sc, cfg.camera, opts)
+        op.forward()
+        dt = time.perf_counter() - t0
+        del op
+        if s >= args.warmup:
+            times.append(dt)
+    total = sum(times)
+    value = len(times) / total
+    cores = orc.num_threads()
+    line = {"metric": METRIC, "value": round(value, 5), "unit": "frames/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * total / len(times), 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE c3 distributions)", "impl": "reference",
+            "config": {"workload": "c3_forward_1M_640x480", "gaussians": g.n, "image": "640x480",
+                       "frames_per_step": 1, "frequency_hz": 30e6},
+            "cpu_baseline": {"value": round(value, 5), "unit": "frames/s", "cores": cores, "kind": "port",
+                             "sample": f"{len(times)} of the 300 c3 frames (RenderPass ctor + forward each), "
+                                       "oracle/ restatement of splat.cpp in fp64 with OpenMP over tiles"},
+            "e2e": {"value": round(value, 5), "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--train-steps", type=int, default=3)
+    ap.add_argument("--train-n", type=int, default=None)
+    ap.add_argument("--cpu-frames", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else max(args.warmup, 1)
+    dist = Dist(args.gpus)
+    if args.impl == "reference":
+        rc = run_reference(args, dist)
+        dist.close()
+        return rc
+
+    import torch  # noqa: F401  (timing events / pinned host buffers; load before libtsb)
+    import paper_2505_05356_b200 as tsb
+    from paper_2505_05356_b200 import synthetic
+
+    value, ms_step, e2e, roof, info, ctx = bench_c3(args, dist, tsb, synthetic)
+    train = None
+    if not args.no_train:
+        train = bench_train_c4(args, dist, tsb, synthetic, ctx)
+    cpu = None
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
+        v_cpu, cores = cpu_baseline_c3(args.cpu_frames)
+        cpu = {"value": round(v_cpu, 5), "unit": "frames/s", "cores": cores, "kind": "port",
+               "sample": f"{args.cpu_frames} of the 300 c3 frames (ctor + forward), oracle/ fp64 OpenMP"}
+    if dist.rank == 0:
+        clk = info.pop("clock")
+        line = {"metric": METRIC, "value": round(value, 3), "unit": "frames/s", "n_gpus": dist.world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (seeded BASELINE c3 distributions; no dataset named)",
+                "config": {"workload": "c3_forward_1M_640x480", "gaussians": 1_000_000, "image": "640x480",
+                           "frames_per_step": 300, "frequency_hz": 30e6, "keyframes": 2,
+                           "parallelism": f"frames split over {dist.world} rank(s)",
+                           "l2": "inputs larger than L2 (~0.4 GB touched per frame)",
+                           "precision": "fp64 preprocess, fp32 raster, fp64 fix-up of ambiguous pixels"},
+                "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+                "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"]},
+                "gpu_launches": info["launches"], "train": train, "detail": info}
+        print(json.dumps(line), flush=True)
+    dist.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -116,6 +116,18 @@ void* tsb_ctx_stream(tsb_ctx* ctx);
 /* Number of kernels this context has launched (bench.py gpu_launches). */
 int64_t tsb_ctx_launch_count(tsb_ctx* ctx);
 
+/* Per-stage device timing (CUDA events recorded on the context stream around each
+ * stage's kernels).  Stages: see TSB_STAGE_*.  tsb_ctx_stage_times synchronises,
+ * returns summed milliseconds and launch counts per stage, and resets. */
+enum {
+    TSB_STAGE_PREPROCESS = 0, TSB_STAGE_DEPTH_SORT = 1, TSB_STAGE_SCAN = 2, TSB_STAGE_DUPLICATE = 3,
+    TSB_STAGE_TILE_SORT = 4, TSB_STAGE_RANGES = 5, TSB_STAGE_RASTER_FWD = 6, TSB_STAGE_FIXUP = 7,
+    TSB_STAGE_LOSS = 8, TSB_STAGE_RASTER_BWD = 9, TSB_STAGE_CHAIN = 10, TSB_STAGE_ADAM = 11,
+    TSB_STAGE_ALLREDUCE = 12, TSB_NUM_STAGES = 13
+};
+int tsb_ctx_set_profiling(tsb_ctx* ctx, int enabled);
+int tsb_ctx_stage_times(tsb_ctx* ctx, double* ms /* TSB_NUM_STAGES */, int64_t* calls /* TSB_NUM_STAGES */);
+
 /* ---- scene: parameters, gradients, Adam state (trainer.cpp:63-132) ------- */
 int tsb_scene_create(tsb_ctx* ctx, const tsb_scene_desc* desc, tsb_scene** out);
 void tsb_scene_destroy(tsb_scene* s);

@@ -21,6 +21,10 @@ CH_QUAD, CH_DEPTH, CH_WEIGHT, CH_TRANSM, CH_COUNTS = 1, 2, 4, 8, 16
  OUT_D_QUAD) = range(8)
 
 
+STAGES = ["preprocess", "depth_sort", "scan", "duplicate", "tile_sort", "ranges", "raster_fwd", "fixup", "loss",
+          "raster_bwd", "chain", "adam", "allreduce"]
+
+
 class TsbError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(msg)
@@ -71,6 +75,8 @@ SIGNATURES = {
     "tsb_ctx_synchronize": (C.c_int, [_vp]),
     "tsb_ctx_stream": (_vp, [_vp]),
     "tsb_ctx_launch_count": (C.c_int64, [_vp]),
+    "tsb_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
+    "tsb_ctx_stage_times": (C.c_int, [_vp, _dp, _lp]),
     "tsb_scene_create": (C.c_int, [_vp, C.POINTER(SceneDesc), C.POINTER(_vp)]),
     "tsb_scene_destroy": (None, [_vp]),
     "tsb_scene_set_params": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -5,6 +5,7 @@
 // stream.  tsb_pass_prepare synchronises once per frame to learn the number of
 // tile keys (the CUB radix sort needs it on the host).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -64,7 +65,41 @@ struct tsb_ctx {
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
     void* pinned = nullptr;  // small pinned staging (K, V readback)
+    // stage profiling: event pairs recorded on `stream`
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<std::pair<int, size_t>> ev_marks;  // (stage, index of start event)
 };
+
+namespace {
+// RAII stage marker: records a start event on construction and a stop event on
+// destruction, both on the context stream (only when profiling is enabled).
+struct Stage {
+    tsb_ctx* c;
+    int stage;
+    size_t idx = 0;
+    bool on;
+    Stage(tsb_ctx* ctx, int s) : c(ctx), stage(s), on(ctx->profiling) {
+        if (!on) return;
+        if (c->ev_used + 2 > c->ev_pool.size()) {
+            for (int i = 0; i < 64; ++i) {
+                cudaEvent_t e;
+                cudaEventCreate(&e);
+                c->ev_pool.push_back(e);
+            }
+        }
+        idx = c->ev_used;
+        c->ev_used += 2;
+        cudaEventRecord(c->ev_pool[idx], c->stream);
+    }
+    ~Stage() {
+        if (!on) return;
+        cudaEventRecord(c->ev_pool[idx + 1], c->stream);
+        c->ev_marks.emplace_back(stage, idx);
+    }
+};
+}  // namespace
 
 struct tsb_scene {
     tsb_ctx* ctx = nullptr;
@@ -158,10 +193,35 @@ int tsb_ctx_create(int device, tsb_ctx** out) {
     return TSB_OK;
 }
 
+int tsb_ctx_set_profiling(tsb_ctx* c, int enabled) {
+    if (!c) return fail(TSB_ERR_INVALID, "null context");
+    c->profiling = enabled != 0;
+    return TSB_OK;
+}
+
+int tsb_ctx_stage_times(tsb_ctx* c, double* ms, int64_t* calls) {
+    if (!c) return fail(TSB_ERR_INVALID, "null context");
+    TSB_CUDA(cudaStreamSynchronize(c->stream));
+    for (int i = 0; i < TSB_NUM_STAGES; ++i) {
+        if (ms) ms[i] = 0.0;
+        if (calls) calls[i] = 0;
+    }
+    for (const auto& m : c->ev_marks) {
+        float t = 0.f;
+        TSB_CUDA(cudaEventElapsedTime(&t, c->ev_pool[m.second], c->ev_pool[m.second + 1]));
+        if (ms) ms[m.first] += t;
+        if (calls) calls[m.first] += 1;
+    }
+    c->ev_marks.clear();
+    c->ev_used = 0;
+    return TSB_OK;
+}
+
 void tsb_ctx_destroy(tsb_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     cudaFreeHost(c->pinned);
     cudaStreamDestroy(c->stream);
     delete c;
@@ -370,8 +430,11 @@ int tsb_scene_adam_step(tsb_scene* s, const tsb_adam_config* cfg) {
     for (int c = 0; c < 4; ++c) lr[8 + c] = cfg->rotation;
     for (int k = 0; k < s->d.n_keyframes; ++k)
         for (int c = 0; c < 3; ++c) lr[(size_t)(3 + k) * 4 + c] = cfg->motion;
-    launch_adam(s->params, s->grads, s->m, s->v, s->d.n, s->narrays, lr.data(), cfg->beta1, cfg->beta2, cfg->eps,
-                bc1, bc2, s->densify, s->ctx->stream);
+    {
+        Stage sg(s->ctx, TSB_STAGE_ADAM);
+        launch_adam(s->params, s->grads, s->m, s->v, s->d.n, s->narrays, lr.data(), cfg->beta1, cfg->beta2,
+                    cfg->eps, bc1, bc2, s->densify, s->ctx->stream);
+    }
     s->ctx->launches++;
     TSB_CHECK_LAUNCH();
     s->densify_count++;
@@ -606,10 +669,19 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
 
     const SceneK S = scenek(s);
     TSB_CUDA(cudaMemsetAsync(p->counters, 0, sizeof(int32_t) * 4, st));
-    launch_preprocess(S, C, O, p->frame, p->key_a, p->gidx_a, p->touched, p->rect, p->rec, p->counters, st);
-    launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, n, p->temp, p->temp_bytes, st);
-    launch_gather_counts(p->gidx_b, p->touched, p->cnt_sorted, n, st);
-    launch_scan(p->cnt_sorted, p->offsets, n, p->temp, p->temp_bytes, st);
+    {
+        Stage sg(p->ctx, TSB_STAGE_PREPROCESS);
+        launch_preprocess(S, C, O, p->frame, p->key_a, p->gidx_a, p->touched, p->rect, p->rec, p->counters, st);
+    }
+    {
+        Stage sg(p->ctx, TSB_STAGE_DEPTH_SORT);
+        launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, n, p->temp, p->temp_bytes, st);
+    }
+    {
+        Stage sg(p->ctx, TSB_STAGE_SCAN);
+        launch_gather_counts(p->gidx_b, p->touched, p->cnt_sorted, n, st);
+        launch_scan(p->cnt_sorted, p->offsets, n, p->temp, p->temp_bytes, st);
+    }
     p->ctx->launches += 2;
     TSB_CHECK_LAUNCH();
     // K = offsets[n-1] + cnt[n-1]; V = counters[0]
@@ -625,10 +697,20 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     p->V = (int32_t)hp[2];
     if ((rc = ensure_keys(p, p->K))) return rc;
     if ((rc = ensure_temp(p))) return rc;
-    launch_duplicate(p->gidx_b, p->offsets, p->cnt_sorted, p->rect, p->tkey_a, p->tval_a, n, O.ts, O.tiles_x, st);
-    launch_sort_tiles(p->tkey_a, p->tkey_b, p->tval_a, p->tval_b, p->K, bits_for(p->ntiles), p->temp, p->temp_bytes,
-                      st);
-    launch_ranges(p->tkey_b, p->K, p->ranges, p->ntiles, st);
+    {
+        Stage sg(p->ctx, TSB_STAGE_DUPLICATE);
+        launch_duplicate(p->gidx_b, p->offsets, p->cnt_sorted, p->rect, p->tkey_a, p->tval_a, n, O.ts, O.tiles_x,
+                         st);
+    }
+    {
+        Stage sg(p->ctx, TSB_STAGE_TILE_SORT);
+        launch_sort_tiles(p->tkey_a, p->tkey_b, p->tval_a, p->tval_b, p->K, bits_for(p->ntiles), p->temp,
+                          p->temp_bytes, st);
+    }
+    {
+        Stage sg(p->ctx, TSB_STAGE_RANGES);
+        launch_ranges(p->tkey_b, p->K, p->ranges, p->ntiles, st);
+    }
     p->ctx->launches += 2;
     TSB_CHECK_LAUNCH();
     p->prepared = true;
@@ -657,11 +739,18 @@ int run_forward(tsb_pass* p, const float* target, bool loss) {
     cudaStream_t st = p->ctx->stream;
     PixK px = pixk(p);
     TSB_CUDA(cudaMemsetAsync(p->counters + 1, 0, sizeof(int32_t), st));
-    launch_raster_fwd(p->rec, p->ranges, p->tval_b, p->opt, p->W, p->H, p->nf, px, loss ? target : nullptr,
-                      p->chw, p->loss_part, st);
-    launch_fixup(scenek(p->scene), p->cam, p->opt, p->frame, p->ranges, p->tval_b, px, p->nf, st);
+    {
+        Stage sg(p->ctx, TSB_STAGE_RASTER_FWD);
+        launch_raster_fwd(p->rec, p->ranges, p->tval_b, p->opt, p->W, p->H, p->nf, px, loss ? target : nullptr,
+                          p->chw, p->loss_part, st);
+    }
+    {
+        Stage sg(p->ctx, TSB_STAGE_FIXUP);
+        launch_fixup(scenek(p->scene), p->cam, p->opt, p->frame, p->ranges, p->tval_b, px, p->nf, st);
+    }
     p->ctx->launches += 2;
     if (loss) {
+        Stage sg(p->ctx, TSB_STAGE_LOSS);
         TSB_CUDA(cudaMemsetAsync(p->loss_dev, 0, sizeof(double), st));
         launch_fixup_loss(px, p->W, p->H, p->nf, target, p->chw, p->loss_dev, p->W * p->H, st);
         launch_reduce_partials(p->loss_part, p->nblocks, 1, p->loss_dev, 1.0 / ((double)p->W * p->H), st);
@@ -771,10 +860,16 @@ int tsb_pass_backward(tsb_pass* p, int where, const float* d_quad) {
     tsb_scene* s = p->scene;
     float dpsi[2];
     for (int f = 0; f < p->nf; ++f) dpsi[f] = (float)(4.0 * M_PI * s->d.frequency[f] / s->d.speed_of_light);
-    launch_raster_bwd(p->rec, p->ranges, p->tval_b, p->opt, p->W, p->H, p->nf, dpsi, pixk(p), up, p->screen,
-                      s->d.n, p->bg_part, st);
-    launch_reduce_partials(p->bg_part, p->nblocks, 4 * p->nf, s->stats, 1.0, st);
-    launch_chain(scenek(s), p->cam, p->opt, p->frame, p->touched, p->screen, s->grads, st);
+    {
+        Stage sg(p->ctx, TSB_STAGE_RASTER_BWD);
+        launch_raster_bwd(p->rec, p->ranges, p->tval_b, p->opt, p->W, p->H, p->nf, dpsi, pixk(p), up, p->screen,
+                          s->d.n, p->bg_part, st);
+        launch_reduce_partials(p->bg_part, p->nblocks, 4 * p->nf, s->stats, 1.0, st);
+    }
+    {
+        Stage sg(p->ctx, TSB_STAGE_CHAIN);
+        launch_chain(scenek(s), p->cam, p->opt, p->frame, p->touched, p->screen, s->grads, st);
+    }
     p->ctx->launches += 3;
     TSB_CHECK_LAUNCH();
     return TSB_OK;
@@ -891,6 +986,48 @@ int tsb_pass_debug_fixups(tsb_pass* p, int32_t* count) {
 // ---------------------------------------------------------------------------
 // NCCL
 // ---------------------------------------------------------------------------
+// NCCL is resolved with dlopen on first use instead of being a link-time
+// dependency: a process that already loaded an NCCL (e.g. PyTorch's bundled
+// libnccl.so.2) keeps using that one, and pure render users never load it.
+namespace {
+struct NcclApi {
+    bool tried = false, ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+bool nccl_load() {
+    if (g_nccl.tried) return g_nccl.ok;
+    g_nccl.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        g_err = std::string("dlopen(libnccl.so.2) failed: ") + dlerror();
+        return false;
+    }
+#define TSB_SYM(field, name) g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name))
+    TSB_SYM(GetUniqueId, "ncclGetUniqueId");
+    TSB_SYM(CommInitRank, "ncclCommInitRank");
+    TSB_SYM(CommDestroy, "ncclCommDestroy");
+    TSB_SYM(AllReduce, "ncclAllReduce");
+    TSB_SYM(GroupStart, "ncclGroupStart");
+    TSB_SYM(GroupEnd, "ncclGroupEnd");
+    TSB_SYM(GetErrorString, "ncclGetErrorString");
+#undef TSB_SYM
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllReduce &&
+                g_nccl.GroupStart && g_nccl.GroupEnd && g_nccl.GetErrorString;
+    if (!g_nccl.ok) g_err = "libnccl.so.2 lacks required symbols";
+    return g_nccl.ok;
+}
+}  // namespace
+
 struct tsb_comm {
     ncclComm_t comm = nullptr;
     tsb_ctx* ctx = nullptr;
@@ -899,9 +1036,10 @@ struct tsb_comm {
 int tsb_comm_unique_id(void* out) {
     if (!out) return fail(TSB_ERR_INVALID, "null argument");
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    if (!nccl_load()) return TSB_ERR_NCCL;
     ncclUniqueId id;
-    ncclResult_t r = ncclGetUniqueId(&id);
-    if (r != ncclSuccess) return fail(TSB_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    ncclResult_t r = g_nccl.GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(TSB_ERR_NCCL, std::string("ncclGetUniqueId: ") + g_nccl.GetErrorString(r));
     std::memcpy(out, &id, sizeof id);
     return TSB_OK;
 }
@@ -910,14 +1048,15 @@ int tsb_comm_create(tsb_ctx* ctx, const void* unique_id, int nranks, int rank, t
     if (!ctx || !unique_id || !out) return fail(TSB_ERR_INVALID, "tsb_comm_create: null argument");
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(TSB_ERR_INVALID, "tsb_comm_create: bad rank");
     TSB_CUDA(cudaSetDevice(ctx->device));
+    if (!nccl_load()) return TSB_ERR_NCCL;
     ncclUniqueId id;
     std::memcpy(&id, unique_id, sizeof id);
     tsb_comm* c = new tsb_comm();
     c->ctx = ctx;
-    ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+    ncclResult_t r = g_nccl.CommInitRank(&c->comm, nranks, id, rank);
     if (r != ncclSuccess) {
         delete c;
-        return fail(TSB_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        return fail(TSB_ERR_NCCL, std::string("ncclCommInitRank: ") + g_nccl.GetErrorString(r));
     }
     *out = c;
     return TSB_OK;
@@ -925,7 +1064,7 @@ int tsb_comm_create(tsb_ctx* ctx, const void* unique_id, int nranks, int rank, t
 
 void tsb_comm_destroy(tsb_comm* c) {
     if (!c) return;
-    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->comm && g_nccl.ok) g_nccl.CommDestroy(c->comm);
     delete c;
 }
 
@@ -933,12 +1072,15 @@ int tsb_scene_allreduce_grads(tsb_scene* s, tsb_comm* c) {
     if (!s || !c) return fail(TSB_ERR_INVALID, "null argument");
     const size_t nel = (size_t)s->narrays * (size_t)s->d.n * 4;
     cudaStream_t st = s->ctx->stream;
-    ncclResult_t r = ncclGroupStart();
-    if (r == ncclSuccess && nel > 0) r = ncclAllReduce(s->grads, s->grads, nel, ncclFloat, ncclSum, c->comm, st);
-    if (r == ncclSuccess) r = ncclAllReduce(s->stats, s->stats, 9, ncclDouble, ncclSum, c->comm, st);
-    ncclResult_t r2 = ncclGroupEnd();
+    Stage sg(s->ctx, TSB_STAGE_ALLREDUCE);
+    ncclResult_t r = g_nccl.GroupStart();
+    if (r == ncclSuccess && nel > 0)
+        r = g_nccl.AllReduce(s->grads, s->grads, nel, ncclFloat, ncclSum, c->comm, st);
+    if (r == ncclSuccess) r = g_nccl.AllReduce(s->stats, s->stats, 9, ncclDouble, ncclSum, c->comm, st);
+    ncclResult_t r2 = g_nccl.GroupEnd();
     if (r != ncclSuccess || r2 != ncclSuccess)
-        return fail(TSB_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
+        return fail(TSB_ERR_NCCL,
+                    std::string("ncclAllReduce: ") + g_nccl.GetErrorString(r != ncclSuccess ? r : r2));
     return TSB_OK;
 }
 

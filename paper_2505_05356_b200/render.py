@@ -161,6 +161,16 @@ class Context:
     def launch_count(self) -> int:
         return int(lib().tsb_ctx_launch_count(self._h))
 
+    def set_profiling(self, on: bool):
+        check(lib().tsb_ctx_set_profiling(self._h, 1 if on else 0))
+
+    def stage_times(self):
+        """{stage: (ms_total, calls)} since the last call (synchronises)."""
+        ms = (C.c_double * len(_abi.STAGES))()
+        calls = (C.c_int64 * len(_abi.STAGES))()
+        check(lib().tsb_ctx_stage_times(self._h, ms, calls))
+        return {name: (ms[i], calls[i]) for i, name in enumerate(_abi.STAGES)}
+
     def close(self):
         if getattr(self, "_h", None):
             lib().tsb_ctx_destroy(self._h)

@@ -20,6 +20,17 @@ def rel_err(a, b, floor_frac=1e-6):
     return float((np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), floor)).max())
 
 
+def rel_err_quantile(a, b, floor_frac=1e-6, q=0.9999):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    mask = np.isfinite(b)
+    if not mask.any():
+        return 0.0
+    a, b = a[mask], b[mask]
+    floor = max(floor_frac * np.abs(b).max(), 1e-300)
+    return float(np.quantile(np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), floor), q))
+
+
 def oracle_scene(gset, frame, tof, freq_index=0):
     f = tof.frequencies[freq_index]
     return orc.scene_from_dc(gset.rendered_means(frame), gset.log_scale, gset.rotation, gset.opacity_logit,
