@@ -164,13 +164,8 @@ def stage_bytes(stage, n, k, v, ntiles, n_keyframes, npx, nf=1):
         return n * (8 + 8 * 24)
     if stage == "scan":
         return n * (4 + 4 + 4 + 4)
-    if stage == "duplicate":
-        return n * (4 + 4 + 4) + v * 8 + k * 6
-    if stage == "tile_sort":  # 16-bit keys + 32-bit values, ceil(bits/8) passes of r+w 6 B, + upsweep 2 B
-        bits = max(1, math.ceil(math.log2(max(ntiles, 2))))
-        return k * (2 + 12 * math.ceil(bits / 8))
-    if stage == "ranges":
-        return k * 2 + ntiles * 8
+    if stage == "binning":  # count + emit each read (gidx 4 B + rect 8 B) per visible rank; 4 B per list entry
+        return v * 24 + k * 4
     return None
 
 

@@ -53,7 +53,8 @@ enum {
     TSB_CH_DEPTH = 1u << 1,     /* depth_raw and depth */
     TSB_CH_WEIGHT = 1u << 2,    /* weight (= alpha, sum_k w_k); always computed */
     TSB_CH_TRANSM = 1u << 3,    /* transmittance T_N; always computed */
-    TSB_CH_COUNTS = 1u << 4     /* per-pixel n_contrib / n_processed (parity) */
+    TSB_CH_COUNTS = 1u << 4,    /* per-pixel n_contrib / n_processed (parity) */
+    TSB_CH_FULL_LISTS = 1u << 5 /* bin every tile's complete list (parity); default stops at termination */
 };
 
 /* CameraModel (camera.hpp:9-17).  R row-major; p_cam = R p_world + t. */
@@ -120,7 +121,7 @@ int64_t tsb_ctx_launch_count(tsb_ctx* ctx);
  * stage's kernels).  Stages: see TSB_STAGE_*.  tsb_ctx_stage_times synchronises,
  * returns summed milliseconds and launch counts per stage, and resets. */
 enum {
-    TSB_STAGE_PREPROCESS = 0, TSB_STAGE_DEPTH_SORT = 1, TSB_STAGE_SCAN = 2, TSB_STAGE_DUPLICATE = 3,
+    TSB_STAGE_PREPROCESS = 0, TSB_STAGE_DEPTH_SORT = 1, TSB_STAGE_SCAN = 2, TSB_STAGE_BINNING = 3,
     TSB_STAGE_TILE_SORT = 4, TSB_STAGE_RANGES = 5, TSB_STAGE_RASTER_FWD = 6, TSB_STAGE_FIXUP = 7,
     TSB_STAGE_LOSS = 8, TSB_STAGE_RASTER_BWD = 9, TSB_STAGE_CHAIN = 10, TSB_STAGE_ADAM = 11,
     TSB_STAGE_ALLREDUCE = 12, TSB_NUM_STAGES = 13

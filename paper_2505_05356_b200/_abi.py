@@ -16,12 +16,12 @@ HEADER_PATH = Path(__file__).resolve().parent.parent / "include" / "tsb.h"
 
 TSB_OK, TSB_ERR_INVALID, TSB_ERR_CUDA, TSB_ERR_NOMEM, TSB_ERR_UNSUPPORTED, TSB_ERR_NCCL = range(6)
 TSB_HOST, TSB_DEVICE = 0, 1
-CH_QUAD, CH_DEPTH, CH_WEIGHT, CH_TRANSM, CH_COUNTS = 1, 2, 4, 8, 16
+CH_QUAD, CH_DEPTH, CH_WEIGHT, CH_TRANSM, CH_COUNTS, CH_FULL_LISTS = 1, 2, 4, 8, 16, 32
 (OUT_QUAD, OUT_DEPTH_RAW, OUT_DEPTH, OUT_WEIGHT, OUT_TRANSM, OUT_N_CONTRIB, OUT_N_PROCESSED,
  OUT_D_QUAD) = range(8)
 
 
-STAGES = ["preprocess", "depth_sort", "scan", "duplicate", "tile_sort", "ranges", "raster_fwd", "fixup", "loss",
+STAGES = ["preprocess", "depth_sort", "scan", "binning", "tile_sort", "ranges", "raster_fwd", "fixup", "loss",
           "raster_bwd", "chain", "adam", "allreduce"]
 
 

@@ -125,23 +125,30 @@ struct tsb_pass {
     uint32_t channels = 0;
     int nf = 1, W = 0, H = 0, ntiles = 0, nblocks = 0;
     bool prepared = false, forwarded = false, have_loss = false;
-    int32_t V = 0;
-    int64_t K = 0;
+    int32_t V = -1;  // visible count (read back lazily)
     // capacities
     int n_cap = 0, px_cap = 0, blk_cap = 0, tiles_cap = 0;
-    int64_t k_cap = 0;
     size_t temp_bytes = 0;
+    size_t hist_cap = 0;       // uint32 entries
+    uint32_t vals_cap = 0;     // list entries
+    int chunk_cap = 0;         // chunks x tiles of ranges
     // per Gaussian
     uint64_t *key_a = nullptr, *key_b = nullptr;
     uint32_t *gidx_a = nullptr, *gidx_b = nullptr;
-    uint32_t *touched = nullptr, *cnt_sorted = nullptr, *offsets = nullptr;
+    uint32_t* touched = nullptr;
     uint2* rect = nullptr;
     RecK rec{};
     float* screen = nullptr;  // [8][n]
-    // per key
-    uint16_t *tkey_a = nullptr, *tkey_b = nullptr;
-    uint32_t *tval_a = nullptr, *tval_b = nullptr;
-    uint2* ranges = nullptr;
+    // chunked binning
+    std::vector<int> chunk_seg0, chunk_nseg;  // schedule (segments)
+    int nchunks = 0;                          // chunks binned by the last forward
+    uint32_t* hist = nullptr;
+    uint32_t* tile_len = nullptr;
+    uint4* ranges_all = nullptr;  // [chunk_cap][ntiles]
+    int* chunk_rank0 = nullptr;   // device [chunk_cap]
+    uint32_t* vals = nullptr;
+    int32_t* block_done = nullptr;
+    int32_t* tile_blocks_done = nullptr;
     // per pixel
     float* out = nullptr;
     int32_t *n_contrib = nullptr, *n_processed = nullptr, *last = nullptr;
@@ -149,8 +156,11 @@ struct tsb_pass {
     float* d_quad = nullptr;
     float* target = nullptr;
     int32_t* flagged = nullptr;
+    float* st_f = nullptr;
+    int32_t* st_i = nullptr;
     // misc
-    int32_t* counters = nullptr;  // [0] n_visible, [1] n_flagged
+    int32_t* counters = nullptr;  // [0] n_visible, [1] n_flagged, [2] overflow, [3] blocks done
+    uint32_t* list_off = nullptr;
     double* loss_part = nullptr;
     double* bg_part = nullptr;
     double* loss_dev = nullptr;
@@ -451,7 +461,8 @@ int tsb_pass_create(tsb_ctx* ctx, tsb_pass** out) {
     tsb_pass* p = new tsb_pass();
     p->ctx = ctx;
     int rc;
-    if ((rc = dev_alloc(&p->counters, 4)) || (rc = dev_alloc(&p->loss_dev, 1)) || (rc = dev_alloc(&p->chw, 8))) {
+    if ((rc = dev_alloc(&p->counters, 4)) || (rc = dev_alloc(&p->loss_dev, 1)) || (rc = dev_alloc(&p->chw, 8)) ||
+        (rc = dev_alloc(&p->list_off, 1))) {
         tsb_pass_destroy(p);
         return rc;
     }
@@ -461,17 +472,17 @@ int tsb_pass_create(tsb_ctx* ctx, tsb_pass** out) {
 
 namespace {
 
+constexpr int kChunk0Segments = 65536 / kSeg;  // first depth chunk: 64K ranks, then doubling
+
 void free_gauss(tsb_pass* p) {
     dev_free(p->key_a); dev_free(p->key_b); dev_free(p->gidx_a); dev_free(p->gidx_b);
-    dev_free(p->touched); dev_free(p->cnt_sorted); dev_free(p->offsets); dev_free(p->rect);
+    dev_free(p->touched); dev_free(p->rect);
     dev_free(p->rec.A); dev_free(p->rec.B); dev_free(p->rec.C); dev_free(p->rec.D); dev_free(p->screen);
-}
-void free_keys(tsb_pass* p) {
-    dev_free(p->tkey_a); dev_free(p->tkey_b); dev_free(p->tval_a); dev_free(p->tval_b);
 }
 void free_pixels(tsb_pass* p) {
     dev_free(p->out); dev_free(p->n_contrib); dev_free(p->n_processed); dev_free(p->last);
     dev_free(p->T_pre); dev_free(p->d_quad); dev_free(p->target); dev_free(p->flagged);
+    dev_free(p->st_f); dev_free(p->st_i);
 }
 
 int ensure_gauss(tsb_pass* p, int n) {
@@ -480,41 +491,19 @@ int ensure_gauss(tsb_pass* p, int n) {
     const int cap = std::max(n, 1);
     int rc;
     if ((rc = dev_alloc(&p->key_a, cap)) || (rc = dev_alloc(&p->key_b, cap)) || (rc = dev_alloc(&p->gidx_a, cap)) ||
-        (rc = dev_alloc(&p->gidx_b, cap)) || (rc = dev_alloc(&p->touched, cap)) ||
-        (rc = dev_alloc(&p->cnt_sorted, cap)) || (rc = dev_alloc(&p->offsets, cap)) ||
-        (rc = dev_alloc(&p->rect, cap)) || (rc = dev_alloc(&p->rec.A, cap)) || (rc = dev_alloc(&p->rec.B, cap)) ||
-        (rc = dev_alloc(&p->rec.C, cap)) || (rc = dev_alloc(&p->rec.D, cap)) ||
-        (rc = dev_alloc(&p->screen, (size_t)8 * cap)))
+        (rc = dev_alloc(&p->gidx_b, cap)) || (rc = dev_alloc(&p->touched, cap)) || (rc = dev_alloc(&p->rect, cap)) ||
+        (rc = dev_alloc(&p->rec.A, cap)) || (rc = dev_alloc(&p->rec.B, cap)) || (rc = dev_alloc(&p->rec.C, cap)) ||
+        (rc = dev_alloc(&p->rec.D, cap)) || (rc = dev_alloc(&p->screen, (size_t)8 * cap)))
         return rc;
     TSB_CUDA(cudaMemsetAsync(p->screen, 0, sizeof(float) * 8 * (size_t)cap, p->ctx->stream));
     p->n_cap = cap;
-    p->temp_bytes = 0;  // recompute temp size
-    return TSB_OK;
-}
-
-int ensure_temp(tsb_pass* p) {
-    const size_t need = binning_temp_bytes(p->n_cap, std::max<int64_t>(p->k_cap, 1));
-    if (need <= p->temp_bytes && p->temp) return TSB_OK;
     dev_free(p->temp);
-    TSB_CUDA(cudaMalloc(&p->temp, need));
-    p->temp_bytes = need;
+    p->temp_bytes = depth_sort_temp_bytes(cap);
+    TSB_CUDA(cudaMalloc(&p->temp, p->temp_bytes));
     return TSB_OK;
 }
 
-int ensure_keys(tsb_pass* p, int64_t k) {
-    if (k <= p->k_cap && p->tkey_a) return TSB_OK;
-    free_keys(p);
-    const int64_t cap = std::max<int64_t>((int64_t)(k * 1.25) + 1024, 1);
-    int rc;
-    if ((rc = dev_alloc(&p->tkey_a, cap)) || (rc = dev_alloc(&p->tkey_b, cap)) || (rc = dev_alloc(&p->tval_a, cap)) ||
-        (rc = dev_alloc(&p->tval_b, cap)))
-        return rc;
-    p->k_cap = cap;
-    p->temp_bytes = 0;
-    return TSB_OK;
-}
-
-int ensure_pixels(tsb_pass* p, int W, int H, int nf, int ntiles, int nblocks) {
+int ensure_pixels(tsb_pass* p, int W, int H, int ntiles, int nblocks) {
     const int npx = W * H;
     const int nch = out_channels(2);
     if (npx > p->px_cap) {
@@ -523,24 +512,77 @@ int ensure_pixels(tsb_pass* p, int W, int H, int nf, int ntiles, int nblocks) {
         if ((rc = dev_alloc(&p->out, (size_t)nch * npx)) || (rc = dev_alloc(&p->n_contrib, npx)) ||
             (rc = dev_alloc(&p->n_processed, npx)) || (rc = dev_alloc(&p->last, npx)) ||
             (rc = dev_alloc(&p->T_pre, npx)) || (rc = dev_alloc(&p->d_quad, (size_t)8 * npx)) ||
-            (rc = dev_alloc(&p->target, (size_t)8 * npx)) || (rc = dev_alloc(&p->flagged, npx)))
+            (rc = dev_alloc(&p->target, (size_t)8 * npx)) || (rc = dev_alloc(&p->flagged, npx)) ||
+            (rc = dev_alloc(&p->st_f, (size_t)9 * npx)) || (rc = dev_alloc(&p->st_i, (size_t)3 * npx)))
             return rc;
         p->px_cap = npx;
     }
     if (nblocks > p->blk_cap) {
         dev_free(p->loss_part);
         dev_free(p->bg_part);
+        dev_free(p->block_done);
         int rc;
-        if ((rc = dev_alloc(&p->loss_part, nblocks)) || (rc = dev_alloc(&p->bg_part, (size_t)8 * nblocks))) return rc;
+        if ((rc = dev_alloc(&p->loss_part, nblocks)) || (rc = dev_alloc(&p->bg_part, (size_t)8 * nblocks)) ||
+            (rc = dev_alloc(&p->block_done, nblocks)))
+            return rc;
         p->blk_cap = nblocks;
     }
     if (ntiles > p->tiles_cap) {
-        dev_free(p->ranges);
+        dev_free(p->tile_len);
+        dev_free(p->tile_blocks_done);
+        dev_free(p->ranges_all);
+        p->chunk_cap = 0;
         int rc;
-        if ((rc = dev_alloc(&p->ranges, ntiles))) return rc;
+        if ((rc = dev_alloc(&p->tile_len, ntiles)) || (rc = dev_alloc(&p->tile_blocks_done, ntiles))) return rc;
         p->tiles_cap = ntiles;
     }
-    (void)nf;
+    return TSB_OK;
+}
+
+// Geometric depth-chunk schedule over the n ranks (segments of kSeg ranks).
+int plan_chunks(tsb_pass* p, int n) {
+    p->chunk_seg0.clear();
+    p->chunk_nseg.clear();
+    const int nseg_total = (n + kSeg - 1) / kSeg;
+    int s0 = 0, len = kChunk0Segments;
+    while (s0 < nseg_total) {
+        const int l = std::min(len, nseg_total - s0);
+        p->chunk_seg0.push_back(s0);
+        p->chunk_nseg.push_back(l);
+        s0 += l;
+        if (p->chunk_seg0.size() >= 2) len *= 2;
+    }
+    const int nch = std::max<int>(1, (int)p->chunk_seg0.size());
+    size_t hist_need = 1;
+    for (int l : p->chunk_nseg) hist_need = std::max(hist_need, (size_t)l * p->ntiles);
+    if (hist_need > p->hist_cap) {
+        dev_free(p->hist);
+        int rc;
+        if ((rc = dev_alloc(&p->hist, hist_need))) return rc;
+        p->hist_cap = hist_need;
+    }
+    if (nch > p->chunk_cap || !p->ranges_all) {
+        dev_free(p->ranges_all);
+        dev_free(p->chunk_rank0);
+        int rc;
+        if ((rc = dev_alloc(&p->ranges_all, (size_t)nch * p->tiles_cap)) || (rc = dev_alloc(&p->chunk_rank0, nch)))
+            return rc;
+        p->chunk_cap = nch;
+    }
+    std::vector<int> r0(nch, 0);
+    for (size_t c = 0; c < p->chunk_seg0.size(); ++c) r0[c] = p->chunk_seg0[c] * kSeg;
+    TSB_CUDA(cudaMemcpy(p->chunk_rank0, r0.data(), sizeof(int) * nch, cudaMemcpyHostToDevice));
+    return TSB_OK;
+}
+
+int ensure_vals(tsb_pass* p, uint64_t need) {
+    if (need <= p->vals_cap && p->vals) return TSB_OK;
+    if (need > 0xF0000000ull) return fail(TSB_ERR_UNSUPPORTED, "render: more than 4e9 tile-list entries");
+    dev_free(p->vals);
+    const uint64_t cap = std::min<uint64_t>(std::max<uint64_t>(need, 1 << 20), 0xF0000000ull);
+    int rc;
+    if ((rc = dev_alloc(&p->vals, (size_t)cap))) return rc;
+    p->vals_cap = (uint32_t)cap;
     return TSB_OK;
 }
 
@@ -576,10 +618,13 @@ SceneK scenek(const tsb_scene* s) {
     return k;
 }
 
-int bits_for(int ntiles) {
-    int b = 1;
-    while ((1 << b) < ntiles) ++b;
-    return b;
+int read_visible(tsb_pass* p) {
+    if (p->V >= 0) return TSB_OK;
+    int32_t* h = (int32_t*)((char*)p->ctx->pinned + 1024);
+    TSB_CUDA(cudaMemcpyAsync(h, p->counters, 4, cudaMemcpyDeviceToHost, p->ctx->stream));
+    TSB_CUDA(cudaStreamSynchronize(p->ctx->stream));
+    p->V = h[0];
+    return TSB_OK;
 }
 
 }  // namespace
@@ -589,15 +634,11 @@ void tsb_pass_destroy(tsb_pass* p) {
     cudaSetDevice(p->ctx->device);
     cudaStreamSynchronize(p->ctx->stream);
     free_gauss(p);
-    free_keys(p);
     free_pixels(p);
-    dev_free(p->ranges);
-    dev_free(p->counters);
-    dev_free(p->loss_part);
-    dev_free(p->bg_part);
-    dev_free(p->loss_dev);
-    dev_free(p->chw);
-    dev_free(p->temp);
+    dev_free(p->hist); dev_free(p->tile_len); dev_free(p->ranges_all); dev_free(p->chunk_rank0);
+    dev_free(p->vals); dev_free(p->block_done); dev_free(p->tile_blocks_done);
+    dev_free(p->counters); dev_free(p->list_off);
+    dev_free(p->loss_part); dev_free(p->bg_part); dev_free(p->loss_dev); dev_free(p->chw); dev_free(p->temp);
     delete p;
 }
 
@@ -664,8 +705,10 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     const int n = s->d.n;
     int rc;
     if ((rc = ensure_gauss(p, n))) return rc;
-    if ((rc = ensure_pixels(p, p->W, p->H, p->nf, p->ntiles, p->nblocks))) return rc;
-    if ((rc = ensure_temp(p))) return rc;
+    if ((rc = ensure_pixels(p, p->W, p->H, p->ntiles, p->nblocks))) return rc;
+    if ((rc = plan_chunks(p, n))) return rc;
+    if ((rc = ensure_vals(p, std::max<uint64_t>({(uint64_t)n * 8, (uint64_t)p->ntiles * 1024, 1u << 20}))))
+        return rc;
 
     const SceneK S = scenek(s);
     TSB_CUDA(cudaMemsetAsync(p->counters, 0, sizeof(int32_t) * 4, st));
@@ -677,42 +720,10 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
         Stage sg(p->ctx, TSB_STAGE_DEPTH_SORT);
         launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, n, p->temp, p->temp_bytes, st);
     }
-    {
-        Stage sg(p->ctx, TSB_STAGE_SCAN);
-        launch_gather_counts(p->gidx_b, p->touched, p->cnt_sorted, n, st);
-        launch_scan(p->cnt_sorted, p->offsets, n, p->temp, p->temp_bytes, st);
-    }
-    p->ctx->launches += 2;
+    p->ctx->launches += 1;
     TSB_CHECK_LAUNCH();
-    // K = offsets[n-1] + cnt[n-1]; V = counters[0]
-    uint32_t* hp = (uint32_t*)p->ctx->pinned;
-    hp[0] = hp[1] = 0;
-    if (n > 0) {
-        TSB_CUDA(cudaMemcpyAsync(hp, p->offsets + (n - 1), 4, cudaMemcpyDeviceToHost, st));
-        TSB_CUDA(cudaMemcpyAsync(hp + 1, p->cnt_sorted + (n - 1), 4, cudaMemcpyDeviceToHost, st));
-    }
-    TSB_CUDA(cudaMemcpyAsync(hp + 2, p->counters, 4, cudaMemcpyDeviceToHost, st));
-    TSB_CUDA(cudaStreamSynchronize(st));
-    p->K = (int64_t)hp[0] + (int64_t)hp[1];
-    p->V = (int32_t)hp[2];
-    if ((rc = ensure_keys(p, p->K))) return rc;
-    if ((rc = ensure_temp(p))) return rc;
-    {
-        Stage sg(p->ctx, TSB_STAGE_DUPLICATE);
-        launch_duplicate(p->gidx_b, p->offsets, p->cnt_sorted, p->rect, p->tkey_a, p->tval_a, n, O.ts, O.tiles_x,
-                         st);
-    }
-    {
-        Stage sg(p->ctx, TSB_STAGE_TILE_SORT);
-        launch_sort_tiles(p->tkey_a, p->tkey_b, p->tval_a, p->tval_b, p->K, bits_for(p->ntiles), p->temp,
-                          p->temp_bytes, st);
-    }
-    {
-        Stage sg(p->ctx, TSB_STAGE_RANGES);
-        launch_ranges(p->tkey_b, p->K, p->ranges, p->ntiles, st);
-    }
-    p->ctx->launches += 2;
-    TSB_CHECK_LAUNCH();
+    p->V = -1;
+    p->nchunks = 0;
     p->prepared = true;
     return TSB_OK;
 }
@@ -720,48 +731,142 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
 int tsb_pass_visible_count(tsb_pass* p, int32_t* out) {
     if (!p || !out) return fail(TSB_ERR_INVALID, "null argument");
     if (!p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
+    int rc = read_visible(p);
+    if (rc) return rc;
     *out = p->V;
     return TSB_OK;
 }
 
 int tsb_pass_num_keys(tsb_pass* p, int64_t* out) {
     if (!p || !out) return fail(TSB_ERR_INVALID, "null argument");
-    if (!p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
-    *out = p->K;
+    if (!p->forwarded) return fail(TSB_ERR_INVALID, "tile lists are built by forward()");
+    uint32_t* h = (uint32_t*)((char*)p->ctx->pinned + 1040);
+    TSB_CUDA(cudaMemcpyAsync(h, p->list_off, 4, cudaMemcpyDeviceToHost, p->ctx->stream));
+    TSB_CUDA(cudaStreamSynchronize(p->ctx->stream));
+    *out = (int64_t)h[0];
     return TSB_OK;
 }
 
 namespace {
 
+// Chunked binning + forward composite (+ fused loss); see tsb_bin.cu.
 int run_forward(tsb_pass* p, const float* target, bool loss) {
     if (!p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
     TSB_CUDA(cudaSetDevice(p->ctx->device));
     cudaStream_t st = p->ctx->stream;
     PixK px = pixk(p);
-    TSB_CUDA(cudaMemsetAsync(p->counters + 1, 0, sizeof(int32_t), st));
-    {
-        Stage sg(p->ctx, TSB_STAGE_RASTER_FWD);
-        launch_raster_fwd(p->rec, p->ranges, p->tval_b, p->opt, p->W, p->H, p->nf, px, loss ? target : nullptr,
-                          p->chw, p->loss_part, st);
+    const bool full = (p->channels & TSB_CH_FULL_LISTS) != 0;
+    const int n = p->scene->d.n;
+    int32_t* hc = (int32_t*)((char*)p->ctx->pinned + 2048);
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        TSB_CUDA(cudaMemsetAsync(p->counters + 1, 0, sizeof(int32_t) * 3, st));
+        TSB_CUDA(cudaMemsetAsync(p->list_off, 0, sizeof(uint32_t), st));
+        TSB_CUDA(cudaMemsetAsync(p->block_done, 0, sizeof(int32_t) * p->nblocks, st));
+        TSB_CUDA(cudaMemsetAsync(p->tile_blocks_done, 0, sizeof(int32_t) * p->ntiles, st));
+        if (loss) TSB_CUDA(cudaMemsetAsync(p->loss_part, 0, sizeof(double) * p->nblocks, st));
+        FwdState fs{p->st_f, p->st_i, p->W * p->H};
+        BinK B{};
+        B.sorted_gidx = p->gidx_b;
+        B.rect = p->rect;
+        B.n_visible = p->counters;
+        B.ts = p->opt.ts;
+        B.tiles_x = p->opt.tiles_x;
+        B.tiles_y = p->opt.tiles_y;
+        B.ntiles = p->ntiles;
+        B.tile_blocks_done = p->tile_blocks_done;
+        B.blocks_per_tile = p->opt.sub * p->opt.sub;
+        B.skip_done = full ? 0 : 1;
+        B.hist = p->hist;
+        B.tile_len = p->tile_len;
+        B.vals = p->vals;
+        B.list_off = p->list_off;
+        B.capacity = p->vals_cap;
+        B.overflow = p->counters + 2;
+        int nch = 0;
+        const int total_chunks = (int)p->chunk_seg0.size();
+        for (int c = 0; c < std::max(total_chunks, 1); ++c) {
+            const int seg0 = total_chunks ? p->chunk_seg0[c] : 0;
+            const int nseg = total_chunks ? p->chunk_nseg[c] : 0;
+            B.seg0 = seg0;
+            B.nseg = nseg;
+            B.chunk = c;
+            B.ranges = p->ranges_all + (size_t)c * p->ntiles;
+            B.prev_ranges = c ? p->ranges_all + (size_t)(c - 1) * p->ntiles : nullptr;
+            if (nseg > 0) {
+                Stage sg(p->ctx, TSB_STAGE_BINNING);
+                launch_bin_chunk(B, st);
+                p->ctx->launches += 4;
+            } else {
+                TSB_CUDA(cudaMemsetAsync(B.ranges, 0, sizeof(uint4) * p->ntiles, st));
+            }
+            ChunkK ck;
+            ck.ranges = B.ranges;
+            ck.first = c == 0;
+            ck.chunk_end_rank = (seg0 + nseg) * kSeg;
+            ck.n_visible = p->counters;
+            ck.block_done = p->block_done;
+            ck.tile_blocks_done = p->tile_blocks_done;
+            ck.blocks_done_total = p->counters + 3;
+            ck.overflow = p->counters + 2;
+            {
+                Stage sg(p->ctx, TSB_STAGE_RASTER_FWD);
+                launch_raster_fwd(p->rec, ck, p->vals, p->opt, p->W, p->H, p->nf, px, fs, loss ? target : nullptr,
+                                  p->chw, p->loss_part, st);
+                p->ctx->launches += 1;
+            }
+            TSB_CHECK_LAUNCH();
+            nch = c + 1;
+            if (c + 1 >= total_chunks) break;
+            // continue only while some tile is unfinished and visible ranks remain
+            TSB_CUDA(cudaMemcpyAsync(hc, p->counters, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, st));
+            TSB_CUDA(cudaStreamSynchronize(st));
+            p->V = hc[0];
+            if (hc[2]) break;  // overflow: retry below
+            if (ck.chunk_end_rank >= hc[0]) break;
+            if (!full && hc[3] >= p->nblocks) break;
+        }
+        TSB_CUDA(cudaMemcpyAsync(hc, p->counters, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, st));
+        uint32_t* hl = (uint32_t*)(hc + 8);
+        TSB_CUDA(cudaMemcpyAsync(hl, p->list_off, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        TSB_CUDA(cudaStreamSynchronize(st));
+        p->V = hc[0];
+        if (hc[2]) {  // list storage overflow: grow and redo the frame
+            int rc = ensure_vals(p, (uint64_t)p->vals_cap * 2 + (uint64_t)hl[0]);
+            if (rc) return rc;
+            continue;
+        }
+        p->nchunks = nch;
+        FixupK fx;
+        fx.ranges_all = p->ranges_all;
+        fx.nchunks = nch;
+        fx.chunk_rank0 = p->chunk_rank0;
+        fx.binned_end_rank = total_chunks ? (p->chunk_seg0[nch - 1] + p->chunk_nseg[nch - 1]) * kSeg : 0;
+        fx.vals = p->vals;
+        fx.sorted_gidx = p->gidx_b;
+        fx.rect = p->rect;
+        fx.n_visible = p->counters;
+        fx.overflow = p->counters + 2;
+        {
+            Stage sg(p->ctx, TSB_STAGE_FIXUP);
+            launch_fixup(scenek(p->scene), p->cam, p->opt, p->frame, fx, px, p->nf, st);
+            p->ctx->launches += 1;
+        }
+        if (loss) {
+            Stage sg(p->ctx, TSB_STAGE_LOSS);
+            TSB_CUDA(cudaMemsetAsync(p->loss_dev, 0, sizeof(double), st));
+            launch_fixup_loss(px, p->W, p->H, p->nf, target, p->chw, p->loss_dev, p->W * p->H, st);
+            launch_reduce_partials(p->loss_part, p->nblocks, 1, p->loss_dev, 1.0 / ((double)p->W * p->H), st);
+            // scene loss accumulator += this pass's loss
+            launch_reduce_partials(p->loss_dev, 1, 1, p->scene->stats + 8, 1.0, st);
+            p->ctx->launches += 3;
+        }
+        TSB_CHECK_LAUNCH();
+        p->forwarded = true;
+        p->have_loss = loss;
+        (void)n;
+        return TSB_OK;
     }
-    {
-        Stage sg(p->ctx, TSB_STAGE_FIXUP);
-        launch_fixup(scenek(p->scene), p->cam, p->opt, p->frame, p->ranges, p->tval_b, px, p->nf, st);
-    }
-    p->ctx->launches += 2;
-    if (loss) {
-        Stage sg(p->ctx, TSB_STAGE_LOSS);
-        TSB_CUDA(cudaMemsetAsync(p->loss_dev, 0, sizeof(double), st));
-        launch_fixup_loss(px, p->W, p->H, p->nf, target, p->chw, p->loss_dev, p->W * p->H, st);
-        launch_reduce_partials(p->loss_part, p->nblocks, 1, p->loss_dev, 1.0 / ((double)p->W * p->H), st);
-        // scene loss accumulator += this pass's loss
-        launch_reduce_partials(p->loss_dev, 1, 1, p->scene->stats + 8, 1.0, st);
-        p->ctx->launches += 3;
-    }
-    TSB_CHECK_LAUNCH();
-    p->forwarded = true;
-    p->have_loss = loss;
-    return TSB_OK;
+    return fail(TSB_ERR_NOMEM, "render: tile-list storage kept overflowing");
 }
 
 }  // namespace
@@ -862,8 +967,8 @@ int tsb_pass_backward(tsb_pass* p, int where, const float* d_quad) {
     for (int f = 0; f < p->nf; ++f) dpsi[f] = (float)(4.0 * M_PI * s->d.frequency[f] / s->d.speed_of_light);
     {
         Stage sg(p->ctx, TSB_STAGE_RASTER_BWD);
-        launch_raster_bwd(p->rec, p->ranges, p->tval_b, p->opt, p->W, p->H, p->nf, dpsi, pixk(p), up, p->screen,
-                          s->d.n, p->bg_part, st);
+        launch_raster_bwd(p->rec, p->ranges_all, p->nchunks, p->vals, p->opt, p->W, p->H, p->nf, dpsi, pixk(p), up,
+                          p->screen, s->d.n, p->bg_part, st);
         launch_reduce_partials(p->bg_part, p->nblocks, 4 * p->nf, s->stats, 1.0, st);
     }
     {
@@ -878,6 +983,8 @@ int tsb_pass_backward(tsb_pass* p, int where, const float* d_quad) {
 // ---- debug / parity ----
 int tsb_pass_debug_prepared(tsb_pass* p, int32_t* gidx, int32_t* rect) {
     if (!p || !p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
+    int rc = read_visible(p);
+    if (rc) return rc;
     cudaStream_t st = p->ctx->stream;
     const int V = p->V;
     std::vector<uint32_t> g(V > 0 ? V : 1);
@@ -889,53 +996,62 @@ int tsb_pass_debug_prepared(tsb_pass* p, int32_t* gidx, int32_t* rect) {
     for (int i = 0; i < V; ++i) {
         if (gidx) gidx[i] = (int32_t)g[i];
         if (rect) {
-            const uint2 rc = r[g[i]];
-            rect[4 * i + 0] = rc.x & 0xffff;
-            rect[4 * i + 1] = rc.x >> 16;
-            rect[4 * i + 2] = rc.y & 0xffff;
-            rect[4 * i + 3] = rc.y >> 16;
+            const uint2 rc2 = r[g[i]];
+            rect[4 * i + 0] = rc2.x & 0xffff;
+            rect[4 * i + 1] = rc2.x >> 16;
+            rect[4 * i + 2] = rc2.y & 0xffff;
+            rect[4 * i + 3] = rc2.y >> 16;
         }
     }
     return TSB_OK;
 }
 
 int tsb_pass_debug_tiles(tsb_pass* p, int32_t* tiles_x, int32_t* tiles_y, int64_t* offsets, int32_t* ids) {
-    if (!p || !p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
+    if (!p || !p->forwarded) return fail(TSB_ERR_INVALID, "tile lists are built by forward()");
     if (tiles_x) *tiles_x = p->opt.tiles_x;
     if (tiles_y) *tiles_y = p->opt.tiles_y;
+    int rc = read_visible(p);
+    if (rc) return rc;
     cudaStream_t st = p->ctx->stream;
-    std::vector<uint2> rg(p->ntiles);
-    TSB_CUDA(cudaMemcpyAsync(rg.data(), p->ranges, sizeof(uint2) * p->ntiles, cudaMemcpyDeviceToHost, st));
-    std::vector<uint32_t> vals((size_t)std::max<int64_t>(p->K, 1));
+    const int nt = p->ntiles, nch = p->nchunks;
+    std::vector<uint4> rg((size_t)std::max(nch * nt, 1));
+    if (nch > 0)
+        TSB_CUDA(cudaMemcpyAsync(rg.data(), p->ranges_all, sizeof(uint4) * nch * nt, cudaMemcpyDeviceToHost, st));
+    int64_t k = 0;
+    uint32_t* hl = (uint32_t*)((char*)p->ctx->pinned + 1056);
+    TSB_CUDA(cudaMemcpyAsync(hl, p->list_off, 4, cudaMemcpyDeviceToHost, st));
+    TSB_CUDA(cudaStreamSynchronize(st));
+    k = hl[0];
+    std::vector<uint32_t> vals((size_t)std::max<int64_t>(k, 1));
     std::vector<uint32_t> order((size_t)std::max(p->V, 1));
-    if (ids && p->K > 0) {
-        TSB_CUDA(cudaMemcpyAsync(vals.data(), p->tval_b, sizeof(uint32_t) * p->K, cudaMemcpyDeviceToHost, st));
+    if (ids && k > 0) {
+        TSB_CUDA(cudaMemcpyAsync(vals.data(), p->vals, sizeof(uint32_t) * k, cudaMemcpyDeviceToHost, st));
         if (p->V > 0)
             TSB_CUDA(cudaMemcpyAsync(order.data(), p->gidx_b, sizeof(uint32_t) * p->V, cudaMemcpyDeviceToHost, st));
+        TSB_CUDA(cudaStreamSynchronize(st));
     }
-    TSB_CUDA(cudaStreamSynchronize(st));
-    // ranges are contiguous in tile order: offsets[t] = start of tile t
-    if (offsets) {
-        int64_t acc = 0;
-        for (int t = 0; t < p->ntiles; ++t) {
-            offsets[t] = acc;
-            acc += (int64_t)rg[t].y - rg[t].x;
+    // per tile: concatenation of its chunk sub-lists (values are Gaussian indices;
+    // the reference lists hold prepared (rank) indices)
+    std::vector<int32_t> rank_of((size_t)std::max(p->scene->d.n, 1), -1);
+    for (int r = 0; r < p->V; ++r) rank_of[order[r]] = r;
+    int64_t acc = 0;
+    for (int t = 0; t < nt; ++t) {
+        if (offsets) offsets[t] = acc;
+        for (int c = 0; c < nch; ++c) {
+            const uint4 r = rg[(size_t)c * nt + t];
+            if (ids)
+                for (uint32_t e = 0; e < r.y; ++e) ids[acc + e] = rank_of[vals[r.x + e]];
+            acc += r.y;
         }
-        offsets[p->ntiles] = acc;
     }
-    if (ids && p->K > 0) {
-        // values are Gaussian indices; the reference lists hold prepared (rank) indices
-        std::vector<int32_t> rank_of((size_t)std::max(p->scene->d.n, 1), -1);
-        for (int r = 0; r < p->V; ++r) rank_of[order[r]] = r;
-        int64_t o = 0;
-        for (int t = 0; t < p->ntiles; ++t)
-            for (uint32_t e = rg[t].x; e < rg[t].y; ++e) ids[o++] = rank_of[vals[e]];
-    }
+    if (offsets) offsets[nt] = acc;
     return TSB_OK;
 }
 
 int tsb_pass_debug_records(tsb_pass* p, float* rec12) {
     if (!p || !p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
+    int rc = read_visible(p);
+    if (rc) return rc;
     cudaStream_t st = p->ctx->stream;
     const int n = p->scene->d.n, V = p->V;
     std::vector<float4> A(std::max(n, 1)), B(std::max(n, 1)), C(std::max(n, 1)), D(std::max(n, 1));
@@ -952,14 +1068,14 @@ int tsb_pass_debug_records(tsb_pass* p, float* rec12) {
         const uint32_t i = g[r];
         float* o = rec12 + 12 * (size_t)r;
         const float l11 = B[i].x, l12 = B[i].y, l22 = B[i].z;
-        o[0] = A[i].x + A[i].z;  // mean x (approximate: rounded sum)
+        o[0] = A[i].x + A[i].z;  // mean x (rounded sum of base and offset)
         o[1] = A[i].y + A[i].w;
-        o[2] = l11 * l11;            // conic a
-        o[3] = l11 * l12;            // conic b
+        o[2] = l11 * l11;              // conic a
+        o[3] = l11 * l12;              // conic b
         o[4] = l12 * l12 + l22 * l22;  // conic c
-        o[5] = B[i].w;
-        o[6] = C[i].x;
-        o[7] = C[i].y;
+        o[5] = B[i].w;                 // opacity
+        o[6] = C[i].x;                 // coef
+        o[7] = C[i].y;                 // depth
         o[8] = C[i].z;
         o[9] = C[i].w;
         o[10] = p->nf > 1 ? D[i].x : 0.f;

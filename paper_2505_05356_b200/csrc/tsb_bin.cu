@@ -5,28 +5,33 @@
 //   1. depth sort: stable LSD radix sort of the fp64 depth bits (value = Gaussian
 //      index, input in index order -> ties broken by index exactly as the
 //      reference's comparator does).  The position in this order is the rank.
-//   2. gather tiles-touched into rank order, exclusive scan -> key offsets.
-//   3. duplicate: rank r writes (tile, gidx) for every tile of its rect, in rank
-//      order (values are Gaussian indices; records stay Gaussian-indexed).
-//   4. tile sort: stable radix sort of the 16-bit tile ids only (the emission
-//      is already rank-ordered, so only ceil(log2 tiles) bits need sorting).
-//   5. tile ranges [start, end) by boundary detection.
+//   2. depth-chunked counting sort by tile, no key materialisation:
+//      ranks are cut into segments of kSeg (one warp each) and segments into
+//      geometrically growing chunks.  Per chunk:
+//        k_bin_count  per (tile, segment) entry counts.  A warp handles 32 ranks
+//                     at a time; a tile is covered by lane j iff bit j of
+//                     colmask[tx] & rowmask[ty] (two ballot-built masks), so the
+//                     covering lanes of any tile are known in O(1).
+//        k_bin_scan   per tile: exclusive scan over the chunk's segments; tile
+//                     lengths; exclusive scan over tiles -> chunk ranges.
+//        k_bin_emit   stable scatter of Gaussian indices: position = cursor of
+//                     (tile, segment) + number of lower lanes covering the tile.
+//      The tile lists of a chunk are exactly the reference's lists restricted
+//      to that chunk's ranks, so their concatenation over chunks is the
+//      reference list.  Tiles whose pixels have all terminated are skipped by
+//      later chunks (the composite never reads past termination), unless the
+//      caller asks for full lists (parity mode).
 #include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 
 #include "tsb_internal.h"
 
 namespace tsb {
 
-size_t binning_temp_bytes(int n, int64_t k_cap) {
-    size_t a = 0, b = 0, c = 0;
+size_t depth_sort_temp_bytes(int n) {
+    size_t a = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, a, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
                                     (uint32_t*)nullptr, n > 0 ? n : 1, 0, 64);
-    cub::DeviceRadixSort::SortPairs(nullptr, b, (uint16_t*)nullptr, (uint16_t*)nullptr, (uint32_t*)nullptr,
-                                    (uint32_t*)nullptr, (int)(k_cap > 0 ? k_cap : 1), 0, 16);
-    cub::DeviceScan::ExclusiveSum(nullptr, c, (uint32_t*)nullptr, (uint32_t*)nullptr, n > 0 ? n : 1);
-    size_t m = a > b ? a : b;
-    return m > c ? m : c;
+    return a;
 }
 
 void launch_sort_depth(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n,
@@ -35,71 +40,242 @@ void launch_sort_depth(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in,
     cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, n, 0, 64, st);
 }
 
-__global__ void k_gather_counts(const uint32_t* __restrict__ sorted_gidx, const uint32_t* __restrict__ touched,
-                                uint32_t* __restrict__ cnt_sorted, int n) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < n) cnt_sorted[r] = touched[sorted_gidx[r]];
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kWarpsPerCta = 4;
+constexpr int kSmemTiles = 4096;  // per-warp shared-memory tile counters up to this many tiles
+
+__device__ __forceinline__ bool tile_done(const BinK& B, int t) {
+    return B.skip_done && B.tile_blocks_done[t] >= B.blocks_per_tile;
 }
 
-void launch_gather_counts(const uint32_t* sorted_gidx, const uint32_t* touched, uint32_t* cnt_sorted, int n,
-                          cudaStream_t st) {
-    if (n <= 0) return;
-    k_gather_counts<<<(n + 255) / 256, 256, 0, st>>>(sorted_gidx, touched, cnt_sorted, n);
+struct Box {
+    int x0, x1, y0, y1;  // union of the batch's tile rects (inclusive); empty when x0 > x1
+};
+
+// Load the 32 ranks of one batch and build the per-column / per-row lane masks:
+// lane j covers tile (tx, ty) iff bit j of colmask[tx] & rowmask[ty].
+__device__ __forceinline__ Box load_batch(const BinK& B, int r, int V, uint32_t* colmask, uint32_t* rowmask,
+                                          uint32_t* gids, int lane) {
+    int tx0 = 1, tx1 = 0, ty0 = 1, ty1 = 0;
+    uint32_t g = 0;
+    if (r < V) {
+        g = B.sorted_gidx[r];
+        const uint2 rc = B.rect[g];
+        const int x0 = rc.x & 0xffff, x1 = rc.x >> 16, y0 = rc.y & 0xffff, y1 = rc.y >> 16;
+        tx0 = x0 / B.ts;
+        tx1 = (x1 - 1) / B.ts;
+        ty0 = y0 / B.ts;
+        ty1 = (y1 - 1) / B.ts;
+    }
+    gids[lane] = g;
+    const bool valid = tx0 <= tx1;
+    Box u;
+    u.x0 = __reduce_min_sync(0xffffffffu, valid ? tx0 : 0x7fffffff);
+    u.x1 = __reduce_max_sync(0xffffffffu, valid ? tx1 : -1);
+    u.y0 = __reduce_min_sync(0xffffffffu, valid ? ty0 : 0x7fffffff);
+    u.y1 = __reduce_max_sync(0xffffffffu, valid ? ty1 : -1);
+    for (int tx = u.x0; tx <= u.x1; ++tx) {
+        const uint32_t m = __ballot_sync(0xffffffffu, valid && tx0 <= tx && tx <= tx1);
+        if (lane == 0) colmask[tx] = m;
+    }
+    for (int ty = u.y0; ty <= u.y1; ++ty) {
+        const uint32_t m = __ballot_sync(0xffffffffu, valid && ty0 <= ty && ty <= ty1);
+        if (lane == 0) rowmask[ty] = m;
+    }
+    __syncwarp();
+    return u;
 }
 
-void launch_scan(const uint32_t* in, uint32_t* out, int n, void* temp, size_t temp_bytes, cudaStream_t st) {
-    if (n <= 0) return;
-    cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, out, n, st);
-}
+}  // namespace
 
-__global__ void __launch_bounds__(256) k_duplicate(const uint32_t* __restrict__ sorted_gidx,
-                                                   const uint32_t* __restrict__ offsets,
-                                                   const uint32_t* __restrict__ cnt_sorted,
-                                                   const uint2* __restrict__ rect,
-                                                   uint16_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                                                   int n, int ts, int tiles_x) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    if (cnt_sorted[r] == 0) return;  // culled Gaussians sort to the end with 0 tiles
-    const uint32_t g = sorted_gidx[r];
-    const uint2 rc = rect[g];
-    const int x0 = rc.x & 0xffff, x1 = rc.x >> 16, y0 = rc.y & 0xffff, y1 = rc.y >> 16;
-    const int tx0 = x0 / ts, tx1 = (x1 - 1) / ts, ty0 = y0 / ts, ty1 = (y1 - 1) / ts;
-    uint32_t o = offsets[r];
-    for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx) {
-            keys[o] = (uint16_t)(ty * tiles_x + tx);
-            vals[o] = g;
-            ++o;
+// Per (segment, tile) entry counts of one depth chunk.  One warp per segment of
+// kSeg ranks; per batch of 32 ranks the lanes walk the tiles of the batch's
+// union box (no per-pair work: the number of coverers is popc of two masks).
+template <bool SMEM>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_bin_count(BinK B) {
+    extern __shared__ uint32_t smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int segl = blockIdx.x * kWarpsPerCta + wib;
+    if (segl >= B.nseg) return;
+    const int per_warp = 32 + B.tiles_x + B.tiles_y + (SMEM ? B.ntiles : 0);
+    uint32_t* gids = smem + wib * per_warp;
+    uint32_t* colmask = gids + 32;
+    uint32_t* rowmask = colmask + B.tiles_x;
+    uint32_t* cnt = SMEM ? rowmask + B.tiles_y : B.hist + (size_t)segl * B.ntiles;
+    const int V = *B.n_visible;
+    const int r0 = (B.seg0 + segl) * kSeg;
+    for (int t = lane; t < B.ntiles; t += 32) cnt[t] = 0u;
+    __syncwarp();
+    if (r0 < V) {
+        for (int b = 0; b < kSeg; b += 32) {
+            const Box u = load_batch(B, r0 + b + lane, V, colmask, rowmask, gids, lane);
+            const int bw = u.x1 - u.x0 + 1;
+            const int area = bw > 0 ? bw * (u.y1 - u.y0 + 1) : 0;
+            for (int i = lane; i < area; i += 32) {
+                const int ty = u.y0 + i / bw, tx = u.x0 + i % bw;
+                const uint32_t m = colmask[tx] & rowmask[ty];
+                if (m) {
+                    const int t = ty * B.tiles_x + tx;
+                    if (!tile_done(B, t)) cnt[t] += (uint32_t)__popc(m);
+                }
+            }
+            __syncwarp();
         }
+    }
+    if (SMEM) {
+        __syncwarp();
+        uint32_t* h = B.hist + (size_t)segl * B.ntiles;
+        for (int t = lane; t < B.ntiles; t += 32) h[t] = cnt[t];
+    }
 }
 
-void launch_duplicate(const uint32_t* sorted_gidx, const uint32_t* offsets, const uint32_t* cnt_sorted,
-                      const uint2* rect, uint16_t* keys, uint32_t* vals, int n, int ts, int tiles_x,
-                      cudaStream_t st) {
-    if (n <= 0) return;
-    k_duplicate<<<(n + 255) / 256, 256, 0, st>>>(sorted_gidx, offsets, cnt_sorted, rect, keys, vals, n, ts,
-                                                 tiles_x);
+// Per tile: exclusive scan over the chunk's segments (in place, segment-major
+// layout) and the tile's length.  Block = 32 tiles x 8 warps; warp w owns a
+// contiguous range of segments.
+__global__ void __launch_bounds__(256) k_bin_scan_segments(BinK B) {
+    __shared__ uint32_t part[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int t = blockIdx.x * 32 + lane;
+    const int per = (B.nseg + 7) / 8;
+    const int s0 = w * per, s1 = min(B.nseg, s0 + per);
+    uint32_t sum = 0;
+    if (t < B.ntiles)
+        for (int s = s0; s < s1; ++s) sum += B.hist[(size_t)s * B.ntiles + t];
+    part[w][lane] = sum;
+    __syncthreads();
+    uint32_t off = 0, tot = 0;
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t v = part[i][lane];
+        if (i < w) off += v;
+        tot += v;
+    }
+    if (t < B.ntiles) {
+        for (int s = s0; s < s1; ++s) {
+            uint32_t* h = B.hist + (size_t)s * B.ntiles + t;
+            const uint32_t v = *h;
+            *h = off;
+            off += v;
+        }
+        if (w == 0) B.tile_len[t] = tot;
+    }
 }
 
-void launch_sort_tiles(uint16_t* keys_in, uint16_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int64_t k,
-                       int bits, void* temp, size_t temp_bytes, cudaStream_t st) {
-    if (k <= 0) return;
-    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)k, 0, bits, st);
+// Exclusive scan of tile lengths -> this chunk's ranges; advances the running
+// list offset.  One block.
+__global__ void k_bin_scan_tiles(BinK B) {
+    __shared__ uint32_t warp_sums[32];
+    __shared__ uint32_t s_carry;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    const uint32_t base = *B.list_off;
+    for (int t0 = 0; t0 < B.ntiles; t0 += blockDim.x) {
+        const int t = t0 + tid;
+        const uint32_t v = t < B.ntiles ? B.tile_len[t] : 0u;
+        uint32_t inc = v;
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += u;
+        }
+        if (lane == 31) warp_sums[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t ws = lane < nw ? warp_sums[lane] : 0u;
+            uint32_t wi = ws;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xffffffffu, wi, d);
+                if (lane >= d) wi += u;
+            }
+            if (lane < nw) warp_sums[lane] = wi - ws;
+        }
+        __syncthreads();
+        const uint32_t carry = s_carry;
+        if (t < B.ntiles) {
+            const uint32_t start = base + carry + warp_sums[wid] + inc - v;
+            const uint32_t cum = B.chunk == 0 ? 0u : B.prev_ranges[t].z + B.prev_ranges[t].y;
+            const uint32_t skipped = (B.skip_done && B.tile_blocks_done[t] >= B.blocks_per_tile) ? 1u : 0u;
+            B.ranges[t] = make_uint4(start, v, cum, skipped);
+        }
+        __syncthreads();
+        if (tid == blockDim.x - 1) s_carry = carry + warp_sums[wid] + inc;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const uint32_t end = base + s_carry;
+        *B.list_off = end;
+        if (end > B.capacity) *B.overflow = 1;
+    }
 }
 
-__global__ void k_ranges(const uint16_t* __restrict__ keys, int64_t k, uint2* __restrict__ ranges) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= k) return;
-    const uint32_t t = keys[i];
-    if (i == 0 || keys[i - 1] != t) ranges[t].x = (uint32_t)i;
-    if (i == k - 1 || keys[i + 1] != t) ranges[t].y = (uint32_t)(i + 1);
+// Stable scatter of one depth chunk.  Lanes walk the batch's union tiles; the
+// coverers of tile t (bits of colmask & rowmask, in rank order) are written as
+// one contiguous run at the (segment, tile) cursor, which then advances.
+template <bool SMEM>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_bin_emit(BinK B) {
+    extern __shared__ uint32_t smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int segl = blockIdx.x * kWarpsPerCta + wib;
+    if (segl >= B.nseg) return;
+    if (*B.overflow) return;
+    const int V = *B.n_visible;
+    const int r0 = (B.seg0 + segl) * kSeg;
+    if (r0 >= V) return;
+    const int per_warp = 32 + B.tiles_x + B.tiles_y + (SMEM ? B.ntiles : 0);
+    uint32_t* gids = smem + wib * per_warp;
+    uint32_t* colmask = gids + 32;
+    uint32_t* rowmask = colmask + B.tiles_x;
+    uint32_t* h = B.hist + (size_t)segl * B.ntiles;
+    uint32_t* cur = SMEM ? rowmask + B.tiles_y : h;
+    for (int t = lane; t < B.ntiles; t += 32) cur[t] = B.ranges[t].x + h[t];
+    __syncwarp();
+    for (int b = 0; b < kSeg; b += 32) {
+        const Box u = load_batch(B, r0 + b + lane, V, colmask, rowmask, gids, lane);
+        const int bw = u.x1 - u.x0 + 1;
+        const int area = bw > 0 ? bw * (u.y1 - u.y0 + 1) : 0;
+        for (int i = lane; i < area; i += 32) {
+            const int ty = u.y0 + i / bw, tx = u.x0 + i % bw;
+            uint32_t m = colmask[tx] & rowmask[ty];
+            if (!m) continue;
+            const int t = ty * B.tiles_x + tx;
+            if (tile_done(B, t)) continue;
+            uint32_t c = cur[t];
+            cur[t] = c + (uint32_t)__popc(m);
+            while (m) {
+                const int j = __ffs(m) - 1;
+                m &= m - 1u;
+                B.vals[c++] = gids[j];
+            }
+        }
+        __syncwarp();
+    }
 }
 
-void launch_ranges(const uint16_t* keys, int64_t k, uint2* ranges, int ntiles, cudaStream_t st) {
-    cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)ntiles, st);
-    if (k <= 0) return;
-    k_ranges<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(keys, k, ranges);
+void launch_bin_chunk(const BinK& B, cudaStream_t st) {
+    const bool sm = B.ntiles <= kSmemTiles;
+    const size_t smem =
+        sizeof(uint32_t) * (size_t)(32 + B.tiles_x + B.tiles_y + (sm ? B.ntiles : 0)) * kWarpsPerCta;
+    const int grid = (B.nseg + kWarpsPerCta - 1) / kWarpsPerCta;
+    static bool attr = false;
+    if (!attr) {
+        const int mx = 200 * 1024;
+        cudaFuncSetAttribute(k_bin_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_bin_emit<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_bin_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_bin_emit<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        attr = true;
+    }
+    if (sm)
+        k_bin_count<true><<<grid, 32 * kWarpsPerCta, smem, st>>>(B);
+    else
+        k_bin_count<false><<<grid, 32 * kWarpsPerCta, smem, st>>>(B);
+    k_bin_scan_segments<<<(B.ntiles + 31) / 32, 256, 0, st>>>(B);
+    k_bin_scan_tiles<<<1, 1024, 0, st>>>(B);
+    if (sm)
+        k_bin_emit<true><<<grid, 32 * kWarpsPerCta, smem, st>>>(B);
+    else
+        k_bin_emit<false><<<grid, 32 * kWarpsPerCta, smem, st>>>(B);
 }
 
 }  // namespace tsb

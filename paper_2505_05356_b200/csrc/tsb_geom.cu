@@ -72,105 +72,142 @@ void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const Fram
 // list entries in parallel (the same prep64 the preprocess used), then the warp
 // walks them in order exactly as splat.cpp:260-297 does.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, FrameK F,
-                                               const uint2* __restrict__ ranges,
-                                               const uint32_t* __restrict__ tile_vals, PixK px,
-                                               int nf) {
-    const int lane = threadIdx.x & 31;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    const int count = *px.n_flagged;
-    const int W = C.W, H = C.H;
-    const size_t HW = (size_t)W * H;
-    for (int i = warp; i < count; i += nwarps) {
-        const int pix = px.flagged[i];
-        const int x = pix % W, y = pix / W;
-        const int tile = (y / O.ts) * O.tiles_x + (x / O.ts);
-        const uint2 rg = ranges[tile];
-        const double pcx = x + 0.5, pcy = y + 0.5;
-        double T = 1.0, SW = 0.0, SD = 0.0, Tpre = 1.0;
-        double accQ[8];
-        for (int c = 0; c < 8; ++c) accQ[c] = 0.0;
-        int nc = 0, processed = (int)(rg.y - rg.x), last_eff = -1;
-        bool done = false;
-        for (uint32_t b = rg.x; b < rg.y && !done; b += 32) {
-            const uint32_t e = b + lane;
-            bool inc = false;
-            double alpha = 0, coef = 0, depth = 0, sn[2] = {0, 0}, cs[2] = {0, 0};
-            if (e < rg.y) {
-                Prep64 s;
-                prep64(S, C, O, F, (int)tile_vals[e], s);  // visible by construction
-                if (!(x < s.x0 || x >= s.x1 || y < s.y0 || y >= s.y1)) {
-                    const double dx = pcx - s.mean[0], dy = pcy - s.mean[1];
-                    const double maha = s.ca * dx * dx + 2.0 * s.cb * dx * dy + s.cc * dy * dy;
-                    if (!(maha > O.cut2 || maha < 0.0)) {
-                        const double g = exp(-0.5 * maha);
-                        alpha = s.opacity * g;
-                        if (!(alpha < O.alpha_thr)) {
-                            inc = true;
-                            coef = s.coef;
-                            depth = s.depth;
-                            for (int f = 0; f < nf; ++f) {
-                                sincos(phase_of_depth(s.depth, S.freq[f], S.c), &sn[f], &cs[f]);
-                            }
-                        }
-                    }
-                }
-            }
-            const unsigned incm = __ballot_sync(0xffffffffu, inc);
-            const int nb = min(32u, rg.y - b);
-            for (int j = 0; j < nb; ++j) {
-                if (!((incm >> j) & 1u)) continue;
-                const double a = __shfl_sync(0xffffffffu, alpha, j);
-                const double cf = __shfl_sync(0xffffffffu, coef, j);
-                const double dp = __shfl_sync(0xffffffffu, depth, j);
-                double s_[2], c_[2];
-                for (int f = 0; f < 2; ++f) {
-                    s_[f] = __shfl_sync(0xffffffffu, sn[f], j);
-                    c_[f] = __shfl_sync(0xffffffffu, cs[f], j);
-                }
-                ++nc;
-                const double w = a * T;
-                const double w2 = a * T * T;
-                const double cq = cf * w2;
-                for (int f = 0; f < nf; ++f) {
-                    accQ[4 * f + 0] += cq * s_[f];
-                    accQ[4 * f + 1] += cq * c_[f];
-                    accQ[4 * f + 2] -= cq * s_[f];
-                    accQ[4 * f + 3] -= cq * c_[f];
-                }
-                SW += w;
-                SD += w * dp;
-                Tpre = T;
-                T *= 1.0 - a;
-                if (T == 0.0 && last_eff < 0) last_eff = (int)(b + j + 1 - rg.x);
-                if (T < O.floor_T) {
-                    processed = (int)(b + j + 1 - rg.x);
-                    done = true;
-                    break;
+struct FixupAcc {
+    double T, SW, SD, Tpre, accQ[8];
+    int nc, processed, last_eff;
+    bool done;
+};
+
+// One batch of up to 32 candidate entries (lane-parallel fp64 evaluation, then
+// an in-order sequential composite exactly as splat.cpp:260-297).
+__device__ __forceinline__ void fixup_batch(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F, int nf,
+                                            int x, int y, bool is_entry, int g, int entry_idx, FixupAcc& a) {
+    const double pcx = x + 0.5, pcy = y + 0.5;
+    bool inc = false;
+    double alpha = 0, coef = 0, depth = 0, sn[2] = {0, 0}, cs[2] = {0, 0};
+    if (is_entry) {
+        Prep64 s;
+        prep64(S, C, O, F, g, s);  // visible by construction
+        if (!(x < s.x0 || x >= s.x1 || y < s.y0 || y >= s.y1)) {
+            const double dx = pcx - s.mean[0], dy = pcy - s.mean[1];
+            const double maha = s.ca * dx * dx + 2.0 * s.cb * dx * dy + s.cc * dy * dy;
+            if (!(maha > O.cut2 || maha < 0.0)) {
+                const double gg = exp(-0.5 * maha);
+                alpha = s.opacity * gg;
+                if (!(alpha < O.alpha_thr)) {
+                    inc = true;
+                    coef = s.coef;
+                    depth = s.depth;
+                    for (int f = 0; f < nf; ++f) sincos(phase_of_depth(s.depth, S.freq[f], S.c), &sn[f], &cs[f]);
                 }
             }
         }
-        if (lane == 0) {
-            const size_t o = (size_t)y * W + x;
-            for (int c = 0; c < 4 * nf; ++c)
-                px.out[c * HW + o] = (float)(accQ[c] + O.bg_quad[c] * T * T);
-            px.out[ch_depth_raw(nf) * HW + o] = (float)SD;
-            px.out[ch_depth(nf) * HW + o] = SW > O.cov_eps ? (float)(SD / SW) : __int_as_float(0x7fc00000);
-            px.out[ch_weight(nf) * HW + o] = (float)SW;
-            px.out[ch_T(nf) * HW + o] = (float)T;
-            if (px.n_contrib) px.n_contrib[o] = nc;
-            if (px.n_processed) px.n_processed[o] = processed;
-            const int le = last_eff >= 0 ? last_eff : processed;
-            px.last[o] = le | (int)0x80000000;
-            px.T_pre[o] = (float)Tpre;
+    }
+    const unsigned incm = __ballot_sync(0xffffffffu, inc);
+    for (int j = 0; j < 32; ++j) {
+        if (!((incm >> j) & 1u)) continue;
+        const double al = __shfl_sync(0xffffffffu, alpha, j);
+        const double cf = __shfl_sync(0xffffffffu, coef, j);
+        const double dp = __shfl_sync(0xffffffffu, depth, j);
+        const int ei = __shfl_sync(0xffffffffu, entry_idx, j);
+        double s_[2], c_[2];
+        for (int f = 0; f < 2; ++f) {
+            s_[f] = __shfl_sync(0xffffffffu, sn[f], j);
+            c_[f] = __shfl_sync(0xffffffffu, cs[f], j);
+        }
+        ++a.nc;
+        const double w = al * a.T;
+        const double w2 = al * a.T * a.T;
+        const double cq = cf * w2;
+        for (int f = 0; f < nf; ++f) {
+            a.accQ[4 * f + 0] += cq * s_[f];
+            a.accQ[4 * f + 1] += cq * c_[f];
+            a.accQ[4 * f + 2] -= cq * s_[f];
+            a.accQ[4 * f + 3] -= cq * c_[f];
+        }
+        a.SW += w;
+        a.SD += w * dp;
+        a.Tpre = a.T;
+        a.T *= 1.0 - al;
+        if (a.T == 0.0 && a.last_eff < 0) a.last_eff = ei + 1;
+        if (a.T < O.floor_T) {
+            a.processed = ei + 1;
+            a.done = true;
+            return;
         }
     }
 }
 
-void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
-                  const uint2* ranges, const uint32_t* tile_vals, const PixK& px, int nf, cudaStream_t st) {
-    k_fixup<<<148 * 4, 128, 0, st>>>(S, C, O, F, ranges, tile_vals, px, nf);
+__global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, FrameK F, FixupK fx, PixK px, int nf) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int count = *fx.overflow ? 0 : *px.n_flagged;
+    const int W = C.W, H = C.H;
+    const int ntiles = O.tiles_x * O.tiles_y;
+    const size_t HW = (size_t)W * H;
+    const int V = *fx.n_visible;
+    const uint32_t lanes_below = (1u << lane) - 1u;
+    for (int i = warp; i < count; i += nwarps) {
+        const int pix = px.flagged[i];
+        const int x = pix % W, y = pix / W;
+        const int tx = x / O.ts, ty = y / O.ts;
+        const int tile = ty * O.tiles_x + tx;
+        FixupAcc a;
+        a.T = 1.0; a.SW = 0.0; a.SD = 0.0; a.Tpre = 1.0;
+        for (int c = 0; c < 8; ++c) a.accQ[c] = 0.0;
+        a.nc = 0; a.processed = 0; a.last_eff = -1; a.done = false;
+        int scan_from = -1;  // rank where the tile stopped being binned
+        for (int ch = 0; ch < fx.nchunks && !a.done; ++ch) {
+            const uint4 rg = fx.ranges_all[(size_t)ch * ntiles + tile];  // (start, len, cum, skipped)
+            if (rg.w) {
+                scan_from = fx.chunk_rank0[ch];
+                break;
+            }
+            a.processed = (int)(rg.z + rg.y);
+            const uint32_t end = rg.x + rg.y;
+            for (uint32_t b = rg.x; b < end && !a.done; b += 32) {
+                const uint32_t e = b + lane;
+                const bool is_e = e < end;
+                fixup_batch(S, C, O, F, nf, x, y, is_e, is_e ? (int)fx.vals[e] : 0, (int)(rg.z + (e - rg.x)), a);
+            }
+        }
+        if (!a.done && scan_from < 0 && fx.binned_end_rank < V) scan_from = fx.binned_end_rank;
+        // Rare: the exact composite continues past the binned entries of this tile;
+        // walk the remaining Gaussians in rank (== list) order directly.
+        for (int r0 = scan_from; r0 >= 0 && r0 < V && !a.done; r0 += 32) {
+            const int r = r0 + lane;
+            int g = 0;
+            bool cov = false;
+            if (r < V) {
+                g = (int)fx.sorted_gidx[r];
+                const uint2 rc = fx.rect[g];
+                const int x0 = rc.x & 0xffff, x1 = rc.x >> 16, y0 = rc.y & 0xffff, y1 = rc.y >> 16;
+                cov = x0 / O.ts <= tx && tx <= (x1 - 1) / O.ts && y0 / O.ts <= ty && ty <= (y1 - 1) / O.ts;
+            }
+            const unsigned cm = __ballot_sync(0xffffffffu, cov);
+            fixup_batch(S, C, O, F, nf, x, y, cov, g, a.processed + __popc(cm & lanes_below), a);
+            if (!a.done) a.processed += __popc(cm);
+        }
+        if (lane == 0) {
+            const size_t o = (size_t)y * W + x;
+            for (int c = 0; c < 4 * nf; ++c) px.out[c * HW + o] = (float)(a.accQ[c] + O.bg_quad[c] * a.T * a.T);
+            px.out[ch_depth_raw(nf) * HW + o] = (float)a.SD;
+            px.out[ch_depth(nf) * HW + o] = a.SW > O.cov_eps ? (float)(a.SD / a.SW) : __int_as_float(0x7fc00000);
+            px.out[ch_weight(nf) * HW + o] = (float)a.SW;
+            px.out[ch_T(nf) * HW + o] = (float)a.T;
+            if (px.n_contrib) px.n_contrib[o] = a.nc;
+            if (px.n_processed) px.n_processed[o] = a.processed;
+            const int le = a.last_eff >= 0 ? a.last_eff : a.processed;
+            px.last[o] = le | (int)0x80000000;
+            px.T_pre[o] = (float)a.Tpre;
+        }
+    }
+}
+
+void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F, const FixupK& fx,
+                  const PixK& px, int nf, cudaStream_t st) {
+    k_fixup<<<148 * 4, 128, 0, st>>>(S, C, O, F, fx, px, nf);
 }
 
 // ---------------------------------------------------------------------------

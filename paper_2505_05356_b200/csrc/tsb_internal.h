@@ -57,6 +57,46 @@ struct RecK {
     float4* D;  // sin(psi_1), cos(psi_1), 0, 0   (second frequency only)
 };
 
+// Depth-chunked binning (tsb_bin.cu).  Ranks are cut into segments of kSeg
+// (one warp each); chunk c covers segments [seg0, seg0 + nseg).
+constexpr int kSeg = 64;
+struct BinK {
+    const uint32_t* sorted_gidx;
+    const uint2* rect;
+    const int32_t* n_visible;
+    int ts, tiles_x, tiles_y, ntiles;
+    const int32_t* tile_blocks_done;  // raster blocks finished per tile
+    int blocks_per_tile;
+    int skip_done;                    // 0: emit full lists (parity mode)
+    uint32_t* hist;                   // [nseg][ntiles] counts -> exclusive offsets within the tile
+    int seg0, nseg, chunk;
+    uint32_t* tile_len;               // [ntiles]
+    uint4* ranges;                    // [ntiles] this chunk: (start, len, cum entries before, 0)
+    const uint4* prev_ranges;         // previous chunk's ranges (chunk > 0)
+    uint32_t* vals;                   // list storage (Gaussian indices)
+    uint32_t* list_off;               // device running offset into vals
+    uint32_t capacity;
+    int32_t* overflow;
+};
+
+// Forward state carried across chunk launches (SoA planes of npx).
+struct FwdState {
+    float* f;    // 9 planes: T, Tpre, SW, SD, errT, accS0, accC0, accS1, accC1
+    int32_t* i;  // 3 planes: n_contrib, flags (1 done, 2 fixup, 4 finalized), last_eff
+    int npx;
+};
+
+struct ChunkK {
+    const uint4* ranges;  // this chunk's per-tile ranges
+    int first;            // chunk 0: initialise state
+    int chunk_end_rank;   // last chunk when >= n_visible
+    const int32_t* n_visible;
+    int32_t* block_done;        // per raster block
+    int32_t* tile_blocks_done;  // per tile
+    int32_t* blocks_done_total;
+    const int32_t* overflow;    // list storage overflowed: the host re-runs the frame
+};
+
 // Per-pixel raster state written by the forward pass for the backward pass.
 struct PixK {
     float* out;          // [C][H][W] planar outputs: quad(4*nf), depth_raw, depth, weight, T
@@ -81,32 +121,34 @@ __host__ __device__ inline int ch_T(int nf) { return 4 * nf + 3; }
 void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
                        uint64_t* depth_key, uint32_t* gidx, uint32_t* touched, uint2* rect, RecK rec,
                        int32_t* n_visible, cudaStream_t st);
-void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
-                  const uint2* ranges, const uint32_t* tile_vals, const PixK& px, int nf, cudaStream_t st);
+struct FixupK {
+    const uint4* ranges_all;  // [nchunks][ntiles] (start, len, cum, skipped)
+    int nchunks;
+    const int* chunk_rank0;   // device [nchunks] first rank of each chunk
+    int binned_end_rank;      // first rank after the last binned chunk
+    const uint32_t* vals;
+    const uint32_t* sorted_gidx;
+    const uint2* rect;
+    const int32_t* n_visible;
+    const int32_t* overflow;
+};
+void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F, const FixupK& fx,
+                  const PixK& px, int nf, cudaStream_t st);
 void launch_chain(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
                   const uint32_t* touched, float* screen, float4* grads, cudaStream_t st);
 // tsb_bin.cu
-size_t binning_temp_bytes(int n, int64_t k_cap);
-void launch_gather_counts(const uint32_t* sorted_gidx, const uint32_t* touched, uint32_t* cnt_sorted,
-                          int n, cudaStream_t st);
-void launch_scan(const uint32_t* in, uint32_t* out, int n, void* temp, size_t temp_bytes,
-                 cudaStream_t st);
+size_t depth_sort_temp_bytes(int n);
 void launch_sort_depth(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, uint32_t* vals_out,
                        int n, void* temp, size_t temp_bytes, cudaStream_t st);
-void launch_duplicate(const uint32_t* sorted_gidx, const uint32_t* offsets, const uint32_t* cnt_sorted,
-                      const uint2* rect, uint16_t* keys, uint32_t* vals, int n, int ts, int tiles_x,
-                      cudaStream_t st);
-void launch_sort_tiles(uint16_t* keys_in, uint16_t* keys_out, uint32_t* vals_in, uint32_t* vals_out,
-                       int64_t k, int bits, void* temp, size_t temp_bytes, cudaStream_t st);
-void launch_ranges(const uint16_t* keys, int64_t k, uint2* ranges, int ntiles, cudaStream_t st);
+void launch_bin_chunk(const BinK& B, cudaStream_t st);
 // tsb_raster.cu
-void launch_raster_fwd(const RecK& rec, const uint2* ranges, const uint32_t* tile_vals, const OptK& O,
-                       int W, int H, int nf, PixK px, const float* target, const float* ch_w,
+void launch_raster_fwd(const RecK& rec, const ChunkK& ck, const uint32_t* tile_vals, const OptK& O,
+                       int W, int H, int nf, PixK px, FwdState fs, const float* target, const float* ch_w,
                        double* loss_part, cudaStream_t st);
 void launch_fixup_loss(const PixK& px, int W, int H, int nf, const float* target, const float* ch_w,
                        double* loss_extra, int max_flag, cudaStream_t st);
-void launch_raster_bwd(const RecK& rec, const uint2* ranges, const uint32_t* tile_vals, const OptK& O,
-                       int W, int H, int nf, const float* dpsi, PixK px, const float* d_quad,
+void launch_raster_bwd(const RecK& rec, const uint4* ranges_all, int nchunks, const uint32_t* tile_vals,
+                       const OptK& O, int W, int H, int nf, const float* dpsi, PixK px, const float* d_quad,
                        float* screen, int scap, double* bg_part, cudaStream_t st);
 void launch_reduce_partials(const double* part, int nparts, int width, double* out,
                             double scale, cudaStream_t st);

@@ -64,88 +64,117 @@ struct Smem {
 };
 
 // ---------------------------------------------------------------------------
+// Forward composite of one depth chunk.  Per-pixel state (T, accumulators,
+// counters) is carried across chunk launches in FwdState; a pixel is finalised
+// (outputs, fix-up flag, loss epilogue) in the launch in which it terminates,
+// or in the last chunk.  Blocks whose pixels are all done mark themselves so
+// later chunks neither bin nor raster them.
 template <int NF>
-__global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, const uint2* __restrict__ ranges,
-                                                                const uint32_t* __restrict__ vals, OptK O, int W,
-                                                                int H, PixK px, const float* __restrict__ target,
+__global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK ck, const uint32_t* __restrict__ vals,
+                                                                OptK O, int W, int H, PixK px, FwdState fs,
+                                                                const float* __restrict__ target,
                                                                 const float* __restrict__ chw,
                                                                 double* __restrict__ loss_part) {
     __shared__ Smem<NF> sm;
     __shared__ float red[kRasterThreads / 32];
+    if (ck.block_done[blockIdx.x] || *ck.overflow) return;
     const int nsub = O.sub * O.sub;
     const int tile = blockIdx.x / nsub, sb = blockIdx.x % nsub;
     const int tid = threadIdx.x;
     const int lx = (sb % O.sub) * kTile + (tid % kTile), ly = (sb / O.sub) * kTile + (tid / kTile);
     const int x = (tile % O.tiles_x) * O.ts + lx, y = (tile / O.tiles_x) * O.ts + ly;
     const bool active = lx < O.ts && ly < O.ts && x < W && y < H;
-    const uint2 rg = ranges[tile];
+    const uint4 rg = ck.ranges[tile];  // (start, len, cum, -)
     const float pcx = (float)x + 0.5f, pcy = (float)y + 0.5f;
+    const size_t HW = (size_t)W * H, o = active ? (size_t)y * W + x : 0;
 
     float T = 1.f, Tpre = 1.f, SW = 0.f, SD = 0.f, errT = 0.f;
     float accS[NF], accC[NF];
 #pragma unroll
     for (int f = 0; f < NF; ++f) accS[f] = accC[f] = 0.f;
-    int nc = 0, processed = (int)(rg.y - rg.x), last_eff = -1;
-    bool done = !active, flag = false;
+    int nc = 0, flags = 0, last_eff = -1;
+    if (active && !ck.first) {
+        T = fs.f[0 * (size_t)fs.npx + o];
+        Tpre = fs.f[1 * (size_t)fs.npx + o];
+        SW = fs.f[2 * (size_t)fs.npx + o];
+        SD = fs.f[3 * (size_t)fs.npx + o];
+        errT = fs.f[4 * (size_t)fs.npx + o];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            accS[f] = fs.f[(5 + 2 * f) * (size_t)fs.npx + o];
+            accC[f] = fs.f[(6 + 2 * f) * (size_t)fs.npx + o];
+        }
+        nc = fs.i[0 * (size_t)fs.npx + o];
+        flags = fs.i[1 * (size_t)fs.npx + o];
+        last_eff = fs.i[2 * (size_t)fs.npx + o];
+    }
+    const bool was_done = !active || (flags & 1);
+    bool done = was_done, flag = (flags & 2) != 0;
+    int processed = (int)(rg.z + rg.y);
     const float cut2 = O.cut2_f, thr = O.alpha_thr_f, fl = O.floor_f;
     const float bandM = kBandMaha * cut2, bandA = kBandAlpha * thr;
+    const uint32_t end = rg.x + rg.y;
 
-    for (uint32_t b = rg.x; b < rg.y; b += kRasterThreads) {
-        const uint32_t e = b + tid;
-        if (e < rg.y) {
-            const uint32_t r = vals[e];
-            sm.A[tid] = rec.A[r];
-            sm.B[tid] = rec.B[r];
-            sm.C[tid] = rec.C[r];
-            if (NF > 1) sm.D[tid] = rec.D[r];
-        }
-        __syncthreads();
-        if (!done) {
-            const int nb = min((uint32_t)kRasterThreads, rg.y - b);
-            for (int j = 0; j < nb; ++j) {
-                const float4 A = sm.A[j], B = sm.B[j];
-                Eval ev;
-                eval_entry(A, B, pcx, pcy, ev);
-                const float dm = ev.maha - cut2;
-                if (fabsf(dm) <= bandM) flag = true;
-                if (dm > 0.f) continue;
-                eval_alpha(B, ev);
-                const float da = ev.alpha - thr;
-                if (fabsf(da) <= bandA) flag = true;
-                if (da < 0.f) continue;
-                ++nc;
-                const float4 Cc = sm.C[j];
-                const float w = ev.alpha * T;
-                const float w2 = w * T;
-                const float cq = Cc.x * w2;
-                accS[0] = fmaf(cq, Cc.z, accS[0]);
-                accC[0] = fmaf(cq, Cc.w, accC[0]);
-                if (NF > 1) {
-                    const float4 Dd = sm.D[j];
-                    accS[NF - 1] = fmaf(cq, Dd.x, accS[NF - 1]);
-                    accC[NF - 1] = fmaf(cq, Dd.y, accC[NF - 1]);
-                }
-                SW += w;
-                SD = fmaf(w, Cc.y, SD);
-                Tpre = T;
-                const float om = 1.f - ev.alpha;
-                T = T * om;
-                errT += kEpsAlpha * __fdividef(ev.alpha, om) + 1.2e-7f;
-                if (T < fl * (1.f + 4.f * errT) && T > fl * (1.f - 4.f * errT)) flag = true;
-                if (T == 0.f && last_eff < 0) last_eff = (int)(b + j + 1 - rg.x);
-                if (T < fl) {
-                    processed = (int)(b + j + 1 - rg.x);
-                    done = true;
-                    break;
+    if (__syncthreads_count(done) < kRasterThreads) {
+        for (uint32_t b = rg.x; b < end; b += kRasterThreads) {
+            const uint32_t e = b + tid;
+            if (e < end) {
+                const uint32_t r = vals[e];
+                sm.A[tid] = rec.A[r];
+                sm.B[tid] = rec.B[r];
+                sm.C[tid] = rec.C[r];
+                if (NF > 1) sm.D[tid] = rec.D[r];
+            }
+            __syncthreads();
+            if (!done) {
+                const int nb = min((uint32_t)kRasterThreads, end - b);
+                for (int j = 0; j < nb; ++j) {
+                    const float4 A = sm.A[j], B = sm.B[j];
+                    Eval ev;
+                    eval_entry(A, B, pcx, pcy, ev);
+                    const float dm = ev.maha - cut2;
+                    if (fabsf(dm) <= bandM) flag = true;
+                    if (dm > 0.f) continue;
+                    eval_alpha(B, ev);
+                    const float da = ev.alpha - thr;
+                    if (fabsf(da) <= bandA) flag = true;
+                    if (da < 0.f) continue;
+                    ++nc;
+                    const float4 Cc = sm.C[j];
+                    const float w = ev.alpha * T;
+                    const float w2 = w * T;
+                    const float cq = Cc.x * w2;
+                    accS[0] = fmaf(cq, Cc.z, accS[0]);
+                    accC[0] = fmaf(cq, Cc.w, accC[0]);
+                    if (NF > 1) {
+                        const float4 Dd = sm.D[j];
+                        accS[NF - 1] = fmaf(cq, Dd.x, accS[NF - 1]);
+                        accC[NF - 1] = fmaf(cq, Dd.y, accC[NF - 1]);
+                    }
+                    SW += w;
+                    SD = fmaf(w, Cc.y, SD);
+                    Tpre = T;
+                    const float om = 1.f - ev.alpha;
+                    T = T * om;
+                    errT += kEpsAlpha * __fdividef(ev.alpha, om) + 1.2e-7f;
+                    if (T < fl * (1.f + 4.f * errT) && T > fl * (1.f - 4.f * errT)) flag = true;
+                    const int gidx_e = (int)(rg.z + (b - rg.x) + j + 1);
+                    if (T == 0.f && last_eff < 0) last_eff = gidx_e;
+                    if (T < fl) {
+                        processed = gidx_e;
+                        done = true;
+                        break;
+                    }
                 }
             }
+            if (__syncthreads_count(done) == kRasterThreads) break;
         }
-        if (__syncthreads_count(done) == kRasterThreads) break;
     }
 
+    const bool is_last = ck.chunk_end_rank >= *ck.n_visible;
+    const bool finalize = !was_done && (done || is_last);
     float lpx = 0.f;
-    if (active) {
-        const size_t HW = (size_t)W * H, o = (size_t)y * W + x;
+    if (finalize) {
         const float T2 = T * T;
         float q[4 * NF];
 #pragma unroll
@@ -165,6 +194,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, const u
         if (px.n_processed) px.n_processed[o] = processed;
         px.last[o] = last_eff >= 0 ? last_eff : processed;
         px.T_pre[o] = Tpre;
+        fs.i[1 * (size_t)fs.npx + o] = 1;  // done (read by later chunks only if the block is not done)
         if (flag) {
             const int slot = atomicAdd(px.n_flagged, 1);
             px.flagged[slot] = (int)o;
@@ -177,7 +207,22 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, const u
                 px.d_quad[c * HW + o] = chw[c] * s2 * r;
             }
         }
+    } else if (!was_done) {
+        fs.f[0 * (size_t)fs.npx + o] = T;
+        fs.f[1 * (size_t)fs.npx + o] = Tpre;
+        fs.f[2 * (size_t)fs.npx + o] = SW;
+        fs.f[3 * (size_t)fs.npx + o] = SD;
+        fs.f[4 * (size_t)fs.npx + o] = errT;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            fs.f[(5 + 2 * f) * (size_t)fs.npx + o] = accS[f];
+            fs.f[(6 + 2 * f) * (size_t)fs.npx + o] = accC[f];
+        }
+        fs.i[0 * (size_t)fs.npx + o] = nc;
+        fs.i[1 * (size_t)fs.npx + o] = flag ? 2 : 0;
+        fs.i[2 * (size_t)fs.npx + o] = last_eff;
     }
+    const bool block_finished = __syncthreads_count(done || is_last) == kRasterThreads;
     if (target) {
         for (int m = 16; m > 0; m >>= 1) lpx += __shfl_xor_sync(0xffffffffu, lpx, m);
         if ((tid & 31) == 0) red[tid >> 5] = lpx;
@@ -185,8 +230,13 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, const u
         if (tid == 0) {
             double s = 0.0;
             for (int i = 0; i < kRasterThreads / 32; ++i) s += red[i];
-            loss_part[blockIdx.x] = s;
+            loss_part[blockIdx.x] += s;
         }
+    }
+    if (block_finished && tid == 0) {
+        ck.block_done[blockIdx.x] = 1;
+        atomicAdd(&ck.tile_blocks_done[tile], 1);
+        atomicAdd(ck.blocks_done_total, 1);
     }
 }
 
@@ -244,10 +294,10 @@ __device__ __forceinline__ float reduce_scatter8(float v[8], int lane) {
 }
 
 template <int NF>
-__global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const uint2* __restrict__ ranges,
-                                                                const uint32_t* __restrict__ vals, OptK O, int W,
-                                                                int H, float dpsi0, float dpsi1, PixK px,
-                                                                const float* __restrict__ d_quad,
+__global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const uint4* __restrict__ ranges_all,
+                                                                int nchunks, const uint32_t* __restrict__ vals,
+                                                                OptK O, int W, int H, float dpsi0, float dpsi1,
+                                                                PixK px, const float* __restrict__ d_quad,
                                                                 float* __restrict__ screen, int scap,
                                                                 double* __restrict__ bg_part) {
     __shared__ Smem<NF> sm;
@@ -256,14 +306,14 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
     __shared__ int smax[kRasterThreads / 32];
     __shared__ float sbg[kRasterThreads / 32][4 * NF];
     const int nsub = O.sub * O.sub;
+    const int ntiles = O.tiles_x * O.tiles_y;
     const int tile = blockIdx.x / nsub, sb = blockIdx.x % nsub;
     const int tid = threadIdx.x, lane = tid & 31;
     const int lx = (sb % O.sub) * kTile + (tid % kTile), ly = (sb / O.sub) * kTile + (tid / kTile);
     const int x = (tile % O.tiles_x) * O.ts + lx, y = (tile / O.tiles_x) * O.ts + ly;
     const bool active = lx < O.ts && ly < O.ts && x < W && y < H;
-    const uint2 rg = ranges[tile];
     const float pcx = (float)x + 0.5f, pcy = (float)y + 0.5f;
-    const size_t HW = (size_t)W * H, o = (size_t)y * W + x;
+    const size_t HW = (size_t)W * H, o = active ? (size_t)y * W + x : 0;
 
     int last = 0;
     float Tnext = 0.f, A = 0.f;
@@ -315,11 +365,15 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
     bool first = true;
     const float cut2 = O.cut2_f, thr = O.alpha_thr_f;
 
-    if (bmax > 0) {
-        const int nbatch = (bmax + kRasterThreads - 1) / kRasterThreads;
+    // entries are walked back to front over the concatenation of the chunk lists
+    for (int c = nchunks - 1; c >= 0 && bmax > 0; --c) {
+        const uint4 rg = ranges_all[(size_t)c * ntiles + tile];  // (start, len, cum)
+        if ((int)rg.z >= bmax || rg.y == 0) continue;
+        const int n_here = min((int)rg.y, bmax - (int)rg.z);
+        const int nbatch = (n_here + kRasterThreads - 1) / kRasterThreads;
         for (int bi = nbatch - 1; bi >= 0; --bi) {
             const uint32_t b = rg.x + (uint32_t)bi * kRasterThreads;
-            const int nb = min(kRasterThreads, bmax - bi * kRasterThreads);
+            const int nb = min(kRasterThreads, n_here - bi * kRasterThreads);
             if (tid < nb) {
                 const uint32_t r = vals[b + tid];
                 srank[tid] = r;
@@ -330,7 +384,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
             }
             __syncthreads();
             for (int j = nb - 1; j >= 0; --j) {
-                const int el = bi * kRasterThreads + j;
+                const int el = (int)rg.z + bi * kRasterThreads + j;
                 bool contrib = false;
                 float g8[8];
                 if (el < last) {
@@ -347,8 +401,8 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
                             Tnext = Tk;
                             const float4 Cc = sm.C[j];
                             const float coef = Cc.x;
-                            float su = us[0] * Cc.z + uc[0] * Cc.w;       // upQ . basis
-                            float sd = dpsi0 * (us[0] * Cc.w - uc[0] * Cc.z);  // upQ . dbasis
+                            float su = us[0] * Cc.z + uc[0] * Cc.w;            // upQ . basis / coef
+                            float sd = dpsi0 * (us[0] * Cc.w - uc[0] * Cc.z);  // upQ . dbasis / coef
                             if (NF > 1) {
                                 const float4 Dd = sm.D[j];
                                 su += us[NF - 1] * Dd.x + uc[NF - 1] * Dd.y;
@@ -374,7 +428,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
                 if (__any_sync(0xffffffffu, contrib)) {
                     if (!contrib) {
 #pragma unroll
-                        for (int c = 0; c < 8; ++c) g8[c] = 0.f;
+                        for (int cc = 0; cc < 8; ++cc) g8[cc] = 0.f;
                     }
                     const float s = reduce_scatter8(g8, lane);
                     if ((lane & 3) == 0) {
@@ -387,10 +441,10 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
             if (tid < nb) {
                 const uint32_t r = srank[tid];
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const float v = sacc[tid][c];
-                    if (v != 0.f) atomicAdd(&screen[(size_t)c * scap + r], v);
-                    sacc[tid][c] = 0.f;
+                for (int cc = 0; cc < 8; ++cc) {
+                    const float v = sacc[tid][cc];
+                    if (v != 0.f) atomicAdd(&screen[(size_t)cc * scap + r], v);
+                    sacc[tid][cc] = 0.f;
                 }
             }
             __syncthreads();
@@ -398,14 +452,16 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
     }
 }
 
-void launch_raster_fwd(const RecK& rec, const uint2* ranges, const uint32_t* tile_vals, const OptK& O, int W,
-                       int H, int nf, PixK px, const float* target, const float* ch_w, double* loss_part,
+void launch_raster_fwd(const RecK& rec, const ChunkK& ck, const uint32_t* tile_vals, const OptK& O, int W, int H,
+                       int nf, PixK px, FwdState fs, const float* target, const float* ch_w, double* loss_part,
                        cudaStream_t st) {
     const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
     if (nf > 1)
-        k_raster_fwd<2><<<grid, kRasterThreads, 0, st>>>(rec, ranges, tile_vals, O, W, H, px, target, ch_w, loss_part);
+        k_raster_fwd<2><<<grid, kRasterThreads, 0, st>>>(rec, ck, tile_vals, O, W, H, px, fs, target, ch_w,
+                                                        loss_part);
     else
-        k_raster_fwd<1><<<grid, kRasterThreads, 0, st>>>(rec, ranges, tile_vals, O, W, H, px, target, ch_w, loss_part);
+        k_raster_fwd<1><<<grid, kRasterThreads, 0, st>>>(rec, ck, tile_vals, O, W, H, px, fs, target, ch_w,
+                                                        loss_part);
 }
 
 void launch_fixup_loss(const PixK& px, int W, int H, int nf, const float* target, const float* ch_w,
@@ -414,16 +470,16 @@ void launch_fixup_loss(const PixK& px, int W, int H, int nf, const float* target
     k_fixup_loss<<<64, 256, 0, st>>>(px, W, H, nf, target, ch_w, loss_extra);
 }
 
-void launch_raster_bwd(const RecK& rec, const uint2* ranges, const uint32_t* tile_vals, const OptK& O, int W,
-                       int H, int nf, const float* dpsi, PixK px, const float* d_quad, float* screen, int scap,
-                       double* bg_part, cudaStream_t st) {
+void launch_raster_bwd(const RecK& rec, const uint4* ranges_all, int nchunks, const uint32_t* tile_vals,
+                       const OptK& O, int W, int H, int nf, const float* dpsi, PixK px, const float* d_quad,
+                       float* screen, int scap, double* bg_part, cudaStream_t st) {
     const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
     if (nf > 1)
-        k_raster_bwd<2><<<grid, kRasterThreads, 0, st>>>(rec, ranges, tile_vals, O, W, H, dpsi[0], dpsi[1], px,
-                                                        d_quad, screen, scap, bg_part);
+        k_raster_bwd<2><<<grid, kRasterThreads, 0, st>>>(rec, ranges_all, nchunks, tile_vals, O, W, H, dpsi[0],
+                                                        dpsi[1], px, d_quad, screen, scap, bg_part);
     else
-        k_raster_bwd<1><<<grid, kRasterThreads, 0, st>>>(rec, ranges, tile_vals, O, W, H, dpsi[0], 0.f, px,
-                                                        d_quad, screen, scap, bg_part);
+        k_raster_bwd<1><<<grid, kRasterThreads, 0, st>>>(rec, ranges_all, nchunks, tile_vals, O, W, H, dpsi[0],
+                                                        0.f, px, d_quad, screen, scap, bg_part);
 }
 
 __global__ void k_reduce_partials(const double* __restrict__ part, int nparts, int width,

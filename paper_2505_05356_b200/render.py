@@ -83,7 +83,9 @@ class RenderOptions:
     coverage_eps: float = 1e-12
     tile_size: int = 16
     bg_quad: Sequence[float] = (0.0, 0.0, 0.0, 0.0)
-    counts: bool = False  # also emit per-pixel n_contrib / n_processed (parity diagnostics)
+    counts: bool = False      # also emit per-pixel n_contrib / n_processed (parity diagnostics)
+    full_lists: bool = False  # bin every tile's complete list (parity); default stops binning a tile
+                              # once all its pixels have terminated (identical outputs)
 
     def to_abi(self) -> _abi.RenderOptions:
         o = _abi.RenderOptions()
@@ -94,7 +96,7 @@ class RenderOptions:
         o.coverage_eps = float(self.coverage_eps)
         o.tile_size = int(self.tile_size)
         o.channels = _abi.CH_QUAD | _abi.CH_DEPTH | _abi.CH_WEIGHT | _abi.CH_TRANSM | (
-            _abi.CH_COUNTS if self.counts else 0)
+            _abi.CH_COUNTS if self.counts else 0) | (_abi.CH_FULL_LISTS if self.full_lists else 0)
         bq = np.zeros(8)
         b = np.asarray(self.bg_quad, dtype=np.float64).reshape(-1)[:8]
         bq[: b.size] = b

@@ -75,7 +75,7 @@ def check_images(out, ref, nf=1, f=0):
 def test_c0_forward_full(tsb, ctx):
     from paper_2505_05356_b200 import synthetic
     cfg = synthetic.config("c0")
-    opts = tsb.RenderOptions(counts=True)
+    opts = tsb.RenderOptions(counts=True, full_lists=True)
     _, rp, out, op, ref = render_both(tsb, ctx, cfg.scene, cfg.camera, cfg.tof, cfg.frames[0], opts)
     check_integers(rp, op, out, ref)
     check_images(out, ref)
@@ -93,10 +93,35 @@ def test_tile_size_invariance_and_lists(tsb, ctx, tile_size):
     from paper_2505_05356_b200 import synthetic
     g = synthetic.gaussians(3000, 5, n_keyframes=2)
     cam = synthetic.camera(200, 150, 180.0)
-    opts = tsb.RenderOptions(tile_size=tile_size, counts=True, bg_quad=(0.3, 0.1, -0.2, 0.4))
+    opts = tsb.RenderOptions(tile_size=tile_size, counts=True, full_lists=True, bg_quad=(0.3, 0.1, -0.2, 0.4))
     _, rp, out, op, ref = render_both(tsb, ctx, g, cam, synthetic.ToFConfig(30e6), (0, 0.25), opts)
     check_integers(rp, op, out, ref)
     check_images(out, ref)
+
+
+@pytest.mark.parametrize("name,n", [("c0", None), ("c1", None), ("c3", 300_000)])
+def test_early_termination_is_bit_identical(tsb, ctx, name, n):
+    """Binning stops for tiles whose pixels have all terminated; every output bit and
+    count must equal the full-list render (and the oracle's integers)."""
+    from paper_2505_05356_b200 import synthetic
+    cfg = synthetic.config(name, n)
+    cam = cfg.camera
+    scene = gpu_scene(tsb, ctx, cfg.scene, cfg.tof)
+    full = tsb.RenderPass(ctx).prepare(scene, cam, tsb.RenderOptions(counts=True, full_lists=True),
+                                       cfg.frames[0]).forward()
+    lazy = tsb.RenderPass(ctx).prepare(scene, cam, tsb.RenderOptions(counts=True), cfg.frames[0]).forward()
+    a, b = full.outputs(), lazy.outputs()
+    for k in a:
+        assert np.array_equal(a[k], b[k], equal_nan=True), k
+    assert lazy.num_keys() <= full.num_keys()
+    op = orc.OraclePass(oracle_scene(cfg.scene, cfg.frames[0], cfg.tof), cam, tsb.RenderOptions())
+    assert full.num_keys() == op.num_keys()
+    ref = op.forward()
+    assert np.array_equal(b["n_contrib"], ref["n_contrib"])
+    assert np.array_equal(b["n_processed"], ref["n_processed"])
+    goff, gids = full.debug_tiles()
+    ooff, oids = op.tile_lists()
+    assert np.array_equal(goff, ooff) and np.array_equal(gids, oids)
 
 
 def test_empty_scene_background(tsb, ctx):
