@@ -133,7 +133,9 @@ struct tsb_pass {
     uint32_t vals_cap = 0;     // list entries
     int chunk_cap = 0;         // chunks x tiles of ranges
     // per Gaussian
-    uint64_t *key_a = nullptr, *key_b = nullptr;
+    uint32_t *key_a = nullptr, *key_b = nullptr;  // fp32 depth keys
+    double* depth64 = nullptr;
+    uint64_t *k64_a = nullptr, *k64_b = nullptr;  // exact fallback (long equal-key runs)
     uint32_t *gidx_a = nullptr, *gidx_b = nullptr;
     uint32_t* touched = nullptr;
     uint2* rect = nullptr;
@@ -159,7 +161,7 @@ struct tsb_pass {
     float* st_f = nullptr;
     int32_t* st_i = nullptr;
     // misc
-    int32_t* counters = nullptr;  // [0] n_visible, [1] n_flagged, [2] overflow, [3] blocks done
+    int32_t* counters = nullptr;  // [0] n_visible, [1] n_flagged, [2] overflow, [3] blocks done, [4] long tie run
     uint32_t* list_off = nullptr;
     double* loss_part = nullptr;
     double* bg_part = nullptr;
@@ -461,7 +463,7 @@ int tsb_pass_create(tsb_ctx* ctx, tsb_pass** out) {
     tsb_pass* p = new tsb_pass();
     p->ctx = ctx;
     int rc;
-    if ((rc = dev_alloc(&p->counters, 4)) || (rc = dev_alloc(&p->loss_dev, 1)) || (rc = dev_alloc(&p->chw, 8)) ||
+    if ((rc = dev_alloc(&p->counters, 8)) || (rc = dev_alloc(&p->loss_dev, 1)) || (rc = dev_alloc(&p->chw, 8)) ||
         (rc = dev_alloc(&p->list_off, 1))) {
         tsb_pass_destroy(p);
         return rc;
@@ -476,6 +478,7 @@ constexpr int kChunk0Segments = 65536 / kSeg;  // first depth chunk: 64K ranks, 
 
 void free_gauss(tsb_pass* p) {
     dev_free(p->key_a); dev_free(p->key_b); dev_free(p->gidx_a); dev_free(p->gidx_b);
+    dev_free(p->depth64); dev_free(p->k64_a); dev_free(p->k64_b);
     dev_free(p->touched); dev_free(p->rect);
     dev_free(p->rec.A); dev_free(p->rec.B); dev_free(p->rec.C); dev_free(p->rec.D); dev_free(p->screen);
 }
@@ -491,6 +494,7 @@ int ensure_gauss(tsb_pass* p, int n) {
     const int cap = std::max(n, 1);
     int rc;
     if ((rc = dev_alloc(&p->key_a, cap)) || (rc = dev_alloc(&p->key_b, cap)) || (rc = dev_alloc(&p->gidx_a, cap)) ||
+        (rc = dev_alloc(&p->depth64, cap)) ||
         (rc = dev_alloc(&p->gidx_b, cap)) || (rc = dev_alloc(&p->touched, cap)) || (rc = dev_alloc(&p->rect, cap)) ||
         (rc = dev_alloc(&p->rec.A, cap)) || (rc = dev_alloc(&p->rec.B, cap)) || (rc = dev_alloc(&p->rec.C, cap)) ||
         (rc = dev_alloc(&p->rec.D, cap)) || (rc = dev_alloc(&p->screen, (size_t)8 * cap)))
@@ -711,16 +715,18 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
         return rc;
 
     const SceneK S = scenek(s);
-    TSB_CUDA(cudaMemsetAsync(p->counters, 0, sizeof(int32_t) * 4, st));
+    TSB_CUDA(cudaMemsetAsync(p->counters, 0, sizeof(int32_t) * 8, st));
     {
         Stage sg(p->ctx, TSB_STAGE_PREPROCESS);
-        launch_preprocess(S, C, O, p->frame, p->key_a, p->gidx_a, p->touched, p->rect, p->rec, p->counters, st);
+        launch_preprocess(S, C, O, p->frame, p->key_a, p->depth64, p->gidx_a, p->touched, p->rect, p->rec,
+                          p->counters, st);
     }
     {
         Stage sg(p->ctx, TSB_STAGE_DEPTH_SORT);
-        launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, n, p->temp, p->temp_bytes, st);
+        launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, p->depth64, p->counters, p->counters + 4, n,
+                          p->temp, p->temp_bytes, st);
     }
-    p->ctx->launches += 1;
+    p->ctx->launches += 2;
     TSB_CHECK_LAUNCH();
     p->V = -1;
     p->nchunks = 0;
@@ -818,18 +824,31 @@ int run_forward(tsb_pass* p, const float* target, bool loss) {
             nch = c + 1;
             if (c + 1 >= total_chunks) break;
             // continue only while some tile is unfinished and visible ranks remain
-            TSB_CUDA(cudaMemcpyAsync(hc, p->counters, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, st));
+            TSB_CUDA(cudaMemcpyAsync(hc, p->counters, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost, st));
             TSB_CUDA(cudaStreamSynchronize(st));
             p->V = hc[0];
-            if (hc[2]) break;  // overflow: retry below
+            if (hc[2] || hc[4]) break;  // overflow / long tie run: retry below
             if (ck.chunk_end_rank >= hc[0]) break;
             if (!full && hc[3] >= p->nblocks) break;
         }
-        TSB_CUDA(cudaMemcpyAsync(hc, p->counters, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, st));
+        TSB_CUDA(cudaMemcpyAsync(hc, p->counters, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost, st));
         uint32_t* hl = (uint32_t*)(hc + 8);
         TSB_CUDA(cudaMemcpyAsync(hl, p->list_off, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         TSB_CUDA(cudaStreamSynchronize(st));
         p->V = hc[0];
+        if (hc[4]) {  // an equal-fp32-key run too long for k_fix_ties: exact 64-bit sort, redo the frame
+            const int nn = p->scene->d.n;
+            if (!p->k64_a) {
+                int rc = dev_alloc(&p->k64_a, (size_t)p->n_cap);
+                if (!rc) rc = dev_alloc(&p->k64_b, (size_t)p->n_cap);
+                if (rc) return rc;
+            }
+            launch_sort_depth64(p->depth64, p->key_a, p->k64_a, p->k64_b, p->gidx_a, p->gidx_b, nn, p->temp,
+                                p->temp_bytes, st);
+            TSB_CUDA(cudaMemsetAsync(p->counters + 4, 0, sizeof(int32_t), st));
+            p->ctx->launches += 1;
+            continue;
+        }
         if (hc[2]) {  // list storage overflow: grow and redo the frame
             int rc = ensure_vals(p, (uint64_t)p->vals_cap * 2 + (uint64_t)hl[0]);
             if (rc) return rc;

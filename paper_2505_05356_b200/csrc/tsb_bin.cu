@@ -28,16 +28,77 @@
 namespace tsb {
 
 size_t depth_sort_temp_bytes(int n) {
-    size_t a = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, a, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
+    size_t a = 0, b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, n > 0 ? n : 1, 0, 32);
+    cub::DeviceRadixSort::SortPairs(nullptr, b, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
                                     (uint32_t*)nullptr, n > 0 ? n : 1, 0, 64);
-    return a;
+    return a > b ? a : b;
 }
 
-void launch_sort_depth(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n,
-                       void* temp, size_t temp_bytes, cudaStream_t st) {
+constexpr int kMaxTieRun = 64;
+
+// Re-sort each run of equal fp32 keys by (fp64 depth, index) -- the reference's
+// comparator (splat.cpp:181-184).  One thread per run start; runs are short
+// (fp32 spacing ~1e-7 relative), insertion sort in local memory.
+__global__ void k_fix_ties(const uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                           const double* __restrict__ depth64, const int32_t* __restrict__ n_visible,
+                           int32_t* __restrict__ long_run) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int V = *n_visible;
+    if (r >= V - 1) return;
+    const uint32_t k = keys[r];
+    if (keys[r + 1] != k || (r > 0 && keys[r - 1] == k)) return;  // not the start of a run (>= 2)
+    int L = 2;
+    while (r + L < V && keys[r + L] == k) ++L;
+    if (L > kMaxTieRun) {
+        *long_run = 1;
+        return;
+    }
+    uint32_t g[kMaxTieRun];
+    double d[kMaxTieRun];
+    for (int i = 0; i < L; ++i) {
+        g[i] = vals[r + i];
+        d[i] = depth64[g[i]];
+    }
+    for (int i = 1; i < L; ++i) {
+        const uint32_t gi = g[i];
+        const double di = d[i];
+        int j = i - 1;
+        while (j >= 0 && (d[j] > di || (d[j] == di && g[j] > gi))) {
+            g[j + 1] = g[j];
+            d[j + 1] = d[j];
+            --j;
+        }
+        g[j + 1] = gi;
+        d[j + 1] = di;
+    }
+    for (int i = 0; i < L; ++i) vals[r + i] = g[i];
+}
+
+void launch_sort_depth(uint32_t* keys_in, uint32_t* keys_out, uint32_t* vals_in, uint32_t* vals_out,
+                       const double* depth64, const int32_t* n_visible, int32_t* long_run, int n, void* temp,
+                       size_t temp_bytes, cudaStream_t st) {
     if (n <= 0) return;
-    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, n, 0, 64, st);
+    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, n, 0, 32, st);
+    k_fix_ties<<<(n + 255) / 256, 256, 0, st>>>(keys_out, vals_out, depth64, n_visible, long_run);
+}
+
+__global__ void k_key64(const double* __restrict__ depth64, const uint32_t* __restrict__ key32,
+                        uint64_t* __restrict__ k64, uint32_t* __restrict__ vals, int n) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    k64[g] = key32[g] == 0xffffffffu ? ~0ull : (uint64_t)__double_as_longlong(depth64[g]);
+    vals[g] = (uint32_t)g;
+}
+
+// Exact fallback: 64-bit fp64 depth keys (8 radix passes).
+void launch_sort_depth64(const double* depth64, const uint32_t* key32, uint64_t* k64_a, uint64_t* k64_b,
+                         uint32_t* vals_in, uint32_t* vals_out, int n, void* temp, size_t temp_bytes,
+                         cudaStream_t st) {
+    if (n <= 0) return;
+    k_key64<<<(n + 255) / 256, 256, 0, st>>>(depth64, key32, k64_a, vals_in, n);
+    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k64_a, k64_b, vals_in, vals_out, n, 0, 64, st);
 }
 
 // ---------------------------------------------------------------------------

@@ -14,7 +14,8 @@ namespace tsb {
 // into rank order).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, FrameK F,
-                                                    uint64_t* __restrict__ depth_key,
+                                                    uint32_t* __restrict__ depth_key,
+                                                    double* __restrict__ depth64,
                                                     uint32_t* __restrict__ gidx,
                                                     uint32_t* __restrict__ touched,
                                                     uint2* __restrict__ rect, RecK rec,
@@ -26,7 +27,10 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, Fr
         vis = prep64(S, C, O, F, gi, s);
         gidx[gi] = (uint32_t)gi;
         if (vis) {
-            depth_key[gi] = (uint64_t)__double_as_longlong(s.depth);
+            // fp32 rounding is monotone, so this 32-bit key orders like the fp64
+            // depth except inside runs of equal keys (resolved by k_fix_ties).
+            depth_key[gi] = __float_as_uint((float)s.depth);
+            depth64[gi] = s.depth;
             const int ts = O.ts;
             const int tx0 = s.x0 / ts, tx1 = (s.x1 - 1) / ts;
             const int ty0 = s.y0 / ts, ty1 = (s.y1 - 1) / ts;
@@ -48,7 +52,7 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, Fr
                 rec.D[gi] = make_float4((float)sn, (float)cs, 0.f, 0.f);
             }
         } else {
-            depth_key[gi] = ~0ull;
+            depth_key[gi] = 0xffffffffu;
             touched[gi] = 0u;
         }
     }
@@ -57,11 +61,11 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, Fr
 }
 
 void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
-                       uint64_t* depth_key, uint32_t* gidx, uint32_t* touched, uint2* rect, RecK rec,
-                       int32_t* n_visible, cudaStream_t st) {
+                       uint32_t* depth_key, double* depth64, uint32_t* gidx, uint32_t* touched, uint2* rect,
+                       RecK rec, int32_t* n_visible, cudaStream_t st) {
     if (S.n <= 0) return;
     const int bs = 256;
-    k_preprocess<<<(S.n + bs - 1) / bs, bs, 0, st>>>(S, C, O, F, depth_key, gidx, touched, rect, rec,
+    k_preprocess<<<(S.n + bs - 1) / bs, bs, 0, st>>>(S, C, O, F, depth_key, depth64, gidx, touched, rect, rec,
                                                       n_visible);
 }
 

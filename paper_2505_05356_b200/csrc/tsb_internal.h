@@ -119,8 +119,8 @@ __host__ __device__ inline int ch_T(int nf) { return 4 * nf + 3; }
 // ---- launchers (defined in the .cu files) ----
 // tsb_geom.cu (fp64, compiled without FMA contraction)
 void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
-                       uint64_t* depth_key, uint32_t* gidx, uint32_t* touched, uint2* rect, RecK rec,
-                       int32_t* n_visible, cudaStream_t st);
+                       uint32_t* depth_key, double* depth64, uint32_t* gidx, uint32_t* touched, uint2* rect,
+                       RecK rec, int32_t* n_visible, cudaStream_t st);
 struct FixupK {
     const uint4* ranges_all;  // [nchunks][ntiles] (start, len, cum, skipped)
     int nchunks;
@@ -138,8 +138,15 @@ void launch_chain(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F
                   const uint32_t* touched, float* screen, float4* grads, cudaStream_t st);
 // tsb_bin.cu
 size_t depth_sort_temp_bytes(int n);
-void launch_sort_depth(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, uint32_t* vals_out,
-                       int n, void* temp, size_t temp_bytes, cudaStream_t st);
+// Global (depth, index) order: stable sort on fp32 depth keys, then exact fp64
+// re-sort of equal-key runs (runs longer than kMaxTieRun set *long_run; the host
+// then falls back to launch_sort_depth64).
+void launch_sort_depth(uint32_t* keys_in, uint32_t* keys_out, uint32_t* vals_in, uint32_t* vals_out,
+                       const double* depth64, const int32_t* n_visible, int32_t* long_run, int n, void* temp,
+                       size_t temp_bytes, cudaStream_t st);
+void launch_sort_depth64(const double* depth64, const uint32_t* key32, uint64_t* k64_a, uint64_t* k64_b,
+                         uint32_t* vals_in, uint32_t* vals_out, int n, void* temp, size_t temp_bytes,
+                         cudaStream_t st);
 void launch_bin_chunk(const BinK& B, cudaStream_t st);
 // tsb_raster.cu
 void launch_raster_fwd(const RecK& rec, const ChunkK& ck, const uint32_t* tile_vals, const OptK& O,

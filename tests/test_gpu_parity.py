@@ -297,3 +297,24 @@ def test_two_frequency_step(tsb, ctx):
     cfg = synthetic.config("c2", n=20_000)
     cam = synthetic.camera(320, 288, 262.5, 160, 144)
     _train_step_compare(tsb, ctx, cfg, cam)
+
+
+@pytest.mark.parametrize("run", [8, 200])
+def test_depth_ties_match_reference_order(tsb, ctx, run):
+    """splat.cpp:181-184: (depth, index) order.  Gaussians whose fp64 depths differ by less
+    than an fp32 ulp (and exact duplicates) must still come out in the reference order,
+    through the in-kernel tie re-sort (short runs) and the exact 64-bit fallback (long runs)."""
+    from paper_2505_05356_b200 import synthetic
+    rng = np.random.default_rng(3)
+    g = synthetic.gaussians(2000, 9)
+    pos = g.position.copy()
+    base = np.array([0.1, -0.05, 2.5], np.float32)
+    for i in range(run):  # same fp32 depth bucket, tiny fp64 differences, some exact duplicates
+        j = 7 * i + 3
+        pos[j] = base
+        pos[j, 0] = np.float32(base[0] + (i % 5) * 1e-7)
+    g.position = pos
+    cam = synthetic.camera(160, 120, 150.0)
+    opts = tsb.RenderOptions(counts=True, full_lists=True)
+    _, rp, out, op, ref = render_both(tsb, ctx, g, cam, tsb.ToFConfig(), (0, 0.0), opts)
+    check_integers(rp, op, out, ref)
