@@ -146,6 +146,7 @@ struct tsb_pass {
     int nchunks = 0;                          // chunks binned by the last forward
     uint32_t* hist = nullptr;
     uint32_t* tile_len = nullptr;
+    uint32_t* tile_start = nullptr;
     uint4* ranges_all = nullptr;  // [chunk_cap][ntiles]
     int* chunk_rank0 = nullptr;   // device [chunk_cap]
     uint32_t* vals = nullptr;
@@ -533,11 +534,14 @@ int ensure_pixels(tsb_pass* p, int W, int H, int ntiles, int nblocks) {
     }
     if (ntiles > p->tiles_cap) {
         dev_free(p->tile_len);
+        dev_free(p->tile_start);
         dev_free(p->tile_blocks_done);
         dev_free(p->ranges_all);
         p->chunk_cap = 0;
         int rc;
-        if ((rc = dev_alloc(&p->tile_len, ntiles)) || (rc = dev_alloc(&p->tile_blocks_done, ntiles))) return rc;
+        if ((rc = dev_alloc(&p->tile_len, ntiles)) || (rc = dev_alloc(&p->tile_start, ntiles)) ||
+            (rc = dev_alloc(&p->tile_blocks_done, ntiles)))
+            return rc;
         p->tiles_cap = ntiles;
     }
     return TSB_OK;
@@ -639,7 +643,7 @@ void tsb_pass_destroy(tsb_pass* p) {
     cudaStreamSynchronize(p->ctx->stream);
     free_gauss(p);
     free_pixels(p);
-    dev_free(p->hist); dev_free(p->tile_len); dev_free(p->ranges_all); dev_free(p->chunk_rank0);
+    dev_free(p->hist); dev_free(p->tile_len); dev_free(p->tile_start); dev_free(p->ranges_all); dev_free(p->chunk_rank0);
     dev_free(p->vals); dev_free(p->block_done); dev_free(p->tile_blocks_done);
     dev_free(p->counters); dev_free(p->list_off);
     dev_free(p->loss_part); dev_free(p->bg_part); dev_free(p->loss_dev); dev_free(p->chw); dev_free(p->temp);
@@ -784,6 +788,7 @@ int run_forward(tsb_pass* p, const float* target, bool loss) {
         B.skip_done = full ? 0 : 1;
         B.hist = p->hist;
         B.tile_len = p->tile_len;
+        B.tile_start = p->tile_start;
         B.vals = p->vals;
         B.list_off = p->list_off;
         B.capacity = p->vals_cap;

@@ -104,8 +104,8 @@ void launch_sort_depth64(const double* depth64, const uint32_t* key32, uint64_t*
 // ---------------------------------------------------------------------------
 namespace {
 
-constexpr int kWarpsPerCta = 4;
-constexpr int kSmemTiles = 4096;  // per-warp shared-memory tile counters up to this many tiles
+constexpr int kBinThreads = 128;  // one CTA per segment; all threads share a batch's tiles
+constexpr int kSmemTiles = 8192;  // per-CTA shared-memory tile counters up to this many tiles
 
 __device__ __forceinline__ bool tile_done(const BinK& B, int t) {
     return B.skip_done && B.tile_blocks_done[t] >= B.blocks_per_tile;
@@ -115,10 +115,11 @@ struct Box {
     int x0, x1, y0, y1;  // union of the batch's tile rects (inclusive); empty when x0 > x1
 };
 
-// Load the 32 ranks of one batch and build the per-column / per-row lane masks:
-// lane j covers tile (tx, ty) iff bit j of colmask[tx] & rowmask[ty].
-__device__ __forceinline__ Box load_batch(const BinK& B, int r, int V, uint32_t* colmask, uint32_t* rowmask,
-                                          uint32_t* gids, int lane) {
+// Warp 0 loads the 32 ranks of one batch and builds the per-column / per-row
+// lane masks: lane j covers tile (tx, ty) iff bit j of colmask[tx] & rowmask[ty].
+// Returns the union box (valid in every thread after the caller's barrier).
+__device__ __forceinline__ void load_batch_warp0(const BinK& B, int r, int V, uint32_t* colmask, uint32_t* rowmask,
+                                                 uint32_t* gids, int* box, int lane) {
     int tx0 = 1, tx1 = 0, ty0 = 1, ty1 = 0;
     uint32_t g = 0;
     if (r < V) {
@@ -132,84 +133,89 @@ __device__ __forceinline__ Box load_batch(const BinK& B, int r, int V, uint32_t*
     }
     gids[lane] = g;
     const bool valid = tx0 <= tx1;
-    Box u;
-    u.x0 = __reduce_min_sync(0xffffffffu, valid ? tx0 : 0x7fffffff);
-    u.x1 = __reduce_max_sync(0xffffffffu, valid ? tx1 : -1);
-    u.y0 = __reduce_min_sync(0xffffffffu, valid ? ty0 : 0x7fffffff);
-    u.y1 = __reduce_max_sync(0xffffffffu, valid ? ty1 : -1);
-    for (int tx = u.x0; tx <= u.x1; ++tx) {
+    const int ux0 = __reduce_min_sync(0xffffffffu, valid ? tx0 : 0x7fffffff);
+    const int ux1 = __reduce_max_sync(0xffffffffu, valid ? tx1 : -1);
+    const int uy0 = __reduce_min_sync(0xffffffffu, valid ? ty0 : 0x7fffffff);
+    const int uy1 = __reduce_max_sync(0xffffffffu, valid ? ty1 : -1);
+    for (int tx = ux0; tx <= ux1; ++tx) {
         const uint32_t m = __ballot_sync(0xffffffffu, valid && tx0 <= tx && tx <= tx1);
         if (lane == 0) colmask[tx] = m;
     }
-    for (int ty = u.y0; ty <= u.y1; ++ty) {
+    for (int ty = uy0; ty <= uy1; ++ty) {
         const uint32_t m = __ballot_sync(0xffffffffu, valid && ty0 <= ty && ty <= ty1);
         if (lane == 0) rowmask[ty] = m;
     }
-    __syncwarp();
-    return u;
+    if (lane == 0) {
+        box[0] = ux0;
+        box[1] = ux1;
+        box[2] = uy0;
+        box[3] = uy1;
+    }
 }
 
 }  // namespace
 
-// Per (segment, tile) entry counts of one depth chunk.  One warp per segment of
-// kSeg ranks; per batch of 32 ranks the lanes walk the tiles of the batch's
-// union box (no per-pair work: the number of coverers is popc of two masks).
+// Per (segment, tile) entry counts of one depth chunk.  One CTA per segment of
+// kSeg ranks; per batch of 32 ranks the threads walk the tiles of the batch's
+// union box (the number of coverers of a tile is popc of two masks).
 template <bool SMEM>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_bin_count(BinK B) {
+__global__ void __launch_bounds__(kBinThreads) k_bin_count(BinK B) {
     extern __shared__ uint32_t smem[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int segl = blockIdx.x * kWarpsPerCta + wib;
-    if (segl >= B.nseg) return;
-    const int per_warp = 32 + B.tiles_x + B.tiles_y + (SMEM ? B.ntiles : 0);
-    uint32_t* gids = smem + wib * per_warp;
+    __shared__ int box[4];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int segl = blockIdx.x;
+    uint32_t* gids = smem;
     uint32_t* colmask = gids + 32;
     uint32_t* rowmask = colmask + B.tiles_x;
     uint32_t* cnt = SMEM ? rowmask + B.tiles_y : B.hist + (size_t)segl * B.ntiles;
     const int V = *B.n_visible;
     const int r0 = (B.seg0 + segl) * kSeg;
-    for (int t = lane; t < B.ntiles; t += 32) cnt[t] = 0u;
-    __syncwarp();
+    for (int t = tid; t < B.ntiles; t += kBinThreads) cnt[t] = 0u;
+    __syncthreads();
     if (r0 < V) {
-        for (int b = 0; b < kSeg; b += 32) {
-            const Box u = load_batch(B, r0 + b + lane, V, colmask, rowmask, gids, lane);
-            const int bw = u.x1 - u.x0 + 1;
-            const int area = bw > 0 ? bw * (u.y1 - u.y0 + 1) : 0;
-            for (int i = lane; i < area; i += 32) {
-                const int ty = u.y0 + i / bw, tx = u.x0 + i % bw;
+        for (int b = 0; b < kSeg && r0 + b < V; b += 32) {
+            if (tid < 32) load_batch_warp0(B, r0 + b + lane, V, colmask, rowmask, gids, box, lane);
+            __syncthreads();
+            const int bw = box[1] - box[0] + 1;
+            const int area = bw > 0 ? bw * (box[3] - box[2] + 1) : 0;
+            for (int i = tid; i < area; i += kBinThreads) {
+                const int q = i / bw;
+                const int ty = box[2] + q, tx = box[0] + (i - q * bw);
                 const uint32_t m = colmask[tx] & rowmask[ty];
                 if (m) {
                     const int t = ty * B.tiles_x + tx;
                     if (!tile_done(B, t)) cnt[t] += (uint32_t)__popc(m);
                 }
             }
-            __syncwarp();
+            __syncthreads();
         }
     }
     if (SMEM) {
-        __syncwarp();
         uint32_t* h = B.hist + (size_t)segl * B.ntiles;
-        for (int t = lane; t < B.ntiles; t += 32) h[t] = cnt[t];
+        for (int t = tid; t < B.ntiles; t += kBinThreads) h[t] = cnt[t];
     }
 }
 
 // Per tile: exclusive scan over the chunk's segments (in place, segment-major
-// layout) and the tile's length.  Block = 32 tiles x 8 warps; warp w owns a
+// layout) and the tile's length.  Block = 32 tiles x 32 warps; warp w owns a
 // contiguous range of segments.
-__global__ void __launch_bounds__(256) k_bin_scan_segments(BinK B) {
-    __shared__ uint32_t part[8][32];
+__global__ void __launch_bounds__(1024) k_bin_scan_segments(BinK B) {
+    __shared__ uint32_t part[32][33];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int t = blockIdx.x * 32 + lane;
-    const int per = (B.nseg + 7) / 8;
+    const int per = (B.nseg + 31) / 32;
     const int s0 = w * per, s1 = min(B.nseg, s0 + per);
     uint32_t sum = 0;
-    if (t < B.ntiles)
+    if (t < B.ntiles) {
+#pragma unroll 4
         for (int s = s0; s < s1; ++s) sum += B.hist[(size_t)s * B.ntiles + t];
+    }
     part[w][lane] = sum;
     __syncthreads();
     uint32_t off = 0, tot = 0;
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 32; ++i) {
         const uint32_t v = part[i][lane];
-        if (i < w) off += v;
+        off += i < w ? v : 0u;
         tot += v;
     }
     if (t < B.ntiles) {
@@ -258,6 +264,7 @@ __global__ void k_bin_scan_tiles(BinK B) {
             const uint32_t cum = B.chunk == 0 ? 0u : B.prev_ranges[t].z + B.prev_ranges[t].y;
             const uint32_t skipped = (B.skip_done && B.tile_blocks_done[t] >= B.blocks_per_tile) ? 1u : 0u;
             B.ranges[t] = make_uint4(start, v, cum, skipped);
+            B.tile_start[t] = start;
         }
         __syncthreads();
         if (tid == blockDim.x - 1) s_carry = carry + warp_sums[wid] + inc;
@@ -270,33 +277,34 @@ __global__ void k_bin_scan_tiles(BinK B) {
     }
 }
 
-// Stable scatter of one depth chunk.  Lanes walk the batch's union tiles; the
+// Stable scatter of one depth chunk.  Threads walk the batch's union tiles; the
 // coverers of tile t (bits of colmask & rowmask, in rank order) are written as
 // one contiguous run at the (segment, tile) cursor, which then advances.
 template <bool SMEM>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_bin_emit(BinK B) {
+__global__ void __launch_bounds__(kBinThreads) k_bin_emit(BinK B) {
     extern __shared__ uint32_t smem[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int segl = blockIdx.x * kWarpsPerCta + wib;
-    if (segl >= B.nseg) return;
+    __shared__ int box[4];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int segl = blockIdx.x;
     if (*B.overflow) return;
     const int V = *B.n_visible;
     const int r0 = (B.seg0 + segl) * kSeg;
     if (r0 >= V) return;
-    const int per_warp = 32 + B.tiles_x + B.tiles_y + (SMEM ? B.ntiles : 0);
-    uint32_t* gids = smem + wib * per_warp;
+    uint32_t* gids = smem;
     uint32_t* colmask = gids + 32;
     uint32_t* rowmask = colmask + B.tiles_x;
     uint32_t* h = B.hist + (size_t)segl * B.ntiles;
     uint32_t* cur = SMEM ? rowmask + B.tiles_y : h;
-    for (int t = lane; t < B.ntiles; t += 32) cur[t] = B.ranges[t].x + h[t];
-    __syncwarp();
-    for (int b = 0; b < kSeg; b += 32) {
-        const Box u = load_batch(B, r0 + b + lane, V, colmask, rowmask, gids, lane);
-        const int bw = u.x1 - u.x0 + 1;
-        const int area = bw > 0 ? bw * (u.y1 - u.y0 + 1) : 0;
-        for (int i = lane; i < area; i += 32) {
-            const int ty = u.y0 + i / bw, tx = u.x0 + i % bw;
+    for (int t = tid; t < B.ntiles; t += kBinThreads) cur[t] = B.tile_start[t] + h[t];
+    __syncthreads();
+    for (int b = 0; b < kSeg && r0 + b < V; b += 32) {
+        if (tid < 32) load_batch_warp0(B, r0 + b + lane, V, colmask, rowmask, gids, box, lane);
+        __syncthreads();
+        const int bw = box[1] - box[0] + 1;
+        const int area = bw > 0 ? bw * (box[3] - box[2] + 1) : 0;
+        for (int i = tid; i < area; i += kBinThreads) {
+            const int q = i / bw;
+            const int ty = box[2] + q, tx = box[0] + (i - q * bw);
             uint32_t m = colmask[tx] & rowmask[ty];
             if (!m) continue;
             const int t = ty * B.tiles_x + tx;
@@ -309,15 +317,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_bin_emit(BinK B) {
                 B.vals[c++] = gids[j];
             }
         }
-        __syncwarp();
+        __syncthreads();
     }
 }
 
 void launch_bin_chunk(const BinK& B, cudaStream_t st) {
     const bool sm = B.ntiles <= kSmemTiles;
-    const size_t smem =
-        sizeof(uint32_t) * (size_t)(32 + B.tiles_x + B.tiles_y + (sm ? B.ntiles : 0)) * kWarpsPerCta;
-    const int grid = (B.nseg + kWarpsPerCta - 1) / kWarpsPerCta;
+    const size_t smem = sizeof(uint32_t) * (size_t)(32 + B.tiles_x + B.tiles_y + (sm ? B.ntiles : 0));
+    const int grid = B.nseg;
     static bool attr = false;
     if (!attr) {
         const int mx = 200 * 1024;
@@ -328,15 +335,15 @@ void launch_bin_chunk(const BinK& B, cudaStream_t st) {
         attr = true;
     }
     if (sm)
-        k_bin_count<true><<<grid, 32 * kWarpsPerCta, smem, st>>>(B);
+        k_bin_count<true><<<grid, kBinThreads, smem, st>>>(B);
     else
-        k_bin_count<false><<<grid, 32 * kWarpsPerCta, smem, st>>>(B);
-    k_bin_scan_segments<<<(B.ntiles + 31) / 32, 256, 0, st>>>(B);
+        k_bin_count<false><<<grid, kBinThreads, smem, st>>>(B);
+    k_bin_scan_segments<<<(B.ntiles + 31) / 32, 1024, 0, st>>>(B);
     k_bin_scan_tiles<<<1, 1024, 0, st>>>(B);
     if (sm)
-        k_bin_emit<true><<<grid, 32 * kWarpsPerCta, smem, st>>>(B);
+        k_bin_emit<true><<<grid, kBinThreads, smem, st>>>(B);
     else
-        k_bin_emit<false><<<grid, 32 * kWarpsPerCta, smem, st>>>(B);
+        k_bin_emit<false><<<grid, kBinThreads, smem, st>>>(B);
 }
 
 }  // namespace tsb

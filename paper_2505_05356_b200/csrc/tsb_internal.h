@@ -71,6 +71,7 @@ struct BinK {
     uint32_t* hist;                   // [nseg][ntiles] counts -> exclusive offsets within the tile
     int seg0, nseg, chunk;
     uint32_t* tile_len;               // [ntiles]
+    uint32_t* tile_start;             // [ntiles] this chunk's list start per tile
     uint4* ranges;                    // [ntiles] this chunk: (start, len, cum entries before, 0)
     const uint4* prev_ranges;         // previous chunk's ranges (chunk > 0)
     uint32_t* vals;                   // list storage (Gaussian indices)
