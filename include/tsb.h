@@ -215,6 +215,8 @@ int tsb_pass_debug_records(tsb_pass* p, float* rec12 /* 12 per rank */);
 int tsb_pass_debug_screen_grads(tsb_pass* p, float* g8 /* 8 per rank */);
 /* Pixels the fp32 raster flagged as decision-ambiguous and recomposited in fp64. */
 int tsb_pass_debug_fixups(tsb_pass* p, int32_t* count);
+/* The fixed pixels themselves: pixel index | reason << 24 (1 maha, 2 alpha, 4 T band). */
+int tsb_pass_debug_fixup_list(tsb_pass* p, int32_t* entries, int32_t capacity, int32_t* count);
 
 /* ---- data-parallel gradient reduction (trainer.cpp:123-131 -> NCCL) ----- */
 int tsb_comm_unique_id(void* out /* 128 bytes */);

@@ -101,6 +101,7 @@ SIGNATURES = {
     "tsb_pass_debug_records": (C.c_int, [_vp, _fp]),
     "tsb_pass_debug_screen_grads": (C.c_int, [_vp, _fp]),
     "tsb_pass_debug_fixups": (C.c_int, [_vp, _ip]),
+    "tsb_pass_debug_fixup_list": (C.c_int, [_vp, _ip, C.c_int32, _ip]),
     "tsb_comm_unique_id": (C.c_int, [_vp]),
     "tsb_comm_create": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.POINTER(_vp)]),
     "tsb_comm_destroy": (None, [_vp]),

@@ -511,6 +511,7 @@ int ensure_gauss(tsb_pass* p, int n) {
 int ensure_pixels(tsb_pass* p, int W, int H, int ntiles, int nblocks) {
     const int npx = W * H;
     const int nch = out_channels(2);
+    if (npx >= (1 << 24)) return fail(TSB_ERR_UNSUPPORTED, "render: more than 16M pixels");
     if (npx > p->px_cap) {
         free_pixels(p);
         int rc;
@@ -1120,6 +1121,17 @@ int tsb_pass_debug_fixups(tsb_pass* p, int32_t* count) {
     TSB_CUDA(cudaMemcpyAsync(h, p->counters + 1, 4, cudaMemcpyDeviceToHost, p->ctx->stream));
     TSB_CUDA(cudaStreamSynchronize(p->ctx->stream));
     *count = *h;
+    return TSB_OK;
+}
+
+int tsb_pass_debug_fixup_list(tsb_pass* p, int32_t* entries, int32_t capacity, int32_t* count) {
+    int32_t n = 0;
+    int rc = tsb_pass_debug_fixups(p, &n);
+    if (rc) return rc;
+    if (count) *count = n;
+    if (entries && n > 0) {
+        TSB_CUDA(cudaMemcpy(entries, p->flagged, sizeof(int32_t) * std::min(n, capacity), cudaMemcpyDeviceToHost));
+    }
     return TSB_OK;
 }
 

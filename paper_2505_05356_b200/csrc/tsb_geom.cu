@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, FrameK 
     const int V = *fx.n_visible;
     const uint32_t lanes_below = (1u << lane) - 1u;
     for (int i = warp; i < count; i += nwarps) {
-        const int pix = px.flagged[i];
+        const int pix = px.flagged[i] & 0xffffff;
         const int x = pix % W, y = pix / W;
         const int tx = x / O.ts, ty = y / O.ts;
         const int tile = ty * O.tiles_x + tx;

@@ -49,11 +49,24 @@ __device__ __forceinline__ void eval_alpha(const float4& B, Eval& e) {
     e.alpha = __fmul_rn(B.w, e.g);
 }
 
-// Error-band constants: measured fp32-vs-fp64
-// maha error is ~1e-7 relative with the factored conic; alpha ~1.5e-6 relative.
-constexpr float kBandMaha = 2.0e-5f;   // relative to cutoff^2
-constexpr float kBandAlpha = 8.0e-6f;  // relative to the threshold
-constexpr float kEpsAlpha = 2.0e-6f;   // per-contributor alpha error used in the T bound
+// Decision error bounds.  An evaluation whose maha
+// or alpha lands within a coarse window of its threshold gets a first-order bound
+// on its fp32 error (rare branch); the pixel is sent to the fp64 fix-up when the
+// decision lies inside twice that bound.
+constexpr float kEps = 5.9604645e-8f;      // 2^-24
+constexpr float kCoarseMaha = 1e-3f;       // relative window that triggers the precise bound
+constexpr float kCoarseAlpha = 1e-4f;
+constexpr float kEx2Err = 2.5e-7f;         // ex2.approx.ftz.f32 relative error bound (+ margin)
+
+// |fl32(maha) - maha_exact| bound from the rounding of mean offset, L, dx, dy, p, q.
+__device__ __forceinline__ float maha_err_bound(const float4& A, const float4& B, const Eval& e) {
+    const float ddx = kEps * (fabsf(A.z) + fabsf(e.dx));
+    const float ddy = kEps * (fabsf(A.w) + fabsf(e.dy));
+    const float a = fabsf(B.x * e.dx), b = fabsf(B.y * e.dy);
+    const float dp = kEps * (a + 2.f * b + fabsf(e.p)) + fabsf(B.x) * ddx + fabsf(B.y) * ddy;
+    const float dq = 2.f * kEps * fabsf(e.q) + fabsf(B.z) * ddy;
+    return 2.f * fabsf(e.p) * dp + 2.f * fabsf(e.q) * dq + kEps * (e.q * e.q + e.maha);
+}
 
 template <int NF>
 struct Smem {
@@ -109,10 +122,11 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
         last_eff = fs.i[2 * (size_t)fs.npx + o];
     }
     const bool was_done = !active || (flags & 1);
-    bool done = was_done, flag = (flags & 2) != 0;
+    bool done = was_done;
+    int flag = (flags >> 1) & 7;  // reasons: 1 maha band, 2 alpha band, 4 T band
     int processed = (int)(rg.z + rg.y);
     const float cut2 = O.cut2_f, thr = O.alpha_thr_f, fl = O.floor_f;
-    const float bandM = kBandMaha * cut2, bandA = kBandAlpha * thr;
+    const float coarseM = kCoarseMaha * cut2, coarseA = kCoarseAlpha * thr;
     const uint32_t end = rg.x + rg.y;
 
     if (__syncthreads_count(done) < kRasterThreads) {
@@ -133,11 +147,15 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
                     Eval ev;
                     eval_entry(A, B, pcx, pcy, ev);
                     const float dm = ev.maha - cut2;
-                    if (fabsf(dm) <= bandM) flag = true;
+                    if (fabsf(dm) <= coarseM && fabsf(dm) <= 2.f * maha_err_bound(A, B, ev)) flag |= 1;
                     if (dm > 0.f) continue;
                     eval_alpha(B, ev);
                     const float da = ev.alpha - thr;
-                    if (fabsf(da) <= bandA) flag = true;
+                    if (fabsf(da) <= coarseA) {
+                        const float rel = 3.f * kEps + kEx2Err + 0.5f * maha_err_bound(A, B, ev) +
+                                          kEps * ev.maha;
+                        if (fabsf(da) <= 2.f * ev.alpha * rel) flag |= 2;
+                    }
                     if (da < 0.f) continue;
                     ++nc;
                     const float4 Cc = sm.C[j];
@@ -156,8 +174,9 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
                     Tpre = T;
                     const float om = 1.f - ev.alpha;
                     T = T * om;
-                    errT += kEpsAlpha * __fdividef(ev.alpha, om) + 1.2e-7f;
-                    if (T < fl * (1.f + 4.f * errT) && T > fl * (1.f - 4.f * errT)) flag = true;
+                    // relative error of (1 - alpha) from alpha's error, plus the product rounding
+                    errT += (4.f * kEps + kEx2Err + 2.f * kEps * ev.maha) * __fdividef(ev.alpha, om) + 2.f * kEps;
+                    if (T < fl * (1.f + 2.f * errT) && T > fl * (1.f - 2.f * errT)) flag |= 4;
                     const int gidx_e = (int)(rg.z + (b - rg.x) + j + 1);
                     if (T == 0.f && last_eff < 0) last_eff = gidx_e;
                     if (T < fl) {
@@ -197,7 +216,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
         fs.i[1 * (size_t)fs.npx + o] = 1;  // done (read by later chunks only if the block is not done)
         if (flag) {
             const int slot = atomicAdd(px.n_flagged, 1);
-            px.flagged[slot] = (int)o;
+            px.flagged[slot] = (int)o | (flag << 24);
         } else if (target) {
             const float s2 = 2.f / (float)HW;
 #pragma unroll
@@ -219,7 +238,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
             fs.f[(6 + 2 * f) * (size_t)fs.npx + o] = accC[f];
         }
         fs.i[0 * (size_t)fs.npx + o] = nc;
-        fs.i[1 * (size_t)fs.npx + o] = flag ? 2 : 0;
+        fs.i[1 * (size_t)fs.npx + o] = flag << 1;
         fs.i[2 * (size_t)fs.npx + o] = last_eff;
     }
     const bool block_finished = __syncthreads_count(done || is_last) == kRasterThreads;
@@ -246,7 +265,7 @@ __global__ void k_fixup_loss(PixK px, int W, int H, int nf, const float* __restr
     const int count = *px.n_flagged;
     double l = 0.0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
-        const size_t HW = (size_t)W * H, o = (size_t)px.flagged[i];
+        const size_t HW = (size_t)W * H, o = (size_t)(px.flagged[i] & 0xffffff);
         const float s2 = 2.f / (float)HW;
         for (int c = 0; c < 4 * nf; ++c) {
             const float r = px.out[c * HW + o] - target[c * HW + o];

@@ -424,6 +424,15 @@ class RenderPass:
         check(lib().tsb_pass_debug_fixups(self._h, C.byref(c)))
         return c.value
 
+    def debug_fixup_list(self):
+        """(pixel index, reason bits) of the pixels recomposited in fp64."""
+        n = self.debug_fixups()
+        a = np.zeros(max(n, 1), np.int32)
+        c = C.c_int32()
+        check(lib().tsb_pass_debug_fixup_list(self._h, a.ctypes.data_as(_abi._ip), int(a.size), C.byref(c)))
+        a = a[:n]
+        return a & 0xFFFFFF, (a >> 24) & 7
+
     def close(self):
         if getattr(self, "_h", None):
             lib().tsb_pass_destroy(self._h)
