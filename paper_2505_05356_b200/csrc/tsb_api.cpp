@@ -135,7 +135,6 @@ struct tsb_pass {
     // per Gaussian
     uint32_t *key_a = nullptr, *key_b = nullptr;  // fp32 depth keys
     double* depth64 = nullptr;
-    uint64_t *k64_a = nullptr, *k64_b = nullptr;  // exact fallback (long equal-key runs)
     uint32_t *gidx_a = nullptr, *gidx_b = nullptr;
     uint32_t* touched = nullptr;
     uint2* rect = nullptr;
@@ -168,7 +167,7 @@ struct tsb_pass {
     double* bg_part = nullptr;
     double* loss_dev = nullptr;
     float* chw = nullptr;
-    void* temp = nullptr;
+    uint32_t* sort_scratch = nullptr;
 };
 
 extern "C" {
@@ -479,7 +478,7 @@ constexpr int kChunk0Segments = 65536 / kSeg;  // first depth chunk: 64K ranks, 
 
 void free_gauss(tsb_pass* p) {
     dev_free(p->key_a); dev_free(p->key_b); dev_free(p->gidx_a); dev_free(p->gidx_b);
-    dev_free(p->depth64); dev_free(p->k64_a); dev_free(p->k64_b);
+    dev_free(p->depth64); dev_free(p->sort_scratch);
     dev_free(p->touched); dev_free(p->rect);
     dev_free(p->rec.A); dev_free(p->rec.B); dev_free(p->rec.C); dev_free(p->rec.D); dev_free(p->screen);
 }
@@ -502,9 +501,7 @@ int ensure_gauss(tsb_pass* p, int n) {
         return rc;
     TSB_CUDA(cudaMemsetAsync(p->screen, 0, sizeof(float) * 8 * (size_t)cap, p->ctx->stream));
     p->n_cap = cap;
-    dev_free(p->temp);
-    p->temp_bytes = depth_sort_temp_bytes(cap);
-    TSB_CUDA(cudaMalloc(&p->temp, p->temp_bytes));
+    if ((rc = dev_alloc(&p->sort_scratch, radix_sort_scratch_words(cap)))) return rc;
     return TSB_OK;
 }
 
@@ -647,7 +644,7 @@ void tsb_pass_destroy(tsb_pass* p) {
     dev_free(p->hist); dev_free(p->tile_len); dev_free(p->tile_start); dev_free(p->ranges_all); dev_free(p->chunk_rank0);
     dev_free(p->vals); dev_free(p->block_done); dev_free(p->tile_blocks_done);
     dev_free(p->counters); dev_free(p->list_off);
-    dev_free(p->loss_part); dev_free(p->bg_part); dev_free(p->loss_dev); dev_free(p->chw); dev_free(p->temp);
+    dev_free(p->loss_part); dev_free(p->bg_part); dev_free(p->loss_dev); dev_free(p->chw);
     delete p;
 }
 
@@ -728,10 +725,10 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     }
     {
         Stage sg(p->ctx, TSB_STAGE_DEPTH_SORT);
-        launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, p->depth64, p->counters, p->counters + 4, n,
-                          p->temp, p->temp_bytes, st);
+        p->ctx->launches += launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, p->depth64, p->counters,
+                                              p->counters + 4, n, p->sort_scratch, st);
     }
-    p->ctx->launches += 2;
+    p->ctx->launches += 1;
     TSB_CHECK_LAUNCH();
     p->V = -1;
     p->nchunks = 0;
@@ -777,7 +774,7 @@ int run_forward(tsb_pass* p, const float* target, bool loss) {
         if (loss) TSB_CUDA(cudaMemsetAsync(p->loss_part, 0, sizeof(double) * p->nblocks, st));
         FwdState fs{p->st_f, p->st_i, p->W * p->H};
         BinK B{};
-        B.sorted_gidx = p->gidx_b;
+        B.sorted_gidx = p->gidx_a;
         B.rect = p->rect;
         B.n_visible = p->counters;
         B.ts = p->opt.ts;
@@ -844,15 +841,9 @@ int run_forward(tsb_pass* p, const float* target, bool loss) {
         p->V = hc[0];
         if (hc[4]) {  // an equal-fp32-key run too long for k_fix_ties: exact 64-bit sort, redo the frame
             const int nn = p->scene->d.n;
-            if (!p->k64_a) {
-                int rc = dev_alloc(&p->k64_a, (size_t)p->n_cap);
-                if (!rc) rc = dev_alloc(&p->k64_b, (size_t)p->n_cap);
-                if (rc) return rc;
-            }
-            launch_sort_depth64(p->depth64, p->key_a, p->k64_a, p->k64_b, p->gidx_a, p->gidx_b, nn, p->temp,
-                                p->temp_bytes, st);
+            p->ctx->launches += launch_sort_depth64(p->depth64, p->touched, p->key_a, p->key_b, p->gidx_a,
+                                                    p->gidx_b, nn, p->sort_scratch, st);
             TSB_CUDA(cudaMemsetAsync(p->counters + 4, 0, sizeof(int32_t), st));
-            p->ctx->launches += 1;
             continue;
         }
         if (hc[2]) {  // list storage overflow: grow and redo the frame
@@ -867,7 +858,7 @@ int run_forward(tsb_pass* p, const float* target, bool loss) {
         fx.chunk_rank0 = p->chunk_rank0;
         fx.binned_end_rank = total_chunks ? (p->chunk_seg0[nch - 1] + p->chunk_nseg[nch - 1]) * kSeg : 0;
         fx.vals = p->vals;
-        fx.sorted_gidx = p->gidx_b;
+        fx.sorted_gidx = p->gidx_a;
         fx.rect = p->rect;
         fx.n_visible = p->counters;
         fx.overflow = p->counters + 2;
@@ -1013,7 +1004,7 @@ int tsb_pass_debug_prepared(tsb_pass* p, int32_t* gidx, int32_t* rect) {
     cudaStream_t st = p->ctx->stream;
     const int V = p->V;
     std::vector<uint32_t> g(V > 0 ? V : 1);
-    if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), p->gidx_b, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, st));
+    if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), p->gidx_a, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, st));
     std::vector<uint2> r((size_t)std::max(p->scene->d.n, 1));
     if (rect && p->scene->d.n > 0)
         TSB_CUDA(cudaMemcpyAsync(r.data(), p->rect, sizeof(uint2) * p->scene->d.n, cudaMemcpyDeviceToHost, st));
@@ -1052,7 +1043,7 @@ int tsb_pass_debug_tiles(tsb_pass* p, int32_t* tiles_x, int32_t* tiles_y, int64_
     if (ids && k > 0) {
         TSB_CUDA(cudaMemcpyAsync(vals.data(), p->vals, sizeof(uint32_t) * k, cudaMemcpyDeviceToHost, st));
         if (p->V > 0)
-            TSB_CUDA(cudaMemcpyAsync(order.data(), p->gidx_b, sizeof(uint32_t) * p->V, cudaMemcpyDeviceToHost, st));
+            TSB_CUDA(cudaMemcpyAsync(order.data(), p->gidx_a, sizeof(uint32_t) * p->V, cudaMemcpyDeviceToHost, st));
         TSB_CUDA(cudaStreamSynchronize(st));
     }
     // per tile: concatenation of its chunk sub-lists (values are Gaussian indices;
@@ -1087,7 +1078,7 @@ int tsb_pass_debug_records(tsb_pass* p, float* rec12) {
         TSB_CUDA(cudaMemcpyAsync(C.data(), p->rec.C, sizeof(float4) * n, cudaMemcpyDeviceToHost, st));
         if (p->nf > 1) TSB_CUDA(cudaMemcpyAsync(D.data(), p->rec.D, sizeof(float4) * n, cudaMemcpyDeviceToHost, st));
     }
-    if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), p->gidx_b, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, st));
+    if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), p->gidx_a, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, st));
     TSB_CUDA(cudaStreamSynchronize(st));
     for (int r = 0; r < V; ++r) {
         const uint32_t i = g[r];

@@ -21,34 +21,18 @@
 //      reference list.  Tiles whose pixels have all terminated are skipped by
 //      later chunks (the composite never reads past termination), unless the
 //      caller asks for full lists (parity mode).
-#include <cub/device/device_radix_sort.cuh>
-
 #include "tsb_internal.h"
 
 namespace tsb {
-
-size_t depth_sort_temp_bytes(int n) {
-    size_t a = 0, b = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, a, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
-                                    (uint32_t*)nullptr, n > 0 ? n : 1, 0, 32);
-    cub::DeviceRadixSort::SortPairs(nullptr, b, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
-                                    (uint32_t*)nullptr, n > 0 ? n : 1, 0, 64);
-    return a > b ? a : b;
-}
 
 constexpr int kMaxTieRun = 64;
 
 // Re-sort each run of equal fp32 keys by (fp64 depth, index) -- the reference's
 // comparator (splat.cpp:181-184).  One thread per run start; runs are short
 // (fp32 spacing ~1e-7 relative), insertion sort in local memory.
-__global__ void k_fix_ties(const uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                           const double* __restrict__ depth64, const int32_t* __restrict__ n_visible,
-                           int32_t* __restrict__ long_run) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    const int V = *n_visible;
-    if (r >= V - 1) return;
+__device__ __noinline__ void sort_run(const uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                      const double* __restrict__ depth64, int r, int V, int32_t* long_run) {
     const uint32_t k = keys[r];
-    if (keys[r + 1] != k || (r > 0 && keys[r - 1] == k)) return;  // not the start of a run (>= 2)
     int L = 2;
     while (r + L < V && keys[r + L] == k) ++L;
     if (L > kMaxTieRun) {
@@ -76,29 +60,61 @@ __global__ void k_fix_ties(const uint32_t* __restrict__ keys, uint32_t* __restri
     for (int i = 0; i < L; ++i) vals[r + i] = g[i];
 }
 
-void launch_sort_depth(uint32_t* keys_in, uint32_t* keys_out, uint32_t* vals_in, uint32_t* vals_out,
-                       const double* depth64, const int32_t* n_visible, int32_t* long_run, int n, void* temp,
-                       size_t temp_bytes, cudaStream_t st) {
-    if (n <= 0) return;
-    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, n, 0, 32, st);
-    k_fix_ties<<<(n + 255) / 256, 256, 0, st>>>(keys_out, vals_out, depth64, n_visible, long_run);
+// Re-sort each run of equal fp32 keys by (fp64 depth, index) -- the reference's
+// comparator (splat.cpp:181-184).  Each thread scans 4 consecutive ranks (one
+// 16-byte load + the neighbours); run starts are rare and handled out of line.
+__global__ void k_fix_ties(const uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                           const double* __restrict__ depth64, const int32_t* __restrict__ n_visible,
+                           int32_t* __restrict__ long_run) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    const int V = *n_visible;
+    const int r0 = 4 * q;
+    if (r0 >= V - 1) return;
+    const uint4 k4 = reinterpret_cast<const uint4*>(keys)[q];
+    const uint32_t kk[6] = {r0 > 0 ? keys[r0 - 1] : ~k4.x, k4.x, k4.y, k4.z, k4.w,
+                            r0 + 4 < V ? keys[r0 + 4] : ~k4.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int r = r0 + j;
+        if (r >= V - 1) break;
+        if (kk[j + 2] == kk[j + 1] && kk[j] != kk[j + 1]) sort_run(keys, vals, depth64, r, V, long_run);
+    }
 }
 
-__global__ void k_key64(const double* __restrict__ depth64, const uint32_t* __restrict__ key32,
-                        uint64_t* __restrict__ k64, uint32_t* __restrict__ vals, int n) {
+int launch_sort_depth(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, const double* depth64,
+                      const int32_t* n_visible, int32_t* long_run, int n, uint32_t* scratch, cudaStream_t st) {
+    if (n <= 0) return 0;
+    int launches = radix_sort32(keys_a, keys_b, vals_a, vals_b, n, scratch, st);
+    k_fix_ties<<<(n / 4 + 256) / 256, 256, 0, st>>>(keys_a, vals_a, depth64, n_visible, long_run);
+    return launches + 1;
+}
+
+// Exact fallback for long equal-fp32 runs: stable LSD on the fp64 depth bits as two
+// 32-bit sorts (low word, then high word gathered through the permutation).
+__global__ void k_key_lo(const double* __restrict__ depth64, const uint32_t* __restrict__ touched,
+                         uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, int n) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
-    k64[g] = key32[g] == 0xffffffffu ? ~0ull : (uint64_t)__double_as_longlong(depth64[g]);
+    keys[g] = touched[g] ? (uint32_t)(__double_as_longlong(depth64[g]) & 0xffffffffull) : 0u;
     vals[g] = (uint32_t)g;
 }
 
-// Exact fallback: 64-bit fp64 depth keys (8 radix passes).
-void launch_sort_depth64(const double* depth64, const uint32_t* key32, uint64_t* k64_a, uint64_t* k64_b,
-                         uint32_t* vals_in, uint32_t* vals_out, int n, void* temp, size_t temp_bytes,
-                         cudaStream_t st) {
-    if (n <= 0) return;
-    k_key64<<<(n + 255) / 256, 256, 0, st>>>(depth64, key32, k64_a, vals_in, n);
-    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k64_a, k64_b, vals_in, vals_out, n, 0, 64, st);
+__global__ void k_key_hi(const double* __restrict__ depth64, const uint32_t* __restrict__ touched,
+                         uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t g = vals[i];
+    keys[i] = touched[g] ? (uint32_t)((unsigned long long)__double_as_longlong(depth64[g]) >> 32) : 0xffffffffu;
+}
+
+int launch_sort_depth64(const double* depth64, const uint32_t* touched, uint32_t* keys_a, uint32_t* keys_b,
+                        uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch, cudaStream_t st) {
+    if (n <= 0) return 0;
+    k_key_lo<<<(n + 255) / 256, 256, 0, st>>>(depth64, touched, keys_a, vals_a, n);
+    int l = radix_sort32(keys_a, keys_b, vals_a, vals_b, n, scratch, st);
+    k_key_hi<<<(n + 255) / 256, 256, 0, st>>>(depth64, touched, keys_a, vals_a, n);
+    l += radix_sort32(keys_a, keys_b, vals_a, vals_b, n, scratch, st);
+    return l + 2;
 }
 
 // ---------------------------------------------------------------------------

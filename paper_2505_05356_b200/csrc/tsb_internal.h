@@ -138,16 +138,18 @@ void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F
 void launch_chain(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
                   const uint32_t* touched, float* screen, float4* grads, cudaStream_t st);
 // tsb_bin.cu
-size_t depth_sort_temp_bytes(int n);
+// tsb_sort.cu: hand-written onesweep LSD radix sort of 32-bit keys + values (4 passes);
+// the result is back in (keys_a, vals_a).  Returns the number of kernels launched.
+size_t radix_sort_scratch_words(int n);
+int radix_sort32(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch,
+                 cudaStream_t st);
 // Global (depth, index) order: stable sort on fp32 depth keys, then exact fp64
-// re-sort of equal-key runs (runs longer than kMaxTieRun set *long_run; the host
-// then falls back to launch_sort_depth64).
-void launch_sort_depth(uint32_t* keys_in, uint32_t* keys_out, uint32_t* vals_in, uint32_t* vals_out,
-                       const double* depth64, const int32_t* n_visible, int32_t* long_run, int n, void* temp,
-                       size_t temp_bytes, cudaStream_t st);
-void launch_sort_depth64(const double* depth64, const uint32_t* key32, uint64_t* k64_a, uint64_t* k64_b,
-                         uint32_t* vals_in, uint32_t* vals_out, int n, void* temp, size_t temp_bytes,
-                         cudaStream_t st);
+// re-sort of equal-key runs (runs longer than 64 set *long_run; the host then
+// runs launch_sort_depth64).  Results in (keys_a, vals_a).
+int launch_sort_depth(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, const double* depth64,
+                      const int32_t* n_visible, int32_t* long_run, int n, uint32_t* scratch, cudaStream_t st);
+int launch_sort_depth64(const double* depth64, const uint32_t* touched, uint32_t* keys_a, uint32_t* keys_b,
+                        uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch, cudaStream_t st);
 void launch_bin_chunk(const BinK& B, cudaStream_t st);
 // tsb_raster.cu
 void launch_raster_fwd(const RecK& rec, const ChunkK& ck, const uint32_t* tile_vals, const OptK& O,

@@ -1,0 +1,259 @@
+// Hand-written stable LSD radix sort (Onesweep: one kernel per 8-bit digit pass
+// with decoupled look-back) of 32-bit keys with 32-bit values.  Used for the
+// global (depth, index) order: keys are fp32 depth bits, values Gaussian indices
+// in index order, so stability gives the reference's index tie-break
+// (splat.cpp:181-184).
+//
+//   k_sort_hist      one pass over the keys: histograms of all four digits
+//                    (warp-aggregated shared-memory atomics), into global.
+//   k_sort_scan      exclusive scan of each digit histogram -> digit offsets.
+//   k_onesweep       per pass: a CTA takes the next tile (atomic ticket, so
+//                    earlier tiles are always running -> forward progress),
+//                    ranks its 2048 items stably (warp-striped slots, match_any
+//                    peers, per-warp digit counters), publishes its per-digit
+//                    counts, looks back over earlier tiles' published counts /
+//                    inclusive prefixes, stages the tile in shared memory in
+//                    digit order and writes it out with consecutive threads
+//                    writing consecutive positions of each digit run.
+#include <cuda_runtime.h>
+
+#include "tsb_internal.h"
+
+namespace tsb {
+
+namespace {
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortIPT = 16;
+constexpr int kSortTile = kSortThreads * kSortIPT;  // 4096 items
+constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCountMask = (1u << 30) - 1u;
+
+// Lanes holding the same 8-bit digit, from 8 ballots (cheaper than match.any).
+__device__ __forceinline__ unsigned peers8(uint32_t d, bool valid) {
+    unsigned m = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const unsigned bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        m &= ((d >> b) & 1u) ? bb : ~bb;
+    }
+    return valid ? m : 0u;
+}
+}  // namespace
+
+// All four digit histograms in one pass.  Per-warp sub-histograms; the lanes that
+// share lane 0's digit (the common case for the high, low-entropy digits) are
+// counted with one atomic by lane 0, the others add their own.
+__global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint32_t* __restrict__ keys, int n,
+                                                            uint32_t* __restrict__ hist /* [4][256] */,
+                                                            uint32_t* __restrict__ status, int status_words) {
+    __shared__ uint32_t h[kSortWarps][4][256];
+    // clear the look-back status words of all four passes (used only after this kernel)
+    for (int i = blockIdx.x * kSortThreads + threadIdx.x; i < status_words; i += gridDim.x * kSortThreads)
+        status[i] = 0u;
+    for (int i = threadIdx.x; i < kSortWarps * 4 * 256; i += kSortThreads) (&h[0][0][0])[i] = 0u;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int n4 = n >> 2;
+    const uint4* k4 = reinterpret_cast<const uint4*>(keys);
+    for (int i = blockIdx.x * kSortThreads + threadIdx.x; i - (int)threadIdx.x < n4 + 1;
+         i += gridDim.x * kSortThreads) {
+        uint32_t kk[4];
+        bool valid[4];
+        if (i < n4) {
+            const uint4 q = k4[i];
+            kk[0] = q.x; kk[1] = q.y; kk[2] = q.z; kk[3] = q.w;
+            valid[0] = valid[1] = valid[2] = valid[3] = true;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int idx = 4 * n4 + 4 * (i - n4) + j;
+                valid[j] = i >= n4 && (i - n4) == 0 && idx < n;
+                kk[j] = valid[j] ? keys[idx] : 0u;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const uint32_t d = (kk[j] >> (8 * p)) & 255u;
+                const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
+                const bool v0 = __shfl_sync(0xffffffffu, valid[j], 0);
+                const unsigned same = __ballot_sync(0xffffffffu, valid[j] && v0 && d == d0);
+                if (lane == 0 && same) atomicAdd(&h[warp][p][d0], (uint32_t)__popc(same));
+                else if (valid[j] && !((same >> lane) & 1u)) atomicAdd(&h[warp][p][d], 1u);
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 4 * 256; i += kSortThreads) {
+        uint32_t v = 0;
+        for (int w = 0; w < kSortWarps; ++w) v += (&h[w][0][0])[i];
+        if (v) atomicAdd(&hist[i], v);
+    }
+}
+
+__global__ void k_sort_scan(uint32_t* __restrict__ hist /* in: counts, out: exclusive offsets */) {
+    // 4 warps, one per digit pass; each lane owns 8 consecutive bins
+    const int p = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* h = hist + 256 * p;
+    uint32_t v[8], s = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        v[j] = h[lane * 8 + j];
+        s += v[j];
+    }
+    uint32_t inc = s;
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += u;
+    }
+    uint32_t run = inc - s;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        h[lane * 8 + j] = run;
+        run += v[j];
+    }
+}
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) { return *(const volatile uint32_t*)p; }
+
+__global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint32_t* __restrict__ keys_in,
+                                                           const uint32_t* __restrict__ vals_in,
+                                                           uint32_t* __restrict__ keys_out,
+                                                           uint32_t* __restrict__ vals_out, int n, int shift,
+                                                           const uint32_t* __restrict__ digit_off,
+                                                           uint32_t* status, uint32_t* tile_ticket) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint32_t warp_cnt[kSortWarps][256];  // counts, then exclusive offsets across warps
+    __shared__ uint32_t block_start[256];            // exclusive scan over digits of the tile counts
+    __shared__ uint32_t global_base[256];
+    __shared__ uint32_t s_keys[kSortTile];
+    __shared__ uint32_t s_vals[kSortTile];
+    __shared__ uint32_t s_wsum[kSortWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(tile_ticket, 1u);
+    for (int i = tid; i < kSortWarps * 256; i += kSortThreads) (&warp_cnt[0][0])[i] = 0u;
+    __syncthreads();
+    const int tile = (int)s_tile;
+    const int base = tile * kSortTile;
+
+    // load warp-striped: slot i of lane l is item (warp*32*IPT + i*32 + l) of the tile
+    uint32_t k[kSortIPT], v[kSortIPT], lr[kSortIPT];
+#pragma unroll
+    for (int i = 0; i < kSortIPT; ++i) {
+        const int idx = base + warp * 32 * kSortIPT + i * 32 + lane;
+        const bool valid = idx < n;
+        k[i] = valid ? keys_in[idx] : 0u;
+        v[i] = valid ? vals_in[idx] : 0u;
+        lr[i] = valid ? 0u : 0xffffffffu;
+    }
+    // stable rank within the warp (slot order, then lane order == item order)
+    const unsigned lt_mask = (1u << lane) - 1u;
+#pragma unroll
+    for (int i = 0; i < kSortIPT; ++i) {
+        const bool valid = lr[i] == 0u;
+        const uint32_t d = (k[i] >> shift) & 255u;
+        const unsigned peers = peers8(d, valid);
+        uint32_t cur = 0;
+        if (valid) {
+            cur = warp_cnt[warp][d];
+            lr[i] = cur + (uint32_t)__popc(peers & lt_mask);
+        }
+        __syncwarp();
+        if (valid && (peers & lt_mask) == 0u) warp_cnt[warp][d] = cur + (uint32_t)__popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+
+    // per digit (thread d): exclusive offsets across warps, tile count, block scan
+    const int d = tid;  // kSortThreads == 256 digits
+    uint32_t total = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) {
+        const uint32_t c = warp_cnt[w][d];
+        warp_cnt[w][d] = total;
+        total += c;
+    }
+    {
+        uint32_t inc = total;
+        for (int s = 1; s < 32; s <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, inc, s);
+            if (lane >= s) inc += u;
+        }
+        if (lane == 31) s_wsum[warp] = inc;
+        __syncthreads();
+        uint32_t woff = 0;
+        for (int w = 0; w < warp; ++w) woff += s_wsum[w];
+        block_start[d] = woff + inc - total;
+    }
+    // decoupled look-back for this digit's global offset
+    uint32_t* st = status + (size_t)tile * 256;
+    if (tile == 0) {
+        atomicExch(&st[d], kFlagInc | total);
+        global_base[d] = digit_off[d];
+    } else {
+        atomicExch(&st[d], kFlagAgg | total);
+        uint32_t prefix = 0;
+        for (int t = tile - 1; t >= 0; --t) {
+            uint32_t s;
+            do {
+                s = ld_volatile(status + (size_t)t * 256 + d);
+            } while ((s & ~kCountMask) == 0u);
+            prefix += s & kCountMask;
+            if ((s & ~kCountMask) == kFlagInc) break;
+        }
+        atomicExch(&st[d], kFlagInc | (prefix + total));
+        global_base[d] = digit_off[d] + prefix;
+    }
+    __syncthreads();
+
+    // stage the tile in digit order
+#pragma unroll
+    for (int i = 0; i < kSortIPT; ++i) {
+        if (lr[i] == 0xffffffffu) continue;
+        const uint32_t dd = (k[i] >> shift) & 255u;
+        const uint32_t pos = block_start[dd] + warp_cnt[warp][dd] + lr[i];
+        s_keys[pos] = k[i];
+        s_vals[pos] = v[i];
+    }
+    __syncthreads();
+    const int count = min(kSortTile, n - base);
+    for (int j = tid; j < count; j += kSortThreads) {
+        const uint32_t key = s_keys[j];
+        const uint32_t dd = (key >> shift) & 255u;
+        const uint32_t o = global_base[dd] + (uint32_t)j - block_start[dd];
+        keys_out[o] = key;
+        vals_out[o] = s_vals[j];
+    }
+}
+
+size_t radix_sort_scratch_words(int n) {
+    const int tiles = (n + kSortTile - 1) / kSortTile;
+    return (size_t)4 * 256 + 4 + (size_t)4 * tiles * 256;  // hist/offsets, tickets, status per pass
+}
+
+// keys/vals: double buffers; result ends in (keys_b, vals_b) after 4 passes
+// when the pass count is even it ends in *_a -- we always do 4 passes and
+// return the buffer holding the result.
+int radix_sort32(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch,
+                 cudaStream_t st) {
+    if (n <= 0) return 0;
+    const int tiles = (n + kSortTile - 1) / kSortTile;
+    uint32_t* hist = scratch;
+    uint32_t* tickets = scratch + 4 * 256;
+    uint32_t* status = tickets + 4;
+    cudaMemsetAsync(scratch, 0, sizeof(uint32_t) * (4 * 256 + 4), st);
+    const int hgrid = max(1, min(148 * 2, (n / 4 + kSortThreads - 1) / kSortThreads));
+    k_sort_hist<<<hgrid, kSortThreads, 0, st>>>(keys_a, n, hist, status, 4 * 256 * tiles);
+    k_sort_scan<<<1, 128, 0, st>>>(hist);
+    uint32_t *ki = keys_a, *ko = keys_b, *vi = vals_a, *vo = vals_b;
+    for (int p = 0; p < 4; ++p) {
+        k_onesweep<<<tiles, kSortThreads, 0, st>>>(ki, vi, ko, vo, n, 8 * p, hist + 256 * p,
+                                                   status + (size_t)p * 256 * tiles, tickets + p);
+        uint32_t* t = ki; ki = ko; ko = t;
+        t = vi; vi = vo; vo = t;
+    }
+    return 6;  // kernels launched; result is back in (keys_a, vals_a)
+}
+
+}  // namespace tsb
