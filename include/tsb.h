@@ -114,6 +114,10 @@ void tsb_ctx_destroy(tsb_ctx* ctx);
 int tsb_ctx_synchronize(tsb_ctx* ctx);
 /* The context's cudaStream_t (as void*), for callers that time on it. */
 void* tsb_ctx_stream(tsb_ctx* ctx);
+/* Each render pass runs on its own stream (forked from the context stream by
+ * events), so passes used for consecutive frames overlap.  tsb_ctx_join makes the
+ * context stream wait for all work enqueued so far on every pass of the context. */
+int tsb_ctx_join(tsb_ctx* ctx);
 /* Number of kernels this context has launched (bench.py gpu_launches). */
 int64_t tsb_ctx_launch_count(tsb_ctx* ctx);
 
@@ -165,6 +169,7 @@ int tsb_scene_adam_step(tsb_scene* s, const tsb_adam_config* cfg);
 /* A pass is a reusable per-frame workspace: prepare() == the RenderPass ctor
  * (prepare + depth sort + build_tiles, splat.cpp:90-200). */
 int tsb_pass_create(tsb_ctx* ctx, tsb_pass** out);
+void* tsb_pass_stream(tsb_pass* p);
 void tsb_pass_destroy(tsb_pass* p);
 int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam,
                      const tsb_render_options* opt, const tsb_frame* frame);

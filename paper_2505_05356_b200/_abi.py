@@ -74,6 +74,8 @@ SIGNATURES = {
     "tsb_ctx_destroy": (None, [_vp]),
     "tsb_ctx_synchronize": (C.c_int, [_vp]),
     "tsb_ctx_stream": (_vp, [_vp]),
+    "tsb_ctx_join": (C.c_int, [_vp]),
+    "tsb_pass_stream": (_vp, [_vp]),
     "tsb_ctx_launch_count": (C.c_int64, [_vp]),
     "tsb_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "tsb_ctx_stage_times": (C.c_int, [_vp, _dp, _lp]),

@@ -70,6 +70,7 @@ struct tsb_ctx {
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     std::vector<std::pair<int, size_t>> ev_marks;  // (stage, index of start event)
+    std::vector<tsb_pass*> passes;                 // joined by tsb_ctx_join
 };
 
 namespace {
@@ -80,7 +81,8 @@ struct Stage {
     int stage;
     size_t idx = 0;
     bool on;
-    Stage(tsb_ctx* ctx, int s) : c(ctx), stage(s), on(ctx->profiling) {
+    cudaStream_t stream;
+    Stage(tsb_ctx* ctx, int s, cudaStream_t st) : c(ctx), stage(s), on(ctx->profiling), stream(st) {
         if (!on) return;
         if (c->ev_used + 2 > c->ev_pool.size()) {
             for (int i = 0; i < 64; ++i) {
@@ -91,11 +93,11 @@ struct Stage {
         }
         idx = c->ev_used;
         c->ev_used += 2;
-        cudaEventRecord(c->ev_pool[idx], c->stream);
+        cudaEventRecord(c->ev_pool[idx], stream);
     }
     ~Stage() {
         if (!on) return;
-        cudaEventRecord(c->ev_pool[idx + 1], c->stream);
+        cudaEventRecord(c->ev_pool[idx + 1], stream);
         c->ev_marks.emplace_back(stage, idx);
     }
 };
@@ -114,10 +116,15 @@ struct tsb_scene {
     float* staging = nullptr; // 4n floats for host<->device (un)packing
     int64_t step = 0;
     int64_t densify_count = 0;
+    cudaEvent_t params_ev = nullptr;  // last parameter write (ctx stream)
+    cudaEvent_t grads_ev = nullptr;   // last gradient/stats write (any stream)
 };
 
 struct tsb_pass {
     tsb_ctx* ctx = nullptr;
+    cudaStream_t stream = nullptr;   // each pass runs on its own stream (frames overlap)
+    cudaEvent_t done_ev = nullptr;   // recorded after every enqueue (tsb_ctx_join)
+    void* pinned = nullptr;          // per-pass pinned staging
     tsb_scene* scene = nullptr;
     CamK cam{};
     OptK opt{};
@@ -239,13 +246,21 @@ void tsb_ctx_destroy(tsb_ctx* c) {
     delete c;
 }
 
-int tsb_ctx_synchronize(tsb_ctx* c) {
+int tsb_ctx_join(tsb_ctx* c) {
     if (!c) return fail(TSB_ERR_INVALID, "null context");
+    for (tsb_pass* p : c->passes) TSB_CUDA(cudaStreamWaitEvent(c->stream, p->done_ev, 0));
+    return TSB_OK;
+}
+
+int tsb_ctx_synchronize(tsb_ctx* c) {
+    int rc = tsb_ctx_join(c);
+    if (rc) return rc;
     TSB_CUDA(cudaStreamSynchronize(c->stream));
     return TSB_OK;
 }
 
 void* tsb_ctx_stream(tsb_ctx* c) { return c ? (void*)c->stream : nullptr; }
+void* tsb_pass_stream(tsb_pass* p) { return p ? (void*)p->stream : nullptr; }
 int64_t tsb_ctx_launch_count(tsb_ctx* c) { return c ? c->launches : 0; }
 
 // ---------------------------------------------------------------------------
@@ -279,12 +294,19 @@ int tsb_scene_create(tsb_ctx* ctx, const tsb_scene_desc* d, tsb_scene** out) {
         return rc;
     }
     cudaStream_t st = ctx->stream;
+    if (cudaEventCreateWithFlags(&s->params_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->grads_ev, cudaEventDisableTiming) != cudaSuccess) {
+        tsb_scene_destroy(s);
+        return fail(TSB_ERR_CUDA, "tsb_scene_create: event creation failed");
+    }
     cudaMemsetAsync(s->params, 0, nel * sizeof(float4), st);
     cudaMemsetAsync(s->grads, 0, nel * sizeof(float4), st);
     cudaMemsetAsync(s->m, 0, nel * sizeof(float4), st);
     cudaMemsetAsync(s->v, 0, nel * sizeof(float4), st);
     cudaMemsetAsync(s->densify, 0, sizeof(float) * std::max(d->n, 1), st);
     cudaMemsetAsync(s->stats, 0, sizeof(double) * 9, st);
+    cudaEventRecord(s->params_ev, st);
+    cudaEventRecord(s->grads_ev, st);
     TSB_CUDA(cudaStreamSynchronize(st));
     *out = s;
     return TSB_OK;
@@ -301,6 +323,8 @@ void tsb_scene_destroy(tsb_scene* s) {
     dev_free(s->densify);
     dev_free(s->stats);
     dev_free(s->staging);
+    if (s->params_ev) cudaEventDestroy(s->params_ev);
+    if (s->grads_ev) cudaEventDestroy(s->grads_ev);
     delete s;
 }
 
@@ -346,6 +370,7 @@ int tsb_scene_set_params(tsb_scene* s, int where, const float* position, const f
     TSB_CUDA(cudaSetDevice(s->ctx->device));
     const int n = s->d.n;
     int rc;
+    if ((rc = tsb_ctx_join(s->ctx))) return rc;  // passes may still be reading the parameters
     if ((rc = pack_one(s, s->params, position, where, 3, 0))) return rc;
     if ((rc = pack_one(s, s->params, opacity_logit, where, 1, 3))) return rc;
     if ((rc = pack_one(s, s->params + n, log_scale, where, 3, 0))) return rc;
@@ -355,6 +380,7 @@ int tsb_scene_set_params(tsb_scene* s, int where, const float* position, const f
         for (int k = 0; k < s->d.n_keyframes; ++k)
             if ((rc = pack_one(s, s->params + (size_t)(3 + k) * n, motion + (size_t)k * 3 * n, where, 3, 0)))
                 return rc;
+    TSB_CUDA(cudaEventRecord(s->params_ev, s->ctx->stream));
     return TSB_OK;
 }
 
@@ -382,6 +408,7 @@ int tsb_scene_get_grads(tsb_scene* s, float* d_position, float* d_log_scale, flo
     TSB_CUDA(cudaSetDevice(s->ctx->device));
     const int n = s->d.n;
     int rc;
+    TSB_CUDA(cudaStreamWaitEvent(s->ctx->stream, s->grads_ev, 0));
     if ((rc = unpack_one(s, s->grads, d_position, 3, 0))) return rc;
     if ((rc = unpack_one(s, s->grads, d_opacity_logit, 1, 3))) return rc;
     if ((rc = unpack_one(s, s->grads + n, d_log_scale, 3, 0))) return rc;
@@ -402,8 +429,10 @@ int tsb_scene_zero_grads(tsb_scene* s) {
     if (!s) return fail(TSB_ERR_INVALID, "null scene");
     TSB_CUDA(cudaSetDevice(s->ctx->device));
     const size_t nel = (size_t)s->narrays * (size_t)std::max(s->d.n, 1);
+    TSB_CUDA(cudaStreamWaitEvent(s->ctx->stream, s->grads_ev, 0));
     TSB_CUDA(cudaMemsetAsync(s->grads, 0, nel * sizeof(float4), s->ctx->stream));
     TSB_CUDA(cudaMemsetAsync(s->stats, 0, sizeof(double) * 9, s->ctx->stream));
+    TSB_CUDA(cudaEventRecord(s->grads_ev, s->ctx->stream));
     return TSB_OK;
 }
 
@@ -419,6 +448,7 @@ int tsb_scene_get_densify_stat(tsb_scene* s, float* grad_norm_sum, int64_t* coun
     if (!s) return fail(TSB_ERR_INVALID, "null scene");
     TSB_CUDA(cudaSetDevice(s->ctx->device));
     if (grad_norm_sum && s->d.n > 0) {
+        TSB_CUDA(cudaStreamWaitEvent(s->ctx->stream, s->grads_ev, 0));
         TSB_CUDA(cudaMemcpyAsync(grad_norm_sum, s->densify, sizeof(float) * s->d.n, cudaMemcpyDeviceToHost,
                                  s->ctx->stream));
         TSB_CUDA(cudaStreamSynchronize(s->ctx->stream));
@@ -430,6 +460,11 @@ int tsb_scene_get_densify_stat(tsb_scene* s, float* grad_norm_sum, int64_t* coun
 int tsb_scene_adam_step(tsb_scene* s, const tsb_adam_config* cfg) {
     if (!s || !cfg) return fail(TSB_ERR_INVALID, "tsb_scene_adam_step: null argument");
     TSB_CUDA(cudaSetDevice(s->ctx->device));
+    {
+        int rc = tsb_ctx_join(s->ctx);
+        if (rc) return rc;
+    }
+    TSB_CUDA(cudaStreamWaitEvent(s->ctx->stream, s->grads_ev, 0));
     s->step += 1;
     const double t = (double)s->step;
     const double bc1 = 1.0 - std::pow(cfg->beta1, t);
@@ -443,7 +478,7 @@ int tsb_scene_adam_step(tsb_scene* s, const tsb_adam_config* cfg) {
     for (int k = 0; k < s->d.n_keyframes; ++k)
         for (int c = 0; c < 3; ++c) lr[(size_t)(3 + k) * 4 + c] = cfg->motion;
     {
-        Stage sg(s->ctx, TSB_STAGE_ADAM);
+        Stage sg(s->ctx, TSB_STAGE_ADAM, s->ctx->stream);
         launch_adam(s->params, s->grads, s->m, s->v, s->d.n, s->narrays, lr.data(), cfg->beta1, cfg->beta2,
                     cfg->eps, bc1, bc2, s->densify, s->ctx->stream);
     }
@@ -451,6 +486,8 @@ int tsb_scene_adam_step(tsb_scene* s, const tsb_adam_config* cfg) {
     TSB_CHECK_LAUNCH();
     s->densify_count++;
     TSB_CUDA(cudaMemsetAsync(s->stats, 0, sizeof(double) * 9, s->ctx->stream));
+    TSB_CUDA(cudaEventRecord(s->params_ev, s->ctx->stream));
+    TSB_CUDA(cudaEventRecord(s->grads_ev, s->ctx->stream));
     return TSB_OK;
 }
 
@@ -462,12 +499,19 @@ int tsb_pass_create(tsb_ctx* ctx, tsb_pass** out) {
     TSB_CUDA(cudaSetDevice(ctx->device));
     tsb_pass* p = new tsb_pass();
     p->ctx = ctx;
+    if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->done_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaMallocHost(&p->pinned, 4096) != cudaSuccess) {
+        tsb_pass_destroy(p);
+        return fail(TSB_ERR_CUDA, "tsb_pass_create: stream/event/pinned allocation failed");
+    }
     int rc;
     if ((rc = dev_alloc(&p->counters, 8)) || (rc = dev_alloc(&p->loss_dev, 1)) || (rc = dev_alloc(&p->chw, 8)) ||
         (rc = dev_alloc(&p->list_off, 1))) {
         tsb_pass_destroy(p);
         return rc;
     }
+    ctx->passes.push_back(p);
     *out = p;
     return TSB_OK;
 }
@@ -499,7 +543,7 @@ int ensure_gauss(tsb_pass* p, int n) {
         (rc = dev_alloc(&p->rec.A, cap)) || (rc = dev_alloc(&p->rec.B, cap)) || (rc = dev_alloc(&p->rec.C, cap)) ||
         (rc = dev_alloc(&p->rec.D, cap)) || (rc = dev_alloc(&p->screen, (size_t)8 * cap)))
         return rc;
-    TSB_CUDA(cudaMemsetAsync(p->screen, 0, sizeof(float) * 8 * (size_t)cap, p->ctx->stream));
+    TSB_CUDA(cudaMemsetAsync(p->screen, 0, sizeof(float) * 8 * (size_t)cap, p->stream));
     p->n_cap = cap;
     if ((rc = dev_alloc(&p->sort_scratch, radix_sort_scratch_words(cap)))) return rc;
     return TSB_OK;
@@ -626,9 +670,9 @@ SceneK scenek(const tsb_scene* s) {
 
 int read_visible(tsb_pass* p) {
     if (p->V >= 0) return TSB_OK;
-    int32_t* h = (int32_t*)((char*)p->ctx->pinned + 1024);
-    TSB_CUDA(cudaMemcpyAsync(h, p->counters, 4, cudaMemcpyDeviceToHost, p->ctx->stream));
-    TSB_CUDA(cudaStreamSynchronize(p->ctx->stream));
+    int32_t* h = (int32_t*)((char*)p->pinned + 1024);
+    TSB_CUDA(cudaMemcpyAsync(h, p->counters, 4, cudaMemcpyDeviceToHost, p->stream));
+    TSB_CUDA(cudaStreamSynchronize(p->stream));
     p->V = h[0];
     return TSB_OK;
 }
@@ -638,13 +682,18 @@ int read_visible(tsb_pass* p) {
 void tsb_pass_destroy(tsb_pass* p) {
     if (!p) return;
     cudaSetDevice(p->ctx->device);
-    cudaStreamSynchronize(p->ctx->stream);
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    auto& v = p->ctx->passes;
+    v.erase(std::remove(v.begin(), v.end(), p), v.end());
     free_gauss(p);
     free_pixels(p);
     dev_free(p->hist); dev_free(p->tile_len); dev_free(p->tile_start); dev_free(p->ranges_all); dev_free(p->chunk_rank0);
     dev_free(p->vals); dev_free(p->block_done); dev_free(p->tile_blocks_done);
     dev_free(p->counters); dev_free(p->list_off);
     dev_free(p->loss_part); dev_free(p->bg_part); dev_free(p->loss_dev); dev_free(p->chw);
+    if (p->pinned) cudaFreeHost(p->pinned);
+    if (p->done_ev) cudaEventDestroy(p->done_ev);
+    if (p->stream) cudaStreamDestroy(p->stream);
     delete p;
 }
 
@@ -662,7 +711,7 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     if (cam->width > 32767 || cam->height > 32767)
         return fail(TSB_ERR_UNSUPPORTED, "render: image dimensions above 32767 are not supported");
     TSB_CUDA(cudaSetDevice(p->ctx->device));
-    cudaStream_t st = p->ctx->stream;
+    cudaStream_t st = p->stream;
 
     p->scene = s;
     p->nf = s->d.n_freq;
@@ -717,14 +766,15 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
         return rc;
 
     const SceneK S = scenek(s);
+    TSB_CUDA(cudaStreamWaitEvent(st, s->params_ev, 0));
     TSB_CUDA(cudaMemsetAsync(p->counters, 0, sizeof(int32_t) * 8, st));
     {
-        Stage sg(p->ctx, TSB_STAGE_PREPROCESS);
+        Stage sg(p->ctx, TSB_STAGE_PREPROCESS, st);
         launch_preprocess(S, C, O, p->frame, p->key_a, p->depth64, p->gidx_a, p->touched, p->rect, p->rec,
                           p->counters, st);
     }
     {
-        Stage sg(p->ctx, TSB_STAGE_DEPTH_SORT);
+        Stage sg(p->ctx, TSB_STAGE_DEPTH_SORT, st);
         p->ctx->launches += launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, p->depth64, p->counters,
                                               p->counters + 4, n, p->sort_scratch, st);
     }
@@ -733,6 +783,7 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     p->V = -1;
     p->nchunks = 0;
     p->prepared = true;
+    TSB_CUDA(cudaEventRecord(p->done_ev, st));
     return TSB_OK;
 }
 
@@ -748,9 +799,9 @@ int tsb_pass_visible_count(tsb_pass* p, int32_t* out) {
 int tsb_pass_num_keys(tsb_pass* p, int64_t* out) {
     if (!p || !out) return fail(TSB_ERR_INVALID, "null argument");
     if (!p->forwarded) return fail(TSB_ERR_INVALID, "tile lists are built by forward()");
-    uint32_t* h = (uint32_t*)((char*)p->ctx->pinned + 1040);
-    TSB_CUDA(cudaMemcpyAsync(h, p->list_off, 4, cudaMemcpyDeviceToHost, p->ctx->stream));
-    TSB_CUDA(cudaStreamSynchronize(p->ctx->stream));
+    uint32_t* h = (uint32_t*)((char*)p->pinned + 1040);
+    TSB_CUDA(cudaMemcpyAsync(h, p->list_off, 4, cudaMemcpyDeviceToHost, p->stream));
+    TSB_CUDA(cudaStreamSynchronize(p->stream));
     *out = (int64_t)h[0];
     return TSB_OK;
 }
@@ -761,11 +812,11 @@ namespace {
 int run_forward(tsb_pass* p, const float* target, bool loss) {
     if (!p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
     TSB_CUDA(cudaSetDevice(p->ctx->device));
-    cudaStream_t st = p->ctx->stream;
+    cudaStream_t st = p->stream;
     PixK px = pixk(p);
     const bool full = (p->channels & TSB_CH_FULL_LISTS) != 0;
     const int n = p->scene->d.n;
-    int32_t* hc = (int32_t*)((char*)p->ctx->pinned + 2048);
+    int32_t* hc = (int32_t*)((char*)p->pinned + 2048);
     for (int attempt = 0; attempt < 8; ++attempt) {
         TSB_CUDA(cudaMemsetAsync(p->counters + 1, 0, sizeof(int32_t) * 3, st));
         TSB_CUDA(cudaMemsetAsync(p->list_off, 0, sizeof(uint32_t), st));
@@ -802,7 +853,7 @@ int run_forward(tsb_pass* p, const float* target, bool loss) {
             B.ranges = p->ranges_all + (size_t)c * p->ntiles;
             B.prev_ranges = c ? p->ranges_all + (size_t)(c - 1) * p->ntiles : nullptr;
             if (nseg > 0) {
-                Stage sg(p->ctx, TSB_STAGE_BINNING);
+                Stage sg(p->ctx, TSB_STAGE_BINNING, st);
                 launch_bin_chunk(B, st);
                 p->ctx->launches += 4;
             } else {
@@ -818,7 +869,7 @@ int run_forward(tsb_pass* p, const float* target, bool loss) {
             ck.blocks_done_total = p->counters + 3;
             ck.overflow = p->counters + 2;
             {
-                Stage sg(p->ctx, TSB_STAGE_RASTER_FWD);
+                Stage sg(p->ctx, TSB_STAGE_RASTER_FWD, st);
                 launch_raster_fwd(p->rec, ck, p->vals, p->opt, p->W, p->H, p->nf, px, fs, loss ? target : nullptr,
                                   p->chw, p->loss_part, st);
                 p->ctx->launches += 1;
@@ -863,23 +914,26 @@ int run_forward(tsb_pass* p, const float* target, bool loss) {
         fx.n_visible = p->counters;
         fx.overflow = p->counters + 2;
         {
-            Stage sg(p->ctx, TSB_STAGE_FIXUP);
+            Stage sg(p->ctx, TSB_STAGE_FIXUP, st);
             launch_fixup(scenek(p->scene), p->cam, p->opt, p->frame, fx, px, p->nf, st);
             p->ctx->launches += 1;
         }
         if (loss) {
-            Stage sg(p->ctx, TSB_STAGE_LOSS);
+            Stage sg(p->ctx, TSB_STAGE_LOSS, st);
             TSB_CUDA(cudaMemsetAsync(p->loss_dev, 0, sizeof(double), st));
             launch_fixup_loss(px, p->W, p->H, p->nf, target, p->chw, p->loss_dev, p->W * p->H, st);
             launch_reduce_partials(p->loss_part, p->nblocks, 1, p->loss_dev, 1.0 / ((double)p->W * p->H), st);
-            // scene loss accumulator += this pass's loss
+            // scene loss accumulator += this pass's loss (serialised with other gradient writers)
+            TSB_CUDA(cudaStreamWaitEvent(st, p->scene->grads_ev, 0));
             launch_reduce_partials(p->loss_dev, 1, 1, p->scene->stats + 8, 1.0, st);
+            TSB_CUDA(cudaEventRecord(p->scene->grads_ev, st));
             p->ctx->launches += 3;
         }
         TSB_CHECK_LAUNCH();
         p->forwarded = true;
         p->have_loss = loss;
         (void)n;
+        TSB_CUDA(cudaEventRecord(p->done_ev, st));
         return TSB_OK;
     }
     return fail(TSB_ERR_NOMEM, "render: tile-list storage kept overflowing");
@@ -897,7 +951,7 @@ int tsb_pass_forward_loss(tsb_pass* p, int where, const float* target, const dou
     if (!p || !target || !channel_weight) return fail(TSB_ERR_INVALID, "tsb_pass_forward_loss: null argument");
     if (!p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
     TSB_CUDA(cudaSetDevice(p->ctx->device));
-    cudaStream_t st = p->ctx->stream;
+    cudaStream_t st = p->stream;
     const size_t nq = (size_t)4 * p->nf * p->W * p->H;
     const float* dt = target;
     if (where == TSB_HOST) {
@@ -908,14 +962,14 @@ int tsb_pass_forward_loss(tsb_pass* p, int where, const float* target, const dou
     }
     float w[8] = {0};
     for (int c = 0; c < 4 * p->nf; ++c) w[c] = (float)channel_weight[c];
-    float* hw = (float*)p->ctx->pinned + 16;
+    float* hw = (float*)p->pinned + 16;
     TSB_CUDA(cudaStreamSynchronize(st));  // pinned staging reuse
     std::memcpy(hw, w, sizeof w);
     TSB_CUDA(cudaMemcpyAsync(p->chw, hw, sizeof w, cudaMemcpyHostToDevice, st));
     int rc = run_forward(p, dt, true);
     if (rc) return rc;
     if (loss_out) {
-        double* hl = (double*)((char*)p->ctx->pinned + 256);
+        double* hl = (double*)((char*)p->pinned + 256);
         TSB_CUDA(cudaMemcpyAsync(hl, p->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
         TSB_CUDA(cudaStreamSynchronize(st));
         *loss_out = *hl;
@@ -955,8 +1009,8 @@ int tsb_pass_download(tsb_pass* p, int which, void* host, size_t bytes) {
     int rc = tsb_pass_output(p, which, &d, &b);
     if (rc) return rc;
     if (!host || bytes < b) return fail(TSB_ERR_INVALID, "tsb_pass_download: host buffer too small");
-    TSB_CUDA(cudaMemcpyAsync(host, d, b, cudaMemcpyDeviceToHost, p->ctx->stream));
-    TSB_CUDA(cudaStreamSynchronize(p->ctx->stream));
+    TSB_CUDA(cudaMemcpyAsync(host, d, b, cudaMemcpyDeviceToHost, p->stream));
+    TSB_CUDA(cudaStreamSynchronize(p->stream));
     return TSB_OK;
 }
 
@@ -964,7 +1018,7 @@ int tsb_pass_backward(tsb_pass* p, int where, const float* d_quad) {
     if (!p) return fail(TSB_ERR_INVALID, "null pass");
     if (!p->forwarded) return fail(TSB_ERR_INVALID, "backward requires a forward pass");
     TSB_CUDA(cudaSetDevice(p->ctx->device));
-    cudaStream_t st = p->ctx->stream;
+    cudaStream_t st = p->stream;
     const float* up = p->d_quad;
     if (d_quad) {
         const size_t nq = (size_t)4 * p->nf * p->W * p->H;
@@ -981,18 +1035,21 @@ int tsb_pass_backward(tsb_pass* p, int where, const float* d_quad) {
     tsb_scene* s = p->scene;
     float dpsi[2];
     for (int f = 0; f < p->nf; ++f) dpsi[f] = (float)(4.0 * M_PI * s->d.frequency[f] / s->d.speed_of_light);
+    TSB_CUDA(cudaStreamWaitEvent(st, s->grads_ev, 0));
     {
-        Stage sg(p->ctx, TSB_STAGE_RASTER_BWD);
+        Stage sg(p->ctx, TSB_STAGE_RASTER_BWD, st);
         launch_raster_bwd(p->rec, p->ranges_all, p->nchunks, p->vals, p->opt, p->W, p->H, p->nf, dpsi, pixk(p), up,
                           p->screen, s->d.n, p->bg_part, st);
         launch_reduce_partials(p->bg_part, p->nblocks, 4 * p->nf, s->stats, 1.0, st);
     }
     {
-        Stage sg(p->ctx, TSB_STAGE_CHAIN);
+        Stage sg(p->ctx, TSB_STAGE_CHAIN, st);
         launch_chain(scenek(s), p->cam, p->opt, p->frame, p->touched, p->screen, s->grads, st);
     }
     p->ctx->launches += 3;
     TSB_CHECK_LAUNCH();
+    TSB_CUDA(cudaEventRecord(s->grads_ev, st));
+    TSB_CUDA(cudaEventRecord(p->done_ev, st));
     return TSB_OK;
 }
 
@@ -1001,7 +1058,7 @@ int tsb_pass_debug_prepared(tsb_pass* p, int32_t* gidx, int32_t* rect) {
     if (!p || !p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
     int rc = read_visible(p);
     if (rc) return rc;
-    cudaStream_t st = p->ctx->stream;
+    cudaStream_t st = p->stream;
     const int V = p->V;
     std::vector<uint32_t> g(V > 0 ? V : 1);
     if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), p->gidx_a, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, st));
@@ -1028,13 +1085,13 @@ int tsb_pass_debug_tiles(tsb_pass* p, int32_t* tiles_x, int32_t* tiles_y, int64_
     if (tiles_y) *tiles_y = p->opt.tiles_y;
     int rc = read_visible(p);
     if (rc) return rc;
-    cudaStream_t st = p->ctx->stream;
+    cudaStream_t st = p->stream;
     const int nt = p->ntiles, nch = p->nchunks;
     std::vector<uint4> rg((size_t)std::max(nch * nt, 1));
     if (nch > 0)
         TSB_CUDA(cudaMemcpyAsync(rg.data(), p->ranges_all, sizeof(uint4) * nch * nt, cudaMemcpyDeviceToHost, st));
     int64_t k = 0;
-    uint32_t* hl = (uint32_t*)((char*)p->ctx->pinned + 1056);
+    uint32_t* hl = (uint32_t*)((char*)p->pinned + 1056);
     TSB_CUDA(cudaMemcpyAsync(hl, p->list_off, 4, cudaMemcpyDeviceToHost, st));
     TSB_CUDA(cudaStreamSynchronize(st));
     k = hl[0];
@@ -1068,7 +1125,7 @@ int tsb_pass_debug_records(tsb_pass* p, float* rec12) {
     if (!p || !p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
     int rc = read_visible(p);
     if (rc) return rc;
-    cudaStream_t st = p->ctx->stream;
+    cudaStream_t st = p->stream;
     const int n = p->scene->d.n, V = p->V;
     std::vector<float4> A(std::max(n, 1)), B(std::max(n, 1)), C(std::max(n, 1)), D(std::max(n, 1));
     std::vector<uint32_t> g(std::max(V, 1));
@@ -1108,9 +1165,9 @@ int tsb_pass_debug_screen_grads(tsb_pass* p, float* g8) {
 
 int tsb_pass_debug_fixups(tsb_pass* p, int32_t* count) {
     if (!p || !count) return fail(TSB_ERR_INVALID, "null argument");
-    int32_t* h = (int32_t*)((char*)p->ctx->pinned + 512);
-    TSB_CUDA(cudaMemcpyAsync(h, p->counters + 1, 4, cudaMemcpyDeviceToHost, p->ctx->stream));
-    TSB_CUDA(cudaStreamSynchronize(p->ctx->stream));
+    int32_t* h = (int32_t*)((char*)p->pinned + 512);
+    TSB_CUDA(cudaMemcpyAsync(h, p->counters + 1, 4, cudaMemcpyDeviceToHost, p->stream));
+    TSB_CUDA(cudaStreamSynchronize(p->stream));
     *count = *h;
     return TSB_OK;
 }
@@ -1215,7 +1272,8 @@ int tsb_scene_allreduce_grads(tsb_scene* s, tsb_comm* c) {
     if (!s || !c) return fail(TSB_ERR_INVALID, "null argument");
     const size_t nel = (size_t)s->narrays * (size_t)s->d.n * 4;
     cudaStream_t st = s->ctx->stream;
-    Stage sg(s->ctx, TSB_STAGE_ALLREDUCE);
+    TSB_CUDA(cudaStreamWaitEvent(st, s->grads_ev, 0));
+    Stage sg(s->ctx, TSB_STAGE_ALLREDUCE, st);
     ncclResult_t r = g_nccl.GroupStart();
     if (r == ncclSuccess && nel > 0)
         r = g_nccl.AllReduce(s->grads, s->grads, nel, ncclFloat, ncclSum, c->comm, st);
@@ -1224,6 +1282,7 @@ int tsb_scene_allreduce_grads(tsb_scene* s, tsb_comm* c) {
     if (r != ncclSuccess || r2 != ncclSuccess)
         return fail(TSB_ERR_NCCL,
                     std::string("ncclAllReduce: ") + g_nccl.GetErrorString(r != ncclSuccess ? r : r2));
+    TSB_CUDA(cudaEventRecord(s->grads_ev, st));
     return TSB_OK;
 }
 

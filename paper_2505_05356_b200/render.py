@@ -160,6 +160,10 @@ class Context:
     def synchronize(self):
         check(lib().tsb_ctx_synchronize(self._h))
 
+    def join(self):
+        """Make the context stream wait for all work enqueued on this context's passes."""
+        check(lib().tsb_ctx_join(self._h))
+
     def launch_count(self) -> int:
         return int(lib().tsb_ctx_launch_count(self._h))
 
