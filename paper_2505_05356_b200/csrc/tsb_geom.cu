@@ -220,6 +220,86 @@ void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F
 // (trainer.cpp:313-314, 329-331), and accumulate into the scene gradient
 // buffer (GroupGrads::add).  Clears the screen-gradient slots it consumed.
 // ---------------------------------------------------------------------------
+// Intermediates the chain needs, recomputed in fp64 with reciprocals instead of
+// divisions (values agree with prep64 to a few ulp; the chain has no decisions
+// except the frustum-clamp flags and the 0 < r < 1 gate, which use the same
+// comparisons as prep64 on the same inputs).
+struct Chain64 {
+    double p[3], depth, opacity, refl_raw, M[6], cov3d[9], tx, ty, ca, cb, cc, Rq[9], uq[4], sv[3], qn;
+    bool clx, cly;
+};
+
+__device__ __forceinline__ void chain_prep(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F, int gi,
+                                           Chain64& s) {
+    double x[3];
+    frame_mean(S, F, gi, x);
+    const double* R = C.R;
+    for (int i = 0; i < 3; ++i) s.p[i] = R[i * 3 + 0] * x[0] + R[i * 3 + 1] * x[1] + R[i * 3 + 2] * x[2] + C.t[i];
+    s.depth = sqrt(s.p[0] * s.p[0] + s.p[1] * s.p[1] + s.p[2] * s.p[2]);
+    const float4 po = S.pos_op[gi];
+    s.opacity = 1.0 / (1.0 + exp(-(double)po.w));
+    const double z = s.p[2], iz = 1.0 / z;
+    const float4 qf = S.quat[gi];
+    const double q[4] = {(double)qf.x, (double)qf.y, (double)qf.z, (double)qf.w};
+    const double qq = q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3];
+    s.qn = sqrt(qq);
+    const double iq = qq > 0.0 ? 1.0 / s.qn : 1.0;
+    for (int i = 0; i < 4; ++i) s.uq[i] = q[i] * iq;
+    {
+        const double w = s.uq[0], xx = s.uq[1], y = s.uq[2], zz = s.uq[3];
+        s.Rq[0] = 1 - 2 * (y * y + zz * zz); s.Rq[1] = 2 * (xx * y - w * zz);     s.Rq[2] = 2 * (xx * zz + w * y);
+        s.Rq[3] = 2 * (xx * y + w * zz);     s.Rq[4] = 1 - 2 * (xx * xx + zz * zz); s.Rq[5] = 2 * (y * zz - w * xx);
+        s.Rq[6] = 2 * (xx * zz - w * y);     s.Rq[7] = 2 * (y * zz + w * xx);     s.Rq[8] = 1 - 2 * (xx * xx + y * y);
+    }
+    const float4 sa = S.scale_amp[gi];
+    s.sv[0] = exp((double)sa.x);
+    s.sv[1] = exp((double)sa.y);
+    s.sv[2] = exp((double)sa.z);
+    double M3[9];
+    for (int r = 0; r < 3; ++r)
+        for (int j = 0; j < 3; ++j) M3[r * 3 + j] = s.Rq[r * 3 + j] * s.sv[j];
+    for (int i = 0; i < 3; ++i)
+        for (int j = i; j < 3; ++j) {
+            s.cov3d[i * 3 + j] = M3[i * 3 + 0] * M3[j * 3 + 0] + M3[i * 3 + 1] * M3[j * 3 + 1] +
+                                 M3[i * 3 + 2] * M3[j * 3 + 2];
+            s.cov3d[j * 3 + i] = s.cov3d[i * 3 + j];
+        }
+    // same comparisons as prep64 (splat.cpp:136-140) for the clamp routing
+    const double rx = s.p[0] / z, ry = s.p[1] / z;
+    s.clx = rx < -C.lim_x || rx > C.lim_x;
+    s.cly = ry < -C.lim_y || ry > C.lim_y;
+    s.tx = clampd(rx, -C.lim_x, C.lim_x) * z;
+    s.ty = clampd(ry, -C.lim_y, C.lim_y) * z;
+    const double J[6] = {C.fx * iz, 0.0, -C.fx * s.tx * iz * iz, 0.0, C.fy * iz, -C.fy * s.ty * iz * iz};
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 3; ++j)
+            s.M[i * 3 + j] = J[i * 3 + 0] * R[0 * 3 + j] + J[i * 3 + 1] * R[1 * 3 + j] + J[i * 3 + 2] * R[2 * 3 + j];
+    double T23[6];
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 3; ++j)
+            T23[i * 3 + j] = s.M[i * 3 + 0] * s.cov3d[0 * 3 + j] + s.M[i * 3 + 1] * s.cov3d[1 * 3 + j] +
+                             s.M[i * 3 + 2] * s.cov3d[2 * 3 + j];
+    double c2[4];
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j)
+            c2[i * 2 + j] = T23[i * 3 + 0] * s.M[j * 3 + 0] + T23[i * 3 + 1] * s.M[j * 3 + 1] +
+                            T23[i * 3 + 2] * s.M[j * 3 + 2];
+    c2[0] += O.dilation;
+    c2[3] += O.dilation;
+    const double idet = 1.0 / (c2[0] * c2[3] - c2[1] * c2[1]);
+    s.ca = c2[3] * idet;
+    s.cb = -c2[1] * idet;
+    s.cc = c2[0] * idet;
+    // the gate 0 < r_raw < 1 must see prep64's exact value
+    s.refl_raw = (double)sa.w * 0.28209479177387814;
+}
+
+// ---------------------------------------------------------------------------
+// k_chain: per visible Gaussian, chain the 8 screen-space gradients back to the
+// parameters (splat.cpp:551-648) in fp64, then through the trajectory
+// (trainer.cpp:313-314, 329-331), and accumulate into the scene gradient
+// buffer (GroupGrads::add).  Clears the screen-gradient slots it consumed.
+// ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) k_chain(SceneK S, CamK C, OptK O, FrameK F,
                                                const uint32_t* __restrict__ touched,
                                                float* __restrict__ screen,
@@ -227,22 +307,28 @@ __global__ void __launch_bounds__(128) k_chain(SceneK S, CamK C, OptK O, FrameK 
     const int gi = blockIdx.x * blockDim.x + threadIdx.x;
     if (gi >= S.n || touched[gi] == 0u) return;
     float g8[8];
+    bool any = false;
     for (int c = 0; c < 8; ++c) {
         g8[c] = screen[(size_t)c * S.n + gi];
-        screen[(size_t)c * S.n + gi] = 0.f;
+        any |= g8[c] != 0.f;
     }
-    Prep64 s;
-    prep64(S, C, O, F, gi, s);
+    // The chain is linear in the screen-space gradients: a splat no pixel reached
+    // (e.g. behind every tile's termination point) contributes exactly nothing.
+    if (!any) return;
+    for (int c = 0; c < 8; ++c) screen[(size_t)c * S.n + gi] = 0.f;
+    Chain64 s;
+    chain_prep(S, C, O, F, gi, s);
     const double d_mean0 = g8[0], d_mean1 = g8[1], d_ca = g8[2], d_cb = g8[3], d_cc = g8[4];
     const double d_op = g8[5], d_coef = g8[6], d_dep = g8[7];
     const double* R = C.R;
 
     const double d_logit = d_op * s.opacity * (1.0 - s.opacity);
     const double r_cl = clampd(s.refl_raw, 0.0, 1.0);
-    const double d2 = s.depth * s.depth;
-    const double d_depth = d_dep + d_coef * (-2.0 * S.s_int * r_cl / (d2 * s.depth));
+    const double id = 1.0 / s.depth;
+    const double id2 = id * id;
+    const double d_depth = d_dep + d_coef * (-2.0 * S.s_int * r_cl * id2 * id);
     double d_amp = 0.0;
-    if (s.refl_raw > 0.0 && s.refl_raw < 1.0) d_amp = 0.28209479177387814 * (d_coef * S.s_int / d2);
+    if (s.refl_raw > 0.0 && s.refl_raw < 1.0) d_amp = 0.28209479177387814 * (d_coef * S.s_int * id2);
 
     const double Q[4] = {s.ca, s.cb, s.cb, s.cc};
     const double GQ[4] = {d_ca, 0.5 * d_cb, 0.5 * d_cb, d_cc};
@@ -268,32 +354,26 @@ __global__ void __launch_bounds__(128) k_chain(SceneK S, CamK C, OptK O, FrameK 
     for (int a = 0; a < 2; ++a)
         for (int j = 0; j < 3; ++j)
             dJ[a * 3 + j] = dM[a * 3 + 0] * R[j * 3 + 0] + dM[a * 3 + 1] * R[j * 3 + 1] + dM[a * 3 + 2] * R[j * 3 + 2];
-    const double z = s.p[2], z2 = z * z, z3 = z2 * z;
+    const double z = s.p[2], iz = 1.0 / z, iz2 = iz * iz, iz3 = iz2 * iz;
     double dp[3] = {0, 0, 0};
-    const double dtx = dJ[2] * (-C.fx / z2);
-    const double dty = dJ[5] * (-C.fy / z2);
-    dp[2] += dJ[0] * (-C.fx / z2) + dJ[4] * (-C.fy / z2) + dJ[2] * (2.0 * C.fx * s.tx / z3) +
-             dJ[5] * (2.0 * C.fy * s.ty / z3);
-    if (s.clx) dp[2] += dtx * (s.tx / z); else dp[0] += dtx;
-    if (s.cly) dp[2] += dty * (s.ty / z); else dp[1] += dty;
-    dp[0] += d_mean0 * C.fx / z;
-    dp[2] += d_mean0 * (-C.fx * s.p[0] / z2);
-    dp[1] += d_mean1 * C.fy / z;
-    dp[2] += d_mean1 * (-C.fy * s.p[1] / z2);
-    for (int a = 0; a < 3; ++a) dp[a] += d_depth * (s.p[a] / s.depth);
+    const double dtx = dJ[2] * (-C.fx * iz2);
+    const double dty = dJ[5] * (-C.fy * iz2);
+    dp[2] += dJ[0] * (-C.fx * iz2) + dJ[4] * (-C.fy * iz2) + dJ[2] * (2.0 * C.fx * s.tx * iz3) +
+             dJ[5] * (2.0 * C.fy * s.ty * iz3);
+    if (s.clx) dp[2] += dtx * (s.tx * iz); else dp[0] += dtx;
+    if (s.cly) dp[2] += dty * (s.ty * iz); else dp[1] += dty;
+    dp[0] += d_mean0 * C.fx * iz;
+    dp[2] += d_mean0 * (-C.fx * s.p[0] * iz2);
+    dp[1] += d_mean1 * C.fy * iz;
+    dp[2] += d_mean1 * (-C.fy * s.p[1] * iz2);
+    for (int a = 0; a < 3; ++a) dp[a] += d_depth * (s.p[a] * id);
     double dpos[3];
     for (int a = 0; a < 3; ++a) dpos[a] = R[0 * 3 + a] * dp[0] + R[1 * 3 + a] * dp[1] + R[2 * 3 + a] * dp[2];
 
     // cov3d = M3 M3^T, M3 = R(q) diag(exp(log_scale))
-    const float4 qf = S.quat[gi];
-    const double q[4] = {(double)qf.x, (double)qf.y, (double)qf.z, (double)qf.w};
-    double uq[4], Rq[9];
-    quat_rot(q, uq, Rq);
-    const float4 sa = S.scale_amp[gi];
-    const double sv[3] = {exp((double)sa.x), exp((double)sa.y), exp((double)sa.z)};
     double M3[9], dM3[9];
     for (int rr = 0; rr < 3; ++rr)
-        for (int j = 0; j < 3; ++j) M3[rr * 3 + j] = Rq[rr * 3 + j] * sv[j];
+        for (int j = 0; j < 3; ++j) M3[rr * 3 + j] = s.Rq[rr * 3 + j] * s.sv[j];
     for (int rr = 0; rr < 3; ++rr)
         for (int j = 0; j < 3; ++j) {
             double t = 0;
@@ -303,13 +383,13 @@ __global__ void __launch_bounds__(128) k_chain(SceneK S, CamK C, OptK O, FrameK 
     double dls[3];
     for (int j = 0; j < 3; ++j) {
         double ds = 0;
-        for (int rr = 0; rr < 3; ++rr) ds += Rq[rr * 3 + j] * dM3[rr * 3 + j];
-        dls[j] = ds * sv[j];
+        for (int rr = 0; rr < 3; ++rr) ds += s.Rq[rr * 3 + j] * dM3[rr * 3 + j];
+        dls[j] = ds * s.sv[j];
     }
     double dRq[9];
     for (int rr = 0; rr < 3; ++rr)
-        for (int j = 0; j < 3; ++j) dRq[rr * 3 + j] = dM3[rr * 3 + j] * sv[j];
-    const double w = uq[0], x = uq[1], y = uq[2], zq = uq[3];
+        for (int j = 0; j < 3; ++j) dRq[rr * 3 + j] = dM3[rr * 3 + j] * s.sv[j];
+    const double w = s.uq[0], x = s.uq[1], y = s.uq[2], zq = s.uq[3];
     const double dR[4][9] = {{0, -zq, y, zq, 0, -x, -y, x, 0},
                              {0, y, zq, y, -2 * x, -w, zq, w, -2 * x},
                              {-2 * y, x, w, x, 0, zq, -w, zq, -2 * y},
@@ -317,13 +397,13 @@ __global__ void __launch_bounds__(128) k_chain(SceneK S, CamK C, OptK O, FrameK 
     double duq[4];
     for (int c = 0; c < 4; ++c) {
         double t = 0;
-        for (int k = 0; k < 9; ++k) t += dRq[k] * (dR[c][k] * 2.0);
-        duq[c] = t;
+        for (int k = 0; k < 9; ++k) t += dRq[k] * dR[c][k];
+        duq[c] = 2.0 * t;
     }
-    const double qn = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
-    const double ud = uq[0] * duq[0] + uq[1] * duq[1] + uq[2] * duq[2] + uq[3] * duq[3];
+    const double ud = s.uq[0] * duq[0] + s.uq[1] * duq[1] + s.uq[2] * duq[2] + s.uq[3] * duq[3];
+    const double iqn = 1.0 / s.qn;
     double dq[4];
-    for (int c = 0; c < 4; ++c) dq[c] = (duq[c] - uq[c] * ud) / qn;
+    for (int c = 0; c < 4; ++c) dq[c] = (duq[c] - s.uq[c] * ud) * iqn;
 
     // accumulate (GroupGrads::add; canonical += dXi + dXip1 == dP)
     const int n = S.n;
