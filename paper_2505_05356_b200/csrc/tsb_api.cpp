@@ -143,6 +143,7 @@ struct tsb_pass {
     uint32_t *key_a = nullptr, *key_b = nullptr;  // fp32 depth keys
     double* depth64 = nullptr;
     uint32_t *gidx_a = nullptr, *gidx_b = nullptr;
+    uint32_t* sorted = nullptr;  // global (depth, index) order: gidx_b, or gidx_a after the exact fallback
     uint32_t* touched = nullptr;
     uint2* rect = nullptr;
     RecK rec{};
@@ -175,6 +176,12 @@ struct tsb_pass {
     double* loss_dev = nullptr;
     float* chw = nullptr;
     uint32_t* sort_scratch = nullptr;
+    // fp64 fix-up record cache
+    int* fx_stamp = nullptr;
+    int* fx_work = nullptr;
+    int* fx_work_n = nullptr;
+    Rec64* fx_cache = nullptr;
+    int frame_stamp = 0;
 };
 
 extern "C" {
@@ -507,7 +514,7 @@ int tsb_pass_create(tsb_ctx* ctx, tsb_pass** out) {
     }
     int rc;
     if ((rc = dev_alloc(&p->counters, 8)) || (rc = dev_alloc(&p->loss_dev, 1)) || (rc = dev_alloc(&p->chw, 8)) ||
-        (rc = dev_alloc(&p->list_off, 1))) {
+        (rc = dev_alloc(&p->list_off, 1)) || (rc = dev_alloc(&p->fx_work_n, 1))) {
         tsb_pass_destroy(p);
         return rc;
     }
@@ -523,6 +530,7 @@ constexpr int kChunk0Segments = 65536 / kSeg;  // first depth chunk: 64K ranks, 
 void free_gauss(tsb_pass* p) {
     dev_free(p->key_a); dev_free(p->key_b); dev_free(p->gidx_a); dev_free(p->gidx_b);
     dev_free(p->depth64); dev_free(p->sort_scratch);
+    dev_free(p->fx_stamp); dev_free(p->fx_work); dev_free(p->fx_cache);
     dev_free(p->touched); dev_free(p->rect);
     dev_free(p->rec.A); dev_free(p->rec.B); dev_free(p->rec.C); dev_free(p->rec.D); dev_free(p->screen);
 }
@@ -545,7 +553,11 @@ int ensure_gauss(tsb_pass* p, int n) {
         return rc;
     TSB_CUDA(cudaMemsetAsync(p->screen, 0, sizeof(float) * 8 * (size_t)cap, p->stream));
     p->n_cap = cap;
-    if ((rc = dev_alloc(&p->sort_scratch, radix_sort_scratch_words(cap)))) return rc;
+    if ((rc = dev_alloc(&p->sort_scratch, radix_sort_scratch_words(cap))) || (rc = dev_alloc(&p->fx_stamp, cap)) ||
+        (rc = dev_alloc(&p->fx_work, cap)) || (rc = dev_alloc(&p->fx_cache, cap)))
+        return rc;
+    TSB_CUDA(cudaMemsetAsync(p->fx_stamp, 0, sizeof(int) * (size_t)cap, p->stream));
+    p->frame_stamp = 0;
     return TSB_OK;
 }
 
@@ -689,7 +701,7 @@ void tsb_pass_destroy(tsb_pass* p) {
     free_pixels(p);
     dev_free(p->hist); dev_free(p->tile_len); dev_free(p->tile_start); dev_free(p->ranges_all); dev_free(p->chunk_rank0);
     dev_free(p->vals); dev_free(p->block_done); dev_free(p->tile_blocks_done);
-    dev_free(p->counters); dev_free(p->list_off);
+    dev_free(p->counters); dev_free(p->list_off); dev_free(p->fx_work_n);
     dev_free(p->loss_part); dev_free(p->bg_part); dev_free(p->loss_dev); dev_free(p->chw);
     if (p->pinned) cudaFreeHost(p->pinned);
     if (p->done_ev) cudaEventDestroy(p->done_ev);
@@ -768,16 +780,19 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     const SceneK S = scenek(s);
     TSB_CUDA(cudaStreamWaitEvent(st, s->params_ev, 0));
     TSB_CUDA(cudaMemsetAsync(p->counters, 0, sizeof(int32_t) * 8, st));
+    TSB_CUDA(cudaMemsetAsync(p->counters + 5, 0xff, sizeof(int32_t), st));  // key range min
+    uint32_t* key_range = reinterpret_cast<uint32_t*>(p->counters + 5);
     {
         Stage sg(p->ctx, TSB_STAGE_PREPROCESS, st);
         launch_preprocess(S, C, O, p->frame, p->key_a, p->depth64, p->gidx_a, p->touched, p->rect, p->rec,
-                          p->counters, st);
+                          p->counters, key_range, st);
     }
     {
         Stage sg(p->ctx, TSB_STAGE_DEPTH_SORT, st);
         p->ctx->launches += launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, p->depth64, p->counters,
-                                              p->counters + 4, n, p->sort_scratch, st);
+                                              p->counters + 4, key_range, n, p->sort_scratch, st);
     }
+    p->sorted = p->gidx_b;
     p->ctx->launches += 1;
     TSB_CHECK_LAUNCH();
     p->V = -1;
@@ -825,7 +840,7 @@ int run_forward(tsb_pass* p, const float* target, bool loss) {
         if (loss) TSB_CUDA(cudaMemsetAsync(p->loss_part, 0, sizeof(double) * p->nblocks, st));
         FwdState fs{p->st_f, p->st_i, p->W * p->H};
         BinK B{};
-        B.sorted_gidx = p->gidx_a;
+        B.sorted_gidx = p->sorted;
         B.rect = p->rect;
         B.n_visible = p->counters;
         B.ts = p->opt.ts;
@@ -894,6 +909,7 @@ int run_forward(tsb_pass* p, const float* target, bool loss) {
             const int nn = p->scene->d.n;
             p->ctx->launches += launch_sort_depth64(p->depth64, p->touched, p->key_a, p->key_b, p->gidx_a,
                                                     p->gidx_b, nn, p->sort_scratch, st);
+            p->sorted = p->gidx_a;
             TSB_CUDA(cudaMemsetAsync(p->counters + 4, 0, sizeof(int32_t), st));
             continue;
         }
@@ -909,14 +925,19 @@ int run_forward(tsb_pass* p, const float* target, bool loss) {
         fx.chunk_rank0 = p->chunk_rank0;
         fx.binned_end_rank = total_chunks ? (p->chunk_seg0[nch - 1] + p->chunk_nseg[nch - 1]) * kSeg : 0;
         fx.vals = p->vals;
-        fx.sorted_gidx = p->gidx_a;
+        fx.sorted_gidx = p->sorted;
         fx.rect = p->rect;
         fx.n_visible = p->counters;
         fx.overflow = p->counters + 2;
+        fx.stamp = p->fx_stamp;
+        fx.frame_stamp = ++p->frame_stamp;
+        fx.work = p->fx_work;
+        fx.work_n = p->fx_work_n;
+        fx.cache = p->fx_cache;
         {
             Stage sg(p->ctx, TSB_STAGE_FIXUP, st);
             launch_fixup(scenek(p->scene), p->cam, p->opt, p->frame, fx, px, p->nf, st);
-            p->ctx->launches += 1;
+            p->ctx->launches += 3;
         }
         if (loss) {
             Stage sg(p->ctx, TSB_STAGE_LOSS, st);
@@ -1061,7 +1082,7 @@ int tsb_pass_debug_prepared(tsb_pass* p, int32_t* gidx, int32_t* rect) {
     cudaStream_t st = p->stream;
     const int V = p->V;
     std::vector<uint32_t> g(V > 0 ? V : 1);
-    if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), p->gidx_a, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, st));
+    if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), p->sorted, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, st));
     std::vector<uint2> r((size_t)std::max(p->scene->d.n, 1));
     if (rect && p->scene->d.n > 0)
         TSB_CUDA(cudaMemcpyAsync(r.data(), p->rect, sizeof(uint2) * p->scene->d.n, cudaMemcpyDeviceToHost, st));
@@ -1100,7 +1121,7 @@ int tsb_pass_debug_tiles(tsb_pass* p, int32_t* tiles_x, int32_t* tiles_y, int64_
     if (ids && k > 0) {
         TSB_CUDA(cudaMemcpyAsync(vals.data(), p->vals, sizeof(uint32_t) * k, cudaMemcpyDeviceToHost, st));
         if (p->V > 0)
-            TSB_CUDA(cudaMemcpyAsync(order.data(), p->gidx_a, sizeof(uint32_t) * p->V, cudaMemcpyDeviceToHost, st));
+            TSB_CUDA(cudaMemcpyAsync(order.data(), p->sorted, sizeof(uint32_t) * p->V, cudaMemcpyDeviceToHost, st));
         TSB_CUDA(cudaStreamSynchronize(st));
     }
     // per tile: concatenation of its chunk sub-lists (values are Gaussian indices;
@@ -1135,7 +1156,7 @@ int tsb_pass_debug_records(tsb_pass* p, float* rec12) {
         TSB_CUDA(cudaMemcpyAsync(C.data(), p->rec.C, sizeof(float4) * n, cudaMemcpyDeviceToHost, st));
         if (p->nf > 1) TSB_CUDA(cudaMemcpyAsync(D.data(), p->rec.D, sizeof(float4) * n, cudaMemcpyDeviceToHost, st));
     }
-    if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), p->gidx_a, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, st));
+    if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), p->sorted, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, st));
     TSB_CUDA(cudaStreamSynchronize(st));
     for (int r = 0; r < V; ++r) {
         const uint32_t i = g[r];

@@ -82,10 +82,11 @@ __global__ void k_fix_ties(const uint32_t* __restrict__ keys, uint32_t* __restri
 }
 
 int launch_sort_depth(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, const double* depth64,
-                      const int32_t* n_visible, int32_t* long_run, int n, uint32_t* scratch, cudaStream_t st) {
+                      const int32_t* n_visible, int32_t* long_run, const uint32_t* key_range, int n,
+                      uint32_t* scratch, cudaStream_t st) {
     if (n <= 0) return 0;
-    int launches = radix_sort32(keys_a, keys_b, vals_a, vals_b, n, scratch, st);
-    k_fix_ties<<<(n / 4 + 256) / 256, 256, 0, st>>>(keys_a, vals_a, depth64, n_visible, long_run);
+    int launches = radix_sort24(keys_a, keys_b, vals_a, vals_b, n, scratch, key_range, st);
+    k_fix_ties<<<(n / 4 + 256) / 256, 256, 0, st>>>(keys_b, vals_b, depth64, n_visible, long_run);
     return launches + 1;
 }
 

@@ -19,7 +19,9 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, Fr
                                                     uint32_t* __restrict__ gidx,
                                                     uint32_t* __restrict__ touched,
                                                     uint2* __restrict__ rect, RecK rec,
-                                                    int32_t* __restrict__ n_visible) {
+                                                    int32_t* __restrict__ n_visible,
+                                                    uint32_t* __restrict__ key_range) {
+    uint32_t kmine = 0xffffffffu, kmaxe = 0u;
     const int gi = blockIdx.x * blockDim.x + threadIdx.x;
     bool vis = false;
     if (gi < S.n) {
@@ -31,6 +33,7 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, Fr
             // depth except inside runs of equal keys (resolved by k_fix_ties).
             depth_key[gi] = __float_as_uint((float)s.depth);
             depth64[gi] = s.depth;
+            kmine = kmaxe = depth_key[gi];
             const int ts = O.ts;
             const int tx0 = s.x0 / ts, tx1 = (s.x1 - 1) / ts;
             const int ty0 = s.y0 / ts, ty1 = (s.y1 - 1) / ts;
@@ -56,17 +59,40 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, Fr
             touched[gi] = 0u;
         }
     }
+    // block-level reduction, then one atomic per block for each of count / min / max
+    __shared__ uint32_t s_cnt[8], s_min[8], s_max[8];
     const unsigned m = __ballot_sync(0xffffffffu, vis);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(n_visible, __popc(m));
+    kmine = __reduce_min_sync(0xffffffffu, kmine);
+    kmaxe = __reduce_max_sync(0xffffffffu, kmaxe);
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        s_cnt[w] = __popc(m);
+        s_min[w] = kmine;
+        s_max[w] = kmaxe;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t c = 0, lo = 0xffffffffu, hi = 0u;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+            c += s_cnt[i];
+            lo = min(lo, s_min[i]);
+            hi = max(hi, s_max[i]);
+        }
+        if (c) {
+            atomicAdd(n_visible, (int)c);
+            atomicMin(&key_range[0], lo);
+            atomicMax(&key_range[1], hi);
+        }
+    }
 }
 
 void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
                        uint32_t* depth_key, double* depth64, uint32_t* gidx, uint32_t* touched, uint2* rect,
-                       RecK rec, int32_t* n_visible, cudaStream_t st) {
+                       RecK rec, int32_t* n_visible, uint32_t* key_range, cudaStream_t st) {
     if (S.n <= 0) return;
     const int bs = 256;
     k_preprocess<<<(S.n + bs - 1) / bs, bs, 0, st>>>(S, C, O, F, depth_key, depth64, gidx, touched, rect, rec,
-                                                      n_visible);
+                                                      n_visible, key_range);
 }
 
 // ---------------------------------------------------------------------------
@@ -82,70 +108,157 @@ struct FixupAcc {
     bool done;
 };
 
-// One batch of up to 32 candidate entries (lane-parallel fp64 evaluation, then
-// an in-order sequential composite exactly as splat.cpp:260-297).
-__device__ __forceinline__ void fixup_batch(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F, int nf,
-                                            int x, int y, bool is_entry, int g, int entry_idx, FixupAcc& a) {
-    const double pcx = x + 0.5, pcy = y + 0.5;
-    bool inc = false;
-    double alpha = 0, coef = 0, depth = 0, sn[2] = {0, 0}, cs[2] = {0, 0};
-    if (is_entry) {
-        Prep64 s;
-        prep64(S, C, O, F, g, s);  // visible by construction
-        if (!(x < s.x0 || x >= s.x1 || y < s.y0 || y >= s.y1)) {
-            const double dx = pcx - s.mean[0], dy = pcy - s.mean[1];
-            const double maha = s.ca * dx * dx + 2.0 * s.cb * dx * dy + s.cc * dy * dy;
-            if (!(maha > O.cut2 || maha < 0.0)) {
-                const double gg = exp(-0.5 * maha);
-                alpha = s.opacity * gg;
-                if (!(alpha < O.alpha_thr)) {
-                    inc = true;
-                    coef = s.coef;
-                    depth = s.depth;
-                    for (int f = 0; f < nf; ++f) sincos(phase_of_depth(s.depth, S.freq[f], S.c), &sn[f], &cs[f]);
+__device__ __forceinline__ Rec64 make_rec64(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F, int g) {
+    Prep64 s;
+    prep64(S, C, O, F, g, s);  // visible by construction
+    Rec64 r;
+    r.m0 = make_double4(s.mean[0], s.mean[1], s.ca, s.cb);
+    r.m1 = make_double4(s.cc, s.opacity, s.coef, s.depth);
+    r.rect = make_int4(s.x0, s.x1, s.y0, s.y1);
+    return r;
+}
+
+// Mark the Gaussians the flagged pixels will visit (their tile lists up to the
+// fp32 termination point + a margin) and queue each once for the record cache.
+__global__ void __launch_bounds__(128) k_fixup_mark(OptK O, FixupK fx, PixK px, int W) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int count = *fx.overflow ? 0 : *px.n_flagged;
+    const int ntiles = O.tiles_x * O.tiles_y;
+    for (int i = warp; i < count; i += nwarps) {
+        const int pix = px.flagged[i] & 0xffffff;
+        const int x = pix % W, y = pix / W;
+        const int tile = (y / O.ts) * O.tiles_x + (x / O.ts);
+        const int limit = (px.last[pix] & 0x7fffffff) + 64;
+        for (int ch = 0; ch < fx.nchunks; ++ch) {
+            const uint4 rg = fx.ranges_all[(size_t)ch * ntiles + tile];
+            if (rg.w || (int)rg.z >= limit) break;
+            const uint32_t end = rg.x + min(rg.y, (uint32_t)(limit - (int)rg.z));
+            for (uint32_t e = rg.x + lane; e < end; e += 32) {
+                const uint32_t g = fx.vals[e];
+                if (atomicExch(&fx.stamp[g], fx.frame_stamp) != fx.frame_stamp) {
+                    const int slot = atomicAdd(fx.work_n, 1);
+                    fx.work[slot] = (int)g;
                 }
             }
         }
     }
-    const unsigned incm = __ballot_sync(0xffffffffu, inc);
-    for (int j = 0; j < 32; ++j) {
-        if (!((incm >> j) & 1u)) continue;
-        const double al = __shfl_sync(0xffffffffu, alpha, j);
-        const double cf = __shfl_sync(0xffffffffu, coef, j);
-        const double dp = __shfl_sync(0xffffffffu, depth, j);
-        const int ei = __shfl_sync(0xffffffffu, entry_idx, j);
-        double s_[2], c_[2];
-        for (int f = 0; f < 2; ++f) {
-            s_[f] = __shfl_sync(0xffffffffu, sn[f], j);
-            c_[f] = __shfl_sync(0xffffffffu, cs[f], j);
-        }
-        ++a.nc;
-        const double w = al * a.T;
-        const double w2 = al * a.T * a.T;
-        const double cq = cf * w2;
-        for (int f = 0; f < nf; ++f) {
-            a.accQ[4 * f + 0] += cq * s_[f];
-            a.accQ[4 * f + 1] += cq * c_[f];
-            a.accQ[4 * f + 2] -= cq * s_[f];
-            a.accQ[4 * f + 3] -= cq * c_[f];
-        }
-        a.SW += w;
-        a.SD += w * dp;
-        a.Tpre = a.T;
-        a.T *= 1.0 - al;
-        if (a.T == 0.0 && a.last_eff < 0) a.last_eff = ei + 1;
-        if (a.T < O.floor_T) {
-            a.processed = ei + 1;
-            a.done = true;
-            return;
-        }
+}
+
+__global__ void __launch_bounds__(128) k_fixup_records(SceneK S, CamK C, OptK O, FrameK F, FixupK fx) {
+    const int n = *fx.work_n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int g = fx.work[i];
+        fx.cache[g] = make_rec64(S, C, O, F, g);
     }
 }
 
+// Per warp: evaluate up to 32 candidate entries in parallel (lane j: entry j).
+// Only the transmittance product T *= (1 - alpha) and the termination test are
+// inherently sequential (they decide the integers); lane 0 runs that chain over
+// the batch's contributors from shared memory, then every lane adds its own
+// weighted terms and the warp reduces them (fp64; summation order differs from
+// the reference only at the 1e-16 level).
+struct FixSlot {
+    double om;     // 1 - alpha (contributors)
+    double Tpre;   // T before this entry (written by lane 0)
+    int contrib;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+    for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+    return v;
+}
+
+__device__ __forceinline__ void fixup_batch(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
+                                            const FixupK& fx, int nf, int x, int y, bool is_entry, int g,
+                                            int entry_idx, FixSlot* slot, FixupAcc& a, int lane) {
+    const double pcx = x + 0.5, pcy = y + 0.5;
+    bool inc = false;
+    double alpha = 0.0, coef = 0.0, depth = 0.0;
+    if (is_entry) {
+        const Rec64 r = fx.stamp[g] == fx.frame_stamp ? fx.cache[g] : make_rec64(S, C, O, F, g);
+        if (!(x < r.rect.x || x >= r.rect.y || y < r.rect.z || y >= r.rect.w)) {
+            const double dx = pcx - r.m0.x, dy = pcy - r.m0.y;
+            const double maha = r.m0.z * dx * dx + 2.0 * r.m0.w * dx * dy + r.m1.x * dy * dy;
+            if (!(maha > O.cut2 || maha < 0.0)) {
+                const double gg = exp(-0.5 * maha);
+                alpha = r.m1.y * gg;
+                if (!(alpha < O.alpha_thr)) {
+                    inc = true;
+                    coef = r.m1.z;
+                    depth = r.m1.w;
+                }
+            }
+        }
+    }
+    slot[lane].contrib = inc ? 1 : 0;
+    slot[lane].om = 1.0 - alpha;
+    __syncwarp();
+    int jterm = 32, le = -1;
+    if (lane == 0) {
+        double T = a.T;
+        for (int j = 0; j < 32; ++j) {
+            if (!slot[j].contrib) continue;
+            slot[j].Tpre = T;
+            T *= slot[j].om;
+            if (T == 0.0 && le < 0) le = j;
+            if (T < O.floor_T) {
+                jterm = j;
+                break;
+            }
+        }
+        a.T = T;
+    }
+    __syncwarp();
+    jterm = __shfl_sync(0xffffffffu, jterm, 0);
+    le = __shfl_sync(0xffffffffu, le, 0);
+    a.T = __shfl_sync(0xffffffffu, a.T, 0);
+    const bool mine = inc && lane <= jterm;
+    double w = 0.0, w2 = 0.0, q[8];
+    for (int c = 0; c < 8; ++c) q[c] = 0.0;
+    if (mine) {
+        const double Tk = slot[lane].Tpre;
+        w = alpha * Tk;
+        w2 = alpha * Tk * Tk;
+        const double cq = coef * w2;
+        for (int f = 0; f < nf; ++f) {
+            double sn, cs;
+            sincos(phase_of_depth(depth, S.freq[f], S.c), &sn, &cs);
+            q[4 * f + 0] = cq * sn;
+            q[4 * f + 1] = cq * cs;
+        }
+    }
+    const unsigned mm = __ballot_sync(0xffffffffu, mine);
+    if (mm) {
+        for (int f = 0; f < nf; ++f) {
+            const double s0 = warp_sum(q[4 * f + 0]), s1 = warp_sum(q[4 * f + 1]);
+            a.accQ[4 * f + 0] += s0;
+            a.accQ[4 * f + 1] += s1;
+            a.accQ[4 * f + 2] -= s0;
+            a.accQ[4 * f + 3] -= s1;
+        }
+        a.SW += warp_sum(w);
+        a.SD += warp_sum(w * depth);
+        a.nc += __popc(mm);
+        const int last_lane = 31 - __clz(mm);
+        a.Tpre = __shfl_sync(0xffffffffu, mine ? slot[lane].Tpre : 0.0, last_lane);
+    }
+    if (le >= 0 && a.last_eff < 0) a.last_eff = __shfl_sync(0xffffffffu, entry_idx, le) + 1;
+    if (jterm < 32) {
+        a.processed = __shfl_sync(0xffffffffu, entry_idx, jterm) + 1;
+        a.done = true;
+    }
+    __syncwarp();
+}
+
 __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, FrameK F, FixupK fx, PixK px, int nf) {
+    __shared__ FixSlot slots[4][32];
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    FixSlot* slot = slots[threadIdx.x >> 5];
     const int count = *fx.overflow ? 0 : *px.n_flagged;
     const int W = C.W, H = C.H;
     const int ntiles = O.tiles_x * O.tiles_y;
@@ -168,13 +281,14 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, FrameK 
                 scan_from = fx.chunk_rank0[ch];
                 break;
             }
-            a.processed = (int)(rg.z + rg.y);
             const uint32_t end = rg.x + rg.y;
             for (uint32_t b = rg.x; b < end && !a.done; b += 32) {
                 const uint32_t e = b + lane;
                 const bool is_e = e < end;
-                fixup_batch(S, C, O, F, nf, x, y, is_e, is_e ? (int)fx.vals[e] : 0, (int)(rg.z + (e - rg.x)), a);
+                fixup_batch(S, C, O, F, fx, nf, x, y, is_e, is_e ? (int)fx.vals[e] : 0, (int)(rg.z + (e - rg.x)),
+                            slot, a, lane);
             }
+            if (!a.done) a.processed = (int)(rg.z + rg.y);
         }
         if (!a.done && scan_from < 0 && fx.binned_end_rank < V) scan_from = fx.binned_end_rank;
         // Rare: the exact composite continues past the binned entries of this tile;
@@ -190,7 +304,7 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, FrameK 
                 cov = x0 / O.ts <= tx && tx <= (x1 - 1) / O.ts && y0 / O.ts <= ty && ty <= (y1 - 1) / O.ts;
             }
             const unsigned cm = __ballot_sync(0xffffffffu, cov);
-            fixup_batch(S, C, O, F, nf, x, y, cov, g, a.processed + __popc(cm & lanes_below), a);
+            fixup_batch(S, C, O, F, fx, nf, x, y, cov, g, a.processed + __popc(cm & lanes_below), slot, a, lane);
             if (!a.done) a.processed += __popc(cm);
         }
         if (lane == 0) {
@@ -211,15 +325,12 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, FrameK 
 
 void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F, const FixupK& fx,
                   const PixK& px, int nf, cudaStream_t st) {
+    cudaMemsetAsync(fx.work_n, 0, sizeof(int), st);
+    k_fixup_mark<<<148 * 2, 128, 0, st>>>(O, fx, px, C.W);
+    k_fixup_records<<<148 * 4, 128, 0, st>>>(S, C, O, F, fx);
     k_fixup<<<148 * 4, 128, 0, st>>>(S, C, O, F, fx, px, nf);
 }
 
-// ---------------------------------------------------------------------------
-// k_chain: per visible Gaussian, chain the 8 screen-space gradients back to the
-// parameters (splat.cpp:551-648) in fp64, then through the trajectory
-// (trainer.cpp:313-314, 329-331), and accumulate into the scene gradient
-// buffer (GroupGrads::add).  Clears the screen-gradient slots it consumed.
-// ---------------------------------------------------------------------------
 // Intermediates the chain needs, recomputed in fp64 with reciprocals instead of
 // divisions (values agree with prep64 to a few ulp; the chain has no decisions
 // except the frustum-clamp flags and the 0 < r < 1 gate, which use the same

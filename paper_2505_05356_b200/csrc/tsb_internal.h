@@ -121,7 +121,14 @@ __host__ __device__ inline int ch_T(int nf) { return 4 * nf + 3; }
 // tsb_geom.cu (fp64, compiled without FMA contraction)
 void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
                        uint32_t* depth_key, double* depth64, uint32_t* gidx, uint32_t* touched, uint2* rect,
-                       RecK rec, int32_t* n_visible, cudaStream_t st);
+                       RecK rec, int32_t* n_visible, uint32_t* key_range, cudaStream_t st);
+// fp64 record cache for the fix-up (valid when stamp[g] == frame stamp).
+struct Rec64 {
+    double4 m0;  // mean x, mean y, conic a, conic b
+    double4 m1;  // conic c, opacity, coef, depth
+    int4 rect;   // x0, x1, y0, y1
+};
+
 struct FixupK {
     const uint4* ranges_all;  // [nchunks][ntiles] (start, len, cum, skipped)
     int nchunks;
@@ -132,6 +139,11 @@ struct FixupK {
     const uint2* rect;
     const int32_t* n_visible;
     const int32_t* overflow;
+    int* stamp;        // [n] frame stamp of the cached record
+    int frame_stamp;
+    int* work;         // [n] Gaussians queued for the record cache
+    int* work_n;
+    Rec64* cache;      // [n]
 };
 void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F, const FixupK& fx,
                   const PixK& px, int nf, cudaStream_t st);
@@ -143,11 +155,16 @@ void launch_chain(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F
 size_t radix_sort_scratch_words(int n);
 int radix_sort32(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch,
                  cudaStream_t st);
+// 3 passes over keys compressed to 23 bits with the device-side key range
+// (range[0] = min, range[1] = max); result in (keys_b, vals_b).
+int radix_sort24(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch,
+                 const uint32_t* range, cudaStream_t st);
 // Global (depth, index) order: stable sort on fp32 depth keys, then exact fp64
 // re-sort of equal-key runs (runs longer than 64 set *long_run; the host then
 // runs launch_sort_depth64).  Results in (keys_a, vals_a).
 int launch_sort_depth(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, const double* depth64,
-                      const int32_t* n_visible, int32_t* long_run, int n, uint32_t* scratch, cudaStream_t st);
+                      const int32_t* n_visible, int32_t* long_run, const uint32_t* key_range, int n,
+                      uint32_t* scratch, cudaStream_t st);  // result in (keys_b, vals_b)
 int launch_sort_depth64(const double* depth64, const uint32_t* touched, uint32_t* keys_a, uint32_t* keys_b,
                         uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch, cudaStream_t st);
 void launch_bin_chunk(const BinK& B, cudaStream_t st);

@@ -37,9 +37,11 @@ struct Eval {
     float dx, dy, p, q, maha, g, alpha;
 };
 
-__device__ __forceinline__ void eval_entry(const float4& A, const float4& B, float pcx, float pcy, Eval& e) {
-    e.dx = __fsub_rn(__fsub_rn(pcx, A.x), A.z);
-    e.dy = __fsub_rn(__fsub_rn(pcy, A.y), A.w);
+// A (staged) = (mean.x - block origin, mean.y - block origin, error scale x, error scale y);
+// (lx, ly) = pixel centre relative to the block origin (exact).
+__device__ __forceinline__ void eval_entry(const float4& A, const float4& B, float lx, float ly, Eval& e) {
+    e.dx = __fsub_rn(lx, A.x);
+    e.dy = __fsub_rn(ly, A.y);
     e.p = __fmaf_rn(B.x, e.dx, __fmul_rn(B.y, e.dy));
     e.q = __fmul_rn(B.z, e.dy);
     e.maha = __fmaf_rn(e.p, e.p, __fmul_rn(e.q, e.q));
@@ -58,14 +60,24 @@ constexpr float kCoarseMaha = 1e-3f;       // relative window that triggers the 
 constexpr float kCoarseAlpha = 1e-4f;
 constexpr float kEx2Err = 2.5e-7f;         // ex2.approx.ftz.f32 relative error bound (+ margin)
 
-// |fl32(maha) - maha_exact| bound from the rounding of mean offset, L, dx, dy, p, q.
+// |fl32(maha) - maha_exact| bound from the rounding of mean offsets (A.z, A.w carry
+// |mean - rect origin| + |mean - block origin|), L, dx, dy, p, q.
 __device__ __forceinline__ float maha_err_bound(const float4& A, const float4& B, const Eval& e) {
-    const float ddx = kEps * (fabsf(A.z) + fabsf(e.dx));
-    const float ddy = kEps * (fabsf(A.w) + fabsf(e.dy));
+    const float ddx = kEps * (A.z + fabsf(e.dx));
+    const float ddy = kEps * (A.w + fabsf(e.dy));
     const float a = fabsf(B.x * e.dx), b = fabsf(B.y * e.dy);
     const float dp = kEps * (a + 2.f * b + fabsf(e.p)) + fabsf(B.x) * ddx + fabsf(B.y) * ddy;
     const float dq = 2.f * kEps * fabsf(e.q) + fabsf(B.z) * ddy;
     return 2.f * fabsf(e.p) * dp + 2.f * fabsf(e.q) * dq + kEps * (e.q * e.q + e.maha);
+}
+
+// Stage a record's mean relative to the block origin: (rect origin - block origin)
+// is an exact small integer, so one rounding is added; its size enters the
+// error scale used by maha_err_bound.
+__device__ __forceinline__ float4 stage_A(const float4& a, float ox, float oy) {
+    const float mx = __fadd_rn(__fsub_rn(a.x, ox), a.z);
+    const float my = __fadd_rn(__fsub_rn(a.y, oy), a.w);
+    return make_float4(mx, my, fabsf(a.z) + fabsf(mx), fabsf(a.w) + fabsf(my));
 }
 
 template <int NF>
@@ -98,7 +110,8 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
     const int x = (tile % O.tiles_x) * O.ts + lx, y = (tile / O.tiles_x) * O.ts + ly;
     const bool active = lx < O.ts && ly < O.ts && x < W && y < H;
     const uint4 rg = ck.ranges[tile];  // (start, len, cum, -)
-    const float pcx = (float)x + 0.5f, pcy = (float)y + 0.5f;
+    const float ox = (float)(x - (tid % kTile)), oy = (float)(y - (tid / kTile));  // block origin
+    const float pcx = (float)(tid % kTile) + 0.5f, pcy = (float)(tid / kTile) + 0.5f;
     const size_t HW = (size_t)W * H, o = active ? (size_t)y * W + x : 0;
 
     float T = 1.f, Tpre = 1.f, SW = 0.f, SD = 0.f, errT = 0.f;
@@ -134,7 +147,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
             const uint32_t e = b + tid;
             if (e < end) {
                 const uint32_t r = vals[e];
-                sm.A[tid] = rec.A[r];
+                sm.A[tid] = stage_A(rec.A[r], ox, oy);
                 sm.B[tid] = rec.B[r];
                 sm.C[tid] = rec.C[r];
                 if (NF > 1) sm.D[tid] = rec.D[r];
@@ -147,8 +160,11 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
                     Eval ev;
                     eval_entry(A, B, pcx, pcy, ev);
                     const float dm = ev.maha - cut2;
-                    if (fabsf(dm) <= coarseM && fabsf(dm) <= 2.f * maha_err_bound(A, B, ev)) flag |= 1;
-                    if (dm > 0.f) continue;
+                    if (dm > coarseM) continue;  // clearly outside (most entries)
+                    if (dm >= -coarseM) {
+                        if (fabsf(dm) <= 2.f * maha_err_bound(A, B, ev)) flag |= 1;
+                        if (dm > 0.f) continue;
+                    }
                     eval_alpha(B, ev);
                     const float da = ev.alpha - thr;
                     if (fabsf(da) <= coarseA) {
@@ -331,7 +347,8 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
     const int lx = (sb % O.sub) * kTile + (tid % kTile), ly = (sb / O.sub) * kTile + (tid / kTile);
     const int x = (tile % O.tiles_x) * O.ts + lx, y = (tile / O.tiles_x) * O.ts + ly;
     const bool active = lx < O.ts && ly < O.ts && x < W && y < H;
-    const float pcx = (float)x + 0.5f, pcy = (float)y + 0.5f;
+    const float ox = (float)(x - (tid % kTile)), oy = (float)(y - (tid / kTile));  // block origin
+    const float pcx = (float)(tid % kTile) + 0.5f, pcy = (float)(tid / kTile) + 0.5f;
     const size_t HW = (size_t)W * H, o = active ? (size_t)y * W + x : 0;
 
     int last = 0;
@@ -396,7 +413,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
             if (tid < nb) {
                 const uint32_t r = vals[b + tid];
                 srank[tid] = r;
-                sm.A[tid] = rec.A[r];
+                sm.A[tid] = stage_A(rec.A[r], ox, oy);
                 sm.B[tid] = rec.B[r];
                 sm.C[tid] = rec.C[r];
                 if (NF > 1) sm.D[tid] = rec.D[r];

@@ -43,14 +43,30 @@ __device__ __forceinline__ unsigned peers8(uint32_t d, bool valid) {
 // All four digit histograms in one pass.  Per-warp sub-histograms; the lanes that
 // share lane 0's digit (the common case for the high, low-entropy digits) are
 // counted with one atomic by lane 0, the others add their own.
+// Keys are compressed to 23 significant bits: k' = (k - kmin) >> shift, with kmin and
+// shift from the key range the preprocess recorded (range[0] = min, range[1] = max of
+// the keys that are not 0xffffffff).  Culled keys (0xffffffff) map to 0xffffff.
+__device__ __forceinline__ void key_xform(const uint32_t* range, uint32_t& kmin, uint32_t& shift) {
+    kmin = range[0];
+    const uint32_t span = range[1] >= range[0] ? range[1] - range[0] : 0u;
+    const int bits = span ? 32 - __clz(span) : 0;
+    shift = bits > 23 ? (uint32_t)(bits - 23) : 0u;  // visible keys < 2^23 < the culled sentinel
+}
+__device__ __forceinline__ uint32_t key24(uint32_t k, uint32_t kmin, uint32_t shift) {
+    return k == 0xffffffffu ? 0xffffffu : ((k - kmin) >> shift);
+}
+
 __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint32_t* __restrict__ keys, int n,
-                                                            uint32_t* __restrict__ hist /* [4][256] */,
-                                                            uint32_t* __restrict__ status, int status_words) {
-    __shared__ uint32_t h[kSortWarps][4][256];
+                                                            uint32_t* __restrict__ hist /* [3][256] */,
+                                                            uint32_t* __restrict__ status, int status_words,
+                                                            const uint32_t* __restrict__ range) {
+    uint32_t kmin, kshift;
+    key_xform(range, kmin, kshift);
+    __shared__ uint32_t h[kSortWarps][3][256];
     // clear the look-back status words of all four passes (used only after this kernel)
     for (int i = blockIdx.x * kSortThreads + threadIdx.x; i < status_words; i += gridDim.x * kSortThreads)
         status[i] = 0u;
-    for (int i = threadIdx.x; i < kSortWarps * 4 * 256; i += kSortThreads) (&h[0][0][0])[i] = 0u;
+    for (int i = threadIdx.x; i < kSortWarps * 3 * 256; i += kSortThreads) (&h[0][0][0])[i] = 0u;
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int n4 = n >> 2;
@@ -72,9 +88,11 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint32_t* __re
             }
         }
 #pragma unroll
+        for (int j = 0; j < 4; ++j) kk[j] = key24(kk[j], kmin, kshift);
+#pragma unroll
         for (int j = 0; j < 4; ++j) {
 #pragma unroll
-            for (int p = 0; p < 4; ++p) {
+            for (int p = 0; p < 3; ++p) {
                 const uint32_t d = (kk[j] >> (8 * p)) & 255u;
                 const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
                 const bool v0 = __shfl_sync(0xffffffffu, valid[j], 0);
@@ -85,7 +103,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint32_t* __re
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < 4 * 256; i += kSortThreads) {
+    for (int i = threadIdx.x; i < 3 * 256; i += kSortThreads) {
         uint32_t v = 0;
         for (int w = 0; w < kSortWarps; ++w) v += (&h[w][0][0])[i];
         if (v) atomicAdd(&hist[i], v);
@@ -93,7 +111,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint32_t* __re
 }
 
 __global__ void k_sort_scan(uint32_t* __restrict__ hist /* in: counts, out: exclusive offsets */) {
-    // 4 warps, one per digit pass; each lane owns 8 consecutive bins
+    // one warp per digit pass; each lane owns 8 consecutive bins
     const int p = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t* h = hist + 256 * p;
     uint32_t v[8], s = 0;
@@ -122,7 +140,8 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint32_t* __res
                                                            uint32_t* __restrict__ keys_out,
                                                            uint32_t* __restrict__ vals_out, int n, int shift,
                                                            const uint32_t* __restrict__ digit_off,
-                                                           uint32_t* status, uint32_t* tile_ticket) {
+                                                           uint32_t* status, uint32_t* tile_ticket,
+                                                           const uint32_t* __restrict__ range) {
     __shared__ uint32_t s_tile;
     __shared__ uint32_t warp_cnt[kSortWarps][256];  // counts, then exclusive offsets across warps
     __shared__ uint32_t block_start[256];            // exclusive scan over digits of the tile counts
@@ -146,6 +165,12 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint32_t* __res
         k[i] = valid ? keys_in[idx] : 0u;
         v[i] = valid ? vals_in[idx] : 0u;
         lr[i] = valid ? 0u : 0xffffffffu;
+    }
+    if (range) {  // first pass: compress the raw fp32 keys to 24 bits
+        uint32_t kmin, kshift;
+        key_xform(range, kmin, kshift);
+#pragma unroll
+        for (int i = 0; i < kSortIPT; ++i) k[i] = key24(k[i], kmin, kshift);
     }
     // stable rank within the warp (slot order, then lane order == item order)
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -193,14 +218,25 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint32_t* __res
         global_base[d] = digit_off[d];
     } else {
         atomicExch(&st[d], kFlagAgg | total);
+        // look back 8 predecessors per round trip: sum aggregates until an inclusive prefix
         uint32_t prefix = 0;
-        for (int t = tile - 1; t >= 0; --t) {
-            uint32_t s;
-            do {
-                s = ld_volatile(status + (size_t)t * 256 + d);
-            } while ((s & ~kCountMask) == 0u);
-            prefix += s & kCountMask;
-            if ((s & ~kCountMask) == kFlagInc) break;
+        int t = tile - 1;
+        bool found = false;
+        while (!found) {
+            uint32_t sv[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) sv[j] = t - j >= 0 ? ld_volatile(status + (size_t)(t - j) * 256 + d) : kFlagInc;
+            int j = 0;
+            for (; j < 8; ++j) {
+                const uint32_t f = sv[j] & ~kCountMask;
+                if (f == 0u) break;  // not published yet: re-poll from here
+                prefix += sv[j] & kCountMask;
+                if (f == kFlagInc) {
+                    found = true;
+                    break;
+                }
+            }
+            t -= j;
         }
         atomicExch(&st[d], kFlagInc | (prefix + total));
         global_base[d] = digit_off[d] + prefix;
@@ -232,9 +268,47 @@ size_t radix_sort_scratch_words(int n) {
     return (size_t)4 * 256 + 4 + (size_t)4 * tiles * 256;  // hist/offsets, tickets, status per pass
 }
 
+// 24-bit compressed keys, 3 passes; the output keys are the compressed keys (equal
+// compressed keys stay in input order -- callers re-sort such runs exactly).
+int radix_sort24(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch,
+                 const uint32_t* range, cudaStream_t st) {
+    if (n <= 0) return 0;
+    const int tiles = (n + kSortTile - 1) / kSortTile;
+    uint32_t* hist = scratch;
+    uint32_t* tickets = scratch + 4 * 256;
+    uint32_t* status = tickets + 4;
+    cudaMemsetAsync(scratch, 0, sizeof(uint32_t) * (4 * 256 + 4), st);
+    const int hgrid = max(1, min(148 * 2, (n / 4 + kSortThreads - 1) / kSortThreads));
+    k_sort_hist<<<hgrid, kSortThreads, 0, st>>>(keys_a, n, hist, status, 3 * 256 * tiles, range);
+    k_sort_scan<<<1, 96, 0, st>>>(hist);
+    // 3 passes ping-pong a->b->a->b; finish in b, then the caller uses b
+    k_onesweep<<<tiles, kSortThreads, 0, st>>>(keys_a, vals_a, keys_b, vals_b, n, 0, hist, status, tickets, range);
+    k_onesweep<<<tiles, kSortThreads, 0, st>>>(keys_b, vals_b, keys_a, vals_a, n, 8, hist + 256,
+                                               status + (size_t)256 * tiles, tickets + 1, nullptr);
+    k_onesweep<<<tiles, kSortThreads, 0, st>>>(keys_a, vals_a, keys_b, vals_b, n, 16, hist + 512,
+                                               status + (size_t)512 * tiles, tickets + 2, nullptr);
+    return 5;
+}
+
 // keys/vals: double buffers; result ends in (keys_b, vals_b) after 4 passes
 // when the pass count is even it ends in *_a -- we always do 4 passes and
 // return the buffer holding the result.
+// Full 32-bit keys, 4 passes (exact 64-bit fallback uses two of these).  Result in (keys_a, vals_a).
+__global__ void k_sort_hist32(const uint32_t* __restrict__ keys, int n, uint32_t* __restrict__ hist,
+                              uint32_t* __restrict__ status, int status_words) {
+    __shared__ uint32_t h[4][256];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < status_words; i += gridDim.x * blockDim.x) status[i] = 0u;
+    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&h[0][0])[i] = 0u;
+    __syncthreads();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t k = keys[i];
+        for (int p = 0; p < 4; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255u], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x)
+        if ((&h[0][0])[i]) atomicAdd(&hist[i], (&h[0][0])[i]);
+}
+
 int radix_sort32(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch,
                  cudaStream_t st) {
     if (n <= 0) return 0;
@@ -243,17 +317,16 @@ int radix_sort32(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t*
     uint32_t* tickets = scratch + 4 * 256;
     uint32_t* status = tickets + 4;
     cudaMemsetAsync(scratch, 0, sizeof(uint32_t) * (4 * 256 + 4), st);
-    const int hgrid = max(1, min(148 * 2, (n / 4 + kSortThreads - 1) / kSortThreads));
-    k_sort_hist<<<hgrid, kSortThreads, 0, st>>>(keys_a, n, hist, status, 4 * 256 * tiles);
+    k_sort_hist32<<<148 * 2, 256, 0, st>>>(keys_a, n, hist, status, 4 * 256 * tiles);
     k_sort_scan<<<1, 128, 0, st>>>(hist);
     uint32_t *ki = keys_a, *ko = keys_b, *vi = vals_a, *vo = vals_b;
     for (int p = 0; p < 4; ++p) {
         k_onesweep<<<tiles, kSortThreads, 0, st>>>(ki, vi, ko, vo, n, 8 * p, hist + 256 * p,
-                                                   status + (size_t)p * 256 * tiles, tickets + p);
+                                                   status + (size_t)p * 256 * tiles, tickets + p, nullptr);
         uint32_t* t = ki; ki = ko; ko = t;
         t = vi; vi = vo; vo = t;
     }
-    return 6;  // kernels launched; result is back in (keys_a, vals_a)
+    return 6;
 }
 
 }  // namespace tsb

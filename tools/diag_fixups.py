@@ -20,3 +20,6 @@ out = rp.outputs()
 print("after fixup n_contrib mismatches:", int((out["n_contrib"] != ref["n_contrib"]).sum()))
 T = ref["transmittance"].ravel()[pix]
 print("T/floor of T-flagged pixels (quantiles):", np.quantile(T[(why & 4) > 0] / 1e-4, [0, .1, .5, .9, 1]) if (why & 4).any() else None)
+npr = ref["n_processed"].ravel()[pix]
+print("walk length (entries) of flagged pixels: quantiles", np.quantile(npr, [0, .5, .9, .99, 1]))
+print("all pixels walk length quantiles", np.quantile(ref["n_processed"], [.5, .9, .99, 1]))
