@@ -124,8 +124,10 @@ namespace {
 constexpr int kBinThreads = 128;  // one CTA per segment; all threads share a batch's tiles
 constexpr int kSmemTiles = 8192;  // per-CTA shared-memory tile counters up to this many tiles
 
+// Tiles whose pixels have all terminated are not binned again.  No tile can be
+// finished before the first chunk's raster, so chunk 0 skips the (global) check.
 __device__ __forceinline__ bool tile_done(const BinK& B, int t) {
-    return B.skip_done && B.tile_blocks_done[t] >= B.blocks_per_tile;
+    return B.skip_done && B.chunk > 0 && B.tile_blocks_done[t] >= B.blocks_per_tile;
 }
 
 struct Box {
