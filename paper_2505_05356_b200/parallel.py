@@ -41,19 +41,23 @@ class FrameShardedTrainer:
         self.adam = adam
         self.comm, self.rank, self.world = comm, rank, world
         self.channel_weight = list(channel_weight or [0.25] * (4 * scene.n_freq))
-        self.rp = RenderPass(ctx)
+        # two passes (two streams): frame i's backward overlaps frame i+1's preprocess/sort/binning;
+        # gradient writes are serialised by the scene's event chain inside the library
+        self.passes = [RenderPass(ctx), RenderPass(ctx)]
+        self.rp = self.passes[0]
 
     def step(self, frames: Sequence, target: Callable[[int], object]) -> None:
         """frames: the iteration's (key, w) frames (all ranks pass the same list);
         target(i) -> host array (4*n_freq, H, W) or an int device pointer for frame i."""
-        for i in shard_indices(len(frames), self.rank, self.world):
-            self.rp.prepare(self.scene, self.camera, self.options, frames[i])
+        for k, i in enumerate(shard_indices(len(frames), self.rank, self.world)):
+            rp = self.passes[k % 2]
+            rp.prepare(self.scene, self.camera, self.options, frames[i])
             t = target(i)
             if isinstance(t, int):
-                self.rp.forward_loss(None, self.channel_weight, sync=False, device_ptr=t)
+                rp.forward_loss(None, self.channel_weight, sync=False, device_ptr=t)
             else:
-                self.rp.forward_loss(t, self.channel_weight, sync=False)
-            self.rp.backward()
+                rp.forward_loss(t, self.channel_weight, sync=False)
+            rp.backward()
         if self.comm is not None and self.world > 1:
             self.scene.allreduce_grads(self.comm)
         self.scene.adam_step(self.lr, self.adam)
