@@ -77,7 +77,18 @@ __global__ void k_fix_ties(const uint32_t* __restrict__ keys, uint32_t* __restri
     for (int j = 0; j < 4; ++j) {
         const int r = r0 + j;
         if (r >= V - 1) break;
-        if (kk[j + 2] == kk[j + 1] && kk[j] != kk[j + 1]) sort_run(keys, vals, depth64, r, V, long_run);
+        if (!(kk[j + 2] == kk[j + 1] && kk[j] != kk[j + 1])) continue;  // not a run start
+        const bool len2 = r + 2 >= V || keys[r + 2] != kk[j + 1];
+        if (len2) {  // the common case: a compare-exchange in registers
+            const uint32_t g0 = vals[r], g1 = vals[r + 1];
+            const double d0 = depth64[g0], d1 = depth64[g1];
+            if (d0 > d1 || (d0 == d1 && g0 > g1)) {
+                vals[r] = g1;
+                vals[r + 1] = g0;
+            }
+        } else {
+            sort_run(keys, vals, depth64, r, V, long_run);
+        }
     }
 }
 
