@@ -165,6 +165,12 @@ typedef struct {
  * densify statistic (trainer.cpp:381-384); clears the gradients afterwards. */
 int tsb_scene_adam_step(tsb_scene* s, const tsb_adam_config* cfg);
 
+/* AdamState::step on one flat parameter vector (trainer.cpp:18-31): m, v, params
+ * updated in place; t is the step count after increment.  `where`: pointers are
+ * host (copied through the device) or device memory. */
+int tsb_adam_step_flat(tsb_ctx* ctx, int where, float* params, const float* grads, float* m, float* v, size_t n,
+                       int64_t t, double lr, double beta1, double beta2, double eps);
+
 /* ---- render pass (RenderPass, splat.hpp:97-117) ------------------------- */
 /* A pass is a reusable per-frame workspace: prepare() == the RenderPass ctor
  * (prepare + depth sort + build_tiles, splat.cpp:90-200). */

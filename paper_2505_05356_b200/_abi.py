@@ -88,6 +88,8 @@ SIGNATURES = {
     "tsb_scene_get_adam_state": (C.c_int, [_vp, _fp, _fp]),
     "tsb_scene_get_densify_stat": (C.c_int, [_vp, _fp, _lp]),
     "tsb_scene_adam_step": (C.c_int, [_vp, C.POINTER(AdamConfig)]),
+    "tsb_adam_step_flat": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, C.c_size_t, C.c_int64, C.c_double,
+                                      C.c_double, C.c_double, C.c_double]),
     "tsb_pass_create": (C.c_int, [_vp, C.POINTER(_vp)]),
     "tsb_pass_destroy": (None, [_vp]),
     "tsb_pass_prepare": (C.c_int, [_vp, _vp, C.POINTER(Camera), C.POINTER(RenderOptions), C.POINTER(Frame)]),

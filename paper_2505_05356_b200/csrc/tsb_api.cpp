@@ -498,6 +498,40 @@ int tsb_scene_adam_step(tsb_scene* s, const tsb_adam_config* cfg) {
     return TSB_OK;
 }
 
+int tsb_adam_step_flat(tsb_ctx* ctx, int where, float* params, const float* grads, float* m, float* v, size_t n,
+                       int64_t t, double lr, double beta1, double beta2, double eps) {
+    if (!ctx || (n && (!params || !grads || !m || !v))) return fail(TSB_ERR_INVALID, "adam_step: null argument");
+    if (t < 1) return fail(TSB_ERR_INVALID, "adam_step: step count must be >= 1");
+    if (n == 0) return TSB_OK;
+    TSB_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const double bc1 = 1.0 - std::pow(beta1, (double)t), bc2 = 1.0 - std::pow(beta2, (double)t);
+    if (where == TSB_DEVICE) {
+        launch_adam_flat(params, grads, m, v, n, lr, beta1, beta2, eps, bc1, bc2, st);
+        ctx->launches++;
+        TSB_CHECK_LAUNCH();
+        return TSB_OK;
+    }
+    if (where != TSB_HOST) return fail(TSB_ERR_INVALID, "bad memory kind");
+    float* d = nullptr;
+    int rc = dev_alloc(&d, 4 * n);
+    if (rc) return rc;
+    const size_t b = n * sizeof(float);
+    cudaMemcpyAsync(d, params, b, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d + n, grads, b, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d + 2 * n, m, b, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d + 3 * n, v, b, cudaMemcpyHostToDevice, st);
+    launch_adam_flat(d, d + n, d + 2 * n, d + 3 * n, n, lr, beta1, beta2, eps, bc1, bc2, st);
+    ctx->launches++;
+    cudaMemcpyAsync(params, d, b, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(m, d + 2 * n, b, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(v, d + 3 * n, b, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    cudaFree(d);
+    if (e != cudaSuccess) return fail(TSB_ERR_CUDA, std::string("adam_step: ") + cudaGetErrorString(e));
+    return TSB_OK;
+}
+
 // ---------------------------------------------------------------------------
 // render pass
 // ---------------------------------------------------------------------------

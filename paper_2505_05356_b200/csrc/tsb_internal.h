@@ -187,4 +187,7 @@ void launch_adam(float4* params, float4* grads, float4* m, float4* v, int n, int
                  const double* lr4 /* host [narrays*4] */, double beta1, double beta2, double eps,
                  double bc1, double bc2, float* densify, cudaStream_t st);
 
+void launch_adam_flat(float* p, const float* g, float* m, float* v, size_t n, double lr, double b1, double b2,
+                      double eps, double bc1, double bc2, cudaStream_t st);
+
 }  // namespace tsb

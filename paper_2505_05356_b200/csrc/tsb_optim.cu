@@ -7,6 +7,8 @@
 // (trainer.cpp:381-384) and the gradient clear ride along in the same pass.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "tsb_internal.h"
 
 namespace tsb {
@@ -44,11 +46,12 @@ struct LrTable {
 //   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;  p -= (lr/bc1) m / (sqrt(v/bc2) + eps)
 __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ P, float4* __restrict__ G,
                                               float4* __restrict__ M, float4* __restrict__ V, int n, int narrays,
-                                              LrTable lr, float b1, float b2, float eps, float inv_bc2,
-                                              float* __restrict__ densify) {
+                                              LrTable lr, float b1, float b2, float c1, float c2, float eps,
+                                              float inv_bc2, float* __restrict__ densify) {
+    // c1 = 1 - beta1, c2 = 1 - beta2 are formed in double on the host: 1 - fp32(0.999)
+    // would carry a 1.3e-5 relative error into every second moment.
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const float c1 = 1.f - b1, c2 = 1.f - b2;
     for (int a = 0; a < narrays; ++a) {
         const size_t k = (size_t)a * n + i;
         const float4 g4 = G[k];
@@ -77,7 +80,30 @@ void launch_adam(float4* params, float4* grads, float4* m, float4* v, int n, int
     LrTable t;
     for (int i = 0; i < kMaxArrays * 4; ++i) t.lr_bc1[i] = i < narrays * 4 ? (float)(lr4[i] / bc1) : 0.f;
     k_adam<<<(n + 255) / 256, 256, 0, st>>>(params, grads, m, v, n, narrays, t, (float)beta1, (float)beta2,
-                                            (float)eps, (float)(1.0 / bc2), densify);
+                                            (float)(1.0 - beta1), (float)(1.0 - beta2), (float)eps,
+                                            (float)(1.0 / bc2), densify);
+}
+
+// AdamState::step on a flat vector (trainer.cpp:18-31).
+__global__ void k_adam_flat(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                            float* __restrict__ v, size_t n, float lr_bc1, float b1, float b2, float c1, float c2,
+                            float eps, float inv_bc2) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const float gi = g[i];
+        const float mi = b1 * m[i] + c1 * gi;
+        const float vi = b2 * v[i] + c2 * (gi * gi);
+        m[i] = mi;
+        v[i] = vi;
+        p[i] -= lr_bc1 * (mi / (sqrtf(vi * inv_bc2) + eps));
+    }
+}
+
+void launch_adam_flat(float* p, const float* g, float* m, float* v, size_t n, double lr, double b1, double b2,
+                      double eps, double bc1, double bc2, cudaStream_t st) {
+    if (n == 0) return;
+    const int grid = (int)std::min<size_t>((n + 255) / 256, 148 * 8);
+    k_adam_flat<<<grid, 256, 0, st>>>(p, g, m, v, n, (float)(lr / bc1), (float)b1, (float)b2, (float)(1.0 - b1),
+                                      (float)(1.0 - b2), (float)eps, (float)(1.0 / bc2));
 }
 
 }  // namespace tsb
