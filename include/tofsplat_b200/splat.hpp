@@ -98,7 +98,7 @@ struct Gaussian {
 struct CanonicalScene {
     std::vector<Gaussian> gaussians;
     std::array<double, 4> bg_quad{0, 0, 0, 0};
-    int sh_degree = 0;  // the B200 path evaluates degree-0 reflectivity
+    int sh_degree = 0;  // 0..3: reflectivity SH degree evaluated on the GPU
     ToFConfig tof;
     int size() const { return static_cast<int>(gaussians.size()); }
 };
@@ -168,7 +168,7 @@ public:
         tsb_scene_desc d{};
         d.n = n;
         d.n_keyframes = 0;
-        d.sh_degree = 0;
+        d.sh_degree = in.scene->sh_degree;
         d.n_freq = 1;
         d.frequency[0] = in.scene->tof.modulation_frequency;
         d.source_intensity = in.scene->tof.source_intensity;
@@ -189,6 +189,12 @@ public:
         }
         tsb_check(tsb_scene_set_params(s, TSB_HOST, pos.data(), ls.data(), rot.data(), op.data(), refl.data(),
                                        nullptr));
+        if (d.sh_degree > 0) {
+            std::vector<float> sh(16 * (size_t)n);
+            for (int i = 0; i < n; ++i)
+                for (int k = 0; k < 16; ++k) sh[16 * (size_t)i + k] = (float)in.scene->gaussians[i].reflectivity_sh[k];
+            tsb_check(tsb_scene_set_sh(s, TSB_HOST, sh.data()));
+        }
         tsb_pass* p = nullptr;
         tsb_check(tsb_pass_create(ctx, &p));
         pass_.reset(p);
@@ -255,6 +261,12 @@ public:
             g.d_reflectivity_sh(0, i) = drf[i];
         }
         for (int k = 0; k < 4; ++k) g.d_bg_quad[k] = dbg[k];
+        if (in_.scene->sh_degree > 0) {
+            std::vector<float> dsh(16 * (size_t)n);
+            tsb_check(tsb_scene_get_sh(scene_.get(), dsh.data(), 1));
+            for (int i = 0; i < n; ++i)
+                for (int k = 0; k < 16; ++k) g.d_reflectivity_sh(k, i) = dsh[16 * (size_t)i + k];
+        }
         return g;
     }
 

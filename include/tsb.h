@@ -150,6 +150,11 @@ int tsb_scene_get_grads(tsb_scene* s, float* d_position, float* d_log_scale, flo
                         float* d_opacity_logit, float* d_reflectivity_dc, float* d_motion,
                         double* d_bg_quad, double* loss);
 int tsb_scene_zero_grads(tsb_scene* s);
+/* View-dependent reflectivity (sh_degree 1..3; sh.hpp:26-50, splat.cpp:163-165): all 16
+ * reflectivity SH coefficients per Gaussian, [n][16] (coefficient 0 == reflectivity_dc).
+ * tsb_scene_get_sh returns the parameters (grads = 0) or their accumulated gradients (grads = 1). */
+int tsb_scene_set_sh(tsb_scene* s, int where, const float* refl_sh);
+int tsb_scene_get_sh(tsb_scene* s, float* refl_sh, int grads);
 /* Adam moments (AdamState m_/v_, trainer.cpp:18-31), same layout as the params. */
 int tsb_scene_get_adam_state(tsb_scene* s, float* m_position, float* v_position);
 /* Densification statistic sum_i ||dL/dx_canon,i|| (trainer.cpp:381-384), n floats. */

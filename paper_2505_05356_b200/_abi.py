@@ -85,6 +85,8 @@ SIGNATURES = {
     "tsb_scene_get_params": (C.c_int, [_vp, _fp, _fp, _fp, _fp, _fp, _fp]),
     "tsb_scene_get_grads": (C.c_int, [_vp, _fp, _fp, _fp, _fp, _fp, _fp, _dp, _dp]),
     "tsb_scene_zero_grads": (C.c_int, [_vp]),
+    "tsb_scene_set_sh": (C.c_int, [_vp, C.c_int, _vp]),
+    "tsb_scene_get_sh": (C.c_int, [_vp, _fp, C.c_int]),
     "tsb_scene_get_adam_state": (C.c_int, [_vp, _fp, _fp]),
     "tsb_scene_get_densify_stat": (C.c_int, [_vp, _fp, _lp]),
     "tsb_scene_adam_step": (C.c_int, [_vp, C.POINTER(AdamConfig)]),

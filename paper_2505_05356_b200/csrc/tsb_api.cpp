@@ -280,8 +280,6 @@ int tsb_scene_create(tsb_ctx* ctx, const tsb_scene_desc* d, tsb_scene** out) {
     if (d->n_keyframes < 0 || d->n_keyframes == 1 || d->n_keyframes > kMaxKeyframes)
         return fail(TSB_ERR_INVALID, "scene: n_keyframes must be 0 or in [2, 16]");
     if (d->sh_degree < 0 || d->sh_degree > 3) return fail(TSB_ERR_INVALID, "scene: sh_degree must be in [0, 3]");
-    if (d->sh_degree != 0)
-        return fail(TSB_ERR_UNSUPPORTED, "scene: only sh_degree 0 reflectivity is implemented on the B200 path");
     if (d->n_freq < 1 || d->n_freq > 2) return fail(TSB_ERR_INVALID, "scene: n_freq must be 1 or 2");
     for (int f = 0; f < d->n_freq; ++f)
         if (!(d->frequency[f] > 0.0)) return fail(TSB_ERR_INVALID, "scene: modulation frequency must be > 0");
@@ -291,7 +289,7 @@ int tsb_scene_create(tsb_ctx* ctx, const tsb_scene_desc* d, tsb_scene** out) {
     tsb_scene* s = new tsb_scene();
     s->ctx = ctx;
     s->d = *d;
-    s->narrays = 3 + d->n_keyframes;
+    s->narrays = 3 + d->n_keyframes + (d->sh_degree > 0 ? 4 : 0);
     const size_t nel = (size_t)s->narrays * (size_t)std::max(d->n, 1);
     int rc = TSB_OK;
     if ((rc = dev_alloc(&s->params, nel)) || (rc = dev_alloc(&s->grads, nel)) || (rc = dev_alloc(&s->m, nel)) ||
@@ -432,6 +430,56 @@ int tsb_scene_get_grads(tsb_scene* s, float* d_position, float* d_log_scale, flo
     return TSB_OK;
 }
 
+int tsb_scene_set_sh(tsb_scene* s, int where, const float* refl_sh) {
+    if (!s || !refl_sh) return fail(TSB_ERR_INVALID, "tsb_scene_set_sh: null argument");
+    if (s->d.sh_degree == 0) return fail(TSB_ERR_INVALID, "tsb_scene_set_sh: scene has sh_degree 0");
+    if (where != TSB_HOST && where != TSB_DEVICE) return fail(TSB_ERR_INVALID, "bad memory kind");
+    TSB_CUDA(cudaSetDevice(s->ctx->device));
+    int rc;
+    if ((rc = tsb_ctx_join(s->ctx))) return rc;
+    const int n = s->d.n;
+    if (n == 0) return TSB_OK;
+    cudaStream_t st = s->ctx->stream;
+    const float* src = refl_sh;
+    float* tmp = nullptr;
+    if (where == TSB_HOST) {
+        if ((rc = dev_alloc(&tmp, (size_t)16 * n))) return rc;
+        TSB_CUDA(cudaMemcpyAsync(tmp, refl_sh, sizeof(float) * 16 * (size_t)n, cudaMemcpyHostToDevice, st));
+        src = tmp;
+    }
+    launch_pack_sh(s->params + (3 + (size_t)s->d.n_keyframes) * n, s->params + n, src, n, st);
+    s->ctx->launches += 1;
+    TSB_CHECK_LAUNCH();
+    TSB_CUDA(cudaStreamSynchronize(st));
+    if (tmp) cudaFree(tmp);
+    TSB_CUDA(cudaEventRecord(s->params_ev, st));
+    return TSB_OK;
+}
+
+int tsb_scene_get_sh(tsb_scene* s, float* refl_sh, int grads) {
+    if (!s || !refl_sh) return fail(TSB_ERR_INVALID, "tsb_scene_get_sh: null argument");
+    TSB_CUDA(cudaSetDevice(s->ctx->device));
+    const int n = s->d.n;
+    if (n == 0) return TSB_OK;
+    cudaStream_t st = s->ctx->stream;
+    const float4* base = grads ? s->grads : s->params;
+    if (grads) TSB_CUDA(cudaStreamWaitEvent(st, s->grads_ev, 0));
+    float* tmp = nullptr;
+    int rc;
+    if ((rc = dev_alloc(&tmp, (size_t)16 * n))) return rc;
+    TSB_CUDA(cudaMemsetAsync(tmp, 0, sizeof(float) * 16 * (size_t)n, st));
+    if (s->d.sh_degree > 0) launch_unpack_sh(base + (3 + (size_t)s->d.n_keyframes) * n, tmp, n, st);
+    s->ctx->launches += 1;
+    TSB_CUDA(cudaMemcpyAsync(refl_sh, tmp, sizeof(float) * 16 * (size_t)n, cudaMemcpyDeviceToHost, st));
+    TSB_CUDA(cudaStreamSynchronize(st));
+    cudaFree(tmp);
+    // coefficient 0 from scale_amp.w
+    std::vector<float> dc(n);
+    if ((rc = unpack_one(s, base + n, dc.data(), 1, 3))) return rc;
+    for (int i = 0; i < n; ++i) refl_sh[16 * (size_t)i] = dc[i];
+    return TSB_OK;
+}
+
 int tsb_scene_zero_grads(tsb_scene* s) {
     if (!s) return fail(TSB_ERR_INVALID, "null scene");
     TSB_CUDA(cudaSetDevice(s->ctx->device));
@@ -484,6 +532,9 @@ int tsb_scene_adam_step(tsb_scene* s, const tsb_adam_config* cfg) {
     for (int c = 0; c < 4; ++c) lr[8 + c] = cfg->rotation;
     for (int k = 0; k < s->d.n_keyframes; ++k)
         for (int c = 0; c < 3; ++c) lr[(size_t)(3 + k) * 4 + c] = cfg->motion;
+    if (s->d.sh_degree > 0)  // reflectivity SH coefficients 1..15 use the reflectivity rate
+        for (int a = 0; a < 4; ++a)
+            for (int c = 0; c < (a < 3 ? 4 : 3); ++c) lr[(size_t)(3 + s->d.n_keyframes + a) * 4 + c] = cfg->reflectivity;
     {
         Stage sg(s->ctx, TSB_STAGE_ADAM, s->ctx->stream);
         launch_adam(s->params, s->grads, s->m, s->v, s->d.n, s->narrays, lr.data(), cfg->beta1, cfg->beta2,
@@ -711,6 +762,7 @@ SceneK scenek(const tsb_scene* s) {
     k.scale_amp = s->params + n;
     k.quat = s->params + 2 * n;
     k.motion = s->params + 3 * n;
+    k.sh = s->d.sh_degree > 0 ? s->params + (3 + (size_t)s->d.n_keyframes) * n : nullptr;
     return k;
 }
 

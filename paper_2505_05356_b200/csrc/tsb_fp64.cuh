@@ -10,6 +10,101 @@
 
 namespace tsb {
 
+// sh_basis (sh.hpp:26-50), same expressions and evaluation order as the oracle.
+__device__ __forceinline__ void sh_basis64(const double* d, int degree, double* b) {
+    const double C0 = 0.28209479177387814, C1 = 0.4886025119029199;
+    const double C2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005, -1.0925484305920792,
+                          0.5462742152960396};
+    const double C3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658, 0.3731763325901154,
+                          -0.4570457994644658, 1.445305721320277, -0.5900435899266435};
+    const double x = d[0], y = d[1], z = d[2];
+    for (int k = 0; k < 16; ++k) b[k] = 0.0;
+    b[0] = C0;
+    if (degree < 1) return;
+    b[1] = -C1 * y;
+    b[2] = C1 * z;
+    b[3] = -C1 * x;
+    if (degree < 2) return;
+    const double xx = x * x, yy = y * y, zz = z * z;
+    b[4] = C2[0] * x * y;
+    b[5] = C2[1] * y * z;
+    b[6] = C2[2] * (2.0 * zz - xx - yy);
+    b[7] = C2[3] * x * z;
+    b[8] = C2[4] * (xx - yy);
+    if (degree < 3) return;
+    b[9] = C3[0] * y * (3.0 * xx - yy);
+    b[10] = C3[1] * x * y * z;
+    b[11] = C3[2] * y * (4.0 * zz - xx - yy);
+    b[12] = C3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+    b[13] = C3[4] * x * (4.0 * zz - xx - yy);
+    b[14] = C3[5] * z * (xx - yy);
+    b[15] = C3[6] * x * (xx - 3.0 * yy);
+}
+
+// sh_basis_jacobian (sh.hpp:53-79): J[k][a] = d b_k / d dir_a.
+__device__ __forceinline__ void sh_jacobian64(const double* d, int degree, double J[16][3]) {
+    const double C1 = 0.4886025119029199;
+    const double C2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005, -1.0925484305920792,
+                          0.5462742152960396};
+    const double C3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658, 0.3731763325901154,
+                          -0.4570457994644658, 1.445305721320277, -0.5900435899266435};
+    const double x = d[0], y = d[1], z = d[2];
+    for (int k = 0; k < 16; ++k) J[k][0] = J[k][1] = J[k][2] = 0.0;
+    if (degree < 1) return;
+    J[1][1] = -C1;
+    J[2][2] = C1;
+    J[3][0] = -C1;
+    if (degree < 2) return;
+    const double xx = x * x, yy = y * y, zz = z * z;
+    J[4][0] = C2[0] * y; J[4][1] = C2[0] * x;
+    J[5][1] = C2[1] * z; J[5][2] = C2[1] * y;
+    J[6][0] = -2.0 * C2[2] * x; J[6][1] = -2.0 * C2[2] * y; J[6][2] = 4.0 * C2[2] * z;
+    J[7][0] = C2[3] * z; J[7][2] = C2[3] * x;
+    J[8][0] = 2.0 * C2[4] * x; J[8][1] = -2.0 * C2[4] * y;
+    if (degree < 3) return;
+    J[9][0] = C3[0] * 6.0 * x * y; J[9][1] = C3[0] * (3.0 * xx - 3.0 * yy);
+    J[10][0] = C3[1] * y * z; J[10][1] = C3[1] * x * z; J[10][2] = C3[1] * x * y;
+    J[11][0] = -2.0 * C3[2] * x * y; J[11][1] = C3[2] * (4.0 * zz - xx - 3.0 * yy); J[11][2] = 8.0 * C3[2] * y * z;
+    J[12][0] = -6.0 * C3[3] * x * z; J[12][1] = -6.0 * C3[3] * y * z;
+    J[12][2] = C3[3] * (6.0 * zz - 3.0 * xx - 3.0 * yy);
+    J[13][0] = C3[4] * (4.0 * zz - 3.0 * xx - yy); J[13][1] = -2.0 * C3[4] * x * y; J[13][2] = 8.0 * C3[4] * x * z;
+    J[14][0] = 2.0 * C3[5] * x * z; J[14][1] = -2.0 * C3[5] * y * z; J[14][2] = C3[5] * (xx - yy);
+    J[15][0] = C3[6] * (3.0 * xx - 3.0 * yy); J[15][1] = -6.0 * C3[6] * x * y;
+}
+
+// The 16 reflectivity SH coefficients of Gaussian gi (coefficient 0 lives in scale_amp.w).
+__device__ __forceinline__ void refl_coeffs(const SceneK& S, int gi, double* c) {
+    c[0] = (double)S.scale_amp[gi].w;
+    for (int a = 0; a < 4; ++a) {
+        const float4 v = S.sh[(size_t)a * S.n + gi];
+        const int k = 1 + 4 * a;
+        c[k] = v.x;
+        c[k + 1] = v.y;
+        c[k + 2] = v.z;
+        if (a < 3) c[k + 3] = v.w;
+    }
+}
+
+// sum_k refl_sh[k] b_k(view_dir) for sh_degree > 0 (out of line: keeps the
+// degree-0 kernels' register budget).
+__device__ __noinline__ double refl_sh_eval(const SceneK& S, int gi, double v0, double v1, double v2) {
+    const double v[3] = {v0, v1, v2};
+    double b[16], c[16];
+    sh_basis64(v, S.sh_degree, b);
+    refl_coeffs(S, gi, c);
+    double rr = 0.0;
+    for (int k = 0; k < 16; ++k) rr += c[k] * b[k];
+    return rr;
+}
+
+// view_dir = (x - center) / depth and r_raw = sum_k refl_sh[k] b[k] (splat.cpp:163-165).
+__device__ __forceinline__ double refl_raw64(const SceneK& S, const CamK& C, int gi, const double* x, double depth,
+                                             double* view_dir) {
+    for (int i = 0; i < 3; ++i) view_dir[i] = (x[i] - C.center[i]) / depth;
+    if (S.sh_degree == 0) return (double)S.scale_amp[gi].w * 0.28209479177387814;
+    return refl_sh_eval(S, gi, view_dir[0], view_dir[1], view_dir[2]);
+}
+
 struct Prep64 {
     double x[3];  // rendered world mean (trajectory-interpolated)
     double p[3];  // camera-space mean
@@ -20,6 +115,7 @@ struct Prep64 {
     double c11;  // dilated cov2d(1,1): l22 = 1/sqrt(c11)
     double coef;
     double refl_raw;
+    double view_dir[3];
     double M[6];      // J W (2x3 row-major)
     double cov3d[9];  // row-major
     double tx, ty;
@@ -73,7 +169,7 @@ __device__ __forceinline__ void quat_rot(const double* q, double* u, double* R) 
 }
 
 // RenderPassImpl::prepare for one Gaussian (splat.cpp:114-176).  Returns true when
-// the splat survives culling.  Only sh_degree 0 is handled (refl_raw = C0 * dc).
+// the splat survives culling.
 __device__ __forceinline__ bool prep64(const SceneK& S, const CamK& C, const OptK& O,
                                        const FrameK& F, int gi, Prep64& s) {
     frame_mean(S, F, gi, s.x);
@@ -143,8 +239,8 @@ __device__ __forceinline__ bool prep64(const SceneK& S, const CamK& C, const Opt
     v = d2i_like_x86(ceil(s.mean[1] + radius)) + 1; s.y1 = v < C.H ? v : C.H;
     if (s.x0 >= s.x1 || s.y0 >= s.y1) return false;
 
-    // sh_degree 0: view-independent reflectivity (sh.hpp:26-31; splat.cpp:163-167)
-    s.refl_raw = (double)sa.w * 0.28209479177387814;
+    // view-dependent reflectivity (sh.hpp:26-50; splat.cpp:163-167)
+    s.refl_raw = refl_raw64(S, C, gi, s.x, s.depth, s.view_dir);
     const double r = clampd(s.refl_raw, 0.0, 1.0);
     s.coef = S.s_int * r / (s.depth * s.depth);
     return true;

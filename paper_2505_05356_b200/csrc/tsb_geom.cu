@@ -337,6 +337,7 @@ void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F
 // comparisons as prep64 on the same inputs).
 struct Chain64 {
     double p[3], depth, opacity, refl_raw, M[6], cov3d[9], tx, ty, ca, cb, cc, Rq[9], uq[4], sv[3], qn;
+    double view_dir[3];
     bool clx, cly;
 };
 
@@ -402,7 +403,24 @@ __device__ __forceinline__ void chain_prep(const SceneK& S, const CamK& C, const
     s.cb = -c2[1] * idet;
     s.cc = c2[0] * idet;
     // the gate 0 < r_raw < 1 must see prep64's exact value
-    s.refl_raw = (double)sa.w * 0.28209479177387814;
+    s.refl_raw = refl_raw64(S, C, gi, x, s.depth, s.view_dir);
+}
+
+// Reflectivity SH part of the chain for sh_degree > 0 (out of line so the common
+// degree-0 path keeps its register budget): d_refl[k] = b_k d_r and
+// d_dir = Jb^T (refl_sh * d_r) (splat.cpp:579-583).
+__device__ __noinline__ void sh_chain(const SceneK& S, int gi, const double* view_dir, double d_r, double* d_refl,
+                                      double* d_dir) {
+    double b[16], c[16], Jb[16][3];
+    sh_basis64(view_dir, S.sh_degree, b);
+    refl_coeffs(S, gi, c);
+    sh_jacobian64(view_dir, S.sh_degree, Jb);
+    for (int k = 0; k < 16; ++k) d_refl[k] = b[k] * d_r;
+    for (int a = 0; a < 3; ++a) {
+        double t = 0.0;
+        for (int k = 0; k < 16; ++k) t += Jb[k][a] * (c[k] * d_r);
+        d_dir[a] = t;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -411,7 +429,7 @@ __device__ __forceinline__ void chain_prep(const SceneK& S, const CamK& C, const
 // (trainer.cpp:313-314, 329-331), and accumulate into the scene gradient
 // buffer (GroupGrads::add).  Clears the screen-gradient slots it consumed.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_chain(SceneK S, CamK C, OptK O, FrameK F,
+__global__ void __launch_bounds__(128, 4) k_chain(SceneK S, CamK C, OptK O, FrameK F,
                                                const uint32_t* __restrict__ touched,
                                                float* __restrict__ screen,
                                                float4* __restrict__ grads) {
@@ -438,8 +456,20 @@ __global__ void __launch_bounds__(128) k_chain(SceneK S, CamK C, OptK O, FrameK 
     const double id = 1.0 / s.depth;
     const double id2 = id * id;
     const double d_depth = d_dep + d_coef * (-2.0 * S.s_int * r_cl * id2 * id);
+    // reflectivity SH through coef = s_int * r / d^2 (splat.cpp:573-583), gated by 0 < r_raw < 1
+    double d_refl[16];
+    double d_dir[3] = {0.0, 0.0, 0.0};
     double d_amp = 0.0;
-    if (s.refl_raw > 0.0 && s.refl_raw < 1.0) d_amp = 0.28209479177387814 * (d_coef * S.s_int * id2);
+    const bool gated = s.refl_raw > 0.0 && s.refl_raw < 1.0;
+    if (gated) {
+        const double d_r = d_coef * S.s_int * id2;
+        if (S.sh_degree == 0) {
+            d_amp = 0.28209479177387814 * d_r;
+        } else {
+            sh_chain(S, gi, s.view_dir, d_r, d_refl, d_dir);
+            d_amp = d_refl[0];
+        }
+    }
 
     const double Q[4] = {s.ca, s.cb, s.cb, s.cc};
     const double GQ[4] = {d_ca, 0.5 * d_cb, 0.5 * d_cb, d_cc};
@@ -478,8 +508,12 @@ __global__ void __launch_bounds__(128) k_chain(SceneK S, CamK C, OptK O, FrameK 
     dp[1] += d_mean1 * C.fy * iz;
     dp[2] += d_mean1 * (-C.fy * s.p[1] * iz2);
     for (int a = 0; a < 3; ++a) dp[a] += d_depth * (s.p[a] * id);
+    // view_dir = (x - C)/|x - C| feeds the world position directly (splat.cpp:619-622)
+    const double vd = s.view_dir[0] * d_dir[0] + s.view_dir[1] * d_dir[1] + s.view_dir[2] * d_dir[2];
     double dpos[3];
-    for (int a = 0; a < 3; ++a) dpos[a] = R[0 * 3 + a] * dp[0] + R[1 * 3 + a] * dp[1] + R[2 * 3 + a] * dp[2];
+    for (int a = 0; a < 3; ++a)
+        dpos[a] = (d_dir[a] - s.view_dir[a] * vd) * id + R[0 * 3 + a] * dp[0] + R[1 * 3 + a] * dp[1] +
+                  R[2 * 3 + a] * dp[2];
 
     // cov3d = M3 M3^T, M3 = R(q) diag(exp(log_scale))
     double M3[9], dM3[9];
@@ -527,6 +561,18 @@ __global__ void __launch_bounds__(128) k_chain(SceneK S, CamK C, OptK O, FrameK 
     float4 g2 = grads[2 * n + gi];
     g2.x += (float)dq[0]; g2.y += (float)dq[1]; g2.z += (float)dq[2]; g2.w += (float)dq[3];
     grads[2 * n + gi] = g2;
+    if (S.sh_degree > 0 && gated) {
+        float4* gs = grads + (size_t)(3 + S.nk) * n + gi;
+        for (int a = 0; a < 4; ++a) {
+            float4 v = gs[(size_t)a * n];
+            const int k = 1 + 4 * a;
+            v.x += (float)d_refl[k];
+            v.y += (float)d_refl[k + 1];
+            v.z += (float)d_refl[k + 2];
+            if (a < 3) v.w += (float)d_refl[k + 3];
+            gs[(size_t)a * n] = v;
+        }
+    }
     if (S.nk > 0) {
         const double wa = 1.0 - F.w, wb = F.w;
         float4* gm = grads + (size_t)(3 + F.key) * n + gi;

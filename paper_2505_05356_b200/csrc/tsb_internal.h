@@ -11,7 +11,7 @@ namespace tsb {
 constexpr int kTile = 16;          // raster CTA block edge (pixels)
 constexpr int kRasterThreads = kTile * kTile;
 constexpr int kMaxKeyframes = 16;
-constexpr int kMaxArrays = 3 + kMaxKeyframes;  // pos_op, scale_amp, quat, motion[k]
+constexpr int kMaxArrays = 3 + kMaxKeyframes + 4;  // pos_op, scale_amp, quat, motion[k], sh[4]
 
 // Camera constants the kernels use (camera.hpp:9-49 + splat.cpp:109-111).
 struct CamK {
@@ -41,6 +41,7 @@ struct SceneK {
     const float4* scale_amp;  // log_scale xyz, reflectivity_dc
     const float4* quat;       // w, x, y, z
     const float4* motion;     // [nk][n] keyframe offsets (xyz, 0)
+    const float4* sh;         // [4][n] reflectivity SH coefficients 1..15 (+pad); null when sh_degree == 0
 };
 
 struct FrameK {
@@ -183,6 +184,9 @@ void launch_reduce_partials(const double* part, int nparts, int width, double* o
 void launch_pack_params(float4* dst, const float* src, int n, int comps, int comp0, int ncomp_dst,
                         cudaStream_t st);
 void launch_unpack(const float4* src, float* dst, int n, int comps, int comp0, cudaStream_t st);
+// SH coefficients 1..15 of a [n][16] host-layout array <-> the 4 float4 SH arrays
+void launch_pack_sh(float4* dst4, float4* scale_amp, const float* src16, int n, cudaStream_t st);
+void launch_unpack_sh(const float4* src4, float* dst16, int n, cudaStream_t st);
 void launch_adam(float4* params, float4* grads, float4* m, float4* v, int n, int narrays,
                  const double* lr4 /* host [narrays*4] */, double beta1, double beta2, double eps,
                  double bc1, double bc2, float* densify, cudaStream_t st);

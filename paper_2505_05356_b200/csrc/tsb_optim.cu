@@ -28,6 +28,39 @@ __global__ void k_unpack(const float4* __restrict__ src, float* __restrict__ dst
     for (int c = 0; c < comps; ++c) dst[(size_t)i * comps + c] = s[comp0 + c];
 }
 
+__global__ void k_pack_sh(float4* __restrict__ dst, float4* __restrict__ scale_amp, const float* __restrict__ src,
+                          int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float* s = src + (size_t)i * 16;
+    scale_amp[i].w = s[0];
+    for (int a = 0; a < 4; ++a) {
+        const int k = 1 + 4 * a;
+        dst[(size_t)a * n + i] = make_float4(s[k], s[k + 1], s[k + 2], a < 3 ? s[k + 3] : 0.f);
+    }
+}
+
+__global__ void k_unpack_sh(const float4* __restrict__ src, float* __restrict__ dst, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float* d = dst + (size_t)i * 16;
+    for (int a = 0; a < 4; ++a) {
+        const float4 v = src[(size_t)a * n + i];
+        const int k = 1 + 4 * a;
+        d[k] = v.x;
+        d[k + 1] = v.y;
+        d[k + 2] = v.z;
+        if (a < 3) d[k + 3] = v.w;
+    }
+}
+
+void launch_pack_sh(float4* dst4, float4* scale_amp, const float* src16, int n, cudaStream_t st) {
+    if (n > 0) k_pack_sh<<<(n + 255) / 256, 256, 0, st>>>(dst4, scale_amp, src16, n);
+}
+void launch_unpack_sh(const float4* src4, float* dst16, int n, cudaStream_t st) {
+    if (n > 0) k_unpack_sh<<<(n + 255) / 256, 256, 0, st>>>(src4, dst16, n);
+}
+
 void launch_pack_params(float4* dst, const float* src, int n, int comps, int comp0, int, cudaStream_t st) {
     if (n <= 0) return;
     k_pack<<<(n + 255) / 256, 256, 0, st>>>(dst, src, n, comps, comp0);

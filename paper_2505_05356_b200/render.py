@@ -235,6 +235,16 @@ class GaussianScene:
         check(lib().tsb_scene_set_params(self._h, _abi.TSB_HOST, *[a.ctypes.data for a in arrs],
                                          mo.ctypes.data if mo is not None else None))
 
+    def set_sh(self, refl_sh):
+        """All 16 reflectivity SH coefficients per Gaussian, (n, 16) (sh_degree > 0)."""
+        a = _f32(refl_sh, self.n, 16)
+        check(lib().tsb_scene_set_sh(self._h, _abi.TSB_HOST, a.ctypes.data))
+
+    def get_sh(self, grads: bool = False):
+        out = np.zeros((self.n, 16), np.float32)
+        check(lib().tsb_scene_get_sh(self._h, _ptr(out), 1 if grads else 0))
+        return out
+
     def set_params_device(self, position, log_scale, rotation, opacity_logit, reflectivity_dc, motion=None):
         """Device pointers (ints) in the same SoA layout."""
         check(lib().tsb_scene_set_params(self._h, _abi.TSB_DEVICE, position, log_scale, rotation, opacity_logit,
