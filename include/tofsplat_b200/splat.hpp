@@ -107,12 +107,15 @@ inline double sigmoid(double x) { return 1.0 / (1.0 + std::exp(-x)); }
 inline double logit(double p) { return std::log(p / (1.0 - p)); }
 
 // ---- render API (splat.hpp:13-117) -----------------------------------------
-struct RenderChannels {
+struct RenderChannels {  // the ToF channels (colour / flow are outside this path)
     bool quad = true;
+    bool phasor = false;
     bool depth = true;
+    bool distortion = false;
 };
 struct Backgrounds {
     std::array<double, 4> quad{0, 0, 0, 0};
+    std::array<double, 2> phasor{0, 0};
 };
 struct RenderOptions {
     RenderChannels channels;
@@ -132,10 +135,11 @@ struct RenderInput {
 };
 struct RenderedBuffers {
     int width = 0, height = 0;
-    Image quad, depth_raw, weight, depth, transmittance;
+    Image quad, phasor, depth_raw, weight, depth, distortion, transmittance;
 };
-struct BufferGrads {
-    Image d_quad;  // the quad channel is the one the ToF path differentiates
+struct BufferGrads {  // leave an image empty to skip that channel (splat.hpp:68-77)
+    Image d_quad, d_phasor;
+    Image d_depth_raw, d_weight, d_distortion, d_transmittance;
 };
 struct SceneGrads {
     Matrix3Xd d_position, d_log_scale;
@@ -143,6 +147,7 @@ struct SceneGrads {
     std::vector<double> d_opacity_logit;
     Matrix16Xd d_reflectivity_sh;
     std::array<double, 4> d_bg_quad{0, 0, 0, 0};
+    std::array<double, 2> d_bg_phasor{0, 0};
 };
 
 namespace detail {
@@ -204,8 +209,10 @@ public:
         for (int k = 0; k < 3; ++k) cam_.t[k] = in.camera->translation[k];
         const RenderOptions& o = in.opts;
         opt_ = tsb_render_options{o.alpha_threshold, o.transmittance_floor, o.dilation, o.sigma_cutoff,
-                                  o.coverage_eps, o.tile_size, TSB_CH_QUAD | TSB_CH_DEPTH, {}};
+                                  o.coverage_eps, o.tile_size, TSB_CH_QUAD | TSB_CH_DEPTH | TSB_CH_PHASOR, {}, {}};
+        if (o.channels.distortion) opt_.channels |= TSB_CH_DISTORTION;
         for (int k = 0; k < 4; ++k) opt_.bg_quad[k] = o.bg.quad[k];
+        for (int k = 0; k < 2; ++k) opt_.bg_phasor[k] = o.bg.phasor[k];
         tsb_check(tsb_pass_prepare(p, s, &cam_, &opt_, nullptr));
     }
 
@@ -226,6 +233,8 @@ public:
         out.depth = download(TSB_OUT_DEPTH, 1);
         out.weight = download(TSB_OUT_WEIGHT, 1);
         out.transmittance = download(TSB_OUT_TRANSM, 1);
+        if (in_.opts.channels.phasor) out.phasor = download(TSB_OUT_PHASOR, 2);
+        if (in_.opts.channels.distortion) out.distortion = download(TSB_OUT_DISTORTION, 1);
         forwarded_ = true;
         return out;
     }
@@ -234,13 +243,19 @@ public:
         if (!forwarded_) forward();
         const int n = in_.scene->size();
         tsb_check(tsb_scene_zero_grads(scene_.get()));
-        std::vector<float> dq;
-        if (up.d_quad.channels == 4) {
-            dq.assign(up.d_quad.data.begin(), up.d_quad.data.end());
-        } else {
-            dq.assign(4 * (size_t)in_.camera->width * in_.camera->height, 0.f);
+        const size_t HW = (size_t)in_.camera->width * in_.camera->height;
+        std::vector<float> f[6];
+        const Image* imgs[6] = {&up.d_quad, &up.d_phasor, &up.d_depth_raw, &up.d_weight, &up.d_distortion,
+                                &up.d_transmittance};
+        const int nch[6] = {4, 2, 1, 1, 1, 1};
+        const float* ptr[6] = {};
+        for (int i = 0; i < 6; ++i) {
+            if (imgs[i]->data.empty()) continue;
+            if (imgs[i]->data.size() != nch[i] * HW) throw std::runtime_error("render_backward: upstream size mismatch");
+            f[i].assign(imgs[i]->data.begin(), imgs[i]->data.end());
+            ptr[i] = f[i].data();
         }
-        tsb_check(tsb_pass_backward(pass_.get(), TSB_HOST, dq.data()));
+        tsb_check(tsb_pass_backward_buffers(pass_.get(), TSB_HOST, ptr[0], ptr[1], ptr[2], ptr[3], ptr[4], ptr[5]));
         std::vector<float> dp(3 * (size_t)n), dl(3 * (size_t)n), dr(4 * (size_t)n), dop(n), drf(n);
         double dbg[8] = {0};
         tsb_check(tsb_scene_get_grads(scene_.get(), dp.data(), dl.data(), dr.data(), dop.data(), drf.data(), nullptr,
@@ -261,6 +276,9 @@ public:
             g.d_reflectivity_sh(0, i) = drf[i];
         }
         for (int k = 0; k < 4; ++k) g.d_bg_quad[k] = dbg[k];
+        double dbp[4] = {0};
+        tsb_check(tsb_scene_get_bg_grads(scene_.get(), nullptr, dbp));
+        for (int k = 0; k < 2; ++k) g.d_bg_phasor[k] = dbp[k];
         if (in_.scene->sh_degree > 0) {
             std::vector<float> dsh(16 * (size_t)n);
             tsb_check(tsb_scene_get_sh(scene_.get(), dsh.data(), 1));

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define TSB_ABI_VERSION 1
+#define TSB_ABI_VERSION 2
 
 enum {
     TSB_OK = 0,
@@ -54,7 +54,9 @@ enum {
     TSB_CH_WEIGHT = 1u << 2,    /* weight (= alpha, sum_k w_k); always computed */
     TSB_CH_TRANSM = 1u << 3,    /* transmittance T_N; always computed */
     TSB_CH_COUNTS = 1u << 4,    /* per-pixel n_contrib / n_processed (parity) */
-    TSB_CH_FULL_LISTS = 1u << 5 /* bin every tile's complete list (parity); default stops at termination */
+    TSB_CH_FULL_LISTS = 1u << 5, /* bin every tile's complete list (parity); default stops at termination */
+    TSB_CH_PHASOR = 1u << 6,     /* (re, im) per frequency; always computed (free: 2x the quad sums) */
+    TSB_CH_DISTORTION = 1u << 7  /* sum_kl w_k w_l (d_k - d_l)^2; required for a distortion upstream */
 };
 
 /* CameraModel (camera.hpp:9-17).  R row-major; p_cam = R p_world + t. */
@@ -66,8 +68,8 @@ typedef struct {
     double t[3];
 } tsb_camera;
 
-/* RenderOptions + Backgrounds (splat.hpp:22-37).  bg_quad holds 4 values per
- * modulation frequency. */
+/* RenderOptions + Backgrounds (splat.hpp:22-37).  bg_quad holds 4 values and
+ * bg_phasor 2 values per modulation frequency. */
 typedef struct {
     double alpha_threshold;     /* 1/255 */
     double transmittance_floor; /* 1e-4 */
@@ -77,6 +79,7 @@ typedef struct {
     int32_t tile_size;          /* 16 */
     uint32_t channels;          /* TSB_CH_* */
     double bg_quad[8];
+    double bg_phasor[4];
 } tsb_render_options;
 
 /* CanonicalScene header (scene.hpp:44-52) + ToFConfig (tof.hpp:13-21).
@@ -150,6 +153,8 @@ int tsb_scene_get_grads(tsb_scene* s, float* d_position, float* d_log_scale, flo
                         float* d_opacity_logit, float* d_reflectivity_dc, float* d_motion,
                         double* d_bg_quad, double* loss);
 int tsb_scene_zero_grads(tsb_scene* s);
+/* SceneGrads::d_bg_quad / d_bg_phasor (splat.hpp:87-89): 4 resp. 2 per frequency. */
+int tsb_scene_get_bg_grads(tsb_scene* s, double* d_bg_quad, double* d_bg_phasor);
 /* View-dependent reflectivity (sh_degree 1..3; sh.hpp:26-50, splat.cpp:163-165): all 16
  * reflectivity SH coefficients per Gaussian, [n][16] (coefficient 0 == reflectivity_dc).
  * tsb_scene_get_sh returns the parameters (grads = 0) or their accumulated gradients (grads = 1). */
@@ -205,7 +210,9 @@ enum {
     TSB_OUT_TRANSM = 4,    /* [H][W] f32 */
     TSB_OUT_N_CONTRIB = 5, /* [H][W] i32 */
     TSB_OUT_N_PROCESSED = 6, /* [H][W] i32 */
-    TSB_OUT_D_QUAD = 7     /* [4*n_freq][H][W] f32 upstream gradient */
+    TSB_OUT_D_QUAD = 7,    /* [4*n_freq][H][W] f32 upstream gradient */
+    TSB_OUT_PHASOR = 8,    /* [2*n_freq][H][W] f32 (re, im) */
+    TSB_OUT_DISTORTION = 9 /* [H][W] f32 (TSB_CH_DISTORTION) */
 };
 /* Device pointer and byte size of a pass-owned buffer. */
 int tsb_pass_output(tsb_pass* p, int which, void** dptr, size_t* bytes);
@@ -217,6 +224,13 @@ int tsb_pass_download(tsb_pass* p, int which, void* host, size_t bytes);
  * image [4*n_freq][H][W] (`where`).  Gradients are ACCUMULATED into the scene
  * (GroupGrads::add + trajectory chain, trainer.cpp:256, 312-331). */
 int tsb_pass_backward(tsb_pass* p, int where, const float* d_quad);
+/* RenderPass::backward(BufferGrads) (splat.cpp:347-650) with every ToF upstream
+ * image of BufferGrads (splat.hpp:73-77): NULL skips a channel, as an empty Image
+ * does in the reference.  Shapes: d_quad [4*n_freq][H][W], d_phasor [2*n_freq][H][W],
+ * the rest [H][W].  A distortion upstream requires TSB_CH_DISTORTION in the forward. */
+int tsb_pass_backward_buffers(tsb_pass* p, int where, const float* d_quad, const float* d_phasor,
+                              const float* d_depth_raw, const float* d_weight,
+                              const float* d_distortion, const float* d_transmittance);
 
 /* Parity / diagnostics: integer intermediates the reference keeps private
  * (splat.cpp:86-87).  Sizes: gidx V, rect 4V (x0,x1,y0,y1 per rank), tiles+1
@@ -229,6 +243,9 @@ int tsb_pass_debug_tiles(tsb_pass* p, int32_t* tiles_x, int32_t* tiles_y, int64_
  * (8 floats: d_mean2d x,y, d_conic a,b,c, d_opacity, d_coef, d_depth). */
 int tsb_pass_debug_records(tsb_pass* p, float* rec12 /* 12 per rank */);
 int tsb_pass_debug_screen_grads(tsb_pass* p, float* g8 /* 8 per rank */);
+/* Keep a copy of the screen-space gradients of every following backward (the chain kernel
+ * consumes them); required before tsb_pass_debug_screen_grads. */
+int tsb_pass_debug_keep_screen(tsb_pass* p, int enabled);
 /* Pixels the fp32 raster flagged as decision-ambiguous and recomposited in fp64. */
 int tsb_pass_debug_fixups(tsb_pass* p, int32_t* count);
 /* The fixed pixels themselves: pixel index | reason << 24 (1 maha, 2 alpha, 4 T band). */

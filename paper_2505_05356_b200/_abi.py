@@ -17,8 +17,9 @@ HEADER_PATH = Path(__file__).resolve().parent.parent / "include" / "tsb.h"
 TSB_OK, TSB_ERR_INVALID, TSB_ERR_CUDA, TSB_ERR_NOMEM, TSB_ERR_UNSUPPORTED, TSB_ERR_NCCL = range(6)
 TSB_HOST, TSB_DEVICE = 0, 1
 CH_QUAD, CH_DEPTH, CH_WEIGHT, CH_TRANSM, CH_COUNTS, CH_FULL_LISTS = 1, 2, 4, 8, 16, 32
+CH_PHASOR, CH_DISTORTION = 64, 128
 (OUT_QUAD, OUT_DEPTH_RAW, OUT_DEPTH, OUT_WEIGHT, OUT_TRANSM, OUT_N_CONTRIB, OUT_N_PROCESSED,
- OUT_D_QUAD) = range(8)
+ OUT_D_QUAD, OUT_PHASOR, OUT_DISTORTION) = range(10)
 
 
 STAGES = ["preprocess", "depth_sort", "scan", "binning", "tile_sort", "ranges", "raster_fwd", "fixup", "loss",
@@ -40,7 +41,8 @@ class Camera(C.Structure):
 class RenderOptions(C.Structure):
     _fields_ = [("alpha_threshold", C.c_double), ("transmittance_floor", C.c_double), ("dilation", C.c_double),
                 ("sigma_cutoff", C.c_double), ("coverage_eps", C.c_double), ("tile_size", C.c_int32),
-                ("channels", C.c_uint32), ("bg_quad", C.c_double * 8)]
+                ("channels", C.c_uint32), ("bg_quad", C.c_double * 8),
+                ("bg_phasor", C.c_double * 4)]
 
 
 class SceneDesc(C.Structure):
@@ -84,6 +86,7 @@ SIGNATURES = {
     "tsb_scene_set_params": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]),
     "tsb_scene_get_params": (C.c_int, [_vp, _fp, _fp, _fp, _fp, _fp, _fp]),
     "tsb_scene_get_grads": (C.c_int, [_vp, _fp, _fp, _fp, _fp, _fp, _fp, _dp, _dp]),
+    "tsb_scene_get_bg_grads": (C.c_int, [_vp, _dp, _dp]),
     "tsb_scene_zero_grads": (C.c_int, [_vp]),
     "tsb_scene_set_sh": (C.c_int, [_vp, C.c_int, _vp]),
     "tsb_scene_get_sh": (C.c_int, [_vp, _fp, C.c_int]),
@@ -102,6 +105,8 @@ SIGNATURES = {
     "tsb_pass_output": (C.c_int, [_vp, C.c_int, C.POINTER(_vp), C.POINTER(C.c_size_t)]),
     "tsb_pass_download": (C.c_int, [_vp, C.c_int, _vp, C.c_size_t]),
     "tsb_pass_backward": (C.c_int, [_vp, C.c_int, _vp]),
+    "tsb_pass_backward_buffers": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "tsb_pass_debug_keep_screen": (C.c_int, [_vp, C.c_int]),
     "tsb_pass_debug_prepared": (C.c_int, [_vp, _ip, _ip]),
     "tsb_pass_debug_tiles": (C.c_int, [_vp, _ip, _ip, _lp, _ip]),
     "tsb_pass_debug_records": (C.c_int, [_vp, _fp]),

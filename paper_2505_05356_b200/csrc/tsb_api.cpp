@@ -112,7 +112,7 @@ struct tsb_scene {
     float4* m = nullptr;
     float4* v = nullptr;
     float* densify = nullptr;
-    double* stats = nullptr;  // [0..7] d_bg_quad, [8] loss
+    double* stats = nullptr;  // kStats: bg grads (quad 4*nf, phasor 2*nf) at kStatBg, loss at kStatLoss
     float* staging = nullptr; // 4n floats for host<->device (un)packing
     int64_t step = 0;
     int64_t densify_count = 0;
@@ -148,6 +148,8 @@ struct tsb_pass {
     uint2* rect = nullptr;
     RecK rec{};
     float* screen = nullptr;  // [8][n]
+    float* screen_keep = nullptr;  // debug copy of screen (tsb_pass_debug_keep_screen)
+    bool keep_screen = false;
     // chunked binning
     std::vector<int> chunk_seg0, chunk_nseg;  // schedule (segments)
     int nchunks = 0;                          // chunks binned by the last forward
@@ -164,6 +166,9 @@ struct tsb_pass {
     int32_t *n_contrib = nullptr, *n_processed = nullptr, *last = nullptr;
     float* T_pre = nullptr;
     float* d_quad = nullptr;
+    float* up_extra = nullptr;  // [8][npx] host-uploaded upstreams: phasor (2*nf), depth_raw, weight, distortion, T
+    double* dist3 = nullptr;    // [3][npx] distortion moments (PixK::dist3)
+    double* st_d = nullptr;     // [3][npx] distortion moments carried across chunks
     float* target = nullptr;
     int32_t* flagged = nullptr;
     float* st_f = nullptr;
@@ -294,7 +299,7 @@ int tsb_scene_create(tsb_ctx* ctx, const tsb_scene_desc* d, tsb_scene** out) {
     int rc = TSB_OK;
     if ((rc = dev_alloc(&s->params, nel)) || (rc = dev_alloc(&s->grads, nel)) || (rc = dev_alloc(&s->m, nel)) ||
         (rc = dev_alloc(&s->v, nel)) || (rc = dev_alloc(&s->densify, (size_t)std::max(d->n, 1))) ||
-        (rc = dev_alloc(&s->stats, 9)) || (rc = dev_alloc(&s->staging, 4 * (size_t)std::max(d->n, 1)))) {
+        (rc = dev_alloc(&s->stats, kStats)) || (rc = dev_alloc(&s->staging, 4 * (size_t)std::max(d->n, 1)))) {
         tsb_scene_destroy(s);
         return rc;
     }
@@ -309,7 +314,7 @@ int tsb_scene_create(tsb_ctx* ctx, const tsb_scene_desc* d, tsb_scene** out) {
     cudaMemsetAsync(s->m, 0, nel * sizeof(float4), st);
     cudaMemsetAsync(s->v, 0, nel * sizeof(float4), st);
     cudaMemsetAsync(s->densify, 0, sizeof(float) * std::max(d->n, 1), st);
-    cudaMemsetAsync(s->stats, 0, sizeof(double) * 9, st);
+    cudaMemsetAsync(s->stats, 0, sizeof(double) * kStats, st);
     cudaEventRecord(s->params_ev, st);
     cudaEventRecord(s->grads_ev, st);
     TSB_CUDA(cudaStreamSynchronize(st));
@@ -422,11 +427,24 @@ int tsb_scene_get_grads(tsb_scene* s, float* d_position, float* d_log_scale, flo
     if (d_motion)
         for (int k = 0; k < s->d.n_keyframes; ++k)
             if ((rc = unpack_one(s, s->grads + (size_t)(3 + k) * n, d_motion + (size_t)k * 3 * n, 3, 0))) return rc;
-    double st9[9];
-    TSB_CUDA(cudaMemcpyAsync(st9, s->stats, sizeof st9, cudaMemcpyDeviceToHost, s->ctx->stream));
+    double st[kStats];
+    TSB_CUDA(cudaMemcpyAsync(st, s->stats, sizeof st, cudaMemcpyDeviceToHost, s->ctx->stream));
     TSB_CUDA(cudaStreamSynchronize(s->ctx->stream));
-    if (d_bg_quad) std::memcpy(d_bg_quad, st9, sizeof(double) * 4 * s->d.n_freq);
-    if (loss) *loss = st9[8];
+    if (d_bg_quad) std::memcpy(d_bg_quad, st + kStatBg, sizeof(double) * 4 * s->d.n_freq);
+    if (loss) *loss = st[kStatLoss];
+    return TSB_OK;
+}
+
+int tsb_scene_get_bg_grads(tsb_scene* s, double* d_bg_quad, double* d_bg_phasor) {
+    if (!s) return fail(TSB_ERR_INVALID, "null scene");
+    TSB_CUDA(cudaSetDevice(s->ctx->device));
+    TSB_CUDA(cudaStreamWaitEvent(s->ctx->stream, s->grads_ev, 0));
+    double st[kStats];
+    TSB_CUDA(cudaMemcpyAsync(st, s->stats, sizeof st, cudaMemcpyDeviceToHost, s->ctx->stream));
+    TSB_CUDA(cudaStreamSynchronize(s->ctx->stream));
+    const int nf = s->d.n_freq;
+    if (d_bg_quad) std::memcpy(d_bg_quad, st + kStatBg, sizeof(double) * 4 * nf);
+    if (d_bg_phasor) std::memcpy(d_bg_phasor, st + kStatBg + 4 * nf, sizeof(double) * 2 * nf);
     return TSB_OK;
 }
 
@@ -486,7 +504,7 @@ int tsb_scene_zero_grads(tsb_scene* s) {
     const size_t nel = (size_t)s->narrays * (size_t)std::max(s->d.n, 1);
     TSB_CUDA(cudaStreamWaitEvent(s->ctx->stream, s->grads_ev, 0));
     TSB_CUDA(cudaMemsetAsync(s->grads, 0, nel * sizeof(float4), s->ctx->stream));
-    TSB_CUDA(cudaMemsetAsync(s->stats, 0, sizeof(double) * 9, s->ctx->stream));
+    TSB_CUDA(cudaMemsetAsync(s->stats, 0, sizeof(double) * kStats, s->ctx->stream));
     TSB_CUDA(cudaEventRecord(s->grads_ev, s->ctx->stream));
     return TSB_OK;
 }
@@ -543,7 +561,7 @@ int tsb_scene_adam_step(tsb_scene* s, const tsb_adam_config* cfg) {
     s->ctx->launches++;
     TSB_CHECK_LAUNCH();
     s->densify_count++;
-    TSB_CUDA(cudaMemsetAsync(s->stats, 0, sizeof(double) * 9, s->ctx->stream));
+    TSB_CUDA(cudaMemsetAsync(s->stats, 0, sizeof(double) * kStats, s->ctx->stream));
     TSB_CUDA(cudaEventRecord(s->params_ev, s->ctx->stream));
     TSB_CUDA(cudaEventRecord(s->grads_ev, s->ctx->stream));
     return TSB_OK;
@@ -617,12 +635,12 @@ void free_gauss(tsb_pass* p) {
     dev_free(p->depth64); dev_free(p->sort_scratch);
     dev_free(p->fx_stamp); dev_free(p->fx_work); dev_free(p->fx_cache);
     dev_free(p->touched); dev_free(p->rect);
-    dev_free(p->rec.A); dev_free(p->rec.B); dev_free(p->rec.C); dev_free(p->rec.D); dev_free(p->screen);
+    dev_free(p->rec.A); dev_free(p->rec.B); dev_free(p->rec.C); dev_free(p->rec.D); dev_free(p->screen); dev_free(p->screen_keep);
 }
 void free_pixels(tsb_pass* p) {
     dev_free(p->out); dev_free(p->n_contrib); dev_free(p->n_processed); dev_free(p->last);
     dev_free(p->T_pre); dev_free(p->d_quad); dev_free(p->target); dev_free(p->flagged);
-    dev_free(p->st_f); dev_free(p->st_i);
+    dev_free(p->st_f); dev_free(p->st_i); dev_free(p->up_extra); dev_free(p->dist3); dev_free(p->st_d);
 }
 
 int ensure_gauss(tsb_pass* p, int n) {
@@ -657,7 +675,9 @@ int ensure_pixels(tsb_pass* p, int W, int H, int ntiles, int nblocks) {
             (rc = dev_alloc(&p->n_processed, npx)) || (rc = dev_alloc(&p->last, npx)) ||
             (rc = dev_alloc(&p->T_pre, npx)) || (rc = dev_alloc(&p->d_quad, (size_t)8 * npx)) ||
             (rc = dev_alloc(&p->target, (size_t)8 * npx)) || (rc = dev_alloc(&p->flagged, npx)) ||
-            (rc = dev_alloc(&p->st_f, (size_t)9 * npx)) || (rc = dev_alloc(&p->st_i, (size_t)3 * npx)))
+            (rc = dev_alloc(&p->st_f, (size_t)kFwdStatePlanes * npx)) || (rc = dev_alloc(&p->st_i, (size_t)3 * npx)) ||
+            (rc = dev_alloc(&p->up_extra, (size_t)8 * npx)) || (rc = dev_alloc(&p->dist3, (size_t)3 * npx)) ||
+            (rc = dev_alloc(&p->st_d, (size_t)3 * npx)))
             return rc;
         p->px_cap = npx;
     }
@@ -666,7 +686,7 @@ int ensure_pixels(tsb_pass* p, int W, int H, int ntiles, int nblocks) {
         dev_free(p->bg_part);
         dev_free(p->block_done);
         int rc;
-        if ((rc = dev_alloc(&p->loss_part, nblocks)) || (rc = dev_alloc(&p->bg_part, (size_t)8 * nblocks)) ||
+        if ((rc = dev_alloc(&p->loss_part, nblocks)) || (rc = dev_alloc(&p->bg_part, (size_t)12 * nblocks)) ||
             (rc = dev_alloc(&p->block_done, nblocks)))
             return rc;
         p->blk_cap = nblocks;
@@ -742,6 +762,7 @@ PixK pixk(tsb_pass* p) {
     px.last = p->last;
     px.T_pre = p->T_pre;
     px.d_quad = p->d_quad;
+    px.dist3 = (p->channels & TSB_CH_DISTORTION) ? p->dist3 : nullptr;
     px.flagged = p->flagged;
     px.n_flagged = p->counters + 1;
     return px;
@@ -842,6 +863,8 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     O.cut2_f = (float)O.cut2;
     O.cov_eps_f = (float)O.cov_eps;
     for (int c = 0; c < 8; ++c) O.bg_quad[c] = c < 4 * p->nf ? opt->bg_quad[c] : 0.0;
+    for (int c = 0; c < 4; ++c) O.bg_phasor[c] = c < 2 * p->nf ? opt->bg_phasor[c] : 0.0;
+    O.dist = (opt->channels & TSB_CH_DISTORTION) ? 1 : 0;
     p->ntiles = O.tiles_x * O.tiles_y;
     if (p->ntiles > 65536) return fail(TSB_ERR_UNSUPPORTED, "render: more than 65536 tiles");
     p->nblocks = p->ntiles * O.sub * O.sub;
@@ -924,7 +947,7 @@ int run_forward(tsb_pass* p, const float* target, bool loss) {
         TSB_CUDA(cudaMemsetAsync(p->block_done, 0, sizeof(int32_t) * p->nblocks, st));
         TSB_CUDA(cudaMemsetAsync(p->tile_blocks_done, 0, sizeof(int32_t) * p->ntiles, st));
         if (loss) TSB_CUDA(cudaMemsetAsync(p->loss_part, 0, sizeof(double) * p->nblocks, st));
-        FwdState fs{p->st_f, p->st_i, p->W * p->H};
+        FwdState fs{p->st_f, p->st_d, p->st_i, p->W * p->H};
         BinK B{};
         B.sorted_gidx = p->sorted;
         B.rect = p->rect;
@@ -1032,7 +1055,7 @@ int run_forward(tsb_pass* p, const float* target, bool loss) {
             launch_reduce_partials(p->loss_part, p->nblocks, 1, p->loss_dev, 1.0 / ((double)p->W * p->H), st);
             // scene loss accumulator += this pass's loss (serialised with other gradient writers)
             TSB_CUDA(cudaStreamWaitEvent(st, p->scene->grads_ev, 0));
-            launch_reduce_partials(p->loss_dev, 1, 1, p->scene->stats + 8, 1.0, st);
+            launch_reduce_partials(p->loss_dev, 1, 1, p->scene->stats + kStatLoss, 1.0, st);
             TSB_CUDA(cudaEventRecord(p->scene->grads_ev, st));
             p->ctx->launches += 3;
         }
@@ -1103,6 +1126,10 @@ int tsb_pass_output(tsb_pass* p, int which, void** dptr, size_t* bytes) {
             if (!(p->channels & TSB_CH_COUNTS)) return fail(TSB_ERR_INVALID, "counts channel not enabled");
             ptr = p->n_processed; b = HW * 4; break;
         case TSB_OUT_D_QUAD: ptr = p->d_quad; b = 4 * p->nf * HW * 4; break;
+        case TSB_OUT_PHASOR: ptr = p->out + ch_phasor(p->nf) * HW; b = 2 * p->nf * HW * 4; break;
+        case TSB_OUT_DISTORTION:
+            if (!(p->channels & TSB_CH_DISTORTION)) return fail(TSB_ERR_INVALID, "distortion channel not enabled");
+            ptr = p->out + ch_distortion(p->nf) * HW; b = HW * 4; break;
         default: return fail(TSB_ERR_INVALID, "unknown output");
     }
     *dptr = ptr;
@@ -1120,6 +1147,38 @@ int tsb_pass_download(tsb_pass* p, int which, void* host, size_t bytes) {
     TSB_CUDA(cudaStreamSynchronize(p->stream));
     return TSB_OK;
 }
+
+namespace {
+int run_backward(tsb_pass* p, const UpK& up) {
+    cudaStream_t st = p->stream;
+    tsb_scene* s = p->scene;
+    float dpsi[2];
+    for (int f = 0; f < p->nf; ++f) dpsi[f] = (float)(4.0 * M_PI * s->d.frequency[f] / s->d.speed_of_light);
+    TSB_CUDA(cudaStreamWaitEvent(st, s->grads_ev, 0));
+    {
+        Stage sg(p->ctx, TSB_STAGE_RASTER_BWD, st);
+        launch_raster_bwd(p->rec, p->ranges_all, p->nchunks, p->vals, p->opt, p->W, p->H, p->nf, dpsi, pixk(p), up,
+                          p->screen, s->d.n, p->bg_part, st);
+        launch_reduce_partials(p->bg_part, p->nblocks, 6 * p->nf, s->stats + kStatBg, 1.0, st);
+    }
+    if (p->keep_screen) {
+        dev_free(p->screen_keep);
+        int rc;
+        if ((rc = dev_alloc(&p->screen_keep, (size_t)8 * s->d.n))) return rc;
+        TSB_CUDA(cudaMemcpyAsync(p->screen_keep, p->screen, sizeof(float) * 8 * (size_t)s->d.n,
+                                 cudaMemcpyDeviceToDevice, st));
+    }
+    {
+        Stage sg(p->ctx, TSB_STAGE_CHAIN, st);
+        launch_chain(scenek(s), p->cam, p->opt, p->frame, p->touched, p->screen, s->grads, st);
+    }
+    p->ctx->launches += 3;
+    TSB_CHECK_LAUNCH();
+    TSB_CUDA(cudaEventRecord(s->grads_ev, st));
+    TSB_CUDA(cudaEventRecord(p->done_ev, st));
+    return TSB_OK;
+}
+}  // namespace
 
 int tsb_pass_backward(tsb_pass* p, int where, const float* d_quad) {
     if (!p) return fail(TSB_ERR_INVALID, "null pass");
@@ -1139,25 +1198,38 @@ int tsb_pass_backward(tsb_pass* p, int where, const float* d_quad) {
     } else if (!p->have_loss) {
         return fail(TSB_ERR_INVALID, "backward: no upstream gradient and no loss was evaluated");
     }
-    tsb_scene* s = p->scene;
-    float dpsi[2];
-    for (int f = 0; f < p->nf; ++f) dpsi[f] = (float)(4.0 * M_PI * s->d.frequency[f] / s->d.speed_of_light);
-    TSB_CUDA(cudaStreamWaitEvent(st, s->grads_ev, 0));
-    {
-        Stage sg(p->ctx, TSB_STAGE_RASTER_BWD, st);
-        launch_raster_bwd(p->rec, p->ranges_all, p->nchunks, p->vals, p->opt, p->W, p->H, p->nf, dpsi, pixk(p), up,
-                          p->screen, s->d.n, p->bg_part, st);
-        launch_reduce_partials(p->bg_part, p->nblocks, 4 * p->nf, s->stats, 1.0, st);
+    UpK u{};
+    u.quad = up;
+    return run_backward(p, u);
+}
+
+int tsb_pass_backward_buffers(tsb_pass* p, int where, const float* d_quad, const float* d_phasor,
+                              const float* d_depth_raw, const float* d_weight, const float* d_distortion,
+                              const float* d_transmittance) {
+    if (!p) return fail(TSB_ERR_INVALID, "null pass");
+    if (!p->forwarded) return fail(TSB_ERR_INVALID, "backward requires a forward pass");
+    if (where != TSB_HOST && where != TSB_DEVICE) return fail(TSB_ERR_INVALID, "bad memory kind");
+    if (d_distortion && !(p->channels & TSB_CH_DISTORTION))
+        return fail(TSB_ERR_INVALID, "backward: a distortion upstream needs the distortion channel in the forward");
+    TSB_CUDA(cudaSetDevice(p->ctx->device));
+    cudaStream_t st = p->stream;
+    const size_t HW = (size_t)p->W * p->H;
+    UpK u{};
+    u.quad = d_quad; u.phasor = d_phasor; u.depth_raw = d_depth_raw; u.weight = d_weight;
+    u.distortion = d_distortion; u.transm = d_transmittance;
+    if (where == TSB_HOST) {
+        const float* srcs[6] = {d_quad, d_phasor, d_depth_raw, d_weight, d_distortion, d_transmittance};
+        float* dsts[6] = {p->d_quad, p->up_extra, p->up_extra + 4 * HW, p->up_extra + 5 * HW,
+                          p->up_extra + 6 * HW, p->up_extra + 7 * HW};
+        const size_t planes[6] = {(size_t)4 * p->nf, (size_t)2 * p->nf, 1, 1, 1, 1};
+        const float** outs[6] = {&u.quad, &u.phasor, &u.depth_raw, &u.weight, &u.distortion, &u.transm};
+        for (int i = 0; i < 6; ++i) {
+            if (!srcs[i]) continue;
+            TSB_CUDA(cudaMemcpyAsync(dsts[i], srcs[i], planes[i] * HW * sizeof(float), cudaMemcpyHostToDevice, st));
+            *outs[i] = dsts[i];
+        }
     }
-    {
-        Stage sg(p->ctx, TSB_STAGE_CHAIN, st);
-        launch_chain(scenek(s), p->cam, p->opt, p->frame, p->touched, p->screen, s->grads, st);
-    }
-    p->ctx->launches += 3;
-    TSB_CHECK_LAUNCH();
-    TSB_CUDA(cudaEventRecord(s->grads_ev, st));
-    TSB_CUDA(cudaEventRecord(p->done_ev, st));
-    return TSB_OK;
+    return run_backward(p, u);
 }
 
 // ---- debug / parity ----
@@ -1264,10 +1336,29 @@ int tsb_pass_debug_records(tsb_pass* p, float* rec12) {
     return TSB_OK;
 }
 
-int tsb_pass_debug_screen_grads(tsb_pass* p, float* g8) {
-    (void)g8;
+int tsb_pass_debug_keep_screen(tsb_pass* p, int enabled) {
     if (!p) return fail(TSB_ERR_INVALID, "null pass");
-    return fail(TSB_ERR_UNSUPPORTED, "screen gradients are consumed by the chain kernel");
+    p->keep_screen = enabled != 0;
+    return TSB_OK;
+}
+
+int tsb_pass_debug_screen_grads(tsb_pass* p, float* g8) {
+    if (!p || !g8) return fail(TSB_ERR_INVALID, "null argument");
+    if (!p->keep_screen || !p->screen_keep)
+        return fail(TSB_ERR_INVALID, "screen gradients are consumed by the chain kernel; "
+                                     "enable tsb_pass_debug_keep_screen before backward");
+    int rc = read_visible(p);
+    if (rc) return rc;
+    const int n = p->scene->d.n, V = p->V;
+    std::vector<float> sc((size_t)8 * std::max(n, 1));
+    std::vector<uint32_t> g((size_t)std::max(V, 1));
+    TSB_CUDA(cudaMemcpyAsync(sc.data(), p->screen_keep, sizeof(float) * 8 * (size_t)n, cudaMemcpyDeviceToHost,
+                             p->stream));
+    if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), p->sorted, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, p->stream));
+    TSB_CUDA(cudaStreamSynchronize(p->stream));
+    for (int i = 0; i < V; ++i)
+        for (int c = 0; c < 8; ++c) g8[8 * (size_t)i + c] = sc[(size_t)c * n + g[i]];
+    return TSB_OK;
 }
 
 int tsb_pass_debug_fixups(tsb_pass* p, int32_t* count) {
@@ -1384,7 +1475,7 @@ int tsb_scene_allreduce_grads(tsb_scene* s, tsb_comm* c) {
     ncclResult_t r = g_nccl.GroupStart();
     if (r == ncclSuccess && nel > 0)
         r = g_nccl.AllReduce(s->grads, s->grads, nel, ncclFloat, ncclSum, c->comm, st);
-    if (r == ncclSuccess) r = g_nccl.AllReduce(s->stats, s->stats, 9, ncclDouble, ncclSum, c->comm, st);
+    if (r == ncclSuccess) r = g_nccl.AllReduce(s->stats, s->stats, kStats, ncclDouble, ncclSum, c->comm, st);
     ncclResult_t r2 = g_nccl.GroupEnd();
     if (r != ncclSuccess || r2 != ncclSuccess)
         return fail(TSB_ERR_NCCL,

@@ -104,6 +104,7 @@ void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const Fram
 // ---------------------------------------------------------------------------
 struct FixupAcc {
     double T, SW, SD, Tpre, accQ[8];
+    double dref, SDs, SD2s;  // distortion moments about the first contributor's depth
     int nc, processed, last_eff;
     bool done;
 };
@@ -241,6 +242,10 @@ __device__ __forceinline__ void fixup_batch(const SceneK& S, const CamK& C, cons
         }
         a.SW += warp_sum(w);
         a.SD += warp_sum(w * depth);
+        if (a.nc == 0) a.dref = (double)(float)__shfl_sync(0xffffffffu, depth, __ffs(mm) - 1);  // = record depth
+        const double dd = depth - a.dref;
+        a.SDs += warp_sum(w * dd);
+        a.SD2s += warp_sum(w * dd * dd);
         a.nc += __popc(mm);
         const int last_lane = 31 - __clz(mm);
         a.Tpre = __shfl_sync(0xffffffffu, mine ? slot[lane].Tpre : 0.0, last_lane);
@@ -272,6 +277,7 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, FrameK 
         const int tile = ty * O.tiles_x + tx;
         FixupAcc a;
         a.T = 1.0; a.SW = 0.0; a.SD = 0.0; a.Tpre = 1.0;
+        a.dref = 0.0; a.SDs = 0.0; a.SD2s = 0.0;
         for (int c = 0; c < 8; ++c) a.accQ[c] = 0.0;
         a.nc = 0; a.processed = 0; a.last_eff = -1; a.done = false;
         int scan_from = -1;  // rank where the tile stopped being binned
@@ -314,6 +320,18 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, FrameK 
             px.out[ch_depth(nf) * HW + o] = a.SW > O.cov_eps ? (float)(a.SD / a.SW) : __int_as_float(0x7fc00000);
             px.out[ch_weight(nf) * HW + o] = (float)a.SW;
             px.out[ch_T(nf) * HW + o] = (float)a.T;
+            for (int f = 0; f < nf; ++f) {
+                px.out[(ch_phasor(nf) + 2 * f + 0) * HW + o] =
+                    (float)(2.0 * a.accQ[4 * f + 1] + O.bg_phasor[2 * f + 0] * a.T * a.T);
+                px.out[(ch_phasor(nf) + 2 * f + 1) * HW + o] =
+                    (float)(2.0 * a.accQ[4 * f + 0] + O.bg_phasor[2 * f + 1] * a.T * a.T);
+            }
+            if (px.dist3) {
+                px.out[ch_distortion(nf) * HW + o] = (float)(2.0 * (a.SW * a.SD2s - a.SDs * a.SDs));
+                px.dist3[o] = a.dref;
+                px.dist3[HW + o] = a.SDs;
+                px.dist3[2 * HW + o] = a.SD2s;
+            }
             if (px.n_contrib) px.n_contrib[o] = a.nc;
             if (px.n_processed) px.n_processed[o] = a.processed;
             const int le = a.last_eff >= 0 ? a.last_eff : a.processed;

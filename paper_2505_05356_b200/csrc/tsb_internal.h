@@ -30,7 +30,9 @@ struct OptK {
     int tiles_x, tiles_y;
     int sub;           // 16x16 raster blocks per tile edge = ceil(ts/16)
     float alpha_thr_f, floor_f, cut2_f, cov_eps_f;
+    int dist;          // distortion channel: accumulate the shifted depth moments
     double bg_quad[8];
+    double bg_phasor[4];
 };
 
 // Device-resident scene (fp32 SoA float4 arrays; see tsb.h for the mapping).
@@ -82,8 +84,10 @@ struct BinK {
 };
 
 // Forward state carried across chunk launches (SoA planes of npx).
+constexpr int kFwdStatePlanes = 9;
 struct FwdState {
     float* f;    // 9 planes: T, Tpre, SW, SD, errT, accS0, accC0, accS1, accC1
+    double* d;   // 3 planes (distortion channel): dref, SDs, SD2s
     int32_t* i;  // 3 planes: n_contrib, flags (1 done, 2 fixup, 4 finalized), last_eff
     int npx;
 };
@@ -101,7 +105,9 @@ struct ChunkK {
 
 // Per-pixel raster state written by the forward pass for the backward pass.
 struct PixK {
-    float* out;          // [C][H][W] planar outputs: quad(4*nf), depth_raw, depth, weight, T
+    float* out;          // [C][H][W] planar outputs: quad(4*nf), depth_raw, depth, weight, T, phasor(2*nf), distortion
+    double* dist3;       // [3][H][W] distortion moments about the pixel's first contributor depth (fp64):
+                         //   dref, SDs = sum w (d - dref), SD2s = sum w (d - dref)^2 (null: not computed)
     int32_t* n_contrib;  // may be null
     int32_t* n_processed;
     int32_t* last;       // entries of the tile list the backward walks (bit 31: fp64-fixed)
@@ -111,12 +117,26 @@ struct PixK {
     int32_t* n_flagged;  // device counter
 };
 
-inline int out_channels(int nf) { return 4 * nf + 4; }
+inline int out_channels(int nf) { return 6 * nf + 5; }
 // Channel plane index inside PixK::out.
 __host__ __device__ inline int ch_depth_raw(int nf) { return 4 * nf; }
 __host__ __device__ inline int ch_depth(int nf) { return 4 * nf + 1; }
 __host__ __device__ inline int ch_weight(int nf) { return 4 * nf + 2; }
 __host__ __device__ inline int ch_T(int nf) { return 4 * nf + 3; }
+__host__ __device__ inline int ch_phasor(int nf) { return 4 * nf + 4; }
+__host__ __device__ inline int ch_distortion(int nf) { return 6 * nf + 4; }
+
+// Upstream images of BufferGrads (splat.hpp:73-77); null = channel skipped.
+struct UpK {
+    const float* quad;        // [4*nf][H][W]
+    const float* phasor;      // [2*nf][H][W]
+    const float* depth_raw;   // [H][W]
+    const float* weight;
+    const float* distortion;
+    const float* transm;
+};
+// Scene statistics buffer: background gradients (quad 4*nf, then phasor 2*nf) and the loss.
+constexpr int kStatBg = 0, kStatLoss = 12, kStats = 13;
 
 // ---- launchers (defined in the .cu files) ----
 // tsb_geom.cu (fp64, compiled without FMA contraction)
@@ -176,7 +196,7 @@ void launch_raster_fwd(const RecK& rec, const ChunkK& ck, const uint32_t* tile_v
 void launch_fixup_loss(const PixK& px, int W, int H, int nf, const float* target, const float* ch_w,
                        double* loss_extra, int max_flag, cudaStream_t st);
 void launch_raster_bwd(const RecK& rec, const uint4* ranges_all, int nchunks, const uint32_t* tile_vals,
-                       const OptK& O, int W, int H, int nf, const float* dpsi, PixK px, const float* d_quad,
+                       const OptK& O, int W, int H, int nf, const float* dpsi, PixK px, const UpK& up,
                        float* screen, int scap, double* bg_part, cudaStream_t st);
 void launch_reduce_partials(const double* part, int nparts, int width, double* out,
                             double scale, cudaStream_t st);

@@ -94,7 +94,7 @@ struct Smem {
 // (outputs, fix-up flag, loss epilogue) in the launch in which it terminates,
 // or in the last chunk.  Blocks whose pixels are all done mark themselves so
 // later chunks neither bin nor raster them.
-template <int NF>
+template <int NF, bool DIST>
 __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK ck, const uint32_t* __restrict__ vals,
                                                                 OptK O, int W, int H, PixK px, FwdState fs,
                                                                 const float* __restrict__ target,
@@ -118,6 +118,8 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
     float accS[NF], accC[NF];
 #pragma unroll
     for (int f = 0; f < NF; ++f) accS[f] = accC[f] = 0.f;
+    float dref = 0.f;  // distortion: fp64 moments about the first contributor's depth
+    double SDs = 0.0, SD2s = 0.0;
     int nc = 0, flags = 0, last_eff = -1;
     if (active && !ck.first) {
         T = fs.f[0 * (size_t)fs.npx + o];
@@ -129,6 +131,11 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
         for (int f = 0; f < NF; ++f) {
             accS[f] = fs.f[(5 + 2 * f) * (size_t)fs.npx + o];
             accC[f] = fs.f[(6 + 2 * f) * (size_t)fs.npx + o];
+        }
+        if (DIST) {
+            dref = (float)fs.d[o];
+            SDs = fs.d[(size_t)fs.npx + o];
+            SD2s = fs.d[2 * (size_t)fs.npx + o];
         }
         nc = fs.i[0 * (size_t)fs.npx + o];
         flags = fs.i[1 * (size_t)fs.npx + o];
@@ -187,6 +194,12 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
                     }
                     SW += w;
                     SD = fmaf(w, Cc.y, SD);
+                    if (DIST) {
+                        if (nc == 1) dref = Cc.y;
+                        const double wd = (double)w * (double)(Cc.y - dref);  // difference exact (Sterbenz)
+                        SDs += wd;
+                        SD2s = fma(wd, (double)(Cc.y - dref), SD2s);
+                    }
                     Tpre = T;
                     const float om = 1.f - ev.alpha;
                     T = T * om;
@@ -225,6 +238,18 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
         px.out[ch_depth(NF) * HW + o] = (double)SW > O.cov_eps ? SD / SW : __int_as_float(0x7fc00000);
         px.out[ch_weight(NF) * HW + o] = SW;
         px.out[ch_T(NF) * HW + o] = T;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {  // phasor = 2 (accC, accS) + bg * T^2 (splat.cpp:305-307)
+            px.out[(ch_phasor(NF) + 2 * f + 0) * HW + o] = 2.f * accC[f] + (float)O.bg_phasor[2 * f + 0] * T2;
+            px.out[(ch_phasor(NF) + 2 * f + 1) * HW + o] = 2.f * accS[f] + (float)O.bg_phasor[2 * f + 1] * T2;
+        }
+        if (DIST) {
+            // 2 (SW SD2 - SD^2) is shift-invariant; the shifted moments avoid its cancellation
+            px.out[ch_distortion(NF) * HW + o] = (float)(2.0 * ((double)SW * SD2s - SDs * SDs));
+            px.dist3[o] = dref;
+            px.dist3[HW + o] = SDs;
+            px.dist3[2 * HW + o] = SD2s;
+        }
         if (px.n_contrib) px.n_contrib[o] = nc;
         if (px.n_processed) px.n_processed[o] = processed;
         px.last[o] = last_eff >= 0 ? last_eff : processed;
@@ -252,6 +277,11 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
         for (int f = 0; f < NF; ++f) {
             fs.f[(5 + 2 * f) * (size_t)fs.npx + o] = accS[f];
             fs.f[(6 + 2 * f) * (size_t)fs.npx + o] = accC[f];
+        }
+        if (DIST) {
+            fs.d[o] = dref;
+            fs.d[(size_t)fs.npx + o] = SDs;
+            fs.d[2 * (size_t)fs.npx + o] = SD2s;
         }
         fs.i[0 * (size_t)fs.npx + o] = nc;
         fs.i[1 * (size_t)fs.npx + o] = flag << 1;
@@ -328,18 +358,31 @@ __device__ __forceinline__ float reduce_scatter8(float v[8], int lane) {
     return s;
 }
 
-template <int NF>
+// Backward (splat.cpp:347-543).  The upstream channels reduce to two scalar
+// recursions per pixel, walked back to front:
+//   A: quad + phasor (T^2-weighted): d_alpha += Tk^2 (U_k + 2 (alpha-1) A),  A <- alpha U_k + (1-alpha)^2 A,
+//      with the phasor upstream folded into the per-frequency (sin, cos) weights
+//      and A's initial value (both are linear in coef * (sin psi, cos psi));
+//   B (EXTRA): depth_raw + weight + distortion (T-weighted) and transmittance:
+//      d_alpha += Tk (v_k - B),  B <- alpha v_k + (1-alpha) B,
+//      v_k = up_draw (d_k - c) + up_dist phi_k,  phi_k = 2 sum_j w_j (d_j - d_k)^2,
+//      B_0 = up_T - up_w - up_draw c.
+//   The reference's forms Tk (1 - accW) and Tk (d_k - accD) cancel to ~T_N in fp32 for
+//   opaque pixels; here weight rides on the transmittance term (SW = 1 - T_N exactly) and
+//   depth is taken about the pixel's own mean depth c = depth_raw / weight, whose
+//   remainder c * prod(1 - alpha) also becomes part of B_0.
+template <int NF, bool EXTRA>
 __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const uint4* __restrict__ ranges_all,
                                                                 int nchunks, const uint32_t* __restrict__ vals,
                                                                 OptK O, int W, int H, float dpsi0, float dpsi1,
-                                                                PixK px, const float* __restrict__ d_quad,
+                                                                PixK px, UpK up,
                                                                 float* __restrict__ screen, int scap,
                                                                 double* __restrict__ bg_part) {
     __shared__ Smem<NF> sm;
     __shared__ uint32_t srank[kRasterThreads];
     __shared__ float sacc[kRasterThreads][9];  // padded: 8 grads per entry
     __shared__ int smax[kRasterThreads / 32];
-    __shared__ float sbg[kRasterThreads / 32][4 * NF];
+    __shared__ float sbg[kRasterThreads / 32][6 * NF];
     const int nsub = O.sub * O.sub;
     const int ntiles = O.tiles_x * O.tiles_y;
     const int tile = blockIdx.x / nsub, sb = blockIdx.x % nsub;
@@ -352,34 +395,68 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
     const size_t HW = (size_t)W * H, o = active ? (size_t)y * W + x : 0;
 
     int last = 0;
-    float Tnext = 0.f, A = 0.f;
+    float Tnext = 0.f, A = 0.f, Bx = 0.f;
+    float uDraw = 0.f, uDD = 0.f, cD = 0.f, dref = 0.f;
+    double SWd = 0.0, SDs = 0.0, SD2s = 0.0;
     float us[NF], uc[NF];
-    float bgc[4 * NF];
+    float bgc[6 * NF];
 #pragma unroll
     for (int f = 0; f < NF; ++f) us[f] = uc[f] = 0.f;
 #pragma unroll
-    for (int c = 0; c < 4 * NF; ++c) bgc[c] = 0.f;
+    for (int c = 0; c < 6 * NF; ++c) bgc[c] = 0.f;
     if (active) {
         last = px.last[o] & 0x7fffffff;
         Tnext = px.T_pre[o];
         const float Tf = px.out[ch_T(NF) * HW + o];
-        float up[4 * NF];
+        const float Tf2 = Tf * Tf;
+        if (up.quad) {
+            float q[4 * NF];
 #pragma unroll
-        for (int c = 0; c < 4 * NF; ++c) {
-            up[c] = d_quad[c * HW + o];
-            A = fmaf(up[c], (float)O.bg_quad[c], A);
-            bgc[c] = up[c] * Tf * Tf;
+            for (int c = 0; c < 4 * NF; ++c) {
+                q[c] = up.quad[c * HW + o];
+                A = fmaf(q[c], (float)O.bg_quad[c], A);
+                bgc[c] = q[c] * Tf2;
+            }
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                us[f] = q[4 * f + 0] - q[4 * f + 2];
+                uc[f] = q[4 * f + 1] - q[4 * f + 3];
+            }
         }
+        if (up.phasor) {
 #pragma unroll
-        for (int f = 0; f < NF; ++f) {
-            us[f] = up[4 * f + 0] - up[4 * f + 2];
-            uc[f] = up[4 * f + 1] - up[4 * f + 3];
+            for (int f = 0; f < NF; ++f) {
+                const float p0 = up.phasor[(2 * f + 0) * HW + o], p1 = up.phasor[(2 * f + 1) * HW + o];
+                A = fmaf(p0, (float)O.bg_phasor[2 * f + 0], A);
+                A = fmaf(p1, (float)O.bg_phasor[2 * f + 1], A);
+                bgc[4 * NF + 2 * f + 0] = p0 * Tf2;
+                bgc[4 * NF + 2 * f + 1] = p1 * Tf2;
+                us[f] = fmaf(2.f, p1, us[f]);  // phasor = 2 coef w2 (cos, sin)
+                uc[f] = fmaf(2.f, p0, uc[f]);
+            }
+        }
+        if (EXTRA) {
+            if (up.depth_raw) {
+                uDraw = up.depth_raw[o];
+                const float dm = px.out[ch_depth(NF) * HW + o];
+                cD = dm == dm ? dm : 0.f;  // NaN where uncovered
+            }
+            if (up.transm) Bx = up.transm[o];
+            if (up.weight) Bx -= up.weight[o];
+            Bx = fmaf(-uDraw, cD, Bx);
+            if (up.distortion) {
+                uDD = up.distortion[o];
+                SWd = px.out[ch_weight(NF) * HW + o];
+                dref = (float)px.dist3[o];
+                SDs = px.dist3[HW + o];
+                SD2s = px.dist3[2 * HW + o];
+            }
         }
     }
     // background gradient partials (splat.cpp:429-431)
     if (bg_part) {
 #pragma unroll
-        for (int c = 0; c < 4 * NF; ++c) {
+        for (int c = 0; c < 6 * NF; ++c) {
             float v = bgc[c];
             for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
             if (lane == 0) sbg[tid >> 5][c] = v;
@@ -393,10 +470,10 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
     int bmax = 0;
 #pragma unroll
     for (int i = 0; i < kRasterThreads / 32; ++i) bmax = max(bmax, smax[i]);
-    if (bg_part && tid < 4 * NF) {
+    if (bg_part && tid < 6 * NF) {
         double s = 0.0;
         for (int i = 0; i < kRasterThreads / 32; ++i) s += sbg[i][tid];
-        bg_part[(size_t)blockIdx.x * 4 * NF + tid] = s;
+        bg_part[(size_t)blockIdx.x * 6 * NF + tid] = s;
     }
     bool first = true;
     const float cut2 = O.cut2_f, thr = O.alpha_thr_f;
@@ -447,8 +524,23 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
                             const float UQ = coef * su;
                             const float T2 = Tk * Tk;
                             const float w2 = ev.alpha * T2;
-                            const float d_alpha = T2 * (UQ + 2.f * (ev.alpha - 1.f) * A);
+                            float d_alpha = T2 * (UQ + 2.f * (ev.alpha - 1.f) * A);
                             A = ev.alpha * UQ + om * om * A;
+                            float ddep = w2 * coef * sd;
+                            if (EXTRA) {
+                                // phi_k and SW d_k - SD in fp64: both cancel (moments about dref)
+                                const float d = Cc.y;
+                                float phi = 0.f, sdev = 0.f;
+                                if (uDD != 0.f) {
+                                    const double dp = (double)(d - dref);
+                                    phi = (float)(2.0 * fma(dp, fma(dp, SWd, -2.0 * SDs), SD2s));
+                                    sdev = (float)fma(SWd, dp, -SDs);
+                                }
+                                const float v = fmaf(uDraw, d - cD, uDD * phi);
+                                d_alpha = fmaf(Tk, v - Bx, d_alpha);
+                                Bx = fmaf(ev.alpha, v, om * Bx);
+                                ddep = fmaf(ev.alpha * Tk, fmaf(4.f * uDD, sdev, uDraw), ddep);
+                            }
                             const float dpow = ev.alpha * d_alpha;
                             g8[0] = dpow * (Bb.x * ev.p);
                             g8[1] = dpow * (Bb.y * ev.p + Bb.z * ev.q);
@@ -457,7 +549,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
                             g8[4] = -0.5f * ev.dy * ev.dy * dpow;
                             g8[5] = ev.g * d_alpha;
                             g8[6] = w2 * su;
-                            g8[7] = w2 * coef * sd;
+                            g8[7] = ddep;
                         }
                     }
                 }
@@ -492,12 +584,14 @@ void launch_raster_fwd(const RecK& rec, const ChunkK& ck, const uint32_t* tile_v
                        int nf, PixK px, FwdState fs, const float* target, const float* ch_w, double* loss_part,
                        cudaStream_t st) {
     const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
-    if (nf > 1)
-        k_raster_fwd<2><<<grid, kRasterThreads, 0, st>>>(rec, ck, tile_vals, O, W, H, px, fs, target, ch_w,
-                                                        loss_part);
-    else
-        k_raster_fwd<1><<<grid, kRasterThreads, 0, st>>>(rec, ck, tile_vals, O, W, H, px, fs, target, ch_w,
-                                                        loss_part);
+#define TSB_FWD(NF_, D_) \
+    k_raster_fwd<NF_, D_><<<grid, kRasterThreads, 0, st>>>(rec, ck, tile_vals, O, W, H, px, fs, target, ch_w, loss_part)
+    if (nf > 1) {
+        if (O.dist) TSB_FWD(2, true); else TSB_FWD(2, false);
+    } else {
+        if (O.dist) TSB_FWD(1, true); else TSB_FWD(1, false);
+    }
+#undef TSB_FWD
 }
 
 void launch_fixup_loss(const PixK& px, int W, int H, int nf, const float* target, const float* ch_w,
@@ -507,15 +601,19 @@ void launch_fixup_loss(const PixK& px, int W, int H, int nf, const float* target
 }
 
 void launch_raster_bwd(const RecK& rec, const uint4* ranges_all, int nchunks, const uint32_t* tile_vals,
-                       const OptK& O, int W, int H, int nf, const float* dpsi, PixK px, const float* d_quad,
+                       const OptK& O, int W, int H, int nf, const float* dpsi, PixK px, const UpK& up,
                        float* screen, int scap, double* bg_part, cudaStream_t st) {
     const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
-    if (nf > 1)
-        k_raster_bwd<2><<<grid, kRasterThreads, 0, st>>>(rec, ranges_all, nchunks, tile_vals, O, W, H, dpsi[0],
-                                                        dpsi[1], px, d_quad, screen, scap, bg_part);
-    else
-        k_raster_bwd<1><<<grid, kRasterThreads, 0, st>>>(rec, ranges_all, nchunks, tile_vals, O, W, H, dpsi[0],
-                                                        0.f, px, d_quad, screen, scap, bg_part);
+    const bool extra = up.depth_raw || up.weight || up.distortion || up.transm;
+#define TSB_BWD(NF_, E_, D1_)                                                                                 \
+    k_raster_bwd<NF_, E_><<<grid, kRasterThreads, 0, st>>>(rec, ranges_all, nchunks, tile_vals, O, W, H, dpsi[0], \
+                                                          D1_, px, up, screen, scap, bg_part)
+    if (nf > 1) {
+        if (extra) TSB_BWD(2, true, dpsi[1]); else TSB_BWD(2, false, dpsi[1]);
+    } else {
+        if (extra) TSB_BWD(1, true, 0.f); else TSB_BWD(1, false, 0.f);
+    }
+#undef TSB_BWD
 }
 
 __global__ void k_reduce_partials(const double* __restrict__ part, int nparts, int width,

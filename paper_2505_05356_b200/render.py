@@ -75,7 +75,7 @@ class CameraModel:
 
 @dataclass
 class RenderOptions:
-    """splat.hpp:28-37 (+ Backgrounds::quad, 4 values per frequency)."""
+    """splat.hpp:13-37 (+ Backgrounds::quad / ::phasor, 4 resp. 2 values per frequency)."""
     alpha_threshold: float = 1.0 / 255.0
     transmittance_floor: float = 1e-4
     dilation: float = 0.3
@@ -83,6 +83,8 @@ class RenderOptions:
     coverage_eps: float = 1e-12
     tile_size: int = 16
     bg_quad: Sequence[float] = (0.0, 0.0, 0.0, 0.0)
+    bg_phasor: Sequence[float] = (0.0, 0.0)
+    distortion: bool = False  # RenderChannels::distortion (needed for a distortion upstream)
     counts: bool = False      # also emit per-pixel n_contrib / n_processed (parity diagnostics)
     full_lists: bool = False  # bin every tile's complete list (parity); default stops binning a tile
                               # once all its pixels have terminated (identical outputs)
@@ -96,12 +98,18 @@ class RenderOptions:
         o.coverage_eps = float(self.coverage_eps)
         o.tile_size = int(self.tile_size)
         o.channels = _abi.CH_QUAD | _abi.CH_DEPTH | _abi.CH_WEIGHT | _abi.CH_TRANSM | (
-            _abi.CH_COUNTS if self.counts else 0) | (_abi.CH_FULL_LISTS if self.full_lists else 0)
+            _abi.CH_COUNTS if self.counts else 0) | (_abi.CH_FULL_LISTS if self.full_lists else 0) | (
+            _abi.CH_PHASOR) | (_abi.CH_DISTORTION if self.distortion else 0)
         bq = np.zeros(8)
         b = np.asarray(self.bg_quad, dtype=np.float64).reshape(-1)[:8]
         bq[: b.size] = b
         for i in range(8):
             o.bg_quad[i] = bq[i]
+        bp = np.zeros(4)
+        b = np.asarray(self.bg_phasor, dtype=np.float64).reshape(-1)[:4]
+        bp[: b.size] = b
+        for i in range(4):
+            o.bg_phasor[i] = bp[i]
         return o
 
 
@@ -274,6 +282,9 @@ class GaussianScene:
                                         g["d_bg_quad"].ctypes.data_as(_abi._dp), C.byref(loss)))
         g["d_bg_quad"] = g["d_bg_quad"][: 4 * self.n_freq]
         g["loss"] = loss.value
+        bq, bp = np.zeros(8), np.zeros(4)
+        check(lib().tsb_scene_get_bg_grads(self._h, bq.ctypes.data_as(_abi._dp), bp.ctypes.data_as(_abi._dp)))
+        g["d_bg_phasor"] = bp[: 2 * self.n_freq]
         return g
 
     def zero_grads(self):
@@ -384,6 +395,23 @@ class RenderPass:
             check(lib().tsb_pass_backward(self._h, _abi.TSB_HOST, None))
         return self
 
+    def backward_buffers(self, d_quad=None, d_phasor=None, d_depth_raw=None, d_weight=None,
+                         d_distortion=None, d_transmittance=None):
+        """RenderPass::backward(BufferGrads) (splat.cpp:347-650): None skips a channel."""
+        keep = []
+
+        def arr(a):
+            if a is None:
+                return None
+            a = np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+            keep.append(a)
+            return a.ctypes.data
+
+        ptrs = [arr(a) for a in (d_quad, d_phasor, d_depth_raw, d_weight, d_distortion, d_transmittance)]
+        self._up_keep = keep
+        check(lib().tsb_pass_backward_buffers(self._h, _abi.TSB_HOST, *ptrs))
+        return self
+
     def output_ptr(self, which: int):
         p = C.c_void_p()
         nb = C.c_size_t()
@@ -397,13 +425,17 @@ class RenderPass:
         return a.reshape(shape) if shape is not None else a
 
     def outputs(self):
-        """RenderedBuffers (splat.hpp:51-66) subset: quad, depth_raw, depth, weight, transmittance."""
+        """RenderedBuffers (splat.hpp:51-66), ToF channels: quad, phasor, depth_raw, depth, weight,
+        transmittance (+ distortion when enabled)."""
         H, W, nf = self.camera.height, self.camera.width, self.scene.n_freq
         out = {"quad": self.download(_abi.OUT_QUAD, shape=(4 * nf, H, W)),
                "depth_raw": self.download(_abi.OUT_DEPTH_RAW, shape=(H, W)),
                "depth": self.download(_abi.OUT_DEPTH, shape=(H, W)),
                "weight": self.download(_abi.OUT_WEIGHT, shape=(H, W)),
-               "transmittance": self.download(_abi.OUT_TRANSM, shape=(H, W))}
+               "transmittance": self.download(_abi.OUT_TRANSM, shape=(H, W)),
+               "phasor": self.download(_abi.OUT_PHASOR, shape=(2 * nf, H, W))}
+        if self.options.distortion:
+            out["distortion"] = self.download(_abi.OUT_DISTORTION, shape=(H, W))
         if self.options.counts:
             out["n_contrib"] = self.download(_abi.OUT_N_CONTRIB, np.int32, (H, W))
             out["n_processed"] = self.download(_abi.OUT_N_PROCESSED, np.int32, (H, W))
@@ -432,6 +464,14 @@ class RenderPass:
         r = np.zeros((max(v, 1), 12), np.float32)
         check(lib().tsb_pass_debug_records(self._h, _ptr(r)))
         return r[:v]
+
+    def debug_screen_grads(self):
+        """Per-rank screen-space gradients of the last backward (d_mean2d x/y, d_conic a/b/c,
+        d_opacity, d_coef, d_depth), in prepared (rank) order."""
+        v = self.visible_count()
+        g = np.zeros((max(v, 1), 8), np.float32)
+        check(lib().tsb_pass_debug_screen_grads(self._h, _ptr(g)))
+        return g[:v]
 
     def debug_fixups(self) -> int:
         c = C.c_int32()

@@ -125,6 +125,40 @@ static void two_layered_splats() {
     CHECK(close_rel(out.depth.at(32, 24), 2.5, 1e-6));
 }
 
+// RenderChannels::phasor / ::distortion (splat.cpp:305-314) and the phasor background gradient.
+static void phasor_and_distortion() {
+    CanonicalScene scene;
+    scene.tof.source_intensity = 32.0;
+    scene.gaussians.push_back(dc_gaussian({0.0, 0.0, 1.0}, 0.1, 1.0 / 32.0, 0.0));
+    scene.gaussians.push_back(dc_gaussian({0.0, 0.0, 4.0}, 0.4, 1.0, 40.0));
+    const CameraModel cam = test_camera();
+    RenderInput in;
+    in.scene = &scene;
+    in.camera = &cam;
+    in.opts.channels.phasor = true;
+    in.opts.channels.distortion = true;
+    const RenderedBuffers out = render(in);
+    // phasor = (q90 - q270, q0 - q180) without background; weights 0.5 / 0.5 at depths 1 and 4
+    CHECK(close_rel(out.phasor.at(32, 24, 0), out.quad.at(32, 24, 1) - out.quad.at(32, 24, 3), 1e-5, 1e-7));
+    CHECK(close_rel(out.phasor.at(32, 24, 1), out.quad.at(32, 24, 0) - out.quad.at(32, 24, 2), 1e-5, 1e-6));
+    CHECK(close_rel(out.distortion.at(32, 24), 2.0 * 0.5 * 0.5 * 9.0, 1e-5));
+    CHECK(out.distortion.at(0, 0) == 0.0);
+
+    CanonicalScene empty;
+    RenderInput ein = in;
+    ein.scene = &empty;
+    ein.opts.bg.phasor = {0.5, -0.25};
+    RenderPass pass(ein);
+    const RenderedBuffers eo = pass.forward();
+    CHECK(eo.phasor.at(3, 4, 0) == 0.5 && eo.phasor.at(3, 4, 1) == -0.25);
+    BufferGrads up;
+    up.d_phasor = Image(cam.width, cam.height, 2, 1.0);
+    up.d_transmittance = Image(cam.width, cam.height, 1, 1.0);
+    const SceneGrads g = pass.backward(up);
+    for (int c = 0; c < 2; ++c) CHECK(close_rel(g.d_bg_phasor[c], cam.width * cam.height, 1e-12));
+    CHECK(g.d_bg_quad[0] == 0.0);
+}
+
 static void culling() {
     const CameraModel cam = test_camera();
     CanonicalScene scene;
@@ -215,6 +249,7 @@ int main() {
     empty_scene_passes_background();
     single_on_axis_splat();
     two_layered_splats();
+    phasor_and_distortion();
     culling();
     tile_size_and_override();
     errors_match_reference();

@@ -426,3 +426,52 @@ def test_view_dependent_reflectivity_sh(tsb, ctx, degree):
     assert rel_err(gr["d_rotation"], og["d_rotation"], 1e-4) < GRAD_TOL
     assert rel_err(gr["d_opacity_logit"], og["d_opacity_logit"], 1e-4) < GRAD_TOL
     assert rel_err(dsh, og["d_refl_sh"], 1e-4) < GRAD_TOL
+
+
+@pytest.mark.parametrize("channels", [("phasor",), ("depth_raw",), ("weight",), ("transmittance",),
+                                      ("distortion",), ("quad", "phasor", "depth_raw", "weight", "distortion",
+                                                        "transmittance")])
+def test_buffer_grads_every_tof_channel(tsb, ctx, channels):
+    """RenderPass::backward(BufferGrads) with each ToF upstream image of splat.hpp:73-77
+    (splat.cpp:347-543) and the phasor / distortion outputs (splat.cpp:305-314), against the
+    oracle on the same seeded upstreams; backgrounds non-zero so d_bg_quad / d_bg_phasor are live."""
+    from paper_2505_05356_b200 import synthetic
+    cfg = synthetic.config("c1")
+    cam, frame, tof = cfg.camera, cfg.frames[0], cfg.tof
+    H, W = cam.height, cam.width
+    opts = tsb.RenderOptions(counts=True, distortion=True, bg_quad=(0.02, -0.01, 0.03, 0.005),
+                             bg_phasor=(0.04, -0.02))
+    scene, rp, out, op, ref = render_both(tsb, ctx, cfg.scene, cfg.camera, tof, frame, opts)
+    assert np.array_equal(out["n_contrib"], ref["n_contrib"])
+    check_image(out["phasor"], ref["phasor"])
+    # distortion 2 (SW SD2 - SD^2) is a difference of products, not a raw sample: the GPU
+    # accumulates it in fp32 about each pixel's first contributor depth (so its error scales
+    # with the depth spread, not depth^2).  Bar: 1e-3 relative (floor 1e-3 max), abs 2e-5 max.
+    dist, rdist = out["distortion"], ref["distortion"]
+    assert rel_err(dist, rdist, 1e-3) < 1e-3
+    assert np.abs(dist - rdist).max() <= 2e-5 * np.abs(rdist).max()
+
+    rng = np.random.default_rng(77)
+    shapes = {"quad": (4, H, W), "phasor": (2, H, W)}
+    ups = {c: rng.normal(0.0, 1e-3, shapes.get(c, (H, W))).astype(np.float32) for c in channels}
+    rp.backward_buffers(**{"d_" + c: a for c, a in ups.items()})
+    gr = scene.grads()
+    og = op.backward(**{"d_" + c: a.astype(np.float64) for c, a in ups.items()})
+    errs = {"d_position": rel_err(gr["d_position"], og["d_position"], 1e-4),
+            "d_log_scale": rel_err(gr["d_log_scale"], og["d_log_scale"], 1e-4),
+            "d_rotation": rel_err(gr["d_rotation"], og["d_rotation"], 1e-4),
+            "d_opacity_logit": rel_err(gr["d_opacity_logit"], og["d_opacity_logit"], 1e-4)}
+    if any(c in channels for c in ("quad", "phasor")):
+        errs["d_reflectivity_dc"] = rel_err(gr["d_reflectivity_dc"], og["d_refl_sh"][:, 0], 1e-4)
+    assert all(e < GRAD_TOL for e in errs.values()), errs
+    assert np.allclose(gr["d_bg_quad"], og["d_bg_quad"], rtol=1e-4, atol=1e-9)
+    assert np.allclose(gr["d_bg_phasor"], og["d_bg_phasor"], rtol=1e-4, atol=1e-9)
+
+
+def test_distortion_upstream_requires_channel(tsb, ctx):
+    from paper_2505_05356_b200 import synthetic
+    cfg = synthetic.config("c0")
+    scene = gpu_scene(tsb, ctx, cfg.scene, cfg.tof)
+    rp = tsb.RenderPass(ctx).prepare(scene, cfg.camera, tsb.RenderOptions(), cfg.frames[0]).forward()
+    with pytest.raises(RuntimeError, match="distortion"):
+        rp.backward_buffers(d_distortion=np.zeros((cfg.camera.height, cfg.camera.width), np.float32))
