@@ -203,8 +203,8 @@ def bench_c3(args, dist, tsb, synthetic):
     ctx = tsb.Context(dist.local)
     scene = tsb.GaussianScene(ctx, g.n, g.n_keyframes, cfg.tof)
     scene.set_params(g.position, g.log_scale, g.rotation, g.opacity_logit, g.reflectivity_dc, g.motion)
-    # two passes (two streams) alternate over frames so consecutive frames overlap
-    passes = [tsb.RenderPass(ctx) for _ in range(2)]
+    # render passes (one stream each) rotate over frames so consecutive frames overlap on the device
+    passes = [tsb.RenderPass(ctx) for _ in range(args.passes)]
     rp = passes[0]
     opts = tsb.RenderOptions()
     my_frames = cfg.frames[dist.rank::dist.world]
@@ -230,6 +230,7 @@ def bench_c3(args, dist, tsb, synthetic):
         ms = timer.stop_ms()
     ctx.synchronize()
     launches = ctx.launch_count() - l0
+    redos = ctx.redo_count()
     # per-stage device times (roofline): same frames, one pass, stage events on its stream
     ctx.stage_times()
     ctx.set_profiling(True)
@@ -248,8 +249,11 @@ def bench_c3(args, dist, tsb, synthetic):
     # every step, D2H of every rendered frame's quad/depth/weight into pinned host memory.
     import torch
     H, W = cfg.camera.height, cfg.camera.width
-    pin = {k_: torch.empty(sz, dtype=torch.float32, pin_memory=True).numpy() for k_, sz in
-           [("quad", 4 * H * W), ("depth", H * W), ("weight", H * W)]}
+    # one pinned landing buffer set per pass: a pass's previous frame has landed (and is
+    # consumed) when the pass is prepared again
+    pins = [{k_: torch.empty(sz, dtype=torch.float32, pin_memory=True).numpy() for k_, sz in
+             [("quad", 4 * H * W), ("depth", H * W), ("weight", H * W)]} for _ in passes]
+    pin = pins[0]
     host = {k_: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy() for k_, a in
             [("position", g.position), ("log_scale", g.log_scale), ("rotation", g.rotation),
              ("opacity_logit", g.opacity_logit), ("reflectivity_dc", g.reflectivity_dc), ("motion", g.motion)]}
@@ -260,12 +264,15 @@ def bench_c3(args, dist, tsb, synthetic):
         scene.set_params(host["position"], host["log_scale"], host["rotation"], host["opacity_logit"],
                          host["reflectivity_dc"], host["motion"])
         for i, fr in enumerate(my_frames):
-            q = passes[i % 2]
+            j = i % len(passes)
+            q = passes[j]
             q.prepare(scene, cfg.camera, opts, fr)
             q.forward()
-            for which, buf in ((tsb._abi.OUT_QUAD, pin["quad"]), (tsb._abi.OUT_DEPTH, pin["depth"]),
-                               (tsb._abi.OUT_WEIGHT, pin["weight"])):
-                tsb._abi.check(tsb._abi.lib().tsb_pass_download(q.handle, which, buf.ctypes.data, buf.nbytes))
+            for which, buf in ((tsb._abi.OUT_QUAD, pins[j]["quad"]), (tsb._abi.OUT_DEPTH, pins[j]["depth"]),
+                               (tsb._abi.OUT_WEIGHT, pins[j]["weight"])):
+                q.download_async(which, buf)
+        for q in passes:
+            q.wait()
 
     e2e_step()
     dist.barrier()
@@ -275,14 +282,16 @@ def bench_c3(args, dist, tsb, synthetic):
     ctx.synchronize()
     e2e_s = dist.max(time.perf_counter() - t0)
     e2e = {"value": round(frames_total / e2e_s, 3), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
-           "d2h_bytes_per_step": int(d2h), "timer": "host wall clock around synchronous API calls"}
+           "d2h_bytes_per_step": int(d2h),
+           "timer": "host wall clock; scene H2D from pinned memory, every frame's quad/depth/weight D2H into pinned "
+                    "per-pass buffers (tsb_pass_download_async), all landed before the clock stops"}
 
     shapes = dict(n=g.n, k=k, v=v, ntiles=((W + 15) // 16) * ((H + 15) // 16), n_keyframes=g.n_keyframes,
                   npx=H * W)
     stage_ms = {name: (t / args.steps, c // args.steps) for name, (t, c) in st.items()}
     roof = pick_roofline(stage_ms, shapes, load_peaks())
     info = {"visible": v, "keys_per_frame": k, "fixup_pixels_last_frame": fixups, "clock": clk.summary(),
-            "launches": launches, "passes_in_flight": len(passes),
+            "launches": launches, "passes_in_flight": len(passes), "redone_frames": redos,
             "stage_timing": "separate single-pass loop after the timed region (events on the pass stream)"}
     return value, ms_max / args.steps, e2e, roof, info, ctx
 
@@ -312,7 +321,7 @@ def bench_train_c4(args, dist, tsb, synthetic, ctx):
         comm = tsb.Comm(ctx, uid, dist.world, dist.rank)
     from paper_2505_05356_b200.parallel import FrameShardedTrainer, shard_indices
     trainer = FrameShardedTrainer(ctx, scene, cam, opts, lr=tsb.LrTable.uniform(cfg.lr), comm=comm,
-                                  rank=dist.rank, world=dist.world)
+                                  rank=dist.rank, world=dist.world, passes=args.train_passes)
     mine = {f: j for j, f in enumerate(shard_indices(len(cfg.frames), dist.rank, dist.world))}
 
     def it():
@@ -342,7 +351,7 @@ def bench_train_c4(args, dist, tsb, synthetic, ctx):
            "iters_per_s": round(args.train_steps / (ms_max / 1e3), 4),
            "ms_per_iter": round(ms_max / args.train_steps, 3),
            "stage_ms_per_iter": {k: round(v[0], 3) for k, v in st.items() if v[1]},
-           "keys_per_frame_last": trainer.rp.num_keys(), "passes_in_flight": 2,
+           "keys_per_frame_last": trainer.rp.num_keys(), "passes_in_flight": len(trainer.passes),
            "path": "parallel.FrameShardedTrainer (public API)"}
     if comm:
         comm.close()
@@ -415,6 +424,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--passes", type=int, default=6, help="render passes (streams) in flight")
+    ap.add_argument("--train-passes", type=int, default=3)
     ap.add_argument("--train-steps", type=int, default=3)
     ap.add_argument("--train-n", type=int, default=None)
     ap.add_argument("--cpu-frames", type=int, default=2)

@@ -123,6 +123,11 @@ void* tsb_ctx_stream(tsb_ctx* ctx);
 int tsb_ctx_join(tsb_ctx* ctx);
 /* Number of kernels this context has launched (bench.py gpu_launches). */
 int64_t tsb_ctx_launch_count(tsb_ctx* ctx);
+/* Frames redone after a device-side abort (tile-list storage overflow or an
+ * over-long fp32 depth tie run).  Passes never wait for the device inside
+ * prepare/forward/backward; a pass is settled (synchronised, and redone if its
+ * frame aborted) before its results are read or the scene it read is changed. */
+int64_t tsb_ctx_redo_count(tsb_ctx* ctx);
 
 /* Per-stage device timing (CUDA events recorded on the context stream around each
  * stage's kernels).  Stages: see TSB_STAGE_*.  tsb_ctx_stage_times synchronises,
@@ -218,6 +223,13 @@ enum {
 int tsb_pass_output(tsb_pass* p, int which, void** dptr, size_t* bytes);
 /* Copy a pass-owned buffer to host memory (synchronous). */
 int tsb_pass_download(tsb_pass* p, int which, void* host, size_t bytes);
+/* Enqueue the copy of a pass-owned buffer into host memory (pinned memory for
+ * overlap) without waiting.  The bytes are valid once the pass is settled:
+ * tsb_pass_wait, tsb_ctx_synchronize, or the pass's next tsb_pass_prepare (a
+ * frame redone after a device-side abort re-issues its downloads). */
+int tsb_pass_download_async(tsb_pass* p, int which, void* host, size_t bytes);
+/* Settle the pass (redo an aborted frame) and wait for everything enqueued on it. */
+int tsb_pass_wait(tsb_pass* p);
 
 /* RenderPass::backward (splat.cpp:347-650) for the quad channel.  d_quad: NULL
  * uses the loss residual written by tsb_pass_forward_loss, else an upstream
@@ -246,6 +258,9 @@ int tsb_pass_debug_screen_grads(tsb_pass* p, float* g8 /* 8 per rank */);
 /* Keep a copy of the screen-space gradients of every following backward (the chain kernel
  * consumes them); required before tsb_pass_debug_screen_grads. */
 int tsb_pass_debug_keep_screen(tsb_pass* p, int enabled);
+/* Test hook: shrink the pass's tile-list storage to `entries` (>= 1) so the next
+ * frame overflows and exercises the device-side abort + settle/redo path. */
+int tsb_pass_debug_set_list_capacity(tsb_pass* p, uint32_t entries);
 /* Pixels the fp32 raster flagged as decision-ambiguous and recomposited in fp64. */
 int tsb_pass_debug_fixups(tsb_pass* p, int32_t* count);
 /* The fixed pixels themselves: pixel index | reason << 24 (1 maha, 2 alpha, 4 T band). */

@@ -79,6 +79,7 @@ SIGNATURES = {
     "tsb_ctx_join": (C.c_int, [_vp]),
     "tsb_pass_stream": (_vp, [_vp]),
     "tsb_ctx_launch_count": (C.c_int64, [_vp]),
+    "tsb_ctx_redo_count": (C.c_int64, [_vp]),
     "tsb_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "tsb_ctx_stage_times": (C.c_int, [_vp, _dp, _lp]),
     "tsb_scene_create": (C.c_int, [_vp, C.POINTER(SceneDesc), C.POINTER(_vp)]),
@@ -104,9 +105,12 @@ SIGNATURES = {
     "tsb_pass_forward_loss": (C.c_int, [_vp, C.c_int, _vp, _dp, _dp]),
     "tsb_pass_output": (C.c_int, [_vp, C.c_int, C.POINTER(_vp), C.POINTER(C.c_size_t)]),
     "tsb_pass_download": (C.c_int, [_vp, C.c_int, _vp, C.c_size_t]),
+    "tsb_pass_download_async": (C.c_int, [_vp, C.c_int, _vp, C.c_size_t]),
+    "tsb_pass_wait": (C.c_int, [_vp]),
     "tsb_pass_backward": (C.c_int, [_vp, C.c_int, _vp]),
     "tsb_pass_backward_buffers": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]),
     "tsb_pass_debug_keep_screen": (C.c_int, [_vp, C.c_int]),
+    "tsb_pass_debug_set_list_capacity": (C.c_int, [_vp, C.c_uint32]),
     "tsb_pass_debug_prepared": (C.c_int, [_vp, _ip, _ip]),
     "tsb_pass_debug_tiles": (C.c_int, [_vp, _ip, _ip, _lp, _ip]),
     "tsb_pass_debug_records": (C.c_int, [_vp, _fp]),

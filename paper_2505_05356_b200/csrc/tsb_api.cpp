@@ -1,9 +1,13 @@
 // C-ABI implementation (include/tsb.h): contexts, device scenes, reusable
 // render-pass workspaces, fused Adam, NCCL gradient reduction.
 //
-// Host code only; every device operation is stream-ordered on the context's
-// stream.  tsb_pass_prepare synchronises once per frame to learn the number of
-// tile keys (the CUB radix sort needs it on the host).
+// Host code only; every device operation is stream-ordered.  A render pass
+// never waits for the device inside prepare/forward/backward: every depth chunk
+// is enqueued and decides on the device whether it has work (tsb_bin.cu
+// chunk_live), and the frame's abort word (list-storage overflow, over-long
+// fp32 tie run) is read back asynchronously.  The pass is *settled* -- synchronised,
+// and on an abort redone with more storage / the exact sort -- before anything
+// observes its results or changes what it read (settle / settle_all).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -71,6 +75,7 @@ struct tsb_ctx {
     size_t ev_used = 0;
     std::vector<std::pair<int, size_t>> ev_marks;  // (stage, index of start event)
     std::vector<tsb_pass*> passes;                 // joined by tsb_ctx_join
+    int64_t redos = 0;                             // frames redone after a device-side abort
 };
 
 namespace {
@@ -187,6 +192,19 @@ struct tsb_pass {
     int* fx_work_n = nullptr;
     Rec64* fx_cache = nullptr;
     int frame_stamp = 0;
+    // deferred settle: what was enqueued since the last check of the abort word
+    bool pending = false;
+    bool pend_loss = false, pend_bwd = false;
+    const float* pend_target = nullptr;
+    ChW pend_chw{};
+    UpK pend_up{};
+    struct Download {
+        int which;
+        void* host;
+        size_t bytes;
+    };
+    std::vector<Download> pend_dl;  // asynchronous output downloads of the unsettled frame
+    int planned_n = -1, planned_tiles = -1;  // chunk plan cache
 };
 
 extern "C" {
@@ -258,11 +276,26 @@ void tsb_ctx_destroy(tsb_ctx* c) {
     delete c;
 }
 
+namespace {
+int settle(tsb_pass* p);
+int settle_all(tsb_ctx* c) {
+    for (tsb_pass* p : c->passes) {
+        int rc = settle(p);
+        if (rc) return rc;
+    }
+    return TSB_OK;
+}
+}  // namespace
+
 int tsb_ctx_join(tsb_ctx* c) {
     if (!c) return fail(TSB_ERR_INVALID, "null context");
+    int rc = settle_all(c);
+    if (rc) return rc;
     for (tsb_pass* p : c->passes) TSB_CUDA(cudaStreamWaitEvent(c->stream, p->done_ev, 0));
     return TSB_OK;
 }
+
+int64_t tsb_ctx_redo_count(tsb_ctx* c) { return c ? c->redos : 0; }
 
 int tsb_ctx_synchronize(tsb_ctx* c) {
     int rc = tsb_ctx_join(c);
@@ -415,6 +448,10 @@ int tsb_scene_get_grads(tsb_scene* s, float* d_position, float* d_log_scale, flo
                         float* d_opacity_logit, float* d_reflectivity_dc, float* d_motion, double* d_bg_quad,
                         double* loss) {
     if (!s) return fail(TSB_ERR_INVALID, "null scene");
+    {
+        int rc0 = settle_all(s->ctx);
+        if (rc0) return rc0;
+    }
     TSB_CUDA(cudaSetDevice(s->ctx->device));
     const int n = s->d.n;
     int rc;
@@ -437,6 +474,10 @@ int tsb_scene_get_grads(tsb_scene* s, float* d_position, float* d_log_scale, flo
 
 int tsb_scene_get_bg_grads(tsb_scene* s, double* d_bg_quad, double* d_bg_phasor) {
     if (!s) return fail(TSB_ERR_INVALID, "null scene");
+    {
+        int rc0 = settle_all(s->ctx);
+        if (rc0) return rc0;
+    }
     TSB_CUDA(cudaSetDevice(s->ctx->device));
     TSB_CUDA(cudaStreamWaitEvent(s->ctx->stream, s->grads_ev, 0));
     double st[kStats];
@@ -476,6 +517,10 @@ int tsb_scene_set_sh(tsb_scene* s, int where, const float* refl_sh) {
 
 int tsb_scene_get_sh(tsb_scene* s, float* refl_sh, int grads) {
     if (!s || !refl_sh) return fail(TSB_ERR_INVALID, "tsb_scene_get_sh: null argument");
+    if (grads) {
+        int rc0 = settle_all(s->ctx);
+        if (rc0) return rc0;
+    }
     TSB_CUDA(cudaSetDevice(s->ctx->device));
     const int n = s->d.n;
     if (n == 0) return TSB_OK;
@@ -500,6 +545,10 @@ int tsb_scene_get_sh(tsb_scene* s, float* refl_sh, int grads) {
 
 int tsb_scene_zero_grads(tsb_scene* s) {
     if (!s) return fail(TSB_ERR_INVALID, "null scene");
+    {
+        int rc0 = settle_all(s->ctx);
+        if (rc0) return rc0;
+    }
     TSB_CUDA(cudaSetDevice(s->ctx->device));
     const size_t nel = (size_t)s->narrays * (size_t)std::max(s->d.n, 1);
     TSB_CUDA(cudaStreamWaitEvent(s->ctx->stream, s->grads_ev, 0));
@@ -519,6 +568,10 @@ int tsb_scene_get_adam_state(tsb_scene* s, float* m_position, float* v_position)
 
 int tsb_scene_get_densify_stat(tsb_scene* s, float* grad_norm_sum, int64_t* count) {
     if (!s) return fail(TSB_ERR_INVALID, "null scene");
+    {
+        int rc0 = settle_all(s->ctx);
+        if (rc0) return rc0;
+    }
     TSB_CUDA(cudaSetDevice(s->ctx->device));
     if (grad_norm_sum && s->d.n > 0) {
         TSB_CUDA(cudaStreamWaitEvent(s->ctx->stream, s->grads_ev, 0));
@@ -765,6 +818,7 @@ PixK pixk(tsb_pass* p) {
     px.dist3 = (p->channels & TSB_CH_DISTORTION) ? p->dist3 : nullptr;
     px.flagged = p->flagged;
     px.n_flagged = p->counters + 1;
+    px.abort = p->counters + 2;
     return px;
 }
 
@@ -788,6 +842,8 @@ SceneK scenek(const tsb_scene* s) {
 }
 
 int read_visible(tsb_pass* p) {
+    int rc0 = settle(p);
+    if (rc0) return rc0;
     if (p->V >= 0) return TSB_OK;
     int32_t* h = (int32_t*)((char*)p->pinned + 1024);
     TSB_CUDA(cudaMemcpyAsync(h, p->counters, 4, cudaMemcpyDeviceToHost, p->stream));
@@ -819,7 +875,12 @@ void tsb_pass_destroy(tsb_pass* p) {
 int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb_render_options* opt,
                      const tsb_frame* frame) {
     if (!p) return fail(TSB_ERR_INVALID, "null pass");
+    {
+        int rc0 = settle(p);  // the previous frame of this pass (its buffers are reused)
+        if (rc0) return rc0;
+    }
     p->prepared = p->forwarded = p->have_loss = false;
+    p->pend_loss = p->pend_bwd = false;
     // RenderPassImpl ctor checks (splat.cpp:91-100)
     if (!s || !cam) return fail(TSB_ERR_INVALID, "render: scene and camera required");
     if (!(cam->fx > 0 && cam->fy > 0 && cam->width > 0 && cam->height > 0 && cam->near_plane > 0 &&
@@ -882,7 +943,11 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     int rc;
     if ((rc = ensure_gauss(p, n))) return rc;
     if ((rc = ensure_pixels(p, p->W, p->H, p->ntiles, p->nblocks))) return rc;
-    if ((rc = plan_chunks(p, n))) return rc;
+    if (n != p->planned_n || p->ntiles != p->planned_tiles) {
+        if ((rc = plan_chunks(p, n))) return rc;
+        p->planned_n = n;
+        p->planned_tiles = p->ntiles;
+    }
     if ((rc = ensure_vals(p, std::max<uint64_t>({(uint64_t)n * 8, (uint64_t)p->ntiles * 1024, 1u << 20}))))
         return rc;
 
@@ -899,7 +964,7 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     {
         Stage sg(p->ctx, TSB_STAGE_DEPTH_SORT, st);
         p->ctx->launches += launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, p->depth64, p->counters,
-                                              p->counters + 4, key_range, n, p->sort_scratch, st);
+                                              p->counters + 2, key_range, n, p->sort_scratch, st);
     }
     p->sorted = p->gidx_b;
     p->ctx->launches += 1;
@@ -923,6 +988,8 @@ int tsb_pass_visible_count(tsb_pass* p, int32_t* out) {
 int tsb_pass_num_keys(tsb_pass* p, int64_t* out) {
     if (!p || !out) return fail(TSB_ERR_INVALID, "null argument");
     if (!p->forwarded) return fail(TSB_ERR_INVALID, "tile lists are built by forward()");
+    int rc0 = settle(p);
+    if (rc0) return rc0;
     uint32_t* h = (uint32_t*)((char*)p->pinned + 1040);
     TSB_CUDA(cudaMemcpyAsync(h, p->list_off, 4, cudaMemcpyDeviceToHost, p->stream));
     TSB_CUDA(cudaStreamSynchronize(p->stream));
@@ -932,148 +999,189 @@ int tsb_pass_num_keys(tsb_pass* p, int64_t* out) {
 
 namespace {
 
-// Chunked binning + forward composite (+ fused loss); see tsb_bin.cu.
-int run_forward(tsb_pass* p, const float* target, bool loss) {
-    if (!p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
+// Chunked binning + forward composite (+ fused loss); see tsb_bin.cu.  Enqueues
+// every planned chunk; chunks without work return on the device.  Ends with an
+// asynchronous read-back of the counters (visible count, abort word) that
+// settle() inspects.
+int enqueue_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw) {
     TSB_CUDA(cudaSetDevice(p->ctx->device));
     cudaStream_t st = p->stream;
     PixK px = pixk(p);
     const bool full = (p->channels & TSB_CH_FULL_LISTS) != 0;
-    const int n = p->scene->d.n;
-    int32_t* hc = (int32_t*)((char*)p->pinned + 2048);
-    for (int attempt = 0; attempt < 8; ++attempt) {
-        TSB_CUDA(cudaMemsetAsync(p->counters + 1, 0, sizeof(int32_t) * 3, st));
-        TSB_CUDA(cudaMemsetAsync(p->list_off, 0, sizeof(uint32_t), st));
-        TSB_CUDA(cudaMemsetAsync(p->block_done, 0, sizeof(int32_t) * p->nblocks, st));
-        TSB_CUDA(cudaMemsetAsync(p->tile_blocks_done, 0, sizeof(int32_t) * p->ntiles, st));
-        if (loss) TSB_CUDA(cudaMemsetAsync(p->loss_part, 0, sizeof(double) * p->nblocks, st));
-        FwdState fs{p->st_f, p->st_d, p->st_i, p->W * p->H};
-        BinK B{};
-        B.sorted_gidx = p->sorted;
-        B.rect = p->rect;
-        B.n_visible = p->counters;
-        B.ts = p->opt.ts;
-        B.tiles_x = p->opt.tiles_x;
-        B.tiles_y = p->opt.tiles_y;
-        B.ntiles = p->ntiles;
-        B.tile_blocks_done = p->tile_blocks_done;
-        B.blocks_per_tile = p->opt.sub * p->opt.sub;
-        B.skip_done = full ? 0 : 1;
-        B.hist = p->hist;
-        B.tile_len = p->tile_len;
-        B.tile_start = p->tile_start;
-        B.vals = p->vals;
-        B.list_off = p->list_off;
-        B.capacity = p->vals_cap;
-        B.overflow = p->counters + 2;
-        int nch = 0;
-        const int total_chunks = (int)p->chunk_seg0.size();
-        for (int c = 0; c < std::max(total_chunks, 1); ++c) {
-            const int seg0 = total_chunks ? p->chunk_seg0[c] : 0;
-            const int nseg = total_chunks ? p->chunk_nseg[c] : 0;
-            B.seg0 = seg0;
-            B.nseg = nseg;
-            B.chunk = c;
-            B.ranges = p->ranges_all + (size_t)c * p->ntiles;
-            B.prev_ranges = c ? p->ranges_all + (size_t)(c - 1) * p->ntiles : nullptr;
-            if (nseg > 0) {
-                Stage sg(p->ctx, TSB_STAGE_BINNING, st);
-                launch_bin_chunk(B, st);
-                p->ctx->launches += 4;
-            } else {
-                TSB_CUDA(cudaMemsetAsync(B.ranges, 0, sizeof(uint4) * p->ntiles, st));
-            }
-            ChunkK ck;
-            ck.ranges = B.ranges;
-            ck.first = c == 0;
-            ck.chunk_end_rank = (seg0 + nseg) * kSeg;
-            ck.n_visible = p->counters;
-            ck.block_done = p->block_done;
-            ck.tile_blocks_done = p->tile_blocks_done;
-            ck.blocks_done_total = p->counters + 3;
-            ck.overflow = p->counters + 2;
-            {
-                Stage sg(p->ctx, TSB_STAGE_RASTER_FWD, st);
-                launch_raster_fwd(p->rec, ck, p->vals, p->opt, p->W, p->H, p->nf, px, fs, loss ? target : nullptr,
-                                  p->chw, p->loss_part, st);
-                p->ctx->launches += 1;
-            }
-            TSB_CHECK_LAUNCH();
-            nch = c + 1;
-            if (c + 1 >= total_chunks) break;
-            // continue only while some tile is unfinished and visible ranks remain
-            TSB_CUDA(cudaMemcpyAsync(hc, p->counters, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost, st));
-            TSB_CUDA(cudaStreamSynchronize(st));
-            p->V = hc[0];
-            if (hc[2] || hc[4]) break;  // overflow / long tie run: retry below
-            if (ck.chunk_end_rank >= hc[0]) break;
-            if (!full && hc[3] >= p->nblocks) break;
+    // counters[2] (abort word) is not cleared here: the depth sort of prepare may have set it
+    TSB_CUDA(cudaMemsetAsync(p->counters + 1, 0, sizeof(int32_t), st));
+    TSB_CUDA(cudaMemsetAsync(p->counters + 3, 0, sizeof(int32_t), st));
+    TSB_CUDA(cudaMemsetAsync(p->list_off, 0, sizeof(uint32_t), st));
+    TSB_CUDA(cudaMemsetAsync(p->block_done, 0, sizeof(int32_t) * p->nblocks, st));
+    TSB_CUDA(cudaMemsetAsync(p->tile_blocks_done, 0, sizeof(int32_t) * p->ntiles, st));
+    if (loss) TSB_CUDA(cudaMemsetAsync(p->loss_part, 0, sizeof(double) * p->nblocks, st));
+    FwdState fs{p->st_f, p->st_d, p->st_i, p->W * p->H};
+    BinK B{};
+    B.sorted_gidx = p->sorted;
+    B.rect = p->rect;
+    B.n_visible = p->counters;
+    B.ts = p->opt.ts;
+    B.tiles_x = p->opt.tiles_x;
+    B.tiles_y = p->opt.tiles_y;
+    B.ntiles = p->ntiles;
+    B.tile_blocks_done = p->tile_blocks_done;
+    B.blocks_per_tile = p->opt.sub * p->opt.sub;
+    B.skip_done = full ? 0 : 1;
+    B.hist = p->hist;
+    B.tile_len = p->tile_len;
+    B.tile_start = p->tile_start;
+    B.vals = p->vals;
+    B.list_off = p->list_off;
+    B.capacity = p->vals_cap;
+    B.overflow = p->counters + 2;
+    B.nblocks = p->nblocks;
+    B.blocks_done_total = p->counters + 3;
+    const int total_chunks = (int)p->chunk_seg0.size();
+    const int nplanned = std::max(total_chunks, 1);
+    for (int c = 0; c < nplanned; ++c) {
+        const int seg0 = total_chunks ? p->chunk_seg0[c] : 0;
+        const int nseg = total_chunks ? p->chunk_nseg[c] : 0;
+        B.seg0 = seg0;
+        B.nseg = nseg;
+        B.chunk = c;
+        B.ranges = p->ranges_all + (size_t)c * p->ntiles;
+        B.prev_ranges = c ? p->ranges_all + (size_t)(c - 1) * p->ntiles : nullptr;
+        if (nseg > 0) {
+            Stage sg(p->ctx, TSB_STAGE_BINNING, st);
+            launch_bin_chunk(B, st);
+            p->ctx->launches += 4;
+        } else {
+            TSB_CUDA(cudaMemsetAsync(B.ranges, 0, sizeof(uint4) * p->ntiles, st));
         }
-        TSB_CUDA(cudaMemcpyAsync(hc, p->counters, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost, st));
-        uint32_t* hl = (uint32_t*)(hc + 8);
-        TSB_CUDA(cudaMemcpyAsync(hl, p->list_off, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-        TSB_CUDA(cudaStreamSynchronize(st));
-        p->V = hc[0];
-        if (hc[4]) {  // an equal-fp32-key run too long for k_fix_ties: exact 64-bit sort, redo the frame
-            const int nn = p->scene->d.n;
-            p->ctx->launches += launch_sort_depth64(p->depth64, p->touched, p->key_a, p->key_b, p->gidx_a,
-                                                    p->gidx_b, nn, p->sort_scratch, st);
-            p->sorted = p->gidx_a;
-            TSB_CUDA(cudaMemsetAsync(p->counters + 4, 0, sizeof(int32_t), st));
-            continue;
-        }
-        if (hc[2]) {  // list storage overflow: grow and redo the frame
-            int rc = ensure_vals(p, (uint64_t)p->vals_cap * 2 + (uint64_t)hl[0]);
-            if (rc) return rc;
-            continue;
-        }
-        p->nchunks = nch;
-        FixupK fx;
-        fx.ranges_all = p->ranges_all;
-        fx.nchunks = nch;
-        fx.chunk_rank0 = p->chunk_rank0;
-        fx.binned_end_rank = total_chunks ? (p->chunk_seg0[nch - 1] + p->chunk_nseg[nch - 1]) * kSeg : 0;
-        fx.vals = p->vals;
-        fx.sorted_gidx = p->sorted;
-        fx.rect = p->rect;
-        fx.n_visible = p->counters;
-        fx.overflow = p->counters + 2;
-        fx.stamp = p->fx_stamp;
-        fx.frame_stamp = ++p->frame_stamp;
-        fx.work = p->fx_work;
-        fx.work_n = p->fx_work_n;
-        fx.cache = p->fx_cache;
+        ChunkK ck;
+        ck.ranges = B.ranges;
+        ck.first = c == 0;
+        ck.chunk_end_rank = (seg0 + nseg) * kSeg;
+        ck.n_visible = p->counters;
+        ck.block_done = p->block_done;
+        ck.tile_blocks_done = p->tile_blocks_done;
+        ck.blocks_done_total = p->counters + 3;
+        ck.overflow = p->counters + 2;
         {
-            Stage sg(p->ctx, TSB_STAGE_FIXUP, st);
-            launch_fixup(scenek(p->scene), p->cam, p->opt, p->frame, fx, px, p->nf, st);
-            p->ctx->launches += 3;
-        }
-        if (loss) {
-            Stage sg(p->ctx, TSB_STAGE_LOSS, st);
-            TSB_CUDA(cudaMemsetAsync(p->loss_dev, 0, sizeof(double), st));
-            launch_fixup_loss(px, p->W, p->H, p->nf, target, p->chw, p->loss_dev, p->W * p->H, st);
-            launch_reduce_partials(p->loss_part, p->nblocks, 1, p->loss_dev, 1.0 / ((double)p->W * p->H), st);
-            // scene loss accumulator += this pass's loss (serialised with other gradient writers)
-            TSB_CUDA(cudaStreamWaitEvent(st, p->scene->grads_ev, 0));
-            launch_reduce_partials(p->loss_dev, 1, 1, p->scene->stats + kStatLoss, 1.0, st);
-            TSB_CUDA(cudaEventRecord(p->scene->grads_ev, st));
-            p->ctx->launches += 3;
+            Stage sg(p->ctx, TSB_STAGE_RASTER_FWD, st);
+            launch_raster_fwd(p->rec, ck, p->vals, p->opt, p->W, p->H, p->nf, px, fs, loss ? target : nullptr, chw,
+                              p->loss_part, st);
+            p->ctx->launches += 1;
         }
         TSB_CHECK_LAUNCH();
-        p->forwarded = true;
-        p->have_loss = loss;
-        (void)n;
-        TSB_CUDA(cudaEventRecord(p->done_ev, st));
-        return TSB_OK;
     }
-    return fail(TSB_ERR_NOMEM, "render: tile-list storage kept overflowing");
+    p->nchunks = nplanned;
+    FixupK fx;
+    fx.ranges_all = p->ranges_all;
+    fx.nchunks = nplanned;
+    fx.chunk_rank0 = p->chunk_rank0;
+    fx.binned_end_rank = total_chunks ? (p->chunk_seg0.back() + p->chunk_nseg.back()) * kSeg : 0;
+    fx.vals = p->vals;
+    fx.sorted_gidx = p->sorted;
+    fx.rect = p->rect;
+    fx.n_visible = p->counters;
+    fx.overflow = p->counters + 2;
+    fx.stamp = p->fx_stamp;
+    fx.frame_stamp = ++p->frame_stamp;
+    fx.work = p->fx_work;
+    fx.work_n = p->fx_work_n;
+    fx.cache = p->fx_cache;
+    {
+        Stage sg(p->ctx, TSB_STAGE_FIXUP, st);
+        launch_fixup(scenek(p->scene), p->cam, p->opt, p->frame, fx, px, p->nf, st);
+        p->ctx->launches += 3;
+    }
+    if (loss) {
+        Stage sg(p->ctx, TSB_STAGE_LOSS, st);
+        TSB_CUDA(cudaMemsetAsync(p->loss_dev, 0, sizeof(double), st));
+        launch_fixup_loss(px, p->W, p->H, p->nf, target, chw, p->loss_dev, st);
+        launch_reduce_partials(p->loss_part, p->nblocks, 1, p->loss_dev, 1.0 / ((double)p->W * p->H), px.abort, st);
+        // scene loss accumulator += this pass's loss (serialised with other gradient writers)
+        TSB_CUDA(cudaStreamWaitEvent(st, p->scene->grads_ev, 0));
+        launch_reduce_partials(p->loss_dev, 1, 1, p->scene->stats + kStatLoss, 1.0, px.abort, st);
+        TSB_CUDA(cudaEventRecord(p->scene->grads_ev, st));
+        p->ctx->launches += 3;
+    }
+    TSB_CHECK_LAUNCH();
+    int32_t* hc = (int32_t*)((char*)p->pinned + 2048);
+    TSB_CUDA(cudaMemcpyAsync(hc, p->counters, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost, st));
+    TSB_CUDA(cudaMemcpyAsync(hc + 8, p->list_off, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    p->forwarded = true;
+    p->have_loss = loss;
+    p->pending = true;
+    p->pend_loss = loss;
+    p->pend_target = loss ? target : nullptr;
+    p->pend_chw = chw;
+    p->pend_bwd = false;
+    p->pend_dl.clear();
+    TSB_CUDA(cudaEventRecord(p->done_ev, st));
+    return TSB_OK;
+}
+
+int output_ptr(tsb_pass* p, int which, void** dptr, size_t* bytes);
+
+int enqueue_backward(tsb_pass* p, const UpK& up);
+
+// Wait for the pass's enqueued frame and check its abort word.  An aborted
+// frame wrote nothing (every kernel after the abort returns at entry); it is
+// redone with more list storage / the exact 64-bit depth sort, including its
+// loss and backward.  Its inputs are still intact: everything that changes the
+// scene settles all passes first.
+int settle(tsb_pass* p) {
+    for (int attempt = 0; p->pending; ++attempt) {
+        TSB_CUDA(cudaSetDevice(p->ctx->device));
+        TSB_CUDA(cudaStreamSynchronize(p->stream));
+        p->pending = false;
+        const int32_t* hc = (const int32_t*)((const char*)p->pinned + 2048);
+        p->V = hc[0];
+        const int ab = hc[2];
+        if (!ab) return TSB_OK;
+        if (attempt >= 8) return fail(TSB_ERR_NOMEM, "render: tile-list storage kept overflowing");
+        p->ctx->redos++;
+        cudaStream_t st = p->stream;
+        if (ab & 2) {  // an equal-fp32-key run too long for k_fix_ties: exact 64-bit sort
+            p->ctx->launches += launch_sort_depth64(p->depth64, p->touched, p->key_a, p->key_b, p->gidx_a, p->gidx_b,
+                                                    p->scene->d.n, p->sort_scratch, st);
+            p->sorted = p->gidx_a;
+        }
+        if (ab & 1) {  // list storage overflow: grow
+            const uint32_t used = (uint32_t)hc[8];
+            int rc = ensure_vals(p, (uint64_t)p->vals_cap * 2 + (uint64_t)used);
+            if (rc) return rc;
+        }
+        TSB_CUDA(cudaMemsetAsync(p->counters + 2, 0, sizeof(int32_t), st));
+        const bool bwd = p->pend_bwd;
+        const UpK up = p->pend_up;
+        const std::vector<tsb_pass::Download> dls = p->pend_dl;
+        int rc = enqueue_forward(p, p->pend_target, p->pend_loss, p->pend_chw);
+        if (rc) return rc;
+        if (bwd && (rc = enqueue_backward(p, up))) return rc;
+        for (const auto& d : dls) {  // re-issue the frame's asynchronous downloads
+            void* dp = nullptr;
+            size_t b = 0;
+            if ((rc = output_ptr(p, d.which, &dp, &b))) return rc;
+            TSB_CUDA(cudaMemcpyAsync(d.host, dp, std::min(b, d.bytes), cudaMemcpyDeviceToHost, st));
+            p->pend_dl.push_back(d);
+        }
+        TSB_CUDA(cudaEventRecord(p->done_ev, st));
+    }
+    return TSB_OK;
+}
+
+int run_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw) {
+    if (!p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
+    if (p->pending) {  // a second forward of the same prepared frame
+        int rc = settle(p);
+        if (rc) return rc;
+    }
+    return enqueue_forward(p, target, loss, chw);
 }
 
 }  // namespace
 
 int tsb_pass_forward(tsb_pass* p) {
     if (!p) return fail(TSB_ERR_INVALID, "null pass");
-    return run_forward(p, nullptr, false);
+    return run_forward(p, nullptr, false, ChW{});
 }
 
 int tsb_pass_forward_loss(tsb_pass* p, int where, const float* target, const double* channel_weight,
@@ -1090,15 +1198,12 @@ int tsb_pass_forward_loss(tsb_pass* p, int where, const float* target, const dou
     } else if (where != TSB_DEVICE) {
         return fail(TSB_ERR_INVALID, "bad memory kind");
     }
-    float w[8] = {0};
-    for (int c = 0; c < 4 * p->nf; ++c) w[c] = (float)channel_weight[c];
-    float* hw = (float*)p->pinned + 16;
-    TSB_CUDA(cudaStreamSynchronize(st));  // pinned staging reuse
-    std::memcpy(hw, w, sizeof w);
-    TSB_CUDA(cudaMemcpyAsync(p->chw, hw, sizeof w, cudaMemcpyHostToDevice, st));
-    int rc = run_forward(p, dt, true);
+    ChW w{};
+    for (int c = 0; c < 4 * p->nf; ++c) w.w[c] = (float)channel_weight[c];
+    int rc = run_forward(p, dt, true, w);
     if (rc) return rc;
     if (loss_out) {
+        if ((rc = settle(p))) return rc;
         double* hl = (double*)((char*)p->pinned + 256);
         TSB_CUDA(cudaMemcpyAsync(hl, p->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
         TSB_CUDA(cudaStreamSynchronize(st));
@@ -1107,7 +1212,9 @@ int tsb_pass_forward_loss(tsb_pass* p, int where, const float* target, const dou
     return TSB_OK;
 }
 
-int tsb_pass_output(tsb_pass* p, int which, void** dptr, size_t* bytes) {
+namespace {
+// Device address and size of output `which` (no settle).
+int output_ptr(tsb_pass* p, int which, void** dptr, size_t* bytes) {
     if (!p || !dptr) return fail(TSB_ERR_INVALID, "null argument");
     if (!p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
     const size_t HW = (size_t)p->W * p->H;
@@ -1136,6 +1243,37 @@ int tsb_pass_output(tsb_pass* p, int which, void** dptr, size_t* bytes) {
     if (bytes) *bytes = b;
     return TSB_OK;
 }
+}  // namespace
+
+int tsb_pass_output(tsb_pass* p, int which, void** dptr, size_t* bytes) {
+    if (!p || !dptr) return fail(TSB_ERR_INVALID, "null argument");
+    if (!p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
+    int rc = settle(p);
+    if (rc) return rc;
+    return output_ptr(p, which, dptr, bytes);
+}
+
+int tsb_pass_download_async(tsb_pass* p, int which, void* host, size_t bytes) {
+    if (!p || !host) return fail(TSB_ERR_INVALID, "null argument");
+    if (!p->forwarded) return fail(TSB_ERR_INVALID, "download requires a forward pass");
+    void* d = nullptr;
+    size_t b = 0;
+    int rc = output_ptr(p, which, &d, &b);
+    if (rc) return rc;
+    if (bytes < b) return fail(TSB_ERR_INVALID, "tsb_pass_download_async: host buffer too small");
+    TSB_CUDA(cudaMemcpyAsync(host, d, b, cudaMemcpyDeviceToHost, p->stream));
+    TSB_CUDA(cudaEventRecord(p->done_ev, p->stream));
+    if (p->pending) p->pend_dl.push_back({which, host, bytes});
+    return TSB_OK;
+}
+
+int tsb_pass_wait(tsb_pass* p) {
+    if (!p) return fail(TSB_ERR_INVALID, "null pass");
+    int rc = settle(p);
+    if (rc) return rc;
+    TSB_CUDA(cudaStreamSynchronize(p->stream));
+    return TSB_OK;
+}
 
 int tsb_pass_download(tsb_pass* p, int which, void* host, size_t bytes) {
     void* d = nullptr;
@@ -1149,18 +1287,21 @@ int tsb_pass_download(tsb_pass* p, int which, void* host, size_t bytes) {
 }
 
 namespace {
-int run_backward(tsb_pass* p, const UpK& up) {
+int enqueue_backward(tsb_pass* p, const UpK& up) {
     cudaStream_t st = p->stream;
     tsb_scene* s = p->scene;
     float dpsi[2];
     for (int f = 0; f < p->nf; ++f) dpsi[f] = (float)(4.0 * M_PI * s->d.frequency[f] / s->d.speed_of_light);
-    TSB_CUDA(cudaStreamWaitEvent(st, s->grads_ev, 0));
+    const PixK px = pixk(p);
     {
+        // per-pass outputs only (screen gradients, background partials): overlaps other passes
         Stage sg(p->ctx, TSB_STAGE_RASTER_BWD, st);
-        launch_raster_bwd(p->rec, p->ranges_all, p->nchunks, p->vals, p->opt, p->W, p->H, p->nf, dpsi, pixk(p), up,
+        launch_raster_bwd(p->rec, p->ranges_all, p->nchunks, p->vals, p->opt, p->W, p->H, p->nf, dpsi, px, up,
                           p->screen, s->d.n, p->bg_part, st);
-        launch_reduce_partials(p->bg_part, p->nblocks, 6 * p->nf, s->stats + kStatBg, 1.0, st);
     }
+    // scene gradient writers are serialised by the scene's event chain
+    TSB_CUDA(cudaStreamWaitEvent(st, s->grads_ev, 0));
+    launch_reduce_partials(p->bg_part, p->nblocks, 6 * p->nf, s->stats + kStatBg, 1.0, px.abort, st);
     if (p->keep_screen) {
         dev_free(p->screen_keep);
         int rc;
@@ -1170,13 +1311,24 @@ int run_backward(tsb_pass* p, const UpK& up) {
     }
     {
         Stage sg(p->ctx, TSB_STAGE_CHAIN, st);
+        // an aborted frame left the screen gradients zero: the chain adds nothing
         launch_chain(scenek(s), p->cam, p->opt, p->frame, p->touched, p->screen, s->grads, st);
     }
     p->ctx->launches += 3;
     TSB_CHECK_LAUNCH();
     TSB_CUDA(cudaEventRecord(s->grads_ev, st));
     TSB_CUDA(cudaEventRecord(p->done_ev, st));
+    p->pend_bwd = true;
+    p->pend_up = up;
     return TSB_OK;
+}
+
+int run_backward(tsb_pass* p, const UpK& up) {
+    if (p->pend_bwd && p->pending) {  // a second backward of one unsettled frame: settle the first
+        int rc = settle(p);
+        if (rc) return rc;
+    }
+    return enqueue_backward(p, up);
 }
 }  // namespace
 
@@ -1336,6 +1488,18 @@ int tsb_pass_debug_records(tsb_pass* p, float* rec12) {
     return TSB_OK;
 }
 
+int tsb_pass_debug_set_list_capacity(tsb_pass* p, uint32_t entries) {
+    if (!p || entries == 0) return fail(TSB_ERR_INVALID, "tsb_pass_debug_set_list_capacity: bad argument");
+    int rc = settle(p);
+    if (rc) return rc;
+    TSB_CUDA(cudaSetDevice(p->ctx->device));
+    TSB_CUDA(cudaStreamSynchronize(p->stream));
+    dev_free(p->vals);
+    if ((rc = dev_alloc(&p->vals, entries))) return rc;
+    p->vals_cap = entries;
+    return TSB_OK;
+}
+
 int tsb_pass_debug_keep_screen(tsb_pass* p, int enabled) {
     if (!p) return fail(TSB_ERR_INVALID, "null pass");
     p->keep_screen = enabled != 0;
@@ -1363,6 +1527,8 @@ int tsb_pass_debug_screen_grads(tsb_pass* p, float* g8) {
 
 int tsb_pass_debug_fixups(tsb_pass* p, int32_t* count) {
     if (!p || !count) return fail(TSB_ERR_INVALID, "null argument");
+    int rc0 = settle(p);
+    if (rc0) return rc0;
     int32_t* h = (int32_t*)((char*)p->pinned + 512);
     TSB_CUDA(cudaMemcpyAsync(h, p->counters + 1, 4, cudaMemcpyDeviceToHost, p->stream));
     TSB_CUDA(cudaStreamSynchronize(p->stream));
@@ -1468,6 +1634,10 @@ void tsb_comm_destroy(tsb_comm* c) {
 
 int tsb_scene_allreduce_grads(tsb_scene* s, tsb_comm* c) {
     if (!s || !c) return fail(TSB_ERR_INVALID, "null argument");
+    {
+        int rc0 = settle_all(s->ctx);  // a redone frame must add its gradients before the reduction
+        if (rc0) return rc0;
+    }
     const size_t nel = (size_t)s->narrays * (size_t)s->d.n * 4;
     cudaStream_t st = s->ctx->stream;
     TSB_CUDA(cudaStreamWaitEvent(st, s->grads_ev, 0));

@@ -36,7 +36,7 @@ __device__ __noinline__ void sort_run(const uint32_t* __restrict__ keys, uint32_
     int L = 2;
     while (r + L < V && keys[r + L] == k) ++L;
     if (L > kMaxTieRun) {
-        *long_run = 1;
+        atomicOr(long_run, 2);  // abort the frame; the host redoes it with the exact 64-bit sort
         return;
     }
     uint32_t g[kMaxTieRun];
@@ -141,6 +141,18 @@ __device__ __forceinline__ bool tile_done(const BinK& B, int t) {
     return B.skip_done && B.chunk > 0 && B.tile_blocks_done[t] >= B.blocks_per_tile;
 }
 
+// Every planned chunk is launched; a chunk is live only while the frame is not
+// aborted, visible ranks remain and (unless full lists are requested) some raster
+// block has not terminated.  The host never waits between chunks.  Inputs are
+// written only by earlier kernels of the stream, so all kernels of a chunk agree
+// (the abort word can only turn on, which every later kernel honours anyway).
+__device__ __forceinline__ bool chunk_live(const BinK& B) {
+    if (*B.overflow) return false;
+    if (B.chunk == 0) return true;
+    if (B.seg0 * kSeg >= *B.n_visible) return false;
+    return !(B.skip_done && *B.blocks_done_total >= B.nblocks);
+}
+
 struct Box {
     int x0, x1, y0, y1;  // union of the batch's tile rects (inclusive); empty when x0 > x1
 };
@@ -194,6 +206,7 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_count(BinK B) {
     __shared__ int box[4];
     const int tid = threadIdx.x, lane = tid & 31;
     const int segl = blockIdx.x;
+    if (!chunk_live(B)) return;
     uint32_t* gids = smem;
     uint32_t* colmask = gids + 32;
     uint32_t* rowmask = colmask + B.tiles_x;
@@ -231,6 +244,7 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_count(BinK B) {
 // contiguous range of segments.
 __global__ void __launch_bounds__(1024) k_bin_scan_segments(BinK B) {
     __shared__ uint32_t part[32][33];
+    if (!chunk_live(B)) return;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int t = blockIdx.x * 32 + lane;
     const int per = (B.nseg + 31) / 32;
@@ -268,6 +282,13 @@ __global__ void k_bin_scan_tiles(BinK B) {
     if (tid == 0) s_carry = 0;
     __syncthreads();
     const uint32_t base = *B.list_off;
+    if (!chunk_live(B)) {  // empty chunk: every tile skipped (the fix-up scans ranks from here)
+        for (int t = tid; t < B.ntiles; t += blockDim.x) {
+            const uint32_t cum = B.chunk == 0 ? 0u : B.prev_ranges[t].z + B.prev_ranges[t].y;
+            B.ranges[t] = make_uint4(base, 0u, cum, 1u);
+        }
+        return;
+    }
     for (int t0 = 0; t0 < B.ntiles; t0 += blockDim.x) {
         const int t = t0 + tid;
         const uint32_t v = t < B.ntiles ? B.tile_len[t] : 0u;
@@ -303,7 +324,7 @@ __global__ void k_bin_scan_tiles(BinK B) {
     if (tid == 0) {
         const uint32_t end = base + s_carry;
         *B.list_off = end;
-        if (end > B.capacity) *B.overflow = 1;
+        if (end > B.capacity) atomicOr(B.overflow, 1);
     }
 }
 
@@ -316,7 +337,7 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_emit(BinK B) {
     __shared__ int box[4];
     const int tid = threadIdx.x, lane = tid & 31;
     const int segl = blockIdx.x;
-    if (*B.overflow) return;
+    if (!chunk_live(B)) return;
     const int V = *B.n_visible;
     const int r0 = (B.seg0 + segl) * kSeg;
     if (r0 >= V) return;

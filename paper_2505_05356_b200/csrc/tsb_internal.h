@@ -80,7 +80,9 @@ struct BinK {
     uint32_t* vals;                   // list storage (Gaussian indices)
     uint32_t* list_off;               // device running offset into vals
     uint32_t capacity;
-    int32_t* overflow;
+    int32_t* overflow;                // abort word: bit 0 list overflow, bit 1 long tie run
+    int nblocks;                      // raster blocks of the frame
+    const int32_t* blocks_done_total; // raster blocks finished so far
 };
 
 // Forward state carried across chunk launches (SoA planes of npx).
@@ -115,6 +117,12 @@ struct PixK {
     float* d_quad;       // [4*nf][H][W] upstream (written by loss epilogue)
     int32_t* flagged;    // list of fp64-fixup pixels
     int32_t* n_flagged;  // device counter
+    const int32_t* abort;  // frame abort word (overflow / long tie run): later kernels do nothing
+};
+
+// Per-channel loss weights, passed by value (no staging copy, no host sync).
+struct ChW {
+    float w[8];
 };
 
 inline int out_channels(int nf) { return 6 * nf + 5; }
@@ -181,8 +189,8 @@ int radix_sort32(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t*
 int radix_sort24(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch,
                  const uint32_t* range, cudaStream_t st);
 // Global (depth, index) order: stable sort on fp32 depth keys, then exact fp64
-// re-sort of equal-key runs (runs longer than 64 set *long_run; the host then
-// runs launch_sort_depth64).  Results in (keys_a, vals_a).
+// re-sort of equal-key runs (runs longer than 64 set bit 1 of *abort; the host then
+// runs launch_sort_depth64 and redoes the frame).
 int launch_sort_depth(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, const double* depth64,
                       const int32_t* n_visible, int32_t* long_run, const uint32_t* key_range, int n,
                       uint32_t* scratch, cudaStream_t st);  // result in (keys_b, vals_b)
@@ -191,15 +199,16 @@ int launch_sort_depth64(const double* depth64, const uint32_t* touched, uint32_t
 void launch_bin_chunk(const BinK& B, cudaStream_t st);
 // tsb_raster.cu
 void launch_raster_fwd(const RecK& rec, const ChunkK& ck, const uint32_t* tile_vals, const OptK& O,
-                       int W, int H, int nf, PixK px, FwdState fs, const float* target, const float* ch_w,
+                       int W, int H, int nf, PixK px, FwdState fs, const float* target, const ChW& ch_w,
                        double* loss_part, cudaStream_t st);
-void launch_fixup_loss(const PixK& px, int W, int H, int nf, const float* target, const float* ch_w,
-                       double* loss_extra, int max_flag, cudaStream_t st);
+void launch_fixup_loss(const PixK& px, int W, int H, int nf, const float* target, const ChW& ch_w,
+                       double* loss_extra, cudaStream_t st);
 void launch_raster_bwd(const RecK& rec, const uint4* ranges_all, int nchunks, const uint32_t* tile_vals,
                        const OptK& O, int W, int H, int nf, const float* dpsi, PixK px, const UpK& up,
                        float* screen, int scap, double* bg_part, cudaStream_t st);
+// out[c] = (out[c] + sum_i part[i][c]) * scale; nothing when *abort != 0 (abort may be null).
 void launch_reduce_partials(const double* part, int nparts, int width, double* out,
-                            double scale, cudaStream_t st);
+                            double scale, const int32_t* abort, cudaStream_t st);
 // tsb_optim.cu
 void launch_pack_params(float4* dst, const float* src, int n, int comps, int comp0, int ncomp_dst,
                         cudaStream_t st);

@@ -97,8 +97,7 @@ struct Smem {
 template <int NF, bool DIST>
 __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK ck, const uint32_t* __restrict__ vals,
                                                                 OptK O, int W, int H, PixK px, FwdState fs,
-                                                                const float* __restrict__ target,
-                                                                const float* __restrict__ chw,
+                                                                const float* __restrict__ target, ChW chw,
                                                                 double* __restrict__ loss_part) {
     __shared__ Smem<NF> sm;
     __shared__ float red[kRasterThreads / 32];
@@ -263,8 +262,8 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
 #pragma unroll
             for (int c = 0; c < 4 * NF; ++c) {
                 const float r = q[c] - target[c * HW + o];
-                lpx = fmaf(chw[c] * r, r, lpx);
-                px.d_quad[c * HW + o] = chw[c] * s2 * r;
+                lpx = fmaf(chw.w[c] * r, r, lpx);
+                px.d_quad[c * HW + o] = chw.w[c] * s2 * r;
             }
         }
     } else if (!was_done) {
@@ -306,8 +305,9 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
 }
 
 // Loss + d_quad for the fp64-fixed pixels (after k_fixup).
-__global__ void k_fixup_loss(PixK px, int W, int H, int nf, const float* __restrict__ target,
-                             const float* __restrict__ chw, double* __restrict__ loss_extra) {
+__global__ void k_fixup_loss(PixK px, int W, int H, int nf, const float* __restrict__ target, ChW chw,
+                             double* __restrict__ loss_extra) {
+    if (*px.abort) return;
     const int count = *px.n_flagged;
     double l = 0.0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
@@ -315,8 +315,8 @@ __global__ void k_fixup_loss(PixK px, int W, int H, int nf, const float* __restr
         const float s2 = 2.f / (float)HW;
         for (int c = 0; c < 4 * nf; ++c) {
             const float r = px.out[c * HW + o] - target[c * HW + o];
-            l += (double)(chw[c] * r * r);
-            px.d_quad[c * HW + o] = chw[c] * s2 * r;
+            l += (double)(chw.w[c] * r * r);
+            px.d_quad[c * HW + o] = chw.w[c] * s2 * r;
         }
     }
     for (int m = 16; m > 0; m >>= 1) l += __shfl_xor_sync(0xffffffffu, l, m);
@@ -383,6 +383,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
     __shared__ float sacc[kRasterThreads][9];  // padded: 8 grads per entry
     __shared__ int smax[kRasterThreads / 32];
     __shared__ float sbg[kRasterThreads / 32][6 * NF];
+    if (*px.abort) return;  // aborted frame: no gradient is written (the host redoes it)
     const int nsub = O.sub * O.sub;
     const int ntiles = O.tiles_x * O.tiles_y;
     const int tile = blockIdx.x / nsub, sb = blockIdx.x % nsub;
@@ -581,7 +582,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
 }
 
 void launch_raster_fwd(const RecK& rec, const ChunkK& ck, const uint32_t* tile_vals, const OptK& O, int W, int H,
-                       int nf, PixK px, FwdState fs, const float* target, const float* ch_w, double* loss_part,
+                       int nf, PixK px, FwdState fs, const float* target, const ChW& ch_w, double* loss_part,
                        cudaStream_t st) {
     const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
 #define TSB_FWD(NF_, D_) \
@@ -594,9 +595,8 @@ void launch_raster_fwd(const RecK& rec, const ChunkK& ck, const uint32_t* tile_v
 #undef TSB_FWD
 }
 
-void launch_fixup_loss(const PixK& px, int W, int H, int nf, const float* target, const float* ch_w,
-                       double* loss_extra, int max_flag, cudaStream_t st) {
-    (void)max_flag;
+void launch_fixup_loss(const PixK& px, int W, int H, int nf, const float* target, const ChW& ch_w,
+                       double* loss_extra, cudaStream_t st) {
     k_fixup_loss<<<64, 256, 0, st>>>(px, W, H, nf, target, ch_w, loss_extra);
 }
 
@@ -617,9 +617,10 @@ void launch_raster_bwd(const RecK& rec, const uint4* ranges_all, int nchunks, co
 }
 
 __global__ void k_reduce_partials(const double* __restrict__ part, int nparts, int width,
-                                  double* __restrict__ out, double scale) {
+                                  double* __restrict__ out, double scale, const int32_t* __restrict__ abort) {
     // one block; column c summed in a fixed order (deterministic)
     __shared__ double s[256];
+    if (abort && *abort) return;
     for (int c = 0; c < width; ++c) {
         double a = 0.0;
         for (int i = threadIdx.x; i < nparts; i += blockDim.x) a += part[(size_t)i * width + c];
@@ -634,8 +635,9 @@ __global__ void k_reduce_partials(const double* __restrict__ part, int nparts, i
     }
 }
 
-void launch_reduce_partials(const double* part, int nparts, int width, double* out, double scale, cudaStream_t st) {
-    k_reduce_partials<<<1, 256, 0, st>>>(part, nparts, width, out, scale);
+void launch_reduce_partials(const double* part, int nparts, int width, double* out, double scale,
+                            const int32_t* abort, cudaStream_t st) {
+    k_reduce_partials<<<1, 256, 0, st>>>(part, nparts, width, out, scale, abort);
 }
 
 }  // namespace tsb

@@ -34,23 +34,25 @@ class FrameShardedTrainer:
     def __init__(self, ctx: Context, scene: GaussianScene, camera: CameraModel,
                  options: Optional[RenderOptions] = None, lr: Optional[LrTable] = None,
                  adam: AdamParams = AdamParams(), comm: Optional[Comm] = None, rank: int = 0, world: int = 1,
-                 channel_weight: Optional[Sequence[float]] = None):
+                 channel_weight: Optional[Sequence[float]] = None, passes: int = 3):
         self.ctx, self.scene, self.camera = ctx, scene, camera
         self.options = options or RenderOptions()
         self.lr = lr or LrTable()
         self.adam = adam
         self.comm, self.rank, self.world = comm, rank, world
         self.channel_weight = list(channel_weight or [0.25] * (4 * scene.n_freq))
-        # two passes (two streams): frame i's backward overlaps frame i+1's preprocess/sort/binning;
-        # gradient writes are serialised by the scene's event chain inside the library
-        self.passes = [RenderPass(ctx), RenderPass(ctx)]
+        # render passes (one stream each) rotate over frames: frame i's backward overlaps the
+        # preprocess/sort/binning of the next frames; nothing waits for the device until a pass
+        # is reused (it settles its previous frame) and at the allreduce / Adam step.  Gradient
+        # writes are serialised by the scene's event chain inside the library.
+        self.passes = [RenderPass(ctx) for _ in range(max(1, passes))]
         self.rp = self.passes[0]
 
     def step(self, frames: Sequence, target: Callable[[int], object]) -> None:
         """frames: the iteration's (key, w) frames (all ranks pass the same list);
         target(i) -> host array (4*n_freq, H, W) or an int device pointer for frame i."""
         for k, i in enumerate(shard_indices(len(frames), self.rank, self.world)):
-            rp = self.passes[k % 2]
+            rp = self.passes[k % len(self.passes)]
             rp.prepare(self.scene, self.camera, self.options, frames[i])
             t = target(i)
             if isinstance(t, int):

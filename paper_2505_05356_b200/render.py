@@ -175,6 +175,10 @@ class Context:
     def launch_count(self) -> int:
         return int(lib().tsb_ctx_launch_count(self._h))
 
+    def redo_count(self) -> int:
+        """Frames redone after a device-side abort (list overflow / long tie run)."""
+        return int(lib().tsb_ctx_redo_count(self._h))
+
     def set_profiling(self, on: bool):
         check(lib().tsb_ctx_set_profiling(self._h, 1 if on else 0))
 
@@ -424,6 +428,16 @@ class RenderPass:
         check(lib().tsb_pass_download(self._h, which, a.ctypes.data, nb))
         return a.reshape(shape) if shape is not None else a
 
+    def download_async(self, which: int, host: np.ndarray):
+        """Enqueue a device->host copy of output `which` into `host` (ideally pinned);
+        valid after wait() / Context.synchronize() / this pass's next prepare()."""
+        check(lib().tsb_pass_download_async(self._h, which, host.ctypes.data, host.nbytes))
+        return self
+
+    def wait(self):
+        check(lib().tsb_pass_wait(self._h))
+        return self
+
     def outputs(self):
         """RenderedBuffers (splat.hpp:51-66), ToF channels: quad, phasor, depth_raw, depth, weight,
         transmittance (+ distortion when enabled)."""
@@ -472,6 +486,12 @@ class RenderPass:
         g = np.zeros((max(v, 1), 8), np.float32)
         check(lib().tsb_pass_debug_screen_grads(self._h, _ptr(g)))
         return g[:v]
+
+    def debug_set_list_capacity(self, entries: int):
+        """Test hook (call between prepare and forward): shrink the tile-list storage so the
+        frame overflows and takes the device-side abort + redo path."""
+        check(lib().tsb_pass_debug_set_list_capacity(self._h, int(entries)))
+        return self
 
     def debug_fixups(self) -> int:
         c = C.c_int32()

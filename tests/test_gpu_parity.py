@@ -475,3 +475,48 @@ def test_distortion_upstream_requires_channel(tsb, ctx):
     rp = tsb.RenderPass(ctx).prepare(scene, cfg.camera, tsb.RenderOptions(), cfg.frames[0]).forward()
     with pytest.raises(RuntimeError, match="distortion"):
         rp.backward_buffers(d_distortion=np.zeros((cfg.camera.height, cfg.camera.width), np.float32))
+
+
+def test_list_overflow_abort_and_redo(tsb, ctx):
+    """The host never waits between depth chunks; a frame whose tile lists overflow their
+    storage aborts on the device (nothing written) and is redone when the pass is settled.
+    Outputs and loss must equal an un-aborted render bit for bit, gradients up to the
+    order of their atomic additions."""
+    from paper_2505_05356_b200 import synthetic
+    g = synthetic.gaussians(6000, 21, n_keyframes=2)
+    tg = synthetic.gaussians(6000, 22, n_keyframes=2)
+    cam = synthetic.camera(160, 120, 140.0)
+    tof = tsb.ToFConfig(30e6)
+    frame = (0, 0.4)
+    opts = tsb.RenderOptions(counts=True)
+    tscene = gpu_scene(tsb, ctx, tg, tof)
+    target = tsb.RenderPass(ctx).prepare(tscene, cam, opts, frame).forward().outputs()["quad"]
+    w = [0.25] * 4
+
+    def run(cap):
+        scene = gpu_scene(tsb, ctx, g, tof)
+        rp = tsb.RenderPass(ctx).prepare(scene, cam, opts, frame)
+        if cap:
+            rp.debug_set_list_capacity(cap)
+        rp.forward_loss(target, w, sync=False)
+        rp.backward()
+        buf = np.full((4, cam.height, cam.width), np.nan, np.float32)
+        rp.download_async(tsb._abi.OUT_QUAD, buf)  # re-issued by the redo
+        grads = scene.grads()  # settles the pass (redo happens here when it aborted)
+        rp.wait()
+        out = rp.outputs()
+        assert np.array_equal(buf, out["quad"])
+        return out, grads, rp.num_keys()
+
+    r0 = ctx.redo_count()
+    a, ga, ka = run(None)
+    assert ctx.redo_count() == r0
+    b, gb, kb = run(64)
+    assert ctx.redo_count() == r0 + 1, "the overflowed frame was not redone"
+    assert ka == kb
+    for k in a:
+        assert np.array_equal(a[k], b[k], equal_nan=True), k
+    assert ga["loss"] == gb["loss"]
+    for k in ga:  # gradient atomics may add in a different order: summation-order tolerance
+        x, y = np.asarray(ga[k], np.float64), np.asarray(gb[k], np.float64)
+        assert np.abs(x - y).max() <= 1e-5 * max(np.abs(x).max(), 1e-30), k
