@@ -21,6 +21,8 @@
 //      reference list.  Tiles whose pixels have all terminated are skipped by
 //      later chunks (the composite never reads past termination), unless the
 //      caller asks for full lists (parity mode).
+#include <algorithm>
+
 #include "tsb_internal.h"
 
 namespace tsb {
@@ -195,27 +197,42 @@ __device__ __forceinline__ void load_batch_warp0(const BinK& B, int r, int V, ui
     }
 }
 
+// done[t / 32] bit t: tile t is not binned by this chunk
+__device__ __forceinline__ void stage_done(const BinK& B, uint32_t* done) {
+    const bool check = B.skip_done && B.chunk > 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int t0 = warp * 32; t0 < B.ntiles; t0 += nwarps * 32) {
+        const int t = t0 + lane;
+        const bool d = check && t < B.ntiles && B.tile_blocks_done[t] >= B.blocks_per_tile;
+        const uint32_t bits = __ballot_sync(0xffffffffu, d);
+        if (lane == 0) done[t0 >> 5] = bits;
+    }
+}
+__device__ __forceinline__ bool is_done(const uint32_t* done, int t) { return (done[t >> 5] >> (t & 31)) & 1u; }
+
 }  // namespace
 
-// Per (segment, tile) entry counts of one depth chunk.  One CTA per segment of
-// kSeg ranks; per batch of 32 ranks the threads walk the tiles of the batch's
-// union box (the number of coverers of a tile is popc of two masks).
+// Per (segment, tile) entry counts of one depth chunk.  CTAs stride over the
+// chunk's segments of kSeg ranks; per batch of 32 ranks the threads walk the
+// tiles of the batch's union box (the number of coverers of a tile is popc of
+// two masks).
 template <bool SMEM>
 __global__ void __launch_bounds__(kBinThreads) k_bin_count(BinK B) {
     extern __shared__ uint32_t smem[];
     __shared__ int box[4];
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int segl = blockIdx.x;
     if (!chunk_live(B)) return;
-    uint32_t* gids = smem;
+    const int tid = threadIdx.x, lane = tid & 31;
+    uint32_t* done = smem;
+    uint32_t* gids = done + ((B.ntiles + 31) >> 5);
     uint32_t* colmask = gids + 32;
     uint32_t* rowmask = colmask + B.tiles_x;
-    uint32_t* cnt = SMEM ? rowmask + B.tiles_y : B.hist + (size_t)segl * B.ntiles;
+    stage_done(B, done);
     const int V = *B.n_visible;
-    const int r0 = (B.seg0 + segl) * kSeg;
-    for (int t = tid; t < B.ntiles; t += kBinThreads) cnt[t] = 0u;
-    __syncthreads();
-    if (r0 < V) {
+    for (int segl = blockIdx.x; segl < B.nseg; segl += gridDim.x) {
+        uint32_t* cnt = SMEM ? rowmask + B.tiles_y : B.hist + (size_t)segl * B.ntiles;
+        const int r0 = (B.seg0 + segl) * kSeg;
+        for (int t = tid; t < B.ntiles; t += kBinThreads) cnt[t] = 0u;
+        __syncthreads();
         for (int b = 0; b < kSeg && r0 + b < V; b += 32) {
             if (tid < 32) load_batch_warp0(B, r0 + b + lane, V, colmask, rowmask, gids, box, lane);
             __syncthreads();
@@ -227,15 +244,16 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_count(BinK B) {
                 const uint32_t m = colmask[tx] & rowmask[ty];
                 if (m) {
                     const int t = ty * B.tiles_x + tx;
-                    if (!tile_done(B, t)) cnt[t] += (uint32_t)__popc(m);
+                    if (!is_done(done, t)) cnt[t] += (uint32_t)__popc(m);
                 }
             }
             __syncthreads();
         }
-    }
-    if (SMEM) {
-        uint32_t* h = B.hist + (size_t)segl * B.ntiles;
-        for (int t = tid; t < B.ntiles; t += kBinThreads) h[t] = cnt[t];
+        if (SMEM) {
+            uint32_t* h = B.hist + (size_t)segl * B.ntiles;
+            for (int t = tid; t < B.ntiles; t += kBinThreads) h[t] = cnt[t];
+        }
+        __syncthreads();
     }
 }
 
@@ -328,73 +346,318 @@ __global__ void k_bin_scan_tiles(BinK B) {
     }
 }
 
-// Stable scatter of one depth chunk.  Threads walk the batch's union tiles; the
-// coverers of tile t (bits of colmask & rowmask, in rank order) are written as
-// one contiguous run at the (segment, tile) cursor, which then advances.
-template <bool SMEM>
-__global__ void __launch_bounds__(kBinThreads) k_bin_emit(BinK B) {
+// Stable scatter of one depth chunk.  CTAs stride over segments; per batch of
+// 32 ranks the threads walk the batch's union tiles and the coverers of tile t
+// (bits of colmask & rowmask, in rank order) form one contiguous run at the
+// (segment, tile) cursor.  STAGED: runs are first laid out tile-major in a
+// shared-memory buffer (local exclusive scan of the segment's per-tile counts),
+// then flushed with consecutive threads writing consecutive list entries -- a
+// few coalesced runs per tile instead of one scattered 4-byte store per entry.
+// A segment with more entries than the buffer holds writes directly.
+template <bool STAGED>
+__global__ void __launch_bounds__(kBinThreads) k_bin_emit(BinK B, int cap) {
     extern __shared__ uint32_t smem[];
     __shared__ int box[4];
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int segl = blockIdx.x;
+    __shared__ uint32_t s_wsum[kBinThreads / 32];
+    __shared__ uint32_t s_total;
     if (!chunk_live(B)) return;
-    const int V = *B.n_visible;
-    const int r0 = (B.seg0 + segl) * kSeg;
-    if (r0 >= V) return;
-    uint32_t* gids = smem;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nt = B.ntiles;
+    uint32_t* done = smem;
+    uint32_t* gids = done + ((nt + 31) >> 5);
     uint32_t* colmask = gids + 32;
     uint32_t* rowmask = colmask + B.tiles_x;
-    uint32_t* h = B.hist + (size_t)segl * B.ntiles;
-    uint32_t* cur = SMEM ? rowmask + B.tiles_y : h;
-    for (int t = tid; t < B.ntiles; t += kBinThreads) cur[t] = B.tile_start[t] + h[t];
-    __syncthreads();
-    for (int b = 0; b < kSeg && r0 + b < V; b += 32) {
-        if (tid < 32) load_batch_warp0(B, r0 + b + lane, V, colmask, rowmask, gids, box, lane);
-        __syncthreads();
-        const int bw = box[1] - box[0] + 1;
-        const int area = bw > 0 ? bw * (box[3] - box[2] + 1) : 0;
-        for (int i = tid; i < area; i += kBinThreads) {
-            const int q = i / bw;
-            const int ty = box[2] + q, tx = box[0] + (i - q * bw);
-            uint32_t m = colmask[tx] & rowmask[ty];
-            if (!m) continue;
-            const int t = ty * B.tiles_x + tx;
-            if (tile_done(B, t)) continue;
-            uint32_t c = cur[t];
-            cur[t] = c + (uint32_t)__popc(m);
-            while (m) {
-                const int j = __ffs(m) - 1;
-                m &= m - 1u;
-                B.vals[c++] = gids[j];
+    uint32_t* cur_s = rowmask + B.tiles_y;  // STAGED: local cursor (or global cursor when over capacity)
+    uint32_t* delta = cur_s + nt;          // STAGED: global list position - local position
+    uint32_t* seg_g = delta + nt;          // STAGED: the segment's Gaussian indices
+    uint16_t* buf_t = reinterpret_cast<uint16_t*>(seg_g + kSeg);
+    uint8_t* buf_r = reinterpret_cast<uint8_t*>(buf_t + cap);
+    stage_done(B, done);
+    const int V = *B.n_visible;
+    for (int segl = blockIdx.x; segl < B.nseg; segl += gridDim.x) {
+        const int r0 = (B.seg0 + segl) * kSeg;
+        if (r0 >= V) break;  // uniform; later segments of this CTA are past V too
+        uint32_t* h = B.hist + (size_t)segl * nt;
+        uint32_t* cur = STAGED ? cur_s : h;  // !STAGED: the hist row becomes the cursor in place
+        uint32_t total = 0xffffffffu;
+        if (STAGED) {
+            // this segment's per-tile counts -> tile-major local offsets (exclusive scan)
+            const uint32_t* hn = segl + 1 < B.nseg ? h + nt : B.tile_len;
+            for (int t = tid; t < nt; t += kBinThreads) {
+                const uint32_t ht = h[t];
+                cur[t] = hn[t] - ht;
+                delta[t] = B.tile_start[t] + ht;
             }
+            for (int i = tid; i < kSeg; i += kBinThreads) seg_g[i] = r0 + i < V ? B.sorted_gidx[r0 + i] : 0u;
+            __syncthreads();
+            const int per = (nt + kBinThreads - 1) / kBinThreads;
+            const int t0 = tid * per, t1 = min(nt, t0 + per);
+            uint32_t sum = 0;
+            for (int t = t0; t < t1; ++t) sum += cur[t];
+            uint32_t inc = sum;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += u;
+            }
+            if (lane == 31) s_wsum[warp] = inc;
+            __syncthreads();
+            uint32_t run = inc - sum;
+            for (int w = 0; w < warp; ++w) run += s_wsum[w];
+            if (tid == kBinThreads - 1) s_total = run + sum;
+            for (int t = t0; t < t1; ++t) {
+                const uint32_t c = cur[t];
+                cur[t] = run;
+                delta[t] -= run;
+                run += c;
+            }
+            __syncthreads();
+            total = s_total;
+        }
+        const bool staged = STAGED && total <= (uint32_t)cap;
+        if (!staged) {
+            for (int t = tid; t < nt; t += kBinThreads) cur[t] = B.tile_start[t] + h[t];
+            __syncthreads();
+        }
+        for (int b = 0; b < kSeg && r0 + b < V; b += 32) {
+            if (tid < 32) load_batch_warp0(B, r0 + b + lane, V, colmask, rowmask, gids, box, lane);
+            __syncthreads();
+            const int bw = box[1] - box[0] + 1;
+            const int area = bw > 0 ? bw * (box[3] - box[2] + 1) : 0;
+            for (int i = tid; i < area; i += kBinThreads) {
+                const int q = i / bw;
+                const int ty = box[2] + q, tx = box[0] + (i - q * bw);
+                uint32_t m = colmask[tx] & rowmask[ty];
+                if (!m) continue;
+                const int t = ty * B.tiles_x + tx;
+                if (is_done(done, t)) continue;
+                uint32_t c = cur[t];
+                cur[t] = c + (uint32_t)__popc(m);
+                if (staged) {
+                    while (m) {
+                        const int j = __ffs(m) - 1;
+                        m &= m - 1u;
+                        buf_t[c] = (uint16_t)t;
+                        buf_r[c] = (uint8_t)(b + j);
+                        ++c;
+                    }
+                } else {
+                    while (m) {
+                        const int j = __ffs(m) - 1;
+                        m &= m - 1u;
+                        B.vals[c++] = gids[j];
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (staged)
+            for (uint32_t i = tid; i < total; i += kBinThreads) B.vals[delta[buf_t[i]] + i] = seg_g[buf_r[i]];
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Segment-parallel binning (default).  One CTA of kSeg threads per segment of
+// kSeg ranks (CTAs stride over the chunk's segments); warp w builds the column /
+// row ballot masks of batch w (ranks 32w..32w+31), all batches at once.  Each
+// thread then owns tiles t = tid, tid + kSeg, ...: the coverers of tile t in
+// batch b are the bits of colm[b][tx] & rowm[b][ty], in rank order, so a thread
+// emits its tiles' complete runs for the segment with no cursor shared across
+// threads and no barrier between batches.
+//   count: hist[segment][t] = sum_b popc(...)            (coalesced row store)
+//   emit:  runs are laid out in a shared-memory buffer (thread-major order, a
+//          block scan of the per-thread totals), then flushed with consecutive
+//          threads writing consecutive list entries.  Over capacity: direct.
+// ---------------------------------------------------------------------------
+constexpr int kSegThreads = kSeg;
+constexpr int kSegBatches = kSeg / 32;
+
+struct SegSmem {
+    uint32_t* done;
+    uint32_t* colm;  // [kSegBatches][tiles_x]
+    uint32_t* rowm;  // [kSegBatches][tiles_y]
+    uint32_t* seg_g; // [kSeg]
+};
+
+__device__ __forceinline__ size_t seg_fixed_words(const BinK& B) {
+    return (size_t)((B.ntiles + 31) >> 5) + (size_t)kSegBatches * (B.tiles_x + B.tiles_y) + kSeg;
+}
+
+__device__ __forceinline__ SegSmem seg_smem(const BinK& B, uint32_t* smem) {
+    SegSmem m;
+    m.done = smem;
+    m.colm = m.done + ((B.ntiles + 31) >> 5);
+    m.rowm = m.colm + kSegBatches * B.tiles_x;
+    m.seg_g = m.rowm + kSegBatches * B.tiles_y;
+    return m;
+}
+
+// Load the segment's ranks and build every batch's masks (ends with a barrier).
+__device__ __forceinline__ void seg_masks(const BinK& B, const SegSmem& m, int r0, int V) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int tx0 = 1, tx1 = 0, ty0 = 1, ty1 = 0;
+    uint32_t g = 0;
+    const int r = r0 + tid;
+    if (r < V) {
+        g = B.sorted_gidx[r];
+        const uint2 rc = B.rect[g];
+        const int x0 = rc.x & 0xffff, x1 = rc.x >> 16, y0 = rc.y & 0xffff, y1 = rc.y >> 16;
+        tx0 = x0 / B.ts;
+        tx1 = (x1 - 1) / B.ts;
+        ty0 = y0 / B.ts;
+        ty1 = (y1 - 1) / B.ts;
+    }
+    m.seg_g[tid] = g;
+    for (int i = tid; i < kSegBatches * (B.tiles_x + B.tiles_y); i += kSegThreads) m.colm[i] = 0u;  // colm, rowm
+    __syncthreads();
+    const bool valid = tx0 <= tx1 && ty0 <= ty1;
+    const int ux0 = __reduce_min_sync(0xffffffffu, valid ? tx0 : 0x7fffffff);
+    const int ux1 = __reduce_max_sync(0xffffffffu, valid ? tx1 : -1);
+    const int uy0 = __reduce_min_sync(0xffffffffu, valid ? ty0 : 0x7fffffff);
+    const int uy1 = __reduce_max_sync(0xffffffffu, valid ? ty1 : -1);
+    uint32_t* cm = m.colm + warp * B.tiles_x;
+    uint32_t* rm = m.rowm + warp * B.tiles_y;
+    for (int tx = ux0; tx <= ux1; ++tx) {
+        const uint32_t b = __ballot_sync(0xffffffffu, valid && tx0 <= tx && tx <= tx1);
+        if (lane == 0) cm[tx] = b;
+    }
+    for (int ty = uy0; ty <= uy1; ++ty) {
+        const uint32_t b = __ballot_sync(0xffffffffu, valid && ty0 <= ty && ty <= ty1);
+        if (lane == 0) rm[ty] = b;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t tile_count(const BinK& B, const SegSmem& m, int tx, int ty) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int b = 0; b < kSegBatches; ++b) c += __popc(m.colm[b * B.tiles_x + tx] & m.rowm[b * B.tiles_y + ty]);
+    return c;
+}
+
+__global__ void __launch_bounds__(kSegThreads) k_bin_count_seg(BinK B) {
+    extern __shared__ uint32_t smem[];
+    if (!chunk_live(B)) return;
+    const SegSmem m = seg_smem(B, smem);
+    stage_done(B, m.done);
+    const int V = *B.n_visible;
+    for (int segl = blockIdx.x; segl < B.nseg; segl += gridDim.x) {
+        const int r0 = (B.seg0 + segl) * kSeg;
+        uint32_t* h = B.hist + (size_t)segl * B.ntiles;
+        if (r0 >= V) {  // uniform
+            for (int t = threadIdx.x; t < B.ntiles; t += kSegThreads) h[t] = 0u;
+            continue;
+        }
+        seg_masks(B, m, r0, V);
+        for (int t = threadIdx.x; t < B.ntiles; t += kSegThreads) {
+            const int ty = t / B.tiles_x, tx = t - ty * B.tiles_x;
+            h[t] = is_done(m.done, t) ? 0u : tile_count(B, m, tx, ty);
         }
         __syncthreads();
     }
 }
 
+__global__ void __launch_bounds__(kSegThreads) k_bin_emit_seg(BinK B, int cap) {
+    extern __shared__ uint32_t smem[];
+    __shared__ uint32_t s_wsum[kSegThreads / 32];
+    if (!chunk_live(B)) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nt = B.ntiles;
+    const SegSmem m = seg_smem(B, smem);
+    uint32_t* delta = m.seg_g + kSeg;  // [ntiles] global list position - buffer position
+    uint16_t* buf_t = reinterpret_cast<uint16_t*>(delta + nt);
+    uint8_t* buf_r = reinterpret_cast<uint8_t*>(buf_t + cap);
+    stage_done(B, m.done);
+    const int V = *B.n_visible;
+    for (int segl = blockIdx.x; segl < B.nseg; segl += gridDim.x) {
+        const int r0 = (B.seg0 + segl) * kSeg;
+        if (r0 >= V) break;  // uniform; later segments of this CTA are past V too
+        const uint32_t* h = B.hist + (size_t)segl * nt;
+        seg_masks(B, m, r0, V);
+        // this thread's entry total -> its buffer base (block exclusive scan)
+        uint32_t mine = 0;
+        for (int t = tid; t < nt; t += kSegThreads) {
+            const int ty = t / B.tiles_x, tx = t - ty * B.tiles_x;
+            if (!is_done(m.done, t)) mine += tile_count(B, m, tx, ty);
+        }
+        uint32_t inc = mine;
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += u;
+        }
+        if (lane == 31) s_wsum[warp] = inc;
+        __syncthreads();
+        uint32_t c = inc - mine, total = 0;
+#pragma unroll
+        for (int w = 0; w < kSegThreads / 32; ++w) {
+            const uint32_t v = s_wsum[w];
+            c += w < warp ? v : 0u;
+            total += v;
+        }
+        const bool staged = total <= (uint32_t)cap;
+        for (int t = tid; t < nt; t += kSegThreads) {
+            if (is_done(m.done, t)) continue;
+            const int ty = t / B.tiles_x, tx = t - ty * B.tiles_x;
+            uint32_t gpos = B.tile_start[t] + h[t];
+            if (staged) delta[t] = gpos - c;
+#pragma unroll
+            for (int b = 0; b < kSegBatches; ++b) {
+                uint32_t mm = m.colm[b * B.tiles_x + tx] & m.rowm[b * B.tiles_y + ty];
+                while (mm) {
+                    const int j = __ffs(mm) - 1;
+                    mm &= mm - 1u;
+                    if (staged) {
+                        buf_t[c] = (uint16_t)t;
+                        buf_r[c] = (uint8_t)(b * 32 + j);
+                        ++c;
+                    } else {
+                        B.vals[gpos++] = m.seg_g[b * 32 + j];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (staged)
+            for (uint32_t i = tid; i < total; i += kSegThreads) B.vals[delta[buf_t[i]] + i] = m.seg_g[buf_r[i]];
+        __syncthreads();
+    }
+}
+
 void launch_bin_chunk(const BinK& B, cudaStream_t st) {
-    const bool sm = B.ntiles <= kSmemTiles;
-    const size_t smem = sizeof(uint32_t) * (size_t)(32 + B.tiles_x + B.tiles_y + (sm ? B.ntiles : 0));
-    const int grid = B.nseg;
     static bool attr = false;
     if (!attr) {
         const int mx = 200 * 1024;
         cudaFuncSetAttribute(k_bin_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(k_bin_emit<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(k_bin_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_bin_emit<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(k_bin_emit<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_bin_count_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_bin_emit_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         attr = true;
     }
-    if (sm)
-        k_bin_count<true><<<grid, kBinThreads, smem, st>>>(B);
+    const size_t seg_fixed = sizeof(uint32_t) * ((size_t)((B.ntiles + 31) >> 5) +
+                                                 (size_t)kSegBatches * (B.tiles_x + B.tiles_y) + kSeg);
+    const int cap = B.ntiles <= 2048 ? 6144 : 16384;
+    const size_t seg_emit = seg_fixed + sizeof(uint32_t) * (size_t)B.ntiles + 3 * (size_t)cap + 16;
+    if (seg_emit <= 200 * 1024 && B.ntiles <= 65535) {
+        k_bin_count_seg<<<std::min(B.nseg, 148 * 12), kSegThreads, seg_fixed, st>>>(B);
+        k_bin_scan_segments<<<(B.ntiles + 31) / 32, 1024, 0, st>>>(B);
+        k_bin_scan_tiles<<<1, 1024, 0, st>>>(B);
+        k_bin_emit_seg<<<std::min(B.nseg, 148 * 8), kSegThreads, seg_emit, st>>>(B, cap);
+        return;
+    }
+    // very large tile grids: batch-walk kernels with global cursors
+    const size_t base = sizeof(uint32_t) * (size_t)((B.ntiles + 31) / 32 + 32 + B.tiles_x + B.tiles_y);
+    const bool cnt_sm = B.ntiles <= kSmemTiles;
+    const size_t cnt_smem = base + (cnt_sm ? sizeof(uint32_t) * (size_t)B.ntiles : 0);
+    const int grid = std::min(B.nseg, 148 * 8);
+    if (cnt_sm)
+        k_bin_count<true><<<grid, kBinThreads, cnt_smem, st>>>(B);
     else
-        k_bin_count<false><<<grid, kBinThreads, smem, st>>>(B);
+        k_bin_count<false><<<grid, kBinThreads, cnt_smem, st>>>(B);
     k_bin_scan_segments<<<(B.ntiles + 31) / 32, 1024, 0, st>>>(B);
     k_bin_scan_tiles<<<1, 1024, 0, st>>>(B);
-    if (sm)
-        k_bin_emit<true><<<grid, kBinThreads, smem, st>>>(B);
-    else
-        k_bin_emit<false><<<grid, kBinThreads, smem, st>>>(B);
+    k_bin_emit<false><<<grid, kBinThreads, base, st>>>(B, 0);
 }
 
 }  // namespace tsb

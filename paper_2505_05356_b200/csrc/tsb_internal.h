@@ -62,7 +62,7 @@ struct RecK {
 
 // Depth-chunked binning (tsb_bin.cu).  Ranks are cut into segments of kSeg
 // (one warp each); chunk c covers segments [seg0, seg0 + nseg).
-constexpr int kSeg = 64;
+constexpr int kSeg = 128;
 struct BinK {
     const uint32_t* sorted_gidx;
     const uint2* rect;

@@ -99,6 +99,19 @@ def test_tile_size_invariance_and_lists(tsb, ctx, tile_size):
     check_images(out, ref)
 
 
+@pytest.mark.parametrize("ts,w,h", [(2, 320, 240), (1, 200, 150)])
+def test_many_tiles_binning_paths(tsb, ctx, ts, w, h):
+    """Large tile grids: 19,200 tiles (segment kernels, big staging tables) and 30,000
+    tiles (batch-walk kernels with global cursors) must give the oracle's lists exactly."""
+    from paper_2505_05356_b200 import synthetic
+    g = synthetic.gaussians(2500, 8, n_keyframes=2)
+    cam = synthetic.camera(w, h, 0.9 * w)
+    opts = tsb.RenderOptions(tile_size=ts, counts=True, full_lists=True)
+    _, rp, out, op, ref = render_both(tsb, ctx, g, cam, synthetic.ToFConfig(30e6), (0, 0.5), opts)
+    check_integers(rp, op, out, ref)
+    check_images(out, ref)
+
+
 @pytest.mark.parametrize("name,n", [("c0", None), ("c1", None), ("c3", 300_000)])
 def test_early_termination_is_bit_identical(tsb, ctx, name, n):
     """Binning stops for tiles whose pixels have all terminated; every output bit and
