@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -76,6 +77,7 @@ struct tsb_ctx {
     std::vector<std::pair<int, size_t>> ev_marks;  // (stage, index of start event)
     std::vector<tsb_pass*> passes;                 // joined by tsb_ctx_join
     int64_t redos = 0;                             // frames redone after a device-side abort
+    bool use_graphs = true;                        // forward as a CUDA graph (TSB_NO_GRAPHS=1 disables)
 };
 
 namespace {
@@ -205,7 +207,18 @@ struct tsb_pass {
     };
     std::vector<Download> pend_dl;  // asynchronous output downloads of the unsettled frame
     int planned_n = -1, planned_tiles = -1;  // chunk plan cache
+    // forward CUDA graph (conditional chunk nodes), rebuilt when forward_key changes
+    cudaStream_t cap_stream = nullptr;
+    FrameDev* frame_dev = nullptr;
+    cudaGraphExec_t fwd_exec = nullptr;
+    std::string fwd_key;
+    int fwd_fixed = 0;
+    bool count_live = false;
 };
+
+namespace {
+constexpr size_t kFrameSlot = 3072;  // FrameDev staging offset in tsb_pass::pinned
+}
 
 extern "C" {
 
@@ -227,6 +240,7 @@ int tsb_ctx_create(int device, tsb_ctx** out) {
     TSB_CUDA(cudaSetDevice(device));
     tsb_ctx* c = new tsb_ctx();
     c->device = device;
+    if (const char* ng = std::getenv("TSB_NO_GRAPHS")) c->use_graphs = !(ng[0] == '1');
     e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
         delete c;
@@ -663,6 +677,7 @@ int tsb_pass_create(tsb_ctx* ctx, tsb_pass** out) {
     tsb_pass* p = new tsb_pass();
     p->ctx = ctx;
     if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->done_ev, cudaEventDisableTiming) != cudaSuccess ||
         cudaMallocHost(&p->pinned, 4096) != cudaSuccess) {
         tsb_pass_destroy(p);
@@ -670,10 +685,11 @@ int tsb_pass_create(tsb_ctx* ctx, tsb_pass** out) {
     }
     int rc;
     if ((rc = dev_alloc(&p->counters, 8)) || (rc = dev_alloc(&p->loss_dev, 1)) || (rc = dev_alloc(&p->chw, 8)) ||
-        (rc = dev_alloc(&p->list_off, 1)) || (rc = dev_alloc(&p->fx_work_n, 1))) {
+        (rc = dev_alloc(&p->list_off, 1)) || (rc = dev_alloc(&p->fx_work_n, 1)) || (rc = dev_alloc(&p->frame_dev, 1))) {
         tsb_pass_destroy(p);
         return rc;
     }
+    bin_init();
     ctx->passes.push_back(p);
     *out = p;
     return TSB_OK;
@@ -807,7 +823,7 @@ int ensure_vals(tsb_pass* p, uint64_t need) {
 }
 
 PixK pixk(tsb_pass* p) {
-    PixK px;
+    PixK px{};
     px.out = p->out;
     const bool counts = (p->channels & TSB_CH_COUNTS) != 0;
     px.n_contrib = counts ? p->n_contrib : nullptr;
@@ -823,7 +839,7 @@ PixK pixk(tsb_pass* p) {
 }
 
 SceneK scenek(const tsb_scene* s) {
-    SceneK k;
+    SceneK k{};
     k.n = s->d.n;
     k.nk = s->d.n_keyframes;
     k.nf = s->d.n_freq;
@@ -868,6 +884,9 @@ void tsb_pass_destroy(tsb_pass* p) {
     dev_free(p->loss_part); dev_free(p->bg_part); dev_free(p->loss_dev); dev_free(p->chw);
     if (p->pinned) cudaFreeHost(p->pinned);
     if (p->done_ev) cudaEventDestroy(p->done_ev);
+    if (p->fwd_exec) cudaGraphExecDestroy(p->fwd_exec);
+    dev_free(p->frame_dev);
+    if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
     if (p->stream) cudaStreamDestroy(p->stream);
     delete p;
 }
@@ -1003,14 +1022,22 @@ namespace {
 // every planned chunk; chunks without work return on the device.  Ends with an
 // asynchronous read-back of the counters (visible count, abort word) that
 // settle() inspects.
-int enqueue_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw) {
-    TSB_CUDA(cudaSetDevice(p->ctx->device));
-    cudaStream_t st = p->stream;
+// Issue the forward's device work on `st`: per-frame values H2D, every planned
+// depth chunk (binning + raster), the fp64 fix-up, the pass-local part of the
+// loss and the counters read-back.  graph: `st` is capturing; chunks c >= 1 go
+// into conditional nodes gated on the device (k_chunk_gate), so a dead chunk
+// costs one tiny kernel instead of five launches.
+int record_forward(tsb_pass* p, cudaStream_t st, bool loss, const ChW& chw, bool graph, int* fixed_launches) {
     PixK px = pixk(p);
     const bool full = (p->channels & TSB_CH_FULL_LISTS) != 0;
+    int fixed = 0;
+    const FrameDev* fd = p->frame_dev;
+    TSB_CUDA(cudaMemcpyAsync(p->frame_dev, (char*)p->pinned + kFrameSlot, sizeof(FrameDev), cudaMemcpyHostToDevice,
+                             st));
     // counters[2] (abort word) is not cleared here: the depth sort of prepare may have set it
     TSB_CUDA(cudaMemsetAsync(p->counters + 1, 0, sizeof(int32_t), st));
     TSB_CUDA(cudaMemsetAsync(p->counters + 3, 0, sizeof(int32_t), st));
+    TSB_CUDA(cudaMemsetAsync(p->counters + 7, 0, sizeof(int32_t), st));
     TSB_CUDA(cudaMemsetAsync(p->list_off, 0, sizeof(uint32_t), st));
     TSB_CUDA(cudaMemsetAsync(p->block_done, 0, sizeof(int32_t) * p->nblocks, st));
     TSB_CUDA(cudaMemsetAsync(p->tile_blocks_done, 0, sizeof(int32_t) * p->ntiles, st));
@@ -1046,13 +1073,6 @@ int enqueue_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw)
         B.chunk = c;
         B.ranges = p->ranges_all + (size_t)c * p->ntiles;
         B.prev_ranges = c ? p->ranges_all + (size_t)(c - 1) * p->ntiles : nullptr;
-        if (nseg > 0) {
-            Stage sg(p->ctx, TSB_STAGE_BINNING, st);
-            launch_bin_chunk(B, st);
-            p->ctx->launches += 4;
-        } else {
-            TSB_CUDA(cudaMemsetAsync(B.ranges, 0, sizeof(uint4) * p->ntiles, st));
-        }
         ChunkK ck;
         ck.ranges = B.ranges;
         ck.first = c == 0;
@@ -1062,13 +1082,49 @@ int enqueue_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw)
         ck.tile_blocks_done = p->tile_blocks_done;
         ck.blocks_done_total = p->counters + 3;
         ck.overflow = p->counters + 2;
+        cudaStream_t cs = st;
+        if (graph && c > 0) {
+            // gate kernel, then an IF node whose body is captured on the pass's capture stream
+            cudaStreamCaptureStatus status;
+            cudaGraph_t g = nullptr;
+            const cudaGraphNode_t* deps = nullptr;
+            size_t ndeps = 0;
+            TSB_CUDA(cudaStreamGetCaptureInfo(st, &status, nullptr, &g, &deps, &ndeps));
+            cudaGraphConditionalHandle h;
+            TSB_CUDA(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
+            launch_chunk_gate(B, h, p->counters + 7, st);
+            TSB_CHECK_LAUNCH();
+            ++fixed;
+            TSB_CUDA(cudaStreamGetCaptureInfo(st, &status, nullptr, &g, &deps, &ndeps));
+            cudaGraphNodeParams np = {};
+            np.type = cudaGraphNodeTypeConditional;
+            np.conditional.handle = h;
+            np.conditional.type = cudaGraphCondTypeIf;
+            np.conditional.size = 1;
+            cudaGraphNode_t node;
+            TSB_CUDA(cudaGraphAddNode(&node, g, deps, ndeps, &np));
+            TSB_CUDA(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+            TSB_CUDA(cudaStreamBeginCaptureToGraph(p->cap_stream, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                   cudaStreamCaptureModeThreadLocal));
+            cs = p->cap_stream;
+        }
+        if (nseg > 0) {
+            Stage sg(p->ctx, TSB_STAGE_BINNING, cs);
+            launch_bin_chunk(B, cs);
+        } else {
+            TSB_CUDA(cudaMemsetAsync(B.ranges, 0, sizeof(uint4) * p->ntiles, cs));
+        }
         {
-            Stage sg(p->ctx, TSB_STAGE_RASTER_FWD, st);
-            launch_raster_fwd(p->rec, ck, p->vals, p->opt, p->W, p->H, p->nf, px, fs, loss ? target : nullptr, chw,
-                              p->loss_part, st);
-            p->ctx->launches += 1;
+            Stage sg(p->ctx, TSB_STAGE_RASTER_FWD, cs);
+            launch_raster_fwd(p->rec, ck, p->vals, p->opt, p->W, p->H, p->nf, px, fs, fd, loss, chw, p->loss_part, cs);
         }
         TSB_CHECK_LAUNCH();
+        if (cs != st) {
+            cudaGraph_t body = nullptr;
+            TSB_CUDA(cudaStreamEndCapture(cs, &body));
+        } else {
+            fixed += nseg > 0 ? 5 : 1;
+        }
     }
     p->nchunks = nplanned;
     FixupK fx;
@@ -1082,30 +1138,104 @@ int enqueue_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw)
     fx.n_visible = p->counters;
     fx.overflow = p->counters + 2;
     fx.stamp = p->fx_stamp;
-    fx.frame_stamp = ++p->frame_stamp;
     fx.work = p->fx_work;
     fx.work_n = p->fx_work_n;
     fx.cache = p->fx_cache;
     {
         Stage sg(p->ctx, TSB_STAGE_FIXUP, st);
-        launch_fixup(scenek(p->scene), p->cam, p->opt, p->frame, fx, px, p->nf, st);
-        p->ctx->launches += 3;
+        launch_fixup(scenek(p->scene), p->cam, p->opt, fd, fx, px, p->nf, st);
+        fixed += 3;
     }
     if (loss) {
         Stage sg(p->ctx, TSB_STAGE_LOSS, st);
         TSB_CUDA(cudaMemsetAsync(p->loss_dev, 0, sizeof(double), st));
-        launch_fixup_loss(px, p->W, p->H, p->nf, target, chw, p->loss_dev, st);
+        launch_fixup_loss(px, p->W, p->H, p->nf, fd, chw, p->loss_dev, st);
         launch_reduce_partials(p->loss_part, p->nblocks, 1, p->loss_dev, 1.0 / ((double)p->W * p->H), px.abort, st);
-        // scene loss accumulator += this pass's loss (serialised with other gradient writers)
-        TSB_CUDA(cudaStreamWaitEvent(st, p->scene->grads_ev, 0));
-        launch_reduce_partials(p->loss_dev, 1, 1, p->scene->stats + kStatLoss, 1.0, px.abort, st);
-        TSB_CUDA(cudaEventRecord(p->scene->grads_ev, st));
-        p->ctx->launches += 3;
+        fixed += 2;
     }
     TSB_CHECK_LAUNCH();
     int32_t* hc = (int32_t*)((char*)p->pinned + 2048);
     TSB_CUDA(cudaMemcpyAsync(hc, p->counters, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost, st));
     TSB_CUDA(cudaMemcpyAsync(hc + 8, p->list_off, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    *fixed_launches = fixed;
+    return TSB_OK;
+}
+
+// Everything a captured forward graph depends on, as bytes (a change rebuilds it).
+std::string forward_key(tsb_pass* p, bool loss, const ChW& chw) {
+    std::string k;
+    auto add = [&k](const void* d, size_t n) { k.append((const char*)d, n); };
+    const SceneK S = scenek(p->scene);
+    const PixK px = pixk(p);
+    const void* ptrs[] = {p->sorted, p->rect, p->counters, p->tile_blocks_done, p->hist, p->tile_len, p->tile_start,
+                          p->vals, p->list_off, p->ranges_all, p->block_done, p->rec.A, p->rec.B, p->rec.C, p->rec.D,
+                          p->st_f, p->st_d, p->st_i, p->loss_part, p->loss_dev, p->chunk_rank0, p->fx_stamp,
+                          p->fx_work, p->fx_work_n, p->fx_cache, p->frame_dev, p->pinned};
+    add(ptrs, sizeof ptrs);
+    add(&S, sizeof S);
+    add(&px, sizeof px);
+    add(&p->cam, sizeof p->cam);
+    add(&p->opt, sizeof p->opt);
+    add(&chw, sizeof chw);
+    const int ints[] = {p->W, p->H, p->nf, (int)p->channels, p->ntiles, p->nblocks, (int)p->vals_cap, loss ? 1 : 0,
+                        p->ctx->profiling ? 1 : 0};
+    add(ints, sizeof ints);
+    add(p->chunk_seg0.data(), sizeof(int) * p->chunk_seg0.size());
+    add(p->chunk_nseg.data(), sizeof(int) * p->chunk_nseg.size());
+    return k;
+}
+
+int enqueue_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw) {
+    TSB_CUDA(cudaSetDevice(p->ctx->device));
+    cudaStream_t st = p->stream;
+    FrameDev* slot = (FrameDev*)((char*)p->pinned + kFrameSlot);
+    slot->F = p->frame;
+    slot->target = loss ? target : nullptr;
+    slot->stamp = ++p->frame_stamp;
+    slot->pad = 0;
+    int fixed = 0;
+    // Graphs: not while stage events are being recorded (profiling runs the same kernels eagerly).
+    const bool use_graph = p->ctx->use_graphs && !p->ctx->profiling;
+    if (use_graph) {
+        std::string key = forward_key(p, loss, chw);
+        if (!p->fwd_exec || key != p->fwd_key) {
+            if (p->fwd_exec) cudaGraphExecDestroy(p->fwd_exec);
+            p->fwd_exec = nullptr;
+            TSB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            int rc = record_forward(p, st, loss, chw, true, &fixed);
+            cudaGraph_t g = nullptr;
+            cudaError_t e = cudaStreamEndCapture(st, &g);
+            if (rc) {
+                if (g) cudaGraphDestroy(g);
+                return rc;
+            }
+            if (e != cudaSuccess) return fail(TSB_ERR_CUDA, std::string("forward graph capture: ") + cudaGetErrorString(e));
+            e = cudaGraphInstantiate(&p->fwd_exec, g, 0);
+            cudaGraphDestroy(g);
+            if (e != cudaSuccess) {
+                p->fwd_exec = nullptr;
+                return fail(TSB_ERR_CUDA, std::string("forward graph instantiate: ") + cudaGetErrorString(e));
+            }
+            p->fwd_key = std::move(key);
+            p->fwd_fixed = fixed;
+        }
+        TSB_CUDA(cudaGraphLaunch(p->fwd_exec, st));
+        p->ctx->launches += p->fwd_fixed;
+        p->count_live = true;
+    } else {
+        int rc = record_forward(p, st, loss, chw, false, &fixed);
+        if (rc) return rc;
+        p->ctx->launches += fixed;
+        p->count_live = false;
+    }
+    if (loss) {
+        // scene loss accumulator += this pass's loss (serialised with other gradient writers)
+        TSB_CUDA(cudaStreamWaitEvent(st, p->scene->grads_ev, 0));
+        launch_reduce_partials(p->loss_dev, 1, 1, p->scene->stats + kStatLoss, 1.0, p->counters + 2, st);
+        TSB_CUDA(cudaEventRecord(p->scene->grads_ev, st));
+        p->ctx->launches += 1;
+        TSB_CHECK_LAUNCH();
+    }
     p->forwarded = true;
     p->have_loss = loss;
     p->pending = true;
@@ -1134,6 +1264,8 @@ int settle(tsb_pass* p) {
         p->pending = false;
         const int32_t* hc = (const int32_t*)((const char*)p->pinned + 2048);
         p->V = hc[0];
+        if (p->count_live) p->ctx->launches += 5 * (int64_t)hc[7];  // bodies of live chunks (graph)
+        p->count_live = false;
         const int ab = hc[2];
         if (!ab) return TSB_OK;
         if (attempt >= 8) return fail(TSB_ERR_NOMEM, "render: tile-list storage kept overflowing");

@@ -623,7 +623,29 @@ __global__ void __launch_bounds__(kSegThreads) k_bin_emit_seg(BinK B, int cap) {
     }
 }
 
-void launch_bin_chunk(const BinK& B, cudaStream_t st) {
+// Graph gate of a depth chunk (c >= 1): the chunk's conditional node runs its
+// binning + raster body only when the chunk is live; a dead chunk's ranges are
+// written here exactly as k_bin_scan_tiles would (empty, every tile skipped).
+__global__ void k_chunk_gate(BinK B, cudaGraphConditionalHandle h, int32_t* live_chunks) {
+    const bool live = chunk_live(B);
+    if (threadIdx.x == 0) {
+        cudaGraphSetConditional(h, live ? 1u : 0u);
+        if (live) atomicAdd(live_chunks, 1);
+    }
+    if (live) return;
+    const uint32_t base = *B.list_off;
+    for (int t = threadIdx.x; t < B.ntiles; t += blockDim.x) {
+        const uint32_t cum = B.chunk == 0 ? 0u : B.prev_ranges[t].z + B.prev_ranges[t].y;
+        B.ranges[t] = make_uint4(base, 0u, cum, 1u);
+    }
+}
+
+void launch_chunk_gate(const BinK& B, cudaGraphConditionalHandle h, int32_t* live_chunks, cudaStream_t st) {
+    k_chunk_gate<<<1, 1024, 0, st>>>(B, h, live_chunks);
+}
+
+// Kernel attributes (outside any stream capture: called when a pass is created).
+void bin_init() {
     static bool attr = false;
     if (!attr) {
         const int mx = 200 * 1024;
@@ -635,6 +657,9 @@ void launch_bin_chunk(const BinK& B, cudaStream_t st) {
         cudaFuncSetAttribute(k_bin_emit_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         attr = true;
     }
+}
+
+void launch_bin_chunk(const BinK& B, cudaStream_t st) {
     const size_t seg_fixed = sizeof(uint32_t) * ((size_t)((B.ntiles + 31) >> 5) +
                                                  (size_t)kSegBatches * (B.tiles_x + B.tiles_y) + kSeg);
     const int cap = B.ntiles <= 2048 ? 6144 : 16384;

@@ -121,12 +121,13 @@ __device__ __forceinline__ Rec64 make_rec64(const SceneK& S, const CamK& C, cons
 
 // Mark the Gaussians the flagged pixels will visit (their tile lists up to the
 // fp32 termination point + a margin) and queue each once for the record cache.
-__global__ void __launch_bounds__(128) k_fixup_mark(OptK O, FixupK fx, PixK px, int W) {
+__global__ void __launch_bounds__(128) k_fixup_mark(OptK O, FixupK fx, PixK px, int W, const FrameDev* __restrict__ fd) {
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int count = *fx.overflow ? 0 : *px.n_flagged;
     const int ntiles = O.tiles_x * O.tiles_y;
+    const int stamp = fd->stamp;
     for (int i = warp; i < count; i += nwarps) {
         const int pix = px.flagged[i] & 0xffffff;
         const int x = pix % W, y = pix / W;
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(128) k_fixup_mark(OptK O, FixupK fx, PixK px, 
             const uint32_t end = rg.x + min(rg.y, (uint32_t)(limit - (int)rg.z));
             for (uint32_t e = rg.x + lane; e < end; e += 32) {
                 const uint32_t g = fx.vals[e];
-                if (atomicExch(&fx.stamp[g], fx.frame_stamp) != fx.frame_stamp) {
+                if (atomicExch(&fx.stamp[g], stamp) != stamp) {
                     const int slot = atomicAdd(fx.work_n, 1);
                     fx.work[slot] = (int)g;
                 }
@@ -147,8 +148,10 @@ __global__ void __launch_bounds__(128) k_fixup_mark(OptK O, FixupK fx, PixK px, 
     }
 }
 
-__global__ void __launch_bounds__(128) k_fixup_records(SceneK S, CamK C, OptK O, FrameK F, FixupK fx) {
+__global__ void __launch_bounds__(128) k_fixup_records(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd,
+                                                       FixupK fx) {
     const int n = *fx.work_n;
+    const FrameK F = fd->F;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int g = fx.work[i];
         fx.cache[g] = make_rec64(S, C, O, F, g);
@@ -173,13 +176,13 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 __device__ __forceinline__ void fixup_batch(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
-                                            const FixupK& fx, int nf, int x, int y, bool is_entry, int g,
+                                            const FixupK& fx, int stamp, int nf, int x, int y, bool is_entry, int g,
                                             int entry_idx, FixSlot* slot, FixupAcc& a, int lane) {
     const double pcx = x + 0.5, pcy = y + 0.5;
     bool inc = false;
     double alpha = 0.0, coef = 0.0, depth = 0.0;
     if (is_entry) {
-        const Rec64 r = fx.stamp[g] == fx.frame_stamp ? fx.cache[g] : make_rec64(S, C, O, F, g);
+        const Rec64 r = fx.stamp[g] == stamp ? fx.cache[g] : make_rec64(S, C, O, F, g);
         if (!(x < r.rect.x || x >= r.rect.y || y < r.rect.z || y >= r.rect.w)) {
             const double dx = pcx - r.m0.x, dy = pcy - r.m0.y;
             const double maha = r.m0.z * dx * dx + 2.0 * r.m0.w * dx * dy + r.m1.x * dy * dy;
@@ -258,8 +261,11 @@ __device__ __forceinline__ void fixup_batch(const SceneK& S, const CamK& C, cons
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, FrameK F, FixupK fx, PixK px, int nf) {
+__global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd, FixupK fx,
+                                               PixK px, int nf) {
     __shared__ FixSlot slots[4][32];
+    const FrameK F = fd->F;
+    const int stamp = fd->stamp;
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -291,7 +297,7 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, FrameK 
             for (uint32_t b = rg.x; b < end && !a.done; b += 32) {
                 const uint32_t e = b + lane;
                 const bool is_e = e < end;
-                fixup_batch(S, C, O, F, fx, nf, x, y, is_e, is_e ? (int)fx.vals[e] : 0, (int)(rg.z + (e - rg.x)),
+                fixup_batch(S, C, O, F, fx, stamp, nf, x, y, is_e, is_e ? (int)fx.vals[e] : 0, (int)(rg.z + (e - rg.x)),
                             slot, a, lane);
             }
             if (!a.done) a.processed = (int)(rg.z + rg.y);
@@ -310,7 +316,7 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, FrameK 
                 cov = x0 / O.ts <= tx && tx <= (x1 - 1) / O.ts && y0 / O.ts <= ty && ty <= (y1 - 1) / O.ts;
             }
             const unsigned cm = __ballot_sync(0xffffffffu, cov);
-            fixup_batch(S, C, O, F, fx, nf, x, y, cov, g, a.processed + __popc(cm & lanes_below), slot, a, lane);
+            fixup_batch(S, C, O, F, fx, stamp, nf, x, y, cov, g, a.processed + __popc(cm & lanes_below), slot, a, lane);
             if (!a.done) a.processed += __popc(cm);
         }
         if (lane == 0) {
@@ -341,12 +347,12 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, FrameK 
     }
 }
 
-void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F, const FixupK& fx,
+void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd, const FixupK& fx,
                   const PixK& px, int nf, cudaStream_t st) {
     cudaMemsetAsync(fx.work_n, 0, sizeof(int), st);
-    k_fixup_mark<<<148 * 2, 128, 0, st>>>(O, fx, px, C.W);
-    k_fixup_records<<<148 * 4, 128, 0, st>>>(S, C, O, F, fx);
-    k_fixup<<<148 * 4, 128, 0, st>>>(S, C, O, F, fx, px, nf);
+    k_fixup_mark<<<148 * 2, 128, 0, st>>>(O, fx, px, C.W, fd);
+    k_fixup_records<<<148 * 4, 128, 0, st>>>(S, C, O, fd, fx);
+    k_fixup<<<148 * 4, 128, 0, st>>>(S, C, O, fd, fx, px, nf);
 }
 
 // Intermediates the chain needs, recomputed in fp64 with reciprocals instead of

@@ -51,6 +51,16 @@ struct FrameK {
     double w;
 };
 
+// Per-frame values the forward kernels read from device memory (so one captured
+// CUDA graph serves every frame): written by a host->device copy from the pass's
+// pinned staging slot at the start of each forward.
+struct FrameDev {
+    FrameK F;
+    const float* target;  // loss target (planar [4*nf][H][W]) or null
+    int stamp;            // fix-up record-cache stamp
+    int pad;
+};
+
 // fp32 raster records, indexed by Gaussian (SoA).  The conic is stored
 // factored, conic = L^T L, L = [[l11, l12], [0, l22]] (see tsb_raster.cu).
 struct RecK {
@@ -168,13 +178,12 @@ struct FixupK {
     const uint2* rect;
     const int32_t* n_visible;
     const int32_t* overflow;
-    int* stamp;        // [n] frame stamp of the cached record
-    int frame_stamp;
+    int* stamp;        // [n] frame stamp of the cached record (FrameDev::stamp)
     int* work;         // [n] Gaussians queued for the record cache
     int* work_n;
     Rec64* cache;      // [n]
 };
-void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F, const FixupK& fx,
+void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd, const FixupK& fx,
                   const PixK& px, int nf, cudaStream_t st);
 void launch_chain(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
                   const uint32_t* touched, float* screen, float4* grads, cudaStream_t st);
@@ -196,13 +205,17 @@ int launch_sort_depth(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint
                       uint32_t* scratch, cudaStream_t st);  // result in (keys_b, vals_b)
 int launch_sort_depth64(const double* depth64, const uint32_t* touched, uint32_t* keys_a, uint32_t* keys_b,
                         uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch, cudaStream_t st);
+void bin_init();  // kernel attributes; call before any capture
 void launch_bin_chunk(const BinK& B, cudaStream_t st);
 // tsb_raster.cu
 void launch_raster_fwd(const RecK& rec, const ChunkK& ck, const uint32_t* tile_vals, const OptK& O,
-                       int W, int H, int nf, PixK px, FwdState fs, const float* target, const ChW& ch_w,
+                       int W, int H, int nf, PixK px, FwdState fs, const FrameDev* fd, bool loss, const ChW& ch_w,
                        double* loss_part, cudaStream_t st);
-void launch_fixup_loss(const PixK& px, int W, int H, int nf, const float* target, const ChW& ch_w,
+void launch_fixup_loss(const PixK& px, int W, int H, int nf, const FrameDev* fd, const ChW& ch_w,
                        double* loss_extra, cudaStream_t st);
+// CUDA-graph gate of depth chunk c >= 1: sets the chunk's IF-node condition to its
+// liveness (tsb_bin.cu chunk_live); a dead chunk's ranges are written empty here.
+void launch_chunk_gate(const BinK& B, cudaGraphConditionalHandle h, int32_t* live_chunks, cudaStream_t st);
 void launch_raster_bwd(const RecK& rec, const uint4* ranges_all, int nchunks, const uint32_t* tile_vals,
                        const OptK& O, int W, int H, int nf, const float* dpsi, PixK px, const UpK& up,
                        float* screen, int scap, double* bg_part, cudaStream_t st);

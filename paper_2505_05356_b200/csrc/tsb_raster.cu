@@ -97,11 +97,12 @@ struct Smem {
 template <int NF, bool DIST>
 __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK ck, const uint32_t* __restrict__ vals,
                                                                 OptK O, int W, int H, PixK px, FwdState fs,
-                                                                const float* __restrict__ target, ChW chw,
+                                                                const FrameDev* __restrict__ fd, int loss, ChW chw,
                                                                 double* __restrict__ loss_part) {
     __shared__ Smem<NF> sm;
     __shared__ float red[kRasterThreads / 32];
     if (ck.block_done[blockIdx.x] || *ck.overflow) return;
+    const float* __restrict__ target = loss ? fd->target : nullptr;
     const int nsub = O.sub * O.sub;
     const int tile = blockIdx.x / nsub, sb = blockIdx.x % nsub;
     const int tid = threadIdx.x;
@@ -305,9 +306,10 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
 }
 
 // Loss + d_quad for the fp64-fixed pixels (after k_fixup).
-__global__ void k_fixup_loss(PixK px, int W, int H, int nf, const float* __restrict__ target, ChW chw,
+__global__ void k_fixup_loss(PixK px, int W, int H, int nf, const FrameDev* __restrict__ fd, ChW chw,
                              double* __restrict__ loss_extra) {
     if (*px.abort) return;
+    const float* __restrict__ target = fd->target;
     const int count = *px.n_flagged;
     double l = 0.0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
@@ -582,11 +584,12 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
 }
 
 void launch_raster_fwd(const RecK& rec, const ChunkK& ck, const uint32_t* tile_vals, const OptK& O, int W, int H,
-                       int nf, PixK px, FwdState fs, const float* target, const ChW& ch_w, double* loss_part,
-                       cudaStream_t st) {
+                       int nf, PixK px, FwdState fs, const FrameDev* fd, bool loss, const ChW& ch_w,
+                       double* loss_part, cudaStream_t st) {
     const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
 #define TSB_FWD(NF_, D_) \
-    k_raster_fwd<NF_, D_><<<grid, kRasterThreads, 0, st>>>(rec, ck, tile_vals, O, W, H, px, fs, target, ch_w, loss_part)
+    k_raster_fwd<NF_, D_><<<grid, kRasterThreads, 0, st>>>(rec, ck, tile_vals, O, W, H, px, fs, fd, loss ? 1 : 0, ch_w, \
+                                                           loss_part)
     if (nf > 1) {
         if (O.dist) TSB_FWD(2, true); else TSB_FWD(2, false);
     } else {
@@ -595,9 +598,9 @@ void launch_raster_fwd(const RecK& rec, const ChunkK& ck, const uint32_t* tile_v
 #undef TSB_FWD
 }
 
-void launch_fixup_loss(const PixK& px, int W, int H, int nf, const float* target, const ChW& ch_w,
+void launch_fixup_loss(const PixK& px, int W, int H, int nf, const FrameDev* fd, const ChW& ch_w,
                        double* loss_extra, cudaStream_t st) {
-    k_fixup_loss<<<64, 256, 0, st>>>(px, W, H, nf, target, ch_w, loss_extra);
+    k_fixup_loss<<<64, 256, 0, st>>>(px, W, H, nf, fd, ch_w, loss_extra);
 }
 
 void launch_raster_bwd(const RecK& rec, const uint4* ranges_all, int nchunks, const uint32_t* tile_vals,
