@@ -210,10 +210,14 @@ struct tsb_pass {
     // forward CUDA graph (conditional chunk nodes), rebuilt when forward_key changes
     cudaStream_t cap_stream = nullptr;
     FrameDev* frame_dev = nullptr;
-    cudaGraphExec_t fwd_exec = nullptr;
-    std::string fwd_key;
-    int fwd_fixed = 0;
+    struct FwdGraph {
+        cudaGraphExec_t exec = nullptr;
+        std::string key;
+        int fixed = 0;
+    };
+    FwdGraph fwd[2];            // [0]: forward only, [1]: deferred prepare + forward
     bool count_live = false;
+    bool prep_deferred = false; // prepare's device work not issued yet
 };
 
 namespace {
@@ -292,9 +296,11 @@ void tsb_ctx_destroy(tsb_ctx* c) {
 
 namespace {
 int settle(tsb_pass* p);
+int flush_prepare(tsb_pass* p);
 int settle_all(tsb_ctx* c) {
     for (tsb_pass* p : c->passes) {
-        int rc = settle(p);
+        int rc = flush_prepare(p);  // a prepared frame reads the scene as it is now
+        if (!rc) rc = settle(p);
         if (rc) return rc;
     }
     return TSB_OK;
@@ -858,7 +864,9 @@ SceneK scenek(const tsb_scene* s) {
 }
 
 int read_visible(tsb_pass* p) {
-    int rc0 = settle(p);
+    int rc0 = flush_prepare(p);
+    if (rc0) return rc0;
+    rc0 = settle(p);
     if (rc0) return rc0;
     if (p->V >= 0) return TSB_OK;
     int32_t* h = (int32_t*)((char*)p->pinned + 1024);
@@ -884,7 +892,8 @@ void tsb_pass_destroy(tsb_pass* p) {
     dev_free(p->loss_part); dev_free(p->bg_part); dev_free(p->loss_dev); dev_free(p->chw);
     if (p->pinned) cudaFreeHost(p->pinned);
     if (p->done_ev) cudaEventDestroy(p->done_ev);
-    if (p->fwd_exec) cudaGraphExecDestroy(p->fwd_exec);
+    for (auto& fg : p->fwd)
+        if (fg.exec) cudaGraphExecDestroy(fg.exec);
     dev_free(p->frame_dev);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
     if (p->stream) cudaStreamDestroy(p->stream);
@@ -910,7 +919,6 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     if (cam->width > 32767 || cam->height > 32767)
         return fail(TSB_ERR_UNSUPPORTED, "render: image dimensions above 32767 are not supported");
     TSB_CUDA(cudaSetDevice(p->ctx->device));
-    cudaStream_t st = p->stream;
 
     p->scene = s;
     p->nf = s->d.n_freq;
@@ -970,28 +978,19 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     if ((rc = ensure_vals(p, std::max<uint64_t>({(uint64_t)n * 8, (uint64_t)p->ntiles * 1024, 1u << 20}))))
         return rc;
 
-    const SceneK S = scenek(s);
-    TSB_CUDA(cudaStreamWaitEvent(st, s->params_ev, 0));
-    TSB_CUDA(cudaMemsetAsync(p->counters, 0, sizeof(int32_t) * 8, st));
-    TSB_CUDA(cudaMemsetAsync(p->counters + 5, 0xff, sizeof(int32_t), st));  // key range min
-    uint32_t* key_range = reinterpret_cast<uint32_t*>(p->counters + 5);
-    {
-        Stage sg(p->ctx, TSB_STAGE_PREPROCESS, st);
-        launch_preprocess(S, C, O, p->frame, p->key_a, p->depth64, p->gidx_a, p->touched, p->rect, p->rec,
-                          p->counters, key_range, st);
-    }
-    {
-        Stage sg(p->ctx, TSB_STAGE_DEPTH_SORT, st);
-        p->ctx->launches += launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, p->depth64, p->counters,
-                                              p->counters + 2, key_range, n, p->sort_scratch, st);
-    }
-    p->sorted = p->gidx_b;
-    p->ctx->launches += 1;
-    TSB_CHECK_LAUNCH();
+    // The device work (preprocess + depth sort) is deferred: it becomes the head of
+    // the forward graph, or is issued eagerly by flush_prepare when something reads
+    // prepare's results before a forward.
+    FrameDev* slot = (FrameDev*)((char*)p->pinned + kFrameSlot);
+    slot->F = p->frame;
+    slot->target = nullptr;
+    slot->stamp = ++p->frame_stamp;
+    slot->pad = 0;
+    p->prep_deferred = true;
+    p->sorted = p->gidx_b;  // launch_sort_depth's result buffer
     p->V = -1;
     p->nchunks = 0;
     p->prepared = true;
-    TSB_CUDA(cudaEventRecord(p->done_ev, st));
     return TSB_OK;
 }
 
@@ -1022,18 +1021,62 @@ namespace {
 // every planned chunk; chunks without work return on the device.  Ends with an
 // asynchronous read-back of the counters (visible count, abort word) that
 // settle() inspects.
+// prepare's device work: per-frame values H2D, counters, preprocess, depth order.
+int record_prepare(tsb_pass* p, cudaStream_t st, int* launches) {
+    const int n = p->scene->d.n;
+    TSB_CUDA(cudaMemcpyAsync(p->frame_dev, (char*)p->pinned + kFrameSlot, sizeof(FrameDev), cudaMemcpyHostToDevice,
+                             st));
+    TSB_CUDA(cudaMemsetAsync(p->counters, 0, sizeof(int32_t) * 8, st));
+    TSB_CUDA(cudaMemsetAsync(p->counters + 5, 0xff, sizeof(int32_t), st));  // key range min
+    uint32_t* key_range = reinterpret_cast<uint32_t*>(p->counters + 5);
+    {
+        Stage sg(p->ctx, TSB_STAGE_PREPROCESS, st);
+        launch_preprocess(scenek(p->scene), p->cam, p->opt, p->frame_dev, p->key_a, p->depth64, p->gidx_a, p->touched,
+                          p->rect, p->rec, p->counters, key_range, st);
+    }
+    int l = n > 0 ? 1 : 0;
+    {
+        Stage sg(p->ctx, TSB_STAGE_DEPTH_SORT, st);
+        l += launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, p->depth64, p->counters, p->counters + 2,
+                               key_range, n, p->sort_scratch, st);
+    }
+    TSB_CHECK_LAUNCH();
+    *launches = l;
+    return TSB_OK;
+}
+
+// Issue a deferred prepare eagerly (something reads its results before a forward).
+int flush_prepare(tsb_pass* p) {
+    if (!p->prep_deferred) return TSB_OK;
+    TSB_CUDA(cudaSetDevice(p->ctx->device));
+    TSB_CUDA(cudaStreamWaitEvent(p->stream, p->scene->params_ev, 0));
+    int l = 0;
+    int rc = record_prepare(p, p->stream, &l);
+    if (rc) return rc;
+    p->ctx->launches += l;
+    p->prep_deferred = false;
+    TSB_CUDA(cudaEventRecord(p->done_ev, p->stream));
+    return TSB_OK;
+}
+
 // Issue the forward's device work on `st`: per-frame values H2D, every planned
 // depth chunk (binning + raster), the fp64 fix-up, the pass-local part of the
 // loss and the counters read-back.  graph: `st` is capturing; chunks c >= 1 go
 // into conditional nodes gated on the device (k_chunk_gate), so a dead chunk
 // costs one tiny kernel instead of five launches.
-int record_forward(tsb_pass* p, cudaStream_t st, bool loss, const ChW& chw, bool graph, int* fixed_launches) {
+int record_forward(tsb_pass* p, cudaStream_t st, bool loss, const ChW& chw, bool graph, bool with_prep,
+                   int* fixed_launches) {
     PixK px = pixk(p);
     const bool full = (p->channels & TSB_CH_FULL_LISTS) != 0;
     int fixed = 0;
     const FrameDev* fd = p->frame_dev;
-    TSB_CUDA(cudaMemcpyAsync(p->frame_dev, (char*)p->pinned + kFrameSlot, sizeof(FrameDev), cudaMemcpyHostToDevice,
-                             st));
+    if (with_prep) {
+        int rc = record_prepare(p, st, &fixed);
+        if (rc) return rc;
+    } else {
+        TSB_CUDA(cudaMemcpyAsync(p->frame_dev, (char*)p->pinned + kFrameSlot, sizeof(FrameDev),
+                                 cudaMemcpyHostToDevice, st));
+    }
     // counters[2] (abort word) is not cleared here: the depth sort of prepare may have set it
     TSB_CUDA(cudaMemsetAsync(p->counters + 1, 0, sizeof(int32_t), st));
     TSB_CUDA(cudaMemsetAsync(p->counters + 3, 0, sizeof(int32_t), st));
@@ -1177,32 +1220,34 @@ std::string forward_key(tsb_pass* p, bool loss, const ChW& chw) {
     add(&p->cam, sizeof p->cam);
     add(&p->opt, sizeof p->opt);
     add(&chw, sizeof chw);
+    const void* prep_ptrs[] = {p->key_a, p->key_b, p->depth64, p->gidx_a, p->gidx_b, p->touched, p->sort_scratch};
+    add(prep_ptrs, sizeof prep_ptrs);
     const int ints[] = {p->W, p->H, p->nf, (int)p->channels, p->ntiles, p->nblocks, (int)p->vals_cap, loss ? 1 : 0,
-                        p->ctx->profiling ? 1 : 0};
+                        p->ctx->profiling ? 1 : 0, p->prep_deferred ? 1 : 0};
     add(ints, sizeof ints);
     add(p->chunk_seg0.data(), sizeof(int) * p->chunk_seg0.size());
     add(p->chunk_nseg.data(), sizeof(int) * p->chunk_nseg.size());
     return k;
 }
 
-int enqueue_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw) {
+int enqueue_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw, bool allow_graph = true) {
     TSB_CUDA(cudaSetDevice(p->ctx->device));
     cudaStream_t st = p->stream;
     FrameDev* slot = (FrameDev*)((char*)p->pinned + kFrameSlot);
-    slot->F = p->frame;
     slot->target = loss ? target : nullptr;
-    slot->stamp = ++p->frame_stamp;
-    slot->pad = 0;
+    const bool with_prep = p->prep_deferred;
+    if (with_prep) TSB_CUDA(cudaStreamWaitEvent(st, p->scene->params_ev, 0));
     int fixed = 0;
     // Graphs: not while stage events are being recorded (profiling runs the same kernels eagerly).
-    const bool use_graph = p->ctx->use_graphs && !p->ctx->profiling;
+    const bool use_graph = allow_graph && p->ctx->use_graphs && !p->ctx->profiling;
     if (use_graph) {
         std::string key = forward_key(p, loss, chw);
-        if (!p->fwd_exec || key != p->fwd_key) {
-            if (p->fwd_exec) cudaGraphExecDestroy(p->fwd_exec);
-            p->fwd_exec = nullptr;
+        tsb_pass::FwdGraph& fg = p->fwd[with_prep ? 1 : 0];
+        if (!fg.exec || key != fg.key) {
+            if (fg.exec) cudaGraphExecDestroy(fg.exec);
+            fg.exec = nullptr;
             TSB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-            int rc = record_forward(p, st, loss, chw, true, &fixed);
+            int rc = record_forward(p, st, loss, chw, true, with_prep, &fixed);
             cudaGraph_t g = nullptr;
             cudaError_t e = cudaStreamEndCapture(st, &g);
             if (rc) {
@@ -1210,24 +1255,25 @@ int enqueue_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw)
                 return rc;
             }
             if (e != cudaSuccess) return fail(TSB_ERR_CUDA, std::string("forward graph capture: ") + cudaGetErrorString(e));
-            e = cudaGraphInstantiate(&p->fwd_exec, g, 0);
+            e = cudaGraphInstantiate(&fg.exec, g, 0);
             cudaGraphDestroy(g);
             if (e != cudaSuccess) {
-                p->fwd_exec = nullptr;
+                fg.exec = nullptr;
                 return fail(TSB_ERR_CUDA, std::string("forward graph instantiate: ") + cudaGetErrorString(e));
             }
-            p->fwd_key = std::move(key);
-            p->fwd_fixed = fixed;
+            fg.key = std::move(key);
+            fg.fixed = fixed;
         }
-        TSB_CUDA(cudaGraphLaunch(p->fwd_exec, st));
-        p->ctx->launches += p->fwd_fixed;
+        TSB_CUDA(cudaGraphLaunch(fg.exec, st));
+        p->ctx->launches += fg.fixed;
         p->count_live = true;
     } else {
-        int rc = record_forward(p, st, loss, chw, false, &fixed);
+        int rc = record_forward(p, st, loss, chw, false, with_prep, &fixed);
         if (rc) return rc;
         p->ctx->launches += fixed;
         p->count_live = false;
     }
+    p->prep_deferred = false;
     if (loss) {
         // scene loss accumulator += this pass's loss (serialised with other gradient writers)
         TSB_CUDA(cudaStreamWaitEvent(st, p->scene->grads_ev, 0));
@@ -1285,7 +1331,7 @@ int settle(tsb_pass* p) {
         const bool bwd = p->pend_bwd;
         const UpK up = p->pend_up;
         const std::vector<tsb_pass::Download> dls = p->pend_dl;
-        int rc = enqueue_forward(p, p->pend_target, p->pend_loss, p->pend_chw);
+        int rc = enqueue_forward(p, p->pend_target, p->pend_loss, p->pend_chw, false);
         if (rc) return rc;
         if (bwd && (rc = enqueue_backward(p, up))) return rc;
         for (const auto& d : dls) {  // re-issue the frame's asynchronous downloads

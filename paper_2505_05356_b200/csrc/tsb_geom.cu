@@ -13,7 +13,7 @@ namespace tsb {
 // the fp32 raster record (indexed by Gaussian; the duplicate kernel gathers it
 // into rank order).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, FrameK F,
+__global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd,
                                                     uint32_t* __restrict__ depth_key,
                                                     double* __restrict__ depth64,
                                                     uint32_t* __restrict__ gidx,
@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, Fr
                                                     uint32_t* __restrict__ key_range) {
     uint32_t kmine = 0xffffffffu, kmaxe = 0u;
     const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+    const FrameK F = fd->F;
     bool vis = false;
     if (gi < S.n) {
         Prep64 s;
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, Fr
     }
 }
 
-void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
+void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* F,
                        uint32_t* depth_key, double* depth64, uint32_t* gidx, uint32_t* touched, uint2* rect,
                        RecK rec, int32_t* n_visible, uint32_t* key_range, cudaStream_t st) {
     if (S.n <= 0) return;

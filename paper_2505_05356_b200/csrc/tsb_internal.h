@@ -158,7 +158,7 @@ constexpr int kStatBg = 0, kStatLoss = 12, kStats = 13;
 
 // ---- launchers (defined in the .cu files) ----
 // tsb_geom.cu (fp64, compiled without FMA contraction)
-void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
+void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* F,
                        uint32_t* depth_key, double* depth64, uint32_t* gidx, uint32_t* touched, uint2* rect,
                        RecK rec, int32_t* n_visible, uint32_t* key_range, cudaStream_t st);
 // fp64 record cache for the fix-up (valid when stamp[g] == frame stamp).
