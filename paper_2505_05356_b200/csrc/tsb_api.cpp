@@ -121,6 +121,7 @@ struct tsb_scene {
     float* densify = nullptr;
     double* stats = nullptr;  // kStats: bg grads (quad 4*nf, phasor 2*nf) at kStatBg, loss at kStatLoss
     float* staging = nullptr; // 4n floats for host<->device (un)packing
+    double* pcache = nullptr; // [7][n]: cov3d (6 planes) + opacity (SceneK::cov6 / opac)
     int64_t step = 0;
     int64_t densify_count = 0;
     cudaEvent_t params_ev = nullptr;  // last parameter write (ctx stream)
@@ -331,6 +332,18 @@ int64_t tsb_ctx_launch_count(tsb_ctx* c) { return c ? c->launches : 0; }
 // ---------------------------------------------------------------------------
 // scene
 // ---------------------------------------------------------------------------
+namespace {
+SceneK scenek(const tsb_scene* s);
+// Refresh the time-independent cache after a parameter change (ctx stream).
+int refresh_param_cache(tsb_scene* s) {
+    const SceneK S = scenek(s);
+    launch_param_cache(S, s->pcache, s->pcache + 6 * (size_t)s->d.n, s->ctx->stream);
+    if (s->d.n > 0) s->ctx->launches++;
+    TSB_CHECK_LAUNCH();
+    return TSB_OK;
+}
+}  // namespace
+
 int tsb_scene_create(tsb_ctx* ctx, const tsb_scene_desc* d, tsb_scene** out) {
     if (!ctx || !d || !out) return fail(TSB_ERR_INVALID, "tsb_scene_create: null argument");
     *out = nullptr;
@@ -352,7 +365,8 @@ int tsb_scene_create(tsb_ctx* ctx, const tsb_scene_desc* d, tsb_scene** out) {
     int rc = TSB_OK;
     if ((rc = dev_alloc(&s->params, nel)) || (rc = dev_alloc(&s->grads, nel)) || (rc = dev_alloc(&s->m, nel)) ||
         (rc = dev_alloc(&s->v, nel)) || (rc = dev_alloc(&s->densify, (size_t)std::max(d->n, 1))) ||
-        (rc = dev_alloc(&s->stats, kStats)) || (rc = dev_alloc(&s->staging, 4 * (size_t)std::max(d->n, 1)))) {
+        (rc = dev_alloc(&s->stats, kStats)) || (rc = dev_alloc(&s->staging, 4 * (size_t)std::max(d->n, 1))) ||
+        (rc = dev_alloc(&s->pcache, 7 * (size_t)std::max(d->n, 1)))) {
         tsb_scene_destroy(s);
         return rc;
     }
@@ -368,6 +382,10 @@ int tsb_scene_create(tsb_ctx* ctx, const tsb_scene_desc* d, tsb_scene** out) {
     cudaMemsetAsync(s->v, 0, nel * sizeof(float4), st);
     cudaMemsetAsync(s->densify, 0, sizeof(float) * std::max(d->n, 1), st);
     cudaMemsetAsync(s->stats, 0, sizeof(double) * kStats, st);
+    if (int rc2 = refresh_param_cache(s)) {
+        tsb_scene_destroy(s);
+        return rc2;
+    }
     cudaEventRecord(s->params_ev, st);
     cudaEventRecord(s->grads_ev, st);
     TSB_CUDA(cudaStreamSynchronize(st));
@@ -386,6 +404,7 @@ void tsb_scene_destroy(tsb_scene* s) {
     dev_free(s->densify);
     dev_free(s->stats);
     dev_free(s->staging);
+    dev_free(s->pcache);
     if (s->params_ev) cudaEventDestroy(s->params_ev);
     if (s->grads_ev) cudaEventDestroy(s->grads_ev);
     delete s;
@@ -425,6 +444,7 @@ int unpack_one(tsb_scene* s, const float4* src, float* host, int comps, int comp
 
 }  // namespace
 
+
 int tsb_scene_set_params(tsb_scene* s, int where, const float* position, const float* log_scale,
                          const float* rotation, const float* opacity_logit, const float* reflectivity_dc,
                          const float* motion) {
@@ -443,6 +463,7 @@ int tsb_scene_set_params(tsb_scene* s, int where, const float* position, const f
         for (int k = 0; k < s->d.n_keyframes; ++k)
             if ((rc = pack_one(s, s->params + (size_t)(3 + k) * n, motion + (size_t)k * 3 * n, where, 3, 0)))
                 return rc;
+    if ((rc = refresh_param_cache(s))) return rc;
     TSB_CUDA(cudaEventRecord(s->params_ev, s->ctx->stream));
     return TSB_OK;
 }
@@ -634,6 +655,10 @@ int tsb_scene_adam_step(tsb_scene* s, const tsb_adam_config* cfg) {
     s->ctx->launches++;
     TSB_CHECK_LAUNCH();
     s->densify_count++;
+    {
+        int rc = refresh_param_cache(s);
+        if (rc) return rc;
+    }
     TSB_CUDA(cudaMemsetAsync(s->stats, 0, sizeof(double) * kStats, s->ctx->stream));
     TSB_CUDA(cudaEventRecord(s->params_ev, s->ctx->stream));
     TSB_CUDA(cudaEventRecord(s->grads_ev, s->ctx->stream));
@@ -729,6 +754,7 @@ int ensure_gauss(tsb_pass* p, int n) {
         (rc = dev_alloc(&p->rec.A, cap)) || (rc = dev_alloc(&p->rec.B, cap)) || (rc = dev_alloc(&p->rec.C, cap)) ||
         (rc = dev_alloc(&p->rec.D, cap)) || (rc = dev_alloc(&p->screen, (size_t)8 * cap)))
         return rc;
+    p->rec.rect = p->rect;
     TSB_CUDA(cudaMemsetAsync(p->screen, 0, sizeof(float) * 8 * (size_t)cap, p->stream));
     p->n_cap = cap;
     if ((rc = dev_alloc(&p->sort_scratch, radix_sort_scratch_words(cap))) || (rc = dev_alloc(&p->fx_stamp, cap)) ||
@@ -860,6 +886,8 @@ SceneK scenek(const tsb_scene* s) {
     k.quat = s->params + 2 * n;
     k.motion = s->params + 3 * n;
     k.sh = s->d.sh_degree > 0 ? s->params + (3 + (size_t)s->d.n_keyframes) * n : nullptr;
+    k.cov6 = s->pcache;
+    k.opac = s->pcache + 6 * n;
     return k;
 }
 

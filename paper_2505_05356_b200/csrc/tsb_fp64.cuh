@@ -100,8 +100,11 @@ __device__ __noinline__ double refl_sh_eval(const SceneK& S, int gi, double v0, 
 // view_dir = (x - center) / depth and r_raw = sum_k refl_sh[k] b[k] (splat.cpp:163-165).
 __device__ __forceinline__ double refl_raw64(const SceneK& S, const CamK& C, int gi, const double* x, double depth,
                                              double* view_dir) {
+    if (S.sh_degree == 0) {  // view_dir does not enter (its chain term is multiplied by zero)
+        view_dir[0] = view_dir[1] = view_dir[2] = 0.0;
+        return (double)S.scale_amp[gi].w * 0.28209479177387814;
+    }
     for (int i = 0; i < 3; ++i) view_dir[i] = (x[i] - C.center[i]) / depth;
-    if (S.sh_degree == 0) return (double)S.scale_amp[gi].w * 0.28209479177387814;
     return refl_sh_eval(S, gi, view_dir[0], view_dir[1], view_dir[2]);
 }
 
@@ -168,24 +171,13 @@ __device__ __forceinline__ void quat_rot(const double* q, double* u, double* R) 
     R[6] = 2 * (x * zz - w * y);     R[7] = 2 * (y * zz + w * x);     R[8] = 1 - 2 * (x * x + y * y);
 }
 
-// RenderPassImpl::prepare for one Gaussian (splat.cpp:114-176).  Returns true when
-// the splat survives culling.
-__device__ __forceinline__ bool prep64(const SceneK& S, const CamK& C, const OptK& O,
-                                       const FrameK& F, int gi, Prep64& s) {
-    frame_mean(S, F, gi, s.x);
-    const double* R = C.R;
-    for (int i = 0; i < 3; ++i)
-        s.p[i] = R[i * 3 + 0] * s.x[0] + R[i * 3 + 1] * s.x[1] + R[i * 3 + 2] * s.x[2] + C.t[i];
-    if (s.p[2] < C.near_plane) return false;
-    s.depth = sqrt(s.p[0] * s.p[0] + s.p[1] * s.p[1] + s.p[2] * s.p[2]);
-    const float4 po = S.pos_op[gi];
-    s.opacity = 1.0 / (1.0 + exp(-(double)po.w));
-    if (s.opacity < O.alpha_thr) return false;
+// opacity = sigmoid(logit) (scene.hpp:14-15)
+__device__ __forceinline__ double opacity64(const SceneK& S, int gi) {
+    return 1.0 / (1.0 + exp(-(double)S.pos_op[gi].w));
+}
 
-    const double z = s.p[2];
-    s.mean[0] = C.fx * s.p[0] / z + C.cx;
-    s.mean[1] = C.fy * s.p[1] / z + C.cy;
-
+// cov3d = M3 M3^T, M3 = R(q) diag(exp(log_scale)) (scene.cpp:20-33), row-major 3x3.
+__device__ __forceinline__ void cov3d64(const SceneK& S, int gi, double* cov3d) {
     const float4 qf = S.quat[gi];
     const double q[4] = {(double)qf.x, (double)qf.y, (double)qf.z, (double)qf.w};
     double u[4], Rq[9];
@@ -197,8 +189,37 @@ __device__ __forceinline__ bool prep64(const SceneK& S, const CamK& C, const Opt
         for (int j = 0; j < 3; ++j) M3[r * 3 + j] = Rq[r * 3 + j] * sv[j];
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j)
-            s.cov3d[i * 3 + j] = M3[i * 3 + 0] * M3[j * 3 + 0] + M3[i * 3 + 1] * M3[j * 3 + 1] +
-                                 M3[i * 3 + 2] * M3[j * 3 + 2];
+            cov3d[i * 3 + j] = M3[i * 3 + 0] * M3[j * 3 + 0] + M3[i * 3 + 1] * M3[j * 3 + 1] +
+                               M3[i * 3 + 2] * M3[j * 3 + 2];
+}
+
+// RenderPassImpl::prepare for one Gaussian (splat.cpp:114-176).  Returns true when
+// the splat survives culling.
+__device__ __forceinline__ bool prep64(const SceneK& S, const CamK& C, const OptK& O,
+                                       const FrameK& F, int gi, Prep64& s) {
+    frame_mean(S, F, gi, s.x);
+    const double* R = C.R;
+    for (int i = 0; i < 3; ++i)
+        s.p[i] = R[i * 3 + 0] * s.x[0] + R[i * 3 + 1] * s.x[1] + R[i * 3 + 2] * s.x[2] + C.t[i];
+    if (s.p[2] < C.near_plane) return false;
+    s.depth = sqrt(s.p[0] * s.p[0] + s.p[1] * s.p[1] + s.p[2] * s.p[2]);
+    s.opacity = S.opac ? S.opac[gi] : opacity64(S, gi);
+    if (s.opacity < O.alpha_thr) return false;
+
+    const double z = s.p[2];
+    s.mean[0] = C.fx * s.p[0] / z + C.cx;
+    s.mean[1] = C.fy * s.p[1] / z + C.cy;
+
+    if (S.cov6) {
+        const size_t n = (size_t)S.n;
+        const double c00 = S.cov6[gi], c01 = S.cov6[n + gi], c02 = S.cov6[2 * n + gi];
+        const double c11 = S.cov6[3 * n + gi], c12 = S.cov6[4 * n + gi], c22 = S.cov6[5 * n + gi];
+        s.cov3d[0] = c00; s.cov3d[1] = c01; s.cov3d[2] = c02;
+        s.cov3d[3] = c01; s.cov3d[4] = c11; s.cov3d[5] = c12;
+        s.cov3d[6] = c02; s.cov3d[7] = c12; s.cov3d[8] = c22;
+    } else {
+        cov3d64(S, gi, s.cov3d);
+    }
     const double rx = s.p[0] / z, ry = s.p[1] / z;
     s.clx = rx < -C.lim_x || rx > C.lim_x;
     s.cly = ry < -C.lim_y || ry > C.lim_y;

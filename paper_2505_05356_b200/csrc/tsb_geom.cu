@@ -13,6 +13,17 @@ namespace tsb {
 // the fp32 raster record (indexed by Gaussian; the duplicate kernel gathers it
 // into rank order).
 // ---------------------------------------------------------------------------
+// sin/cos of the ToF phase for the fp32 record: exact fp64 reduction modulo 2 pi
+// (phases here are < ~1e3 rad), then fp32 sincosf of the reduced angle -- within
+// 2 ulp of the fp64 result rounded to fp32, for a fraction of the fp64 cost.
+__device__ __forceinline__ void sincos_phase32(double psi, float& sn, float& cs) {
+    constexpr double kTwoPiHi = 6.283185307179586232;     // 2 pi rounded to double
+    constexpr double kTwoPiLo = 2.4492935982947064e-16;   // 2 pi - kTwoPiHi
+    const double k = rint(psi * 0.15915494309189535);
+    const double r = fma(-k, kTwoPiLo, fma(-k, kTwoPiHi, psi));
+    sincosf((float)r, &sn, &cs);
+}
+
 __global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd,
                                                     uint32_t* __restrict__ depth_key,
                                                     double* __restrict__ depth64,
@@ -48,12 +59,12 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, co
             rec.A[gi] = make_float4((float)s.x0, (float)s.y0, (float)(s.mean[0] - (double)s.x0),
                                     (float)(s.mean[1] - (double)s.y0));
             rec.B[gi] = make_float4((float)l11, (float)l12, (float)l22, (float)s.opacity);
-            double sn, cs;
-            sincos(phase_of_depth(s.depth, S.freq[0], S.c), &sn, &cs);
-            rec.C[gi] = make_float4((float)s.coef, (float)s.depth, (float)sn, (float)cs);
+            float sn, cs;
+            sincos_phase32(phase_of_depth(s.depth, S.freq[0], S.c), sn, cs);
+            rec.C[gi] = make_float4((float)s.coef, (float)s.depth, sn, cs);
             if (S.nf > 1) {
-                sincos(phase_of_depth(s.depth, S.freq[1], S.c), &sn, &cs);
-                rec.D[gi] = make_float4((float)sn, (float)cs, 0.f, 0.f);
+                sincos_phase32(phase_of_depth(s.depth, S.freq[1], S.c), sn, cs);
+                rec.D[gi] = make_float4(sn, cs, 0.f, 0.f);
             }
         } else {
             depth_key[gi] = 0xffffffffu;
@@ -85,6 +96,30 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, co
             atomicMax(&key_range[1], hi);
         }
     }
+}
+
+// Time-independent per-Gaussian cache (SceneK::cov6 / opac), after every parameter change.
+__global__ void __launch_bounds__(256) k_param_cache(SceneK S, double* __restrict__ cov6, double* __restrict__ opac) {
+    const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gi >= S.n) return;
+    double c[9];
+    cov3d64(S, gi, c);
+    const size_t n = (size_t)S.n;
+    cov6[gi] = c[0];
+    cov6[n + gi] = c[1];
+    cov6[2 * n + gi] = c[2];
+    cov6[3 * n + gi] = c[4];
+    cov6[4 * n + gi] = c[5];
+    cov6[5 * n + gi] = c[8];
+    opac[gi] = opacity64(S, gi);
+}
+
+void launch_param_cache(const SceneK& S, double* cov6, double* opac, cudaStream_t st) {
+    if (S.n <= 0) return;
+    SceneK raw = S;
+    raw.cov6 = nullptr;
+    raw.opac = nullptr;
+    k_param_cache<<<(S.n + 255) / 256, 256, 0, st>>>(raw, cov6, opac);
 }
 
 void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* F,

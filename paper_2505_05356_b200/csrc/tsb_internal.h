@@ -44,6 +44,12 @@ struct SceneK {
     const float4* quat;       // w, x, y, z
     const float4* motion;     // [nk][n] keyframe offsets (xyz, 0)
     const float4* sh;         // [4][n] reflectivity SH coefficients 1..15 (+pad); null when sh_degree == 0
+    // Time-independent per-Gaussian cache, refreshed whenever the parameters change
+    // (tsb_scene_set_params, Adam): cov3d = M3 M3^T (6 planes xx, xy, xz, yy, yz, zz)
+    // and opacity = sigmoid(logit), computed by the same fp64 code prep64 used inline,
+    // so every frame of a sweep reads them instead of recomputing.  Null: inline.
+    const double* cov6;
+    const double* opac;
 };
 
 struct FrameK {
@@ -68,6 +74,7 @@ struct RecK {
     float4* B;  // l11, l12, l22, opacity
     float4* C;  // coef, depth, sin(psi_0), cos(psi_0)
     float4* D;  // sin(psi_1), cos(psi_1), 0, 0   (second frequency only)
+    const uint2* rect;  // alias of the pass's tile rects: (x0 | x1 << 16, y0 | y1 << 16)
 };
 
 // Depth-chunked binning (tsb_bin.cu).  Ranks are cut into segments of kSeg
@@ -187,6 +194,7 @@ void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameDev*
                   const PixK& px, int nf, cudaStream_t st);
 void launch_chain(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
                   const uint32_t* touched, float* screen, float4* grads, cudaStream_t st);
+void launch_param_cache(const SceneK& S, double* cov6, double* opac, cudaStream_t st);
 // tsb_bin.cu
 // tsb_sort.cu: hand-written onesweep LSD radix sort of 32-bit keys + values (4 passes);
 // the result is back in (keys_a, vals_a).  Returns the number of kernels launched.

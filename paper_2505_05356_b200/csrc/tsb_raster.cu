@@ -25,6 +25,12 @@ namespace tsb {
 
 constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // -0.5 * log2(e)
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -204,8 +210,8 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
                     const float om = 1.f - ev.alpha;
                     T = T * om;
                     // relative error of (1 - alpha) from alpha's error, plus the product rounding
-                    errT += (4.f * kEps + kEx2Err + 2.f * kEps * ev.maha) * __fdividef(ev.alpha, om) + 2.f * kEps;
-                    if (T < fl * (1.f + 2.f * errT) && T > fl * (1.f - 2.f * errT)) flag |= 4;
+                    errT += (4.f * kEps + kEx2Err + 2.f * kEps * ev.maha) * (ev.alpha * rcp_approx(om)) + 2.f * kEps;
+                    if (fabsf(T - fl) < 2.f * fl * errT) flag |= 4;
                     const int gidx_e = (int)(rg.z + (b - rg.x) + j + 1);
                     if (T == 0.f && last_eff < 0) last_eff = gidx_e;
                     if (T < fl) {
