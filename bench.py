@@ -155,45 +155,72 @@ class StreamTimer:
 
 
 # ---------------------------------------------------------------------------
-# algorithmic bytes per launch
-def stage_bytes(stage, n, k, v, ntiles, n_keyframes, npx, nf=1):
-    params = 16 * (3 + min(n_keyframes, 2))  # float4 arrays read by preprocess (pos_op, scale_amp, quat, 2 keys)
-    if stage == "preprocess":
-        return n * (params + 8 + 4 + 4 + 8) + v * (16 * (3 + (nf > 1)))
-    if stage == "depth_sort":  # onesweep, 32-bit keys + values: hist 4 B + 4 passes x (r+w 16 B) + tie scan 4 B
-        return n * (4 + 4 * 16 + 4)
-    if stage == "scan":
-        return n * (4 + 4 + 4 + 4)
-    if stage == "binning":  # count + emit each read (gidx 4 B + rect 8 B) per visible rank; 4 B per list entry
-        return v * 24 + k * 4
-    return None
+# Roofline accounting.  Per-kernel device times come from CUDA
+# events the library records on the pass stream around each stage (profiling
+# mode: the same kernels, issued eagerly), over the same c3 frames.
+#   k_preprocess (HBM): per Gaussian 120 B read (pos_op 16, 2 keyframe offsets 32,
+#     cov3d cache 48, opacity cache 8, scale_amp 16) + 12 B written (index, fp32 key,
+#     tiles touched); per visible Gaussian 64 B written (fp64 depth 8, rect 8, record 48).
+#   k_raster_fwd (FP32): 9 FLOP per (pixel, entry) evaluation (dx, dy, p, q, maha,
+#     threshold) + 14 FLOP per contributing evaluation (alpha, w, w2, quad pair, SW, SD,
+#     T) -- counted live by the kernel in profiling mode.
+def fp32_peak_tflops(sm_mhz):
+    return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
 
 
-def pick_roofline(st, shapes, peaks):
-    # dominant stage by measured time among the HBM-bound stages with byte accounting
-    total = sum(ms for ms, _ in st.values())
-    best = None
-    for name, (ms, calls) in st.items():
-        if calls == 0 or ms <= 0:
-            continue
-        if best is None or ms > st[best][0]:
-            best = name
-    out = {"dominant_stage": best, "stage_ms_per_step": {k: round(v[0], 4) for k, v in st.items() if v[1]}}
-    hbm_best = None
-    for name, (ms, calls) in st.items():
-        if calls and stage_bytes(name, **shapes) is not None and (hbm_best is None or ms > st[hbm_best][0]):
-            hbm_best = name
-    if hbm_best is None:
-        return out
-    ms, calls = st[hbm_best]
-    per_launch_ms = ms / calls
-    bytes_ = stage_bytes(hbm_best, **shapes)
-    achieved = bytes_ / (per_launch_ms * 1e-3) / 1e9
-    out.update({"bound": "hbm", "kernel": hbm_best, "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
-                "algorithmic_bytes_per_launch": int(bytes_), "avg_launch_ms": round(per_launch_ms, 5),
-                "share_of_step": round(ms / total, 4) if total else None, "peak_source": peaks["source"]})
-    return out
+def load_traffic():
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            return {}
+    return {}
+
+
+def rooflines(stage_ms, shapes, evals, contribs, peaks, sm_max_mhz):
+    """stage_ms: {stage: (ms per step, launches per step)}; returns (dominant, all)."""
+    traffic = load_traffic()
+    out = {}
+    ms, calls = stage_ms.get("preprocess", (0.0, 0))
+    if calls:
+        per = ms / calls
+        b = shapes["n"] * 132 + shapes["v"] * 64
+        ach = b / (per * 1e-3) / 1e9
+        t = traffic.get("k_preprocess")
+        out["k_preprocess"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                               "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": t,
+                               "algorithmic_bytes_per_launch": int(b), "avg_launch_ms": round(per, 5),
+                               "peak_source": peaks["source"]}
+    ms, calls = stage_ms.get("raster_fwd", (0.0, 0))
+    if calls and evals:
+        frames = shapes["frames"]
+        per_frame_ms = ms / frames
+        flop = (9 * evals + 14 * contribs) / frames
+        ach = flop / (per_frame_ms * 1e-3) / 1e12
+        pk = fp32_peak_tflops(sm_max_mhz or 1965)
+        t = traffic.get("k_raster_fwd")
+        out["k_raster_fwd"] = {"bound": "fp32", "achieved": round(ach, 2), "peak": round(pk, 1), "unit": "TFLOP/s",
+                               "frac": round(ach / pk, 4), "traffic": t,
+                               "algorithmic_flop_per_frame": int(flop), "evaluations_per_frame": evals // frames,
+                               "contributions_per_frame": contribs // frames,
+                               "avg_ms_per_frame": round(per_frame_ms, 5),
+                               "launches_per_frame": round(calls / frames, 2),
+                               "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x max SM clock",
+                               "issue_slots_busy_ncu": t and t.get("issue_active")}
+    total = sum(v[0] for v in stage_ms.values())
+    share = {k: round(v[0] / total, 4) for k, v in stage_ms.items() if v[1] and total}
+    dom = None
+    for k, st in (("k_preprocess", "preprocess"), ("k_raster_fwd", "raster_fwd")):
+        if k in out:
+            out[k]["share_of_step"] = share.get(st)
+            if dom is None or (share.get(st) or 0) > (out[dom]["share_of_step"] or 0):
+                dom = k
+    res = dict(out[dom]) if dom else {}
+    if dom:
+        res["kernel"] = dom
+    res["stage_share_of_step"] = share
+    return res, out
 
 
 # ---------------------------------------------------------------------------
@@ -233,12 +260,15 @@ def bench_c3(args, dist, tsb, synthetic):
     redos = ctx.redo_count()
     # per-stage device times (roofline): same frames, one pass, stage events on its stream
     ctx.stage_times()
+    ctx.raster_counts()
     ctx.set_profiling(True)
-    for _ in range(args.steps):
+    prof_steps = 1
+    for _ in range(prof_steps):
         step([rp])
     ctx.synchronize()
     ctx.set_profiling(False)
     st = ctx.stage_times()
+    evals, contribs = ctx.raster_counts()
     v, k = rp.visible_count(), rp.num_keys()
     fixups = rp.debug_fixups()
     ms_max = dist.max(ms)
@@ -286,13 +316,15 @@ def bench_c3(args, dist, tsb, synthetic):
            "timer": "host wall clock; scene H2D from pinned memory, every frame's quad/depth/weight D2H into pinned "
                     "per-pass buffers (tsb_pass_download_async), all landed before the clock stops"}
 
-    shapes = dict(n=g.n, k=k, v=v, ntiles=((W + 15) // 16) * ((H + 15) // 16), n_keyframes=g.n_keyframes,
-                  npx=H * W)
-    stage_ms = {name: (t / args.steps, c // args.steps) for name, (t, c) in st.items()}
-    roof = pick_roofline(stage_ms, shapes, load_peaks())
+    shapes = dict(n=g.n, v=v, frames=len(my_frames) * prof_steps)
+    stage_ms = {name: (t / prof_steps, c // prof_steps) for name, (t, c) in st.items() if c}
+    roof, roofs = rooflines(stage_ms, shapes, evals, contribs, load_peaks(), clk.summary()["sm_max_mhz"])
+    roof["stage_ms_per_step"] = {k_: round(t_, 3) for k_, (t_, _) in stage_ms.items()}
     info = {"visible": v, "keys_per_frame": k, "fixup_pixels_last_frame": fixups, "clock": clk.summary(),
             "launches": launches, "passes_in_flight": len(passes), "redone_frames": redos,
-            "stage_timing": "separate single-pass loop after the timed region (events on the pass stream)"}
+            "stage_timing": "one more step on a single pass after the timed region, profiling mode (kernels "
+                            "issued eagerly, events on the pass stream around each stage)"}
+    info["rooflines"] = roofs
     return value, ms_max / args.steps, e2e, roof, info, ctx
 
 
@@ -424,8 +456,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-train", action="store_true")
-    ap.add_argument("--passes", type=int, default=6, help="render passes (streams) in flight")
-    ap.add_argument("--train-passes", type=int, default=3)
+    ap.add_argument("--passes", type=int, default=8, help="render passes (streams) in flight")
+    ap.add_argument("--train-passes", type=int, default=4)
     ap.add_argument("--train-steps", type=int, default=3)
     ap.add_argument("--train-n", type=int, default=None)
     ap.add_argument("--cpu-frames", type=int, default=2)

@@ -136,10 +136,15 @@ enum {
     TSB_STAGE_PREPROCESS = 0, TSB_STAGE_DEPTH_SORT = 1, TSB_STAGE_SCAN = 2, TSB_STAGE_BINNING = 3,
     TSB_STAGE_TILE_SORT = 4, TSB_STAGE_RANGES = 5, TSB_STAGE_RASTER_FWD = 6, TSB_STAGE_FIXUP = 7,
     TSB_STAGE_LOSS = 8, TSB_STAGE_RASTER_BWD = 9, TSB_STAGE_CHAIN = 10, TSB_STAGE_ADAM = 11,
-    TSB_STAGE_ALLREDUCE = 12, TSB_NUM_STAGES = 13
+    TSB_STAGE_ALLREDUCE = 12, TSB_STAGE_BIN_COUNT = 13, TSB_STAGE_BIN_EMIT = 14, TSB_NUM_STAGES = 15
 };
+/* Profiling mode also runs the forward eagerly (no CUDA graph) so each stage's
+ * kernels are bracketed by events, and counts the raster's per-pixel work. */
 int tsb_ctx_set_profiling(tsb_ctx* ctx, int enabled);
 int tsb_ctx_stage_times(tsb_ctx* ctx, double* ms /* TSB_NUM_STAGES */, int64_t* calls /* TSB_NUM_STAGES */);
+/* Forward-raster work since the last call (profiling mode only; resets):
+ * (pixel, list entry) evaluations and contributing evaluations (alpha >= threshold). */
+int tsb_ctx_raster_counts(tsb_ctx* ctx, int64_t* evaluations, int64_t* contributions);
 
 /* ---- scene: parameters, gradients, Adam state (trainer.cpp:63-132) ------- */
 int tsb_scene_create(tsb_ctx* ctx, const tsb_scene_desc* desc, tsb_scene** out);

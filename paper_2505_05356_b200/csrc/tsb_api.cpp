@@ -77,6 +77,7 @@ struct tsb_ctx {
     std::vector<std::pair<int, size_t>> ev_marks;  // (stage, index of start event)
     std::vector<tsb_pass*> passes;                 // joined by tsb_ctx_join
     int64_t redos = 0;                             // frames redone after a device-side abort
+    unsigned long long* work = nullptr;            // raster work counters (profiling)
     bool use_graphs = true;                        // forward as a CUDA graph (TSB_NO_GRAPHS=1 disables)
 };
 
@@ -252,6 +253,8 @@ int tsb_ctx_create(int device, tsb_ctx** out) {
         return fail(TSB_ERR_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
     }
     e = cudaMallocHost(&c->pinned, 4096);
+    if (e == cudaSuccess) e = cudaMalloc(&c->work, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(c->work, 0, 2 * sizeof(unsigned long long));
     if (e != cudaSuccess) {
         cudaStreamDestroy(c->stream);
         delete c;
@@ -291,8 +294,21 @@ void tsb_ctx_destroy(tsb_ctx* c) {
     cudaStreamSynchronize(c->stream);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     cudaFreeHost(c->pinned);
+    if (c->work) cudaFree(c->work);
     cudaStreamDestroy(c->stream);
     delete c;
+}
+
+int tsb_ctx_raster_counts(tsb_ctx* c, int64_t* evaluations, int64_t* contributions) {
+    if (!c) return fail(TSB_ERR_INVALID, "null context");
+    int rc = tsb_ctx_synchronize(c);
+    if (rc) return rc;
+    unsigned long long h[2];
+    TSB_CUDA(cudaMemcpy(h, c->work, sizeof h, cudaMemcpyDeviceToHost));
+    TSB_CUDA(cudaMemset(c->work, 0, sizeof h));
+    if (evaluations) *evaluations = (int64_t)h[0];
+    if (contributions) *contributions = (int64_t)h[1];
+    return TSB_OK;
 }
 
 namespace {
@@ -1153,6 +1169,7 @@ int record_forward(tsb_pass* p, cudaStream_t st, bool loss, const ChW& chw, bool
         ck.tile_blocks_done = p->tile_blocks_done;
         ck.blocks_done_total = p->counters + 3;
         ck.overflow = p->counters + 2;
+        ck.work = p->ctx->profiling ? p->ctx->work : nullptr;
         cudaStream_t cs = st;
         if (graph && c > 0) {
             // gate kernel, then an IF node whose body is captured on the pass's capture stream
@@ -1180,8 +1197,18 @@ int record_forward(tsb_pass* p, cudaStream_t st, bool loss, const ChW& chw, bool
             cs = p->cap_stream;
         }
         if (nseg > 0) {
-            Stage sg(p->ctx, TSB_STAGE_BINNING, cs);
-            launch_bin_chunk(B, cs);
+            {
+                Stage sg(p->ctx, TSB_STAGE_BIN_COUNT, cs);
+                launch_bin_count(B, cs);
+            }
+            {
+                Stage sg(p->ctx, TSB_STAGE_BINNING, cs);
+                launch_bin_scan(B, cs);
+            }
+            {
+                Stage sg(p->ctx, TSB_STAGE_BIN_EMIT, cs);
+                launch_bin_emit(B, cs);
+            }
         } else {
             TSB_CUDA(cudaMemsetAsync(B.ranges, 0, sizeof(uint4) * p->ntiles, cs));
         }

@@ -659,30 +659,49 @@ void bin_init() {
     }
 }
 
-void launch_bin_chunk(const BinK& B, cudaStream_t st) {
-    const size_t seg_fixed = sizeof(uint32_t) * ((size_t)((B.ntiles + 31) >> 5) +
-                                                 (size_t)kSegBatches * (B.tiles_x + B.tiles_y) + kSeg);
-    const int cap = B.ntiles <= 2048 ? 6144 : 16384;
-    const size_t seg_emit = seg_fixed + sizeof(uint32_t) * (size_t)B.ntiles + 3 * (size_t)cap + 16;
-    if (seg_emit <= 200 * 1024 && B.ntiles <= 65535) {
-        k_bin_count_seg<<<std::min(B.nseg, 148 * 12), kSegThreads, seg_fixed, st>>>(B);
-        k_bin_scan_segments<<<(B.ntiles + 31) / 32, 1024, 0, st>>>(B);
-        k_bin_scan_tiles<<<1, 1024, 0, st>>>(B);
-        k_bin_emit_seg<<<std::min(B.nseg, 148 * 8), kSegThreads, seg_emit, st>>>(B, cap);
-        return;
+namespace {
+struct BinPlan {
+    bool seg;            // segment kernels (else batch-walk kernels with global cursors)
+    size_t seg_fixed, seg_emit, base, cnt_smem;
+    bool cnt_sm;
+    int cap;
+};
+BinPlan bin_plan(const BinK& B) {
+    BinPlan P;
+    P.seg_fixed = sizeof(uint32_t) * ((size_t)((B.ntiles + 31) >> 5) + (size_t)kSegBatches * (B.tiles_x + B.tiles_y) +
+                                      kSeg);
+    P.cap = B.ntiles <= 2048 ? 6144 : 16384;
+    P.seg_emit = P.seg_fixed + sizeof(uint32_t) * (size_t)B.ntiles + 3 * (size_t)P.cap + 16;
+    P.seg = P.seg_emit <= 200 * 1024 && B.ntiles <= 65535;
+    P.base = sizeof(uint32_t) * (size_t)((B.ntiles + 31) / 32 + 32 + B.tiles_x + B.tiles_y);
+    P.cnt_sm = B.ntiles <= kSmemTiles;
+    P.cnt_smem = P.base + (P.cnt_sm ? sizeof(uint32_t) * (size_t)B.ntiles : 0);
+    return P;
+}
+}  // namespace
+
+void launch_bin_count(const BinK& B, cudaStream_t st) {
+    const BinPlan P = bin_plan(B);
+    if (P.seg) {
+        k_bin_count_seg<<<std::min(B.nseg, 148 * 12), kSegThreads, P.seg_fixed, st>>>(B);
+    } else if (P.cnt_sm) {
+        k_bin_count<true><<<std::min(B.nseg, 148 * 8), kBinThreads, P.cnt_smem, st>>>(B);
+    } else {
+        k_bin_count<false><<<std::min(B.nseg, 148 * 8), kBinThreads, P.cnt_smem, st>>>(B);
     }
-    // very large tile grids: batch-walk kernels with global cursors
-    const size_t base = sizeof(uint32_t) * (size_t)((B.ntiles + 31) / 32 + 32 + B.tiles_x + B.tiles_y);
-    const bool cnt_sm = B.ntiles <= kSmemTiles;
-    const size_t cnt_smem = base + (cnt_sm ? sizeof(uint32_t) * (size_t)B.ntiles : 0);
-    const int grid = std::min(B.nseg, 148 * 8);
-    if (cnt_sm)
-        k_bin_count<true><<<grid, kBinThreads, cnt_smem, st>>>(B);
-    else
-        k_bin_count<false><<<grid, kBinThreads, cnt_smem, st>>>(B);
+}
+
+void launch_bin_scan(const BinK& B, cudaStream_t st) {
     k_bin_scan_segments<<<(B.ntiles + 31) / 32, 1024, 0, st>>>(B);
     k_bin_scan_tiles<<<1, 1024, 0, st>>>(B);
-    k_bin_emit<false><<<grid, kBinThreads, base, st>>>(B, 0);
+}
+
+void launch_bin_emit(const BinK& B, cudaStream_t st) {
+    const BinPlan P = bin_plan(B);
+    if (P.seg)
+        k_bin_emit_seg<<<std::min(B.nseg, 148 * 8), kSegThreads, P.seg_emit, st>>>(B, P.cap);
+    else  // very large tile grids: batch walk with global cursors (hist row, in place)
+        k_bin_emit<false><<<std::min(B.nseg, 148 * 8), kBinThreads, P.base, st>>>(B, 0);
 }
 
 }  // namespace tsb

@@ -120,6 +120,7 @@ struct ChunkK {
     int32_t* tile_blocks_done;  // per tile
     int32_t* blocks_done_total;
     const int32_t* overflow;    // list storage overflowed: the host re-runs the frame
+    unsigned long long* work;   // profiling: [0] evaluations, [1] contributions (null: not counted)
 };
 
 // Per-pixel raster state written by the forward pass for the backward pass.
@@ -214,7 +215,10 @@ int launch_sort_depth(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint
 int launch_sort_depth64(const double* depth64, const uint32_t* touched, uint32_t* keys_a, uint32_t* keys_b,
                         uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch, cudaStream_t st);
 void bin_init();  // kernel attributes; call before any capture
-void launch_bin_chunk(const BinK& B, cudaStream_t st);
+// one depth chunk: per-(segment, tile) counts, scans (ranges), list emission
+void launch_bin_count(const BinK& B, cudaStream_t st);
+void launch_bin_scan(const BinK& B, cudaStream_t st);
+void launch_bin_emit(const BinK& B, cudaStream_t st);
 // tsb_raster.cu
 void launch_raster_fwd(const RecK& rec, const ChunkK& ck, const uint32_t* tile_vals, const OptK& O,
                        int W, int H, int nf, PixK px, FwdState fs, const FrameDev* fd, bool loss, const ChW& ch_w,

@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
     float accS[NF], accC[NF];
 #pragma unroll
     for (int f = 0; f < NF; ++f) accS[f] = accC[f] = 0.f;
+    uint32_t n_eval = 0, nc0 = 0;  // profiling work counters
     float dref = 0.f;  // distortion: fp64 moments about the first contributor's depth
     double SDs = 0.0, SD2s = 0.0;
     int nc = 0, flags = 0, last_eff = -1;
@@ -149,6 +150,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
     }
     const bool was_done = !active || (flags & 1);
     bool done = was_done;
+    nc0 = (uint32_t)nc;
     int flag = (flags >> 1) & 7;  // reasons: 1 maha band, 2 alpha band, 4 T band
     int processed = (int)(rg.z + rg.y);
     const float cut2 = O.cut2_f, thr = O.alpha_thr_f, fl = O.floor_f;
@@ -169,6 +171,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
             if (!done) {
                 const int nb = min((uint32_t)kRasterThreads, end - b);
                 for (int j = 0; j < nb; ++j) {
+                    if (ck.work) ++n_eval;
                     const float4 A = sm.A[j], B = sm.B[j];
                     Eval ev;
                     eval_entry(A, B, pcx, pcy, ev);
@@ -294,6 +297,17 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
         fs.i[2 * (size_t)fs.npx + o] = last_eff;
     }
     const bool block_finished = __syncthreads_count(done || is_last) == kRasterThreads;
+    if (ck.work) {
+        unsigned long long ev = n_eval, cn = (uint32_t)nc - nc0;
+        for (int m = 16; m > 0; m >>= 1) {
+            ev += __shfl_xor_sync(0xffffffffu, ev, m);
+            cn += __shfl_xor_sync(0xffffffffu, cn, m);
+        }
+        if ((tid & 31) == 0) {
+            atomicAdd(&ck.work[0], ev);
+            atomicAdd(&ck.work[1], cn);
+        }
+    }
     if (target) {
         for (int m = 16; m > 0; m >>= 1) lpx += __shfl_xor_sync(0xffffffffu, lpx, m);
         if ((tid & 31) == 0) red[tid >> 5] = lpx;

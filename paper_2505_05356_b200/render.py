@@ -182,6 +182,12 @@ class Context:
     def set_profiling(self, on: bool):
         check(lib().tsb_ctx_set_profiling(self._h, 1 if on else 0))
 
+    def raster_counts(self):
+        """(evaluations, contributions) of the forward raster since the last call (profiling mode)."""
+        e, c = C.c_int64(), C.c_int64()
+        check(lib().tsb_ctx_raster_counts(self._h, C.byref(e), C.byref(c)))
+        return e.value, c.value
+
     def stage_times(self):
         """{stage: (ms_total, calls)} since the last call (synchronises)."""
         ms = (C.c_double * len(_abi.STAGES))()
