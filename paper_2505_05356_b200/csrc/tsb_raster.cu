@@ -519,7 +519,10 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
                 if (NF > 1) sm.D[tid] = rec.D[r];
             }
             __syncthreads();
-            for (int j = nb - 1; j >= 0; --j) {
+            // entries at or past this warp's furthest termination point cannot contribute
+            // to any of its pixels: start the warp below them (warp-uniform)
+            const int jtop = min(nb, wmax - ((int)rg.z + bi * kRasterThreads));
+            for (int j = jtop - 1; j >= 0; --j) {
                 const int el = (int)rg.z + bi * kRasterThreads + j;
                 bool contrib = false;
                 float g8[8];
