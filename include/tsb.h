@@ -278,6 +278,52 @@ void tsb_comm_destroy(tsb_comm* c);
 /* In-place sum of the scene's gradient buffer (+ bg grads + loss) across ranks. */
 int tsb_scene_allreduce_grads(tsb_scene* s, tsb_comm* c);
 
+/* ---- DeformNet on the tensor cores (deform.hpp:19-66, deform.cpp) -----
+ * MLP (canonical position, time) -> position offset: positional encodings
+ * (deform.cpp:10-26), `hidden_layers` ReLU layers of `width` units, a linear
+ * 3-output layer.  Every layer is a tcgen05 GEMM (kind::tf32 with a 3xTF32 split,
+ * fp32 accumulation in tensor memory).  Parameters are flat in the reference's
+ * get_parameters order (per layer: W row-major, then b).  Limits: width <= 128,
+ * input_dim = 3(1 + 2 l_x) + 1 + 2 l_t <= 128 (the reference's default 4 x 128, l = 10).
+ * Each of TSB_DEFORM_SLOTS caches one forward (DeformNet::Cache) for its backward. */
+#define TSB_DEFORM_SLOTS 4
+typedef struct {
+    int32_t hidden_layers, width, l_x, l_t;
+    double coord_scale;
+} tsb_deform_config;
+typedef struct tsb_deform tsb_deform;
+int tsb_deform_create(tsb_ctx* ctx, const tsb_deform_config* cfg, tsb_deform** out);
+void tsb_deform_destroy(tsb_deform* net);
+int64_t tsb_deform_param_count(const tsb_deform* net);
+int tsb_deform_set_params(tsb_deform* net, int where, const float* flat);   /* DeformNet::set_parameters */
+int tsb_deform_get_params(tsb_deform* net, float* host_flat);               /* DeformNet::get_parameters */
+int tsb_deform_get_grads(tsb_deform* net, float* host_flat);                /* Grads::add_flat_to order */
+int tsb_deform_zero_grads(tsb_deform* net);
+/* DeformNet::offsets (deform.cpp:80-102): positions / offsets are n x 3 row-major
+ * (the columns of a Matrix3Xd), host or device memory. */
+int tsb_deform_offsets(tsb_deform* net, int slot, int where, const float* positions, int64_t n, double t,
+                       float* offsets);
+/* DeformNet::backward (deform.cpp:124-159) for the slot's cached forward: accumulates
+ * dW / db; d_positions (n x 3, nullable) receives the input-position gradient. */
+int tsb_deform_backward(tsb_deform* net, int slot, int where, const float* d_offsets, float* d_positions);
+/* Scene coupling (trainer.cpp:262-271, 325-335): offsets of the scene's canonical
+ * positions at time t become keyframe `keyframe`'s offsets; the backward consumes that
+ * keyframe's accumulated gradient and adds d(offsets)/d(position) to the position grads. */
+int tsb_deform_scene_offsets(tsb_deform* net, int slot, tsb_scene* scene, int keyframe, double t);
+int tsb_deform_scene_backward(tsb_deform* net, int slot, tsb_scene* scene, int keyframe);
+/* Test hook: the slot's cached post-ReLU activations of hidden layer `layer` (n x width). */
+int tsb_deform_debug_activation(tsb_deform* net, int slot, int layer, float* host_out);
+/* AdamState::step on the network parameters (trainer.cpp:18-31, 367-378). */
+int tsb_deform_adam_step(tsb_deform* net, double lr, double beta1, double beta2, double eps);
+
+/* Test hook for the DeformNet GEMM (tsb_mlp.cu): C[m][n] = act(sum_k A(m,k) B(n,k) + bias[n])
+ * on the tcgen05 tensor cores (3xTF32), host buffers, A(m,k) = A[m*a_m + k*a_k],
+ * B(n,k) = B[n*b_n + k*b_k], N <= 128, split over `slices` K ranges then reduced.
+ * mask (nullable, M x N row-major): C *= (mask > 0). */
+int tsb_debug_gemm(tsb_ctx* ctx, int M, int N, int K, int slices, const float* A, int64_t a_m, int64_t a_k,
+                   const float* B, int64_t b_n, int64_t b_k, const float* bias, int relu, const float* mask,
+                   float* C);
+
 /* ---- small host helpers mirroring the Python _core surface --------------- */
 /* unambiguous_range (tof.hpp:36-38), quad_to_depth (tof.hpp:59-65),
  * quad_basis (tof.hpp:75-79); frequency <= 0 uses the default sensor. */

@@ -9,8 +9,8 @@ from ._abi import TsbError, lib as _load_lib
 
 _load_lib()
 
-from .render import (AdamParams, CameraModel, Comm, Context, GaussianScene, LrTable, RenderOptions,  # noqa: E402
+from .render import (AdamParams, CameraModel, Comm, Context, DeformNet, GaussianScene, LrTable, RenderOptions,  # noqa: E402
                      RenderPass, ToFConfig, frame_for_time, quad_basis, quad_to_depth, unambiguous_range)
 
-__all__ = ["AdamParams", "CameraModel", "Comm", "Context", "GaussianScene", "LrTable", "RenderOptions", "RenderPass",
+__all__ = ["AdamParams", "CameraModel", "Comm", "Context", "DeformNet", "GaussianScene", "LrTable", "RenderOptions", "RenderPass",
            "ToFConfig", "TsbError", "frame_for_time", "quad_basis", "quad_to_depth", "unambiguous_range"]

@@ -68,6 +68,11 @@ _ip = C.POINTER(C.c_int32)
 _lp = C.POINTER(C.c_int64)
 _vp = C.c_void_p
 
+
+class DeformConfigC(C.Structure):
+    _fields_ = [("hidden_layers", C.c_int32), ("width", C.c_int32), ("l_x", C.c_int32), ("l_t", C.c_int32),
+                ("coord_scale", C.c_double)]
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "tsb_last_error": (C.c_char_p, []),
@@ -112,6 +117,21 @@ SIGNATURES = {
     "tsb_pass_backward_buffers": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]),
     "tsb_pass_debug_keep_screen": (C.c_int, [_vp, C.c_int]),
     "tsb_pass_debug_set_list_capacity": (C.c_int, [_vp, C.c_uint32]),
+    "tsb_deform_create": (C.c_int, [_vp, _vp, C.POINTER(_vp)]),
+    "tsb_deform_destroy": (None, [_vp]),
+    "tsb_deform_param_count": (C.c_int64, [_vp]),
+    "tsb_deform_set_params": (C.c_int, [_vp, C.c_int, _vp]),
+    "tsb_deform_get_params": (C.c_int, [_vp, _vp]),
+    "tsb_deform_get_grads": (C.c_int, [_vp, _vp]),
+    "tsb_deform_zero_grads": (C.c_int, [_vp]),
+    "tsb_deform_offsets": (C.c_int, [_vp, C.c_int, C.c_int, _vp, C.c_int64, C.c_double, _vp]),
+    "tsb_deform_backward": (C.c_int, [_vp, C.c_int, C.c_int, _vp, _vp]),
+    "tsb_deform_scene_offsets": (C.c_int, [_vp, C.c_int, _vp, C.c_int, C.c_double]),
+    "tsb_deform_scene_backward": (C.c_int, [_vp, C.c_int, _vp, C.c_int]),
+    "tsb_deform_debug_activation": (C.c_int, [_vp, C.c_int, C.c_int, _vp]),
+    "tsb_deform_adam_step": (C.c_int, [_vp, C.c_double, C.c_double, C.c_double, C.c_double]),
+    "tsb_debug_gemm": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_int64, C.c_int64, _vp, C.c_int64,
+                                C.c_int64, _vp, C.c_int, _vp, _vp]),
     "tsb_pass_debug_prepared": (C.c_int, [_vp, _ip, _ip]),
     "tsb_pass_debug_tiles": (C.c_int, [_vp, _ip, _ip, _lp, _ip]),
     "tsb_pass_debug_records": (C.c_int, [_vp, _fp]),

@@ -1900,6 +1900,414 @@ int tsb_scene_allreduce_grads(tsb_scene* s, tsb_comm* c) {
 }
 
 // ---------------------------------------------------------------------------
+// DeformNet (tsb_mlp.cu)
+// ---------------------------------------------------------------------------
+struct tsb_deform {
+    tsb_ctx* ctx = nullptr;
+    tsb_deform_config cfg{};
+    int din = 0, L = 0, width = 0;  // input dim, hidden layers, units
+    std::vector<int> rows, cols;    // per layer: W is rows x cols
+    std::vector<int64_t> w_off, b_off;
+    int64_t P = 0;
+    float *params = nullptr, *grads = nullptr, *m = nullptr, *v = nullptr;
+    int64_t step = 0;
+    struct Slot {
+        int64_t cap = 0, n = 0;
+        float* X = nullptr;            // [cap][din] encodings (column c*ex = scaled position)
+        std::vector<float*> H;         // [L][cap][width] post-ReLU activations
+        bool valid = false;
+    } slots[TSB_DEFORM_SLOTS];
+    int64_t dcap = 0;
+    float *delta_a = nullptr, *delta_b = nullptr;  // [dcap][max(width, din)]
+    float* io = nullptr;                           // [dcap][3] host-staged positions / offsets / grads
+    int64_t io_cap = 0;
+    float* part = nullptr;                         // split-K partials
+    int64_t part_cap = 0;
+};
+
+namespace {
+constexpr int kDeformMaxSlices = 296;
+
+int deform_slot_alloc(tsb_deform* d, tsb_deform::Slot& s, int64_t n) {
+    if (n <= s.cap) return TSB_OK;
+    dev_free(s.X);
+    for (float*& h : s.H) dev_free(h);
+    s.H.assign(d->L, nullptr);
+    s.cap = 0;
+    int rc;
+    if ((rc = dev_alloc(&s.X, (size_t)n * d->din))) return rc;
+    for (int l = 0; l < d->L; ++l)
+        if ((rc = dev_alloc(&s.H[l], (size_t)n * d->width))) return rc;
+    s.cap = n;
+    return TSB_OK;
+}
+
+int deform_scratch(tsb_deform* d, int64_t n) {
+    const int wmax = std::max(d->width, d->din);
+    if (n > d->dcap) {
+        dev_free(d->delta_a);
+        dev_free(d->delta_b);
+        int rc;
+        if ((rc = dev_alloc(&d->delta_a, (size_t)n * wmax)) || (rc = dev_alloc(&d->delta_b, (size_t)n * wmax)))
+            return rc;
+        d->dcap = n;
+    }
+    const int64_t need = (int64_t)kDeformMaxSlices * 128 * 128;
+    if (need > d->part_cap) {
+        dev_free(d->part);
+        int rc;
+        if ((rc = dev_alloc(&d->part, (size_t)need))) return rc;
+        d->part_cap = need;
+    }
+    return TSB_OK;
+}
+
+int deform_io(tsb_deform* d, int64_t n) {
+    if (3 * n <= d->io_cap) return TSB_OK;
+    dev_free(d->io);
+    int rc;
+    if ((rc = dev_alloc(&d->io, (size_t)3 * n))) return rc;
+    d->io_cap = 3 * n;
+    return TSB_OK;
+}
+
+int deform_gemm(tsb_deform* d, GemmArgs g, int slices) {
+    const int r = launch_gemm_tf32x3(g, slices, d->ctx->stream);
+    if (r < 0) return fail(TSB_ERR_UNSUPPORTED, "deform: GEMM N > 128");
+    d->ctx->launches += r;
+    TSB_CHECK_LAUNCH();
+    return TSB_OK;
+}
+
+// Forward of `n` positions (pos[i * pos_stride + c]) at time t into out[i * out_stride + c].
+int deform_forward(tsb_deform* d, int slot, const float* pos, int64_t pos_stride, int64_t n, double t, float* out,
+                   int64_t out_stride) {
+    if (slot < 0 || slot >= TSB_DEFORM_SLOTS) return fail(TSB_ERR_INVALID, "deform: bad slot");
+    tsb_deform::Slot& s = d->slots[slot];
+    int rc;
+    if ((rc = deform_slot_alloc(d, s, std::max<int64_t>(n, 1)))) return rc;
+    cudaStream_t st = d->ctx->stream;
+    DeformEnc te{};
+    te.n = 1 + 2 * d->cfg.l_t;
+    te.v[0] = (float)t;
+    double f = M_PI;
+    for (int l = 0; l < d->cfg.l_t; ++l, f *= 2.0) {
+        te.v[1 + 2 * l] = (float)std::sin(f * t);
+        te.v[2 + 2 * l] = (float)std::cos(f * t);
+    }
+    launch_deform_encode(pos, pos_stride, n, 1.0 / d->cfg.coord_scale, d->cfg.l_x, te, s.X, d->din, st);
+    d->ctx->launches++;
+    const float* prev = s.X;
+    int64_t ld = d->din;
+    for (int l = 0; l <= d->L; ++l) {
+        const bool last = l == d->L;
+        GemmArgs g{};
+        g.A = prev; g.a_m = ld; g.a_k = 1;
+        g.B = d->params + d->w_off[l]; g.b_n = d->cols[l]; g.b_k = 1;
+        g.M = (int)n; g.N = d->rows[l]; g.K = d->cols[l]; g.k_per_slice = ((g.K + 31) / 32) * 32;
+        g.C = last ? out : s.H[l];
+        g.ldc = last ? out_stride : d->width;
+        g.bias = d->params + d->b_off[l];
+        g.relu = last ? 0 : 1;
+        if ((rc = deform_gemm(d, g, 1))) return rc;
+        if (!last) {
+            prev = s.H[l];
+            ld = d->width;
+        }
+    }
+    s.n = n;
+    s.valid = true;
+    return TSB_OK;
+}
+
+// Backward of the slot's forward for d_out[i * dstride + o] (o < 3); d_pos (nullable)
+// receives d(offsets)/d(position) (accumulated when `accumulate`).
+int deform_backward(tsb_deform* d, int slot, const float* d_out, int64_t dstride, float* d_pos, int64_t pstride,
+                    bool accumulate) {
+    if (slot < 0 || slot >= TSB_DEFORM_SLOTS || !d->slots[slot].valid)
+        return fail(TSB_ERR_INVALID, "deform: backward without a cached forward in this slot");
+    tsb_deform::Slot& s = d->slots[slot];
+    const int64_t n = s.n;
+    int rc;
+    if ((rc = deform_scratch(d, std::max<int64_t>(n, 1)))) return rc;
+    cudaStream_t st = d->ctx->stream;
+    const float* delta = d_out;
+    int64_t dld = dstride;
+    float* bufs[2] = {d->delta_a, d->delta_b};
+    int flip = 0;
+    const int slices = (int)std::max<int64_t>(1, std::min<int64_t>(kDeformMaxSlices, (n + 4095) / 4096));
+    const int kps = (int)(((n + slices - 1) / slices + 31) / 32 * 32);
+    const int used = (int)std::max<int64_t>(1, (n + kps - 1) / kps);
+    for (int l = d->L; l >= 0; --l) {
+        const float* below = l == 0 ? s.X : s.H[l - 1];
+        const int K = d->cols[l], O = d->rows[l];
+        // dW_l += delta^T below  (reduction over the n rows, split into row slices)
+        GemmArgs g{};
+        g.A = delta; g.a_m = 1; g.a_k = dld;
+        g.B = below; g.b_n = 1; g.b_k = K;
+        g.M = O; g.N = K; g.K = (int)n; g.k_per_slice = kps;
+        g.C = d->part; g.ldc = K; g.slice_stride = (int64_t)O * K;
+        if ((rc = deform_gemm(d, g, used))) return rc;
+        launch_reduce_slices(d->part, used, (int64_t)O * K, (int64_t)O * K, d->grads + d->w_off[l], true, st);
+        launch_colsum(delta, dld, n, O, d->grads + d->b_off[l], st);
+        d->ctx->launches += 2;
+        if (l == 0 && !d_pos) break;
+        // d_below = delta W_l (gated by the ReLU of the layer below, or the input gradient)
+        float* out = bufs[flip];
+        flip ^= 1;
+        GemmArgs h{};
+        h.A = delta; h.a_m = dld; h.a_k = 1;
+        h.B = d->params + d->w_off[l]; h.b_n = 1; h.b_k = K;
+        h.M = (int)n; h.N = K; h.K = O; h.k_per_slice = ((O + 31) / 32) * 32;
+        h.C = out; h.ldc = K;
+        if (l > 0) {
+            h.mask = s.H[l - 1];
+            h.ldmask = d->width;
+        }
+        if ((rc = deform_gemm(d, h, 1))) return rc;
+        if (l == 0) {
+            launch_deform_chain(out, K, s.X, d->din, n, 1.0 / d->cfg.coord_scale, d->cfg.l_x, d_pos, pstride,
+                                accumulate, st);
+            d->ctx->launches++;
+            break;
+        }
+        delta = out;
+        dld = K;
+    }
+    TSB_CHECK_LAUNCH();
+    return TSB_OK;
+}
+}  // namespace
+
+int tsb_deform_create(tsb_ctx* ctx, const tsb_deform_config* cfg, tsb_deform** out) {
+    if (!ctx || !cfg || !out) return fail(TSB_ERR_INVALID, "tsb_deform_create: null argument");
+    *out = nullptr;
+    if (cfg->hidden_layers < 0 || cfg->width <= 0 || cfg->l_x < 0 || cfg->l_t < 0 || !(cfg->coord_scale > 0.0))
+        return fail(TSB_ERR_INVALID, "DeformNet: invalid config");  // deform.cpp:29-31
+    const int din = 3 * (1 + 2 * cfg->l_x) + 1 + 2 * cfg->l_t;
+    if (cfg->width > 128 || din > 128 || 1 + 2 * cfg->l_t > 64)
+        return fail(TSB_ERR_UNSUPPORTED, "DeformNet: width and input_dim must be <= 128 on this build");
+    TSB_CUDA(cudaSetDevice(ctx->device));
+    tsb_deform* d = new tsb_deform();
+    d->ctx = ctx;
+    d->cfg = *cfg;
+    d->din = din;
+    d->L = cfg->hidden_layers;
+    d->width = cfg->width;
+    int prev = din;
+    for (int l = 0; l <= d->L; ++l) {
+        const int r = l == d->L ? 3 : d->width;
+        d->rows.push_back(r);
+        d->cols.push_back(prev);
+        d->w_off.push_back(d->P);
+        d->P += (int64_t)r * prev;
+        d->b_off.push_back(d->P);
+        d->P += r;
+        prev = r;
+    }
+    int rc;
+    if ((rc = dev_alloc(&d->params, d->P)) || (rc = dev_alloc(&d->grads, d->P)) || (rc = dev_alloc(&d->m, d->P)) ||
+        (rc = dev_alloc(&d->v, d->P))) {
+        tsb_deform_destroy(d);
+        return rc;
+    }
+    cudaStream_t st = ctx->stream;
+    cudaMemsetAsync(d->params, 0, sizeof(float) * d->P, st);
+    cudaMemsetAsync(d->grads, 0, sizeof(float) * d->P, st);
+    cudaMemsetAsync(d->m, 0, sizeof(float) * d->P, st);
+    cudaMemsetAsync(d->v, 0, sizeof(float) * d->P, st);
+    *out = d;
+    return TSB_OK;
+}
+
+void tsb_deform_destroy(tsb_deform* d) {
+    if (!d) return;
+    cudaSetDevice(d->ctx->device);
+    cudaStreamSynchronize(d->ctx->stream);
+    dev_free(d->params); dev_free(d->grads); dev_free(d->m); dev_free(d->v);
+    for (auto& s : d->slots) {
+        dev_free(s.X);
+        for (float*& h : s.H) dev_free(h);
+    }
+    dev_free(d->delta_a); dev_free(d->delta_b); dev_free(d->io); dev_free(d->part);
+    delete d;
+}
+
+int64_t tsb_deform_param_count(const tsb_deform* d) { return d ? d->P : 0; }
+
+int tsb_deform_set_params(tsb_deform* d, int where, const float* flat) {
+    if (!d || !flat) return fail(TSB_ERR_INVALID, "tsb_deform_set_params: null argument");
+    TSB_CUDA(cudaSetDevice(d->ctx->device));
+    TSB_CUDA(cudaMemcpyAsync(d->params, flat, sizeof(float) * d->P,
+                             where == TSB_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, d->ctx->stream));
+    TSB_CUDA(cudaStreamSynchronize(d->ctx->stream));
+    return TSB_OK;
+}
+
+int tsb_deform_get_params(tsb_deform* d, float* flat) {
+    if (!d || !flat) return fail(TSB_ERR_INVALID, "tsb_deform_get_params: null argument");
+    TSB_CUDA(cudaSetDevice(d->ctx->device));
+    TSB_CUDA(cudaMemcpyAsync(flat, d->params, sizeof(float) * d->P, cudaMemcpyDeviceToHost, d->ctx->stream));
+    TSB_CUDA(cudaStreamSynchronize(d->ctx->stream));
+    return TSB_OK;
+}
+
+int tsb_deform_get_grads(tsb_deform* d, float* flat) {
+    if (!d || !flat) return fail(TSB_ERR_INVALID, "tsb_deform_get_grads: null argument");
+    TSB_CUDA(cudaSetDevice(d->ctx->device));
+    TSB_CUDA(cudaMemcpyAsync(flat, d->grads, sizeof(float) * d->P, cudaMemcpyDeviceToHost, d->ctx->stream));
+    TSB_CUDA(cudaStreamSynchronize(d->ctx->stream));
+    return TSB_OK;
+}
+
+int tsb_deform_zero_grads(tsb_deform* d) {
+    if (!d) return fail(TSB_ERR_INVALID, "null network");
+    TSB_CUDA(cudaMemsetAsync(d->grads, 0, sizeof(float) * d->P, d->ctx->stream));
+    return TSB_OK;
+}
+
+int tsb_deform_offsets(tsb_deform* d, int slot, int where, const float* positions, int64_t n, double t,
+                       float* offsets) {
+    if (!d || !positions || !offsets || n < 0) return fail(TSB_ERR_INVALID, "tsb_deform_offsets: bad argument");
+    if (n > 0x7fffffff) return fail(TSB_ERR_UNSUPPORTED, "tsb_deform_offsets: too many points");
+    TSB_CUDA(cudaSetDevice(d->ctx->device));
+    cudaStream_t st = d->ctx->stream;
+    int rc;
+    const float* pos = positions;
+    float* out = offsets;
+    if (where == TSB_HOST) {
+        if ((rc = deform_io(d, std::max<int64_t>(n, 1)))) return rc;
+        TSB_CUDA(cudaMemcpyAsync(d->io, positions, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, st));
+        pos = d->io;
+        out = d->io;  // overwritten after the encoding read it (stream order)
+    } else if (where != TSB_DEVICE) {
+        return fail(TSB_ERR_INVALID, "bad memory kind");
+    }
+    if ((rc = deform_forward(d, slot, pos, 3, n, t, out, 3))) return rc;
+    if (where == TSB_HOST) {
+        TSB_CUDA(cudaMemcpyAsync(offsets, d->io, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, st));
+        TSB_CUDA(cudaStreamSynchronize(st));
+    }
+    return TSB_OK;
+}
+
+int tsb_deform_backward(tsb_deform* d, int slot, int where, const float* d_offsets, float* d_positions) {
+    if (!d || !d_offsets) return fail(TSB_ERR_INVALID, "tsb_deform_backward: null argument");
+    if (slot < 0 || slot >= TSB_DEFORM_SLOTS || !d->slots[slot].valid)
+        return fail(TSB_ERR_INVALID, "deform: backward without a cached forward in this slot");
+    TSB_CUDA(cudaSetDevice(d->ctx->device));
+    cudaStream_t st = d->ctx->stream;
+    const int64_t n = d->slots[slot].n;
+    int rc;
+    if (where == TSB_HOST) {
+        if ((rc = deform_io(d, 2 * std::max<int64_t>(n, 1)))) return rc;
+        TSB_CUDA(cudaMemcpyAsync(d->io, d_offsets, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, st));
+        float* dpos = d_positions ? d->io + 3 * n : nullptr;
+        if ((rc = deform_backward(d, slot, d->io, 3, dpos, 3, false))) return rc;
+        if (d_positions)
+            TSB_CUDA(cudaMemcpyAsync(d_positions, dpos, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, st));
+        TSB_CUDA(cudaStreamSynchronize(st));
+        return TSB_OK;
+    }
+    if (where != TSB_DEVICE) return fail(TSB_ERR_INVALID, "bad memory kind");
+    return deform_backward(d, slot, d_offsets, 3, d_positions, 3, false);
+}
+
+int tsb_deform_scene_offsets(tsb_deform* d, int slot, tsb_scene* s, int keyframe, double t) {
+    if (!d || !s) return fail(TSB_ERR_INVALID, "tsb_deform_scene_offsets: null argument");
+    if (s->ctx != d->ctx) return fail(TSB_ERR_INVALID, "deform: scene and network belong to different contexts");
+    if (keyframe < 0 || keyframe >= s->d.n_keyframes) return fail(TSB_ERR_INVALID, "deform: keyframe out of range");
+    TSB_CUDA(cudaSetDevice(d->ctx->device));
+    int rc = tsb_ctx_join(d->ctx);  // passes may still read the keyframe offsets
+    if (rc) return rc;
+    const size_t n = (size_t)s->d.n;
+    // positions: pos_op lanes xyz; offsets: keyframe plane lanes xyz (lane w stays 0)
+    if ((rc = deform_forward(d, slot, reinterpret_cast<const float*>(s->params), 4, (int64_t)n, t,
+                             reinterpret_cast<float*>(s->params + (size_t)(3 + keyframe) * n), 4)))
+        return rc;
+    TSB_CUDA(cudaEventRecord(s->params_ev, d->ctx->stream));
+    return TSB_OK;
+}
+
+int tsb_deform_scene_backward(tsb_deform* d, int slot, tsb_scene* s, int keyframe) {
+    if (!d || !s) return fail(TSB_ERR_INVALID, "tsb_deform_scene_backward: null argument");
+    if (s->ctx != d->ctx) return fail(TSB_ERR_INVALID, "deform: scene and network belong to different contexts");
+    if (keyframe < 0 || keyframe >= s->d.n_keyframes) return fail(TSB_ERR_INVALID, "deform: keyframe out of range");
+    TSB_CUDA(cudaSetDevice(d->ctx->device));
+    int rc = settle_all(d->ctx);  // every frame's gradients are in (a redone frame adds later otherwise)
+    if (rc) return rc;
+    cudaStream_t st = d->ctx->stream;
+    TSB_CUDA(cudaStreamWaitEvent(st, s->grads_ev, 0));
+    const size_t n = (size_t)s->d.n;
+    // trainer.cpp:329-331: canonical position += dX + din; the chain already added dX
+    if ((rc = deform_backward(d, slot, reinterpret_cast<const float*>(s->grads + (size_t)(3 + keyframe) * n), 4,
+                              reinterpret_cast<float*>(s->grads), 4, true)))
+        return rc;
+    TSB_CUDA(cudaEventRecord(s->grads_ev, st));
+    return TSB_OK;
+}
+
+int tsb_deform_debug_activation(tsb_deform* d, int slot, int layer, float* host_out) {
+    if (!d || !host_out || slot < 0 || slot >= TSB_DEFORM_SLOTS || !d->slots[slot].valid || layer < 0 ||
+        layer >= d->L)
+        return fail(TSB_ERR_INVALID, "tsb_deform_debug_activation: bad argument");
+    const tsb_deform::Slot& s = d->slots[slot];
+    TSB_CUDA(cudaMemcpyAsync(host_out, s.H[layer], sizeof(float) * (size_t)s.n * d->width, cudaMemcpyDeviceToHost,
+                             d->ctx->stream));
+    TSB_CUDA(cudaStreamSynchronize(d->ctx->stream));
+    return TSB_OK;
+}
+
+int tsb_deform_adam_step(tsb_deform* d, double lr, double beta1, double beta2, double eps) {
+    if (!d) return fail(TSB_ERR_INVALID, "null network");
+    d->step += 1;
+    return tsb_adam_step_flat(d->ctx, TSB_DEVICE, d->params, d->grads, d->m, d->v, (size_t)d->P, d->step, lr, beta1,
+                              beta2, eps);
+}
+
+int tsb_debug_gemm(tsb_ctx* ctx, int M, int N, int K, int slices, const float* A, int64_t a_m, int64_t a_k,
+                   const float* B, int64_t b_n, int64_t b_k, const float* bias, int relu, const float* mask,
+                   float* C) {
+    if (!ctx || !A || !B || !C || M <= 0 || N <= 0 || N > 128 || K < 0 || slices < 1)
+        return fail(TSB_ERR_INVALID, "tsb_debug_gemm: bad argument");
+    TSB_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const size_t na = (size_t)std::max<int64_t>(1, (int64_t)(M - 1) * a_m + (int64_t)std::max(K - 1, 0) * a_k + 1);
+    const size_t nb = (size_t)std::max<int64_t>(1, (int64_t)(N - 1) * b_n + (int64_t)std::max(K - 1, 0) * b_k + 1);
+    const int kps = ((K + slices - 1) / slices + 31) / 32 * 32;
+    const int used = std::max(1, (K + std::max(kps, 32) - 1) / std::max(kps, 32));
+    float *dA = nullptr, *dB = nullptr, *dC = nullptr, *dP = nullptr, *dbias = nullptr, *dmask = nullptr;
+    int rc;
+    if ((rc = dev_alloc(&dA, na)) || (rc = dev_alloc(&dB, nb)) || (rc = dev_alloc(&dC, (size_t)M * N)) ||
+        (rc = dev_alloc(&dP, (size_t)used * M * N)) || (rc = dev_alloc(&dbias, N)) || (rc = dev_alloc(&dmask, (size_t)M * N)))
+        return rc;
+    cudaMemcpyAsync(dA, A, na * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dB, B, nb * 4, cudaMemcpyHostToDevice, st);
+    if (bias) cudaMemcpyAsync(dbias, bias, (size_t)N * 4, cudaMemcpyHostToDevice, st);
+    if (mask) cudaMemcpyAsync(dmask, mask, (size_t)M * N * 4, cudaMemcpyHostToDevice, st);
+    GemmArgs g{};
+    g.A = dA; g.a_m = a_m; g.a_k = a_k;
+    g.B = dB; g.b_n = b_n; g.b_k = b_k;
+    g.M = M; g.N = N; g.K = K; g.k_per_slice = std::max(kps, 32);
+    g.C = dP; g.ldc = N; g.slice_stride = (int64_t)M * N;
+    g.bias = used == 1 && bias ? dbias : nullptr;
+    g.relu = used == 1 ? relu : 0;
+    g.mask = used == 1 && mask ? dmask : nullptr;
+    g.ldmask = N;
+    launch_gemm_tf32x3(g, used, st);
+    ctx->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) {
+        launch_reduce_slices(dP, used, (int64_t)M * N, (int64_t)M * N, dC, false, st);
+        cudaMemcpyAsync(C, dC, (size_t)M * N * 4, cudaMemcpyDeviceToHost, st);
+        e = cudaStreamSynchronize(st);
+    }
+    cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dP); cudaFree(dbias); cudaFree(dmask);
+    if (e != cudaSuccess) return fail(TSB_ERR_CUDA, std::string("tsb_debug_gemm: ") + cudaGetErrorString(e));
+    return TSB_OK;
+}
+
+// ---------------------------------------------------------------------------
 // host helpers (tof.hpp)
 // ---------------------------------------------------------------------------
 static double freq_or_default(double f) { return f > 0 ? f : 29.9792458e6; }

@@ -234,6 +234,34 @@ void launch_raster_bwd(const RecK& rec, const uint4* ranges_all, int nchunks, co
 // out[c] = (out[c] + sum_i part[i][c]) * scale; nothing when *abort != 0 (abort may be null).
 void launch_reduce_partials(const double* part, int nparts, int width, double* out,
                             double scale, const int32_t* abort, cudaStream_t st);
+// tsb_mlp.cu: tcgen05 (kind::tf32, 3xTF32) GEMM with strided operands and fused epilogue.
+struct GemmArgs {
+    const float* A;  // A(m, k) = A[m * a_m + k * a_k]
+    int64_t a_m, a_k;
+    const float* B;  // B(n, k) = B[n * b_n + k * b_k]
+    int64_t b_n, b_k;
+    int M, N, K;      // N <= 128
+    int k_per_slice;  // split-K slice length (multiple of 32); grid.y = slices
+    float* C;         // C[slice * slice_stride + m * ldc + n]
+    int64_t ldc, slice_stride;
+    const float* bias;  // [N] or null
+    int relu;
+    const float* mask;  // C *= (mask[m * ldmask + n] > 0) when non-null
+    int64_t ldmask;
+};
+int launch_gemm_tf32x3(const GemmArgs& g, int slices, cudaStream_t st);  // kernels launched (0, 1; -1: N > 128)
+void launch_reduce_slices(const float* part, int slices, int64_t stride, int64_t n, float* out, bool accumulate,
+                          cudaStream_t st);
+// DeformNet (tsb_mlp.cu): time encoding values (computed on the host in fp64), helpers.
+struct DeformEnc {
+    int n;
+    float v[64];
+};
+void launch_deform_encode(const float* pos, int64_t pos_stride, int64_t n, double inv_scale, int l_x,
+                          const DeformEnc& te, float* X, int64_t ldx, cudaStream_t st);
+void launch_deform_chain(const float* d_input, int64_t ldd, const float* X, int64_t ldx, int64_t n, double inv_scale,
+                         int l_x, float* d_pos, int64_t dpos_stride, bool accumulate, cudaStream_t st);
+void launch_colsum(const float* delta, int64_t ld, int64_t n, int cols, float* db, cudaStream_t st);
 // tsb_optim.cu
 void launch_pack_params(float4* dst, const float* src, int n, int comps, int comp0, int ncomp_dst,
                         cudaStream_t st);

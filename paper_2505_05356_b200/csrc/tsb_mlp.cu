@@ -1,0 +1,393 @@
+// DeformNet (deform.hpp:19-66, deform.cpp:28-159) on the 5th-generation tensor cores.
+//
+// The one dense contraction of the system: an MLP mapping (canonical position,
+// time) -> position offset.  Every layer is a tcgen05 GEMM
+//     D[128-row tile x N] = sum_k A(m, k) B(n, k)      (fp32 accumulator in TMEM)
+// issued by one thread with kind::tf32 operands staged in shared memory in the
+// canonical K-major no-swizzle layout (8-row x 16-byte core matrices).  The
+// reference computes in fp64; to stay within the parity tolerances the operands
+// are split 3xTF32 (a = a_hi + a_lo, both tf32; D += a_hi b_hi + a_hi b_lo +
+// a_lo b_hi), which keeps ~fp32 accuracy at a third of the tf32 tensor rate.
+// Operands are read through generic (m, k) / (n, k) strides, so the same kernel
+// serves the forward (X W^T), the input gradient (delta W) and the weight
+// gradient (delta^T H, split over row slices) without transposes in memory.
+// The epilogue (TMEM -> registers) fuses bias, ReLU and the ReLU-gate mask.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "tsb_internal.h"
+
+namespace tsb {
+
+namespace {
+
+constexpr int kGemmThreads = 128;  // 4 warps: staging, one MMA-issuing thread, TMEM epilogue (lane quadrants)
+constexpr int kGemmM = 128;        // rows per tile (TMEM lanes)
+constexpr int kGemmKc = 32;        // K elements staged per round (8 core-matrix columns of 4 tf32)
+constexpr uint32_t kCoreBytes = 128;                       // 8 rows x 16 B
+constexpr uint32_t kGroupBytes = (kGemmKc / 4) * kCoreBytes;  // one 8-row group across the K chunk
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// Shared-memory matrix descriptor (tcgen05), K-major, no swizzle:
+// LBO = byte step between core matrices along K, SBO = between 8-row groups.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version 1 (sm_100); base offset 0, SWIZZLE_NONE
+    return d;
+}
+
+// Instruction descriptor: D f32, A/B tf32, both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* mbar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n\t"
+        "DONE_%=:\n\t}" ::"r"(smem_u32(mbar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+// 3xTF32 split: hi = tf32(a) (round to nearest), lo = tf32(a - hi).  The tensor core
+// reads the fp32 bit patterns and ignores the 13 low mantissa bits.
+__device__ __forceinline__ void split_tf32(float a, float& hi, float& lo) {
+    uint32_t h;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(a));
+    hi = __uint_as_float(h);
+    uint32_t l;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(a - hi));
+    lo = __uint_as_float(l);
+}
+
+// Byte offset of element (row r, k) in a K-major no-swizzle tile of the K chunk.
+__device__ __forceinline__ uint32_t core_off(int r, int k) {
+    return (uint32_t)(r >> 3) * kGroupBytes + (uint32_t)(k >> 2) * kCoreBytes + (uint32_t)(r & 7) * 16u +
+           (uint32_t)(k & 3) * 4u;
+}
+
+// Stage rows [r0, r0 + R) x k [k0, k0 + kGemmKc) of X(r, k) = P[r * sr + k * sk]
+// (zero outside rows < nrows, k < kend) into hi / lo tiles.
+__device__ __forceinline__ void stage_tile(const float* __restrict__ P, int64_t sr, int64_t sk, int r0, int nrows,
+                                           int k0, int kend, int R, char* hi, char* lo) {
+    const bool kcontig = sk == 1;
+    for (int idx = threadIdx.x; idx < R * kGemmKc; idx += kGemmThreads) {
+        int r, k;
+        if (kcontig) {
+            r = idx / kGemmKc;
+            k = idx - r * kGemmKc;
+        } else {
+            k = idx / R;
+            r = idx - k * R;
+        }
+        const int gr = r0 + r, gk = k0 + k;
+        const float v = (gr < nrows && gk < kend) ? P[(int64_t)gr * sr + (int64_t)gk * sk] : 0.f;
+        float h, l;
+        split_tf32(v, h, l);
+        const uint32_t o = core_off(r, k);
+        *reinterpret_cast<float*>(hi + o) = h;
+        *reinterpret_cast<float*>(lo + o) = l;
+    }
+}
+
+}  // namespace
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Accumulation precision: the tensor core's fp32 accumulation error grows linearly
+// with the number of K steps (measured: 2e-6 of the result's scale per 256 rows of a
+// delta^T H reduction, 5e-4 per 65,536).  FLUSH kernels (the weight-gradient
+// reductions over all rows) therefore restart the TMEM accumulator every
+// kFlushChunks K chunks and add it into round-to-nearest fp32 registers.
+constexpr int kFlushChunks = 8;  // 256 rows
+
+// D[m, n] = sum_k A(m, k) B(n, k) over this CTA's K slice, m in a 128-row tile,
+// n < N (N <= NT).  Epilogue: + bias[n], ReLU, * (mask(m, n) > 0), store to
+// C + slice * slice_stride (split-K partials are reduced by k_reduce_slices).
+template <int NT, bool FLUSH>
+__global__ void __launch_bounds__(kGemmThreads) k_gemm_tf32x3(GemmArgs g) {
+    extern __shared__ __align__(1024) char smem[];
+    char* a_hi = smem;
+    char* a_lo = a_hi + kGemmM * kGemmKc * 4;
+    char* b_hi = a_lo + kGemmM * kGemmKc * 4;
+    char* b_lo = b_hi + NT * kGemmKc * 4;
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ uint32_t tmem_base_s;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int kTmemCols = NT <= 32 ? 32 : (NT <= 64 ? 64 : (NT <= 128 ? 128 : 256));
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        mbar_init(&mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    const uint32_t tmem = tmem_base_s;
+
+    const int m0 = blockIdx.x * kGemmM;
+    const int slice = blockIdx.y;
+    const int kbeg = slice * g.k_per_slice;
+    const int kend = min(g.K, kbeg + g.k_per_slice);
+    constexpr uint32_t idesc = idesc_tf32(kGemmM, NT);
+    uint32_t phase = 0;
+    bool any = false;
+    float acc[FLUSH ? NT : 1];
+#pragma unroll
+    for (int j = 0; j < (FLUSH ? NT : 1); ++j) acc[j] = 0.f;
+    const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+    int chunk = 0;
+    for (int k0 = kbeg; k0 < kend; k0 += kGemmKc, ++chunk) {
+        const bool group_start = !FLUSH ? !any : (chunk % kFlushChunks) == 0;
+        stage_tile(g.A, g.a_m, g.a_k, m0, g.M, k0, kend, kGemmM, a_hi, a_lo);
+        stage_tile(g.B, g.b_n, g.b_k, 0, g.N, k0, kend, NT, b_hi, b_lo);
+        fence_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            tc_after_sync();
+            const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
+#pragma unroll
+            for (int s = 0; s < kGemmKc / 8; ++s) {  // K = 8 tf32 per MMA = 2 core-matrix columns
+                const uint32_t off = (uint32_t)s * 2u * kCoreBytes;
+                const uint64_t dah = umma_desc(ah + off, kCoreBytes, kGroupBytes);
+                const uint64_t dal = umma_desc(al + off, kCoreBytes, kGroupBytes);
+                const uint64_t dbh = umma_desc(bh + off, kCoreBytes, kGroupBytes);
+                const uint64_t dbl = umma_desc(bl + off, kCoreBytes, kGroupBytes);
+                mma_tf32(tmem, dah, dbh, idesc, (!group_start || s > 0) ? 1u : 0u);
+                mma_tf32(tmem, dah, dbl, idesc, 1u);
+                mma_tf32(tmem, dal, dbh, idesc, 1u);
+            }
+            mma_commit(&mbar);
+        }
+        any = true;
+        mbar_wait(&mbar, phase);
+        phase ^= 1u;
+        tc_after_sync();
+        if (FLUSH && ((chunk % kFlushChunks) == kFlushChunks - 1 || k0 + kGemmKc >= kend)) {
+#pragma unroll
+            for (int c0 = 0; c0 < NT; c0 += 16) {
+                uint32_t v[16];
+                tmem_ld16(tl + (uint32_t)c0, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[(FLUSH ? c0 : 0) + j] += __uint_as_float(v[j]);
+            }
+            tc_before_sync();  // the next group's first MMA overwrites the accumulator
+        }
+    }
+
+    // epilogue: warp w owns TMEM lanes (rows) 32w .. 32w + 31
+    const int m = m0 + warp * 32 + lane;
+    float* C = g.C + (int64_t)slice * g.slice_stride;
+#pragma unroll
+    for (int c0 = 0; c0 < NT; c0 += 16) {
+        uint32_t v[16];
+        if (FLUSH) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(acc[(FLUSH ? c0 : 0) + j]);
+        } else if (any) {
+            tmem_ld16(tl + (uint32_t)c0, v);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = 0u;
+        }
+        if (m < g.M) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int n = c0 + j;
+                if (n >= g.N) break;
+                float x = __uint_as_float(v[j]);
+                if (g.bias) x += g.bias[n];
+                if (g.relu) x = fmaxf(x, 0.f);
+                if (g.mask && !(g.mask[(int64_t)m * g.ldmask + n] > 0.f)) x = 0.f;
+                C[(int64_t)m * g.ldc + n] = x;
+            }
+        }
+    }
+    tc_before_sync();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
+}
+
+// out[i] (+)= sum_s part[s * stride + i]
+__global__ void k_reduce_slices(const float* __restrict__ part, int slices, int64_t stride, int64_t n,
+                                float* __restrict__ out, int accumulate) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int k = 0; k < slices; ++k) s += part[k * stride + i];
+        out[i] = accumulate ? out[i] + (float)s : (float)s;
+    }
+}
+
+size_t gemm_smem_bytes(int nt) { return (size_t)(2 * kGemmM + 2 * nt) * kGemmKc * 4; }
+
+template <int NT, bool F>
+void gemm_attr() {
+    cudaFuncSetAttribute(k_gemm_tf32x3<NT, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(NT));
+}
+
+template <bool F>
+int gemm_dispatch(const GemmArgs& g, dim3 grid, cudaStream_t st) {
+    if (g.N <= 16)
+        k_gemm_tf32x3<16, F><<<grid, kGemmThreads, gemm_smem_bytes(16), st>>>(g);
+    else if (g.N <= 32)
+        k_gemm_tf32x3<32, F><<<grid, kGemmThreads, gemm_smem_bytes(32), st>>>(g);
+    else if (g.N <= 64)
+        k_gemm_tf32x3<64, F><<<grid, kGemmThreads, gemm_smem_bytes(64), st>>>(g);
+    else if (g.N <= 128)
+        k_gemm_tf32x3<128, F><<<grid, kGemmThreads, gemm_smem_bytes(128), st>>>(g);
+    else
+        return -1;
+    return 1;
+}
+
+int launch_gemm_tf32x3(const GemmArgs& g, int slices, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        gemm_attr<16, false>(); gemm_attr<32, false>(); gemm_attr<64, false>(); gemm_attr<128, false>();
+        gemm_attr<16, true>(); gemm_attr<32, true>(); gemm_attr<64, true>(); gemm_attr<128, true>();
+        attr = true;
+    }
+    if (g.M <= 0 || g.N <= 0) return 0;
+    const dim3 grid((g.M + kGemmM - 1) / kGemmM, std::max(1, slices));
+    const bool flush = g.k_per_slice > kFlushChunks * kGemmKc;
+    return flush ? gemm_dispatch<true>(g, grid, st) : gemm_dispatch<false>(g, grid, st);
+}
+
+void launch_reduce_slices(const float* part, int slices, int64_t stride, int64_t n, float* out, bool accumulate,
+                          cudaStream_t st) {
+    if (n <= 0) return;
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    k_reduce_slices<<<grid, 256, 0, st>>>(part, slices, stride, n, out, accumulate ? 1 : 0);
+}
+
+}  // namespace tsb
+
+namespace tsb {
+
+// ---------------------------------------------------------------------------
+// DeformNet helpers (deform.cpp:10-26, 60-78, 142-155)
+// ---------------------------------------------------------------------------
+
+// X[n][c * ex + j] = gamma_j(pos_c / coord_scale), then the (shared) time encoding.
+// gamma = [v, sin(pi 2^l v), cos(pi 2^l v)]: fp64 sincospi (2^l v is exact), rounded once.
+__global__ void k_deform_encode(const float* __restrict__ pos, int64_t pos_stride, int64_t n, double inv_scale,
+                                int l_x, DeformEnc te, float* __restrict__ X, int64_t ldx) {
+    const int ex = 1 + 2 * l_x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float* row = X + i * ldx;
+        for (int c = 0; c < 3; ++c) {
+            const double v = (double)pos[i * pos_stride + c] * inv_scale;
+            float* o = row + c * ex;
+            o[0] = (float)v;
+            double f = v;
+            for (int l = 0; l < l_x; ++l, f *= 2.0) {
+                double s, co;
+                sincospi(f, &s, &co);
+                o[1 + 2 * l] = (float)s;
+                o[2 + 2 * l] = (float)co;
+            }
+        }
+        for (int j = 0; j < te.n; ++j) row[3 * ex + j] = te.v[j];
+    }
+}
+
+// d_pos[i][c] += sum_j gamma'_j(v_c) d_input[i][c * ex + j] / coord_scale (v_c = X[i][c * ex]).
+__global__ void k_deform_chain(const float* __restrict__ d_input, int64_t ldd, const float* __restrict__ X,
+                               int64_t ldx, int64_t n, double inv_scale, int l_x, float* __restrict__ d_pos,
+                               int64_t dpos_stride, int accumulate) {
+    const int ex = 1 + 2 * l_x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        for (int c = 0; c < 3; ++c) {
+            const float* din = d_input + i * ldd + c * ex;
+            const double v = (double)X[i * ldx + c * ex];
+            double acc = din[0];
+            double f = v, fr = M_PI;
+            for (int l = 0; l < l_x; ++l, f *= 2.0, fr *= 2.0) {
+                double s, co;
+                sincospi(f, &s, &co);
+                acc += fr * co * (double)din[1 + 2 * l] - fr * s * (double)din[2 + 2 * l];
+            }
+            float* o = d_pos + i * dpos_stride + c;
+            const float val = (float)(acc * inv_scale);
+            *o = accumulate ? *o + val : val;
+        }
+    }
+}
+
+// db[o] += sum_i delta[i][o]
+__global__ void k_colsum(const float* __restrict__ delta, int64_t ld, int64_t n, int cols, float* __restrict__ db) {
+    const int o = threadIdx.x;
+    if (o >= cols) return;
+    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t i0 = blockIdx.x * per, i1 = min(n, i0 + per);
+    double s = 0.0;
+    for (int64_t i = i0; i < i1; ++i) s += delta[i * ld + o];
+    if (s != 0.0) atomicAdd(&db[o], (float)s);
+}
+
+void launch_deform_encode(const float* pos, int64_t pos_stride, int64_t n, double inv_scale, int l_x,
+                          const DeformEnc& te, float* X, int64_t ldx, cudaStream_t st) {
+    if (n <= 0) return;
+    const int grid = (int)std::min<int64_t>((n + 127) / 128, 148 * 16);
+    k_deform_encode<<<grid, 128, 0, st>>>(pos, pos_stride, n, inv_scale, l_x, te, X, ldx);
+}
+
+void launch_deform_chain(const float* d_input, int64_t ldd, const float* X, int64_t ldx, int64_t n, double inv_scale,
+                         int l_x, float* d_pos, int64_t dpos_stride, bool accumulate, cudaStream_t st) {
+    if (n <= 0) return;
+    const int grid = (int)std::min<int64_t>((n + 127) / 128, 148 * 16);
+    k_deform_chain<<<grid, 128, 0, st>>>(d_input, ldd, X, ldx, n, inv_scale, l_x, d_pos, dpos_stride,
+                                         accumulate ? 1 : 0);
+}
+
+void launch_colsum(const float* delta, int64_t ld, int64_t n, int cols, float* db, cudaStream_t st) {
+    if (n <= 0 || cols <= 0) return;
+    const int grid = (int)std::min<int64_t>((n + 1023) / 1024, 148 * 4);
+    k_colsum<<<grid, ((cols + 31) / 32) * 32, 0, st>>>(delta, ld, n, cols, db);
+}
+
+}  // namespace tsb

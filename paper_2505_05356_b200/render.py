@@ -563,3 +563,91 @@ def quad_basis(depth: float, frequency: float = 0.0):
     out = (C.c_double * 4)()
     lib().tsb_quad_basis(float(depth), float(frequency), out)
     return list(out)
+
+
+class DeformNet:
+    """The reference's DeformNet (deform.hpp:19-66) on the tensor cores: positional
+    encodings -> `hidden_layers` ReLU layers -> 3 offsets; each layer a tcgen05 GEMM
+    (3xTF32).  Parameters are the flat get_parameters order (W row-major, then b)."""
+
+    def __init__(self, ctx: Context, hidden_layers: int = 4, width: int = 128, l_x: int = 10, l_t: int = 10,
+                 coord_scale: float = 1.0):
+        self.ctx = ctx
+        cfg = _abi.DeformConfigC(hidden_layers, width, l_x, l_t, coord_scale)
+        h = C.c_void_p()
+        check(lib().tsb_deform_create(ctx.handle, C.byref(cfg), C.byref(h)))
+        self._h = h
+        self.hidden_layers, self.width, self.l_x, self.l_t, self.coord_scale = hidden_layers, width, l_x, l_t, \
+            coord_scale
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def input_dim(self) -> int:
+        return 3 * (1 + 2 * self.l_x) + 1 + 2 * self.l_t
+
+    @property
+    def parameter_count(self) -> int:
+        return int(lib().tsb_deform_param_count(self._h))
+
+    def set_parameters(self, flat):
+        a = np.ascontiguousarray(flat, np.float32)
+        if a.size != self.parameter_count:
+            raise ValueError("DeformNet::set_parameters: size mismatch")
+        check(lib().tsb_deform_set_params(self._h, _abi.TSB_HOST, a.ctypes.data))
+
+    def get_parameters(self) -> np.ndarray:
+        out = np.empty(self.parameter_count, np.float32)
+        check(lib().tsb_deform_get_params(self._h, out.ctypes.data))
+        return out
+
+    def grads(self) -> np.ndarray:
+        out = np.empty(self.parameter_count, np.float32)
+        check(lib().tsb_deform_get_grads(self._h, out.ctypes.data))
+        return out
+
+    def zero_grads(self):
+        check(lib().tsb_deform_zero_grads(self._h))
+
+    def offsets(self, positions, t: float, slot: int = 0) -> np.ndarray:
+        """positions (n, 3) -> offsets (n, 3); caches the forward in `slot` for backward()."""
+        p = np.ascontiguousarray(positions, np.float32).reshape(-1, 3)
+        out = np.empty_like(p)
+        check(lib().tsb_deform_offsets(self._h, slot, _abi.TSB_HOST, p.ctypes.data, p.shape[0], float(t),
+                                       out.ctypes.data))
+        return out
+
+    def backward(self, d_offsets, slot: int = 0, want_positions: bool = True):
+        """Accumulates dW/db for the slot's forward; returns d(positions) (n, 3) or None."""
+        d = np.ascontiguousarray(d_offsets, np.float32).reshape(-1, 3)
+        dp = np.empty_like(d) if want_positions else None
+        check(lib().tsb_deform_backward(self._h, slot, _abi.TSB_HOST, d.ctypes.data,
+                                        dp.ctypes.data if want_positions else None))
+        return dp
+
+    def scene_offsets(self, scene: "GaussianScene", keyframe: int, t: float, slot: int = 0):
+        check(lib().tsb_deform_scene_offsets(self._h, slot, scene.handle, keyframe, float(t)))
+
+    def scene_backward(self, scene: "GaussianScene", keyframe: int, slot: int = 0):
+        check(lib().tsb_deform_scene_backward(self._h, slot, scene.handle, keyframe))
+
+    def debug_activation(self, layer: int, n: int, slot: int = 0) -> np.ndarray:
+        out = np.empty((n, self.width), np.float32)
+        check(lib().tsb_deform_debug_activation(self._h, slot, layer, out.ctypes.data))
+        return out
+
+    def adam_step(self, lr: float, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-15):
+        check(lib().tsb_deform_adam_step(self._h, lr, beta1, beta2, eps))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tsb_deform_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
