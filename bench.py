@@ -390,6 +390,50 @@ def bench_train_c4(args, dist, tsb, synthetic, ctx):
     return res
 
 
+def bench_deform(args, dist, tsb, synthetic, ctx):
+    """the reference's DeformNet (4 x 128 ReLU MLP, l_x = l_t = 10) on the
+    tcgen05 tensor cores for the c4 scene's 2M canonical positions: offsets into a keyframe
+    plane (forward) and the backward from that keyframe's gradient, device-resident."""
+    import torch
+    n = args.deform_n
+    g = synthetic.gaussians(n, 0, n_keyframes=2)
+    scene = tsb.GaussianScene(ctx, g.n, g.n_keyframes, tsb.ToFConfig(30e6))
+    scene.set_params(g.position, g.log_scale, g.rotation, g.opacity_logit, g.reflectivity_dc, g.motion)
+    net = tsb.DeformNet(ctx)
+    rng = np.random.default_rng(0)
+    net.set_parameters((rng.normal(size=net.parameter_count) * 0.05).astype(np.float32))
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    for _ in range(3):
+        net.scene_offsets(scene, 0, 0.3)
+        net.scene_backward(scene, 0)
+    ctx.synchronize()
+    reps = 5
+    ev[0].record(stream)
+    for _ in range(reps):
+        net.scene_offsets(scene, 0, 0.3)
+    ev[1].record(stream)
+    for _ in range(reps):
+        net.scene_backward(scene, 0)
+    ev[2].record(stream)
+    ctx.synchronize()
+    fwd_ms = ev[0].elapsed_time(ev[1]) / reps
+    bwd_ms = ev[1].elapsed_time(ev[2]) / reps
+    mac = net.input_dim * net.width + (net.hidden_layers - 1) * net.width ** 2 + net.width * 3
+    f_fwd, f_bwd = 2.0 * mac * n, 4.0 * mac * n
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    tf32_peak = peaks.get("bf16_tflops", 2250.0) / 2
+    ach = (f_fwd + f_bwd) / ((fwd_ms + bwd_ms) * 1e-3) / 1e12
+    scene.close()
+    net.close()
+    return {"points": n, "layers": "4x128 ReLU + 3, l_x=l_t=10 (deform.hpp defaults)",
+            "fwd_ms": round(fwd_ms, 3), "bwd_ms": round(bwd_ms, 3),
+            "roofline": {"bound": "tensor", "achieved": round(ach, 2), "unit": "TFLOP/s",
+                         "peak": round(tf32_peak, 1), "frac": round(ach / tf32_peak, 4),
+                         "note": "algorithmic FLOP (2 per MAC, forward + weight/input gradients); the 3xTF32 split "
+                                 "issues 3x these on the tensor cores; peak = measured dense bf16 / 2 (tf32)"}}
+
+
 def cpu_baseline_c3(frames=1):
     """Oracle (reference restatement) on the host cores: RenderPass ctor + forward per frame."""
     from oracle import oracle as orc
@@ -456,6 +500,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--no-deform", action="store_true")
+    ap.add_argument("--deform-n", type=int, default=2_000_000)
     ap.add_argument("--passes", type=int, default=8, help="render passes (streams) in flight")
     ap.add_argument("--train-passes", type=int, default=4)
     ap.add_argument("--train-steps", type=int, default=3)
@@ -478,6 +524,9 @@ def main():
     train = None
     if not args.no_train:
         train = bench_train_c4(args, dist, tsb, synthetic, ctx)
+    deform = None
+    if not args.no_deform and dist.rank == 0:
+        deform = bench_deform(args, dist, tsb, synthetic, ctx)
     cpu = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
         v_cpu, cores = cpu_baseline_c3(args.cpu_frames)
@@ -496,7 +545,7 @@ def main():
                            "precision": "fp64 preprocess, fp32 raster, fp64 fix-up of ambiguous pixels"},
                 "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
                 "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"]},
-                "gpu_launches": info["launches"], "train": train, "detail": info}
+                "gpu_launches": info["launches"], "train": train, "deform_net": deform, "detail": info}
         print(json.dumps(line), flush=True)
     dist.close()
     return 0

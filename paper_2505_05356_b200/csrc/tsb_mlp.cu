@@ -23,7 +23,7 @@ namespace tsb {
 
 namespace {
 
-constexpr int kGemmThreads = 128;  // 4 warps: staging, one MMA-issuing thread, TMEM epilogue (lane quadrants)
+constexpr int kGemmThreads = 256;  // 8 warps stage; thread 0 issues MMAs; warps read TMEM by lane quadrant
 constexpr int kGemmM = 128;        // rows per tile (TMEM lanes)
 constexpr int kGemmKc = 32;        // K elements staged per round (8 core-matrix columns of 4 tf32)
 constexpr uint32_t kCoreBytes = 128;                       // 8 rows x 16 B
@@ -97,9 +97,52 @@ __device__ __forceinline__ uint32_t core_off(int r, int k) {
 }
 
 // Stage rows [r0, r0 + R) x k [k0, k0 + kGemmKc) of X(r, k) = P[r * sr + k * sk]
-// (zero outside rows < nrows, k < kend) into hi / lo tiles.
+// (zero outside rows < nrows, k < kend) into hi / lo tiles.  Fast paths: 16-byte loads
+// along K (one core-matrix row, stored whole; consecutive threads take consecutive rows
+// of a core matrix, so the shared stores are conflict-free) or along rows (transposed
+// operands: four rows of one k per load).
+__device__ __forceinline__ void split4(const float4 v, float4& h, float4& l) {
+    split_tf32(v.x, h.x, l.x);
+    split_tf32(v.y, h.y, l.y);
+    split_tf32(v.z, h.z, l.z);
+    split_tf32(v.w, h.w, l.w);
+}
+
 __device__ __forceinline__ void stage_tile(const float* __restrict__ P, int64_t sr, int64_t sk, int r0, int nrows,
                                            int k0, int kend, int R, char* hi, char* lo) {
+    const bool aligned = ((uintptr_t)P & 15) == 0;
+    if (sk == 1 && (sr & 3) == 0 && aligned && k0 + kGemmKc <= kend) {
+        for (int idx = threadIdx.x; idx < R * (kGemmKc / 4); idx += kGemmThreads) {
+            const int r8 = idx & 7, q = (idx >> 3) & 7, rg = idx >> 6;
+            const int r = rg * 8 + r8, gr = r0 + r;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (gr < nrows) v = __ldg(reinterpret_cast<const float4*>(P + (int64_t)gr * sr + k0 + 4 * q));
+            float4 h, l;
+            split4(v, h, l);
+            const uint32_t o = core_off(r, 4 * q);
+            *reinterpret_cast<float4*>(hi + o) = h;
+            *reinterpret_cast<float4*>(lo + o) = l;
+        }
+        return;
+    }
+    if (sr == 1 && (sk & 3) == 0 && aligned && r0 + R <= nrows && (r0 & 3) == 0) {
+        const int rq_n = R / 4;
+        for (int idx = threadIdx.x; idx < kGemmKc * rq_n; idx += kGemmThreads) {
+            const int k = idx / rq_n, rq = idx - k * rq_n, gk = k0 + k;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (gk < kend) v = __ldg(reinterpret_cast<const float4*>(P + (r0 + 4 * rq) + (int64_t)gk * sk));
+            float4 h, l;
+            split4(v, h, l);
+            const float hv[4] = {h.x, h.y, h.z, h.w}, lv[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t o = core_off(4 * rq + i, k);
+                *reinterpret_cast<float*>(hi + o) = hv[i];
+                *reinterpret_cast<float*>(lo + o) = lv[i];
+            }
+        }
+        return;
+    }
     const bool kcontig = sk == 1;
     for (int idx = threadIdx.x; idx < R * kGemmKc; idx += kGemmThreads) {
         int r, k;
@@ -139,20 +182,25 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
 // kFlushChunks K chunks and add it into round-to-nearest fp32 registers.
 constexpr int kFlushChunks = 8;  // 256 rows
 
-// D[m, n] = sum_k A(m, k) B(n, k) over this CTA's K slice, m in a 128-row tile,
-// n < N (N <= NT).  Epilogue: + bias[n], ReLU, * (mask(m, n) > 0), store to
-// C + slice * slice_stride (split-K partials are reduced by k_reduce_slices).
+constexpr int kGemmStages = 2;  // shared-memory ring: staging chunk c+1 overlaps the MMAs of chunk c
+
+__host__ __device__ constexpr size_t gemm_stage_bytes(int nt) { return (size_t)(kGemmM + nt) * kGemmKc * 4 * 2; }
+
+// D[m, n] = sum_k A(m, k) B(n, k) over this CTA's K slice for 128-row tiles (CTAs
+// stride over the tiles), n < N (N <= NT).  Every thread stages; thread 0 issues the
+// 3xTF32 MMAs of a chunk and commits them to that stage's mbarrier, so the threads
+// stage the next chunk while the tensor core works.  Epilogue per tile: + bias[n],
+// ReLU, * (mask(m, n) > 0), store to C + slice * slice_stride (split-K partials are
+// reduced by k_reduce_slices).
 template <int NT, bool FLUSH>
-__global__ void __launch_bounds__(kGemmThreads) k_gemm_tf32x3(GemmArgs g) {
+__global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g) {
     extern __shared__ __align__(1024) char smem[];
-    char* a_hi = smem;
-    char* a_lo = a_hi + kGemmM * kGemmKc * 4;
-    char* b_hi = a_lo + kGemmM * kGemmKc * 4;
-    char* b_lo = b_hi + NT * kGemmKc * 4;
-    __shared__ __align__(8) uint64_t mbar;
+    __shared__ __align__(8) uint64_t mb_stage[kGemmStages];
+    __shared__ __align__(8) uint64_t mb_tile;
     __shared__ uint32_t tmem_base_s;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr int kTmemCols = NT <= 32 ? 32 : (NT <= 64 ? 64 : (NT <= 128 ? 128 : 256));
+    constexpr uint32_t kABytes = kGemmM * kGemmKc * 4, kBBytes = NT * kGemmKc * 4;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
                      "n"(kTmemCols)
@@ -160,91 +208,142 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_tf32x3(GemmArgs g) {
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     if (tid == 0) {
-        mbar_init(&mbar, 1);
+        for (int i = 0; i < kGemmStages; ++i) mbar_init(&mb_stage[i], 1);
+        mbar_init(&mb_tile, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
     const uint32_t tmem = tmem_base_s;
+    // TMEM lane quadrant of this warp (warps w and w + 4 share it and split the columns)
+    const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    constexpr int kColHalf = NT >= 32 ? NT / 2 : NT;
+    const int col0 = NT >= 32 ? (warp >> 2) * kColHalf : 0;
+    const bool epi_warp = NT >= 32 || warp < 4;
 
-    const int m0 = blockIdx.x * kGemmM;
     const int slice = blockIdx.y;
     const int kbeg = slice * g.k_per_slice;
     const int kend = min(g.K, kbeg + g.k_per_slice);
+    const int ntiles = (g.M + kGemmM - 1) / kGemmM;
     constexpr uint32_t idesc = idesc_tf32(kGemmM, NT);
-    uint32_t phase = 0;
-    bool any = false;
-    float acc[FLUSH ? NT : 1];
-#pragma unroll
-    for (int j = 0; j < (FLUSH ? NT : 1); ++j) acc[j] = 0.f;
-    const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
-    int chunk = 0;
-    for (int k0 = kbeg; k0 < kend; k0 += kGemmKc, ++chunk) {
-        const bool group_start = !FLUSH ? !any : (chunk % kFlushChunks) == 0;
-        stage_tile(g.A, g.a_m, g.a_k, m0, g.M, k0, kend, kGemmM, a_hi, a_lo);
-        stage_tile(g.B, g.b_n, g.b_k, 0, g.N, k0, kend, NT, b_hi, b_lo);
-        fence_async_smem();
-        __syncthreads();
-        if (tid == 0) {
-            tc_after_sync();
-            const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
-#pragma unroll
-            for (int s = 0; s < kGemmKc / 8; ++s) {  // K = 8 tf32 per MMA = 2 core-matrix columns
-                const uint32_t off = (uint32_t)s * 2u * kCoreBytes;
-                const uint64_t dah = umma_desc(ah + off, kCoreBytes, kGroupBytes);
-                const uint64_t dal = umma_desc(al + off, kCoreBytes, kGroupBytes);
-                const uint64_t dbh = umma_desc(bh + off, kCoreBytes, kGroupBytes);
-                const uint64_t dbl = umma_desc(bl + off, kCoreBytes, kGroupBytes);
-                mma_tf32(tmem, dah, dbh, idesc, (!group_start || s > 0) ? 1u : 0u);
-                mma_tf32(tmem, dah, dbl, idesc, 1u);
-                mma_tf32(tmem, dal, dbh, idesc, 1u);
-            }
-            mma_commit(&mbar);
-        }
-        any = true;
-        mbar_wait(&mbar, phase);
-        phase ^= 1u;
-        tc_after_sync();
-        if (FLUSH && ((chunk % kFlushChunks) == kFlushChunks - 1 || k0 + kGemmKc >= kend)) {
-#pragma unroll
-            for (int c0 = 0; c0 < NT; c0 += 16) {
-                uint32_t v[16];
-                tmem_ld16(tl + (uint32_t)c0, v);
-#pragma unroll
-                for (int j = 0; j < 16; ++j) acc[(FLUSH ? c0 : 0) + j] += __uint_as_float(v[j]);
-            }
-            tc_before_sync();  // the next group's first MMA overwrites the accumulator
-        }
-    }
-
-    // epilogue: warp w owns TMEM lanes (rows) 32w .. 32w + 31
-    const int m = m0 + warp * 32 + lane;
     float* C = g.C + (int64_t)slice * g.slice_stride;
+    uint32_t c = 0;        // chunks issued by this CTA (stage ring position)
+    uint32_t tphase = 0;   // mb_tile completions waited for
+    float acc[FLUSH ? kColHalf : 1];
+
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int m0 = tile * kGemmM;
+        bool any = false;
 #pragma unroll
-    for (int c0 = 0; c0 < NT; c0 += 16) {
-        uint32_t v[16];
-        if (FLUSH) {
+        for (int j = 0; j < (FLUSH ? kColHalf : 1); ++j) acc[j] = 0.f;
+        int chunk = 0;
+        for (int k0 = kbeg; k0 < kend; k0 += kGemmKc, ++chunk, ++c) {
+            const int st = (int)(c % kGemmStages);
+            if (c >= (uint32_t)kGemmStages) mbar_wait(&mb_stage[st], ((c / kGemmStages) - 1) & 1u);
+            char* a_hi = smem + (size_t)st * gemm_stage_bytes(NT);
+            char* a_lo = a_hi + kABytes;
+            char* b_hi = a_lo + kABytes;
+            char* b_lo = b_hi + kBBytes;
+            stage_tile(g.A, g.a_m, g.a_k, m0, g.M, k0, kend, kGemmM, a_hi, a_lo);
+            stage_tile(g.B, g.b_n, g.b_k, 0, g.N, k0, kend, NT, b_hi, b_lo);
+            fence_async_smem();
+            __syncthreads();
+            const bool group_start = FLUSH ? (chunk % kFlushChunks) == 0 : !any;
+            const bool group_end = FLUSH ? ((chunk % kFlushChunks) == kFlushChunks - 1 || k0 + kGemmKc >= kend)
+                                         : k0 + kGemmKc >= kend;
+            if (tid == 0) {
+                tc_after_sync();
+                const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(acc[(FLUSH ? c0 : 0) + j]);
-        } else if (any) {
-            tmem_ld16(tl + (uint32_t)c0, v);
-        } else {
+                for (int s = 0; s < kGemmKc / 8; ++s) {  // K = 8 tf32 per MMA = 2 core-matrix columns
+                    const uint32_t off = (uint32_t)s * 2u * kCoreBytes;
+                    const uint64_t dah = umma_desc(ah + off, kCoreBytes, kGroupBytes);
+                    const uint64_t dal = umma_desc(al + off, kCoreBytes, kGroupBytes);
+                    const uint64_t dbh = umma_desc(bh + off, kCoreBytes, kGroupBytes);
+                    const uint64_t dbl = umma_desc(bl + off, kCoreBytes, kGroupBytes);
+                    mma_tf32(tmem, dah, dbh, idesc, (!group_start || s > 0) ? 1u : 0u);
+                    mma_tf32(tmem, dah, dbl, idesc, 1u);
+                    mma_tf32(tmem, dal, dbh, idesc, 1u);
+                }
+                mma_commit(&mb_stage[st]);
+                if (group_end) mma_commit(&mb_tile);
+            }
+            any = true;
+            if (FLUSH && group_end) {
+                mbar_wait(&mb_tile, tphase & 1u);
+                ++tphase;
+                tc_after_sync();
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = 0u;
-        }
-        if (m < g.M) {
+                for (int cc = 0; cc < kColHalf; cc += 16) {
+                    uint32_t v[16];
+                    tmem_ld16(tl + (uint32_t)(col0 + cc), v);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int n = c0 + j;
-                if (n >= g.N) break;
-                float x = __uint_as_float(v[j]);
-                if (g.bias) x += g.bias[n];
-                if (g.relu) x = fmaxf(x, 0.f);
-                if (g.mask && !(g.mask[(int64_t)m * g.ldmask + n] > 0.f)) x = 0.f;
-                C[(int64_t)m * g.ldc + n] = x;
+                    for (int j = 0; j < 16; ++j) acc[(FLUSH ? cc : 0) + j] += __uint_as_float(v[j]);
+                }
+                tc_before_sync();  // the next group's first MMA overwrites the accumulator
             }
         }
+        if (!FLUSH && any) {
+            mbar_wait(&mb_tile, tphase & 1u);
+            ++tphase;
+            tc_after_sync();
+        }
+
+        // epilogue: this warp's TMEM lane quadrant (rows), its column half
+        const int m = m0 + (warp & 3) * 32 + lane;
+        if (epi_warp) {
+#pragma unroll
+            for (int cc = 0; cc < kColHalf; cc += 16) {
+                const int n0 = col0 + cc;
+                uint32_t v[16];
+                if (FLUSH) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(acc[(FLUSH ? cc : 0) + j]);
+                } else if (any) {
+                    tmem_ld16(tl + (uint32_t)n0, v);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = 0u;
+                }
+                if (m < g.M && n0 < g.N) {
+                    float x[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        x[j] = __uint_as_float(v[j]);
+                        if (g.bias && n0 + j < g.N) x[j] += __ldg(g.bias + n0 + j);
+                        if (g.relu) x[j] = fmaxf(x[j], 0.f);
+                    }
+                    float* crow = C + (int64_t)m * g.ldc + n0;
+                    const float* mrow = g.mask ? g.mask + (int64_t)m * g.ldmask + n0 : nullptr;
+                    const bool vec = n0 + 16 <= g.N && ((uintptr_t)crow & 15) == 0 &&
+                                     (!mrow || ((uintptr_t)mrow & 15) == 0);
+                    if (vec) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            float4 o = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+                            if (mrow) {
+                                const float4 mk = __ldg(reinterpret_cast<const float4*>(mrow) + q);
+                                if (!(mk.x > 0.f)) o.x = 0.f;
+                                if (!(mk.y > 0.f)) o.y = 0.f;
+                                if (!(mk.z > 0.f)) o.z = 0.f;
+                                if (!(mk.w > 0.f)) o.w = 0.f;
+                            }
+                            reinterpret_cast<float4*>(crow)[q] = o;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            if (n0 + j >= g.N) break;
+                            float xv = x[j];
+                            if (mrow && !(mrow[j] > 0.f)) xv = 0.f;
+                            crow[j] = xv;
+                        }
+                    }
+                }
+            }
+        }
+        tc_before_sync();  // the next tile's first MMA overwrites the accumulator
     }
     tc_before_sync();
     __syncthreads();
@@ -262,7 +361,7 @@ __global__ void k_reduce_slices(const float* __restrict__ part, int slices, int6
     }
 }
 
-size_t gemm_smem_bytes(int nt) { return (size_t)(2 * kGemmM + 2 * nt) * kGemmKc * 4; }
+size_t gemm_smem_bytes(int nt) { return (size_t)kGemmStages * gemm_stage_bytes(nt); }
 
 template <int NT, bool F>
 void gemm_attr() {
@@ -292,7 +391,9 @@ int launch_gemm_tf32x3(const GemmArgs& g, int slices, cudaStream_t st) {
         attr = true;
     }
     if (g.M <= 0 || g.N <= 0) return 0;
-    const dim3 grid((g.M + kGemmM - 1) / kGemmM, std::max(1, slices));
+    const int ntiles = (g.M + kGemmM - 1) / kGemmM;
+    const int per_sm = g.N <= 32 ? 2 : 1;  // shared-memory / TMEM residency
+    const dim3 grid(std::min(ntiles, std::max(1, 148 * per_sm / std::max(1, slices))), std::max(1, slices));
     const bool flush = g.k_per_slice > kFlushChunks * kGemmKc;
     return flush ? gemm_dispatch<true>(g, grid, st) : gemm_dispatch<false>(g, grid, st);
 }
