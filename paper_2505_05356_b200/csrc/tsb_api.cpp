@@ -1923,6 +1923,11 @@ struct tsb_deform {
     int64_t io_cap = 0;
     float* part = nullptr;                         // split-K partials
     int64_t part_cap = 0;
+    // fused forward (k_mlp_fwd_fused): weights pre-split / pre-laid-out per K chunk
+    bool fused = false;
+    MlpLayout lay{};
+    char* wpack = nullptr;
+    bool packed = false;
 };
 
 namespace {
@@ -1994,6 +1999,40 @@ int deform_forward(tsb_deform* d, int slot, const float* pos, int64_t pos_stride
     for (int l = 0; l < d->cfg.l_t; ++l, f *= 2.0) {
         te.v[1 + 2 * l] = (float)std::sin(f * t);
         te.v[2 + 2 * l] = (float)std::cos(f * t);
+    }
+    static const bool unfused = [] {
+        const char* e = std::getenv("TSB_MLP_UNFUSED");
+        return e && e[0] == '1';
+    }();
+    if (d->fused && !unfused) {
+        if (!d->packed) {
+            launch_pack_weights(d->lay, d->params, d->wpack, st);
+            d->ctx->launches++;
+            d->packed = true;
+        }
+        MlpFwdArgs a{};
+        a.lay = d->lay;
+        a.pos = pos;
+        a.pos_stride = pos_stride;
+        a.n = n;
+        a.inv_scale = 1.0 / d->cfg.coord_scale;
+        a.l_x = d->cfg.l_x;
+        a.din = d->din;
+        a.te = te;
+        a.wpack = d->wpack;
+        a.params = d->params;
+        a.X = s.X;
+        a.ldx = d->din;
+        for (int l = 0; l < d->L; ++l) a.H[l] = s.H[l];
+        a.ldh = d->width;
+        a.out = out;
+        a.out_stride = out_stride;
+        launch_mlp_fwd_fused(a, st);
+        d->ctx->launches++;
+        TSB_CHECK_LAUNCH();
+        s.n = n;
+        s.valid = true;
+        return TSB_OK;
     }
     launch_deform_encode(pos, pos_stride, n, 1.0 / d->cfg.coord_scale, d->cfg.l_x, te, s.X, d->din, st);
     d->ctx->launches++;
@@ -2111,6 +2150,31 @@ int tsb_deform_create(tsb_ctx* ctx, const tsb_deform_config* cfg, tsb_deform** o
         tsb_deform_destroy(d);
         return rc;
     }
+    // fused forward: hidden width a multiple of 32, the encoding halves within the kernel's buffers
+    const int ex = 1 + 2 * cfg->l_x, et = 1 + 2 * cfg->l_t;
+    d->fused = d->L + 1 <= kMlpMaxLayers && d->width % 32 == 0 && 2 * ex <= 64 && ex + et <= 64;
+    if (d->fused) {
+        MlpLayout& lay = d->lay;
+        lay.layers = d->L + 1;
+        lay.total_chunks = 0;
+        int64_t off = 0;
+        for (int l = 0; l <= d->L; ++l) {
+            lay.rows[l] = d->rows[l];
+            lay.cols[l] = d->cols[l];
+            lay.cols_pad[l] = (d->cols[l] + 31) / 32 * 32;
+            lay.nt[l] = l == d->L ? 16 : d->width;
+            lay.chunks[l] = lay.cols_pad[l] / 32;
+            lay.w_off[l] = d->w_off[l];
+            lay.b_off[l] = d->b_off[l];
+            lay.chunk_off[l] = off;
+            off += (int64_t)lay.chunks[l] * lay.nt[l] * 32 * 8;
+            lay.total_chunks += lay.chunks[l];
+        }
+        if ((rc = dev_alloc(&d->wpack, (size_t)off))) {
+            tsb_deform_destroy(d);
+            return rc;
+        }
+    }
     cudaStream_t st = ctx->stream;
     cudaMemsetAsync(d->params, 0, sizeof(float) * d->P, st);
     cudaMemsetAsync(d->grads, 0, sizeof(float) * d->P, st);
@@ -2129,7 +2193,7 @@ void tsb_deform_destroy(tsb_deform* d) {
         dev_free(s.X);
         for (float*& h : s.H) dev_free(h);
     }
-    dev_free(d->delta_a); dev_free(d->delta_b); dev_free(d->io); dev_free(d->part);
+    dev_free(d->delta_a); dev_free(d->delta_b); dev_free(d->io); dev_free(d->part); dev_free(d->wpack);
     delete d;
 }
 
@@ -2140,6 +2204,7 @@ int tsb_deform_set_params(tsb_deform* d, int where, const float* flat) {
     TSB_CUDA(cudaSetDevice(d->ctx->device));
     TSB_CUDA(cudaMemcpyAsync(d->params, flat, sizeof(float) * d->P,
                              where == TSB_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, d->ctx->stream));
+    d->packed = false;
     TSB_CUDA(cudaStreamSynchronize(d->ctx->stream));
     return TSB_OK;
 }
@@ -2261,6 +2326,7 @@ int tsb_deform_debug_activation(tsb_deform* d, int slot, int layer, float* host_
 int tsb_deform_adam_step(tsb_deform* d, double lr, double beta1, double beta2, double eps) {
     if (!d) return fail(TSB_ERR_INVALID, "null network");
     d->step += 1;
+    d->packed = false;
     return tsb_adam_step_flat(d->ctx, TSB_DEVICE, d->params, d->grads, d->m, d->v, (size_t)d->P, d->step, lr, beta1,
                               beta2, eps);
 }

@@ -257,6 +257,32 @@ struct DeformEnc {
     int n;
     float v[64];
 };
+constexpr int kMlpMaxLayers = 9;  // 8 hidden + output
+struct MlpLayout {
+    int layers;       // hidden + 1
+    int total_chunks; // sum of chunks
+    int rows[kMlpMaxLayers], cols[kMlpMaxLayers], nt[kMlpMaxLayers], chunks[kMlpMaxLayers],
+        cols_pad[kMlpMaxLayers];
+    int64_t w_off[kMlpMaxLayers], b_off[kMlpMaxLayers], chunk_off[kMlpMaxLayers];  // floats / floats / bytes
+};
+struct MlpFwdArgs {
+    MlpLayout lay;
+    const float* pos;
+    int64_t pos_stride, n;
+    double inv_scale;
+    int l_x, din;
+    DeformEnc te;
+    const char* wpack;
+    const float* params;
+    float* X;  // encodings [n][ldx] (nullable)
+    int64_t ldx;
+    float* H[kMlpMaxLayers];  // hidden activations [n][ldh] (nullable)
+    int64_t ldh;
+    float* out;
+    int64_t out_stride;
+};
+void launch_pack_weights(const MlpLayout& lay, const float* params, char* out, cudaStream_t st);
+void launch_mlp_fwd_fused(const MlpFwdArgs& a, cudaStream_t st);
 void launch_deform_encode(const float* pos, int64_t pos_stride, int64_t n, double inv_scale, int l_x,
                           const DeformEnc& te, float* X, int64_t ldx, cudaStream_t st);
 void launch_deform_chain(const float* d_input, int64_t ldd, const float* X, int64_t ldx, int64_t n, double inv_scale,

@@ -459,14 +459,22 @@ __global__ void k_deform_chain(const float* __restrict__ d_input, int64_t ldd, c
     }
 }
 
-// db[o] += sum_i delta[i][o]
+// db[o] += sum_i delta[i][o]: each block sums a slab of rows with 8 independent loads in
+// flight per thread (fp32 partials of 8 rows, fp64 across), one atomic per column.
 __global__ void k_colsum(const float* __restrict__ delta, int64_t ld, int64_t n, int cols, float* __restrict__ db) {
     const int o = threadIdx.x;
     if (o >= cols) return;
     const int64_t per = (n + gridDim.x - 1) / gridDim.x;
     const int64_t i0 = blockIdx.x * per, i1 = min(n, i0 + per);
     double s = 0.0;
-    for (int64_t i = i0; i < i1; ++i) s += delta[i * ld + o];
+    int64_t i = i0;
+    for (; i + 8 <= i1; i += 8) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __ldg(delta + (i + j) * ld + o);
+        s += (double)(((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7])));
+    }
+    for (; i < i1; ++i) s += delta[i * ld + o];
     if (s != 0.0) atomicAdd(&db[o], (float)s);
 }
 
@@ -487,8 +495,302 @@ void launch_deform_chain(const float* d_input, int64_t ldd, const float* X, int6
 
 void launch_colsum(const float* delta, int64_t ld, int64_t n, int cols, float* db, cudaStream_t st) {
     if (n <= 0 || cols <= 0) return;
-    const int grid = (int)std::min<int64_t>((n + 1023) / 1024, 148 * 4);
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
     k_colsum<<<grid, ((cols + 31) / 32) * 32, 0, st>>>(delta, ld, n, cols, db);
+}
+
+}  // namespace tsb
+
+// ===========================================================================
+// Fused DeformNet forward: one persistent CTA per SM walks 128-row tiles; the
+// tile's activations never leave the SM.  Per tile: positional encoding -> A
+// (3xTF32 hi/lo, canonical K-major, shared memory) -> for every layer the
+// tensor core accumulates A x W_l^T in TMEM while the weights stream through a
+// 3-stage shared-memory ring by bulk copies (cp.async.bulk + mbarrier
+// complete_tx) from a pre-split, pre-laid-out copy (k_pack_weights); the
+// epilogue adds the bias, applies ReLU, optionally stores the activation for the
+// backward, and writes it back split into A for the next layer.  The last
+// layer's 3 outputs go to `out`.
+// ===========================================================================
+namespace tsb {
+namespace {
+constexpr int kMlpThreads = 512;  // 16 warps: the epilogue is latency-bound
+constexpr int kMlpStages = 3;
+constexpr uint32_t kMlpASbo = (128 / 4) * kCoreBytes;          // A tile: K extent 128 -> 4096 B per 8-row group
+constexpr uint32_t kMlpAHalf = 128 * 128 * 4;                  // hi (then lo) A buffer
+constexpr uint32_t kMlpStageBytes = 128 * kGemmKc * 4 * 2;     // largest weight chunk (N = 128, hi + lo)
+
+__device__ __forceinline__ uint32_t a_off(int r, int k) {
+    return (uint32_t)(r >> 3) * kMlpASbo + (uint32_t)(k >> 2) * kCoreBytes + (uint32_t)(r & 7) * 16u +
+           (uint32_t)(k & 3) * 4u;
+}
+
+// 3xTF32 split for operands held in shared memory: hi = tf32(x) (round to nearest), lo =
+// x - hi exactly (the tensor core truncates lo to tf32, an error below 2^-21 |x|), so hi +
+// lo reproduces x and the activations can be stored from the A buffer without a copy.
+__device__ __forceinline__ void split_exact(float x, float& hi, float& lo) {
+    uint32_t h;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+    hi = __uint_as_float(h);
+    lo = x - hi;
+}
+__device__ __forceinline__ void split_exact(double x, float& hi, float& lo) { split_exact((float)x, hi, lo); }
+
+// rows m0 .. m0+127 (< n), columns [0, ncols) of the A tile -> dst[m * ld + c], coalesced:
+// per iteration a warp covers 8 rows x 4 consecutive column quads (no index division).
+__device__ __forceinline__ void store_rows(const char* A_hi, const char* A_lo, float* dst, int64_t ld, int64_t m0,
+                                           int64_t n, int ncols) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int r8 = lane & 7, qi = lane >> 3, nq = ncols / 4;
+    for (int rg = warp; rg < 16; rg += nwarps) {
+        const int r = rg * 8 + r8;
+        const int64_t m = m0 + r;
+        if (m >= n) continue;
+        float* row = dst + m * ld;
+        const bool al = (((uintptr_t)row) & 15) == 0;
+        for (int q = qi; q < nq; q += 4) {
+            const float4 h = *reinterpret_cast<const float4*>(A_hi + a_off(r, 4 * q));
+            const float4 l = *reinterpret_cast<const float4*>(A_lo + a_off(r, 4 * q));
+            const float4 v = make_float4(h.x + l.x, h.y + l.y, h.z + l.z, h.w + l.w);
+            if (al) {
+                *reinterpret_cast<float4*>(row + 4 * q) = v;
+            } else {
+                row[4 * q] = v.x; row[4 * q + 1] = v.y; row[4 * q + 2] = v.z; row[4 * q + 3] = v.w;
+            }
+        }
+        if (qi == 0)
+            for (int c = 4 * nq; c < ncols; ++c)
+                row[c] = *reinterpret_cast<const float*>(A_hi + a_off(r, c)) +
+                         *reinterpret_cast<const float*>(A_lo + a_off(r, c));
+    }
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+        : "memory");
+}
+}  // namespace
+
+// W_l (rows x cols, row-major, inside the flat parameters) -> per 32-wide K chunk a
+// block [hi | lo] of NT_l x 32 tf32 in the canonical K-major layout (zero padded).
+__global__ void k_pack_weights(MlpLayout lay, const float* __restrict__ params, char* __restrict__ out) {
+    const int l = blockIdx.y;
+    if (l >= lay.layers) return;
+    const int nt = lay.nt[l], rows = lay.rows[l], cols = lay.cols[l];
+    const int nchunks = lay.chunks[l];
+    const float* W = params + lay.w_off[l];
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nchunks * nt * kGemmKc;
+         idx += gridDim.x * blockDim.x) {
+        const int c = idx / (nt * kGemmKc), rem = idx - c * nt * kGemmKc;
+        const int n = rem / kGemmKc, k = rem - n * kGemmKc, gk = c * kGemmKc + k;
+        const float w = (n < rows && gk < cols) ? W[(int64_t)n * cols + gk] : 0.f;
+        float h, lo;
+        split_tf32(w, h, lo);
+        char* blk = out + lay.chunk_off[l] + (int64_t)c * nt * kGemmKc * 8;
+        const uint32_t o = core_off(n, k);
+        *reinterpret_cast<float*>(blk + o) = h;
+        *reinterpret_cast<float*>(blk + (int64_t)nt * kGemmKc * 4 + o) = lo;
+    }
+}
+
+__global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_fwd_fused(MlpFwdArgs a) {
+    extern __shared__ __align__(1024) char smem[];
+    __shared__ __align__(8) uint64_t mb_full[kMlpStages], mb_empty[kMlpStages], mb_layer;
+    __shared__ uint32_t tmem_base_s;
+    char* A_hi = smem;
+    char* A_lo = smem + kMlpAHalf;
+    char* ring = smem + 2 * kMlpAHalf;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const MlpLayout& lay = a.lay;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tmem_base_s))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < kMlpStages; ++i) {
+            mbar_init(&mb_full[i], 1);
+            mbar_init(&mb_empty[i], 1);
+        }
+        mbar_init(&mb_layer, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    const uint32_t tmem = tmem_base_s;
+    const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const int ntiles = (int)((a.n + 127) / 128);
+    const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const uint32_t total = (uint32_t)my_tiles * (uint32_t)lay.total_chunks;  // weight chunks this CTA consumes
+
+    // chunk q of this CTA -> (layer, chunk in layer)
+    auto chunk_src = [&](uint32_t q, uint32_t& bytes) -> const char* {
+        const uint32_t local = q % (uint32_t)lay.total_chunks;
+        int l = 0;
+        uint32_t base = 0;
+        while (local >= base + (uint32_t)lay.chunks[l]) {
+            base += lay.chunks[l];
+            ++l;
+        }
+        bytes = (uint32_t)lay.nt[l] * kGemmKc * 8u;
+        return a.wpack + lay.chunk_off[l] + (int64_t)(local - base) * bytes;
+    };
+    auto issue_copy = [&](uint32_t q) {  // thread 0 only
+        if (q >= total) return;
+        const int st = (int)(q % kMlpStages);
+        if (q >= (uint32_t)kMlpStages) mbar_wait(&mb_empty[st], ((q / kMlpStages) - 1) & 1u);
+        uint32_t bytes;
+        const char* src = chunk_src(q, bytes);
+        bulk_g2s(ring + (size_t)st * kMlpStageBytes, src, bytes, &mb_full[st]);
+    };
+    if (tid == 0)
+        for (uint32_t q = 0; q < (uint32_t)kMlpStages - 1; ++q) issue_copy(q);
+
+    uint32_t q = 0;          // next chunk to consume
+    uint32_t lphase = 0;     // mb_layer completions
+    const int ex = 1 + 2 * a.l_x;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t m0 = (int64_t)tile * 128;
+        // ---- positional encoding of the tile's rows (four threads per row: x, y, z, time + padding) ----
+        {
+            const int r = tid & 127, part = tid >> 7;
+            const int64_t m = m0 + r;
+            const int kb = part * ex;
+            if (part < 3) {
+                const double v = m < a.n ? (double)a.pos[m * a.pos_stride + part] * a.inv_scale : 0.0;
+                float h, lo;
+                split_exact(v, h, lo);
+                *reinterpret_cast<float*>(A_hi + a_off(r, kb)) = h;
+                *reinterpret_cast<float*>(A_lo + a_off(r, kb)) = lo;
+                double f = v;
+                for (int l = 0; l < a.l_x; ++l, f *= 2.0) {
+                    double sn, co;
+                    sincospi(f, &sn, &co);
+                    split_exact(sn, h, lo);
+                    *reinterpret_cast<float*>(A_hi + a_off(r, kb + 1 + 2 * l)) = h;
+                    *reinterpret_cast<float*>(A_lo + a_off(r, kb + 1 + 2 * l)) = lo;
+                    split_exact(co, h, lo);
+                    *reinterpret_cast<float*>(A_hi + a_off(r, kb + 2 + 2 * l)) = h;
+                    *reinterpret_cast<float*>(A_lo + a_off(r, kb + 2 + 2 * l)) = lo;
+                }
+            } else {
+                for (int k = kb; k < lay.cols_pad[0]; ++k) {
+                    const float x = k - kb < a.te.n ? a.te.v[k - kb] : 0.f;
+                    float h, lo;
+                    split_exact(x, h, lo);
+                    *reinterpret_cast<float*>(A_hi + a_off(r, k)) = h;
+                    *reinterpret_cast<float*>(A_lo + a_off(r, k)) = lo;
+                }
+            }
+        }
+        fence_async_smem();
+        __syncthreads();
+        if (a.X) {
+            store_rows(A_hi, A_lo, a.X, a.ldx, m0, a.n, a.din);
+            __syncthreads();  // layer 0's epilogue overwrites A
+        }
+
+        for (int l = 0; l < lay.layers; ++l) {
+            const int nt = lay.nt[l];
+            if (tid == 0) {
+                tc_after_sync();
+                const uint32_t idesc = idesc_tf32(128, nt);
+                const uint32_t ah = smem_u32(A_hi), al = smem_u32(A_lo);
+                for (int c = 0; c < lay.chunks[l]; ++c, ++q) {
+                    const int st = (int)(q % kMlpStages);
+                    mbar_wait(&mb_full[st], (q / kMlpStages) & 1u);
+                    const uint32_t bh = smem_u32(ring + (size_t)st * kMlpStageBytes);
+                    const uint32_t bl = bh + (uint32_t)nt * kGemmKc * 4;
+#pragma unroll
+                    for (int s = 0; s < kGemmKc / 8; ++s) {
+                        const uint32_t aoff = (uint32_t)(c * (kGemmKc / 4) + 2 * s) * kCoreBytes;
+                        const uint32_t boff = (uint32_t)(2 * s) * kCoreBytes;
+                        const uint64_t dah = umma_desc(ah + aoff, kCoreBytes, kMlpASbo);
+                        const uint64_t dal = umma_desc(al + aoff, kCoreBytes, kMlpASbo);
+                        const uint64_t dbh = umma_desc(bh + boff, kCoreBytes, kGroupBytes);
+                        const uint64_t dbl = umma_desc(bl + boff, kCoreBytes, kGroupBytes);
+                        mma_tf32(tmem, dah, dbh, idesc, (c > 0 || s > 0) ? 1u : 0u);
+                        mma_tf32(tmem, dah, dbl, idesc, 1u);
+                        mma_tf32(tmem, dal, dbh, idesc, 1u);
+                    }
+                    mma_commit(&mb_empty[st]);
+                    issue_copy(q + kMlpStages - 1);
+                }
+                mma_commit(&mb_layer);
+            } else if (tid != 0) {
+                q += lay.chunks[l];
+            }
+            mbar_wait(&mb_layer, lphase & 1u);
+            ++lphase;
+            tc_after_sync();
+            // ---- epilogue: bias, ReLU; split back into A for the next layer ----
+            const int r = (warp & 3) * 32 + lane;
+            const int64_t m = m0 + r;
+            const float* bias = a.params + lay.b_off[l];
+            const bool hidden = l + 1 < lay.layers;
+            if (hidden) {
+                const int q4 = nt / 4, c0 = (warp >> 2) * q4;
+                for (int cc = 0; cc < q4; cc += 16) {
+                    uint32_t v[16];
+                    tmem_ld16(tl + (uint32_t)(c0 + cc), v);
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4) {
+                        const int col = c0 + cc + j;
+                        float4 x;
+                        x.x = fmaxf(__uint_as_float(v[j]) + __ldg(bias + col), 0.f);
+                        x.y = fmaxf(__uint_as_float(v[j + 1]) + __ldg(bias + col + 1), 0.f);
+                        x.z = fmaxf(__uint_as_float(v[j + 2]) + __ldg(bias + col + 2), 0.f);
+                        x.w = fmaxf(__uint_as_float(v[j + 3]) + __ldg(bias + col + 3), 0.f);
+                        float4 h, lo;
+                        split_exact(x.x, h.x, lo.x);
+                        split_exact(x.y, h.y, lo.y);
+                        split_exact(x.z, h.z, lo.z);
+                        split_exact(x.w, h.w, lo.w);
+                        *reinterpret_cast<float4*>(A_hi + a_off(r, col)) = h;
+                        *reinterpret_cast<float4*>(A_lo + a_off(r, col)) = lo;
+                    }
+                }
+            } else if (warp < 4) {
+                uint32_t v[16];
+                tmem_ld16(tl, v);
+                if (m < a.n)
+                    for (int j = 0; j < 3; ++j) a.out[m * a.out_stride + j] = __uint_as_float(v[j]) + __ldg(bias + j);
+            }
+            fence_async_smem();
+            tc_before_sync();
+            __syncthreads();
+            // the activation for the backward: hi + lo is the fp32 value exactly; coalesced rows
+            if (hidden && a.H[l]) {
+                store_rows(A_hi, A_lo, a.H[l], a.ldh, m0, a.n, nt);
+                __syncthreads();  // the next layer's epilogue overwrites A
+            }
+        }
+    }
+    tc_before_sync();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
+}
+
+size_t mlp_fused_smem_bytes() { return 2 * (size_t)kMlpAHalf + (size_t)kMlpStages * kMlpStageBytes; }
+
+void launch_pack_weights(const MlpLayout& lay, const float* params, char* out, cudaStream_t st) {
+    k_pack_weights<<<dim3(64, lay.layers), 256, 0, st>>>(lay, params, out);
+}
+
+void launch_mlp_fwd_fused(const MlpFwdArgs& a, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_mlp_fwd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mlp_fused_smem_bytes());
+        attr = true;
+    }
+    if (a.n <= 0) return;
+    const int ntiles = (int)((a.n + 127) / 128);
+    k_mlp_fwd_fused<<<std::min(ntiles, 148), kMlpThreads, mlp_fused_smem_bytes(), st>>>(a);
 }
 
 }  // namespace tsb
