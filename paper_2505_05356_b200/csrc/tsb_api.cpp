@@ -1233,7 +1233,7 @@ int record_forward(tsb_pass* p, cudaStream_t st, bool loss, const ChW& chw, bool
             cudaGraph_t body = nullptr;
             TSB_CUDA(cudaStreamEndCapture(cs, &body));
         } else {
-            fixed += nseg > 0 ? 5 : 1;
+            fixed += bin_chunk_kernels(B) + 1;
         }
     }
     p->nchunks = nplanned;
@@ -1377,7 +1377,7 @@ int settle(tsb_pass* p) {
         p->pending = false;
         const int32_t* hc = (const int32_t*)((const char*)p->pinned + 2048);
         p->V = hc[0];
-        if (p->count_live) p->ctx->launches += 5 * (int64_t)hc[7];  // bodies of live chunks (graph)
+        if (p->count_live) p->ctx->launches += (int64_t)hc[7];  // kernels of live chunk bodies (graph)
         p->count_live = false;
         const int ab = hc[2];
         if (!ab) return TSB_OK;

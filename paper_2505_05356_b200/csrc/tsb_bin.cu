@@ -292,7 +292,9 @@ __global__ void __launch_bounds__(1024) k_bin_scan_segments(BinK B) {
 }
 
 // Exclusive scan of tile lengths -> this chunk's ranges; advances the running
-// list offset.  One block.
+// list offset.  One block.  SEGS: also does k_bin_scan_segments' per-tile scan over
+// the chunk's segments first (small chunks: one launch instead of two).
+template <bool SEGS>
 __global__ void k_bin_scan_tiles(BinK B) {
     __shared__ uint32_t warp_sums[32];
     __shared__ uint32_t s_carry;
@@ -306,6 +308,19 @@ __global__ void k_bin_scan_tiles(BinK B) {
             B.ranges[t] = make_uint4(base, 0u, cum, 1u);
         }
         return;
+    }
+    if (SEGS) {
+        for (int t = tid; t < B.ntiles; t += blockDim.x) {
+            uint32_t off = 0;
+            for (int sg = 0; sg < B.nseg; ++sg) {
+                uint32_t* h = B.hist + (size_t)sg * B.ntiles + t;
+                const uint32_t c = *h;
+                *h = off;
+                off += c;
+            }
+            B.tile_len[t] = off;
+        }
+        __syncthreads();
     }
     for (int t0 = 0; t0 < B.ntiles; t0 += blockDim.x) {
         const int t = t0 + tid;
@@ -626,11 +641,11 @@ __global__ void __launch_bounds__(kSegThreads) k_bin_emit_seg(BinK B, int cap) {
 // Graph gate of a depth chunk (c >= 1): the chunk's conditional node runs its
 // binning + raster body only when the chunk is live; a dead chunk's ranges are
 // written here exactly as k_bin_scan_tiles would (empty, every tile skipped).
-__global__ void k_chunk_gate(BinK B, cudaGraphConditionalHandle h, int32_t* live_chunks) {
+__global__ void k_chunk_gate(BinK B, cudaGraphConditionalHandle h, int32_t* body_launches, int nkern) {
     const bool live = chunk_live(B);
     if (threadIdx.x == 0) {
         cudaGraphSetConditional(h, live ? 1u : 0u);
-        if (live) atomicAdd(live_chunks, 1);
+        if (live) atomicAdd(body_launches, nkern);
     }
     if (live) return;
     const uint32_t base = *B.list_off;
@@ -640,9 +655,11 @@ __global__ void k_chunk_gate(BinK B, cudaGraphConditionalHandle h, int32_t* live
     }
 }
 
-void launch_chunk_gate(const BinK& B, cudaGraphConditionalHandle h, int32_t* live_chunks, cudaStream_t st) {
-    k_chunk_gate<<<1, 1024, 0, st>>>(B, h, live_chunks);
+void launch_chunk_gate(const BinK& B, cudaGraphConditionalHandle h, int32_t* body_launches, cudaStream_t st) {
+    k_chunk_gate<<<1, 1024, 0, st>>>(B, h, body_launches, bin_chunk_kernels(B) + 1);
 }
+
+int bin_chunk_kernels(const BinK& B) { return B.nseg <= 0 ? 0 : (B.nseg <= 64 ? 3 : 4); }
 
 // Kernel attributes (outside any stream capture: called when a pass is created).
 void bin_init() {
@@ -692,8 +709,12 @@ void launch_bin_count(const BinK& B, cudaStream_t st) {
 }
 
 void launch_bin_scan(const BinK& B, cudaStream_t st) {
+    if (B.nseg <= 64) {  // small depth chunk: one block does both scans
+        k_bin_scan_tiles<true><<<1, 1024, 0, st>>>(B);
+        return;
+    }
     k_bin_scan_segments<<<(B.ntiles + 31) / 32, 1024, 0, st>>>(B);
-    k_bin_scan_tiles<<<1, 1024, 0, st>>>(B);
+    k_bin_scan_tiles<false><<<1, 1024, 0, st>>>(B);
 }
 
 void launch_bin_emit(const BinK& B, cudaStream_t st) {

@@ -202,7 +202,7 @@ void launch_param_cache(const SceneK& S, double* cov6, double* opac, cudaStream_
 size_t radix_sort_scratch_words(int n);
 int radix_sort32(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch,
                  cudaStream_t st);
-// 3 passes over keys compressed to 23 bits with the device-side key range
+// 3 passes over keys compressed to 24 bits with the device-side key range
 // (range[0] = min, range[1] = max); result in (keys_b, vals_b).
 int radix_sort24(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch,
                  const uint32_t* range, cudaStream_t st);
@@ -227,7 +227,9 @@ void launch_fixup_loss(const PixK& px, int W, int H, int nf, const FrameDev* fd,
                        double* loss_extra, cudaStream_t st);
 // CUDA-graph gate of depth chunk c >= 1: sets the chunk's IF-node condition to its
 // liveness (tsb_bin.cu chunk_live); a dead chunk's ranges are written empty here.
-void launch_chunk_gate(const BinK& B, cudaGraphConditionalHandle h, int32_t* live_chunks, cudaStream_t st);
+// (the gate adds the chunk body's kernel count to *body_launches when live)
+void launch_chunk_gate(const BinK& B, cudaGraphConditionalHandle h, int32_t* body_launches, cudaStream_t st);
+int bin_chunk_kernels(const BinK& B);  // binning kernels of one depth chunk
 void launch_raster_bwd(const RecK& rec, const uint4* ranges_all, int nchunks, const uint32_t* tile_vals,
                        const OptK& O, int W, int H, int nf, const float* dpsi, PixK px, const UpK& up,
                        float* screen, int scap, double* bg_part, cudaStream_t st);

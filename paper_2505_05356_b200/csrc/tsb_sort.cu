@@ -43,14 +43,15 @@ __device__ __forceinline__ unsigned peers8(uint32_t d, bool valid) {
 // All four digit histograms in one pass.  Per-warp sub-histograms; the lanes that
 // share lane 0's digit (the common case for the high, low-entropy digits) are
 // counted with one atomic by lane 0, the others add their own.
-// Keys are compressed to 23 significant bits: k' = (k - kmin) >> shift, with kmin and
+// Keys are compressed to 24 bits: k' = (k - kmin) >> shift (< 0xffffff), with kmin and
 // shift from the key range the preprocess recorded (range[0] = min, range[1] = max of
 // the keys that are not 0xffffffff).  Culled keys (0xffffffff) map to 0xffffff.
 __device__ __forceinline__ void key_xform(const uint32_t* range, uint32_t& kmin, uint32_t& shift) {
     kmin = range[0];
     const uint32_t span = range[1] >= range[0] ? range[1] - range[0] : 0u;
     const int bits = span ? 32 - __clz(span) : 0;
-    shift = bits > 23 ? (uint32_t)(bits - 23) : 0u;  // visible keys < 2^23 < the culled sentinel
+    shift = bits > 24 ? (uint32_t)(bits - 24) : 0u;
+    if ((span >> shift) >= 0xffffffu) ++shift;  // visible keys stay below the culled sentinel
 }
 __device__ __forceinline__ uint32_t key24(uint32_t k, uint32_t kmin, uint32_t shift) {
     return k == 0xffffffffu ? 0xffffffu : ((k - kmin) >> shift);
