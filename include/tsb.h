@@ -211,6 +211,11 @@ int tsb_pass_num_keys(tsb_pass* p, int64_t* out);
 int tsb_pass_forward(tsb_pass* p);
 int tsb_pass_forward_loss(tsb_pass* p, int where, const float* target,
                           const double* channel_weight /* 4*n_freq */, double* loss_out /* may be NULL: no sync */);
+/* The trainer's full image loss per quad channel c (losses.cpp:148-166, trainer.cpp:210-219):
+ * sum_c channel_weight[c] * [(1 - ssim_mix) mse_c + ssim_mix (1 - SSIM_c)], SSIM with the
+ * reference's 11-tap Gaussian window; d_quad for the backward.  ssim_mix 0 = forward_loss. */
+int tsb_pass_forward_image_loss(tsb_pass* p, int where, const float* target, const double* channel_weight,
+                                double ssim_mix, double* loss_out);
 
 enum {
     TSB_OUT_QUAD = 0,      /* [4*n_freq][H][W] f32 */

@@ -109,6 +109,7 @@ SIGNATURES = {
     "tsb_pass_num_keys": (C.c_int, [_vp, _lp]),
     "tsb_pass_forward": (C.c_int, [_vp]),
     "tsb_pass_forward_loss": (C.c_int, [_vp, C.c_int, _vp, _dp, _dp]),
+    "tsb_pass_forward_image_loss": (C.c_int, [_vp, C.c_int, _vp, _dp, C.c_double, _dp]),
     "tsb_pass_output": (C.c_int, [_vp, C.c_int, C.POINTER(_vp), C.POINTER(C.c_size_t)]),
     "tsb_pass_download": (C.c_int, [_vp, C.c_int, _vp, C.c_size_t]),
     "tsb_pass_download_async": (C.c_int, [_vp, C.c_int, _vp, C.c_size_t]),

@@ -201,6 +201,12 @@ struct tsb_pass {
     bool pend_loss = false, pend_bwd = false;
     const float* pend_target = nullptr;
     ChW pend_chw{};
+    double pend_mix = 0.0;
+    double pend_chw_full[8] = {0};  // the loss's channel weights before the (1 - lambda) mse scaling
+    double mix = 0.0;          // SSIM weight of the current forward's image loss
+    double* ssim_g = nullptr;  // SSIM gradient planes [4 * nf][3][npx]
+    double* ssim_part = nullptr;
+    int ssim_cap_px = 0, ssim_cap_blocks = 0;
     UpK pend_up{};
     struct Download {
         int which;
@@ -737,6 +743,7 @@ int tsb_pass_create(tsb_ctx* ctx, tsb_pass** out) {
         return rc;
     }
     bin_init();
+    ssim_init();
     ctx->passes.push_back(p);
     *out = p;
     return TSB_OK;
@@ -946,6 +953,7 @@ void tsb_pass_destroy(tsb_pass* p) {
     dev_free(p->vals); dev_free(p->block_done); dev_free(p->tile_blocks_done);
     dev_free(p->counters); dev_free(p->list_off); dev_free(p->fx_work_n);
     dev_free(p->loss_part); dev_free(p->bg_part); dev_free(p->loss_dev); dev_free(p->chw);
+    dev_free(p->ssim_g); dev_free(p->ssim_part);
     if (p->pinned) cudaFreeHost(p->pinned);
     if (p->done_ev) cudaEventDestroy(p->done_ev);
     for (auto& fg : p->fwd)
@@ -1262,6 +1270,26 @@ int record_forward(tsb_pass* p, cudaStream_t st, bool loss, const ChW& chw, bool
         launch_fixup_loss(px, p->W, p->H, p->nf, fd, chw, p->loss_dev, st);
         launch_reduce_partials(p->loss_part, p->nblocks, 1, p->loss_dev, 1.0 / ((double)p->W * p->H), px.abort, st);
         fixed += 2;
+        if (p->mix > 0.0) {  // lambda (1 - SSIM) per weighted quad channel (losses.cpp:148-166)
+            SsimArgs sa{};
+            const double npx = (double)p->W * p->H;
+            for (int c = 0; c < 4 * p->nf; ++c) {
+                const double w = p->pend_chw_full[c];
+                if (w == 0.0) continue;
+                sa.chans[sa.nz] = c;
+                sa.scale[sa.nz] = -w * p->mix / npx;
+                sa.lam_w[sa.nz] = w * p->mix;
+                ++sa.nz;
+            }
+            sa.g = p->ssim_g;
+            sa.part = p->ssim_part;
+            sa.d_quad = p->d_quad;
+            sa.loss = p->loss_dev;
+            sa.abort = px.abort;
+            sa.fd = fd;
+            launch_ssim(p->out, p->W, p->H, sa, st);
+            fixed += 3;
+        }
     }
     TSB_CHECK_LAUNCH();
     int32_t* hc = (int32_t*)((char*)p->pinned + 2048);
@@ -1287,6 +1315,10 @@ std::string forward_key(tsb_pass* p, bool loss, const ChW& chw) {
     add(&p->cam, sizeof p->cam);
     add(&p->opt, sizeof p->opt);
     add(&chw, sizeof chw);
+    add(&p->mix, sizeof p->mix);
+    add(p->pend_chw_full, sizeof p->pend_chw_full);
+    const void* sptrs[] = {p->ssim_g, p->ssim_part};
+    add(sptrs, sizeof sptrs);
     const void* prep_ptrs[] = {p->key_a, p->key_b, p->depth64, p->gidx_a, p->gidx_b, p->touched, p->sort_scratch};
     add(prep_ptrs, sizeof prep_ptrs);
     const int ints[] = {p->W, p->H, p->nf, (int)p->channels, p->ntiles, p->nblocks, (int)p->vals_cap, loss ? 1 : 0,
@@ -1426,12 +1458,23 @@ int run_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw) {
 
 int tsb_pass_forward(tsb_pass* p) {
     if (!p) return fail(TSB_ERR_INVALID, "null pass");
+    if (p->pending) {
+        int rc0 = settle(p);
+        if (rc0) return rc0;
+    }
+    p->mix = 0.0;
     return run_forward(p, nullptr, false, ChW{});
 }
 
 int tsb_pass_forward_loss(tsb_pass* p, int where, const float* target, const double* channel_weight,
                           double* loss_out) {
+    return tsb_pass_forward_image_loss(p, where, target, channel_weight, 0.0, loss_out);
+}
+
+int tsb_pass_forward_image_loss(tsb_pass* p, int where, const float* target, const double* channel_weight,
+                                double ssim_mix, double* loss_out) {
     if (!p || !target || !channel_weight) return fail(TSB_ERR_INVALID, "tsb_pass_forward_loss: null argument");
+    if (!(ssim_mix >= 0.0 && ssim_mix <= 1.0)) return fail(TSB_ERR_INVALID, "forward_loss: ssim_mix must be in [0, 1]");
     if (!p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
     TSB_CUDA(cudaSetDevice(p->ctx->device));
     cudaStream_t st = p->stream;
@@ -1444,7 +1487,26 @@ int tsb_pass_forward_loss(tsb_pass* p, int where, const float* target, const dou
         return fail(TSB_ERR_INVALID, "bad memory kind");
     }
     ChW w{};
-    for (int c = 0; c < 4 * p->nf; ++c) w.w[c] = (float)channel_weight[c];
+    for (int c = 0; c < 4 * p->nf; ++c) w.w[c] = (float)(channel_weight[c] * (1.0 - ssim_mix));
+    if (p->pending) {  // a second forward of the same prepared frame
+        int rc0 = settle(p);
+        if (rc0) return rc0;
+    }
+    for (int c = 0; c < 8; ++c) p->pend_chw_full[c] = c < 4 * p->nf ? channel_weight[c] : 0.0;
+    p->mix = ssim_mix;
+    if (ssim_mix > 0.0) {
+        const int npx = p->W * p->H, nb = ssim_blocks(p->W, p->H);
+        if (npx > p->ssim_cap_px || nb > p->ssim_cap_blocks) {
+            dev_free(p->ssim_g);
+            dev_free(p->ssim_part);
+            p->ssim_cap_px = p->ssim_cap_blocks = 0;
+            int rc1;
+            if ((rc1 = dev_alloc(&p->ssim_g, (size_t)8 * 3 * npx)) || (rc1 = dev_alloc(&p->ssim_part, (size_t)8 * nb)))
+                return rc1;
+            p->ssim_cap_px = npx;
+            p->ssim_cap_blocks = nb;
+        }
+    }
     int rc = run_forward(p, dt, true, w);
     if (rc) return rc;
     if (loss_out) {

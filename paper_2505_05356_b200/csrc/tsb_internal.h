@@ -290,6 +290,22 @@ void launch_deform_encode(const float* pos, int64_t pos_stride, int64_t n, doubl
 void launch_deform_chain(const float* d_input, int64_t ldd, const float* X, int64_t ldx, int64_t n, double inv_scale,
                          int l_x, float* d_pos, int64_t dpos_stride, bool accumulate, cudaStream_t st);
 void launch_colsum(const float* delta, int64_t ld, int64_t n, int cols, float* db, cudaStream_t st);
+// tsb_ssim.cu: lambda's part of the trainer image loss for the quad channels.
+struct SsimArgs {
+    int nz;                  // channels with a non-zero SSIM weight
+    int chans[8];            // their quad channel indices
+    double scale[8];         // d_quad[c] += scale * dS/dx:  -w_c lambda / npx
+    double lam_w[8];         // loss += lam_w (1 - mean S):  w_c lambda
+    double* g;               // [nz][3][H][W] gradient planes
+    double* part;            // [nz][blocks] partial sums of S
+    float* d_quad;
+    double* loss;
+    const int32_t* abort;
+    const FrameDev* fd;      // the frame's target (fd->target)
+};
+void ssim_init();  // window constants (outside any stream capture)
+int ssim_blocks(int W, int H);
+void launch_ssim(const float* x, int W, int H, const SsimArgs& a, cudaStream_t st);
 // tsb_optim.cu
 void launch_pack_params(float4* dst, const float* src, int n, int comps, int comp0, int ncomp_dst,
                         cudaStream_t st);

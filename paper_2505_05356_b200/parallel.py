@@ -34,13 +34,14 @@ class FrameShardedTrainer:
     def __init__(self, ctx: Context, scene: GaussianScene, camera: CameraModel,
                  options: Optional[RenderOptions] = None, lr: Optional[LrTable] = None,
                  adam: AdamParams = AdamParams(), comm: Optional[Comm] = None, rank: int = 0, world: int = 1,
-                 channel_weight: Optional[Sequence[float]] = None, passes: int = 3):
+                 channel_weight: Optional[Sequence[float]] = None, passes: int = 3, ssim_mix: float = 0.0):
         self.ctx, self.scene, self.camera = ctx, scene, camera
         self.options = options or RenderOptions()
         self.lr = lr or LrTable()
         self.adam = adam
         self.comm, self.rank, self.world = comm, rank, world
         self.channel_weight = list(channel_weight or [0.25] * (4 * scene.n_freq))
+        self.ssim_mix = ssim_mix  # LossWeights::ssim_mix (trainer.hpp:49; BASELINE configs use 0)
         # render passes (one stream each) rotate over frames: frame i's backward overlaps the
         # preprocess/sort/binning of the next frames; nothing waits for the device until a pass
         # is reused (it settles its previous frame) and at the allreduce / Adam step.  Gradient
@@ -56,9 +57,9 @@ class FrameShardedTrainer:
             rp.prepare(self.scene, self.camera, self.options, frames[i])
             t = target(i)
             if isinstance(t, int):
-                rp.forward_loss(None, self.channel_weight, sync=False, device_ptr=t)
+                rp.forward_loss(None, self.channel_weight, sync=False, device_ptr=t, ssim_mix=self.ssim_mix)
             else:
-                rp.forward_loss(t, self.channel_weight, sync=False)
+                rp.forward_loss(t, self.channel_weight, sync=False, ssim_mix=self.ssim_mix)
             rp.backward()
         if self.comm is not None and self.world > 1:
             self.scene.allreduce_grads(self.comm)

@@ -375,22 +375,24 @@ class RenderPass:
         check(lib().tsb_pass_forward(self._h))
         return self
 
-    def forward_loss(self, target, channel_weight=None, sync=True, device_ptr=None):
-        """Forward + fused L2 loss (sum_c w_c mse_c; reference trainer weight quad/4 per
-        channel, trainer.cpp:210-219).  target: host array (4*n_freq, H, W) or a device pointer."""
+    def forward_loss(self, target, channel_weight=None, sync=True, device_ptr=None, ssim_mix: float = 0.0):
+        """Forward + the trainer's image loss per quad channel, sum_c w_c [(1 - ssim_mix) mse_c +
+        ssim_mix (1 - SSIM_c)] (losses.cpp:148-166; weight quad/4 per channel, trainer.cpp:210-219;
+        ssim_mix 0 = pure L2, fused into the raster epilogue).  target: host array
+        (4*n_freq, H, W) or a device pointer."""
         nf = self.scene.n_freq
         if channel_weight is None:
             channel_weight = [0.25] * (4 * nf)
         w = (C.c_double * 8)(*([float(x) for x in channel_weight] + [0.0] * (8 - len(channel_weight))))
         loss = C.c_double()
         if device_ptr is not None:
-            check(lib().tsb_pass_forward_loss(self._h, _abi.TSB_DEVICE, C.c_void_p(device_ptr), w,
-                                              C.byref(loss) if sync else None))
+            check(lib().tsb_pass_forward_image_loss(self._h, _abi.TSB_DEVICE, C.c_void_p(device_ptr), w,
+                                                    float(ssim_mix), C.byref(loss) if sync else None))
         else:
             t = np.ascontiguousarray(np.asarray(target, dtype=np.float32))
             self._target_keep = t
-            check(lib().tsb_pass_forward_loss(self._h, _abi.TSB_HOST, t.ctypes.data, w,
-                                              C.byref(loss) if sync else None))
+            check(lib().tsb_pass_forward_image_loss(self._h, _abi.TSB_HOST, t.ctypes.data, w, float(ssim_mix),
+                                                    C.byref(loss) if sync else None))
         return loss.value if sync else None
 
     def backward(self, d_quad=None, device_ptr=None):

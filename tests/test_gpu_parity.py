@@ -533,3 +533,40 @@ def test_list_overflow_abort_and_redo(tsb, ctx):
     for k in ga:  # gradient atomics may add in a different order: summation-order tolerance
         x, y = np.asarray(ga[k], np.float64), np.asarray(gb[k], np.float64)
         assert np.abs(x - y).max() <= 1e-5 * max(np.abs(x).max(), 1e-30), k
+
+
+def test_image_loss_with_ssim_mix(tsb, ctx):
+    """The trainer's default image loss (losses.cpp:148-166, ssim_mix 0.2; trainer.cpp:210-219):
+    loss (1e-5 rel), the upstream d_quad it produces (normwise 1e-5) and the parameter
+    gradients through the backward (1e-3) vs the oracle."""
+    from oracle import losses as ol
+    from paper_2505_05356_b200 import synthetic
+    cfg = synthetic.config("c1", n=20_000)
+    cam = synthetic.camera(320, 240, 262.5)
+    g, tgt, frame, tof = cfg.scene, cfg.target, cfg.frames[0], cfg.tof
+    opts = tsb.RenderOptions(counts=True)
+    tscene = gpu_scene(tsb, ctx, tgt, tof)
+    rp = tsb.RenderPass(ctx).prepare(tscene, cam, opts, frame).forward()
+    target = rp.outputs()["quad"].astype(np.float32)
+    target = (target + np.random.default_rng(5).normal(0.0, 0.01, target.shape)).astype(np.float32)
+    scene = gpu_scene(tsb, ctx, g, tof)
+    rp.prepare(scene, cam, opts, frame)
+    mix = 0.2
+    loss = rp.forward_loss(target, [0.25] * 4, ssim_mix=mix)
+    d_quad = rp.download(tsb._abi.OUT_D_QUAD, shape=(4, cam.height, cam.width))
+    rp.backward()
+    gr = scene.grads()
+    op = orc.OraclePass(oracle_scene(g, frame, tof), cam, opts)
+    ref = op.forward()
+    oloss, od = 0.0, np.zeros((4, cam.height, cam.width))
+    for m in range(4):
+        v, d = ol.image_loss(ref["quad"][m][None], target[m][None].astype(np.float64), mix, True)
+        oloss += 0.25 * v
+        od[m] = 0.25 * d[0]
+    assert loss == pytest.approx(oloss, rel=1e-5)
+    assert np.abs(d_quad - od).max() <= 1e-5 * np.abs(od).max()
+    og = op.backward(d_quad=od)
+    for name, a, b in (("d_position", gr["d_position"], og["d_position"]),
+                       ("d_opacity_logit", gr["d_opacity_logit"], og["d_opacity_logit"]),
+                       ("d_log_scale", gr["d_log_scale"], og["d_log_scale"])):
+        assert rel_err(a, b, 1e-4) < GRAD_TOL, name
