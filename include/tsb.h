@@ -188,6 +188,19 @@ int tsb_scene_adam_step(tsb_scene* s, const tsb_adam_config* cfg);
 /* AdamState::step on one flat parameter vector (trainer.cpp:18-31): m, v, params
  * updated in place; t is the step count after increment.  `where`: pointers are
  * host (copied through the device) or device memory. */
+/* Densification surgery (trainer.cpp:385-470) with the Adam reindex (AdamState::reindex,
+ * trainer.cpp:33-47), on the device: prune splats with sigmoid(opacity_logit) < opacity_floor
+ * (in index order, never below min_count), then every survivor whose mean densify
+ * statistic exceeds grad_threshold splits in two along its largest axis (largest scale >
+ * split_scale_fraction x scene_extent) or is cloned.  New order: kept Gaussians, then the
+ * extras in their parents' order; Adam moments follow kept Gaussians and start at zero for
+ * new ones; gradients and the densify statistic are cleared.  *n_new = the new count. */
+typedef struct {
+    double grad_threshold, opacity_floor, split_scale_fraction, split_shrink;
+    int32_t min_count;
+} tsb_densify_config;
+int tsb_scene_densify(tsb_scene* s, const tsb_densify_config* cfg, double scene_extent, int32_t* n_new);
+
 int tsb_adam_step_flat(tsb_ctx* ctx, int where, float* params, const float* grads, float* m, float* v, size_t n,
                        int64_t t, double lr, double beta1, double beta2, double eps);
 

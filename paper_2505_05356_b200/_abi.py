@@ -69,6 +69,11 @@ _lp = C.POINTER(C.c_int64)
 _vp = C.c_void_p
 
 
+class DensifyConfigC(C.Structure):
+    _fields_ = [("grad_threshold", C.c_double), ("opacity_floor", C.c_double), ("split_scale_fraction", C.c_double),
+                ("split_shrink", C.c_double), ("min_count", C.c_int32)]
+
+
 class DeformConfigC(C.Structure):
     _fields_ = [("hidden_layers", C.c_int32), ("width", C.c_int32), ("l_x", C.c_int32), ("l_t", C.c_int32),
                 ("coord_scale", C.c_double)]
@@ -118,6 +123,7 @@ SIGNATURES = {
     "tsb_pass_backward_buffers": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]),
     "tsb_pass_debug_keep_screen": (C.c_int, [_vp, C.c_int]),
     "tsb_pass_debug_set_list_capacity": (C.c_int, [_vp, C.c_uint32]),
+    "tsb_scene_densify": (C.c_int, [_vp, _vp, C.c_double, C.POINTER(C.c_int32)]),
     "tsb_deform_create": (C.c_int, [_vp, _vp, C.POINTER(_vp)]),
     "tsb_deform_destroy": (None, [_vp]),
     "tsb_deform_param_count": (C.c_int64, [_vp]),

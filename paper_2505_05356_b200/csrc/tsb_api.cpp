@@ -687,6 +687,75 @@ int tsb_scene_adam_step(tsb_scene* s, const tsb_adam_config* cfg) {
     return TSB_OK;
 }
 
+int tsb_scene_densify(tsb_scene* s, const tsb_densify_config* cfg, double scene_extent, int32_t* n_new_out) {
+    if (!s || !cfg) return fail(TSB_ERR_INVALID, "tsb_scene_densify: null argument");
+    if (!(cfg->split_shrink > 0.0)) return fail(TSB_ERR_INVALID, "densify: split_shrink must be > 0");
+    TSB_CUDA(cudaSetDevice(s->ctx->device));
+    int rc = tsb_ctx_join(s->ctx);  // every pass is settled and has finished reading the scene
+    if (rc) return rc;
+    cudaStream_t st = s->ctx->stream;
+    TSB_CUDA(cudaStreamWaitEvent(st, s->grads_ev, 0));
+    const int n = s->d.n;
+    const size_t nn = (size_t)std::max(n, 1);
+    DensifyScratch w{};
+    const size_t nb = nn / 1024 + 2;
+    if ((rc = dev_alloc(&w.transparent, nn)) || (rc = dev_alloc(&w.tprefix, nn)) || (rc = dev_alloc(&w.keep, nn)) ||
+        (rc = dev_alloc(&w.extra, nn)) || (rc = dev_alloc(&w.kpos, nn)) || (rc = dev_alloc(&w.epos, nn)) ||
+        (rc = dev_alloc(&w.scan_tmp, nb)) || (rc = dev_alloc(&w.totals, 4)) || (rc = dev_alloc(&w.decision, nn))) {
+        dev_free(w.transparent); dev_free(w.tprefix); dev_free(w.keep); dev_free(w.extra); dev_free(w.kpos);
+        dev_free(w.epos); dev_free(w.scan_tmp); dev_free(w.totals); dev_free(w.decision);
+        return rc;
+    }
+    DensifyK D{};
+    D.grad_sum = s->densify;
+    D.count = s->densify_count;
+    D.grad_threshold = cfg->grad_threshold;
+    D.opacity_floor = cfg->opacity_floor;
+    D.split_scale = cfg->split_scale_fraction * scene_extent;
+    D.split_shrink = cfg->split_shrink;
+    D.min_count = cfg->min_count;
+    const SceneK S = scenek(s);
+    launch_densify_plan(S, D, w, st);
+    s->ctx->launches += n > 0 ? 11 : 0;
+    uint32_t tot[3] = {0, 0, 0};
+    cudaError_t e = cudaMemcpyAsync(tot, w.totals, sizeof tot, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    const uint32_t n_kept = tot[0], n_extra = tot[1];
+    const int n_new = (int)(n_kept + n_extra);
+    float4 *P2 = nullptr, *G2 = nullptr, *M2 = nullptr, *V2 = nullptr;
+    float *dens2 = nullptr, *stg2 = nullptr;
+    double* pc2 = nullptr;
+    const size_t nel2 = (size_t)s->narrays * (size_t)std::max(n_new, 1);
+    if (e == cudaSuccess && !((rc = dev_alloc(&P2, nel2)) || (rc = dev_alloc(&G2, nel2)) || (rc = dev_alloc(&M2, nel2)) ||
+                              (rc = dev_alloc(&V2, nel2)) || (rc = dev_alloc(&dens2, (size_t)std::max(n_new, 1))) ||
+                              (rc = dev_alloc(&stg2, 4 * (size_t)std::max(n_new, 1))) ||
+                              (rc = dev_alloc(&pc2, 7 * (size_t)std::max(n_new, 1))))) {
+        launch_densify_scatter(S, D, w, n_kept, s->narrays, s->params, s->m, s->v, P2, M2, V2, n_new, st);
+        s->ctx->launches += n > 0 ? 1 : 0;
+        cudaMemsetAsync(G2, 0, nel2 * sizeof(float4), st);
+        cudaMemsetAsync(dens2, 0, sizeof(float) * std::max(n_new, 1), st);
+        e = cudaStreamSynchronize(st);
+    }
+    dev_free(w.transparent); dev_free(w.tprefix); dev_free(w.keep); dev_free(w.extra); dev_free(w.kpos);
+    dev_free(w.epos); dev_free(w.scan_tmp); dev_free(w.totals); dev_free(w.decision);
+    if (e != cudaSuccess || rc) {
+        dev_free(P2); dev_free(G2); dev_free(M2); dev_free(V2); dev_free(dens2); dev_free(stg2); dev_free(pc2);
+        if (rc) return rc;
+        return fail(TSB_ERR_CUDA, std::string("densify: ") + cudaGetErrorString(e));
+    }
+    dev_free(s->params); dev_free(s->grads); dev_free(s->m); dev_free(s->v); dev_free(s->densify);
+    dev_free(s->staging); dev_free(s->pcache);
+    s->params = P2; s->grads = G2; s->m = M2; s->v = V2; s->densify = dens2; s->staging = stg2; s->pcache = pc2;
+    s->d.n = n_new;
+    s->densify_count = 0;
+    TSB_CUDA(cudaMemsetAsync(s->stats, 0, sizeof(double) * kStats, st));
+    if ((rc = refresh_param_cache(s))) return rc;
+    TSB_CUDA(cudaEventRecord(s->params_ev, st));
+    TSB_CUDA(cudaEventRecord(s->grads_ev, st));
+    if (n_new_out) *n_new_out = n_new;
+    return TSB_OK;
+}
+
 int tsb_adam_step_flat(tsb_ctx* ctx, int where, float* params, const float* grads, float* m, float* v, size_t n,
                        int64_t t, double lr, double beta1, double beta2, double eps) {
     if (!ctx || (n && (!params || !grads || !m || !v))) return fail(TSB_ERR_INVALID, "adam_step: null argument");

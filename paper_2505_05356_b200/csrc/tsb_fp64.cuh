@@ -87,7 +87,7 @@ __device__ __forceinline__ void refl_coeffs(const SceneK& S, int gi, double* c) 
 
 // sum_k refl_sh[k] b_k(view_dir) for sh_degree > 0 (out of line: keeps the
 // degree-0 kernels' register budget).
-__device__ __noinline__ double refl_sh_eval(const SceneK& S, int gi, double v0, double v1, double v2) {
+static __device__ __noinline__ double refl_sh_eval(const SceneK& S, int gi, double v0, double v1, double v2) {
     const double v[3] = {v0, v1, v2};
     double b[16], c[16];
     sh_basis64(v, S.sh_degree, b);

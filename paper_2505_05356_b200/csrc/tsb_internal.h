@@ -306,6 +306,21 @@ struct SsimArgs {
 void ssim_init();  // window constants (outside any stream capture)
 int ssim_blocks(int W, int H);
 void launch_ssim(const float* x, int W, int H, const SsimArgs& a, cudaStream_t st);
+// tsb_densify.cu: densification surgery (trainer.cpp:385-470).
+struct DensifyK {
+    const float* grad_sum;  // densify statistic: sum of |dL/dx_canon| per Gaussian
+    int64_t count;          // iterations accumulated
+    double grad_threshold, opacity_floor, split_scale /* fraction x scene extent */, split_shrink;
+    int min_count;
+};
+struct DensifyScratch {
+    uint32_t *transparent, *tprefix, *keep, *extra, *kpos, *epos, *scan_tmp, *totals;  // totals: kept, extra, transp
+    uint8_t* decision;
+};
+void launch_densify_plan(const SceneK& S, const DensifyK& D, DensifyScratch& w, cudaStream_t st);
+void launch_densify_scatter(const SceneK& S, const DensifyK& D, const DensifyScratch& w, uint32_t n_kept, int narrays,
+                            const float4* P, const float4* M, const float4* V, float4* P2, float4* M2, float4* V2,
+                            int n_new, cudaStream_t st);
 // tsb_optim.cu
 void launch_pack_params(float4* dst, const float* src, int n, int comps, int comp0, int ncomp_dst,
                         cudaStream_t st);

@@ -137,6 +137,14 @@ class LrTable:
         return LrTable(lr, lr, lr, lr, lr, lr)
 
 
+def scene_extent(positions) -> float:
+    """scene_extent_of (trainer.cpp:140-147): max distance from the centroid (>= 1e-9; 1 when empty)."""
+    p = np.asarray(positions, np.float64).reshape(-1, 3)
+    if p.shape[0] == 0:
+        return 1.0
+    return max(float(np.linalg.norm(p - p.mean(axis=0), axis=1).max()), 1e-9)
+
+
 def frame_for_time(t: float, n_keyframes: int):
     """Keyframe segment and weight for normalised time t in [0, 1]: i = floor(t K),
     w = t K - i with K = n_keyframes - 1 (the trajectory lerp of trainer.cpp:259-279 /
@@ -240,6 +248,16 @@ class GaussianScene:
     @property
     def handle(self):
         return self._h
+
+    def densify(self, scene_extent: float, grad_threshold: float = 5e-5, opacity_floor: float = 5e-3,
+                split_scale_fraction: float = 0.01, split_shrink: float = 1.6, min_count: int = 16) -> int:
+        """Densification surgery + Adam reindex on the device (trainer.cpp:385-470, DensifyConfig
+        defaults trainer.hpp:68-78); returns the new Gaussian count."""
+        cfg = _abi.DensifyConfigC(grad_threshold, opacity_floor, split_scale_fraction, split_shrink, min_count)
+        n = C.c_int32()
+        check(lib().tsb_scene_densify(self._h, C.byref(cfg), float(scene_extent), C.byref(n)))
+        self.n = int(n.value)
+        return self.n
 
     def set_params(self, position, log_scale, rotation, opacity_logit, reflectivity_dc, motion=None):
         """Host numpy arrays (float32 SoA: position (n,3), log_scale (n,3), rotation (n,4) wxyz,

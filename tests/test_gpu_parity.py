@@ -570,3 +570,45 @@ def test_image_loss_with_ssim_mix(tsb, ctx):
                        ("d_opacity_logit", gr["d_opacity_logit"], og["d_opacity_logit"]),
                        ("d_log_scale", gr["d_log_scale"], og["d_log_scale"])):
         assert rel_err(a, b, 1e-4) < GRAD_TOL, name
+
+
+def test_densify_surgery_matches_oracle(tsb, ctx):
+    """tsb_scene_densify (trainer.cpp:385-470) vs the oracle on the GPU's own statistic:
+    kept / pruned / cloned / split Gaussians in the reference order, split children, Adam
+    moments reindexed (AdamState::reindex), statistic cleared; then the grown scene renders."""
+    from oracle import densify as odn
+    from paper_2505_05356_b200 import synthetic
+    g = synthetic.gaussians(6000, 17, n_keyframes=2)
+    g.opacity_logit[::7] = -8.0  # transparent ones to prune
+    tof = tsb.ToFConfig(30e6)
+    scene = gpu_scene(tsb, ctx, g, tof)
+    cam = synthetic.camera(160, 120, 140.0)
+    tgt = synthetic.gaussians(6000, 18, n_keyframes=2)
+    target = tsb.RenderPass(ctx).prepare(gpu_scene(tsb, ctx, tgt, tof), cam, tsb.RenderOptions(), (0, 0.5)) \
+        .forward().outputs()["quad"]
+    rp = tsb.RenderPass(ctx)
+    for it in range(3):
+        rp.prepare(scene, cam, tsb.RenderOptions(), (0, 0.3 * it)).forward_loss(target, sync=False)
+        rp.backward()
+        scene.adam_step(tsb.LrTable.uniform(1e-3))
+    prm = scene.get_params()
+    stat, count = scene.densify_stat()
+    m, v = scene.adam_moments_position()
+    extent = tsb.render.scene_extent(prm["position"])
+    thr = float(np.quantile(stat / count, 0.7))
+    n_new = scene.densify(extent, grad_threshold=thr, opacity_floor=5e-3, split_scale_fraction=0.02,
+                          min_count=16)
+    ref, src = odn.densify(prm, stat, count, extent, grad_threshold=thr, opacity_floor=5e-3,
+                           split_scale_fraction=0.02, min_count=16)
+    assert n_new == ref["position"].shape[0] and n_new != g.n
+    assert sum(1 for s in src if s < 0) > 0 and len(set(src) - {-1}) < g.n
+    got = scene.get_params()
+    for k in ("position", "log_scale", "rotation", "opacity_logit", "reflectivity_dc", "motion"):
+        assert np.allclose(got[k], ref[k], rtol=0, atol=1e-6), k
+    m2, v2 = scene.adam_moments_position()
+    rm, rv = odn.adam_reindex(m, v, src)
+    assert np.array_equal(m2, rm) and np.array_equal(v2, rv)
+    s2, c2 = scene.densify_stat()
+    assert c2 == 0 and not s2.any()
+    out = tsb.RenderPass(ctx).prepare(scene, cam, tsb.RenderOptions(), (0, 0.5)).forward().outputs()
+    assert np.isfinite(out["quad"]).all()
