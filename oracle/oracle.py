@@ -14,6 +14,7 @@ import ctypes as C
 import os
 import subprocess
 from dataclasses import dataclass
+from typing import Optional
 from pathlib import Path
 
 import numpy as np
@@ -51,6 +52,8 @@ def lib():
         L.orc_pass_tile_lists.argtypes = [C.c_void_p, lp, ip]
         L.orc_pass_forward.argtypes = [C.c_void_p] + [dp] * 7 + [ip, ip]
         L.orc_pass_backward.argtypes = [C.c_void_p] + [dp] * 14
+        L.orc_pass_forward_ext.argtypes = [C.c_void_p] + [dp] * 6
+        L.orc_pass_backward_ext.argtypes = [C.c_void_p] + [dp] * 21
         L.orc_mse.restype = C.c_double
         L.orc_mse.argtypes = [dp, dp, C.c_size_t, dp]
         L.orc_adam_step.argtypes = [dp, dp, dp, dp, C.c_size_t, C.c_int64, C.c_double, C.c_double,
@@ -75,14 +78,15 @@ class _Options(C.Structure):
     _fields_ = [("alpha_threshold", C.c_double), ("transmittance_floor", C.c_double),
                 ("dilation", C.c_double), ("sigma_cutoff", C.c_double), ("coverage_eps", C.c_double),
                 ("tile_size", C.c_int32), ("_pad", C.c_int32), ("bg_quad", C.c_double * 4),
-                ("bg_phasor", C.c_double * 2)]
+                ("bg_phasor", C.c_double * 2), ("bg_color", C.c_double * 3)]
 
 
 class _Scene(C.Structure):
     _fields_ = [("n", C.c_int32), ("sh_degree", C.c_int32), ("modulation_frequency", C.c_double),
                 ("source_intensity", C.c_double), ("speed_of_light", C.c_double),
                 ("position", C.c_void_p), ("log_scale", C.c_void_p), ("rotation", C.c_void_p),
-                ("opacity_logit", C.c_void_p), ("refl_sh", C.c_void_p)]
+                ("opacity_logit", C.c_void_p), ("refl_sh", C.c_void_p), ("color_sh", C.c_void_p),
+                ("motion_fwd", C.c_void_p), ("motion_bwd", C.c_void_p)]
 
 
 def _dp(a):
@@ -112,6 +116,9 @@ class OScene:
     modulation_frequency: float = 29.9792458e6
     source_intensity: float = 1.0
     speed_of_light: float = 299792458.0
+    color_sh: Optional[np.ndarray] = None    # (n, 48): [16 c + k] = Gaussian::color_sh(k, c)
+    motion_fwd: Optional[np.ndarray] = None  # (n, 3) RenderInput::motion_fwd
+    motion_bwd: Optional[np.ndarray] = None
 
     @property
     def n(self):
@@ -158,6 +165,9 @@ def _options(opt) -> _Options:
     bp = np.asarray(getattr(opt, "bg_phasor", np.zeros(2)), dtype=np.float64).reshape(-1)
     for i in range(2):
         o.bg_phasor[i] = bp[i] if bp.size > i else 0.0
+    bc = np.asarray(getattr(opt, "bg_color", np.zeros(3)), dtype=np.float64).reshape(-1)
+    for i in range(3):
+        o.bg_color[i] = bc[i] if bc.size > i else 0.0
     return o
 
 
@@ -177,6 +187,12 @@ class OraclePass:
         s.source_intensity = scene.source_intensity
         s.speed_of_light = scene.speed_of_light
         s.position, s.log_scale, s.rotation, s.opacity_logit, s.refl_sh = [a.ctypes.data for a in self._keep]
+        for name, comps in (("color_sh", 48), ("motion_fwd", 3), ("motion_bwd", 3)):
+            a = getattr(scene, name, None)
+            if a is not None:
+                a = _f64(a, (scene.n, comps))
+                self._keep.append(a)
+                setattr(s, name, a.ctypes.data)
         self._s, self._c, self._o = s, _camera(camera), _options(options)
         self.width, self.height = int(camera.width), int(camera.height)
         h = L.orc_pass_create(C.byref(self._s), C.byref(self._c), C.byref(self._o))
@@ -232,8 +248,18 @@ class OraclePass:
         out["n_processed"] = npr
         return out
 
+    def forward_ext(self):
+        """Colour and flow channels (splat.cpp:273-294, 301-334)."""
+        W, H = self.width, self.height
+        out = {k: np.zeros((c, H, W)) for k, c in
+               [("color", 3), ("motion_fwd_acc", 3), ("motion_bwd_acc", 3), ("flow_fwd", 2), ("flow_bwd", 2),
+                ("flow_valid", 2)]}
+        lib().orc_pass_forward_ext(self._h, *[_dp(out[k]) for k in ("color", "motion_fwd_acc", "motion_bwd_acc",
+                                                                     "flow_fwd", "flow_bwd", "flow_valid")])
+        return out
+
     def backward(self, d_quad=None, d_phasor=None, d_depth_raw=None, d_weight=None, d_distortion=None,
-                 d_transmittance=None):
+                 d_transmittance=None, d_color=None, d_motion_fwd_acc=None, d_motion_bwd_acc=None):
         n, v = self.scene.n, self.visible_count()
         W, H = self.width, self.height
 
@@ -241,13 +267,16 @@ class OraclePass:
             return None if a is None else _f64(a, (c, H, W))
 
         ups = [up(d_quad, 4), up(d_phasor, 2), up(d_depth_raw, 1), up(d_weight, 1), up(d_distortion, 1),
-               up(d_transmittance, 1)]
+               up(d_transmittance, 1), up(d_color, 3), up(d_motion_fwd_acc, 3), up(d_motion_bwd_acc, 3)]
         g = {"d_position": np.zeros((n, 3)), "d_log_scale": np.zeros((n, 3)), "d_rotation": np.zeros((n, 4)),
              "d_opacity_logit": np.zeros(n), "d_refl_sh": np.zeros((n, 16)), "d_bg_quad": np.zeros(4),
-             "d_bg_phasor": np.zeros(2), "screen": np.zeros((max(v, 1), 8))}
-        lib().orc_pass_backward(self._h, *[_dp(a) for a in ups], _dp(g["d_position"]), _dp(g["d_log_scale"]),
-                                _dp(g["d_rotation"]), _dp(g["d_opacity_logit"]), _dp(g["d_refl_sh"]),
-                                _dp(g["d_bg_quad"]), _dp(g["d_bg_phasor"]), _dp(g["screen"]))
+             "d_bg_phasor": np.zeros(2), "d_color_sh": np.zeros((n, 48)), "d_motion_fwd": np.zeros((n, 3)),
+             "d_motion_bwd": np.zeros((n, 3)), "d_bg_color": np.zeros(3), "screen": np.zeros((max(v, 1), 8))}
+        lib().orc_pass_backward_ext(self._h, *[_dp(a) for a in ups], _dp(g["d_position"]), _dp(g["d_log_scale"]),
+                                    _dp(g["d_rotation"]), _dp(g["d_opacity_logit"]), _dp(g["d_refl_sh"]),
+                                    _dp(g["d_bg_quad"]), _dp(g["d_bg_phasor"]), _dp(g["d_color_sh"]),
+                                    _dp(g["d_motion_fwd"]), _dp(g["d_motion_bwd"]), _dp(g["d_bg_color"]),
+                                    _dp(g["screen"]))
         g["screen"] = g["screen"][:v]
         return g
 

@@ -155,6 +155,8 @@ typedef struct {
     double view_dir[3];
     double refl_raw;
     double sh_b[SHN];
+    double color_raw[3], color[3];  /* splat.cpp:172-173 */
+    double mf[3], mb[3];            /* splat.cpp:174-175 */
 } Prepared;
 
 struct orc_pass {
@@ -285,6 +287,15 @@ static void prepare(orc_pass* P) {
         s.sin_psi = sin(psi);
         s.cos_psi = cos(psi);
         s.dpsi_dd = 4.0 * M_PI * sc->modulation_frequency / sc->speed_of_light;
+        for (int c = 0; c < 3; ++c) {  /* color_raw = color_sh^T sh_b, clamped to [0, 1] */
+            double cr = 0.0;
+            if (sc->color_sh)
+                for (int k = 0; k < SHN; ++k) cr += sc->color_sh[48 * (size_t)gi + SHN * c + k] * s.sh_b[k];
+            s.color_raw[c] = cr;
+            s.color[c] = clampd(cr, 0.0, 1.0);
+            s.mf[c] = sc->motion_fwd ? sc->motion_fwd[3 * gi + c] : 0.0;
+            s.mb[c] = sc->motion_bwd ? sc->motion_bwd[3 * gi + c] : 0.0;
+        }
         P->prep[nv++] = s;
     }
     P->nvis = nv;
@@ -432,11 +443,98 @@ void orc_pass_forward(const orc_pass* P, double* quad, double* phasor, double* d
     }
 }
 
+/* ---- colour and flow channels (splat.cpp:273-294, 301-334) ------------------ */
+void orc_pass_forward_ext(const orc_pass* P, double* color, double* mf_acc, double* mb_acc, double* flow_fwd,
+                          double* flow_bwd, double* flow_valid) {
+    const orc_camera* cam = &P->cam;
+    const int W = cam->width, H = cam->height;
+    const size_t HW = (size_t)W * H;
+    const orc_options* opt = &P->opt;
+    const double cutoff2 = opt->sigma_cutoff * opt->sigma_cutoff;
+    const int ts = opt->tile_size > 1 ? opt->tile_size : 1;
+    const int ntiles = P->tiles_x * P->tiles_y;
+    const double* R = cam->R;
+#pragma omp parallel for schedule(static)
+    for (int tile = 0; tile < ntiles; ++tile) {
+        const int32_t* ids = P->tile_ids + P->tile_off[tile];
+        const int64_t nids = P->tile_off[tile + 1] - P->tile_off[tile];
+        const int px0 = (tile % P->tiles_x) * ts, px1 = px0 + ts < W ? px0 + ts : W;
+        const int py0 = (tile / P->tiles_x) * ts, py1 = py0 + ts < H ? py0 + ts : H;
+        for (int y = py0; y < py1; ++y) {
+            for (int x = px0; x < px1; ++x) {
+                const double pcx = x + 0.5, pcy = y + 0.5;
+                double T = 1.0, SW = 0, SD = 0;
+                double accC[3] = {0, 0, 0}, accMf[3] = {0, 0, 0}, accMb[3] = {0, 0, 0};
+                for (int64_t e = 0; e < nids; ++e) {
+                    const Prepared* s = &P->prep[ids[e]];
+                    if (x < s->x0 || x >= s->x1 || y < s->y0 || y >= s->y1) continue;
+                    const double dx = pcx - s->mean2d[0], dy = pcy - s->mean2d[1];
+                    const double maha = s->conic_a * dx * dx + 2.0 * s->conic_b * dx * dy + s->conic_c * dy * dy;
+                    if (maha > cutoff2 || maha < 0.0) continue;
+                    const double alpha = s->opacity * exp(-0.5 * maha);
+                    if (alpha < opt->alpha_threshold) continue;
+                    const double w = alpha * T;
+                    for (int c = 0; c < 3; ++c) {
+                        accC[c] += w * s->color[c];
+                        accMf[c] += w * s->mf[c];
+                        accMb[c] += w * s->mb[c];
+                    }
+                    SW += w;
+                    SD += w * s->depth;
+                    T *= 1.0 - alpha;
+                    if (T < opt->transmittance_floor) break;
+                }
+                const size_t o = (size_t)y * W + x;
+                for (int c = 0; c < 3; ++c) {
+                    if (color) color[c * HW + o] = accC[c] + opt->bg_color[c] * T;
+                    if (mf_acc) mf_acc[c * HW + o] = accMf[c];
+                    if (mb_acc) mb_acc[c * HW + o] = accMb[c];
+                }
+                for (int c = 0; c < 2; ++c) {
+                    if (flow_fwd) flow_fwd[c * HW + o] = 0.0;
+                    if (flow_bwd) flow_bwd[c * HW + o] = 0.0;
+                    if (flow_valid) flow_valid[c * HW + o] = 0.0;
+                }
+                if (SW > opt->coverage_eps) {
+                    /* cam.backproject (camera.hpp:34-43): optical_center + dist * normalize(R^T d_cam),
+                     * d_cam = ((px - cx) / fx, (py - cy) / fy, 1), dist = SD / SW (radial depth) */
+                    const double dist = SD / SW;
+                    const double dc[3] = {(pcx - cam->cx) / cam->fx, (pcy - cam->cy) / cam->fy, 1.0};
+                    double dir[3], center[3];
+                    for (int a = 0; a < 3; ++a) {
+                        dir[a] = R[0 * 3 + a] * dc[0] + R[1 * 3 + a] * dc[1] + R[2 * 3 + a] * dc[2];
+                        center[a] = -(R[0 * 3 + a] * cam->t[0] + R[1 * 3 + a] * cam->t[1] + R[2 * 3 + a] * cam->t[2]);
+                    }
+                    const double dn = sqrt(dir[0] * dir[0] + dir[1] * dir[1] + dir[2] * dir[2]);
+                    double xd[3];
+                    for (int a = 0; a < 3; ++a) xd[a] = center[a] + dist * (dir[a] / dn);
+                    for (int k = 0; k < 2; ++k) {
+                        const double* mo = k == 0 ? accMf : accMb;
+                        double* fl = k == 0 ? flow_fwd : flow_bwd;
+                        double q[3], p[3];
+                        for (int a = 0; a < 3; ++a) q[a] = xd[a] + mo[a];
+                        for (int i = 0; i < 3; ++i)
+                            p[i] = R[i * 3 + 0] * q[0] + R[i * 3 + 1] * q[1] + R[i * 3 + 2] * q[2] + cam->t[i];
+                        if (p[2] > 0.0) {
+                            if (fl) {
+                                fl[o] = cam->fx * p[0] / p[2] + cam->cx - pcx;
+                                fl[HW + o] = cam->fy * p[1] / p[2] + cam->cy - pcy;
+                            }
+                            if (flow_valid) flow_valid[k * HW + o] = 1.0;
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
 /* ---- backward (splat.cpp:347-650) --------------------------------------- */
 typedef struct {
     double d_mean2d[2];
     double d_conic_a, d_conic_b, d_conic_c;
     double d_opacity, d_coef, d_depth;
+    double d_color[3], d_mf[3], d_mb[3];
 } SplatGrad;
 
 typedef struct {
@@ -450,6 +548,18 @@ void orc_pass_backward(const orc_pass* P, const double* d_quad, const double* d_
                        double* d_position, double* d_log_scale, double* d_rotation,
                        double* d_opacity_logit, double* d_refl_sh, double* d_bg_quad,
                        double* d_bg_phasor, double* screen) {
+    orc_pass_backward_ext(P, d_quad, d_phasor, d_depth_raw, d_weight, d_distortion, d_transmittance, NULL, NULL, NULL,
+                          d_position, d_log_scale, d_rotation, d_opacity_logit, d_refl_sh, d_bg_quad, d_bg_phasor,
+                          NULL, NULL, NULL, NULL, screen);
+}
+
+void orc_pass_backward_ext(const orc_pass* P, const double* d_quad, const double* d_phasor,
+                           const double* d_depth_raw, const double* d_weight, const double* d_distortion,
+                           const double* d_transmittance, const double* d_color, const double* d_mf_acc,
+                           const double* d_mb_acc, double* d_position, double* d_log_scale, double* d_rotation,
+                           double* d_opacity_logit, double* d_refl_sh, double* d_bg_quad, double* d_bg_phasor,
+                           double* d_color_sh, double* d_motion_fwd, double* d_motion_bwd, double* d_bg_color,
+                           double* screen) {
     const orc_scene* sc = &P->scene;
     const orc_camera* cam = &P->cam;
     const orc_options* opt = &P->opt;
@@ -463,7 +573,7 @@ void orc_pass_backward(const orc_pass* P, const double* d_quad, const double* d_
 
     const int nthreads = orc_num_threads();
     SplatGrad* tl = (SplatGrad*)calloc((size_t)nthreads * (nvis > 0 ? nvis : 1), sizeof(SplatGrad));
-    double* tl_bg = (double*)calloc((size_t)nthreads * 6, sizeof(double));
+    double* tl_bg = (double*)calloc((size_t)nthreads * 9, sizeof(double));
 
 #pragma omp parallel
     {
@@ -472,7 +582,7 @@ void orc_pass_backward(const orc_pass* P, const double* d_quad, const double* d_
         tid = omp_get_thread_num();
 #endif
         SplatGrad* sg = tl + (size_t)tid * (nvis > 0 ? nvis : 1);
-        double* bgg = tl_bg + 6 * tid;
+        double* bgg = tl_bg + 9 * tid;
         size_t cap = 256;
         Entry* entries = (Entry*)malloc(sizeof(Entry) * cap);
 #pragma omp for schedule(static)
@@ -511,6 +621,11 @@ void orc_pass_backward(const orc_pass* P, const double* d_quad, const double* d_
                     const size_t o = (size_t)y * W + x;
                     double upQ[4] = {0, 0, 0, 0}, upP[2] = {0, 0};
                     double upDraw = 0, upW = 0, upDD = 0, upT = 0;
+                    double upC[3] = {0, 0, 0}, upMf[3] = {0, 0, 0}, upMb[3] = {0, 0, 0};
+                    if (d_color) for (int c = 0; c < 3; ++c) upC[c] = d_color[c * HW + o];
+                    if (d_mf_acc) for (int c = 0; c < 3; ++c) upMf[c] = d_mf_acc[c * HW + o];
+                    if (d_mb_acc) for (int c = 0; c < 3; ++c) upMb[c] = d_mb_acc[c * HW + o];
+                    if (d_color) for (int c = 0; c < 3; ++c) bgg[6 + c] += upC[c] * T_final;
                     if (d_quad) for (int c = 0; c < 4; ++c) upQ[c] = d_quad[c * HW + o];
                     if (d_phasor) for (int c = 0; c < 2; ++c) upP[c] = d_phasor[c * HW + o];
                     if (d_depth_raw) upDraw = d_depth_raw[o];
@@ -525,6 +640,8 @@ void orc_pass_backward(const orc_pass* P, const double* d_quad, const double* d_
                     for (int c = 0; c < 4; ++c) accQ[c] = opt->bg_quad[c];
                     for (int c = 0; c < 2; ++c) accP[c] = opt->bg_phasor[c];
                     double accD = 0, accW = 0, accPhi = 0, Rsuf = 1.0;
+                    double accC[3], accMf[3] = {0, 0, 0}, accMb[3] = {0, 0, 0};
+                    for (int c = 0; c < 3; ++c) accC[c] = opt->bg_color[c];
                     for (long e = (long)ne - 1; e >= 0; --e) {
                         const Entry* en = &entries[e];
                         const Prepared* s = &P->prep[en->idx];
@@ -532,6 +649,13 @@ void orc_pass_backward(const orc_pass* P, const double* d_quad, const double* d_
                         const double alpha = en->alpha, Tk = en->T, one_m = 1.0 - alpha;
                         const double w = alpha * Tk, w2 = alpha * Tk * Tk, Tk2 = Tk * Tk;
                         double d_alpha = 0;
+                        if (d_color) {
+                            double t = 0;
+                            for (int c = 0; c < 3; ++c) t += upC[c] * (Tk * (s->color[c] - accC[c]));
+                            d_alpha += t;
+                            for (int c = 0; c < 3; ++c) ga->d_color[c] += upC[c] * w;
+                            for (int c = 0; c < 3; ++c) accC[c] = alpha * s->color[c] + one_m * accC[c];
+                        }
                         if (d_quad) {
                             const double basis[4] = {s->sin_psi, s->cos_psi, -s->sin_psi, -s->cos_psi};
                             double qk[4], t1 = 0, t2 = 0, t3 = 0;
@@ -573,6 +697,20 @@ void orc_pass_backward(const orc_pass* P, const double* d_quad, const double* d_
                             ga->d_depth += upDD * 4.0 * w * (SW * s->depth - SD);
                             accPhi = alpha * phi + one_m * accPhi;
                         }
+                        if (d_mf_acc) {
+                            double t = 0;
+                            for (int c = 0; c < 3; ++c) t += upMf[c] * (Tk * (s->mf[c] - accMf[c]));
+                            d_alpha += t;
+                            for (int c = 0; c < 3; ++c) ga->d_mf[c] += upMf[c] * w;
+                            for (int c = 0; c < 3; ++c) accMf[c] = alpha * s->mf[c] + one_m * accMf[c];
+                        }
+                        if (d_mb_acc) {
+                            double t = 0;
+                            for (int c = 0; c < 3; ++c) t += upMb[c] * (Tk * (s->mb[c] - accMb[c]));
+                            d_alpha += t;
+                            for (int c = 0; c < 3; ++c) ga->d_mb[c] += upMb[c] * w;
+                            for (int c = 0; c < 3; ++c) accMb[c] = alpha * s->mb[c] + one_m * accMb[c];
+                        }
                         if (d_transmittance) d_alpha -= upT * Tk * Rsuf;
                         Rsuf *= one_m;
 
@@ -592,7 +730,7 @@ void orc_pass_backward(const orc_pass* P, const double* d_quad, const double* d_
 
     /* fixed-order reduction (splat.cpp:521-543) */
     SplatGrad* acc = tl;
-    double bg[6];
+    double bg[9];
     memcpy(bg, tl_bg, sizeof bg);
     for (int t = 1; t < nthreads; ++t) {
         const SplatGrad* a = tl + (size_t)t * (nvis > 0 ? nvis : 1);
@@ -606,11 +744,20 @@ void orc_pass_backward(const orc_pass* P, const double* d_quad, const double* d_
             b->d_opacity += a[i].d_opacity;
             b->d_coef += a[i].d_coef;
             b->d_depth += a[i].d_depth;
+            for (int c = 0; c < 3; ++c) {
+                b->d_color[c] += a[i].d_color[c];
+                b->d_mf[c] += a[i].d_mf[c];
+                b->d_mb[c] += a[i].d_mb[c];
+            }
         }
-        for (int c = 0; c < 6; ++c) bg[c] += tl_bg[6 * t + c];
+        for (int c = 0; c < 9; ++c) bg[c] += tl_bg[9 * t + c];
     }
     if (d_bg_quad) for (int c = 0; c < 4; ++c) d_bg_quad[c] = bg[c];
     if (d_bg_phasor) for (int c = 0; c < 2; ++c) d_bg_phasor[c] = bg[4 + c];
+    if (d_bg_color) for (int c = 0; c < 3; ++c) d_bg_color[c] = bg[6 + c];
+    if (d_color_sh) memset(d_color_sh, 0, sizeof(double) * 48 * (size_t)n);
+    if (d_motion_fwd) memset(d_motion_fwd, 0, sizeof(double) * 3 * (size_t)n);
+    if (d_motion_bwd) memset(d_motion_bwd, 0, sizeof(double) * 3 * (size_t)n);
 
     if (d_position) memset(d_position, 0, sizeof(double) * 3 * (size_t)n);
     if (d_log_scale) memset(d_log_scale, 0, sizeof(double) * 3 * (size_t)n);
@@ -633,6 +780,30 @@ void orc_pass_backward(const orc_pass* P, const double* d_quad, const double* d_
         double d_dir[3] = {0, 0, 0};
         double Jb[SHN * 3];
         orc_sh_basis_jacobian(s->view_dir, sc->sh_degree, Jb);
+
+        /* colour SH: the clamp gates each channel (splat.cpp:560-571) */
+        if (g->d_color[0] != 0.0 || g->d_color[1] != 0.0 || g->d_color[2] != 0.0) {
+            double dcol[3];
+            for (int c = 0; c < 3; ++c)
+                dcol[c] = (s->color_raw[c] > 0.0 && s->color_raw[c] < 1.0) ? g->d_color[c] : 0.0;
+            if (d_color_sh)
+                for (int c = 0; c < 3; ++c)
+                    for (int k = 0; k < SHN; ++k) d_color_sh[48 * (size_t)gi + SHN * c + k] += s->sh_b[k] * dcol[c];
+            if (sc->color_sh) /* d_dir += Jb^T (color_sh dcol) */
+                for (int a = 0; a < 3; ++a) {
+                    double acc_ = 0;
+                    for (int k = 0; k < SHN; ++k) {
+                        double cs = 0;
+                        for (int c = 0; c < 3; ++c) cs += sc->color_sh[48 * (size_t)gi + SHN * c + k] * dcol[c];
+                        acc_ += Jb[k * 3 + a] * cs;
+                    }
+                    d_dir[a] += acc_;
+                }
+        }
+        for (int c = 0; c < 3; ++c) {
+            if (d_motion_fwd) d_motion_fwd[3 * gi + c] += g->d_mf[c];
+            if (d_motion_bwd) d_motion_bwd[3 * gi + c] += g->d_mb[c];
+        }
 
         const double r_cl = clampd(s->refl_raw, 0.0, 1.0);
         const double d2 = s->depth * s->depth;

@@ -25,8 +25,9 @@
  * finite-difference gradcheck (proj/src/gradcheck.cpp) against it.  The
  * reference itself cannot be built here (Eigen3 absent), so these KATs are the pin.
  *
- * Colour and flow channels are not part of the ToF hot path
- * and are not restated.
+ * Colour and flow channels (splat.cpp:172-175, 273-294,
+ * 301-334, 419-504, 560-571, 645-646) are restated by orc_pass_forward_ext /
+ * orc_pass_backward_ext.
  */
 #ifndef TOFSPLAT_ORACLE_H
 #define TOFSPLAT_ORACLE_H
@@ -58,6 +59,7 @@ typedef struct {
     int32_t _pad;
     double bg_quad[4];
     double bg_phasor[2];
+    double bg_color[3];         /* Backgrounds::color */
 } orc_options;
 
 /* CanonicalScene / Gaussian (proj/include/tofsplat/scene.hpp:23-52), SoA.
@@ -70,6 +72,9 @@ typedef struct {
     const double* rotation;      /* 4n, (w,x,y,z) raw */
     const double* opacity_logit; /* n */
     const double* refl_sh;       /* 16n */
+    const double* color_sh;      /* 48n, [16 c + k] (Gaussian::color_sh(k, c)); NULL: black */
+    const double* motion_fwd;    /* 3n (RenderInput::motion_fwd); NULL: zero */
+    const double* motion_bwd;    /* 3n */
 } orc_scene;
 
 typedef struct orc_pass orc_pass;
@@ -107,6 +112,22 @@ void orc_pass_backward(const orc_pass* p, const double* d_quad, const double* d_
                        double* d_position, double* d_log_scale, double* d_rotation,
                        double* d_opacity_logit, double* d_refl_sh, double* d_bg_quad,
                        double* d_bg_phasor, double* screen);
+
+/* Colour and flow channels of RenderPass::forward (splat.cpp:273-294, 301-334); any may be NULL.
+ * color [3][H][W] (+ bg_color T), motion accumulators [3][H][W], flow [2][H][W] (pixel
+ * displacement of the depth-backprojected point moved by the accumulated motion),
+ * flow_valid [2][H][W] (fwd, bwd). */
+void orc_pass_forward_ext(const orc_pass* p, double* color, double* motion_fwd_acc, double* motion_bwd_acc,
+                          double* flow_fwd, double* flow_bwd, double* flow_valid);
+/* RenderPass::backward with every upstream of BufferGrads, including d_color [3][H][W] and the
+ * motion accumulators; adds d_color_sh (48n), d_motion_fwd / d_motion_bwd (3n), d_bg_color (3). */
+void orc_pass_backward_ext(const orc_pass* p, const double* d_quad, const double* d_phasor,
+                           const double* d_depth_raw, const double* d_weight, const double* d_distortion,
+                           const double* d_transmittance, const double* d_color, const double* d_motion_fwd_acc,
+                           const double* d_motion_bwd_acc, double* d_position, double* d_log_scale,
+                           double* d_rotation, double* d_opacity_logit, double* d_refl_sh, double* d_bg_quad,
+                           double* d_bg_phasor, double* d_color_sh, double* d_motion_fwd, double* d_motion_bwd,
+                           double* d_bg_color, double* screen);
 
 /* mse (losses.cpp:9-25): returns mean sq. error; d_pred (may be NULL) += 2/n (pred-target). */
 double orc_mse(const double* pred, const double* target, size_t n, double* d_pred);

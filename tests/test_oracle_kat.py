@@ -362,3 +362,72 @@ def test_gradcheck_oracle_backward(seed):
     for name, arr, an in groups:
         worst[name] = max(rel(an[idx], probe(arr, idx)) for idx in np.ndindex(arr.shape))
     assert max(worst.values()) < 1e-3, worst
+
+
+def _objective_ext(sc, cam, opts, ups):
+    p = orc.OraclePass(sc, cam, opts)
+    out, ext = p.forward(), p.forward_ext()
+    return (np.sum(out["quad"] * ups["d_quad"]) + np.sum(out["depth_raw"] * ups["d_depth_raw"][0]) +
+            np.sum(ext["color"] * ups["d_color"]) + np.sum(ext["motion_fwd_acc"] * ups["d_motion_fwd_acc"]) +
+            np.sum(ext["motion_bwd_acc"] * ups["d_motion_bwd_acc"]))
+
+
+def test_gradcheck_oracle_colour_and_motion_channels():
+    """gradcheck.cpp (all channels) for the colour and flow accumulators: colour SH (degree 3,
+    clamp gates), motion vectors, colour background, and their effect on positions/opacity."""
+    sc, cam, opts, ups = _gradcheck_setup(5)
+    rng = np.random.default_rng(9)
+    n, h, w = sc.n, cam.height, cam.width
+    cs = np.zeros((n, 48))
+    for c in range(3):
+        cs[:, 16 * c] = rng.uniform(0.2, 0.8, n) / SH_C0
+        cs[:, 16 * c + 1:16 * c + 16] = rng.uniform(-0.05, 0.05, (n, 15))
+    sc.color_sh = cs
+    sc.motion_fwd = rng.uniform(-0.1, 0.1, (n, 3))
+    sc.motion_bwd = rng.uniform(-0.1, 0.1, (n, 3))
+    opts.bg_color = rng.uniform(0, 1, 3)
+    ups = {"d_quad": ups["d_quad"], "d_depth_raw": ups["d_depth_raw"], "d_color": rng.uniform(-1, 1, (3, h, w)),
+           "d_motion_fwd_acc": rng.uniform(-1, 1, (3, h, w)), "d_motion_bwd_acc": rng.uniform(-1, 1, (3, h, w))}
+    g = orc.OraclePass(sc, cam, opts).backward(**ups)
+    hstep = 1e-5
+
+    def probe(arr, idx):
+        orig = arr[idx]
+        arr[idx] = orig + hstep
+        jp = _objective_ext(sc, cam, opts, ups)
+        arr[idx] = orig - hstep
+        jm = _objective_ext(sc, cam, opts, ups)
+        arr[idx] = orig
+        return (jp - jm) / (2 * hstep)
+
+    def rel(a, b):
+        return abs(a - b) / max(abs(a), abs(b), 1e-6)
+
+    worst = {}
+    for name, arr, an in [("color_sh", sc.color_sh, g["d_color_sh"]), ("motion_fwd", sc.motion_fwd, g["d_motion_fwd"]),
+                          ("motion_bwd", sc.motion_bwd, g["d_motion_bwd"]), ("bg_color", opts.bg_color, g["d_bg_color"]),
+                          ("position", sc.position, g["d_position"]), ("opacity", sc.opacity_logit,
+                                                                       g["d_opacity_logit"])]:
+        worst[name] = max(rel(an[idx], probe(arr, idx)) for idx in np.ndindex(arr.shape))
+    assert max(worst.values()) < 1e-3, worst
+
+
+def test_flow_projection_closed_form():
+    """A single opaque splat moving by m: flow = projection of (backprojected point + m) minus the
+    pixel (splat.cpp:315-333); valid where covered and in front."""
+    cam = Cam(16, 16, 20.0, cx=8.0, cy=8.0)
+    sc = orc.OScene(np.array([[0.0, 0.0, 2.0]]), np.log(np.full((1, 3), 0.5)), np.array([[1.0, 0, 0, 0]]),
+                    np.array([8.0]), np.zeros((1, 16)), 0, F_DEFAULT, 1.0, C_LIGHT)
+    sc.motion_fwd = np.array([[0.1, -0.05, 0.0]])
+    sc.motion_bwd = np.array([[0.0, 0.0, -3.0]])  # moves behind the camera: bwd flow invalid
+    ext = orc.OraclePass(sc, cam, Opts()).forward_ext()
+    out = orc.OraclePass(sc, cam, Opts()).forward()
+    y, x = 8, 8
+    SW = out["weight"][y, x]
+    depth = out["depth"][y, x]
+    d = np.array([(x + 0.5 - 8.0) / 20.0, (y + 0.5 - 8.0) / 20.0, 1.0])
+    xd = depth * d / np.linalg.norm(d) + ext["motion_fwd_acc"][:, y, x]
+    assert ext["flow_valid"][0, y, x] == 1.0 and SW > 0.9
+    assert np.isclose(ext["flow_fwd"][0, y, x], 20.0 * xd[0] / xd[2] + 8.0 - (x + 0.5), atol=1e-12)
+    assert np.isclose(ext["flow_fwd"][1, y, x], 20.0 * xd[1] / xd[2] + 8.0 - (y + 0.5), atol=1e-12)
+    assert ext["flow_valid"][1, y, x] == 0.0
