@@ -93,11 +93,13 @@ struct Gaussian {
     std::array<double, 4> rotation{1, 0, 0, 0};  // (w, x, y, z)
     double opacity_logit = 0.0;
     std::array<double, kShCoeffCount> reflectivity_sh{};
+    std::array<std::array<double, 3>, kShCoeffCount> color_sh{};  // color_sh(k, c) = color_sh[k][c]
 };
 
 struct CanonicalScene {
     std::vector<Gaussian> gaussians;
     std::array<double, 4> bg_quad{0, 0, 0, 0};
+    std::array<double, 3> bg_color{0, 0, 0};
     int sh_degree = 0;  // 0..3: reflectivity SH degree evaluated on the GPU
     ToFConfig tof;
     int size() const { return static_cast<int>(gaussians.size()); }
@@ -107,13 +109,16 @@ inline double sigmoid(double x) { return 1.0 / (1.0 + std::exp(-x)); }
 inline double logit(double p) { return std::log(p / (1.0 - p)); }
 
 // ---- render API (splat.hpp:13-117) -----------------------------------------
-struct RenderChannels {  // the ToF channels (colour / flow are outside this path)
+struct RenderChannels {
+    bool color = false;
     bool quad = true;
     bool phasor = false;
     bool depth = true;
     bool distortion = false;
+    bool flow = false;  // implies depth (backprojection needs it)
 };
 struct Backgrounds {
+    std::array<double, 3> color{0, 0, 0};
     std::array<double, 4> quad{0, 0, 0, 0};
     std::array<double, 2> phasor{0, 0};
 };
@@ -131,22 +136,29 @@ struct RenderInput {
     const CanonicalScene* scene = nullptr;
     const CameraModel* camera = nullptr;
     const Matrix3Xd* positions = nullptr;  // optional override of the means (one column per Gaussian)
+    const Matrix3Xd* motion_fwd = nullptr;  // per-Gaussian motions for the flow channel
+    const Matrix3Xd* motion_bwd = nullptr;
     RenderOptions opts;
 };
 struct RenderedBuffers {
     int width = 0, height = 0;
-    Image quad, phasor, depth_raw, weight, depth, distortion, transmittance;
+    Image color, quad, phasor, depth_raw, weight, depth, distortion, transmittance;
+    Image motion_fwd_acc, motion_bwd_acc, flow_fwd, flow_bwd, flow_valid;
 };
 struct BufferGrads {  // leave an image empty to skip that channel (splat.hpp:68-77)
-    Image d_quad, d_phasor;
+    Image d_color, d_quad, d_phasor;
     Image d_depth_raw, d_weight, d_distortion, d_transmittance;
+    Image d_motion_fwd_acc, d_motion_bwd_acc;
 };
 struct SceneGrads {
     Matrix3Xd d_position, d_log_scale;
     Matrix4Xd d_rotation;
     std::vector<double> d_opacity_logit;
     Matrix16Xd d_reflectivity_sh;
+    std::vector<std::array<std::array<double, 3>, kShCoeffCount>> d_color_sh;
+    Matrix3Xd d_motion_fwd, d_motion_bwd;
     std::array<double, 4> d_bg_quad{0, 0, 0, 0};
+    std::array<double, 3> d_bg_color{0, 0, 0};
     std::array<double, 2> d_bg_phasor{0, 0};
 };
 
@@ -178,6 +190,10 @@ public:
         d.frequency[0] = in.scene->tof.modulation_frequency;
         d.source_intensity = in.scene->tof.source_intensity;
         d.speed_of_light = in.scene->tof.speed_of_light;
+        const bool color = in.opts.channels.color;
+        d.color = color ? 1 : 0;
+        if (in.motion_fwd && in.motion_fwd->cols() != n) throw std::runtime_error("render: motion_fwd count mismatch");
+        if (in.motion_bwd && in.motion_bwd->cols() != n) throw std::runtime_error("render: motion_bwd count mismatch");
         tsb_scene* s = nullptr;
         tsb_check(tsb_scene_create(ctx, &d, &s));
         scene_.reset(s);
@@ -200,6 +216,14 @@ public:
                 for (int k = 0; k < 16; ++k) sh[16 * (size_t)i + k] = (float)in.scene->gaussians[i].reflectivity_sh[k];
             tsb_check(tsb_scene_set_sh(s, TSB_HOST, sh.data()));
         }
+        if (color) {
+            std::vector<float> cs(48 * (size_t)n);
+            for (int i = 0; i < n; ++i)
+                for (int c = 0; c < 3; ++c)
+                    for (int k = 0; k < 16; ++k)
+                        cs[48 * (size_t)i + 16 * c + k] = (float)in.scene->gaussians[i].color_sh[k][c];
+            tsb_check(tsb_scene_set_color(s, TSB_HOST, cs.data()));
+        }
         tsb_pass* p = nullptr;
         tsb_check(tsb_pass_create(ctx, &p));
         pass_.reset(p);
@@ -211,9 +235,23 @@ public:
         opt_ = tsb_render_options{o.alpha_threshold, o.transmittance_floor, o.dilation, o.sigma_cutoff,
                                   o.coverage_eps, o.tile_size, TSB_CH_QUAD | TSB_CH_DEPTH | TSB_CH_PHASOR, {}, {}};
         if (o.channels.distortion) opt_.channels |= TSB_CH_DISTORTION;
+        if (o.channels.color) opt_.channels |= TSB_CH_COLOR;
+        if (o.channels.flow) opt_.channels |= TSB_CH_FLOW;
         for (int k = 0; k < 4; ++k) opt_.bg_quad[k] = o.bg.quad[k];
         for (int k = 0; k < 2; ++k) opt_.bg_phasor[k] = o.bg.phasor[k];
+        for (int k = 0; k < 3; ++k) opt_.bg_color[k] = o.bg.color[k];
         tsb_check(tsb_pass_prepare(p, s, &cam_, &opt_, nullptr));
+        if (o.channels.flow && (in.motion_fwd || in.motion_bwd)) {
+            std::vector<float> m[2];
+            const Matrix3Xd* src[2] = {in.motion_fwd, in.motion_bwd};
+            for (int k = 0; k < 2; ++k) {
+                if (!src[k]) continue;
+                m[k].resize(3 * (size_t)n);
+                for (int i = 0; i < n; ++i)
+                    for (int a = 0; a < 3; ++a) m[k][3 * (size_t)i + a] = (float)(*src[k])(a, i);
+            }
+            tsb_check(tsb_pass_set_motion(p, TSB_HOST, src[0] ? m[0].data() : nullptr, src[1] ? m[1].data() : nullptr));
+        }
     }
 
     int visible_count() const {
@@ -235,6 +273,14 @@ public:
         out.transmittance = download(TSB_OUT_TRANSM, 1);
         if (in_.opts.channels.phasor) out.phasor = download(TSB_OUT_PHASOR, 2);
         if (in_.opts.channels.distortion) out.distortion = download(TSB_OUT_DISTORTION, 1);
+        if (in_.opts.channels.color) out.color = download(TSB_OUT_COLOR, 3);
+        if (in_.opts.channels.flow) {
+            out.motion_fwd_acc = download(TSB_OUT_MOTION_FWD_ACC, 3);
+            out.motion_bwd_acc = download(TSB_OUT_MOTION_BWD_ACC, 3);
+            out.flow_fwd = download(TSB_OUT_FLOW_FWD, 2);
+            out.flow_bwd = download(TSB_OUT_FLOW_BWD, 2);
+            out.flow_valid = download(TSB_OUT_FLOW_VALID, 2);
+        }
         forwarded_ = true;
         return out;
     }
@@ -244,18 +290,19 @@ public:
         const int n = in_.scene->size();
         tsb_check(tsb_scene_zero_grads(scene_.get()));
         const size_t HW = (size_t)in_.camera->width * in_.camera->height;
-        std::vector<float> f[6];
-        const Image* imgs[6] = {&up.d_quad, &up.d_phasor, &up.d_depth_raw, &up.d_weight, &up.d_distortion,
-                                &up.d_transmittance};
-        const int nch[6] = {4, 2, 1, 1, 1, 1};
-        const float* ptr[6] = {};
-        for (int i = 0; i < 6; ++i) {
+        std::vector<float> f[9];
+        const Image* imgs[9] = {&up.d_quad, &up.d_phasor, &up.d_depth_raw, &up.d_weight, &up.d_distortion,
+                                &up.d_transmittance, &up.d_color, &up.d_motion_fwd_acc, &up.d_motion_bwd_acc};
+        const int nch[9] = {4, 2, 1, 1, 1, 1, 3, 3, 3};
+        const float* ptr[9] = {};
+        for (int i = 0; i < 9; ++i) {
             if (imgs[i]->data.empty()) continue;
             if (imgs[i]->data.size() != nch[i] * HW) throw std::runtime_error("render_backward: upstream size mismatch");
             f[i].assign(imgs[i]->data.begin(), imgs[i]->data.end());
             ptr[i] = f[i].data();
         }
-        tsb_check(tsb_pass_backward_buffers(pass_.get(), TSB_HOST, ptr[0], ptr[1], ptr[2], ptr[3], ptr[4], ptr[5]));
+        tsb_check(tsb_pass_backward_ext(pass_.get(), TSB_HOST, ptr[0], ptr[1], ptr[2], ptr[3], ptr[4], ptr[5], ptr[6],
+                                        ptr[7], ptr[8]));
         std::vector<float> dp(3 * (size_t)n), dl(3 * (size_t)n), dr(4 * (size_t)n), dop(n), drf(n);
         double dbg[8] = {0};
         tsb_check(tsb_scene_get_grads(scene_.get(), dp.data(), dl.data(), dr.data(), dop.data(), drf.data(), nullptr,
@@ -284,6 +331,28 @@ public:
             tsb_check(tsb_scene_get_sh(scene_.get(), dsh.data(), 1));
             for (int i = 0; i < n; ++i)
                 for (int k = 0; k < 16; ++k) g.d_reflectivity_sh(k, i) = dsh[16 * (size_t)i + k];
+        }
+        g.d_color_sh.assign(n, {});
+        g.d_motion_fwd = Matrix3Xd(n);
+        g.d_motion_bwd = Matrix3Xd(n);
+        if (in_.opts.channels.color) {
+            std::vector<float> dcs(48 * (size_t)n);
+            tsb_check(tsb_scene_get_color(scene_.get(), dcs.data(), 1));
+            for (int i = 0; i < n; ++i)
+                for (int c = 0; c < 3; ++c)
+                    for (int k = 0; k < 16; ++k) g.d_color_sh[i][k][c] = dcs[48 * (size_t)i + 16 * c + k];
+            double dbc[3] = {0, 0, 0};
+            tsb_check(tsb_scene_get_bg_color_grad(scene_.get(), dbc));
+            for (int k = 0; k < 3; ++k) g.d_bg_color[k] = dbc[k];
+        }
+        if (!up.d_color.data.empty() || !up.d_motion_fwd_acc.data.empty() || !up.d_motion_bwd_acc.data.empty()) {
+            std::vector<float> mf(3 * (size_t)n), mb(3 * (size_t)n);
+            tsb_check(tsb_pass_get_motion_grads(pass_.get(), mf.data(), mb.data()));
+            for (int i = 0; i < n; ++i)
+                for (int a = 0; a < 3; ++a) {
+                    g.d_motion_fwd(a, i) = mf[3 * (size_t)i + a];
+                    g.d_motion_bwd(a, i) = mb[3 * (size_t)i + a];
+                }
         }
         return g;
     }

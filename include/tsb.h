@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define TSB_ABI_VERSION 2
+#define TSB_ABI_VERSION 3
 
 enum {
     TSB_OK = 0,
@@ -56,7 +56,9 @@ enum {
     TSB_CH_COUNTS = 1u << 4,    /* per-pixel n_contrib / n_processed (parity) */
     TSB_CH_FULL_LISTS = 1u << 5, /* bin every tile's complete list (parity); default stops at termination */
     TSB_CH_PHASOR = 1u << 6,     /* (re, im) per frequency; always computed (free: 2x the quad sums) */
-    TSB_CH_DISTORTION = 1u << 7  /* sum_kl w_k w_l (d_k - d_l)^2; required for a distortion upstream */
+    TSB_CH_DISTORTION = 1u << 7, /* sum_kl w_k w_l (d_k - d_l)^2; required for a distortion upstream */
+    TSB_CH_COLOR = 1u << 8,      /* RGB from the colour SH (scene created with color = 1), + bg_color T */
+    TSB_CH_FLOW = 1u << 9        /* motion accumulators + projected flow (tsb_pass_set_motion) */
 };
 
 /* CameraModel (camera.hpp:9-17).  R row-major; p_cam = R p_world + t. */
@@ -80,6 +82,7 @@ typedef struct {
     uint32_t channels;          /* TSB_CH_* */
     double bg_quad[8];
     double bg_phasor[4];
+    double bg_color[3];         /* Backgrounds::color */
 } tsb_render_options;
 
 /* CanonicalScene header (scene.hpp:44-52) + ToFConfig (tof.hpp:13-21).
@@ -93,6 +96,8 @@ typedef struct {
     double frequency[2];  /* Hz */
     double source_intensity;
     double speed_of_light;
+    int32_t color;        /* 1: the scene carries colour SH (Gaussian::color_sh, 16 x 3) */
+    int32_t _pad;
 } tsb_scene_desc;
 
 /* Frame selector for dynamic scenes: rendered mean = (1-w)(x + d_k) + w (x + d_{k+1})
@@ -170,6 +175,13 @@ int tsb_scene_get_bg_grads(tsb_scene* s, double* d_bg_quad, double* d_bg_phasor)
  * tsb_scene_get_sh returns the parameters (grads = 0) or their accumulated gradients (grads = 1). */
 int tsb_scene_set_sh(tsb_scene* s, int where, const float* refl_sh);
 int tsb_scene_get_sh(tsb_scene* s, float* refl_sh, int grads);
+/* Colour SH (Gaussian::color_sh, scene.hpp:23-38; tsb_scene_desc.color = 1): [n][48], row i =
+ * Gaussian i's Eigen 16x3 block in storage order (coefficient k of channel c at 16 c + k).
+ * tsb_scene_get_color returns the parameters (grads = 0) or SceneGrads::d_color_sh (grads = 1). */
+int tsb_scene_set_color(tsb_scene* s, int where, const float* color_sh);
+int tsb_scene_get_color(tsb_scene* s, float* color_sh, int grads);
+/* SceneGrads::d_bg_color (splat.hpp:87-89), accumulated like the other background grads. */
+int tsb_scene_get_bg_color_grad(tsb_scene* s, double* d_bg_color);
 /* Adam moments (AdamState m_/v_, trainer.cpp:18-31), same layout as the params. */
 int tsb_scene_get_adam_state(tsb_scene* s, float* m_position, float* v_position);
 /* Densification statistic sum_i ||dL/dx_canon,i|| (trainer.cpp:381-384), n floats. */
@@ -180,6 +192,7 @@ int tsb_scene_get_densify_stat(tsb_scene* s, float* grad_norm_sum, int64_t* coun
 typedef struct {
     double position, log_scale, rotation, opacity, reflectivity, motion;
     double beta1, beta2, eps; /* AdamParams, trainer.hpp:14-18 */
+    double color;             /* colour SH (LrTable::color) */
 } tsb_adam_config;
 /* One fused AdamState::step over every group (trainer.cpp:18-31, 339-366) +
  * densify statistic (trainer.cpp:381-384); clears the gradients afterwards. */
@@ -240,10 +253,21 @@ enum {
     TSB_OUT_N_PROCESSED = 6, /* [H][W] i32 */
     TSB_OUT_D_QUAD = 7,    /* [4*n_freq][H][W] f32 upstream gradient */
     TSB_OUT_PHASOR = 8,    /* [2*n_freq][H][W] f32 (re, im) */
-    TSB_OUT_DISTORTION = 9 /* [H][W] f32 (TSB_CH_DISTORTION) */
+    TSB_OUT_DISTORTION = 9, /* [H][W] f32 (TSB_CH_DISTORTION) */
+    TSB_OUT_COLOR = 10,          /* [3][H][W] f32 (TSB_CH_COLOR) */
+    TSB_OUT_MOTION_FWD_ACC = 11, /* [3][H][W] f32 sum_k w_k motion_fwd_k (TSB_CH_FLOW) */
+    TSB_OUT_MOTION_BWD_ACC = 12, /* [3][H][W] */
+    TSB_OUT_FLOW_FWD = 13,       /* [2][H][W] pixel displacement */
+    TSB_OUT_FLOW_BWD = 14,       /* [2][H][W] */
+    TSB_OUT_FLOW_VALID = 15      /* [2][H][W] 1 where covered and projected in front (fwd, bwd) */
 };
 /* Device pointer and byte size of a pass-owned buffer. */
 int tsb_pass_output(tsb_pass* p, int which, void** dptr, size_t* bytes);
+/* Per-Gaussian motions of the frame (RenderInput::motion_fwd / motion_bwd, splat.hpp:46-47;
+ * n x 3 row-major = Matrix3Xd columns; NULL = zero) for TSB_CH_FLOW.  Call after prepare. */
+int tsb_pass_set_motion(tsb_pass* p, int where, const float* motion_fwd, const float* motion_bwd);
+/* SceneGrads::d_motion_fwd / d_motion_bwd (splat.hpp:86) of the last backward, n x 3 each. */
+int tsb_pass_get_motion_grads(tsb_pass* p, float* d_motion_fwd, float* d_motion_bwd);
 /* Copy a pass-owned buffer to host memory (synchronous). */
 int tsb_pass_download(tsb_pass* p, int which, void* host, size_t bytes);
 /* Enqueue the copy of a pass-owned buffer into host memory (pinned memory for
@@ -266,6 +290,12 @@ int tsb_pass_backward(tsb_pass* p, int where, const float* d_quad);
 int tsb_pass_backward_buffers(tsb_pass* p, int where, const float* d_quad, const float* d_phasor,
                               const float* d_depth_raw, const float* d_weight,
                               const float* d_distortion, const float* d_transmittance);
+/* The same with the colour / flow upstreams of BufferGrads (splat.hpp:73-77): d_color [3][H][W]
+ * (needs TSB_CH_COLOR in the forward), d_motion_fwd_acc / d_motion_bwd_acc [3][H][W] (TSB_CH_FLOW). */
+int tsb_pass_backward_ext(tsb_pass* p, int where, const float* d_quad, const float* d_phasor,
+                          const float* d_depth_raw, const float* d_weight, const float* d_distortion,
+                          const float* d_transmittance, const float* d_color, const float* d_motion_fwd_acc,
+                          const float* d_motion_bwd_acc);
 
 /* Parity / diagnostics: integer intermediates the reference keeps private
  * (splat.cpp:86-87).  Sizes: gidx V, rect 4V (x0,x1,y0,y1 per rank), tiles+1

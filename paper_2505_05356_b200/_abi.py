@@ -17,9 +17,10 @@ HEADER_PATH = Path(__file__).resolve().parent.parent / "include" / "tsb.h"
 TSB_OK, TSB_ERR_INVALID, TSB_ERR_CUDA, TSB_ERR_NOMEM, TSB_ERR_UNSUPPORTED, TSB_ERR_NCCL = range(6)
 TSB_HOST, TSB_DEVICE = 0, 1
 CH_QUAD, CH_DEPTH, CH_WEIGHT, CH_TRANSM, CH_COUNTS, CH_FULL_LISTS = 1, 2, 4, 8, 16, 32
-CH_PHASOR, CH_DISTORTION = 64, 128
+CH_PHASOR, CH_DISTORTION, CH_COLOR, CH_FLOW = 64, 128, 256, 512
 (OUT_QUAD, OUT_DEPTH_RAW, OUT_DEPTH, OUT_WEIGHT, OUT_TRANSM, OUT_N_CONTRIB, OUT_N_PROCESSED,
- OUT_D_QUAD, OUT_PHASOR, OUT_DISTORTION) = range(10)
+ OUT_D_QUAD, OUT_PHASOR, OUT_DISTORTION, OUT_COLOR, OUT_MOTION_FWD_ACC, OUT_MOTION_BWD_ACC, OUT_FLOW_FWD,
+ OUT_FLOW_BWD, OUT_FLOW_VALID) = range(16)
 
 
 STAGES = ["preprocess", "depth_sort", "scan", "binning", "tile_sort", "ranges", "raster_fwd", "fixup", "loss",
@@ -42,12 +43,13 @@ class RenderOptions(C.Structure):
     _fields_ = [("alpha_threshold", C.c_double), ("transmittance_floor", C.c_double), ("dilation", C.c_double),
                 ("sigma_cutoff", C.c_double), ("coverage_eps", C.c_double), ("tile_size", C.c_int32),
                 ("channels", C.c_uint32), ("bg_quad", C.c_double * 8),
-                ("bg_phasor", C.c_double * 4)]
+                ("bg_phasor", C.c_double * 4), ("bg_color", C.c_double * 3)]
 
 
 class SceneDesc(C.Structure):
     _fields_ = [("n", C.c_int32), ("n_keyframes", C.c_int32), ("sh_degree", C.c_int32), ("n_freq", C.c_int32),
-                ("frequency", C.c_double * 2), ("source_intensity", C.c_double), ("speed_of_light", C.c_double)]
+                ("frequency", C.c_double * 2), ("source_intensity", C.c_double), ("speed_of_light", C.c_double),
+                ("color", C.c_int32), ("_pad", C.c_int32)]
 
 
 class Frame(C.Structure):
@@ -57,7 +59,7 @@ class Frame(C.Structure):
 class AdamConfig(C.Structure):
     _fields_ = [("position", C.c_double), ("log_scale", C.c_double), ("rotation", C.c_double),
                 ("opacity", C.c_double), ("reflectivity", C.c_double), ("motion", C.c_double),
-                ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double)]
+                ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double), ("color", C.c_double)]
 
 
 _lib = None
@@ -102,6 +104,9 @@ SIGNATURES = {
     "tsb_scene_zero_grads": (C.c_int, [_vp]),
     "tsb_scene_set_sh": (C.c_int, [_vp, C.c_int, _vp]),
     "tsb_scene_get_sh": (C.c_int, [_vp, _fp, C.c_int]),
+    "tsb_scene_set_color": (C.c_int, [_vp, C.c_int, _vp]),
+    "tsb_scene_get_color": (C.c_int, [_vp, _fp, C.c_int]),
+    "tsb_scene_get_bg_color_grad": (C.c_int, [_vp, _dp]),
     "tsb_scene_get_adam_state": (C.c_int, [_vp, _fp, _fp]),
     "tsb_scene_get_densify_stat": (C.c_int, [_vp, _fp, _lp]),
     "tsb_scene_adam_step": (C.c_int, [_vp, C.POINTER(AdamConfig)]),
@@ -121,6 +126,9 @@ SIGNATURES = {
     "tsb_pass_wait": (C.c_int, [_vp]),
     "tsb_pass_backward": (C.c_int, [_vp, C.c_int, _vp]),
     "tsb_pass_backward_buffers": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "tsb_pass_backward_ext": (C.c_int, [_vp, C.c_int] + [_vp] * 9),
+    "tsb_pass_set_motion": (C.c_int, [_vp, C.c_int, _vp, _vp]),
+    "tsb_pass_get_motion_grads": (C.c_int, [_vp, _fp, _fp]),
     "tsb_pass_debug_keep_screen": (C.c_int, [_vp, C.c_int]),
     "tsb_pass_debug_set_list_capacity": (C.c_int, [_vp, C.c_uint32]),
     "tsb_scene_densify": (C.c_int, [_vp, _vp, C.c_double, C.POINTER(C.c_int32)]),

@@ -224,6 +224,12 @@ struct tsb_pass {
         int fixed = 0;
     };
     FwdGraph fwd[2];            // [0]: forward only, [1]: deferred prepare + forward
+    // colour / flow channels (tsb_ext.cu), allocated on first use
+    float4 *ext_col = nullptr, *ext_mf = nullptr, *ext_mb = nullptr, *ext_dmotion = nullptr;
+    float *ext_out = nullptr, *ext_screen = nullptr, *ext_up = nullptr;
+    double* ext_bg_part = nullptr;
+    int ext_n_cap = 0, ext_px_cap = 0, ext_blk_cap = 0;
+    bool has_mf = false, has_mb = false;
     bool count_live = false;
     bool prep_deferred = false; // prepare's device work not issued yet
 };
@@ -356,6 +362,7 @@ int64_t tsb_ctx_launch_count(tsb_ctx* c) { return c ? c->launches : 0; }
 // ---------------------------------------------------------------------------
 namespace {
 SceneK scenek(const tsb_scene* s);
+int color_base(const tsb_scene* s);
 // Refresh the time-independent cache after a parameter change (ctx stream).
 int refresh_param_cache(tsb_scene* s) {
     const SceneK S = scenek(s);
@@ -382,7 +389,8 @@ int tsb_scene_create(tsb_ctx* ctx, const tsb_scene_desc* d, tsb_scene** out) {
     tsb_scene* s = new tsb_scene();
     s->ctx = ctx;
     s->d = *d;
-    s->narrays = 3 + d->n_keyframes + (d->sh_degree > 0 ? 4 : 0);
+    if (d->color != 0 && d->color != 1) return fail(TSB_ERR_INVALID, "scene: color must be 0 or 1");
+    s->narrays = 3 + d->n_keyframes + (d->sh_degree > 0 ? 4 : 0) + (d->color ? kColorArrays : 0);
     const size_t nel = (size_t)s->narrays * (size_t)std::max(d->n, 1);
     int rc = TSB_OK;
     if ((rc = dev_alloc(&s->params, nel)) || (rc = dev_alloc(&s->grads, nel)) || (rc = dev_alloc(&s->m, nel)) ||
@@ -606,6 +614,71 @@ int tsb_scene_get_sh(tsb_scene* s, float* refl_sh, int grads) {
     return TSB_OK;
 }
 
+int tsb_scene_set_color(tsb_scene* s, int where, const float* color_sh) {
+    if (s && s->d.n == 0 && s->d.color) return TSB_OK;  // nothing to copy (empty vector data may be null)
+    if (!s || !color_sh) return fail(TSB_ERR_INVALID, "tsb_scene_set_color: null argument");
+    if (!s->d.color) return fail(TSB_ERR_INVALID, "tsb_scene_set_color: scene was created without colour");
+    if (where != TSB_HOST && where != TSB_DEVICE) return fail(TSB_ERR_INVALID, "bad memory kind");
+    TSB_CUDA(cudaSetDevice(s->ctx->device));
+    int rc;
+    if ((rc = tsb_ctx_join(s->ctx))) return rc;
+    const int n = s->d.n;
+    if (n == 0) return TSB_OK;
+    cudaStream_t st = s->ctx->stream;
+    const float* src = color_sh;
+    float* tmp = nullptr;
+    if (where == TSB_HOST) {
+        if ((rc = dev_alloc(&tmp, (size_t)48 * n))) return rc;
+        TSB_CUDA(cudaMemcpyAsync(tmp, color_sh, sizeof(float) * 48 * (size_t)n, cudaMemcpyHostToDevice, st));
+        src = tmp;
+    }
+    launch_pack_rows(s->params + (size_t)color_base(s) * n, src, n, kColorArrays, 4, st);
+    s->ctx->launches += 1;
+    TSB_CHECK_LAUNCH();
+    TSB_CUDA(cudaStreamSynchronize(st));
+    if (tmp) cudaFree(tmp);
+    TSB_CUDA(cudaEventRecord(s->params_ev, st));
+    return TSB_OK;
+}
+
+int tsb_scene_get_color(tsb_scene* s, float* color_sh, int grads) {
+    if (s && s->d.n == 0 && s->d.color) return TSB_OK;
+    if (!s || !color_sh) return fail(TSB_ERR_INVALID, "tsb_scene_get_color: null argument");
+    if (!s->d.color) return fail(TSB_ERR_INVALID, "tsb_scene_get_color: scene was created without colour");
+    if (grads) {
+        int rc0 = settle_all(s->ctx);
+        if (rc0) return rc0;
+    }
+    TSB_CUDA(cudaSetDevice(s->ctx->device));
+    const int n = s->d.n;
+    if (n == 0) return TSB_OK;
+    cudaStream_t st = s->ctx->stream;
+    if (grads) TSB_CUDA(cudaStreamWaitEvent(st, s->grads_ev, 0));
+    float* tmp = nullptr;
+    int rc;
+    if ((rc = dev_alloc(&tmp, (size_t)48 * n))) return rc;
+    launch_unpack_rows((grads ? s->grads : s->params) + (size_t)color_base(s) * n, tmp, n, kColorArrays, 4, st);
+    s->ctx->launches += 1;
+    TSB_CUDA(cudaMemcpyAsync(color_sh, tmp, sizeof(float) * 48 * (size_t)n, cudaMemcpyDeviceToHost, st));
+    TSB_CUDA(cudaStreamSynchronize(st));
+    cudaFree(tmp);
+    return TSB_OK;
+}
+
+int tsb_scene_get_bg_color_grad(tsb_scene* s, double* d_bg_color) {
+    if (!s || !d_bg_color) return fail(TSB_ERR_INVALID, "null argument");
+    {
+        int rc0 = settle_all(s->ctx);
+        if (rc0) return rc0;
+    }
+    TSB_CUDA(cudaSetDevice(s->ctx->device));
+    TSB_CUDA(cudaStreamWaitEvent(s->ctx->stream, s->grads_ev, 0));
+    double* h = d_bg_color;
+    TSB_CUDA(cudaMemcpyAsync(h, s->stats + kStatBgColor, sizeof(double) * 3, cudaMemcpyDeviceToHost, s->ctx->stream));
+    TSB_CUDA(cudaStreamSynchronize(s->ctx->stream));
+    return TSB_OK;
+}
+
 int tsb_scene_zero_grads(tsb_scene* s) {
     if (!s) return fail(TSB_ERR_INVALID, "null scene");
     {
@@ -669,6 +742,9 @@ int tsb_scene_adam_step(tsb_scene* s, const tsb_adam_config* cfg) {
     if (s->d.sh_degree > 0)  // reflectivity SH coefficients 1..15 use the reflectivity rate
         for (int a = 0; a < 4; ++a)
             for (int c = 0; c < (a < 3 ? 4 : 3); ++c) lr[(size_t)(3 + s->d.n_keyframes + a) * 4 + c] = cfg->reflectivity;
+    if (s->d.color)  // colour SH: LrTable::color (trainer.cpp:363-365)
+        for (int a = 0; a < kColorArrays; ++a)
+            for (int c = 0; c < 4; ++c) lr[(size_t)(color_base(s) + a) * 4 + c] = cfg->color;
     {
         Stage sg(s->ctx, TSB_STAGE_ADAM, s->ctx->stream);
         launch_adam(s->params, s->grads, s->m, s->v, s->d.n, s->narrays, lr.data(), cfg->beta1, cfg->beta2,
@@ -974,6 +1050,9 @@ PixK pixk(tsb_pass* p) {
     return px;
 }
 
+// first colour SH array: after pos_op, scale_amp, quat, the keyframe offsets and the reflectivity SH
+int color_base(const tsb_scene* s) { return 3 + s->d.n_keyframes + (s->d.sh_degree > 0 ? 4 : 0); }
+
 SceneK scenek(const tsb_scene* s) {
     SceneK k{};
     k.n = s->d.n;
@@ -990,10 +1069,13 @@ SceneK scenek(const tsb_scene* s) {
     k.quat = s->params + 2 * n;
     k.motion = s->params + 3 * n;
     k.sh = s->d.sh_degree > 0 ? s->params + (3 + (size_t)s->d.n_keyframes) * n : nullptr;
+    k.color_sh = s->d.color ? s->params + (size_t)color_base(s) * n : nullptr;
     k.cov6 = s->pcache;
     k.opac = s->pcache + 6 * n;
     return k;
 }
+
+int ensure_ext(tsb_pass* p);
 
 int read_visible(tsb_pass* p) {
     int rc0 = flush_prepare(p);
@@ -1023,6 +1105,8 @@ void tsb_pass_destroy(tsb_pass* p) {
     dev_free(p->counters); dev_free(p->list_off); dev_free(p->fx_work_n);
     dev_free(p->loss_part); dev_free(p->bg_part); dev_free(p->loss_dev); dev_free(p->chw);
     dev_free(p->ssim_g); dev_free(p->ssim_part);
+    dev_free(p->ext_col); dev_free(p->ext_mf); dev_free(p->ext_mb); dev_free(p->ext_dmotion);
+    dev_free(p->ext_out); dev_free(p->ext_screen); dev_free(p->ext_up); dev_free(p->ext_bg_part);
     if (p->pinned) cudaFreeHost(p->pinned);
     if (p->done_ev) cudaEventDestroy(p->done_ev);
     for (auto& fg : p->fwd)
@@ -1086,6 +1170,7 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     for (int c = 0; c < 8; ++c) O.bg_quad[c] = c < 4 * p->nf ? opt->bg_quad[c] : 0.0;
     for (int c = 0; c < 4; ++c) O.bg_phasor[c] = c < 2 * p->nf ? opt->bg_phasor[c] : 0.0;
     O.dist = (opt->channels & TSB_CH_DISTORTION) ? 1 : 0;
+    for (int c = 0; c < 3; ++c) O.bg_color[c] = opt->bg_color[c];
     p->ntiles = O.tiles_x * O.tiles_y;
     if (p->ntiles > 65536) return fail(TSB_ERR_UNSUPPORTED, "render: more than 65536 tiles");
     p->nblocks = p->ntiles * O.sub * O.sub;
@@ -1110,6 +1195,8 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     }
     if ((rc = ensure_vals(p, std::max<uint64_t>({(uint64_t)n * 8, (uint64_t)p->ntiles * 1024, 1u << 20}))))
         return rc;
+    p->has_mf = p->has_mb = false;  // RenderInput::motion_* belong to one frame
+    if ((p->channels & (TSB_CH_COLOR | TSB_CH_FLOW)) && (rc = ensure_ext(p))) return rc;
 
     // The device work (preprocess + depth sort) is deferred: it becomes the head of
     // the forward graph, or is issued eagerly by flush_prepare when something reads
@@ -1149,6 +1236,70 @@ int tsb_pass_num_keys(tsb_pass* p, int64_t* out) {
 }
 
 namespace {
+
+// fp64 fix-up arguments of the pass's current chunk plan.
+FixupK fixk(tsb_pass* p) {
+    const int total_chunks = (int)p->chunk_seg0.size();
+    FixupK fx;
+    fx.ranges_all = p->ranges_all;
+    fx.nchunks = std::max(total_chunks, 1);
+    fx.chunk_rank0 = p->chunk_rank0;
+    fx.binned_end_rank = total_chunks ? (p->chunk_seg0.back() + p->chunk_nseg.back()) * kSeg : 0;
+    fx.vals = p->vals;
+    fx.sorted_gidx = p->sorted;
+    fx.rect = p->rect;
+    fx.n_visible = p->counters;
+    fx.overflow = p->counters + 2;
+    fx.stamp = p->fx_stamp;
+    fx.work = p->fx_work;
+    fx.work_n = p->fx_work_n;
+    fx.cache = p->fx_cache;
+    return fx;
+}
+
+// Colour / flow buffers, allocated on first use.
+int ensure_ext(tsb_pass* p) {
+    const int n = std::max(p->scene->d.n, 1), npx = std::max(p->W * p->H, 1), nb = std::max(p->nblocks, 1);
+    int rc;
+    if (n > p->ext_n_cap) {
+        dev_free(p->ext_col); dev_free(p->ext_mf); dev_free(p->ext_mb); dev_free(p->ext_dmotion);
+        dev_free(p->ext_screen);
+        p->ext_n_cap = 0;
+        if ((rc = dev_alloc(&p->ext_col, n)) || (rc = dev_alloc(&p->ext_mf, n)) || (rc = dev_alloc(&p->ext_mb, n)) ||
+            (rc = dev_alloc(&p->ext_dmotion, (size_t)2 * n)) || (rc = dev_alloc(&p->ext_screen, (size_t)9 * n)))
+            return rc;
+        TSB_CUDA(cudaMemsetAsync(p->ext_screen, 0, sizeof(float) * 9 * (size_t)n, p->stream));
+        TSB_CUDA(cudaMemsetAsync(p->ext_dmotion, 0, sizeof(float4) * 2 * (size_t)n, p->stream));
+        p->ext_n_cap = n;
+    }
+    if (npx > p->ext_px_cap) {
+        dev_free(p->ext_out); dev_free(p->ext_up);
+        p->ext_px_cap = 0;
+        if ((rc = dev_alloc(&p->ext_out, (size_t)kExtPlanes * npx)) || (rc = dev_alloc(&p->ext_up, (size_t)9 * npx)))
+            return rc;
+        p->ext_px_cap = npx;
+    }
+    if (nb > p->ext_blk_cap) {
+        dev_free(p->ext_bg_part);
+        p->ext_blk_cap = 0;
+        if ((rc = dev_alloc(&p->ext_bg_part, (size_t)3 * nb))) return rc;
+        p->ext_blk_cap = nb;
+    }
+    return TSB_OK;
+}
+
+ExtK extk(tsb_pass* p) {
+    ExtK E{};
+    E.col = (p->channels & TSB_CH_COLOR) && p->scene->d.color ? p->ext_col : nullptr;
+    E.mf = p->has_mf ? p->ext_mf : nullptr;
+    E.mb = p->has_mb ? p->ext_mb : nullptr;
+    E.out = p->ext_out;
+    E.screen = p->ext_screen;
+    E.d_motion = p->ext_dmotion;
+    E.bg_part = p->ext_bg_part;
+    E.flow = (p->channels & TSB_CH_FLOW) ? 1 : 0;
+    return E;
+}
 
 // Chunked binning + forward composite (+ fused loss); see tsb_bin.cu.  Enqueues
 // every planned chunk; chunks without work return on the device.  Ends with an
@@ -1314,20 +1465,7 @@ int record_forward(tsb_pass* p, cudaStream_t st, bool loss, const ChW& chw, bool
         }
     }
     p->nchunks = nplanned;
-    FixupK fx;
-    fx.ranges_all = p->ranges_all;
-    fx.nchunks = nplanned;
-    fx.chunk_rank0 = p->chunk_rank0;
-    fx.binned_end_rank = total_chunks ? (p->chunk_seg0.back() + p->chunk_nseg.back()) * kSeg : 0;
-    fx.vals = p->vals;
-    fx.sorted_gidx = p->sorted;
-    fx.rect = p->rect;
-    fx.n_visible = p->counters;
-    fx.overflow = p->counters + 2;
-    fx.stamp = p->fx_stamp;
-    fx.work = p->fx_work;
-    fx.work_n = p->fx_work_n;
-    fx.cache = p->fx_cache;
+    const FixupK fx = fixk(p);
     {
         Stage sg(p->ctx, TSB_STAGE_FIXUP, st);
         launch_fixup(scenek(p->scene), p->cam, p->opt, fd, fx, px, p->nf, st);
@@ -1442,6 +1580,18 @@ int enqueue_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw,
         p->count_live = false;
     }
     p->prep_deferred = false;
+    // chunks the backward walks (record_forward sets it too, but a replayed graph skips it)
+    p->nchunks = std::max((int)p->chunk_seg0.size(), 1);
+    if (p->channels & (TSB_CH_COLOR | TSB_CH_FLOW)) {
+        // colour / flow channels beside the graph (tsb_ext.cu); an aborted frame skips them
+        const ExtK E = extk(p);
+        const SceneK S = scenek(p->scene);
+        launch_ext_prep(S, p->cam, p->frame_dev, p->touched, E, p->counters + 2, st);
+        launch_ext_fwd(p->rec, S, p->cam, p->opt, p->frame_dev, p->ranges_all, p->nchunks, p->vals, fixk(p), pixk(p),
+                       p->nf, E, st);
+        p->ctx->launches += (E.col && S.n > 0 ? 1 : 0) + 1;
+        TSB_CHECK_LAUNCH();
+    }
     if (loss) {
         // scene loss accumulator += this pass's loss (serialised with other gradient writers)
         TSB_CUDA(cudaStreamWaitEvent(st, p->scene->grads_ev, 0));
@@ -1613,6 +1763,19 @@ int output_ptr(tsb_pass* p, int which, void** dptr, size_t* bytes) {
         case TSB_OUT_DISTORTION:
             if (!(p->channels & TSB_CH_DISTORTION)) return fail(TSB_ERR_INVALID, "distortion channel not enabled");
             ptr = p->out + ch_distortion(p->nf) * HW; b = HW * 4; break;
+        case TSB_OUT_COLOR:
+            if (!(p->channels & TSB_CH_COLOR)) return fail(TSB_ERR_INVALID, "colour channel not enabled");
+            ptr = p->ext_out; b = 3 * HW * 4; break;
+        case TSB_OUT_MOTION_FWD_ACC:
+        case TSB_OUT_MOTION_BWD_ACC:
+        case TSB_OUT_FLOW_FWD:
+        case TSB_OUT_FLOW_BWD:
+        case TSB_OUT_FLOW_VALID: {
+            if (!(p->channels & TSB_CH_FLOW)) return fail(TSB_ERR_INVALID, "flow channel not enabled");
+            static const int plane[5] = {3, 6, 9, 11, 13}, planes[5] = {3, 3, 2, 2, 2};
+            const int i = which - TSB_OUT_MOTION_FWD_ACC;
+            ptr = p->ext_out + plane[i] * HW; b = planes[i] * HW * 4; break;
+        }
         default: return fail(TSB_ERR_INVALID, "unknown output");
     }
     *dptr = ptr;
@@ -1669,15 +1832,27 @@ int enqueue_backward(tsb_pass* p, const UpK& up) {
     float dpsi[2];
     for (int f = 0; f < p->nf; ++f) dpsi[f] = (float)(4.0 * M_PI * s->d.frequency[f] / s->d.speed_of_light);
     const PixK px = pixk(p);
+    const bool ext = up.color || up.mf || up.mb;
+    const ExtK E = extk(p);
     {
         // per-pass outputs only (screen gradients, background partials): overlaps other passes
         Stage sg(p->ctx, TSB_STAGE_RASTER_BWD, st);
         launch_raster_bwd(p->rec, p->ranges_all, p->nchunks, p->vals, p->opt, p->W, p->H, p->nf, dpsi, px, up,
                           p->screen, s->d.n, p->bg_part, st);
+        if (ext) {  // colour / motion upstreams: adds to the same screen gradients (tsb_ext.cu)
+            TSB_CUDA(cudaMemsetAsync(p->ext_dmotion, 0, sizeof(float4) * 2 * (size_t)std::max(s->d.n, 1), st));
+            launch_ext_bwd(p->rec, p->opt, p->W, p->H, p->nf, p->ranges_all, p->nchunks, p->vals, px, up, E,
+                           p->screen, s->d.n, st);
+            p->ctx->launches += 1;
+        }
     }
     // scene gradient writers are serialised by the scene's event chain
     TSB_CUDA(cudaStreamWaitEvent(st, s->grads_ev, 0));
     launch_reduce_partials(p->bg_part, p->nblocks, 6 * p->nf, s->stats + kStatBg, 1.0, px.abort, st);
+    if (ext) {
+        launch_reduce_partials(p->ext_bg_part, p->nblocks, 3, s->stats + kStatBgColor, 1.0, px.abort, st);
+        p->ctx->launches += 1;
+    }
     if (p->keep_screen) {
         dev_free(p->screen_keep);
         int rc;
@@ -1689,6 +1864,10 @@ int enqueue_backward(tsb_pass* p, const UpK& up) {
         Stage sg(p->ctx, TSB_STAGE_CHAIN, st);
         // an aborted frame left the screen gradients zero: the chain adds nothing
         launch_chain(scenek(s), p->cam, p->opt, p->frame, p->touched, p->screen, s->grads, st);
+        if (ext) {
+            launch_chain_ext(scenek(s), p->cam, p->frame, p->touched, E, s->grads, st);
+            p->ctx->launches += 1;
+        }
     }
     p->ctx->launches += 3;
     TSB_CHECK_LAUNCH();
@@ -1734,7 +1913,19 @@ int tsb_pass_backward(tsb_pass* p, int where, const float* d_quad) {
 int tsb_pass_backward_buffers(tsb_pass* p, int where, const float* d_quad, const float* d_phasor,
                               const float* d_depth_raw, const float* d_weight, const float* d_distortion,
                               const float* d_transmittance) {
+    return tsb_pass_backward_ext(p, where, d_quad, d_phasor, d_depth_raw, d_weight, d_distortion, d_transmittance,
+                                 nullptr, nullptr, nullptr);
+}
+
+int tsb_pass_backward_ext(tsb_pass* p, int where, const float* d_quad, const float* d_phasor,
+                          const float* d_depth_raw, const float* d_weight, const float* d_distortion,
+                          const float* d_transmittance, const float* d_color, const float* d_motion_fwd_acc,
+                          const float* d_motion_bwd_acc) {
     if (!p) return fail(TSB_ERR_INVALID, "null pass");
+    if (d_color && !(p->channels & TSB_CH_COLOR))
+        return fail(TSB_ERR_INVALID, "backward: a colour upstream needs the colour channel in the forward");
+    if ((d_motion_fwd_acc || d_motion_bwd_acc) && !(p->channels & TSB_CH_FLOW))
+        return fail(TSB_ERR_INVALID, "backward: a motion upstream needs the flow channel in the forward");
     if (!p->forwarded) return fail(TSB_ERR_INVALID, "backward requires a forward pass");
     if (where != TSB_HOST && where != TSB_DEVICE) return fail(TSB_ERR_INVALID, "bad memory kind");
     if (d_distortion && !(p->channels & TSB_CH_DISTORTION))
@@ -1745,19 +1936,77 @@ int tsb_pass_backward_buffers(tsb_pass* p, int where, const float* d_quad, const
     UpK u{};
     u.quad = d_quad; u.phasor = d_phasor; u.depth_raw = d_depth_raw; u.weight = d_weight;
     u.distortion = d_distortion; u.transm = d_transmittance;
+    u.color = d_color; u.mf = d_motion_fwd_acc; u.mb = d_motion_bwd_acc;
     if (where == TSB_HOST) {
-        const float* srcs[6] = {d_quad, d_phasor, d_depth_raw, d_weight, d_distortion, d_transmittance};
-        float* dsts[6] = {p->d_quad, p->up_extra, p->up_extra + 4 * HW, p->up_extra + 5 * HW,
-                          p->up_extra + 6 * HW, p->up_extra + 7 * HW};
-        const size_t planes[6] = {(size_t)4 * p->nf, (size_t)2 * p->nf, 1, 1, 1, 1};
-        const float** outs[6] = {&u.quad, &u.phasor, &u.depth_raw, &u.weight, &u.distortion, &u.transm};
-        for (int i = 0; i < 6; ++i) {
+        const float* srcs[9] = {d_quad, d_phasor, d_depth_raw, d_weight, d_distortion, d_transmittance,
+                                d_color, d_motion_fwd_acc, d_motion_bwd_acc};
+        float* dsts[9] = {p->d_quad, p->up_extra, p->up_extra + 4 * HW, p->up_extra + 5 * HW,
+                          p->up_extra + 6 * HW, p->up_extra + 7 * HW, p->ext_up, p->ext_up + 3 * HW,
+                          p->ext_up + 6 * HW};
+        const size_t planes[9] = {(size_t)4 * p->nf, (size_t)2 * p->nf, 1, 1, 1, 1, 3, 3, 3};
+        const float** outs[9] = {&u.quad, &u.phasor, &u.depth_raw, &u.weight, &u.distortion, &u.transm,
+                                 &u.color, &u.mf, &u.mb};
+        for (int i = 0; i < 9; ++i) {
             if (!srcs[i]) continue;
             TSB_CUDA(cudaMemcpyAsync(dsts[i], srcs[i], planes[i] * HW * sizeof(float), cudaMemcpyHostToDevice, st));
             *outs[i] = dsts[i];
         }
     }
     return run_backward(p, u);
+}
+
+int tsb_pass_set_motion(tsb_pass* p, int where, const float* motion_fwd, const float* motion_bwd) {
+    if (!p) return fail(TSB_ERR_INVALID, "null pass");
+    if (!p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
+    if (where != TSB_HOST && where != TSB_DEVICE) return fail(TSB_ERR_INVALID, "bad memory kind");
+    TSB_CUDA(cudaSetDevice(p->ctx->device));
+    if (p->pending) {  // the motions belong to the next forward of this frame
+        int rc0 = settle(p);
+        if (rc0) return rc0;
+    }
+    int rc;
+    if ((rc = ensure_ext(p))) return rc;
+    const int n = p->scene->d.n;
+    cudaStream_t st = p->stream;
+    const float* src[2] = {motion_fwd, motion_bwd};
+    float4* dst[2] = {p->ext_mf, p->ext_mb};
+    for (int k = 0; k < 2; ++k) {
+        if (!src[k] || n == 0) continue;
+        const float* d = src[k];
+        if (where == TSB_HOST) {  // stage through the (idle) screen buffer's first 3n floats
+            TSB_CUDA(cudaMemcpyAsync(p->ext_screen, src[k], sizeof(float) * 3 * (size_t)n, cudaMemcpyHostToDevice, st));
+            d = p->ext_screen;
+        }
+        launch_pack_rows(dst[k], d, n, 1, 3, st);
+        p->ctx->launches += 1;
+        if (where == TSB_HOST)
+            TSB_CUDA(cudaMemsetAsync(p->ext_screen, 0, sizeof(float) * 3 * (size_t)n, st));
+    }
+    TSB_CHECK_LAUNCH();
+    p->has_mf = motion_fwd != nullptr;
+    p->has_mb = motion_bwd != nullptr;
+    return TSB_OK;
+}
+
+int tsb_pass_get_motion_grads(tsb_pass* p, float* d_motion_fwd, float* d_motion_bwd) {
+    if (!p) return fail(TSB_ERR_INVALID, "null pass");
+    if (!p->ext_dmotion) return fail(TSB_ERR_INVALID, "no colour / flow backward has run on this pass");
+    int rc = settle(p);
+    if (rc) return rc;
+    const int n = p->scene->d.n;
+    if (n == 0) return TSB_OK;
+    cudaStream_t st = p->stream;
+    float* out[2] = {d_motion_fwd, d_motion_bwd};
+    for (int k = 0; k < 2; ++k) {
+        if (!out[k]) continue;
+        float* tmp = nullptr;
+        if ((rc = dev_alloc(&tmp, (size_t)3 * n))) return rc;
+        launch_unpack_rows(p->ext_dmotion + (size_t)k * n, tmp, n, 1, 3, st);
+        TSB_CUDA(cudaMemcpyAsync(out[k], tmp, sizeof(float) * 3 * (size_t)n, cudaMemcpyDeviceToHost, st));
+        TSB_CUDA(cudaStreamSynchronize(st));
+        cudaFree(tmp);
+    }
+    return TSB_OK;
 }
 
 // ---- debug / parity ----

@@ -1,0 +1,472 @@
+// Colour and flow channels of RenderPass (TSB_CH_COLOR / TSB_CH_FLOW):
+//   forward   splat.cpp:273-294 (colour + motion accumulators), 301-334 (bg colour,
+//             backprojection of the composited depth and reprojection of x + motion);
+//   backward  splat.cpp:361-505 for the colour / motion upstreams;
+//   chain     splat.cpp:560-571 (colour SH, clamp-gated, + the view-direction term).
+//
+// These channels ride beside the ToF hot path instead of inside it: the forward
+// kernels of tsb_raster.cu keep their register budget, and the extra work is
+// paid only by frames that ask for colour or flow.
+//   k_ext_prep  per visible Gaussian: colour = clamp(color_sh^T b(view_dir)) in fp64;
+//   k_ext_fwd   per pixel: re-walks the tile lists the forward walked (up to the
+//               pixel's termination entry) with the forward's own decisions -- the
+//               same fp32 evaluation bits for ordinary pixels, the fp64 records of
+//               the fix-up for the pixels the fix-up recomposited -- and accumulates
+//               w_k (colour, motion_fwd, motion_bwd); the flow projection reads the
+//               final depth_raw / weight of the forward;
+//   k_ext_bwd   per pixel, back to front: the upstreams are all T-weighted linear
+//               channels, so they reduce to one scalar recursion
+//                 d_alpha += Tk (v_k - B),  B <- alpha v_k + (1 - alpha) B,
+//                 v_k = up_c . colour_k + up_mf . mf_k + up_mb . mb_k,  B_0 = up_c . bg_colour;
+//               the d_alpha part is linear, so its screen-space gradients are added
+//               to the ToF backward's (same buffer); the 9 per-entry terms w_k up
+//               go to the extension's own screen buffer;
+//   k_chain_ext per Gaussian: colour SH gradients (gated 0 < colour_raw < 1), the
+//               view-direction term into the position (and keyframe) gradients, and
+//               SceneGrads::d_motion_fwd / d_motion_bwd.
+// Compiled with -fmad=false (fp64 colour and records round as the oracle does); the
+// fp32 evaluation uses explicit-rounding intrinsics (tsb_raster.cuh), unaffected.
+#include <cuda_runtime.h>
+
+#include "tsb_fp64.cuh"
+#include "tsb_raster.cuh"
+
+namespace tsb {
+
+namespace {
+
+// color_raw = color_sh^T b(view_dir) (splat.cpp:163-173), fp64, same order as the oracle.
+struct Color64 {
+    double raw[3], view_dir[3], depth, b[16];
+};
+
+__device__ __forceinline__ float color_coef(const SceneK& S, int gi, int f) {
+    const float4 v = S.color_sh[(size_t)(f >> 2) * S.n + gi];
+    const int l = f & 3;
+    return l == 0 ? v.x : (l == 1 ? v.y : (l == 2 ? v.z : v.w));
+}
+
+__device__ __forceinline__ void color64(const SceneK& S, const CamK& C, const FrameK& F, int gi, Color64& c) {
+    double x[3], p[3];
+    frame_mean(S, F, gi, x);
+    const double* R = C.R;
+    for (int i = 0; i < 3; ++i) p[i] = R[i * 3 + 0] * x[0] + R[i * 3 + 1] * x[1] + R[i * 3 + 2] * x[2] + C.t[i];
+    c.depth = sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
+    for (int i = 0; i < 3; ++i) c.view_dir[i] = (x[i] - C.center[i]) / c.depth;
+    sh_basis64(c.view_dir, S.sh_degree, c.b);
+    for (int ch = 0; ch < 3; ++ch) {
+        double cr = 0.0;
+        if (S.color_sh)
+            for (int k = 0; k < 16; ++k) cr += (double)color_coef(S, gi, 16 * ch + k) * c.b[k];
+        c.raw[ch] = cr;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_ext_prep(SceneK S, CamK C, const FrameDev* __restrict__ fd,
+                                                  const uint32_t* __restrict__ touched, float4* __restrict__ col,
+                                                  const int32_t* __restrict__ abort) {
+    const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gi >= S.n || *abort || touched[gi] == 0u) return;
+    Color64 c;
+    color64(S, C, fd->F, gi, c);
+    col[gi] = make_float4((float)clampd(c.raw[0], 0.0, 1.0), (float)clampd(c.raw[1], 0.0, 1.0),
+                          (float)clampd(c.raw[2], 0.0, 1.0), 0.f);
+}
+
+struct PixMap {
+    int tile, x, y;
+    bool active;
+    float ox, oy, pcx, pcy;
+    size_t HW, o;
+};
+
+__device__ __forceinline__ PixMap pix_map(const OptK& O, int W, int H) {
+    PixMap m;
+    const int nsub = O.sub * O.sub;
+    m.tile = blockIdx.x / nsub;
+    const int sb = blockIdx.x % nsub, tid = threadIdx.x;
+    const int lx = (sb % O.sub) * kTile + (tid % kTile), ly = (sb / O.sub) * kTile + (tid / kTile);
+    m.x = (m.tile % O.tiles_x) * O.ts + lx;
+    m.y = (m.tile / O.tiles_x) * O.ts + ly;
+    m.active = lx < O.ts && ly < O.ts && m.x < W && m.y < H;
+    m.ox = (float)(m.x - (tid % kTile));
+    m.oy = (float)(m.y - (tid / kTile));
+    m.pcx = (float)(tid % kTile) + 0.5f;
+    m.pcy = (float)(tid / kTile) + 0.5f;
+    m.HW = (size_t)W * H;
+    m.o = m.active ? (size_t)m.y * W + m.x : 0;
+    return m;
+}
+
+__device__ __forceinline__ int block_max(int v, int* smax) {
+    for (int m = 16; m > 0; m >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, m));
+    if ((threadIdx.x & 31) == 0) smax[threadIdx.x >> 5] = v;
+    __syncthreads();
+    int b = 0;
+#pragma unroll
+    for (int i = 0; i < kRasterThreads / 32; ++i) b = max(b, smax[i]);
+    return b;
+}
+
+__device__ __forceinline__ float4 ld_or_zero(const float4* p, uint32_t i) {
+    return p ? p[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+__global__ void __launch_bounds__(kRasterThreads) k_ext_fwd(RecK rec, SceneK S, CamK C, OptK O,
+                                                            const FrameDev* __restrict__ fd,
+                                                            const uint4* __restrict__ ranges_all, int nchunks,
+                                                            const uint32_t* __restrict__ vals, FixupK fx, PixK px,
+                                                            int nf, ExtK E) {
+    __shared__ float4 sA[kRasterThreads], sB[kRasterThreads];
+    __shared__ float4 sC[kRasterThreads], sMf[kRasterThreads], sMb[kRasterThreads];
+    __shared__ uint32_t sg[kRasterThreads];
+    __shared__ int smax[kRasterThreads / 32];
+    if (*px.abort) return;
+    const int W = C.W, H = C.H, tid = threadIdx.x;
+    const PixMap m = pix_map(O, W, H);
+    const int ntiles = O.tiles_x * O.tiles_y;
+    int last = 0;
+    bool fixed = false;
+    if (m.active) {
+        const int l = px.last[m.o];
+        fixed = l < 0;
+        last = l & 0x7fffffff;
+    }
+    const int bmax = block_max(last, smax);
+    const FrameK F = fd->F;
+    const int stamp = fd->stamp;
+    float T = 1.f;
+    double Td = 1.0;
+    double acc[9];  // fp64 sums: the motion channels are signed and cancel
+#pragma unroll
+    for (int c = 0; c < 9; ++c) acc[c] = 0.0;
+    for (int c = 0; c < nchunks; ++c) {
+        const uint4 rg = ranges_all[(size_t)c * ntiles + m.tile];  // (start, len, cum)
+        if ((int)rg.z >= bmax) break;
+        const int n_here = min((int)rg.y, bmax - (int)rg.z);
+        for (int b0 = 0; b0 < n_here; b0 += kRasterThreads) {
+            const int nb = min(kRasterThreads, n_here - b0);
+            __syncthreads();
+            if (tid < nb) {
+                const uint32_t r = vals[rg.x + b0 + tid];
+                sg[tid] = r;
+                sA[tid] = stage_A(rec.A[r], m.ox, m.oy);
+                sB[tid] = rec.B[r];
+                sC[tid] = ld_or_zero(E.col, r);
+                sMf[tid] = ld_or_zero(E.mf, r);
+                sMb[tid] = ld_or_zero(E.mb, r);
+            }
+            __syncthreads();
+            const int jmax = min(nb, last - ((int)rg.z + b0));
+            for (int j = 0; j < jmax; ++j) {
+                float w;
+                if (!fixed) {  // the forward's fp32 decisions, bit for bit
+                    const float4 A = sA[j], B = sB[j];
+                    Eval ev;
+                    eval_entry(A, B, m.pcx, m.pcy, ev);
+                    if (ev.maha - O.cut2_f > 0.f) continue;
+                    eval_alpha(B, ev);
+                    if (ev.alpha - O.alpha_thr_f < 0.f) continue;
+                    w = ev.alpha * T;
+                    T = T * (1.f - ev.alpha);
+                } else {  // the fix-up's fp64 decisions (k_fixup, tsb_geom.cu)
+                    const int g = (int)sg[j];
+                    const Rec64 r = fx.stamp[g] == stamp ? fx.cache[g] : make_rec64(S, C, O, F, g);
+                    if (m.x < r.rect.x || m.x >= r.rect.y || m.y < r.rect.z || m.y >= r.rect.w) continue;
+                    const double dx = (m.x + 0.5) - r.m0.x, dy = (m.y + 0.5) - r.m0.y;
+                    const double maha = r.m0.z * dx * dx + 2.0 * r.m0.w * dx * dy + r.m1.x * dy * dy;
+                    if (maha > O.cut2 || maha < 0.0) continue;
+                    const double alpha = r.m1.y * exp(-0.5 * maha);
+                    if (alpha < O.alpha_thr) continue;
+                    w = (float)(alpha * Td);
+                    Td *= 1.0 - alpha;
+                }
+                const float4 cc = sC[j], mf = sMf[j], mb = sMb[j];
+                const double wd = w;
+                acc[0] = fma(wd, (double)cc.x, acc[0]);
+                acc[1] = fma(wd, (double)cc.y, acc[1]);
+                acc[2] = fma(wd, (double)cc.z, acc[2]);
+                acc[3] = fma(wd, (double)mf.x, acc[3]);
+                acc[4] = fma(wd, (double)mf.y, acc[4]);
+                acc[5] = fma(wd, (double)mf.z, acc[5]);
+                acc[6] = fma(wd, (double)mb.x, acc[6]);
+                acc[7] = fma(wd, (double)mb.y, acc[7]);
+                acc[8] = fma(wd, (double)mb.z, acc[8]);
+            }
+        }
+    }
+    if (!m.active) return;
+    const size_t HW = m.HW, o = m.o;
+    const double Tfin = px.out[ch_T(nf) * HW + o];
+    for (int c = 0; c < 3; ++c) E.out[c * HW + o] = (float)(acc[c] + O.bg_color[c] * Tfin);
+    for (int c = 3; c < 9; ++c) E.out[c * HW + o] = (float)acc[c];
+    for (int c = 9; c < kExtPlanes; ++c) E.out[c * HW + o] = 0.f;
+    if (!E.flow) return;
+    const double SW = px.out[ch_weight(nf) * HW + o];
+    if (!(SW > O.cov_eps)) return;
+    // cam.backproject (camera.hpp:34-43): optical centre + dist * normalize(R^T d_cam)
+    const double SD = px.out[ch_depth_raw(nf) * HW + o];
+    const double dist = SD / SW;
+    const double pcx = m.x + 0.5, pcy = m.y + 0.5;
+    const double dc[3] = {(pcx - C.cx) / C.fx, (pcy - C.cy) / C.fy, 1.0};
+    const double* R = C.R;
+    double dir[3];
+    for (int a = 0; a < 3; ++a) dir[a] = R[0 * 3 + a] * dc[0] + R[1 * 3 + a] * dc[1] + R[2 * 3 + a] * dc[2];
+    const double dn = sqrt(dir[0] * dir[0] + dir[1] * dir[1] + dir[2] * dir[2]);
+    double xd[3];
+    for (int a = 0; a < 3; ++a) xd[a] = C.center[a] + dist * (dir[a] / dn);
+    for (int k = 0; k < 2; ++k) {
+        double q[3], p[3];
+        for (int a = 0; a < 3; ++a) q[a] = xd[a] + acc[3 + 3 * k + a];
+        for (int i = 0; i < 3; ++i) p[i] = R[i * 3 + 0] * q[0] + R[i * 3 + 1] * q[1] + R[i * 3 + 2] * q[2] + C.t[i];
+        if (p[2] > 0.0) {
+            E.out[(9 + 2 * k) * HW + o] = (float)(C.fx * p[0] / p[2] + C.cx - pcx);
+            E.out[(10 + 2 * k) * HW + o] = (float)(C.fy * p[1] / p[2] + C.cy - pcy);
+            E.out[(13 + k) * HW + o] = 1.f;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kRasterThreads) k_ext_bwd(RecK rec, OptK O, int W, int H, int nf,
+                                                            const uint4* __restrict__ ranges_all, int nchunks,
+                                                            const uint32_t* __restrict__ vals, PixK px, UpK up,
+                                                            ExtK E, float* __restrict__ screen, int scap) {
+    __shared__ float4 sA[kRasterThreads], sB[kRasterThreads];
+    __shared__ float4 sC[kRasterThreads], sMf[kRasterThreads], sMb[kRasterThreads];
+    __shared__ uint32_t srank[kRasterThreads];
+    __shared__ float sacc[kRasterThreads][17];
+    __shared__ int smax[kRasterThreads / 32];
+    __shared__ float sbg[kRasterThreads / 32][3];
+    if (*px.abort) return;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const PixMap m = pix_map(O, W, H);
+    const int ntiles = O.tiles_x * O.tiles_y;
+    const size_t HW = m.HW, o = m.o;
+    int last = 0;
+    float Tnext = 0.f, Bx = 0.f;
+    float u[9], bgc[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int c = 0; c < 9; ++c) u[c] = 0.f;
+    if (m.active) {
+        last = px.last[o] & 0x7fffffff;
+        Tnext = px.T_pre[o];
+        const float Tf = px.out[ch_T(nf) * HW + o];
+        for (int c = 0; c < 3; ++c) {
+            if (up.color) {
+                u[c] = up.color[c * HW + o];
+                Bx = fmaf(u[c], (float)O.bg_color[c], Bx);
+                bgc[c] = u[c] * Tf;  // d_bg_color (splat.cpp:427-428)
+            }
+            if (up.mf) u[3 + c] = up.mf[c * HW + o];
+            if (up.mb) u[6 + c] = up.mb[c * HW + o];
+        }
+    }
+    for (int c = 0; c < 3; ++c) {
+        float v = bgc[c];
+        for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+        if (lane == 0) sbg[tid >> 5][c] = v;
+    }
+    int wmax = last;
+    for (int s = 16; s > 0; s >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, s));
+    if (lane == 0) smax[tid >> 5] = wmax;
+    for (int c = 0; c < 17; ++c) sacc[tid][c] = 0.f;
+    __syncthreads();
+    int bmax = 0;
+#pragma unroll
+    for (int i = 0; i < kRasterThreads / 32; ++i) bmax = max(bmax, smax[i]);
+    if (tid < 3) {
+        double s = 0.0;
+        for (int i = 0; i < kRasterThreads / 32; ++i) s += sbg[i][tid];
+        E.bg_part[(size_t)blockIdx.x * 3 + tid] = s;
+    }
+    bool first = true;
+    const float cut2 = O.cut2_f, thr = O.alpha_thr_f;
+    for (int c = nchunks - 1; c >= 0 && bmax > 0; --c) {
+        const uint4 rg = ranges_all[(size_t)c * ntiles + m.tile];
+        if ((int)rg.z >= bmax || rg.y == 0) continue;
+        const int n_here = min((int)rg.y, bmax - (int)rg.z);
+        const int nbatch = (n_here + kRasterThreads - 1) / kRasterThreads;
+        for (int bi = nbatch - 1; bi >= 0; --bi) {
+            const uint32_t b = rg.x + (uint32_t)bi * kRasterThreads;
+            const int nb = min(kRasterThreads, n_here - bi * kRasterThreads);
+            if (tid < nb) {
+                const uint32_t r = vals[b + tid];
+                srank[tid] = r;
+                sA[tid] = stage_A(rec.A[r], m.ox, m.oy);
+                sB[tid] = rec.B[r];
+                sC[tid] = ld_or_zero(E.col, r);
+                sMf[tid] = ld_or_zero(E.mf, r);
+                sMb[tid] = ld_or_zero(E.mb, r);
+            }
+            __syncthreads();
+            const int jtop = min(nb, wmax - ((int)rg.z + bi * kRasterThreads));
+            for (int j = jtop - 1; j >= 0; --j) {
+                const int el = (int)rg.z + bi * kRasterThreads + j;
+                bool contrib = false;
+                float ga[8], gb[8];
+                if (el < last) {
+                    const float4 Aa = sA[j], Bb = sB[j];
+                    Eval ev;
+                    eval_entry(Aa, Bb, m.pcx, m.pcy, ev);
+                    if (!(ev.maha - cut2 > 0.f)) {
+                        eval_alpha(Bb, ev);
+                        if (!(ev.alpha - thr < 0.f)) {
+                            contrib = true;
+                            const float om = 1.f - ev.alpha;
+                            const float Tk = first ? Tnext : __fdiv_rn(Tnext, om);
+                            first = false;
+                            Tnext = Tk;
+                            const float4 cc = sC[j], mf = sMf[j], mb = sMb[j];
+                            float v = u[0] * cc.x;
+                            v = fmaf(u[1], cc.y, v);
+                            v = fmaf(u[2], cc.z, v);
+                            v = fmaf(u[3], mf.x, v);
+                            v = fmaf(u[4], mf.y, v);
+                            v = fmaf(u[5], mf.z, v);
+                            v = fmaf(u[6], mb.x, v);
+                            v = fmaf(u[7], mb.y, v);
+                            v = fmaf(u[8], mb.z, v);
+                            const float d_alpha = Tk * (v - Bx);
+                            Bx = fmaf(ev.alpha, v, om * Bx);
+                            const float dpow = ev.alpha * d_alpha;
+                            const float w = ev.alpha * Tk;
+                            ga[0] = dpow * (Bb.x * ev.p);
+                            ga[1] = dpow * (Bb.y * ev.p + Bb.z * ev.q);
+                            ga[2] = -0.5f * ev.dx * ev.dx * dpow;
+                            ga[3] = -ev.dx * ev.dy * dpow;
+                            ga[4] = -0.5f * ev.dy * ev.dy * dpow;
+                            ga[5] = ev.g * d_alpha;
+                            ga[6] = w * u[0];
+                            ga[7] = w * u[1];
+#pragma unroll
+                            for (int k = 0; k < 7; ++k) gb[k] = w * u[2 + k];
+                            gb[7] = 0.f;
+                        }
+                    }
+                }
+                if (__any_sync(0xffffffffu, contrib)) {
+                    if (!contrib) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) ga[k] = gb[k] = 0.f;
+                    }
+                    const float s1 = reduce_scatter8(ga, lane);
+                    const float s2 = reduce_scatter8(gb, lane);
+                    if ((lane & 3) == 0) {
+                        const int vi = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+                        atomicAdd(&sacc[j][vi], s1);
+                        atomicAdd(&sacc[j][8 + vi], s2);
+                    }
+                }
+            }
+            __syncthreads();
+            if (tid < nb) {
+                const uint32_t r = srank[tid];
+                for (int k = 0; k < 15; ++k) {
+                    const float v = sacc[tid][k];
+                    if (v != 0.f) {
+                        if (k < 6) atomicAdd(&screen[(size_t)k * scap + r], v);
+                        else atomicAdd(&E.screen[(size_t)(k - 6) * scap + r], v);
+                    }
+                    sacc[tid][k] = 0.f;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(128) k_chain_ext(SceneK S, CamK C, FrameK F, const uint32_t* __restrict__ touched,
+                                                   ExtK E, float4* __restrict__ grads) {
+    const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gi >= S.n || touched[gi] == 0u) return;
+    const size_t n = (size_t)S.n;
+    float g[9];
+    bool any = false;
+    for (int c = 0; c < 9; ++c) {
+        g[c] = E.screen[c * n + gi];
+        any |= g[c] != 0.f;
+    }
+    if (!any) return;
+    for (int c = 0; c < 9; ++c) E.screen[c * n + gi] = 0.f;
+    if (E.d_motion) {  // SceneGrads::d_motion_fwd / d_motion_bwd (splat.cpp:646-647)
+        float4 a = E.d_motion[gi], b = E.d_motion[n + gi];
+        a.x += g[3]; a.y += g[4]; a.z += g[5];
+        b.x += g[6]; b.y += g[7]; b.z += g[8];
+        E.d_motion[gi] = a;
+        E.d_motion[n + gi] = b;
+    }
+    if (!S.color_sh || (g[0] == 0.f && g[1] == 0.f && g[2] == 0.f)) return;
+    Color64 c;
+    color64(S, C, F, gi, c);
+    double dcol[3];
+    for (int ch = 0; ch < 3; ++ch) dcol[ch] = (c.raw[ch] > 0.0 && c.raw[ch] < 1.0) ? (double)g[ch] : 0.0;
+    // d_color_sh[k][c] = b_k dcol_c  (flat 16 c + k)
+    float4* gc = grads + (S.color_sh - S.pos_op) + gi;
+    for (int a = 0; a < kColorArrays; ++a) {
+        float d[4];
+        for (int l = 0; l < 4; ++l) {
+            const int f = 4 * a + l;
+            d[l] = (float)(c.b[f & 15] * dcol[f >> 4]);
+        }
+        float4 v = gc[(size_t)a * n];
+        v.x += d[0]; v.y += d[1]; v.z += d[2]; v.w += d[3];
+        gc[(size_t)a * n] = v;
+    }
+    if (S.sh_degree == 0) return;  // the basis is constant: no view-direction term
+    // d_dir = Jb^T (color_sh dcol); view_dir = (x - C) / |x - C| feeds the position
+    double Jb[16][3];
+    sh_jacobian64(c.view_dir, S.sh_degree, Jb);
+    double d_dir[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < 16; ++k) {
+        double t = 0.0;
+        for (int ch = 0; ch < 3; ++ch) t += (double)color_coef(S, gi, 16 * ch + k) * dcol[ch];
+        for (int a = 0; a < 3; ++a) d_dir[a] += Jb[k][a] * t;
+    }
+    const double vd = c.view_dir[0] * d_dir[0] + c.view_dir[1] * d_dir[1] + c.view_dir[2] * d_dir[2];
+    double dpos[3];
+    for (int a = 0; a < 3; ++a) dpos[a] = (d_dir[a] - c.view_dir[a] * vd) / c.depth;
+    float4 g0 = grads[gi];
+    g0.x += (float)dpos[0]; g0.y += (float)dpos[1]; g0.z += (float)dpos[2];
+    grads[gi] = g0;
+    if (S.nk > 0) {
+        const double wa = 1.0 - F.w, wb = F.w;
+        float4* gm = grads + (size_t)(3 + F.key) * n + gi;
+        float4 a = *gm;
+        a.x += (float)(wa * dpos[0]); a.y += (float)(wa * dpos[1]); a.z += (float)(wa * dpos[2]);
+        *gm = a;
+        float4* gm2 = grads + (size_t)(3 + F.key + 1) * n + gi;
+        float4 b = *gm2;
+        b.x += (float)(wb * dpos[0]); b.y += (float)(wb * dpos[1]); b.z += (float)(wb * dpos[2]);
+        *gm2 = b;
+    }
+}
+
+}  // namespace
+
+void launch_ext_prep(const SceneK& S, const CamK& C, const FrameDev* fd, const uint32_t* touched, const ExtK& E,
+                     const int32_t* abort, cudaStream_t st) {
+    if (S.n <= 0 || !E.col) return;
+    k_ext_prep<<<(S.n + 255) / 256, 256, 0, st>>>(S, C, fd, touched, E.col, abort);
+}
+
+void launch_ext_fwd(const RecK& rec, const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd,
+                    const uint4* ranges_all, int nchunks, const uint32_t* vals, const FixupK& fx, const PixK& px,
+                    int nf, const ExtK& E, cudaStream_t st) {
+    const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
+    k_ext_fwd<<<grid, kRasterThreads, 0, st>>>(rec, S, C, O, fd, ranges_all, nchunks, vals, fx, px, nf, E);
+}
+
+void launch_ext_bwd(const RecK& rec, const OptK& O, int W, int H, int nf, const uint4* ranges_all, int nchunks,
+                    const uint32_t* vals, const PixK& px, const UpK& up, const ExtK& E, float* screen, int scap,
+                    cudaStream_t st) {
+    const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
+    k_ext_bwd<<<grid, kRasterThreads, 0, st>>>(rec, O, W, H, nf, ranges_all, nchunks, vals, px, up, E, screen, scap);
+}
+
+void launch_chain_ext(const SceneK& S, const CamK& C, const FrameK& F, const uint32_t* touched, const ExtK& E,
+                      float4* grads, cudaStream_t st) {
+    if (S.n <= 0) return;
+    k_chain_ext<<<(S.n + 127) / 128, 128, 0, st>>>(S, C, F, touched, E, grads);
+}
+
+}  // namespace tsb

@@ -272,4 +272,16 @@ __device__ __forceinline__ double phase_of_depth(double depth, double f, double 
     return 4.0 * M_PI * depth * f / c;
 }
 
+// fp64 record of a visible Gaussian for the pixel fix-up (tsb_geom.cu) and the
+// fp64-fixed pixels of the colour / flow channels (tsb_ext.cu).
+__device__ __forceinline__ Rec64 make_rec64(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F, int g) {
+    Prep64 s;
+    prep64(S, C, O, F, g, s);  // visible by construction
+    Rec64 r;
+    r.m0 = make_double4(s.mean[0], s.mean[1], s.ca, s.cb);
+    r.m1 = make_double4(s.cc, s.opacity, s.coef, s.depth);
+    r.rect = make_int4(s.x0, s.x1, s.y0, s.y1);
+    return r;
+}
+
 }  // namespace tsb

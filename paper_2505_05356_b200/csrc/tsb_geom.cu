@@ -145,16 +145,6 @@ struct FixupAcc {
     bool done;
 };
 
-__device__ __forceinline__ Rec64 make_rec64(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F, int g) {
-    Prep64 s;
-    prep64(S, C, O, F, g, s);  // visible by construction
-    Rec64 r;
-    r.m0 = make_double4(s.mean[0], s.mean[1], s.ca, s.cb);
-    r.m1 = make_double4(s.cc, s.opacity, s.coef, s.depth);
-    r.rect = make_int4(s.x0, s.x1, s.y0, s.y1);
-    return r;
-}
-
 // Mark the Gaussians the flagged pixels will visit (their tile lists up to the
 // fp32 termination point + a margin) and queue each once for the record cache.
 __global__ void __launch_bounds__(128) k_fixup_mark(OptK O, FixupK fx, PixK px, int W, const FrameDev* __restrict__ fd) {

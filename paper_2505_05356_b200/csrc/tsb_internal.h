@@ -11,7 +11,8 @@ namespace tsb {
 constexpr int kTile = 16;          // raster CTA block edge (pixels)
 constexpr int kRasterThreads = kTile * kTile;
 constexpr int kMaxKeyframes = 16;
-constexpr int kMaxArrays = 3 + kMaxKeyframes + 4;  // pos_op, scale_amp, quat, motion[k], sh[4]
+constexpr int kColorArrays = 12;  // colour SH: 48 coefficients ([c][k], splat.hpp color_sh) in 12 float4 arrays
+constexpr int kMaxArrays = 3 + kMaxKeyframes + 4 + kColorArrays;  // pos_op, scale_amp, quat, motion[k], sh[4], color[12]
 
 // Camera constants the kernels use (camera.hpp:9-49 + splat.cpp:109-111).
 struct CamK {
@@ -33,6 +34,7 @@ struct OptK {
     int dist;          // distortion channel: accumulate the shifted depth moments
     double bg_quad[8];
     double bg_phasor[4];
+    double bg_color[3];
 };
 
 // Device-resident scene (fp32 SoA float4 arrays; see tsb.h for the mapping).
@@ -44,6 +46,7 @@ struct SceneK {
     const float4* quat;       // w, x, y, z
     const float4* motion;     // [nk][n] keyframe offsets (xyz, 0)
     const float4* sh;         // [4][n] reflectivity SH coefficients 1..15 (+pad); null when sh_degree == 0
+    const float4* color_sh;   // [12][n] colour SH, flat coefficient 16 c + k in array (16 c + k) / 4; null: no colour
     // Time-independent per-Gaussian cache, refreshed whenever the parameters change
     // (tsb_scene_set_params, Adam): cov3d = M3 M3^T (6 planes xx, xy, xz, yy, yz, zz)
     // and opacity = sigmoid(logit), computed by the same fp64 code prep64 used inline,
@@ -160,9 +163,12 @@ struct UpK {
     const float* weight;
     const float* distortion;
     const float* transm;
+    const float* color;       // [3][H][W] colour (TSB_CH_COLOR)
+    const float* mf;          // [3][H][W] motion_fwd_acc (TSB_CH_FLOW)
+    const float* mb;          // [3][H][W] motion_bwd_acc
 };
 // Scene statistics buffer: background gradients (quad 4*nf, then phasor 2*nf) and the loss.
-constexpr int kStatBg = 0, kStatLoss = 12, kStats = 13;
+constexpr int kStatBg = 0, kStatLoss = 12, kStatBgColor = 13, kStats = 16;
 
 // ---- launchers (defined in the .cu files) ----
 // tsb_geom.cu (fp64, compiled without FMA contraction)
@@ -321,6 +327,28 @@ void launch_densify_plan(const SceneK& S, const DensifyK& D, DensifyScratch& w, 
 void launch_densify_scatter(const SceneK& S, const DensifyK& D, const DensifyScratch& w, uint32_t n_kept, int narrays,
                             const float4* P, const float4* M, const float4* V, float4* P2, float4* M2, float4* V2,
                             int n_new, cudaStream_t st);
+// tsb_ext.cu: colour and flow channels (splat.cpp:273-334 forward, 361-505 backward, 560-571 chain).
+constexpr int kExtPlanes = 15;  // colour 3, motion_fwd_acc 3, motion_bwd_acc 3, flow_fwd 2, flow_bwd 2, flow_valid 2
+struct ExtK {
+    float4* col;          // [n] clamped colour of the frame (rgb, 0); null: no colour channel
+    const float4* mf;     // [n] motion_fwd (xyz, 0) or null (zero)
+    const float4* mb;     // [n] motion_bwd or null
+    float* out;           // [kExtPlanes][H][W]
+    float* screen;        // [9][n] per-Gaussian d_color, d_motion_fwd, d_motion_bwd (summed over pixels)
+    float4* d_motion;     // [2][n] SceneGrads::d_motion_fwd / d_motion_bwd of the last backward
+    double* bg_part;      // [blocks][3] d_bg_color partials
+    int flow;             // flow outputs requested
+};
+void launch_ext_prep(const SceneK& S, const CamK& C, const FrameDev* fd, const uint32_t* touched, const ExtK& E,
+                     const int32_t* abort, cudaStream_t st);
+void launch_ext_fwd(const RecK& rec, const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd,
+                    const uint4* ranges_all, int nchunks, const uint32_t* vals, const FixupK& fx, const PixK& px,
+                    int nf, const ExtK& E, cudaStream_t st);
+void launch_ext_bwd(const RecK& rec, const OptK& O, int W, int H, int nf, const uint4* ranges_all, int nchunks,
+                    const uint32_t* vals, const PixK& px, const UpK& up, const ExtK& E, float* screen, int scap,
+                    cudaStream_t st);
+void launch_chain_ext(const SceneK& S, const CamK& C, const FrameK& F, const uint32_t* touched, const ExtK& E,
+                      float4* grads, cudaStream_t st);
 // tsb_optim.cu
 void launch_pack_params(float4* dst, const float* src, int n, int comps, int comp0, int ncomp_dst,
                         cudaStream_t st);
@@ -328,6 +356,9 @@ void launch_unpack(const float4* src, float* dst, int n, int comps, int comp0, c
 // SH coefficients 1..15 of a [n][16] host-layout array <-> the 4 float4 SH arrays
 void launch_pack_sh(float4* dst4, float4* scale_amp, const float* src16, int n, cudaStream_t st);
 void launch_unpack_sh(const float4* src4, float* dst16, int n, cudaStream_t st);
+// [n][4 * na] host-layout rows <-> na float4 arrays (colour SH: na = 12; motions: na = 1 with 3 comps)
+void launch_pack_rows(float4* dst, const float* src, int n, int na, int comps, cudaStream_t st);
+void launch_unpack_rows(const float4* src, float* dst, int n, int na, int comps, cudaStream_t st);
 void launch_adam(float4* params, float4* grads, float4* m, float4* v, int n, int narrays,
                  const double* lr4 /* host [narrays*4] */, double beta1, double beta2, double eps,
                  double bc1, double bc2, float* densify, cudaStream_t st);

@@ -54,6 +54,36 @@ __global__ void k_unpack_sh(const float4* __restrict__ src, float* __restrict__ 
     }
 }
 
+// Rows of na * comps floats <-> na float4 arrays (lanes >= comps zero).
+__global__ void k_pack_rows(float4* __restrict__ dst, const float* __restrict__ src, int n, int na, int comps) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float* s = src + (size_t)i * na * comps;
+    for (int a = 0; a < na; ++a) {
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int c = 0; c < comps; ++c) v[c] = s[a * comps + c];
+        dst[(size_t)a * n + i] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+}
+
+__global__ void k_unpack_rows(const float4* __restrict__ src, float* __restrict__ dst, int n, int na, int comps) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float* d = dst + (size_t)i * na * comps;
+    for (int a = 0; a < na; ++a) {
+        const float4 q = src[(size_t)a * n + i];
+        const float v[4] = {q.x, q.y, q.z, q.w};
+        for (int c = 0; c < comps; ++c) d[a * comps + c] = v[c];
+    }
+}
+
+void launch_pack_rows(float4* dst, const float* src, int n, int na, int comps, cudaStream_t st) {
+    if (n > 0) k_pack_rows<<<(n + 255) / 256, 256, 0, st>>>(dst, src, n, na, comps);
+}
+void launch_unpack_rows(const float4* src, float* dst, int n, int na, int comps, cudaStream_t st) {
+    if (n > 0) k_unpack_rows<<<(n + 255) / 256, 256, 0, st>>>(src, dst, n, na, comps);
+}
+
 void launch_pack_sh(float4* dst4, float4* scale_amp, const float* src16, int n, cudaStream_t st) {
     if (n > 0) k_pack_sh<<<(n + 255) / 256, 256, 0, st>>>(dst4, scale_amp, src16, n);
 }

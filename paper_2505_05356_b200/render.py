@@ -88,6 +88,9 @@ class RenderOptions:
     counts: bool = False      # also emit per-pixel n_contrib / n_processed (parity diagnostics)
     full_lists: bool = False  # bin every tile's complete list (parity); default stops binning a tile
                               # once all its pixels have terminated (identical outputs)
+    color: bool = False       # RenderChannels::color (scene created with color=True)
+    flow: bool = False        # RenderChannels::flow (motions via RenderPass.set_motion)
+    bg_color: Sequence[float] = (0.0, 0.0, 0.0)
 
     def to_abi(self) -> _abi.RenderOptions:
         o = _abi.RenderOptions()
@@ -99,7 +102,8 @@ class RenderOptions:
         o.tile_size = int(self.tile_size)
         o.channels = _abi.CH_QUAD | _abi.CH_DEPTH | _abi.CH_WEIGHT | _abi.CH_TRANSM | (
             _abi.CH_COUNTS if self.counts else 0) | (_abi.CH_FULL_LISTS if self.full_lists else 0) | (
-            _abi.CH_PHASOR) | (_abi.CH_DISTORTION if self.distortion else 0)
+            _abi.CH_PHASOR) | (_abi.CH_DISTORTION if self.distortion else 0) | (
+            _abi.CH_COLOR if self.color else 0) | (_abi.CH_FLOW if self.flow else 0)
         bq = np.zeros(8)
         b = np.asarray(self.bg_quad, dtype=np.float64).reshape(-1)[:8]
         bq[: b.size] = b
@@ -110,6 +114,9 @@ class RenderOptions:
         bp[: b.size] = b
         for i in range(4):
             o.bg_phasor[i] = bp[i]
+        bc = np.asarray(self.bg_color, dtype=np.float64).reshape(-1)
+        for i in range(3):
+            o.bg_color[i] = float(bc[i]) if bc.size > i else 0.0
         return o
 
 
@@ -131,10 +138,11 @@ class LrTable:
     opacity: float = 0.05
     reflectivity: float = 1.6e-4
     motion: float = 1.6e-4
+    color: float = 1.6e-3
 
     @staticmethod
     def uniform(lr: float) -> "LrTable":
-        return LrTable(lr, lr, lr, lr, lr, lr)
+        return LrTable(lr, lr, lr, lr, lr, lr, lr)
 
 
 def scene_extent(positions) -> float:
@@ -230,10 +238,12 @@ class GaussianScene:
     """Device-resident Gaussian parameters, gradients and Adam moments."""
 
     def __init__(self, ctx: Context, n: int, n_keyframes: int = 0, tof: Optional[ToFConfig] = None,
-                 sh_degree: int = 0):
+                 sh_degree: int = 0, color: bool = False):
         tof = tof or ToFConfig()
         d = _abi.SceneDesc()
         d.n, d.n_keyframes, d.sh_degree = int(n), int(n_keyframes), int(sh_degree)
+        d.color = 1 if color else 0
+        self.color = bool(color)
         fr = tof.frequencies
         d.n_freq = len(fr)
         for i, f in enumerate(fr):
@@ -281,6 +291,18 @@ class GaussianScene:
         check(lib().tsb_scene_get_sh(self._h, _ptr(out), 1 if grads else 0))
         return out
 
+    def set_color(self, color_sh):
+        """Colour SH per Gaussian, (n, 16, 3) -- Gaussian::color_sh, coefficient k of channel c
+        at [i, k, c] (scene created with color=True)."""
+        a = np.ascontiguousarray(np.asarray(color_sh, np.float32).reshape(self.n, 16, 3).transpose(0, 2, 1))
+        check(lib().tsb_scene_set_color(self._h, _abi.TSB_HOST, a.ctypes.data))
+
+    def get_color(self, grads: bool = False):
+        """(n, 16, 3) colour SH parameters, or SceneGrads::d_color_sh when grads."""
+        out = np.zeros((self.n, 3, 16), np.float32)
+        check(lib().tsb_scene_get_color(self._h, _ptr(out), 1 if grads else 0))
+        return out.transpose(0, 2, 1).copy()
+
     def set_params_device(self, position, log_scale, rotation, opacity_logit, reflectivity_dc, motion=None):
         """Device pointers (ints) in the same SoA layout."""
         check(lib().tsb_scene_set_params(self._h, _abi.TSB_DEVICE, position, log_scale, rotation, opacity_logit,
@@ -313,6 +335,9 @@ class GaussianScene:
         bq, bp = np.zeros(8), np.zeros(4)
         check(lib().tsb_scene_get_bg_grads(self._h, bq.ctypes.data_as(_abi._dp), bp.ctypes.data_as(_abi._dp)))
         g["d_bg_phasor"] = bp[: 2 * self.n_freq]
+        bc = np.zeros(3)
+        check(lib().tsb_scene_get_bg_color_grad(self._h, bc.ctypes.data_as(_abi._dp)))
+        g["d_bg_color"] = bc
         return g
 
     def zero_grads(self):
@@ -320,7 +345,7 @@ class GaussianScene:
 
     def adam_step(self, lr: LrTable, adam: AdamParams = AdamParams()):
         cfg = _abi.AdamConfig(lr.position, lr.log_scale, lr.rotation, lr.opacity, lr.reflectivity, lr.motion,
-                              adam.beta1, adam.beta2, adam.eps)
+                              adam.beta1, adam.beta2, adam.eps, lr.color)
         check(lib().tsb_scene_adam_step(self._h, C.byref(cfg)))
 
     def adam_moments_position(self):
@@ -339,9 +364,10 @@ class GaussianScene:
         check(lib().tsb_scene_allreduce_grads(self._h, comm.handle))
 
     def close(self):
-        if getattr(self, "_h", None):
+        # after the context is gone (interpreter teardown, GC cycles) the handle is dropped, not freed
+        if getattr(self, "_h", None) and getattr(getattr(self, "ctx", None), "_h", None):
             lib().tsb_scene_destroy(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         try:
@@ -426,7 +452,8 @@ class RenderPass:
         return self
 
     def backward_buffers(self, d_quad=None, d_phasor=None, d_depth_raw=None, d_weight=None,
-                         d_distortion=None, d_transmittance=None):
+                         d_distortion=None, d_transmittance=None, d_color=None, d_motion_fwd_acc=None,
+                         d_motion_bwd_acc=None):
         """RenderPass::backward(BufferGrads) (splat.cpp:347-650): None skips a channel."""
         keep = []
 
@@ -437,10 +464,28 @@ class RenderPass:
             keep.append(a)
             return a.ctypes.data
 
-        ptrs = [arr(a) for a in (d_quad, d_phasor, d_depth_raw, d_weight, d_distortion, d_transmittance)]
+        ptrs = [arr(a) for a in (d_quad, d_phasor, d_depth_raw, d_weight, d_distortion, d_transmittance,
+                                 d_color, d_motion_fwd_acc, d_motion_bwd_acc)]
         self._up_keep = keep
-        check(lib().tsb_pass_backward_buffers(self._h, _abi.TSB_HOST, *ptrs))
+        check(lib().tsb_pass_backward_ext(self._h, _abi.TSB_HOST, *ptrs))
         return self
+
+    def set_motion(self, motion_fwd=None, motion_bwd=None):
+        """RenderInput::motion_fwd / motion_bwd (splat.hpp:46-47): (n, 3) per-Gaussian motions of
+        this frame for the flow channel; None = zero.  Call after prepare()."""
+        n = self.scene.n
+        a = None if motion_fwd is None else _f32(motion_fwd, n, 3)
+        b = None if motion_bwd is None else _f32(motion_bwd, n, 3)
+        check(lib().tsb_pass_set_motion(self._h, _abi.TSB_HOST, a.ctypes.data if a is not None else None,
+                                        b.ctypes.data if b is not None else None))
+        return self
+
+    def motion_grads(self):
+        """SceneGrads::d_motion_fwd / d_motion_bwd of the last backward, (n, 3) each."""
+        n = self.scene.n
+        a, b = np.zeros((n, 3), np.float32), np.zeros((n, 3), np.float32)
+        check(lib().tsb_pass_get_motion_grads(self._h, _ptr(a), _ptr(b)))
+        return a, b
 
     def output_ptr(self, which: int):
         p = C.c_void_p()
@@ -476,6 +521,14 @@ class RenderPass:
                "phasor": self.download(_abi.OUT_PHASOR, shape=(2 * nf, H, W))}
         if self.options.distortion:
             out["distortion"] = self.download(_abi.OUT_DISTORTION, shape=(H, W))
+        if self.options.color:
+            out["color"] = self.download(_abi.OUT_COLOR, shape=(3, H, W))
+        if self.options.flow:
+            out["motion_fwd_acc"] = self.download(_abi.OUT_MOTION_FWD_ACC, shape=(3, H, W))
+            out["motion_bwd_acc"] = self.download(_abi.OUT_MOTION_BWD_ACC, shape=(3, H, W))
+            out["flow_fwd"] = self.download(_abi.OUT_FLOW_FWD, shape=(2, H, W))
+            out["flow_bwd"] = self.download(_abi.OUT_FLOW_BWD, shape=(2, H, W))
+            out["flow_valid"] = self.download(_abi.OUT_FLOW_VALID, shape=(2, H, W))
         if self.options.counts:
             out["n_contrib"] = self.download(_abi.OUT_N_CONTRIB, np.int32, (H, W))
             out["n_processed"] = self.download(_abi.OUT_N_PROCESSED, np.int32, (H, W))
@@ -534,9 +587,10 @@ class RenderPass:
         return a & 0xFFFFFF, (a >> 24) & 7
 
     def close(self):
-        if getattr(self, "_h", None):
+        # after the context is gone (interpreter teardown, GC cycles) the handle is dropped, not freed
+        if getattr(self, "_h", None) and getattr(getattr(self, "ctx", None), "_h", None):
             lib().tsb_pass_destroy(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         try:
@@ -662,9 +716,10 @@ class DeformNet:
         check(lib().tsb_deform_adam_step(self._h, lr, beta1, beta2, eps))
 
     def close(self):
-        if getattr(self, "_h", None):
+        # after the context is gone (interpreter teardown, GC cycles) the handle is dropped, not freed
+        if getattr(self, "_h", None) and getattr(getattr(self, "ctx", None), "_h", None):
             lib().tsb_deform_destroy(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         try:

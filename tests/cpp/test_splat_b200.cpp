@@ -245,6 +245,71 @@ static void adam_steps() {
     CHECK(close_rel(q[0], -0.01, 1e-6) && close_rel(q[1], 0.01, 1e-6) && close_rel(q[2], -0.01, 1e-6));
 }
 
+// Colour channel + background colour gradient (test_splat.cpp:62-101, colour parts).
+static void colour_background() {
+    CanonicalScene scene;
+    const CameraModel cam = test_camera();
+    RenderInput in;
+    in.scene = &scene;
+    in.camera = &cam;
+    in.opts.channels.color = true;
+    in.opts.bg.color = {0.2, 0.4, 0.6};
+    RenderPass pass(in);
+    const RenderedBuffers out = pass.forward();
+    bool all_bg = true;
+    for (int y = 0; y < out.height; ++y)
+        for (int x = 0; x < out.width; ++x)
+            for (int c = 0; c < 3; ++c) all_bg &= out.color.at(x, y, c) == (float)in.opts.bg.color[c];
+    CHECK(all_bg);
+    BufferGrads up;
+    up.d_color = Image(out.width, out.height, 3);
+    std::fill(up.d_color.data.begin(), up.d_color.data.end(), 1.0);
+    const SceneGrads g = pass.backward(up);
+    const double npx = out.width * out.height;
+    for (int c = 0; c < 3; ++c) CHECK(close_rel(g.d_bg_color[c], npx, 1e-6));
+    // an opaque grey splat on axis: colour = c alpha + bg (1 - alpha)
+    CanonicalScene one;
+    Gaussian gs = dc_gaussian({0.0, 0.0, 2.0}, 0.2, 0.5, logit(0.7));
+    for (int c = 0; c < 3; ++c) gs.color_sh[0][c] = (0.25 + 0.25 * c) / SH_C0;
+    one.gaussians.push_back(gs);
+    in.scene = &one;
+    const RenderedBuffers o1 = render(in);
+    const double alpha = o1.weight.at(32, 24);
+    for (int c = 0; c < 3; ++c)
+        CHECK(close_rel(o1.color.at(32, 24, c), (0.25 + 0.25 * c) * alpha + in.opts.bg.color[c] * (1.0 - alpha), 1e-5));
+}
+
+// Flow channel (test_splat.cpp:294-333).
+static void flow_projection() {
+    const CameraModel cam = test_camera(64, 48, 50.0);
+    CanonicalScene scene;
+    scene.gaussians.push_back(dc_gaussian({0.0, 0.0, 2.0}, 0.2, 0.5, 40.0));
+    Matrix3Xd motion_fwd(1), motion_bwd(1);
+    const double mf[3] = {0.1, -0.05, 0.3}, mb[3] = {-0.2, 0.0, 0.1};
+    for (int a = 0; a < 3; ++a) {
+        motion_fwd(a, 0) = mf[a];
+        motion_bwd(a, 0) = mb[a];
+    }
+    RenderInput in;
+    in.scene = &scene;
+    in.camera = &cam;
+    in.motion_fwd = &motion_fwd;
+    in.motion_bwd = &motion_bwd;
+    in.opts.channels.flow = true;
+    const RenderedBuffers out = render(in);
+    const int cx = 32, cy = 24;
+    CHECK(out.flow_valid.at(cx, cy, 0) == 1.0 && out.flow_valid.at(cx, cy, 1) == 1.0);
+    CHECK(close_rel(out.flow_fwd.at(cx, cy, 0), 50.0 * 0.1 / 2.3, 1e-5));
+    CHECK(close_rel(out.flow_fwd.at(cx, cy, 1), 50.0 * -0.05 / 2.3, 1e-5));
+    CHECK(close_rel(out.flow_bwd.at(cx, cy, 0), 50.0 * -0.2 / 2.1, 1e-5));
+    CHECK(std::abs(out.flow_bwd.at(cx, cy, 1)) < 1e-5);
+    const int x = 36, y = 24;
+    const double w = out.weight.at(x, y);
+    CHECK(w > 0.1);
+    for (int c = 0; c < 3; ++c) CHECK(close_rel(out.motion_fwd_acc.at(x, y, c), w * mf[c], 1e-5));
+    CHECK(out.flow_valid.at(0, 0, 0) == 0.0 && out.flow_fwd.at(0, 0, 0) == 0.0);
+}
+
 int main() {
     empty_scene_passes_background();
     single_on_axis_splat();
@@ -254,6 +319,8 @@ int main() {
     tile_size_and_override();
     errors_match_reference();
     adam_steps();
+    colour_background();
+    flow_projection();
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
 }

@@ -24,7 +24,7 @@ def test_header_symbols_exported_and_bound():
     for n in names:
         assert hasattr(L, n), f"{n} declared in tsb.h but not exported by libtsb.so"
         assert n in _abi.SIGNATURES, f"{n} has no ctypes signature"
-    assert L.tsb_abi_version() == 2
+    assert L.tsb_abi_version() == 3
 
 
 def test_library_is_sm100a_code():

@@ -1,0 +1,178 @@
+"""Colour and flow channels of RenderPass on the B200 (tsb_ext.cu) against the CPU oracle.
+
+Forward: splat.cpp:273-294 (colour / motion accumulators), 301-334 (bg colour, flow by
+backprojection of the composited depth + reprojection of x + motion, flow_valid).
+Backward: the colour / motion upstreams of BufferGrads (splat.cpp:361-505) and their chain
+(colour SH gated by 0 < colour_raw < 1, view-direction term, d_motion_*; splat.cpp:560-571).
+Tolerances as the ToF channels: images 1e-4 relative, gradients 1e-3 relative."""
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+
+from helpers import rel_err, rel_err_quantile
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4
+GRAD_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def tsb():
+    import paper_2505_05356_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(tsb):
+    return tsb.Context(0)
+
+
+def _colour_sh(rng, n, degree):
+    """(n, 16, 3): DC around mid-grey (some channels pushed out of [0, 1] so the clamp gate
+    is exercised), small higher-order terms up to `degree`."""
+    cs = np.zeros((n, 16, 3), np.float32)
+    c0 = 0.28209479177387814
+    cs[:, 0, :] = (rng.uniform(0.1, 0.9, (n, 3)) / c0).astype(np.float32)
+    out = rng.uniform(size=(n, 3)) < 0.08
+    cs[:, 0, :][out] = (rng.choice([-0.5, 1.6], size=out.sum()) / c0).astype(np.float32)
+    nk = (degree + 1) ** 2
+    if nk > 1:
+        cs[:, 1:nk, :] = (0.1 * (rng.uniform(size=(n, nk - 1, 3)) - 0.5)).astype(np.float32)
+    return cs
+
+
+def _setup(tsb, ctx, degree, n=3000, seed=31):
+    from paper_2505_05356_b200 import synthetic
+    g = synthetic.gaussians(n, seed, n_keyframes=2)
+    rng = np.random.default_rng(seed + 1)
+    sh = np.zeros((n, 16), np.float32)
+    sh[:, 0] = g.reflectivity_dc
+    if degree > 0:
+        sh[:, 1:(degree + 1) ** 2] = (0.05 * (rng.uniform(size=(n, (degree + 1) ** 2 - 1)) - 0.5)).astype(np.float32)
+    cs = _colour_sh(rng, n, degree)
+    mf = (0.05 * rng.normal(size=(n, 3))).astype(np.float32)
+    mb = (0.05 * rng.normal(size=(n, 3))).astype(np.float32)
+    tof = tsb.ToFConfig(30e6)
+    scene = tsb.GaussianScene(ctx, n, 2, tof, sh_degree=degree, color=True)
+    scene.set_params(g.position, g.log_scale, g.rotation, g.opacity_logit, g.reflectivity_dc, g.motion)
+    if degree > 0:
+        scene.set_sh(sh)
+    scene.set_color(cs)
+    return g, sh, cs, mf, mb, scene, tof
+
+
+def _oscene(g, frame, sh, cs, mf, mb, degree):
+    n = g.n
+    return orc.OScene(g.rendered_means(frame), g.log_scale.astype(np.float64), g.rotation.astype(np.float64),
+                      g.opacity_logit.astype(np.float64), sh.astype(np.float64), degree, 30e6, 1.0, 299792458.0,
+                      color_sh=cs.astype(np.float64).transpose(0, 2, 1).reshape(n, 48).copy(),
+                      motion_fwd=None if mf is None else mf.astype(np.float64),
+                      motion_bwd=None if mb is None else mb.astype(np.float64))
+
+
+def _check_img(a, b, floor=1e-3):
+    assert rel_err(a, b, floor) < IMG_TOL
+    assert np.abs(np.asarray(a, np.float64) - b).max() <= 2e-6 * max(np.abs(b).max(), 1e-30)
+
+
+def _check_signed(a, b):
+    """Motion accumulators sum signed terms that cancel (like the raw samples, see
+    test_gpu_parity.check_image): 1e-4 relative above 1e-2 max, 99.9th percentile of the
+    relative error above 1e-3 max below 1e-4, absolute error below 2e-6 max everywhere."""
+    assert rel_err(a, b, 1e-2) < IMG_TOL
+    assert rel_err_quantile(a, b, 1e-3, 0.999) < IMG_TOL
+    assert np.abs(np.asarray(a, np.float64) - b).max() <= 2e-6 * max(np.abs(b).max(), 1e-30)
+
+
+def test_color_sh_roundtrip(tsb, ctx):
+    _, _, cs, _, _, scene, _ = _setup(tsb, ctx, 2, n=500)
+    assert np.array_equal(scene.get_color(), cs)
+
+
+@pytest.mark.parametrize("degree", [0, 3])
+def test_color_flow_forward_and_backward(tsb, ctx, degree):
+    from paper_2505_05356_b200 import synthetic
+    g, sh, cs, mf, mb, scene, tof = _setup(tsb, ctx, degree)
+    cam = synthetic.camera(200, 150, 180.0)
+    H, W = cam.height, cam.width
+    frame = (0, 0.4)
+    opts = tsb.RenderOptions(counts=True, color=True, flow=True, bg_color=(0.2, 0.5, 0.8))
+    rp = tsb.RenderPass(ctx).prepare(scene, cam, opts, frame)
+    rp.set_motion(mf, mb)
+    rp.forward()
+    out = rp.outputs()
+
+    op = orc.OraclePass(_oscene(g, frame, sh, cs, mf, mb, degree), cam, opts)
+    ref = op.forward()
+    ext = op.forward_ext()
+    assert np.array_equal(out["n_contrib"], ref["n_contrib"])
+    _check_img(out["color"], ext["color"])
+    for k in ("motion_fwd_acc", "motion_bwd_acc"):
+        _check_signed(out[k], ext[k])
+    assert np.array_equal(out["flow_valid"], ext["flow_valid"])
+    for k in ("flow_fwd", "flow_bwd"):
+        # flow is a pixel displacement: absolute tolerance (1e-4 px + 1e-4 relative)
+        d = np.abs(out[k].astype(np.float64) - ext[k])
+        assert (d <= 1e-4 + 1e-4 * np.abs(ext[k])).all(), d.max()
+
+    rng = np.random.default_rng(5)
+    ups = {"d_color": rng.normal(0, 1e-3, (3, H, W)).astype(np.float32),
+           "d_motion_fwd_acc": rng.normal(0, 1e-3, (3, H, W)).astype(np.float32),
+           "d_motion_bwd_acc": rng.normal(0, 1e-3, (3, H, W)).astype(np.float32),
+           "d_quad": rng.normal(0, 1e-3, (4, H, W)).astype(np.float32)}
+    rp.backward_buffers(**ups)
+    gr = scene.grads()
+    dcs = scene.get_color(grads=True)
+    dmf, dmb = rp.motion_grads()
+    og = op.backward(**{k: v.astype(np.float64) for k, v in ups.items()})
+    k, w = frame
+    errs = {"d_position": rel_err(gr["d_position"], og["d_position"], 1e-4),
+            "d_log_scale": rel_err(gr["d_log_scale"], og["d_log_scale"], 1e-4),
+            "d_rotation": rel_err(gr["d_rotation"], og["d_rotation"], 1e-4),
+            "d_opacity_logit": rel_err(gr["d_opacity_logit"], og["d_opacity_logit"], 1e-4),
+            "d_motion_k": rel_err(gr["d_motion"][k], (1 - w) * og["d_position"], 1e-4),
+            "d_motion_k1": rel_err(gr["d_motion"][k + 1], w * og["d_position"], 1e-4),
+            "d_color_sh": rel_err(dcs.transpose(0, 2, 1).reshape(g.n, 48), og["d_color_sh"], 1e-4),
+            "d_motion_fwd": rel_err(dmf, og["d_motion_fwd"], 1e-4),
+            "d_motion_bwd": rel_err(dmb, og["d_motion_bwd"], 1e-4)}
+    assert all(e < GRAD_TOL for e in errs.values()), errs
+    assert np.allclose(gr["d_bg_color"], og["d_bg_color"], rtol=1e-4, atol=1e-9)
+    # the colour gate: clamped channels get no SH gradient
+    assert np.abs(og["d_color_sh"]).max() > 0
+
+
+def test_color_only_upstream_and_no_motion(tsb, ctx):
+    """Colour upstream alone, flow without motions (zero motion -> flow of the static point)."""
+    from paper_2505_05356_b200 import synthetic
+    g, sh, cs, _, _, scene, tof = _setup(tsb, ctx, 1, n=2000, seed=44)
+    cam = synthetic.camera(160, 120, 150.0)
+    frame = (0, 0.0)
+    opts = tsb.RenderOptions(color=True, flow=True, bg_color=(1.0, 0.0, 0.5))
+    rp = tsb.RenderPass(ctx).prepare(scene, cam, opts, frame).forward()
+    out = rp.outputs()
+    op = orc.OraclePass(_oscene(g, frame, sh, cs, None, None, 1), cam, opts)
+    op.forward()
+    ext = op.forward_ext()
+    _check_img(out["color"], ext["color"])
+    assert np.array_equal(out["flow_valid"], ext["flow_valid"])
+    assert np.abs(out["flow_fwd"] - ext["flow_fwd"]).max() <= 1e-4
+    up = np.random.default_rng(2).normal(0, 1e-3, (3, 120, 160)).astype(np.float32)
+    rp.backward_buffers(d_color=up)
+    gr = scene.grads()
+    og = op.backward(d_color=up.astype(np.float64))
+    assert rel_err(gr["d_position"], og["d_position"], 1e-4) < GRAD_TOL
+    assert rel_err(scene.get_color(grads=True).transpose(0, 2, 1).reshape(g.n, 48), og["d_color_sh"], 1e-4) < GRAD_TOL
+    assert np.allclose(gr["d_bg_color"], og["d_bg_color"], rtol=1e-4, atol=1e-9)
+
+
+def test_color_upstream_requires_channel(tsb, ctx):
+    from paper_2505_05356_b200 import synthetic
+    _, _, _, _, _, scene, _ = _setup(tsb, ctx, 0, n=300)
+    cam = synthetic.camera(64, 48, 60.0)
+    rp = tsb.RenderPass(ctx).prepare(scene, cam, tsb.RenderOptions(), (0, 0.0)).forward()
+    with pytest.raises(RuntimeError, match="colour"):
+        rp.backward_buffers(d_color=np.zeros((3, 48, 64), np.float32))
+    with pytest.raises(RuntimeError, match="motion"):
+        rp.backward_buffers(d_motion_fwd_acc=np.zeros((3, 48, 64), np.float32))

@@ -612,3 +612,26 @@ def test_densify_surgery_matches_oracle(tsb, ctx):
     assert c2 == 0 and not s2.any()
     out = tsb.RenderPass(ctx).prepare(scene, cam, tsb.RenderOptions(), (0, 0.5)).forward().outputs()
     assert np.isfinite(out["quad"]).all()
+
+
+def test_graph_replay_backward_walks_every_chunk(tsb, ctx):
+    """Re-preparing a pass with the same scene and camera replays its cached forward graph;
+    the backward must still walk every depth chunk of the replayed frame (regression: the
+    replay skipped the host-side chunk count and the backward of iterations >= 2 was empty)."""
+    from paper_2505_05356_b200 import synthetic
+    cfg = synthetic.config("c1")
+    cam, frame = cfg.camera, cfg.frames[0]
+    scene = gpu_scene(tsb, ctx, cfg.scene, cfg.tof)
+    rng = np.random.default_rng(9)
+    target = rng.normal(0, 0.05, (4, cam.height, cam.width)).astype(np.float32)
+    rp = tsb.RenderPass(ctx)
+    grads = []
+    for _ in range(3):
+        scene.zero_grads()
+        rp.prepare(scene, cam, tsb.RenderOptions(), frame)
+        rp.forward_loss(target)
+        rp.backward()
+        grads.append(scene.grads()["d_position"])
+    assert np.abs(grads[0]).max() > 0
+    for g in grads[1:]:  # equal up to the order of the float atomics
+        assert rel_err(g, grads[0], 1e-4) < GRAD_TOL
