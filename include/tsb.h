@@ -259,13 +259,23 @@ enum {
     TSB_OUT_MOTION_BWD_ACC = 12, /* [3][H][W] */
     TSB_OUT_FLOW_FWD = 13,       /* [2][H][W] pixel displacement */
     TSB_OUT_FLOW_BWD = 14,       /* [2][H][W] */
-    TSB_OUT_FLOW_VALID = 15      /* [2][H][W] 1 where covered and projected in front (fwd, bwd) */
+    TSB_OUT_FLOW_VALID = 15,     /* [2][H][W] 1 where covered and projected in front (fwd, bwd) */
+    TSB_OUT_D_MOTION_FWD_ACC = 16, /* [3][H][W] FlowLossResult::d_motion_fwd_acc (tsb_pass_flow_loss) */
+    TSB_OUT_D_MOTION_BWD_ACC = 17  /* [3][H][W] */
 };
 /* Device pointer and byte size of a pass-owned buffer. */
 int tsb_pass_output(tsb_pass* p, int which, void** dptr, size_t* bytes);
 /* Per-Gaussian motions of the frame (RenderInput::motion_fwd / motion_bwd, splat.hpp:46-47;
  * n x 3 row-major = Matrix3Xd columns; NULL = zero) for TSB_CH_FLOW.  Call after prepare. */
 int tsb_pass_set_motion(tsb_pass* p, int where, const float* motion_fwd, const float* motion_bwd);
+/* flow_loss (losses.cpp:168-251) of the pass's last forward (needs TSB_CH_FLOW; settles it):
+ * targets [3][H][W] = (u, v, valid) per direction or NULL.  value = mean squared flow error
+ * over the directions with valid pixels; the motion-accumulator gradients, multiplied by
+ * `weight` (the trainer's loss.flow factor, trainer.cpp:297-305), stay on the device as
+ * outputs TSB_OUT_D_MOTION_FWD_ACC / _BWD_ACC (has_grads bit 0 / 1) for a
+ * tsb_pass_backward_ext(TSB_DEVICE, ...). */
+int tsb_pass_flow_loss(tsb_pass* p, int where, const float* target_fwd, const float* target_bwd, double weight,
+                       double* value, int64_t* valid_pixels, int32_t* has_grads);
 /* SceneGrads::d_motion_fwd / d_motion_bwd (splat.hpp:86) of the last backward, n x 3 each. */
 int tsb_pass_get_motion_grads(tsb_pass* p, float* d_motion_fwd, float* d_motion_bwd);
 /* Copy a pass-owned buffer to host memory (synchronous). */

@@ -20,7 +20,7 @@ CH_QUAD, CH_DEPTH, CH_WEIGHT, CH_TRANSM, CH_COUNTS, CH_FULL_LISTS = 1, 2, 4, 8, 
 CH_PHASOR, CH_DISTORTION, CH_COLOR, CH_FLOW = 64, 128, 256, 512
 (OUT_QUAD, OUT_DEPTH_RAW, OUT_DEPTH, OUT_WEIGHT, OUT_TRANSM, OUT_N_CONTRIB, OUT_N_PROCESSED,
  OUT_D_QUAD, OUT_PHASOR, OUT_DISTORTION, OUT_COLOR, OUT_MOTION_FWD_ACC, OUT_MOTION_BWD_ACC, OUT_FLOW_FWD,
- OUT_FLOW_BWD, OUT_FLOW_VALID) = range(16)
+ OUT_FLOW_BWD, OUT_FLOW_VALID, OUT_D_MOTION_FWD_ACC, OUT_D_MOTION_BWD_ACC) = range(18)
 
 
 STAGES = ["preprocess", "depth_sort", "scan", "binning", "tile_sort", "ranges", "raster_fwd", "fixup", "loss",
@@ -128,6 +128,7 @@ SIGNATURES = {
     "tsb_pass_backward_buffers": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]),
     "tsb_pass_backward_ext": (C.c_int, [_vp, C.c_int] + [_vp] * 9),
     "tsb_pass_set_motion": (C.c_int, [_vp, C.c_int, _vp, _vp]),
+    "tsb_pass_flow_loss": (C.c_int, [_vp, C.c_int, _vp, _vp, C.c_double, _dp, _lp, _ip]),
     "tsb_pass_get_motion_grads": (C.c_int, [_vp, _fp, _fp]),
     "tsb_pass_debug_keep_screen": (C.c_int, [_vp, C.c_int]),
     "tsb_pass_debug_set_list_capacity": (C.c_int, [_vp, C.c_uint32]),

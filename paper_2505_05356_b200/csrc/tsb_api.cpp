@@ -228,6 +228,9 @@ struct tsb_pass {
     float4 *ext_col = nullptr, *ext_mf = nullptr, *ext_mb = nullptr, *ext_dmotion = nullptr;
     float *ext_out = nullptr, *ext_screen = nullptr, *ext_up = nullptr;
     double* ext_bg_part = nullptr;
+    float *ext_dmacc = nullptr, *ext_ftgt = nullptr;  // flow loss: d_motion_*_acc [6][npx], targets [6][npx]
+    double *ext_fl_part = nullptr, *ext_fl_res = nullptr;
+    bool fl_grad[2] = {false, false};
     int ext_n_cap = 0, ext_px_cap = 0, ext_blk_cap = 0;
     bool has_mf = false, has_mb = false;
     bool count_live = false;
@@ -1107,6 +1110,7 @@ void tsb_pass_destroy(tsb_pass* p) {
     dev_free(p->ssim_g); dev_free(p->ssim_part);
     dev_free(p->ext_col); dev_free(p->ext_mf); dev_free(p->ext_mb); dev_free(p->ext_dmotion);
     dev_free(p->ext_out); dev_free(p->ext_screen); dev_free(p->ext_up); dev_free(p->ext_bg_part);
+    dev_free(p->ext_dmacc); dev_free(p->ext_ftgt); dev_free(p->ext_fl_part); dev_free(p->ext_fl_res);
     if (p->pinned) cudaFreeHost(p->pinned);
     if (p->done_ev) cudaEventDestroy(p->done_ev);
     for (auto& fg : p->fwd)
@@ -1273,9 +1277,13 @@ int ensure_ext(tsb_pass* p) {
         p->ext_n_cap = n;
     }
     if (npx > p->ext_px_cap) {
-        dev_free(p->ext_out); dev_free(p->ext_up);
+        dev_free(p->ext_out); dev_free(p->ext_up); dev_free(p->ext_dmacc); dev_free(p->ext_ftgt);
+        dev_free(p->ext_fl_part); dev_free(p->ext_fl_res);
         p->ext_px_cap = 0;
-        if ((rc = dev_alloc(&p->ext_out, (size_t)kExtPlanes * npx)) || (rc = dev_alloc(&p->ext_up, (size_t)9 * npx)))
+        if ((rc = dev_alloc(&p->ext_out, (size_t)kExtPlanes * npx)) || (rc = dev_alloc(&p->ext_up, (size_t)9 * npx)) ||
+            (rc = dev_alloc(&p->ext_dmacc, (size_t)6 * npx)) || (rc = dev_alloc(&p->ext_ftgt, (size_t)6 * npx)) ||
+            (rc = dev_alloc(&p->ext_fl_part, (size_t)4 * flow_loss_parts(npx))) ||
+            (rc = dev_alloc(&p->ext_fl_res, 4)))
             return rc;
         p->ext_px_cap = npx;
     }
@@ -1776,6 +1784,12 @@ int output_ptr(tsb_pass* p, int which, void** dptr, size_t* bytes) {
             const int i = which - TSB_OUT_MOTION_FWD_ACC;
             ptr = p->ext_out + plane[i] * HW; b = planes[i] * HW * 4; break;
         }
+        case TSB_OUT_D_MOTION_FWD_ACC:
+        case TSB_OUT_D_MOTION_BWD_ACC: {
+            const int k = which - TSB_OUT_D_MOTION_FWD_ACC;
+            if (!p->fl_grad[k]) return fail(TSB_ERR_INVALID, "no flow-loss gradient for this direction");
+            ptr = p->ext_dmacc + (size_t)3 * k * HW; b = 3 * HW * 4; break;
+        }
         default: return fail(TSB_ERR_INVALID, "unknown output");
     }
     *dptr = ptr;
@@ -1985,6 +1999,51 @@ int tsb_pass_set_motion(tsb_pass* p, int where, const float* motion_fwd, const f
     TSB_CHECK_LAUNCH();
     p->has_mf = motion_fwd != nullptr;
     p->has_mb = motion_bwd != nullptr;
+    return TSB_OK;
+}
+
+int tsb_pass_flow_loss(tsb_pass* p, int where, const float* target_fwd, const float* target_bwd, double weight,
+                       double* value, int64_t* valid_pixels, int32_t* has_grads) {
+    if (!p) return fail(TSB_ERR_INVALID, "null pass");
+    if (!p->forwarded || !(p->channels & TSB_CH_FLOW))
+        return fail(TSB_ERR_INVALID, "flow_loss: render lacks flow channels");
+    if (where != TSB_HOST && where != TSB_DEVICE) return fail(TSB_ERR_INVALID, "bad memory kind");
+    TSB_CUDA(cudaSetDevice(p->ctx->device));
+    int rc = settle(p);  // the loss reads a finished (not aborted) forward
+    if (rc) return rc;
+    cudaStream_t st = p->stream;
+    const size_t HW = (size_t)p->W * p->H;
+    FlowK F{};
+    const float* tg[2] = {target_fwd, target_bwd};
+    for (int k = 0; k < 2; ++k) {
+        p->fl_grad[k] = false;
+        if (!tg[k]) continue;
+        if (where == TSB_HOST) {
+            TSB_CUDA(cudaMemcpyAsync(p->ext_ftgt + 3 * k * HW, tg[k], sizeof(float) * 3 * HW, cudaMemcpyHostToDevice, st));
+            F.target[k] = p->ext_ftgt + 3 * k * HW;
+        } else {
+            F.target[k] = tg[k];
+        }
+    }
+    double res[4] = {0.0, 0.0, 0.0, 0.0};
+    if (F.target[0] || F.target[1]) {
+        F.d_macc = p->ext_dmacc;
+        F.part = p->ext_fl_part;
+        F.res = p->ext_fl_res;
+        F.abort = p->counters + 2;
+        launch_flow_loss(p->cam, p->nf, p->out, p->ext_out, F, weight, st);
+        p->ctx->launches += 3;
+        TSB_CHECK_LAUNCH();
+        double* h = (double*)((char*)p->pinned + 320);
+        TSB_CUDA(cudaMemcpyAsync(h, p->ext_fl_res, sizeof(double) * 4, cudaMemcpyDeviceToHost, st));
+        TSB_CUDA(cudaStreamSynchronize(st));
+        std::memcpy(res, h, sizeof res);
+        const bool used = res[1] > 0.0;
+        for (int k = 0; k < 2; ++k) p->fl_grad[k] = used && F.target[k] != nullptr;
+    }
+    if (value) *value = res[0];
+    if (valid_pixels) *valid_pixels = (int64_t)res[1];
+    if (has_grads) *has_grads = (p->fl_grad[0] ? 1 : 0) | (p->fl_grad[1] ? 2 : 0);
     return TSB_OK;
 }
 

@@ -441,7 +441,116 @@ __global__ void __launch_bounds__(128) k_chain_ext(SceneK S, CamK C, FrameK F, c
     }
 }
 
+// ---- flow loss (losses.cpp:168-251) -------------------------------------------
+// Per pixel and direction: valid = target.valid > 0.5 and flow_valid > 0.5; residual of the
+// rendered flow; the unscaled pull-back 2 r through the projection at the frozen
+// backprojected point (camera.hpp:34-43) + the motion accumulator; block partial sums of the
+// squared error and of the valid count.  The scale 1 / (count used) needs the totals, so it
+// is applied by k_flow_scale after k_flow_reduce.
+__global__ void __launch_bounds__(256) k_flow_loss(CamK C, int nf, const float* __restrict__ out_tof,
+                                                   const float* __restrict__ ext, FlowK F) {
+    __shared__ double red[4][8];
+    const int W = C.W, H = C.H;
+    const size_t HW = (size_t)W * H;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};  // sse_fwd, count_fwd, sse_bwd, count_bwd
+    if (i < (int)HW && !*F.abort) {
+        const int x = i % W, y = i / W;
+        const double pcx = x + 0.5, pcy = y + 0.5;
+        for (int k = 0; k < 2; ++k) {
+            const float* tgt = F.target[k];
+            float* d = F.d_macc + (size_t)3 * k * HW;
+            if (!tgt) continue;
+            const bool valid = tgt[2 * HW + i] > 0.5f && ext[(13 + k) * HW + i] > 0.5f;
+            if (!valid) {
+                d[i] = d[HW + i] = d[2 * HW + i] = 0.f;
+                continue;
+            }
+            const double ru = (double)ext[(9 + 2 * k) * HW + i] - (double)tgt[i];
+            const double rv = (double)ext[(10 + 2 * k) * HW + i] - (double)tgt[HW + i];
+            v[2 * k] = ru * ru + rv * rv;
+            v[2 * k + 1] = 1.0;
+            const double du = 2.0 * ru, dv = 2.0 * rv;
+            const double depth = out_tof[ch_depth(nf) * HW + i];
+            const double dc[3] = {(pcx - C.cx) / C.fx, (pcy - C.cy) / C.fy, 1.0};
+            const double* R = C.R;
+            double dir[3];
+            for (int a = 0; a < 3; ++a) dir[a] = R[0 * 3 + a] * dc[0] + R[1 * 3 + a] * dc[1] + R[2 * 3 + a] * dc[2];
+            const double dn = sqrt(dir[0] * dir[0] + dir[1] * dir[1] + dir[2] * dir[2]);
+            double q[3], pc[3];
+            for (int a = 0; a < 3; ++a)
+                q[a] = C.center[a] + depth * (dir[a] / dn) + (double)ext[(3 + 3 * k + a) * HW + i];
+            for (int r = 0; r < 3; ++r) pc[r] = R[r * 3 + 0] * q[0] + R[r * 3 + 1] * q[1] + R[r * 3 + 2] * q[2] + C.t[r];
+            const double z = pc[2], z2 = z * z;
+            const double dp[3] = {C.fx * du / z, C.fy * dv / z, -(C.fx * pc[0] * du + C.fy * pc[1] * dv) / z2};
+            for (int a = 0; a < 3; ++a)
+                d[(size_t)a * HW + i] = (float)(R[0 * 3 + a] * dp[0] + R[1 * 3 + a] * dp[1] + R[2 * 3 + a] * dp[2]);
+        }
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int c = 0; c < 4; ++c) {
+        double t = v[c];
+        for (int m = 16; m > 0; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+        if (lane == 0) red[c][w] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double t = 0.0;
+        for (int j = 0; j < 8; ++j) t += red[threadIdx.x][j];
+        F.part[(size_t)blockIdx.x * 4 + threadIdx.x] = t;
+    }
+}
+
+// res: [0] value, [1] valid pixels, [2] / [3] gradient scale per direction (0: no gradient).
+__global__ void k_flow_reduce(FlowK F, int nparts, double weight) {
+    __shared__ double s[4][256];
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x)
+        for (int c = 0; c < 4; ++c) a[c] += F.part[(size_t)i * 4 + c];
+    for (int c = 0; c < 4; ++c) s[c][threadIdx.x] = a[c];
+    __syncthreads();
+    for (int m = blockDim.x / 2; m > 0; m >>= 1) {
+        if ((int)threadIdx.x < m)
+            for (int c = 0; c < 4; ++c) s[c][threadIdx.x] += s[c][threadIdx.x + m];
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    int used = 0;
+    double value = 0.0, count = 0.0;
+    for (int k = 0; k < 2; ++k) {
+        if (!F.target[k] || s[2 * k + 1][0] == 0.0) continue;
+        value += s[2 * k][0] / s[2 * k + 1][0];
+        count += s[2 * k + 1][0];
+        ++used;
+    }
+    F.res[0] = used ? value / used : 0.0;
+    F.res[1] = count;
+    for (int k = 0; k < 2; ++k)
+        F.res[2 + k] = (used && F.target[k] && s[2 * k + 1][0] > 0.0) ? weight / (s[2 * k + 1][0] * used) : 0.0;
+}
+
+__global__ void __launch_bounds__(256) k_flow_scale(FlowK F, int npx) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= npx) return;
+    for (int k = 0; k < 2; ++k) {
+        if (!F.target[k]) continue;
+        const float sc = (float)F.res[2 + k];
+        float* d = F.d_macc + (size_t)3 * k * npx;
+        for (int a = 0; a < 3; ++a) d[(size_t)a * npx + i] *= sc;
+    }
+}
+
 }  // namespace
+
+int flow_loss_parts(int npx) { return (npx + 255) / 256; }
+
+void launch_flow_loss(const CamK& C, int nf, const float* out_tof, const float* ext, const FlowK& F, double weight,
+                      cudaStream_t st) {
+    const int npx = C.W * C.H, nb = flow_loss_parts(npx);
+    k_flow_loss<<<nb, 256, 0, st>>>(C, nf, out_tof, ext, F);
+    k_flow_reduce<<<1, 256, 0, st>>>(F, nb, weight);
+    k_flow_scale<<<nb, 256, 0, st>>>(F, npx);
+}
 
 void launch_ext_prep(const SceneK& S, const CamK& C, const FrameDev* fd, const uint32_t* touched, const ExtK& E,
                      const int32_t* abort, cudaStream_t st) {

@@ -347,6 +347,17 @@ void launch_ext_fwd(const RecK& rec, const SceneK& S, const CamK& C, const OptK&
 void launch_ext_bwd(const RecK& rec, const OptK& O, int W, int H, int nf, const uint4* ranges_all, int nchunks,
                     const uint32_t* vals, const PixK& px, const UpK& up, const ExtK& E, float* screen, int scap,
                     cudaStream_t st);
+// flow_loss (losses.cpp:168-251) on the rendered flow channels; 3 kernels.
+struct FlowK {
+    const float* target[2];  // [3][H][W] (u, v, valid) per direction, null = absent
+    float* d_macc;           // [6][H][W]: d_motion_fwd_acc, d_motion_bwd_acc (scaled by the loss weight)
+    double* part;            // [flow_loss_parts][4]
+    double* res;             // [4]: value, valid pixels, gradient scale fwd / bwd (0: no gradient)
+    const int32_t* abort;
+};
+int flow_loss_parts(int npx);
+void launch_flow_loss(const CamK& C, int nf, const float* out_tof, const float* ext, const FlowK& F, double weight,
+                      cudaStream_t st);
 void launch_chain_ext(const SceneK& S, const CamK& C, const FrameK& F, const uint32_t* touched, const ExtK& E,
                       float4* grads, cudaStream_t st);
 // tsb_optim.cu

@@ -480,6 +480,47 @@ class RenderPass:
                                         b.ctypes.data if b is not None else None))
         return self
 
+    def flow_loss(self, target_fwd=None, target_bwd=None, weight: float = 1.0):
+        """flow_loss (losses.cpp:168-251) of the last forward (flow channel): targets (3, H, W) =
+        (u, v, valid) or None.  Returns (value, valid_pixels); the motion-accumulator gradients
+        (x weight) stay on the device for backward_flow()."""
+        H, W = self.camera.height, self.camera.width
+        keep = []
+
+        def arr(a):
+            if a is None:
+                return None
+            a = np.ascontiguousarray(np.asarray(a, np.float32))
+            if a.shape != (3, H, W):
+                raise RuntimeError("flow_loss: target shape mismatch")
+            keep.append(a)
+            return a.ctypes.data
+
+        v, n, g = C.c_double(), C.c_int64(), C.c_int32()
+        check(lib().tsb_pass_flow_loss(self._h, _abi.TSB_HOST, arr(target_fwd), arr(target_bwd), float(weight),
+                                       C.byref(v), C.byref(n), C.byref(g)))
+        self._flow_grads = g.value
+        return v.value, n.value
+
+    def flow_loss_grads(self):
+        """(d_motion_fwd_acc, d_motion_bwd_acc) of the last flow_loss, (3, H, W) or None."""
+        H, W = self.camera.height, self.camera.width
+        g = getattr(self, "_flow_grads", 0)
+        return tuple(self.download(w, shape=(3, H, W)) if g & (1 << k) else None
+                     for k, w in enumerate((_abi.OUT_D_MOTION_FWD_ACC, _abi.OUT_D_MOTION_BWD_ACC)))
+
+    def backward_flow(self, with_image_loss: bool = True):
+        """Backward of the trainer's combined loss for this frame: the image-loss residual (the
+        forward_loss d_quad, when with_image_loss) + the flow-loss motion upstreams, all on the
+        device (trainer.cpp:296-310)."""
+        g = getattr(self, "_flow_grads", 0)
+        ptr = lambda w: C.c_void_p(self.output_ptr(w)[0])
+        dq = ptr(_abi.OUT_D_QUAD) if with_image_loss else None
+        mf = ptr(_abi.OUT_D_MOTION_FWD_ACC) if g & 1 else None
+        mb = ptr(_abi.OUT_D_MOTION_BWD_ACC) if g & 2 else None
+        check(lib().tsb_pass_backward_ext(self._h, _abi.TSB_DEVICE, dq, None, None, None, None, None, None, mf, mb))
+        return self
+
     def motion_grads(self):
         """SceneGrads::d_motion_fwd / d_motion_bwd of the last backward, (n, 3) each."""
         n = self.scene.n

@@ -176,3 +176,81 @@ def test_color_upstream_requires_channel(tsb, ctx):
         rp.backward_buffers(d_color=np.zeros((3, 48, 64), np.float32))
     with pytest.raises(RuntimeError, match="motion"):
         rp.backward_buffers(d_motion_fwd_acc=np.zeros((3, 48, 64), np.float32))
+
+
+def test_flow_loss_and_its_backward(tsb, ctx):
+    """flow_loss (losses.cpp:168-251) on the device against oracle/losses.flow_loss on the oracle's
+    render, then the backward of image loss + weighted flow loss (trainer.cpp:285-317)."""
+    from oracle import losses as ol
+    from paper_2505_05356_b200 import synthetic
+    g, sh, cs, mf, mb, scene, tof = _setup(tsb, ctx, 0, n=3000, seed=52)
+    cam = synthetic.camera(200, 150, 180.0)
+    H, W = cam.height, cam.width
+    frame = (0, 0.6)
+    opts = tsb.RenderOptions(counts=True, flow=True)
+    rp = tsb.RenderPass(ctx).prepare(scene, cam, opts, frame)
+    rp.set_motion(mf, mb)
+    rng = np.random.default_rng(17)
+    target = rng.normal(0, 0.05, (4, H, W)).astype(np.float32)
+    loss = rp.forward_loss(target)
+    out = rp.outputs()
+    tf = np.stack([rng.uniform(-2, 2, (H, W)), rng.uniform(-2, 2, (H, W)),
+                   (rng.uniform(size=(H, W)) > 0.3).astype(float)]).astype(np.float32)
+    tb = np.stack([rng.uniform(-2, 2, (H, W)), rng.uniform(-2, 2, (H, W)), np.ones((H, W))]).astype(np.float32)
+    weight = 0.7
+    value, valid = rp.flow_loss(tf, tb, weight)
+    dmf_up, dmb_up = rp.flow_loss_grads()
+
+    op = orc.OraclePass(_oscene(g, frame, sh, cs, mf, mb, 0), cam, opts)
+    ref = dict(op.forward())
+    ref.update(op.forward_ext())
+    assert np.array_equal(out["flow_valid"], ref["flow_valid"])
+    fl = ol.flow_loss(ref, cam, tf.astype(np.float64), tb.astype(np.float64))
+    assert valid == fl["valid_pixels"] > 0
+    assert value == pytest.approx(fl["value"], rel=1e-4)
+    assert rel_err(dmf_up, weight * fl["d_motion_fwd_acc"], 1e-4) < GRAD_TOL
+    assert rel_err(dmb_up, weight * fl["d_motion_bwd_acc"], 1e-4) < GRAD_TOL
+
+    rp.backward_flow()
+    gr = scene.grads()
+    dmf, dmb = rp.motion_grads()
+    d_quad = np.zeros((4, H, W))
+    for m in range(4):
+        _, d = orc.mse(ref["quad"][m], target[m].astype(np.float64))
+        d_quad[m] = 0.25 * d
+    og = op.backward(d_quad=d_quad, d_motion_fwd_acc=weight * fl["d_motion_fwd_acc"],
+                     d_motion_bwd_acc=weight * fl["d_motion_bwd_acc"])
+    errs = {"d_position": rel_err(gr["d_position"], og["d_position"], 1e-4),
+            "d_opacity_logit": rel_err(gr["d_opacity_logit"], og["d_opacity_logit"], 1e-4),
+            "d_log_scale": rel_err(gr["d_log_scale"], og["d_log_scale"], 1e-4),
+            "d_motion_fwd": rel_err(dmf, og["d_motion_fwd"], 1e-4),
+            "d_motion_bwd": rel_err(dmb, og["d_motion_bwd"], 1e-4)}
+    assert all(e < GRAD_TOL for e in errs.values()), errs
+    assert loss > 0
+
+
+def test_flow_loss_masking_and_errors(tsb, ctx):
+    """test_losses.cpp:162-217 semantics on the device: target = render -> 0; + (3, 0) -> 9;
+    a direction without targets has no gradient; empty validity -> 0 and no gradient."""
+    from paper_2505_05356_b200 import synthetic
+    _, _, _, mf, mb, scene, _ = _setup(tsb, ctx, 0, n=1500, seed=61)
+    cam = synthetic.camera(96, 64, 90.0)
+    rp = tsb.RenderPass(ctx).prepare(scene, cam, tsb.RenderOptions(flow=True), (0, 0.3))
+    rp.set_motion(mf, mb)
+    rp.forward()
+    out = rp.outputs()
+    tf = np.concatenate([out["flow_fwd"], np.ones((1, 64, 96), np.float32)])
+    v, n = rp.flow_loss(tf, None)
+    assert abs(v) < 1e-12 and n == int((out["flow_valid"][0] > 0.5).sum()) > 0
+    t3 = tf.copy()
+    t3[0] += 3.0
+    v, _ = rp.flow_loss(t3, None)
+    assert v == pytest.approx(9.0, rel=1e-6)
+    assert rp.flow_loss_grads()[1] is None and rp.flow_loss_grads()[0] is not None
+    none = tf.copy()
+    none[2] = 0.0
+    v, n = rp.flow_loss(none, None)
+    assert v == 0.0 and n == 0 and rp.flow_loss_grads() == (None, None)
+    rq = tsb.RenderPass(ctx).prepare(scene, cam, tsb.RenderOptions(), (0, 0.3)).forward()
+    with pytest.raises(RuntimeError, match="flow channels"):
+        rq.flow_loss(tf, None)
