@@ -281,9 +281,10 @@ int tsb_pass_get_motion_grads(tsb_pass* p, float* d_motion_fwd, float* d_motion_
 /* Copy a pass-owned buffer to host memory (synchronous). */
 int tsb_pass_download(tsb_pass* p, int which, void* host, size_t bytes);
 /* Enqueue the copy of a pass-owned buffer into host memory (pinned memory for
- * overlap) without waiting.  The bytes are valid once the pass is settled:
- * tsb_pass_wait, tsb_ctx_synchronize, or the pass's next tsb_pass_prepare (a
- * frame redone after a device-side abort re-issues its downloads). */
+ * overlap) without waiting.  The bytes are valid after tsb_pass_wait or
+ * tsb_ctx_synchronize (a frame redone after a device-side abort re-issues its
+ * downloads).  The pass's next tsb_pass_prepare waits only for the forward, so
+ * copies of consecutive frames stay in flight behind it (stream-ordered). */
 int tsb_pass_download_async(tsb_pass* p, int which, void* host, size_t bytes);
 /* Settle the pass (redo an aborted frame) and wait for everything enqueued on it. */
 int tsb_pass_wait(tsb_pass* p);

@@ -133,6 +133,8 @@ struct tsb_pass {
     tsb_ctx* ctx = nullptr;
     cudaStream_t stream = nullptr;   // each pass runs on its own stream (frames overlap)
     cudaEvent_t done_ev = nullptr;   // recorded after every enqueue (tsb_ctx_join)
+    cudaEvent_t fwd_ev = nullptr;    // end of the last forward (its abort word is final): settle waits here,
+                                     // not for the frame's backward or downloads
     void* pinned = nullptr;          // per-pass pinned staging
     tsb_scene* scene = nullptr;
     CamK cam{};
@@ -880,6 +882,7 @@ int tsb_pass_create(tsb_ctx* ctx, tsb_pass** out) {
     if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->done_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->fwd_ev, cudaEventDisableTiming) != cudaSuccess ||
         cudaMallocHost(&p->pinned, 4096) != cudaSuccess) {
         tsb_pass_destroy(p);
         return fail(TSB_ERR_CUDA, "tsb_pass_create: stream/event/pinned allocation failed");
@@ -1113,6 +1116,7 @@ void tsb_pass_destroy(tsb_pass* p) {
     dev_free(p->ext_dmacc); dev_free(p->ext_ftgt); dev_free(p->ext_fl_part); dev_free(p->ext_fl_res);
     if (p->pinned) cudaFreeHost(p->pinned);
     if (p->done_ev) cudaEventDestroy(p->done_ev);
+    if (p->fwd_ev) cudaEventDestroy(p->fwd_ev);
     for (auto& fg : p->fwd)
         if (fg.exec) cudaGraphExecDestroy(fg.exec);
     dev_free(p->frame_dev);
@@ -1616,6 +1620,7 @@ int enqueue_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw,
     p->pend_chw = chw;
     p->pend_bwd = false;
     p->pend_dl.clear();
+    TSB_CUDA(cudaEventRecord(p->fwd_ev, st));
     TSB_CUDA(cudaEventRecord(p->done_ev, st));
     return TSB_OK;
 }
@@ -1624,7 +1629,8 @@ int output_ptr(tsb_pass* p, int which, void** dptr, size_t* bytes);
 
 int enqueue_backward(tsb_pass* p, const UpK& up);
 
-// Wait for the pass's enqueued frame and check its abort word.  An aborted
+// Wait for the pass's enqueued forward (not its backward or downloads: they stay
+// in flight behind it on the pass stream) and check its abort word.  An aborted
 // frame wrote nothing (every kernel after the abort returns at entry); it is
 // redone with more list storage / the exact 64-bit depth sort, including its
 // loss and backward.  Its inputs are still intact: everything that changes the
@@ -1632,7 +1638,7 @@ int enqueue_backward(tsb_pass* p, const UpK& up);
 int settle(tsb_pass* p) {
     for (int attempt = 0; p->pending; ++attempt) {
         TSB_CUDA(cudaSetDevice(p->ctx->device));
-        TSB_CUDA(cudaStreamSynchronize(p->stream));
+        TSB_CUDA(cudaEventSynchronize(p->fwd_ev));
         p->pending = false;
         const int32_t* hc = (const int32_t*)((const char*)p->pinned + 2048);
         p->V = hc[0];

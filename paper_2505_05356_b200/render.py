@@ -542,7 +542,7 @@ class RenderPass:
 
     def download_async(self, which: int, host: np.ndarray):
         """Enqueue a device->host copy of output `which` into `host` (ideally pinned);
-        valid after wait() / Context.synchronize() / this pass's next prepare()."""
+        valid after wait() / Context.synchronize() (prepare() of the next frame does not wait for it)."""
         check(lib().tsb_pass_download_async(self._h, which, host.ctypes.data, host.nbytes))
         return self
 
