@@ -11,7 +11,8 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libtsb.so"
+# TSB_LIB: an alternative in-tree build of the same ABI (A/B timing experiments)
+LIB_PATH = Path(os.environ.get("TSB_LIB") or Path(__file__).resolve().parent / "lib" / "libtsb.so")
 HEADER_PATH = Path(__file__).resolve().parent.parent / "include" / "tsb.h"
 
 TSB_OK, TSB_ERR_INVALID, TSB_ERR_CUDA, TSB_ERR_NOMEM, TSB_ERR_UNSUPPORTED, TSB_ERR_NCCL = range(6)
