@@ -73,10 +73,11 @@ __device__ __forceinline__ void sh_jacobian64(const double* d, int degree, doubl
 }
 
 // The 16 reflectivity SH coefficients of Gaussian gi (coefficient 0 lives in scale_amp.w).
-__device__ __forceinline__ void refl_coeffs(const SceneK& S, int gi, double* c) {
-    c[0] = (double)S.scale_amp[gi].w;
+__device__ __forceinline__ void refl_coeffs(const float4* __restrict__ scale_amp, const float4* __restrict__ sh, int n,
+                                            int gi, double* c) {
+    c[0] = (double)scale_amp[gi].w;
     for (int a = 0; a < 4; ++a) {
-        const float4 v = S.sh[(size_t)a * S.n + gi];
+        const float4 v = sh[(size_t)a * n + gi];
         const int k = 1 + 4 * a;
         c[k] = v.x;
         c[k + 1] = v.y;
@@ -86,12 +87,14 @@ __device__ __forceinline__ void refl_coeffs(const SceneK& S, int gi, double* c) 
 }
 
 // sum_k refl_sh[k] b_k(view_dir) for sh_degree > 0 (out of line: keeps the
-// degree-0 kernels' register budget).
-static __device__ __noinline__ double refl_sh_eval(const SceneK& S, int gi, double v0, double v1, double v2) {
+// degree-0 kernels' register budget).  Scalar arguments only: a SceneK reference
+// would make every caller copy the struct to its stack at entry.
+static __device__ __noinline__ double refl_sh_eval(const float4* scale_amp, const float4* sh, int n, int degree,
+                                                   int gi, double v0, double v1, double v2) {
     const double v[3] = {v0, v1, v2};
     double b[16], c[16];
-    sh_basis64(v, S.sh_degree, b);
-    refl_coeffs(S, gi, c);
+    sh_basis64(v, degree, b);
+    refl_coeffs(scale_amp, sh, n, gi, c);
     double rr = 0.0;
     for (int k = 0; k < 16; ++k) rr += c[k] * b[k];
     return rr;
@@ -105,7 +108,7 @@ __device__ __forceinline__ double refl_raw64(const SceneK& S, const CamK& C, int
         return (double)S.scale_amp[gi].w * 0.28209479177387814;
     }
     for (int i = 0; i < 3; ++i) view_dir[i] = (x[i] - C.center[i]) / depth;
-    return refl_sh_eval(S, gi, view_dir[0], view_dir[1], view_dir[2]);
+    return refl_sh_eval(S.scale_amp, S.sh, S.n, S.sh_degree, gi, view_dir[0], view_dir[1], view_dir[2]);
 }
 
 struct Prep64 {

@@ -459,12 +459,12 @@ __device__ __forceinline__ void chain_prep(const SceneK& S, const CamK& C, const
 // Reflectivity SH part of the chain for sh_degree > 0 (out of line so the common
 // degree-0 path keeps its register budget): d_refl[k] = b_k d_r and
 // d_dir = Jb^T (refl_sh * d_r) (splat.cpp:579-583).
-__device__ __noinline__ void sh_chain(const SceneK& S, int gi, const double* view_dir, double d_r, double* d_refl,
-                                      double* d_dir) {
+__device__ __noinline__ void sh_chain(const float4* scale_amp, const float4* sh, int n, int degree, int gi,
+                                      const double* view_dir, double d_r, double* d_refl, double* d_dir) {
     double b[16], c[16], Jb[16][3];
-    sh_basis64(view_dir, S.sh_degree, b);
-    refl_coeffs(S, gi, c);
-    sh_jacobian64(view_dir, S.sh_degree, Jb);
+    sh_basis64(view_dir, degree, b);
+    refl_coeffs(scale_amp, sh, n, gi, c);
+    sh_jacobian64(view_dir, degree, Jb);
     for (int k = 0; k < 16; ++k) d_refl[k] = b[k] * d_r;
     for (int a = 0; a < 3; ++a) {
         double t = 0.0;
@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(128, 4) k_chain(SceneK S, CamK C, OptK O, Fram
         if (S.sh_degree == 0) {
             d_amp = 0.28209479177387814 * d_r;
         } else {
-            sh_chain(S, gi, s.view_dir, d_r, d_refl, d_dir);
+            sh_chain(S.scale_amp, S.sh, S.n, S.sh_degree, gi, s.view_dir, d_r, d_refl, d_dir);
             d_amp = d_refl[0];
         }
     }
