@@ -313,9 +313,9 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_bwd(RecK rec, OptK O, in
                         if (!(ev.alpha - thr < 0.f)) {
                             contrib = true;
                             const float om = 1.f - ev.alpha;
-                            // T before this entry, back from the last contributor's; a 2-ulp quotient (the
-                            // error grows ~linearly with depth, far inside the 1e-3 gradient tolerance)
-                            const float Tk = first ? Tnext : __fdividef(Tnext, om);
+                            // T before this entry, back from the last contributor's (correctly rounded:
+                            // these channels are T-weighted like the ones of k_raster_bwd<EXTRA>)
+                            const float Tk = first ? Tnext : __fdiv_rn(Tnext, om);
                             first = false;
                             Tnext = Tk;
                             const float4 cc = sC[j], mf = sMf[j], mb = sMb[j];

@@ -457,20 +457,33 @@ __device__ __forceinline__ void chain_prep(const SceneK& S, const CamK& C, const
 }
 
 // Reflectivity SH part of the chain for sh_degree > 0 (out of line so the common
-// degree-0 path keeps its register budget): d_refl[k] = b_k d_r and
-// d_dir = Jb^T (refl_sh * d_r) (splat.cpp:579-583).
-__device__ __noinline__ void sh_chain(const float4* scale_amp, const float4* sh, int n, int degree, int gi,
-                                      const double* view_dir, double d_r, double* d_refl, double* d_dir) {
+// degree-0 path keeps its register budget): d_refl[k] = b_k d_r, accumulated into the
+// SH gradient arrays (coefficients 1..15; coefficient 0 is the caller's), and the
+// returned d_dir = Jb^T (refl_sh * d_r) (splat.cpp:579-583).  Arguments and result by
+// value: arrays or references would live in the caller's local memory.
+__device__ __noinline__ double3 sh_chain(const float4* scale_amp, const float4* sh, int n, int degree, int gi,
+                                         double v0, double v1, double v2, double d_r, float4* gs) {
+    const double view_dir[3] = {v0, v1, v2};
     double b[16], c[16], Jb[16][3];
     sh_basis64(view_dir, degree, b);
     refl_coeffs(scale_amp, sh, n, gi, c);
     sh_jacobian64(view_dir, degree, Jb);
-    for (int k = 0; k < 16; ++k) d_refl[k] = b[k] * d_r;
+    for (int a = 0; a < 4; ++a) {
+        float4 v = gs[(size_t)a * n];
+        const int k = 1 + 4 * a;
+        v.x += (float)(b[k] * d_r);
+        v.y += (float)(b[k + 1] * d_r);
+        v.z += (float)(b[k + 2] * d_r);
+        if (a < 3) v.w += (float)(b[k + 3] * d_r);
+        gs[(size_t)a * n] = v;
+    }
+    double d[3];
     for (int a = 0; a < 3; ++a) {
         double t = 0.0;
         for (int k = 0; k < 16; ++k) t += Jb[k][a] * (c[k] * d_r);
-        d_dir[a] = t;
+        d[a] = t;
     }
+    return make_double3(d[0], d[1], d[2]);
 }
 
 // ---------------------------------------------------------------------------
@@ -507,17 +520,18 @@ __global__ void __launch_bounds__(128, 4) k_chain(SceneK S, CamK C, OptK O, Fram
     const double id2 = id * id;
     const double d_depth = d_dep + d_coef * (-2.0 * S.s_int * r_cl * id2 * id);
     // reflectivity SH through coef = s_int * r / d^2 (splat.cpp:573-583), gated by 0 < r_raw < 1
-    double d_refl[16];
     double d_dir[3] = {0.0, 0.0, 0.0};
     double d_amp = 0.0;
     const bool gated = s.refl_raw > 0.0 && s.refl_raw < 1.0;
     if (gated) {
         const double d_r = d_coef * S.s_int * id2;
-        if (S.sh_degree == 0) {
-            d_amp = 0.28209479177387814 * d_r;
-        } else {
-            sh_chain(S.scale_amp, S.sh, S.n, S.sh_degree, gi, s.view_dir, d_r, d_refl, d_dir);
-            d_amp = d_refl[0];
+        d_amp = 0.28209479177387814 * d_r;  // b_0 d_r
+        if (S.sh_degree > 0) {
+            const double3 dd = sh_chain(S.scale_amp, S.sh, S.n, S.sh_degree, gi, s.view_dir[0], s.view_dir[1],
+                                        s.view_dir[2], d_r, grads + (size_t)(3 + S.nk) * S.n + gi);
+            d_dir[0] = dd.x;
+            d_dir[1] = dd.y;
+            d_dir[2] = dd.z;
         }
     }
 
@@ -611,18 +625,6 @@ __global__ void __launch_bounds__(128, 4) k_chain(SceneK S, CamK C, OptK O, Fram
     float4 g2 = grads[2 * n + gi];
     g2.x += (float)dq[0]; g2.y += (float)dq[1]; g2.z += (float)dq[2]; g2.w += (float)dq[3];
     grads[2 * n + gi] = g2;
-    if (S.sh_degree > 0 && gated) {
-        float4* gs = grads + (size_t)(3 + S.nk) * n + gi;
-        for (int a = 0; a < 4; ++a) {
-            float4 v = gs[(size_t)a * n];
-            const int k = 1 + 4 * a;
-            v.x += (float)d_refl[k];
-            v.y += (float)d_refl[k + 1];
-            v.z += (float)d_refl[k + 2];
-            if (a < 3) v.w += (float)d_refl[k + 3];
-            gs[(size_t)a * n] = v;
-        }
-    }
     if (S.nk > 0) {
         const double wa = 1.0 - F.w, wb = F.w;
         float4* gm = grads + (size_t)(3 + F.key) * n + gi;

@@ -439,9 +439,11 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
                         if (!(ev.alpha - thr < 0.f)) {
                             contrib = true;
                             const float om = 1.f - ev.alpha;
-                            // T before this entry, back from the last contributor's; a 2-ulp quotient (the
-                            // error grows ~linearly with depth, far inside the 1e-3 gradient tolerance)
-                            const float Tk = first ? Tnext : __fdividef(Tnext, om);
+                            // T before this entry, back from the last contributor's.  The quad / phasor
+                            // path takes a 2-ulp quotient (error ~linear in depth, far inside the 1e-3
+                            // gradient tolerance); the T-weighted channels, whose recursion runs on
+                            // differences of nearly equal terms, keep the correctly rounded one.
+                            const float Tk = first ? Tnext : (EXTRA ? __fdiv_rn(Tnext, om) : __fdividef(Tnext, om));
                             first = false;
                             Tnext = Tk;
                             const float4 Cc = sm.C[j];
