@@ -253,7 +253,9 @@ __device__ __forceinline__ void fixup_batch(const SceneK& S, const CamK& C, cons
         w = alpha * Tk;
         w2 = alpha * Tk * Tk;
         const double cq = coef * w2;
-        for (int f = 0; f < nf; ++f) {
+        #pragma unroll
+        for (int f = 0; f < 2; ++f) {
+            if (f >= nf) break;
             double sn, cs;
             sincos(phase_of_depth(depth, S.freq[f], S.c), &sn, &cs);
             q[4 * f + 0] = cq * sn;
@@ -262,7 +264,9 @@ __device__ __forceinline__ void fixup_batch(const SceneK& S, const CamK& C, cons
     }
     const unsigned mm = __ballot_sync(0xffffffffu, mine);
     if (mm) {
-        for (int f = 0; f < nf; ++f) {
+        #pragma unroll
+        for (int f = 0; f < 2; ++f) {
+            if (f >= nf) break;
             const double s0 = warp_sum(q[4 * f + 0]), s1 = warp_sum(q[4 * f + 1]);
             a.accQ[4 * f + 0] += s0;
             a.accQ[4 * f + 1] += s1;
@@ -347,12 +351,16 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, const F
         }
         if (lane == 0) {
             const size_t o = (size_t)y * W + x;
-            for (int c = 0; c < 4 * nf; ++c) px.out[c * HW + o] = (float)(a.accQ[c] + O.bg_quad[c] * a.T * a.T);
+            #pragma unroll
+            for (int c = 0; c < 8; ++c)
+                if (c < 4 * nf) px.out[c * HW + o] = (float)(a.accQ[c] + O.bg_quad[c] * a.T * a.T);
             px.out[ch_depth_raw(nf) * HW + o] = (float)a.SD;
             px.out[ch_depth(nf) * HW + o] = a.SW > O.cov_eps ? (float)(a.SD / a.SW) : __int_as_float(0x7fc00000);
             px.out[ch_weight(nf) * HW + o] = (float)a.SW;
             px.out[ch_T(nf) * HW + o] = (float)a.T;
-            for (int f = 0; f < nf; ++f) {
+            #pragma unroll
+            for (int f = 0; f < 2; ++f) {
+                if (f >= nf) break;
                 px.out[(ch_phasor(nf) + 2 * f + 0) * HW + o] =
                     (float)(2.0 * a.accQ[4 * f + 1] + O.bg_phasor[2 * f + 0] * a.T * a.T);
                 px.out[(ch_phasor(nf) + 2 * f + 1) * HW + o] =
