@@ -276,6 +276,13 @@ int tsb_pass_set_motion(tsb_pass* p, int where, const float* motion_fwd, const f
  * tsb_pass_backward_ext(TSB_DEVICE, ...). */
 int tsb_pass_flow_loss(tsb_pass* p, int where, const float* target_fwd, const float* target_bwd, double weight,
                        double* value, int64_t* valid_pixels, int32_t* has_grads);
+/* One render stack of write_render_stacks (eval.cpp:96-121, 165-185) from the pass's last
+ * forward (needs TSB_CH_DISTORTION; colour written when TSB_CH_COLOR): into `dir` (created),
+ * quad_QQQQQ_p0/_p90/_p180/_p270.pfm (first frequency), depth_QQQQQ.pfm (mean depth where
+ * weight > 0.5, NaN elsewhere), dtof_QQQQQ.pfm (depth decoded from the rendered quad),
+ * dd_QQQQQ.pfm (distortion) and color_QQQQQ.pfm, QQQQQ = quartet zero-padded to 5 digits.
+ * The derived planes are computed on the device; the files are written on the host. */
+int tsb_pass_render_stack(tsb_pass* p, const char* dir, int quartet);
 /* SceneGrads::d_motion_fwd / d_motion_bwd (splat.hpp:86) of the last backward, n x 3 each. */
 int tsb_pass_get_motion_grads(tsb_pass* p, float* d_motion_fwd, float* d_motion_bwd);
 /* Copy a pass-owned buffer to host memory (synchronous). */
@@ -382,6 +389,12 @@ int tsb_deform_adam_step(tsb_deform* net, double lr, double beta1, double beta2,
 int tsb_debug_gemm(tsb_ctx* ctx, int M, int N, int K, int slices, const float* A, int64_t a_m, int64_t a_k,
                    const float* B, int64_t b_n, int64_t b_k, const float* bias, int relu, const float* mask,
                    float* C);
+
+/* Portable FloatMap I/O (pfm.hpp, pfm.cpp:51-114) on planar [C][H][W] fp32 images: "Pf" = 1
+ * channel, "PF" = 3 channels; rows bottom to top; written little-endian (scale -1.0), read in
+ * either byte order.  tsb_read_pfm with planar = NULL only reports the dimensions.  Host only. */
+int tsb_write_pfm(const char* path, const float* planar, int width, int height, int channels);
+int tsb_read_pfm(const char* path, float* planar, size_t capacity_floats, int* width, int* height, int* channels);
 
 /* ---- small host helpers mirroring the Python _core surface --------------- */
 /* unambiguous_range (tof.hpp:36-38), quad_to_depth (tof.hpp:59-65),

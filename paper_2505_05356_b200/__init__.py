@@ -10,7 +10,9 @@ from ._abi import TsbError, lib as _load_lib
 _load_lib()
 
 from .render import (AdamParams, CameraModel, Comm, Context, DeformNet, GaussianScene, LrTable, RenderOptions,  # noqa: E402
-                     RenderPass, ToFConfig, frame_for_time, quad_basis, quad_to_depth, unambiguous_range)
+                     RenderPass, ToFConfig, frame_for_time, quad_basis, quad_to_depth, read_pfm, unambiguous_range,
+                     write_pfm)
 
 __all__ = ["AdamParams", "CameraModel", "Comm", "Context", "DeformNet", "GaussianScene", "LrTable", "RenderOptions", "RenderPass",
-           "ToFConfig", "TsbError", "frame_for_time", "quad_basis", "quad_to_depth", "unambiguous_range"]
+           "ToFConfig", "TsbError", "frame_for_time", "quad_basis", "quad_to_depth", "read_pfm", "unambiguous_range",
+           "write_pfm"]

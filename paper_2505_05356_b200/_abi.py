@@ -159,6 +159,9 @@ SIGNATURES = {
     "tsb_comm_create": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.POINTER(_vp)]),
     "tsb_comm_destroy": (None, [_vp]),
     "tsb_scene_allreduce_grads": (C.c_int, [_vp, _vp]),
+    "tsb_write_pfm": (C.c_int, [C.c_char_p, _vp, C.c_int, C.c_int, C.c_int]),
+    "tsb_read_pfm": (C.c_int, [C.c_char_p, _vp, C.c_size_t, _ip, _ip, _ip]),
+    "tsb_pass_render_stack": (C.c_int, [_vp, C.c_char_p, C.c_int]),
     "tsb_unambiguous_range": (C.c_double, [C.c_double]),
     "tsb_quad_to_depth": (C.c_double, [C.c_double] * 5),
     "tsb_quad_basis": (None, [C.c_double, C.c_double, _dp]),

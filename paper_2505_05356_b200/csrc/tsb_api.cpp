@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <filesystem>
 #include <string>
 #include <vector>
 
@@ -64,6 +65,11 @@ void dev_free(T*& p) {
 }
 
 }  // namespace
+
+namespace tsb {
+// error reporting for the host-only TUs (tsb_io.cpp)
+int io_fail(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace tsb
 
 struct tsb_ctx {
     int device = 0;
@@ -2050,6 +2056,52 @@ int tsb_pass_flow_loss(tsb_pass* p, int where, const float* target_fwd, const fl
     if (value) *value = res[0];
     if (valid_pixels) *valid_pixels = (int64_t)res[1];
     if (has_grads) *has_grads = (p->fl_grad[0] ? 1 : 0) | (p->fl_grad[1] ? 2 : 0);
+    return TSB_OK;
+}
+
+int tsb_pass_render_stack(tsb_pass* p, const char* dir, int quartet) {
+    if (!p || !dir) return fail(TSB_ERR_INVALID, "tsb_pass_render_stack: null argument");
+    if (!p->forwarded) return fail(TSB_ERR_INVALID, "render_stack: requires a forward pass");
+    if (!(p->channels & TSB_CH_DISTORTION))
+        return fail(TSB_ERR_INVALID, "render_stack: needs the distortion channel (eval.cpp:104)");
+    if (quartet < 0 || quartet > 99999) return fail(TSB_ERR_INVALID, "render_stack: quartet index out of range");
+    int rc = settle(p);
+    if (rc) return rc;
+    std::error_code ec;
+    std::filesystem::create_directories(dir, ec);
+    if (ec) return fail(TSB_ERR_INVALID, std::string("render_stack: cannot create ") + dir + ": " + ec.message());
+    const int npx = p->W * p->H;
+    const size_t HW = (size_t)npx;
+    float* planes = nullptr;
+    if ((rc = dev_alloc(&planes, 2 * HW))) return rc;
+    cudaStream_t st = p->stream;
+    launch_stack_planes(p->out, p->nf, npx, p->scene->d.frequency[0], p->scene->d.speed_of_light, planes, st);
+    p->ctx->launches += 1;
+    TSB_CHECK_LAUNCH();
+    // host copies: quad (first frequency), gated depth + d_ToF, distortion, colour
+    const bool color = (p->channels & TSB_CH_COLOR) != 0;
+    std::vector<float> h((size_t)(4 + 2 + 1 + (color ? 3 : 0)) * HW);
+    TSB_CUDA(cudaMemcpyAsync(h.data(), p->out, sizeof(float) * 4 * HW, cudaMemcpyDeviceToHost, st));
+    TSB_CUDA(cudaMemcpyAsync(h.data() + 4 * HW, planes, sizeof(float) * 2 * HW, cudaMemcpyDeviceToHost, st));
+    TSB_CUDA(cudaMemcpyAsync(h.data() + 6 * HW, p->out + ch_distortion(p->nf) * HW, sizeof(float) * HW,
+                             cudaMemcpyDeviceToHost, st));
+    if (color)
+        TSB_CUDA(cudaMemcpyAsync(h.data() + 7 * HW, p->ext_out, sizeof(float) * 3 * HW, cudaMemcpyDeviceToHost, st));
+    TSB_CUDA(cudaStreamSynchronize(st));
+    cudaFree(planes);
+    // file names of write_render_stacks (eval.cpp:78-82, 168-184)
+    auto name = [&](const char* stem, const char* suffix) {
+        char buf[64];
+        std::snprintf(buf, sizeof buf, "%s_%05d%s.pfm", stem, quartet, suffix);
+        return (std::filesystem::path(dir) / buf).string();
+    };
+    static const char* kPhase[4] = {"_p0", "_p90", "_p180", "_p270"};
+    for (int m = 0; m < 4; ++m)
+        if ((rc = tsb_write_pfm(name("quad", kPhase[m]).c_str(), h.data() + m * HW, p->W, p->H, 1))) return rc;
+    if ((rc = tsb_write_pfm(name("depth", "").c_str(), h.data() + 4 * HW, p->W, p->H, 1))) return rc;
+    if ((rc = tsb_write_pfm(name("dtof", "").c_str(), h.data() + 5 * HW, p->W, p->H, 1))) return rc;
+    if ((rc = tsb_write_pfm(name("dd", "").c_str(), h.data() + 6 * HW, p->W, p->H, 1))) return rc;
+    if (color && (rc = tsb_write_pfm(name("color", "").c_str(), h.data() + 7 * HW, p->W, p->H, 3))) return rc;
     return TSB_OK;
 }
 

@@ -542,7 +542,33 @@ __global__ void __launch_bounds__(256) k_flow_scale(FlowK F, int npx) {
     }
 }
 
+// write_render_stacks' derived planes (eval.cpp:96-121, 20-34): mean depth gated at
+// coverage weight > 0.5 (NaN elsewhere) and d_ToF decoded from the rendered quad of the
+// first frequency (tof.hpp:64-71: phase of (q90 - q270, q0 - q180) in [0, 2 pi), NaN
+// where both differences vanish).
+__global__ void __launch_bounds__(256) k_stack_planes(const float* __restrict__ out, int nf, int npx, double freq,
+                                                      double c, float* __restrict__ dst) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= npx) return;
+    const size_t n = (size_t)npx;
+    const float nanf = __int_as_float(0x7fc00000);
+    dst[i] = out[ch_weight(nf) * n + i] > 0.5f ? out[ch_depth(nf) * n + i] : nanf;
+    const double re = (double)out[n + i] - (double)out[3 * n + i];
+    const double im = (double)out[i] - (double)out[2 * n + i];
+    float d = nanf;
+    if (!(re == 0.0 && im == 0.0)) {
+        double psi = atan2(im, re);
+        if (psi < 0.0) psi += 2.0 * M_PI;
+        d = (float)(psi * c / (4.0 * M_PI * freq));
+    }
+    dst[n + i] = d;
+}
+
 }  // namespace
+
+void launch_stack_planes(const float* out, int nf, int npx, double freq, double c, float* dst, cudaStream_t st) {
+    if (npx > 0) k_stack_planes<<<(npx + 255) / 256, 256, 0, st>>>(out, nf, npx, freq, c, dst);
+}
 
 int flow_loss_parts(int npx) { return (npx + 255) / 256; }
 

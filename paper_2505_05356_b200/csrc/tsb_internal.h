@@ -356,6 +356,8 @@ struct FlowK {
     const int32_t* abort;
 };
 int flow_loss_parts(int npx);
+// render-stack planes (eval.cpp:96-121): [0] depth gated at weight > 0.5, [1] d_ToF from the quad
+void launch_stack_planes(const float* out, int nf, int npx, double freq, double c, float* dst, cudaStream_t st);
 void launch_flow_loss(const CamK& C, int nf, const float* out_tof, const float* ext, const FlowK& F, double weight,
                       cudaStream_t st);
 void launch_chain_ext(const SceneK& S, const CamK& C, const FrameK& F, const uint32_t* touched, const ExtK& E,

@@ -521,6 +521,13 @@ class RenderPass:
         check(lib().tsb_pass_backward_ext(self._h, _abi.TSB_DEVICE, dq, None, None, None, None, None, None, mf, mb))
         return self
 
+    def write_render_stack(self, directory, quartet: int):
+        """One render stack of write_render_stacks (eval.cpp:96-121, 165-185) from the last forward
+        (options.distortion required; colour written when options.color): quad planes, gated
+        depth, d_ToF, distortion (and colour) as PFM files named as the reference names them."""
+        check(lib().tsb_pass_render_stack(self._h, str(directory).encode(), int(quartet)))
+        return self
+
     def motion_grads(self):
         """SceneGrads::d_motion_fwd / d_motion_bwd of the last backward, (n, 3) each."""
         n = self.scene.n
@@ -666,6 +673,25 @@ class Comm:
 
 
 # ---- Python _core surface (bindings.cpp:43-63) ----
+def write_pfm(path, img) -> None:
+    """write_pfm (pfm.cpp:51-75): planar (C, H, W) or (H, W) float image, C in {1, 3}."""
+    a = np.ascontiguousarray(np.asarray(img, np.float32))
+    if a.ndim == 2:
+        a = a[None]
+    c, h, w = a.shape
+    check(lib().tsb_write_pfm(str(path).encode(), a.ctypes.data, w, h, c))
+
+
+def read_pfm(path) -> np.ndarray:
+    """read_pfm (pfm.cpp:77-114) -> planar (C, H, W) float32."""
+    w, h, c = C.c_int32(), C.c_int32(), C.c_int32()
+    p = str(path).encode()
+    check(lib().tsb_read_pfm(p, None, 0, C.byref(w), C.byref(h), C.byref(c)))
+    out = np.empty((c.value, h.value, w.value), np.float32)
+    check(lib().tsb_read_pfm(p, out.ctypes.data, out.size, C.byref(w), C.byref(h), C.byref(c)))
+    return out
+
+
 def unambiguous_range(frequency: float = 0.0) -> float:
     return float(lib().tsb_unambiguous_range(float(frequency)))
 

@@ -254,3 +254,38 @@ def test_flow_loss_masking_and_errors(tsb, ctx):
     rq = tsb.RenderPass(ctx).prepare(scene, cam, tsb.RenderOptions(), (0, 0.3)).forward()
     with pytest.raises(RuntimeError, match="flow channels"):
         rq.flow_loss(tf, None)
+
+
+def test_render_stack_files(tsb, ctx, tmp_path):
+    """write_render_stacks (eval.cpp:96-121, 165-185) for one quartet: the PFM files and
+    their planes against the pass's own outputs and the numpy restatement (oracle/pfm.py)."""
+    from oracle import pfm as opfm
+    from paper_2505_05356_b200 import synthetic
+    g, sh, cs, _, _, scene, tof = _setup(tsb, ctx, 0, n=2500, seed=71)
+    cam = synthetic.camera(96, 72, 90.0)
+    opts = tsb.RenderOptions(distortion=True, color=True, bg_color=(0.1, 0.2, 0.3))
+    rp = tsb.RenderPass(ctx).prepare(scene, cam, opts, (0, 0.5)).forward()
+    out = rp.outputs()
+    rp.write_render_stack(tmp_path, 7)
+    assert sorted(p.name for p in tmp_path.iterdir()) == sorted(opfm.stack_names(7, color=True))
+    rd = lambda name: opfm.read_pfm(tmp_path / name)
+    for m, s in enumerate(("_p0", "_p90", "_p180", "_p270")):
+        assert np.array_equal(rd(f"quad_00007{s}.pfm")[0], out["quad"][m])
+    depth = rd("depth_00007.pfm")[0]
+    want = opfm.stack_depth(out["depth"], out["weight"])
+    assert np.array_equal(np.isnan(depth), np.isnan(want))
+    assert np.array_equal(depth[~np.isnan(depth)], want[~np.isnan(want)].astype(np.float32))
+    assert 0 < np.isnan(depth).sum() < depth.size
+    dtof = rd("dtof_00007.pfm")[0].astype(np.float64)
+    wd = opfm.quad_to_depth(out["quad"][:4], 30e6)
+    assert np.array_equal(np.isnan(dtof), np.isnan(wd))
+    du = tsb.unambiguous_range(30e6)
+    diff = np.abs(dtof - wd)[~np.isnan(wd)]
+    diff = np.minimum(diff, du - diff)  # phase wrap at 0 / d_u
+    assert diff.max() <= 1e-6 * du
+    assert np.array_equal(rd("dd_00007.pfm")[0], out["distortion"])
+    assert np.array_equal(rd("color_00007.pfm"), out["color"])
+    # without the distortion channel the stack is refused (eval.cpp:104 renders it)
+    rq = tsb.RenderPass(ctx).prepare(scene, cam, tsb.RenderOptions(), (0, 0.5)).forward()
+    with pytest.raises(RuntimeError, match="distortion"):
+        rq.write_render_stack(tmp_path / "x", 0)
