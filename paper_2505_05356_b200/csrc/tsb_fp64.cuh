@@ -135,6 +135,15 @@ __device__ __forceinline__ int d2i_like_x86(double v) {
     return (int)v;
 }
 
+// 1/x to a few ulps: hardware approximation + two Newton steps (no correctly rounded
+// division and its slow path) -- only for values that end in an fp32 record.
+__device__ __forceinline__ double rcp64(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = fma(r, fma(-x, r, 1.0), r);
+    return fma(r, fma(-x, r, 1.0), r);
+}
+
 __device__ __forceinline__ double clampd(double v, double lo, double hi) {
     return v < lo ? lo : (v > hi ? hi : v);
 }
@@ -197,7 +206,13 @@ __device__ __forceinline__ void cov3d64(const SceneK& S, int gi, double* cov3d) 
 }
 
 // RenderPassImpl::prepare for one Gaussian (splat.cpp:114-176).  Returns true when
-// the splat survives culling.
+// the splat survives culling.  EXACT: every value rounds as the reference's (the fp64
+// fix-up decides with them).  !EXACT (the preprocess): the values that only feed the
+// fp32 raster record -- the conic and coef -- come from one reciprocal of det and of
+// depth^2 instead of four correctly rounded divisions (a few fp64 ulps, far below the
+// fp32 rounding of the record); cc is not formed.  Every decision (culls, clamps, rect,
+// depth order) still uses exactly rounded values.
+template <bool EXACT = true>
 __device__ __forceinline__ bool prep64(const SceneK& S, const CamK& C, const OptK& O,
                                        const FrameK& F, int gi, Prep64& s) {
     frame_mean(S, F, gi, s.x);
@@ -248,9 +263,16 @@ __device__ __forceinline__ bool prep64(const SceneK& S, const CamK& C, const Opt
     c2[3] += O.dilation;
     const double det = c2[0] * c2[3] - c2[1] * c2[1];
     if (!(det > 0.0)) return false;
-    s.ca = c2[3] / det;
-    s.cb = -c2[1] / det;
-    s.cc = c2[0] / det;
+    if (EXACT) {
+        s.ca = c2[3] / det;
+        s.cb = -c2[1] / det;
+        s.cc = c2[0] / det;
+    } else {
+        const double idet = rcp64(det);
+        s.ca = c2[3] * idet;
+        s.cb = -c2[1] * idet;
+        s.cc = 0.0;
+    }
     s.c11 = c2[3];
     const double mid = 0.5 * (c2[0] + c2[3]);
     const double disc = mid * mid - det;
@@ -266,7 +288,7 @@ __device__ __forceinline__ bool prep64(const SceneK& S, const CamK& C, const Opt
     // view-dependent reflectivity (sh.hpp:26-50; splat.cpp:163-167)
     s.refl_raw = refl_raw64(S, C, gi, s.x, s.depth, s.view_dir);
     const double r = clampd(s.refl_raw, 0.0, 1.0);
-    s.coef = S.s_int * r / (s.depth * s.depth);
+    s.coef = EXACT ? S.s_int * r / (s.depth * s.depth) : S.s_int * r * rcp64(s.depth * s.depth);
     return true;
 }
 

@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, co
     bool vis = false;
     if (gi < S.n) {
         Prep64 s;
-        vis = prep64(S, C, O, F, gi, s);
+        vis = prep64<false>(S, C, O, F, gi, s);
         gidx[gi] = (uint32_t)gi;
         if (vis) {
             // fp32 rounding is monotone, so this 32-bit key orders like the fp64
@@ -54,8 +54,8 @@ __global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, co
                                   (uint32_t)s.y0 | ((uint32_t)s.y1 << 16));
             // factored conic (Cholesky of [[a, b], [b, c]]) in fp64, rounded once
             const double l11 = sqrt(s.ca);
-            const double l12 = s.cb / l11;
-            const double l22 = 1.0 / sqrt(s.c11);
+            const double l12 = s.cb * rcp64(l11);
+            const double l22 = rsqrt(s.c11);
             rec.A[gi] = make_float4((float)s.x0, (float)s.y0, (float)(s.mean[0] - (double)s.x0),
                                     (float)(s.mean[1] - (double)s.y0));
             rec.B[gi] = make_float4((float)l11, (float)l12, (float)l22, (float)s.opacity);
