@@ -24,7 +24,7 @@ __device__ __forceinline__ void sincos_phase32(double psi, float& sn, float& cs)
     sincosf((float)r, &sn, &cs);
 }
 
-__global__ void __launch_bounds__(256) k_preprocess(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd,
+__global__ void __launch_bounds__(256, 5) k_preprocess(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd,
                                                     uint32_t* __restrict__ depth_key,
                                                     double* __restrict__ depth64,
                                                     uint32_t* __restrict__ gidx,
