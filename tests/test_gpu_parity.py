@@ -634,4 +634,4 @@ def test_graph_replay_backward_walks_every_chunk(tsb, ctx):
         grads.append(scene.grads()["d_position"])
     assert np.abs(grads[0]).max() > 0
     for g in grads[1:]:  # equal up to the order of the float atomics
-        assert rel_err(g, grads[0], 1e-4) < GRAD_TOL
+        assert rel_err(g, grads[0], 1e-3) < GRAD_TOL
