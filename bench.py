@@ -503,7 +503,7 @@ def main():
     ap.add_argument("--no-deform", action="store_true")
     ap.add_argument("--deform-n", type=int, default=2_000_000)
     ap.add_argument("--passes", type=int, default=12, help="render passes (streams) in flight")
-    ap.add_argument("--train-passes", type=int, default=4)
+    ap.add_argument("--train-passes", type=int, default=12)
     ap.add_argument("--train-steps", type=int, default=3)
     ap.add_argument("--train-n", type=int, default=None)
     ap.add_argument("--cpu-frames", type=int, default=2)
