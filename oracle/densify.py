@@ -28,7 +28,7 @@ def quat_to_rotation(q):
 def densify(params: dict, grad_sum, count, extent, grad_threshold=5e-5, opacity_floor=5e-3,
             split_scale_fraction=0.01, split_shrink=1.6, min_count=16):
     """params: position (n,3), log_scale (n,3), rotation (n,4), opacity_logit (n,), reflectivity_dc (n,),
-    motion (k,n,3) or None (fp32).  Returns (new params dict (fp32), src list: old index or -1)."""
+    motion (k,n,3) or None, optional refl_sh (n,16) / color_sh (n,16,3) (fp32).  Returns (new params dict (fp32), src list: old index or -1)."""
     n = params["position"].shape[0]
     logit = params["opacity_logit"].astype(np.float64)
     drop = np.zeros(n, bool)
@@ -62,6 +62,9 @@ def densify(params: dict, grad_sum, count, extent, grad_threshold=5e-5, opacity_
         out[key] = params[key][order].copy()
     if params.get("motion") is not None:
         out["motion"] = params["motion"][:, order].copy()
+    for key in ("refl_sh", "color_sh"):  # per-Gaussian appearance follows its parent (trainer.cpp:429-474)
+        if params.get(key) is not None:
+            out[key] = params[key][order].copy()
     for j, (i, pos, ls) in enumerate(extras):
         if pos is not None:
             out["position"][len(keep) + j] = pos.astype(np.float32)

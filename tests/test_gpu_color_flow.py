@@ -289,3 +289,34 @@ def test_render_stack_files(tsb, ctx, tmp_path):
     rq = tsb.RenderPass(ctx).prepare(scene, cam, tsb.RenderOptions(), (0, 0.5)).forward()
     with pytest.raises(RuntimeError, match="distortion"):
         rq.write_render_stack(tmp_path / "x", 0)
+
+
+def test_densify_carries_colour_and_sh(tsb, ctx):
+    """Densification surgery (trainer.cpp:385-470) on a scene with reflectivity SH (degree 2)
+    and colour SH: every appearance coefficient follows its parent (kept, cloned, split)."""
+    from oracle import densify as odn
+    from paper_2505_05356_b200 import synthetic
+    g, sh, cs, _, _, scene, tof = _setup(tsb, ctx, 2, n=4000, seed=83)
+    cam = synthetic.camera(128, 96, 110.0)
+    rng = np.random.default_rng(84)
+    target = rng.normal(0, 0.05, (4, 96, 128)).astype(np.float32)
+    rp = tsb.RenderPass(ctx)
+    for it in range(2):
+        rp.prepare(scene, cam, tsb.RenderOptions(), (0, 0.4 * it)).forward_loss(target, sync=False)
+        rp.backward()
+        scene.adam_step(tsb.LrTable.uniform(1e-3))
+    prm = scene.get_params()
+    prm["refl_sh"] = scene.get_sh()
+    prm["color_sh"] = scene.get_color()
+    stat, count = scene.densify_stat()
+    extent = tsb.render.scene_extent(prm["position"])
+    thr = float(np.quantile(stat / count, 0.6))
+    n_new = scene.densify(extent, grad_threshold=thr, split_scale_fraction=0.02, min_count=16)
+    ref, src = odn.densify(prm, stat, count, extent, grad_threshold=thr, split_scale_fraction=0.02, min_count=16)
+    assert n_new == ref["position"].shape[0] and any(s < 0 for s in src)
+    assert np.array_equal(scene.get_color(), ref["color_sh"])
+    got_sh = scene.get_sh()
+    assert np.array_equal(got_sh[:, 1:], ref["refl_sh"][:, 1:])
+    assert np.array_equal(got_sh[:, 0], ref["reflectivity_dc"])
+    out = tsb.RenderPass(ctx).prepare(scene, cam, tsb.RenderOptions(color=True), (0, 0.5)).forward().outputs()
+    assert np.isfinite(out["color"]).all()
