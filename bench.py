@@ -15,7 +15,11 @@ workload with all host threads, one frame per step.
 """
 from __future__ import annotations
 
-import argparse
+import os as _os
+
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "16")  # before any CUDA context (see the package)
+
+import argparse  # noqa: E402
 import json
 import math
 import os
@@ -502,8 +506,8 @@ def main():
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--no-deform", action="store_true")
     ap.add_argument("--deform-n", type=int, default=2_000_000)
-    ap.add_argument("--passes", type=int, default=12, help="render passes (streams) in flight")
-    ap.add_argument("--train-passes", type=int, default=12)
+    ap.add_argument("--passes", type=int, default=24, help="render passes (streams) in flight")
+    ap.add_argument("--train-passes", type=int, default=16)
     ap.add_argument("--train-steps", type=int, default=3)
     ap.add_argument("--train-n", type=int, default=None)
     ap.add_argument("--cpu-frames", type=int, default=2)

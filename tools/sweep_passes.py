@@ -12,7 +12,7 @@ ctx = tsb.Context(0)
 scene = tsb.GaussianScene(ctx, g.n, g.n_keyframes, cfg.tof)
 scene.set_params(g.position, g.log_scale, g.rotation, g.opacity_logit, g.reflectivity_dc, g.motion)
 opts = tsb.RenderOptions()
-pool = [tsb.RenderPass(ctx) for _ in range(16)]
+pool = [tsb.RenderPass(ctx) for _ in range(32)]
 for npass in [int(a) for a in (sys.argv[1:] or ["1", "2", "3", "4", "6"])]:
     ps = pool[:npass]
     for rep in range(3):
