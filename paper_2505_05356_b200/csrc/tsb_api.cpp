@@ -161,6 +161,8 @@ struct tsb_pass {
     double* depth64 = nullptr;
     uint32_t *gidx_a = nullptr, *gidx_b = nullptr;
     uint32_t* sorted = nullptr;  // global (depth, index) order: gidx_b, or gidx_a after the exact fallback
+    uint32_t* order_dbg = nullptr;  // debug copy of the exact order (equal-key runs resolved)
+    int order_dbg_cap = 0;
     uint32_t* touched = nullptr;
     uint2* rect = nullptr;
     RecK rec{};
@@ -1116,7 +1118,7 @@ void tsb_pass_destroy(tsb_pass* p) {
     dev_free(p->vals); dev_free(p->block_done); dev_free(p->tile_blocks_done);
     dev_free(p->counters); dev_free(p->list_off); dev_free(p->fx_work_n);
     dev_free(p->loss_part); dev_free(p->bg_part); dev_free(p->loss_dev); dev_free(p->chw);
-    dev_free(p->ssim_g); dev_free(p->ssim_part);
+    dev_free(p->ssim_g); dev_free(p->ssim_part); dev_free(p->order_dbg);
     dev_free(p->ext_col); dev_free(p->ext_mf); dev_free(p->ext_mb); dev_free(p->ext_dmotion);
     dev_free(p->ext_out); dev_free(p->ext_screen); dev_free(p->ext_up); dev_free(p->ext_bg_part);
     dev_free(p->ext_dmacc); dev_free(p->ext_ftgt); dev_free(p->ext_fl_part); dev_free(p->ext_fl_res);
@@ -1251,6 +1253,16 @@ int tsb_pass_num_keys(tsb_pass* p, int64_t* out) {
 
 namespace {
 
+// Equal-key runs of the depth order are resolved where it is read (tsb_ties.cuh); after the
+// exact 64-bit fallback (sorted == gidx_a) the order has none.
+TieK tiek(tsb_pass* p) {
+    TieK t;
+    t.keys = p->sorted == p->gidx_a ? nullptr : p->key_b;
+    t.depth64 = p->depth64;
+    t.abort = p->counters + 2;
+    return t;
+}
+
 // fp64 fix-up arguments of the pass's current chunk plan.
 FixupK fixk(tsb_pass* p) {
     const int total_chunks = (int)p->chunk_seg0.size();
@@ -1261,6 +1273,7 @@ FixupK fixk(tsb_pass* p) {
     fx.binned_end_rank = total_chunks ? (p->chunk_seg0.back() + p->chunk_nseg.back()) * kSeg : 0;
     fx.vals = p->vals;
     fx.sorted_gidx = p->sorted;
+    fx.ties = tiek(p);
     fx.rect = p->rect;
     fx.n_visible = p->counters;
     fx.overflow = p->counters + 2;
@@ -1339,8 +1352,7 @@ int record_prepare(tsb_pass* p, cudaStream_t st, int* launches) {
     int l = n > 0 ? 1 : 0;
     {
         Stage sg(p->ctx, TSB_STAGE_DEPTH_SORT, st);
-        l += launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, p->depth64, p->counters, p->counters + 2,
-                               key_range, n, p->sort_scratch, st);
+        l += launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, key_range, n, p->sort_scratch, st);
     }
     TSB_CHECK_LAUNCH();
     *launches = l;
@@ -1390,6 +1402,7 @@ int record_forward(tsb_pass* p, cudaStream_t st, bool loss, const ChW& chw, bool
     FwdState fs{p->st_f, p->st_d, p->st_i, p->W * p->H};
     BinK B{};
     B.sorted_gidx = p->sorted;
+    B.ties = tiek(p);
     B.rect = p->rect;
     B.n_visible = p->counters;
     B.ts = p->opt.ts;
@@ -2127,6 +2140,25 @@ int tsb_pass_get_motion_grads(tsb_pass* p, float* d_motion_fwd, float* d_motion_
 }
 
 // ---- debug / parity ----
+namespace {
+// The exact (depth, index) order of the prepared frame on the device (runs of equal
+// compressed keys resolved as the binning resolves them).
+int order_device(tsb_pass* p, const uint32_t** out) {
+    const int n = std::max(p->scene->d.n, 1);
+    if (n > p->order_dbg_cap) {
+        dev_free(p->order_dbg);
+        p->order_dbg_cap = 0;
+        int rc;
+        if ((rc = dev_alloc(&p->order_dbg, n))) return rc;
+        p->order_dbg_cap = n;
+    }
+    launch_materialize_order(p->sorted, tiek(p), p->counters, p->scene->d.n, p->order_dbg, p->stream);
+    TSB_CHECK_LAUNCH();
+    *out = p->order_dbg;
+    return TSB_OK;
+}
+}  // namespace
+
 int tsb_pass_debug_prepared(tsb_pass* p, int32_t* gidx, int32_t* rect) {
     if (!p || !p->prepared) return fail(TSB_ERR_INVALID, "pass not prepared");
     int rc = read_visible(p);
@@ -2134,7 +2166,9 @@ int tsb_pass_debug_prepared(tsb_pass* p, int32_t* gidx, int32_t* rect) {
     cudaStream_t st = p->stream;
     const int V = p->V;
     std::vector<uint32_t> g(V > 0 ? V : 1);
-    if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), p->sorted, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, st));
+    const uint32_t* order = nullptr;
+    if ((rc = order_device(p, &order))) return rc;
+    if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), order, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, st));
     std::vector<uint2> r((size_t)std::max(p->scene->d.n, 1));
     if (rect && p->scene->d.n > 0)
         TSB_CUDA(cudaMemcpyAsync(r.data(), p->rect, sizeof(uint2) * p->scene->d.n, cudaMemcpyDeviceToHost, st));
@@ -2172,8 +2206,11 @@ int tsb_pass_debug_tiles(tsb_pass* p, int32_t* tiles_x, int32_t* tiles_y, int64_
     std::vector<uint32_t> order((size_t)std::max(p->V, 1));
     if (ids && k > 0) {
         TSB_CUDA(cudaMemcpyAsync(vals.data(), p->vals, sizeof(uint32_t) * k, cudaMemcpyDeviceToHost, st));
+        const uint32_t* od = nullptr;
+        int rc2;
+        if ((rc2 = order_device(p, &od))) return rc2;
         if (p->V > 0)
-            TSB_CUDA(cudaMemcpyAsync(order.data(), p->sorted, sizeof(uint32_t) * p->V, cudaMemcpyDeviceToHost, st));
+            TSB_CUDA(cudaMemcpyAsync(order.data(), od, sizeof(uint32_t) * p->V, cudaMemcpyDeviceToHost, st));
         TSB_CUDA(cudaStreamSynchronize(st));
     }
     // per tile: concatenation of its chunk sub-lists (values are Gaussian indices;
@@ -2208,7 +2245,12 @@ int tsb_pass_debug_records(tsb_pass* p, float* rec12) {
         TSB_CUDA(cudaMemcpyAsync(C.data(), p->rec.C, sizeof(float4) * n, cudaMemcpyDeviceToHost, st));
         if (p->nf > 1) TSB_CUDA(cudaMemcpyAsync(D.data(), p->rec.D, sizeof(float4) * n, cudaMemcpyDeviceToHost, st));
     }
-    if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), p->sorted, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, st));
+    {
+        const uint32_t* od = nullptr;
+        int rc2;
+        if ((rc2 = order_device(p, &od))) return rc2;
+        if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), od, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, st));
+    }
     TSB_CUDA(cudaStreamSynchronize(st));
     for (int r = 0; r < V; ++r) {
         const uint32_t i = g[r];
@@ -2260,7 +2302,12 @@ int tsb_pass_debug_screen_grads(tsb_pass* p, float* g8) {
     std::vector<uint32_t> g((size_t)std::max(V, 1));
     TSB_CUDA(cudaMemcpyAsync(sc.data(), p->screen_keep, sizeof(float) * 8 * (size_t)n, cudaMemcpyDeviceToHost,
                              p->stream));
-    if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), p->sorted, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, p->stream));
+    {
+        const uint32_t* od = nullptr;
+        int rc2;
+        if ((rc2 = order_device(p, &od))) return rc2;
+        if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), od, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, p->stream));
+    }
     TSB_CUDA(cudaStreamSynchronize(p->stream));
     for (int i = 0; i < V; ++i)
         for (int c = 0; c < 8; ++c) g8[8 * (size_t)i + c] = sc[(size_t)c * n + g[i]];

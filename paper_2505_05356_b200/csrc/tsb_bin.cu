@@ -24,83 +24,27 @@
 #include <algorithm>
 
 #include "tsb_internal.h"
+#include "tsb_ties.cuh"
 
 namespace tsb {
 
-constexpr int kMaxTieRun = 64;
-
-// Re-sort each run of equal fp32 keys by (fp64 depth, index) -- the reference's
-// comparator (splat.cpp:181-184).  One thread per run start; runs are short
-// (fp32 spacing ~1e-7 relative), insertion sort in local memory.
-__device__ __noinline__ void sort_run(const uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                                      const double* __restrict__ depth64, int r, int V, int32_t* long_run) {
-    const uint32_t k = keys[r];
-    int L = 2;
-    while (r + L < V && keys[r + L] == k) ++L;
-    if (L > kMaxTieRun) {
-        atomicOr(long_run, 2);  // abort the frame; the host redoes it with the exact 64-bit sort
-        return;
-    }
-    uint32_t g[kMaxTieRun];
-    double d[kMaxTieRun];
-    for (int i = 0; i < L; ++i) {
-        g[i] = vals[r + i];
-        d[i] = depth64[g[i]];
-    }
-    for (int i = 1; i < L; ++i) {
-        const uint32_t gi = g[i];
-        const double di = d[i];
-        int j = i - 1;
-        while (j >= 0 && (d[j] > di || (d[j] == di && g[j] > gi))) {
-            g[j + 1] = g[j];
-            d[j + 1] = d[j];
-            --j;
-        }
-        g[j + 1] = gi;
-        d[j + 1] = di;
-    }
-    for (int i = 0; i < L; ++i) vals[r + i] = g[i];
-}
-
-// Re-sort each run of equal fp32 keys by (fp64 depth, index) -- the reference's
-// comparator (splat.cpp:181-184).  Each thread scans 4 consecutive ranks (one
-// 16-byte load + the neighbours); run starts are rare and handled out of line.
-__global__ void k_fix_ties(const uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                           const double* __restrict__ depth64, const int32_t* __restrict__ n_visible,
-                           int32_t* __restrict__ long_run) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    const int V = *n_visible;
-    const int r0 = 4 * q;
-    if (r0 >= V - 1) return;
-    const uint4 k4 = reinterpret_cast<const uint4*>(keys)[q];
-    const uint32_t kk[6] = {r0 > 0 ? keys[r0 - 1] : ~k4.x, k4.x, k4.y, k4.z, k4.w,
-                            r0 + 4 < V ? keys[r0 + 4] : ~k4.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int r = r0 + j;
-        if (r >= V - 1) break;
-        if (!(kk[j + 2] == kk[j + 1] && kk[j] != kk[j + 1])) continue;  // not a run start
-        const bool len2 = r + 2 >= V || keys[r + 2] != kk[j + 1];
-        if (len2) {  // the common case: a compare-exchange in registers
-            const uint32_t g0 = vals[r], g1 = vals[r + 1];
-            const double d0 = depth64[g0], d1 = depth64[g1];
-            if (d0 > d1 || (d0 == d1 && g0 > g1)) {
-                vals[r] = g1;
-                vals[r + 1] = g0;
-            }
-        } else {
-            sort_run(keys, vals, depth64, r, V, long_run);
-        }
-    }
-}
-
-int launch_sort_depth(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, const double* depth64,
-                      const int32_t* n_visible, int32_t* long_run, const uint32_t* key_range, int n,
-                      uint32_t* scratch, cudaStream_t st) {
+int launch_sort_depth(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b,
+                      const uint32_t* key_range, int n, uint32_t* scratch, cudaStream_t st) {
     if (n <= 0) return 0;
-    int launches = radix_sort24(keys_a, keys_b, vals_a, vals_b, n, scratch, key_range, st);
-    k_fix_ties<<<(n / 4 + 256) / 256, 256, 0, st>>>(keys_b, vals_b, depth64, n_visible, long_run);
-    return launches + 1;
+    return radix_sort24(keys_a, keys_b, vals_a, vals_b, n, scratch, key_range, st);
+}
+
+__global__ void k_materialize_order(const uint32_t* __restrict__ sorted, TieK T, const int32_t* __restrict__ n_visible,
+                                    uint32_t* __restrict__ out) {
+    const int V = *n_visible;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < V; r += gridDim.x * blockDim.x)
+        out[r] = sorted_at(sorted, T, r, V);
+}
+
+void launch_materialize_order(const uint32_t* sorted, const TieK& T, const int32_t* n_visible, int n, uint32_t* out,
+                              cudaStream_t st) {
+    if (n <= 0) return;
+    k_materialize_order<<<std::min(148 * 8, (n + 255) / 256), 256, 0, st>>>(sorted, T, n_visible, out);
 }
 
 // Exact fallback for long equal-fp32 runs: stable LSD on the fp64 depth bits as two
@@ -167,7 +111,7 @@ __device__ __forceinline__ void load_batch_warp0(const BinK& B, int r, int V, ui
     int tx0 = 1, tx1 = 0, ty0 = 1, ty1 = 0;
     uint32_t g = 0;
     if (r < V) {
-        g = B.sorted_gidx[r];
+        g = sorted_at(B.sorted_gidx, B.ties, r, V);
         const uint2 rc = B.rect[g];
         const int x0 = rc.x & 0xffff, x1 = rc.x >> 16, y0 = rc.y & 0xffff, y1 = rc.y >> 16;
         tx0 = x0 / B.ts;
@@ -403,7 +347,7 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_emit(BinK B, int cap) {
                 cur[t] = hn[t] - ht;
                 delta[t] = B.tile_start[t] + ht;
             }
-            for (int i = tid; i < kSeg; i += kBinThreads) seg_g[i] = r0 + i < V ? B.sorted_gidx[r0 + i] : 0u;
+            for (int i = tid; i < kSeg; i += kBinThreads) seg_g[i] = r0 + i < V ? sorted_at(B.sorted_gidx, B.ties, r0 + i, V) : 0u;
             __syncthreads();
             const int per = (nt + kBinThreads - 1) / kBinThreads;
             const int t0 = tid * per, t1 = min(nt, t0 + per);
@@ -514,7 +458,7 @@ __device__ __forceinline__ void seg_masks(const BinK& B, const SegSmem& m, int r
     uint32_t g = 0;
     const int r = r0 + tid;
     if (r < V) {
-        g = B.sorted_gidx[r];
+        g = sorted_at(B.sorted_gidx, B.ties, r, V);
         const uint2 rc = B.rect[g];
         const int x0 = rc.x & 0xffff, x1 = rc.x >> 16, y0 = rc.y & 0xffff, y1 = rc.y >> 16;
         tx0 = x0 / B.ts;

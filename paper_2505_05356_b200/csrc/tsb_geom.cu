@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include "tsb_fp64.cuh"
+#include "tsb_ties.cuh"
 
 namespace tsb {
 
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, const F
             int g = 0;
             bool cov = false;
             if (r < V) {
-                g = (int)fx.sorted_gidx[r];
+                g = (int)sorted_at(fx.sorted_gidx, fx.ties, r, V);
                 const uint2 rc = fx.rect[g];
                 const int x0 = rc.x & 0xffff, x1 = rc.x >> 16, y0 = rc.y & 0xffff, y1 = rc.y >> 16;
                 cov = x0 / O.ts <= tx && tx <= (x1 - 1) / O.ts && y0 / O.ts <= ty && ty <= (y1 - 1) / O.ts;

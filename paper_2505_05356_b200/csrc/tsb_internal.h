@@ -80,11 +80,19 @@ struct RecK {
     const uint2* rect;  // alias of the pass's tile rects: (x0 | x1 << 16, y0 | y1 << 16)
 };
 
+// Equal-key runs of the depth sort, resolved by the readers of the order (tsb_ties.cuh).
+struct TieK {
+    const uint32_t* keys;    // sorted compressed depth keys; null: the order is already exact
+    const double* depth64;   // fp64 depth per Gaussian
+    int32_t* abort;          // frame abort word (bit 1: a run longer than kMaxTieRun)
+};
+
 // Depth-chunked binning (tsb_bin.cu).  Ranks are cut into segments of kSeg
 // (one warp each); chunk c covers segments [seg0, seg0 + nseg).
 constexpr int kSeg = 128;
 struct BinK {
     const uint32_t* sorted_gidx;
+    TieK ties;
     const uint2* rect;
     const int32_t* n_visible;
     int ts, tiles_x, tiles_y, ntiles;
@@ -189,6 +197,7 @@ struct FixupK {
     int binned_end_rank;      // first rank after the last binned chunk
     const uint32_t* vals;
     const uint32_t* sorted_gidx;
+    TieK ties;
     const uint2* rect;
     const int32_t* n_visible;
     const int32_t* overflow;
@@ -212,12 +221,13 @@ int radix_sort32(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t*
 // (range[0] = min, range[1] = max); result in (keys_b, vals_b).
 int radix_sort24(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch,
                  const uint32_t* range, cudaStream_t st);
-// Global (depth, index) order: stable sort on fp32 depth keys, then exact fp64
-// re-sort of equal-key runs (runs longer than 64 set bit 1 of *abort; the host then
-// runs launch_sort_depth64 and redoes the frame).
-int launch_sort_depth(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, const double* depth64,
-                      const int32_t* n_visible, int32_t* long_run, const uint32_t* key_range, int n,
-                      uint32_t* scratch, cudaStream_t st);  // result in (keys_b, vals_b)
+// Global (depth, index) order: stable sort on compressed fp32 depth keys; runs of equal
+// keys are ordered by the fp64 depth where the order is read (sorted_at, tsb_ties.cuh).
+int launch_sort_depth(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b,
+                      const uint32_t* key_range, int n, uint32_t* scratch, cudaStream_t st);  // -> (keys_b, vals_b)
+// out[r] = Gaussian at rank r of the exact order, r < *n_visible (debug / parity copies)
+void launch_materialize_order(const uint32_t* sorted, const TieK& T, const int32_t* n_visible, int n, uint32_t* out,
+                              cudaStream_t st);
 int launch_sort_depth64(const double* depth64, const uint32_t* touched, uint32_t* keys_a, uint32_t* keys_b,
                         uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch, cudaStream_t st);
 void bin_init();  // kernel attributes; call before any capture
