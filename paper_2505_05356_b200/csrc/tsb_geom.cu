@@ -385,9 +385,9 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, const F
 void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd, const FixupK& fx,
                   const PixK& px, int nf, cudaStream_t st) {
     cudaMemsetAsync(fx.work_n, 0, sizeof(int), st);
-    k_fixup_mark<<<148 * 2, 128, 0, st>>>(O, fx, px, C.W, fd);
-    k_fixup_records<<<148 * 4, 128, 0, st>>>(S, C, O, fd, fx);
-    k_fixup<<<148 * 4, 128, 0, st>>>(S, C, O, fd, fx, px, nf);
+    k_fixup_mark<<<148, 128, 0, st>>>(O, fx, px, C.W, fd);
+    k_fixup_records<<<148, 128, 0, st>>>(S, C, O, fd, fx);
+    k_fixup<<<148, 128, 0, st>>>(S, C, O, fd, fx, px, nf);
 }
 
 // Intermediates the chain needs, recomputed in fp64 with reciprocals instead of
