@@ -15,7 +15,7 @@ namespace tsb {
 
 constexpr int kMaxTieRun = 8;
 
-static __device__ __noinline__ uint32_t sorted_in_run(const uint32_t* __restrict__ sorted, const TieK& T, int r, int V,
+static __device__ __forceinline__ uint32_t sorted_in_run(const uint32_t* __restrict__ sorted, const TieK& T, int r, int V,
                                                uint32_t k) {
     int s = r;
     while (s > 0 && T.keys[s - 1] == k && r - s < kMaxTieRun) --s;
