@@ -38,7 +38,9 @@ struct Smem {
 // (outputs, fix-up flag, loss epilogue) in the launch in which it terminates,
 // or in the last chunk.  Blocks whose pixels are all done mark themselves so
 // later chunks neither bin nor raster them.
-template <int NF, bool DIST>
+// WORK: count evaluations / contributions (profiling runs only; a template so the
+// per-evaluation counter costs nothing otherwise).
+template <int NF, bool DIST, bool WORK>
 __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK ck, const uint32_t* __restrict__ vals,
                                                                 OptK O, int W, int H, PixK px, FwdState fs,
                                                                 const FrameDev* __restrict__ fd, int loss, ChW chw,
@@ -93,6 +95,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
     int processed = (int)(rg.z + rg.y);
     const float cut2 = O.cut2_f, thr = O.alpha_thr_f, fl = O.floor_f;
     const float coarseM = kCoarseMaha * cut2, coarseA = kCoarseAlpha * thr;
+    const float outside = cut2 + coarseM;  // maha above this is outside, with no ambiguity to check
     const uint32_t end = rg.x + rg.y;
 
     if (__syncthreads_count(done) < kRasterThreads) {
@@ -109,12 +112,12 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
             if (!done) {
                 const int nb = min((uint32_t)kRasterThreads, end - b);
                 for (int j = 0; j < nb; ++j) {
-                    if (ck.work) ++n_eval;
+                    if (WORK) ++n_eval;
                     const float4 A = sm.A[j], B = sm.B[j];
                     Eval ev;
                     eval_entry(A, B, pcx, pcy, ev);
+                    if (ev.maha > outside) continue;  // clearly outside (most entries)
                     const float dm = ev.maha - cut2;
-                    if (dm > coarseM) continue;  // clearly outside (most entries)
                     if (dm >= -coarseM) {
                         if (fabsf(dm) <= 2.f * maha_err_bound(A, B, ev)) flag |= 1;
                         if (dm > 0.f) continue;
@@ -235,7 +238,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
         fs.i[2 * (size_t)fs.npx + o] = last_eff;
     }
     const bool block_finished = __syncthreads_count(done || is_last) == kRasterThreads;
-    if (ck.work) {
+    if (WORK) {
         unsigned long long ev = n_eval, cn = (uint32_t)nc - nc0;
         for (int m = 16; m > 0; m >>= 1) {
             ev += __shfl_xor_sync(0xffffffffu, ev, m);
@@ -518,9 +521,15 @@ void launch_raster_fwd(const RecK& rec, const ChunkK& ck, const uint32_t* tile_v
                        int nf, PixK px, FwdState fs, const FrameDev* fd, bool loss, const ChW& ch_w,
                        double* loss_part, cudaStream_t st) {
     const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
-#define TSB_FWD(NF_, D_) \
-    k_raster_fwd<NF_, D_><<<grid, kRasterThreads, 0, st>>>(rec, ck, tile_vals, O, W, H, px, fs, fd, loss ? 1 : 0, ch_w, \
-                                                           loss_part)
+#define TSB_FWD(NF_, D_)                                                                                        \
+    do {                                                                                                       \
+        if (ck.work)                                                                                           \
+            k_raster_fwd<NF_, D_, true><<<grid, kRasterThreads, 0, st>>>(rec, ck, tile_vals, O, W, H, px, fs, fd, \
+                                                                          loss ? 1 : 0, ch_w, loss_part);       \
+        else                                                                                                   \
+            k_raster_fwd<NF_, D_, false><<<grid, kRasterThreads, 0, st>>>(rec, ck, tile_vals, O, W, H, px, fs,    \
+                                                                           fd, loss ? 1 : 0, ch_w, loss_part);  \
+    } while (0)
     if (nf > 1) {
         if (O.dist) TSB_FWD(2, true); else TSB_FWD(2, false);
     } else {
