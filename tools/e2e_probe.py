@@ -4,6 +4,8 @@ import sys
 import time
 sys.path.insert(0, '.')
 import numpy as np
+import os
+UPLOAD = os.environ.get('UPLOAD', '1') == '1'
 import torch
 import paper_2505_05356_b200 as tsb
 from paper_2505_05356_b200 import synthetic
@@ -25,7 +27,7 @@ for npass in [int(a) for a in (sys.argv[1:] or ["8", "12", "16"])]:
             for _ in passes]
 
     def e2e_step():
-        scene.set_params(host["position"], host["log_scale"], host["rotation"], host["opacity_logit"],
+        if UPLOAD: scene.set_params(host["position"], host["log_scale"], host["rotation"], host["opacity_logit"],
                          host["reflectivity_dc"], host["motion"])
         for i, fr in enumerate(cfg.frames):
             j = i % npass
