@@ -193,7 +193,15 @@ struct tsb_pass {
     float* st_f = nullptr;
     int32_t* st_i = nullptr;
     // misc
-    int32_t* counters = nullptr;  // [0] n_visible, [1] n_flagged, [2] overflow, [3] blocks done, [4] long tie run
+    int32_t* counters = nullptr;  // [0] n_visible, [1] n_flagged, [2] abort word, [3] blocks done, [4] prefix end
+    // Nearest-prefix depth order (tsb_sort.cu): a frame sorts only its nearest kcap
+    // Gaussians; one that runs past them is redone with the full order and the pass's
+    // cap grows (x4, then the full sort).
+    int kcap = 0;               // prefix cap of the next frames (0: full sort)
+    bool prefix = false;        // the prepared frame's order is only a prefix
+    int32_t* n_bin = nullptr;   // end of the sorted order: counters + 4 (prefix) or counters
+    uint32_t *sel_keys = nullptr, *sel_vals = nullptr, *sel_scratch = nullptr;
+    int sel_cap = 0;
     uint32_t* list_off = nullptr;
     double* loss_part = nullptr;
     double* bg_part = nullptr;
@@ -249,6 +257,7 @@ struct tsb_pass {
 
 namespace {
 constexpr size_t kFrameSlot = 3072;  // FrameDev staging offset in tsb_pass::pinned
+constexpr int kPrefixCap0 = 65536;  // initial nearest-prefix cap of the depth order (16 sort tiles)
 }
 
 extern "C" {
@@ -901,6 +910,12 @@ int tsb_pass_create(tsb_ctx* ctx, tsb_pass** out) {
         tsb_pass_destroy(p);
         return rc;
     }
+    p->n_bin = p->counters;
+    static const int prefix_cap = [] {
+        const char* e = std::getenv("TSB_PREFIX");  // initial prefix cap; 0 disables
+        return e ? std::max(0, std::atoi(e)) : kPrefixCap0;
+    }();
+    p->kcap = prefix_cap;
     bin_init();
     ssim_init();
     ctx->passes.push_back(p);
@@ -1117,6 +1132,7 @@ void tsb_pass_destroy(tsb_pass* p) {
     dev_free(p->hist); dev_free(p->tile_len); dev_free(p->tile_start); dev_free(p->ranges_all); dev_free(p->chunk_rank0);
     dev_free(p->vals); dev_free(p->block_done); dev_free(p->tile_blocks_done);
     dev_free(p->counters); dev_free(p->list_off); dev_free(p->fx_work_n);
+    dev_free(p->sel_keys); dev_free(p->sel_vals); dev_free(p->sel_scratch);
     dev_free(p->loss_part); dev_free(p->bg_part); dev_free(p->loss_dev); dev_free(p->chw);
     dev_free(p->ssim_g); dev_free(p->ssim_part); dev_free(p->order_dbg);
     dev_free(p->ext_col); dev_free(p->ext_mf); dev_free(p->ext_mb); dev_free(p->ext_dmotion);
@@ -1224,6 +1240,20 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     slot->pad = 0;
     p->prep_deferred = true;
     p->sorted = p->gidx_b;  // launch_sort_depth's result buffer
+    {
+        const int n = p->scene->d.n;
+        p->prefix = !(p->channels & TSB_CH_FULL_LISTS) && p->kcap > 0 && n > p->kcap;
+        if (p->prefix && p->kcap > p->sel_cap) {
+            dev_free(p->sel_keys); dev_free(p->sel_vals); dev_free(p->sel_scratch);
+            p->sel_cap = 0;
+            int rc1;
+            if ((rc1 = dev_alloc(&p->sel_keys, p->kcap)) || (rc1 = dev_alloc(&p->sel_vals, p->kcap)) ||
+                (rc1 = dev_alloc(&p->sel_scratch, prefix_sort_scratch_words(p->kcap))))
+                return rc1;
+            p->sel_cap = p->kcap;
+        }
+        p->n_bin = p->prefix ? p->counters + 4 : p->counters;
+    }
     p->V = -1;
     p->nchunks = 0;
     p->prepared = true;
@@ -1275,7 +1305,8 @@ FixupK fixk(tsb_pass* p) {
     fx.sorted_gidx = p->sorted;
     fx.ties = tiek(p);
     fx.rect = p->rect;
-    fx.n_visible = p->counters;
+    fx.n_visible = p->n_bin;
+    fx.n_all = p->counters;
     fx.overflow = p->counters + 2;
     fx.stamp = p->fx_stamp;
     fx.work = p->fx_work;
@@ -1352,7 +1383,12 @@ int record_prepare(tsb_pass* p, cudaStream_t st, int* launches) {
     int l = n > 0 ? 1 : 0;
     {
         Stage sg(p->ctx, TSB_STAGE_DEPTH_SORT, st);
-        l += launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, key_range, n, p->sort_scratch, st);
+        if (p->prefix)
+            l += radix_sort24_prefix(p->key_a, p->key_b, p->gidx_b, p->sel_keys, p->sel_vals, n, p->kcap,
+                                     p->sort_scratch, p->sel_scratch, key_range, p->counters, p->counters + 4,
+                                     p->counters + 2, st);
+        else
+            l += launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, key_range, n, p->sort_scratch, st);
     }
     TSB_CHECK_LAUNCH();
     *launches = l;
@@ -1404,7 +1440,7 @@ int record_forward(tsb_pass* p, cudaStream_t st, bool loss, const ChW& chw, bool
     B.sorted_gidx = p->sorted;
     B.ties = tiek(p);
     B.rect = p->rect;
-    B.n_visible = p->counters;
+    B.n_visible = p->n_bin;
     B.ts = p->opt.ts;
     B.tiles_x = p->opt.tiles_x;
     B.tiles_y = p->opt.tiles_y;
@@ -1435,7 +1471,8 @@ int record_forward(tsb_pass* p, cudaStream_t st, bool loss, const ChW& chw, bool
         ck.ranges = B.ranges;
         ck.first = c == 0;
         ck.chunk_end_rank = (seg0 + nseg) * kSeg;
-        ck.n_visible = p->counters;
+        ck.n_visible = p->n_bin;
+        ck.n_all = p->counters;
         ck.block_done = p->block_done;
         ck.tile_blocks_done = p->tile_blocks_done;
         ck.blocks_done_total = p->counters + 3;
@@ -1557,10 +1594,11 @@ std::string forward_key(tsb_pass* p, bool loss, const ChW& chw) {
     add(p->pend_chw_full, sizeof p->pend_chw_full);
     const void* sptrs[] = {p->ssim_g, p->ssim_part};
     add(sptrs, sizeof sptrs);
-    const void* prep_ptrs[] = {p->key_a, p->key_b, p->depth64, p->gidx_a, p->gidx_b, p->touched, p->sort_scratch};
+    const void* prep_ptrs[] = {p->key_a, p->key_b, p->depth64, p->gidx_a, p->gidx_b, p->touched, p->sort_scratch,
+                               p->n_bin, p->sel_keys, p->sel_vals, p->sel_scratch};
     add(prep_ptrs, sizeof prep_ptrs);
     const int ints[] = {p->W, p->H, p->nf, (int)p->channels, p->ntiles, p->nblocks, (int)p->vals_cap, loss ? 1 : 0,
-                        p->ctx->profiling ? 1 : 0, p->prep_deferred ? 1 : 0};
+                        p->ctx->profiling ? 1 : 0, p->prep_deferred ? 1 : 0, p->prefix ? p->kcap : 0};
     add(ints, sizeof ints);
     add(p->chunk_seg0.data(), sizeof(int) * p->chunk_seg0.size());
     add(p->chunk_nseg.data(), sizeof(int) * p->chunk_nseg.size());
@@ -1668,7 +1706,19 @@ int settle(tsb_pass* p) {
         if (attempt >= 8) return fail(TSB_ERR_NOMEM, "render: tile-list storage kept overflowing");
         p->ctx->redos++;
         cudaStream_t st = p->stream;
-        if (ab & 2) {  // an equal-fp32-key run too long for k_fix_ties: exact 64-bit sort
+        if (ab & 8) {  // the prefix order ran out before every pixel terminated: the full order
+            const int n = p->scene->d.n;
+            p->kcap = (int64_t)p->kcap * 4 >= n ? 0 : p->kcap * 4;  // later frames: a longer prefix
+            p->prefix = false;
+            p->n_bin = p->counters;
+            if (!(ab & 2)) {
+                p->ctx->launches += launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b,
+                                                      reinterpret_cast<uint32_t*>(p->counters + 5), n,
+                                                      p->sort_scratch, st);
+                p->sorted = p->gidx_b;
+            }
+        }
+        if (ab & 2) {  // an equal-key run too long to resolve on read: exact 64-bit sort
             p->ctx->launches += launch_sort_depth64(p->depth64, p->touched, p->key_a, p->key_b, p->gidx_a, p->gidx_b,
                                                     p->scene->d.n, p->sort_scratch, st);
             p->sorted = p->gidx_a;
@@ -2151,6 +2201,13 @@ int order_device(tsb_pass* p, const uint32_t** out) {
         int rc;
         if ((rc = dev_alloc(&p->order_dbg, n))) return rc;
         p->order_dbg_cap = n;
+    }
+    if (p->prefix) {  // the frame sorted only its nearest prefix: the whole order now (raw keys are intact)
+        p->ctx->launches += launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b,
+                                              reinterpret_cast<uint32_t*>(p->counters + 5), p->scene->d.n,
+                                              p->sort_scratch, p->stream);
+        p->prefix = false;
+        p->n_bin = p->counters;
     }
     launch_materialize_order(p->sorted, tiek(p), p->counters, p->scene->d.n, p->order_dbg, p->stream);
     TSB_CHECK_LAUNCH();

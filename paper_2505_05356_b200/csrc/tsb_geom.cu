@@ -350,6 +350,8 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, const F
             fixup_batch(S, C, O, F, fx, stamp, nf, x, y, cov, g, a.processed + __popc(cm & lanes_below), slot, a, lane);
             if (!a.done) a.processed += __popc(cm);
         }
+        // the prefix order ended with the pixel alive: the frame is redone with the full order
+        if (!a.done && lane == 0 && V < *fx.n_all) atomicOr(fx.overflow, 8);
         if (lane == 0) {
             const size_t o = (size_t)y * W + x;
             #pragma unroll

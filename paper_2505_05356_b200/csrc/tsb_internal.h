@@ -108,7 +108,7 @@ struct BinK {
     uint32_t* vals;                   // list storage (Gaussian indices)
     uint32_t* list_off;               // device running offset into vals
     uint32_t capacity;
-    int32_t* overflow;                // abort word: bit 0 list overflow, bit 1 long tie run
+    int32_t* overflow;                // abort word: bit 0 list overflow, bit 1 long tie run, bit 3 prefix short
     int nblocks;                      // raster blocks of the frame
     const int32_t* blocks_done_total; // raster blocks finished so far
 };
@@ -126,11 +126,12 @@ struct ChunkK {
     const uint4* ranges;  // this chunk's per-tile ranges
     int first;            // chunk 0: initialise state
     int chunk_end_rank;   // last chunk when >= n_visible
-    const int32_t* n_visible;
+    const int32_t* n_visible;   // end of the sorted order (the prefix end under the prefix sort)
+    const int32_t* n_all;       // visible Gaussians
     int32_t* block_done;        // per raster block
     int32_t* tile_blocks_done;  // per tile
     int32_t* blocks_done_total;
-    const int32_t* overflow;    // list storage overflowed: the host re-runs the frame
+    int32_t* overflow;          // abort word (list overflow, ...): the host re-runs the frame
     unsigned long long* work;   // profiling: [0] evaluations, [1] contributions (null: not counted)
 };
 
@@ -199,8 +200,9 @@ struct FixupK {
     const uint32_t* sorted_gidx;
     TieK ties;
     const uint2* rect;
-    const int32_t* n_visible;
-    const int32_t* overflow;
+    const int32_t* n_visible;  // end of the sorted order (prefix end under the prefix sort)
+    const int32_t* n_all;      // visible Gaussians
+    int32_t* overflow;
     int* stamp;        // [n] frame stamp of the cached record (FrameDev::stamp)
     int* work;         // [n] Gaussians queued for the record cache
     int* work_n;
@@ -221,6 +223,13 @@ int radix_sort32(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t*
 // (range[0] = min, range[1] = max); result in (keys_b, vals_b).
 int radix_sort24(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch,
                  const uint32_t* range, cudaStream_t st);
+// Nearest-prefix order (tsb_sort.cu): sorts only ranks [0, *n_bin) of the order,
+// n_bin <= cap, into (keys_out, vals_out); keys stay intact; raises abort bit 3 when
+// even the nearest top digit exceeds cap.
+size_t prefix_sort_scratch_words(int cap);
+int radix_sort24_prefix(const uint32_t* keys, uint32_t* keys_out, uint32_t* vals_out, uint32_t* tmp_keys,
+                        uint32_t* tmp_vals, int n, int cap, uint32_t* scratch, uint32_t* ps, const uint32_t* range,
+                        const int32_t* n_visible, int32_t* n_bin, int32_t* abort_word, cudaStream_t st);
 // Global (depth, index) order: stable sort on compressed fp32 depth keys; runs of equal
 // keys are ordered by the fp64 depth where the order is read (sorted_at, tsb_ties.cuh).
 int launch_sort_depth(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b,

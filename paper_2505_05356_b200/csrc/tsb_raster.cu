@@ -171,6 +171,8 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
 
     const bool is_last = ck.chunk_end_rank >= *ck.n_visible;
     const bool finalize = !was_done && (done || is_last);
+    // the prefix order ended with the pixel alive: the frame is redone with the full order
+    if (finalize && !done && *ck.n_all > *ck.n_visible) atomicOr(ck.overflow, 8);
     float lpx = 0.f;
     if (finalize) {
         const float T2 = T * T;

@@ -142,7 +142,8 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(const uint32_t* __
                                                            uint32_t* __restrict__ vals_out, int n, int shift,
                                                            const uint32_t* __restrict__ digit_off,
                                                            uint32_t* status, uint32_t* tile_ticket,
-                                                           const uint32_t* __restrict__ range) {
+                                                           const uint32_t* __restrict__ range,
+                                                           const int32_t* __restrict__ n_dev) {
     __shared__ uint32_t s_tile;
     __shared__ uint32_t warp_cnt[kSortWarps][256];  // counts, then exclusive offsets across warps
     __shared__ uint32_t block_start[256];            // exclusive scan over digits of the tile counts
@@ -156,6 +157,10 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(const uint32_t* __
     __syncthreads();
     const int tile = (int)s_tile;
     const int base = tile * kSortTile;
+    if (n_dev) {  // element count known on the device only: tiles past it have nothing to do
+        n = *n_dev;
+        if (base >= n) return;
+    }
 
     // load warp-striped: slot i of lane l is item (warp*32*IPT + i*32 + l) of the tile
     uint32_t k[kSortIPT], v[kSortIPT], lr[kSortIPT];
@@ -283,11 +288,11 @@ int radix_sort24(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t*
     k_sort_hist<<<hgrid, kSortThreads, 0, st>>>(keys_a, n, hist, status, 3 * 256 * tiles, range);
     k_sort_scan<<<1, 96, 0, st>>>(hist);
     // 3 passes ping-pong a->b->a->b; finish in b, then the caller uses b
-    k_onesweep<<<tiles, kSortThreads, 0, st>>>(keys_a, vals_a, keys_b, vals_b, n, 0, hist, status, tickets, range);
+    k_onesweep<<<tiles, kSortThreads, 0, st>>>(keys_a, vals_a, keys_b, vals_b, n, 0, hist, status, tickets, range, nullptr);
     k_onesweep<<<tiles, kSortThreads, 0, st>>>(keys_b, vals_b, keys_a, vals_a, n, 8, hist + 256,
-                                               status + (size_t)256 * tiles, tickets + 1, nullptr);
+                                               status + (size_t)256 * tiles, tickets + 1, nullptr, nullptr);
     k_onesweep<<<tiles, kSortThreads, 0, st>>>(keys_a, vals_a, keys_b, vals_b, n, 16, hist + 512,
-                                               status + (size_t)512 * tiles, tickets + 2, nullptr);
+                                               status + (size_t)512 * tiles, tickets + 2, nullptr, nullptr);
     return 5;
 }
 
@@ -323,11 +328,156 @@ int radix_sort32(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t*
     uint32_t *ki = keys_a, *ko = keys_b, *vi = vals_a, *vo = vals_b;
     for (int p = 0; p < 4; ++p) {
         k_onesweep<<<tiles, kSortThreads, 0, st>>>(ki, vi, ko, vo, n, 8 * p, hist + 256 * p,
-                                                   status + (size_t)p * 256 * tiles, tickets + p, nullptr);
+                                                   status + (size_t)p * 256 * tiles, tickets + p, nullptr, nullptr);
         uint32_t* t = ki; ki = ko; ko = t;
         t = vi; vi = vo; vo = t;
     }
     return 6;
+}
+
+// ---- Nearest-prefix depth order ----
+// A frame reads the order only up to the rank where its last tile terminates; on
+// dense scenes that is a few thousand of a million ranks.  The prefix sort orders
+// only the Gaussians whose top key digit is at most b*, the largest digit whose
+// cumulative visible count fits in `cap`: those are exactly ranks [0, n_bin) of the
+// full order (equal compressed keys share their top digit, so no run is split).
+// The readers treat n_bin as the end of the order; a pixel still alive there while
+// n_bin < n_visible raises bit 3 of the abort word and the host redoes the frame
+// with the full sort (the raw keys are left intact for that).
+//
+//   k_sort_hist       (shared with the full sort) digit histograms of all keys
+//   k_prefix_select   one warp: b*, n_bin, the selection's top-digit histogram
+//   k_prefix_compact  gathers the selection (warp-aggregated slots) + its low-digit
+//                     histograms; clears the look-back status of the 3 passes
+//   k_sort_scan, 3 x k_onesweep over the selection (count read on the device)
+namespace {
+constexpr int kPrefHistC = 0, kPrefTickets = 768, kPrefSel = 772, kPrefCount = 773, kPrefStatus = 776;
+}
+
+__global__ void k_prefix_select(const uint32_t* __restrict__ hist, int n, int cap,
+                                const int32_t* __restrict__ n_visible, uint32_t* __restrict__ ps,
+                                int32_t* __restrict__ n_bin, int32_t* __restrict__ abort_word) {
+    const int lane = threadIdx.x;
+    const int V = *n_visible;
+    uint32_t v[8], s = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int b = lane * 8 + j;
+        v[j] = hist[512 + b] - (b == 255 ? (uint32_t)(n - V) : 0u);  // culled keys sit in digit 255
+        s += v[j];
+    }
+    uint32_t inc = s;
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += u;
+    }
+    // digits whose inclusive cumulative count fits in cap (a prefix of the digits)
+    uint32_t run = inc - s;
+    int fit = 0;
+    uint32_t fit_cum = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        run += v[j];
+        if (run <= (uint32_t)cap) {
+            ++fit;
+            fit_cum = run;
+        }
+    }
+    int nfit = fit;
+    for (int d = 16; d; d >>= 1) nfit += __shfl_xor_sync(0xffffffffu, nfit, d);
+    uint32_t nb = fit_cum;  // the largest fitting cumulative count (lanes' values are monotone)
+    for (int d = 16; d; d >>= 1) nb = max(nb, __shfl_xor_sync(0xffffffffu, nb, d));
+    if (nfit == 0) nb = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int b = lane * 8 + j;
+        ps[kPrefHistC + b] = 0u;
+        ps[kPrefHistC + 256 + b] = 0u;
+        ps[kPrefHistC + 512 + b] = b < nfit ? v[j] : 0u;
+    }
+    if (lane < 4) ps[kPrefTickets + lane] = 0u;
+    if (lane == 0) {
+        ps[kPrefSel] = (uint32_t)nfit;  // selected: top digit < nfit
+        ps[kPrefCount] = 0u;
+        *n_bin = (int32_t)nb;
+        if (nb == 0 && V > 0) atomicOr(abort_word, 8);  // the nearest digit alone exceeds cap
+    }
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_prefix_compact(const uint32_t* __restrict__ keys, int n,
+                                                                 const uint32_t* __restrict__ range,
+                                                                 uint32_t* __restrict__ ps, int status_words,
+                                                                 uint32_t* __restrict__ sel_keys,
+                                                                 uint32_t* __restrict__ sel_vals) {
+    uint32_t kmin, kshift;
+    key_xform(range, kmin, kshift);
+    for (int i = blockIdx.x * kSortThreads + threadIdx.x; i < status_words; i += gridDim.x * kSortThreads)
+        ps[kPrefStatus + i] = 0u;
+    const uint32_t nsel = ps[kPrefSel];
+    uint32_t* hist = ps + kPrefHistC;
+    uint32_t* count = ps + kPrefCount;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const int n4 = (n + 3) >> 2;
+    const bool aligned_tail = (n & 3) == 0;
+    const uint4* k4 = reinterpret_cast<const uint4*>(keys);
+    for (int i = blockIdx.x * kSortThreads + threadIdx.x; i - (int)threadIdx.x < n4; i += gridDim.x * kSortThreads) {
+        uint32_t kk[4];
+        if (i < n4 && (aligned_tail || i + 1 < n4)) {
+            const uint4 q = k4[i];
+            kk[0] = q.x; kk[1] = q.y; kk[2] = q.z; kk[3] = q.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) kk[j] = i < n4 && 4 * i + j < n ? keys[4 * i + j] : 0xffffffffu;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t c = key24(kk[j], kmin, kshift);
+            const bool pick = kk[j] != 0xffffffffu && (c >> 16) < nsel;
+            const unsigned m = __ballot_sync(0xffffffffu, pick);
+            if (!m) continue;
+            const int leader = __ffs(m) - 1;
+            uint32_t base = 0;
+            if (lane == leader) base = atomicAdd(count, (uint32_t)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (pick) {
+                const uint32_t slot = base + (uint32_t)__popc(m & lt_mask);
+                sel_keys[slot] = kk[j];
+                sel_vals[slot] = (uint32_t)(4 * i + j);
+                atomicAdd(&hist[c & 255u], 1u);
+                atomicAdd(&hist[256 + ((c >> 8) & 255u)], 1u);
+            }
+        }
+    }
+}
+
+size_t prefix_sort_scratch_words(int cap) {
+    const int tiles = (cap + kSortTile - 1) / kSortTile;
+    return (size_t)kPrefStatus + (size_t)3 * 256 * tiles;
+}
+
+int radix_sort24_prefix(const uint32_t* keys, uint32_t* keys_out, uint32_t* vals_out, uint32_t* tmp_keys,
+                        uint32_t* tmp_vals, int n, int cap, uint32_t* scratch, uint32_t* ps, const uint32_t* range,
+                        const int32_t* n_visible, int32_t* n_bin, int32_t* abort_word, cudaStream_t st) {
+    if (n <= 0) return 0;
+    const int ctiles = (cap + kSortTile - 1) / kSortTile;
+    uint32_t* hist = scratch;
+    cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 3 * 256, st);
+    const int hgrid = max(1, min(148 * 2, (n / 4 + kSortThreads - 1) / kSortThreads));
+    k_sort_hist<<<hgrid, kSortThreads, 0, st>>>(keys, n, hist, nullptr, 0, range);
+    k_prefix_select<<<1, 32, 0, st>>>(hist, n, cap, n_visible, ps, n_bin, abort_word);
+    k_prefix_compact<<<hgrid, kSortThreads, 0, st>>>(keys, n, range, ps, 3 * 256 * ctiles, tmp_keys, tmp_vals);
+    uint32_t* hc = ps + kPrefHistC;
+    uint32_t* tk = ps + kPrefTickets;
+    uint32_t* status = ps + kPrefStatus;
+    k_sort_scan<<<1, 96, 0, st>>>(hc);
+    k_onesweep<<<ctiles, kSortThreads, 0, st>>>(tmp_keys, tmp_vals, keys_out, vals_out, cap, 0, hc, status, tk, range,
+                                                n_bin);
+    k_onesweep<<<ctiles, kSortThreads, 0, st>>>(keys_out, vals_out, tmp_keys, tmp_vals, cap, 8, hc + 256,
+                                                status + (size_t)256 * ctiles, tk + 1, nullptr, n_bin);
+    k_onesweep<<<ctiles, kSortThreads, 0, st>>>(tmp_keys, tmp_vals, keys_out, vals_out, cap, 16, hc + 512,
+                                                status + (size_t)512 * ctiles, tk + 2, nullptr, n_bin);
+    return 7;
 }
 
 }  // namespace tsb

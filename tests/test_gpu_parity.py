@@ -5,6 +5,7 @@ tile ranges, per-pixel contributor counts); floating point within the tolerances
 of BASELINE.json's north_star: rendered raw samples 1e-4 relative, gradients
 1e-3 relative (floors as in SURVEY.md App. D)."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -523,6 +524,8 @@ def test_list_overflow_abort_and_redo(tsb, ctx):
 
     r0 = ctx.redo_count()
     a, ga, ka = run(None)
+    if "TSB_PREFIX" in os.environ:  # a forced short depth-order prefix redoes frames too
+        pytest.skip("redo accounting with a forced prefix cap")
     assert ctx.redo_count() == r0
     b, gb, kb = run(64)
     assert ctx.redo_count() == r0 + 1, "the overflowed frame was not redone"

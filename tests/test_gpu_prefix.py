@@ -1,0 +1,67 @@
+"""Nearest-prefix depth order (tsb_sort.cu).
+
+A frame sorts only the Gaussians of its nearest top key digits (at most the pass's
+cap); the readers treat the prefix end as the end of the order, and a pixel still
+alive there aborts the frame, which is redone with the full order.  These tests
+check that the prefix frame is the full-order frame bit for bit, and re-run the
+whole GPU suite with a 256-Gaussian cap so every parity test also goes through the
+prefix + abort + full-order redo path."""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.fixture(scope="module")
+def tsb():
+    import paper_2505_05356_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(tsb):
+    return tsb.Context(0)
+
+
+@pytest.mark.skipif("TSB_PREFIX" in os.environ, reason="runs with the default cap only")
+def test_prefix_frame_equals_full_order_frame(tsb, ctx):
+    """c3 at full size: 1M Gaussians, every tile terminates within the nearest 64K ranks,
+    so the default pass sorts only a prefix; outputs, lists and gradients equal those of a
+    full-lists pass (which always sorts everything)."""
+    from paper_2505_05356_b200 import synthetic
+    from helpers import gpu_scene, rel_err
+    cfg = synthetic.config("c3")
+    frame = cfg.frames[17]
+    scene = gpu_scene(tsb, ctx, cfg.scene, cfg.tof)
+    target = np.zeros((4, cfg.camera.height, cfg.camera.width), np.float32)
+    res = {}
+    for full in (False, True):
+        r0 = ctx.redo_count()
+        opts = tsb.RenderOptions(counts=True, full_lists=full)
+        rp = tsb.RenderPass(ctx).prepare(scene, cfg.camera, opts, frame)
+        rp.forward_loss(target, [0.25] * 4)
+        rp.backward()
+        res[full] = (rp.outputs(), scene.grads(), ctx.redo_count() - r0, rp.visible_count())
+        scene.zero_grads()
+    (a, ga, ra, va), (b, gb, rb, vb) = res[False], res[True]
+    assert ra == 0, "c3 frame ran past the default prefix (redone)"
+    assert va == vb
+    for k in ("quad", "depth_raw", "weight", "transmittance", "n_contrib", "n_processed"):
+        assert np.array_equal(a[k], b[k], equal_nan=True), k
+    for k in ga:  # accumulated with atomics: equal up to summation order
+        assert rel_err(np.asarray(ga[k]), np.asarray(gb[k]), 1e-3) < 1e-4, k
+
+
+@pytest.mark.skipif("TSB_PREFIX" in os.environ, reason="already inside the forced-prefix run")
+def test_gpu_suite_with_forced_prefix():
+    env = dict(os.environ, TSB_PREFIX="256")
+    r = subprocess.run([sys.executable, "-m", "pytest", str(ROOT / "tests"), "-m", "gpu", "-x", "-q",
+                        "-p", "no:cacheprovider"], cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
