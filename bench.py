@@ -163,8 +163,11 @@ class StreamTimer:
 # events the library records on the pass stream around each stage (profiling
 # mode: the same kernels, issued eagerly), over the same c3 frames.
 #   k_preprocess (HBM): per Gaussian 120 B read (pos_op 16, 2 keyframe offsets 32,
-#     cov3d cache 48, opacity cache 8, scale_amp 16) + 12 B written (index, fp32 key,
-#     tiles touched); per visible Gaussian 64 B written (fp64 depth 8, rect 8, record 48).
+#     cov3d cache 48, opacity cache 8, scale_amp 16) + 8 B written (fp32 key, tiles
+#     touched).  Frames that sort only their nearest prefix (the default, TSB_PREFIX != 0)
+#     run the lean variant: that is all; the records of the prefix are written after the
+#     sort (k_records).  The full variant also writes per Gaussian the index (4 B) and per
+#     visible Gaussian 64 B (fp64 depth 8, rect 8, record 48).
 #   k_raster_fwd (FP32): 9 FLOP per (pixel, entry) evaluation (dx, dy, p, q, maha,
 #     threshold) + 14 FLOP per contributing evaluation (alpha, w, w2, quad pair, SW, SD,
 #     T) -- counted live by the kernel in profiling mode.
@@ -189,7 +192,8 @@ def rooflines(stage_ms, shapes, evals, contribs, peaks, sm_max_mhz):
     ms, calls = stage_ms.get("preprocess", (0.0, 0))
     if calls:
         per = ms / calls
-        b = shapes["n"] * 132 + shapes["v"] * 64
+        lean = os.environ.get("TSB_PREFIX", "1") != "0"
+        b = shapes["n"] * 128 if lean else shapes["n"] * 132 + shapes["v"] * 64
         ach = b / (per * 1e-3) / 1e9
         t = traffic.get("k_preprocess")
         out["k_preprocess"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -369,11 +373,13 @@ def bench_train_c4(args, dist, tsb, synthetic, ctx):
     timer = StreamTimer(ctx)
     dist.barrier()
     ctx.synchronize()
+    redo0 = ctx.redo_count()
     timer.start()
     for _ in range(args.train_steps):
         it()
     ctx.join()
     ms = timer.stop_ms()
+    train_redos = ctx.redo_count() - redo0
     ctx.synchronize()
     # per-stage times: one more iteration with stage events
     ctx.stage_times()
@@ -388,6 +394,7 @@ def bench_train_c4(args, dist, tsb, synthetic, ctx):
            "ms_per_iter": round(ms_max / args.train_steps, 3),
            "stage_ms_per_iter": {k: round(v[0], 3) for k, v in st.items() if v[1]},
            "keys_per_frame_last": trainer.rp.num_keys(), "passes_in_flight": len(trainer.passes),
+           "redone_frames_timed": train_redos,
            "path": "parallel.FrameShardedTrainer (public API)"}
     if comm:
         comm.close()

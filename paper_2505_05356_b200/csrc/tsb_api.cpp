@@ -257,7 +257,7 @@ struct tsb_pass {
 
 namespace {
 constexpr size_t kFrameSlot = 3072;  // FrameDev staging offset in tsb_pass::pinned
-constexpr int kPrefixCap0 = 65536;  // initial nearest-prefix cap of the depth order (16 sort tiles)
+constexpr int kPrefixCap0 = 16384;  // initial nearest-prefix cap of the depth order (4 sort tiles)
 }
 
 extern "C" {
@@ -1378,16 +1378,19 @@ int record_prepare(tsb_pass* p, cudaStream_t st, int* launches) {
     {
         Stage sg(p->ctx, TSB_STAGE_PREPROCESS, st);
         launch_preprocess(scenek(p->scene), p->cam, p->opt, p->frame_dev, p->key_a, p->depth64, p->gidx_a, p->touched,
-                          p->rect, p->rec, p->counters, key_range, st);
+                          p->rect, p->rec, p->counters, key_range, p->prefix, st);
     }
     int l = n > 0 ? 1 : 0;
     {
         Stage sg(p->ctx, TSB_STAGE_DEPTH_SORT, st);
-        if (p->prefix)
+        if (p->prefix) {
             l += radix_sort24_prefix(p->key_a, p->key_b, p->gidx_b, p->sel_keys, p->sel_vals, n, p->kcap,
                                      p->sort_scratch, p->sel_scratch, key_range, p->counters, p->counters + 4,
                                      p->counters + 2, st);
-        else
+            // records of the prefix (the lean preprocess wrote keys only)
+            l += launch_records(scenek(p->scene), p->cam, p->opt, p->frame_dev, p->gidx_b, p->counters + 4,
+                                p->kcap, p->key_a, p->depth64, p->gidx_a, p->rect, p->rec, st);
+        } else
             l += launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, key_range, n, p->sort_scratch, st);
     }
     TSB_CHECK_LAUNCH();
@@ -1692,6 +1695,26 @@ int enqueue_backward(tsb_pass* p, const UpK& up);
 // redone with more list storage / the exact 64-bit depth sort, including its
 // loss and backward.  Its inputs are still intact: everything that changes the
 // scene settles all passes first.
+// A prefix-sorted frame's full order, for a redo or a debug read: records of every
+// visible Gaussian (the lean preprocess skipped them) and the full depth sort
+// (exact64: the exact 64-bit sort instead).  The raw keys are intact.
+void full_order(tsb_pass* p, bool exact64, cudaStream_t st) {
+    const int n = p->scene->d.n;
+    p->ctx->launches += launch_records(scenek(p->scene), p->cam, p->opt, p->frame_dev, nullptr, nullptr, n, p->key_a,
+                                       p->depth64, p->gidx_a, p->rect, p->rec, st);
+    if (exact64) {
+        p->ctx->launches += launch_sort_depth64(p->depth64, p->touched, p->key_a, p->key_b, p->gidx_a, p->gidx_b, n,
+                                                p->sort_scratch, st);
+        p->sorted = p->gidx_a;
+    } else {
+        p->ctx->launches += launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b,
+                                              reinterpret_cast<uint32_t*>(p->counters + 5), n, p->sort_scratch, st);
+        p->sorted = p->gidx_b;
+    }
+    p->prefix = false;
+    p->n_bin = p->counters;
+}
+
 int settle(tsb_pass* p) {
     for (int attempt = 0; p->pending; ++attempt) {
         TSB_CUDA(cudaSetDevice(p->ctx->device));
@@ -1706,19 +1729,13 @@ int settle(tsb_pass* p) {
         if (attempt >= 8) return fail(TSB_ERR_NOMEM, "render: tile-list storage kept overflowing");
         p->ctx->redos++;
         cudaStream_t st = p->stream;
-        if (ab & 8) {  // the prefix order ran out before every pixel terminated: the full order
-            const int n = p->scene->d.n;
-            p->kcap = (int64_t)p->kcap * 4 >= n ? 0 : p->kcap * 4;  // later frames: a longer prefix
-            p->prefix = false;
-            p->n_bin = p->counters;
-            if (!(ab & 2)) {
-                p->ctx->launches += launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b,
-                                                      reinterpret_cast<uint32_t*>(p->counters + 5), n,
-                                                      p->sort_scratch, st);
-                p->sorted = p->gidx_b;
+        if (p->prefix && (ab & (8 | 2))) {  // the full order (+ the records the lean preprocess skipped)
+            if (ab & 8) {  // the prefix ran out before every pixel terminated: later frames sort a longer one
+                const int n = p->scene->d.n;
+                p->kcap = (int64_t)p->kcap * 4 >= n ? 0 : p->kcap * 4;
             }
-        }
-        if (ab & 2) {  // an equal-key run too long to resolve on read: exact 64-bit sort
+            full_order(p, (ab & 2) != 0, st);
+        } else if (ab & 2) {  // an equal-key run too long to resolve on read: exact 64-bit sort
             p->ctx->launches += launch_sort_depth64(p->depth64, p->touched, p->key_a, p->key_b, p->gidx_a, p->gidx_b,
                                                     p->scene->d.n, p->sort_scratch, st);
             p->sorted = p->gidx_a;
@@ -2202,13 +2219,7 @@ int order_device(tsb_pass* p, const uint32_t** out) {
         if ((rc = dev_alloc(&p->order_dbg, n))) return rc;
         p->order_dbg_cap = n;
     }
-    if (p->prefix) {  // the frame sorted only its nearest prefix: the whole order now (raw keys are intact)
-        p->ctx->launches += launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b,
-                                              reinterpret_cast<uint32_t*>(p->counters + 5), p->scene->d.n,
-                                              p->sort_scratch, p->stream);
-        p->prefix = false;
-        p->n_bin = p->counters;
-    }
+    if (p->prefix) full_order(p, false, p->stream);  // the frame sorted only its nearest prefix
     launch_materialize_order(p->sorted, tiek(p), p->counters, p->scene->d.n, p->order_dbg, p->stream);
     TSB_CHECK_LAUNCH();
     *out = p->order_dbg;

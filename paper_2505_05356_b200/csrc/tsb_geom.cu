@@ -25,6 +25,32 @@ __device__ __forceinline__ void sincos_phase32(double psi, float& sn, float& cs)
     sincosf((float)r, &sn, &cs);
 }
 
+// The per-Gaussian values the binning / raster / tie resolution read: fp64 depth,
+// tile rect and the fp32 raster record.
+__device__ __forceinline__ void write_records(const SceneK& S, const Prep64& s, int gi, double* __restrict__ depth64,
+                                              uint2* __restrict__ rect, const RecK& rec) {
+    depth64[gi] = s.depth;
+    rect[gi] = make_uint2((uint32_t)s.x0 | ((uint32_t)s.x1 << 16), (uint32_t)s.y0 | ((uint32_t)s.y1 << 16));
+    // factored conic (Cholesky of [[a, b], [b, c]]) in fp64, rounded once
+    const double l11 = sqrt(s.ca);
+    const double l12 = s.cb * rcp64(l11);
+    const double l22 = rsqrt(s.c11);
+    rec.A[gi] = make_float4((float)s.x0, (float)s.y0, (float)(s.mean[0] - (double)s.x0),
+                            (float)(s.mean[1] - (double)s.y0));
+    rec.B[gi] = make_float4((float)l11, (float)l12, (float)l22, (float)s.opacity);
+    float sn, cs;
+    sincos_phase32(phase_of_depth(s.depth, S.freq[0], S.c), sn, cs);
+    rec.C[gi] = make_float4((float)s.coef, (float)s.depth, sn, cs);
+    if (S.nf > 1) {
+        sincos_phase32(phase_of_depth(s.depth, S.freq[1], S.c), sn, cs);
+        rec.D[gi] = make_float4(sn, cs, 0.f, 0.f);
+    }
+}
+
+// LEAN (prefix-sorted frames): only the sort key, tiles touched and the visible
+// count / key range; the records of the Gaussians the frame reads -- its sorted
+// prefix -- are written after the sort by k_records.
+template <bool LEAN>
 __global__ void __launch_bounds__(256, 5) k_preprocess(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd,
                                                     uint32_t* __restrict__ depth_key,
                                                     double* __restrict__ depth64,
@@ -40,33 +66,17 @@ __global__ void __launch_bounds__(256, 5) k_preprocess(SceneK S, CamK C, OptK O,
     if (gi < S.n) {
         Prep64 s;
         vis = prep64<false>(S, C, O, F, gi, s);
-        gidx[gi] = (uint32_t)gi;
+        if (!LEAN) gidx[gi] = (uint32_t)gi;
         if (vis) {
             // fp32 rounding is monotone, so this 32-bit key orders like the fp64
-            // depth except inside runs of equal keys (resolved by k_fix_ties).
+            // depth except inside runs of equal keys (resolved where read, tsb_ties.cuh).
             depth_key[gi] = __float_as_uint((float)s.depth);
-            depth64[gi] = s.depth;
             kmine = kmaxe = depth_key[gi];
             const int ts = O.ts;
             const int tx0 = s.x0 / ts, tx1 = (s.x1 - 1) / ts;
             const int ty0 = s.y0 / ts, ty1 = (s.y1 - 1) / ts;
             touched[gi] = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
-            rect[gi] = make_uint2((uint32_t)s.x0 | ((uint32_t)s.x1 << 16),
-                                  (uint32_t)s.y0 | ((uint32_t)s.y1 << 16));
-            // factored conic (Cholesky of [[a, b], [b, c]]) in fp64, rounded once
-            const double l11 = sqrt(s.ca);
-            const double l12 = s.cb * rcp64(l11);
-            const double l22 = rsqrt(s.c11);
-            rec.A[gi] = make_float4((float)s.x0, (float)s.y0, (float)(s.mean[0] - (double)s.x0),
-                                    (float)(s.mean[1] - (double)s.y0));
-            rec.B[gi] = make_float4((float)l11, (float)l12, (float)l22, (float)s.opacity);
-            float sn, cs;
-            sincos_phase32(phase_of_depth(s.depth, S.freq[0], S.c), sn, cs);
-            rec.C[gi] = make_float4((float)s.coef, (float)s.depth, sn, cs);
-            if (S.nf > 1) {
-                sincos_phase32(phase_of_depth(s.depth, S.freq[1], S.c), sn, cs);
-                rec.D[gi] = make_float4(sn, cs, 0.f, 0.f);
-            }
+            if (!LEAN) write_records(S, s, gi, depth64, rect, rec);
         } else {
             depth_key[gi] = 0xffffffffu;
             touched[gi] = 0u;
@@ -125,11 +135,44 @@ void launch_param_cache(const SceneK& S, double* cov6, double* opac, cudaStream_
 
 void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* F,
                        uint32_t* depth_key, double* depth64, uint32_t* gidx, uint32_t* touched, uint2* rect,
-                       RecK rec, int32_t* n_visible, uint32_t* key_range, cudaStream_t st) {
+                       RecK rec, int32_t* n_visible, uint32_t* key_range, bool lean, cudaStream_t st) {
     if (S.n <= 0) return;
     const int bs = 256;
-    k_preprocess<<<(S.n + bs - 1) / bs, bs, 0, st>>>(S, C, O, F, depth_key, depth64, gidx, touched, rect, rec,
-                                                      n_visible, key_range);
+    if (lean)
+        k_preprocess<true><<<(S.n + bs - 1) / bs, bs, 0, st>>>(S, C, O, F, depth_key, depth64, gidx, touched, rect,
+                                                               rec, n_visible, key_range);
+    else
+        k_preprocess<false><<<(S.n + bs - 1) / bs, bs, 0, st>>>(S, C, O, F, depth_key, depth64, gidx, touched, rect,
+                                                                rec, n_visible, key_range);
+}
+
+// Records of a lean-preprocessed frame: the Gaussians list[0, *count) (its sorted
+// prefix), or with list == null every visible Gaussian (then also the identity
+// order the full sort starts from).  Same prep64 on the same inputs as k_preprocess.
+__global__ void __launch_bounds__(256, 5) k_records(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd,
+                                                 const uint32_t* __restrict__ list, const int32_t* __restrict__ count,
+                                                 int n, const uint32_t* __restrict__ depth_key,
+                                                 double* __restrict__ depth64, uint32_t* __restrict__ gidx,
+                                                 uint2* __restrict__ rect, RecK rec) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (list ? *count : n)) return;
+    const int gi = list ? (int)list[i] : i;
+    if (!list) {
+        gidx[gi] = (uint32_t)gi;
+        if (depth_key[gi] == 0xffffffffu) return;
+    }
+    const FrameK F = fd->F;
+    Prep64 s;
+    prep64<false>(S, C, O, F, gi, s);
+    write_records(S, s, gi, depth64, rect, rec);
+}
+
+int launch_records(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* F, const uint32_t* list,
+                   const int32_t* count, int n, const uint32_t* depth_key, double* depth64, uint32_t* gidx,
+                   uint2* rect, RecK rec, cudaStream_t st) {
+    if (n <= 0) return 0;
+    k_records<<<(n + 255) / 256, 256, 0, st>>>(S, C, O, F, list, count, n, depth_key, depth64, gidx, rect, rec);
+    return 1;
 }
 
 // ---------------------------------------------------------------------------

@@ -183,7 +183,12 @@ constexpr int kStatBg = 0, kStatLoss = 12, kStatBgColor = 13, kStats = 16;
 // tsb_geom.cu (fp64, compiled without FMA contraction)
 void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* F,
                        uint32_t* depth_key, double* depth64, uint32_t* gidx, uint32_t* touched, uint2* rect,
-                       RecK rec, int32_t* n_visible, uint32_t* key_range, cudaStream_t st);
+                       RecK rec, int32_t* n_visible, uint32_t* key_range, bool lean, cudaStream_t st);
+// depth64 / rect / raster records of list[0, *count) (a lean frame's sorted prefix), or of
+// every visible Gaussian plus the identity order when list is null.  Returns launches.
+int launch_records(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* F, const uint32_t* list,
+                   const int32_t* count, int n, const uint32_t* depth_key, double* depth64, uint32_t* gidx,
+                   uint2* rect, RecK rec, cudaStream_t st);
 // fp64 record cache for the fix-up (valid when stamp[g] == frame stamp).
 struct Rec64 {
     double4 m0;  // mean x, mean y, conic a, conic b

@@ -416,7 +416,9 @@ __global__ void __launch_bounds__(kSortThreads) k_prefix_compact(const uint32_t*
     const uint32_t nsel = ps[kPrefSel];
     uint32_t* hist = ps + kPrefHistC;
     uint32_t* count = ps + kPrefCount;
-    const int lane = threadIdx.x & 31;
+    __shared__ uint32_t s_wcnt[kSortWarps];
+    __shared__ uint32_t s_base;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int n4 = (n + 3) >> 2;
     const bool aligned_tail = (n & 3) == 0;
@@ -430,23 +432,41 @@ __global__ void __launch_bounds__(kSortThreads) k_prefix_compact(const uint32_t*
 #pragma unroll
             for (int j = 0; j < 4; ++j) kk[j] = i < n4 && 4 * i + j < n ? keys[4 * i + j] : 0xffffffffu;
         }
+        uint32_t c[4];
+        unsigned m[4];
+        uint32_t wtot = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const uint32_t c = key24(kk[j], kmin, kshift);
-            const bool pick = kk[j] != 0xffffffffu && (c >> 16) < nsel;
-            const unsigned m = __ballot_sync(0xffffffffu, pick);
-            if (!m) continue;
-            const int leader = __ffs(m) - 1;
-            uint32_t base = 0;
-            if (lane == leader) base = atomicAdd(count, (uint32_t)__popc(m));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (pick) {
-                const uint32_t slot = base + (uint32_t)__popc(m & lt_mask);
-                sel_keys[slot] = kk[j];
-                sel_vals[slot] = (uint32_t)(4 * i + j);
-                atomicAdd(&hist[c & 255u], 1u);
-                atomicAdd(&hist[256 + ((c >> 8) & 255u)], 1u);
+            c[j] = key24(kk[j], kmin, kshift);
+            m[j] = __ballot_sync(0xffffffffu, kk[j] != 0xffffffffu && (c[j] >> 16) < nsel);
+            wtot += (uint32_t)__popc(m[j]);
+        }
+        // one global slot reservation per block and iteration (a single counter word
+        // cannot take one atomic per warp at this rate)
+        if (lane == 0) s_wcnt[warp] = wtot;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t t = 0;
+            for (int w = 0; w < kSortWarps; ++w) {
+                const uint32_t v = s_wcnt[w];
+                s_wcnt[w] = t;
+                t += v;
             }
+            s_base = t ? atomicAdd(count, t) : 0u;
+        }
+        __syncthreads();
+        uint32_t slot = s_base + s_wcnt[warp];
+        __syncthreads();  // s_wcnt / s_base are rewritten by the next iteration
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if ((m[j] >> lane) & 1u) {
+                const uint32_t sl = slot + (uint32_t)__popc(m[j] & lt_mask);
+                sel_keys[sl] = kk[j];
+                sel_vals[sl] = (uint32_t)(4 * i + j);
+                atomicAdd(&hist[c[j] & 255u], 1u);
+                atomicAdd(&hist[256 + ((c[j] >> 8) & 255u)], 1u);
+            }
+            slot += (uint32_t)__popc(m[j]);
         }
     }
 }
