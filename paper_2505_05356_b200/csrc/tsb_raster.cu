@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
     const float pcx = (float)(tid % kTile) + 0.5f, pcy = (float)(tid / kTile) + 0.5f;
     const size_t HW = (size_t)W * H, o = active ? (size_t)y * W + x : 0;
 
-    float T = 1.f, Tpre = 1.f, SW = 0.f, SD = 0.f, errT = 0.f;
+    float T = 1.f, Tpre = 1.f, SW = 0.f, SD = 0.f, dT = 0.f;  // dT: absolute error bound of T
     float accS[NF], accC[NF];
 #pragma unroll
     for (int f = 0; f < NF; ++f) accS[f] = accC[f] = 0.f;
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
         Tpre = fs.f[1 * (size_t)fs.npx + o];
         SW = fs.f[2 * (size_t)fs.npx + o];
         SD = fs.f[3 * (size_t)fs.npx + o];
-        errT = fs.f[4 * (size_t)fs.npx + o];
+        dT = fs.f[4 * (size_t)fs.npx + o];
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
             accS[f] = fs.f[(5 + 2 * f) * (size_t)fs.npx + o];
@@ -96,6 +96,8 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
     const float cut2 = O.cut2_f, thr = O.alpha_thr_f, fl = O.floor_f;
     const float coarseM = kCoarseMaha * cut2, coarseA = kCoarseAlpha * thr;
     const float outside = cut2 + coarseM;  // maha above this is outside, with no ambiguity to check
+    // common-path tests with one compare each; the exact windows are re-tested inside
+    const float m_lo = cut2 - 2.f * coarseM, a_hi = thr + 2.f * coarseA;
     const uint32_t end = rg.x + rg.y;
 
     if (__syncthreads_count(done) < kRasterThreads) {
@@ -117,19 +119,21 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
                     Eval ev;
                     eval_entry(A, B, pcx, pcy, ev);
                     if (ev.maha > outside) continue;  // clearly outside (most entries)
-                    const float dm = ev.maha - cut2;
-                    if (dm >= -coarseM) {
-                        if (fabsf(dm) <= 2.f * maha_err_bound(A, B, ev)) flag |= 1;
+                    if (ev.maha >= m_lo) {
+                        const float dm = ev.maha - cut2;
+                        if (dm >= -coarseM && fabsf(dm) <= 2.f * maha_err_bound(A, B, ev)) flag |= 1;
                         if (dm > 0.f) continue;
                     }
                     eval_alpha(B, ev);
-                    const float da = ev.alpha - thr;
-                    if (fabsf(da) <= coarseA) {
-                        const float rel = 3.f * kEps + kEx2Err + 0.5f * maha_err_bound(A, B, ev) +
-                                          kEps * ev.maha;
-                        if (fabsf(da) <= 2.f * ev.alpha * rel) flag |= 2;
+                    if (ev.alpha <= a_hi) {
+                        const float da = ev.alpha - thr;
+                        if (fabsf(da) <= coarseA) {
+                            const float rel = 3.f * kEps + kEx2Err + 0.5f * maha_err_bound(A, B, ev) +
+                                              kEps * ev.maha;
+                            if (fabsf(da) <= 2.f * ev.alpha * rel) flag |= 2;
+                        }
+                        if (da < 0.f) continue;
                     }
-                    if (da < 0.f) continue;
                     ++nc;
                     const float4 Cc = sm.C[j];
                     const float w = ev.alpha * T;
@@ -153,15 +157,23 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
                     Tpre = T;
                     const float om = 1.f - ev.alpha;
                     T = T * om;
-                    // relative error of (1 - alpha) from alpha's error, plus the product rounding
-                    errT += (4.f * kEps + kEx2Err + 2.f * kEps * ev.maha) * (ev.alpha * rcp_approx(om)) + 2.f * kEps;
-                    if (fabsf(T - fl) < 2.f * fl * errT) flag |= 4;
-                    const int gidx_e = (int)(rg.z + (b - rg.x) + j + 1);
-                    if (T == 0.f && last_eff < 0) last_eff = gidx_e;
-                    if (T < fl) {
-                        processed = gidx_e;
-                        done = true;
-                        break;
+                    // Absolute error bound of T: T_k * sum_k [rel err of (1 - alpha_k) + product
+                    // rounding] = dT_{k-1} (1 - alpha_k) + (4 eps + ex2 err + 2 eps maha_k) w_k
+                    // + 2 eps T_k -- the relative bound times T, without a division.
+                    dT = fmaf(dT, om, fmaf(w, fmaf(2.f * kEps, ev.maha, 4.f * kEps + kEx2Err), 2.f * kEps * T));
+                    if (T < fmaf(2.f, dT, fl)) {  // near or below the floor (rare)
+                        if (T > fl) {
+                            flag |= 4;  // above, within the band: T - fl < 2 dT, and dT >= fl * rel err
+                        } else {
+                            if (fl - T < 2.f * fl * __fdividef(dT, T)) flag |= 4;  // |T - fl| < 2 fl rel err
+                            const int gidx_e = (int)(rg.z + (b - rg.x) + j + 1);
+                            if (T == 0.f && last_eff < 0) last_eff = gidx_e;
+                            if (T < fl) {
+                                processed = gidx_e;
+                                done = true;
+                                break;
+                            }
+                        }
                     }
                 }
             }
@@ -224,7 +236,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
         fs.f[1 * (size_t)fs.npx + o] = Tpre;
         fs.f[2 * (size_t)fs.npx + o] = SW;
         fs.f[3 * (size_t)fs.npx + o] = SD;
-        fs.f[4 * (size_t)fs.npx + o] = errT;
+        fs.f[4 * (size_t)fs.npx + o] = dT;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
             fs.f[(5 + 2 * f) * (size_t)fs.npx + o] = accS[f];
