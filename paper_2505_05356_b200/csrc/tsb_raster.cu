@@ -30,7 +30,26 @@ struct Smem {
     float4 B[kRasterThreads];
     float4 C[kRasterThreads];
     float4 D[NF > 1 ? kRasterThreads : 1];
+    uint8_t wmask[kRasterThreads];                      // per staged entry: warps it can reach
+    uint8_t list[kRasterThreads / 32][kRasterThreads];  // per warp: its entries, in list order
 };
+
+// Warps of a 16 x 16 block (warp w: block rows 2w, 2w + 1) with a pixel centre that
+// can lie inside the entry's maha <= `outside` ellipse.  Bounding box of the ellipse
+// from the factored conic (half-widths sqrt(M Sigma_xx), sqrt(M Sigma_yy), Sigma = (L^T
+// L)^-1), widened by 1 % and 0.01 px: every pixel outside it evaluates maha > outside
+// in fp32 -- the entry's `continue` -- so skipping the entry for that warp changes
+// nothing.  Degenerate records reach every warp.
+__device__ __forceinline__ uint32_t warps_reached(const float4& a, const float4& b, float outside) {
+    const float s = sqrtf(outside) * 1.01f;
+    const float hy = __fdividef(s, fabsf(b.z)) + 0.01f;
+    const float hx = __fdividef(s * sqrtf(fmaf(b.y, b.y, b.z * b.z)), fabsf(b.x * b.z)) + 0.01f;
+    if (!(hx <= 1e30f && hy <= 1e30f)) return 0xffu;
+    if (a.x + hx < 0.5f || a.x - hx > (float)kTile - 0.5f) return 0u;
+    const int k0 = max((int)ceilf(a.y - hy - 0.5f), 0), k1 = min((int)floorf(a.y + hy - 0.5f), kTile - 1);
+    if (k0 > k1) return 0u;
+    return ((2u << (k1 >> 1)) - 1u) & ~((1u << (k0 >> 1)) - 1u);
+}
 
 // ---------------------------------------------------------------------------
 // Forward composite of one depth chunk.  Per-pixel state (T, accumulators,
@@ -105,15 +124,30 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
             const uint32_t e = b + tid;
             if (e < end) {
                 const uint32_t r = vals[e];
-                sm.A[tid] = stage_A(rec.A[r], ox, oy);
-                sm.B[tid] = rec.B[r];
+                const float4 a = stage_A(rec.A[r], ox, oy), bb = rec.B[r];
+                sm.A[tid] = a;
+                sm.B[tid] = bb;
                 sm.C[tid] = rec.C[r];
                 if (NF > 1) sm.D[tid] = rec.D[r];
+                sm.wmask[tid] = (uint8_t)warps_reached(a, bb, outside);
             }
             __syncthreads();
+            const int nb = min((uint32_t)kRasterThreads, end - b);
+            int cnt = 0;
+            if (__any_sync(0xffffffffu, !done)) {  // this warp's entries, in order
+                const int lane = tid & 31, warp = tid >> 5;
+                for (int c = 0; c < nb; c += 32) {
+                    const bool t = c + lane < nb && ((sm.wmask[c + lane] >> warp) & 1u);
+                    const unsigned bal = __ballot_sync(0xffffffffu, t);
+                    if (t) sm.list[warp][cnt + __popc(bal & ((1u << lane) - 1u))] = (uint8_t)(c + lane);
+                    cnt += __popc(bal);
+                }
+                __syncwarp();
+            }
             if (!done) {
-                const int nb = min((uint32_t)kRasterThreads, end - b);
-                for (int j = 0; j < nb; ++j) {
+                const uint8_t* wl = sm.list[tid >> 5];
+                for (int k = 0; k < cnt; ++k) {
+                    const int j = wl[k];
                     if (WORK) ++n_eval;
                     const float4 A = sm.A[j], B = sm.B[j];
                     Eval ev;
