@@ -468,16 +468,20 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
             if (tid < nb) {
                 const uint32_t r = vals[b + tid];
                 srank[tid] = r;
-                sm.A[tid] = stage_A(rec.A[r], ox, oy);
-                sm.B[tid] = rec.B[r];
+                const float4 a = stage_A(rec.A[r], ox, oy), bb = rec.B[r];
+                sm.A[tid] = a;
+                sm.B[tid] = bb;
                 sm.C[tid] = rec.C[r];
                 if (NF > 1) sm.D[tid] = rec.D[r];
+                sm.wmask[tid] = (uint8_t)warps_reached(a, bb, cut2);
             }
             __syncthreads();
             // entries at or past this warp's furthest termination point cannot contribute
             // to any of its pixels: start the warp below them (warp-uniform)
             const int jtop = min(nb, wmax - ((int)rg.z + bi * kRasterThreads));
+            const uint32_t wbit = 1u << (tid >> 5);
             for (int j = jtop - 1; j >= 0; --j) {
+                if (!(sm.wmask[j] & wbit)) continue;  // outside for every pixel of the warp
                 const int el = (int)rg.z + bi * kRasterThreads + j;
                 bool contrib = false;
                 float g8[8];
