@@ -47,6 +47,79 @@ __device__ __forceinline__ void write_records(const SceneK& S, const Prep64& s, 
     }
 }
 
+// Visibility and fp64 depth of one Gaussian for a lean frame (below), without the fp64
+// EWA projection.  The depth (sort key) and the near / opacity culls are computed with
+// the same expressions as prep64, so they are bit-identical.  The rect only decides
+// visibility here: with a = mean - r, b = mean + r, the clamped rect of prep64 is
+// non-empty iff b > -1 and a < W (per axis) and det > 0.  The projected covariance runs
+// in fp32 next to a bound of its magnitudes (|M| |Sigma| |M|^T); a decision within 1e-4
+// of those magnitudes of its threshold (fp32 errors are ~1e-6 of them) is left to the
+// exact fp64 prep64.  The discriminant uses the cancellation-free form
+// ((c0 - c3) / 2)^2 + c1^2 (equal to mid^2 - det).  Returns 0 culled, 1 visible,
+// 2 undecided.
+__device__ __forceinline__ int lean_visible(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F, int gi,
+                                            double& depth) {
+    double x[3];
+    frame_mean(S, F, gi, x);
+    const double* R = C.R;
+    double p[3];
+    for (int i = 0; i < 3; ++i) p[i] = R[i * 3 + 0] * x[0] + R[i * 3 + 1] * x[1] + R[i * 3 + 2] * x[2] + C.t[i];
+    if (p[2] < C.near_plane) return 0;
+    depth = sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
+    const double op = S.opac ? S.opac[gi] : opacity64(S, gi);
+    if (op < O.alpha_thr) return 0;
+    if (!S.cov6) return 2;
+    const double iz = rcp64(p[2]);
+    const float mx = (float)(C.fx * p[0] * iz + C.cx), my = (float)(C.fy * p[1] * iz + C.cy);
+    const float limx = (float)C.lim_x, limy = (float)C.lim_y;
+    const float txz = fminf(fmaxf((float)(p[0] * iz), -limx), limx);  // clamped tx / z
+    const float tyz = fminf(fmaxf((float)(p[1] * iz), -limy), limy);
+    const float fxz = (float)(C.fx * iz), fyz = (float)(C.fy * iz);
+    // M = J W (2 x 3), J = [[fx/z, 0, -fx tx/z^2], [0, fy/z, -fy ty/z^2]]
+    float M[6], Ma[6];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const float r0 = (float)R[0 * 3 + j], r1 = (float)R[1 * 3 + j], r2 = (float)R[2 * 3 + j];
+        M[j] = fxz * (r0 - txz * r2);
+        M[3 + j] = fyz * (r1 - tyz * r2);
+        Ma[j] = fabsf(fxz) * (fabsf(r0) + fabsf(txz * r2));
+        Ma[3 + j] = fabsf(fyz) * (fabsf(r1) + fabsf(tyz * r2));
+    }
+    const size_t n = (size_t)S.n;
+    const float c00 = (float)S.cov6[gi], c01 = (float)S.cov6[n + gi], c02 = (float)S.cov6[2 * n + gi];
+    const float c11 = (float)S.cov6[3 * n + gi], c12 = (float)S.cov6[4 * n + gi], c22 = (float)S.cov6[5 * n + gi];
+    const float V[9] = {c00, c01, c02, c01, c11, c12, c02, c12, c22};
+    float T[6], Ta[6];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            T[i * 3 + j] = M[i * 3 + 0] * V[j] + M[i * 3 + 1] * V[3 + j] + M[i * 3 + 2] * V[6 + j];
+            Ta[i * 3 + j] = Ma[i * 3 + 0] * fabsf(V[j]) + Ma[i * 3 + 1] * fabsf(V[3 + j]) + Ma[i * 3 + 2] * fabsf(V[6 + j]);
+        }
+    const float dil = (float)O.dilation;
+    const float a0 = T[0] * M[0] + T[1] * M[1] + T[2] * M[2] + dil;
+    const float a1 = T[0] * M[3] + T[1] * M[4] + T[2] * M[5];
+    const float a3 = T[3] * M[3] + T[4] * M[4] + T[5] * M[5] + dil;
+    const float b0 = Ta[0] * Ma[0] + Ta[1] * Ma[1] + Ta[2] * Ma[2] + fabsf(dil);
+    const float b1 = Ta[0] * Ma[3] + Ta[1] * Ma[4] + Ta[2] * Ma[5];
+    const float b3 = Ta[3] * Ma[3] + Ta[4] * Ma[4] + Ta[5] * Ma[5] + fabsf(dil);
+    const float det = a0 * a3 - a1 * a1;
+    const float dtol = 1e-4f * (b0 * b3 + b1 * b1);
+    if (!(fabsf(det) > dtol)) return 2;  // also NaN
+    if (det < 0.f) return 0;
+    const float h = 0.5f * (a0 - a3);
+    const float disc = h * h + a1 * a1;
+    const float lam = 0.5f * (a0 + a3) + sqrtf(fmaxf(disc, 0.1f));
+    const float r = (float)O.sigma_cutoff * sqrtf(lam);
+    const float tol = 1e-4f * (r * fmaxf(1.f, (b0 + b3) / lam) + fabsf(mx) + fabsf(my) + 1.f);
+    if (!(tol < 1e8f)) return 2;  // huge or non-finite: prep64 (x86 int conversion semantics)
+    const float bx = mx + r + 1.f, ax = (float)C.W - (mx - r);
+    const float by = my + r + 1.f, ay = (float)C.H - (my - r);
+    if (fabsf(bx) <= tol || fabsf(ax) <= tol || fabsf(by) <= tol || fabsf(ay) <= tol) return 2;
+    return (bx > 0.f && ax > 0.f && by > 0.f && ay > 0.f) ? 1 : 0;
+}
+
 // LEAN (prefix-sorted frames): only the sort key, tiles touched and the visible
 // count / key range; the records of the Gaussians the frame reads -- its sorted
 // prefix -- are written after the sort by k_records.
@@ -63,7 +136,25 @@ __global__ void __launch_bounds__(256, 5) k_preprocess(SceneK S, CamK C, OptK O,
     const int gi = blockIdx.x * blockDim.x + threadIdx.x;
     const FrameK F = fd->F;
     bool vis = false;
-    if (gi < S.n) {
+    if (gi < S.n && LEAN) {
+        // only visibility and the key: touched is a visibility flag for its readers
+        double depth = 0.0;
+        int v = lean_visible(S, C, O, F, gi, depth);
+        if (v == 2) {
+            Prep64 s;
+            v = prep64<false>(S, C, O, F, gi, s) ? 1 : 0;
+            depth = s.depth;
+        }
+        vis = v == 1;
+        if (vis) {
+            depth_key[gi] = __float_as_uint((float)depth);
+            kmine = kmaxe = depth_key[gi];
+            touched[gi] = 1u;
+        } else {
+            depth_key[gi] = 0xffffffffu;
+            touched[gi] = 0u;
+        }
+    } else if (gi < S.n) {
         Prep64 s;
         vis = prep64<false>(S, C, O, F, gi, s);
         if (!LEAN) gidx[gi] = (uint32_t)gi;

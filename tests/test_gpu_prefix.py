@@ -65,3 +65,26 @@ def test_gpu_suite_with_forced_prefix():
     r = subprocess.run([sys.executable, "-m", "pytest", str(ROOT / "tests"), "-m", "gpu", "-x", "-q",
                         "-p", "no:cacheprovider"], cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+
+
+@pytest.mark.skipif("TSB_PREFIX" in os.environ, reason="runs with the default cap only")
+@pytest.mark.parametrize("name,cam", [("c0", None), ("c1", None), ("c1", (97, 61, 40.0, 30.0, 20.0)),
+                                      ("c2", (200, 150, 400.0, -30.0, 170.0))])
+def test_lean_visibility_equals_exact(tsb, ctx, name, cam):
+    """A prefix-sorted frame decides visibility with the fp32 bounded test of the lean
+    preprocess (exact fp64 where undecided); the visible set, hence the order and every
+    output, equals the full-order frame's (exact fp64 preprocess).  Off-centre principal
+    points put many splats across the image border."""
+    from paper_2505_05356_b200 import synthetic
+    from helpers import gpu_scene
+    cfg = synthetic.config(name, n=60_000)
+    camera = cfg.camera if cam is None else synthetic.camera(cam[0], cam[1], cam[2], cam[3], cam[4])
+    scene = gpu_scene(tsb, ctx, cfg.scene, cfg.tof)
+    res = {}
+    for full in (False, True):
+        opts = tsb.RenderOptions(counts=True, full_lists=full)
+        rp = tsb.RenderPass(ctx).prepare(scene, camera, opts, cfg.frames[0]).forward()
+        res[full] = (rp.visible_count(), rp.outputs())
+    assert res[False][0] == res[True][0]
+    for k in ("quad", "depth_raw", "weight", "transmittance", "n_contrib", "n_processed"):
+        assert np.array_equal(res[False][1][k], res[True][1][k], equal_nan=True), k
