@@ -128,7 +128,8 @@ struct tsb_scene {
     float* densify = nullptr;
     double* stats = nullptr;  // kStats: bg grads (quad 4*nf, phasor 2*nf) at kStatBg, loss at kStatLoss
     float* staging = nullptr; // 4n floats for host<->device (un)packing
-    double* pcache = nullptr; // [7][n]: cov3d (6 planes) + opacity (SceneK::cov6 / opac)
+    double* pcache = nullptr; // [7][n] doubles: cov3d (6 planes) + opacity, then [6][n] floats: fp32 cov3d
+                              // (SceneK::cov6 / opac / cov6f); kPcacheWords doubles per Gaussian
     int64_t step = 0;
     int64_t densify_count = 0;
     cudaEvent_t params_ev = nullptr;  // last parameter write (ctx stream)
@@ -388,7 +389,8 @@ int color_base(const tsb_scene* s);
 // Refresh the time-independent cache after a parameter change (ctx stream).
 int refresh_param_cache(tsb_scene* s) {
     const SceneK S = scenek(s);
-    launch_param_cache(S, s->pcache, s->pcache + 6 * (size_t)s->d.n, s->ctx->stream);
+    launch_param_cache(S, s->pcache, s->pcache + 6 * (size_t)s->d.n,
+                       reinterpret_cast<float*>(s->pcache + 7 * (size_t)s->d.n), s->ctx->stream);
     if (s->d.n > 0) s->ctx->launches++;
     TSB_CHECK_LAUNCH();
     return TSB_OK;
@@ -418,7 +420,7 @@ int tsb_scene_create(tsb_ctx* ctx, const tsb_scene_desc* d, tsb_scene** out) {
     if ((rc = dev_alloc(&s->params, nel)) || (rc = dev_alloc(&s->grads, nel)) || (rc = dev_alloc(&s->m, nel)) ||
         (rc = dev_alloc(&s->v, nel)) || (rc = dev_alloc(&s->densify, (size_t)std::max(d->n, 1))) ||
         (rc = dev_alloc(&s->stats, kStats)) || (rc = dev_alloc(&s->staging, 4 * (size_t)std::max(d->n, 1))) ||
-        (rc = dev_alloc(&s->pcache, 7 * (size_t)std::max(d->n, 1)))) {
+        (rc = dev_alloc(&s->pcache, kPcacheWords * (size_t)std::max(d->n, 1)))) {
         tsb_scene_destroy(s);
         return rc;
     }
@@ -827,7 +829,7 @@ int tsb_scene_densify(tsb_scene* s, const tsb_densify_config* cfg, double scene_
     if (e == cudaSuccess && !((rc = dev_alloc(&P2, nel2)) || (rc = dev_alloc(&G2, nel2)) || (rc = dev_alloc(&M2, nel2)) ||
                               (rc = dev_alloc(&V2, nel2)) || (rc = dev_alloc(&dens2, (size_t)std::max(n_new, 1))) ||
                               (rc = dev_alloc(&stg2, 4 * (size_t)std::max(n_new, 1))) ||
-                              (rc = dev_alloc(&pc2, 7 * (size_t)std::max(n_new, 1))))) {
+                              (rc = dev_alloc(&pc2, kPcacheWords * (size_t)std::max(n_new, 1))))) {
         launch_densify_scatter(S, D, w, n_kept, s->narrays, s->params, s->m, s->v, P2, M2, V2, n_new, st);
         s->ctx->launches += n > 0 ? 1 : 0;
         cudaMemsetAsync(G2, 0, nel2 * sizeof(float4), st);
@@ -1101,6 +1103,7 @@ SceneK scenek(const tsb_scene* s) {
     k.color_sh = s->d.color ? s->params + (size_t)color_base(s) * n : nullptr;
     k.cov6 = s->pcache;
     k.opac = s->pcache + 6 * n;
+    k.cov6f = reinterpret_cast<const float*>(s->pcache + 7 * n);
     return k;
 }
 

@@ -86,8 +86,14 @@ __device__ __forceinline__ int lean_visible(const SceneK& S, const CamK& C, cons
         Ma[3 + j] = fabsf(fyz) * (fabsf(r1) + fabsf(tyz * r2));
     }
     const size_t n = (size_t)S.n;
-    const float c00 = (float)S.cov6[gi], c01 = (float)S.cov6[n + gi], c02 = (float)S.cov6[2 * n + gi];
-    const float c11 = (float)S.cov6[3 * n + gi], c12 = (float)S.cov6[4 * n + gi], c22 = (float)S.cov6[5 * n + gi];
+    float c00, c01, c02, c11, c12, c22;
+    if (S.cov6f) {  // 24 B instead of 48
+        c00 = S.cov6f[gi]; c01 = S.cov6f[n + gi]; c02 = S.cov6f[2 * n + gi];
+        c11 = S.cov6f[3 * n + gi]; c12 = S.cov6f[4 * n + gi]; c22 = S.cov6f[5 * n + gi];
+    } else {
+        c00 = (float)S.cov6[gi]; c01 = (float)S.cov6[n + gi]; c02 = (float)S.cov6[2 * n + gi];
+        c11 = (float)S.cov6[3 * n + gi]; c12 = (float)S.cov6[4 * n + gi]; c22 = (float)S.cov6[5 * n + gi];
+    }
     const float V[9] = {c00, c01, c02, c01, c11, c12, c02, c12, c22};
     float T[6], Ta[6];
 #pragma unroll
@@ -201,7 +207,8 @@ __global__ void __launch_bounds__(256, 5) k_preprocess(SceneK S, CamK C, OptK O,
 }
 
 // Time-independent per-Gaussian cache (SceneK::cov6 / opac), after every parameter change.
-__global__ void __launch_bounds__(256) k_param_cache(SceneK S, double* __restrict__ cov6, double* __restrict__ opac) {
+__global__ void __launch_bounds__(256) k_param_cache(SceneK S, double* __restrict__ cov6, double* __restrict__ opac,
+                                                     float* __restrict__ cov6f) {
     const int gi = blockIdx.x * blockDim.x + threadIdx.x;
     if (gi >= S.n) return;
     double c[9];
@@ -213,15 +220,19 @@ __global__ void __launch_bounds__(256) k_param_cache(SceneK S, double* __restric
     cov6[3 * n + gi] = c[4];
     cov6[4 * n + gi] = c[5];
     cov6[5 * n + gi] = c[8];
+    const int pl[6] = {0, 1, 2, 4, 5, 8};
+#pragma unroll
+    for (int k = 0; k < 6; ++k) cov6f[k * n + gi] = (float)c[pl[k]];
     opac[gi] = opacity64(S, gi);
 }
 
-void launch_param_cache(const SceneK& S, double* cov6, double* opac, cudaStream_t st) {
+void launch_param_cache(const SceneK& S, double* cov6, double* opac, float* cov6f, cudaStream_t st) {
     if (S.n <= 0) return;
     SceneK raw = S;
     raw.cov6 = nullptr;
     raw.opac = nullptr;
-    k_param_cache<<<(S.n + 255) / 256, 256, 0, st>>>(raw, cov6, opac);
+    raw.cov6f = nullptr;
+    k_param_cache<<<(S.n + 255) / 256, 256, 0, st>>>(raw, cov6, opac, cov6f);
 }
 
 void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* F,

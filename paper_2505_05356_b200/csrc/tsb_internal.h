@@ -53,6 +53,7 @@ struct SceneK {
     // so every frame of a sweep reads them instead of recomputing.  Null: inline.
     const double* cov6;
     const double* opac;
+    const float* cov6f;  // fp32 copy of cov6 (lean visibility bound) or null
 };
 
 struct FrameK {
@@ -217,7 +218,8 @@ void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameDev*
                   const PixK& px, int nf, cudaStream_t st);
 void launch_chain(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
                   const uint32_t* touched, float* screen, float4* grads, cudaStream_t st);
-void launch_param_cache(const SceneK& S, double* cov6, double* opac, cudaStream_t st);
+void launch_param_cache(const SceneK& S, double* cov6, double* opac, float* cov6f, cudaStream_t st);
+constexpr size_t kPcacheWords = 10;  // doubles per Gaussian of the parameter cache (7 fp64 + 6 fp32 words)
 // tsb_bin.cu
 // tsb_sort.cu: hand-written onesweep LSD radix sort of 32-bit keys + values (4 passes);
 // the result is back in (keys_a, vals_a).  Returns the number of kernels launched.
