@@ -34,21 +34,31 @@ struct Smem {
     uint8_t list[kRasterThreads / 32][kRasterThreads];  // per warp: its entries, in list order
 };
 
-// Warps of a 16 x 16 block (warp w: block rows 2w, 2w + 1) with a pixel centre that
-// can lie inside the entry's maha <= `outside` ellipse.  Bounding box of the ellipse
-// from the factored conic (half-widths sqrt(M Sigma_xx), sqrt(M Sigma_yy), Sigma = (L^T
-// L)^-1), widened by 1 % and 0.01 px: every pixel outside it evaluates maha > outside
-// in fp32 -- the entry's `continue` -- so skipping the entry for that warp changes
-// nothing.  Degenerate records reach every warp.
+// Pixel of thread tid in its 16 x 16 block: warp w owns the 8 x 4 sub-block at
+// (8 (w & 1), 4 (w >> 1)), lane l its pixel (l & 7, l >> 3) -- compact warp footprints
+// keep a warp's lanes on the same splats and let whole warps skip entries.
+__device__ __forceinline__ int block_px(int tid) { return ((tid >> 5) & 1) * 8 + (tid & 7); }
+__device__ __forceinline__ int block_py(int tid) { return (tid >> 6) * 4 + ((tid >> 3) & 3); }
+
+// Warps of a 16 x 16 block (layout above) with a pixel centre that can lie inside the
+// entry's maha <= `outside` ellipse.  Bounding box of the ellipse from the factored
+// conic (half-widths sqrt(M Sigma_xx), sqrt(M Sigma_yy), Sigma = (L^T L)^-1), widened by
+// 1 % and 0.01 px: every pixel outside it evaluates maha > outside in fp32 -- the
+// entry's `continue` -- so skipping the entry for that warp changes nothing.
+// Degenerate records reach every warp.
 __device__ __forceinline__ uint32_t warps_reached(const float4& a, const float4& b, float outside) {
     const float s = sqrtf(outside) * 1.01f;
     const float hy = __fdividef(s, fabsf(b.z)) + 0.01f;
     const float hx = __fdividef(s * sqrtf(fmaf(b.y, b.y, b.z * b.z)), fabsf(b.x * b.z)) + 0.01f;
     if (!(hx <= 1e30f && hy <= 1e30f)) return 0xffu;
-    if (a.x + hx < 0.5f || a.x - hx > (float)kTile - 0.5f) return 0u;
-    const int k0 = max((int)ceilf(a.y - hy - 0.5f), 0), k1 = min((int)floorf(a.y + hy - 0.5f), kTile - 1);
-    if (k0 > k1) return 0u;
-    return ((2u << (k1 >> 1)) - 1u) & ~((1u << (k0 >> 1)) - 1u);
+    // pixel centres 0.5 + k: column halves [0.5, 7.5], [8.5, 15.5]; row quarters of 4
+    const int kx0 = max((int)ceilf(a.x - hx - 0.5f), 0), kx1 = min((int)floorf(a.x + hx - 0.5f), kTile - 1);
+    const int ky0 = max((int)ceilf(a.y - hy - 0.5f), 0), ky1 = min((int)floorf(a.y + hy - 0.5f), kTile - 1);
+    if (kx0 > kx1 || ky0 > ky1) return 0u;
+    const uint32_t cols = (kx0 < 8 ? 0x55u : 0u) | (kx1 >= 8 ? 0xaau : 0u);  // warp parity = column half
+    const int q0 = ky0 >> 2, q1 = ky1 >> 2;                                   // warp >> 1 = row quarter
+    const uint32_t rows = ((4u << (2 * q1)) - 1u) & ~((1u << (2 * q0)) - 1u);
+    return cols & rows;
 }
 
 // ---------------------------------------------------------------------------
@@ -71,12 +81,13 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
     const int nsub = O.sub * O.sub;
     const int tile = blockIdx.x / nsub, sb = blockIdx.x % nsub;
     const int tid = threadIdx.x;
-    const int lx = (sb % O.sub) * kTile + (tid % kTile), ly = (sb / O.sub) * kTile + (tid / kTile);
+    const int bx_ = block_px(tid), by_ = block_py(tid);
+    const int lx = (sb % O.sub) * kTile + bx_, ly = (sb / O.sub) * kTile + by_;
     const int x = (tile % O.tiles_x) * O.ts + lx, y = (tile / O.tiles_x) * O.ts + ly;
     const bool active = lx < O.ts && ly < O.ts && x < W && y < H;
     const uint4 rg = ck.ranges[tile];  // (start, len, cum, -)
-    const float ox = (float)(x - (tid % kTile)), oy = (float)(y - (tid / kTile));  // block origin
-    const float pcx = (float)(tid % kTile) + 0.5f, pcy = (float)(tid / kTile) + 0.5f;
+    const float ox = (float)(x - bx_), oy = (float)(y - by_);  // block origin
+    const float pcx = (float)bx_ + 0.5f, pcy = (float)by_ + 0.5f;
     const size_t HW = (size_t)W * H, o = active ? (size_t)y * W + x : 0;
 
     float T = 1.f, Tpre = 1.f, SW = 0.f, SD = 0.f, dT = 0.f;  // dT: absolute error bound of T
@@ -365,11 +376,12 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
     const int ntiles = O.tiles_x * O.tiles_y;
     const int tile = blockIdx.x / nsub, sb = blockIdx.x % nsub;
     const int tid = threadIdx.x, lane = tid & 31;
-    const int lx = (sb % O.sub) * kTile + (tid % kTile), ly = (sb / O.sub) * kTile + (tid / kTile);
+    const int bx_ = block_px(tid), by_ = block_py(tid);
+    const int lx = (sb % O.sub) * kTile + bx_, ly = (sb / O.sub) * kTile + by_;
     const int x = (tile % O.tiles_x) * O.ts + lx, y = (tile / O.tiles_x) * O.ts + ly;
     const bool active = lx < O.ts && ly < O.ts && x < W && y < H;
-    const float ox = (float)(x - (tid % kTile)), oy = (float)(y - (tid / kTile));  // block origin
-    const float pcx = (float)(tid % kTile) + 0.5f, pcy = (float)(tid / kTile) + 0.5f;
+    const float ox = (float)(x - bx_), oy = (float)(y - by_);  // block origin
+    const float pcx = (float)bx_ + 0.5f, pcy = (float)by_ + 0.5f;
     const size_t HW = (size_t)W * H, o = active ? (size_t)y * W + x : 0;
 
     int last = 0;
