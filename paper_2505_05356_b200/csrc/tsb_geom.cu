@@ -130,7 +130,7 @@ __device__ __forceinline__ int lean_visible(const SceneK& S, const CamK& C, cons
 // count / key range; the records of the Gaussians the frame reads -- its sorted
 // prefix -- are written after the sort by k_records.
 template <bool LEAN>
-__global__ void __launch_bounds__(256, 5) k_preprocess(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd,
+__global__ void __launch_bounds__(256, LEAN ? 6 : 5) k_preprocess(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd,
                                                     uint32_t* __restrict__ depth_key,
                                                     double* __restrict__ depth64,
                                                     uint32_t* __restrict__ gidx,
