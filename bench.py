@@ -46,6 +46,33 @@ def load_peaks():
     return PEAKS_FALLBACK
 
 
+def workload_config(world: int) -> dict:
+    """The c3 sweep both arms measure (same dict in the ours and reference lines)."""
+    return {"workload": "c3_forward_1M_640x480", "gaussians": 1_000_000, "image": "640x480", "frames": 300,
+            "frame_times": "t = i/299", "frequency_hz": 30e6, "keyframes": 2,
+            "outputs": "quad (4 raw samples) + depth_raw + depth + weight",
+            "parallelism": f"frames split over {world} rank(s)",
+            "l2": "inputs larger than L2 (~0.4 GB touched per frame)"}
+
+
+def relaunch_distributed(args) -> int:
+    """`bench.py --gpus N` outside torchrun: start N ranks (one per GPU) the way the driver
+    does, rank 0's JSON line is this process's output."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    # communicator set-up lines (ring / NVLS choice) on stderr, the JSON line stays alone on stdout
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 # ---------------------------------------------------------------------------
 # clocks (pynvml sampling during the timed region)
 class ClockSampler:
@@ -159,18 +186,24 @@ class StreamTimer:
 
 
 # ---------------------------------------------------------------------------
-# Roofline accounting.  Per-kernel device times come from CUDA
-# events the library records on the pass stream around each stage (profiling
-# mode: the same kernels, issued eagerly), over the same c3 frames.
-#   k_preprocess (HBM): per Gaussian 120 B read (pos_op 16, 2 keyframe offsets 32,
-#     cov3d cache 48, opacity cache 8, scale_amp 16) + 8 B written (fp32 key, tiles
-#     touched).  Frames that sort only their nearest prefix (the default, TSB_PREFIX != 0)
-#     run the lean variant: that is all; the records of the prefix are written after the
-#     sort (k_records).  The full variant also writes per Gaussian the index (4 B) and per
-#     visible Gaussian 64 B (fp64 depth 8, rect 8, record 48).
-#   k_raster_fwd (FP32): 9 FLOP per (pixel, entry) evaluation (dx, dy, p, q, maha,
-#     threshold) + 14 FLOP per contributing evaluation (alpha, w, w2, quad pair, SW, SD,
-#     T) -- counted live by the kernel in profiling mode.
+# Roofline accounting.  Algorithmic work per unit (SURVEY.md 8(d),
+# DESIGN.md 4):
+#   k_preprocess (HBM): the lean variant prefix-sorted frames run reads 80 B per Gaussian
+#     (pos_op 16, two keyframe offsets 32, fp32 cov3d cache 24, fp64 opacity cache 8) and
+#     writes 8 B (fp32 key, tiles-touched flag) = 88 B; the full variant (TSB_PREFIX=0)
+#     writes 4 B more per Gaussian and 64 B per visible Gaussian (fp64 depth, rect, record).
+#   binning (HBM): SURVEY 8(d) "scan + duplicate" = 12 B per tile-list entry.
+#   k_raster_fwd (FP32): SURVEY 8(d) 23 FLOP (17 FP32 inst, FMA = 2) per (pixel, entry)
+#     evaluation; evaluations counted live by the kernel in profiling mode.
+#   k_adam (HBM): 28 B per parameter element (read p, g, m, v; write p, m, v) + 4 B per
+#     Gaussian for the densify statistic.
+# Times: CUDA events the library records on each pass's stream around every stage.
+#   serialised -- one more sweep on ONE pass after the timed region: a launch's own
+#     duration (what ncu's launch list measures; `achieved` / `frac`);
+#   overlapped -- one more sweep over all passes (24 frames in flight, as timed, but issued
+#     eagerly so the stage events exist): the stage's share of the summed event time,
+#     scaled to the timed ms_per_step, gives its attributed time in the step
+#     (`in_step`; these times add up to ms_per_step).
 def fp32_peak_tflops(sm_mhz):
     return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
 
@@ -185,49 +218,57 @@ def load_traffic():
     return {}
 
 
-def rooflines(stage_ms, shapes, evals, contribs, peaks, sm_max_mhz):
-    """stage_ms: {stage: (ms per step, launches per step)}; returns (dominant, all)."""
-    traffic = load_traffic()
+FAMILIES = {"k_preprocess": ("preprocess",), "depth_sort": ("depth_sort",),
+            "binning": ("bin_count", "binning", "bin_emit", "scan", "ranges", "tile_sort"),
+            "k_raster_fwd": ("raster_fwd",), "k_fixup": ("fixup",), "loss": ("loss",),
+            "k_raster_bwd": ("raster_bwd",), "k_chain": ("chain",), "k_adam": ("adam",), "allreduce": ("allreduce",)}
+
+
+def family_ms(stage_ms):
     out = {}
-    ms, calls = stage_ms.get("preprocess", (0.0, 0))
-    if calls:
-        per = ms / calls
-        lean = os.environ.get("TSB_PREFIX", "1") != "0"
-        b = shapes["n"] * 128 if lean else shapes["n"] * 132 + shapes["v"] * 64
-        ach = b / (per * 1e-3) / 1e9
-        t = traffic.get("k_preprocess")
-        out["k_preprocess"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                               "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": t,
-                               "algorithmic_bytes_per_launch": int(b), "avg_launch_ms": round(per, 5),
-                               "peak_source": peaks["source"]}
-    ms, calls = stage_ms.get("raster_fwd", (0.0, 0))
-    if calls and evals:
-        frames = shapes["frames"]
-        per_frame_ms = ms / frames
-        flop = (9 * evals + 14 * contribs) / frames
-        ach = flop / (per_frame_ms * 1e-3) / 1e12
-        pk = fp32_peak_tflops(sm_max_mhz or 1965)
-        t = traffic.get("k_raster_fwd")
-        out["k_raster_fwd"] = {"bound": "fp32", "achieved": round(ach, 2), "peak": round(pk, 1), "unit": "TFLOP/s",
-                               "frac": round(ach / pk, 4), "traffic": t,
-                               "algorithmic_flop_per_frame": int(flop), "evaluations_per_frame": evals // frames,
-                               "contributions_per_frame": contribs // frames,
-                               "avg_ms_per_frame": round(per_frame_ms, 5),
-                               "launches_per_frame": round(calls / frames, 2),
-                               "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x max SM clock",
-                               "issue_slots_busy_ncu": t and t.get("issue_active")}
-    total = sum(v[0] for v in stage_ms.values())
-    share = {k: round(v[0] / total, 4) for k, v in stage_ms.items() if v[1] and total}
-    dom = None
-    for k, st in (("k_preprocess", "preprocess"), ("k_raster_fwd", "raster_fwd")):
-        if k in out:
-            out[k]["share_of_step"] = share.get(st)
-            if dom is None or (share.get(st) or 0) > (out[dom]["share_of_step"] or 0):
-                dom = k
-    res = dict(out[dom]) if dom else {}
+    for fam, stages in FAMILIES.items():
+        ms = sum(stage_ms.get(st, (0.0, 0))[0] for st in stages)
+        calls = sum(stage_ms.get(st, (0.0, 0))[1] for st in stages)
+        if calls:
+            out[fam] = (ms, calls)
+    return out
+
+
+def rooflines(ser, ovl, ms_per_step, work, peaks, sm_max_mhz):
+    """ser / ovl: {family: (ms summed over the sweep, launches)} serialised / overlapped;
+    work: {family: (algorithmic units per sweep, unit, bound, peak)}.  Returns (dominant, all)."""
+    traffic = load_traffic()
+    tot_ser = sum(v[0] for v in ser.values()) or 1.0
+    tot_ovl = sum(v[0] for v in ovl.values()) or 1.0
+    out = {}
+    for fam, (ms, calls) in ser.items():
+        o = {"share_of_step": round(ms / tot_ser, 4), "launches_per_sweep": calls,
+             "avg_launch_ms": round(ms / calls, 5)}
+        share_ovl = ovl.get(fam, (0.0, 0))[0] / tot_ovl
+        o["in_step"] = {"share": round(share_ovl, 4), "ms": round(share_ovl * ms_per_step, 4)}
+        if fam in work:
+            units, unit, bound, pk = work[fam]
+            scale = 1e9 if unit == "GB/s" else 1e12
+            ach = units / (ms * 1e-3) / scale
+            o.update({"bound": bound, "achieved": round(ach, 3), "peak": pk, "unit": unit,
+                      "frac": round(ach / pk, 4), "algorithmic_per_sweep": int(units)})
+            if share_ovl > 0:
+                a2 = units / (share_ovl * ms_per_step * 1e-3) / scale
+                o["in_step"].update({"achieved": round(a2, 3), "frac": round(a2 / pk, 4)})
+        t = traffic.get(fam)
+        if t is not None:
+            o["traffic"] = t
+        out[fam] = o
+    dom = max((f for f in out if "frac" in out[f]), key=lambda f: out[f]["share_of_step"], default=None)
+    res = {}
     if dom:
-        res["kernel"] = dom
-    res["stage_share_of_step"] = share
+        d = out[dom]
+        res = {"bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"], "unit": d["unit"],
+               "frac": d["frac"], "traffic": (d.get("traffic") or {}).get("dram_bytes_per_launch"),
+               "kernel": dom, "share_of_step": d["share_of_step"], "avg_launch_ms": d["avg_launch_ms"],
+               "in_step": d["in_step"]}
+    res["stage_share_of_step"] = {f: o["share_of_step"] for f, o in out.items()}
+    res["peak_source"] = {"hbm": peaks["source"], "fp32": f"derived: 148 SMs x 128 FP32 lanes x 2 x {sm_max_mhz} MHz"}
     return res, out
 
 
@@ -266,16 +307,20 @@ def bench_c3(args, dist, tsb, synthetic):
     ctx.synchronize()
     launches = ctx.launch_count() - l0
     redos = ctx.redo_count()
-    # per-stage device times (roofline): same frames, one pass, stage events on its stream
+    # per-stage device times (roofline): the same sweep again, (1) over all passes with stage
+    # events (overlapped, eager), (2) on one pass (serialised launches); see rooflines()
     ctx.stage_times()
     ctx.raster_counts()
     ctx.set_profiling(True)
-    prof_steps = 1
-    for _ in range(prof_steps):
-        step([rp])
+    step(passes)
+    ctx.join()
+    ctx.synchronize()
+    st_ovl = ctx.stage_times()
+    ctx.raster_counts()
+    step([rp])
     ctx.synchronize()
     ctx.set_profiling(False)
-    st = ctx.stage_times()
+    st_ser = ctx.stage_times()
     evals, contribs = ctx.raster_counts()
     v, k = rp.visible_count(), rp.num_keys()
     fixups = rp.debug_fixups()
@@ -324,14 +369,23 @@ def bench_c3(args, dist, tsb, synthetic):
            "timer": "host wall clock; scene H2D from pinned memory, every frame's quad/depth/weight D2H into pinned "
                     "per-pass buffers (tsb_pass_download_async), all landed before the clock stops"}
 
-    shapes = dict(n=g.n, v=v, frames=len(my_frames) * prof_steps)
-    stage_ms = {name: (t / prof_steps, c // prof_steps) for name, (t, c) in st.items() if c}
-    roof, roofs = rooflines(stage_ms, shapes, evals, contribs, load_peaks(), clk.summary()["sm_max_mhz"])
-    roof["stage_ms_per_step"] = {k_: round(t_, 3) for k_, (t_, _) in stage_ms.items()}
+    nfr = len(my_frames)
+    lean = os.environ.get("TSB_PREFIX", "1") != "0"
+    peaks = load_peaks()
+    pk_fp32 = round(fp32_peak_tflops(clk.summary()["sm_max_mhz"] or 1965), 1)
+    work = {"k_preprocess": (nfr * (g.n * 88 if lean else g.n * 92 + v * 64), "GB/s", "hbm", peaks["hbm_gbs"]),
+            "binning": (nfr * k * 12, "GB/s", "hbm", peaks["hbm_gbs"]),
+            "k_raster_fwd": (23 * evals, "TFLOP/s", "fp32", pk_fp32)}
+    ser, ovl = family_ms(st_ser), family_ms(st_ovl)
+    roof, roofs = rooflines(ser, ovl, ms_max / args.steps, work, peaks, clk.summary()["sm_max_mhz"])
+    roof["evaluations_per_frame"] = evals // max(nfr, 1)
+    roof["contributions_per_frame"] = contribs // max(nfr, 1)
     info = {"visible": v, "keys_per_frame": k, "fixup_pixels_last_frame": fixups, "clock": clk.summary(),
             "launches": launches, "passes_in_flight": len(passes), "redone_frames": redos,
-            "stage_timing": "one more step on a single pass after the timed region, profiling mode (kernels "
-                            "issued eagerly, events on the pass stream around each stage)"}
+            "stage_ms_serialised_sweep": {f: round(t_, 3) for f, (t_, _) in ser.items()},
+            "stage_ms_overlapped_sweep": {f: round(t_, 3) for f, (t_, _) in ovl.items()},
+            "stage_timing": "after the timed region: the same 300-frame sweep over all passes with stage events "
+                            "(overlapped, eager) and on one pass (serialised)"}
     info["rooflines"] = roofs
     return value, ms_max / args.steps, e2e, roof, info, ctx
 
@@ -389,12 +443,21 @@ def bench_train_c4(args, dist, tsb, synthetic, ctx):
     ctx.set_profiling(False)
     st = ctx.stage_times()
     ms_max = dist.max(ms)
+    adam = None
+    if st.get("adam", (0, 0))[1]:
+        ms_a, calls_a = st["adam"]
+        per = ms_a / calls_a
+        b = g.n * (18 * 28 + 4)  # 18 parameters per Gaussian x 28 B + densify stat
+        pk = load_peaks()["hbm_gbs"]
+        adam = {"bound": "hbm", "achieved": round(b / (per * 1e-3) / 1e9, 1), "peak": pk, "unit": "GB/s",
+                "frac": round(b / (per * 1e-3) / 1e9 / pk, 4), "avg_launch_ms": round(per, 4),
+                "algorithmic_bytes_per_launch": b}
     res = {"config": "c4", "n_gaussians": g.n, "image": f"{W}x{H}", "frames_per_iter": len(cfg.frames),
            "iters_per_s": round(args.train_steps / (ms_max / 1e3), 4),
            "ms_per_iter": round(ms_max / args.train_steps, 3),
            "stage_ms_per_iter": {k: round(v[0], 3) for k, v in st.items() if v[1]},
            "keys_per_frame_last": trainer.rp.num_keys(), "passes_in_flight": len(trainer.passes),
-           "redone_frames_timed": train_redos,
+           "redone_frames_timed": train_redos, "k_adam_roofline": adam,
            "path": "parallel.FrameShardedTrainer (public API)"}
     if comm:
         comm.close()
@@ -468,10 +531,15 @@ def cpu_baseline_c3(frames=1):
 
 # ---------------------------------------------------------------------------
 def run_reference(args, dist):
+    """Reference arm: the CPU restatement of the reference hot path (oracle/, "port" -- the
+    reference itself needs Eigen, absent here) on the same c3 workload, all host threads.
+    Each step renders one of the sweep's 300 frames (RenderPass ctor + forward, the
+    reference's per-frame unit); frames/s is per frame, so it compares with the GPU arm's
+    300-frame steps.  Inputs come from the seeded generator without mapping libtsb.so."""
     if dist.rank != 0:
         return 0
     from oracle import oracle as orc
-    from paper_2505_05356_b200 import synthetic
+    from paper_2505_05356_b200 import synthetic  # numpy only; the package maps libtsb.so lazily
     cfg = synthetic.config("c3")
     g = cfg.scene
     opts = type("O", (), {})()
@@ -490,18 +558,32 @@ def run_reference(args, dist):
     total = sum(times)
     value = len(times) / total
     cores = orc.num_threads()
+    sample = (f"{len(times)} of the sweep's 300 c3 frames, one per step (frame (37 s) mod 300; RenderPass ctor + "
+              "forward each), oracle/ restatement of splat.cpp in fp64 with OpenMP over tiles")
     line = {"metric": METRIC, "value": round(value, 5), "unit": "frames/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * total / len(times), 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded BASELINE c3 distributions)", "impl": "reference",
-            "config": {"workload": "c3_forward_1M_640x480", "gaussians": g.n, "image": "640x480",
-                       "frames_per_step": 1, "frequency_hz": 30e6},
+            "data": "synthetic (seeded BASELINE c3 distributions; no dataset named)", "impl": "reference",
+            "config": workload_config(dist.world),
             "cpu_baseline": {"value": round(value, 5), "unit": "frames/s", "cores": cores, "kind": "port",
-                             "sample": f"{len(times)} of the 300 c3 frames (RenderPass ctor + forward each), "
-                                       "oracle/ restatement of splat.cpp in fp64 with OpenMP over tiles"},
-            "e2e": {"value": round(value, 5), "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                             "sample": sample},
+            "e2e": {"value": round(value, 5), "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "native_libraries": [str(x) for x in loaded_libraries()]}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def loaded_libraries():
+    """In-tree shared objects mapped by this process (reference-arm hygiene check)."""
+    out = []
+    try:
+        for ln in open("/proc/self/maps"):
+            p_ = ln.split()[-1] if len(ln.split()) >= 6 else ""
+            if p_.endswith(".so") and str(ROOT) in p_ and p_ not in out:
+                out.append(p_)
+    except OSError:
+        pass
+    return [os.path.relpath(x, ROOT) for x in out]
 
 
 def main():
@@ -521,6 +603,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else max(args.warmup, 1)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(args)
     dist = Dist(args.gpus)
     if args.impl == "reference":
         rc = run_reference(args, dist)
@@ -549,11 +633,8 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (seeded BASELINE c3 distributions; no dataset named)",
-                "config": {"workload": "c3_forward_1M_640x480", "gaussians": 1_000_000, "image": "640x480",
-                           "frames_per_step": 300, "frequency_hz": 30e6, "keyframes": 2,
-                           "parallelism": f"frames split over {dist.world} rank(s)",
-                           "l2": "inputs larger than L2 (~0.4 GB touched per frame)",
-                           "precision": "fp64 preprocess, fp32 raster, fp64 fix-up of ambiguous pixels"},
+                "config": workload_config(dist.world),
+                "precision": "fp64 preprocess, fp32 raster, fp64 fix-up of ambiguous pixels",
                 "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
                 "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"]},
                 "gpu_launches": info["launches"], "train": train, "deform_net": deform, "detail": info}

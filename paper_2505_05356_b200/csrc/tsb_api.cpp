@@ -85,6 +85,10 @@ struct tsb_ctx {
     int64_t redos = 0;                             // frames redone after a device-side abort
     unsigned long long* work = nullptr;            // raster work counters (profiling)
     bool use_graphs = true;                        // forward as a CUDA graph (TSB_NO_GRAPHS=1 disables)
+    // nearest-prefix cap learned by any pass of the context (a pass whose prefix ran out
+    // grows it; the others start their next frame from it instead of rediscovering it)
+    int kcap_learned = 0;
+    bool prefix_off = false;  // some pass needed the full order at every cap
 };
 
 namespace {
@@ -1245,6 +1249,8 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     p->sorted = p->gidx_b;  // launch_sort_depth's result buffer
     {
         const int n = p->scene->d.n;
+        if (p->ctx->prefix_off) p->kcap = 0;
+        else if (p->kcap > 0) p->kcap = std::max(p->kcap, p->ctx->kcap_learned);
         p->prefix = !(p->channels & TSB_CH_FULL_LISTS) && p->kcap > 0 && n > p->kcap;
         if (p->prefix && p->kcap > p->sel_cap) {
             dev_free(p->sel_keys); dev_free(p->sel_vals); dev_free(p->sel_scratch);
@@ -1392,7 +1398,7 @@ int record_prepare(tsb_pass* p, cudaStream_t st, int* launches) {
                                      p->counters + 2, st);
             // records of the prefix (the lean preprocess wrote keys only)
             l += launch_records(scenek(p->scene), p->cam, p->opt, p->frame_dev, p->gidx_b, p->counters + 4,
-                                p->kcap, p->key_a, p->depth64, p->gidx_a, p->rect, p->rec, st);
+                                p->kcap, p->key_a, p->depth64, p->gidx_a, p->rect, p->rec, p->counters + 2, st);
         } else
             l += launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, key_range, n, p->sort_scratch, st);
     }
@@ -1704,7 +1710,7 @@ int enqueue_backward(tsb_pass* p, const UpK& up);
 void full_order(tsb_pass* p, bool exact64, cudaStream_t st) {
     const int n = p->scene->d.n;
     p->ctx->launches += launch_records(scenek(p->scene), p->cam, p->opt, p->frame_dev, nullptr, nullptr, n, p->key_a,
-                                       p->depth64, p->gidx_a, p->rect, p->rec, st);
+                                       p->depth64, p->gidx_a, p->rect, p->rec, p->counters + 2, st);
     if (exact64) {
         p->ctx->launches += launch_sort_depth64(p->depth64, p->touched, p->key_a, p->key_b, p->gidx_a, p->gidx_b, n,
                                                 p->sort_scratch, st);
@@ -1714,6 +1720,22 @@ void full_order(tsb_pass* p, bool exact64, cudaStream_t st) {
                                               reinterpret_cast<uint32_t*>(p->counters + 5), n, p->sort_scratch, st);
         p->sorted = p->gidx_b;
     }
+    p->prefix = false;
+    p->n_bin = p->counters;
+}
+
+// The frame from the exact (non-lean) preprocess and the full depth sort: the redo of a
+// frame whose lean visibility test disagreed with prep64 (abort bit 16).
+void exact_order(tsb_pass* p, cudaStream_t st) {
+    const int n = p->scene->d.n;
+    uint32_t* key_range = reinterpret_cast<uint32_t*>(p->counters + 5);
+    cudaMemsetAsync(p->counters, 0, sizeof(int32_t) * 8, st);
+    cudaMemsetAsync(key_range, 0xff, sizeof(int32_t), st);
+    launch_preprocess(scenek(p->scene), p->cam, p->opt, p->frame_dev, p->key_a, p->depth64, p->gidx_a, p->touched,
+                      p->rect, p->rec, p->counters, key_range, false, st);
+    p->ctx->launches += 1 + launch_sort_depth(p->key_a, p->key_b, p->gidx_a, p->gidx_b, key_range, n,
+                                              p->sort_scratch, st);
+    p->sorted = p->gidx_b;
     p->prefix = false;
     p->n_bin = p->counters;
 }
@@ -1732,10 +1754,14 @@ int settle(tsb_pass* p) {
         if (attempt >= 8) return fail(TSB_ERR_NOMEM, "render: tile-list storage kept overflowing");
         p->ctx->redos++;
         cudaStream_t st = p->stream;
-        if (p->prefix && (ab & (8 | 2))) {  // the full order (+ the records the lean preprocess skipped)
+        if (ab & 16) {  // lean / exact visibility disagreed: exact preprocess + full sort
+            exact_order(p, st);  // an over-long tie run of this order aborts the next attempt (bit 2)
+        } else if (p->prefix && (ab & (8 | 2))) {  // the full order (+ the records the lean preprocess skipped)
             if (ab & 8) {  // the prefix ran out before every pixel terminated: later frames sort a longer one
                 const int n = p->scene->d.n;
                 p->kcap = (int64_t)p->kcap * 4 >= n ? 0 : p->kcap * 4;
+                if (p->kcap == 0) p->ctx->prefix_off = true;
+                else p->ctx->kcap_learned = std::max(p->ctx->kcap_learned, p->kcap);
             }
             full_order(p, (ab & 2) != 0, st);
         } else if (ab & 2) {  // an equal-key run too long to resolve on read: exact 64-bit sort
@@ -2310,17 +2336,19 @@ int tsb_pass_debug_records(tsb_pass* p, float* rec12) {
     const int n = p->scene->d.n, V = p->V;
     std::vector<float4> A(std::max(n, 1)), B(std::max(n, 1)), C(std::max(n, 1)), D(std::max(n, 1));
     std::vector<uint32_t> g(std::max(V, 1));
+    {
+        // first: on a prefix-sorted frame order_device() runs full_order, whose k_records
+        // writes the records of every visible Gaussian past the prefix
+        const uint32_t* od = nullptr;
+        int rc2;
+        if ((rc2 = order_device(p, &od))) return rc2;
+        if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), od, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, st));
+    }
     if (n > 0) {
         TSB_CUDA(cudaMemcpyAsync(A.data(), p->rec.A, sizeof(float4) * n, cudaMemcpyDeviceToHost, st));
         TSB_CUDA(cudaMemcpyAsync(B.data(), p->rec.B, sizeof(float4) * n, cudaMemcpyDeviceToHost, st));
         TSB_CUDA(cudaMemcpyAsync(C.data(), p->rec.C, sizeof(float4) * n, cudaMemcpyDeviceToHost, st));
         if (p->nf > 1) TSB_CUDA(cudaMemcpyAsync(D.data(), p->rec.D, sizeof(float4) * n, cudaMemcpyDeviceToHost, st));
-    }
-    {
-        const uint32_t* od = nullptr;
-        int rc2;
-        if ((rc2 = order_device(p, &od))) return rc2;
-        if (V > 0) TSB_CUDA(cudaMemcpyAsync(g.data(), od, sizeof(uint32_t) * V, cudaMemcpyDeviceToHost, st));
     }
     TSB_CUDA(cudaStreamSynchronize(st));
     for (int r = 0; r < V; ++r) {

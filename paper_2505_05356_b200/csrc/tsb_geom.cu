@@ -119,7 +119,10 @@ __device__ __forceinline__ int lean_visible(const SceneK& S, const CamK& C, cons
     const float lam = 0.5f * (a0 + a3) + sqrtf(fmaxf(disc, 0.1f));
     const float r = (float)O.sigma_cutoff * sqrtf(lam);
     const float tol = 1e-4f * (r * fmaxf(1.f, (b0 + b3) / lam) + fabsf(mx) + fabsf(my) + 1.f);
-    if (!(tol < 1e8f)) return 2;  // huge or non-finite: prep64 (x86 int conversion semantics)
+    // huge or non-finite: prep64.  Its rect bounds go through x86 int conversion (INT_MIN
+    // past 2^31), which culls splats the plain geometric test keeps, so anything whose
+    // mean +- radius gets anywhere near 2^31 px is decided exactly.
+    if (!(tol < 1e8f && fabsf(mx) + r < 1e9f && fabsf(my) + r < 1e9f)) return 2;
     const float bx = mx + r + 1.f, ax = (float)C.W - (mx - r);
     const float by = my + r + 1.f, ay = (float)C.H - (my - r);
     if (fabsf(bx) <= tol || fabsf(ax) <= tol || fabsf(by) <= tol || fabsf(ay) <= tol) return 2;
@@ -255,7 +258,7 @@ __global__ void __launch_bounds__(256, 5) k_records(SceneK S, CamK C, OptK O, co
                                                  const uint32_t* __restrict__ list, const int32_t* __restrict__ count,
                                                  int n, const uint32_t* __restrict__ depth_key,
                                                  double* __restrict__ depth64, uint32_t* __restrict__ gidx,
-                                                 uint2* __restrict__ rect, RecK rec) {
+                                                 uint2* __restrict__ rect, RecK rec, int32_t* __restrict__ abort) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (list ? *count : n)) return;
     const int gi = list ? (int)list[i] : i;
@@ -265,15 +268,21 @@ __global__ void __launch_bounds__(256, 5) k_records(SceneK S, CamK C, OptK O, co
     }
     const FrameK F = fd->F;
     Prep64 s;
-    prep64<false>(S, C, O, F, gi, s);
+    // The lean preprocess kept this Gaussian; the exact test must agree.  If it does
+    // not, the frame is redone from the exact (non-lean) preprocess (abort bit 16).
+    if (!prep64<false>(S, C, O, F, gi, s)) {
+        atomicOr(abort, 16);
+        return;
+    }
     write_records(S, s, gi, depth64, rect, rec);
 }
 
 int launch_records(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* F, const uint32_t* list,
                    const int32_t* count, int n, const uint32_t* depth_key, double* depth64, uint32_t* gidx,
-                   uint2* rect, RecK rec, cudaStream_t st) {
+                   uint2* rect, RecK rec, int32_t* abort, cudaStream_t st) {
     if (n <= 0) return 0;
-    k_records<<<(n + 255) / 256, 256, 0, st>>>(S, C, O, F, list, count, n, depth_key, depth64, gidx, rect, rec);
+    k_records<<<(n + 255) / 256, 256, 0, st>>>(S, C, O, F, list, count, n, depth_key, depth64, gidx, rect, rec,
+                                               abort);
     return 1;
 }
 

@@ -189,7 +189,7 @@ void launch_preprocess(const SceneK& S, const CamK& C, const OptK& O, const Fram
 // every visible Gaussian plus the identity order when list is null.  Returns launches.
 int launch_records(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* F, const uint32_t* list,
                    const int32_t* count, int n, const uint32_t* depth_key, double* depth64, uint32_t* gidx,
-                   uint2* rect, RecK rec, cudaStream_t st);
+                   uint2* rect, RecK rec, int32_t* abort, cudaStream_t st);
 // fp64 record cache for the fix-up (valid when stamp[g] == frame stamp).
 struct Rec64 {
     double4 m0;  // mean x, mean y, conic a, conic b
