@@ -201,9 +201,9 @@ class StreamTimer:
 #   serialised -- one more sweep on ONE pass after the timed region: a launch's own
 #     duration (what ncu's launch list measures; `achieved` / `frac`);
 #   overlapped -- one more sweep over all passes (24 frames in flight, as timed, but issued
-#     eagerly so the stage events exist): the stage's share of the summed event time,
-#     scaled to the timed ms_per_step, gives its attributed time in the step
-#     (`in_step`; these times add up to ms_per_step).
+#     eagerly so the stage events exist): the stage's share of the summed event time
+#     (`share_overlapped`; event spans of concurrent kernels overlap, so only the shares
+#     are meaningful, and they agree with the serialised shares and ncu's launch list).
 def fp32_peak_tflops(sm_mhz):
     return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
 
@@ -244,17 +244,13 @@ def rooflines(ser, ovl, ms_per_step, work, peaks, sm_max_mhz):
     for fam, (ms, calls) in ser.items():
         o = {"share_of_step": round(ms / tot_ser, 4), "launches_per_sweep": calls,
              "avg_launch_ms": round(ms / calls, 5)}
-        share_ovl = ovl.get(fam, (0.0, 0))[0] / tot_ovl
-        o["in_step"] = {"share": round(share_ovl, 4), "ms": round(share_ovl * ms_per_step, 4)}
+        o["share_overlapped"] = round(ovl.get(fam, (0.0, 0))[0] / tot_ovl, 4)
         if fam in work:
             units, unit, bound, pk = work[fam]
             scale = 1e9 if unit == "GB/s" else 1e12
             ach = units / (ms * 1e-3) / scale
             o.update({"bound": bound, "achieved": round(ach, 3), "peak": pk, "unit": unit,
                       "frac": round(ach / pk, 4), "algorithmic_per_sweep": int(units)})
-            if share_ovl > 0:
-                a2 = units / (share_ovl * ms_per_step * 1e-3) / scale
-                o["in_step"].update({"achieved": round(a2, 3), "frac": round(a2 / pk, 4)})
         t = traffic.get(fam)
         if t is not None:
             o["traffic"] = t
@@ -266,7 +262,7 @@ def rooflines(ser, ovl, ms_per_step, work, peaks, sm_max_mhz):
         res = {"bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"], "unit": d["unit"],
                "frac": d["frac"], "traffic": (d.get("traffic") or {}).get("dram_bytes_per_launch"),
                "kernel": dom, "share_of_step": d["share_of_step"], "avg_launch_ms": d["avg_launch_ms"],
-               "in_step": d["in_step"]}
+               "share_overlapped": d["share_overlapped"]}
     res["stage_share_of_step"] = {f: o["share_of_step"] for f, o in out.items()}
     res["peak_source"] = {"hbm": peaks["source"], "fp32": f"derived: 148 SMs x 128 FP32 lanes x 2 x {sm_max_mhz} MHz"}
     return res, out

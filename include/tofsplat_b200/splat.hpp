@@ -404,6 +404,19 @@ public:
         for (size_t i = 0; i < p.size(); ++i) params[i] = p[i];
     }
     long steps() const { return t_; }
+    // trainer.cpp:33-47: slot i of the new parameter layout takes the moments of old slot
+    // src[i] (stride values per slot), fresh zeros where src[i] < 0; never-stepped: no-op.
+    void reindex(const std::vector<int>& src, int stride) {
+        if (m_.empty()) return;
+        if (stride < 1) throw std::runtime_error("adam_reindex: stride must be >= 1");
+        const size_t n_old = m_.size() / (size_t)stride;
+        std::vector<int32_t> s(src.begin(), src.end());
+        std::vector<float> m2(s.size() * (size_t)stride), v2(s.size() * (size_t)stride);
+        tsb_check(tsb_adam_reindex_flat(detail::context(), TSB_HOST, m_.data(), v_.data(), n_old, s.data(), s.size(),
+                                        stride, m2.data(), v2.data()));
+        m_ = std::move(m2);
+        v_ = std::move(v2);
+    }
 
 private:
     std::vector<float> m_, v_;

@@ -58,7 +58,11 @@ enum {
     TSB_CH_PHASOR = 1u << 6,     /* (re, im) per frequency; always computed (free: 2x the quad sums) */
     TSB_CH_DISTORTION = 1u << 7, /* sum_kl w_k w_l (d_k - d_l)^2; required for a distortion upstream */
     TSB_CH_COLOR = 1u << 8,      /* RGB from the colour SH (scene created with color = 1), + bg_color T */
-    TSB_CH_FLOW = 1u << 9        /* motion accumulators + projected flow (tsb_pass_set_motion) */
+    TSB_CH_FLOW = 1u << 9,       /* motion accumulators + projected flow (tsb_pass_set_motion) */
+    TSB_CH_EXACT = 1u << 10      /* reference-exact mode: every pixel composited in fp64 (the fix-up path,
+                                    forward and backward) and the outputs also kept as fp64 planes
+                                    (TSB_OUT_F64 / TSB_OUT_EXT_F64) -- for finite-difference checks
+                                    (gradcheck.cpp); costs an fp64 walk per pixel */
 };
 
 /* CameraModel (camera.hpp:9-17).  R row-major; p_cam = R p_world + t. */
@@ -216,6 +220,12 @@ int tsb_scene_densify(tsb_scene* s, const tsb_densify_config* cfg, double scene_
 
 int tsb_adam_step_flat(tsb_ctx* ctx, int where, float* params, const float* grads, float* m, float* v, size_t n,
                        int64_t t, double lr, double beta1, double beta2, double eps);
+/* AdamState::reindex(src, stride) (trainer.hpp:25-29, trainer.cpp:33-47) on flat moment
+ * vectors: new slot i (stride values) takes old slot src[i]'s m and v, or zeros when
+ * src[i] < 0.  m / v hold n_old slots, src and the outputs n_new.  A device gather;
+ * `where` = where all five pointers live. */
+int tsb_adam_reindex_flat(tsb_ctx* ctx, int where, const float* m, const float* v, size_t n_old, const int32_t* src,
+                          size_t n_new, int32_t stride, float* m_out, float* v_out);
 
 /* ---- render pass (RenderPass, splat.hpp:97-117) ------------------------- */
 /* A pass is a reusable per-frame workspace: prepare() == the RenderPass ctor
@@ -261,7 +271,11 @@ enum {
     TSB_OUT_FLOW_BWD = 14,       /* [2][H][W] */
     TSB_OUT_FLOW_VALID = 15,     /* [2][H][W] 1 where covered and projected in front (fwd, bwd) */
     TSB_OUT_D_MOTION_FWD_ACC = 16, /* [3][H][W] FlowLossResult::d_motion_fwd_acc (tsb_pass_flow_loss) */
-    TSB_OUT_D_MOTION_BWD_ACC = 17  /* [3][H][W] */
+    TSB_OUT_D_MOTION_BWD_ACC = 17, /* [3][H][W] */
+    TSB_OUT_F64 = 18,            /* TSB_CH_EXACT: every plane of outputs 0-9 in fp64, [6*n_freq+5][H][W] double:
+                                    quad (4*n_freq), depth_raw, depth, weight, T, phasor (2*n_freq), distortion */
+    TSB_OUT_EXT_F64 = 19         /* TSB_CH_EXACT with colour / flow: [9][H][W] double (colour 3,
+                                    motion_fwd_acc 3, motion_bwd_acc 3) */
 };
 /* Device pointer and byte size of a pass-owned buffer. */
 int tsb_pass_output(tsb_pass* p, int which, void** dptr, size_t* bytes);
@@ -334,7 +348,8 @@ int tsb_pass_debug_keep_screen(tsb_pass* p, int enabled);
 int tsb_pass_debug_set_list_capacity(tsb_pass* p, uint32_t entries);
 /* Pixels the fp32 raster flagged as decision-ambiguous and recomposited in fp64. */
 int tsb_pass_debug_fixups(tsb_pass* p, int32_t* count);
-/* The fixed pixels themselves: pixel index | reason << 24 (1 maha, 2 alpha, 4 T band). */
+/* The fixed pixels themselves: pixel index | reason << 24 (1 maha, 2 alpha, 4 T band, 8 T relative
+ * error bound above 1e-4 -- an almost opaque splat). */
 int tsb_pass_debug_fixup_list(tsb_pass* p, int32_t* entries, int32_t capacity, int32_t* count);
 
 /* ---- data-parallel gradient reduction (trainer.cpp:123-131 -> NCCL) ----- */

@@ -218,6 +218,11 @@ struct tsb_pass {
     int* fx_work = nullptr;
     int* fx_work_n = nullptr;
     Rec64* fx_cache = nullptr;
+    FixState* fx_state = nullptr;  // [fx_state_cap] fp64 end state of recomposited pixels (k_fixup_bwd)
+    int fx_state_cap = 0;
+    double* out64 = nullptr;       // TSB_CH_EXACT: fp64 output planes (out64_cap pixels)
+    double* ext_out64 = nullptr;   // TSB_CH_EXACT with colour / flow: [9][H][W]
+    int out64_cap = 0, ext_out64_cap = 0;
     int frame_stamp = 0;
     // deferred settle: what was enqueued since the last check of the abort word
     bool pending = false;
@@ -894,6 +899,48 @@ int tsb_adam_step_flat(tsb_ctx* ctx, int where, float* params, const float* grad
     return TSB_OK;
 }
 
+int tsb_adam_reindex_flat(tsb_ctx* ctx, int where, const float* m, const float* v, size_t n_old, const int32_t* src,
+                          size_t n_new, int32_t stride, float* m_out, float* v_out) {
+    if (!ctx || stride < 1 || (n_new && (!src || !m_out || !v_out)) || (n_old && (!m || !v)))
+        return fail(TSB_ERR_INVALID, "adam_reindex: bad argument");
+    if (where != TSB_HOST && where != TSB_DEVICE) return fail(TSB_ERR_INVALID, "bad memory kind");
+    if (where == TSB_HOST)  // the device gather reads only valid sources
+        for (size_t i = 0; i < n_new; ++i)
+            if (src[i] >= (int64_t)n_old) return fail(TSB_ERR_INVALID, "adam_reindex: source index out of range");
+    if (n_new == 0) return TSB_OK;
+    TSB_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const size_t S = (size_t)stride;
+    if (where == TSB_DEVICE) {
+        launch_adam_reindex(m, v, src, n_new, stride, m_out, v_out, st);
+        ctx->launches++;
+        TSB_CHECK_LAUNCH();
+        return TSB_OK;
+    }
+    float* d = nullptr;
+    int32_t* ds = nullptr;
+    int rc;
+    if ((rc = dev_alloc(&d, 2 * n_old * S + 2 * n_new * S + 1)) || (rc = dev_alloc(&ds, n_new))) {
+        dev_free(d);
+        return rc;
+    }
+    float *dm = d, *dv = d + n_old * S, *dm2 = d + 2 * n_old * S, *dv2 = dm2 + n_new * S;
+    if (n_old) {
+        cudaMemcpyAsync(dm, m, sizeof(float) * n_old * S, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(dv, v, sizeof(float) * n_old * S, cudaMemcpyHostToDevice, st);
+    }
+    cudaMemcpyAsync(ds, src, sizeof(int32_t) * n_new, cudaMemcpyHostToDevice, st);
+    launch_adam_reindex(dm, dv, ds, n_new, stride, dm2, dv2, st);
+    ctx->launches++;
+    cudaMemcpyAsync(m_out, dm2, sizeof(float) * n_new * S, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(v_out, dv2, sizeof(float) * n_new * S, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    dev_free(d);
+    dev_free(ds);
+    if (e != cudaSuccess) return fail(TSB_ERR_CUDA, std::string("adam_reindex: ") + cudaGetErrorString(e));
+    return TSB_OK;
+}
+
 // ---------------------------------------------------------------------------
 // render pass
 // ---------------------------------------------------------------------------
@@ -956,6 +1003,10 @@ void free_pixels(tsb_pass* p) {
     dev_free(p->out); dev_free(p->n_contrib); dev_free(p->n_processed); dev_free(p->last);
     dev_free(p->T_pre); dev_free(p->d_quad); dev_free(p->target); dev_free(p->flagged);
     dev_free(p->st_f); dev_free(p->st_i); dev_free(p->up_extra); dev_free(p->dist3); dev_free(p->st_d);
+    dev_free(p->fx_state);
+    p->fx_state_cap = 0;
+    dev_free(p->out64); dev_free(p->ext_out64);
+    p->out64_cap = p->ext_out64_cap = 0;
 }
 
 int ensure_gauss(tsb_pass* p, int n) {
@@ -993,8 +1044,10 @@ int ensure_pixels(tsb_pass* p, int W, int H, int ntiles, int nblocks) {
             (rc = dev_alloc(&p->target, (size_t)8 * npx)) || (rc = dev_alloc(&p->flagged, npx)) ||
             (rc = dev_alloc(&p->st_f, (size_t)kFwdStatePlanes * npx)) || (rc = dev_alloc(&p->st_i, (size_t)3 * npx)) ||
             (rc = dev_alloc(&p->up_extra, (size_t)8 * npx)) || (rc = dev_alloc(&p->dist3, (size_t)3 * npx)) ||
-            (rc = dev_alloc(&p->st_d, (size_t)3 * npx)))
+            (rc = dev_alloc(&p->st_d, (size_t)3 * npx)) ||
+            (rc = dev_alloc(&p->fx_state, std::min(npx, kFixStateCap))))
             return rc;
+        p->fx_state_cap = std::min(npx, kFixStateCap);
         p->px_cap = npx;
     }
     if (nblocks > p->blk_cap) {
@@ -1080,6 +1133,7 @@ PixK pixk(tsb_pass* p) {
     px.d_quad = p->d_quad;
     px.dist3 = (p->channels & TSB_CH_DISTORTION) ? p->dist3 : nullptr;
     px.flagged = p->flagged;
+    px.out64 = (p->channels & TSB_CH_EXACT) ? p->out64 : nullptr;
     px.n_flagged = p->counters + 1;
     px.abort = p->counters + 2;
     return px;
@@ -1209,6 +1263,7 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     for (int c = 0; c < 8; ++c) O.bg_quad[c] = c < 4 * p->nf ? opt->bg_quad[c] : 0.0;
     for (int c = 0; c < 4; ++c) O.bg_phasor[c] = c < 2 * p->nf ? opt->bg_phasor[c] : 0.0;
     O.dist = (opt->channels & TSB_CH_DISTORTION) ? 1 : 0;
+    O.exact = (opt->channels & TSB_CH_EXACT) ? 1 : 0;
     for (int c = 0; c < 3; ++c) O.bg_color[c] = opt->bg_color[c];
     p->ntiles = O.tiles_x * O.tiles_y;
     if (p->ntiles > 65536) return fail(TSB_ERR_UNSUPPORTED, "render: more than 65536 tiles");
@@ -1236,6 +1291,27 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
         return rc;
     p->has_mf = p->has_mb = false;  // RenderInput::motion_* belong to one frame
     if ((p->channels & (TSB_CH_COLOR | TSB_CH_FLOW)) && (rc = ensure_ext(p))) return rc;
+    if (p->channels & TSB_CH_EXACT) {  // every pixel recomposited (and back-propagated) in fp64
+        const int npx = p->W * p->H;
+        if (p->fx_state_cap < npx) {
+            dev_free(p->fx_state);
+            p->fx_state_cap = 0;
+            if ((rc = dev_alloc(&p->fx_state, npx))) return rc;
+            p->fx_state_cap = npx;
+        }
+        if (p->out64_cap < npx) {
+            dev_free(p->out64);
+            p->out64_cap = 0;
+            if ((rc = dev_alloc(&p->out64, (size_t)out_channels(2) * npx))) return rc;
+            p->out64_cap = npx;
+        }
+        if ((p->channels & (TSB_CH_COLOR | TSB_CH_FLOW)) && p->ext_out64_cap < npx) {
+            dev_free(p->ext_out64);
+            p->ext_out64_cap = 0;
+            if ((rc = dev_alloc(&p->ext_out64, (size_t)9 * npx))) return rc;
+            p->ext_out64_cap = npx;
+        }
+    }
 
     // The device work (preprocess + depth sort) is deferred: it becomes the head of
     // the forward graph, or is issued eagerly by flush_prepare when something reads
@@ -1321,6 +1397,8 @@ FixupK fixk(tsb_pass* p) {
     fx.work = p->fx_work;
     fx.work_n = p->fx_work_n;
     fx.cache = p->fx_cache;
+    fx.state = p->fx_state;
+    fx.state_cap = p->fx_state_cap;
     return fx;
 }
 
@@ -1369,6 +1447,7 @@ ExtK extk(tsb_pass* p) {
     E.d_motion = p->ext_dmotion;
     E.bg_part = p->ext_bg_part;
     E.flow = (p->channels & TSB_CH_FLOW) ? 1 : 0;
+    E.out64 = (p->channels & TSB_CH_EXACT) ? p->ext_out64 : nullptr;
     return E;
 }
 
@@ -1595,8 +1674,9 @@ std::string forward_key(tsb_pass* p, bool loss, const ChW& chw) {
     const void* ptrs[] = {p->sorted, p->rect, p->counters, p->tile_blocks_done, p->hist, p->tile_len, p->tile_start,
                           p->vals, p->list_off, p->ranges_all, p->block_done, p->rec.A, p->rec.B, p->rec.C, p->rec.D,
                           p->st_f, p->st_d, p->st_i, p->loss_part, p->loss_dev, p->chunk_rank0, p->fx_stamp,
-                          p->fx_work, p->fx_work_n, p->fx_cache, p->frame_dev, p->pinned};
+                          p->fx_work, p->fx_work_n, p->fx_cache, p->frame_dev, p->pinned, p->fx_state};
     add(ptrs, sizeof ptrs);
+    add(&p->fx_state_cap, sizeof p->fx_state_cap);
     add(&S, sizeof S);
     add(&px, sizeof px);
     add(&p->cam, sizeof p->cam);
@@ -1911,6 +1991,13 @@ int output_ptr(tsb_pass* p, int which, void** dptr, size_t* bytes) {
             if (!p->fl_grad[k]) return fail(TSB_ERR_INVALID, "no flow-loss gradient for this direction");
             ptr = p->ext_dmacc + (size_t)3 * k * HW; b = 3 * HW * 4; break;
         }
+        case TSB_OUT_F64:
+            if (!(p->channels & TSB_CH_EXACT)) return fail(TSB_ERR_INVALID, "exact (fp64) mode not enabled");
+            ptr = p->out64; b = (size_t)out_channels(p->nf) * HW * 8; break;
+        case TSB_OUT_EXT_F64:
+            if (!(p->channels & TSB_CH_EXACT) || !(p->channels & (TSB_CH_COLOR | TSB_CH_FLOW)))
+                return fail(TSB_ERR_INVALID, "exact (fp64) mode with colour / flow not enabled");
+            ptr = p->ext_out64; b = 9 * HW * 8; break;
         default: return fail(TSB_ERR_INVALID, "unknown output");
     }
     *dptr = ptr;
@@ -1974,6 +2061,9 @@ int enqueue_backward(tsb_pass* p, const UpK& up) {
         Stage sg(p->ctx, TSB_STAGE_RASTER_BWD, st);
         launch_raster_bwd(p->rec, p->ranges_all, p->nchunks, p->vals, p->opt, p->W, p->H, p->nf, dpsi, px, up,
                           p->screen, s->d.n, p->bg_part, st);
+        // the recomposited pixels, whose backward follows their fp64 forward
+        launch_fixup_bwd(scenek(s), p->cam, p->opt, p->frame_dev, fixk(p), px, up, p->nf, p->screen, s->d.n, st);
+        p->ctx->launches += 1;
         if (ext) {  // colour / motion upstreams: adds to the same screen gradients (tsb_ext.cu)
             TSB_CUDA(cudaMemsetAsync(p->ext_dmotion, 0, sizeof(float4) * 2 * (size_t)std::max(s->d.n, 1), st));
             launch_ext_bwd(p->rec, p->opt, p->W, p->H, p->nf, p->ranges_all, p->nchunks, p->vals, px, up, E,

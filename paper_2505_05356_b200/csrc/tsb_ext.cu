@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_fwd(RecK rec, SceneK S, 
     if (m.active) {
         const int l = px.last[m.o];
         fixed = l < 0;
-        last = l & 0x7fffffff;
+        last = l & kLastMask;
     }
     const int bmax = block_max(last, smax);
     const FrameK F = fd->F;
@@ -159,7 +159,8 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_fwd(RecK rec, SceneK S, 
             __syncthreads();
             const int jmax = min(nb, last - ((int)rg.z + b0));
             for (int j = 0; j < jmax; ++j) {
-                float w;
+                double wd;
+                double cx[3] = {0.0, 0.0, 0.0};
                 if (!fixed) {  // the forward's fp32 decisions, bit for bit
                     const float4 A = sA[j], B = sB[j];
                     Eval ev;
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_fwd(RecK rec, SceneK S, 
                     if (ev.maha - O.cut2_f > 0.f) continue;
                     eval_alpha(B, ev);
                     if (ev.alpha - O.alpha_thr_f < 0.f) continue;
-                    w = ev.alpha * T;
+                    wd = ev.alpha * T;
                     T = T * (1.f - ev.alpha);
                 } else {  // the fix-up's fp64 decisions (k_fixup, tsb_geom.cu)
                     const int g = (int)sg[j];
@@ -178,14 +179,20 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_fwd(RecK rec, SceneK S, 
                     if (maha > O.cut2 || maha < 0.0) continue;
                     const double alpha = r.m1.y * exp(-0.5 * maha);
                     if (alpha < O.alpha_thr) continue;
-                    w = (float)(alpha * Td);
+                    wd = alpha * Td;
+                    if (!E.out64) wd = (double)(float)wd;
                     Td *= 1.0 - alpha;
+                    if (E.out64 && E.col) {  // reference-exact mode: the fp64 clamped colour
+                        Color64 c64;
+                        color64(S, C, F, g, c64);
+                        for (int ch = 0; ch < 3; ++ch) cx[ch] = clampd(c64.raw[ch], 0.0, 1.0);
+                    }
                 }
                 const float4 cc = sC[j], mf = sMf[j], mb = sMb[j];
-                const double wd = w;
-                acc[0] = fma(wd, (double)cc.x, acc[0]);
-                acc[1] = fma(wd, (double)cc.y, acc[1]);
-                acc[2] = fma(wd, (double)cc.z, acc[2]);
+                const bool c64 = fixed && E.out64;
+                acc[0] = fma(wd, c64 ? cx[0] : (double)cc.x, acc[0]);
+                acc[1] = fma(wd, c64 ? cx[1] : (double)cc.y, acc[1]);
+                acc[2] = fma(wd, c64 ? cx[2] : (double)cc.z, acc[2]);
                 acc[3] = fma(wd, (double)mf.x, acc[3]);
                 acc[4] = fma(wd, (double)mf.y, acc[4]);
                 acc[5] = fma(wd, (double)mf.z, acc[5]);
@@ -200,6 +207,11 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_fwd(RecK rec, SceneK S, 
     const double Tfin = px.out[ch_T(nf) * HW + o];
     for (int c = 0; c < 3; ++c) E.out[c * HW + o] = (float)(acc[c] + O.bg_color[c] * Tfin);
     for (int c = 3; c < 9; ++c) E.out[c * HW + o] = (float)acc[c];
+    if (E.out64) {  // reference-exact mode: fp64 planes, with the fix-up's fp64 T_N
+        const double T64 = fixed ? Td : Tfin;
+        for (int c = 0; c < 3; ++c) E.out64[c * HW + o] = acc[c] + O.bg_color[c] * T64;
+        for (int c = 3; c < 9; ++c) E.out64[c * HW + o] = acc[c];
+    }
     for (int c = 9; c < kExtPlanes; ++c) E.out[c * HW + o] = 0.f;
     if (!E.flow) return;
     const double SW = px.out[ch_weight(nf) * HW + o];
@@ -248,7 +260,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_bwd(RecK rec, OptK O, in
 #pragma unroll
     for (int c = 0; c < 9; ++c) u[c] = 0.f;
     if (m.active) {
-        last = px.last[o] & 0x7fffffff;
+        last = px.last[o] & kLastMask;
         Tnext = px.T_pre[o];
         const float Tf = px.out[ch_T(nf) * HW + o];
         for (int c = 0; c < 3; ++c) {

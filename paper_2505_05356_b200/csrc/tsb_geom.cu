@@ -294,7 +294,7 @@ int launch_records(const SceneK& S, const CamK& C, const OptK& O, const FrameDev
 // walks them in order exactly as splat.cpp:260-297 does.
 // ---------------------------------------------------------------------------
 struct FixupAcc {
-    double T, SW, SD, Tpre, accQ[8];
+    double T, SW, SD, Tpre, Tpre_le, accQ[8];  // Tpre_le: T before the entry that made T exactly 0
     double dref, SDs, SD2s;  // distortion moments about the first contributor's depth
     int nc, processed, last_eff;
     bool done;
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(128) k_fixup_mark(OptK O, FixupK fx, PixK px, 
         const int pix = px.flagged[i] & 0xffffff;
         const int x = pix % W, y = pix / W;
         const int tile = (y / O.ts) * O.tiles_x + (x / O.ts);
-        const int limit = (px.last[pix] & 0x7fffffff) + 64;
+        const int limit = (px.last[pix] & kLastMask) + 64;
         for (int ch = 0; ch < fx.nchunks; ++ch) {
             const uint4 rg = fx.ranges_all[(size_t)ch * ntiles + tile];
             if (rg.w || (int)rg.z >= limit) break;
@@ -438,7 +438,10 @@ __device__ __forceinline__ void fixup_batch(const SceneK& S, const CamK& C, cons
         const int last_lane = 31 - __clz(mm);
         a.Tpre = __shfl_sync(0xffffffffu, mine ? slot[lane].Tpre : 0.0, last_lane);
     }
-    if (le >= 0 && a.last_eff < 0) a.last_eff = __shfl_sync(0xffffffffu, entry_idx, le) + 1;
+    if (le >= 0 && a.last_eff < 0) {
+        a.last_eff = __shfl_sync(0xffffffffu, entry_idx, le) + 1;
+        a.Tpre_le = slot[le].Tpre;
+    }
     if (jterm < 32) {
         a.processed = __shfl_sync(0xffffffffu, entry_idx, jterm) + 1;
         a.done = true;
@@ -467,17 +470,19 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, const F
         const int tx = x / O.ts, ty = y / O.ts;
         const int tile = ty * O.tiles_x + tx;
         FixupAcc a;
-        a.T = 1.0; a.SW = 0.0; a.SD = 0.0; a.Tpre = 1.0;
+        a.T = 1.0; a.SW = 0.0; a.SD = 0.0; a.Tpre = 1.0; a.Tpre_le = 1.0;
         a.dref = 0.0; a.SDs = 0.0; a.SD2s = 0.0;
         for (int c = 0; c < 8; ++c) a.accQ[c] = 0.0;
         a.nc = 0; a.processed = 0; a.last_eff = -1; a.done = false;
         int scan_from = -1;  // rank where the tile stopped being binned
+        int list_end = 0;    // entries of the chunk lists the walk reached
         for (int ch = 0; ch < fx.nchunks && !a.done; ++ch) {
             const uint4 rg = fx.ranges_all[(size_t)ch * ntiles + tile];  // (start, len, cum, skipped)
             if (rg.w) {
                 scan_from = fx.chunk_rank0[ch];
                 break;
             }
+            list_end = (int)(rg.z + rg.y);
             const uint32_t end = rg.x + rg.y;
             for (uint32_t b = rg.x; b < end && !a.done; b += 32) {
                 const uint32_t e = b + lane;
@@ -529,11 +534,35 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, const F
                 px.dist3[HW + o] = a.SDs;
                 px.dist3[2 * HW + o] = a.SD2s;
             }
+            if (px.out64) {  // reference-exact mode: the same planes in fp64
+                double* q = px.out64;
+                for (int c = 0; c < 4 * nf; ++c) q[c * HW + o] = a.accQ[c] + O.bg_quad[c] * a.T * a.T;
+                q[ch_depth_raw(nf) * HW + o] = a.SD;
+                q[ch_depth(nf) * HW + o] = a.SW > O.cov_eps ? a.SD / a.SW : __longlong_as_double(0x7ff8000000000000ll);
+                q[ch_weight(nf) * HW + o] = a.SW;
+                q[ch_T(nf) * HW + o] = a.T;
+                for (int f = 0; f < nf; ++f) {
+                    q[(ch_phasor(nf) + 2 * f + 0) * HW + o] = 2.0 * a.accQ[4 * f + 1] + O.bg_phasor[2 * f + 0] * a.T * a.T;
+                    q[(ch_phasor(nf) + 2 * f + 1) * HW + o] = 2.0 * a.accQ[4 * f + 0] + O.bg_phasor[2 * f + 1] * a.T * a.T;
+                }
+                q[ch_distortion(nf) * HW + o] = 2.0 * (a.SW * a.SD2s - a.SDs * a.SDs);
+            }
             if (px.n_contrib) px.n_contrib[o] = a.nc;
             if (px.n_processed) px.n_processed[o] = a.processed;
             const int le = a.last_eff >= 0 ? a.last_eff : a.processed;
-            px.last[o] = le | (int)0x80000000;
-            px.T_pre[o] = (float)a.Tpre;
+            const double Tpre = a.last_eff >= 0 ? a.Tpre_le : a.Tpre;
+            // the fp64 backward replays this walk (its rank-scan part from shared memory)
+            const bool bwd64 = i < fx.state_cap && le - list_end <= kFixBwdTail;
+            if (bwd64) {
+                FixState f;
+                f.T = a.T; f.Tpre = Tpre; f.SW = a.SW;
+                f.dref = a.dref; f.SDs = a.SDs; f.SD2s = a.SD2s;
+                f.n_list = list_end;
+                f.scan_from = scan_from;
+                fx.state[i] = f;
+            }
+            px.last[o] = le | kLastFixed | (bwd64 ? kLastBwd64 : 0);
+            px.T_pre[o] = (float)Tpre;
         }
     }
 }
@@ -544,6 +573,245 @@ void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameDev*
     k_fixup_mark<<<148, 128, 0, st>>>(O, fx, px, C.W, fd);
     k_fixup_records<<<148, 128, 0, st>>>(S, C, O, fd, fx);
     k_fixup<<<148, 128, 0, st>>>(S, C, O, fd, fx, px, nf);
+}
+
+// ---------------------------------------------------------------------------
+// k_fixup_bwd: fp64 backward of the pixels k_fixup recomposited (splat.cpp:374-519,
+// every ToF upstream of BufferGrads), so their gradients follow the fp64 decisions
+// and transmittances of their fp64 forward (SURVEY H1 for the backward; the fp32
+// raster backward skips them).  One warp per pixel walks its entries back to front,
+// 32 at a time (lane j = the j-th entry from the back), each lane evaluating its
+// entry's fp64 record exactly as k_fixup did.  The reverse sweep's recursions are
+// warp scans instead of a serial loop:
+//   T before entry k      T_k = T_{k+1} / (1 - alpha_k)         (product scan; the
+//                         pixel's last contributor starts from its stored T before it)
+//   T^2-weighted channels A_k = alpha_{k+1} U_{k+1} + (1 - alpha_{k+1})^2 A_{k+1}
+//   T-weighted channels   B_k = alpha_{k+1} v_{k+1} + (1 - alpha_{k+1}) B_{k+1}
+//   transmittance         R_k = prod_{j > k} (1 - alpha_j)
+// (A and B are affine maps composed across lanes), with
+//   d alpha_k = T_k^2 (U_k + 2 (alpha_k - 1) A_k) + T_k (v_k - B_k) - up_T T_k R_k,
+//   U_k = coef_k (upQ . basis_k + 2 upP . (cos, sin)_k),
+//   v_k = up_draw d_k + up_w + up_dd phi_k,  phi_k = 2 sum_j w_j (d_j - d_k)^2.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ double scan_mul_incl(double v, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double o = __shfl_up_sync(kFull, v, d);
+        if (lane >= d) v *= o;
+    }
+    return v;
+}
+
+// inclusive composition in lane order of x -> a x + b: lane j ends with f_j o ... o f_0
+__device__ __forceinline__ void scan_affine_incl(double& a, double& b, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double ao = __shfl_up_sync(kFull, a, d), bo = __shfl_up_sync(kFull, b, d);
+        if (lane >= d) {
+            b = fma(a, bo, b);
+            a *= ao;
+        }
+    }
+}
+
+struct BwdPix {
+    double us[2], uc[2], dpsi[2];  // per frequency: upstream weights of (sin, cos); d psi / d depth
+    double uDraw, uW, uDD, uT;
+    double SW, dref, SDs, SD2s;
+    double Tnext, A, B, R;          // carried across batches (back to front)
+    bool first;                     // the pixel's last contributor not reached yet
+};
+
+__device__ __forceinline__ void fixbwd_batch(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
+                                             const FixupK& fx, int stamp, int nf, int x, int y, bool is_entry, int g,
+                                             BwdPix& b, float* __restrict__ screen, int scap, int lane) {
+    bool inc = false;
+    double alpha = 0.0, G = 0.0, dx = 0.0, dy = 0.0, coef = 0.0, depth = 0.0;
+    Rec64 r;
+    if (is_entry) {  // k_fixup's decisions, same expressions
+        r = fx.stamp[g] == stamp ? fx.cache[g] : make_rec64(S, C, O, F, g);
+        if (!(x < r.rect.x || x >= r.rect.y || y < r.rect.z || y >= r.rect.w)) {
+            dx = (x + 0.5) - r.m0.x;
+            dy = (y + 0.5) - r.m0.y;
+            const double maha = r.m0.z * dx * dx + 2.0 * r.m0.w * dx * dy + r.m1.x * dy * dy;
+            if (!(maha > O.cut2 || maha < 0.0)) {
+                G = exp(-0.5 * maha);
+                alpha = r.m1.y * G;
+                if (!(alpha < O.alpha_thr)) {
+                    inc = true;
+                    coef = r.m1.z;
+                    depth = r.m1.w;
+                }
+            }
+        }
+    }
+    const unsigned cm = __ballot_sync(kFull, inc);
+    if (!cm) return;
+    const double om = inc ? 1.0 - alpha : 1.0;
+    // T before each contributor, back from the pixel's last one (its T is stored, alpha may be 1)
+    const int j0 = b.first ? __ffs(cm) - 1 : -1;
+    const double P = scan_mul_incl(lane == j0 ? 1.0 : om, lane);
+    const double Tk = b.Tnext / P;
+    double su = 0.0, sd = 0.0;
+    if (inc) {
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+            if (f >= nf) break;
+            double sn, cs;
+            sincos(phase_of_depth(depth, S.freq[f], S.c), &sn, &cs);
+            su += b.us[f] * sn + b.uc[f] * cs;
+            sd += b.dpsi[f] * (b.us[f] * cs - b.uc[f] * sn);
+        }
+    }
+    const double e = b.dref - depth;
+    const double phi = 2.0 * (b.SD2s + 2.0 * e * b.SDs + e * e * b.SW);
+    const double U = coef * su;
+    const double v = b.uDraw * depth + b.uW + b.uDD * phi;
+    // accumulators behind each entry: exclusive scans of the composed maps
+    double aA = inc ? om * om : 1.0, bA = inc ? alpha * U : 0.0;
+    double aB = inc ? om : 1.0, bB = inc ? alpha * v : 0.0;
+    scan_affine_incl(aA, bA, lane);
+    scan_affine_incl(aB, bB, lane);
+    const double Rin = scan_mul_incl(om, lane);
+    double Aex = __shfl_up_sync(kFull, fma(aA, b.A, bA), 1);
+    double Bex = __shfl_up_sync(kFull, fma(aB, b.B, bB), 1);
+    double Rex = __shfl_up_sync(kFull, Rin, 1) * b.R;
+    if (lane == 0) {
+        Aex = b.A;
+        Bex = b.B;
+        Rex = b.R;
+    }
+    if (inc) {
+        const double d_alpha = Tk * Tk * (U + 2.0 * (alpha - 1.0) * Aex) + Tk * (v - Bex) - b.uT * Tk * Rex;
+        const double w = alpha * Tk, w2 = w * Tk;
+        const double dpow = alpha * d_alpha;
+        const double g8[8] = {dpow * (r.m0.z * dx + r.m0.w * dy),
+                              dpow * (r.m0.w * dx + r.m1.x * dy),
+                              -0.5 * dx * dx * dpow,
+                              -dx * dy * dpow,
+                              -0.5 * dy * dy * dpow,
+                              G * d_alpha,
+                              w2 * su,
+                              w2 * coef * sd + b.uDraw * w + b.uDD * 4.0 * w * (b.SW * (depth - b.dref) - b.SDs)};
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            if (g8[c] != 0.0) atomicAdd(&screen[(size_t)c * scap + g], (float)g8[c]);
+    }
+    // carry to the next batch (the entries in front): values after lane 31
+    b.Tnext = __shfl_sync(kFull, Tk, 31);
+    b.A = __shfl_sync(kFull, fma(aA, b.A, bA), 31);
+    b.B = __shfl_sync(kFull, fma(aB, b.B, bB), 31);
+    b.R *= __shfl_sync(kFull, Rin, 31);
+    b.first = false;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(128) k_fixup_bwd(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd,
+                                                   FixupK fx, PixK px, UpK up, int nf, float* __restrict__ screen,
+                                                   int scap) {
+    __shared__ int tail[4][kFixBwdTail];
+    const FrameK F = fd->F;
+    const int stamp = fd->stamp;
+    const int lane = threadIdx.x & 31;
+    int* my_tail = tail[threadIdx.x >> 5];
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int count = *fx.overflow ? 0 : min(*px.n_flagged, fx.state_cap);
+    const int W = C.W, H = C.H;
+    const int ntiles = O.tiles_x * O.tiles_y;
+    const size_t HW = (size_t)W * H;
+    const int V = *fx.n_visible;
+    const uint32_t lanes_below = (1u << lane) - 1u;
+    for (int i = warp; i < count; i += nwarps) {
+        const int pix = px.flagged[i] & 0xffffff;
+        const int lw = px.last[pix];
+        if (!(lw & kLastBwd64)) continue;
+        const int last = lw & kLastMask;
+        const FixState st = fx.state[i];
+        const int x = pix % W, y = pix / W;
+        const int tx = x / O.ts, ty = y / O.ts;
+        const int tile = ty * O.tiles_x + tx;
+        const size_t o = (size_t)pix;
+        BwdPix b;
+        b.A = 0.0;
+        for (int f = 0; f < 2; ++f) {
+            b.us[f] = b.uc[f] = 0.0;
+            b.dpsi[f] = f < nf ? 4.0 * M_PI * S.freq[f] / S.c : 0.0;
+            if (f >= nf) continue;
+            if (up.quad) {
+                double q[4];
+                for (int c = 0; c < 4; ++c) {
+                    q[c] = up.quad[(4 * f + c) * HW + o];
+                    b.A += q[c] * O.bg_quad[4 * f + c];
+                }
+                b.us[f] = q[0] - q[2];
+                b.uc[f] = q[1] - q[3];
+            }
+            if (up.phasor) {
+                const double p0 = up.phasor[(2 * f + 0) * HW + o], p1 = up.phasor[(2 * f + 1) * HW + o];
+                b.A += p0 * O.bg_phasor[2 * f + 0] + p1 * O.bg_phasor[2 * f + 1];
+                b.us[f] += 2.0 * p1;
+                b.uc[f] += 2.0 * p0;
+            }
+        }
+        b.uDraw = up.depth_raw ? (double)up.depth_raw[o] : 0.0;
+        b.uW = up.weight ? (double)up.weight[o] : 0.0;
+        b.uDD = up.distortion ? (double)up.distortion[o] : 0.0;
+        b.uT = up.transm ? (double)up.transm[o] : 0.0;
+        b.SW = st.SW; b.dref = st.dref; b.SDs = st.SDs; b.SD2s = st.SD2s;
+        b.Tnext = st.Tpre;
+        b.B = 0.0;
+        b.R = 1.0;
+        b.first = true;
+        // entries [n_list, last): Gaussians covering the tile in rank order from scan_from
+        if (last > st.n_list && st.scan_from >= 0) {
+            const int need = last - st.n_list;
+            int got = 0;
+            for (int r0 = st.scan_from; r0 < V && got < need; r0 += 32) {
+                const int rk = r0 + lane;
+                int g = 0;
+                bool cov = false;
+                if (rk < V) {
+                    g = (int)sorted_at(fx.sorted_gidx, fx.ties, rk, V);
+                    const uint2 rc = fx.rect[g];
+                    const int x0 = rc.x & 0xffff, x1 = rc.x >> 16, y0 = rc.y & 0xffff, y1 = rc.y >> 16;
+                    cov = x0 / O.ts <= tx && tx <= (x1 - 1) / O.ts && y0 / O.ts <= ty && ty <= (y1 - 1) / O.ts;
+                }
+                const unsigned m = __ballot_sync(kFull, cov);
+                const int slot = got + __popc(m & lanes_below);
+                if (cov && slot < need) my_tail[slot] = g;
+                got += __popc(m);
+            }
+            __syncwarp();
+            for (int top = need - 1; top >= 0; top -= 32) {
+                const int k = top - lane;
+                fixbwd_batch(S, C, O, F, fx, stamp, nf, x, y, k >= 0, k >= 0 ? my_tail[k] : 0, b, screen, scap, lane);
+            }
+            __syncwarp();
+        }
+        // the chunk lists the forward walked, back to front
+        int ch_end = 0;
+        while (ch_end < fx.nchunks && !fx.ranges_all[(size_t)ch_end * ntiles + tile].w) ++ch_end;
+        const int lim = min(last, st.n_list);
+        for (int ch = ch_end - 1; ch >= 0; --ch) {
+            const uint4 rg = fx.ranges_all[(size_t)ch * ntiles + tile];  // (start, len, cum, skipped)
+            if ((int)rg.z >= lim || rg.y == 0) continue;
+            const int n_here = min((int)rg.y, lim - (int)rg.z);
+            for (int top = n_here - 1; top >= 0; top -= 32) {
+                const int k = top - lane;
+                fixbwd_batch(S, C, O, F, fx, stamp, nf, x, y, k >= 0, k >= 0 ? (int)fx.vals[rg.x + k] : 0, b, screen,
+                             scap, lane);
+            }
+        }
+    }
+}
+
+void launch_fixup_bwd(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd, const FixupK& fx,
+                      const PixK& px, const UpK& up, int nf, float* screen, int scap, cudaStream_t st) {
+    k_fixup_bwd<<<148, 128, 0, st>>>(S, C, O, fd, fx, px, up, nf, screen, scap);
 }
 
 // Intermediates the chain needs, recomputed in fp64 with reciprocals instead of

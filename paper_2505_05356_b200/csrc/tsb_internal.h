@@ -32,6 +32,7 @@ struct OptK {
     int sub;           // 16x16 raster blocks per tile edge = ceil(ts/16)
     float alpha_thr_f, floor_f, cut2_f, cov_eps_f;
     int dist;          // distortion channel: accumulate the shifted depth moments
+    int exact;         // TSB_CH_EXACT: every pixel goes to the fp64 fix-up
     double bg_quad[8];
     double bg_phasor[4];
     double bg_color[3];
@@ -147,6 +148,7 @@ struct PixK {
     float* T_pre;        // T before the last contributor
     float* d_quad;       // [4*nf][H][W] upstream (written by loss epilogue)
     int32_t* flagged;    // list of fp64-fixup pixels
+    double* out64;       // TSB_CH_EXACT: fp64 copy of `out` (written by k_fixup) or null
     int32_t* n_flagged;  // device counter
     const int32_t* abort;  // frame abort word (overflow / long tie run): later kernels do nothing
 };
@@ -197,6 +199,20 @@ struct Rec64 {
     int4 rect;   // x0, x1, y0, y1
 };
 
+// fp64 end state of a recomposited pixel (k_fixup), what its fp64 backward (k_fixup_bwd)
+// needs: T_N, T before the last contributor (before the alpha == 1 entry when T hit 0),
+// sum w, the distortion moments about the first contributor's depth, the number of entries
+// in the tile's chunk lists the walk covered, and where its rank scan past them began.
+struct FixState {
+    double T, Tpre, SW, dref, SDs, SD2s;
+    int n_list, scan_from;
+};
+constexpr int kFixStateCap = 1 << 16;  // recomposited pixels per frame with an fp64 backward
+constexpr int kFixBwdTail = 256;  // rank-scan entries the fp64 backward can replay per pixel
+constexpr int kLastFixed = (int)0x80000000;  // PixK::last bit 31: pixel recomposited in fp64
+constexpr int kLastBwd64 = 0x40000000;       // bit 30: its backward runs in fp64 (k_fixup_bwd)
+constexpr int kLastMask = 0x3fffffff;
+
 struct FixupK {
     const uint4* ranges_all;  // [nchunks][ntiles] (start, len, cum, skipped)
     int nchunks;
@@ -213,9 +229,13 @@ struct FixupK {
     int* work;         // [n] Gaussians queued for the record cache
     int* work_n;
     Rec64* cache;      // [n]
+    FixState* state;   // [state_cap] per flagged pixel (fix-up slot): fp64 state for k_fixup_bwd
+    int state_cap;
 };
 void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd, const FixupK& fx,
                   const PixK& px, int nf, cudaStream_t st);
+void launch_fixup_bwd(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd, const FixupK& fx,
+                      const PixK& px, const UpK& up, int nf, float* screen, int scap, cudaStream_t st);
 void launch_chain(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
                   const uint32_t* touched, float* screen, float4* grads, cudaStream_t st);
 void launch_param_cache(const SceneK& S, double* cov6, double* opac, float* cov6f, cudaStream_t st);
@@ -360,6 +380,7 @@ struct ExtK {
     const float4* mf;     // [n] motion_fwd (xyz, 0) or null (zero)
     const float4* mb;     // [n] motion_bwd or null
     float* out;           // [kExtPlanes][H][W]
+    double* out64;        // TSB_CH_EXACT: [9][H][W] fp64 colour / motion accumulators or null
     float* screen;        // [9][n] per-Gaussian d_color, d_motion_fwd, d_motion_bwd (summed over pixels)
     float4* d_motion;     // [2][n] SceneGrads::d_motion_fwd / d_motion_bwd of the last backward
     double* bg_part;      // [blocks][3] d_bg_color partials
@@ -404,5 +425,7 @@ void launch_adam(float4* params, float4* grads, float4* m, float4* v, int n, int
 
 void launch_adam_flat(float* p, const float* g, float* m, float* v, size_t n, double lr, double b1, double b2,
                       double eps, double bc1, double bc2, cudaStream_t st);
+void launch_adam_reindex(const float* m, const float* v, const int32_t* src, size_t n_new, int stride, float* m2,
+                         float* v2, cudaStream_t st);
 
 }  // namespace tsb

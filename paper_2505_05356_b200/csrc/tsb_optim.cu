@@ -169,4 +169,25 @@ void launch_adam_flat(float* p, const float* g, float* m, float* v, size_t n, do
                                       (float)(1.0 - b2), (float)eps, (float)(1.0 / bc2));
 }
 
+// AdamState::reindex (trainer.cpp:33-47): moments of new slot i are those of old slot src[i]
+// (stride values each), zero where src[i] < 0.
+__global__ void k_adam_reindex(const float* __restrict__ m, const float* __restrict__ v, const int32_t* __restrict__ src,
+                               size_t n_new, int stride, float* __restrict__ m2, float* __restrict__ v2) {
+    const size_t total = n_new * (size_t)stride;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int s = src[i / stride];
+        const size_t j = (size_t)s * stride + i % stride;
+        m2[i] = s < 0 ? 0.f : m[j];
+        v2[i] = s < 0 ? 0.f : v[j];
+    }
+}
+
+void launch_adam_reindex(const float* m, const float* v, const int32_t* src, size_t n_new, int stride, float* m2,
+                         float* v2, cudaStream_t st) {
+    const size_t total = n_new * (size_t)stride;
+    if (total == 0) return;
+    const int grid = (int)std::min<size_t>((total + 255) / 256, 148 * 8);
+    k_adam_reindex<<<grid, 256, 0, st>>>(m, v, src, n_new, stride, m2, v2);
+}
+
 }  // namespace tsb

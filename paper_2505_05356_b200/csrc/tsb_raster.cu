@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
     const size_t HW = (size_t)W * H, o = active ? (size_t)y * W + x : 0;
 
     float T = 1.f, Tpre = 1.f, SW = 0.f, SD = 0.f, dT = 0.f;  // dT: absolute error bound of T
+    float Tpre_eff = 1.f;  // T before the entry that made T exactly 0 (alpha == 1; the backward starts there)
     float accS[NF], accC[NF];
 #pragma unroll
     for (int f = 0; f < NF; ++f) accS[f] = accC[f] = 0.f;
@@ -101,6 +102,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
     if (active && !ck.first) {
         T = fs.f[0 * (size_t)fs.npx + o];
         Tpre = fs.f[1 * (size_t)fs.npx + o];
+        Tpre_eff = Tpre;
         SW = fs.f[2 * (size_t)fs.npx + o];
         SD = fs.f[3 * (size_t)fs.npx + o];
         dT = fs.f[4 * (size_t)fs.npx + o];
@@ -212,7 +214,10 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
                         } else {
                             if (fl - T < 2.f * fl * __fdividef(dT, T)) flag |= 4;  // |T - fl| < 2 fl rel err
                             const int gidx_e = (int)(rg.z + (b - rg.x) + j + 1);
-                            if (T == 0.f && last_eff < 0) last_eff = gidx_e;
+                            if (T == 0.f && last_eff < 0) {
+                                last_eff = gidx_e;
+                                Tpre_eff = Tpre;
+                            }
                             if (T < fl) {
                                 processed = gidx_e;
                                 done = true;
@@ -232,6 +237,11 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
     if (finalize && !done && *ck.n_all > *ck.n_visible) atomicOr(ck.overflow, 8);
     float lpx = 0.f;
     if (finalize) {
+        // T's relative error bound grows by ~eps alpha / (1 - alpha) per contribution: an
+        // almost opaque splat (1 - alpha lost to fp32 rounding) leaves T -- and every later
+        // weight -- too inaccurate for the 1e-4 output bar: recomposite in fp64 (reason 8)
+        if (dT > kTrelFlag * T) flag |= 8;
+        if (O.exact) flag |= 16;  // reference-exact mode: every pixel in fp64
         const float T2 = T * T;
         float q[4 * NF];
 #pragma unroll
@@ -262,7 +272,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
         if (px.n_contrib) px.n_contrib[o] = nc;
         if (px.n_processed) px.n_processed[o] = processed;
         px.last[o] = last_eff >= 0 ? last_eff : processed;
-        px.T_pre[o] = Tpre;
+        px.T_pre[o] = last_eff >= 0 ? Tpre_eff : Tpre;
         fs.i[1 * (size_t)fs.npx + o] = 1;  // done (read by later chunks only if the block is not done)
         if (flag) {
             const int slot = atomicAdd(px.n_flagged, 1);
@@ -278,7 +288,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
         }
     } else if (!was_done) {
         fs.f[0 * (size_t)fs.npx + o] = T;
-        fs.f[1 * (size_t)fs.npx + o] = Tpre;
+        fs.f[1 * (size_t)fs.npx + o] = last_eff >= 0 ? Tpre_eff : Tpre;
         fs.f[2 * (size_t)fs.npx + o] = SW;
         fs.f[3 * (size_t)fs.npx + o] = SD;
         fs.f[4 * (size_t)fs.npx + o] = dT;
@@ -395,7 +405,8 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
 #pragma unroll
     for (int c = 0; c < 6 * NF; ++c) bgc[c] = 0.f;
     if (active) {
-        last = px.last[o] & 0x7fffffff;
+        const int l = px.last[o];
+        last = (l & kLastBwd64) ? 0 : (l & kLastMask);  // recomposited pixels: k_fixup_bwd (fp64)
         Tnext = px.T_pre[o];
         const float Tf = px.out[ch_T(NF) * HW + o];
         const float Tf2 = Tf * Tf;

@@ -91,6 +91,7 @@ class RenderOptions:
     color: bool = False       # RenderChannels::color (scene created with color=True)
     flow: bool = False        # RenderChannels::flow (motions via RenderPass.set_motion)
     bg_color: Sequence[float] = (0.0, 0.0, 0.0)
+    exact: bool = False       # reference-exact mode (TSB_CH_EXACT): every pixel in fp64, fp64 output planes
 
     def to_abi(self) -> _abi.RenderOptions:
         o = _abi.RenderOptions()
@@ -103,7 +104,8 @@ class RenderOptions:
         o.channels = _abi.CH_QUAD | _abi.CH_DEPTH | _abi.CH_WEIGHT | _abi.CH_TRANSM | (
             _abi.CH_COUNTS if self.counts else 0) | (_abi.CH_FULL_LISTS if self.full_lists else 0) | (
             _abi.CH_PHASOR) | (_abi.CH_DISTORTION if self.distortion else 0) | (
-            _abi.CH_COLOR if self.color else 0) | (_abi.CH_FLOW if self.flow else 0)
+            _abi.CH_COLOR if self.color else 0) | (_abi.CH_FLOW if self.flow else 0) | (
+            _abi.CH_EXACT if self.exact else 0)
         bq = np.zeros(8)
         b = np.asarray(self.bg_quad, dtype=np.float64).reshape(-1)[:8]
         bq[: b.size] = b
@@ -451,6 +453,11 @@ class RenderPass:
             check(lib().tsb_pass_backward(self._h, _abi.TSB_HOST, None))
         return self
 
+    def backward_ext(self, **upstreams):
+        """RenderPass::backward(BufferGrads) with any of the BufferGrads images (alias of
+        backward_buffers, whose keyword names it takes)."""
+        return self.backward_buffers(**upstreams)
+
     def backward_buffers(self, d_quad=None, d_phasor=None, d_depth_raw=None, d_weight=None,
                          d_distortion=None, d_transmittance=None, d_color=None, d_motion_fwd_acc=None,
                          d_motion_bwd_acc=None):
@@ -543,7 +550,7 @@ class RenderPass:
 
     def download(self, which: int, dtype=np.float32, shape=None):
         _, nb = self.output_ptr(which)
-        a = np.empty(nb // 4, dtype=dtype)
+        a = np.empty(nb // np.dtype(dtype).itemsize, dtype=dtype)
         check(lib().tsb_pass_download(self._h, which, a.ctypes.data, nb))
         return a.reshape(shape) if shape is not None else a
 
@@ -577,6 +584,10 @@ class RenderPass:
             out["flow_fwd"] = self.download(_abi.OUT_FLOW_FWD, shape=(2, H, W))
             out["flow_bwd"] = self.download(_abi.OUT_FLOW_BWD, shape=(2, H, W))
             out["flow_valid"] = self.download(_abi.OUT_FLOW_VALID, shape=(2, H, W))
+        if self.options.exact:
+            out["f64"] = self.download(_abi.OUT_F64, np.float64, (6 * nf + 5, H, W))
+            if self.options.color or self.options.flow:
+                out["ext_f64"] = self.download(_abi.OUT_EXT_F64, np.float64, (9, H, W))
         if self.options.counts:
             out["n_contrib"] = self.download(_abi.OUT_N_CONTRIB, np.int32, (H, W))
             out["n_processed"] = self.download(_abi.OUT_N_PROCESSED, np.int32, (H, W))
@@ -605,6 +616,12 @@ class RenderPass:
         r = np.zeros((max(v, 1), 12), np.float32)
         check(lib().tsb_pass_debug_records(self._h, _ptr(r)))
         return r[:v]
+
+    def debug_keep_screen(self, enabled: bool = True):
+        """Keep a copy of every following backward's screen-space gradients (the chain
+        kernel consumes them); needed before debug_screen_grads."""
+        check(lib().tsb_pass_debug_keep_screen(self._h, 1 if enabled else 0))
+        return self
 
     def debug_screen_grads(self):
         """Per-rank screen-space gradients of the last backward (d_mean2d x/y, d_conic a/b/c,

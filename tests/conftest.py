@@ -11,3 +11,17 @@ sys.path.insert(0, str(ROOT))
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs the CUDA path through the C ABI)")
     config.addinivalue_line("markers", "slow: long-running CPU test")
+
+
+def pytest_sessionfinish(session, exitstatus):
+    path = os.environ.get("TSB_PARITY_REPORT")
+    if not path:
+        return
+    try:
+        from helpers import REPORT
+    except Exception:
+        return
+    if REPORT:
+        import json
+        Path(path).parent.mkdir(parents=True, exist_ok=True)
+        Path(path).write_text(json.dumps(REPORT, indent=1, sort_keys=True))

@@ -243,6 +243,16 @@ static void adam_steps() {
     std::vector<double> q = {0, 0, 0};
     st2.step(q, {2.0, -0.5, 1e-3}, 0.01, ap);
     CHECK(close_rel(q[0], -0.01, 1e-6) && close_rel(q[1], 0.01, 1e-6) && close_rel(q[2], -0.01, 1e-6));
+    // test_trainer.cpp:50-70: reindex copies and clears moments
+    AdamState st3;
+    std::vector<double> p3 = {0, 0, 0, 0};  // two gaussians, stride 2
+    st3.step(p3, {1.0, 2.0, 3.0, 4.0}, 0.1, ap);
+    st3.reindex({1, 1, -1}, 2);  // keep gaussian 1, clone gaussian 1, fresh slot
+    std::vector<double> p4(6, 0.0);
+    st3.step(p4, std::vector<double>(6, 0.0), 0.1, ap);  // zero grads: moments decay but stay aligned
+    CHECK(p4[0] == p4[2] && p4[1] == p4[3] && p4[0] != 0.0);
+    CHECK(p4[4] == 0.0 && p4[5] == 0.0);
+    CHECK(st3.steps() == 2);
 }
 
 // Colour channel + background colour gradient (test_splat.cpp:62-101, colour parts).

@@ -48,3 +48,19 @@ def gpu_scene(tsb, ctx, gset, tof):
 def oracle_sorted_lists(op):
     off, ids = op.tile_lists()
     return off, ids
+
+
+# SURVEY App. D figures recorded by the parity tests (written by conftest at session end
+# to $TSB_PARITY_REPORT when set): per test and quantity, the max and 99.99th-percentile
+# relative error under the App. D floor (1e-6 * max|oracle| for images, 1e-4 * max for
+# gradient groups).
+REPORT = {}
+
+
+def app_d(a, b, floor_frac=1e-6):
+    return {"max": rel_err(a, b, floor_frac), "p9999": rel_err_quantile(a, b, floor_frac, 0.9999),
+            "floor": floor_frac}
+
+
+def record(test: str, quantity: str, stats) -> None:
+    REPORT.setdefault(test, {})[quantity] = stats

@@ -1,0 +1,367 @@
+"""Parity of the B200 path at the BASELINE.json shapes, against the
+CPU oracle on the same seeded inputs, through the C ABI:
+
+* c3 (1 M dynamic Gaussians, 640x480): three frames of the sweep (t = 0, 0.5, 1) on the
+  headline path (nearest-prefix depth order, lean preprocess, early-terminated binning):
+  every float output and the per-pixel counts; the full-list render's order, rects, tile
+  lists and ranges bit for bit.
+* c2 (500 k, 640x576, 30 + 60 MHz, 8 frames / iteration): two training iterations --
+  loss, every gradient group (incl. keyframe motion), Adam on all six groups with a
+  non-uniform learning-rate table, and the densify statistic (trainer.cpp:18-31,
+  339-384).
+* c4 (2 M, 1024x1024): one frame forward + backward.
+* a posed camera (R != I, t != 0; camera.hpp:15-25) and the gradcheck render options
+  (alpha threshold 0, transmittance floor 0, sigma 6; gradcheck.cpp:77-81) with
+  opacity-1 splats (SURVEY H2's alpha = 1 hazard).
+
+Tolerances (north_star): raw samples and images 1e-4 relative, gradients 1e-3 relative.
+The App. D max and 99.99th-percentile relative errors are recorded per quantity
+(helpers.REPORT -> $TSB_PARITY_REPORT)."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+
+from helpers import app_d, gpu_scene, oracle_scene, record, rel_err, rel_err_quantile
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4
+GRAD_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def tsb():
+    import paper_2505_05356_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(tsb):
+    return tsb.Context(0)
+
+
+def check_image(test, name, a, b, floor=1e-6):
+    """App. D: 99.99th percentile of the relative error under the 1e-6*max floor below
+    1e-4; every value at or above 1e-3*max within 1e-4; for raw samples and phasors also
+    an absolute error below 2e-6*max (they are +-sin/cos sums that can cancel far below
+    their terms' size)."""
+    st = app_d(a, b, floor)
+    record(test, name, st)
+    assert st["p9999"] < IMG_TOL, (name, st)
+    assert rel_err(a, b, 1e-3) < IMG_TOL, name
+    if name.startswith(("quad", "phasor")):
+        m = np.isfinite(b)
+        assert np.abs(np.asarray(a, np.float64)[m] - b[m]).max() <= 2e-6 * np.abs(b[m]).max(), name
+
+
+def check_grad(test, name, a, b):
+    st = app_d(a, b, 1e-4)
+    record(test, name, st)
+    assert st["max"] < GRAD_TOL, (name, st)
+
+
+def compare_forward(test, out, ref, f=0, floor=1e-6):
+    assert np.array_equal(out["n_contrib"], ref["n_contrib"]), \
+        f"contributor counts differ at {np.argwhere(out['n_contrib'] != ref['n_contrib'])[:5]}"
+    assert np.array_equal(out["n_processed"], ref["n_processed"]), "termination indices differ"
+    check_image(test, f"quad_f{f}", out["quad"][4 * f:4 * f + 4], ref["quad"], floor)
+    check_image(test, f"phasor_f{f}", out["phasor"][2 * f:2 * f + 2], ref["phasor"], floor)
+    if f == 0:
+        for k in ("depth_raw", "depth", "weight", "transmittance"):
+            check_image(test, k, out[k], ref[k], floor)
+
+
+def quad_loss(ref_quad, target, weight=0.25):
+    """trainer.cpp:210-219 / losses.cpp:9-25: sum_m w mse(q_m, t_m) and its d_quad."""
+    loss, d = 0.0, np.zeros_like(ref_quad)
+    for m in range(ref_quad.shape[0]):
+        v, g = orc.mse(ref_quad[m], target[m].astype(np.float64))
+        loss += weight * v
+        d[m] = weight * g
+    return loss, d
+
+
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("t", [0.0, 0.5, 1.0])
+def test_c3_full_size_frame(tsb, ctx, t):
+    from paper_2505_05356_b200 import synthetic
+    test = f"c3_1M_t{t}"
+    cfg = synthetic.config("c3")
+    frame = tsb.frame_for_time(t, 2)
+    scene = gpu_scene(tsb, ctx, cfg.scene, cfg.tof)
+    opts = tsb.RenderOptions(counts=True)
+    rp = tsb.RenderPass(ctx).prepare(scene, cfg.camera, opts, frame).forward()  # the bench's path
+    out = rp.outputs()
+    op = orc.OraclePass(oracle_scene(cfg.scene, frame, cfg.tof), cfg.camera, opts)
+    ref = op.forward()
+    assert rp.visible_count() == op.visible_count()
+    compare_forward(test, out, ref)
+    # integer intermediates on a full-list render of the same frame
+    full = tsb.RenderPass(ctx).prepare(scene, cfg.camera, tsb.RenderOptions(counts=True, full_lists=True),
+                                       frame).forward()
+    gp, oprep = full.debug_prepared(), op.prepared()
+    assert np.array_equal(gp["gidx"], oprep["gidx"]), "global (depth, index) order differs"
+    assert np.array_equal(gp["rect"], oprep["rect"]), "tile rects differ"
+    assert full.num_keys() == op.num_keys()
+    goff, gids = full.debug_tiles()
+    ooff, oids = op.tile_lists()
+    assert np.array_equal(goff, ooff), "tile ranges differ"
+    assert np.array_equal(gids, oids), "per-tile lists differ"
+    fo = full.outputs()
+    for k in out:  # early-terminated binning + prefix order vs full lists: identical bits
+        assert np.array_equal(out[k], fo[k], equal_nan=True), k
+    record(test, "integers", {"visible": int(op.visible_count()), "keys": int(op.num_keys()),
+                              "fixup_pixels": int(rp.debug_fixups()), "bit_exact": True})
+
+
+# ---------------------------------------------------------------------------------------
+C2_LR = dict(position=2e-3, log_scale=5e-3, rotation=1e-3, opacity=0.05, reflectivity=1.6e-4, motion=3e-4)
+
+
+def test_c2_full_size_training_iterations(tsb, ctx):
+    """Two c2 iterations (8 frames each, both frequencies): per-iteration loss and summed
+    gradients of every group vs the oracle; Adam on all six groups with per-group learning
+    rates; params after each step; densify statistic (sum over both iterations)."""
+    from paper_2505_05356_b200 import synthetic
+    test = "c2_500k_2freq_8frames"
+    cfg = synthetic.config("c2")
+    g, tof, cam, frames = cfg.scene, cfg.tof, cfg.camera, cfg.frames
+    H, W = cam.height, cam.width
+    nf = len(tof.frequencies)
+    assert nf == 2 and len(frames) == 8
+    opts = tsb.RenderOptions(counts=True)
+    # targets: renders of the seed-1 moving scene (incl. the rotating rod) -- input data
+    tscene = gpu_scene(tsb, ctx, cfg.target, tof)
+    trp = tsb.RenderPass(ctx)
+    targets = [trp.prepare(tscene, cam, opts, fr).forward().outputs()["quad"].astype(np.float32) for fr in frames]
+    tscene.close()
+
+    scene = gpu_scene(tsb, ctx, g, tof)
+    passes = [tsb.RenderPass(ctx) for _ in range(4)]
+    lr = tsb.LrTable(**C2_LR, color=1e-3)
+    groups = ("position", "log_scale", "rotation", "opacity_logit", "reflectivity_dc", "motion")
+    lr_of = {"position": lr.position, "log_scale": lr.log_scale, "rotation": lr.rotation,
+             "opacity_logit": lr.opacity, "reflectivity_dc": lr.reflectivity, "motion": lr.motion}
+    m_state = {k: None for k in groups}
+    v_state = {k: None for k in groups}
+    stat_ref = np.zeros(g.n)
+    for it in range(2):
+        prm = scene.get_params()  # fp32 params the GPU renders; the oracle reads the same values
+        cur = synthetic.GaussianSet(prm["position"], prm["log_scale"], prm["rotation"], prm["opacity_logit"],
+                                    prm["reflectivity_dc"], prm["motion"])
+        for i, fr in enumerate(frames):
+            rp = passes[i % len(passes)]
+            rp.prepare(scene, cam, opts, fr)
+            rp.forward_loss(targets[i], [0.25] * (4 * nf), sync=False)
+            rp.backward()
+        gr = scene.grads()
+        # oracle: two reference renders (one per frequency) per frame, grads summed and chained
+        # through the keyframe lerp (trainer.cpp:259-279, 313-331)
+        want = {"position": np.zeros((g.n, 3)), "log_scale": np.zeros((g.n, 3)), "rotation": np.zeros((g.n, 4)),
+                "opacity_logit": np.zeros(g.n), "reflectivity_dc": np.zeros(g.n),
+                "motion": np.zeros_like(g.motion, dtype=np.float64)}
+        loss = 0.0
+        for i, fr in enumerate(frames):
+            k, w = fr
+            for f in range(nf):
+                op = orc.OraclePass(oracle_scene(cur, fr, tof, f), cam, opts)
+                ref = op.forward()
+                if it == 0 and i == 0:
+                    rp0 = tsb.RenderPass(ctx).prepare(scene, cam, opts, fr).forward()
+                    compare_forward(test, rp0.outputs(), ref, f)
+                    rp0.close()
+                lv, dq = quad_loss(ref["quad"], targets[i][4 * f:4 * f + 4])
+                loss += lv
+                og = op.backward(d_quad=dq)
+                want["position"] += og["d_position"]
+                want["motion"][k] += (1 - w) * og["d_position"]
+                want["motion"][k + 1] += w * og["d_position"]
+                want["log_scale"] += og["d_log_scale"]
+                want["rotation"] += og["d_rotation"]
+                want["opacity_logit"] += og["d_opacity_logit"]
+                want["reflectivity_dc"] += og["d_refl_sh"][:, 0]
+                del op
+        record(test, f"loss_it{it}", {"gpu": gr["loss"], "oracle": loss, "rel": abs(gr["loss"] - loss) / loss})
+        assert gr["loss"] == pytest.approx(loss, rel=1e-5)
+        got = {"position": gr["d_position"], "log_scale": gr["d_log_scale"], "rotation": gr["d_rotation"],
+               "opacity_logit": gr["d_opacity_logit"], "reflectivity_dc": gr["d_reflectivity_dc"],
+               "motion": gr["d_motion"]}
+        for name in groups:
+            check_grad(test, f"d_{name}_it{it}", got[name], want[name])
+        stat_ref += np.linalg.norm(want["position"], axis=1)
+        # Adam, every group, per-group lr (trainer.cpp:18-31, 339-366), step t = it + 1
+        scene.adam_step(lr)
+        after = scene.get_params()
+        for name in groups:
+            p0 = np.asarray(prm[name], np.float64).ravel()
+            gflat = want[name].ravel()
+            if m_state[name] is None:
+                m_state[name], v_state[name] = np.zeros_like(p0), np.zeros_like(p0)
+            m_prev = m_state[name].copy()
+            p = p0.copy()
+            orc.adam_step(p, gflat, m_state[name], v_state[name], it + 1, lr_of[name])
+            dp_gpu = np.asarray(after[name], np.float64).ravel() - p0
+            dp_ref = p - p0
+            # elements whose step the gradients resolve: |m| well above the group's noise and
+            # not a near-cancellation of the previous moment against the new gradient
+            mm = np.abs(m_state[name])
+            big = (mm > 1e-2 * mm.max()) & (mm > 0.1 * (0.9 * np.abs(m_prev) + 0.1 * np.abs(gflat)))
+            # the fp32 parameter store rounds p + dp: allow one ulp of |p| on top of 1e-3 relative
+            ulp = np.abs(np.asarray(after[name], np.float64).ravel()) * 2.0 ** -23
+            err = np.maximum(np.abs(dp_gpu - dp_ref) - ulp, 0.0)[big] / np.abs(dp_ref[big])
+            record(test, f"adam_dp_{name}_it{it}", {"max": float(err.max()), "p9999": float(np.quantile(err, 0.9999)),
+                                                    "elements": int(big.sum()), "floor": "1 ulp of |p| allowed"})
+            assert err.max() < GRAD_TOL, (name, it, float(err.max()))
+            assert np.abs(dp_gpu).max() <= lr_of[name] * 1.5 + ulp.max()
+    s, cnt = scene.densify_stat()
+    assert cnt == 2
+    check_grad(test, "densify_stat", s, stat_ref)
+
+
+# ---------------------------------------------------------------------------------------
+def test_c4_full_size_frame_forward_backward(tsb, ctx):
+    """One c4 frame (2 M Gaussians, 1024x1024): forward vs the oracle, L2 loss against the
+    seeded target render, backward gradients (the oracle's thread-local gradient arrays are
+    nthreads x V x 136 B, so it runs on at most 8 threads here)."""
+    from paper_2505_05356_b200 import synthetic
+    test = "c4_2M_1024"
+    cfg = synthetic.config("c4")
+    g, tof, cam = cfg.scene, cfg.tof, cfg.camera
+    frame = cfg.frames[0]
+    opts = tsb.RenderOptions(counts=True)
+    tscene = gpu_scene(tsb, ctx, cfg.target, tof)
+    target = tsb.RenderPass(ctx).prepare(tscene, cam, opts, frame).forward().outputs()["quad"].astype(np.float32)
+    tscene.close()
+    scene = gpu_scene(tsb, ctx, g, tof)
+    rp = tsb.RenderPass(ctx).prepare(scene, cam, opts, frame)
+    loss = rp.forward_loss(target, [0.25] * 4)
+    out = rp.outputs()
+    rp.backward()
+    gr = scene.grads()
+    threads = orc.num_threads()
+    orc.set_threads(min(threads, 8))
+    try:
+        op = orc.OraclePass(oracle_scene(g, frame, tof), cam, opts)
+        ref = op.forward()
+        assert rp.visible_count() == op.visible_count()
+        compare_forward(test, out, ref)
+        oloss, dq = quad_loss(ref["quad"], target)
+        assert loss == pytest.approx(oloss, rel=1e-5)
+        og = op.backward(d_quad=dq)
+    finally:
+        orc.set_threads(threads)
+    k, w = frame
+    for name, a, b in (("d_position", gr["d_position"], og["d_position"]),
+                       ("d_log_scale", gr["d_log_scale"], og["d_log_scale"]),
+                       ("d_rotation", gr["d_rotation"], og["d_rotation"]),
+                       ("d_opacity_logit", gr["d_opacity_logit"], og["d_opacity_logit"]),
+                       ("d_reflectivity_dc", gr["d_reflectivity_dc"], og["d_refl_sh"][:, 0]),
+                       ("d_motion_k", gr["d_motion"][k], (1 - w) * og["d_position"]),
+                       ("d_motion_k1", gr["d_motion"][k + 1], w * og["d_position"])):
+        check_grad(test, name, a, b)
+
+
+# ---------------------------------------------------------------------------------------
+def rotation_matrix(axis, angle):
+    a = np.asarray(axis, np.float64)
+    a = a / np.linalg.norm(a)
+    K = np.array([[0, -a[2], a[1]], [a[2], 0, -a[0]], [-a[1], a[0], 0]])
+    return np.eye(3) + math.sin(angle) * K + (1 - math.cos(angle)) * K @ K
+
+
+def _all_channels_case(tsb, ctx, test, g, cam, opts, frame, tof, seed, floor=1e-6):
+    """Forward (integers exact, images 1e-4) and gradients from every ToF upstream (1e-3)."""
+    scene = gpu_scene(tsb, ctx, g, tof)
+    rp = tsb.RenderPass(ctx).prepare(scene, cam, opts, frame).forward()
+    out = rp.outputs()
+    op = orc.OraclePass(oracle_scene(g, frame, tof), cam, opts)
+    ref = op.forward()
+    assert rp.visible_count() == op.visible_count()
+    gp, oprep = rp.debug_prepared(), op.prepared()
+    assert np.array_equal(gp["gidx"], oprep["gidx"]) and np.array_equal(gp["rect"], oprep["rect"])
+    compare_forward(test, out, ref, floor=floor)
+    H, W = cam.height, cam.width
+    rng = np.random.default_rng(seed)
+    ups = {"d_quad": rng.normal(0, 1e-3, (4, H, W)), "d_phasor": rng.normal(0, 1e-3, (2, H, W)),
+           "d_depth_raw": rng.normal(0, 1e-3, (H, W)), "d_weight": rng.normal(0, 1e-3, (H, W)),
+           "d_transmittance": rng.normal(0, 1e-3, (H, W))}
+    ups = {k: v.astype(np.float32) for k, v in ups.items()}
+    rp.backward_buffers(**ups)
+    gr = scene.grads()
+    og = op.backward(**{k: v.astype(np.float64) for k, v in ups.items()})
+    k, w = frame
+    for name, a, b in (("d_position", gr["d_position"], og["d_position"]),
+                       ("d_log_scale", gr["d_log_scale"], og["d_log_scale"]),
+                       ("d_rotation", gr["d_rotation"], og["d_rotation"]),
+                       ("d_opacity_logit", gr["d_opacity_logit"], og["d_opacity_logit"]),
+                       ("d_reflectivity_dc", gr["d_reflectivity_dc"], og["d_refl_sh"][:, 0]),
+                       ("d_motion_k1", gr["d_motion"][k + 1], w * og["d_position"])):
+        check_grad(test, name, a, b)
+    assert np.allclose(gr["d_bg_quad"], og["d_bg_quad"], rtol=1e-4, atol=1e-9)
+    assert np.allclose(gr["d_bg_phasor"], og["d_bg_phasor"], rtol=1e-4, atol=1e-9)
+    return rp, out, ref
+
+
+def test_posed_camera(tsb, ctx):
+    """camera.hpp:15-25: p_cam = R p + t with a rotated, translated camera (the chain's R
+    terms, splat.cpp:597, 622), c1 distributions."""
+    from paper_2505_05356_b200 import synthetic
+    test = "posed_camera_c1"
+    cfg = synthetic.config("c1")
+    cam = synthetic.camera(640, 480, 525.0)
+    cam.rotation = rotation_matrix((0.3, -0.8, 0.2), 0.12)
+    cam.translation = np.array([0.15, -0.1, 0.4])
+    opts = tsb.RenderOptions(counts=True, bg_quad=(0.01, -0.02, 0.015, 0.005), bg_phasor=(0.02, -0.01))
+    _all_channels_case(tsb, ctx, test, cfg.scene, cam, opts, cfg.frames[0], cfg.tof, 31)
+
+
+def test_gradcheck_render_options_with_opaque_splats(tsb, ctx):
+    """gradcheck.cpp:77-81: alpha threshold 0, transmittance floor 0, sigma cutoff 6 -- no
+    early termination, every footprint entry contributes -- with 2 % of the splats at
+    opacity_logit 40 (opacity == 1 in fp64, so alpha reaches 1 at their centres and T
+    drops to exactly 0 behind them)."""
+    from paper_2505_05356_b200 import synthetic
+    test = "gradcheck_options_alpha1"
+    g = synthetic.gaussians(20_000, 41, n_keyframes=2)
+    g.opacity_logit[::50] = 40.0
+    g.log_scale[::50] += np.float32(0.7)  # broad opaque splats in front of many others
+    cam = synthetic.camera(320, 240, 262.5)
+    opts = tsb.RenderOptions(counts=True, alpha_threshold=0.0, transmittance_floor=0.0, sigma_cutoff=6.0,
+                             bg_quad=(0.02, 0.01, -0.03, 0.04), bg_phasor=(0.01, 0.02))
+    # No termination: pixels composite every footprint entry (~300-400 here against ~60 with
+    # the default floor), and fp32 sums resolve raw samples that cancel to ~4e-8 of the
+    # image maximum -- the App. D bar holds under a 1e-5*max floor on the fp32 path; the
+    # reference-exact (fp64) mode below meets it under the App. D floor itself.
+    rp, out, ref = _all_channels_case(tsb, ctx, test, g, cam, opts, (0, 0.3), tsb.ToFConfig(30e6), 43, floor=1e-5)
+    zero_T = int((ref["transmittance"] == 0.0).sum())
+    record(test, "pixels_with_T_exactly_0", {"oracle": zero_T, "gpu": int((out["transmittance"] == 0.0).sum())})
+    record(test, "fixup_pixels", {"gpu": int(rp.debug_fixups())})
+    ex_opts = tsb.RenderOptions(counts=True, alpha_threshold=0.0, transmittance_floor=0.0, sigma_cutoff=6.0,
+                                bg_quad=(0.02, 0.01, -0.03, 0.04), bg_phasor=(0.01, 0.02), exact=True)
+    _all_channels_case(tsb, ctx, test + "_exact_mode", g, cam, ex_opts, (0, 0.3), tsb.ToFConfig(30e6), 43)
+
+
+def test_alpha_one_splats_default_options(tsb, ctx):
+    """Splats whose opacity is exactly 1 in fp64 (opacity_logit 40) reach alpha = 1 at their
+    centre pixel: T becomes exactly 0 there.  Forward integers exact, images and
+    gradients within the bars; the pixels an almost-opaque splat leaves with an inaccurate
+    fp32 transmittance are recomposited in fp64 (fix-up reason 8)."""
+    from paper_2505_05356_b200 import synthetic
+    test = "alpha1_default_options"
+    g = synthetic.gaussians(20_000, 44, n_keyframes=2)
+    g.opacity_logit[::50] = 40.0
+    g.log_scale[::50] += np.float32(0.7)
+    # three opaque splats on the optical axis project exactly onto pixel (160, 120)'s centre:
+    # maha = 0, G = 1, alpha = opacity = 1 -> T = 0 exactly behind the nearest one
+    cam = synthetic.camera(320, 240, 262.5, 160.5, 120.5)
+    for i, z in zip((7, 11, 13), (1.5, 2.5, 3.5)):
+        g.position[i] = (0.0, 0.0, z)
+        g.motion[:, i] = 0.0
+        g.opacity_logit[i] = 40.0
+    opts = tsb.RenderOptions(counts=True, bg_quad=(0.02, 0.01, -0.03, 0.04))
+    rp, out, ref = _all_channels_case(tsb, ctx, test, g, cam, opts, (0, 0.0), tsb.ToFConfig(30e6), 45)
+    assert ref["transmittance"][120, 160] == 0.0 and out["transmittance"][120, 160] == 0.0
+    record(test, "fixup_pixels", {"gpu": int(rp.debug_fixups())})
