@@ -59,10 +59,15 @@ enum {
     TSB_CH_DISTORTION = 1u << 7, /* sum_kl w_k w_l (d_k - d_l)^2; required for a distortion upstream */
     TSB_CH_COLOR = 1u << 8,      /* RGB from the colour SH (scene created with color = 1), + bg_color T */
     TSB_CH_FLOW = 1u << 9,       /* motion accumulators + projected flow (tsb_pass_set_motion) */
-    TSB_CH_EXACT = 1u << 10      /* reference-exact mode: every pixel composited in fp64 (the fix-up path,
+    TSB_CH_EXACT = 1u << 10,     /* reference-exact mode: every pixel composited in fp64 (the fix-up path,
                                     forward and backward) and the outputs also kept as fp64 planes
                                     (TSB_OUT_F64 / TSB_OUT_EXT_F64) -- for finite-difference checks
                                     (gradcheck.cpp); costs an fp64 walk per pixel */
+    TSB_CH_DETERMINISTIC = 1u << 11 /* bit-reproducible ToF gradients and loss (the reference's fixed-order
+                                    reduction, splat.cpp:521-543): every raster block writes its per-entry
+                                    sums to a private (rank, tile, sub-block) slot, reduced per Gaussian in
+                                    a fixed order; no float atomics on the path (colour / flow upstreams
+                                    excepted).  Costs a slot buffer and a host sync per backward */
 };
 
 /* CameraModel (camera.hpp:9-17).  R row-major; p_cam = R p_world + t. */
@@ -237,6 +242,10 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam,
                      const tsb_render_options* opt, const tsb_frame* frame);
 /* RenderPass::visible_count (splat.hpp:108). */
 int tsb_pass_visible_count(tsb_pass* p, int32_t* out);
+/* Total length of the reference's tile lists (splat.cpp:187-200) for the frame: sum over
+ * tiles of the visible Gaussians whose tile rect covers the tile.  The raster never
+ * materialises these lists (each block scans the depth order for its own tile and stops
+ * at termination); this count is computed on demand (parity / diagnostics). */
 int tsb_pass_num_keys(tsb_pass* p, int64_t* out);
 
 /* RenderPass::forward (splat.cpp:209-339).  Results stay in pass-owned device
@@ -331,7 +340,8 @@ int tsb_pass_backward_ext(tsb_pass* p, int where, const float* d_quad, const flo
 
 /* Parity / diagnostics: integer intermediates the reference keeps private
  * (splat.cpp:86-87).  Sizes: gidx V, rect 4V (x0,x1,y0,y1 per rank), tiles+1
- * offsets, K ids (indices into the prepared order). */
+ * offsets, K ids (indices into the prepared order; the complete lists, built on
+ * demand from the depth order). */
 int tsb_pass_debug_prepared(tsb_pass* p, int32_t* gidx, int32_t* rect);
 int tsb_pass_debug_tiles(tsb_pass* p, int32_t* tiles_x, int32_t* tiles_y, int64_t* offsets,
                          int32_t* ids);
@@ -343,8 +353,8 @@ int tsb_pass_debug_screen_grads(tsb_pass* p, float* g8 /* 8 per rank */);
 /* Keep a copy of the screen-space gradients of every following backward (the chain kernel
  * consumes them); required before tsb_pass_debug_screen_grads. */
 int tsb_pass_debug_keep_screen(tsb_pass* p, int enabled);
-/* Test hook: shrink the pass's tile-list storage to `entries` (>= 1) so the next
- * frame overflows and exercises the device-side abort + settle/redo path. */
+/* Test hook (`entries` >= 1, otherwise unused): the next forward aborts on the device once,
+ * exercising the abort + settle/redo path (the pass has no list storage to overflow). */
 int tsb_pass_debug_set_list_capacity(tsb_pass* p, uint32_t entries);
 /* Pixels the fp32 raster flagged as decision-ambiguous and recomposited in fp64. */
 int tsb_pass_debug_fixups(tsb_pass* p, int32_t* count);

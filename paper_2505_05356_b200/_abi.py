@@ -18,7 +18,7 @@ HEADER_PATH = Path(__file__).resolve().parent.parent / "include" / "tsb.h"
 TSB_OK, TSB_ERR_INVALID, TSB_ERR_CUDA, TSB_ERR_NOMEM, TSB_ERR_UNSUPPORTED, TSB_ERR_NCCL = range(6)
 TSB_HOST, TSB_DEVICE = 0, 1
 CH_QUAD, CH_DEPTH, CH_WEIGHT, CH_TRANSM, CH_COUNTS, CH_FULL_LISTS = 1, 2, 4, 8, 16, 32
-CH_PHASOR, CH_DISTORTION, CH_COLOR, CH_FLOW, CH_EXACT = 64, 128, 256, 512, 1024
+CH_PHASOR, CH_DISTORTION, CH_COLOR, CH_FLOW, CH_EXACT, CH_DETERMINISTIC = 64, 128, 256, 512, 1024, 2048
 (OUT_QUAD, OUT_DEPTH_RAW, OUT_DEPTH, OUT_WEIGHT, OUT_TRANSM, OUT_N_CONTRIB, OUT_N_PROCESSED,
  OUT_D_QUAD, OUT_PHASOR, OUT_DISTORTION, OUT_COLOR, OUT_MOTION_FWD_ACC, OUT_MOTION_BWD_ACC, OUT_FLOW_FWD,
  OUT_FLOW_BWD, OUT_FLOW_VALID, OUT_D_MOTION_FWD_ACC, OUT_D_MOTION_BWD_ACC, OUT_F64, OUT_EXT_F64) = range(20)

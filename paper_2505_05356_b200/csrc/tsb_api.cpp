@@ -158,9 +158,7 @@ struct tsb_pass {
     // capacities
     int n_cap = 0, px_cap = 0, blk_cap = 0, tiles_cap = 0;
     size_t temp_bytes = 0;
-    size_t hist_cap = 0;       // uint32 entries
-    uint32_t vals_cap = 0;     // list entries
-    int chunk_cap = 0;         // chunks x tiles of ranges
+
     // per Gaussian
     uint32_t *key_a = nullptr, *key_b = nullptr;  // fp32 depth keys
     double* depth64 = nullptr;
@@ -171,20 +169,20 @@ struct tsb_pass {
     uint32_t* touched = nullptr;
     uint2* rect = nullptr;
     RecK rec{};
-    float* screen = nullptr;  // [8][n]
-    float* screen_keep = nullptr;  // debug copy of screen (tsb_pass_debug_keep_screen)
+    double* screen = nullptr;  // [8][n] screen-space gradients, accumulated in fp64 across blocks
+    double* screen_keep = nullptr;  // debug copy of screen (tsb_pass_debug_keep_screen)
     bool keep_screen = false;
-    // chunked binning
-    std::vector<int> chunk_seg0, chunk_nseg;  // schedule (segments)
-    int nchunks = 0;                          // chunks binned by the last forward
-    uint32_t* hist = nullptr;
-    uint32_t* tile_len = nullptr;
-    uint32_t* tile_start = nullptr;
-    uint4* ranges_all = nullptr;  // [chunk_cap][ntiles]
-    int* chunk_rank0 = nullptr;   // device [chunk_cap]
-    uint32_t* vals = nullptr;
-    int32_t* block_done = nullptr;
-    int32_t* tile_blocks_done = nullptr;
+    // the rank order the raster blocks scan (ScanK): Gaussian and tile rect per rank
+    uint32_t* ord = nullptr;
+    uint2* trect = nullptr;
+    int2* blk_term = nullptr;  // per raster block: where its forward scan stopped
+    uint32_t* blk_list = nullptr;  // per raster block: the list entries its forward consumed (kBlkListCap)
+    // deterministic backward (TSB_CH_DETERMINISTIC): slot offsets per rank, slots, fix-up pixel index
+    uint32_t* det_off = nullptr;
+    float* det_part = nullptr;
+    size_t det_cap = 0;
+    int det_off_cap = 0;
+    int* fix_idx = nullptr;
     // per pixel
     float* out = nullptr;
     int32_t *n_contrib = nullptr, *n_processed = nullptr, *last = nullptr;
@@ -192,13 +190,10 @@ struct tsb_pass {
     float* d_quad = nullptr;
     float* up_extra = nullptr;  // [8][npx] host-uploaded upstreams: phasor (2*nf), depth_raw, weight, distortion, T
     double* dist3 = nullptr;    // [3][npx] distortion moments (PixK::dist3)
-    double* st_d = nullptr;     // [3][npx] distortion moments carried across chunks
     float* target = nullptr;
     int32_t* flagged = nullptr;
-    float* st_f = nullptr;
-    int32_t* st_i = nullptr;
     // misc
-    int32_t* counters = nullptr;  // [0] n_visible, [1] n_flagged, [2] abort word, [3] blocks done, [4] prefix end
+    int32_t* counters = nullptr;  // [0] n_visible, [1] n_flagged, [2] abort word, [4] prefix end, [5] key range
     // Nearest-prefix depth order (tsb_sort.cu): a frame sorts only its nearest kcap
     // Gaussians; one that runs past them is redone with the full order and the pass's
     // cap grows (x4, then the full sort).
@@ -207,7 +202,6 @@ struct tsb_pass {
     int32_t* n_bin = nullptr;   // end of the sorted order: counters + 4 (prefix) or counters
     uint32_t *sel_keys = nullptr, *sel_vals = nullptr, *sel_scratch = nullptr;
     int sel_cap = 0;
-    uint32_t* list_off = nullptr;
     double* loss_part = nullptr;
     double* bg_part = nullptr;
     double* loss_dev = nullptr;
@@ -242,8 +236,7 @@ struct tsb_pass {
         size_t bytes;
     };
     std::vector<Download> pend_dl;  // asynchronous output downloads of the unsettled frame
-    int planned_n = -1, planned_tiles = -1;  // chunk plan cache
-    // forward CUDA graph (conditional chunk nodes), rebuilt when forward_key changes
+    // forward CUDA graph, rebuilt when forward_key changes
     cudaStream_t cap_stream = nullptr;
     FrameDev* frame_dev = nullptr;
     struct FwdGraph {
@@ -261,8 +254,8 @@ struct tsb_pass {
     bool fl_grad[2] = {false, false};
     int ext_n_cap = 0, ext_px_cap = 0, ext_blk_cap = 0;
     bool has_mf = false, has_mb = false;
-    bool count_live = false;
     bool prep_deferred = false; // prepare's device work not issued yet
+    bool debug_abort = false;   // test hook: the next forward aborts once
 };
 
 namespace {
@@ -959,7 +952,7 @@ int tsb_pass_create(tsb_ctx* ctx, tsb_pass** out) {
     }
     int rc;
     if ((rc = dev_alloc(&p->counters, 8)) || (rc = dev_alloc(&p->loss_dev, 1)) || (rc = dev_alloc(&p->chw, 8)) ||
-        (rc = dev_alloc(&p->list_off, 1)) || (rc = dev_alloc(&p->fx_work_n, 1)) || (rc = dev_alloc(&p->frame_dev, 1))) {
+        (rc = dev_alloc(&p->fx_work_n, 1)) || (rc = dev_alloc(&p->frame_dev, 1))) {
         tsb_pass_destroy(p);
         return rc;
     }
@@ -969,7 +962,7 @@ int tsb_pass_create(tsb_ctx* ctx, tsb_pass** out) {
         return e ? std::max(0, std::atoi(e)) : kPrefixCap0;
     }();
     p->kcap = prefix_cap;
-    bin_init();
+    raster_init();
     ssim_init();
     ctx->passes.push_back(p);
     *out = p;
@@ -978,32 +971,19 @@ int tsb_pass_create(tsb_ctx* ctx, tsb_pass** out) {
 
 namespace {
 
-// First depth chunk (ranks), then the same again, then doubling.  Pixels terminate
-// after ~1-3 % of their tile list and the nearest ranks are the largest splats, so
-// small first chunks bin far fewer never-read entries (TSB_CHUNK0 overrides).
-// Default: 4 ranks per tile, clamped to [4K, 64K] (measured best on c3: 1,200 tiles,
-// and c4: 4,096 tiles).
-int chunk0_segments(int ntiles) {
-    static const int env = [] {
-        const char* e = std::getenv("TSB_CHUNK0");
-        return e ? std::max(kSeg, std::atoi(e)) : 0;
-    }();
-    const int ranks = env ? env : std::min(65536, std::max(4096, 4 * ntiles));
-    return (ranks + kSeg - 1) / kSeg;
-}
-
 void free_gauss(tsb_pass* p) {
     dev_free(p->key_a); dev_free(p->key_b); dev_free(p->gidx_a); dev_free(p->gidx_b);
     dev_free(p->depth64); dev_free(p->sort_scratch);
     dev_free(p->fx_stamp); dev_free(p->fx_work); dev_free(p->fx_cache);
     dev_free(p->touched); dev_free(p->rect);
     dev_free(p->rec.A); dev_free(p->rec.B); dev_free(p->rec.C); dev_free(p->rec.D); dev_free(p->screen); dev_free(p->screen_keep);
+    dev_free(p->ord); dev_free(p->trect);
 }
 void free_pixels(tsb_pass* p) {
     dev_free(p->out); dev_free(p->n_contrib); dev_free(p->n_processed); dev_free(p->last);
     dev_free(p->T_pre); dev_free(p->d_quad); dev_free(p->target); dev_free(p->flagged);
-    dev_free(p->st_f); dev_free(p->st_i); dev_free(p->up_extra); dev_free(p->dist3); dev_free(p->st_d);
-    dev_free(p->fx_state);
+    dev_free(p->up_extra); dev_free(p->dist3);
+    dev_free(p->fx_state); dev_free(p->fix_idx);
     p->fx_state_cap = 0;
     dev_free(p->out64); dev_free(p->ext_out64);
     p->out64_cap = p->ext_out64_cap = 0;
@@ -1018,10 +998,11 @@ int ensure_gauss(tsb_pass* p, int n) {
         (rc = dev_alloc(&p->depth64, cap)) ||
         (rc = dev_alloc(&p->gidx_b, cap)) || (rc = dev_alloc(&p->touched, cap)) || (rc = dev_alloc(&p->rect, cap)) ||
         (rc = dev_alloc(&p->rec.A, cap)) || (rc = dev_alloc(&p->rec.B, cap)) || (rc = dev_alloc(&p->rec.C, cap)) ||
-        (rc = dev_alloc(&p->rec.D, cap)) || (rc = dev_alloc(&p->screen, (size_t)8 * cap)))
+        (rc = dev_alloc(&p->rec.D, cap)) || (rc = dev_alloc(&p->screen, (size_t)8 * cap)) ||
+        (rc = dev_alloc(&p->ord, cap)) || (rc = dev_alloc(&p->trect, cap)))
         return rc;
     p->rec.rect = p->rect;
-    TSB_CUDA(cudaMemsetAsync(p->screen, 0, sizeof(float) * 8 * (size_t)cap, p->stream));
+    TSB_CUDA(cudaMemsetAsync(p->screen, 0, sizeof(double) * 8 * (size_t)cap, p->stream));
     p->n_cap = cap;
     if ((rc = dev_alloc(&p->sort_scratch, radix_sort_scratch_words(cap))) || (rc = dev_alloc(&p->fx_stamp, cap)) ||
         (rc = dev_alloc(&p->fx_work, cap)) || (rc = dev_alloc(&p->fx_cache, cap)))
@@ -1042,10 +1023,8 @@ int ensure_pixels(tsb_pass* p, int W, int H, int ntiles, int nblocks) {
             (rc = dev_alloc(&p->n_processed, npx)) || (rc = dev_alloc(&p->last, npx)) ||
             (rc = dev_alloc(&p->T_pre, npx)) || (rc = dev_alloc(&p->d_quad, (size_t)8 * npx)) ||
             (rc = dev_alloc(&p->target, (size_t)8 * npx)) || (rc = dev_alloc(&p->flagged, npx)) ||
-            (rc = dev_alloc(&p->st_f, (size_t)kFwdStatePlanes * npx)) || (rc = dev_alloc(&p->st_i, (size_t)3 * npx)) ||
             (rc = dev_alloc(&p->up_extra, (size_t)8 * npx)) || (rc = dev_alloc(&p->dist3, (size_t)3 * npx)) ||
-            (rc = dev_alloc(&p->st_d, (size_t)3 * npx)) ||
-            (rc = dev_alloc(&p->fx_state, std::min(npx, kFixStateCap))))
+            (rc = dev_alloc(&p->fx_state, std::min(npx, kFixStateCap))) || (rc = dev_alloc(&p->fix_idx, npx)))
             return rc;
         p->fx_state_cap = std::min(npx, kFixStateCap);
         p->px_cap = npx;
@@ -1053,72 +1032,16 @@ int ensure_pixels(tsb_pass* p, int W, int H, int ntiles, int nblocks) {
     if (nblocks > p->blk_cap) {
         dev_free(p->loss_part);
         dev_free(p->bg_part);
-        dev_free(p->block_done);
+        dev_free(p->blk_term);
+        dev_free(p->blk_list);
         int rc;
         if ((rc = dev_alloc(&p->loss_part, nblocks)) || (rc = dev_alloc(&p->bg_part, (size_t)12 * nblocks)) ||
-            (rc = dev_alloc(&p->block_done, nblocks)))
+            (rc = dev_alloc(&p->blk_term, nblocks)) || (rc = dev_alloc(&p->blk_list, (size_t)kBlkListCap * nblocks)))
             return rc;
+        TSB_CUDA(cudaMemsetAsync(p->blk_term, 0, sizeof(int2) * (size_t)nblocks, p->stream));
         p->blk_cap = nblocks;
     }
-    if (ntiles > p->tiles_cap) {
-        dev_free(p->tile_len);
-        dev_free(p->tile_start);
-        dev_free(p->tile_blocks_done);
-        dev_free(p->ranges_all);
-        p->chunk_cap = 0;
-        int rc;
-        if ((rc = dev_alloc(&p->tile_len, ntiles)) || (rc = dev_alloc(&p->tile_start, ntiles)) ||
-            (rc = dev_alloc(&p->tile_blocks_done, ntiles)))
-            return rc;
-        p->tiles_cap = ntiles;
-    }
-    return TSB_OK;
-}
-
-// Geometric depth-chunk schedule over the n ranks (segments of kSeg ranks).
-int plan_chunks(tsb_pass* p, int n) {
-    p->chunk_seg0.clear();
-    p->chunk_nseg.clear();
-    const int nseg_total = (n + kSeg - 1) / kSeg;
-    int s0 = 0, len = chunk0_segments(p->ntiles);
-    while (s0 < nseg_total) {
-        const int l = std::min(len, nseg_total - s0);
-        p->chunk_seg0.push_back(s0);
-        p->chunk_nseg.push_back(l);
-        s0 += l;
-        if (p->chunk_seg0.size() >= 2) len *= 2;
-    }
-    const int nch = std::max<int>(1, (int)p->chunk_seg0.size());
-    size_t hist_need = 1;
-    for (int l : p->chunk_nseg) hist_need = std::max(hist_need, (size_t)l * p->ntiles);
-    if (hist_need > p->hist_cap) {
-        dev_free(p->hist);
-        int rc;
-        if ((rc = dev_alloc(&p->hist, hist_need))) return rc;
-        p->hist_cap = hist_need;
-    }
-    if (nch > p->chunk_cap || !p->ranges_all) {
-        dev_free(p->ranges_all);
-        dev_free(p->chunk_rank0);
-        int rc;
-        if ((rc = dev_alloc(&p->ranges_all, (size_t)nch * p->tiles_cap)) || (rc = dev_alloc(&p->chunk_rank0, nch)))
-            return rc;
-        p->chunk_cap = nch;
-    }
-    std::vector<int> r0(nch, 0);
-    for (size_t c = 0; c < p->chunk_seg0.size(); ++c) r0[c] = p->chunk_seg0[c] * kSeg;
-    TSB_CUDA(cudaMemcpy(p->chunk_rank0, r0.data(), sizeof(int) * nch, cudaMemcpyHostToDevice));
-    return TSB_OK;
-}
-
-int ensure_vals(tsb_pass* p, uint64_t need) {
-    if (need <= p->vals_cap && p->vals) return TSB_OK;
-    if (need > 0xF0000000ull) return fail(TSB_ERR_UNSUPPORTED, "render: more than 4e9 tile-list entries");
-    dev_free(p->vals);
-    const uint64_t cap = std::min<uint64_t>(std::max<uint64_t>(need, 1 << 20), 0xF0000000ull);
-    int rc;
-    if ((rc = dev_alloc(&p->vals, (size_t)cap))) return rc;
-    p->vals_cap = (uint32_t)cap;
+    (void)ntiles;
     return TSB_OK;
 }
 
@@ -1166,6 +1089,7 @@ SceneK scenek(const tsb_scene* s) {
 }
 
 int ensure_ext(tsb_pass* p);
+int tile_counts(tsb_pass* p, std::vector<uint32_t>& counts);
 
 int read_visible(tsb_pass* p) {
     int rc0 = flush_prepare(p);
@@ -1190,9 +1114,9 @@ void tsb_pass_destroy(tsb_pass* p) {
     v.erase(std::remove(v.begin(), v.end(), p), v.end());
     free_gauss(p);
     free_pixels(p);
-    dev_free(p->hist); dev_free(p->tile_len); dev_free(p->tile_start); dev_free(p->ranges_all); dev_free(p->chunk_rank0);
-    dev_free(p->vals); dev_free(p->block_done); dev_free(p->tile_blocks_done);
-    dev_free(p->counters); dev_free(p->list_off); dev_free(p->fx_work_n);
+    dev_free(p->blk_term); dev_free(p->blk_list);
+    dev_free(p->det_off); dev_free(p->det_part);
+    dev_free(p->counters); dev_free(p->fx_work_n);
     dev_free(p->sel_keys); dev_free(p->sel_vals); dev_free(p->sel_scratch);
     dev_free(p->loss_part); dev_free(p->bg_part); dev_free(p->loss_dev); dev_free(p->chw);
     dev_free(p->ssim_g); dev_free(p->ssim_part); dev_free(p->order_dbg);
@@ -1282,13 +1206,6 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     int rc;
     if ((rc = ensure_gauss(p, n))) return rc;
     if ((rc = ensure_pixels(p, p->W, p->H, p->ntiles, p->nblocks))) return rc;
-    if (n != p->planned_n || p->ntiles != p->planned_tiles) {
-        if ((rc = plan_chunks(p, n))) return rc;
-        p->planned_n = n;
-        p->planned_tiles = p->ntiles;
-    }
-    if ((rc = ensure_vals(p, std::max<uint64_t>({(uint64_t)n * 8, (uint64_t)p->ntiles * 1024, 1u << 20}))))
-        return rc;
     p->has_mf = p->has_mb = false;  // RenderInput::motion_* belong to one frame
     if ((p->channels & (TSB_CH_COLOR | TSB_CH_FLOW)) && (rc = ensure_ext(p))) return rc;
     if (p->channels & TSB_CH_EXACT) {  // every pixel recomposited (and back-propagated) in fp64
@@ -1340,7 +1257,6 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
         p->n_bin = p->prefix ? p->counters + 4 : p->counters;
     }
     p->V = -1;
-    p->nchunks = 0;
     p->prepared = true;
     return TSB_OK;
 }
@@ -1357,12 +1273,13 @@ int tsb_pass_visible_count(tsb_pass* p, int32_t* out) {
 int tsb_pass_num_keys(tsb_pass* p, int64_t* out) {
     if (!p || !out) return fail(TSB_ERR_INVALID, "null argument");
     if (!p->forwarded) return fail(TSB_ERR_INVALID, "tile lists are built by forward()");
-    int rc0 = settle(p);
-    if (rc0) return rc0;
-    uint32_t* h = (uint32_t*)((char*)p->pinned + 1040);
-    TSB_CUDA(cudaMemcpyAsync(h, p->list_off, 4, cudaMemcpyDeviceToHost, p->stream));
-    TSB_CUDA(cudaStreamSynchronize(p->stream));
-    *out = (int64_t)h[0];
+    int rc = settle(p);
+    if (rc) return rc;
+    std::vector<uint32_t> counts;
+    if ((rc = tile_counts(p, counts))) return rc;
+    int64_t k = 0;
+    for (uint32_t c : counts) k += c;
+    *out = k;
     return TSB_OK;
 }
 
@@ -1378,20 +1295,27 @@ TieK tiek(tsb_pass* p) {
     return t;
 }
 
-// fp64 fix-up arguments of the pass's current chunk plan.
+// The rank order the raster kernels scan (ScanK) of the pass's current frame.
+ScanK scank(tsb_pass* p) {
+    ScanK sc;
+    sc.ord = p->ord;
+    sc.trect = p->trect;
+    sc.n_rank = p->n_bin;
+    sc.n_all = p->counters;
+    sc.blk_term = p->blk_term;
+    sc.blk_list = p->blk_list;
+    sc.abort = p->counters + 2;
+    sc.work = p->ctx->profiling ? p->ctx->work : nullptr;
+    sc.det_off = nullptr;
+    sc.det_part = nullptr;
+    sc.nsub2 = p->opt.sub * p->opt.sub;
+    return sc;
+}
+
+// fp64 fix-up arguments of the pass's current frame.
 FixupK fixk(tsb_pass* p) {
-    const int total_chunks = (int)p->chunk_seg0.size();
     FixupK fx;
-    fx.ranges_all = p->ranges_all;
-    fx.nchunks = std::max(total_chunks, 1);
-    fx.chunk_rank0 = p->chunk_rank0;
-    fx.binned_end_rank = total_chunks ? (p->chunk_seg0.back() + p->chunk_nseg.back()) * kSeg : 0;
-    fx.vals = p->vals;
-    fx.sorted_gidx = p->sorted;
-    fx.ties = tiek(p);
-    fx.rect = p->rect;
-    fx.n_visible = p->n_bin;
-    fx.n_all = p->counters;
+    fx.sc = scank(p);
     fx.overflow = p->counters + 2;
     fx.stamp = p->fx_stamp;
     fx.work = p->fx_work;
@@ -1399,6 +1323,7 @@ FixupK fixk(tsb_pass* p) {
     fx.cache = p->fx_cache;
     fx.state = p->fx_state;
     fx.state_cap = p->fx_state_cap;
+    fx.fix_idx = p->fix_idx;
     return fx;
 }
 
@@ -1500,15 +1425,13 @@ int flush_prepare(tsb_pass* p) {
     return TSB_OK;
 }
 
-// Issue the forward's device work on `st`: per-frame values H2D, every planned
-// depth chunk (binning + raster), the fp64 fix-up, the pass-local part of the
-// loss and the counters read-back.  graph: `st` is capturing; chunks c >= 1 go
-// into conditional nodes gated on the device (k_chunk_gate), so a dead chunk
-// costs one tiny kernel instead of five launches.
+// Issue the forward's device work on `st`: per-frame values H2D, the scan arrays of
+// the frame's order, the raster (one launch: every block scans the order for its own
+// tile), the fp64 fix-up, the pass-local part of the loss and the counters read-back.
 int record_forward(tsb_pass* p, cudaStream_t st, bool loss, const ChW& chw, bool graph, bool with_prep,
                    int* fixed_launches) {
+    (void)graph;
     PixK px = pixk(p);
-    const bool full = (p->channels & TSB_CH_FULL_LISTS) != 0;
     int fixed = 0;
     const FrameDev* fd = p->frame_dev;
     if (with_prep) {
@@ -1520,110 +1443,20 @@ int record_forward(tsb_pass* p, cudaStream_t st, bool loss, const ChW& chw, bool
     }
     // counters[2] (abort word) is not cleared here: the depth sort of prepare may have set it
     TSB_CUDA(cudaMemsetAsync(p->counters + 1, 0, sizeof(int32_t), st));
-    TSB_CUDA(cudaMemsetAsync(p->counters + 3, 0, sizeof(int32_t), st));
-    TSB_CUDA(cudaMemsetAsync(p->counters + 7, 0, sizeof(int32_t), st));
-    TSB_CUDA(cudaMemsetAsync(p->list_off, 0, sizeof(uint32_t), st));
-    TSB_CUDA(cudaMemsetAsync(p->block_done, 0, sizeof(int32_t) * p->nblocks, st));
-    TSB_CUDA(cudaMemsetAsync(p->tile_blocks_done, 0, sizeof(int32_t) * p->ntiles, st));
-    if (loss) TSB_CUDA(cudaMemsetAsync(p->loss_part, 0, sizeof(double) * p->nblocks, st));
-    FwdState fs{p->st_f, p->st_d, p->st_i, p->W * p->H};
-    BinK B{};
-    B.sorted_gidx = p->sorted;
-    B.ties = tiek(p);
-    B.rect = p->rect;
-    B.n_visible = p->n_bin;
-    B.ts = p->opt.ts;
-    B.tiles_x = p->opt.tiles_x;
-    B.tiles_y = p->opt.tiles_y;
-    B.ntiles = p->ntiles;
-    B.tile_blocks_done = p->tile_blocks_done;
-    B.blocks_per_tile = p->opt.sub * p->opt.sub;
-    B.skip_done = full ? 0 : 1;
-    B.hist = p->hist;
-    B.tile_len = p->tile_len;
-    B.tile_start = p->tile_start;
-    B.vals = p->vals;
-    B.list_off = p->list_off;
-    B.capacity = p->vals_cap;
-    B.overflow = p->counters + 2;
-    B.nblocks = p->nblocks;
-    B.blocks_done_total = p->counters + 3;
-    const int total_chunks = (int)p->chunk_seg0.size();
-    const int nplanned = std::max(total_chunks, 1);
-    for (int c = 0; c < nplanned; ++c) {
-        const int seg0 = total_chunks ? p->chunk_seg0[c] : 0;
-        const int nseg = total_chunks ? p->chunk_nseg[c] : 0;
-        B.seg0 = seg0;
-        B.nseg = nseg;
-        B.chunk = c;
-        B.ranges = p->ranges_all + (size_t)c * p->ntiles;
-        B.prev_ranges = c ? p->ranges_all + (size_t)(c - 1) * p->ntiles : nullptr;
-        ChunkK ck;
-        ck.ranges = B.ranges;
-        ck.first = c == 0;
-        ck.chunk_end_rank = (seg0 + nseg) * kSeg;
-        ck.n_visible = p->n_bin;
-        ck.n_all = p->counters;
-        ck.block_done = p->block_done;
-        ck.tile_blocks_done = p->tile_blocks_done;
-        ck.blocks_done_total = p->counters + 3;
-        ck.overflow = p->counters + 2;
-        ck.work = p->ctx->profiling ? p->ctx->work : nullptr;
-        cudaStream_t cs = st;
-        if (graph && c > 0) {
-            // gate kernel, then an IF node whose body is captured on the pass's capture stream
-            cudaStreamCaptureStatus status;
-            cudaGraph_t g = nullptr;
-            const cudaGraphNode_t* deps = nullptr;
-            size_t ndeps = 0;
-            TSB_CUDA(cudaStreamGetCaptureInfo(st, &status, nullptr, &g, &deps, &ndeps));
-            cudaGraphConditionalHandle h;
-            TSB_CUDA(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
-            launch_chunk_gate(B, h, p->counters + 7, st);
-            TSB_CHECK_LAUNCH();
-            ++fixed;
-            TSB_CUDA(cudaStreamGetCaptureInfo(st, &status, nullptr, &g, &deps, &ndeps));
-            cudaGraphNodeParams np = {};
-            np.type = cudaGraphNodeTypeConditional;
-            np.conditional.handle = h;
-            np.conditional.type = cudaGraphCondTypeIf;
-            np.conditional.size = 1;
-            cudaGraphNode_t node;
-            TSB_CUDA(cudaGraphAddNode(&node, g, deps, ndeps, &np));
-            TSB_CUDA(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
-            TSB_CUDA(cudaStreamBeginCaptureToGraph(p->cap_stream, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
-                                                   cudaStreamCaptureModeThreadLocal));
-            cs = p->cap_stream;
-        }
-        if (nseg > 0) {
-            {
-                Stage sg(p->ctx, TSB_STAGE_BIN_COUNT, cs);
-                launch_bin_count(B, cs);
-            }
-            {
-                Stage sg(p->ctx, TSB_STAGE_BINNING, cs);
-                launch_bin_scan(B, cs);
-            }
-            {
-                Stage sg(p->ctx, TSB_STAGE_BIN_EMIT, cs);
-                launch_bin_emit(B, cs);
-            }
-        } else {
-            TSB_CUDA(cudaMemsetAsync(B.ranges, 0, sizeof(uint4) * p->ntiles, cs));
-        }
-        {
-            Stage sg(p->ctx, TSB_STAGE_RASTER_FWD, cs);
-            launch_raster_fwd(p->rec, ck, p->vals, p->opt, p->W, p->H, p->nf, px, fs, fd, loss, chw, p->loss_part, cs);
-        }
-        TSB_CHECK_LAUNCH();
-        if (cs != st) {
-            cudaGraph_t body = nullptr;
-            TSB_CUDA(cudaStreamEndCapture(cs, &body));
-        } else {
-            fixed += bin_chunk_kernels(B) + 1;
-        }
+    if (p->debug_abort) {  // test hook (eager forward): abort this frame once
+        TSB_CUDA(cudaMemsetAsync(p->counters + 2, 0x20, 1, st));
+        p->debug_abort = false;
     }
-    p->nchunks = nplanned;
+    {
+        Stage sg(p->ctx, TSB_STAGE_BINNING, st);
+        launch_order_ranks(p->sorted, tiek(p), p->rect, p->opt.ts, p->n_bin, p->scene->d.n, p->ord, p->trect, st);
+        fixed += p->scene->d.n > 0 ? 1 : 0;
+    }
+    {
+        Stage sg(p->ctx, TSB_STAGE_RASTER_FWD, st);
+        launch_raster_fwd(p->rec, scank(p), p->opt, p->W, p->H, p->nf, px, fd, loss, chw, p->loss_part, st);
+        fixed += 1;
+    }
     const FixupK fx = fixk(p);
     {
         Stage sg(p->ctx, TSB_STAGE_FIXUP, st);
@@ -1633,7 +1466,8 @@ int record_forward(tsb_pass* p, cudaStream_t st, bool loss, const ChW& chw, bool
     if (loss) {
         Stage sg(p->ctx, TSB_STAGE_LOSS, st);
         TSB_CUDA(cudaMemsetAsync(p->loss_dev, 0, sizeof(double), st));
-        launch_fixup_loss(px, p->W, p->H, p->nf, fd, chw, p->loss_dev, st);
+        launch_fixup_loss(px, p->W, p->H, p->nf, fd, chw, p->loss_dev, (p->channels & TSB_CH_DETERMINISTIC) != 0,
+                          st);
         launch_reduce_partials(p->loss_part, p->nblocks, 1, p->loss_dev, 1.0 / ((double)p->W * p->H), px.abort, st);
         fixed += 2;
         if (p->mix > 0.0) {  // lambda (1 - SSIM) per weighted quad channel (losses.cpp:148-166)
@@ -1660,7 +1494,6 @@ int record_forward(tsb_pass* p, cudaStream_t st, bool loss, const ChW& chw, bool
     TSB_CHECK_LAUNCH();
     int32_t* hc = (int32_t*)((char*)p->pinned + 2048);
     TSB_CUDA(cudaMemcpyAsync(hc, p->counters, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost, st));
-    TSB_CUDA(cudaMemcpyAsync(hc + 8, p->list_off, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     *fixed_launches = fixed;
     return TSB_OK;
 }
@@ -1671,10 +1504,9 @@ std::string forward_key(tsb_pass* p, bool loss, const ChW& chw) {
     auto add = [&k](const void* d, size_t n) { k.append((const char*)d, n); };
     const SceneK S = scenek(p->scene);
     const PixK px = pixk(p);
-    const void* ptrs[] = {p->sorted, p->rect, p->counters, p->tile_blocks_done, p->hist, p->tile_len, p->tile_start,
-                          p->vals, p->list_off, p->ranges_all, p->block_done, p->rec.A, p->rec.B, p->rec.C, p->rec.D,
-                          p->st_f, p->st_d, p->st_i, p->loss_part, p->loss_dev, p->chunk_rank0, p->fx_stamp,
-                          p->fx_work, p->fx_work_n, p->fx_cache, p->frame_dev, p->pinned, p->fx_state};
+    const void* ptrs[] = {p->sorted, p->rect, p->counters, p->ord, p->trect, p->blk_term, p->blk_list, p->rec.A, p->rec.B,
+                          p->rec.C, p->rec.D, p->loss_part, p->loss_dev, p->fx_stamp, p->fx_work, p->fx_work_n,
+                          p->fx_cache, p->frame_dev, p->pinned, p->fx_state};
     add(ptrs, sizeof ptrs);
     add(&p->fx_state_cap, sizeof p->fx_state_cap);
     add(&S, sizeof S);
@@ -1689,11 +1521,10 @@ std::string forward_key(tsb_pass* p, bool loss, const ChW& chw) {
     const void* prep_ptrs[] = {p->key_a, p->key_b, p->depth64, p->gidx_a, p->gidx_b, p->touched, p->sort_scratch,
                                p->n_bin, p->sel_keys, p->sel_vals, p->sel_scratch};
     add(prep_ptrs, sizeof prep_ptrs);
-    const int ints[] = {p->W, p->H, p->nf, (int)p->channels, p->ntiles, p->nblocks, (int)p->vals_cap, loss ? 1 : 0,
-                        p->ctx->profiling ? 1 : 0, p->prep_deferred ? 1 : 0, p->prefix ? p->kcap : 0};
+    const int ints[] = {p->W, p->H, p->nf, (int)p->channels, p->ntiles, p->nblocks, loss ? 1 : 0,
+                        p->ctx->profiling ? 1 : 0, p->prep_deferred ? 1 : 0, p->prefix ? p->kcap : 0,
+                        p->scene->d.n};
     add(ints, sizeof ints);
-    add(p->chunk_seg0.data(), sizeof(int) * p->chunk_seg0.size());
-    add(p->chunk_nseg.data(), sizeof(int) * p->chunk_nseg.size());
     return k;
 }
 
@@ -1706,7 +1537,7 @@ int enqueue_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw,
     if (with_prep) TSB_CUDA(cudaStreamWaitEvent(st, p->scene->params_ev, 0));
     int fixed = 0;
     // Graphs: not while stage events are being recorded (profiling runs the same kernels eagerly).
-    const bool use_graph = allow_graph && p->ctx->use_graphs && !p->ctx->profiling;
+    const bool use_graph = allow_graph && p->ctx->use_graphs && !p->ctx->profiling && !p->debug_abort;
     if (use_graph) {
         std::string key = forward_key(p, loss, chw);
         tsb_pass::FwdGraph& fg = p->fwd[with_prep ? 1 : 0];
@@ -1733,23 +1564,18 @@ int enqueue_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw,
         }
         TSB_CUDA(cudaGraphLaunch(fg.exec, st));
         p->ctx->launches += fg.fixed;
-        p->count_live = true;
     } else {
         int rc = record_forward(p, st, loss, chw, false, with_prep, &fixed);
         if (rc) return rc;
         p->ctx->launches += fixed;
-        p->count_live = false;
     }
     p->prep_deferred = false;
-    // chunks the backward walks (record_forward sets it too, but a replayed graph skips it)
-    p->nchunks = std::max((int)p->chunk_seg0.size(), 1);
     if (p->channels & (TSB_CH_COLOR | TSB_CH_FLOW)) {
         // colour / flow channels beside the graph (tsb_ext.cu); an aborted frame skips them
         const ExtK E = extk(p);
         const SceneK S = scenek(p->scene);
         launch_ext_prep(S, p->cam, p->frame_dev, p->touched, E, p->counters + 2, st);
-        launch_ext_fwd(p->rec, S, p->cam, p->opt, p->frame_dev, p->ranges_all, p->nchunks, p->vals, fixk(p), pixk(p),
-                       p->nf, E, st);
+        launch_ext_fwd(p->rec, S, p->cam, p->opt, p->frame_dev, scank(p), fixk(p), pixk(p), p->nf, E, st);
         p->ctx->launches += (E.col && S.n > 0 ? 1 : 0) + 1;
         TSB_CHECK_LAUNCH();
     }
@@ -1827,11 +1653,9 @@ int settle(tsb_pass* p) {
         p->pending = false;
         const int32_t* hc = (const int32_t*)((const char*)p->pinned + 2048);
         p->V = hc[0];
-        if (p->count_live) p->ctx->launches += (int64_t)hc[7];  // kernels of live chunk bodies (graph)
-        p->count_live = false;
         const int ab = hc[2];
         if (!ab) return TSB_OK;
-        if (attempt >= 8) return fail(TSB_ERR_NOMEM, "render: tile-list storage kept overflowing");
+        if (attempt >= 8) return fail(TSB_ERR_UNSUPPORTED, "render: frame kept aborting (depth order)");
         p->ctx->redos++;
         cudaStream_t st = p->stream;
         if (ab & 16) {  // lean / exact visibility disagreed: exact preprocess + full sort
@@ -1848,11 +1672,6 @@ int settle(tsb_pass* p) {
             p->ctx->launches += launch_sort_depth64(p->depth64, p->touched, p->key_a, p->key_b, p->gidx_a, p->gidx_b,
                                                     p->scene->d.n, p->sort_scratch, st);
             p->sorted = p->gidx_a;
-        }
-        if (ab & 1) {  // list storage overflow: grow
-            const uint32_t used = (uint32_t)hc[8];
-            int rc = ensure_vals(p, (uint64_t)p->vals_cap * 2 + (uint64_t)used);
-            if (rc) return rc;
         }
         TSB_CUDA(cudaMemsetAsync(p->counters + 2, 0, sizeof(int32_t), st));
         const bool bwd = p->pend_bwd;
@@ -2059,15 +1878,51 @@ int enqueue_backward(tsb_pass* p, const UpK& up) {
     {
         // per-pass outputs only (screen gradients, background partials): overlaps other passes
         Stage sg(p->ctx, TSB_STAGE_RASTER_BWD, st);
-        launch_raster_bwd(p->rec, p->ranges_all, p->nchunks, p->vals, p->opt, p->W, p->H, p->nf, dpsi, px, up,
-                          p->screen, s->d.n, p->bg_part, st);
+        ScanK sc = scank(p);
+        FixupK fx = fixk(p);
+        const bool det = (p->channels & TSB_CH_DETERMINISTIC) != 0;
+        if (det) {  // slots: offsets over the frame's ranks, sized on the host (one sync), cleared
+            const int n = s->d.n;
+            if (p->det_off_cap < p->n_cap + 2) {
+                dev_free(p->det_off);
+                p->det_off_cap = 0;
+                int rc;
+                if ((rc = dev_alloc(&p->det_off, (size_t)p->n_cap + 2))) return rc;
+                p->det_off_cap = p->n_cap + 2;
+            }
+            uint32_t* total = p->det_off + p->det_off_cap - 1;  // past every rank's offset
+            launch_det_offsets(sc, p->det_off, total, st);
+            uint32_t* h = (uint32_t*)((char*)p->pinned + 1072);
+            TSB_CUDA(cudaMemcpyAsync(h, total, 4, cudaMemcpyDeviceToHost, st));
+            TSB_CUDA(cudaStreamSynchronize(st));
+            const size_t slots = std::max<size_t>(h[0], 1);
+            if (slots > p->det_cap) {
+                dev_free(p->det_part);
+                p->det_cap = 0;
+                int rc;
+                if ((rc = dev_alloc(&p->det_part, 8 * slots))) return rc;
+                p->det_cap = slots;
+            }
+            TSB_CUDA(cudaMemsetAsync(p->det_part, 0, sizeof(float) * 8 * slots, st));
+            sc.det_off = p->det_off;
+            sc.det_part = p->det_part;
+            fx.sc = sc;
+            p->ctx->launches += 1;
+            (void)n;
+        }
+        launch_raster_bwd(p->rec, sc, p->opt, p->W, p->H, p->nf, dpsi, px, up, p->screen, s->d.n, p->bg_part, st);
         // the recomposited pixels, whose backward follows their fp64 forward
-        launch_fixup_bwd(scenek(s), p->cam, p->opt, p->frame_dev, fixk(p), px, up, p->nf, p->screen, s->d.n, st);
-        p->ctx->launches += 1;
+        if (det) {
+            launch_fixup_bwd_det(scenek(s), p->cam, p->opt, p->frame_dev, fx, px, up, p->nf, st);
+            launch_det_reduce(sc, s->d.n, p->screen, s->d.n, st);
+            p->ctx->launches += 2;
+        } else {
+            launch_fixup_bwd(scenek(s), p->cam, p->opt, p->frame_dev, fx, px, up, p->nf, p->screen, s->d.n, st);
+            p->ctx->launches += 1;
+        }
         if (ext) {  // colour / motion upstreams: adds to the same screen gradients (tsb_ext.cu)
             TSB_CUDA(cudaMemsetAsync(p->ext_dmotion, 0, sizeof(float4) * 2 * (size_t)std::max(s->d.n, 1), st));
-            launch_ext_bwd(p->rec, p->opt, p->W, p->H, p->nf, p->ranges_all, p->nchunks, p->vals, px, up, E,
-                           p->screen, s->d.n, st);
+            launch_ext_bwd(p->rec, p->opt, p->W, p->H, p->nf, scank(p), px, up, E, p->screen, s->d.n, st);
             p->ctx->launches += 1;
         }
     }
@@ -2082,7 +1937,7 @@ int enqueue_backward(tsb_pass* p, const UpK& up) {
         dev_free(p->screen_keep);
         int rc;
         if ((rc = dev_alloc(&p->screen_keep, (size_t)8 * s->d.n))) return rc;
-        TSB_CUDA(cudaMemcpyAsync(p->screen_keep, p->screen, sizeof(float) * 8 * (size_t)s->d.n,
+        TSB_CUDA(cudaMemcpyAsync(p->screen_keep, p->screen, sizeof(double) * 8 * (size_t)s->d.n,
                                  cudaMemcpyDeviceToDevice, st));
     }
     {
@@ -2339,9 +2194,28 @@ int order_device(tsb_pass* p, const uint32_t** out) {
         p->order_dbg_cap = n;
     }
     if (p->prefix) full_order(p, false, p->stream);  // the frame sorted only its nearest prefix
+    // the scan arrays over the full order (its first ranks are the prefix's: the forward's
+    // scan positions stay valid for a backward that follows)
+    launch_order_ranks(p->sorted, tiek(p), p->rect, p->opt.ts, p->n_bin, p->scene->d.n, p->ord, p->trect, p->stream);
     launch_materialize_order(p->sorted, tiek(p), p->counters, p->scene->d.n, p->order_dbg, p->stream);
     TSB_CHECK_LAUNCH();
     *out = p->order_dbg;
+    return TSB_OK;
+}
+// Complete tile-list lengths (splat.cpp:187-200) over the full order.
+int tile_counts(tsb_pass* p, std::vector<uint32_t>& counts) {
+    const uint32_t* od = nullptr;
+    int rc = order_device(p, &od);
+    if (rc) return rc;
+    const int nt = p->ntiles;
+    uint32_t* dc = nullptr;
+    if ((rc = dev_alloc(&dc, (size_t)nt))) return rc;
+    launch_tile_counts(scank(p), p->opt.tiles_x, nt, dc, p->stream);
+    counts.assign((size_t)nt, 0u);
+    TSB_CUDA(cudaMemcpyAsync(counts.data(), dc, sizeof(uint32_t) * nt, cudaMemcpyDeviceToHost, p->stream));
+    cudaError_t e = cudaStreamSynchronize(p->stream);
+    dev_free(dc);
+    if (e != cudaSuccess) return fail(TSB_ERR_CUDA, std::string("tile counts: ") + cudaGetErrorString(e));
     return TSB_OK;
 }
 }  // namespace
@@ -2377,44 +2251,31 @@ int tsb_pass_debug_tiles(tsb_pass* p, int32_t* tiles_x, int32_t* tiles_y, int64_
     if (!p || !p->forwarded) return fail(TSB_ERR_INVALID, "tile lists are built by forward()");
     if (tiles_x) *tiles_x = p->opt.tiles_x;
     if (tiles_y) *tiles_y = p->opt.tiles_y;
-    int rc = read_visible(p);
+    int rc = settle(p);
     if (rc) return rc;
-    cudaStream_t st = p->stream;
-    const int nt = p->ntiles, nch = p->nchunks;
-    std::vector<uint4> rg((size_t)std::max(nch * nt, 1));
-    if (nch > 0)
-        TSB_CUDA(cudaMemcpyAsync(rg.data(), p->ranges_all, sizeof(uint4) * nch * nt, cudaMemcpyDeviceToHost, st));
-    int64_t k = 0;
-    uint32_t* hl = (uint32_t*)((char*)p->pinned + 1056);
-    TSB_CUDA(cudaMemcpyAsync(hl, p->list_off, 4, cudaMemcpyDeviceToHost, st));
-    TSB_CUDA(cudaStreamSynchronize(st));
-    k = hl[0];
-    std::vector<uint32_t> vals((size_t)std::max<int64_t>(k, 1));
-    std::vector<uint32_t> order((size_t)std::max(p->V, 1));
-    if (ids && k > 0) {
-        TSB_CUDA(cudaMemcpyAsync(vals.data(), p->vals, sizeof(uint32_t) * k, cudaMemcpyDeviceToHost, st));
-        const uint32_t* od = nullptr;
-        int rc2;
-        if ((rc2 = order_device(p, &od))) return rc2;
-        if (p->V > 0)
-            TSB_CUDA(cudaMemcpyAsync(order.data(), od, sizeof(uint32_t) * p->V, cudaMemcpyDeviceToHost, st));
-        TSB_CUDA(cudaStreamSynchronize(st));
-    }
-    // per tile: concatenation of its chunk sub-lists (values are Gaussian indices;
-    // the reference lists hold prepared (rank) indices)
-    std::vector<int32_t> rank_of((size_t)std::max(p->scene->d.n, 1), -1);
-    for (int r = 0; r < p->V; ++r) rank_of[order[r]] = r;
-    int64_t acc = 0;
-    for (int t = 0; t < nt; ++t) {
-        if (offsets) offsets[t] = acc;
-        for (int c = 0; c < nch; ++c) {
-            const uint4 r = rg[(size_t)c * nt + t];
-            if (ids)
-                for (uint32_t e = 0; e < r.y; ++e) ids[acc + e] = rank_of[vals[r.x + e]];
-            acc += r.y;
+    std::vector<uint32_t> counts;
+    if ((rc = tile_counts(p, counts))) return rc;  // over the full order
+    const int nt = p->ntiles;
+    std::vector<int64_t> off((size_t)nt + 1, 0);
+    for (int t = 0; t < nt; ++t) off[t + 1] = off[t] + counts[t];
+    if (offsets)
+        for (int t = 0; t <= nt; ++t) offsets[t] = off[t];
+    if (ids && off[nt] > 0) {
+        cudaStream_t st = p->stream;
+        int64_t* doff = nullptr;
+        uint32_t* dids = nullptr;
+        if ((rc = dev_alloc(&doff, (size_t)nt + 1)) || (rc = dev_alloc(&dids, (size_t)off[nt]))) {
+            dev_free(doff);
+            return rc;
         }
+        TSB_CUDA(cudaMemcpyAsync(doff, off.data(), sizeof(int64_t) * (nt + 1), cudaMemcpyHostToDevice, st));
+        launch_tile_lists(scank(p), p->opt.tiles_x, nt, doff, dids, st);
+        TSB_CUDA(cudaMemcpyAsync(ids, dids, sizeof(uint32_t) * (size_t)off[nt], cudaMemcpyDeviceToHost, st));
+        cudaError_t e = cudaStreamSynchronize(st);
+        dev_free(doff);
+        dev_free(dids);
+        if (e != cudaSuccess) return fail(TSB_ERR_CUDA, std::string("debug_tiles: ") + cudaGetErrorString(e));
     }
-    if (offsets) offsets[nt] = acc;
     return TSB_OK;
 }
 
@@ -2465,11 +2326,7 @@ int tsb_pass_debug_set_list_capacity(tsb_pass* p, uint32_t entries) {
     if (!p || entries == 0) return fail(TSB_ERR_INVALID, "tsb_pass_debug_set_list_capacity: bad argument");
     int rc = settle(p);
     if (rc) return rc;
-    TSB_CUDA(cudaSetDevice(p->ctx->device));
-    TSB_CUDA(cudaStreamSynchronize(p->stream));
-    dev_free(p->vals);
-    if ((rc = dev_alloc(&p->vals, entries))) return rc;
-    p->vals_cap = entries;
+    p->debug_abort = true;  // the next forward aborts on the device once (settle redoes it)
     return TSB_OK;
 }
 
@@ -2487,9 +2344,9 @@ int tsb_pass_debug_screen_grads(tsb_pass* p, float* g8) {
     int rc = read_visible(p);
     if (rc) return rc;
     const int n = p->scene->d.n, V = p->V;
-    std::vector<float> sc((size_t)8 * std::max(n, 1));
+    std::vector<double> sc((size_t)8 * std::max(n, 1));
     std::vector<uint32_t> g((size_t)std::max(V, 1));
-    TSB_CUDA(cudaMemcpyAsync(sc.data(), p->screen_keep, sizeof(float) * 8 * (size_t)n, cudaMemcpyDeviceToHost,
+    TSB_CUDA(cudaMemcpyAsync(sc.data(), p->screen_keep, sizeof(double) * 8 * (size_t)n, cudaMemcpyDeviceToHost,
                              p->stream));
     {
         const uint32_t* od = nullptr;

@@ -113,18 +113,17 @@ __device__ __forceinline__ float4 ld_or_zero(const float4* p, uint32_t i) {
 }
 
 __global__ void __launch_bounds__(kRasterThreads) k_ext_fwd(RecK rec, SceneK S, CamK C, OptK O,
-                                                            const FrameDev* __restrict__ fd,
-                                                            const uint4* __restrict__ ranges_all, int nchunks,
-                                                            const uint32_t* __restrict__ vals, FixupK fx, PixK px,
-                                                            int nf, ExtK E) {
+                                                            const FrameDev* __restrict__ fd, ScanK sc, FixupK fx,
+                                                            PixK px, int nf, ExtK E) {
     __shared__ float4 sA[kRasterThreads], sB[kRasterThreads];
     __shared__ float4 sC[kRasterThreads], sMf[kRasterThreads], sMb[kRasterThreads];
     __shared__ uint32_t sg[kRasterThreads];
     __shared__ int smax[kRasterThreads / 32];
+    __shared__ int wsum[2][kRasterThreads / 32];
     if (*px.abort) return;
     const int W = C.W, H = C.H, tid = threadIdx.x;
     const PixMap m = pix_map(O, W, H);
-    const int ntiles = O.tiles_x * O.tiles_y;
+    const int ttx = m.tile % O.tiles_x, tty = m.tile / O.tiles_x;
     int last = 0;
     bool fixed = false;
     if (m.active) {
@@ -140,24 +139,28 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_fwd(RecK rec, SceneK S, 
     double acc[9];  // fp64 sums: the motion channels are signed and cancel
 #pragma unroll
     for (int c = 0; c < 9; ++c) acc[c] = 0.0;
-    for (int c = 0; c < nchunks; ++c) {
-        const uint4 rg = ranges_all[(size_t)c * ntiles + m.tile];  // (start, len, cum)
-        if ((int)rg.z >= bmax) break;
-        const int n_here = min((int)rg.y, bmax - (int)rg.z);
-        for (int b0 = 0; b0 < n_here; b0 += kRasterThreads) {
-            const int nb = min(kRasterThreads, n_here - b0);
-            __syncthreads();
-            if (tid < nb) {
-                const uint32_t r = vals[rg.x + b0 + tid];
-                sg[tid] = r;
-                sA[tid] = stage_A(rec.A[r], m.ox, m.oy);
-                sB[tid] = rec.B[r];
-                sC[tid] = ld_or_zero(E.col, r);
-                sMf[tid] = ld_or_zero(E.mf, r);
-                sMb[tid] = ld_or_zero(E.mb, r);
-            }
-            __syncthreads();
-            const int jmax = min(nb, last - ((int)rg.z + b0));
+    // the tile's list up to the block's furthest pixel: the rank order scanned upwards
+    const int V = *sc.n_rank;
+    int pass = 0;
+    for (int r0 = 0, ebase = 0; r0 < V && ebase < bmax; r0 += kRasterThreads, ++pass) {
+        const int rr = r0 + tid;
+        const bool cov = rr < V && tile_covers(sc.trect[rr], ttx, tty);
+        int total;
+        const int pos = scan_compact(cov, wsum[pass & 1], total);  // (its barrier follows the last pass's reads)
+        if (pos >= 0) {
+            const uint32_t r = sc.ord[rr];
+            sg[pos] = r;
+            sA[pos] = stage_A(rec.A[r], m.ox, m.oy);
+            sB[pos] = rec.B[r];
+            sC[pos] = ld_or_zero(E.col, r);
+            sMf[pos] = ld_or_zero(E.mf, r);
+            sMb[pos] = ld_or_zero(E.mb, r);
+        }
+        __syncthreads();
+        {
+            const int nb = total;
+            const int jmax = min(nb, last - ebase);
+            ebase += total;
             for (int j = 0; j < jmax; ++j) {
                 double wd;
                 double cx[3] = {0.0, 0.0, 0.0};
@@ -239,20 +242,22 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_fwd(RecK rec, SceneK S, 
     }
 }
 
-__global__ void __launch_bounds__(kRasterThreads) k_ext_bwd(RecK rec, OptK O, int W, int H, int nf,
-                                                            const uint4* __restrict__ ranges_all, int nchunks,
-                                                            const uint32_t* __restrict__ vals, PixK px, UpK up,
-                                                            ExtK E, float* __restrict__ screen, int scap) {
+constexpr int kExtSub = 16;  // entries per slot round: 8 warps x 16 entries x 16 floats
+
+__global__ void __launch_bounds__(kRasterThreads) k_ext_bwd(RecK rec, OptK O, int W, int H, int nf, ScanK sc,
+                                                            PixK px, UpK up, ExtK E, double* __restrict__ screen,
+                                                            int scap) {
     __shared__ float4 sA[kRasterThreads], sB[kRasterThreads];
     __shared__ float4 sC[kRasterThreads], sMf[kRasterThreads], sMb[kRasterThreads];
     __shared__ uint32_t srank[kRasterThreads];
-    __shared__ float sacc[kRasterThreads][17];
+    __shared__ float slot[kRasterThreads / 32][kExtSub][16];  // per warp, per entry: its reduced gradients
     __shared__ int smax[kRasterThreads / 32];
+    __shared__ int wsum[2][kRasterThreads / 32];
     __shared__ float sbg[kRasterThreads / 32][3];
     if (*px.abort) return;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const PixMap m = pix_map(O, W, H);
-    const int ntiles = O.tiles_x * O.tiles_y;
+    const int ttx = m.tile % O.tiles_x, tty = m.tile / O.tiles_x;
     const size_t HW = m.HW, o = m.o;
     int last = 0;
     float Tnext = 0.f, Bx = 0.f;
@@ -281,7 +286,6 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_bwd(RecK rec, OptK O, in
     int wmax = last;
     for (int s = 16; s > 0; s >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, s));
     if (lane == 0) smax[tid >> 5] = wmax;
-    for (int c = 0; c < 17; ++c) sacc[tid][c] = 0.f;
     __syncthreads();
     int bmax = 0;
 #pragma unroll
@@ -293,27 +297,36 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_bwd(RecK rec, OptK O, in
     }
     bool first = true;
     const float cut2 = O.cut2_f, thr = O.alpha_thr_f;
-    for (int c = nchunks - 1; c >= 0 && bmax > 0; --c) {
-        const uint4 rg = ranges_all[(size_t)c * ntiles + m.tile];
-        if ((int)rg.z >= bmax || rg.y == 0) continue;
-        const int n_here = min((int)rg.y, bmax - (int)rg.z);
-        const int nbatch = (n_here + kRasterThreads - 1) / kRasterThreads;
-        for (int bi = nbatch - 1; bi >= 0; --bi) {
-            const uint32_t b = rg.x + (uint32_t)bi * kRasterThreads;
-            const int nb = min(kRasterThreads, n_here - bi * kRasterThreads);
-            if (tid < nb) {
-                const uint32_t r = vals[b + tid];
-                srank[tid] = r;
-                sA[tid] = stage_A(rec.A[r], m.ox, m.oy);
-                sB[tid] = rec.B[r];
-                sC[tid] = ld_or_zero(E.col, r);
-                sMf[tid] = ld_or_zero(E.mf, r);
-                sMb[tid] = ld_or_zero(E.mb, r);
-            }
+    // the tile's list back to front: the rank order scanned downwards from where the forward stopped
+    const int2 bt = sc.blk_term[blockIdx.x];
+    const uint32_t wbit = 1u << warp;
+    int pass = 0;
+    for (int r_hi = bt.x, e_top = bt.y; bmax > 0 && r_hi > 0 && e_top > 0; r_hi -= kRasterThreads, ++pass) {
+        const int rr = r_hi - 1 - tid;
+        const bool cov = rr >= 0 && tile_covers(sc.trect[rr], ttx, tty);
+        int total;
+        const int pos = scan_compact(cov, wsum[pass & 1], total);  // descending rank order
+        const int e_lo = e_top - total;
+        if (pos >= 0) {
+            const int j = total - 1 - pos;  // ascending
+            const uint32_t r = sc.ord[rr];
+            srank[j] = r;
+            sA[j] = stage_A(rec.A[r], m.ox, m.oy);
+            sB[j] = rec.B[r];
+            sC[j] = ld_or_zero(E.col, r);
+            sMf[j] = ld_or_zero(E.mf, r);
+            sMb[j] = ld_or_zero(E.mb, r);
+        }
+        e_top = e_lo;
+        __syncthreads();
+        for (int hi = total; hi > 0; hi -= kExtSub) {
+            const int lo = max(0, hi - kExtSub);
+            for (int k = tid; k < (kRasterThreads / 32) * kExtSub * 16; k += kRasterThreads) (&slot[0][0][0])[k] = 0.f;
             __syncthreads();
-            const int jtop = min(nb, wmax - ((int)rg.z + bi * kRasterThreads));
-            for (int j = jtop - 1; j >= 0; --j) {
-                const int el = (int)rg.z + bi * kRasterThreads + j;
+            const int jtop = min(hi, wmax - e_lo);
+            for (int j = jtop - 1; j >= lo; --j) {
+                const int el = e_lo + j;
+                (void)wbit;
                 bool contrib = false;
                 float ga[8], gb[8];
                 if (el < last) {
@@ -367,21 +380,22 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_bwd(RecK rec, OptK O, in
                     const float s2 = reduce_scatter8(gb, lane);
                     if ((lane & 3) == 0) {
                         const int vi = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-                        atomicAdd(&sacc[j][vi], s1);
-                        atomicAdd(&sacc[j][8 + vi], s2);
+                        slot[warp][j - lo][vi] = s1;
+                        slot[warp][j - lo][8 + vi] = s2;
                     }
                 }
             }
             __syncthreads();
-            if (tid < nb) {
-                const uint32_t r = srank[tid];
-                for (int k = 0; k < 15; ++k) {
-                    const float v = sacc[tid][k];
-                    if (v != 0.f) {
-                        if (k < 6) atomicAdd(&screen[(size_t)k * scap + r], v);
-                        else atomicAdd(&E.screen[(size_t)(k - 6) * scap + r], v);
-                    }
-                    sacc[tid][k] = 0.f;
+            // fixed-order sum over the warps; 15 values per entry (d_alpha part + colour / motion w up)
+            for (int k = tid; k < (hi - lo) * 15; k += kRasterThreads) {
+                const int je = k / 15, c = k - je * 15;
+                float v = 0.f;
+#pragma unroll
+                for (int w = 0; w < kRasterThreads / 32; ++w) v += slot[w][je][c];
+                if (v != 0.f) {
+                    const uint32_t r = srank[lo + je];
+                    if (c < 6) atomicAdd(&screen[(size_t)c * scap + r], (double)v);
+                    else atomicAdd(&E.screen[(size_t)(c - 6) * scap + r], v);
                 }
             }
             __syncthreads();
@@ -599,17 +613,15 @@ void launch_ext_prep(const SceneK& S, const CamK& C, const FrameDev* fd, const u
 }
 
 void launch_ext_fwd(const RecK& rec, const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd,
-                    const uint4* ranges_all, int nchunks, const uint32_t* vals, const FixupK& fx, const PixK& px,
-                    int nf, const ExtK& E, cudaStream_t st) {
+                    const ScanK& sc, const FixupK& fx, const PixK& px, int nf, const ExtK& E, cudaStream_t st) {
     const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
-    k_ext_fwd<<<grid, kRasterThreads, 0, st>>>(rec, S, C, O, fd, ranges_all, nchunks, vals, fx, px, nf, E);
+    k_ext_fwd<<<grid, kRasterThreads, 0, st>>>(rec, S, C, O, fd, sc, fx, px, nf, E);
 }
 
-void launch_ext_bwd(const RecK& rec, const OptK& O, int W, int H, int nf, const uint4* ranges_all, int nchunks,
-                    const uint32_t* vals, const PixK& px, const UpK& up, const ExtK& E, float* screen, int scap,
-                    cudaStream_t st) {
+void launch_ext_bwd(const RecK& rec, const OptK& O, int W, int H, int nf, const ScanK& sc, const PixK& px,
+                    const UpK& up, const ExtK& E, double* screen, int scap, cudaStream_t st) {
     const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
-    k_ext_bwd<<<grid, kRasterThreads, 0, st>>>(rec, O, W, H, nf, ranges_all, nchunks, vals, px, up, E, screen, scap);
+    k_ext_bwd<<<grid, kRasterThreads, 0, st>>>(rec, O, W, H, nf, sc, px, up, E, screen, scap);
 }
 
 void launch_chain_ext(const SceneK& S, const CamK& C, const FrameK& F, const uint32_t* touched, const ExtK& E,

@@ -307,24 +307,26 @@ __global__ void __launch_bounds__(128) k_fixup_mark(OptK O, FixupK fx, PixK px, 
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int count = *fx.overflow ? 0 : *px.n_flagged;
-    const int ntiles = O.tiles_x * O.tiles_y;
     const int stamp = fd->stamp;
+    const int V = *fx.sc.n_rank;
     for (int i = warp; i < count; i += nwarps) {
         const int pix = px.flagged[i] & 0xffffff;
         const int x = pix % W, y = pix / W;
-        const int tile = (y / O.ts) * O.tiles_x + (x / O.ts);
+        const int tx = x / O.ts, ty = y / O.ts;
         const int limit = (px.last[pix] & kLastMask) + 64;
-        for (int ch = 0; ch < fx.nchunks; ++ch) {
-            const uint4 rg = fx.ranges_all[(size_t)ch * ntiles + tile];
-            if (rg.w || (int)rg.z >= limit) break;
-            const uint32_t end = rg.x + min(rg.y, (uint32_t)(limit - (int)rg.z));
-            for (uint32_t e = rg.x + lane; e < end; e += 32) {
-                const uint32_t g = fx.vals[e];
+        int e = 0;
+        for (int r0 = 0; r0 < V && e < limit; r0 += 32) {
+            const int r = r0 + lane;
+            const bool cov = r < V && tile_covers(fx.sc.trect[r], tx, ty);
+            const unsigned m = __ballot_sync(0xffffffffu, cov);
+            if (cov && e + __popc(m & ((1u << lane) - 1u)) < limit) {
+                const uint32_t g = fx.sc.ord[r];
                 if (atomicExch(&fx.stamp[g], stamp) != stamp) {
                     const int slot = atomicAdd(fx.work_n, 1);
                     fx.work[slot] = (int)g;
                 }
             }
+            e += __popc(m);
         }
     }
 }
@@ -449,9 +451,54 @@ __device__ __forceinline__ void fixup_batch(const SceneK& S, const CamK& C, cons
     __syncwarp();
 }
 
+// A warp's scan of the rank order for one pixel's tile: kScanRanks ranks per step (lane
+// j tests ranks r0 + 32 k + j), covering ranks appended in rank order (ascending or
+// descending scan) to the warp's queue, so the expensive per-entry fp64 work always runs
+// on full batches of 32 entries (a tile list holds ~1-7 % of the ranks).
+constexpr int kScanK = 4;                    // rank groups of 32 per step
+constexpr int kQueue = 32 + 32 * kScanK;     // entries a queue can hold after a step
+__device__ __forceinline__ void queue_step(const ScanK& sc, int r0, int V, bool descending, int tx, int ty,
+                                           int* qg, int* qr, int& qn, int lane) {
+    const uint32_t below = (1u << lane) - 1u;
+#pragma unroll
+    for (int k = 0; k < kScanK; ++k) {
+        const int r = descending ? r0 - 1 - (32 * k + lane) : r0 + 32 * k + lane;
+        const bool cov = r >= 0 && r < V && tile_covers(sc.trect[r], tx, ty);
+        const unsigned m = __ballot_sync(0xffffffffu, cov);
+        if (cov) {
+            qg[qn + __popc(m & below)] = (int)sc.ord[r];
+            qr[qn + __popc(m & below)] = r;
+        }
+        qn += __popc(m);
+    }
+    __syncwarp();
+}
+// drop the first 32 queued entries
+__device__ __forceinline__ void queue_pop32(int* qg, int* qr, int& qn, int lane) {
+    int g[kQueue / 32 - 1], r[kQueue / 32 - 1];
+#pragma unroll
+    for (int k = 0; k < kQueue / 32 - 1; ++k) {
+        const int i = 32 + 32 * k + lane;
+        g[k] = i < qn ? qg[i] : 0;
+        r[k] = i < qn ? qr[i] : 0;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kQueue / 32 - 1; ++k) {
+        const int i = 32 * k + lane;
+        if (i + 32 < qn) {
+            qg[i] = g[k];
+            qr[i] = r[k];
+        }
+    }
+    qn = max(qn - 32, 0);
+    __syncwarp();
+}
+
 __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd, FixupK fx,
                                                PixK px, int nf) {
     __shared__ FixSlot slots[4][32];
+    __shared__ int queue_g[4][kQueue], queue_r[4][kQueue];
     const FrameK F = fd->F;
     const int stamp = fd->stamp;
     const int lane = threadIdx.x & 31;
@@ -459,58 +506,37 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, const F
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     FixSlot* slot = slots[threadIdx.x >> 5];
     const int count = *fx.overflow ? 0 : *px.n_flagged;
-    const int W = C.W, H = C.H;
-    const int ntiles = O.tiles_x * O.tiles_y;
-    const size_t HW = (size_t)W * H;
-    const int V = *fx.n_visible;
+    const int W = C.W;
+    const size_t HW = (size_t)W * C.H;
+    const int V = *fx.sc.n_rank;
     const uint32_t lanes_below = (1u << lane) - 1u;
     for (int i = warp; i < count; i += nwarps) {
         const int pix = px.flagged[i] & 0xffffff;
         const int x = pix % W, y = pix / W;
         const int tx = x / O.ts, ty = y / O.ts;
-        const int tile = ty * O.tiles_x + tx;
         FixupAcc a;
         a.T = 1.0; a.SW = 0.0; a.SD = 0.0; a.Tpre = 1.0; a.Tpre_le = 1.0;
         a.dref = 0.0; a.SDs = 0.0; a.SD2s = 0.0;
         for (int c = 0; c < 8; ++c) a.accQ[c] = 0.0;
         a.nc = 0; a.processed = 0; a.last_eff = -1; a.done = false;
-        int scan_from = -1;  // rank where the tile stopped being binned
-        int list_end = 0;    // entries of the chunk lists the walk reached
-        for (int ch = 0; ch < fx.nchunks && !a.done; ++ch) {
-            const uint4 rg = fx.ranges_all[(size_t)ch * ntiles + tile];  // (start, len, cum, skipped)
-            if (rg.w) {
-                scan_from = fx.chunk_rank0[ch];
-                break;
+        // the tile's list: ranks whose tile rect covers the tile, in rank order, 32 at a time
+        int* qg = queue_g[threadIdx.x >> 5];
+        int* qr = queue_r[threadIdx.x >> 5];
+        int qn = 0, r_end = V;
+        for (int r0 = 0; !a.done && (r0 < V || qn > 0); r0 += 32 * kScanK) {
+            if (r0 < V) queue_step(fx.sc, r0, V, false, tx, ty, qg, qr, qn, lane);
+            const bool flush = r0 + 32 * kScanK >= V;  // no more ranks: run the partial batch
+            while (!a.done && (qn >= 32 || (flush && qn > 0))) {
+                const bool is_e = lane < qn;
+                const int e0 = a.processed;
+                fixup_batch(S, C, O, F, fx, stamp, nf, x, y, is_e, is_e ? qg[lane] : 0, e0 + lane, slot, a, lane);
+                if (!a.done) a.processed = e0 + min(qn, 32);
+                else r_end = qr[a.processed - 1 - e0] + 1;  // rank after the terminating entry
+                queue_pop32(qg, qr, qn, lane);
             }
-            list_end = (int)(rg.z + rg.y);
-            const uint32_t end = rg.x + rg.y;
-            for (uint32_t b = rg.x; b < end && !a.done; b += 32) {
-                const uint32_t e = b + lane;
-                const bool is_e = e < end;
-                fixup_batch(S, C, O, F, fx, stamp, nf, x, y, is_e, is_e ? (int)fx.vals[e] : 0, (int)(rg.z + (e - rg.x)),
-                            slot, a, lane);
-            }
-            if (!a.done) a.processed = (int)(rg.z + rg.y);
-        }
-        if (!a.done && scan_from < 0 && fx.binned_end_rank < V) scan_from = fx.binned_end_rank;
-        // Rare: the exact composite continues past the binned entries of this tile;
-        // walk the remaining Gaussians in rank (== list) order directly.
-        for (int r0 = scan_from; r0 >= 0 && r0 < V && !a.done; r0 += 32) {
-            const int r = r0 + lane;
-            int g = 0;
-            bool cov = false;
-            if (r < V) {
-                g = (int)sorted_at(fx.sorted_gidx, fx.ties, r, V);
-                const uint2 rc = fx.rect[g];
-                const int x0 = rc.x & 0xffff, x1 = rc.x >> 16, y0 = rc.y & 0xffff, y1 = rc.y >> 16;
-                cov = x0 / O.ts <= tx && tx <= (x1 - 1) / O.ts && y0 / O.ts <= ty && ty <= (y1 - 1) / O.ts;
-            }
-            const unsigned cm = __ballot_sync(0xffffffffu, cov);
-            fixup_batch(S, C, O, F, fx, stamp, nf, x, y, cov, g, a.processed + __popc(cm & lanes_below), slot, a, lane);
-            if (!a.done) a.processed += __popc(cm);
         }
         // the prefix order ended with the pixel alive: the frame is redone with the full order
-        if (!a.done && lane == 0 && V < *fx.n_all) atomicOr(fx.overflow, 8);
+        if (!a.done && lane == 0 && V < *fx.sc.n_all) atomicOr(fx.overflow, 8);
         if (lane == 0) {
             const size_t o = (size_t)y * W + x;
             #pragma unroll
@@ -551,15 +577,16 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, const F
             if (px.n_processed) px.n_processed[o] = a.processed;
             const int le = a.last_eff >= 0 ? a.last_eff : a.processed;
             const double Tpre = a.last_eff >= 0 ? a.Tpre_le : a.Tpre;
-            // the fp64 backward replays this walk (its rank-scan part from shared memory)
-            const bool bwd64 = i < fx.state_cap && le - list_end <= kFixBwdTail;
+            // the fp64 backward replays this walk back to front from where it stopped
+            const bool bwd64 = i < fx.state_cap;
             if (bwd64) {
                 FixState f;
                 f.T = a.T; f.Tpre = Tpre; f.SW = a.SW;
                 f.dref = a.dref; f.SDs = a.SDs; f.SD2s = a.SD2s;
-                f.n_list = list_end;
-                f.scan_from = scan_from;
+                f.r_end = r_end;
+                f.e_end = a.processed;
                 fx.state[i] = f;
+                fx.fix_idx[o] = i;
             }
             px.last[o] = le | kLastFixed | (bwd64 ? kLastBwd64 : 0);
             px.T_pre[o] = (float)Tpre;
@@ -625,9 +652,31 @@ struct BwdPix {
     bool first;                     // the pixel's last contributor not reached yet
 };
 
+// Where a recomposited pixel's per-entry gradients go: added atomically to the pass's
+// screen-space gradients, or (deterministic mode) to the (rank, tile, sub-block) slot the
+// raster backward filled, by the one warp that owns that raster block.
+struct AtomicOut {
+    double* screen;
+    int scap;
+    __device__ __forceinline__ void add(int c, int g, int r, double v) const {
+        (void)r;
+        atomicAdd(&screen[(size_t)c * scap + g], v);
+    }
+};
+struct DetOut {
+    ScanK sc;
+    int tx, ty, sb;
+    __device__ __forceinline__ void add(int c, int g, int r, double v) const {
+        (void)g;
+        float* p = &sc.det_part[det_slot(sc, r, sc.trect[r], tx, ty, sb) * 8 + c];
+        *p = (float)((double)*p + v);
+    }
+};
+
+template <class Out>
 __device__ __forceinline__ void fixbwd_batch(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
                                              const FixupK& fx, int stamp, int nf, int x, int y, bool is_entry, int g,
-                                             BwdPix& b, float* __restrict__ screen, int scap, int lane) {
+                                             int rk, BwdPix& b, const Out& out, int lane) {
     bool inc = false;
     double alpha = 0.0, G = 0.0, dx = 0.0, dy = 0.0, coef = 0.0, depth = 0.0;
     Rec64 r;
@@ -698,7 +747,7 @@ __device__ __forceinline__ void fixbwd_batch(const SceneK& S, const CamK& C, con
                               w2 * coef * sd + b.uDraw * w + b.uDD * 4.0 * w * (b.SW * (depth - b.dref) - b.SDs)};
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-            if (g8[c] != 0.0) atomicAdd(&screen[(size_t)c * scap + g], (float)g8[c]);
+            if (g8[c] != 0.0) out.add(c, g, rk, g8[c]);
     }
     // carry to the next batch (the entries in front): values after lane 31
     b.Tnext = __shfl_sync(kFull, Tk, 31);
@@ -709,109 +758,123 @@ __device__ __forceinline__ void fixbwd_batch(const SceneK& S, const CamK& C, con
 }
 }  // namespace
 
+// One recomposited pixel's fp64 backward: k_fixup's walk, back to front.
+template <class Out>
+__device__ void fixbwd_pixel(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F, const FixupK& fx,
+                             const PixK& px, const UpK& up, int nf, int stamp, int i, int pix, int* qg, int* qr,
+                             const Out& out, int lane) {
+    const int W = C.W;
+    const size_t HW = (size_t)W * C.H;
+    const int V = *fx.sc.n_rank;
+    const int last = px.last[pix] & kLastMask;
+    const FixState st = fx.state[i];
+    const int x = pix % W, y = pix / W;
+    const int tx = x / O.ts, ty = y / O.ts;
+    const size_t o = (size_t)pix;
+    BwdPix b;
+    b.A = 0.0;
+    for (int f = 0; f < 2; ++f) {
+        b.us[f] = b.uc[f] = 0.0;
+        b.dpsi[f] = f < nf ? 4.0 * M_PI * S.freq[f] / S.c : 0.0;
+        if (f >= nf) continue;
+        if (up.quad) {
+            double q[4];
+            for (int c = 0; c < 4; ++c) {
+                q[c] = up.quad[(4 * f + c) * HW + o];
+                b.A += q[c] * O.bg_quad[4 * f + c];
+            }
+            b.us[f] = q[0] - q[2];
+            b.uc[f] = q[1] - q[3];
+        }
+        if (up.phasor) {
+            const double p0 = up.phasor[(2 * f + 0) * HW + o], p1 = up.phasor[(2 * f + 1) * HW + o];
+            b.A += p0 * O.bg_phasor[2 * f + 0] + p1 * O.bg_phasor[2 * f + 1];
+            b.us[f] += 2.0 * p1;
+            b.uc[f] += 2.0 * p0;
+        }
+    }
+    b.uDraw = up.depth_raw ? (double)up.depth_raw[o] : 0.0;
+    b.uW = up.weight ? (double)up.weight[o] : 0.0;
+    b.uDD = up.distortion ? (double)up.distortion[o] : 0.0;
+    b.uT = up.transm ? (double)up.transm[o] : 0.0;
+    b.SW = st.SW; b.dref = st.dref; b.SDs = st.SDs; b.SD2s = st.SD2s;
+    b.Tnext = st.Tpre;
+    b.B = 0.0;
+    b.R = 1.0;
+    b.first = true;
+    // the walk of k_fixup back to front: ranks downwards from where it stopped, covering ranks
+    // queued in descending order, so lane j of a batch holds the j-th entry from the back
+    int qn = 0, e_hi = st.e_end;
+    for (int r_hi = st.r_end; e_hi > 0 && (r_hi > 0 || qn > 0); r_hi -= 32 * kScanK) {
+        if (r_hi > 0) queue_step(fx.sc, r_hi, V, true, tx, ty, qg, qr, qn, lane);
+        const bool flush = r_hi - 32 * kScanK <= 0;
+        while (e_hi > 0 && (qn >= 32 || (flush && qn > 0))) {
+            const int e = e_hi - 1 - lane;  // queued entries in descending list order
+            const bool is_q = lane < qn && e >= 0;
+            fixbwd_batch(S, C, O, F, fx, stamp, nf, x, y, is_q && e < last, is_q ? qg[lane] : 0, is_q ? qr[lane] : 0,
+                         b, out, lane);
+            e_hi -= min(qn, 32);
+            queue_pop32(qg, qr, qn, lane);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(128) k_fixup_bwd(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd,
-                                                   FixupK fx, PixK px, UpK up, int nf, float* __restrict__ screen,
+                                                   FixupK fx, PixK px, UpK up, int nf, double* __restrict__ screen,
                                                    int scap) {
-    __shared__ int tail[4][kFixBwdTail];
-    const FrameK F = fd->F;
-    const int stamp = fd->stamp;
+    __shared__ int queue_g[4][kQueue], queue_r[4][kQueue];
     const int lane = threadIdx.x & 31;
-    int* my_tail = tail[threadIdx.x >> 5];
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int count = *fx.overflow ? 0 : min(*px.n_flagged, fx.state_cap);
-    const int W = C.W, H = C.H;
-    const int ntiles = O.tiles_x * O.tiles_y;
-    const size_t HW = (size_t)W * H;
-    const int V = *fx.n_visible;
-    const uint32_t lanes_below = (1u << lane) - 1u;
+    const AtomicOut out{screen, scap};
     for (int i = warp; i < count; i += nwarps) {
         const int pix = px.flagged[i] & 0xffffff;
-        const int lw = px.last[pix];
-        if (!(lw & kLastBwd64)) continue;
-        const int last = lw & kLastMask;
-        const FixState st = fx.state[i];
-        const int x = pix % W, y = pix / W;
-        const int tx = x / O.ts, ty = y / O.ts;
-        const int tile = ty * O.tiles_x + tx;
-        const size_t o = (size_t)pix;
-        BwdPix b;
-        b.A = 0.0;
-        for (int f = 0; f < 2; ++f) {
-            b.us[f] = b.uc[f] = 0.0;
-            b.dpsi[f] = f < nf ? 4.0 * M_PI * S.freq[f] / S.c : 0.0;
-            if (f >= nf) continue;
-            if (up.quad) {
-                double q[4];
-                for (int c = 0; c < 4; ++c) {
-                    q[c] = up.quad[(4 * f + c) * HW + o];
-                    b.A += q[c] * O.bg_quad[4 * f + c];
-                }
-                b.us[f] = q[0] - q[2];
-                b.uc[f] = q[1] - q[3];
-            }
-            if (up.phasor) {
-                const double p0 = up.phasor[(2 * f + 0) * HW + o], p1 = up.phasor[(2 * f + 1) * HW + o];
-                b.A += p0 * O.bg_phasor[2 * f + 0] + p1 * O.bg_phasor[2 * f + 1];
-                b.us[f] += 2.0 * p1;
-                b.uc[f] += 2.0 * p0;
-            }
-        }
-        b.uDraw = up.depth_raw ? (double)up.depth_raw[o] : 0.0;
-        b.uW = up.weight ? (double)up.weight[o] : 0.0;
-        b.uDD = up.distortion ? (double)up.distortion[o] : 0.0;
-        b.uT = up.transm ? (double)up.transm[o] : 0.0;
-        b.SW = st.SW; b.dref = st.dref; b.SDs = st.SDs; b.SD2s = st.SD2s;
-        b.Tnext = st.Tpre;
-        b.B = 0.0;
-        b.R = 1.0;
-        b.first = true;
-        // entries [n_list, last): Gaussians covering the tile in rank order from scan_from
-        if (last > st.n_list && st.scan_from >= 0) {
-            const int need = last - st.n_list;
-            int got = 0;
-            for (int r0 = st.scan_from; r0 < V && got < need; r0 += 32) {
-                const int rk = r0 + lane;
-                int g = 0;
-                bool cov = false;
-                if (rk < V) {
-                    g = (int)sorted_at(fx.sorted_gidx, fx.ties, rk, V);
-                    const uint2 rc = fx.rect[g];
-                    const int x0 = rc.x & 0xffff, x1 = rc.x >> 16, y0 = rc.y & 0xffff, y1 = rc.y >> 16;
-                    cov = x0 / O.ts <= tx && tx <= (x1 - 1) / O.ts && y0 / O.ts <= ty && ty <= (y1 - 1) / O.ts;
-                }
-                const unsigned m = __ballot_sync(kFull, cov);
-                const int slot = got + __popc(m & lanes_below);
-                if (cov && slot < need) my_tail[slot] = g;
-                got += __popc(m);
-            }
-            __syncwarp();
-            for (int top = need - 1; top >= 0; top -= 32) {
-                const int k = top - lane;
-                fixbwd_batch(S, C, O, F, fx, stamp, nf, x, y, k >= 0, k >= 0 ? my_tail[k] : 0, b, screen, scap, lane);
-            }
-            __syncwarp();
-        }
-        // the chunk lists the forward walked, back to front
-        int ch_end = 0;
-        while (ch_end < fx.nchunks && !fx.ranges_all[(size_t)ch_end * ntiles + tile].w) ++ch_end;
-        const int lim = min(last, st.n_list);
-        for (int ch = ch_end - 1; ch >= 0; --ch) {
-            const uint4 rg = fx.ranges_all[(size_t)ch * ntiles + tile];  // (start, len, cum, skipped)
-            if ((int)rg.z >= lim || rg.y == 0) continue;
-            const int n_here = min((int)rg.y, lim - (int)rg.z);
-            for (int top = n_here - 1; top >= 0; top -= 32) {
-                const int k = top - lane;
-                fixbwd_batch(S, C, O, F, fx, stamp, nf, x, y, k >= 0, k >= 0 ? (int)fx.vals[rg.x + k] : 0, b, screen,
-                             scap, lane);
-            }
+        if (!(px.last[pix] & kLastBwd64)) continue;
+        fixbwd_pixel(S, C, O, fd->F, fx, px, up, nf, fd->stamp, i, pix, queue_g[threadIdx.x >> 5],
+                     queue_r[threadIdx.x >> 5], out, lane);
+    }
+}
+
+// Deterministic: warp w owns raster block (tile, sub-block) rb and processes its recomposited
+// pixels in pixel order, adding into that block's own slots after the raster backward.
+__global__ void __launch_bounds__(128) k_fixup_bwd_det(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd,
+                                                       FixupK fx, PixK px, UpK up, int nf) {
+    __shared__ int queue_g[4][kQueue], queue_r[4][kQueue];
+    if (*fx.overflow) return;
+    const int lane = threadIdx.x & 31;
+    const int rb = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nsub2 = O.sub * O.sub;
+    if (rb >= O.tiles_x * O.tiles_y * nsub2) return;
+    const int tile = rb / nsub2, sb = rb % nsub2;
+    const int tx = tile % O.tiles_x, ty = tile / O.tiles_x;
+    const DetOut out{fx.sc, tx, ty, sb};
+    for (int k = 0; k < kTile * kTile; k += 32) {
+        const int q = k + lane;
+        const int lx = (sb % O.sub) * kTile + (q % kTile), ly = (sb / O.sub) * kTile + q / kTile;
+        const int x = tx * O.ts + lx, y = ty * O.ts + ly;
+        const bool valid = lx < O.ts && ly < O.ts && x < C.W && y < C.H;
+        const int pix = valid ? y * C.W + x : 0;
+        unsigned m = __ballot_sync(0xffffffffu, valid && (px.last[pix] & kLastBwd64));
+        while (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1u;
+            const int p = __shfl_sync(0xffffffffu, pix, j);
+            fixbwd_pixel(S, C, O, fd->F, fx, px, up, nf, fd->stamp, fx.fix_idx[p], p, queue_g[threadIdx.x >> 5],
+                         queue_r[threadIdx.x >> 5], out, lane);
         }
     }
 }
 
 void launch_fixup_bwd(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd, const FixupK& fx,
-                      const PixK& px, const UpK& up, int nf, float* screen, int scap, cudaStream_t st) {
+                      const PixK& px, const UpK& up, int nf, double* screen, int scap, cudaStream_t st) {
     k_fixup_bwd<<<148, 128, 0, st>>>(S, C, O, fd, fx, px, up, nf, screen, scap);
+}
+
+void launch_fixup_bwd_det(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd, const FixupK& fx,
+                          const PixK& px, const UpK& up, int nf, cudaStream_t st) {
+    const int nrb = O.tiles_x * O.tiles_y * O.sub * O.sub;
+    k_fixup_bwd_det<<<(nrb + 3) / 4, 128, 0, st>>>(S, C, O, fd, fx, px, up, nf);
 }
 
 // Intermediates the chain needs, recomputed in fp64 with reciprocals instead of
@@ -927,20 +990,20 @@ __device__ __noinline__ double3 sh_chain(const float4* scale_amp, const float4* 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128, 4) k_chain(SceneK S, CamK C, OptK O, FrameK F,
                                                const uint32_t* __restrict__ touched,
-                                               float* __restrict__ screen,
+                                               double* __restrict__ screen,
                                                float4* __restrict__ grads) {
     const int gi = blockIdx.x * blockDim.x + threadIdx.x;
     if (gi >= S.n || touched[gi] == 0u) return;
-    float g8[8];
+    double g8[8];
     bool any = false;
     for (int c = 0; c < 8; ++c) {
         g8[c] = screen[(size_t)c * S.n + gi];
-        any |= g8[c] != 0.f;
+        any |= g8[c] != 0.0;
     }
     // The chain is linear in the screen-space gradients: a splat no pixel reached
     // (e.g. behind every tile's termination point) contributes exactly nothing.
     if (!any) return;
-    for (int c = 0; c < 8; ++c) screen[(size_t)c * S.n + gi] = 0.f;
+    for (int c = 0; c < 8; ++c) screen[(size_t)c * S.n + gi] = 0.0;
     Chain64 s;
     chain_prep(S, C, O, F, gi, s);
     const double d_mean0 = g8[0], d_mean1 = g8[1], d_ca = g8[2], d_cb = g8[3], d_cc = g8[4];
@@ -1072,7 +1135,7 @@ __global__ void __launch_bounds__(128, 4) k_chain(SceneK S, CamK C, OptK O, Fram
 }
 
 void launch_chain(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
-                  const uint32_t* touched, float* screen, float4* grads, cudaStream_t st) {
+                  const uint32_t* touched, double* screen, float4* grads, cudaStream_t st) {
     if (S.n <= 0) return;
     const int bs = 128;
     k_chain<<<(S.n + bs - 1) / bs, bs, 0, st>>>(S, C, O, F, touched, screen, grads);

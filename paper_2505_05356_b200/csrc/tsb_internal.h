@@ -89,53 +89,39 @@ struct TieK {
     int32_t* abort;          // frame abort word (bit 1: a run longer than kMaxTieRun)
 };
 
-// Depth-chunked binning (tsb_bin.cu).  Ranks are cut into segments of kSeg
-// (one warp each); chunk c covers segments [seg0, seg0 + nseg).
-constexpr int kSeg = 128;
-struct BinK {
-    const uint32_t* sorted_gidx;
-    TieK ties;
-    const uint2* rect;
-    const int32_t* n_visible;
-    int ts, tiles_x, tiles_y, ntiles;
-    const int32_t* tile_blocks_done;  // raster blocks finished per tile
-    int blocks_per_tile;
-    int skip_done;                    // 0: emit full lists (parity mode)
-    uint32_t* hist;                   // [nseg][ntiles] counts -> exclusive offsets within the tile
-    int seg0, nseg, chunk;
-    uint32_t* tile_len;               // [ntiles]
-    uint32_t* tile_start;             // [ntiles] this chunk's list start per tile
-    uint4* ranges;                    // [ntiles] this chunk: (start, len, cum entries before, 0)
-    const uint4* prev_ranges;         // previous chunk's ranges (chunk > 0)
-    uint32_t* vals;                   // list storage (Gaussian indices)
-    uint32_t* list_off;               // device running offset into vals
-    uint32_t capacity;
-    int32_t* overflow;                // abort word: bit 0 list overflow, bit 1 long tie run, bit 3 prefix short
-    int nblocks;                      // raster blocks of the frame
-    const int32_t* blocks_done_total; // raster blocks finished so far
+// The frame's depth order as the raster kernels read it.  There are no per-tile
+// lists: the rank-order arrays are scanned by every raster block, which keeps the
+// ranks whose tile rect covers its tile -- exactly the reference's tile list
+// (splat.cpp:187-200, bbox tile ranges in global (depth, index) order) -- up to the
+// point where all its pixels have terminated (SURVEY finding 1: ~1 % of a list).
+//   ord[r]   Gaussian at rank r < *n_rank of the exact order (tsb_ties.cuh resolved)
+//   trect[r] its tile rect, (tx0 | tx1 << 16, ty0 | ty1 << 16)
+constexpr int kBlkListCap = 4096;  // list entries a raster block records for its backward
+struct ScanK {
+    const uint32_t* ord;
+    const uint2* trect;
+    const int32_t* n_rank;   // ranks in the order (the prefix end under the prefix sort)
+    const int32_t* n_all;    // visible Gaussians
+    int2* blk_term;          // per raster block: (rank after its last scanned pass, entries before that rank)
+    uint32_t* blk_list;      // per raster block: the ranks of the first kBlkListCap entries of its list, as
+                             // the forward consumed them (the backward walks them back instead of rescanning)
+    int32_t* abort;          // frame abort word (bit 3: the prefix ended with a pixel alive)
+    unsigned long long* work;  // profiling: [0] evaluations, [1] contributions (null: not counted)
+    // Deterministic backward (TSB_CH_DETERMINISTIC): a private partial-sum slot per (rank, tile
+    // of its rect, raster sub-block), reduced per Gaussian in a fixed order; null: atomics.
+    const uint32_t* det_off;   // [n_rank + 1] first slot of each rank (rect area x sub-blocks, scanned)
+    float* det_part;           // [slots][8]
+    int nsub2;                 // raster blocks per tile
 };
-
-// Forward state carried across chunk launches (SoA planes of npx).
-constexpr int kFwdStatePlanes = 9;
-struct FwdState {
-    float* f;    // 9 planes: T, Tpre, SW, SD, errT, accS0, accC0, accS1, accC1
-    double* d;   // 3 planes (distortion channel): dref, SDs, SD2s
-    int32_t* i;  // 3 planes: n_contrib, flags (1 done, 2 fixup, 4 finalized), last_eff
-    int npx;
-};
-
-struct ChunkK {
-    const uint4* ranges;  // this chunk's per-tile ranges
-    int first;            // chunk 0: initialise state
-    int chunk_end_rank;   // last chunk when >= n_visible
-    const int32_t* n_visible;   // end of the sorted order (the prefix end under the prefix sort)
-    const int32_t* n_all;       // visible Gaussians
-    int32_t* block_done;        // per raster block
-    int32_t* tile_blocks_done;  // per tile
-    int32_t* blocks_done_total;
-    int32_t* overflow;          // abort word (list overflow, ...): the host re-runs the frame
-    unsigned long long* work;   // profiling: [0] evaluations, [1] contributions (null: not counted)
-};
+// The slot of (rank r with tile rect tr, tile (tx, ty), raster sub-block sb).
+__device__ __forceinline__ size_t det_slot(const ScanK& sc, int r, uint2 tr, int tx, int ty, int sb) {
+    const int tx0 = tr.x & 0xffff, w = (int)(tr.x >> 16) - tx0 + 1, ty0 = tr.y & 0xffff;
+    return (size_t)sc.det_off[r] + ((size_t)(ty - ty0) * w + (tx - tx0)) * sc.nsub2 + sb;
+}
+__device__ __forceinline__ bool tile_covers(uint2 tr, int tx, int ty) {
+    return (int)(tr.x & 0xffffu) <= tx && tx <= (int)(tr.x >> 16) && (int)(tr.y & 0xffffu) <= ty &&
+           ty <= (int)(tr.y >> 16);
+}
 
 // Per-pixel raster state written by the forward pass for the backward pass.
 struct PixK {
@@ -201,29 +187,19 @@ struct Rec64 {
 
 // fp64 end state of a recomposited pixel (k_fixup), what its fp64 backward (k_fixup_bwd)
 // needs: T_N, T before the last contributor (before the alpha == 1 entry when T hit 0),
-// sum w, the distortion moments about the first contributor's depth, the number of entries
-// in the tile's chunk lists the walk covered, and where its rank scan past them began.
+// sum w, the distortion moments about the first contributor's depth, and where its walk
+// stopped: the rank after its last processed entry and the entries processed.
 struct FixState {
     double T, Tpre, SW, dref, SDs, SD2s;
-    int n_list, scan_from;
+    int r_end, e_end;
 };
 constexpr int kFixStateCap = 1 << 16;  // recomposited pixels per frame with an fp64 backward
-constexpr int kFixBwdTail = 256;  // rank-scan entries the fp64 backward can replay per pixel
 constexpr int kLastFixed = (int)0x80000000;  // PixK::last bit 31: pixel recomposited in fp64
 constexpr int kLastBwd64 = 0x40000000;       // bit 30: its backward runs in fp64 (k_fixup_bwd)
 constexpr int kLastMask = 0x3fffffff;
 
 struct FixupK {
-    const uint4* ranges_all;  // [nchunks][ntiles] (start, len, cum, skipped)
-    int nchunks;
-    const int* chunk_rank0;   // device [nchunks] first rank of each chunk
-    int binned_end_rank;      // first rank after the last binned chunk
-    const uint32_t* vals;
-    const uint32_t* sorted_gidx;
-    TieK ties;
-    const uint2* rect;
-    const int32_t* n_visible;  // end of the sorted order (prefix end under the prefix sort)
-    const int32_t* n_all;      // visible Gaussians
+    ScanK sc;          // the order the walk scans (ranks whose rect covers the pixel's tile)
     int32_t* overflow;
     int* stamp;        // [n] frame stamp of the cached record (FrameDev::stamp)
     int* work;         // [n] Gaussians queued for the record cache
@@ -231,13 +207,17 @@ struct FixupK {
     Rec64* cache;      // [n]
     FixState* state;   // [state_cap] per flagged pixel (fix-up slot): fp64 state for k_fixup_bwd
     int state_cap;
+    int* fix_idx;      // [npx] fix-up slot of a recomposited pixel (the deterministic backward's lookup)
 };
 void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd, const FixupK& fx,
                   const PixK& px, int nf, cudaStream_t st);
 void launch_fixup_bwd(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd, const FixupK& fx,
-                      const PixK& px, const UpK& up, int nf, float* screen, int scap, cudaStream_t st);
+                      const PixK& px, const UpK& up, int nf, double* screen, int scap, cudaStream_t st);
+// deterministic: the same per pixel, one warp per raster block in pixel order, into the slots
+void launch_fixup_bwd_det(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd, const FixupK& fx,
+                          const PixK& px, const UpK& up, int nf, cudaStream_t st);
 void launch_chain(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F,
-                  const uint32_t* touched, float* screen, float4* grads, cudaStream_t st);
+                  const uint32_t* touched, double* screen, float4* grads, cudaStream_t st);
 void launch_param_cache(const SceneK& S, double* cov6, double* opac, float* cov6f, cudaStream_t st);
 constexpr size_t kPcacheWords = 10;  // doubles per Gaussian of the parameter cache (7 fp64 + 6 fp32 words)
 // tsb_bin.cu
@@ -266,25 +246,25 @@ void launch_materialize_order(const uint32_t* sorted, const TieK& T, const int32
                               cudaStream_t st);
 int launch_sort_depth64(const double* depth64, const uint32_t* touched, uint32_t* keys_a, uint32_t* keys_b,
                         uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch, cudaStream_t st);
-void bin_init();  // kernel attributes; call before any capture
-// one depth chunk: per-(segment, tile) counts, scans (ranges), list emission
-void launch_bin_count(const BinK& B, cudaStream_t st);
-void launch_bin_scan(const BinK& B, cudaStream_t st);
-void launch_bin_emit(const BinK& B, cudaStream_t st);
+// ord / trect of ranks r < *n_rank (the raster kernels' scan arrays, ScanK)
+void launch_order_ranks(const uint32_t* sorted, const TieK& T, const uint2* rect, int ts, const int32_t* n_rank,
+                        int n, uint32_t* ord, uint2* trect, cudaStream_t st);
+// deterministic backward: slot offsets of the ranks (device scan; writes det_off[0..V]) and
+// the fixed-order reduction of the slots into the screen-space gradients (+=)
+void launch_det_offsets(const ScanK& sc, uint32_t* det_off, uint32_t* total, cudaStream_t st);
+void launch_det_reduce(const ScanK& sc, int n, double* screen, int scap, cudaStream_t st);
+// parity / debug: the reference's complete tile lists (splat.cpp:187-200) from the scan arrays
+void launch_tile_counts(const ScanK& sc, int tiles_x, int ntiles, uint32_t* counts, cudaStream_t st);
+void launch_tile_lists(const ScanK& sc, int tiles_x, int ntiles, const int64_t* offsets, uint32_t* ids,
+                       cudaStream_t st);
 // tsb_raster.cu
-void launch_raster_fwd(const RecK& rec, const ChunkK& ck, const uint32_t* tile_vals, const OptK& O,
-                       int W, int H, int nf, PixK px, FwdState fs, const FrameDev* fd, bool loss, const ChW& ch_w,
-                       double* loss_part, cudaStream_t st);
+void raster_init();  // kernel attributes; call before any capture
+void launch_raster_fwd(const RecK& rec, const ScanK& sc, const OptK& O, int W, int H, int nf, PixK px,
+                       const FrameDev* fd, bool loss, const ChW& ch_w, double* loss_part, cudaStream_t st);
 void launch_fixup_loss(const PixK& px, int W, int H, int nf, const FrameDev* fd, const ChW& ch_w,
-                       double* loss_extra, cudaStream_t st);
-// CUDA-graph gate of depth chunk c >= 1: sets the chunk's IF-node condition to its
-// liveness (tsb_bin.cu chunk_live); a dead chunk's ranges are written empty here.
-// (the gate adds the chunk body's kernel count to *body_launches when live)
-void launch_chunk_gate(const BinK& B, cudaGraphConditionalHandle h, int32_t* body_launches, cudaStream_t st);
-int bin_chunk_kernels(const BinK& B);  // binning kernels of one depth chunk
-void launch_raster_bwd(const RecK& rec, const uint4* ranges_all, int nchunks, const uint32_t* tile_vals,
-                       const OptK& O, int W, int H, int nf, const float* dpsi, PixK px, const UpK& up,
-                       float* screen, int scap, double* bg_part, cudaStream_t st);
+                       double* loss_extra, bool deterministic, cudaStream_t st);
+void launch_raster_bwd(const RecK& rec, const ScanK& sc, const OptK& O, int W, int H, int nf, const float* dpsi,
+                       PixK px, const UpK& up, double* screen, int scap, double* bg_part, cudaStream_t st);
 // out[c] = (out[c] + sum_i part[i][c]) * scale; nothing when *abort != 0 (abort may be null).
 void launch_reduce_partials(const double* part, int nparts, int width, double* out,
                             double scale, const int32_t* abort, cudaStream_t st);
@@ -389,11 +369,9 @@ struct ExtK {
 void launch_ext_prep(const SceneK& S, const CamK& C, const FrameDev* fd, const uint32_t* touched, const ExtK& E,
                      const int32_t* abort, cudaStream_t st);
 void launch_ext_fwd(const RecK& rec, const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd,
-                    const uint4* ranges_all, int nchunks, const uint32_t* vals, const FixupK& fx, const PixK& px,
-                    int nf, const ExtK& E, cudaStream_t st);
-void launch_ext_bwd(const RecK& rec, const OptK& O, int W, int H, int nf, const uint4* ranges_all, int nchunks,
-                    const uint32_t* vals, const PixK& px, const UpK& up, const ExtK& E, float* screen, int scap,
-                    cudaStream_t st);
+                    const ScanK& sc, const FixupK& fx, const PixK& px, int nf, const ExtK& E, cudaStream_t st);
+void launch_ext_bwd(const RecK& rec, const OptK& O, int W, int H, int nf, const ScanK& sc, const PixK& px,
+                    const UpK& up, const ExtK& E, double* screen, int scap, cudaStream_t st);
 // flow_loss (losses.cpp:168-251) on the rendered flow channels; 3 kernels.
 struct FlowK {
     const float* target[2];  // [3][H][W] (u, v, valid) per direction, null = absent

@@ -1,10 +1,11 @@
 // Tile rasterizer: forward composite (splat.cpp:209-339) and analytic backward
 // (splat.cpp:347-543) in fp32, one 16x16 CTA per tile, one thread per pixel.
 //
-// Records are staged per batch of 256 list entries in shared memory (each
-// thread loads one rank's record; every thread then reads the same entry ->
-// broadcast, conflict-free).  Termination is block-wide via
-// __syncthreads_count.
+// There are no tile lists: each block scans the global rank order (ScanK, 256 ranks
+// per pass) and stages the records of the ranks whose tile rect covers its tile --
+// the reference's tile list, in order -- in shared memory (every thread then reads the
+// same entry -> broadcast, conflict-free).  Termination is block-wide via
+// __syncthreads_count; the block stops scanning when all its pixels are done.
 //
 // Parity machinery: the reference decides maha <= cutoff^2,
 // alpha >= 1/255 and T < 1e-4 in fp64.  The fp32 composite tracks a bound on
@@ -24,14 +25,19 @@
 
 namespace tsb {
 
+// Staged entries of one block: up to kBatchCap list entries (a scan pass adds at
+// most kRasterThreads; a batch is composited once it holds kRasterThreads or more).
+constexpr int kBatchCap = 2 * kRasterThreads;
+
 template <int NF>
 struct Smem {
-    float4 A[kRasterThreads];
-    float4 B[kRasterThreads];
-    float4 C[kRasterThreads];
-    float4 D[NF > 1 ? kRasterThreads : 1];
-    uint8_t wmask[kRasterThreads];                      // per staged entry: warps it can reach
-    uint8_t list[kRasterThreads / 32][kRasterThreads];  // per warp: its entries, in list order
+    float4 A[kBatchCap];
+    float4 B[kBatchCap];
+    float4 C[kBatchCap];
+    float4 D[NF > 1 ? kBatchCap : 1];
+    uint8_t wmask[kBatchCap];                        // per staged entry: warps it can reach
+    uint16_t list[kRasterThreads / 32][kBatchCap];   // per warp: its entries, in list order
+    int wsum[2][kRasterThreads / 32];                 // scan-pass compaction (double-buffered by pass parity)
 };
 
 // Pixel of thread tid in its 16 x 16 block: warp w owns the 8 x 4 sub-block at
@@ -61,31 +67,42 @@ __device__ __forceinline__ uint32_t warps_reached(const float4& a, const float4&
     return cols & rows;
 }
 
+// Stage the record of Gaussian g at batch slot `slot` (mean relative to the block origin).
+template <int NF, typename SM>
+__device__ __forceinline__ void stage_entry(SM& sm, const RecK& rec, uint32_t g, int slot, float ox, float oy,
+                                            float outside) {
+    const float4 a = stage_A(rec.A[g], ox, oy), bb = rec.B[g];
+    sm.A[slot] = a;
+    sm.B[slot] = bb;
+    sm.C[slot] = rec.C[g];
+    if (NF > 1) sm.D[slot] = rec.D[g];
+    sm.wmask[slot] = (uint8_t)warps_reached(a, bb, outside);
+}
+
 // ---------------------------------------------------------------------------
-// Forward composite of one depth chunk.  Per-pixel state (T, accumulators,
-// counters) is carried across chunk launches in FwdState; a pixel is finalised
-// (outputs, fix-up flag, loss epilogue) in the launch in which it terminates,
-// or in the last chunk.  Blocks whose pixels are all done mark themselves so
-// later chunks neither bin nor raster them.
+// Forward composite (splat.cpp:245-336), one launch per frame.  The block scans the
+// rank order 256 ranks per pass and stages the ranks whose tile rect covers its
+// tile -- its reference tile list, in order -- then composites a batch once it
+// holds >= 256 entries, until every pixel of the block has terminated.  A pixel
+// is finalised (outputs, fix-up flag, loss epilogue) at the end.
 // WORK: count evaluations / contributions (profiling runs only; a template so the
 // per-evaluation counter costs nothing otherwise).
 template <int NF, bool DIST, bool WORK>
-__global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK ck, const uint32_t* __restrict__ vals,
-                                                                OptK O, int W, int H, PixK px, FwdState fs,
+__global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK sc, OptK O, int W, int H, PixK px,
                                                                 const FrameDev* __restrict__ fd, int loss, ChW chw,
                                                                 double* __restrict__ loss_part) {
     __shared__ Smem<NF> sm;
     __shared__ float red[kRasterThreads / 32];
-    if (ck.block_done[blockIdx.x] || *ck.overflow) return;
+    if (*sc.abort) return;
     const float* __restrict__ target = loss ? fd->target : nullptr;
     const int nsub = O.sub * O.sub;
     const int tile = blockIdx.x / nsub, sb = blockIdx.x % nsub;
+    const int ttx = tile % O.tiles_x, tty = tile / O.tiles_x;
     const int tid = threadIdx.x;
     const int bx_ = block_px(tid), by_ = block_py(tid);
     const int lx = (sb % O.sub) * kTile + bx_, ly = (sb / O.sub) * kTile + by_;
-    const int x = (tile % O.tiles_x) * O.ts + lx, y = (tile / O.tiles_x) * O.ts + ly;
+    const int x = ttx * O.ts + lx, y = tty * O.ts + ly;
     const bool active = lx < O.ts && ly < O.ts && x < W && y < H;
-    const uint4 rg = ck.ranges[tile];  // (start, len, cum, -)
     const float ox = (float)(x - bx_), oy = (float)(y - by_);  // block origin
     const float pcx = (float)bx_ + 0.5f, pcy = (float)by_ + 0.5f;
     const size_t HW = (size_t)W * H, o = active ? (size_t)y * W + x : 0;
@@ -95,71 +112,53 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
     float accS[NF], accC[NF];
 #pragma unroll
     for (int f = 0; f < NF; ++f) accS[f] = accC[f] = 0.f;
-    uint32_t n_eval = 0, nc0 = 0;  // profiling work counters
+    uint32_t n_eval = 0;  // profiling work counter
     float dref = 0.f;  // distortion: fp64 moments about the first contributor's depth
     double SDs = 0.0, SD2s = 0.0;
-    int nc = 0, flags = 0, last_eff = -1;
-    if (active && !ck.first) {
-        T = fs.f[0 * (size_t)fs.npx + o];
-        Tpre = fs.f[1 * (size_t)fs.npx + o];
-        Tpre_eff = Tpre;
-        SW = fs.f[2 * (size_t)fs.npx + o];
-        SD = fs.f[3 * (size_t)fs.npx + o];
-        dT = fs.f[4 * (size_t)fs.npx + o];
-#pragma unroll
-        for (int f = 0; f < NF; ++f) {
-            accS[f] = fs.f[(5 + 2 * f) * (size_t)fs.npx + o];
-            accC[f] = fs.f[(6 + 2 * f) * (size_t)fs.npx + o];
-        }
-        if (DIST) {
-            dref = (float)fs.d[o];
-            SDs = fs.d[(size_t)fs.npx + o];
-            SD2s = fs.d[2 * (size_t)fs.npx + o];
-        }
-        nc = fs.i[0 * (size_t)fs.npx + o];
-        flags = fs.i[1 * (size_t)fs.npx + o];
-        last_eff = fs.i[2 * (size_t)fs.npx + o];
-    }
-    const bool was_done = !active || (flags & 1);
-    bool done = was_done;
-    nc0 = (uint32_t)nc;
-    int flag = (flags >> 1) & 7;  // reasons: 1 maha band, 2 alpha band, 4 T band
-    int processed = (int)(rg.z + rg.y);
+    int nc = 0, flag = 0, last_eff = -1, processed = 0;  // flag reasons: 1 maha band, 2 alpha band, 4 T band
+    bool done = !active;
     const float cut2 = O.cut2_f, thr = O.alpha_thr_f, fl = O.floor_f;
     const float coarseM = kCoarseMaha * cut2, coarseA = kCoarseAlpha * thr;
     const float outside = cut2 + coarseM;  // maha above this is outside, with no ambiguity to check
     // common-path tests with one compare each; the exact windows are re-tested inside
     const float m_lo = cut2 - 2.f * coarseM, a_hi = thr + 2.f * coarseA;
-    const uint32_t end = rg.x + rg.y;
+    const int V = *sc.n_rank;
+    int r = 0, ebase = 0, cnt = 0, pass = 0;
 
     if (__syncthreads_count(done) < kRasterThreads) {
-        for (uint32_t b = rg.x; b < end; b += kRasterThreads) {
-            const uint32_t e = b + tid;
-            if (e < end) {
-                const uint32_t r = vals[e];
-                const float4 a = stage_A(rec.A[r], ox, oy), bb = rec.B[r];
-                sm.A[tid] = a;
-                sm.B[tid] = bb;
-                sm.C[tid] = rec.C[r];
-                if (NF > 1) sm.D[tid] = rec.D[r];
-                sm.wmask[tid] = (uint8_t)warps_reached(a, bb, outside);
+        while (r < V) {
+            // scan pass: ranks r .. r + 255, covering ones appended to the batch
+            const int rr = r + tid;
+            const bool cov = rr < V && tile_covers(sc.trect[rr], ttx, tty);
+            int total;
+            const int pos = scan_compact(cov, sm.wsum[pass & 1], total);
+            if (pos >= 0) {
+                const uint32_t g = sc.ord[rr];
+                stage_entry<NF>(sm, rec, g, cnt + pos, ox, oy, outside);
+                const int e = ebase + cnt + pos;  // list index: its rank is recorded for the backward
+                if (e < kBlkListCap) sc.blk_list[(size_t)blockIdx.x * kBlkListCap + e] = (uint32_t)rr;
             }
+            cnt += total;
+            r += kRasterThreads;
+            ++pass;
+            if (cnt < kRasterThreads && r < V) continue;  // keep filling (the next pass's barrier orders the slots)
             __syncthreads();
-            const int nb = min((uint32_t)kRasterThreads, end - b);
-            int cnt = 0;
-            if (__any_sync(0xffffffffu, !done)) {  // this warp's entries, in order
+            const int nb = cnt;
+            // this warp's entries, in order
+            int wcnt = 0;
+            if (__any_sync(0xffffffffu, !done)) {
                 const int lane = tid & 31, warp = tid >> 5;
                 for (int c = 0; c < nb; c += 32) {
                     const bool t = c + lane < nb && ((sm.wmask[c + lane] >> warp) & 1u);
                     const unsigned bal = __ballot_sync(0xffffffffu, t);
-                    if (t) sm.list[warp][cnt + __popc(bal & ((1u << lane) - 1u))] = (uint8_t)(c + lane);
-                    cnt += __popc(bal);
+                    if (t) sm.list[warp][wcnt + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)(c + lane);
+                    wcnt += __popc(bal);
                 }
                 __syncwarp();
             }
             if (!done) {
-                const uint8_t* wl = sm.list[tid >> 5];
-                for (int k = 0; k < cnt; ++k) {
+                const uint16_t* wl = sm.list[tid >> 5];
+                for (int k = 0; k < wcnt; ++k) {
                     const int j = wl[k];
                     if (WORK) ++n_eval;
                     const float4 A = sm.A[j], B = sm.B[j];
@@ -213,7 +212,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
                             flag |= 4;  // above, within the band: T - fl < 2 dT, and dT >= fl * rel err
                         } else {
                             if (fl - T < 2.f * fl * __fdividef(dT, T)) flag |= 4;  // |T - fl| < 2 fl rel err
-                            const int gidx_e = (int)(rg.z + (b - rg.x) + j + 1);
+                            const int gidx_e = ebase + j + 1;
                             if (T == 0.f && last_eff < 0) {
                                 last_eff = gidx_e;
                                 Tpre_eff = Tpre;
@@ -227,16 +226,18 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
                     }
                 }
             }
+            ebase += nb;
+            cnt = 0;
             if (__syncthreads_count(done) == kRasterThreads) break;
         }
     }
-
-    const bool is_last = ck.chunk_end_rank >= *ck.n_visible;
-    const bool finalize = !was_done && (done || is_last);
+    // every rank of the order scanned: a pixel still alive processed the whole list
+    if (!done) processed = ebase;
+    if (tid == 0 && sc.blk_term) sc.blk_term[blockIdx.x] = make_int2(min(r, V), ebase);
     // the prefix order ended with the pixel alive: the frame is redone with the full order
-    if (finalize && !done && *ck.n_all > *ck.n_visible) atomicOr(ck.overflow, 8);
+    if (active && !done && *sc.n_all > V) atomicOr(sc.abort, 8);
     float lpx = 0.f;
-    if (finalize) {
+    if (active) {
         // T's relative error bound grows by ~eps alpha / (1 - alpha) per contribution: an
         // almost opaque splat (1 - alpha lost to fp32 rounding) leaves T -- and every later
         // weight -- too inaccurate for the 1e-4 output bar: recomposite in fp64 (reason 8)
@@ -273,7 +274,6 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
         if (px.n_processed) px.n_processed[o] = processed;
         px.last[o] = last_eff >= 0 ? last_eff : processed;
         px.T_pre[o] = last_eff >= 0 ? Tpre_eff : Tpre;
-        fs.i[1 * (size_t)fs.npx + o] = 1;  // done (read by later chunks only if the block is not done)
         if (flag) {
             const int slot = atomicAdd(px.n_flagged, 1);
             px.flagged[slot] = (int)o | (flag << 24);
@@ -281,41 +281,21 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
             const float s2 = 2.f / (float)HW;
 #pragma unroll
             for (int c = 0; c < 4 * NF; ++c) {
-                const float r = q[c] - target[c * HW + o];
-                lpx = fmaf(chw.w[c] * r, r, lpx);
-                px.d_quad[c * HW + o] = chw.w[c] * s2 * r;
+                const float rr_ = q[c] - target[c * HW + o];
+                lpx = fmaf(chw.w[c] * rr_, rr_, lpx);
+                px.d_quad[c * HW + o] = chw.w[c] * s2 * rr_;
             }
         }
-    } else if (!was_done) {
-        fs.f[0 * (size_t)fs.npx + o] = T;
-        fs.f[1 * (size_t)fs.npx + o] = last_eff >= 0 ? Tpre_eff : Tpre;
-        fs.f[2 * (size_t)fs.npx + o] = SW;
-        fs.f[3 * (size_t)fs.npx + o] = SD;
-        fs.f[4 * (size_t)fs.npx + o] = dT;
-#pragma unroll
-        for (int f = 0; f < NF; ++f) {
-            fs.f[(5 + 2 * f) * (size_t)fs.npx + o] = accS[f];
-            fs.f[(6 + 2 * f) * (size_t)fs.npx + o] = accC[f];
-        }
-        if (DIST) {
-            fs.d[o] = dref;
-            fs.d[(size_t)fs.npx + o] = SDs;
-            fs.d[2 * (size_t)fs.npx + o] = SD2s;
-        }
-        fs.i[0 * (size_t)fs.npx + o] = nc;
-        fs.i[1 * (size_t)fs.npx + o] = flag << 1;
-        fs.i[2 * (size_t)fs.npx + o] = last_eff;
     }
-    const bool block_finished = __syncthreads_count(done || is_last) == kRasterThreads;
     if (WORK) {
-        unsigned long long ev = n_eval, cn = (uint32_t)nc - nc0;
+        unsigned long long ev = n_eval, cn = (uint32_t)nc;
         for (int m = 16; m > 0; m >>= 1) {
             ev += __shfl_xor_sync(0xffffffffu, ev, m);
             cn += __shfl_xor_sync(0xffffffffu, cn, m);
         }
         if ((tid & 31) == 0) {
-            atomicAdd(&ck.work[0], ev);
-            atomicAdd(&ck.work[1], cn);
+            atomicAdd(&sc.work[0], ev);
+            atomicAdd(&sc.work[1], cn);
         }
     }
     if (target) {
@@ -325,13 +305,8 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ChunkK 
         if (tid == 0) {
             double s = 0.0;
             for (int i = 0; i < kRasterThreads / 32; ++i) s += red[i];
-            loss_part[blockIdx.x] += s;
+            loss_part[blockIdx.x] = s;
         }
-    }
-    if (block_finished && tid == 0) {
-        ck.block_done[blockIdx.x] = 1;
-        atomicAdd(&ck.tile_blocks_done[tile], 1);
-        atomicAdd(ck.blocks_done_total, 1);
     }
 }
 
@@ -369,26 +344,45 @@ __global__ void k_fixup_loss(PixK px, int W, int H, int nf, const FrameDev* __re
 //   opaque pixels; here weight rides on the transmittance term (SW = 1 - T_N exactly) and
 //   depth is taken about the pixel's own mean depth c = depth_raw / weight, whose
 //   remainder c * prod(1 - alpha) also becomes part of B_0.
+//   The entries are the block's tile list walked back to front: the rank order is
+//   scanned downwards from where the forward stopped (ScanK::blk_term), 256 ranks per
+//   pass, and a batch is processed once it holds >= 256 entries.  Per entry, each warp
+//   reduces its 8 screen-space gradients with a 9-shuffle reduce-scatter into its own
+//   shared slot (no shared-memory atomics); per 32 entries the block sums the 8 warp
+//   slots in a fixed order and adds each sum to global memory with one atomic.
+constexpr int kBwdSub = 64;  // entries per slot round: 8 warps x 64 entries x 8 floats (dynamic smem)
+constexpr size_t kBwdSlotBytes = sizeof(float) * (kRasterThreads / 32) * kBwdSub * 8;
+
+template <int NF>
+struct BwdSmem {
+    float4 A[kBatchCap];
+    float4 B[kBatchCap];
+    float4 C[kBatchCap];
+    float4 D[NF > 1 ? kBatchCap : 1];
+    uint8_t wmask[kBatchCap];
+    uint32_t grank[kBatchCap];                       // Gaussian of each staged entry
+    uint32_t rrank[kBatchCap];                       // its rank (deterministic slots)
+    int wsum[2][kRasterThreads / 32];
+    int smax[kRasterThreads / 32];
+};
+
 template <int NF, bool EXTRA>
-__global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const uint4* __restrict__ ranges_all,
-                                                                int nchunks, const uint32_t* __restrict__ vals,
-                                                                OptK O, int W, int H, float dpsi0, float dpsi1,
-                                                                PixK px, UpK up,
-                                                                float* __restrict__ screen, int scap,
+__global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, ScanK sc, OptK O, int W, int H, float dpsi0,
+                                                                float dpsi1, PixK px, UpK up,
+                                                                double* __restrict__ screen, int scap,
                                                                 double* __restrict__ bg_part) {
-    __shared__ Smem<NF> sm;
-    __shared__ uint32_t srank[kRasterThreads];
-    __shared__ float sacc[kRasterThreads][9];  // padded: 8 grads per entry
-    __shared__ int smax[kRasterThreads / 32];
+    __shared__ BwdSmem<NF> sm;
     __shared__ float sbg[kRasterThreads / 32][6 * NF];
+    extern __shared__ float slot_mem[];  // [warp][kBwdSub][8]: per warp, per entry: its reduced gradients
+    float (*slot)[kBwdSub][8] = reinterpret_cast<float (*)[kBwdSub][8]>(slot_mem);
     if (*px.abort) return;  // aborted frame: no gradient is written (the host redoes it)
     const int nsub = O.sub * O.sub;
-    const int ntiles = O.tiles_x * O.tiles_y;
     const int tile = blockIdx.x / nsub, sb = blockIdx.x % nsub;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int ttx = tile % O.tiles_x, tty = tile / O.tiles_x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int bx_ = block_px(tid), by_ = block_py(tid);
     const int lx = (sb % O.sub) * kTile + bx_, ly = (sb / O.sub) * kTile + by_;
-    const int x = (tile % O.tiles_x) * O.ts + lx, y = (tile / O.tiles_x) * O.ts + ly;
+    const int x = ttx * O.ts + lx, y = tty * O.ts + ly;
     const bool active = lx < O.ts && ly < O.ts && x < W && y < H;
     const float ox = (float)(x - bx_), oy = (float)(y - by_);  // block origin
     const float pcx = (float)bx_ + 0.5f, pcy = (float)by_ + 0.5f;
@@ -460,17 +454,16 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
         for (int c = 0; c < 6 * NF; ++c) {
             float v = bgc[c];
             for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-            if (lane == 0) sbg[tid >> 5][c] = v;
+            if (lane == 0) sbg[warp][c] = v;
         }
     }
     int wmax = last;
     for (int m = 16; m > 0; m >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, m));
-    if (lane == 0) smax[tid >> 5] = wmax;
-    for (int c = 0; c < 9; ++c) sacc[tid][c] = 0.f;
+    if (lane == 0) sm.smax[warp] = wmax;
     __syncthreads();
     int bmax = 0;
 #pragma unroll
-    for (int i = 0; i < kRasterThreads / 32; ++i) bmax = max(bmax, smax[i]);
+    for (int i = 0; i < kRasterThreads / 32; ++i) bmax = max(bmax, sm.smax[i]);
     if (bg_part && tid < 6 * NF) {
         double s = 0.0;
         for (int i = 0; i < kRasterThreads / 32; ++i) s += sbg[i][tid];
@@ -478,34 +471,63 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
     }
     bool first = true;
     const float cut2 = O.cut2_f, thr = O.alpha_thr_f;
+    const uint32_t wbit = 1u << warp;
 
-    // entries are walked back to front over the concatenation of the chunk lists
-    for (int c = nchunks - 1; c >= 0 && bmax > 0; --c) {
-        const uint4 rg = ranges_all[(size_t)c * ntiles + tile];  // (start, len, cum)
-        if ((int)rg.z >= bmax || rg.y == 0) continue;
-        const int n_here = min((int)rg.y, bmax - (int)rg.z);
-        const int nbatch = (n_here + kRasterThreads - 1) / kRasterThreads;
-        for (int bi = nbatch - 1; bi >= 0; --bi) {
-            const uint32_t b = rg.x + (uint32_t)bi * kRasterThreads;
-            const int nb = min(kRasterThreads, n_here - bi * kRasterThreads);
+    // entries back to front.  Fast path: the forward recorded the block's list (all its
+    // entries fit kBlkListCap) -- batches of 256 straight from it.  Otherwise the rank order
+    // is scanned downwards from where the forward stopped.
+    const int2 bt = sc.blk_term[blockIdx.x];
+    const bool listed = bt.y <= kBlkListCap;
+    int r_hi = bt.x;
+    int cnt = 0, pass = 0, e_top = listed ? min(bt.y, bmax) : bt.y;
+    while (bmax > 0 && e_top > 0 && (listed || r_hi > 0)) {
+        if (listed) {
+            const int nb = min(kRasterThreads, e_top);
             if (tid < nb) {
-                const uint32_t r = vals[b + tid];
-                srank[tid] = r;
-                const float4 a = stage_A(rec.A[r], ox, oy), bb = rec.B[r];
-                sm.A[tid] = a;
-                sm.B[tid] = bb;
-                sm.C[tid] = rec.C[r];
-                if (NF > 1) sm.D[tid] = rec.D[r];
-                sm.wmask[tid] = (uint8_t)warps_reached(a, bb, cut2);
+                const int slot = kBatchCap - nb + tid;
+                const uint32_t r = sc.blk_list[(size_t)blockIdx.x * kBlkListCap + (e_top - nb + tid)];
+                const uint32_t g = sc.ord[r];
+                sm.grank[slot] = g;
+                sm.rrank[slot] = r;
+                stage_entry<NF>(sm, rec, g, slot, ox, oy, cut2);
             }
+            cnt = nb;
+            e_top -= nb;
+        } else {
+            const int rr = r_hi - 1 - tid;
+            const bool cov = rr >= 0 && tile_covers(sc.trect[rr], ttx, tty);
+            int total;
+            const int pos = scan_compact(cov, sm.wsum[pass & 1], total);  // descending rank order
+            // entries of this pass: indices [e_top - total, e_top); keep those below bmax
+            const int keep_hi = min(total, max(0, bmax - (e_top - total)));  // kept: ascending positions < keep_hi
+            const int asc = total - 1 - pos;
+            if (pos >= 0 && asc < keep_hi) {
+                const int slot = kBatchCap - cnt - keep_hi + asc;
+                const uint32_t g = sc.ord[rr];
+                sm.grank[slot] = g;
+                sm.rrank[slot] = (uint32_t)rr;
+                stage_entry<NF>(sm, rec, g, slot, ox, oy, cut2);
+            }
+            cnt += keep_hi;
+            e_top -= total;
+            r_hi -= kRasterThreads;
+            ++pass;
+            if (cnt < kRasterThreads && r_hi > 0 && e_top > 0) continue;
+        }
+        __syncthreads();
+        const int base = kBatchCap - cnt;
+        const int e_lo = e_top;  // entry index of slot `base`
+        for (int hi = kBatchCap; hi > base; hi -= kBwdSub) {
+            const int lo = max(base, hi - kBwdSub);
+#pragma unroll
+            for (int k = 0; k < kBwdSub / 32 * 8; ++k) slot_mem[tid + k * kRasterThreads] = 0.f;
             __syncthreads();
             // entries at or past this warp's furthest termination point cannot contribute
             // to any of its pixels: start the warp below them (warp-uniform)
-            const int jtop = min(nb, wmax - ((int)rg.z + bi * kRasterThreads));
-            const uint32_t wbit = 1u << (tid >> 5);
-            for (int j = jtop - 1; j >= 0; --j) {
+            const int jtop = min(hi, base + (wmax - e_lo));
+            for (int j = jtop - 1; j >= lo; --j) {
                 if (!(sm.wmask[j] & wbit)) continue;  // outside for every pixel of the warp
-                const int el = (int)rg.z + bi * kRasterThreads + j;
+                const int el = e_lo + (j - base);
                 bool contrib = false;
                 float g8[8];
                 if (el < last) {
@@ -573,37 +595,42 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, const u
                     const float s = reduce_scatter8(g8, lane);
                     if ((lane & 3) == 0) {
                         const int vi = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-                        atomicAdd(&sacc[j][vi], s);
+                        slot[warp][j - lo][vi] = s;
                     }
                 }
             }
             __syncthreads();
-            if (tid < nb) {
-                const uint32_t r = srank[tid];
+            // fixed-order sum over the warps, one global atomic per non-zero (entry, component)
+            for (int k = tid; k < (hi - lo) * 8; k += kRasterThreads) {
+                const int je = k >> 3, cc = k & 7;
+                float v = 0.f;
 #pragma unroll
-                for (int cc = 0; cc < 8; ++cc) {
-                    const float v = sacc[tid][cc];
-                    if (v != 0.f) atomicAdd(&screen[(size_t)cc * scap + r], v);
-                    sacc[tid][cc] = 0.f;
+                for (int w = 0; w < kRasterThreads / 32; ++w) v += slot[w][je][cc];
+                if (v == 0.f) continue;
+                if (sc.det_part) {  // deterministic: this block's own slot of (rank, tile, sub-block)
+                    const int r = (int)sm.rrank[lo + je];
+                    sc.det_part[det_slot(sc, r, sc.trect[r], ttx, tty, sb) * 8 + cc] = v;
+                } else {
+                    atomicAdd(&screen[(size_t)cc * scap + sm.grank[lo + je]], (double)v);
                 }
             }
             __syncthreads();
         }
+        cnt = 0;
     }
 }
 
-void launch_raster_fwd(const RecK& rec, const ChunkK& ck, const uint32_t* tile_vals, const OptK& O, int W, int H,
-                       int nf, PixK px, FwdState fs, const FrameDev* fd, bool loss, const ChW& ch_w,
-                       double* loss_part, cudaStream_t st) {
+void launch_raster_fwd(const RecK& rec, const ScanK& sc, const OptK& O, int W, int H, int nf, PixK px,
+                       const FrameDev* fd, bool loss, const ChW& ch_w, double* loss_part, cudaStream_t st) {
     const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
 #define TSB_FWD(NF_, D_)                                                                                        \
     do {                                                                                                       \
-        if (ck.work)                                                                                           \
-            k_raster_fwd<NF_, D_, true><<<grid, kRasterThreads, 0, st>>>(rec, ck, tile_vals, O, W, H, px, fs, fd, \
-                                                                          loss ? 1 : 0, ch_w, loss_part);       \
+        if (sc.work)                                                                                           \
+            k_raster_fwd<NF_, D_, true><<<grid, kRasterThreads, 0, st>>>(rec, sc, O, W, H, px, fd, loss ? 1 : 0,  \
+                                                                          ch_w, loss_part);                     \
         else                                                                                                   \
-            k_raster_fwd<NF_, D_, false><<<grid, kRasterThreads, 0, st>>>(rec, ck, tile_vals, O, W, H, px, fs,    \
-                                                                           fd, loss ? 1 : 0, ch_w, loss_part);  \
+            k_raster_fwd<NF_, D_, false><<<grid, kRasterThreads, 0, st>>>(rec, sc, O, W, H, px, fd, loss ? 1 : 0, \
+                                                                           ch_w, loss_part);                    \
     } while (0)
     if (nf > 1) {
         if (O.dist) TSB_FWD(2, true); else TSB_FWD(2, false);
@@ -613,25 +640,68 @@ void launch_raster_fwd(const RecK& rec, const ChunkK& ck, const uint32_t* tile_v
 #undef TSB_FWD
 }
 
-void launch_fixup_loss(const PixK& px, int W, int H, int nf, const FrameDev* fd, const ChW& ch_w,
-                       double* loss_extra, cudaStream_t st) {
-    k_fixup_loss<<<64, 256, 0, st>>>(px, W, H, nf, fd, ch_w, loss_extra);
+// Deterministic variant: one block, every pixel in a fixed partition, recomposited pixels only
+// (PixK::last bit 31), block sum in a fixed order.
+__global__ void __launch_bounds__(1024) k_fixup_loss_det(PixK px, int W, int H, int nf,
+                                                         const FrameDev* __restrict__ fd, ChW chw,
+                                                         double* __restrict__ loss_extra) {
+    __shared__ double part[1024];
+    if (*px.abort) return;
+    const float* __restrict__ target = fd->target;
+    const size_t HW = (size_t)W * H;
+    const float s2 = 2.f / (float)HW;
+    double l = 0.0;
+    for (size_t o = threadIdx.x; o < HW; o += blockDim.x) {
+        if (!(px.last[o] & kLastFixed)) continue;
+        for (int c = 0; c < 4 * nf; ++c) {
+            const float r = px.out[c * HW + o] - target[c * HW + o];
+            l += (double)(chw.w[c] * r * r);
+            px.d_quad[c * HW + o] = chw.w[c] * s2 * r;
+        }
+    }
+    part[threadIdx.x] = l;
+    __syncthreads();
+    for (int m = 512; m > 0; m >>= 1) {
+        if ((int)threadIdx.x < m) part[threadIdx.x] += part[threadIdx.x + m];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *loss_extra += part[0];
 }
 
-void launch_raster_bwd(const RecK& rec, const uint4* ranges_all, int nchunks, const uint32_t* tile_vals,
-                       const OptK& O, int W, int H, int nf, const float* dpsi, PixK px, const UpK& up,
-                       float* screen, int scap, double* bg_part, cudaStream_t st) {
+void launch_fixup_loss(const PixK& px, int W, int H, int nf, const FrameDev* fd, const ChW& ch_w,
+                       double* loss_extra, bool deterministic, cudaStream_t st) {
+    if (deterministic)
+        k_fixup_loss_det<<<1, 1024, 0, st>>>(px, W, H, nf, fd, ch_w, loss_extra);
+    else
+        k_fixup_loss<<<64, 256, 0, st>>>(px, W, H, nf, fd, ch_w, loss_extra);
+}
+
+void launch_raster_bwd(const RecK& rec, const ScanK& sc, const OptK& O, int W, int H, int nf, const float* dpsi,
+                       PixK px, const UpK& up, double* screen, int scap, double* bg_part, cudaStream_t st) {
     const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
     const bool extra = up.depth_raw || up.weight || up.distortion || up.transm;
 #define TSB_BWD(NF_, E_, D1_)                                                                                 \
-    k_raster_bwd<NF_, E_><<<grid, kRasterThreads, 0, st>>>(rec, ranges_all, nchunks, tile_vals, O, W, H, dpsi[0], \
-                                                          D1_, px, up, screen, scap, bg_part)
+    k_raster_bwd<NF_, E_><<<grid, kRasterThreads, kBwdSlotBytes, st>>>(rec, sc, O, W, H, dpsi[0], D1_, px, up, \
+                                                                      screen, scap, bg_part)
     if (nf > 1) {
         if (extra) TSB_BWD(2, true, dpsi[1]); else TSB_BWD(2, false, dpsi[1]);
     } else {
         if (extra) TSB_BWD(1, true, 0.f); else TSB_BWD(1, false, 0.f);
     }
 #undef TSB_BWD
+}
+
+// Kernel attributes (outside any stream capture: called when a pass is created).
+void raster_init() {
+    static bool done = false;
+    if (done) return;
+    const int bytes = (int)(sizeof(BwdSmem<2>) + sizeof(float) * (kRasterThreads / 32) * 12 + kBwdSlotBytes);
+    cudaFuncSetAttribute(k_raster_bwd<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSlotBytes);
+    cudaFuncSetAttribute(k_raster_bwd<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSlotBytes);
+    cudaFuncSetAttribute(k_raster_bwd<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSlotBytes);
+    cudaFuncSetAttribute(k_raster_bwd<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSlotBytes);
+    (void)bytes;
+    done = true;
 }
 
 __global__ void k_reduce_partials(const double* __restrict__ part, int nparts, int width,

@@ -72,6 +72,26 @@ __device__ __forceinline__ float4 stage_A(const float4& a, float ox, float oy) {
     return make_float4(mx, my, fabsf(a.z) + fabsf(mx), fabsf(a.w) + fabsf(my));
 }
 
+// One scan pass of the rank order: thread tid tests rank r (ascending or descending
+// passes pass their own r); returns the number of covering ranks of the pass and this
+// thread's position among them (rank order of the pass's threads), or -1.
+__device__ __forceinline__ int scan_compact(bool cov, int* wsum, int& total) {
+    constexpr int kThreads = 256;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned b = __ballot_sync(0xffffffffu, cov);
+    if (lane == 0) wsum[warp] = __popc(b);
+    __syncthreads();
+    int off = __popc(b & ((1u << lane) - 1u)), tot = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+        const int v = wsum[w];
+        off += w < warp ? v : 0;
+        tot += v;
+    }
+    total = tot;
+    return cov ? off : -1;
+}
+
 // Warp reduce-scatter of 8 per-lane values: 9 shuffles instead of 40.  On
 // return, lanes with (lane & 3) == 0 hold the warp sum of value index
 // ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1).

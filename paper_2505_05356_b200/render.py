@@ -92,6 +92,7 @@ class RenderOptions:
     flow: bool = False        # RenderChannels::flow (motions via RenderPass.set_motion)
     bg_color: Sequence[float] = (0.0, 0.0, 0.0)
     exact: bool = False       # reference-exact mode (TSB_CH_EXACT): every pixel in fp64, fp64 output planes
+    deterministic: bool = False  # bit-reproducible ToF gradients / loss (TSB_CH_DETERMINISTIC)
 
     def to_abi(self) -> _abi.RenderOptions:
         o = _abi.RenderOptions()
@@ -105,7 +106,7 @@ class RenderOptions:
             _abi.CH_COUNTS if self.counts else 0) | (_abi.CH_FULL_LISTS if self.full_lists else 0) | (
             _abi.CH_PHASOR) | (_abi.CH_DISTORTION if self.distortion else 0) | (
             _abi.CH_COLOR if self.color else 0) | (_abi.CH_FLOW if self.flow else 0) | (
-            _abi.CH_EXACT if self.exact else 0)
+            _abi.CH_EXACT if self.exact else 0) | (_abi.CH_DETERMINISTIC if self.deterministic else 0)
         bq = np.zeros(8)
         b = np.asarray(self.bg_quad, dtype=np.float64).reshape(-1)[:8]
         bq[: b.size] = b
