@@ -300,6 +300,17 @@ struct FixupAcc {
     bool done;
 };
 
+// The raster block (tile, 16 x 16 sub-block) a pixel belongs to: its forward recorded the
+// tile list it consumed (ScanK::blk_list) and where its scan of the order stopped.
+__device__ __forceinline__ int raster_block(const OptK& O, int x, int y) {
+    const int tile = (y / O.ts) * O.tiles_x + x / O.ts;
+    const int sb = ((y % O.ts) / kTile) * O.sub + (x % O.ts) / kTile;
+    return tile * O.sub * O.sub + sb;
+}
+__device__ __forceinline__ const uint32_t* block_list(const ScanK& sc, int rb) {
+    return sc.blk_list + (size_t)rb * kBlkListCap;
+}
+
 // Mark the Gaussians the flagged pixels will visit (their tile lists up to the
 // fp32 termination point + a margin) and queue each once for the record cache.
 __global__ void __launch_bounds__(128) k_fixup_mark(OptK O, FixupK fx, PixK px, int W, const FrameDev* __restrict__ fd) {
@@ -314,8 +325,22 @@ __global__ void __launch_bounds__(128) k_fixup_mark(OptK O, FixupK fx, PixK px, 
         const int x = pix % W, y = pix / W;
         const int tx = x / O.ts, ty = y / O.ts;
         const int limit = (px.last[pix] & kLastMask) + 64;
-        int e = 0;
-        for (int r0 = 0; r0 < V && e < limit; r0 += 32) {
+        int e = 0, r_from = 0;
+        const int rb = raster_block(O, x, y);
+        const int2 bt = fx.sc.blk_term[rb];
+        if (bt.y <= kBlkListCap) {  // the block's recorded list, then the order past its scan
+            const uint32_t* bl = block_list(fx.sc, rb);
+            for (int k = lane; k < min(bt.y, limit); k += 32) {
+                const uint32_t g = fx.sc.ord[bl[k]];
+                if (atomicExch(&fx.stamp[g], stamp) != stamp) {
+                    const int slot = atomicAdd(fx.work_n, 1);
+                    fx.work[slot] = (int)g;
+                }
+            }
+            e = bt.y;
+            r_from = bt.x;
+        }
+        for (int r0 = r_from; r0 < V && e < limit; r0 += 32) {
             const int r = r0 + lane;
             const bool cov = r < V && tile_covers(fx.sc.trect[r], tx, ty);
             const unsigned m = __ballot_sync(0xffffffffu, cov);
@@ -458,12 +483,12 @@ __device__ __forceinline__ void fixup_batch(const SceneK& S, const CamK& C, cons
 constexpr int kScanK = 4;                    // rank groups of 32 per step
 constexpr int kQueue = 32 + 32 * kScanK;     // entries a queue can hold after a step
 __device__ __forceinline__ void queue_step(const ScanK& sc, int r0, int V, bool descending, int tx, int ty,
-                                           int* qg, int* qr, int& qn, int lane) {
+                                           int* qg, int* qr, int& qn, int lane, int r_min = 0) {
     const uint32_t below = (1u << lane) - 1u;
 #pragma unroll
     for (int k = 0; k < kScanK; ++k) {
         const int r = descending ? r0 - 1 - (32 * k + lane) : r0 + 32 * k + lane;
-        const bool cov = r >= 0 && r < V && tile_covers(sc.trect[r], tx, ty);
+        const bool cov = r >= r_min && r < V && tile_covers(sc.trect[r], tx, ty);
         const unsigned m = __ballot_sync(0xffffffffu, cov);
         if (cov) {
             qg[qn + __popc(m & below)] = (int)sc.ord[r];
@@ -519,11 +544,28 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, const F
         a.dref = 0.0; a.SDs = 0.0; a.SD2s = 0.0;
         for (int c = 0; c < 8; ++c) a.accQ[c] = 0.0;
         a.nc = 0; a.processed = 0; a.last_eff = -1; a.done = false;
-        // the tile's list: ranks whose tile rect covers the tile, in rank order, 32 at a time
+        // the tile's list, 32 entries at a time: the entries its raster block recorded, then
+        // (rank order from where that block's scan stopped) the ranks covering the tile
         int* qg = queue_g[threadIdx.x >> 5];
         int* qr = queue_r[threadIdx.x >> 5];
-        int qn = 0, r_end = V;
-        for (int r0 = 0; !a.done && (r0 < V || qn > 0); r0 += 32 * kScanK) {
+        int qn = 0, r_end = V, r_from = 0;
+        {
+            const int rb = raster_block(O, x, y);
+            const int2 bt = fx.sc.blk_term[rb];
+            if (bt.y <= kBlkListCap) {
+                const uint32_t* bl = block_list(fx.sc, rb);
+                for (int e0 = 0; e0 < bt.y && !a.done; e0 += 32) {
+                    const bool is_e = e0 + lane < bt.y;
+                    const int rk = is_e ? (int)bl[e0 + lane] : 0;
+                    fixup_batch(S, C, O, F, fx, stamp, nf, x, y, is_e, is_e ? (int)fx.sc.ord[rk] : 0, e0 + lane, slot,
+                                a, lane);
+                    if (!a.done) a.processed = min(bt.y, e0 + 32);
+                    else r_end = __shfl_sync(0xffffffffu, rk, a.processed - 1 - e0) + 1;
+                }
+                r_from = bt.x;
+            }
+        }
+        for (int r0 = r_from; !a.done && (r0 < V || qn > 0); r0 += 32 * kScanK) {
             if (r0 < V) queue_step(fx.sc, r0, V, false, tx, ty, qg, qr, qn, lane);
             const bool flush = r0 + 32 * kScanK >= V;  // no more ranks: run the partial batch
             while (!a.done && (qn >= 32 || (flush && qn > 0))) {
@@ -802,12 +844,17 @@ __device__ void fixbwd_pixel(const SceneK& S, const CamK& C, const OptK& O, cons
     b.B = 0.0;
     b.R = 1.0;
     b.first = true;
-    // the walk of k_fixup back to front: ranks downwards from where it stopped, covering ranks
-    // queued in descending order, so lane j of a batch holds the j-th entry from the back
+    // the walk of k_fixup back to front: the ranks past the raster block's recorded list
+    // downwards from where the walk stopped (covering ranks queued in descending order, so
+    // lane j of a batch holds the j-th entry from the back), then the recorded list reversed
+    const int rb = raster_block(O, x, y);
+    const int2 bt = fx.sc.blk_term[rb];
+    const bool listed = bt.y <= kBlkListCap;
+    const int r_lo = listed ? bt.x : 0;  // the rank scan covers [r_lo, r_end)
     int qn = 0, e_hi = st.e_end;
-    for (int r_hi = st.r_end; e_hi > 0 && (r_hi > 0 || qn > 0); r_hi -= 32 * kScanK) {
-        if (r_hi > 0) queue_step(fx.sc, r_hi, V, true, tx, ty, qg, qr, qn, lane);
-        const bool flush = r_hi - 32 * kScanK <= 0;
+    for (int r_hi = st.r_end; e_hi > 0 && (r_hi > r_lo || qn > 0); r_hi -= 32 * kScanK) {
+        if (r_hi > r_lo) queue_step(fx.sc, r_hi, V, true, tx, ty, qg, qr, qn, lane, r_lo);
+        const bool flush = r_hi - 32 * kScanK <= r_lo;
         while (e_hi > 0 && (qn >= 32 || (flush && qn > 0))) {
             const int e = e_hi - 1 - lane;  // queued entries in descending list order
             const bool is_q = lane < qn && e >= 0;
@@ -815,6 +862,16 @@ __device__ void fixbwd_pixel(const SceneK& S, const CamK& C, const OptK& O, cons
                          b, out, lane);
             e_hi -= min(qn, 32);
             queue_pop32(qg, qr, qn, lane);
+        }
+    }
+    if (listed) {
+        const uint32_t* bl = block_list(fx.sc, rb);
+        for (; e_hi > 0; e_hi -= 32) {
+            const int e = e_hi - 1 - lane;
+            const bool is_q = e >= 0;
+            const int rk = is_q ? (int)bl[e] : 0;
+            fixbwd_batch(S, C, O, F, fx, stamp, nf, x, y, is_q && e < last, is_q ? (int)fx.sc.ord[rk] : 0, rk, b, out,
+                         lane);
         }
     }
 }
