@@ -448,12 +448,30 @@ def bench_train_c4(args, dist, tsb, synthetic, ctx):
         adam = {"bound": "hbm", "achieved": round(b / (per * 1e-3) / 1e9, 1), "peak": pk, "unit": "GB/s",
                 "frac": round(b / (per * 1e-3) / 1e9 / pk, 4), "avg_launch_ms": round(per, 4),
                 "algorithmic_bytes_per_launch": b}
+    proxy = None
+    if dist.world == 1:
+        # each rank's share at N = 8: 8 of the 64 frames per iteration on one GPU (the pipeline of
+        # 16 passes is then under-filled and drains at every Adam step -- the scaling risk)
+        sub = cfg.frames[:8]
+        for _ in range(2):
+            trainer.step(sub, lambda i: targets[mine[i]].data_ptr())
+        ctx.synchronize()
+        reps = 8
+        timer.start()
+        for _ in range(reps):
+            trainer.step(sub, lambda i: targets[mine[i]].data_ptr())
+        ctx.join()
+        ms8 = timer.stop_ms()
+        proxy = {"frames_per_iter": 8, "iters_per_s": round(reps / (ms8 / 1e3), 3),
+                 "frames_per_s": round(8 * reps / (ms8 / 1e3), 1),
+                 "frames_per_s_64": round(64 * args.train_steps / (ms_max / 1e3), 1),
+                 "note": "per-rank share of c4 at N = 8 on one GPU (iterations include the fused Adam step)"}
     res = {"config": "c4", "n_gaussians": g.n, "image": f"{W}x{H}", "frames_per_iter": len(cfg.frames),
            "iters_per_s": round(args.train_steps / (ms_max / 1e3), 4),
            "ms_per_iter": round(ms_max / args.train_steps, 3),
            "stage_ms_per_iter": {k: round(v[0], 3) for k, v in st.items() if v[1]},
            "keys_per_frame_last": trainer.rp.num_keys(), "passes_in_flight": len(trainer.passes),
-           "redone_frames_timed": train_redos, "k_adam_roofline": adam,
+           "redone_frames_timed": train_redos, "k_adam_roofline": adam, "n8_share_proxy": proxy,
            "path": "parallel.FrameShardedTrainer (public API)"}
     if comm:
         comm.close()

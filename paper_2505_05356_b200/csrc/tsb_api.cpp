@@ -1188,6 +1188,11 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     for (int c = 0; c < 4; ++c) O.bg_phasor[c] = c < 2 * p->nf ? opt->bg_phasor[c] : 0.0;
     O.dist = (opt->channels & TSB_CH_DISTORTION) ? 1 : 0;
     O.exact = (opt->channels & TSB_CH_EXACT) ? 1 : 0;
+    static const float trel = [] {  // TSB_TREL: A/B override of the fix-up's T error threshold
+        const char* e = std::getenv("TSB_TREL");
+        return e ? (float)std::atof(e) : kTrelFlag;
+    }();
+    O.trel_flag = trel;
     for (int c = 0; c < 3; ++c) O.bg_color[c] = opt->bg_color[c];
     p->ntiles = O.tiles_x * O.tiles_y;
     if (p->ntiles > 65536) return fail(TSB_ERR_UNSUPPORTED, "render: more than 65536 tiles");

@@ -33,6 +33,7 @@ struct OptK {
     float alpha_thr_f, floor_f, cut2_f, cov_eps_f;
     int dist;          // distortion channel: accumulate the shifted depth moments
     int exact;         // TSB_CH_EXACT: every pixel goes to the fp64 fix-up
+    float trel_flag;   // relative T error bound above which a pixel is recomposited (fix-up reason 8)
     double bg_quad[8];
     double bg_phasor[4];
     double bg_color[3];
@@ -193,6 +194,10 @@ struct FixState {
     double T, Tpre, SW, dref, SDs, SD2s;
     int r_end, e_end;
 };
+// The bound of T's relative error (first order, worst case: linear in the number of
+// contributions) above which a pixel is recomposited in fp64: an almost opaque splat
+// (1 - alpha lost to fp32 rounding) makes T -- and every later weight -- inaccurate.
+constexpr float kTrelFlag = 1e-4f;
 constexpr int kFixStateCap = 1 << 16;  // recomposited pixels per frame with an fp64 backward
 constexpr int kLastFixed = (int)0x80000000;  // PixK::last bit 31: pixel recomposited in fp64
 constexpr int kLastBwd64 = 0x40000000;       // bit 30: its backward runs in fp64 (k_fixup_bwd)

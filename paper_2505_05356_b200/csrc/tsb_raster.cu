@@ -20,6 +20,8 @@
 // with the ellipse's condition number), and d(maha)/d(mean) falls out of p, q.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "tsb_internal.h"
 #include "tsb_raster.cuh"
 
@@ -233,7 +235,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK s
     }
     // every rank of the order scanned: a pixel still alive processed the whole list
     if (!done) processed = ebase;
-    if (tid == 0 && sc.blk_term) sc.blk_term[blockIdx.x] = make_int2(min(r, V), ebase);
+    if (tid == 0) sc.blk_term[blockIdx.x] = make_int2(min(r, V), ebase);
     // the prefix order ended with the pixel alive: the frame is redone with the full order
     if (active && !done && *sc.n_all > V) atomicOr(sc.abort, 8);
     float lpx = 0.f;
@@ -241,7 +243,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK s
         // T's relative error bound grows by ~eps alpha / (1 - alpha) per contribution: an
         // almost opaque splat (1 - alpha lost to fp32 rounding) leaves T -- and every later
         // weight -- too inaccurate for the 1e-4 output bar: recomposite in fp64 (reason 8)
-        if (dT > kTrelFlag * T) flag |= 8;
+        if (dT > O.trel_flag * T) flag |= 8;
         if (O.exact) flag |= 16;  // reference-exact mode: every pixel in fp64
         const float T2 = T * T;
         float q[4 * NF];
@@ -350,7 +352,7 @@ __global__ void k_fixup_loss(PixK px, int W, int H, int nf, const FrameDev* __re
 //   reduces its 8 screen-space gradients with a 9-shuffle reduce-scatter into its own
 //   shared slot (no shared-memory atomics); per 32 entries the block sums the 8 warp
 //   slots in a fixed order and adds each sum to global memory with one atomic.
-constexpr int kBwdSub = 64;  // entries per slot round: 8 warps x 64 entries x 8 floats (dynamic smem)
+constexpr int kBwdSub = 128;  // entries per slot round: 8 warps x 128 entries x 8 floats (dynamic smem)
 constexpr size_t kBwdSlotBytes = sizeof(float) * (kRasterThreads / 32) * kBwdSub * 8;
 
 template <int NF>
@@ -519,9 +521,12 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, ScanK s
         const int e_lo = e_top;  // entry index of slot `base`
         for (int hi = kBatchCap; hi > base; hi -= kBwdSub) {
             const int lo = max(base, hi - kBwdSub);
+            {  // this warp's slot rows are private: cleared without a block barrier
+                float4* my = reinterpret_cast<float4*>(&slot[warp][0][0]);
 #pragma unroll
-            for (int k = 0; k < kBwdSub / 32 * 8; ++k) slot_mem[tid + k * kRasterThreads] = 0.f;
-            __syncthreads();
+                for (int k = 0; k < kBwdSub * 8 / 4 / 32; ++k) my[lane + 32 * k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                __syncwarp();
+            }
             // entries at or past this warp's furthest termination point cannot contribute
             // to any of its pixels: start the warp below them (warp-uniform)
             const int jtop = min(hi, base + (wmax - e_lo));

@@ -50,7 +50,6 @@ constexpr float kEps = 5.9604645e-8f;      // 2^-24
 constexpr float kCoarseMaha = 1e-3f;       // relative window that triggers the precise bound
 constexpr float kCoarseAlpha = 1e-4f;
 constexpr float kEx2Err = 2.5e-7f;         // ex2.approx.ftz.f32 relative error bound (+ margin)
-constexpr float kTrelFlag = 1e-4f;         // relative T error bound above which a pixel is recomposited
 
 // |fl32(maha) - maha_exact| bound from the rounding of mean offsets (A.z, A.w carry
 // |mean - rect origin| + |mean - block origin|), L, dx, dy, p, q.

@@ -650,7 +650,7 @@ class RenderPass:
         c = C.c_int32()
         check(lib().tsb_pass_debug_fixup_list(self._h, a.ctypes.data_as(_abi._ip), int(a.size), C.byref(c)))
         a = a[:n]
-        return a & 0xFFFFFF, (a >> 24) & 7
+        return a & 0xFFFFFF, (a >> 24) & 31  # reasons: 1 maha, 2 alpha, 4 T band, 8 T error bound, 16 exact mode
 
     def close(self):
         # after the context is gone (interpreter teardown, GC cycles) the handle is dropped, not freed
