@@ -1465,8 +1465,7 @@ int record_forward(tsb_pass* p, cudaStream_t st, bool loss, const ChW& chw, bool
     const FixupK fx = fixk(p);
     {
         Stage sg(p->ctx, TSB_STAGE_FIXUP, st);
-        launch_fixup(scenek(p->scene), p->cam, p->opt, fd, fx, px, p->nf, st);
-        fixed += 3;
+        fixed += launch_fixup(scenek(p->scene), p->cam, p->opt, fd, fx, px, p->nf, st);
     }
     if (loss) {
         Stage sg(p->ctx, TSB_STAGE_LOSS, st);

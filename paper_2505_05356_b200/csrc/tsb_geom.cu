@@ -2,6 +2,8 @@
 // Compiled with -fmad=false (see tsb_fp64.cuh).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "tsb_fp64.cuh"
 #include "tsb_ties.cuh"
 
@@ -636,12 +638,21 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, const F
     }
 }
 
-void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd, const FixupK& fx,
-                  const PixK& px, int nf, cudaStream_t st) {
-    cudaMemsetAsync(fx.work_n, 0, sizeof(int), st);
-    k_fixup_mark<<<148, 128, 0, st>>>(O, fx, px, C.W, fd);
-    k_fixup_records<<<148, 128, 0, st>>>(S, C, O, fd, fx);
+int launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd, const FixupK& fx,
+                 const PixK& px, int nf, cudaStream_t st) {
+    // The record cache (mark + records: each Gaussian's fp64 record computed once per frame
+    // for all the pixels that visit it) -- A/B switch TSB_FIXUP_CACHE=0: records inline.
+    static const bool cache = [] {
+        const char* e = std::getenv("TSB_FIXUP_CACHE");
+        return !e || std::atoi(e) != 0;
+    }();
+    if (cache) {
+        cudaMemsetAsync(fx.work_n, 0, sizeof(int), st);
+        k_fixup_mark<<<148, 128, 0, st>>>(O, fx, px, C.W, fd);
+        k_fixup_records<<<148, 128, 0, st>>>(S, C, O, fd, fx);
+    }
     k_fixup<<<148, 128, 0, st>>>(S, C, O, fd, fx, px, nf);
+    return cache ? 3 : 1;
 }
 
 // ---------------------------------------------------------------------------

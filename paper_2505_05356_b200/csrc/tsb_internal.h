@@ -214,8 +214,8 @@ struct FixupK {
     int state_cap;
     int* fix_idx;      // [npx] fix-up slot of a recomposited pixel (the deterministic backward's lookup)
 };
-void launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd, const FixupK& fx,
-                  const PixK& px, int nf, cudaStream_t st);
+int launch_fixup(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd, const FixupK& fx,
+                 const PixK& px, int nf, cudaStream_t st);  // returns kernels launched
 void launch_fixup_bwd(const SceneK& S, const CamK& C, const OptK& O, const FrameDev* fd, const FixupK& fx,
                       const PixK& px, const UpK& up, int nf, double* screen, int scap, cudaStream_t st);
 // deterministic: the same per pixel, one warp per raster block in pixel order, into the slots

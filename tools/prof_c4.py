@@ -20,6 +20,6 @@ for i in range(1 + frames):
     rp.forward_loss(tgt, sync=False)
     rp.backward()
 ctx.synchronize()
-print("ok", rp.visible_count(), rp.num_keys(), rp.debug_fixups(), ctx.redo_count())
+print("ok", rp.visible_count(), rp.debug_fixups(), ctx.redo_count())
 pix, why = rp.debug_fixup_list()
 print("fixup reasons", {b: int(((why & b) != 0).sum()) for b in (1, 2, 4, 8, 16)})
