@@ -192,7 +192,10 @@ class StreamTimer:
 #     (pos_op 16, two keyframe offsets 32, fp32 cov3d cache 24, fp64 opacity cache 8) and
 #     writes 8 B (fp32 key, tiles-touched flag) = 88 B; the full variant (TSB_PREFIX=0)
 #     writes 4 B more per Gaussian and 64 B per visible Gaussian (fp64 depth, rect, record).
-#   binning (HBM): SURVEY 8(d) "scan + duplicate" = 12 B per tile-list entry.
+#   binning (HBM; k_order_ranks + k_sl_emit): per rank of the frame's order read 12 B (sorted
+#     index, pixel rect) and write 12 B (Gaussian index, tile rect); per (rank, super-tile)
+#     list entry write 12 B (rank, tile rect).  Ranks and entries counted live in profiling
+#     mode (tsb_ctx_scan_counts).
 #   k_raster_fwd (FP32): SURVEY 8(d) 23 FLOP (17 FP32 inst, FMA = 2) per (pixel, entry)
 #     evaluation; evaluations counted live by the kernel in profiling mode.
 #   k_adam (HBM): 28 B per parameter element (read p, g, m, v; write p, m, v) + 4 B per
@@ -313,11 +316,13 @@ def bench_c3(args, dist, tsb, synthetic):
     ctx.synchronize()
     st_ovl = ctx.stage_times()
     ctx.raster_counts()
+    ctx.scan_counts()
     step([rp])
     ctx.synchronize()
     ctx.set_profiling(False)
     st_ser = ctx.stage_times()
     evals, contribs = ctx.raster_counts()
+    ranks, entries = ctx.scan_counts()
     v, k = rp.visible_count(), rp.num_keys()
     fixups = rp.debug_fixups()
     ms_max = dist.max(ms)
@@ -370,12 +375,14 @@ def bench_c3(args, dist, tsb, synthetic):
     peaks = load_peaks()
     pk_fp32 = round(fp32_peak_tflops(clk.summary()["sm_max_mhz"] or 1965), 1)
     work = {"k_preprocess": (nfr * (g.n * 88 if lean else g.n * 92 + v * 64), "GB/s", "hbm", peaks["hbm_gbs"]),
-            "binning": (nfr * k * 12, "GB/s", "hbm", peaks["hbm_gbs"]),
+            "binning": (ranks * 24 + entries * 12, "GB/s", "hbm", peaks["hbm_gbs"]),
             "k_raster_fwd": (23 * evals, "TFLOP/s", "fp32", pk_fp32)}
     ser, ovl = family_ms(st_ser), family_ms(st_ovl)
     roof, roofs = rooflines(ser, ovl, ms_max / args.steps, work, peaks, clk.summary()["sm_max_mhz"])
     roof["evaluations_per_frame"] = evals // max(nfr, 1)
     roof["contributions_per_frame"] = contribs // max(nfr, 1)
+    roof["order_ranks_per_frame"] = ranks // max(nfr, 1)
+    roof["super_tile_entries_per_frame"] = entries // max(nfr, 1)
     info = {"visible": v, "keys_per_frame": k, "fixup_pixels_last_frame": fixups, "clock": clk.summary(),
             "launches": launches, "passes_in_flight": len(passes), "redone_frames": redos,
             "stage_ms_serialised_sweep": {f: round(t_, 3) for f, (t_, _) in ser.items()},

@@ -159,6 +159,9 @@ int tsb_ctx_stage_times(tsb_ctx* ctx, double* ms /* TSB_NUM_STAGES */, int64_t* 
 /* Forward-raster work since the last call (profiling mode only; resets):
  * (pixel, list entry) evaluations and contributing evaluations (alpha >= threshold). */
 int tsb_ctx_raster_counts(tsb_ctx* ctx, int64_t* evaluations, int64_t* contributions);
+/* Order work since the last call (profiling mode only; resets): ranks of the frames'
+ * depth orders and (rank, super-tile) entries of their super-tile lists. */
+int tsb_ctx_scan_counts(tsb_ctx* ctx, int64_t* ranks, int64_t* list_entries);
 
 /* ---- scene: parameters, gradients, Adam state (trainer.cpp:63-132) ------- */
 int tsb_scene_create(tsb_ctx* ctx, const tsb_scene_desc* desc, tsb_scene** out);
@@ -353,8 +356,9 @@ int tsb_pass_debug_screen_grads(tsb_pass* p, float* g8 /* 8 per rank */);
 /* Keep a copy of the screen-space gradients of every following backward (the chain kernel
  * consumes them); required before tsb_pass_debug_screen_grads. */
 int tsb_pass_debug_keep_screen(tsb_pass* p, int enabled);
-/* Test hook (`entries` >= 1, otherwise unused): the next forward aborts on the device once,
- * exercising the abort + settle/redo path (the pass has no list storage to overflow). */
+/* Test hook: the super-tile list storage (entries = (rank, super-tile) pairs) set to
+ * `entries`; a frame that needs more aborts on the device and is redone with grown lists
+ * when the pass settles (the abort + settle/redo path). */
 int tsb_pass_debug_set_list_capacity(tsb_pass* p, uint32_t entries);
 /* Pixels the fp32 raster flagged as decision-ambiguous and recomposited in fp64. */
 int tsb_pass_debug_fixups(tsb_pass* p, int32_t* count);

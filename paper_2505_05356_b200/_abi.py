@@ -94,6 +94,7 @@ SIGNATURES = {
     "tsb_ctx_launch_count": (C.c_int64, [_vp]),
     "tsb_ctx_redo_count": (C.c_int64, [_vp]),
     "tsb_ctx_raster_counts": (C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "tsb_ctx_scan_counts": (C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "tsb_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "tsb_ctx_stage_times": (C.c_int, [_vp, _dp, _lp]),
     "tsb_scene_create": (C.c_int, [_vp, C.POINTER(SceneDesc), C.POINTER(_vp)]),

@@ -100,6 +100,10 @@ struct Stage {
     size_t idx = 0;
     bool on;
     cudaStream_t stream;
+    static bool debug_sync() {  // TSB_DEBUG_SYNC=1 (with TSB_NO_GRAPHS=1): each stage synchronised and checked
+        static const bool on_ = std::getenv("TSB_DEBUG_SYNC") != nullptr;
+        return on_;
+    }
     Stage(tsb_ctx* ctx, int s, cudaStream_t st) : c(ctx), stage(s), on(ctx->profiling), stream(st) {
         if (!on) return;
         if (c->ev_used + 2 > c->ev_pool.size()) {
@@ -114,6 +118,12 @@ struct Stage {
         cudaEventRecord(c->ev_pool[idx], stream);
     }
     ~Stage() {
+        if (debug_sync()) {
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            cudaStreamIsCapturing(stream, &cs);
+            const cudaError_t e = cs == cudaStreamCaptureStatusNone ? cudaStreamSynchronize(stream) : cudaSuccess;
+            if (e != cudaSuccess) std::fprintf(stderr, "tsb debug: stage %d failed: %s\n", stage, cudaGetErrorString(e));
+        }
         if (!on) return;
         cudaEventRecord(c->ev_pool[idx + 1], stream);
         c->ev_marks.emplace_back(stage, idx);
@@ -175,6 +185,11 @@ struct tsb_pass {
     // the rank order the raster blocks scan (ScanK): Gaussian and tile rect per rank
     uint32_t* ord = nullptr;
     uint2* trect = nullptr;
+    // super-tile lists (ScanK::sl_*): per super-tile the ranks meeting it, in rank order
+    uint32_t *sl_hist = nullptr, *sl_off = nullptr, *sl_rank = nullptr;
+    uint2* sl_rect = nullptr;
+    int sl_cap = 0, sl_hist_cap = 0, sl_off_cap = 0;
+    int sup_x = 1, sup_log = 3, nsup = 1;
     int2* blk_term = nullptr;  // per raster block: where its forward scan stopped
     uint32_t* blk_list = nullptr;  // per raster block: the list entries its forward consumed (kBlkListCap)
     // deterministic backward (TSB_CH_DETERMINISTIC): slot offsets per rank, slots, fix-up pixel index
@@ -255,7 +270,6 @@ struct tsb_pass {
     int ext_n_cap = 0, ext_px_cap = 0, ext_blk_cap = 0;
     bool has_mf = false, has_mb = false;
     bool prep_deferred = false; // prepare's device work not issued yet
-    bool debug_abort = false;   // test hook: the next forward aborts once
 };
 
 namespace {
@@ -290,8 +304,8 @@ int tsb_ctx_create(int device, tsb_ctx** out) {
         return fail(TSB_ERR_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
     }
     e = cudaMallocHost(&c->pinned, 4096);
-    if (e == cudaSuccess) e = cudaMalloc(&c->work, 2 * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMemset(c->work, 0, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&c->work, 4 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(c->work, 0, 4 * sizeof(unsigned long long));
     if (e != cudaSuccess) {
         cudaStreamDestroy(c->stream);
         delete c;
@@ -345,6 +359,18 @@ int tsb_ctx_raster_counts(tsb_ctx* c, int64_t* evaluations, int64_t* contributio
     TSB_CUDA(cudaMemset(c->work, 0, sizeof h));
     if (evaluations) *evaluations = (int64_t)h[0];
     if (contributions) *contributions = (int64_t)h[1];
+    return TSB_OK;
+}
+
+int tsb_ctx_scan_counts(tsb_ctx* c, int64_t* ranks, int64_t* list_entries) {
+    if (!c) return fail(TSB_ERR_INVALID, "null context");
+    int rc = tsb_ctx_synchronize(c);
+    if (rc) return rc;
+    unsigned long long h[2];
+    TSB_CUDA(cudaMemcpy(h, c->work + 2, sizeof h, cudaMemcpyDeviceToHost));
+    TSB_CUDA(cudaMemset(c->work + 2, 0, sizeof h));
+    if (ranks) *ranks = (int64_t)h[0];
+    if (list_entries) *list_entries = (int64_t)h[1];
     return TSB_OK;
 }
 
@@ -979,6 +1005,10 @@ void free_gauss(tsb_pass* p) {
     dev_free(p->rec.A); dev_free(p->rec.B); dev_free(p->rec.C); dev_free(p->rec.D); dev_free(p->screen); dev_free(p->screen_keep);
     dev_free(p->ord); dev_free(p->trect);
 }
+void free_super(tsb_pass* p) {
+    dev_free(p->sl_hist); dev_free(p->sl_off); dev_free(p->sl_rank); dev_free(p->sl_rect);
+    p->sl_cap = p->sl_hist_cap = p->sl_off_cap = 0;
+}
 void free_pixels(tsb_pass* p) {
     dev_free(p->out); dev_free(p->n_contrib); dev_free(p->n_processed); dev_free(p->last);
     dev_free(p->T_pre); dev_free(p->d_quad); dev_free(p->target); dev_free(p->flagged);
@@ -1043,6 +1073,65 @@ int ensure_pixels(tsb_pass* p, int W, int H, int ntiles, int nblocks) {
     }
     (void)ntiles;
     return TSB_OK;
+}
+
+// Super-tile geometry of the current camera / tiling and the list storage: the histogram
+// for n ranks, `entries` list entries (0: the default 2n + 64K; grown when a frame's
+// lists overflow -- abort bit 1, settle()).
+int ensure_super(tsb_pass* p, int n, int64_t entries) {
+    int lg = 3;
+    auto sups = [&](int l) {
+        return ((p->opt.tiles_x + (1 << l) - 1) >> l) * ((p->opt.tiles_y + (1 << l) - 1) >> l);
+    };
+    while (sups(lg) > kSlMaxSup) ++lg;
+    p->sup_log = lg;
+    p->sup_x = (p->opt.tiles_x + (1 << lg) - 1) >> lg;
+    p->nsup = sups(lg);
+    int rc;
+    if (p->nsup * kSlMaxBlocks > p->sl_hist_cap) {
+        dev_free(p->sl_hist); dev_free(p->sl_off);
+        p->sl_hist_cap = p->sl_off_cap = 0;
+        if ((rc = dev_alloc(&p->sl_hist, (size_t)p->nsup * kSlMaxBlocks)) ||
+            (rc = dev_alloc(&p->sl_off, (size_t)p->nsup + 1)))
+            return rc;
+        p->sl_hist_cap = p->nsup * kSlMaxBlocks;
+        p->sl_off_cap = p->nsup + 1;
+    }
+    static const int64_t cap0 = [] {  // TSB_SL_CAP: initial list capacity (tests of the overflow redo)
+        const char* e = std::getenv("TSB_SL_CAP");
+        return e ? (int64_t)std::atoll(e) : (int64_t)0;
+    }();
+    const int64_t want = std::min<int64_t>(INT32_MAX / 2, entries > 0 ? entries
+                                                          : cap0 > 0 ? cap0 : 2 * (int64_t)n + 65536);
+    if (want > p->sl_cap) {
+        dev_free(p->sl_rank); dev_free(p->sl_rect);
+        p->sl_cap = 0;
+        if ((rc = dev_alloc(&p->sl_rank, (size_t)want)) || (rc = dev_alloc(&p->sl_rect, (size_t)want))) return rc;
+        p->sl_cap = (int)want;
+    }
+    return TSB_OK;
+}
+
+// Upper bound of the frame's order length (*n_bin): the prefix cap or every Gaussian.
+int rank_bound(tsb_pass* p) {
+    return p->prefix ? std::min(p->kcap, p->scene->d.n) : p->scene->d.n;
+}
+
+SuperK superk(tsb_pass* p) {
+    SuperK k;
+    k.hist = p->sl_hist;
+    k.hist_stride = kSlMaxBlocks;
+    k.ticket = reinterpret_cast<uint32_t*>(p->counters + 3);
+    k.off = p->sl_off;
+    k.rank = p->sl_rank;
+    k.rect = p->sl_rect;
+    k.cap = p->sl_cap;
+    k.total = p->counters + 7;
+    k.sup_x = p->sup_x;
+    k.sup_log = p->sup_log;
+    k.nsup = p->nsup;
+    k.work = p->ctx->profiling ? p->ctx->work : nullptr;
+    return k;
 }
 
 PixK pixk(tsb_pass* p) {
@@ -1114,6 +1203,7 @@ void tsb_pass_destroy(tsb_pass* p) {
     v.erase(std::remove(v.begin(), v.end(), p), v.end());
     free_gauss(p);
     free_pixels(p);
+    free_super(p);
     dev_free(p->blk_term); dev_free(p->blk_list);
     dev_free(p->det_off); dev_free(p->det_part);
     dev_free(p->counters); dev_free(p->fx_work_n);
@@ -1211,6 +1301,7 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     int rc;
     if ((rc = ensure_gauss(p, n))) return rc;
     if ((rc = ensure_pixels(p, p->W, p->H, p->ntiles, p->nblocks))) return rc;
+    if ((rc = ensure_super(p, n, 0))) return rc;
     p->has_mf = p->has_mb = false;  // RenderInput::motion_* belong to one frame
     if ((p->channels & (TSB_CH_COLOR | TSB_CH_FLOW)) && (rc = ensure_ext(p))) return rc;
     if (p->channels & TSB_CH_EXACT) {  // every pixel recomposited (and back-propagated) in fp64
@@ -1314,6 +1405,11 @@ ScanK scank(tsb_pass* p) {
     sc.det_off = nullptr;
     sc.det_part = nullptr;
     sc.nsub2 = p->opt.sub * p->opt.sub;
+    sc.sl_off = p->sl_off;
+    sc.sl_rank = p->sl_rank;
+    sc.sl_rect = p->sl_rect;
+    sc.sup_x = p->sup_x;
+    sc.sup_log = p->sup_log;
     return sc;
 }
 
@@ -1448,14 +1544,10 @@ int record_forward(tsb_pass* p, cudaStream_t st, bool loss, const ChW& chw, bool
     }
     // counters[2] (abort word) is not cleared here: the depth sort of prepare may have set it
     TSB_CUDA(cudaMemsetAsync(p->counters + 1, 0, sizeof(int32_t), st));
-    if (p->debug_abort) {  // test hook (eager forward): abort this frame once
-        TSB_CUDA(cudaMemsetAsync(p->counters + 2, 0x20, 1, st));
-        p->debug_abort = false;
-    }
     {
         Stage sg(p->ctx, TSB_STAGE_BINNING, st);
-        launch_order_ranks(p->sorted, tiek(p), p->rect, p->opt.ts, p->n_bin, p->scene->d.n, p->ord, p->trect, st);
-        fixed += p->scene->d.n > 0 ? 1 : 0;
+        fixed += launch_order_ranks(p->sorted, tiek(p), p->rect, p->opt.ts, p->n_bin, rank_bound(p), p->ord,
+                                    p->trect, superk(p), st);
     }
     {
         Stage sg(p->ctx, TSB_STAGE_RASTER_FWD, st);
@@ -1510,8 +1602,11 @@ std::string forward_key(tsb_pass* p, bool loss, const ChW& chw) {
     const PixK px = pixk(p);
     const void* ptrs[] = {p->sorted, p->rect, p->counters, p->ord, p->trect, p->blk_term, p->blk_list, p->rec.A, p->rec.B,
                           p->rec.C, p->rec.D, p->loss_part, p->loss_dev, p->fx_stamp, p->fx_work, p->fx_work_n,
-                          p->fx_cache, p->frame_dev, p->pinned, p->fx_state};
+                          p->fx_cache, p->frame_dev, p->pinned, p->fx_state, p->sl_hist, p->sl_off, p->sl_rank,
+                          p->sl_rect};
     add(ptrs, sizeof ptrs);
+    const int sl[] = {p->sl_cap, p->sup_x, p->sup_log, p->nsup};
+    add(sl, sizeof sl);
     add(&p->fx_state_cap, sizeof p->fx_state_cap);
     add(&S, sizeof S);
     add(&px, sizeof px);
@@ -1541,7 +1636,7 @@ int enqueue_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw,
     if (with_prep) TSB_CUDA(cudaStreamWaitEvent(st, p->scene->params_ev, 0));
     int fixed = 0;
     // Graphs: not while stage events are being recorded (profiling runs the same kernels eagerly).
-    const bool use_graph = allow_graph && p->ctx->use_graphs && !p->ctx->profiling && !p->debug_abort;
+    const bool use_graph = allow_graph && p->ctx->use_graphs && !p->ctx->profiling;
     if (use_graph) {
         std::string key = forward_key(p, loss, chw);
         tsb_pass::FwdGraph& fg = p->fwd[with_prep ? 1 : 0];
@@ -1658,10 +1753,18 @@ int settle(tsb_pass* p) {
         const int32_t* hc = (const int32_t*)((const char*)p->pinned + 2048);
         p->V = hc[0];
         const int ab = hc[2];
+        static const bool trace = std::getenv("TSB_TRACE") != nullptr;
+        if (trace)
+            std::fprintf(stderr, "tsb trace: pass %p settle attempt %d ab %d V %d nbin %d kcap %d prefix %d\n", (void*)p,
+                         attempt, ab, hc[0], hc[4], p->kcap, (int)p->prefix);
         if (!ab) return TSB_OK;
         if (attempt >= 8) return fail(TSB_ERR_UNSUPPORTED, "render: frame kept aborting (depth order)");
         p->ctx->redos++;
         cudaStream_t st = p->stream;
+        if (ab & 1) {  // the super-tile lists overflowed: grow them to the frame's total
+            int rc = ensure_super(p, p->scene->d.n, (int64_t)hc[7] + hc[7] / 4 + 4096);
+            if (rc) return rc;
+        }
         if (ab & 16) {  // lean / exact visibility disagreed: exact preprocess + full sort
             exact_order(p, st);  // an over-long tie run of this order aborts the next attempt (bit 2)
         } else if (p->prefix && (ab & (8 | 2))) {  // the full order (+ the records the lean preprocess skipped)
@@ -2186,6 +2289,28 @@ int tsb_pass_get_motion_grads(tsb_pass* p, float* d_motion_fwd, float* d_motion_
 
 // ---- debug / parity ----
 namespace {
+// The scan arrays (ord / trect / super-tile lists) of the pass's current order, outside a
+// frame: synchronous, the lists grown until they fit (a debug path must not leave the
+// abort word set for the frame's later kernels).
+int order_ranks_sync(tsb_pass* p) {
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        int32_t ab0 = 0;
+        TSB_CUDA(cudaMemcpyAsync(&ab0, p->counters + 2, 4, cudaMemcpyDeviceToHost, p->stream));
+        TSB_CUDA(cudaStreamSynchronize(p->stream));
+        if (ab0) return fail(TSB_ERR_INVALID, "debug order: the frame aborted");
+        launch_order_ranks(p->sorted, tiek(p), p->rect, p->opt.ts, p->n_bin, rank_bound(p), p->ord, p->trect,
+                           superk(p), p->stream);
+        TSB_CHECK_LAUNCH();
+        int32_t h[8];
+        TSB_CUDA(cudaMemcpyAsync(h, p->counters, sizeof h, cudaMemcpyDeviceToHost, p->stream));
+        TSB_CUDA(cudaStreamSynchronize(p->stream));
+        if (!(h[2] & 1)) return TSB_OK;
+        TSB_CUDA(cudaMemsetAsync(p->counters + 2, 0, 4, p->stream));
+        int rc = ensure_super(p, p->scene->d.n, (int64_t)h[7] + h[7] / 4 + 4096);
+        if (rc) return rc;
+    }
+    return fail(TSB_ERR_UNSUPPORTED, "debug order: super-tile lists");
+}
 // The exact (depth, index) order of the prepared frame on the device (runs of equal
 // compressed keys resolved as the binning resolves them).
 int order_device(tsb_pass* p, const uint32_t** out) {
@@ -2193,14 +2318,15 @@ int order_device(tsb_pass* p, const uint32_t** out) {
     if (n > p->order_dbg_cap) {
         dev_free(p->order_dbg);
         p->order_dbg_cap = 0;
-        int rc;
-        if ((rc = dev_alloc(&p->order_dbg, n))) return rc;
+        int rc0;
+        if ((rc0 = dev_alloc(&p->order_dbg, n))) return rc0;
         p->order_dbg_cap = n;
     }
     if (p->prefix) full_order(p, false, p->stream);  // the frame sorted only its nearest prefix
-    // the scan arrays over the full order (its first ranks are the prefix's: the forward's
-    // scan positions stay valid for a backward that follows)
-    launch_order_ranks(p->sorted, tiek(p), p->rect, p->opt.ts, p->n_bin, p->scene->d.n, p->ord, p->trect, p->stream);
+    // the scan arrays over the full order (its first ranks are the prefix's, and lead every
+    // super-tile list: the forward's scan positions stay valid for a backward that follows)
+    int rc = order_ranks_sync(p);
+    if (rc) return rc;
     launch_materialize_order(p->sorted, tiek(p), p->counters, p->scene->d.n, p->order_dbg, p->stream);
     TSB_CHECK_LAUNCH();
     *out = p->order_dbg;
@@ -2330,7 +2456,12 @@ int tsb_pass_debug_set_list_capacity(tsb_pass* p, uint32_t entries) {
     if (!p || entries == 0) return fail(TSB_ERR_INVALID, "tsb_pass_debug_set_list_capacity: bad argument");
     int rc = settle(p);
     if (rc) return rc;
-    p->debug_abort = true;  // the next forward aborts on the device once (settle redoes it)
+    // the super-tile list storage shrunk to `entries`: a frame that needs more aborts on the
+    // device and is redone with grown lists when the pass settles
+    dev_free(p->sl_rank); dev_free(p->sl_rect);
+    p->sl_cap = 0;
+    if ((rc = dev_alloc(&p->sl_rank, (size_t)entries)) || (rc = dev_alloc(&p->sl_rect, (size_t)entries))) return rc;
+    p->sl_cap = (int)std::min<uint32_t>(entries, INT32_MAX / 2);
     return TSB_OK;
 }
 

@@ -63,27 +63,200 @@ int launch_sort_depth64(const double* depth64, const uint32_t* touched, uint32_t
 
 // ---------------------------------------------------------------------------
 // The scan arrays of the raster kernels (ScanK): rank -> Gaussian (runs of equal
-// compressed keys resolved once here, not by every reader) and its tile rect.
-__global__ void __launch_bounds__(256) k_order_ranks(const uint32_t* __restrict__ sorted, TieK T,
-                                                     const uint2* __restrict__ rect, int ts,
-                                                     const int32_t* __restrict__ n_rank, uint32_t* __restrict__ ord,
-                                                     uint2* __restrict__ trect) {
-    if (*T.abort) return;
-    const int V = *n_rank;
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < V; r += gridDim.x * blockDim.x) {
-        const uint32_t g = sorted_at(sorted, T, r, V);
-        const uint2 rc = rect[g];
-        const int x0 = rc.x & 0xffff, x1 = rc.x >> 16, y0 = rc.y & 0xffff, y1 = rc.y >> 16;
-        ord[r] = g;
-        trect[r] = make_uint2((uint32_t)(x0 / ts) | ((uint32_t)((x1 - 1) / ts) << 16),
-                              (uint32_t)(y0 / ts) | ((uint32_t)((y1 - 1) / ts) << 16));
+// compressed keys resolved once here, not by every reader) and its tile rect, and the
+// super-tile lists.  A block per chunk of kSlChunk ranks; the chunk's rank count per
+// super-tile goes to hist[s][chunk] (shared-memory counters: a rect meets a few
+// super-tiles).
+__device__ __forceinline__ void super_rect(uint2 tr, int lg, int& sx0, int& sx1, int& sy0, int& sy1) {
+    sx0 = (int)(tr.x & 0xffffu) >> lg;
+    sx1 = (int)(tr.x >> 16) >> lg;
+    sy0 = (int)(tr.y & 0xffffu) >> lg;
+    sy1 = (int)(tr.y >> 16) >> lg;
+}
+
+// The block's contiguous range of chunks (the same in k_order_ranks and k_sl_emit: the
+// histogram holds one column per block).
+__device__ __forceinline__ void block_chunks(int V, int& c0, int& c1) {
+    const int nch = (V + kSlChunk - 1) / kSlChunk, per = (nch + gridDim.x - 1) / gridDim.x;
+    c0 = min(nch, (int)blockIdx.x * per);
+    c1 = min(nch, c0 + per);
+}
+
+// The rank -> Gaussian / tile rect arrays and each block's count of (rank, super-tile)
+// pairs per super-tile (shared-memory counters: a rect meets a few super-tiles).  The
+// last block to finish turns the counts into the lists' offsets (super-tile major, blocks
+// in rank order) and sl_off.
+__global__ void __launch_bounds__(kSlChunk) k_order_ranks(const uint32_t* __restrict__ sorted, TieK T,
+                                                          const uint2* __restrict__ rect, int ts,
+                                                          const int32_t* __restrict__ n_rank, uint32_t* __restrict__ ord,
+                                                          uint2* __restrict__ trect, SuperK sk) {
+    __shared__ uint32_t cnt[kSlMaxSup];
+    __shared__ bool is_last;
+    if (block_aborted(T.abort)) return;
+    const int V = *n_rank, tid = threadIdx.x;
+    int c0, c1;
+    block_chunks(V, c0, c1);
+    for (int s = tid; s < sk.nsup; s += kSlChunk) cnt[s] = 0;
+    __syncthreads();
+    for (int c = c0; c < c1; ++c) {
+        const int r = c * kSlChunk + tid;
+        if (r < V) {
+            const uint32_t g = sorted_at(sorted, T, r, V);
+            const uint2 rc = rect[g];
+            const int x0 = rc.x & 0xffff, x1 = rc.x >> 16, y0 = rc.y & 0xffff, y1 = rc.y >> 16;
+            const uint2 tr = make_uint2((uint32_t)(x0 / ts) | ((uint32_t)((x1 - 1) / ts) << 16),
+                                        (uint32_t)(y0 / ts) | ((uint32_t)((y1 - 1) / ts) << 16));
+            ord[r] = g;
+            trect[r] = tr;
+            int sx0, sx1, sy0, sy1;
+            super_rect(tr, sk.sup_log, sx0, sx1, sy0, sy1);
+            for (int sy = sy0; sy <= sy1; ++sy)
+                for (int sx = sx0; sx <= sx1; ++sx) atomicAdd(&cnt[sy * sk.sup_x + sx], 1u);
+        }
+    }
+    __syncthreads();
+    for (int s = tid; s < sk.nsup; s += kSlChunk) {
+        sk.hist[(size_t)s * sk.hist_stride + blockIdx.x] = cnt[s];
+        if (blockIdx.x == 0)  // the padding columns of the row (the scan reads whole uint4)
+            for (int c = gridDim.x; c % 4; ++c) sk.hist[(size_t)s * sk.hist_stride + c] = 0u;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) is_last = atomicAdd(sk.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    // exclusive offsets over (super-tile, block): a thread per super-tile row (its blocks'
+    // counts, contiguous; rows padded to a multiple of 4 columns), the row bases by one
+    // thread (nsup <= 1024 additions)
+    const int G = gridDim.x, nsup = sk.nsup, G4 = (G + 3) / 4;
+    __shared__ uint32_t rowbase[kSlMaxSup + 1];
+    for (int sr = tid; sr < nsup; sr += kSlChunk) {
+        const uint4* row = reinterpret_cast<const uint4*>(sk.hist + (size_t)sr * sk.hist_stride);
+        uint32_t t = 0;
+        for (int q0 = 0; q0 < G4; q0 += 8) {  // 8 loads in flight
+            uint4 v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = q0 + k < G4 ? __ldcg(row + q0 + k) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) t += v[k].x + v[k].y + v[k].z + v[k].w;
+        }
+        rowbase[sr] = t;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t acc = 0;
+        for (int sr = 0; sr < nsup; ++sr) {
+            const uint32_t t = rowbase[sr];
+            rowbase[sr] = acc;
+            sk.off[sr] = acc;
+            acc += t;
+        }
+        rowbase[nsup] = acc;
+    }
+    __syncthreads();
+    for (int sr = tid; sr < nsup; sr += kSlChunk) {
+        uint4* row = reinterpret_cast<uint4*>(sk.hist + (size_t)sr * sk.hist_stride);
+        uint32_t off = rowbase[sr];
+        for (int q0 = 0; q0 < G4; q0 += 8) {
+            uint4 v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = q0 + k < G4 ? __ldcg(row + q0 + k) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (q0 + k >= G4) break;
+                uint4 o;
+                o.x = off; off += v[k].x;
+                o.y = off; off += v[k].y;
+                o.z = off; off += v[k].z;
+                o.w = off; off += v[k].w;
+                row[q0 + k] = o;
+            }
+        }
+    }
+    if (tid == 0) {
+        const uint32_t total = rowbase[nsup];
+        sk.off[nsup] = total;
+        *sk.total = (int32_t)min(total, 0x7fffffffu);
+        if (total > (uint32_t)sk.cap) atomicOr(T.abort, 1);  // the lists need more storage: redo
+        *sk.ticket = 0u;
+        if (sk.work) {
+            atomicAdd(&sk.work[2], (unsigned long long)V);
+            atomicAdd(&sk.work[3], (unsigned long long)total);
+        }
     }
 }
 
-void launch_order_ranks(const uint32_t* sorted, const TieK& T, const uint2* rect, int ts, const int32_t* n_rank,
-                        int n, uint32_t* ord, uint2* trect, cudaStream_t st) {
-    if (n <= 0) return;
-    k_order_ranks<<<std::min(148 * 8, (n + 255) / 256), 256, 0, st>>>(sorted, T, rect, ts, n_rank, ord, trect);
+// Each block's ranks into the lists of the super-tiles their rects meet, in rank order:
+// per super-tile, a warp ballot ranks a chunk's covering lanes; the warp counts of a first
+// sweep give the warps' bases, and the block's running base per super-tile starts at its
+// scanned offset.
+__global__ void __launch_bounds__(kSlChunk) k_sl_emit(const int32_t* __restrict__ n_rank,
+                                                      const uint2* __restrict__ trect, SuperK sk,
+                                                      const int32_t* __restrict__ abort) {
+    __shared__ uint16_t wc[kSlChunk / 32][kSlMaxSup];
+    __shared__ uint32_t base[kSlMaxSup];
+    if (block_aborted(abort)) return;
+    const int V = *n_rank;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t below = (1u << lane) - 1u;
+    int c0, c1;
+    block_chunks(V, c0, c1);
+    if (c0 >= c1) return;
+    for (int s = threadIdx.x; s < sk.nsup; s += kSlChunk) base[s] = sk.hist[(size_t)s * sk.hist_stride + blockIdx.x];
+    const int nsy = (sk.nsup + sk.sup_x - 1) / sk.sup_x;
+    for (int c = c0; c < c1; ++c) {
+        const int r = c * kSlChunk + threadIdx.x;
+        int sx0 = 1, sx1 = 0, sy0 = 1, sy1 = 0;
+        uint2 tr = make_uint2(0u, 0u);
+        if (r < V) {
+            tr = trect[r];
+            super_rect(tr, sk.sup_log, sx0, sx1, sy0, sy1);
+        }
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int sy = 0; sy < nsy; ++sy) {
+                const bool row = sy0 <= sy && sy <= sy1;
+                if (!__any_sync(0xffffffffu, row)) {
+                    if (pass == 0)
+                        for (int sx = lane; sx < sk.sup_x; sx += 32) wc[warp][sy * sk.sup_x + sx] = 0;
+                    continue;
+                }
+                for (int sx = 0; sx < sk.sup_x; ++sx) {
+                    const int s = sy * sk.sup_x + sx;
+                    const bool cov = row && sx0 <= sx && sx <= sx1;
+                    const unsigned b = __ballot_sync(0xffffffffu, cov);
+                    if (pass == 0) {
+                        if (lane == 0) wc[warp][s] = (uint16_t)__popc(b);
+                    } else if (cov) {
+                        uint32_t pos = base[s] + __popc(b & below);
+                        for (int w = 0; w < warp; ++w) pos += wc[w][s];
+                        sk.rank[pos] = (uint32_t)r;
+                        sk.rect[pos] = tr;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        for (int s = threadIdx.x; s < sk.nsup; s += kSlChunk) {
+            uint32_t t = 0;
+#pragma unroll
+            for (int w = 0; w < kSlChunk / 32; ++w) t += wc[w][s];
+            base[s] += t;
+        }
+        __syncthreads();
+    }
+}
+
+int launch_order_ranks(const uint32_t* sorted, const TieK& T, const uint2* rect, int ts, const int32_t* n_rank,
+                       int n, uint32_t* ord, uint2* trect, const SuperK& sk, cudaStream_t st) {
+    if (n <= 0) return 0;
+    const int grid = std::min(sk.hist_stride, (n + kSlChunk - 1) / kSlChunk);
+    // the ticket starts at 0 even when an earlier launch ended early (an abort raised while
+    // its blocks ran leaves it partly counted)
+    cudaMemsetAsync(sk.ticket, 0, sizeof(uint32_t), st);
+    k_order_ranks<<<grid, kSlChunk, 0, st>>>(sorted, T, rect, ts, n_rank, ord, trect, sk);
+    k_sl_emit<<<grid, kSlChunk, 0, st>>>(n_rank, trect, sk, T.abort);
+    return 2;
 }
 
 // Deterministic backward: det_off[r] = sum over ranks r' < r of (rect area in tiles) x
@@ -122,7 +295,7 @@ void launch_det_offsets(const ScanK& sc, uint32_t* det_off, uint32_t* total, cud
 // Each visible Gaussian's screen-space gradients: its slots summed over its rect's tiles
 // (row-major) and the tiles' raster sub-blocks, always in that order.
 __global__ void __launch_bounds__(256) k_det_reduce(ScanK sc, double* __restrict__ screen, int scap) {
-    if (*sc.abort) return;
+    if (block_aborted(sc.abort)) return;
     const int V = *sc.n_rank;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < V; r += gridDim.x * blockDim.x) {
         const uint32_t s0 = sc.det_off[r], s1 = sc.det_off[r + 1];

@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_fwd(RecK rec, SceneK S, 
     __shared__ uint32_t sg[kRasterThreads];
     __shared__ int smax[kRasterThreads / 32];
     __shared__ int wsum[2][kRasterThreads / 32];
-    if (*px.abort) return;
+    if (block_aborted(px.abort)) return;
     const int W = C.W, H = C.H, tid = threadIdx.x;
     const PixMap m = pix_map(O, W, H);
     const int ttx = m.tile % O.tiles_x, tty = m.tile / O.tiles_x;
@@ -140,15 +140,16 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_fwd(RecK rec, SceneK S, 
 #pragma unroll
     for (int c = 0; c < 9; ++c) acc[c] = 0.0;
     // the tile's list up to the block's furthest pixel: the rank order scanned upwards
-    const int V = *sc.n_rank;
+    const ScanSeg seg = scan_seg(sc, ttx, tty);
+    const int V = seg.n;
     int pass = 0;
     for (int r0 = 0, ebase = 0; r0 < V && ebase < bmax; r0 += kRasterThreads, ++pass) {
         const int rr = r0 + tid;
-        const bool cov = rr < V && tile_covers(sc.trect[rr], ttx, tty);
+        const bool cov = rr < V && tile_covers(seg.rect[rr], ttx, tty);
         int total;
         const int pos = scan_compact(cov, wsum[pass & 1], total);  // (its barrier follows the last pass's reads)
         if (pos >= 0) {
-            const uint32_t r = sc.ord[rr];
+            const uint32_t r = sc.ord[seg.rank[rr]];
             sg[pos] = r;
             sA[pos] = stage_A(rec.A[r], m.ox, m.oy);
             sB[pos] = rec.B[r];
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_bwd(RecK rec, OptK O, in
     __shared__ int smax[kRasterThreads / 32];
     __shared__ int wsum[2][kRasterThreads / 32];
     __shared__ float sbg[kRasterThreads / 32][3];
-    if (*px.abort) return;
+    if (block_aborted(px.abort)) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const PixMap m = pix_map(O, W, H);
     const int ttx = m.tile % O.tiles_x, tty = m.tile / O.tiles_x;
@@ -299,17 +300,18 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_bwd(RecK rec, OptK O, in
     const float cut2 = O.cut2_f, thr = O.alpha_thr_f;
     // the tile's list back to front: the rank order scanned downwards from where the forward stopped
     const int2 bt = sc.blk_term[blockIdx.x];
+    const ScanSeg seg = scan_seg(sc, ttx, tty);
     const uint32_t wbit = 1u << warp;
     int pass = 0;
     for (int r_hi = bt.x, e_top = bt.y; bmax > 0 && r_hi > 0 && e_top > 0; r_hi -= kRasterThreads, ++pass) {
         const int rr = r_hi - 1 - tid;
-        const bool cov = rr >= 0 && tile_covers(sc.trect[rr], ttx, tty);
+        const bool cov = rr >= 0 && tile_covers(seg.rect[rr], ttx, tty);
         int total;
         const int pos = scan_compact(cov, wsum[pass & 1], total);  // descending rank order
         const int e_lo = e_top - total;
         if (pos >= 0) {
             const int j = total - 1 - pos;  // ascending
-            const uint32_t r = sc.ord[rr];
+            const uint32_t r = sc.ord[seg.rank[rr]];
             srank[j] = r;
             sA[j] = stage_A(rec.A[r], m.ox, m.oy);
             sB[j] = rec.B[r];

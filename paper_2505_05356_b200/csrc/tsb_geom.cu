@@ -319,13 +319,14 @@ __global__ void __launch_bounds__(128) k_fixup_mark(OptK O, FixupK fx, PixK px, 
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    const int count = *fx.overflow ? 0 : *px.n_flagged;
+    const int count = block_aborted(fx.overflow) ? 0 : *px.n_flagged;
     const int stamp = fd->stamp;
-    const int V = *fx.sc.n_rank;
     for (int i = warp; i < count; i += nwarps) {
         const int pix = px.flagged[i] & 0xffffff;
         const int x = pix % W, y = pix / W;
         const int tx = x / O.ts, ty = y / O.ts;
+        const ScanSeg seg = scan_seg(fx.sc, tx, ty);
+        const int V = seg.n;
         const int limit = (px.last[pix] & kLastMask) + 64;
         int e = 0, r_from = 0;
         const int rb = raster_block(O, x, y);
@@ -344,10 +345,10 @@ __global__ void __launch_bounds__(128) k_fixup_mark(OptK O, FixupK fx, PixK px, 
         }
         for (int r0 = r_from; r0 < V && e < limit; r0 += 32) {
             const int r = r0 + lane;
-            const bool cov = r < V && tile_covers(fx.sc.trect[r], tx, ty);
+            const bool cov = r < V && tile_covers(seg.rect[r], tx, ty);
             const unsigned m = __ballot_sync(0xffffffffu, cov);
             if (cov && e + __popc(m & ((1u << lane) - 1u)) < limit) {
-                const uint32_t g = fx.sc.ord[r];
+                const uint32_t g = fx.sc.ord[seg.rank[r]];
                 if (atomicExch(&fx.stamp[g], stamp) != stamp) {
                     const int slot = atomicAdd(fx.work_n, 1);
                     fx.work[slot] = (int)g;
@@ -484,17 +485,22 @@ __device__ __forceinline__ void fixup_batch(const SceneK& S, const CamK& C, cons
 // on full batches of 32 entries (a tile list holds ~1-7 % of the ranks).
 constexpr int kScanK = 4;                    // rank groups of 32 per step
 constexpr int kQueue = 32 + 32 * kScanK;     // entries a queue can hold after a step
-__device__ __forceinline__ void queue_step(const ScanK& sc, int r0, int V, bool descending, int tx, int ty,
-                                           int* qg, int* qr, int& qn, int lane, int r_min = 0) {
+// Scan positions index the tile's super-tile list (ScanSeg); qr receives the position
+// (pos_out) or the rank.
+__device__ __forceinline__ void queue_step(const ScanK& sc, const ScanSeg& seg, int r0, bool descending, int tx,
+                                           int ty, int* qg, int* qr, int& qn, int lane, bool pos_out,
+                                           int r_min = 0) {
     const uint32_t below = (1u << lane) - 1u;
+    const int V = seg.n;
 #pragma unroll
     for (int k = 0; k < kScanK; ++k) {
         const int r = descending ? r0 - 1 - (32 * k + lane) : r0 + 32 * k + lane;
-        const bool cov = r >= r_min && r < V && tile_covers(sc.trect[r], tx, ty);
+        const bool cov = r >= r_min && r < V && tile_covers(seg.rect[r], tx, ty);
         const unsigned m = __ballot_sync(0xffffffffu, cov);
         if (cov) {
-            qg[qn + __popc(m & below)] = (int)sc.ord[r];
-            qr[qn + __popc(m & below)] = r;
+            const uint32_t rk = seg.rank[r];
+            qg[qn + __popc(m & below)] = (int)sc.ord[rk];
+            qr[qn + __popc(m & below)] = pos_out ? r : (int)rk;
         }
         qn += __popc(m);
     }
@@ -532,15 +538,17 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, const F
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     FixSlot* slot = slots[threadIdx.x >> 5];
-    const int count = *fx.overflow ? 0 : *px.n_flagged;
+    const int count = block_aborted(fx.overflow) ? 0 : *px.n_flagged;
     const int W = C.W;
     const size_t HW = (size_t)W * C.H;
-    const int V = *fx.sc.n_rank;
+    const int V_all = *fx.sc.n_rank;
     const uint32_t lanes_below = (1u << lane) - 1u;
     for (int i = warp; i < count; i += nwarps) {
         const int pix = px.flagged[i] & 0xffffff;
         const int x = pix % W, y = pix / W;
         const int tx = x / O.ts, ty = y / O.ts;
+        const ScanSeg seg = scan_seg(fx.sc, tx, ty);
+        const int V = seg.n;
         FixupAcc a;
         a.T = 1.0; a.SW = 0.0; a.SD = 0.0; a.Tpre = 1.0; a.Tpre_le = 1.0;
         a.dref = 0.0; a.SDs = 0.0; a.SD2s = 0.0;
@@ -562,25 +570,25 @@ __global__ void __launch_bounds__(128) k_fixup(SceneK S, CamK C, OptK O, const F
                     fixup_batch(S, C, O, F, fx, stamp, nf, x, y, is_e, is_e ? (int)fx.sc.ord[rk] : 0, e0 + lane, slot,
                                 a, lane);
                     if (!a.done) a.processed = min(bt.y, e0 + 32);
-                    else r_end = __shfl_sync(0xffffffffu, rk, a.processed - 1 - e0) + 1;
+                    else r_end = bt.x;  // ended inside the list: the backward walks only the list
                 }
                 r_from = bt.x;
             }
         }
         for (int r0 = r_from; !a.done && (r0 < V || qn > 0); r0 += 32 * kScanK) {
-            if (r0 < V) queue_step(fx.sc, r0, V, false, tx, ty, qg, qr, qn, lane);
+            if (r0 < V) queue_step(fx.sc, seg, r0, false, tx, ty, qg, qr, qn, lane, true);
             const bool flush = r0 + 32 * kScanK >= V;  // no more ranks: run the partial batch
             while (!a.done && (qn >= 32 || (flush && qn > 0))) {
                 const bool is_e = lane < qn;
                 const int e0 = a.processed;
                 fixup_batch(S, C, O, F, fx, stamp, nf, x, y, is_e, is_e ? qg[lane] : 0, e0 + lane, slot, a, lane);
                 if (!a.done) a.processed = e0 + min(qn, 32);
-                else r_end = qr[a.processed - 1 - e0] + 1;  // rank after the terminating entry
+                else r_end = qr[a.processed - 1 - e0] + 1;  // position after the terminating entry
                 queue_pop32(qg, qr, qn, lane);
             }
         }
         // the prefix order ended with the pixel alive: the frame is redone with the full order
-        if (!a.done && lane == 0 && V < *fx.sc.n_all) atomicOr(fx.overflow, 8);
+        if (!a.done && lane == 0 && V_all < *fx.sc.n_all) atomicOr(fx.overflow, 8);
         if (lane == 0) {
             const size_t o = (size_t)y * W + x;
             #pragma unroll
@@ -818,11 +826,11 @@ __device__ void fixbwd_pixel(const SceneK& S, const CamK& C, const OptK& O, cons
                              const Out& out, int lane) {
     const int W = C.W;
     const size_t HW = (size_t)W * C.H;
-    const int V = *fx.sc.n_rank;
     const int last = px.last[pix] & kLastMask;
     const FixState st = fx.state[i];
     const int x = pix % W, y = pix / W;
     const int tx = x / O.ts, ty = y / O.ts;
+    const ScanSeg seg = scan_seg(fx.sc, tx, ty);
     const size_t o = (size_t)pix;
     BwdPix b;
     b.A = 0.0;
@@ -864,7 +872,7 @@ __device__ void fixbwd_pixel(const SceneK& S, const CamK& C, const OptK& O, cons
     const int r_lo = listed ? bt.x : 0;  // the rank scan covers [r_lo, r_end)
     int qn = 0, e_hi = st.e_end;
     for (int r_hi = st.r_end; e_hi > 0 && (r_hi > r_lo || qn > 0); r_hi -= 32 * kScanK) {
-        if (r_hi > r_lo) queue_step(fx.sc, r_hi, V, true, tx, ty, qg, qr, qn, lane, r_lo);
+        if (r_hi > r_lo) queue_step(fx.sc, seg, r_hi, true, tx, ty, qg, qr, qn, lane, false, r_lo);
         const bool flush = r_hi - 32 * kScanK <= r_lo;
         while (e_hi > 0 && (qn >= 32 || (flush && qn > 0))) {
             const int e = e_hi - 1 - lane;  // queued entries in descending list order
@@ -894,7 +902,7 @@ __global__ void __launch_bounds__(128) k_fixup_bwd(SceneK S, CamK C, OptK O, con
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    const int count = *fx.overflow ? 0 : min(*px.n_flagged, fx.state_cap);
+    const int count = block_aborted(fx.overflow) ? 0 : min(*px.n_flagged, fx.state_cap);
     const AtomicOut out{screen, scap};
     for (int i = warp; i < count; i += nwarps) {
         const int pix = px.flagged[i] & 0xffffff;
@@ -909,7 +917,7 @@ __global__ void __launch_bounds__(128) k_fixup_bwd(SceneK S, CamK C, OptK O, con
 __global__ void __launch_bounds__(128) k_fixup_bwd_det(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd,
                                                        FixupK fx, PixK px, UpK up, int nf) {
     __shared__ int queue_g[4][kQueue], queue_r[4][kQueue];
-    if (*fx.overflow) return;
+    if (block_aborted(fx.overflow)) return;
     const int lane = threadIdx.x & 31;
     const int rb = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nsub2 = O.sub * O.sub;

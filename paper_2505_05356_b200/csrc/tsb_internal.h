@@ -113,11 +113,52 @@ struct ScanK {
     const uint32_t* det_off;   // [n_rank + 1] first slot of each rank (rect area x sub-blocks, scanned)
     float* det_part;           // [slots][8]
     int nsub2;                 // raster blocks per tile
+    // Super-tile lists: the ranks whose tile rect meets each super-tile (2^sup_log x 2^sup_log
+    // tiles), in rank order, with their rects.  A block scans its super-tile's list instead of
+    // the whole order; scan positions (blk_term.x, FixState::r_end) index that list.
+    const uint32_t* sl_off;    // [nsup + 1]
+    const uint32_t* sl_rank;   // [sl_cap]
+    const uint2* sl_rect;      // [sl_cap]
+    int sup_x, sup_log;
+};
+// One tile's scan list: its super-tile's ranks, rects and length.
+struct ScanSeg {
+    const uint32_t* rank;
+    const uint2* rect;
+    int n;
+};
+__device__ __forceinline__ ScanSeg scan_seg(const ScanK& sc, int tx, int ty) {
+    const int s = (ty >> sc.sup_log) * sc.sup_x + (tx >> sc.sup_log);
+    const uint32_t a = sc.sl_off[s], b = sc.sl_off[s + 1];
+    return ScanSeg{sc.sl_rank + a, sc.sl_rect + a, (int)(b - a)};
+}
+// Build arguments of the super-tile lists (k_order_ranks counts + scan, k_sl_emit).
+constexpr int kSlChunk = 256;     // ranks per counting chunk
+constexpr int kSlMaxSup = 1024;   // super-tiles per frame (the super-tile grows past this)
+constexpr int kSlMaxBlocks = 148 * 2;  // blocks building the lists (contiguous rank ranges each; % 4 == 0)
+struct SuperK {
+    uint32_t* hist;    // [nsup][hist_stride] per-block counts -> exclusive offsets
+    int hist_stride;   // histogram columns = the build grid's upper bound (<= kSlMaxBlocks)
+    uint32_t* ticket;  // blocks of k_order_ranks done (the last scans; reset to 0 by it)
+    uint32_t* off;     // ScanK::sl_off
+    uint32_t* rank;    // ScanK::sl_rank
+    uint2* rect;       // ScanK::sl_rect
+    int cap;           // entries the lists can hold; more: abort bit 1, the total in *total
+    int32_t* total;
+    int sup_x, sup_log, nsup;
+    unsigned long long* work;  // profiling: [2] += ranks, [3] += list entries (null: not counted)
 };
 // The slot of (rank r with tile rect tr, tile (tx, ty), raster sub-block sb).
 __device__ __forceinline__ size_t det_slot(const ScanK& sc, int r, uint2 tr, int tx, int ty, int sb) {
     const int tx0 = tr.x & 0xffff, w = (int)(tr.x >> 16) - tx0 + 1, ty0 = tr.y & 0xffff;
     return (size_t)sc.det_off[r] + ((size_t)(ty - ty0) * w + (tx - tx0)) * sc.nsub2 + sb;
+}
+// Block-uniform test of a frame abort word.  Kernels raise the word while other blocks of
+// the same launch are starting (the raster's bit 8, the tie reader's bit 2, ...), so the
+// threads of one block could read different values; the exit decision -- and with it every
+// barrier and warp collective that follows -- must be the block's.
+__device__ __forceinline__ bool block_aborted(const int32_t* a) {
+    return __syncthreads_or(a != nullptr && *reinterpret_cast<const volatile int32_t*>(a) != 0);
 }
 __device__ __forceinline__ bool tile_covers(uint2 tr, int tx, int ty) {
     return (int)(tr.x & 0xffffu) <= tx && tx <= (int)(tr.x >> 16) && (int)(tr.y & 0xffffu) <= ty &&
@@ -252,8 +293,9 @@ void launch_materialize_order(const uint32_t* sorted, const TieK& T, const int32
 int launch_sort_depth64(const double* depth64, const uint32_t* touched, uint32_t* keys_a, uint32_t* keys_b,
                         uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch, cudaStream_t st);
 // ord / trect of ranks r < *n_rank (the raster kernels' scan arrays, ScanK)
-void launch_order_ranks(const uint32_t* sorted, const TieK& T, const uint2* rect, int ts, const int32_t* n_rank,
-                        int n, uint32_t* ord, uint2* trect, cudaStream_t st);
+// + the super-tile lists (2 kernels; returns the launch count); n: upper bound of *n_rank
+int launch_order_ranks(const uint32_t* sorted, const TieK& T, const uint2* rect, int ts, const int32_t* n_rank,
+                       int n, uint32_t* ord, uint2* trect, const SuperK& sk, cudaStream_t st);
 // deterministic backward: slot offsets of the ranks (device scan; writes det_off[0..V]) and
 // the fixed-order reduction of the slots into the screen-space gradients (+=)
 void launch_det_offsets(const ScanK& sc, uint32_t* det_off, uint32_t* total, cudaStream_t st);

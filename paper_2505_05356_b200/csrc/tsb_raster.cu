@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK s
                                                                 double* __restrict__ loss_part) {
     __shared__ Smem<NF> sm;
     __shared__ float red[kRasterThreads / 32];
-    if (*sc.abort) return;
+    if (block_aborted(sc.abort)) return;
     const float* __restrict__ target = loss ? fd->target : nullptr;
     const int nsub = O.sub * O.sub;
     const int tile = blockIdx.x / nsub, sb = blockIdx.x % nsub;
@@ -124,17 +124,19 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK s
     const float outside = cut2 + coarseM;  // maha above this is outside, with no ambiguity to check
     // common-path tests with one compare each; the exact windows are re-tested inside
     const float m_lo = cut2 - 2.f * coarseM, a_hi = thr + 2.f * coarseA;
-    const int V = *sc.n_rank;
+    const ScanSeg seg = scan_seg(sc, ttx, tty);
+    const int V = seg.n;
     int r = 0, ebase = 0, cnt = 0, pass = 0;
 
     if (__syncthreads_count(done) < kRasterThreads) {
         while (r < V) {
-            // scan pass: ranks r .. r + 255, covering ones appended to the batch
-            const int rr = r + tid;
-            const bool cov = rr < V && tile_covers(sc.trect[rr], ttx, tty);
+            // scan pass: super-tile list positions r .. r + 255, covering ranks appended to the batch
+            const int p = r + tid;
+            const bool cov = p < V && tile_covers(seg.rect[p], ttx, tty);
             int total;
             const int pos = scan_compact(cov, sm.wsum[pass & 1], total);
             if (pos >= 0) {
+                const uint32_t rr = seg.rank[p];
                 const uint32_t g = sc.ord[rr];
                 stage_entry<NF>(sm, rec, g, cnt + pos, ox, oy, outside);
                 const int e = ebase + cnt + pos;  // list index: its rank is recorded for the backward
@@ -237,7 +239,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK s
     if (!done) processed = ebase;
     if (tid == 0) sc.blk_term[blockIdx.x] = make_int2(min(r, V), ebase);
     // the prefix order ended with the pixel alive: the frame is redone with the full order
-    if (active && !done && *sc.n_all > V) atomicOr(sc.abort, 8);
+    if (active && !done && *sc.n_all > *sc.n_rank) atomicOr(sc.abort, 8);
     float lpx = 0.f;
     if (active) {
         // T's relative error bound grows by ~eps alpha / (1 - alpha) per contribution: an
@@ -315,7 +317,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK s
 // Loss + d_quad for the fp64-fixed pixels (after k_fixup).
 __global__ void k_fixup_loss(PixK px, int W, int H, int nf, const FrameDev* __restrict__ fd, ChW chw,
                              double* __restrict__ loss_extra) {
-    if (*px.abort) return;
+    if (block_aborted(px.abort)) return;
     const float* __restrict__ target = fd->target;
     const int count = *px.n_flagged;
     double l = 0.0;
@@ -377,7 +379,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, ScanK s
     __shared__ float sbg[kRasterThreads / 32][6 * NF];
     extern __shared__ float slot_mem[];  // [warp][kBwdSub][8]: per warp, per entry: its reduced gradients
     float (*slot)[kBwdSub][8] = reinterpret_cast<float (*)[kBwdSub][8]>(slot_mem);
-    if (*px.abort) return;  // aborted frame: no gradient is written (the host redoes it)
+    if (block_aborted(px.abort)) return;  // aborted frame: no gradient is written (the host redoes it)
     const int nsub = O.sub * O.sub;
     const int tile = blockIdx.x / nsub, sb = blockIdx.x % nsub;
     const int ttx = tile % O.tiles_x, tty = tile / O.tiles_x;
@@ -480,7 +482,8 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, ScanK s
     // is scanned downwards from where the forward stopped.
     const int2 bt = sc.blk_term[blockIdx.x];
     const bool listed = bt.y <= kBlkListCap;
-    int r_hi = bt.x;
+    const ScanSeg seg = scan_seg(sc, ttx, tty);
+    int r_hi = bt.x;  // super-tile list position
     int cnt = 0, pass = 0, e_top = listed ? min(bt.y, bmax) : bt.y;
     while (bmax > 0 && e_top > 0 && (listed || r_hi > 0)) {
         if (listed) {
@@ -496,8 +499,8 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, ScanK s
             cnt = nb;
             e_top -= nb;
         } else {
-            const int rr = r_hi - 1 - tid;
-            const bool cov = rr >= 0 && tile_covers(sc.trect[rr], ttx, tty);
+            const int p = r_hi - 1 - tid;
+            const bool cov = p >= 0 && tile_covers(seg.rect[p], ttx, tty);
             int total;
             const int pos = scan_compact(cov, sm.wsum[pass & 1], total);  // descending rank order
             // entries of this pass: indices [e_top - total, e_top); keep those below bmax
@@ -505,6 +508,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, ScanK s
             const int asc = total - 1 - pos;
             if (pos >= 0 && asc < keep_hi) {
                 const int slot = kBatchCap - cnt - keep_hi + asc;
+                const uint32_t rr = seg.rank[p];
                 const uint32_t g = sc.ord[rr];
                 sm.grank[slot] = g;
                 sm.rrank[slot] = (uint32_t)rr;
@@ -651,7 +655,7 @@ __global__ void __launch_bounds__(1024) k_fixup_loss_det(PixK px, int W, int H, 
                                                          const FrameDev* __restrict__ fd, ChW chw,
                                                          double* __restrict__ loss_extra) {
     __shared__ double part[1024];
-    if (*px.abort) return;
+    if (block_aborted(px.abort)) return;
     const float* __restrict__ target = fd->target;
     const size_t HW = (size_t)W * H;
     const float s2 = 2.f / (float)HW;
@@ -713,7 +717,7 @@ __global__ void k_reduce_partials(const double* __restrict__ part, int nparts, i
                                   double* __restrict__ out, double scale, const int32_t* __restrict__ abort) {
     // one block; column c summed in a fixed order (deterministic)
     __shared__ double s[256];
-    if (abort && *abort) return;
+    if (block_aborted(abort)) return;
     for (int c = 0; c < width; ++c) {
         double a = 0.0;
         for (int i = threadIdx.x; i < nparts; i += blockDim.x) a += part[(size_t)i * width + c];

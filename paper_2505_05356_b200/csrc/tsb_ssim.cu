@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(kTW* kTH) k_ssim_fwd(const float* __restrict__
     __shared__ double sx[kSH][kSW], sy[kSH][kSW];
     __shared__ double hq[5][kSH][kTW];
     __shared__ double red[kTW * kTH / 32];
-    if (a.abort && *a.abort) return;
+    if (block_aborted(a.abort)) return;
     const float* __restrict__ y = a.fd->target;
     const int c = a.chans[blockIdx.z];
     double* __restrict__ g = a.g;
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kTW* kTH) k_ssim_fwd(const float* __restrict__
 __global__ void __launch_bounds__(kTW* kTH) k_ssim_bwd(const float* __restrict__ x, int W, int H, SsimArgs a) {
     __shared__ double sg[3][kSH][kSW];
     __shared__ double hq[3][kSH][kTW];
-    if (a.abort && *a.abort) return;
+    if (block_aborted(a.abort)) return;
     const float* __restrict__ y = a.fd->target;
     const int c = a.chans[blockIdx.z];
     const double* __restrict__ g = a.g;
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kTW* kTH) k_ssim_bwd(const float* __restrict__
 // loss += sum_z lam_w[z] * (1 - sum_blocks(part[z]) / npx)
 __global__ void k_ssim_loss(SsimArgs a, int nblocks, double npx) {
     __shared__ double s[256];
-    if (a.abort && *a.abort) return;
+    if (block_aborted(a.abort)) return;
     double total = 0.0;
     for (int z = 0; z < a.nz; ++z) {
         double acc = 0.0;

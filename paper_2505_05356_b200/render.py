@@ -207,6 +207,12 @@ class Context:
         check(lib().tsb_ctx_raster_counts(self._h, C.byref(e), C.byref(c)))
         return e.value, c.value
 
+    def scan_counts(self):
+        """(ranks, super-tile list entries) of the frames' orders since the last call (profiling mode)."""
+        r, e = C.c_int64(), C.c_int64()
+        check(lib().tsb_ctx_scan_counts(self._h, C.byref(r), C.byref(e)))
+        return r.value, e.value
+
     def stage_times(self):
         """{stage: (ms_total, calls)} since the last call (synchronises)."""
         ms = (C.c_double * len(_abi.STAGES))()

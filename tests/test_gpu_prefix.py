@@ -88,3 +88,19 @@ def test_lean_visibility_equals_exact(tsb, ctx, name, cam):
     assert res[False][0] == res[True][0]
     for k in ("quad", "depth_raw", "weight", "transmittance", "n_contrib", "n_processed"):
         assert np.array_equal(res[False][1][k], res[True][1][k], equal_nan=True), k
+
+
+@pytest.mark.skipif("TSB_PREFIX" in os.environ, reason="sets its own cap")
+@pytest.mark.parametrize("det", [0, 1])
+def test_abort_raised_mid_launch_is_block_uniform(det):
+    """Regression: the raster raises the abort word (bit 8, prefix too short) while other
+    blocks of the same launch start, and the tie reader raises bit 2 inside k_order_ranks.
+    Every kernel's entry test must be block-uniform (block_aborted) and the list build's
+    ticket must start at 0, or a block runs its barriers / warp collectives with part of
+    its threads gone (illegal addresses in ~60 % of these runs before the fix).  One pass,
+    six training frames per fresh context, cap 256: every context grows its cap through
+    aborted frames (tools/stress_prefix.py)."""
+    env = dict(os.environ, TSB_PREFIX="256")
+    r = subprocess.run([sys.executable, str(ROOT / "tools" / "stress_prefix.py"), "12", str(det), "1", "1"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
