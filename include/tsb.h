@@ -356,9 +356,10 @@ int tsb_pass_debug_screen_grads(tsb_pass* p, float* g8 /* 8 per rank */);
 /* Keep a copy of the screen-space gradients of every following backward (the chain kernel
  * consumes them); required before tsb_pass_debug_screen_grads. */
 int tsb_pass_debug_keep_screen(tsb_pass* p, int enabled);
-/* Test hook: the super-tile list storage (entries = (rank, super-tile) pairs) set to
- * `entries`; a frame that needs more aborts on the device and is redone with grown lists
- * when the pass settles (the abort + settle/redo path). */
+/* Test hook: the pass builds super-tile lists for every frame (not only long orders) and
+ * their storage (entries = (rank, super-tile) pairs) is set to `entries`; a frame that
+ * needs more aborts on the device and is redone with grown lists when the pass settles
+ * (the abort + settle/redo path). */
 int tsb_pass_debug_set_list_capacity(tsb_pass* p, uint32_t entries);
 /* Pixels the fp32 raster flagged as decision-ambiguous and recomposited in fp64. */
 int tsb_pass_debug_fixups(tsb_pass* p, int32_t* count);

@@ -190,6 +190,8 @@ struct tsb_pass {
     uint2* sl_rect = nullptr;
     int sl_cap = 0, sl_hist_cap = 0, sl_off_cap = 0;
     int sup_x = 1, sup_log = 3, nsup = 1;
+    bool sl_lists = false;  // the current frame's order is long enough for the lists (kSlMinRanks)
+    bool force_lists = false;  // test hook (tsb_pass_debug_set_list_capacity): lists at any length
     int2* blk_term = nullptr;  // per raster block: where its forward scan stopped
     uint32_t* blk_list = nullptr;  // per raster block: the list entries its forward consumed (kBlkListCap)
     // deterministic backward (TSB_CH_DETERMINISTIC): slot offsets per rank, slots, fix-up pixel index
@@ -1083,18 +1085,20 @@ int ensure_super(tsb_pass* p, int n, int64_t entries) {
     auto sups = [&](int l) {
         return ((p->opt.tiles_x + (1 << l) - 1) >> l) * ((p->opt.tiles_y + (1 << l) - 1) >> l);
     };
-    while (sups(lg) > kSlMaxSup) ++lg;
+    while (sups(lg) > kSlMaxSup || ((p->opt.tiles_x + (1 << lg) - 1) >> lg) > kSlMaxSupSide ||
+           ((p->opt.tiles_y + (1 << lg) - 1) >> lg) > kSlMaxSupSide)
+        ++lg;
     p->sup_log = lg;
     p->sup_x = (p->opt.tiles_x + (1 << lg) - 1) >> lg;
     p->nsup = sups(lg);
     int rc;
-    if (p->nsup * kSlMaxBlocks > p->sl_hist_cap) {
+    if (p->nsup * (kSlMaxBlocks + 1) > p->sl_hist_cap) {  // + the row totals
         dev_free(p->sl_hist); dev_free(p->sl_off);
         p->sl_hist_cap = p->sl_off_cap = 0;
-        if ((rc = dev_alloc(&p->sl_hist, (size_t)p->nsup * kSlMaxBlocks)) ||
+        if ((rc = dev_alloc(&p->sl_hist, (size_t)p->nsup * (kSlMaxBlocks + 1))) ||
             (rc = dev_alloc(&p->sl_off, (size_t)p->nsup + 1)))
             return rc;
-        p->sl_hist_cap = p->nsup * kSlMaxBlocks;
+        p->sl_hist_cap = p->nsup * (kSlMaxBlocks + 1);
         p->sl_off_cap = p->nsup + 1;
     }
     static const int64_t cap0 = [] {  // TSB_SL_CAP: initial list capacity (tests of the overflow redo)
@@ -1121,7 +1125,7 @@ SuperK superk(tsb_pass* p) {
     SuperK k;
     k.hist = p->sl_hist;
     k.hist_stride = kSlMaxBlocks;
-    k.ticket = reinterpret_cast<uint32_t*>(p->counters + 3);
+    k.row_total = p->sl_hist + (size_t)p->nsup * kSlMaxBlocks;
     k.off = p->sl_off;
     k.rank = p->sl_rank;
     k.rect = p->sl_rect;
@@ -1129,7 +1133,7 @@ SuperK superk(tsb_pass* p) {
     k.total = p->counters + 7;
     k.sup_x = p->sup_x;
     k.sup_log = p->sup_log;
-    k.nsup = p->nsup;
+    k.nsup = p->sl_lists ? p->nsup : 0;
     k.work = p->ctx->profiling ? p->ctx->work : nullptr;
     return k;
 }
@@ -1405,7 +1409,7 @@ ScanK scank(tsb_pass* p) {
     sc.det_off = nullptr;
     sc.det_part = nullptr;
     sc.nsub2 = p->opt.sub * p->opt.sub;
-    sc.sl_off = p->sl_off;
+    sc.sl_off = p->sl_lists ? p->sl_off : nullptr;
     sc.sl_rank = p->sl_rank;
     sc.sl_rect = p->sl_rect;
     sc.sup_x = p->sup_x;
@@ -1605,7 +1609,7 @@ std::string forward_key(tsb_pass* p, bool loss, const ChW& chw) {
                           p->fx_cache, p->frame_dev, p->pinned, p->fx_state, p->sl_hist, p->sl_off, p->sl_rank,
                           p->sl_rect};
     add(ptrs, sizeof ptrs);
-    const int sl[] = {p->sl_cap, p->sup_x, p->sup_log, p->nsup};
+    const int sl[] = {p->sl_cap, p->sup_x, p->sup_log, p->nsup, (int)p->sl_lists};
     add(sl, sizeof sl);
     add(&p->fx_state_cap, sizeof p->fx_state_cap);
     add(&S, sizeof S);
@@ -1634,6 +1638,12 @@ int enqueue_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw,
     slot->target = loss ? target : nullptr;
     const bool with_prep = p->prep_deferred;
     if (with_prep) TSB_CUDA(cudaStreamWaitEvent(st, p->scene->params_ev, 0));
+    static const int sl_min = [] {  // TSB_SL_MIN: order length above which the lists are built (tests: 0)
+        const char* e = std::getenv("TSB_SL_MIN");
+        return e ? std::atoi(e) : kSlMinRanks;
+    }();
+    // (fixed for the frame: its backward and debug reads follow it)
+    p->sl_lists = p->force_lists || rank_bound(p) > sl_min;
     int fixed = 0;
     // Graphs: not while stage events are being recorded (profiling runs the same kernels eagerly).
     const bool use_graph = allow_graph && p->ctx->use_graphs && !p->ctx->profiling;
@@ -2462,6 +2472,7 @@ int tsb_pass_debug_set_list_capacity(tsb_pass* p, uint32_t entries) {
     p->sl_cap = 0;
     if ((rc = dev_alloc(&p->sl_rank, (size_t)entries)) || (rc = dev_alloc(&p->sl_rect, (size_t)entries))) return rc;
     p->sl_cap = (int)std::min<uint32_t>(entries, INT32_MAX / 2);
+    p->force_lists = true;
     return TSB_OK;
 }
 

@@ -64,9 +64,16 @@ int launch_sort_depth64(const double* depth64, const uint32_t* touched, uint32_t
 // ---------------------------------------------------------------------------
 // The scan arrays of the raster kernels (ScanK): rank -> Gaussian (runs of equal
 // compressed keys resolved once here, not by every reader) and its tile rect, and the
-// super-tile lists.  A block per chunk of kSlChunk ranks; the chunk's rank count per
-// super-tile goes to hist[s][chunk] (shared-memory counters: a rect meets a few
-// super-tiles).
+// super-tile lists -- a stable counting sort of the (rank, super-tile) pairs by super-
+// tile, with the pairs never materialised:
+//   k_order_ranks  ord / trect; per block (a contiguous range of 256-rank chunks) the
+//                  pair count per super-tile -> hist[s][block]
+//   k_sl_rowscan   a block per super-tile: hist row -> exclusive offsets, row total
+//   k_sl_emit      the rows' bases (a scan of the totals, per block), then each chunk's
+//                  pairs at their stable positions
+// A rect is a product of a column range and a row range of super-tiles, so a warp's
+// coverage of super-tile (sx, sy) is colmask[sx] & rowmask[sy]: sup_x + sup_y ballots
+// per warp instead of one per super-tile.
 __device__ __forceinline__ void super_rect(uint2 tr, int lg, int& sx0, int& sx1, int& sy0, int& sy1) {
     sx0 = (int)(tr.x & 0xffffu) >> lg;
     sx1 = (int)(tr.x >> 16) >> lg;
@@ -82,24 +89,38 @@ __device__ __forceinline__ void block_chunks(int V, int& c0, int& c1) {
     c1 = min(nch, c0 + per);
 }
 
-// The rank -> Gaussian / tile rect arrays and each block's count of (rank, super-tile)
-// pairs per super-tile (shared-memory counters: a rect meets a few super-tiles).  The
-// last block to finish turns the counts into the lists' offsets (super-tile major, blocks
-// in rank order) and sl_off.
+// The warp's column / row coverage masks of its lanes' super rects (wm[0 .. sup_x) columns,
+// wm[sup_x .. sup_x + sup_y) rows).
+__device__ __forceinline__ void warp_masks(bool valid, int sx0, int sx1, int sy0, int sy1, const SuperK& sk,
+                                           uint32_t* wm, int lane) {
+    const int sup_y = sk.nsup / sk.sup_x;
+    for (int sx = 0; sx < sk.sup_x; ++sx) {
+        const unsigned b = __ballot_sync(0xffffffffu, valid && sx0 <= sx && sx <= sx1);
+        if (lane == 0) wm[sx] = b;
+    }
+    for (int sy = 0; sy < sup_y; ++sy) {
+        const unsigned b = __ballot_sync(0xffffffffu, valid && sy0 <= sy && sy <= sy1);
+        if (lane == 0) wm[sk.sup_x + sy] = b;
+    }
+    __syncwarp();
+}
+
 __global__ void __launch_bounds__(kSlChunk) k_order_ranks(const uint32_t* __restrict__ sorted, TieK T,
                                                           const uint2* __restrict__ rect, int ts,
                                                           const int32_t* __restrict__ n_rank, uint32_t* __restrict__ ord,
                                                           uint2* __restrict__ trect, SuperK sk) {
     __shared__ uint32_t cnt[kSlMaxSup];
-    __shared__ bool is_last;
+    __shared__ uint32_t wmask[kSlChunk / 32][2 * kSlMaxSupSide];
     if (block_aborted(T.abort)) return;
-    const int V = *n_rank, tid = threadIdx.x;
+    const int V = *n_rank, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int c0, c1;
     block_chunks(V, c0, c1);
     for (int s = tid; s < sk.nsup; s += kSlChunk) cnt[s] = 0;
     __syncthreads();
+    uint32_t* wm = wmask[warp];
     for (int c = c0; c < c1; ++c) {
         const int r = c * kSlChunk + tid;
+        int sx0 = 1, sx1 = 0, sy0 = 1, sy1 = 0;
         if (r < V) {
             const uint32_t g = sorted_at(sorted, T, r, V);
             const uint2 rc = rect[g];
@@ -108,140 +129,141 @@ __global__ void __launch_bounds__(kSlChunk) k_order_ranks(const uint32_t* __rest
                                         (uint32_t)(y0 / ts) | ((uint32_t)((y1 - 1) / ts) << 16));
             ord[r] = g;
             trect[r] = tr;
-            int sx0, sx1, sy0, sy1;
             super_rect(tr, sk.sup_log, sx0, sx1, sy0, sy1);
-            for (int sy = sy0; sy <= sy1; ++sy)
-                for (int sx = sx0; sx <= sx1; ++sx) atomicAdd(&cnt[sy * sk.sup_x + sx], 1u);
         }
-    }
-    __syncthreads();
-    for (int s = tid; s < sk.nsup; s += kSlChunk) {
-        sk.hist[(size_t)s * sk.hist_stride + blockIdx.x] = cnt[s];
-        if (blockIdx.x == 0)  // the padding columns of the row (the scan reads whole uint4)
-            for (int c = gridDim.x; c % 4; ++c) sk.hist[(size_t)s * sk.hist_stride + c] = 0u;
-    }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) is_last = atomicAdd(sk.ticket, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!is_last) return;
-    __threadfence();
-    // exclusive offsets over (super-tile, block): a thread per super-tile row (its blocks'
-    // counts, contiguous; rows padded to a multiple of 4 columns), the row bases by one
-    // thread (nsup <= 1024 additions)
-    const int G = gridDim.x, nsup = sk.nsup, G4 = (G + 3) / 4;
-    __shared__ uint32_t rowbase[kSlMaxSup + 1];
-    for (int sr = tid; sr < nsup; sr += kSlChunk) {
-        const uint4* row = reinterpret_cast<const uint4*>(sk.hist + (size_t)sr * sk.hist_stride);
-        uint32_t t = 0;
-        for (int q0 = 0; q0 < G4; q0 += 8) {  // 8 loads in flight
-            uint4 v[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = q0 + k < G4 ? __ldcg(row + q0 + k) : make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) t += v[k].x + v[k].y + v[k].z + v[k].w;
-        }
-        rowbase[sr] = t;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        uint32_t acc = 0;
-        for (int sr = 0; sr < nsup; ++sr) {
-            const uint32_t t = rowbase[sr];
-            rowbase[sr] = acc;
-            sk.off[sr] = acc;
-            acc += t;
-        }
-        rowbase[nsup] = acc;
-    }
-    __syncthreads();
-    for (int sr = tid; sr < nsup; sr += kSlChunk) {
-        uint4* row = reinterpret_cast<uint4*>(sk.hist + (size_t)sr * sk.hist_stride);
-        uint32_t off = rowbase[sr];
-        for (int q0 = 0; q0 < G4; q0 += 8) {
-            uint4 v[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = q0 + k < G4 ? __ldcg(row + q0 + k) : make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                if (q0 + k >= G4) break;
-                uint4 o;
-                o.x = off; off += v[k].x;
-                o.y = off; off += v[k].y;
-                o.z = off; off += v[k].z;
-                o.w = off; off += v[k].w;
-                row[q0 + k] = o;
+        if (sk.nsup > 0 && __any_sync(0xffffffffu, r < V)) {
+            warp_masks(r < V, sx0, sx1, sy0, sy1, sk, wm, lane);
+            for (int s = lane; s < sk.nsup; s += 32) {
+                const int sy = s / sk.sup_x, sx = s - sy * sk.sup_x;
+                const uint32_t k = __popc(wm[sx] & wm[sk.sup_x + sy]);
+                if (k) atomicAdd(&cnt[s], k);
             }
+            __syncwarp();
         }
     }
-    if (tid == 0) {
-        const uint32_t total = rowbase[nsup];
-        sk.off[nsup] = total;
+    __syncthreads();
+    for (int s = tid; s < sk.nsup; s += kSlChunk) sk.hist[(size_t)s * sk.hist_stride + blockIdx.x] = cnt[s];
+}
+
+// Row s of the histogram (one column per k_order_ranks block) -> exclusive offsets within
+// the row; row_total[s] = its sum.
+__global__ void __launch_bounds__(256) k_sl_rowscan(SuperK sk, int G, const int32_t* __restrict__ abort) {
+    __shared__ uint32_t part[256];
+    if (block_aborted(abort)) return;
+    uint32_t* row = sk.hist + (size_t)blockIdx.x * sk.hist_stride;
+    const int tid = threadIdx.x, per = (G + 255) / 256, c0 = min(G, tid * per), c1 = min(G, c0 + per);
+    uint32_t v[(kSlMaxBlocks + 255) / 256];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < (kSlMaxBlocks + 255) / 256; ++k) {
+        v[k] = c0 + k < c1 ? row[c0 + k] : 0u;
+        sum += v[k];
+    }
+    part[tid] = sum;
+    __syncthreads();
+    for (int d = 1; d < 256; d <<= 1) {
+        const uint32_t u = tid >= d ? part[tid - d] : 0u;
+        __syncthreads();
+        part[tid] += u;
+        __syncthreads();
+    }
+    uint32_t off = part[tid] - sum;
+#pragma unroll
+    for (int k = 0; k < (kSlMaxBlocks + 255) / 256; ++k) {
+        if (c0 + k < c1) row[c0 + k] = off;
+        off += v[k];
+    }
+    if (tid == 255) sk.row_total[blockIdx.x] = part[255];
+}
+
+__global__ void __launch_bounds__(kSlChunk) k_sl_emit(const int32_t* __restrict__ n_rank,
+                                                      const uint2* __restrict__ trect, SuperK sk,
+                                                      int32_t* __restrict__ abort) {
+    __shared__ uint32_t base[kSlMaxSup];
+    __shared__ uint16_t wpre[kSlChunk / 32][kSlMaxSup];  // warps before w: their pairs per super-tile
+    __shared__ uint32_t wmask[kSlChunk / 32][2 * kSlMaxSupSide];
+    __shared__ uint32_t part[kSlChunk];
+    if (block_aborted(abort)) return;
+    const int V = *n_rank, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t below = (1u << lane) - 1u;
+    // the rows' bases: exclusive scan of the row totals (nsup <= 1024: 4 per thread)
+    constexpr int kPer = kSlMaxSup / kSlChunk;
+    uint32_t t[kPer], sum = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const int s = tid * kPer + k;
+        t[k] = s < sk.nsup ? sk.row_total[s] : 0u;
+        sum += t[k];
+    }
+    part[tid] = sum;
+    __syncthreads();
+    for (int d = 1; d < kSlChunk; d <<= 1) {
+        const uint32_t u = tid >= d ? part[tid - d] : 0u;
+        __syncthreads();
+        part[tid] += u;
+        __syncthreads();
+    }
+    const uint32_t total = part[kSlChunk - 1];
+    {
+        uint32_t off = part[tid] - sum;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int s = tid * kPer + k;
+            if (s < sk.nsup) {
+                base[s] = off + sk.hist[(size_t)s * sk.hist_stride + blockIdx.x];
+                if (blockIdx.x == 0) sk.off[s] = off;
+            }
+            off += t[k];
+        }
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        sk.off[sk.nsup] = total;
         *sk.total = (int32_t)min(total, 0x7fffffffu);
-        if (total > (uint32_t)sk.cap) atomicOr(T.abort, 1);  // the lists need more storage: redo
-        *sk.ticket = 0u;
+        if (total > (uint32_t)sk.cap) atomicOr(abort, 1);  // the lists need more storage: redo
         if (sk.work) {
             atomicAdd(&sk.work[2], (unsigned long long)V);
             atomicAdd(&sk.work[3], (unsigned long long)total);
         }
     }
-}
-
-// Each block's ranks into the lists of the super-tiles their rects meet, in rank order:
-// per super-tile, a warp ballot ranks a chunk's covering lanes; the warp counts of a first
-// sweep give the warps' bases, and the block's running base per super-tile starts at its
-// scanned offset.
-__global__ void __launch_bounds__(kSlChunk) k_sl_emit(const int32_t* __restrict__ n_rank,
-                                                      const uint2* __restrict__ trect, SuperK sk,
-                                                      const int32_t* __restrict__ abort) {
-    __shared__ uint16_t wc[kSlChunk / 32][kSlMaxSup];
-    __shared__ uint32_t base[kSlMaxSup];
-    if (block_aborted(abort)) return;
-    const int V = *n_rank;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t below = (1u << lane) - 1u;
+    if (total > (uint32_t)sk.cap) return;  // (block-uniform)
     int c0, c1;
     block_chunks(V, c0, c1);
-    if (c0 >= c1) return;
-    for (int s = threadIdx.x; s < sk.nsup; s += kSlChunk) base[s] = sk.hist[(size_t)s * sk.hist_stride + blockIdx.x];
-    const int nsy = (sk.nsup + sk.sup_x - 1) / sk.sup_x;
+    uint32_t* wm = wmask[warp];
     for (int c = c0; c < c1; ++c) {
-        const int r = c * kSlChunk + threadIdx.x;
+        const int r = c * kSlChunk + tid;
         int sx0 = 1, sx1 = 0, sy0 = 1, sy1 = 0;
         uint2 tr = make_uint2(0u, 0u);
         if (r < V) {
             tr = trect[r];
             super_rect(tr, sk.sup_log, sx0, sx1, sy0, sy1);
         }
-        for (int pass = 0; pass < 2; ++pass) {
-            for (int sy = 0; sy < nsy; ++sy) {
-                const bool row = sy0 <= sy && sy <= sy1;
-                if (!__any_sync(0xffffffffu, row)) {
-                    if (pass == 0)
-                        for (int sx = lane; sx < sk.sup_x; sx += 32) wc[warp][sy * sk.sup_x + sx] = 0;
-                    continue;
-                }
-                for (int sx = 0; sx < sk.sup_x; ++sx) {
-                    const int s = sy * sk.sup_x + sx;
-                    const bool cov = row && sx0 <= sx && sx <= sx1;
-                    const unsigned b = __ballot_sync(0xffffffffu, cov);
-                    if (pass == 0) {
-                        if (lane == 0) wc[warp][s] = (uint16_t)__popc(b);
-                    } else if (cov) {
-                        uint32_t pos = base[s] + __popc(b & below);
-                        for (int w = 0; w < warp; ++w) pos += wc[w][s];
-                        sk.rank[pos] = (uint32_t)r;
-                        sk.rect[pos] = tr;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-        for (int s = threadIdx.x; s < sk.nsup; s += kSlChunk) {
-            uint32_t t = 0;
+        warp_masks(r < V, sx0, sx1, sy0, sy1, sk, wm, lane);
+        __syncthreads();
+        // per super-tile: the warps' exclusive prefix of their pair counts, the chunk total
+        for (int s = tid; s < sk.nsup; s += kSlChunk) {
+            const int sy = s / sk.sup_x, sx = s - sy * sk.sup_x;
+            uint32_t run = 0;
 #pragma unroll
-            for (int w = 0; w < kSlChunk / 32; ++w) t += wc[w][s];
-            base[s] += t;
+            for (int w = 0; w < kSlChunk / 32; ++w) {
+                wpre[w][s] = (uint16_t)run;
+                run += __popc(wmask[w][sx] & wmask[w][sk.sup_x + sy]);
+            }
+        }
+        __syncthreads();
+        for (int sy = sy0; sy <= sy1; ++sy) {
+            const uint32_t rm = wm[sk.sup_x + sy];
+            for (int sx = sx0; sx <= sx1; ++sx) {
+                const int s = sy * sk.sup_x + sx;
+                const uint32_t pos = base[s] + wpre[warp][s] + __popc(wm[sx] & rm & below);
+                sk.rank[pos] = (uint32_t)r;
+                sk.rect[pos] = tr;
+            }
+        }
+        __syncthreads();
+        for (int s = tid; s < sk.nsup; s += kSlChunk) {
+            const int sy = s / sk.sup_x, sx = s - sy * sk.sup_x;
+            base[s] += wpre[kSlChunk / 32 - 1][s] +
+                       __popc(wmask[kSlChunk / 32 - 1][sx] & wmask[kSlChunk / 32 - 1][sk.sup_x + sy]);
         }
         __syncthreads();
     }
@@ -251,12 +273,11 @@ int launch_order_ranks(const uint32_t* sorted, const TieK& T, const uint2* rect,
                        int n, uint32_t* ord, uint2* trect, const SuperK& sk, cudaStream_t st) {
     if (n <= 0) return 0;
     const int grid = std::min(sk.hist_stride, (n + kSlChunk - 1) / kSlChunk);
-    // the ticket starts at 0 even when an earlier launch ended early (an abort raised while
-    // its blocks ran leaves it partly counted)
-    cudaMemsetAsync(sk.ticket, 0, sizeof(uint32_t), st);
     k_order_ranks<<<grid, kSlChunk, 0, st>>>(sorted, T, rect, ts, n_rank, ord, trect, sk);
+    if (sk.nsup == 0) return 1;  // a short order: no lists
+    k_sl_rowscan<<<sk.nsup, 256, 0, st>>>(sk, grid, T.abort);
     k_sl_emit<<<grid, kSlChunk, 0, st>>>(n_rank, trect, sk, T.abort);
-    return 2;
+    return 3;
 }
 
 // Deterministic backward: det_off[r] = sum over ranks r' < r of (rect area in tiles) x

@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_fwd(RecK rec, SceneK S, 
         int total;
         const int pos = scan_compact(cov, wsum[pass & 1], total);  // (its barrier follows the last pass's reads)
         if (pos >= 0) {
-            const uint32_t r = sc.ord[seg.rank[rr]];
+            const uint32_t r = sc.ord[seg_rank(seg, rr)];
             sg[pos] = r;
             sA[pos] = stage_A(rec.A[r], m.ox, m.oy);
             sB[pos] = rec.B[r];
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_bwd(RecK rec, OptK O, in
         const int e_lo = e_top - total;
         if (pos >= 0) {
             const int j = total - 1 - pos;  // ascending
-            const uint32_t r = sc.ord[seg.rank[rr]];
+            const uint32_t r = sc.ord[seg_rank(seg, rr)];
             srank[j] = r;
             sA[j] = stage_A(rec.A[r], m.ox, m.oy);
             sB[j] = rec.B[r];

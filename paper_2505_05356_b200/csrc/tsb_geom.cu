@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(128) k_fixup_mark(OptK O, FixupK fx, PixK px, 
             const bool cov = r < V && tile_covers(seg.rect[r], tx, ty);
             const unsigned m = __ballot_sync(0xffffffffu, cov);
             if (cov && e + __popc(m & ((1u << lane) - 1u)) < limit) {
-                const uint32_t g = fx.sc.ord[seg.rank[r]];
+                const uint32_t g = fx.sc.ord[seg_rank(seg, r)];
                 if (atomicExch(&fx.stamp[g], stamp) != stamp) {
                     const int slot = atomicAdd(fx.work_n, 1);
                     fx.work[slot] = (int)g;
@@ -498,7 +498,7 @@ __device__ __forceinline__ void queue_step(const ScanK& sc, const ScanSeg& seg, 
         const bool cov = r >= r_min && r < V && tile_covers(seg.rect[r], tx, ty);
         const unsigned m = __ballot_sync(0xffffffffu, cov);
         if (cov) {
-            const uint32_t rk = seg.rank[r];
+            const uint32_t rk = seg_rank(seg, r);
             qg[qn + __popc(m & below)] = (int)sc.ord[rk];
             qr[qn + __popc(m & below)] = pos_out ? r : (int)rk;
         }

@@ -115,7 +115,8 @@ struct ScanK {
     int nsub2;                 // raster blocks per tile
     // Super-tile lists: the ranks whose tile rect meets each super-tile (2^sup_log x 2^sup_log
     // tiles), in rank order, with their rects.  A block scans its super-tile's list instead of
-    // the whole order; scan positions (blk_term.x, FixState::r_end) index that list.
+    // the whole order; scan positions (blk_term.x, FixState::r_end) index that list.  Null
+    // sl_off (a short order, kSlMinRanks): blocks scan the order itself (positions = ranks).
     const uint32_t* sl_off;    // [nsup + 1]
     const uint32_t* sl_rank;   // [sl_cap]
     const uint2* sl_rect;      // [sl_cap]
@@ -128,22 +129,27 @@ struct ScanSeg {
     int n;
 };
 __device__ __forceinline__ ScanSeg scan_seg(const ScanK& sc, int tx, int ty) {
+    if (!sc.sl_off) return ScanSeg{nullptr, sc.trect, *sc.n_rank};  // short order: the order itself
     const int s = (ty >> sc.sup_log) * sc.sup_x + (tx >> sc.sup_log);
     const uint32_t a = sc.sl_off[s], b = sc.sl_off[s + 1];
     return ScanSeg{sc.sl_rank + a, sc.sl_rect + a, (int)(b - a)};
 }
+// The rank at scan position p.
+__device__ __forceinline__ uint32_t seg_rank(const ScanSeg& sg, int p) { return sg.rank ? sg.rank[p] : (uint32_t)p; }
 // Build arguments of the super-tile lists (k_order_ranks counts + scan, k_sl_emit).
-constexpr int kSlChunk = 256;     // ranks per counting chunk
+constexpr int kSlChunk = 256;     // ranks per chunk
+constexpr int kSlMinRanks = 32768; // orders up to this long are scanned directly (no lists)
 constexpr int kSlMaxSup = 1024;   // super-tiles per frame (the super-tile grows past this)
-constexpr int kSlMaxBlocks = 148 * 2;  // blocks building the lists (contiguous rank ranges each; % 4 == 0)
+constexpr int kSlMaxSupSide = 64; // super-tiles per row / column (likewise)
+constexpr int kSlMaxBlocks = 148 * 8;  // blocks building the lists (contiguous rank ranges each)
 struct SuperK {
-    uint32_t* hist;    // [nsup][hist_stride] per-block counts -> exclusive offsets
-    int hist_stride;   // histogram columns = the build grid's upper bound (<= kSlMaxBlocks)
-    uint32_t* ticket;  // blocks of k_order_ranks done (the last scans; reset to 0 by it)
-    uint32_t* off;     // ScanK::sl_off
-    uint32_t* rank;    // ScanK::sl_rank
-    uint2* rect;       // ScanK::sl_rect
-    int cap;           // entries the lists can hold; more: abort bit 1, the total in *total
+    uint32_t* hist;      // [nsup][hist_stride] per-block pair counts -> offsets within the row
+    int hist_stride;     // histogram columns = the build grid's upper bound (kSlMaxBlocks)
+    uint32_t* row_total; // [nsup] pairs per super-tile
+    uint32_t* off;       // ScanK::sl_off
+    uint32_t* rank;      // ScanK::sl_rank
+    uint2* rect;         // ScanK::sl_rect
+    int cap;             // entries the lists can hold; more: abort bit 1, the total in *total
     int32_t* total;
     int sup_x, sup_log, nsup;
     unsigned long long* work;  // profiling: [2] += ranks, [3] += list entries (null: not counted)
@@ -293,7 +299,7 @@ void launch_materialize_order(const uint32_t* sorted, const TieK& T, const int32
 int launch_sort_depth64(const double* depth64, const uint32_t* touched, uint32_t* keys_a, uint32_t* keys_b,
                         uint32_t* vals_a, uint32_t* vals_b, int n, uint32_t* scratch, cudaStream_t st);
 // ord / trect of ranks r < *n_rank (the raster kernels' scan arrays, ScanK)
-// + the super-tile lists (2 kernels; returns the launch count); n: upper bound of *n_rank
+// + the super-tile lists (3 kernels; returns the launch count); n: upper bound of *n_rank
 int launch_order_ranks(const uint32_t* sorted, const TieK& T, const uint2* rect, int ts, const int32_t* n_rank,
                        int n, uint32_t* ord, uint2* trect, const SuperK& sk, cudaStream_t st);
 // deterministic backward: slot offsets of the ranks (device scan; writes det_off[0..V]) and

@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK s
             int total;
             const int pos = scan_compact(cov, sm.wsum[pass & 1], total);
             if (pos >= 0) {
-                const uint32_t rr = seg.rank[p];
+                const uint32_t rr = seg_rank(seg, p);
                 const uint32_t g = sc.ord[rr];
                 stage_entry<NF>(sm, rec, g, cnt + pos, ox, oy, outside);
                 const int e = ebase + cnt + pos;  // list index: its rank is recorded for the backward
@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, ScanK s
             const int asc = total - 1 - pos;
             if (pos >= 0 && asc < keep_hi) {
                 const int slot = kBatchCap - cnt - keep_hi + asc;
-                const uint32_t rr = seg.rank[p];
+                const uint32_t rr = seg_rank(seg, p);
                 const uint32_t g = sc.ord[rr];
                 sm.grank[slot] = g;
                 sm.rrank[slot] = (uint32_t)rr;

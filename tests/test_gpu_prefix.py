@@ -59,9 +59,24 @@ def test_prefix_frame_equals_full_order_frame(tsb, ctx):
         assert rel_err(np.asarray(ga[k]), np.asarray(gb[k]), 1e-3) < 1e-4, k
 
 
-@pytest.mark.skipif("TSB_PREFIX" in os.environ, reason="already inside the forced-prefix run")
+NESTED = "TSB_PREFIX" in os.environ or "TSB_SL_MIN" in os.environ
+
+
+@pytest.mark.skipif(NESTED, reason="already inside a re-run of the suite")
 def test_gpu_suite_with_forced_prefix():
     env = dict(os.environ, TSB_PREFIX="256")
+    r = subprocess.run([sys.executable, "-m", "pytest", str(ROOT / "tests"), "-m", "gpu", "-x", "-q",
+                        "-p", "no:cacheprovider"], cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+
+
+@pytest.mark.skipif(NESTED, reason="already inside a re-run of the suite")
+def test_gpu_suite_with_super_tile_lists():
+    """Orders up to kSlMinRanks (32K) ranks are scanned directly; longer ones (c4) through
+    the super-tile lists.  Re-run the whole suite with the lists built for every frame, so
+    every parity case also covers the list path (scan positions in the lists, the list
+    build, the fix-up / backward / colour walks over them)."""
+    env = dict(os.environ, TSB_SL_MIN="0")
     r = subprocess.run([sys.executable, "-m", "pytest", str(ROOT / "tests"), "-m", "gpu", "-x", "-q",
                         "-p", "no:cacheprovider"], cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
@@ -90,7 +105,7 @@ def test_lean_visibility_equals_exact(tsb, ctx, name, cam):
         assert np.array_equal(res[False][1][k], res[True][1][k], equal_nan=True), k
 
 
-@pytest.mark.skipif("TSB_PREFIX" in os.environ, reason="sets its own cap")
+@pytest.mark.skipif(NESTED, reason="sets its own cap")
 @pytest.mark.parametrize("det", [0, 1])
 def test_abort_raised_mid_launch_is_block_uniform(det):
     """Regression: the raster raises the abort word (bit 8, prefix too short) while other
