@@ -2667,7 +2667,7 @@ struct tsb_deform {
 };
 
 namespace {
-constexpr int kDeformMaxSlices = 296;
+constexpr int kDeformMaxSlices = 148;  // one CTA per SM (the dW kernel holds ~192 KB of shared memory)
 
 int deform_slot_alloc(tsb_deform* d, tsb_deform::Slot& s, int64_t n) {
     if (n <= s.cap) return TSB_OK;

@@ -9,13 +9,18 @@
 // are split 3xTF32 (a = a_hi + a_lo, both tf32; D += a_hi b_hi + a_hi b_lo +
 // a_lo b_hi), which keeps ~fp32 accuracy at a third of the tf32 tensor rate.
 // Operands are read through generic (m, k) / (n, k) strides, so the same kernel
-// serves the forward (X W^T), the input gradient (delta W) and the weight
-// gradient (delta^T H, split over row slices) without transposes in memory.
-// The epilogue (TMEM -> registers) fuses bias, ReLU and the ReLU-gate mask.
+// serves the input gradient (delta W) and the weight gradient (delta^T H, split over
+// row slices) without transposes in memory: raw fp32 chunks stream into a ring of
+// shared-memory stages several chunks ahead (cp.async, or one TMA bulk copy per operand
+// when a chunk is a contiguous run of full-width rows), every thread splits one chunk
+// into the hi / lo tiles (transposed operands are transposed on that read), and a
+// constant B operand is split once per CTA and kept resident.  The epilogue (TMEM ->
+// registers) fuses bias, ReLU and the ReLU-gate mask.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "tsb_internal.h"
 
@@ -23,7 +28,7 @@ namespace tsb {
 
 namespace {
 
-constexpr int kGemmThreads = 256;  // 8 warps stage; thread 0 issues MMAs; warps read TMEM by lane quadrant
+constexpr int kGemmThreads = 512;  // 16 warps stage; thread 0 issues MMAs; warps read TMEM by lane quadrant
 constexpr int kGemmM = 128;        // rows per tile (TMEM lanes)
 constexpr int kGemmKc = 32;        // K elements staged per round (8 core-matrix columns of 4 tf32)
 constexpr uint32_t kCoreBytes = 128;                       // 8 rows x 16 B
@@ -79,15 +84,13 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 __device__ __forceinline__ void tc_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
-// 3xTF32 split: hi = tf32(a) (round to nearest), lo = tf32(a - hi).  The tensor core
-// reads the fp32 bit patterns and ignores the 13 low mantissa bits.
+// 3xTF32 split: hi = a rounded (half away from zero) to tf32 -- its 13 low mantissa bits
+// zero, by integer add + mask (finite inputs; cvt.rna.tf32 is an emulated sequence on
+// sm_100), lo = a - hi (exact in fp32).  The tensor core reads the fp32 bit patterns and
+// ignores the 13 low mantissa bits, so lo enters truncated to tf32: |error| <= 2^-21 |a|.
 __device__ __forceinline__ void split_tf32(float a, float& hi, float& lo) {
-    uint32_t h;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(a));
-    hi = __uint_as_float(h);
-    uint32_t l;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(a - hi));
-    lo = __uint_as_float(l);
+    hi = __uint_as_float((__float_as_uint(a) + 0x1000u) & 0xffffe000u);
+    lo = a - hi;
 }
 
 // Byte offset of element (row r, k) in a K-major no-swizzle tile of the K chunk.
@@ -182,22 +185,176 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
 // kFlushChunks K chunks and add it into round-to-nearest fp32 registers.
 constexpr int kFlushChunks = 8;  // 256 rows
 
-constexpr int kGemmStages = 2;  // shared-memory ring: staging chunk c+1 overlaps the MMAs of chunk c
+constexpr int kGemmMaxSmem = 227 * 1024 - 2048;  // dynamic (the static barriers / TMEM slot take the rest)
 
-__host__ __device__ constexpr size_t gemm_stage_bytes(int nt) { return (size_t)(kGemmM + nt) * kGemmKc * 4 * 2; }
+// Operand chunks travel global -> shared memory with cp.async (16 B, no registers held)
+// into a ring of raw fp32 stages several chunks ahead of the tensor core; every thread
+// then splits one raw chunk into the hi / lo tf32 tiles the MMAs read.  Raw layouts:
+// K-contiguous operands [row][36 floats] (the 4-float pad keeps the split's 16-byte reads
+// conflict-free), row-contiguous (transposed) operands [k][R] (the split reads four k of
+// one row with scalar loads on distinct banks and stores one 16-byte core-matrix row).
+constexpr int kRawRowF = kGemmKc + 4;
+// raw chunk bytes: layout T ([k][R], row-contiguous operands) or N ([row][36])
+__host__ __device__ constexpr size_t raw_bytes(int r, bool t) { return t ? (size_t)r * kGemmKc * 4 : (size_t)r * kRawRowF * 4; }
+__host__ __device__ constexpr size_t split_bytes(int r) { return (size_t)r * kGemmKc * 4 * 2; }  // hi + lo
+
+// Shared-memory plan of one launch: B resident (every K chunk of B split once per CTA -- B
+// does not depend on the row tile) when it fits and the CTA has more than one tile.
+struct GemmPlan {
+    int b_res;
+    int raw;  // raw stages (chunks in flight: raw - 1), as many as fit (2 .. kMaxRaw)
+    size_t bytes;
+};
+constexpr int kMaxRaw = 6;  // (cp_async_wait_n covers up to 4 pending groups)
+// (one split buffer: measured faster than two with a stage fewer in flight)
+inline size_t gemm_bytes(int nt, int nck, bool b_res, bool ta, bool tb, int raw) {
+    if (b_res) return (size_t)nck * split_bytes(nt) + raw * raw_bytes(kGemmM, ta) + split_bytes(kGemmM);
+    return raw * (raw_bytes(kGemmM, ta) + raw_bytes(nt, tb)) + split_bytes(kGemmM) + split_bytes(nt);
+}
+inline GemmPlan gemm_plan(int nt, int nck, bool many_tiles, bool ta, bool tb) {
+    GemmPlan p{};
+    p.b_res = many_tiles && nck > 0 && gemm_bytes(nt, nck, true, ta, tb, 3) <= (size_t)kGemmMaxSmem;
+    p.raw = 2;
+    while (p.raw < kMaxRaw && gemm_bytes(nt, nck, p.b_res, ta, tb, p.raw + 1) <= (size_t)kGemmMaxSmem) ++p.raw;
+    p.bytes = gemm_bytes(nt, nck, p.b_res, ta, tb, p.raw);
+    return p;
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void cp_async_wait_n(int n) {  // n: block-uniform
+    switch (n) {
+        case 0: cp_async_wait<0>(); break;
+        case 1: cp_async_wait<1>(); break;
+        case 2: cp_async_wait<2>(); break;
+        case 3: cp_async_wait<3>(); break;
+        default: cp_async_wait<4>(); break;
+    }
+}
+
+// 1D bulk copy (TMA engine) global -> shared, completion counted on an mbarrier.
+__device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes) : "memory");
+}
+
+// Mode 2 also takes a partial row tile when every 16-byte run of a k row stays inside the
+// row stride (the runs past nrows are read -- they only feed output rows / columns the
+// epilogue discards -- or zero-filled).
+__device__ __forceinline__ int op_mode(const float* P, int64_t sr, int64_t sk, int r0, int nrows, int k0, int kend,
+                                       int R) {
+    const bool aligned = ((uintptr_t)P & 15) == 0;
+    if (sk == 1 && (sr & 3) == 0 && aligned && k0 + kGemmKc <= kend) return 1;
+    if (sr == 1 && (sk & 3) == 0 && aligned && (r0 & 3) == 0 && (r0 + R <= nrows || (int64_t)((nrows + 3) & ~3) <= sk))
+        return 2;
+    return 0;
+}
+
+// Issue the raw copy of rows [r0, r0 + R) x k [k0, k0 + 32) of X(r, k) = P[r sr + k sk]
+// (zeros outside rows < nrows, k < kend); mode 0 copies synchronously.
+template <int R>
+__device__ __forceinline__ void raw_issue(const float* __restrict__ P, int64_t sr, int64_t sk, int r0, int nrows,
+                                          int k0, int kend, char* raw) {
+    const int mode = op_mode(P, sr, sk, r0, nrows, k0, kend, R);
+    const bool lay_t = sr == 1;  // the raw layout (T: [k][R]) follows the operand, not the chunk
+    const uint32_t base = smem_u32(raw);
+    constexpr int kIt = (R * 8 + kGemmThreads - 1) / kGemmThreads;
+    if (mode == 1 && !lay_t) {
+#pragma unroll
+        for (int it = 0; it < kIt; ++it) {
+            const int idx = threadIdx.x + it * kGemmThreads;
+            if (R * 8 % kGemmThreads && idx >= R * 8) break;
+            const int r = idx >> 3, q = idx & 7, gr = r0 + r;
+            const bool ok = gr < nrows;
+            cp_async16(base + (uint32_t)(r * kRawRowF * 4 + q * 16), ok ? P + (int64_t)gr * sr + k0 + 4 * q : P,
+                       ok ? 16u : 0u);
+        }
+    } else if (mode == 2) {  // (implies layout T)
+        constexpr int rq_n = R / 4;
+#pragma unroll
+        for (int it = 0; it < kIt; ++it) {
+            const int idx = threadIdx.x + it * kGemmThreads;
+            if (R * 8 % kGemmThreads && idx >= R * 8) break;
+            const int k = idx / rq_n, rq = idx - k * rq_n, gk = k0 + k;
+            const bool ok = gk < kend && r0 + 4 * rq < nrows;
+            cp_async16(base + (uint32_t)(k * R * 4 + rq * 16), ok ? P + (r0 + 4 * rq) + (int64_t)gk * sk : P,
+                       ok ? 16u : 0u);
+        }
+    } else {
+        float* rf = reinterpret_cast<float*>(raw);
+        for (int idx = threadIdx.x; idx < R * kGemmKc; idx += kGemmThreads) {
+            const int r = idx / kGemmKc, k = idx - r * kGemmKc, gr = r0 + r, gk = k0 + k;
+            rf[lay_t ? k * R + r : r * kRawRowF + k] =
+                (gr < nrows && gk < kend) ? P[(int64_t)gr * sr + (int64_t)gk * sk] : 0.f;
+        }
+    }
+}
+
+// Split a raw chunk into the K-major no-swizzle hi / lo tiles (core matrices).
+template <int R>
+__device__ __forceinline__ void raw_split(bool lay_t, const char* raw, char* hi, char* lo, int kvalid = kGemmKc) {
+    constexpr int kIt = (R * 8 + kGemmThreads - 1) / kGemmThreads;
+    if (!lay_t) {
+#pragma unroll
+        for (int it = 0; it < kIt; ++it) {
+            const int idx = threadIdx.x + it * kGemmThreads;
+            if (R * 8 % kGemmThreads && idx >= R * 8) break;
+            const int r8 = idx & 7, q = (idx >> 3) & 7, rg = idx >> 6, r = rg * 8 + r8;
+            const float4 v = *reinterpret_cast<const float4*>(raw + r * kRawRowF * 4 + q * 16);
+            float4 h, l;
+            split4(v, h, l);
+            const uint32_t o = core_off(r, 4 * q);
+            *reinterpret_cast<float4*>(hi + o) = h;
+            *reinterpret_cast<float4*>(lo + o) = l;
+        }
+    } else {
+        constexpr int rq_n = R / 4;
+        const float* rf = reinterpret_cast<const float*>(raw);
+#pragma unroll
+        for (int it = 0; it < kIt; ++it) {
+            const int idx = threadIdx.x + it * kGemmThreads;
+            if (R * 8 % kGemmThreads && idx >= R * 8) break;
+            const int kq = idx & 3, rq = (idx >> 2) % rq_n, kb = (idx >> 2) / rq_n, r = 4 * rq + kq;
+            float4 v = make_float4(rf[(4 * kb + 0) * R + r], rf[(4 * kb + 1) * R + r], rf[(4 * kb + 2) * R + r],
+                                   rf[(4 * kb + 3) * R + r]);
+            if (4 * kb + 4 > kvalid) {  // rows past a bulk-copied partial chunk hold stale data
+                if (4 * kb + 0 >= kvalid) v.x = 0.f;
+                if (4 * kb + 1 >= kvalid) v.y = 0.f;
+                if (4 * kb + 2 >= kvalid) v.z = 0.f;
+                if (4 * kb + 3 >= kvalid) v.w = 0.f;
+            }
+            float4 h, l;
+            split4(v, h, l);
+            const uint32_t o = core_off(r, 4 * kb);
+            *reinterpret_cast<float4*>(hi + o) = h;
+            *reinterpret_cast<float4*>(lo + o) = l;
+        }
+    }
+}
 
 // D[m, n] = sum_k A(m, k) B(n, k) over this CTA's K slice for 128-row tiles (CTAs
-// stride over the tiles), n < N (N <= NT).  Every thread stages; thread 0 issues the
-// 3xTF32 MMAs of a chunk and commits them to that stage's mbarrier, so the threads
-// stage the next chunk while the tensor core works.  Epilogue per tile: + bias[n],
+// stride over the tiles), n < N (N <= NT).  The chunks of all the CTA's tiles form one
+// sequence; chunk q + kRaw - 1 is in flight (cp.async) while chunk q is split and
+// multiplied.  Thread 0 issues the 3xTF32 MMAs of a chunk and commits them to mb_mma; the
+// split of the next chunk waits for them (one split buffer).  Epilogue per tile: + bias[n],
 // ReLU, * (mask(m, n) > 0), store to C + slice * slice_stride (split-K partials are
 // reduced by k_reduce_slices).
-template <int NT, bool FLUSH>
-__global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g) {
+template <int NT, bool FLUSH, bool BRES>
+__global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int kRaw) {
     extern __shared__ __align__(1024) char smem[];
-    __shared__ __align__(8) uint64_t mb_stage[kGemmStages];
+    __shared__ __align__(8) uint64_t mb_mma[2];
     __shared__ __align__(8) uint64_t mb_tile;
+    __shared__ __align__(8) uint64_t mb_raw[kMaxRaw];  // bulk mode: raw stage filled
     __shared__ uint32_t tmem_base_s;
+    constexpr int kSplit = 1;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr int kTmemCols = NT <= 32 ? 32 : (NT <= 64 ? 64 : (NT <= 128 ? 128 : 256));
     constexpr uint32_t kABytes = kGemmM * kGemmKc * 4, kBBytes = NT * kGemmKc * 4;
@@ -208,52 +365,136 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g) {
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     if (tid == 0) {
-        for (int i = 0; i < kGemmStages; ++i) mbar_init(&mb_stage[i], 1);
+        mbar_init(&mb_mma[0], 1);
+        mbar_init(&mb_mma[1], 1);
         mbar_init(&mb_tile, 1);
+        for (int i = 0; i < kMaxRaw; ++i) mbar_init(&mb_raw[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
     const uint32_t tmem = tmem_base_s;
-    // TMEM lane quadrant of this warp (warps w and w + 4 share it and split the columns)
+    // TMEM lane quadrant of this warp (warps w, w + 4, ... share it and split the columns
+    // into groups of kColHalf >= 16)
     const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-    constexpr int kColHalf = NT >= 32 ? NT / 2 : NT;
-    const int col0 = NT >= 32 ? (warp >> 2) * kColHalf : 0;
-    const bool epi_warp = NT >= 32 || warp < 4;
+    constexpr int kEpiGroups = NT >= 64 ? 4 : (NT == 32 ? 2 : 1);
+    constexpr int kColHalf = NT / kEpiGroups;
+    const int col0 = ((warp >> 2) % kEpiGroups) * kColHalf;
+    const bool epi_warp = (warp >> 2) < kEpiGroups;
 
     const int slice = blockIdx.y;
     const int kbeg = slice * g.k_per_slice;
     const int kend = min(g.K, kbeg + g.k_per_slice);
     const int ntiles = (g.M + kGemmM - 1) / kGemmM;
+    const int nck = kend > kbeg ? (kend - kbeg + kGemmKc - 1) / kGemmKc : 0;
+    const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     constexpr uint32_t idesc = idesc_tf32(kGemmM, NT);
     float* C = g.C + (int64_t)slice * g.slice_stride;
-    uint32_t c = 0;        // chunks issued by this CTA (stage ring position)
-    uint32_t tphase = 0;   // mb_tile completions waited for
+    // shared memory: [B split chunks (resident)] [split buffers: A hi, A lo (, B hi, B lo)] [raw stages: A (, B)]
+    const bool ta = g.a_m == 1, tb = g.b_n == 1;  // raw layouts
+    char* bres = smem;
+    char* split0 = smem + (BRES ? (size_t)nck * 2 * kBBytes : 0);
+    constexpr size_t kSplitBuf = BRES ? 2 * kABytes : 2 * kABytes + 2 * kBBytes;
+    char* raw0 = split0 + kSplit * kSplitBuf;
+    const size_t raw_sa = raw_bytes(kGemmM, ta), raw_stage = raw_sa + (BRES ? 0 : raw_bytes(NT, tb));
+    auto raw_a = [&](int st) { return raw0 + (size_t)st * raw_stage; };
+    auto raw_b = [&](int st) { return raw0 + (size_t)st * raw_stage + raw_sa; };
+    if (BRES) {  // B split once: through raw stage 0
+        for (int ch = 0; ch < nck; ++ch) {
+            const int k0 = kbeg + ch * kGemmKc;
+            raw_issue<NT>(g.B, g.b_n, g.b_k, 0, g.N, k0, kend, raw_a(0));  // (raw A stage 0 as scratch)
+            cp_async_commit();
+            cp_async_wait<0>();
+            __syncthreads();
+            char* bh = bres + (size_t)ch * 2 * kBBytes;
+            raw_split<NT>(tb, raw_a(0), bh, bh + kBBytes);
+            __syncthreads();
+        }
+    }
+    const int total = my_tiles * nck;
+    // Bulk mode (both operands row-contiguous and full-width: a chunk of each is one
+    // contiguous run of 32 rows): one TMA bulk copy per operand per chunk, completion on the
+    // stage's mbarrier, the whole ring in flight.  Otherwise per-thread cp.async.
+    const bool bulk = !BRES && ta && tb && g.a_k == kGemmM && g.M == kGemmM && g.b_k == NT && g.N == NT &&
+                      (((uintptr_t)g.A | (uintptr_t)g.B) & 15) == 0;
+    // issue cursor: the next chunk to load (tile row m0, chunk ch, raw stage)
+    int is_q = 0, is_m0 = (int)blockIdx.x * kGemmM, is_ch = 0, is_st = 0;
+    auto issue_bulk = [&]() {  // thread 0: the next chunk (nothing past the end)
+        if (is_q < total) {
+            const int k0 = kbeg + is_ch * kGemmKc, rows = min(kGemmKc, kend - k0);
+            const uint32_t ba = (uint32_t)rows * kGemmM * 4, bb = (uint32_t)rows * NT * 4;
+            mbar_expect_tx(&mb_raw[is_st], ba + bb);
+            bulk_copy(smem_u32(raw_a(is_st)), g.A + (int64_t)k0 * kGemmM, ba, &mb_raw[is_st]);
+            bulk_copy(smem_u32(raw_b(is_st)), g.B + (int64_t)k0 * NT, bb, &mb_raw[is_st]);
+            if (++is_ch == nck) {
+                is_ch = 0;
+                is_m0 += (int)gridDim.x * kGemmM;
+            }
+            if (++is_st == kRaw) is_st = 0;
+            ++is_q;
+        }
+    };
+    auto issue = [&]() {  // the next chunk of the sequence (an empty group past the end)
+        if (is_q < total) {
+            const int k0 = kbeg + is_ch * kGemmKc;
+            raw_issue<kGemmM>(g.A, g.a_m, g.a_k, is_m0, g.M, k0, kend, raw_a(is_st));
+            if (!BRES) raw_issue<NT>(g.B, g.b_n, g.b_k, 0, g.N, k0, kend, raw_b(is_st));
+            if (++is_ch == nck) {
+                is_ch = 0;
+                is_m0 += (int)gridDim.x * kGemmM;
+            }
+            if (++is_st == kRaw) is_st = 0;
+            ++is_q;
+        }
+        cp_async_commit();
+    };
+    if (bulk) {
+        if (tid == 0)
+            for (int q = 0; q < kRaw; ++q) issue_bulk();
+    } else {
+        for (int q = 0; q < kRaw - 1; ++q) issue();
+    }
+    int rd_st = 0;         // raw stage of chunk q
+    uint32_t rd_ph = 0;    // its fill parity (bulk mode)
+    uint32_t tphase = 0;  // mb_tile completions waited for
     float acc[FLUSH ? kColHalf : 1];
-
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int m0 = tile * kGemmM;
-        bool any = false;
+    for (int t = 0, q = 0; t < my_tiles; ++t) {
+        const int m0 = ((int)blockIdx.x + t * (int)gridDim.x) * kGemmM;
 #pragma unroll
         for (int j = 0; j < (FLUSH ? kColHalf : 1); ++j) acc[j] = 0.f;
-        int chunk = 0;
-        for (int k0 = kbeg; k0 < kend; k0 += kGemmKc, ++chunk, ++c) {
-            const int st = (int)(c % kGemmStages);
-            if (c >= (uint32_t)kGemmStages) mbar_wait(&mb_stage[st], ((c / kGemmStages) - 1) & 1u);
-            char* a_hi = smem + (size_t)st * gemm_stage_bytes(NT);
+        for (int chunk = 0; chunk < nck; ++chunk, ++q) {
+            const int k0 = kbeg + chunk * kGemmKc;
+            if (bulk) {
+                mbar_wait(&mb_raw[rd_st], rd_ph);  // chunk q landed
+            } else {
+                cp_async_wait_n(kRaw - 2);  // chunk q landed (this thread's copies)
+                __syncthreads();            // ... everyone's; raw stage (q - 1) % kRaw is free again
+                issue();
+            }
+            // the split buffer's previous MMAs (chunk q - kSplit) are done
+            if (q >= kSplit) mbar_wait(&mb_mma[q % kSplit], (uint32_t)(q / kSplit - 1) & 1u);
+            tc_after_sync();
+            char* a_hi = split0 + (size_t)(q % kSplit) * kSplitBuf;
             char* a_lo = a_hi + kABytes;
-            char* b_hi = a_lo + kABytes;
-            char* b_lo = b_hi + kBBytes;
-            stage_tile(g.A, g.a_m, g.a_k, m0, g.M, k0, kend, kGemmM, a_hi, a_lo);
-            stage_tile(g.B, g.b_n, g.b_k, 0, g.N, k0, kend, NT, b_hi, b_lo);
+            char* sb_hi = a_lo + kABytes;  // split B (not resident)
+            const int kvalid = bulk ? min(kGemmKc, kend - k0) : kGemmKc;
+            raw_split<kGemmM>(ta, raw_a(rd_st), a_hi, a_lo, kvalid);
+            if (!BRES) raw_split<NT>(tb, raw_b(rd_st), sb_hi, sb_hi + kBBytes, kvalid);
+            if (++rd_st == kRaw) {
+                rd_st = 0;
+                rd_ph ^= 1u;
+            }
             fence_async_smem();
             __syncthreads();
-            const bool group_start = FLUSH ? (chunk % kFlushChunks) == 0 : !any;
-            const bool group_end = FLUSH ? ((chunk % kFlushChunks) == kFlushChunks - 1 || k0 + kGemmKc >= kend)
-                                         : k0 + kGemmKc >= kend;
+            if (bulk && tid == 0) issue_bulk();  // into the stage just split (chunk q + kRaw)
+            const bool group_start = FLUSH ? (chunk % kFlushChunks) == 0 : chunk == 0;
+            const bool group_end = FLUSH ? ((chunk % kFlushChunks) == kFlushChunks - 1 || chunk + 1 == nck)
+                                         : chunk + 1 == nck;
             if (tid == 0) {
                 tc_after_sync();
+                char* b_hi = BRES ? bres + (size_t)chunk * 2 * kBBytes : sb_hi;
+                char* b_lo = b_hi + kBBytes;
                 const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
 #pragma unroll
                 for (int s = 0; s < kGemmKc / 8; ++s) {  // K = 8 tf32 per MMA = 2 core-matrix columns
@@ -266,10 +507,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g) {
                     mma_tf32(tmem, dah, dbl, idesc, 1u);
                     mma_tf32(tmem, dal, dbh, idesc, 1u);
                 }
-                mma_commit(&mb_stage[st]);
+                mma_commit(&mb_mma[q % kSplit]);
                 if (group_end) mma_commit(&mb_tile);
             }
-            any = true;
             if (FLUSH && group_end) {
                 mbar_wait(&mb_tile, tphase & 1u);
                 ++tphase;
@@ -284,14 +524,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g) {
                 tc_before_sync();  // the next group's first MMA overwrites the accumulator
             }
         }
+        const bool any = nck > 0;
+        // the epilogue's mask loads go out before the wait for the tile's last MMAs
+        const int m = m0 + (warp & 3) * 32 + lane;
+        const bool row_ok = m < g.M;
+        const float* mrow0 = g.mask && row_ok && epi_warp ? g.mask + (int64_t)m * g.ldmask + col0 : nullptr;
+        const bool mvec = mrow0 && ((uintptr_t)mrow0 & 15) == 0 && (g.ldmask & 3) == 0;
+        float4 mk[kColHalf / 4];
+#pragma unroll
+        for (int i = 0; i < kColHalf / 4; ++i)
+            mk[i] = mvec && col0 + 4 * i + 4 <= g.N ? __ldg(reinterpret_cast<const float4*>(mrow0) + i)
+                                                  : make_float4(1.f, 1.f, 1.f, 1.f);
         if (!FLUSH && any) {
             mbar_wait(&mb_tile, tphase & 1u);
             ++tphase;
             tc_after_sync();
         }
 
-        // epilogue: this warp's TMEM lane quadrant (rows), its column half
-        const int m = m0 + (warp & 3) * 32 + lane;
+        // epilogue: this warp's TMEM lane quadrant (rows), its column group.  The mask loads
+        // of the whole group are issued before any store (C may alias nothing, but the
+        // compiler cannot know it: load / store pairs would serialise on memory latency).
         if (epi_warp) {
 #pragma unroll
             for (int cc = 0; cc < kColHalf; cc += 16) {
@@ -306,7 +558,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) v[j] = 0u;
                 }
-                if (m < g.M && n0 < g.N) {
+                if (row_ok && n0 < g.N) {
                     float x[16];
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
@@ -316,20 +568,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g) {
                     }
                     float* crow = C + (int64_t)m * g.ldc + n0;
                     const float* mrow = g.mask ? g.mask + (int64_t)m * g.ldmask + n0 : nullptr;
-                    const bool vec = n0 + 16 <= g.N && ((uintptr_t)crow & 15) == 0 &&
-                                     (!mrow || ((uintptr_t)mrow & 15) == 0);
+                    const bool vec = n0 + 16 <= g.N && ((uintptr_t)crow & 15) == 0 && (!mrow || mvec);
                     if (vec) {
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            float4 o = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
-                            if (mrow) {
-                                const float4 mk = __ldg(reinterpret_cast<const float4*>(mrow) + q);
-                                if (!(mk.x > 0.f)) o.x = 0.f;
-                                if (!(mk.y > 0.f)) o.y = 0.f;
-                                if (!(mk.z > 0.f)) o.z = 0.f;
-                                if (!(mk.w > 0.f)) o.w = 0.f;
-                            }
-                            reinterpret_cast<float4*>(crow)[q] = o;
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            const float4 mq = mk[cc / 4 + q4];
+                            float4 o = make_float4(x[4 * q4], x[4 * q4 + 1], x[4 * q4 + 2], x[4 * q4 + 3]);
+                            if (!(mq.x > 0.f)) o.x = 0.f;
+                            if (!(mq.y > 0.f)) o.y = 0.f;
+                            if (!(mq.z > 0.f)) o.z = 0.f;
+                            if (!(mq.w > 0.f)) o.w = 0.f;
+                            reinterpret_cast<float4*>(crow)[q4] = o;
                         }
                     } else {
 #pragma unroll
@@ -345,6 +594,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g) {
         }
         tc_before_sync();  // the next tile's first MMA overwrites the accumulator
     }
+    cp_async_wait<0>();
     tc_before_sync();
     __syncthreads();
     if (warp == 0)
@@ -361,41 +611,57 @@ __global__ void k_reduce_slices(const float* __restrict__ part, int slices, int6
     }
 }
 
-size_t gemm_smem_bytes(int nt) { return (size_t)kGemmStages * gemm_stage_bytes(nt); }
-
-template <int NT, bool F>
+template <int NT, bool F, bool R>
 void gemm_attr() {
-    cudaFuncSetAttribute(k_gemm_tf32x3<NT, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(NT));
+    cudaFuncSetAttribute(k_gemm_tf32x3<NT, F, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmMaxSmem);
 }
 
-template <bool F>
-int gemm_dispatch(const GemmArgs& g, dim3 grid, cudaStream_t st) {
+template <bool F, bool R>
+int gemm_dispatch(const GemmArgs& g, dim3 grid, const GemmPlan& p, cudaStream_t st) {
+    const size_t bytes = p.bytes;
     if (g.N <= 16)
-        k_gemm_tf32x3<16, F><<<grid, kGemmThreads, gemm_smem_bytes(16), st>>>(g);
+        k_gemm_tf32x3<16, F, R><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
     else if (g.N <= 32)
-        k_gemm_tf32x3<32, F><<<grid, kGemmThreads, gemm_smem_bytes(32), st>>>(g);
+        k_gemm_tf32x3<32, F, R><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
     else if (g.N <= 64)
-        k_gemm_tf32x3<64, F><<<grid, kGemmThreads, gemm_smem_bytes(64), st>>>(g);
+        k_gemm_tf32x3<64, F, R><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
     else if (g.N <= 128)
-        k_gemm_tf32x3<128, F><<<grid, kGemmThreads, gemm_smem_bytes(128), st>>>(g);
+        k_gemm_tf32x3<128, F, R><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
     else
         return -1;
     return 1;
 }
 
+template <bool F, bool R>
+void gemm_attrs() {
+    gemm_attr<16, F, R>(); gemm_attr<32, F, R>(); gemm_attr<64, F, R>(); gemm_attr<128, F, R>();
+}
+
 int launch_gemm_tf32x3(const GemmArgs& g, int slices, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        gemm_attr<16, false>(); gemm_attr<32, false>(); gemm_attr<64, false>(); gemm_attr<128, false>();
-        gemm_attr<16, true>(); gemm_attr<32, true>(); gemm_attr<64, true>(); gemm_attr<128, true>();
+        gemm_attrs<false, false>(); gemm_attrs<false, true>(); gemm_attrs<true, false>(); gemm_attrs<true, true>();
         attr = true;
     }
     if (g.M <= 0 || g.N <= 0) return 0;
     const int ntiles = (g.M + kGemmM - 1) / kGemmM;
-    const int per_sm = g.N <= 32 ? 2 : 1;  // shared-memory / TMEM residency
-    const dim3 grid(std::min(ntiles, std::max(1, 148 * per_sm / std::max(1, slices))), std::max(1, slices));
+    const int nt = g.N <= 16 ? 16 : g.N <= 32 ? 32 : g.N <= 64 ? 64 : 128;
+    const int kps = std::min(g.k_per_slice, std::max(g.K, 0));
+    const int nck = (kps + kGemmKc - 1) / kGemmKc;
+    const int gx = std::min(ntiles, std::max(1, 148 / std::max(1, slices)));
+    const dim3 grid(gx, std::max(1, slices));
+    GemmPlan p = gemm_plan(nt, nck, ntiles > gx, g.a_m == 1, g.b_n == 1);
+    static const int raw_cap = [] {  // TSB_GEMM_RAW: cap on the raw stages (A/B timing)
+        const char* e = std::getenv("TSB_GEMM_RAW");
+        return e ? std::atoi(e) : kMaxRaw;
+    }();
+    if (p.raw > raw_cap && raw_cap >= 2) {
+        p.raw = raw_cap;
+        p.bytes = gemm_bytes(nt, nck, p.b_res, g.a_m == 1, g.b_n == 1, p.raw);
+    }
     const bool flush = g.k_per_slice > kFlushChunks * kGemmKc;
-    return flush ? gemm_dispatch<true>(g, grid, st) : gemm_dispatch<false>(g, grid, st);
+    if (flush) return p.b_res ? gemm_dispatch<true, true>(g, grid, p, st) : gemm_dispatch<true, false>(g, grid, p, st);
+    return p.b_res ? gemm_dispatch<false, true>(g, grid, p, st) : gemm_dispatch<false, false>(g, grid, p, st);
 }
 
 void launch_reduce_slices(const float* part, int slices, int64_t stride, int64_t n, float* out, bool accumulate,

@@ -63,6 +63,18 @@ def test_gemm_transposed_operands_split_k_and_mask(tsb, ctx):
     assert np.abs(got2 - ref2).max() <= 1e-5 * np.abs(ref2).max()
 
 
+@pytest.mark.parametrize("n,slices", [(5000, 7), (131, 1)])
+def test_gemm_bulk_copied_transposed_operands(tsb, ctx, n, slices):
+    """Full-width 128-column operands read transposed (dW of a hidden layer): the chunks are
+    contiguous row runs moved by TMA bulk copies, partial last chunks zero-padded on split."""
+    rng = np.random.default_rng(11)
+    delta = rng.normal(size=(n, 128)).astype(np.float32)
+    H = rng.normal(size=(n, 128)).astype(np.float32)
+    got = gemm(tsb, ctx, delta, 1, 128, H, 1, 128, 128, 128, n, slices=slices)
+    ref = delta.astype(np.float64).T @ H.astype(np.float64)
+    assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max()
+
+
 def _nets(tsb, ctx, cfg, seed, n=3000):
     from oracle import deform as od
     onet = od.DeformNet.init(cfg, seed)
