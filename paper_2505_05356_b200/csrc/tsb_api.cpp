@@ -1410,8 +1410,8 @@ ScanK scank(tsb_pass* p) {
     sc.det_part = nullptr;
     sc.nsub2 = p->opt.sub * p->opt.sub;
     sc.sl_off = p->sl_lists ? p->sl_off : nullptr;
-    sc.sl_rank = p->sl_rank;
-    sc.sl_rect = p->sl_rect;
+    sc.sl_rank = p->sl_lists ? p->sl_rank : nullptr;
+    sc.sl_rect = p->sl_lists ? p->sl_rect : p->trect;
     sc.sup_x = p->sup_x;
     sc.sup_log = p->sup_log;
     return sc;

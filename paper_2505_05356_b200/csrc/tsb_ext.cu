@@ -145,11 +145,11 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_fwd(RecK rec, SceneK S, 
     int pass = 0;
     for (int r0 = 0, ebase = 0; r0 < V && ebase < bmax; r0 += kRasterThreads, ++pass) {
         const int rr = r0 + tid;
-        const bool cov = rr < V && tile_covers(seg.rect[rr], ttx, tty);
+        const bool cov = rr < V && tile_covers(seg_rect(sc, seg, rr), ttx, tty);
         int total;
         const int pos = scan_compact(cov, wsum[pass & 1], total);  // (its barrier follows the last pass's reads)
         if (pos >= 0) {
-            const uint32_t r = sc.ord[seg_rank(seg, rr)];
+            const uint32_t r = sc.ord[seg_rank(sc, seg, rr)];
             sg[pos] = r;
             sA[pos] = stage_A(rec.A[r], m.ox, m.oy);
             sB[pos] = rec.B[r];
@@ -305,13 +305,13 @@ __global__ void __launch_bounds__(kRasterThreads) k_ext_bwd(RecK rec, OptK O, in
     int pass = 0;
     for (int r_hi = bt.x, e_top = bt.y; bmax > 0 && r_hi > 0 && e_top > 0; r_hi -= kRasterThreads, ++pass) {
         const int rr = r_hi - 1 - tid;
-        const bool cov = rr >= 0 && tile_covers(seg.rect[rr], ttx, tty);
+        const bool cov = rr >= 0 && tile_covers(seg_rect(sc, seg, rr), ttx, tty);
         int total;
         const int pos = scan_compact(cov, wsum[pass & 1], total);  // descending rank order
         const int e_lo = e_top - total;
         if (pos >= 0) {
             const int j = total - 1 - pos;  // ascending
-            const uint32_t r = sc.ord[seg_rank(seg, rr)];
+            const uint32_t r = sc.ord[seg_rank(sc, seg, rr)];
             srank[j] = r;
             sA[j] = stage_A(rec.A[r], m.ox, m.oy);
             sB[j] = rec.B[r];

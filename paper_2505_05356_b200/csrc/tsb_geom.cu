@@ -345,10 +345,10 @@ __global__ void __launch_bounds__(128) k_fixup_mark(OptK O, FixupK fx, PixK px, 
         }
         for (int r0 = r_from; r0 < V && e < limit; r0 += 32) {
             const int r = r0 + lane;
-            const bool cov = r < V && tile_covers(seg.rect[r], tx, ty);
+            const bool cov = r < V && tile_covers(seg_rect(fx.sc, seg, r), tx, ty);
             const unsigned m = __ballot_sync(0xffffffffu, cov);
             if (cov && e + __popc(m & ((1u << lane) - 1u)) < limit) {
-                const uint32_t g = fx.sc.ord[seg_rank(seg, r)];
+                const uint32_t g = fx.sc.ord[seg_rank(fx.sc, seg, r)];
                 if (atomicExch(&fx.stamp[g], stamp) != stamp) {
                     const int slot = atomicAdd(fx.work_n, 1);
                     fx.work[slot] = (int)g;
@@ -495,10 +495,10 @@ __device__ __forceinline__ void queue_step(const ScanK& sc, const ScanSeg& seg, 
 #pragma unroll
     for (int k = 0; k < kScanK; ++k) {
         const int r = descending ? r0 - 1 - (32 * k + lane) : r0 + 32 * k + lane;
-        const bool cov = r >= r_min && r < V && tile_covers(seg.rect[r], tx, ty);
+        const bool cov = r >= r_min && r < V && tile_covers(seg_rect(sc, seg, r), tx, ty);
         const unsigned m = __ballot_sync(0xffffffffu, cov);
         if (cov) {
-            const uint32_t rk = seg_rank(seg, r);
+            const uint32_t rk = seg_rank(sc, seg, r);
             qg[qn + __popc(m & below)] = (int)sc.ord[rk];
             qr[qn + __popc(m & below)] = pos_out ? r : (int)rk;
         }

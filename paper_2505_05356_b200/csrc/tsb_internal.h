@@ -118,24 +118,27 @@ struct ScanK {
     // the whole order; scan positions (blk_term.x, FixState::r_end) index that list.  Null
     // sl_off (a short order, kSlMinRanks): blocks scan the order itself (positions = ranks).
     const uint32_t* sl_off;    // [nsup + 1]
-    const uint32_t* sl_rank;   // [sl_cap]
-    const uint2* sl_rect;      // [sl_cap]
+    const uint32_t* sl_rank;   // [sl_cap] (null without lists)
+    const uint2* sl_rect;      // [sl_cap] (trect without lists)
     int sup_x, sup_log;
 };
-// One tile's scan list: its super-tile's ranks, rects and length.
+// One tile's scan list: its offset in the super-tile lists and its length (two 32-bit
+// values: the list pointers stay kernel parameters, not live registers of the scan loops).
 struct ScanSeg {
-    const uint32_t* rank;
-    const uint2* rect;
+    uint32_t off;
     int n;
 };
 __device__ __forceinline__ ScanSeg scan_seg(const ScanK& sc, int tx, int ty) {
-    if (!sc.sl_off) return ScanSeg{nullptr, sc.trect, *sc.n_rank};  // short order: the order itself
+    if (!sc.sl_off) return ScanSeg{0u, *sc.n_rank};  // short order: the order itself
     const int s = (ty >> sc.sup_log) * sc.sup_x + (tx >> sc.sup_log);
     const uint32_t a = sc.sl_off[s], b = sc.sl_off[s + 1];
-    return ScanSeg{sc.sl_rank + a, sc.sl_rect + a, (int)(b - a)};
+    return ScanSeg{a, (int)(b - a)};
 }
-// The rank at scan position p.
-__device__ __forceinline__ uint32_t seg_rank(const ScanSeg& sg, int p) { return sg.rank ? sg.rank[p] : (uint32_t)p; }
+// The tile rect / rank at scan position p (without lists sl_rect is trect and sl_rank null).
+__device__ __forceinline__ uint2 seg_rect(const ScanK& sc, const ScanSeg& sg, int p) { return sc.sl_rect[sg.off + p]; }
+__device__ __forceinline__ uint32_t seg_rank(const ScanK& sc, const ScanSeg& sg, int p) {
+    return sc.sl_rank ? sc.sl_rank[sg.off + p] : (uint32_t)p;
+}
 // Build arguments of the super-tile lists (k_order_ranks counts + scan, k_sl_emit).
 constexpr int kSlChunk = 256;     // ranks per chunk
 constexpr int kSlMinRanks = 32768; // orders up to this long are scanned directly (no lists)

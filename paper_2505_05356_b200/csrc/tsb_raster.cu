@@ -40,6 +40,7 @@ struct Smem {
     uint8_t wmask[kBatchCap];                        // per staged entry: warps it can reach
     uint16_t list[kRasterThreads / 32][kBatchCap];   // per warp: its entries, in list order
     int wsum[2][kRasterThreads / 32];                 // scan-pass compaction (double-buffered by pass parity)
+    int seg_off, seg_n;                               // the block's scan list (block-uniform: kept out of registers)
 };
 
 // Pixel of thread tid in its 16 x 16 block: warp w owns the 8 x 4 sub-block at
@@ -89,7 +90,9 @@ __device__ __forceinline__ void stage_entry(SM& sm, const RecK& rec, uint32_t g,
 // is finalised (outputs, fix-up flag, loss epilogue) at the end.
 // WORK: count evaluations / contributions (profiling runs only; a template so the
 // per-evaluation counter costs nothing otherwise).
-template <int NF, bool DIST, bool WORK>
+// LISTS: the block scans its super-tile list (ScanK::sl_*); otherwise the order itself
+// (a template so the short-order kernel carries none of the list bookkeeping).
+template <int NF, bool DIST, bool WORK, bool LISTS>
 __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK sc, OptK O, int W, int H, PixK px,
                                                                 const FrameDev* __restrict__ fd, int loss, ChW chw,
                                                                 double* __restrict__ loss_part) {
@@ -124,19 +127,24 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK s
     const float outside = cut2 + coarseM;  // maha above this is outside, with no ambiguity to check
     // common-path tests with one compare each; the exact windows are re-tested inside
     const float m_lo = cut2 - 2.f * coarseM, a_hi = thr + 2.f * coarseA;
-    const ScanSeg seg = scan_seg(sc, ttx, tty);
-    const int V = seg.n;
+    if (LISTS && tid == 0) {
+        const ScanSeg sg = scan_seg(sc, ttx, tty);
+        sm.seg_off = (int)sg.off;
+        sm.seg_n = sg.n;
+    }
+    const int V0 = LISTS ? 0 : *sc.n_rank;
     int r = 0, ebase = 0, cnt = 0, pass = 0;
 
-    if (__syncthreads_count(done) < kRasterThreads) {
-        while (r < V) {
-            // scan pass: super-tile list positions r .. r + 255, covering ranks appended to the batch
+    if (__syncthreads_count(done) < kRasterThreads) {  // (also publishes seg_off / seg_n)
+        while (r < (LISTS ? sm.seg_n : V0)) {
+            // scan pass: list positions (ranks without lists) r .. r + 255, covering ones appended to the batch
             const int p = r + tid;
-            const bool cov = p < V && tile_covers(seg.rect[p], ttx, tty);
+            const int Vn = LISTS ? sm.seg_n : V0;
+            const bool cov = p < Vn && tile_covers(LISTS ? sc.sl_rect[sm.seg_off + p] : sc.trect[p], ttx, tty);
             int total;
             const int pos = scan_compact(cov, sm.wsum[pass & 1], total);
             if (pos >= 0) {
-                const uint32_t rr = seg_rank(seg, p);
+                const uint32_t rr = LISTS ? sc.sl_rank[sm.seg_off + p] : (uint32_t)p;
                 const uint32_t g = sc.ord[rr];
                 stage_entry<NF>(sm, rec, g, cnt + pos, ox, oy, outside);
                 const int e = ebase + cnt + pos;  // list index: its rank is recorded for the backward
@@ -145,7 +153,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK s
             cnt += total;
             r += kRasterThreads;
             ++pass;
-            if (cnt < kRasterThreads && r < V) continue;  // keep filling (the next pass's barrier orders the slots)
+            if (cnt < kRasterThreads && r < Vn) continue;  // keep filling (the next pass's barrier orders the slots)
             __syncthreads();
             const int nb = cnt;
             // this warp's entries, in order
@@ -237,7 +245,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK s
     }
     // every rank of the order scanned: a pixel still alive processed the whole list
     if (!done) processed = ebase;
-    if (tid == 0) sc.blk_term[blockIdx.x] = make_int2(min(r, V), ebase);
+    if (tid == 0) sc.blk_term[blockIdx.x] = make_int2(min(r, LISTS ? sm.seg_n : V0), ebase);
     // the prefix order ended with the pixel alive: the frame is redone with the full order
     if (active && !done && *sc.n_all > *sc.n_rank) atomicOr(sc.abort, 8);
     float lpx = 0.f;
@@ -500,7 +508,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, ScanK s
             e_top -= nb;
         } else {
             const int p = r_hi - 1 - tid;
-            const bool cov = p >= 0 && tile_covers(seg.rect[p], ttx, tty);
+            const bool cov = p >= 0 && tile_covers(seg_rect(sc, seg, p), ttx, tty);
             int total;
             const int pos = scan_compact(cov, sm.wsum[pass & 1], total);  // descending rank order
             // entries of this pass: indices [e_top - total, e_top); keep those below bmax
@@ -508,7 +516,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, ScanK s
             const int asc = total - 1 - pos;
             if (pos >= 0 && asc < keep_hi) {
                 const int slot = kBatchCap - cnt - keep_hi + asc;
-                const uint32_t rr = seg_rank(seg, p);
+                const uint32_t rr = seg_rank(sc, seg, p);
                 const uint32_t g = sc.ord[rr];
                 sm.grank[slot] = g;
                 sm.rrank[slot] = (uint32_t)rr;
@@ -632,20 +640,26 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, ScanK s
 void launch_raster_fwd(const RecK& rec, const ScanK& sc, const OptK& O, int W, int H, int nf, PixK px,
                        const FrameDev* fd, bool loss, const ChW& ch_w, double* loss_part, cudaStream_t st) {
     const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
-#define TSB_FWD(NF_, D_)                                                                                        \
+#define TSB_FWD_L(NF_, D_, L_)                                                                                  \
     do {                                                                                                       \
         if (sc.work)                                                                                           \
-            k_raster_fwd<NF_, D_, true><<<grid, kRasterThreads, 0, st>>>(rec, sc, O, W, H, px, fd, loss ? 1 : 0,  \
-                                                                          ch_w, loss_part);                     \
+            k_raster_fwd<NF_, D_, true, L_><<<grid, kRasterThreads, 0, st>>>(rec, sc, O, W, H, px, fd,            \
+                                                                              loss ? 1 : 0, ch_w, loss_part);   \
         else                                                                                                   \
-            k_raster_fwd<NF_, D_, false><<<grid, kRasterThreads, 0, st>>>(rec, sc, O, W, H, px, fd, loss ? 1 : 0, \
-                                                                           ch_w, loss_part);                    \
+            k_raster_fwd<NF_, D_, false, L_><<<grid, kRasterThreads, 0, st>>>(rec, sc, O, W, H, px, fd,           \
+                                                                               loss ? 1 : 0, ch_w, loss_part);  \
+    } while (0)
+#define TSB_FWD(NF_, D_)                  \
+    do {                                  \
+        if (sc.sl_off) TSB_FWD_L(NF_, D_, true); \
+        else TSB_FWD_L(NF_, D_, false);   \
     } while (0)
     if (nf > 1) {
         if (O.dist) TSB_FWD(2, true); else TSB_FWD(2, false);
     } else {
         if (O.dist) TSB_FWD(1, true); else TSB_FWD(1, false);
     }
+#undef TSB_FWD_L
 #undef TSB_FWD
 }
 
