@@ -1287,6 +1287,14 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
         return e ? (float)std::atof(e) : kTrelFlag;
     }();
     O.trel_flag = trel;
+    {  // the raster's thresholds (tsb_raster.cu k_raster_fwd), fp32 as the kernel used them
+        const float coarse_m = kCoarseMaha * O.cut2_f, coarse_a = kCoarseAlpha * O.alpha_thr_f;
+        O.coarse_m_f = coarse_m;
+        O.coarse_a_f = coarse_a;
+        O.outside_f = O.cut2_f + coarse_m;
+        O.m_lo_f = O.cut2_f - 2.f * coarse_m;
+        O.a_hi_f = O.alpha_thr_f + 2.f * coarse_a;
+    }
     for (int c = 0; c < 3; ++c) O.bg_color[c] = opt->bg_color[c];
     p->ntiles = O.tiles_x * O.tiles_y;
     if (p->ntiles > 65536) return fail(TSB_ERR_UNSUPPORTED, "render: more than 65536 tiles");

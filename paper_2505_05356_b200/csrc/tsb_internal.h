@@ -25,6 +25,8 @@ struct CamK {
 };
 
 // Render options (splat.hpp:28-37) in the forms the kernels compare against.
+constexpr float kCoarseMaha = 1e-3f;       // relative window that triggers the precise bound
+constexpr float kCoarseAlpha = 1e-4f;
 struct OptK {
     double alpha_thr, floor_T, dilation, sigma_cutoff, cov_eps, cut2;
     int ts;            // binning tile size
@@ -34,6 +36,9 @@ struct OptK {
     int dist;          // distortion channel: accumulate the shifted depth moments
     int exact;         // TSB_CH_EXACT: every pixel goes to the fp64 fix-up
     float trel_flag;   // relative T error bound above which a pixel is recomposited (fix-up reason 8)
+    // the raster's decision thresholds (host-computed: constant-bank operands in the hot loop,
+    // no registers): coarse windows, the clearly-outside maha, the prefilter edges
+    float coarse_m_f, coarse_a_f, outside_f, m_lo_f, a_hi_f;
     double bg_quad[8];
     double bg_phasor[4];
     double bg_color[3];

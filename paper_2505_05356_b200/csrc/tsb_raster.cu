@@ -123,10 +123,11 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK s
     int nc = 0, flag = 0, last_eff = -1, processed = 0;  // flag reasons: 1 maha band, 2 alpha band, 4 T band
     bool done = !active;
     const float cut2 = O.cut2_f, thr = O.alpha_thr_f, fl = O.floor_f;
-    const float coarseM = kCoarseMaha * cut2, coarseA = kCoarseAlpha * thr;
-    const float outside = cut2 + coarseM;  // maha above this is outside, with no ambiguity to check
-    // common-path tests with one compare each; the exact windows are re-tested inside
-    const float m_lo = cut2 - 2.f * coarseM, a_hi = thr + 2.f * coarseA;
+    // coarse windows; maha above `outside` is outside with no ambiguity to check; common-path
+    // tests with one compare each (the exact windows are re-tested inside).  Host-computed
+    // (OptK): constant-bank operands, so the hot loop neither holds nor recomputes them.
+    const float coarseM = O.coarse_m_f, coarseA = O.coarse_a_f, outside = O.outside_f;
+    const float m_lo = O.m_lo_f, a_hi = O.a_hi_f;
     if (LISTS && tid == 0) {
         const ScanSeg sg = scan_seg(sc, ttx, tty);
         sm.seg_off = (int)sg.off;

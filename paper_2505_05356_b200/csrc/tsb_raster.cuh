@@ -47,8 +47,6 @@ __device__ __forceinline__ void eval_alpha(const float4& B, Eval& e) {
 // on its fp32 error (rare branch); the pixel is sent to the fp64 fix-up when the
 // decision lies inside twice that bound.
 constexpr float kEps = 5.9604645e-8f;      // 2^-24
-constexpr float kCoarseMaha = 1e-3f;       // relative window that triggers the precise bound
-constexpr float kCoarseAlpha = 1e-4f;
 constexpr float kEx2Err = 2.5e-7f;         // ex2.approx.ftz.f32 relative error bound (+ margin)
 
 // |fl32(maha) - maha_exact| bound from the rounding of mean offsets (A.z, A.w carry
