@@ -1261,6 +1261,10 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     for (int i = 0; i < 3; ++i) C.t[i] = cam->t[i];
     C.lim_x = 1.3 * (0.5 * cam->width / cam->fx);
     C.lim_y = 1.3 * (0.5 * cam->height / cam->fy);
+    for (int i = 0; i < 9; ++i) C.Rf[i] = (float)C.R[i];
+    C.fxf = (float)C.fx; C.fyf = (float)C.fy; C.cxf = (float)C.cx; C.cyf = (float)C.cy;
+    C.limxf = (float)C.lim_x; C.limyf = (float)C.lim_y;
+    C.Wf = (float)C.W; C.Hf = (float)C.H;
     for (int i = 0; i < 3; ++i)
         C.center[i] = -(cam->R[0 * 3 + i] * cam->t[0] + cam->R[1 * 3 + i] * cam->t[1] + cam->R[2 * 3 + i] * cam->t[2]);
     OptK& O = p->opt;
@@ -1278,6 +1282,8 @@ int tsb_pass_prepare(tsb_pass* p, tsb_scene* s, const tsb_camera* cam, const tsb
     O.floor_f = (float)O.floor_T;
     O.cut2_f = (float)O.cut2;
     O.cov_eps_f = (float)O.cov_eps;
+    O.dilation_f = (float)O.dilation;
+    O.sigma_cutoff_f = (float)O.sigma_cutoff;
     for (int c = 0; c < 8; ++c) O.bg_quad[c] = c < 4 * p->nf ? opt->bg_quad[c] : 0.0;
     for (int c = 0; c < 4; ++c) O.bg_phasor[c] = c < 2 * p->nf ? opt->bg_phasor[c] : 0.0;
     O.dist = (opt->channels & TSB_CH_DISTORTION) ? 1 : 0;

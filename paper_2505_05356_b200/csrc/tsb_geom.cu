@@ -71,17 +71,19 @@ __device__ __forceinline__ int lean_visible(const SceneK& S, const CamK& C, cons
     const double op = S.opac ? S.opac[gi] : opacity64(S, gi);
     if (op < O.alpha_thr) return 0;
     if (!S.cov6) return 2;
-    const double iz = rcp64(p[2]);
-    const float mx = (float)(C.fx * p[0] * iz + C.cx), my = (float)(C.fy * p[1] * iz + C.cy);
-    const float limx = (float)C.lim_x, limy = (float)C.lim_y;
-    const float txz = fminf(fmaxf((float)(p[0] * iz), -limx), limx);  // clamped tx / z
-    const float tyz = fminf(fmaxf((float)(p[1] * iz), -limy), limy);
-    const float fxz = (float)(C.fx * iz), fyz = (float)(C.fy * iz);
+    // the bound in fp32 from the fp64 camera-space mean (its errors, ~1e-7 relative, sit far
+    // inside the tolerances below); camera constants are host-rounded fp32 copies
+    const float pf0 = (float)p[0], pf1 = (float)p[1], izf = 1.f / (float)p[2];
+    const float mx = C.fxf * (pf0 * izf) + C.cxf, my = C.fyf * (pf1 * izf) + C.cyf;
+    const float limx = C.limxf, limy = C.limyf;
+    const float txz = fminf(fmaxf(pf0 * izf, -limx), limx);  // clamped tx / z
+    const float tyz = fminf(fmaxf(pf1 * izf, -limy), limy);
+    const float fxz = C.fxf * izf, fyz = C.fyf * izf;
     // M = J W (2 x 3), J = [[fx/z, 0, -fx tx/z^2], [0, fy/z, -fy ty/z^2]]
     float M[6], Ma[6];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-        const float r0 = (float)R[0 * 3 + j], r1 = (float)R[1 * 3 + j], r2 = (float)R[2 * 3 + j];
+        const float r0 = C.Rf[0 * 3 + j], r1 = C.Rf[1 * 3 + j], r2 = C.Rf[2 * 3 + j];
         M[j] = fxz * (r0 - txz * r2);
         M[3 + j] = fyz * (r1 - tyz * r2);
         Ma[j] = fabsf(fxz) * (fabsf(r0) + fabsf(txz * r2));
@@ -105,7 +107,7 @@ __device__ __forceinline__ int lean_visible(const SceneK& S, const CamK& C, cons
             T[i * 3 + j] = M[i * 3 + 0] * V[j] + M[i * 3 + 1] * V[3 + j] + M[i * 3 + 2] * V[6 + j];
             Ta[i * 3 + j] = Ma[i * 3 + 0] * fabsf(V[j]) + Ma[i * 3 + 1] * fabsf(V[3 + j]) + Ma[i * 3 + 2] * fabsf(V[6 + j]);
         }
-    const float dil = (float)O.dilation;
+    const float dil = O.dilation_f;
     const float a0 = T[0] * M[0] + T[1] * M[1] + T[2] * M[2] + dil;
     const float a1 = T[0] * M[3] + T[1] * M[4] + T[2] * M[5];
     const float a3 = T[3] * M[3] + T[4] * M[4] + T[5] * M[5] + dil;
@@ -119,14 +121,14 @@ __device__ __forceinline__ int lean_visible(const SceneK& S, const CamK& C, cons
     const float h = 0.5f * (a0 - a3);
     const float disc = h * h + a1 * a1;
     const float lam = 0.5f * (a0 + a3) + sqrtf(fmaxf(disc, 0.1f));
-    const float r = (float)O.sigma_cutoff * sqrtf(lam);
+    const float r = O.sigma_cutoff_f * sqrtf(lam);
     const float tol = 1e-4f * (r * fmaxf(1.f, (b0 + b3) / lam) + fabsf(mx) + fabsf(my) + 1.f);
     // huge or non-finite: prep64.  Its rect bounds go through x86 int conversion (INT_MIN
     // past 2^31), which culls splats the plain geometric test keeps, so anything whose
     // mean +- radius gets anywhere near 2^31 px is decided exactly.
     if (!(tol < 1e8f && fabsf(mx) + r < 1e9f && fabsf(my) + r < 1e9f)) return 2;
-    const float bx = mx + r + 1.f, ax = (float)C.W - (mx - r);
-    const float by = my + r + 1.f, ay = (float)C.H - (my - r);
+    const float bx = mx + r + 1.f, ax = C.Wf - (mx - r);
+    const float by = my + r + 1.f, ay = C.Hf - (my - r);
     if (fabsf(bx) <= tol || fabsf(ax) <= tol || fabsf(by) <= tol || fabsf(ay) <= tol) return 2;
     return (bx > 0.f && ax > 0.f && by > 0.f && ay > 0.f) ? 1 : 0;
 }

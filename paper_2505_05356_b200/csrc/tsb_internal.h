@@ -22,6 +22,8 @@ struct CamK {
     double R[9], t[3];
     double lim_x, lim_y;
     double center[3];
+    // fp32 copies for the lean visibility bound (host-rounded once, not per Gaussian)
+    float Rf[9], fxf, fyf, cxf, cyf, limxf, limyf, Wf, Hf;
 };
 
 // Render options (splat.hpp:28-37) in the forms the kernels compare against.
@@ -33,6 +35,7 @@ struct OptK {
     int tiles_x, tiles_y;
     int sub;           // 16x16 raster blocks per tile edge = ceil(ts/16)
     float alpha_thr_f, floor_f, cut2_f, cov_eps_f;
+    float dilation_f, sigma_cutoff_f;
     int dist;          // distortion channel: accumulate the shifted depth moments
     int exact;         // TSB_CH_EXACT: every pixel goes to the fp64 fix-up
     float trel_flag;   // relative T error bound above which a pixel is recomposited (fix-up reason 8)

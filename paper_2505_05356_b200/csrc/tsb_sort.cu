@@ -57,6 +57,8 @@ __device__ __forceinline__ uint32_t key24(uint32_t k, uint32_t kmin, uint32_t sh
     return k == 0xffffffffu ? 0xffffffu : ((k - kmin) >> shift);
 }
 
+// TOP_ONLY (the prefix sort's selection): the top digit's histogram alone.
+template <bool TOP_ONLY>
 __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint32_t* __restrict__ keys, int n,
                                                             uint32_t* __restrict__ hist /* [3][256] */,
                                                             uint32_t* __restrict__ status, int status_words,
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint32_t* __re
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
 #pragma unroll
-            for (int p = 0; p < 3; ++p) {
+            for (int p = TOP_ONLY ? 2 : 0; p < 3; ++p) {
                 const uint32_t d = (kk[j] >> (8 * p)) & 255u;
                 const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
                 const bool v0 = __shfl_sync(0xffffffffu, valid[j], 0);
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint32_t* __re
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < 3 * 256; i += kSortThreads) {
+    for (int i = TOP_ONLY ? 2 * 256 + threadIdx.x : threadIdx.x; i < 3 * 256; i += kSortThreads) {
         uint32_t v = 0;
         for (int w = 0; w < kSortWarps; ++w) v += (&h[w][0][0])[i];
         if (v) atomicAdd(&hist[i], v);
@@ -285,7 +287,7 @@ int radix_sort24(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t*
     uint32_t* status = tickets + 4;
     cudaMemsetAsync(scratch, 0, sizeof(uint32_t) * (4 * 256 + 4), st);
     const int hgrid = max(1, min(148 * 2, (n / 4 + kSortThreads - 1) / kSortThreads));
-    k_sort_hist<<<hgrid, kSortThreads, 0, st>>>(keys_a, n, hist, status, 3 * 256 * tiles, range);
+    k_sort_hist<false><<<hgrid, kSortThreads, 0, st>>>(keys_a, n, hist, status, 3 * 256 * tiles, range);
     k_sort_scan<<<1, 96, 0, st>>>(hist);
     // 3 passes ping-pong a->b->a->b; finish in b, then the caller uses b
     k_onesweep<<<tiles, kSortThreads, 0, st>>>(keys_a, vals_a, keys_b, vals_b, n, 0, hist, status, tickets, range, nullptr);
@@ -484,7 +486,7 @@ int radix_sort24_prefix(const uint32_t* keys, uint32_t* keys_out, uint32_t* vals
     uint32_t* hist = scratch;
     cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 3 * 256, st);
     const int hgrid = max(1, min(148 * 2, (n / 4 + kSortThreads - 1) / kSortThreads));
-    k_sort_hist<<<hgrid, kSortThreads, 0, st>>>(keys, n, hist, nullptr, 0, range);
+    k_sort_hist<true><<<hgrid, kSortThreads, 0, st>>>(keys, n, hist, nullptr, 0, range);
     k_prefix_select<<<1, 32, 0, st>>>(hist, n, cap, n_visible, ps, n_bin, abort_word);
     k_prefix_compact<<<hgrid, kSortThreads, 0, st>>>(keys, n, range, ps, 3 * 256 * ctiles, tmp_keys, tmp_vals);
     uint32_t* hc = ps + kPrefHistC;
