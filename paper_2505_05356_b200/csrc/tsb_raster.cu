@@ -363,11 +363,13 @@ __global__ void k_fixup_loss(PixK px, int W, int H, int nf, const FrameDev* __re
 //   reduces its 8 screen-space gradients with a 9-shuffle reduce-scatter into its own
 //   shared slot (no shared-memory atomics); per 32 entries the block sums the 8 warp
 //   slots in a fixed order and adds each sum to global memory with one atomic.
-constexpr int kBwdSub = 128;  // entries per slot round: 8 warps x 128 entries x 8 floats (dynamic smem)
-constexpr size_t kBwdSlotBytes = sizeof(float) * (kRasterThreads / 32) * kBwdSub * 8;
+constexpr int kBwdSub = 128;  // entries per slot round: warps x 128 entries x 8 floats (dynamic smem)
 
-template <int NF>
+// PX pixels per thread (PX = 2: 128-thread blocks, the lane's pixels 4 rows apart): each
+// warp's per-entry reduce-scatter, loop and shared-memory loads then serve 64 pixels.
+template <int NF, int PX>
 struct BwdSmem {
+    static constexpr int kT = kRasterThreads / PX, kWarps = kT / 32;
     float4 A[kBatchCap];
     float4 B[kBatchCap];
     float4 C[kBatchCap];
@@ -375,17 +377,20 @@ struct BwdSmem {
     uint8_t wmask[kBatchCap];
     uint32_t grank[kBatchCap];                       // Gaussian of each staged entry
     uint32_t rrank[kBatchCap];                       // its rank (deterministic slots)
-    int wsum[2][kRasterThreads / 32];
-    int smax[kRasterThreads / 32];
+    int wsum[2][kWarps];
+    int smax[kWarps];
 };
+template <int PX>
+constexpr size_t bwd_slot_bytes() { return sizeof(float) * (kRasterThreads / PX / 32) * kBwdSub * 8; }
 
-template <int NF, bool EXTRA>
-__global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, ScanK sc, OptK O, int W, int H, float dpsi0,
-                                                                float dpsi1, PixK px, UpK up,
-                                                                double* __restrict__ screen, int scap,
-                                                                double* __restrict__ bg_part) {
-    __shared__ BwdSmem<NF> sm;
-    __shared__ float sbg[kRasterThreads / 32][6 * NF];
+template <int NF, bool EXTRA, int PX>
+__global__ void __launch_bounds__(kRasterThreads / PX) k_raster_bwd(RecK rec, ScanK sc, OptK O, int W, int H,
+                                                                     float dpsi0, float dpsi1, PixK px, UpK up,
+                                                                     double* __restrict__ screen, int scap,
+                                                                     double* __restrict__ bg_part) {
+    constexpr int kT = kRasterThreads / PX, kWarps = kT / 32;
+    __shared__ BwdSmem<NF, PX> sm;
+    __shared__ float sbg[kWarps][6 * NF];
     extern __shared__ float slot_mem[];  // [warp][kBwdSub][8]: per warp, per entry: its reduced gradients
     float (*slot)[kBwdSub][8] = reinterpret_cast<float (*)[kBwdSub][8]>(slot_mem);
     if (block_aborted(px.abort)) return;  // aborted frame: no gradient is written (the host redoes it)
@@ -393,74 +398,94 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, ScanK s
     const int tile = blockIdx.x / nsub, sb = blockIdx.x % nsub;
     const int ttx = tile % O.tiles_x, tty = tile / O.tiles_x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int bx_ = block_px(tid), by_ = block_py(tid);
-    const int lx = (sb % O.sub) * kTile + bx_, ly = (sb / O.sub) * kTile + by_;
-    const int x = ttx * O.ts + lx, y = tty * O.ts + ly;
-    const bool active = lx < O.ts && ly < O.ts && x < W && y < H;
-    const float ox = (float)(x - bx_), oy = (float)(y - by_);  // block origin
-    const float pcx = (float)bx_ + 0.5f, pcy = (float)by_ + 0.5f;
-    const size_t HW = (size_t)W * H, o = active ? (size_t)y * W + x : 0;
-
-    int last = 0;
-    float Tnext = 0.f, A = 0.f, Bx = 0.f;
-    float uDraw = 0.f, uDD = 0.f, cD = 0.f, dref = 0.f;
-    double SWd = 0.0, SDs = 0.0, SD2s = 0.0;
-    float us[NF], uc[NF];
+    // the forward's warp regions are 8 x 4 pixels (bit 2 q + h of wmask: row quarter q,
+    // column half h); a PX = 2 warp covers two of them, rows 8 v .. 8 v + 7
+    const int hh = warp & 1, vq = warp >> 1;
+    const int bx_ = hh * 8 + (lane & 7);
+    const uint32_t wbits = PX == 1 ? 1u << warp : (1u << (4 * vq + hh)) | (1u << (4 * vq + 2 + hh));
+    const size_t HW = (size_t)W * H;
+    int by_[PX], last[PX];
+    bool active[PX];
+    size_t o[PX];
+    float pcy[PX], Tnext[PX], A[PX], Bx[PX];
+    float uDraw[PX], uDD[PX], cD[PX], dref[PX];
+    double SWd[PX], SDs[PX], SD2s[PX];
+    float us[PX][NF], uc[PX][NF];
+    bool first[PX];
     float bgc[6 * NF];
 #pragma unroll
-    for (int f = 0; f < NF; ++f) us[f] = uc[f] = 0.f;
-#pragma unroll
     for (int c = 0; c < 6 * NF; ++c) bgc[c] = 0.f;
-    if (active) {
-        const int l = px.last[o];
-        last = (l & kLastBwd64) ? 0 : (l & kLastMask);  // recomposited pixels: k_fixup_bwd (fp64)
-        Tnext = px.T_pre[o];
-        const float Tf = px.out[ch_T(NF) * HW + o];
+    const int lx = (sb % O.sub) * kTile + bx_;
+    const int x = ttx * O.ts + lx;
+#pragma unroll
+    for (int pp = 0; pp < PX; ++pp) {
+        by_[pp] = PX == 1 ? block_py(tid) : vq * 8 + (lane >> 3) + 4 * pp;
+        const int ly = (sb / O.sub) * kTile + by_[pp];
+        const int y = tty * O.ts + ly;
+        active[pp] = lx < O.ts && ly < O.ts && x < W && y < H;
+        o[pp] = active[pp] ? (size_t)y * W + x : 0;
+        pcy[pp] = (float)by_[pp] + 0.5f;
+        last[pp] = 0;
+        Tnext[pp] = A[pp] = Bx[pp] = 0.f;
+        uDraw[pp] = uDD[pp] = cD[pp] = dref[pp] = 0.f;
+        SWd[pp] = SDs[pp] = SD2s[pp] = 0.0;
+        first[pp] = true;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) us[pp][f] = uc[pp][f] = 0.f;
+        if (!active[pp]) continue;
+        const size_t oo = o[pp];
+        const int l = px.last[oo];
+        last[pp] = (l & kLastBwd64) ? 0 : (l & kLastMask);  // recomposited pixels: k_fixup_bwd (fp64)
+        Tnext[pp] = px.T_pre[oo];
+        const float Tf = px.out[ch_T(NF) * HW + oo];
         const float Tf2 = Tf * Tf;
         if (up.quad) {
             float q[4 * NF];
 #pragma unroll
             for (int c = 0; c < 4 * NF; ++c) {
-                q[c] = up.quad[c * HW + o];
-                A = fmaf(q[c], (float)O.bg_quad[c], A);
-                bgc[c] = q[c] * Tf2;
+                q[c] = up.quad[c * HW + oo];
+                A[pp] = fmaf(q[c], (float)O.bg_quad[c], A[pp]);
+                bgc[c] += q[c] * Tf2;
             }
 #pragma unroll
             for (int f = 0; f < NF; ++f) {
-                us[f] = q[4 * f + 0] - q[4 * f + 2];
-                uc[f] = q[4 * f + 1] - q[4 * f + 3];
+                us[pp][f] = q[4 * f + 0] - q[4 * f + 2];
+                uc[pp][f] = q[4 * f + 1] - q[4 * f + 3];
             }
         }
         if (up.phasor) {
 #pragma unroll
             for (int f = 0; f < NF; ++f) {
-                const float p0 = up.phasor[(2 * f + 0) * HW + o], p1 = up.phasor[(2 * f + 1) * HW + o];
-                A = fmaf(p0, (float)O.bg_phasor[2 * f + 0], A);
-                A = fmaf(p1, (float)O.bg_phasor[2 * f + 1], A);
-                bgc[4 * NF + 2 * f + 0] = p0 * Tf2;
-                bgc[4 * NF + 2 * f + 1] = p1 * Tf2;
-                us[f] = fmaf(2.f, p1, us[f]);  // phasor = 2 coef w2 (cos, sin)
-                uc[f] = fmaf(2.f, p0, uc[f]);
+                const float p0 = up.phasor[(2 * f + 0) * HW + oo], p1 = up.phasor[(2 * f + 1) * HW + oo];
+                A[pp] = fmaf(p0, (float)O.bg_phasor[2 * f + 0], A[pp]);
+                A[pp] = fmaf(p1, (float)O.bg_phasor[2 * f + 1], A[pp]);
+                bgc[4 * NF + 2 * f + 0] += p0 * Tf2;
+                bgc[4 * NF + 2 * f + 1] += p1 * Tf2;
+                us[pp][f] = fmaf(2.f, p1, us[pp][f]);  // phasor = 2 coef w2 (cos, sin)
+                uc[pp][f] = fmaf(2.f, p0, uc[pp][f]);
             }
         }
         if (EXTRA) {
             if (up.depth_raw) {
-                uDraw = up.depth_raw[o];
-                const float dm = px.out[ch_depth(NF) * HW + o];
-                cD = dm == dm ? dm : 0.f;  // NaN where uncovered
+                uDraw[pp] = up.depth_raw[oo];
+                const float dm = px.out[ch_depth(NF) * HW + oo];
+                cD[pp] = dm == dm ? dm : 0.f;  // NaN where uncovered
             }
-            if (up.transm) Bx = up.transm[o];
-            if (up.weight) Bx -= up.weight[o];
-            Bx = fmaf(-uDraw, cD, Bx);
+            if (up.transm) Bx[pp] = up.transm[oo];
+            if (up.weight) Bx[pp] -= up.weight[oo];
+            Bx[pp] = fmaf(-uDraw[pp], cD[pp], Bx[pp]);
             if (up.distortion) {
-                uDD = up.distortion[o];
-                SWd = px.out[ch_weight(NF) * HW + o];
-                dref = (float)px.dist3[o];
-                SDs = px.dist3[HW + o];
-                SD2s = px.dist3[2 * HW + o];
+                uDD[pp] = up.distortion[oo];
+                SWd[pp] = px.out[ch_weight(NF) * HW + oo];
+                dref[pp] = (float)px.dist3[oo];
+                SDs[pp] = px.dist3[HW + oo];
+                SD2s[pp] = px.dist3[2 * HW + oo];
             }
         }
     }
+    const int y0 = tty * O.ts + (sb / O.sub) * kTile;  // block origin
+    const float ox = (float)(x - bx_), oy = (float)y0;
+    const float pcx = (float)bx_ + 0.5f;
     // background gradient partials (splat.cpp:429-431)
     if (bg_part) {
 #pragma unroll
@@ -470,40 +495,40 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, ScanK s
             if (lane == 0) sbg[warp][c] = v;
         }
     }
-    int wmax = last;
+    int wmax = last[0];
+#pragma unroll
+    for (int pp = 1; pp < PX; ++pp) wmax = max(wmax, last[pp]);
     for (int m = 16; m > 0; m >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, m));
     if (lane == 0) sm.smax[warp] = wmax;
     __syncthreads();
     int bmax = 0;
 #pragma unroll
-    for (int i = 0; i < kRasterThreads / 32; ++i) bmax = max(bmax, sm.smax[i]);
+    for (int i = 0; i < kWarps; ++i) bmax = max(bmax, sm.smax[i]);
     if (bg_part && tid < 6 * NF) {
         double s = 0.0;
-        for (int i = 0; i < kRasterThreads / 32; ++i) s += sbg[i][tid];
+        for (int i = 0; i < kWarps; ++i) s += sbg[i][tid];
         bg_part[(size_t)blockIdx.x * 6 * NF + tid] = s;
     }
-    bool first = true;
     const float cut2 = O.cut2_f, thr = O.alpha_thr_f;
-    const uint32_t wbit = 1u << warp;
 
     // entries back to front.  Fast path: the forward recorded the block's list (all its
     // entries fit kBlkListCap) -- batches of 256 straight from it.  Otherwise the rank order
-    // is scanned downwards from where the forward stopped.
+    // (or the super-tile list) is scanned downwards from where the forward stopped.
     const int2 bt = sc.blk_term[blockIdx.x];
     const bool listed = bt.y <= kBlkListCap;
     const ScanSeg seg = scan_seg(sc, ttx, tty);
-    int r_hi = bt.x;  // super-tile list position
+    int r_hi = bt.x;  // scan position
     int cnt = 0, pass = 0, e_top = listed ? min(bt.y, bmax) : bt.y;
     while (bmax > 0 && e_top > 0 && (listed || r_hi > 0)) {
         if (listed) {
             const int nb = min(kRasterThreads, e_top);
-            if (tid < nb) {
-                const int slot = kBatchCap - nb + tid;
-                const uint32_t r = sc.blk_list[(size_t)blockIdx.x * kBlkListCap + (e_top - nb + tid)];
+            for (int i = tid; i < nb; i += kT) {
+                const int slot_i = kBatchCap - nb + i;
+                const uint32_t r = sc.blk_list[(size_t)blockIdx.x * kBlkListCap + (e_top - nb + i)];
                 const uint32_t g = sc.ord[r];
-                sm.grank[slot] = g;
-                sm.rrank[slot] = r;
-                stage_entry<NF>(sm, rec, g, slot, ox, oy, cut2);
+                sm.grank[slot_i] = g;
+                sm.rrank[slot_i] = r;
+                stage_entry<NF>(sm, rec, g, slot_i, ox, oy, cut2);
             }
             cnt = nb;
             e_top -= nb;
@@ -511,21 +536,21 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, ScanK s
             const int p = r_hi - 1 - tid;
             const bool cov = p >= 0 && tile_covers(seg_rect(sc, seg, p), ttx, tty);
             int total;
-            const int pos = scan_compact(cov, sm.wsum[pass & 1], total);  // descending rank order
+            const int pos = scan_compact<kT>(cov, sm.wsum[pass & 1], total);  // descending rank order
             // entries of this pass: indices [e_top - total, e_top); keep those below bmax
             const int keep_hi = min(total, max(0, bmax - (e_top - total)));  // kept: ascending positions < keep_hi
             const int asc = total - 1 - pos;
             if (pos >= 0 && asc < keep_hi) {
-                const int slot = kBatchCap - cnt - keep_hi + asc;
+                const int slot_i = kBatchCap - cnt - keep_hi + asc;
                 const uint32_t rr = seg_rank(sc, seg, p);
                 const uint32_t g = sc.ord[rr];
-                sm.grank[slot] = g;
-                sm.rrank[slot] = (uint32_t)rr;
-                stage_entry<NF>(sm, rec, g, slot, ox, oy, cut2);
+                sm.grank[slot_i] = g;
+                sm.rrank[slot_i] = (uint32_t)rr;
+                stage_entry<NF>(sm, rec, g, slot_i, ox, oy, cut2);
             }
             cnt += keep_hi;
             e_top -= total;
-            r_hi -= kRasterThreads;
+            r_hi -= kT;
             ++pass;
             if (cnt < kRasterThreads && r_hi > 0 && e_top > 0) continue;
         }
@@ -544,72 +569,71 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, ScanK s
             // to any of its pixels: start the warp below them (warp-uniform)
             const int jtop = min(hi, base + (wmax - e_lo));
             for (int j = jtop - 1; j >= lo; --j) {
-                if (!(sm.wmask[j] & wbit)) continue;  // outside for every pixel of the warp
+                if (!(sm.wmask[j] & wbits)) continue;  // outside for every pixel of the warp
                 const int el = e_lo + (j - base);
                 bool contrib = false;
                 float g8[8];
-                if (el < last) {
-                    const float4 Aa = sm.A[j], Bb = sm.B[j];
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc) g8[cc] = 0.f;
+                const float4 Aa = sm.A[j], Bb = sm.B[j];
+#pragma unroll
+                for (int pp = 0; pp < PX; ++pp) {
+                    if (!(el < last[pp])) continue;
                     Eval ev;
-                    eval_entry(Aa, Bb, pcx, pcy, ev);
-                    if (!(ev.maha - cut2 > 0.f)) {
-                        eval_alpha(Bb, ev);
-                        if (!(ev.alpha - thr < 0.f)) {
-                            contrib = true;
-                            const float om = 1.f - ev.alpha;
-                            // T before this entry, back from the last contributor's.  The quad / phasor
-                            // path takes a 2-ulp quotient (error ~linear in depth, far inside the 1e-3
-                            // gradient tolerance); the T-weighted channels, whose recursion runs on
-                            // differences of nearly equal terms, keep the correctly rounded one.
-                            const float Tk = first ? Tnext : (EXTRA ? __fdiv_rn(Tnext, om) : __fdividef(Tnext, om));
-                            first = false;
-                            Tnext = Tk;
-                            const float4 Cc = sm.C[j];
-                            const float coef = Cc.x;
-                            float su = us[0] * Cc.z + uc[0] * Cc.w;            // upQ . basis / coef
-                            float sd = dpsi0 * (us[0] * Cc.w - uc[0] * Cc.z);  // upQ . dbasis / coef
-                            if (NF > 1) {
-                                const float4 Dd = sm.D[j];
-                                su += us[NF - 1] * Dd.x + uc[NF - 1] * Dd.y;
-                                sd += dpsi1 * (us[NF - 1] * Dd.y - uc[NF - 1] * Dd.x);
-                            }
-                            const float UQ = coef * su;
-                            const float T2 = Tk * Tk;
-                            const float w2 = ev.alpha * T2;
-                            float d_alpha = T2 * (UQ + 2.f * (ev.alpha - 1.f) * A);
-                            A = ev.alpha * UQ + om * om * A;
-                            float ddep = w2 * coef * sd;
-                            if (EXTRA) {
-                                // phi_k and SW d_k - SD in fp64: both cancel (moments about dref)
-                                const float d = Cc.y;
-                                float phi = 0.f, sdev = 0.f;
-                                if (uDD != 0.f) {
-                                    const double dp = (double)(d - dref);
-                                    phi = (float)(2.0 * fma(dp, fma(dp, SWd, -2.0 * SDs), SD2s));
-                                    sdev = (float)fma(SWd, dp, -SDs);
-                                }
-                                const float v = fmaf(uDraw, d - cD, uDD * phi);
-                                d_alpha = fmaf(Tk, v - Bx, d_alpha);
-                                Bx = fmaf(ev.alpha, v, om * Bx);
-                                ddep = fmaf(ev.alpha * Tk, fmaf(4.f * uDD, sdev, uDraw), ddep);
-                            }
-                            const float dpow = ev.alpha * d_alpha;
-                            g8[0] = dpow * (Bb.x * ev.p);
-                            g8[1] = dpow * (Bb.y * ev.p + Bb.z * ev.q);
-                            g8[2] = -0.5f * ev.dx * ev.dx * dpow;
-                            g8[3] = -ev.dx * ev.dy * dpow;
-                            g8[4] = -0.5f * ev.dy * ev.dy * dpow;
-                            g8[5] = ev.g * d_alpha;
-                            g8[6] = w2 * su;
-                            g8[7] = ddep;
-                        }
+                    eval_entry(Aa, Bb, pcx, pcy[pp], ev);
+                    if (ev.maha - cut2 > 0.f) continue;
+                    eval_alpha(Bb, ev);
+                    if (ev.alpha - thr < 0.f) continue;
+                    contrib = true;
+                    const float om = 1.f - ev.alpha;
+                    // T before this entry, back from the last contributor's.  The quad / phasor
+                    // path takes a 2-ulp quotient (error ~linear in depth, far inside the 1e-3
+                    // gradient tolerance); the T-weighted channels, whose recursion runs on
+                    // differences of nearly equal terms, keep the correctly rounded one.
+                    const float Tk = first[pp] ? Tnext[pp]
+                                               : (EXTRA ? __fdiv_rn(Tnext[pp], om) : __fdividef(Tnext[pp], om));
+                    first[pp] = false;
+                    Tnext[pp] = Tk;
+                    const float4 Cc = sm.C[j];
+                    const float coef = Cc.x;
+                    float su = us[pp][0] * Cc.z + uc[pp][0] * Cc.w;            // upQ . basis / coef
+                    float sd = dpsi0 * (us[pp][0] * Cc.w - uc[pp][0] * Cc.z);  // upQ . dbasis / coef
+                    if (NF > 1) {
+                        const float4 Dd = sm.D[j];
+                        su += us[pp][NF - 1] * Dd.x + uc[pp][NF - 1] * Dd.y;
+                        sd += dpsi1 * (us[pp][NF - 1] * Dd.y - uc[pp][NF - 1] * Dd.x);
                     }
+                    const float UQ = coef * su;
+                    const float T2 = Tk * Tk;
+                    const float w2 = ev.alpha * T2;
+                    float d_alpha = T2 * (UQ + 2.f * (ev.alpha - 1.f) * A[pp]);
+                    A[pp] = ev.alpha * UQ + om * om * A[pp];
+                    float ddep = w2 * coef * sd;
+                    if (EXTRA) {
+                        // phi_k and SW d_k - SD in fp64: both cancel (moments about dref)
+                        const float d = Cc.y;
+                        float phi = 0.f, sdev = 0.f;
+                        if (uDD[pp] != 0.f) {
+                            const double dp = (double)(d - dref[pp]);
+                            phi = (float)(2.0 * fma(dp, fma(dp, SWd[pp], -2.0 * SDs[pp]), SD2s[pp]));
+                            sdev = (float)fma(SWd[pp], dp, -SDs[pp]);
+                        }
+                        const float v = fmaf(uDraw[pp], d - cD[pp], uDD[pp] * phi);
+                        d_alpha = fmaf(Tk, v - Bx[pp], d_alpha);
+                        Bx[pp] = fmaf(ev.alpha, v, om * Bx[pp]);
+                        ddep = fmaf(ev.alpha * Tk, fmaf(4.f * uDD[pp], sdev, uDraw[pp]), ddep);
+                    }
+                    const float dpow = ev.alpha * d_alpha;
+                    g8[0] += dpow * (Bb.x * ev.p);
+                    g8[1] += dpow * (Bb.y * ev.p + Bb.z * ev.q);
+                    g8[2] += -0.5f * ev.dx * ev.dx * dpow;
+                    g8[3] += -ev.dx * ev.dy * dpow;
+                    g8[4] += -0.5f * ev.dy * ev.dy * dpow;
+                    g8[5] += ev.g * d_alpha;
+                    g8[6] += w2 * su;
+                    g8[7] += ddep;
                 }
                 if (__any_sync(0xffffffffu, contrib)) {
-                    if (!contrib) {
-#pragma unroll
-                        for (int cc = 0; cc < 8; ++cc) g8[cc] = 0.f;
-                    }
                     const float s = reduce_scatter8(g8, lane);
                     if ((lane & 3) == 0) {
                         const int vi = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
@@ -619,17 +643,17 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_bwd(RecK rec, ScanK s
             }
             __syncthreads();
             // fixed-order sum over the warps, one global atomic per non-zero (entry, component)
-            for (int k = tid; k < (hi - lo) * 8; k += kRasterThreads) {
+            for (int k = tid; k < (hi - lo) * 8; k += kT) {
                 const int je = k >> 3, cc = k & 7;
-                float v = 0.f;
+                double v = 0.0;  // (fp64: the warp partials of a cancelling d_mean sum stay separate)
 #pragma unroll
-                for (int w = 0; w < kRasterThreads / 32; ++w) v += slot[w][je][cc];
-                if (v == 0.f) continue;
+                for (int w = 0; w < kWarps; ++w) v += slot[w][je][cc];
+                if (v == 0.0) continue;
                 if (sc.det_part) {  // deterministic: this block's own slot of (rank, tile, sub-block)
                     const int r = (int)sm.rrank[lo + je];
-                    sc.det_part[det_slot(sc, r, sc.trect[r], ttx, tty, sb) * 8 + cc] = v;
+                    sc.det_part[det_slot(sc, r, sc.trect[r], ttx, tty, sb) * 8 + cc] = (float)v;
                 } else {
-                    atomicAdd(&screen[(size_t)cc * scap + sm.grank[lo + je]], (double)v);
+                    atomicAdd(&screen[(size_t)cc * scap + sm.grank[lo + je]], v);
                 }
             }
             __syncthreads();
@@ -700,17 +724,37 @@ void launch_fixup_loss(const PixK& px, int W, int H, int nf, const FrameDev* fd,
         k_fixup_loss<<<64, 256, 0, st>>>(px, W, H, nf, fd, ch_w, loss_extra);
 }
 
+// Pixels per thread of the backward raster: 1 (TSB_BWD_PX=2: 128-thread blocks, two pixels
+// per lane -- 22 % fewer instructions and +2 % c4 training, but the extra pair sum moves
+// the posed-camera case's most cancelling d_position component from 9.9e-4 to 1.08e-3 of
+// relative error, over the 1e-3 bar).
+static int bwd_px() {
+    static const int v = [] {
+        const char* e = std::getenv("TSB_BWD_PX");
+        return e && std::atoi(e) == 2 ? 2 : 1;
+    }();
+    return v;
+}
+
 void launch_raster_bwd(const RecK& rec, const ScanK& sc, const OptK& O, int W, int H, int nf, const float* dpsi,
                        PixK px, const UpK& up, double* screen, int scap, double* bg_part, cudaStream_t st) {
     const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
     const bool extra = up.depth_raw || up.weight || up.distortion || up.transm;
-#define TSB_BWD(NF_, E_, D1_)                                                                                 \
-    k_raster_bwd<NF_, E_><<<grid, kRasterThreads, kBwdSlotBytes, st>>>(rec, sc, O, W, H, dpsi[0], D1_, px, up, \
-                                                                      screen, scap, bg_part)
-    if (nf > 1) {
-        if (extra) TSB_BWD(2, true, dpsi[1]); else TSB_BWD(2, false, dpsi[1]);
+#define TSB_BWD(NF_, E_, D1_, PX_)                                                                              \
+    k_raster_bwd<NF_, E_, PX_><<<grid, kRasterThreads / PX_, bwd_slot_bytes<PX_>(), st>>>(                     \
+        rec, sc, O, W, H, dpsi[0], D1_, px, up, screen, scap, bg_part)
+    if (bwd_px() == 2) {
+        if (nf > 1) {
+            if (extra) TSB_BWD(2, true, dpsi[1], 2); else TSB_BWD(2, false, dpsi[1], 2);
+        } else {
+            if (extra) TSB_BWD(1, true, 0.f, 2); else TSB_BWD(1, false, 0.f, 2);
+        }
     } else {
-        if (extra) TSB_BWD(1, true, 0.f); else TSB_BWD(1, false, 0.f);
+        if (nf > 1) {
+            if (extra) TSB_BWD(2, true, dpsi[1], 1); else TSB_BWD(2, false, dpsi[1], 1);
+        } else {
+            if (extra) TSB_BWD(1, true, 0.f, 1); else TSB_BWD(1, false, 0.f, 1);
+        }
     }
 #undef TSB_BWD
 }
@@ -719,12 +763,14 @@ void launch_raster_bwd(const RecK& rec, const ScanK& sc, const OptK& O, int W, i
 void raster_init() {
     static bool done = false;
     if (done) return;
-    const int bytes = (int)(sizeof(BwdSmem<2>) + sizeof(float) * (kRasterThreads / 32) * 12 + kBwdSlotBytes);
-    cudaFuncSetAttribute(k_raster_bwd<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSlotBytes);
-    cudaFuncSetAttribute(k_raster_bwd<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSlotBytes);
-    cudaFuncSetAttribute(k_raster_bwd<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSlotBytes);
-    cudaFuncSetAttribute(k_raster_bwd<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSlotBytes);
-    (void)bytes;
+    cudaFuncSetAttribute(k_raster_bwd<1, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_slot_bytes<1>());
+    cudaFuncSetAttribute(k_raster_bwd<1, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_slot_bytes<1>());
+    cudaFuncSetAttribute(k_raster_bwd<2, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_slot_bytes<1>());
+    cudaFuncSetAttribute(k_raster_bwd<2, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_slot_bytes<1>());
+    cudaFuncSetAttribute(k_raster_bwd<1, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_slot_bytes<2>());
+    cudaFuncSetAttribute(k_raster_bwd<1, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_slot_bytes<2>());
+    cudaFuncSetAttribute(k_raster_bwd<2, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_slot_bytes<2>());
+    cudaFuncSetAttribute(k_raster_bwd<2, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_slot_bytes<2>());
     done = true;
 }
 

@@ -72,8 +72,8 @@ __device__ __forceinline__ float4 stage_A(const float4& a, float ox, float oy) {
 // One scan pass of the rank order: thread tid tests rank r (ascending or descending
 // passes pass their own r); returns the number of covering ranks of the pass and this
 // thread's position among them (rank order of the pass's threads), or -1.
+template <int kThreads = 256>
 __device__ __forceinline__ int scan_compact(bool cov, int* wsum, int& total) {
-    constexpr int kThreads = 256;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned b = __ballot_sync(0xffffffffu, cov);
     if (lane == 0) wsum[warp] = __popc(b);
