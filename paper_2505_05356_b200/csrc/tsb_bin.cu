@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(kSlChunk) k_order_ranks(const uint32_t* __rest
     }
     __syncthreads();
     for (int s = tid; s < sk.nsup; s += kSlChunk) sk.hist[(size_t)s * sk.hist_stride + blockIdx.x] = cnt[s];
+    if (sk.work && blockIdx.x == 0 && tid == 0) atomicAdd(&sk.work[2], (unsigned long long)V);  // profiling
 }
 
 // Row s of the histogram (one column per k_order_ranks block) -> exclusive offsets within
@@ -220,10 +221,7 @@ __global__ void __launch_bounds__(kSlChunk) k_sl_emit(const int32_t* __restrict_
         sk.off[sk.nsup] = total;
         *sk.total = (int32_t)min(total, 0x7fffffffu);
         if (total > (uint32_t)sk.cap) atomicOr(abort, 1);  // the lists need more storage: redo
-        if (sk.work) {
-            atomicAdd(&sk.work[2], (unsigned long long)V);
-            atomicAdd(&sk.work[3], (unsigned long long)total);
-        }
+        if (sk.work) atomicAdd(&sk.work[3], (unsigned long long)total);
     }
     if (total > (uint32_t)sk.cap) return;  // (block-uniform)
     int c0, c1;
