@@ -485,6 +485,64 @@ def bench_train_c4(args, dist, tsb, synthetic, ctx):
     return res
 
 
+def bench_train_c2(args, dist, tsb, synthetic, ctx):
+    """c2 (BASELINE config 2): 500 k Gaussians (9 keyframes), 640x576, 30 + 60 MHz (8 raw
+    channels), 8 frames per iteration against a target with a rotating rod, Adam on all six
+    groups with per-group learning rates, densify statistic -- iterations/s through the same
+    public trainer (frames split over ranks)."""
+    import torch
+    cfg = synthetic.config("c2")
+    g, tg = cfg.scene, cfg.target
+    cam, opts = cfg.camera, tsb.RenderOptions()
+    scene = tsb.GaussianScene(ctx, g.n, g.n_keyframes, cfg.tof)
+    scene.set_params(g.position, g.log_scale, g.rotation, g.opacity_logit, g.reflectivity_dc, g.motion)
+    tscene = tsb.GaussianScene(ctx, tg.n, tg.n_keyframes, cfg.tof)
+    tscene.set_params(tg.position, tg.log_scale, tg.rotation, tg.opacity_logit, tg.reflectivity_dc, tg.motion)
+    rp = tsb.RenderPass(ctx)
+    my_frames = cfg.frames[dist.rank::dist.world]
+    H, W = cam.height, cam.width
+    nch = 4 * len(cfg.tof.frequencies)
+    targets = torch.empty((max(len(my_frames), 1), nch, H, W), dtype=torch.float32, device=f"cuda:{dist.local}")
+    for i, fr in enumerate(my_frames):
+        rp.prepare(tscene, cam, opts, fr).forward()
+        targets[i].copy_(torch.from_numpy(rp.download(tsb._abi.OUT_QUAD, shape=(nch, H, W))))
+    tscene.close()
+    torch.cuda.synchronize()
+    comm = None
+    if dist.world > 1:
+        uid = dist.bcast_bytes(tsb.Comm.unique_id() if dist.rank == 0 else b"")
+        comm = tsb.Comm(ctx, uid, dist.world, dist.rank)
+    from paper_2505_05356_b200.parallel import FrameShardedTrainer, shard_indices
+    lr = tsb.LrTable(position=2e-3, log_scale=5e-3, rotation=1e-3, opacity=0.05, reflectivity=1.6e-4, motion=3e-4,
+                     color=1e-3)
+    trainer = FrameShardedTrainer(ctx, scene, cam, opts, lr=lr, comm=comm, rank=dist.rank, world=dist.world,
+                                  passes=8)
+    mine = {f: j for j, f in enumerate(shard_indices(len(cfg.frames), dist.rank, dist.world))}
+
+    def it():
+        trainer.step(cfg.frames, lambda i: targets[mine[i]].data_ptr())
+
+    for _ in range(3):
+        it()
+    ctx.synchronize()
+    timer = StreamTimer(ctx)
+    dist.barrier()
+    ctx.synchronize()
+    steps = 10
+    timer.start()
+    for _ in range(steps):
+        it()
+    ctx.join()
+    ms = dist.max(timer.stop_ms())
+    if comm:
+        comm.close()
+    return {"config": "c2", "n_gaussians": g.n, "image": f"{W}x{H}", "frequencies_hz": list(cfg.tof.frequencies),
+            "frames_per_iter": len(cfg.frames), "iters_per_s": round(steps / (ms / 1e3), 3),
+            "ms_per_iter": round(ms / steps, 3), "frames_per_s": round(steps * len(cfg.frames) / (ms / 1e3), 1),
+            "note": "each iteration: 8 frames forward_loss + backward (both frequencies), Adam on all six groups "
+                    "(per-group lr), densify statistic; the reference runs 200 such iterations"}
+
+
 def bench_deform(args, dist, tsb, synthetic, ctx):
     """the reference's DeformNet (4 x 128 ReLU MLP, l_x = l_t = 10) on the
     tcgen05 tensor cores for the c4 scene's 2M canonical positions: offsets into a keyframe
@@ -640,6 +698,7 @@ def main():
     train = None
     if not args.no_train:
         train = bench_train_c4(args, dist, tsb, synthetic, ctx)
+        train["c2"] = bench_train_c2(args, dist, tsb, synthetic, ctx)
     deform = None
     if not args.no_deform and dist.rank == 0:
         deform = bench_deform(args, dist, tsb, synthetic, ctx)
