@@ -2665,6 +2665,8 @@ struct tsb_deform {
         int64_t cap = 0, n = 0;
         float* X = nullptr;            // [cap][din] encodings (column c*ex = scaled position)
         std::vector<float*> H;         // [L][cap][width] post-ReLU activations
+        std::vector<uint32_t*> Hb;     // [L][cap][width / 32] their ReLU gates as bits (fused forward only)
+        bool bits_valid = false;
         bool valid = false;
     } slots[TSB_DEFORM_SLOTS];
     int64_t dcap = 0;
@@ -2687,12 +2689,16 @@ int deform_slot_alloc(tsb_deform* d, tsb_deform::Slot& s, int64_t n) {
     if (n <= s.cap) return TSB_OK;
     dev_free(s.X);
     for (float*& h : s.H) dev_free(h);
+    for (uint32_t*& h : s.Hb) dev_free(h);
     s.H.assign(d->L, nullptr);
+    s.Hb.assign(d->L, nullptr);
     s.cap = 0;
     int rc;
     if ((rc = dev_alloc(&s.X, (size_t)n * d->din))) return rc;
-    for (int l = 0; l < d->L; ++l)
+    for (int l = 0; l < d->L; ++l) {
         if ((rc = dev_alloc(&s.H[l], (size_t)n * d->width))) return rc;
+        if (d->width % 32 == 0 && (rc = dev_alloc(&s.Hb[l], (size_t)n * (d->width / 32)))) return rc;
+    }
     s.cap = n;
     return TSB_OK;
 }
@@ -2707,7 +2713,7 @@ int deform_scratch(tsb_deform* d, int64_t n) {
             return rc;
         d->dcap = n;
     }
-    const int64_t need = (int64_t)kDeformMaxSlices * 128 * 128;
+    const int64_t need = (int64_t)kDeformMaxSlices * 128 * 128 + (int64_t)kDeformMaxSlices * 128;  // + row sums
     if (need > d->part_cap) {
         dev_free(d->part);
         int rc;
@@ -2773,7 +2779,10 @@ int deform_forward(tsb_deform* d, int slot, const float* pos, int64_t pos_stride
         a.params = d->params;
         a.X = s.X;
         a.ldx = d->din;
-        for (int l = 0; l < d->L; ++l) a.H[l] = s.H[l];
+        for (int l = 0; l < d->L; ++l) {
+            a.H[l] = s.H[l];
+            a.Hbits[l] = d->width % 32 == 0 ? s.Hb[l] : nullptr;
+        }
         a.ldh = d->width;
         a.out = out;
         a.out_stride = out_stride;
@@ -2782,6 +2791,7 @@ int deform_forward(tsb_deform* d, int slot, const float* pos, int64_t pos_stride
         TSB_CHECK_LAUNCH();
         s.n = n;
         s.valid = true;
+        s.bits_valid = d->width % 32 == 0;
         return TSB_OK;
     }
     launch_deform_encode(pos, pos_stride, n, 1.0 / d->cfg.coord_scale, d->cfg.l_x, te, s.X, d->din, st);
@@ -2806,6 +2816,7 @@ int deform_forward(tsb_deform* d, int slot, const float* pos, int64_t pos_stride
     }
     s.n = n;
     s.valid = true;
+    s.bits_valid = false;  // (the layer-by-layer forward writes no gate bits)
     return TSB_OK;
 }
 
@@ -2836,9 +2847,11 @@ int deform_backward(tsb_deform* d, int slot, const float* d_out, int64_t dstride
         g.B = below; g.b_n = 1; g.b_k = K;
         g.M = O; g.N = K; g.K = (int)n; g.k_per_slice = kps;
         g.C = d->part; g.ldc = K; g.slice_stride = (int64_t)O * K;
+        float* rowsum = d->part + (int64_t)kDeformMaxSlices * 128 * 128;  // db_l = column sums of delta (fused)
+        g.rowsum = rowsum;
         if ((rc = deform_gemm(d, g, used))) return rc;
         launch_reduce_slices(d->part, used, (int64_t)O * K, (int64_t)O * K, d->grads + d->w_off[l], true, st);
-        launch_colsum(delta, dld, n, O, d->grads + d->b_off[l], st);
+        launch_reduce_slices(rowsum, used, O, O, d->grads + d->b_off[l], true, st);
         d->ctx->launches += 2;
         if (l == 0 && !d_pos) break;
         // d_below = delta W_l (gated by the ReLU of the layer below, or the input gradient)
@@ -2849,7 +2862,10 @@ int deform_backward(tsb_deform* d, int slot, const float* d_out, int64_t dstride
         h.B = d->params + d->w_off[l]; h.b_n = 1; h.b_k = K;
         h.M = (int)n; h.N = K; h.K = O; h.k_per_slice = ((O + 31) / 32) * 32;
         h.C = out; h.ldc = K;
-        if (l > 0) {
+        if (l > 0 && s.bits_valid) {  // the gate of the layer below, 1 bit per unit
+            h.maskbits = s.Hb[l - 1];
+            h.ldmaskbits = d->width / 32;
+        } else if (l > 0) {
             h.mask = s.H[l - 1];
             h.ldmask = d->width;
         }
@@ -2942,6 +2958,7 @@ void tsb_deform_destroy(tsb_deform* d) {
     for (auto& s : d->slots) {
         dev_free(s.X);
         for (float*& h : s.H) dev_free(h);
+        for (uint32_t*& h : s.Hb) dev_free(h);
     }
     dev_free(d->delta_a); dev_free(d->delta_b); dev_free(d->io); dev_free(d->part); dev_free(d->wpack);
     delete d;

@@ -346,6 +346,9 @@ struct GemmArgs {
     int relu;
     const float* mask;  // C *= (mask[m * ldmask + n] > 0) when non-null
     int64_t ldmask;
+    float* rowsum;      // [slice][M]: sum over this slice's k of A(m, k) (row-contiguous A only), or null
+    const uint32_t* maskbits;  // instead of mask: C *= bit n of maskbits[m * ldmaskbits + n / 32], or null
+    int64_t ldmaskbits;
 };
 int launch_gemm_tf32x3(const GemmArgs& g, int slices, cudaStream_t st);  // kernels launched (0, 1; -1: N > 128)
 void launch_reduce_slices(const float* part, int slices, int64_t stride, int64_t n, float* out, bool accumulate,
@@ -375,6 +378,7 @@ struct MlpFwdArgs {
     float* X;  // encodings [n][ldx] (nullable)
     int64_t ldx;
     float* H[kMlpMaxLayers];  // hidden activations [n][ldh] (nullable)
+    uint32_t* Hbits[kMlpMaxLayers];  // their ReLU gates, 1 bit per unit: [n][ldh / 32] words (nullable)
     int64_t ldh;
     float* out;
     int64_t out_stride;
@@ -385,7 +389,6 @@ void launch_deform_encode(const float* pos, int64_t pos_stride, int64_t n, doubl
                           const DeformEnc& te, float* X, int64_t ldx, cudaStream_t st);
 void launch_deform_chain(const float* d_input, int64_t ldd, const float* X, int64_t ldx, int64_t n, double inv_scale,
                          int l_x, float* d_pos, int64_t dpos_stride, bool accumulate, cudaStream_t st);
-void launch_colsum(const float* delta, int64_t ld, int64_t n, int cols, float* db, cudaStream_t st);
 // tsb_ssim.cu: lambda's part of the trainer image loss for the quad channels.
 struct SsimArgs {
     int nz;                  // channels with a non-zero SSIM weight

@@ -252,7 +252,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
 __device__ __forceinline__ int op_mode(const float* P, int64_t sr, int64_t sk, int r0, int nrows, int k0, int kend,
                                        int R) {
     const bool aligned = ((uintptr_t)P & 15) == 0;
-    if (sk == 1 && (sr & 3) == 0 && aligned && k0 + kGemmKc <= kend) return 1;
+    if (sk == 1 && (sr & 3) == 0 && aligned) return 1;  // (a partial last chunk is zero-filled by cp.async)
     if (sr == 1 && (sk & 3) == 0 && aligned && (r0 & 3) == 0 && (r0 + R <= nrows || (int64_t)((nrows + 3) & ~3) <= sk))
         return 2;
     return 0;
@@ -273,9 +273,10 @@ __device__ __forceinline__ void raw_issue(const float* __restrict__ P, int64_t s
             const int idx = threadIdx.x + it * kGemmThreads;
             if (R * 8 % kGemmThreads && idx >= R * 8) break;
             const int r = idx >> 3, q = idx & 7, gr = r0 + r;
-            const bool ok = gr < nrows;
+            const int kv = kend - k0 - 4 * q;  // valid k of this 16-byte run
+            const bool ok = gr < nrows && kv > 0;
             cp_async16(base + (uint32_t)(r * kRawRowF * 4 + q * 16), ok ? P + (int64_t)gr * sr + k0 + 4 * q : P,
-                       ok ? 16u : 0u);
+                       ok ? (uint32_t)min(kv, 4) * 4u : 0u);
         }
     } else if (mode == 2) {  // (implies layout T)
         constexpr int rq_n = R / 4;
@@ -300,7 +301,8 @@ __device__ __forceinline__ void raw_issue(const float* __restrict__ P, int64_t s
 
 // Split a raw chunk into the K-major no-swizzle hi / lo tiles (core matrices).
 template <int R>
-__device__ __forceinline__ void raw_split(bool lay_t, const char* raw, char* hi, char* lo, int kvalid = kGemmKc) {
+__device__ __forceinline__ void raw_split(bool lay_t, const char* raw, char* hi, char* lo, int kvalid = kGemmKc,
+                                          double* rsum = nullptr) {
     constexpr int kIt = (R * 8 + kGemmThreads - 1) / kGemmThreads;
     if (!lay_t) {
 #pragma unroll
@@ -336,6 +338,7 @@ __device__ __forceinline__ void raw_split(bool lay_t, const char* raw, char* hi,
             const uint32_t o = core_off(r, 4 * kb);
             *reinterpret_cast<float4*>(hi + o) = h;
             *reinterpret_cast<float4*>(lo + o) = l;
+            if (rsum) rsum[it] += (double)((v.x + v.y) + (v.z + v.w));  // the fused row sum (bias gradient)
         }
     }
 }
@@ -457,6 +460,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
     }
     int rd_st = 0;         // raw stage of chunk q
     uint32_t rd_ph = 0;    // its fill parity (bulk mode)
+    // fused row sums of A (the bias gradient of a weight-gradient GEMM): per thread its rows
+    constexpr int kRsIt = (kGemmM * 8 + kGemmThreads - 1) / kGemmThreads;
+    double rsum[kRsIt];
+#pragma unroll
+    for (int i = 0; i < kRsIt; ++i) rsum[i] = 0.0;
+    const bool do_rsum = g.rowsum && ta && !BRES;
     uint32_t tphase = 0;  // mb_tile completions waited for
     float acc[FLUSH ? kColHalf : 1];
     for (int t = 0, q = 0; t < my_tiles; ++t) {
@@ -479,7 +488,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
             char* a_lo = a_hi + kABytes;
             char* sb_hi = a_lo + kABytes;  // split B (not resident)
             const int kvalid = bulk ? min(kGemmKc, kend - k0) : kGemmKc;
-            raw_split<kGemmM>(ta, raw_a(rd_st), a_hi, a_lo, kvalid);
+            raw_split<kGemmM>(ta, raw_a(rd_st), a_hi, a_lo, kvalid, do_rsum ? rsum : nullptr);
             if (!BRES) raw_split<NT>(tb, raw_b(rd_st), sb_hi, sb_hi + kBBytes, kvalid);
             if (++rd_st == kRaw) {
                 rd_st = 0;
@@ -531,6 +540,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
         const float* mrow0 = g.mask && row_ok && epi_warp ? g.mask + (int64_t)m * g.ldmask + col0 : nullptr;
         const bool mvec = mrow0 && ((uintptr_t)mrow0 & 15) == 0 && (g.ldmask & 3) == 0;
         float4 mk[kColHalf / 4];
+        uint32_t mbits = 0xffffffffu;  // gate bits of columns col0 .. col0 + 31 (bit gates)
+        if (g.maskbits && row_ok && epi_warp) mbits = __ldg(g.maskbits + (int64_t)m * g.ldmaskbits + (col0 >> 5));
+        mbits >>= col0 & 31;
 #pragma unroll
         for (int i = 0; i < kColHalf / 4; ++i)
             mk[i] = mvec && col0 + 4 * i + 4 <= g.N ? __ldg(reinterpret_cast<const float4*>(mrow0) + i)
@@ -565,6 +577,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
                         x[j] = __uint_as_float(v[j]);
                         if (g.bias && n0 + j < g.N) x[j] += __ldg(g.bias + n0 + j);
                         if (g.relu) x[j] = fmaxf(x[j], 0.f);
+                        if (!((mbits >> (cc + j)) & 1u)) x[j] = 0.f;
                     }
                     float* crow = C + (int64_t)m * g.ldc + n0;
                     const float* mrow = g.mask ? g.mask + (int64_t)m * g.ldmask + n0 : nullptr;
@@ -597,6 +610,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
     cp_async_wait<0>();
     tc_before_sync();
     __syncthreads();
+    if (do_rsum) {  // per row: the partials of the threads that split its k groups, in a fixed order
+        double* red = reinterpret_cast<double*>(raw0);  // [k group][row] (the ring is idle now)
+        constexpr int rq_n = kGemmM / 4;
+#pragma unroll
+        for (int it = 0; it < kRsIt; ++it) {
+            const int idx = threadIdx.x + it * kGemmThreads;
+            if (idx >= kGemmM * 8) break;
+            const int kq = idx & 3, rq = (idx >> 2) % rq_n, kb = (idx >> 2) / rq_n;
+            red[kb * kGemmM + 4 * rq + kq] = rsum[it];
+        }
+        __syncthreads();
+        if (tid < g.M) {
+            double t = 0.0;
+            for (int kb = 0; kb < kGemmKc / 4; ++kb) t += red[kb * kGemmM + tid];
+            g.rowsum[(int64_t)slice * g.M + tid] = (float)t;
+        }
+    }
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
 }
@@ -725,25 +755,6 @@ __global__ void k_deform_chain(const float* __restrict__ d_input, int64_t ldd, c
     }
 }
 
-// db[o] += sum_i delta[i][o]: each block sums a slab of rows with 8 independent loads in
-// flight per thread (fp32 partials of 8 rows, fp64 across), one atomic per column.
-__global__ void k_colsum(const float* __restrict__ delta, int64_t ld, int64_t n, int cols, float* __restrict__ db) {
-    const int o = threadIdx.x;
-    if (o >= cols) return;
-    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
-    const int64_t i0 = blockIdx.x * per, i1 = min(n, i0 + per);
-    double s = 0.0;
-    int64_t i = i0;
-    for (; i + 8 <= i1; i += 8) {
-        float v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = __ldg(delta + (i + j) * ld + o);
-        s += (double)(((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7])));
-    }
-    for (; i < i1; ++i) s += delta[i * ld + o];
-    if (s != 0.0) atomicAdd(&db[o], (float)s);
-}
-
 void launch_deform_encode(const float* pos, int64_t pos_stride, int64_t n, double inv_scale, int l_x,
                           const DeformEnc& te, float* X, int64_t ldx, cudaStream_t st) {
     if (n <= 0) return;
@@ -757,12 +768,6 @@ void launch_deform_chain(const float* d_input, int64_t ldd, const float* X, int6
     const int grid = (int)std::min<int64_t>((n + 127) / 128, 148 * 16);
     k_deform_chain<<<grid, 128, 0, st>>>(d_input, ldd, X, ldx, n, inv_scale, l_x, d_pos, dpos_stride,
                                          accumulate ? 1 : 0);
-}
-
-void launch_colsum(const float* delta, int64_t ld, int64_t n, int cols, float* db, cudaStream_t st) {
-    if (n <= 0 || cols <= 0) return;
-    const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
-    k_colsum<<<grid, ((cols + 31) / 32) * 32, 0, st>>>(delta, ld, n, cols, db);
 }
 
 }  // namespace tsb
@@ -805,26 +810,44 @@ __device__ __forceinline__ void split_exact(double x, float& hi, float& lo) { sp
 // rows m0 .. m0+127 (< n), columns [0, ncols) of the A tile -> dst[m * ld + c], coalesced:
 // per iteration a warp covers 8 rows x 4 consecutive column quads (no index division).
 __device__ __forceinline__ void store_rows(const char* A_hi, const char* A_lo, float* dst, int64_t ld, int64_t m0,
-                                           int64_t n, int ncols) {
+                                           int64_t n, int ncols, uint32_t* bits = nullptr) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int r8 = lane & 7, qi = lane >> 3, nq = ncols / 4;
+    // bits (ncols a multiple of 32): the ReLU gates, word w of a row = columns 32 w .. 32 w + 31;
+    // the 4 lanes of a row hold 16 consecutive columns per step
+    const int64_t ldw = ncols / 32;
     for (int rg = warp; rg < 16; rg += nwarps) {
         const int r = rg * 8 + r8;
         const int64_t m = m0 + r;
-        if (m >= n) continue;
+        const bool rv = m < n;
         float* row = dst + m * ld;
         const bool al = (((uintptr_t)row) & 15) == 0;
-        for (int q = qi; q < nq; q += 4) {
+        uint32_t word = 0;
+        for (int q = qi, t = 0; q < nq; q += 4, ++t) {
             const float4 h = *reinterpret_cast<const float4*>(A_hi + a_off(r, 4 * q));
             const float4 l = *reinterpret_cast<const float4*>(A_lo + a_off(r, 4 * q));
             const float4 v = make_float4(h.x + l.x, h.y + l.y, h.z + l.z, h.w + l.w);
-            if (al) {
-                *reinterpret_cast<float4*>(row + 4 * q) = v;
-            } else {
-                row[4 * q] = v.x; row[4 * q + 1] = v.y; row[4 * q + 2] = v.z; row[4 * q + 3] = v.w;
+            if (rv) {
+                if (al) {
+                    *reinterpret_cast<float4*>(row + 4 * q) = v;
+                } else {
+                    row[4 * q] = v.x; row[4 * q + 1] = v.y; row[4 * q + 2] = v.z; row[4 * q + 3] = v.w;
+                }
+            }
+            if (bits) {  // (warp-uniform: every lane of the warp runs nq / 4 steps)
+                uint32_t nib = (v.x > 0.f ? 1u : 0u) | (v.y > 0.f ? 2u : 0u) | (v.z > 0.f ? 4u : 0u) |
+                               (v.w > 0.f ? 8u : 0u);
+                nib <<= 4 * qi;
+                nib |= __shfl_xor_sync(0xffffffffu, nib, 8);
+                nib |= __shfl_xor_sync(0xffffffffu, nib, 16);
+                word |= nib << (16 * (t & 1));
+                if (t & 1) {
+                    if (qi == 0 && rv) bits[m * ldw + (t >> 1)] = word;
+                    word = 0;
+                }
             }
         }
-        if (qi == 0)
+        if (qi == 0 && rv)
             for (int c = 4 * nq; c < ncols; ++c)
                 row[c] = *reinterpret_cast<const float*>(A_hi + a_off(r, c)) +
                          *reinterpret_cast<const float*>(A_lo + a_off(r, c));
@@ -1032,7 +1055,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_fwd_fused(MlpFwdArgs a) 
             __syncthreads();
             // the activation for the backward: hi + lo is the fp32 value exactly; coalesced rows
             if (hidden && a.H[l]) {
-                store_rows(A_hi, A_lo, a.H[l], a.ldh, m0, a.n, nt);
+                // + the ReLU gates as bits (the backward's gate reads 1 bit instead of the activation)
+                store_rows(A_hi, A_lo, a.H[l], a.ldh, m0, a.n, nt, a.Hbits[l]);
                 __syncthreads();  // the next layer's epilogue overwrites A
             }
         }
