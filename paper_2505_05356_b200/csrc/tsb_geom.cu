@@ -7,6 +7,10 @@
 #include "tsb_fp64.cuh"
 #include "tsb_ties.cuh"
 
+#ifndef TSB_PRE_CTAS
+#define TSB_PRE_CTAS 6
+#endif
+
 namespace tsb {
 
 // ---------------------------------------------------------------------------
@@ -61,6 +65,17 @@ __device__ __forceinline__ void write_records(const SceneK& S, const Prep64& s, 
 // 2 undecided.
 __device__ __forceinline__ int lean_visible(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F, int gi,
                                             double& depth) {
+    // every load of the test up front (one memory round trip instead of three: the culls
+    // below would otherwise hold the opacity and covariance loads behind them)
+    const size_t n = (size_t)S.n;
+    const bool cached = S.opac && S.cov6f;
+    double op = 0.0;
+    float c00 = 0.f, c01 = 0.f, c02 = 0.f, c11 = 0.f, c12 = 0.f, c22 = 0.f;
+    if (cached) {
+        op = S.opac[gi];
+        c00 = S.cov6f[gi]; c01 = S.cov6f[n + gi]; c02 = S.cov6f[2 * n + gi];
+        c11 = S.cov6f[3 * n + gi]; c12 = S.cov6f[4 * n + gi]; c22 = S.cov6f[5 * n + gi];
+    }
     double x[3];
     frame_mean(S, F, gi, x);
     const double* R = C.R;
@@ -68,7 +83,7 @@ __device__ __forceinline__ int lean_visible(const SceneK& S, const CamK& C, cons
     for (int i = 0; i < 3; ++i) p[i] = R[i * 3 + 0] * x[0] + R[i * 3 + 1] * x[1] + R[i * 3 + 2] * x[2] + C.t[i];
     if (p[2] < C.near_plane) return 0;
     depth = sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
-    const double op = S.opac ? S.opac[gi] : opacity64(S, gi);
+    if (!cached) op = S.opac ? S.opac[gi] : opacity64(S, gi);
     if (op < O.alpha_thr) return 0;
     if (!S.cov6) return 2;
     // the bound in fp32 from the fp64 camera-space mean (its errors, ~1e-7 relative, sit far
@@ -89,12 +104,7 @@ __device__ __forceinline__ int lean_visible(const SceneK& S, const CamK& C, cons
         Ma[j] = fabsf(fxz) * (fabsf(r0) + fabsf(txz * r2));
         Ma[3 + j] = fabsf(fyz) * (fabsf(r1) + fabsf(tyz * r2));
     }
-    const size_t n = (size_t)S.n;
-    float c00, c01, c02, c11, c12, c22;
-    if (S.cov6f) {  // 24 B instead of 48
-        c00 = S.cov6f[gi]; c01 = S.cov6f[n + gi]; c02 = S.cov6f[2 * n + gi];
-        c11 = S.cov6f[3 * n + gi]; c12 = S.cov6f[4 * n + gi]; c22 = S.cov6f[5 * n + gi];
-    } else {
+    if (!cached) {  // (the fp32 cache, 24 B instead of 48, was loaded above)
         c00 = (float)S.cov6[gi]; c01 = (float)S.cov6[n + gi]; c02 = (float)S.cov6[2 * n + gi];
         c11 = (float)S.cov6[3 * n + gi]; c12 = (float)S.cov6[4 * n + gi]; c22 = (float)S.cov6[5 * n + gi];
     }
@@ -137,7 +147,7 @@ __device__ __forceinline__ int lean_visible(const SceneK& S, const CamK& C, cons
 // count / key range; the records of the Gaussians the frame reads -- its sorted
 // prefix -- are written after the sort by k_records.
 template <bool LEAN>
-__global__ void __launch_bounds__(256, LEAN ? 6 : 5) k_preprocess(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd,
+__global__ void __launch_bounds__(256, LEAN ? TSB_PRE_CTAS : 5) k_preprocess(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd,
                                                     uint32_t* __restrict__ depth_key,
                                                     double* __restrict__ depth64,
                                                     uint32_t* __restrict__ gidx,
