@@ -281,6 +281,15 @@ __global__ void __launch_bounds__(256, 5) k_records(SceneK S, CamK C, OptK O, co
         if (depth_key[gi] == 0xffffffffu) return;
     }
     const FrameK F = fd->F;
+    // prep64 reads the opacity, covariance and reflectivity behind its culls (each a
+    // dependent round trip); this Gaussian is known visible, so start them all into L2 now
+    {
+        const size_t n = (size_t)S.n;
+        if (S.opac) asm volatile("prefetch.global.L2 [%0];" ::"l"(S.opac + gi));
+        if (S.cov6)
+            for (int c = 0; c < 6; ++c) asm volatile("prefetch.global.L2 [%0];" ::"l"(S.cov6 + c * n + gi));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(S.scale_amp + gi));
+    }
     Prep64 s;
     // The lean preprocess kept this Gaussian; the exact test must agree.  If it does
     // not, the frame is redone from the exact (non-lean) preprocess (abort bit 16).
