@@ -5,8 +5,11 @@
 //      by the fp64 depth on read (tsb_ties.cuh), or the exact 64-bit sort (below).
 //   2. k_order_ranks: rank -> (Gaussian, tile rect).  Each raster block scans these in
 //      rank order and keeps the ranks whose tile rect covers its tile -- the reference's
-//      tile list -- until its pixels have terminated (tsb_raster.cu), so no list is ever
-//      materialised; k_tile_lists builds the complete lists for parity checks only.
+//      tile list -- until its pixels have terminated (tsb_raster.cu), so no tile list is
+//      ever materialised; k_tile_lists builds the complete lists for parity checks only.
+//   3. long orders (> kSlMinRanks): per 8 x 8-tile super-tile, the ranks meeting it, in
+//      rank order (k_order_ranks counts, k_sl_rowscan, k_sl_emit); a block then scans its
+//      super-tile's list instead of the whole order.
 #include <algorithm>
 
 #include "tsb_internal.h"
