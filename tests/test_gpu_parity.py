@@ -88,6 +88,25 @@ def test_c0_forward_full(tsb, ctx):
     assert rel_err(rec[:, 7], orec[:, 9], 1e-9) < 1e-6  # depth
 
 
+def test_debug_records_of_a_prefix_sorted_frame(tsb, ctx):
+    """on a prefix-sorted frame the debug read of the records must see the records
+    of the full order (k_records of the redo), not only the prefix's: n = 40 K > the 16 K
+    initial cap, default (prefix) lists, every rank's opacity / coef / depth vs the oracle."""
+    from paper_2505_05356_b200 import synthetic
+    g = synthetic.gaussians(40_000, 13, n_keyframes=2)
+    cam = synthetic.camera(320, 240, 260.0)
+    opts = tsb.RenderOptions(counts=True)
+    _, rp, out, op, ref = render_both(tsb, ctx, g, cam, synthetic.ToFConfig(30e6), (0, 0.6), opts)
+    rec = rp.debug_records()
+    oprep = op.prepared()
+    orec = oprep["rec"]
+    assert rec.shape[0] == orec.shape[0] == op.visible_count()
+    assert np.array_equal(rp.debug_prepared()["gidx"], oprep["gidx"])
+    assert rel_err(rec[:, 5], orec[:, 5], 1e-9) < 1e-6  # opacity
+    assert rel_err(rec[:, 6], orec[:, 6], 1e-9) < 1e-6  # coef
+    assert rel_err(rec[:, 7], orec[:, 9], 1e-9) < 1e-6  # depth
+
+
 @pytest.mark.parametrize("tile_size", [5, 16, 32])
 def test_tile_size_invariance_and_lists(tsb, ctx, tile_size):
     """test_splat.cpp:235-266: tile size never changes the result; lists must match the oracle."""
