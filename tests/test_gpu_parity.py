@@ -88,6 +88,27 @@ def test_c0_forward_full(tsb, ctx):
     assert rel_err(rec[:, 7], orec[:, 9], 1e-9) < 1e-6  # depth
 
 
+def test_tile_sizes_multiple_of_16_are_bit_identical(tsb, ctx):
+    """test_splat.cpp:235-266 renders tile sizes 16, 5 and 64 and requires the same bits.  The
+    raster's coordinates are relative to its 16 x 16 block (exact fp32 pixel offsets, the
+    mean rounded once relative to the block): for tile sizes that are multiples of 16 the
+    blocks -- and so every per-pixel operation -- are the same, and the outputs are
+    bit-identical; other sizes (5) move the block origins and agree to ~1e-7."""
+    from paper_2505_05356_b200 import synthetic
+    g = synthetic.gaussians(3000, 5, n_keyframes=2)
+    cam = synthetic.camera(200, 150, 180.0)
+    scene = gpu_scene(tsb, ctx, g, synthetic.ToFConfig(30e6))
+    outs = {}
+    for ts in (16, 32, 64):
+        opts = tsb.RenderOptions(tile_size=ts, counts=True, distortion=True, bg_quad=(0.3, 0.1, -0.2, 0.4))
+        outs[ts] = tsb.RenderPass(ctx).prepare(scene, cam, opts, (0, 0.25)).forward().outputs()
+    for ts in (32, 64):
+        for k in ("quad", "phasor", "depth_raw", "weight", "depth", "distortion", "transmittance", "n_contrib"):
+            a, b = outs[16][k], outs[ts][k]
+            assert np.array_equal(a.view(np.uint32) if a.dtype == np.float32 else a,
+                                  b.view(np.uint32) if b.dtype == np.float32 else b), (ts, k)
+
+
 def test_debug_records_of_a_prefix_sorted_frame(tsb, ctx):
     """on a prefix-sorted frame the debug read of the records must see the records
     of the full order (k_records of the redo), not only the prefix's: n = 40 K > the 16 K
