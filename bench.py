@@ -674,7 +674,7 @@ def main():
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--no-deform", action="store_true")
     ap.add_argument("--deform-n", type=int, default=2_000_000)
-    ap.add_argument("--passes", type=int, default=24, help="render passes (streams) in flight")
+    ap.add_argument("--passes", type=int, default=32, help="render passes (streams) in flight")
     ap.add_argument("--train-passes", type=int, default=16)
     ap.add_argument("--train-steps", type=int, default=3)
     ap.add_argument("--train-n", type=int, default=None)
