@@ -203,7 +203,7 @@ class StreamTimer:
 # Times: CUDA events the library records on each pass's stream around every stage.
 #   serialised -- one more sweep on ONE pass after the timed region: a launch's own
 #     duration (what ncu's launch list measures; `achieved` / `frac`);
-#   overlapped -- one more sweep over all passes (24 frames in flight, as timed, but issued
+#   overlapped -- one more sweep over all passes (32 frames in flight, as timed, but issued
 #     eagerly so the stage events exist): the stage's share of the summed event time
 #     (`share_overlapped`; event spans of concurrent kernels overlap, so only the shares
 #     are meaningful, and they agree with the serialised shares and ncu's launch list).
