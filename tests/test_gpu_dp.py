@@ -59,3 +59,28 @@ def test_frame_sharded_allreduce_matches_single_gpu(tmp_path):
     for name in ("d_position", "d_motion", "d_log_scale"):
         assert rel_err(ranks[0][name], gr[name], 1e-4) < 1e-5 * 10, name
     assert float(ranks[0]["loss"]) == pytest.approx(gr["loss"], rel=1e-9)
+
+
+def test_nccl_allreduce_single_rank_runs_the_product_path():
+    """The library's NCCL path on a 1-GPU box: a one-rank communicator (tsb_comm_create),
+    the gradient + statistics allreduce (tsb_scene_allreduce_grads) after a training frame --
+    the sum over one rank leaves every gradient bit-identical; the communicator is destroyed
+    cleanly.  (The multi-rank case needs >= 2 GPUs: test above.)"""
+    sys.path.insert(0, str(HERE))
+    import dp_worker
+    import paper_2505_05356_b200 as tsb
+    g, cam, frames, targets = dp_worker.setup()
+    ctx = tsb.Context(0)
+    scene = tsb.GaussianScene(ctx, g.n, g.n_keyframes, tsb.ToFConfig(30e6))
+    scene.set_params(g.position, g.log_scale, g.rotation, g.opacity_logit, g.reflectivity_dc, g.motion)
+    rp = tsb.RenderPass(ctx)
+    rp.prepare(scene, cam, tsb.RenderOptions(), frames[0])
+    rp.forward_loss(targets[0], sync=False)
+    rp.backward()
+    before = scene.grads()
+    comm = tsb.Comm(ctx, tsb.Comm.unique_id(), 1, 0)
+    scene.allreduce_grads(comm)
+    after = scene.grads()
+    comm.close()
+    for name in before:
+        assert np.array_equal(np.asarray(before[name]), np.asarray(after[name])), name
