@@ -276,7 +276,7 @@ struct tsb_pass {
 
 namespace {
 constexpr size_t kFrameSlot = 3072;  // FrameDev staging offset in tsb_pass::pinned
-constexpr int kPrefixCap0 = 16384;  // initial nearest-prefix cap of the depth order (4 sort tiles)
+constexpr int kPrefixCap0 = 4096;   // initial nearest-prefix cap of the depth order (c3 terminates within ~3 K ranks)
 }
 
 extern "C" {
