@@ -93,8 +93,8 @@ __device__ __forceinline__ void stage_entry(SM& sm, const RecK& rec, uint32_t g,
 // tile -- its reference tile list, in order -- then composites a batch once it
 // holds >= 256 entries, until every pixel of the block has terminated.  A pixel
 // is finalised (outputs, fix-up flag, loss epilogue) at the end.
-// WORK: count evaluations / contributions (profiling runs only; a template so the
-// per-evaluation counter costs nothing otherwise).
+// WORK: count evaluations / contributions (profiling runs and counts outputs only; a
+// template so the per-evaluation counters cost nothing otherwise).
 // LISTS: the block scans its super-tile list (ScanK::sl_*); otherwise the order itself
 // (a template so the short-order kernel carries none of the list bookkeeping).
 template <int NF, bool DIST, bool WORK, bool LISTS>
@@ -169,21 +169,29 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK s
                 for (int c = 0; c < nb; c += 32) {
                     const bool t = c + lane < nb && ((sm.wmask[c + lane] >> warp) & 1u);
                     const unsigned bal = __ballot_sync(0xffffffffu, t);
-                    if (t) sm.list[warp][wcnt + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)(c + lane);
+                    if (t) sm.list[warp][wcnt + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)((c + lane) * 16);
                     wcnt += __popc(bal);
                 }
                 __syncwarp();
             }
             if (!done) {
+                // per warp: byte offsets of its entries' slots; one compare per window on the
+                // common path (an entry inside the ellipse, clear of both bands)
                 const uint16_t* wl = sm.list[tid >> 5];
-                for (int k = 0; k < wcnt; ++k) {
-                    const int j = wl[k];
+                const uint16_t* const wend = wl + wcnt;
+                const char* const sA = reinterpret_cast<const char*>(sm.A);
+                const char* const sB = reinterpret_cast<const char*>(sm.B);
+                const char* const sC = reinterpret_cast<const char*>(sm.C);
+                const char* const sD = reinterpret_cast<const char*>(sm.D);
+                for (; wl < wend; ++wl) {
+                    const int jo = *wl;
                     if (WORK) ++n_eval;
-                    const float4 A = sm.A[j], B = sm.B[j];
+                    const float4 A = *reinterpret_cast<const float4*>(sA + jo);
+                    const float4 B = *reinterpret_cast<const float4*>(sB + jo);
                     Eval ev;
                     eval_entry(A, B, pcx, pcy, ev);
-                    if (ev.maha > outside) continue;  // clearly outside (most entries)
                     if (ev.maha >= m_lo) {
+                        if (ev.maha > outside) continue;  // clearly outside
                         const float dm = ev.maha - cut2;
                         if (dm >= -coarseM && fabsf(dm) <= 2.f * maha_err_bound(A, B, ev)) flag |= 1;
                         if (dm > 0.f) continue;
@@ -198,15 +206,15 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK s
                         }
                         if (da < 0.f) continue;
                     }
-                    ++nc;
-                    const float4 Cc = sm.C[j];
+                    if (WORK || DIST) ++nc;
+                    const float4 Cc = *reinterpret_cast<const float4*>(sC + jo);
                     const float w = ev.alpha * T;
                     const float w2 = w * T;
                     const float cq = Cc.x * w2;
                     accS[0] = fmaf(cq, Cc.z, accS[0]);
                     accC[0] = fmaf(cq, Cc.w, accC[0]);
                     if (NF > 1) {
-                        const float4 Dd = sm.D[j];
+                        const float4 Dd = *reinterpret_cast<const float4*>(sD + jo);
                         accS[NF - 1] = fmaf(cq, Dd.x, accS[NF - 1]);
                         accC[NF - 1] = fmaf(cq, Dd.y, accC[NF - 1]);
                     }
@@ -230,7 +238,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK s
                             flag |= 4;  // above, within the band: T - fl < 2 dT, and dT >= fl * rel err
                         } else {
                             if (fl - T < 2.f * fl * __fdividef(dT, T)) flag |= 4;  // |T - fl| < 2 fl rel err
-                            const int gidx_e = ebase + j + 1;
+                            const int gidx_e = ebase + (jo >> 4) + 1;
                             if (T == 0.f && last_eff < 0) {
                                 last_eff = gidx_e;
                                 Tpre_eff = Tpre;
@@ -288,7 +296,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK s
             px.dist3[HW + o] = SDs;
             px.dist3[2 * HW + o] = SD2s;
         }
-        if (px.n_contrib) px.n_contrib[o] = nc;
+        if (WORK && px.n_contrib) px.n_contrib[o] = nc;
         if (px.n_processed) px.n_processed[o] = processed;
         px.last[o] = last_eff >= 0 ? last_eff : processed;
         px.T_pre[o] = last_eff >= 0 ? Tpre_eff : Tpre;
@@ -311,7 +319,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_raster_fwd(RecK rec, ScanK s
             ev += __shfl_xor_sync(0xffffffffu, ev, m);
             cn += __shfl_xor_sync(0xffffffffu, cn, m);
         }
-        if ((tid & 31) == 0) {
+        if ((tid & 31) == 0 && sc.work) {
             atomicAdd(&sc.work[0], ev);
             atomicAdd(&sc.work[1], cn);
         }
@@ -672,7 +680,7 @@ void launch_raster_fwd(const RecK& rec, const ScanK& sc, const OptK& O, int W, i
     const int grid = O.tiles_x * O.tiles_y * O.sub * O.sub;
 #define TSB_FWD_L(NF_, D_, L_)                                                                                  \
     do {                                                                                                       \
-        if (sc.work)                                                                                           \
+        if (sc.work || px.n_contrib)                                                                           \
             k_raster_fwd<NF_, D_, true, L_><<<grid, kRasterThreads, 0, st>>>(rec, sc, O, W, H, px, fd,            \
                                                                               loss ? 1 : 0, ch_w, loss_part);   \
         else                                                                                                   \
