@@ -809,9 +809,10 @@ __device__ __forceinline__ void split_exact(double x, float& hi, float& lo) { sp
 
 // rows m0 .. m0+127 (< n), columns [0, ncols) of the A tile -> dst[m * ld + c], coalesced:
 // per iteration a warp covers 8 rows x 4 consecutive column quads (no index division).
+// Warps w0 .. w0 + nwarps - 1 take part (the MMA-issuing warp 0 does not while it issues).
 __device__ __forceinline__ void store_rows(const char* A_hi, const char* A_lo, float* dst, int64_t ld, int64_t m0,
-                                           int64_t n, int ncols, uint32_t* bits = nullptr) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+                                           int64_t n, int ncols, uint32_t* bits, int w0, int nwarps) {
+    const int lane = threadIdx.x & 31, warp = (int)(threadIdx.x >> 5) - w0;
     const int r8 = lane & 7, qi = lane >> 3, nq = ncols / 4;
     // bits (ncols a multiple of 32): the ReLU gates, word w of a row = columns 32 w .. 32 w + 31;
     // the 4 lanes of a row hold 16 consecutive columns per step
@@ -979,13 +980,21 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_fwd_fused(MlpFwdArgs a) 
         }
         fence_async_smem();
         __syncthreads();
-        if (a.X) {
-            store_rows(A_hi, A_lo, a.X, a.ldx, m0, a.n, a.din);
-            __syncthreads();  // layer 0's epilogue overwrites A
-        }
 
         for (int l = 0; l < lay.layers; ++l) {
             const int nt = lay.nt[l];
+            // A holds this layer's input (read-only until its epilogue): warps 1-15 store it for
+            // the backward -- the encoding (X) or the previous layer's activation (H, + its ReLU
+            // gates as bits: the backward's gate reads 1 bit instead of the activation) -- while
+            // thread 0 issues the layer's MMAs
+            const bool store_x = l == 0 && a.X;
+            const bool store_h = l > 0 && a.H[l - 1];
+            if (warp > 0) {
+                if (store_x) store_rows(A_hi, A_lo, a.X, a.ldx, m0, a.n, a.din, nullptr, 1, kMlpThreads / 32 - 1);
+                if (store_h)
+                    store_rows(A_hi, A_lo, a.H[l - 1], a.ldh, m0, a.n, lay.nt[l - 1], a.Hbits[l - 1], 1,
+                               kMlpThreads / 32 - 1);
+            }
             if (tid == 0) {
                 tc_after_sync();
                 const uint32_t idesc = idesc_tf32(128, nt);
@@ -1016,6 +1025,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_fwd_fused(MlpFwdArgs a) 
             }
             mbar_wait(&mb_layer, lphase & 1u);
             ++lphase;
+            if (store_x || store_h) __syncthreads();  // the epilogue overwrites A
             tc_after_sync();
             // ---- epilogue: bias, ReLU; split back into A for the next layer ----
             const int r = (warp & 3) * 32 + lane;
@@ -1053,12 +1063,6 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_fwd_fused(MlpFwdArgs a) 
             fence_async_smem();
             tc_before_sync();
             __syncthreads();
-            // the activation for the backward: hi + lo is the fp32 value exactly; coalesced rows
-            if (hidden && a.H[l]) {
-                // + the ReLU gates as bits (the backward's gate reads 1 bit instead of the activation)
-                store_rows(A_hi, A_lo, a.H[l], a.ldh, m0, a.n, nt, a.Hbits[l]);
-                __syncthreads();  // the next layer's epilogue overwrites A
-            }
         }
     }
     tc_before_sync();
