@@ -300,9 +300,12 @@ __device__ __forceinline__ void raw_issue(const float* __restrict__ P, int64_t s
 }
 
 // Split a raw chunk into the K-major no-swizzle hi / lo tiles (core matrices).
+// Layout T rows are ldr floats apart (R, or the operand's own row stride when a bulk copy
+// brought the chunk in whole; rows past it then hold other data, which only feeds output
+// rows / columns the epilogue discards).
 template <int R>
 __device__ __forceinline__ void raw_split(bool lay_t, const char* raw, char* hi, char* lo, int kvalid = kGemmKc,
-                                          double* rsum = nullptr) {
+                                          double* rsum = nullptr, int ldr = R) {
     constexpr int kIt = (R * 8 + kGemmThreads - 1) / kGemmThreads;
     if (!lay_t) {
 #pragma unroll
@@ -325,8 +328,8 @@ __device__ __forceinline__ void raw_split(bool lay_t, const char* raw, char* hi,
             const int idx = threadIdx.x + it * kGemmThreads;
             if (R * 8 % kGemmThreads && idx >= R * 8) break;
             const int kq = idx & 3, rq = (idx >> 2) % rq_n, kb = (idx >> 2) / rq_n, r = 4 * rq + kq;
-            float4 v = make_float4(rf[(4 * kb + 0) * R + r], rf[(4 * kb + 1) * R + r], rf[(4 * kb + 2) * R + r],
-                                   rf[(4 * kb + 3) * R + r]);
+            float4 v = make_float4(rf[(4 * kb + 0) * ldr + r], rf[(4 * kb + 1) * ldr + r], rf[(4 * kb + 2) * ldr + r],
+                                   rf[(4 * kb + 3) * ldr + r]);
             if (4 * kb + 4 > kvalid) {  // rows past a bulk-copied partial chunk hold stale data
                 if (4 * kb + 0 >= kvalid) v.x = 0.f;
                 if (4 * kb + 1 >= kvalid) v.y = 0.f;
@@ -416,20 +419,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
         }
     }
     const int total = my_tiles * nck;
-    // Bulk mode (both operands row-contiguous and full-width: a chunk of each is one
-    // contiguous run of 32 rows): one TMA bulk copy per operand per chunk, completion on the
-    // stage's mbarrier, the whole ring in flight.  Otherwise per-thread cp.async.
-    const bool bulk = !BRES && ta && tb && g.a_k == kGemmM && g.M == kGemmM && g.b_k == NT && g.N == NT &&
-                      (((uintptr_t)g.A | (uintptr_t)g.B) & 15) == 0;
+    // Bulk mode (both operands row-contiguous with one tile each: M <= row stride <= 128,
+    // N <= row stride <= NT, so a chunk of each is one contiguous run of 32 rows): one TMA
+    // bulk copy per operand per chunk, completion on the stage's mbarrier, the whole ring in
+    // flight.  Otherwise per-thread cp.async.
+    const bool bulk = !BRES && ta && tb && g.M <= g.a_k && g.a_k <= kGemmM && g.N <= g.b_k && g.b_k <= NT &&
+                      ((g.a_k | g.b_k) & 3) == 0 && (((uintptr_t)g.A | (uintptr_t)g.B) & 15) == 0;
+    const int lda = bulk ? (int)g.a_k : kGemmM, ldb = bulk ? (int)g.b_k : NT;  // raw T row strides
     // issue cursor: the next chunk to load (tile row m0, chunk ch, raw stage)
     int is_q = 0, is_m0 = (int)blockIdx.x * kGemmM, is_ch = 0, is_st = 0;
     auto issue_bulk = [&]() {  // thread 0: the next chunk (nothing past the end)
         if (is_q < total) {
             const int k0 = kbeg + is_ch * kGemmKc, rows = min(kGemmKc, kend - k0);
-            const uint32_t ba = (uint32_t)rows * kGemmM * 4, bb = (uint32_t)rows * NT * 4;
+            const uint32_t ba = (uint32_t)rows * lda * 4, bb = (uint32_t)rows * ldb * 4;
             mbar_expect_tx(&mb_raw[is_st], ba + bb);
-            bulk_copy(smem_u32(raw_a(is_st)), g.A + (int64_t)k0 * kGemmM, ba, &mb_raw[is_st]);
-            bulk_copy(smem_u32(raw_b(is_st)), g.B + (int64_t)k0 * NT, bb, &mb_raw[is_st]);
+            bulk_copy(smem_u32(raw_a(is_st)), g.A + (int64_t)k0 * lda, ba, &mb_raw[is_st]);
+            bulk_copy(smem_u32(raw_b(is_st)), g.B + (int64_t)k0 * ldb, bb, &mb_raw[is_st]);
             if (++is_ch == nck) {
                 is_ch = 0;
                 is_m0 += (int)gridDim.x * kGemmM;
@@ -488,8 +493,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
             char* a_lo = a_hi + kABytes;
             char* sb_hi = a_lo + kABytes;  // split B (not resident)
             const int kvalid = bulk ? min(kGemmKc, kend - k0) : kGemmKc;
-            raw_split<kGemmM>(ta, raw_a(rd_st), a_hi, a_lo, kvalid, do_rsum ? rsum : nullptr);
-            if (!BRES) raw_split<NT>(tb, raw_b(rd_st), sb_hi, sb_hi + kBBytes, kvalid);
+            raw_split<kGemmM>(ta, raw_a(rd_st), a_hi, a_lo, kvalid, do_rsum ? rsum : nullptr, lda);
+            if (!BRES) raw_split<NT>(tb, raw_b(rd_st), sb_hi, sb_hi + kBBytes, kvalid, nullptr, ldb);
             if (++rd_st == kRaw) {
                 rd_st = 0;
                 rd_ph ^= 1u;
