@@ -260,18 +260,18 @@ __device__ __forceinline__ int op_mode(const float* P, int64_t sr, int64_t sk, i
 
 // Issue the raw copy of rows [r0, r0 + R) x k [k0, k0 + 32) of X(r, k) = P[r sr + k sk]
 // (zeros outside rows < nrows, k < kend); mode 0 copies synchronously.
-template <int R>
+template <int R, int NTHR = kGemmThreads>
 __device__ __forceinline__ void raw_issue(const float* __restrict__ P, int64_t sr, int64_t sk, int r0, int nrows,
                                           int k0, int kend, char* raw) {
     const int mode = op_mode(P, sr, sk, r0, nrows, k0, kend, R);
     const bool lay_t = sr == 1;  // the raw layout (T: [k][R]) follows the operand, not the chunk
     const uint32_t base = smem_u32(raw);
-    constexpr int kIt = (R * 8 + kGemmThreads - 1) / kGemmThreads;
+    constexpr int kIt = (R * 8 + NTHR - 1) / NTHR;
     if (mode == 1 && !lay_t) {
 #pragma unroll
         for (int it = 0; it < kIt; ++it) {
-            const int idx = threadIdx.x + it * kGemmThreads;
-            if (R * 8 % kGemmThreads && idx >= R * 8) break;
+            const int idx = threadIdx.x + it * NTHR;
+            if (R * 8 % NTHR && idx >= R * 8) break;
             const int r = idx >> 3, q = idx & 7, gr = r0 + r;
             const int kv = kend - k0 - 4 * q;  // valid k of this 16-byte run
             const bool ok = gr < nrows && kv > 0;
@@ -282,8 +282,8 @@ __device__ __forceinline__ void raw_issue(const float* __restrict__ P, int64_t s
         constexpr int rq_n = R / 4;
 #pragma unroll
         for (int it = 0; it < kIt; ++it) {
-            const int idx = threadIdx.x + it * kGemmThreads;
-            if (R * 8 % kGemmThreads && idx >= R * 8) break;
+            const int idx = threadIdx.x + it * NTHR;
+            if (R * 8 % NTHR && idx >= R * 8) break;
             const int k = idx / rq_n, rq = idx - k * rq_n, gk = k0 + k;
             const bool ok = gk < kend && r0 + 4 * rq < nrows;
             cp_async16(base + (uint32_t)(k * R * 4 + rq * 16), ok ? P + (r0 + 4 * rq) + (int64_t)gk * sk : P,
@@ -291,7 +291,7 @@ __device__ __forceinline__ void raw_issue(const float* __restrict__ P, int64_t s
         }
     } else {
         float* rf = reinterpret_cast<float*>(raw);
-        for (int idx = threadIdx.x; idx < R * kGemmKc; idx += kGemmThreads) {
+        for (int idx = threadIdx.x; idx < R * kGemmKc; idx += NTHR) {
             const int r = idx / kGemmKc, k = idx - r * kGemmKc, gr = r0 + r, gk = k0 + k;
             rf[lay_t ? k * R + r : r * kRawRowF + k] =
                 (gr < nrows && gk < kend) ? P[(int64_t)gr * sr + (int64_t)gk * sk] : 0.f;
@@ -303,15 +303,15 @@ __device__ __forceinline__ void raw_issue(const float* __restrict__ P, int64_t s
 // Layout T rows are ldr floats apart (R, or the operand's own row stride when a bulk copy
 // brought the chunk in whole; rows past it then hold other data, which only feeds output
 // rows / columns the epilogue discards).
-template <int R>
+template <int R, int NTHR = kGemmThreads>
 __device__ __forceinline__ void raw_split(bool lay_t, const char* raw, char* hi, char* lo, int kvalid = kGemmKc,
                                           double* rsum = nullptr, int ldr = R) {
-    constexpr int kIt = (R * 8 + kGemmThreads - 1) / kGemmThreads;
+    constexpr int kIt = (R * 8 + NTHR - 1) / NTHR;
     if (!lay_t) {
 #pragma unroll
         for (int it = 0; it < kIt; ++it) {
-            const int idx = threadIdx.x + it * kGemmThreads;
-            if (R * 8 % kGemmThreads && idx >= R * 8) break;
+            const int idx = threadIdx.x + it * NTHR;
+            if (R * 8 % NTHR && idx >= R * 8) break;
             const int r8 = idx & 7, q = (idx >> 3) & 7, rg = idx >> 6, r = rg * 8 + r8;
             const float4 v = *reinterpret_cast<const float4*>(raw + r * kRawRowF * 4 + q * 16);
             float4 h, l;
@@ -325,8 +325,8 @@ __device__ __forceinline__ void raw_split(bool lay_t, const char* raw, char* hi,
         const float* rf = reinterpret_cast<const float*>(raw);
 #pragma unroll
         for (int it = 0; it < kIt; ++it) {
-            const int idx = threadIdx.x + it * kGemmThreads;
-            if (R * 8 % kGemmThreads && idx >= R * 8) break;
+            const int idx = threadIdx.x + it * NTHR;
+            if (R * 8 % NTHR && idx >= R * 8) break;
             const int kq = idx & 3, rq = (idx >> 2) % rq_n, kb = (idx >> 2) / rq_n, r = 4 * rq + kq;
             float4 v = make_float4(rf[(4 * kb + 0) * ldr + r], rf[(4 * kb + 1) * ldr + r], rf[(4 * kb + 2) * ldr + r],
                                    rf[(4 * kb + 3) * ldr + r]);
@@ -636,6 +636,198 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
 }
 
+__device__ __forceinline__ float* C_row(const GemmArgs& g, int m) { return g.C + (int64_t)m * g.ldc; }
+
+// Warp-specialised variant for resident-B GEMMs without split-K (the input gradients
+// delta W and the layer-by-layer forward): warps 0-7 load (cp.async ring), split and issue
+// the MMAs (thread 0); warps 8-15 drain the finished tile's accumulator (bias, ReLU, gate,
+// stores).  Two TMEM accumulators alternate between tiles, so a tile's epilogue runs while
+// the next tile's chunks are loaded, split and multiplied (acc_full: MMAs of the tile done;
+// acc_empty: its epilogue has read the accumulator).
+__device__ __forceinline__ void bar_main() { asm volatile("bar.sync 1, %0;" ::"n"(kGemmThreads / 2) : "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mbar)) : "memory");
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(GemmArgs g, int kRaw) {
+    extern __shared__ __align__(1024) char smem[];
+    __shared__ __align__(8) uint64_t mb_mma, acc_full[2], acc_empty[2];
+    __shared__ uint32_t tmem_base_s;
+    constexpr int kMain = kGemmThreads / 2;
+    constexpr int kEpiWarps = (kGemmThreads - kMain) / 32;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int kAccCols = NT <= 32 ? 32 : (NT <= 64 ? 64 : 128);
+    constexpr int kTmemCols = 2 * kAccCols;
+    constexpr uint32_t kABytes = kGemmM * kGemmKc * 4, kBBytes = NT * kGemmKc * 4;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        mbar_init(&mb_mma, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], kEpiWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    const uint32_t tmem = tmem_base_s;
+    const int kend = g.K;
+    const int ntiles = (g.M + kGemmM - 1) / kGemmM;
+    const int nck = (kend + kGemmKc - 1) / kGemmKc;  // (> 0: the launcher routes K = 0 elsewhere)
+    const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    constexpr uint32_t idesc = idesc_tf32(kGemmM, NT);
+    const bool ta = g.a_m == 1, tb = g.b_n == 1;
+    char* bres = smem;
+    char* split0 = smem + (size_t)nck * 2 * kBBytes;
+    char* raw0 = split0 + 2 * kABytes;
+    const size_t raw_stage = raw_bytes(kGemmM, ta);
+    auto raw_a = [&](int st) { return raw0 + (size_t)st * raw_stage; };
+    for (int ch = 0; ch < nck; ++ch) {  // B split once by all warps, through raw stage 0
+        const int k0 = ch * kGemmKc;
+        raw_issue<NT>(g.B, g.b_n, g.b_k, 0, g.N, k0, kend, raw_a(0));
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+        char* bh = bres + (size_t)ch * 2 * kBBytes;
+        raw_split<NT>(tb, raw_a(0), bh, bh + kBBytes);
+        __syncthreads();
+    }
+    if (warp < kMain / 32) {
+        // ---- loads, split, MMAs ----
+        const int total = my_tiles * nck;
+        int is_q = 0, is_m0 = (int)blockIdx.x * kGemmM, is_ch = 0, is_st = 0;
+        auto issue = [&]() {
+            if (is_q < total) {
+                raw_issue<kGemmM, kMain>(g.A, g.a_m, g.a_k, is_m0, g.M, is_ch * kGemmKc, kend, raw_a(is_st));
+                if (++is_ch == nck) {
+                    is_ch = 0;
+                    is_m0 += (int)gridDim.x * kGemmM;
+                }
+                if (++is_st == kRaw) is_st = 0;
+                ++is_q;
+            }
+            cp_async_commit();
+        };
+        for (int q = 0; q < kRaw - 1; ++q) issue();
+        int rd_st = 0;
+        char* a_hi = split0;
+        char* a_lo = split0 + kABytes;
+        for (int t = 0, q = 0; t < my_tiles; ++t) {
+            const int buf = t & 1;
+            for (int chunk = 0; chunk < nck; ++chunk, ++q) {
+                cp_async_wait_n(kRaw - 2);  // chunk q landed (this thread's copies)
+                bar_main();                 // ... everyone's; raw stage (q - 1) % kRaw is free again
+                issue();
+                if (q >= 1) mbar_wait(&mb_mma, (uint32_t)(q - 1) & 1u);  // the split buffer's MMAs are done
+                tc_after_sync();
+                raw_split<kGemmM, kMain>(ta, raw_a(rd_st), a_hi, a_lo);
+                if (++rd_st == kRaw) rd_st = 0;
+                fence_async_smem();
+                bar_main();
+                if (tid == 0) {
+                    if (chunk == 0 && t >= 2) mbar_wait(&acc_empty[buf], (uint32_t)((t >> 1) - 1) & 1u);
+                    tc_after_sync();
+                    const uint32_t d = tmem + (uint32_t)(buf * kAccCols);
+                    const char* b_hi = bres + (size_t)chunk * 2 * kBBytes;
+                    const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi),
+                                   bl = smem_u32(b_hi + kBBytes);
+#pragma unroll
+                    for (int s = 0; s < kGemmKc / 8; ++s) {
+                        const uint32_t off = (uint32_t)s * 2u * kCoreBytes;
+                        const uint64_t dah = umma_desc(ah + off, kCoreBytes, kGroupBytes);
+                        const uint64_t dal = umma_desc(al + off, kCoreBytes, kGroupBytes);
+                        const uint64_t dbh = umma_desc(bh + off, kCoreBytes, kGroupBytes);
+                        const uint64_t dbl = umma_desc(bl + off, kCoreBytes, kGroupBytes);
+                        mma_tf32(d, dah, dbh, idesc, (chunk > 0 || s > 0) ? 1u : 0u);
+                        mma_tf32(d, dah, dbl, idesc, 1u);
+                        mma_tf32(d, dal, dbh, idesc, 1u);
+                    }
+                    mma_commit(&mb_mma);
+                    if (chunk + 1 == nck) mma_commit(&acc_full[buf]);
+                }
+            }
+        }
+        cp_async_wait<0>();
+    } else {
+        // ---- epilogue: TMEM lane quadrant warp % 4, column half (warp - 8) / 4 ----
+        const int ew = warp - kMain / 32;
+        const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        constexpr int kEpiGroups = NT >= 32 ? 2 : 1;
+        constexpr int kColHalf = NT / kEpiGroups;
+        const int col0 = ((ew >> 2) % kEpiGroups) * kColHalf;
+        const bool epi_warp = (ew >> 2) < kEpiGroups;
+        for (int t = 0; t < my_tiles; ++t) {
+            const int buf = t & 1;
+            const int m0 = ((int)blockIdx.x + t * (int)gridDim.x) * kGemmM;
+            const int m = m0 + (warp & 3) * 32 + lane;
+            const bool row_ok = m < g.M;
+            // the gate loads go out before the wait for the tile's MMAs
+            const float* mrow0 = g.mask && row_ok && epi_warp ? g.mask + (int64_t)m * g.ldmask + col0 : nullptr;
+            const bool mvec = mrow0 && ((uintptr_t)mrow0 & 15) == 0 && (g.ldmask & 3) == 0;
+            uint32_t mb0 = 0xffffffffu, mb1 = 0xffffffffu;  // gate bit words of the column group
+            if (g.maskbits && row_ok && epi_warp) {
+                const uint32_t* pb = g.maskbits + (int64_t)m * g.ldmaskbits + (col0 >> 5);
+                mb0 = __ldg(pb);
+                if (((col0 + kColHalf - 1) >> 5) > (col0 >> 5)) mb1 = __ldg(pb + 1);
+            }
+            mbar_wait(&acc_full[buf], (uint32_t)(t >> 1) & 1u);
+            tc_after_sync();
+            if (epi_warp) {
+#pragma unroll
+                for (int cc = 0; cc < kColHalf; cc += 16) {
+                    const int n0 = col0 + cc;
+                    uint32_t v[16];
+                    tmem_ld16(tl + (uint32_t)(buf * kAccCols + n0), v);
+                    if (!row_ok || n0 >= g.N) continue;
+                    const uint32_t bits = ((n0 >> 5) > (col0 >> 5) ? mb1 : mb0) >> (n0 & 31);
+                    float x[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        x[j] = __uint_as_float(v[j]);
+                        if (g.bias && n0 + j < g.N) x[j] += __ldg(g.bias + n0 + j);
+                        if (g.relu) x[j] = fmaxf(x[j], 0.f);
+                        if (!((bits >> j) & 1u)) x[j] = 0.f;
+                    }
+                    float* crow = C_row(g, m) + n0;
+                    const float* mrow = mrow0 ? mrow0 + cc : nullptr;
+                    if (n0 + 16 <= g.N && ((uintptr_t)crow & 15) == 0 && (!mrow || mvec)) {
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            float4 o = make_float4(x[4 * q4], x[4 * q4 + 1], x[4 * q4 + 2], x[4 * q4 + 3]);
+                            if (mrow) {
+                                const float4 mq = __ldg(reinterpret_cast<const float4*>(mrow) + q4);
+                                if (!(mq.x > 0.f)) o.x = 0.f;
+                                if (!(mq.y > 0.f)) o.y = 0.f;
+                                if (!(mq.z > 0.f)) o.z = 0.f;
+                                if (!(mq.w > 0.f)) o.w = 0.f;
+                            }
+                            reinterpret_cast<float4*>(crow)[q4] = o;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (n0 + j < g.N) crow[j] = (mrow && !(mrow[j] > 0.f)) ? 0.f : x[j];
+                    }
+                }
+            }
+            tc_before_sync();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        }
+    }
+    tc_before_sync();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
+}
+
 // out[i] (+)= sum_s part[s * stride + i]
 __global__ void k_reduce_slices(const float* __restrict__ part, int slices, int64_t stride, int64_t n,
                                 float* __restrict__ out, int accumulate) {
@@ -676,6 +868,10 @@ int launch_gemm_tf32x3(const GemmArgs& g, int slices, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         gemm_attrs<false, false>(); gemm_attrs<false, true>(); gemm_attrs<true, false>(); gemm_attrs<true, true>();
+        cudaFuncSetAttribute(k_gemm_ws<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmMaxSmem);
+        cudaFuncSetAttribute(k_gemm_ws<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmMaxSmem);
+        cudaFuncSetAttribute(k_gemm_ws<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmMaxSmem);
+        cudaFuncSetAttribute(k_gemm_ws<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmMaxSmem);
         attr = true;
     }
     if (g.M <= 0 || g.N <= 0) return 0;
@@ -695,6 +891,18 @@ int launch_gemm_tf32x3(const GemmArgs& g, int slices, cudaStream_t st) {
         p.bytes = gemm_bytes(nt, nck, p.b_res, g.a_m == 1, g.b_n == 1, p.raw);
     }
     const bool flush = g.k_per_slice > kFlushChunks * kGemmKc;
+    static const bool ws_off = [] {  // TSB_GEMM_WS=0: the single-role kernel (A/B timing)
+        const char* e = std::getenv("TSB_GEMM_WS");
+        return e && e[0] == '0';
+    }();
+    if (!flush && p.b_res && nck > 0 && slices <= 1 && g.K <= g.k_per_slice && !ws_off) {
+        const size_t bytes = p.bytes;
+        if (nt == 16) k_gemm_ws<16><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
+        else if (nt == 32) k_gemm_ws<32><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
+        else if (nt == 64) k_gemm_ws<64><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
+        else k_gemm_ws<128><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
+        return 1;
+    }
     if (flush) return p.b_res ? gemm_dispatch<true, true>(g, grid, p, st) : gemm_dispatch<true, false>(g, grid, p, st);
     return p.b_res ? gemm_dispatch<false, true>(g, grid, p, st) : gemm_dispatch<false, false>(g, grid, p, st);
 }

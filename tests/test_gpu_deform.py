@@ -75,6 +75,24 @@ def test_gemm_bulk_copied_transposed_operands(tsb, ctx, n, slices):
     assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max()
 
 
+@pytest.mark.parametrize("N,K", [(128, 128), (84, 128), (128, 3), (32, 64), (16, 40)])
+def test_gemm_many_tiles_resident_weights(tsb, ctx, N, K):
+    """delta W over more row tiles than CTAs (weights resident; the warp-specialised kernel:
+    the epilogue drains one TMEM accumulator while the next tile fills the other), with and
+    without a ReLU gate, partial column groups included."""
+    rng = np.random.default_rng(N * 1000 + K)
+    n = 148 * 128 * 2 + 777
+    delta = rng.normal(size=(n, K)).astype(np.float32)
+    W = rng.normal(size=(K, N)).astype(np.float32)
+    ref = delta.astype(np.float64) @ W.astype(np.float64)
+    tol = 2e-6 * np.abs(ref).max() * np.sqrt(K)
+    got = gemm(tsb, ctx, delta, K, 1, W, 1, N, n, N, K)
+    assert np.abs(got - ref).max() <= tol
+    mask = (rng.random((n, N)) > 0.5).astype(np.float32)
+    got2 = gemm(tsb, ctx, delta, K, 1, W, 1, N, n, N, K, mask=mask)
+    assert np.abs(got2 - ref * mask).max() <= tol
+
+
 def _nets(tsb, ctx, cfg, seed, n=3000):
     from oracle import deform as od
     onet = od.DeformNet.init(cfg, seed)
