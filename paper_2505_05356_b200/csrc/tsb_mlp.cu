@@ -1100,7 +1100,12 @@ __global__ void k_pack_weights(MlpLayout lay, const float* __restrict__ params, 
     }
 }
 
-__global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_fwd_fused(MlpFwdArgs a) {
+__device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, %0;" ::"n"(kMlpThreads) : "memory"); }
+
+// kMlpThreads compute threads (thread 0 issues the MMAs) + one producer warp whose lane 0
+// streams the weight chunks into the ring as stages free up (the MMA issuer never waits
+// for the tensor core, only for data).
+__global__ void __launch_bounds__(kMlpThreads + 32, 1) k_mlp_fwd_fused(MlpFwdArgs a) {
     extern __shared__ __align__(1024) char smem[];
     __shared__ __align__(8) uint64_t mb_full[kMlpStages], mb_empty[kMlpStages], mb_layer;
     __shared__ uint32_t tmem_base_s;
@@ -1143,16 +1148,17 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_fwd_fused(MlpFwdArgs a) 
         bytes = (uint32_t)lay.nt[l] * kGemmKc * 8u;
         return a.wpack + lay.chunk_off[l] + (int64_t)(local - base) * bytes;
     };
-    auto issue_copy = [&](uint32_t q) {  // thread 0 only
-        if (q >= total) return;
-        const int st = (int)(q % kMlpStages);
-        if (q >= (uint32_t)kMlpStages) mbar_wait(&mb_empty[st], ((q / kMlpStages) - 1) & 1u);
-        uint32_t bytes;
-        const char* src = chunk_src(q, bytes);
-        bulk_g2s(ring + (size_t)st * kMlpStageBytes, src, bytes, &mb_full[st]);
-    };
-    if (tid == 0)
-        for (uint32_t q = 0; q < (uint32_t)kMlpStages - 1; ++q) issue_copy(q);
+    if (warp == kMlpThreads / 32) {  // ---- producer warp ----
+        if (lane == 0)
+            for (uint32_t q = 0; q < total; ++q) {
+                const int st = (int)(q % kMlpStages);
+                if (q >= (uint32_t)kMlpStages) mbar_wait(&mb_empty[st], ((q / kMlpStages) - 1) & 1u);
+                uint32_t bytes;
+                const char* src = chunk_src(q, bytes);
+                bulk_g2s(ring + (size_t)st * kMlpStageBytes, src, bytes, &mb_full[st]);
+            }
+        __syncwarp();
+    } else {
 
     uint32_t q = 0;          // next chunk to consume
     uint32_t lphase = 0;     // mb_layer completions
@@ -1192,7 +1198,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_fwd_fused(MlpFwdArgs a) 
             }
         }
         fence_async_smem();
-        __syncthreads();
+        bar_compute();
 
         for (int l = 0; l < lay.layers; ++l) {
             const int nt = lay.nt[l];
@@ -1230,7 +1236,6 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_fwd_fused(MlpFwdArgs a) 
                         mma_tf32(tmem, dal, dbh, idesc, 1u);
                     }
                     mma_commit(&mb_empty[st]);
-                    issue_copy(q + kMlpStages - 1);
                 }
                 mma_commit(&mb_layer);
             } else if (tid != 0) {
@@ -1238,7 +1243,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_fwd_fused(MlpFwdArgs a) 
             }
             mbar_wait(&mb_layer, lphase & 1u);
             ++lphase;
-            if (store_x || store_h) __syncthreads();  // the epilogue overwrites A
+            if (store_x || store_h) bar_compute();  // the epilogue overwrites A
             tc_after_sync();
             // ---- epilogue: bias, ReLU; split back into A for the next layer ----
             const int r = (warp & 3) * 32 + lane;
@@ -1275,13 +1280,276 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_fwd_fused(MlpFwdArgs a) 
             }
             fence_async_smem();
             tc_before_sync();
-            __syncthreads();
+            bar_compute();
         }
     }
+    }  // compute threads
     tc_before_sync();
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
 }
+
+// ---------------------------------------------------------------------------
+// The same forward with the activations in tensor memory.  The layer input A (hi / lo) is
+// the MMA's A operand read from TMEM (tcgen05.mma ... [a-tmem]): the epilogue moves the
+// accumulator D -> registers (bias, ReLU, split) -> A with tcgen05.st, so shared memory
+// holds only the weight ring, which is then deep enough (7 stages of 32 K-columns) to keep
+// the tensor core fed from L2.  TMEM: D at column 0, A hi at 128, A lo at 256 (512
+// allocated, one CTA per SM).  The activations the backward reads (encoding X, hidden H
+// + ReLU gate bits) go to global memory straight from the epilogue's registers.
+// ---------------------------------------------------------------------------
+constexpr int kMlpStagesT = 4;
+constexpr int kStgLd = 132;  // fp32 staging tile row stride (floats): the layer input, stored for the backward
+constexpr uint32_t kTmA = 128, kTmAlo = 256;  // TMEM column offsets
+
+__device__ __forceinline__ void mma_tf32_at(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st1(uint32_t taddr, uint32_t v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+
+// Rows m0 .. m0+127 (< n), columns [0, ncols) of the fp32 staging tile -> dst[m * ld + c], one
+// row per warp instruction (coalesced), + the ReLU gate bits (ncols a multiple of 32).
+__device__ __forceinline__ void store_staged(const float* S, float* dst, int64_t ld, int64_t m0, int64_t n, int ncols,
+                                             uint32_t* bits, int w0, int nwarps) {
+    const int lane = threadIdx.x & 31, warp = (int)(threadIdx.x >> 5) - w0;
+    const int nq = ncols / 4;
+    const int64_t ldw = ncols / 32;
+    for (int rr = warp; rr < 128; rr += nwarps) {
+        const int64_t m = m0 + rr;
+        if (m >= n) break;
+        const float* srow = S + rr * kStgLd;
+        float* drow = dst + m * ld;
+        const bool al = ((((uintptr_t)drow) | (ld * 4)) & 15) == 0;
+        for (int q0 = 0; q0 < nq; q0 += 32) {
+            const int q = q0 + lane;
+            const float4 v = q < nq ? *reinterpret_cast<const float4*>(srow + 4 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (q < nq) {
+                if (al) {
+                    *reinterpret_cast<float4*>(drow + 4 * q) = v;
+                } else {
+                    drow[4 * q] = v.x; drow[4 * q + 1] = v.y; drow[4 * q + 2] = v.z; drow[4 * q + 3] = v.w;
+                }
+            }
+            if (bits) {
+                uint32_t nib = (v.x > 0.f ? 1u : 0u) | (v.y > 0.f ? 2u : 0u) | (v.z > 0.f ? 4u : 0u) | (v.w > 0.f ? 8u : 0u);
+                nib <<= 4 * (lane & 7);
+                nib |= __shfl_xor_sync(0xffffffffu, nib, 1);
+                nib |= __shfl_xor_sync(0xffffffffu, nib, 2);
+                nib |= __shfl_xor_sync(0xffffffffu, nib, 4);
+                if ((lane & 7) == 0 && q < nq) bits[m * ldw + q / 8] = nib;
+            }
+        }
+    }
+}
+
+// kMlpThreads compute threads (thread 0 issues the MMAs) + one producer warp whose lane 0
+// streams the weight chunks into the ring as stages free up (the MMA issuer never waits
+// for the tensor core, only for data).
+__global__ void __launch_bounds__(kMlpThreads + 32, 1) k_mlp_fwd_tm(MlpFwdArgs a) {
+    extern __shared__ __align__(1024) char smem[];
+    __shared__ __align__(8) uint64_t mb_full[kMlpStagesT], mb_empty[kMlpStagesT], mb_layer;
+    __shared__ uint32_t tmem_base_s;
+    char* ring = smem;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const MlpLayout& lay = a.lay;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_s))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < kMlpStagesT; ++i) {
+            mbar_init(&mb_full[i], 1);
+            mbar_init(&mb_empty[i], 1);
+        }
+        mbar_init(&mb_layer, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    const uint32_t tmem = tmem_base_s;
+    const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's lane quadrant
+    const int wg = warp >> 2;                                          // column group (0..3)
+    const int ntiles = (int)((a.n + 127) / 128);
+    const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const uint32_t total = (uint32_t)my_tiles * (uint32_t)lay.total_chunks;
+
+    auto chunk_src = [&](uint32_t q, uint32_t& bytes) -> const char* {
+        const uint32_t local = q % (uint32_t)lay.total_chunks;
+        int l = 0;
+        uint32_t base = 0;
+        while (local >= base + (uint32_t)lay.chunks[l]) {
+            base += lay.chunks[l];
+            ++l;
+        }
+        bytes = (uint32_t)lay.nt[l] * kGemmKc * 8u;
+        return a.wpack + lay.chunk_off[l] + (int64_t)(local - base) * bytes;
+    };
+    if (warp == kMlpThreads / 32) {  // ---- producer warp ----
+        if (lane == 0)
+            for (uint32_t q = 0; q < total; ++q) {
+                const int st = (int)(q % kMlpStagesT);
+                if (q >= (uint32_t)kMlpStagesT) mbar_wait(&mb_empty[st], ((q / kMlpStagesT) - 1) & 1u);
+                uint32_t bytes;
+                const char* src = chunk_src(q, bytes);
+                bulk_g2s(ring + (size_t)st * kMlpStageBytes, src, bytes, &mb_full[st]);
+            }
+        __syncwarp();
+    } else {
+
+    uint32_t q = 0, lphase = 0;
+    const int ex = 1 + 2 * a.l_x;
+    const int kpad0 = lay.chunks[0] * kGemmKc;
+    float* S = reinterpret_cast<float*>(smem + (size_t)kMlpStagesT * kMlpStageBytes);  // [128][kStgLd]
+    const int r = (warp & 3) * 32 + lane;  // = the TMEM lane this thread may access
+    float* srow = S + r * kStgLd;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t m0 = (int64_t)tile * 128;
+        const int64_t m = m0 + r;
+        const bool rv = m < a.n;
+        // ---- positional encoding of the tile's rows into the staging tile (warp group: x, y, z,
+        //      time + zero padding), then A = split(staging) into TMEM ----
+        {
+            const int kb = wg * ex;
+            if (wg < 3) {
+                const double v = rv ? (double)a.pos[m * a.pos_stride + wg] * a.inv_scale : 0.0;
+                srow[kb] = (float)v;
+                double f = v;
+                for (int l = 0; l < a.l_x; ++l, f *= 2.0) {
+                    double sn, co;
+                    sincospi(f, &sn, &co);
+                    srow[kb + 1 + 2 * l] = (float)sn;
+                    srow[kb + 2 + 2 * l] = (float)co;
+                }
+            } else {
+                for (int k = kb; k < kpad0; ++k) srow[k] = k - kb < a.te.n ? a.te.v[k - kb] : 0.f;
+            }
+            bar_compute();
+            for (int ch = wg; ch < kpad0 / 16; ch += 4) {
+                uint32_t hv[16], lv[16];
+#pragma unroll
+                for (int j = 0; j < 16; j += 4) {
+                    const float4 x = *reinterpret_cast<const float4*>(srow + ch * 16 + j);
+                    float h, lo;
+                    split_exact(x.x, h, lo); hv[j] = __float_as_uint(h); lv[j] = __float_as_uint(lo);
+                    split_exact(x.y, h, lo); hv[j + 1] = __float_as_uint(h); lv[j + 1] = __float_as_uint(lo);
+                    split_exact(x.z, h, lo); hv[j + 2] = __float_as_uint(h); lv[j + 2] = __float_as_uint(lo);
+                    split_exact(x.w, h, lo); hv[j + 3] = __float_as_uint(h); lv[j + 3] = __float_as_uint(lo);
+                }
+                tmem_st16(tl + kTmA + (uint32_t)(ch * 16), hv);
+                tmem_st16(tl + kTmAlo + (uint32_t)(ch * 16), lv);
+            }
+            tmem_st_wait();
+        }
+        tc_before_sync();
+        bar_compute();
+
+        for (int l = 0; l < lay.layers; ++l) {
+            const int nt = lay.nt[l];
+            // the staging tile holds this layer's input: warps 1-15 store it for the backward
+            // (X, or H of the layer below + its ReLU gate bits) while thread 0 issues the MMAs
+            if (warp > 0) {
+                if (l == 0 && a.X) store_staged(S, a.X, a.ldx, m0, a.n, a.din, nullptr, 1, kMlpThreads / 32 - 1);
+                if (l > 0 && a.H[l - 1])
+                    store_staged(S, a.H[l - 1], a.ldh, m0, a.n, lay.rows[l - 1], a.Hbits[l - 1], 1,
+                                 kMlpThreads / 32 - 1);
+            }
+            if (tid == 0) {
+                tc_after_sync();
+                const uint32_t idesc = idesc_tf32(128, nt);
+                for (int c = 0; c < lay.chunks[l]; ++c, ++q) {
+                    const int st = (int)(q % kMlpStagesT);
+                    mbar_wait(&mb_full[st], (q / kMlpStagesT) & 1u);
+                    const uint32_t bh = smem_u32(ring + (size_t)st * kMlpStageBytes);
+                    const uint32_t bl = bh + (uint32_t)nt * kGemmKc * 4;
+#pragma unroll
+                    for (int s = 0; s < kGemmKc / 8; ++s) {
+                        const uint32_t k0 = (uint32_t)(c * kGemmKc + 8 * s);
+                        const uint32_t boff = (uint32_t)(2 * s) * kCoreBytes;
+                        const uint64_t dbh = umma_desc(bh + boff, kCoreBytes, kGroupBytes);
+                        const uint64_t dbl = umma_desc(bl + boff, kCoreBytes, kGroupBytes);
+                        mma_tf32_at(tmem, tmem + kTmA + k0, dbh, idesc, (c > 0 || s > 0) ? 1u : 0u);
+                        mma_tf32_at(tmem, tmem + kTmA + k0, dbl, idesc, 1u);
+                        mma_tf32_at(tmem, tmem + kTmAlo + k0, dbh, idesc, 1u);
+                    }
+                    mma_commit(&mb_empty[st]);
+                }
+                mma_commit(&mb_layer);
+            } else {
+                q += lay.chunks[l];
+            }
+            mbar_wait(&mb_layer, lphase & 1u);
+            ++lphase;
+            bar_compute();  // the staging tile is free again
+            tc_after_sync();
+            const float* bias = a.params + lay.b_off[l];
+            const int rows = lay.rows[l];
+            if (l + 1 < lay.layers) {
+                // ---- hidden epilogue: D -> bias, ReLU -> staging (fp32) and A (split) for layer l + 1 ----
+                const int kpn = lay.chunks[l + 1] * kGemmKc;  // the next layer's (padded) K
+                for (int ch = wg; ch < kpn / 16; ch += 4) {
+                    const int col = ch * 16;
+                    uint32_t v[16], hv[16], lv[16];
+                    float x[16];
+                    if (col < nt) {
+                        tmem_ld16(tl + (uint32_t)col, v);
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            x[j] = col + j < rows ? fmaxf(__uint_as_float(v[j]) + __ldg(bias + col + j), 0.f) : 0.f;
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) x[j] = 0.f;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        float h, lo;
+                        split_exact(x[j], h, lo);
+                        hv[j] = __float_as_uint(h);
+                        lv[j] = __float_as_uint(lo);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4)
+                        *reinterpret_cast<float4*>(srow + col + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+                    tmem_st16(tl + kTmA + (uint32_t)col, hv);
+                    tmem_st16(tl + kTmAlo + (uint32_t)col, lv);
+                }
+                tmem_st_wait();
+            } else if (warp < 4) {
+                uint32_t v[16];
+                tmem_ld16(tl, v);
+                if (rv)
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j < rows) a.out[m * a.out_stride + j] = __uint_as_float(v[j]) + __ldg(bias + j);
+            }
+            tc_before_sync();
+            bar_compute();
+        }
+    }
+    }  // compute threads
+    tc_before_sync();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+size_t mlp_tm_smem_bytes() { return (size_t)kMlpStagesT * kMlpStageBytes + (size_t)128 * kStgLd * 4; }
 
 size_t mlp_fused_smem_bytes() { return 2 * (size_t)kMlpAHalf + (size_t)kMlpStages * kMlpStageBytes; }
 
@@ -1293,11 +1561,20 @@ void launch_mlp_fwd_fused(const MlpFwdArgs& a, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_mlp_fwd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mlp_fused_smem_bytes());
+        cudaFuncSetAttribute(k_mlp_fwd_tm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mlp_tm_smem_bytes());
         attr = true;
     }
     if (a.n <= 0) return;
     const int ntiles = (int)((a.n + 127) / 128);
-    k_mlp_fwd_fused<<<std::min(ntiles, 148), kMlpThreads, mlp_fused_smem_bytes(), st>>>(a);
+    static const bool tmem_a = [] {  // TSB_MLP_ATMEM=0: activations in shared memory (A/B timing; 3.5 vs 2.5 ms)
+        const char* e = std::getenv("TSB_MLP_ATMEM");
+        return !(e && e[0] == '0');
+    }();
+    if (tmem_a) {
+        k_mlp_fwd_tm<<<std::min(ntiles, 148), kMlpThreads + 32, mlp_tm_smem_bytes(), st>>>(a);
+        return;
+    }
+    k_mlp_fwd_fused<<<std::min(ntiles, 148), kMlpThreads + 32, mlp_fused_smem_bytes(), st>>>(a);
 }
 
 }  // namespace tsb
