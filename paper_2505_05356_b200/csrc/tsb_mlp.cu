@@ -636,6 +636,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
 }
 
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t* v) {  // (no wait: tmem_wait_ld)
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// 256-bit global store (sm_100): one whole 32-byte sector per thread
+__device__ __forceinline__ void st_v8(float* p, const float* x) {
+    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(x[0]), "f"(x[1]), "f"(x[2]),
+                 "f"(x[3]), "f"(x[4]), "f"(x[5]), "f"(x[6]), "f"(x[7])
+                 : "memory");
+}
+
 __device__ __forceinline__ float* C_row(const GemmArgs& g, int m) { return g.C + (int64_t)m * g.ldc; }
 
 // Warp-specialised variant for resident-B GEMMs without split-K (the input gradients
@@ -779,25 +795,37 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(GemmArgs g, int kRa
             }
             mbar_wait(&acc_full[buf], (uint32_t)(t >> 1) & 1u);
             tc_after_sync();
+            // the whole column group out of TMEM first (one wait), then the accumulator is
+            // released for the tile after next before any store is issued
+            uint32_t v[kColHalf];
             if (epi_warp) {
+#pragma unroll
+                for (int cc = 0; cc < kColHalf; cc += 16) tmem_ld16_nw(tl + (uint32_t)(buf * kAccCols + col0 + cc), v + cc);
+                tmem_wait_ld();
+            }
+            tc_before_sync();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[buf]);
+            if (epi_warp && row_ok) {
 #pragma unroll
                 for (int cc = 0; cc < kColHalf; cc += 16) {
                     const int n0 = col0 + cc;
-                    uint32_t v[16];
-                    tmem_ld16(tl + (uint32_t)(buf * kAccCols + n0), v);
-                    if (!row_ok || n0 >= g.N) continue;
+                    if (n0 >= g.N) continue;
                     const uint32_t bits = ((n0 >> 5) > (col0 >> 5) ? mb1 : mb0) >> (n0 & 31);
                     float x[16];
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
-                        x[j] = __uint_as_float(v[j]);
+                        x[j] = __uint_as_float(v[cc + j]);
                         if (g.bias && n0 + j < g.N) x[j] += __ldg(g.bias + n0 + j);
                         if (g.relu) x[j] = fmaxf(x[j], 0.f);
                         if (!((bits >> j) & 1u)) x[j] = 0.f;
                     }
                     float* crow = C_row(g, m) + n0;
                     const float* mrow = mrow0 ? mrow0 + cc : nullptr;
-                    if (n0 + 16 <= g.N && ((uintptr_t)crow & 15) == 0 && (!mrow || mvec)) {
+                    if (n0 + 16 <= g.N && !mrow && ((uintptr_t)crow & 31) == 0) {
+                        st_v8(crow, x);  // 32-byte stores: whole sectors per lane
+                        st_v8(crow + 8, x + 8);
+                    } else if (n0 + 16 <= g.N && ((uintptr_t)crow & 15) == 0 && (!mrow || mvec)) {
 #pragma unroll
                         for (int q4 = 0; q4 < 4; ++q4) {
                             float4 o = make_float4(x[4 * q4], x[4 * q4 + 1], x[4 * q4 + 2], x[4 * q4 + 3]);
@@ -817,9 +845,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(GemmArgs g, int kRa
                     }
                 }
             }
-            tc_before_sync();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[buf]);
         }
     }
     tc_before_sync();

@@ -1,12 +1,10 @@
 set -e
 mkdir -p gpurun_out
-python -m pytest tests/test_gpu_deform.py -m gpu -x -q 2>&1 | tail -5 > gpurun_out/abd_tests.log
-TSB_MLP_ATMEM=1 python -m pytest tests/test_gpu_deform.py -m gpu -x -q 2>&1 | tail -2 >> gpurun_out/abd_tests.log
+python -m pytest tests/test_gpu_deform.py -m gpu -x -q 2>&1 | tail -3 > gpurun_out/abd_tests.log
 for i in 1 2; do
-  for v in new old tm; do
-    unset TSB_LIB TSB_MLP_ATMEM
+  for v in new old; do
+    unset TSB_LIB
     if [ $v = old ]; then export TSB_LIB=$PWD/build_var/d2/libtsb.so; fi
-    if [ $v = tm ]; then export TSB_MLP_ATMEM=1; fi
     echo "$v$i $(python tools/bench_deform.py 2>&1 | tail -1)" >> gpurun_out/abd_summary.txt
   done
 done
