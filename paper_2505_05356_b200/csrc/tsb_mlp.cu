@@ -207,16 +207,18 @@ struct GemmPlan {
 };
 constexpr int kMaxRaw = 6;  // (cp_async_wait_n covers up to 4 pending groups)
 // (one split buffer: measured faster than two with a stage fewer in flight)
-inline size_t gemm_bytes(int nt, int nck, bool b_res, bool ta, bool tb, int raw) {
+inline size_t gemm_bytes(int nt, int nck, bool b_res, bool ta, bool tb, int raw, int nsplit = 1) {
     if (b_res) return (size_t)nck * split_bytes(nt) + raw * raw_bytes(kGemmM, ta) + split_bytes(kGemmM);
-    return raw * (raw_bytes(kGemmM, ta) + raw_bytes(nt, tb)) + split_bytes(kGemmM) + split_bytes(nt);
+    return raw * (raw_bytes(kGemmM, ta) + raw_bytes(nt, tb)) + nsplit * (split_bytes(kGemmM) + split_bytes(nt));
 }
-inline GemmPlan gemm_plan(int nt, int nck, bool many_tiles, bool ta, bool tb) {
+// flush: a weight-gradient reduction (two split buffers when B is streamed)
+inline GemmPlan gemm_plan(int nt, int nck, bool many_tiles, bool ta, bool tb, bool flush) {
     GemmPlan p{};
     p.b_res = many_tiles && nck > 0 && gemm_bytes(nt, nck, true, ta, tb, 3) <= (size_t)kGemmMaxSmem;
+    const int ns = flush && !p.b_res ? 2 : 1;
     p.raw = 2;
-    while (p.raw < kMaxRaw && gemm_bytes(nt, nck, p.b_res, ta, tb, p.raw + 1) <= (size_t)kGemmMaxSmem) ++p.raw;
-    p.bytes = gemm_bytes(nt, nck, p.b_res, ta, tb, p.raw);
+    while (p.raw < kMaxRaw && gemm_bytes(nt, nck, p.b_res, ta, tb, p.raw + 1, ns) <= (size_t)kGemmMaxSmem) ++p.raw;
+    p.bytes = gemm_bytes(nt, nck, p.b_res, ta, tb, p.raw, ns);
     return p;
 }
 
@@ -360,9 +362,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
     __shared__ __align__(8) uint64_t mb_tile;
     __shared__ __align__(8) uint64_t mb_raw[kMaxRaw];  // bulk mode: raw stage filled
     __shared__ uint32_t tmem_base_s;
-    constexpr int kSplit = 1;
+    // weight-gradient reductions (FLUSH, both operands streamed): two split buffers (the
+    // split of chunk q + 1 overlaps the MMAs of chunk q) and two TMEM accumulators (a
+    // group's flush into registers overlaps the next group's MMAs)
+    constexpr int kSplit = (FLUSH && !BRES) ? 2 : 1;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    constexpr int kTmemCols = NT <= 32 ? 32 : (NT <= 64 ? 64 : (NT <= 128 ? 128 : 256));
+    constexpr int kAccCols = NT <= 32 ? 32 : (NT <= 64 ? 64 : (NT <= 128 ? 128 : 256));
+    constexpr int kTmemCols = FLUSH ? 2 * kAccCols : kAccCols;
     constexpr uint32_t kABytes = kGemmM * kGemmKc * 4, kBBytes = NT * kGemmKc * 4;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
@@ -473,6 +479,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
     const bool do_rsum = g.rowsum && ta && !BRES;
     uint32_t tphase = 0;  // mb_tile completions waited for
     float acc[FLUSH ? kColHalf : 1];
+    int G = -1;  // running accumulation group (FLUSH: its accumulator is G & 1)
+    auto flush = [&](int grp) {  // add group grp's accumulator (MMAs committed to mb_tile) into acc
+        mbar_wait(&mb_tile, tphase & 1u);
+        ++tphase;
+        tc_after_sync();
+#pragma unroll
+        for (int cc = 0; cc < kColHalf; cc += 16) {
+            uint32_t v[16];
+            tmem_ld16(tl + (uint32_t)((grp & 1) * kAccCols + col0 + cc), v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[(FLUSH ? cc : 0) + j] += __uint_as_float(v[j]);
+        }
+        tc_before_sync();  // the group after next overwrites this accumulator
+    };
     for (int t = 0, q = 0; t < my_tiles; ++t) {
         const int m0 = ((int)blockIdx.x + t * (int)gridDim.x) * kGemmM;
 #pragma unroll
@@ -505,6 +525,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
             const bool group_start = FLUSH ? (chunk % kFlushChunks) == 0 : chunk == 0;
             const bool group_end = FLUSH ? ((chunk % kFlushChunks) == kFlushChunks - 1 || chunk + 1 == nck)
                                          : chunk + 1 == nck;
+            if (group_start) ++G;
+            const uint32_t dacc = tmem + (uint32_t)(FLUSH ? (G & 1) * kAccCols : 0);
             if (tid == 0) {
                 tc_after_sync();
                 char* b_hi = BRES ? bres + (size_t)chunk * 2 * kBBytes : sb_hi;
@@ -517,27 +539,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
                     const uint64_t dal = umma_desc(al + off, kCoreBytes, kGroupBytes);
                     const uint64_t dbh = umma_desc(bh + off, kCoreBytes, kGroupBytes);
                     const uint64_t dbl = umma_desc(bl + off, kCoreBytes, kGroupBytes);
-                    mma_tf32(tmem, dah, dbh, idesc, (!group_start || s > 0) ? 1u : 0u);
-                    mma_tf32(tmem, dah, dbl, idesc, 1u);
-                    mma_tf32(tmem, dal, dbh, idesc, 1u);
+                    mma_tf32(dacc, dah, dbh, idesc, (!group_start || s > 0) ? 1u : 0u);
+                    mma_tf32(dacc, dah, dbl, idesc, 1u);
+                    mma_tf32(dacc, dal, dbh, idesc, 1u);
                 }
                 mma_commit(&mb_mma[q % kSplit]);
                 if (group_end) mma_commit(&mb_tile);
             }
-            if (FLUSH && group_end) {
-                mbar_wait(&mb_tile, tphase & 1u);
-                ++tphase;
-                tc_after_sync();
-#pragma unroll
-                for (int cc = 0; cc < kColHalf; cc += 16) {
-                    uint32_t v[16];
-                    tmem_ld16(tl + (uint32_t)(col0 + cc), v);
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) acc[(FLUSH ? cc : 0) + j] += __uint_as_float(v[j]);
-                }
-                tc_before_sync();  // the next group's first MMA overwrites the accumulator
-            }
+            // the previous group's flush, while this group's first MMAs run
+            if (FLUSH && group_start && chunk > 0) flush(G - 1);
         }
+        if (FLUSH && nck > 0) flush(G);  // the tile's last group
         const bool any = nck > 0;
         // the epilogue's mask loads go out before the wait for the tile's last MMAs
         const int m = m0 + (warp & 3) * 32 + lane;
@@ -906,16 +918,16 @@ int launch_gemm_tf32x3(const GemmArgs& g, int slices, cudaStream_t st) {
     const int nck = (kps + kGemmKc - 1) / kGemmKc;
     const int gx = std::min(ntiles, std::max(1, 148 / std::max(1, slices)));
     const dim3 grid(gx, std::max(1, slices));
-    GemmPlan p = gemm_plan(nt, nck, ntiles > gx, g.a_m == 1, g.b_n == 1);
+    const bool flush = g.k_per_slice > kFlushChunks * kGemmKc;
+    GemmPlan p = gemm_plan(nt, nck, ntiles > gx, g.a_m == 1, g.b_n == 1, flush);
     static const int raw_cap = [] {  // TSB_GEMM_RAW: cap on the raw stages (A/B timing)
         const char* e = std::getenv("TSB_GEMM_RAW");
         return e ? std::atoi(e) : kMaxRaw;
     }();
     if (p.raw > raw_cap && raw_cap >= 2) {
         p.raw = raw_cap;
-        p.bytes = gemm_bytes(nt, nck, p.b_res, g.a_m == 1, g.b_n == 1, p.raw);
+        p.bytes = gemm_bytes(nt, nck, p.b_res, g.a_m == 1, g.b_n == 1, p.raw, flush && !p.b_res ? 2 : 1);
     }
-    const bool flush = g.k_per_slice > kFlushChunks * kGemmKc;
     static const bool ws_off = [] {  // TSB_GEMM_WS=0: the single-role kernel (A/B timing)
         const char* e = std::getenv("TSB_GEMM_WS");
         return e && e[0] == '0';
