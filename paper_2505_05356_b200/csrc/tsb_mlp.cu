@@ -307,7 +307,7 @@ __device__ __forceinline__ void raw_issue(const float* __restrict__ P, int64_t s
 // rows / columns the epilogue discards).
 template <int R, int NTHR = kGemmThreads>
 __device__ __forceinline__ void raw_split(bool lay_t, const char* raw, char* hi, char* lo, int kvalid = kGemmKc,
-                                          double* rsum = nullptr, int ldr = R) {
+                                          float* rsum = nullptr, int ldr = R) {
     constexpr int kIt = (R * 8 + NTHR - 1) / NTHR;
     if (!lay_t) {
 #pragma unroll
@@ -343,7 +343,7 @@ __device__ __forceinline__ void raw_split(bool lay_t, const char* raw, char* hi,
             const uint32_t o = core_off(r, 4 * kb);
             *reinterpret_cast<float4*>(hi + o) = h;
             *reinterpret_cast<float4*>(lo + o) = l;
-            if (rsum) rsum[it] += (double)((v.x + v.y) + (v.z + v.w));  // the fused row sum (bias gradient)
+            if (rsum) rsum[it] += (v.x + v.y) + (v.z + v.w);  // the fused row sum (bias gradient), per group
         }
     }
 }
@@ -473,9 +473,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
     uint32_t rd_ph = 0;    // its fill parity (bulk mode)
     // fused row sums of A (the bias gradient of a weight-gradient GEMM): per thread its rows
     constexpr int kRsIt = (kGemmM * 8 + kGemmThreads - 1) / kGemmThreads;
+    // (fp32 within an accumulation group of kFlushChunks chunks, folded into fp64 per group:
+    // an fp64 add chain per chunk stalled the split)
     double rsum[kRsIt];
+    float rsf[kRsIt];
 #pragma unroll
-    for (int i = 0; i < kRsIt; ++i) rsum[i] = 0.0;
+    for (int i = 0; i < kRsIt; ++i) {
+        rsum[i] = 0.0;
+        rsf[i] = 0.f;
+    }
     const bool do_rsum = g.rowsum && ta && !BRES;
     uint32_t tphase = 0;  // mb_tile completions waited for
     float acc[FLUSH ? kColHalf : 1];
@@ -513,7 +519,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
             char* a_lo = a_hi + kABytes;
             char* sb_hi = a_lo + kABytes;  // split B (not resident)
             const int kvalid = bulk ? min(kGemmKc, kend - k0) : kGemmKc;
-            raw_split<kGemmM>(ta, raw_a(rd_st), a_hi, a_lo, kvalid, do_rsum ? rsum : nullptr, lda);
+            raw_split<kGemmM>(ta, raw_a(rd_st), a_hi, a_lo, kvalid, do_rsum ? rsf : nullptr, lda);
             if (!BRES) raw_split<NT>(tb, raw_b(rd_st), sb_hi, sb_hi + kBBytes, kvalid, nullptr, ldb);
             if (++rd_st == kRaw) {
                 rd_st = 0;
@@ -526,6 +532,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
             const bool group_end = FLUSH ? ((chunk % kFlushChunks) == kFlushChunks - 1 || chunk + 1 == nck)
                                          : chunk + 1 == nck;
             if (group_start) ++G;
+            if (do_rsum && group_end) {
+#pragma unroll
+                for (int i = 0; i < kRsIt; ++i) {
+                    rsum[i] += (double)rsf[i];
+                    rsf[i] = 0.f;
+                }
+            }
             const uint32_t dacc = tmem + (uint32_t)(FLUSH ? (G & 1) * kAccCols : 0);
             if (tid == 0) {
                 tc_after_sync();
