@@ -972,8 +972,17 @@ namespace tsb {
 // DeformNet helpers (deform.cpp:10-26, 60-78, 142-155)
 // ---------------------------------------------------------------------------
 
+// sin / cos (pi 2^l v) for l = 0, 1, ...: one fp64 sincospi, then the double-angle step
+// (sin 2x = 2 s c, cos 2x = (c - s)(c + s)) per level -- the fp64 error doubles per level
+// (~1e-13 at level 9), far below the fp32 rounding of the encoding.
+__device__ __forceinline__ void sincospi_double(double& s, double& c) {
+    const double s2 = 2.0 * s * c;
+    c = (c - s) * (c + s);
+    s = s2;
+}
+
 // X[n][c * ex + j] = gamma_j(pos_c / coord_scale), then the (shared) time encoding.
-// gamma = [v, sin(pi 2^l v), cos(pi 2^l v)]: fp64 sincospi (2^l v is exact), rounded once.
+// gamma = [v, sin(pi 2^l v), cos(pi 2^l v)] in fp64, rounded once.
 __global__ void k_deform_encode(const float* __restrict__ pos, int64_t pos_stride, int64_t n, double inv_scale,
                                 int l_x, DeformEnc te, float* __restrict__ X, int64_t ldx) {
     const int ex = 1 + 2 * l_x;
@@ -983,10 +992,10 @@ __global__ void k_deform_encode(const float* __restrict__ pos, int64_t pos_strid
             const double v = (double)pos[i * pos_stride + c] * inv_scale;
             float* o = row + c * ex;
             o[0] = (float)v;
-            double f = v;
-            for (int l = 0; l < l_x; ++l, f *= 2.0) {
-                double s, co;
-                sincospi(f, &s, &co);
+            double s, co;
+            sincospi(v, &s, &co);
+            for (int l = 0; l < l_x; ++l) {
+                if (l) sincospi_double(s, co);
                 o[1 + 2 * l] = (float)s;
                 o[2 + 2 * l] = (float)co;
             }
@@ -1005,10 +1014,10 @@ __global__ void k_deform_chain(const float* __restrict__ d_input, int64_t ldd, c
             const float* din = d_input + i * ldd + c * ex;
             const double v = (double)X[i * ldx + c * ex];
             double acc = din[0];
-            double f = v, fr = M_PI;
-            for (int l = 0; l < l_x; ++l, f *= 2.0, fr *= 2.0) {
-                double s, co;
-                sincospi(f, &s, &co);
+            double fr = M_PI, s, co;
+            sincospi(v, &s, &co);
+            for (int l = 0; l < l_x; ++l, fr *= 2.0) {
+                if (l) sincospi_double(s, co);
                 acc += fr * co * (double)din[1 + 2 * l] - fr * s * (double)din[2 + 2 * l];
             }
             float* o = d_pos + i * dpos_stride + c;
@@ -1226,10 +1235,10 @@ __global__ void __launch_bounds__(kMlpThreads + 32, 1) k_mlp_fwd_fused(MlpFwdArg
                 split_exact(v, h, lo);
                 *reinterpret_cast<float*>(A_hi + a_off(r, kb)) = h;
                 *reinterpret_cast<float*>(A_lo + a_off(r, kb)) = lo;
-                double f = v;
-                for (int l = 0; l < a.l_x; ++l, f *= 2.0) {
-                    double sn, co;
-                    sincospi(f, &sn, &co);
+                double sn, co;
+                sincospi(v, &sn, &co);
+                for (int l = 0; l < a.l_x; ++l) {
+                    if (l) sincospi_double(sn, co);
                     split_exact(sn, h, lo);
                     *reinterpret_cast<float*>(A_hi + a_off(r, kb + 1 + 2 * l)) = h;
                     *reinterpret_cast<float*>(A_lo + a_off(r, kb + 1 + 2 * l)) = lo;
@@ -1481,10 +1490,10 @@ __global__ void __launch_bounds__(kMlpThreads + 32, 1) k_mlp_fwd_tm(MlpFwdArgs a
             if (wg < 3) {
                 const double v = rv ? (double)a.pos[m * a.pos_stride + wg] * a.inv_scale : 0.0;
                 srow[kb] = (float)v;
-                double f = v;
-                for (int l = 0; l < a.l_x; ++l, f *= 2.0) {
-                    double sn, co;
-                    sincospi(f, &sn, &co);
+                double sn, co;
+                sincospi(v, &sn, &co);
+                for (int l = 0; l < a.l_x; ++l) {
+                    if (l) sincospi_double(sn, co);
                     srow[kb + 1 + 2 * l] = (float)sn;
                     srow[kb + 2 + 2 * l] = (float)co;
                 }
