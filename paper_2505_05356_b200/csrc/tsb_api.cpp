@@ -2869,13 +2869,32 @@ int deform_backward(tsb_deform* d, int slot, const float* d_out, int64_t dstride
             h.mask = s.H[l - 1];
             h.ldmask = d->width;
         }
-        if ((rc = deform_gemm(d, h, 1))) return rc;
         if (l == 0) {
+            // the encoding chain fused into the input-gradient epilogue (no d_input round trip)
+            // where the launch allows it, else the GEMM then k_deform_chain
+            GemmArgs hc = h;
+            if (d->cfg.l_x == 10) {
+                hc.chain_x = s.X;
+                hc.chain_ldx = d->din;
+                hc.chain_inv_scale = 1.0 / d->cfg.coord_scale;
+                hc.chain_dpos = d_pos;
+                hc.chain_pstride = pstride;
+                hc.chain_acc = accumulate ? 1 : 0;
+                const int r = launch_gemm_tf32x3(hc, 1, st);
+                if (r >= 0) {
+                    d->ctx->launches += r;
+                    TSB_CHECK_LAUNCH();
+                    break;
+                }
+                if (r != kGemmNoChain) return fail(TSB_ERR_CUDA, "deform: GEMM launch");
+            }
+            if ((rc = deform_gemm(d, h, 1))) return rc;
             launch_deform_chain(out, K, s.X, d->din, n, 1.0 / d->cfg.coord_scale, d->cfg.l_x, d_pos, pstride,
                                 accumulate, st);
             d->ctx->launches++;
             break;
         }
+        if ((rc = deform_gemm(d, h, 1))) return rc;
         delta = out;
         dld = K;
     }

@@ -349,7 +349,17 @@ struct GemmArgs {
     float* rowsum;      // [slice][M]: sum over this slice's k of A(m, k) (row-contiguous A only), or null
     const uint32_t* maskbits;  // instead of mask: C *= bit n of maskbits[m * ldmaskbits + n / 32], or null
     int64_t ldmaskbits;
+    // DeformNet input-gradient chain fused into the epilogue (l_x = 10 encodings): instead of
+    // storing C, chain_dpos[m * chain_pstride + c] (+)= sum_j gamma'_j(v_c) C[m][21 c + j] *
+    // chain_inv_scale with v_c = chain_x[m * chain_ldx + 21 c] (launch_gemm_tf32x3 returns
+    // kGemmNoChain when the launch cannot fuse it)
+    const float* chain_x;
+    int64_t chain_ldx, chain_pstride;
+    double chain_inv_scale;
+    float* chain_dpos;
+    int chain_acc;
 };
+constexpr int kGemmNoChain = -2;
 int launch_gemm_tf32x3(const GemmArgs& g, int slices, cudaStream_t st);  // kernels launched (0, 1; -1: N > 128)
 void launch_reduce_slices(const float* part, int slices, int64_t stride, int64_t n, float* out, bool accumulate,
                           cudaStream_t st);

@@ -661,6 +661,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
 }
 
+// sin / cos (pi 2^l v) for l = 0, 1, ...: one fp64 sincospi, then the double-angle step
+// (sin 2x = 2 s c, cos 2x = (c - s)(c + s)) per level -- the fp64 error doubles per level
+// (~1e-13 at level 9), far below the fp32 rounding of the encoding.
+__device__ __forceinline__ void sincospi_double(double& s, double& c) {
+    const double s2 = 2.0 * s * c;
+    c = (c - s) * (c + s);
+    s = s2;
+}
+
 __device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t* v) {  // (no wait: tmem_wait_ld)
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
@@ -831,7 +840,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(GemmArgs g, int kRa
             tc_before_sync();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[buf]);
-            if (epi_warp && row_ok) {
+            if (NT == 128 && g.chain_x) {  // fused encoding chain (column group 0 holds the 63 x columns)
+                if (epi_warp && row_ok && col0 == 0) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const double xv = (double)__ldg(g.chain_x + (int64_t)m * g.chain_ldx + 21 * c);
+                        double acc = (double)__uint_as_float(v[21 * c]);
+                        double fr = M_PI, sn, cs;
+                        sincospi(xv, &sn, &cs);
+#pragma unroll
+                        for (int l = 0; l < 10; ++l, fr *= 2.0) {
+                            if (l) sincospi_double(sn, cs);
+                            acc += fr * cs * (double)__uint_as_float(v[21 * c + 1 + 2 * l]) -
+                                   fr * sn * (double)__uint_as_float(v[21 * c + 2 + 2 * l]);
+                        }
+                        float* o = g.chain_dpos + (int64_t)m * g.chain_pstride + c;
+                        const float val = (float)(acc * g.chain_inv_scale);
+                        *o = g.chain_acc ? *o + val : val;
+                    }
+                }
+            } else if (epi_warp && row_ok) {
 #pragma unroll
                 for (int cc = 0; cc < kColHalf; cc += 16) {
                     const int n0 = col0 + cc;
@@ -945,7 +973,9 @@ int launch_gemm_tf32x3(const GemmArgs& g, int slices, cudaStream_t st) {
         const char* e = std::getenv("TSB_GEMM_WS");
         return e && e[0] == '0';
     }();
-    if (!flush && p.b_res && nck > 0 && slices <= 1 && g.K <= g.k_per_slice && !ws_off) {
+    const bool ws = !flush && p.b_res && nck > 0 && slices <= 1 && g.K <= g.k_per_slice && !ws_off;
+    if (g.chain_x && (!ws || nt != 128 || g.N < 63)) return kGemmNoChain;
+    if (ws) {
         const size_t bytes = p.bytes;
         if (nt == 16) k_gemm_ws<16><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
         else if (nt == 32) k_gemm_ws<32><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
@@ -971,15 +1001,6 @@ namespace tsb {
 // ---------------------------------------------------------------------------
 // DeformNet helpers (deform.cpp:10-26, 60-78, 142-155)
 // ---------------------------------------------------------------------------
-
-// sin / cos (pi 2^l v) for l = 0, 1, ...: one fp64 sincospi, then the double-angle step
-// (sin 2x = 2 s c, cos 2x = (c - s)(c + s)) per level -- the fp64 error doubles per level
-// (~1e-13 at level 9), far below the fp32 rounding of the encoding.
-__device__ __forceinline__ void sincospi_double(double& s, double& c) {
-    const double s2 = 2.0 * s * c;
-    c = (c - s) * (c + s);
-    s = s2;
-}
 
 // X[n][c * ex + j] = gamma_j(pos_c / coord_scale), then the (shared) time encoding.
 // gamma = [v, sin(pi 2^l v), cos(pi 2^l v)] in fp64, rounded once.

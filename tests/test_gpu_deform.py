@@ -151,6 +151,25 @@ def test_deform_forward_backward_vs_oracle(tsb, ctx, layers, width, lx, lt, scal
     _check(gnet.grads(), 2 * oflat, 1e-3, "accumulated")
 
 
+def test_deform_position_gradient_many_tiles(tsb, ctx):
+    """d(position) at 40k points (more row tiles than CTAs: the encoding chain runs fused
+    in the input-gradient GEMM's epilogue, l_x = 10), then accumulated into a second call."""
+    from oracle import deform as od
+    cfg = od.DeformConfig()
+    onet, gnet, pos, rng = _nets(tsb, ctx, cfg, 23, n=40_000)
+    t = 0.61
+    ref, cache = onet.offsets(pos.astype(np.float64), t, with_cache=True)
+    got = gnet.offsets(pos, t, slot=1)  # (entry-wise offsets are checked above; normwise here)
+    assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max()
+    up = rng.normal(size=pos.shape).astype(np.float32)
+    # the oracle backward through the GPU's ReLU gates (see test_deform_large_batch_and_adam)
+    gates = [gnet.debug_activation(lv, pos.shape[0], slot=1) > 0 for lv in range(cfg.hidden_layers)]
+    _, _, dpos = onet.backward(cache, up.astype(np.float64), gates=gates)
+    gnet.zero_grads()
+    gdpos = gnet.backward(up, slot=1)
+    _check(gdpos, dpos, 1e-3, "d_position")
+
+
 def test_deform_large_batch_and_adam(tsb, ctx):
     """200k points (many row tiles and weight-gradient slices), then one Adam step on the
     network parameters equals the reference AdamState::step (trainer.cpp:18-31)."""
