@@ -307,12 +307,13 @@ __device__ __forceinline__ void raw_issue(const float* __restrict__ P, int64_t s
 // rows / columns the epilogue discards).
 template <int R, int NTHR = kGemmThreads>
 __device__ __forceinline__ void raw_split(bool lay_t, const char* raw, char* hi, char* lo, int kvalid = kGemmKc,
-                                          float* rsum = nullptr, int ldr = R) {
+                                          float* rsum = nullptr, int ldr = R, int t0 = -1) {
     constexpr int kIt = (R * 8 + NTHR - 1) / NTHR;
+    const int tt = t0 < 0 ? (int)threadIdx.x : t0;  // this thread's index among the NTHR splitting
     if (!lay_t) {
 #pragma unroll
         for (int it = 0; it < kIt; ++it) {
-            const int idx = threadIdx.x + it * NTHR;
+            const int idx = tt + it * NTHR;
             if (R * 8 % NTHR && idx >= R * 8) break;
             const int r8 = idx & 7, q = (idx >> 3) & 7, rg = idx >> 6, r = rg * 8 + r8;
             const float4 v = *reinterpret_cast<const float4*>(raw + r * kRawRowF * 4 + q * 16);
@@ -327,7 +328,7 @@ __device__ __forceinline__ void raw_split(bool lay_t, const char* raw, char* hi,
         const float* rf = reinterpret_cast<const float*>(raw);
 #pragma unroll
         for (int it = 0; it < kIt; ++it) {
-            const int idx = threadIdx.x + it * NTHR;
+            const int idx = tt + it * NTHR;
             if (R * 8 % NTHR && idx >= R * 8) break;
             const int kq = idx & 3, rq = (idx >> 2) % rq_n, kb = (idx >> 2) / rq_n, r = 4 * rq + kq;
             float4 v = make_float4(rf[(4 * kb + 0) * ldr + r], rf[(4 * kb + 1) * ldr + r], rf[(4 * kb + 2) * ldr + r],
@@ -540,6 +541,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
                 }
             }
             const uint32_t dacc = tmem + (uint32_t)(FLUSH ? (G & 1) * kAccCols : 0);
+            // the previous group's flush runs after this chunk's MMAs are issued, except when this
+            // chunk alone is a group: its end commit could then complete mb_tile a second time
+            // before the flush waited for the first (a parity wait cannot tell them apart)
+            const bool flush_now = FLUSH && group_start && chunk > 0, flush_first = flush_now && group_end;
+            if (flush_first) flush(G - 1);
             if (tid == 0) {
                 tc_after_sync();
                 char* b_hi = BRES ? bres + (size_t)chunk * 2 * kBBytes : sb_hi;
@@ -560,7 +566,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_tf32x3(GemmArgs g, int
                 if (group_end) mma_commit(&mb_tile);
             }
             // the previous group's flush, while this group's first MMAs run
-            if (FLUSH && group_start && chunk > 0) flush(G - 1);
+            if (flush_now && !flush_first) flush(G - 1);
         }
         if (FLUSH && nck > 0) flush(G);  // the tile's last group
         const bool any = nck > 0;
@@ -906,6 +912,220 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(GemmArgs g, int kRa
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
 }
 
+// Weight-gradient reduction (FLUSH) over one row tile with both operands bulk-copied,
+// warp-specialised: warp 0 issues the bulk copies and the MMAs (thread 0), warps 1-15 split;
+// every warp flushes its share of the accumulators.  Nothing is block-synchronous inside the
+// K loop:
+//   mb_raw[st]     a raw stage landed (TMA complete_tx)
+//   split_full[b]  the 15 split warps have split chunk q (b = q & 1) -> MMAs; its raw stage
+//                  is refilled with chunk q + kRaw
+//   mb_mma[b]      chunk q's MMAs done -> split buffer b may take chunk q + 2
+//   mb_tile        an accumulation group's MMAs done -> flush (each warp its share)
+//   acc_free[a]    all 16 warps flushed accumulator a -> the group after next may use it
+template <int NT>
+__global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_wsf(GemmArgs g, int kRaw) {
+    extern __shared__ __align__(1024) char smem[];
+    __shared__ __align__(8) uint64_t mb_raw[kMaxRaw], split_full[2], mb_mma[2], mb_tile, acc_free[2];
+    __shared__ uint32_t tmem_base_s;
+    constexpr int kSplitThr = kGemmThreads - 32;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int kAccCols = NT <= 32 ? 32 : (NT <= 64 ? 64 : 128);
+    constexpr int kTmemCols = 2 * kAccCols;
+    constexpr uint32_t kABytes = kGemmM * kGemmKc * 4, kBBytes = NT * kGemmKc * 4;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < kMaxRaw; ++i) mbar_init(&mb_raw[i], 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&split_full[b], kSplitThr / 32);
+            mbar_init(&mb_mma[b], 1);
+            mbar_init(&acc_free[b], kGemmThreads / 32);
+        }
+        mbar_init(&mb_tile, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    const uint32_t tmem = tmem_base_s;
+    const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    constexpr int kEpiGroups = NT >= 64 ? 4 : (NT == 32 ? 2 : 1);
+    constexpr int kColHalf = NT / kEpiGroups;
+    const int col0 = ((warp >> 2) % kEpiGroups) * kColHalf;
+    const bool epi_warp = (warp >> 2) < kEpiGroups;
+    const int slice = blockIdx.y;
+    const int kbeg = slice * g.k_per_slice;
+    const int kend = min(g.K, kbeg + g.k_per_slice);
+    const int nck = kend > kbeg ? (kend - kbeg + kGemmKc - 1) / kGemmKc : 0;
+    constexpr uint32_t idesc = idesc_tf32(kGemmM, NT);
+    const int lda = (int)g.a_k, ldb = (int)g.b_k;
+    char* split0 = smem;
+    constexpr size_t kSplitBuf = 2 * kABytes + 2 * kBBytes;
+    char* raw0 = split0 + 2 * kSplitBuf;
+    const size_t raw_sa = raw_bytes(kGemmM, true), raw_stage = raw_sa + raw_bytes(NT, true);
+    auto raw_a = [&](int st) { return raw0 + (size_t)st * raw_stage; };
+    auto raw_b = [&](int st) { return raw0 + (size_t)st * raw_stage + raw_sa; };
+    auto issue_bulk = [&](int q) {  // thread 0: chunk q into raw stage q % kRaw
+        const int k0 = kbeg + q * kGemmKc, rows = min(kGemmKc, kend - k0), st = q % kRaw;
+        const uint32_t ba = (uint32_t)rows * lda * 4, bb = (uint32_t)rows * ldb * 4;
+        mbar_expect_tx(&mb_raw[st], ba + bb);
+        bulk_copy(smem_u32(raw_a(st)), g.A + (int64_t)k0 * lda, ba, &mb_raw[st]);
+        bulk_copy(smem_u32(raw_b(st)), g.B + (int64_t)k0 * ldb, bb, &mb_raw[st]);
+    };
+    float acc[kColHalf];
+#pragma unroll
+    for (int j = 0; j < kColHalf; ++j) acc[j] = 0.f;
+    uint32_t tphase = 0;
+    auto flush = [&](int grp) {
+        mbar_wait(&mb_tile, tphase & 1u);
+        ++tphase;
+        tc_after_sync();
+        if (epi_warp) {
+#pragma unroll
+            for (int cc = 0; cc < kColHalf; cc += 16) {
+                uint32_t v[16];
+                tmem_ld16(tl + (uint32_t)((grp & 1) * kAccCols + col0 + cc), v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[cc + j] += __uint_as_float(v[j]);
+            }
+        }
+        tc_before_sync();
+    };
+    constexpr int kRsIt = (kGemmM * 8 + kSplitThr - 1) / kSplitThr;
+    double rsum[kRsIt];
+    float rsf[kRsIt];
+#pragma unroll
+    for (int i = 0; i < kRsIt; ++i) {
+        rsum[i] = 0.0;
+        rsf[i] = 0.f;
+    }
+    const bool do_rsum = g.rowsum != nullptr;
+    int G = -1;
+    if (warp == 0) {
+        // ---- bulk copies + MMAs ----
+        if (lane == 0)
+            for (int q = 0; q < min(kRaw, nck); ++q) issue_bulk(q);
+        for (int q = 0; q < nck; ++q) {
+            const bool group_start = (q % kFlushChunks) == 0;
+            const bool group_end = (q % kFlushChunks) == kFlushChunks - 1 || q + 1 == nck;
+            if (group_start) ++G;
+            // the previous group's flush: after this chunk's MMAs are issued, except when this
+            // chunk alone is a group (its end commit would complete mb_tile a second time
+            // before this warp waited for the first: a parity wait cannot tell them apart)
+            const bool flush_now = group_start && q > 0, flush_first = flush_now && group_end;
+            if (flush_first) {
+                flush(G - 1);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_free[(G - 1) & 1]);
+            }
+            if (lane == 0) {
+                mbar_wait(&split_full[q & 1], (uint32_t)(q >> 1) & 1u);
+                if (group_start && G >= 2) mbar_wait(&acc_free[G & 1], (uint32_t)((G >> 1) - 1) & 1u);
+                tc_after_sync();
+                const uint32_t dacc = tmem + (uint32_t)((G & 1) * kAccCols);
+                const char* a_hi = split0 + (size_t)(q & 1) * kSplitBuf;
+                const uint32_t ah = smem_u32(a_hi), al = ah + kABytes, bh = al + kABytes, bl = bh + kBBytes;
+#pragma unroll
+                for (int s = 0; s < kGemmKc / 8; ++s) {
+                    const uint32_t off = (uint32_t)s * 2u * kCoreBytes;
+                    const uint64_t dah = umma_desc(ah + off, kCoreBytes, kGroupBytes);
+                    const uint64_t dal = umma_desc(al + off, kCoreBytes, kGroupBytes);
+                    const uint64_t dbh = umma_desc(bh + off, kCoreBytes, kGroupBytes);
+                    const uint64_t dbl = umma_desc(bl + off, kCoreBytes, kGroupBytes);
+                    mma_tf32(dacc, dah, dbh, idesc, (!group_start || s > 0) ? 1u : 0u);
+                    mma_tf32(dacc, dah, dbl, idesc, 1u);
+                    mma_tf32(dacc, dal, dbh, idesc, 1u);
+                }
+                mma_commit(&mb_mma[q & 1]);
+                if (group_end) mma_commit(&mb_tile);
+                if (q + kRaw < nck) issue_bulk(q + kRaw);  // chunk q's raw stage has been split
+            }
+            __syncwarp();
+            if (flush_now && !flush_first) {
+                flush(G - 1);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_free[(G - 1) & 1]);
+            }
+        }
+    } else {
+        // ---- split ----
+        const int t = tid - 32;
+        for (int q = 0; q < nck; ++q) {
+            const bool group_start = (q % kFlushChunks) == 0;
+            const bool group_end = (q % kFlushChunks) == kFlushChunks - 1 || q + 1 == nck;
+            if (group_start) ++G;
+            const bool flush_now = group_start && q > 0, flush_first = flush_now && group_end;  // (as warp 0)
+            if (flush_first) {
+                flush(G - 1);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_free[(G - 1) & 1]);
+            }
+            const int st = q % kRaw;
+            mbar_wait(&mb_raw[st], (uint32_t)(q / kRaw) & 1u);
+            if (q >= 2) mbar_wait(&mb_mma[q & 1], (uint32_t)((q >> 1) - 1) & 1u);
+            char* a_hi = split0 + (size_t)(q & 1) * kSplitBuf;
+            const int kvalid = min(kGemmKc, kend - (kbeg + q * kGemmKc));
+            raw_split<kGemmM, kSplitThr>(true, raw_a(st), a_hi, a_hi + kABytes, kvalid, do_rsum ? rsf : nullptr, lda, t);
+            raw_split<NT, kSplitThr>(true, raw_b(st), a_hi + 2 * kABytes, a_hi + 2 * kABytes + kBBytes, kvalid,
+                                     nullptr, ldb, t);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&split_full[q & 1]);
+            if (do_rsum && group_end) {
+#pragma unroll
+                for (int i = 0; i < kRsIt; ++i) {
+                    rsum[i] += (double)rsf[i];
+                    rsf[i] = 0.f;
+                }
+            }
+            if (flush_now && !flush_first) {
+                flush(G - 1);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_free[(G - 1) & 1]);
+            }
+        }
+    }
+    if (nck > 0) flush(G);  // the last group
+    __syncthreads();
+    // ---- epilogue: this slice's partial D (no bias / ReLU / gate in a weight gradient) ----
+    float* C = g.C + (int64_t)slice * g.slice_stride;
+    const int m = (warp & 3) * 32 + lane;
+    if (epi_warp && m < g.M) {
+        float* crow = C + (int64_t)m * g.ldc;
+#pragma unroll
+        for (int j = 0; j < kColHalf; ++j)
+            if (col0 + j < g.N) crow[col0 + j] = acc[j];
+    }
+    if (do_rsum) {  // per row: the partials of the threads that split its k groups, in a fixed order
+        double* red = reinterpret_cast<double*>(raw0);  // [k group][row] (the ring is idle now)
+        constexpr int rq_n = kGemmM / 4;
+        if (warp > 0) {
+            const int t = tid - 32;
+#pragma unroll
+            for (int it = 0; it < kRsIt; ++it) {
+                const int idx = t + it * kSplitThr;
+                if (idx >= kGemmM * 8) break;
+                const int kq = idx & 3, rq = (idx >> 2) % rq_n, kb = (idx >> 2) / rq_n;
+                red[kb * kGemmM + 4 * rq + kq] = rsum[it];
+            }
+        }
+        __syncthreads();
+        if (tid < g.M) {
+            double tsum = 0.0;
+            for (int kb = 0; kb < kGemmKc / 4; ++kb) tsum += red[kb * kGemmM + tid];
+            g.rowsum[(int64_t)slice * g.M + tid] = (float)tsum;
+        }
+    }
+    tc_before_sync();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
+}
+
 // out[i] (+)= sum_s part[s * stride + i]
 __global__ void k_reduce_slices(const float* __restrict__ part, int slices, int64_t stride, int64_t n,
                                 float* __restrict__ out, int accumulate) {
@@ -950,6 +1170,10 @@ int launch_gemm_tf32x3(const GemmArgs& g, int slices, cudaStream_t st) {
         cudaFuncSetAttribute(k_gemm_ws<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmMaxSmem);
         cudaFuncSetAttribute(k_gemm_ws<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmMaxSmem);
         cudaFuncSetAttribute(k_gemm_ws<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmMaxSmem);
+        cudaFuncSetAttribute(k_gemm_wsf<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmMaxSmem);
+        cudaFuncSetAttribute(k_gemm_wsf<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmMaxSmem);
+        cudaFuncSetAttribute(k_gemm_wsf<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmMaxSmem);
+        cudaFuncSetAttribute(k_gemm_wsf<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmMaxSmem);
         attr = true;
     }
     if (g.M <= 0 || g.N <= 0) return 0;
@@ -981,6 +1205,20 @@ int launch_gemm_tf32x3(const GemmArgs& g, int slices, cudaStream_t st) {
         else if (nt == 32) k_gemm_ws<32><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
         else if (nt == 64) k_gemm_ws<64><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
         else k_gemm_ws<128><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
+        return 1;
+    }
+    static const bool wsf_off = [] {  // TSB_GEMM_WSF=0: the single-role kernel (A/B timing)
+        const char* e = std::getenv("TSB_GEMM_WSF");
+        return e && e[0] == '0';
+    }();
+    const bool bulk_ok = g.a_m == 1 && g.b_n == 1 && g.M <= g.a_k && g.a_k <= kGemmM && g.N <= g.b_k && g.b_k <= nt &&
+                         ((g.a_k | g.b_k) & 3) == 0 && (((uintptr_t)g.A | (uintptr_t)g.B) & 15) == 0;
+    if (flush && !p.b_res && bulk_ok && g.M <= kGemmM && !wsf_off) {
+        const size_t bytes = p.bytes;
+        if (nt == 16) k_gemm_wsf<16><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
+        else if (nt == 32) k_gemm_wsf<32><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
+        else if (nt == 64) k_gemm_wsf<64><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
+        else k_gemm_wsf<128><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
         return 1;
     }
     if (flush) return p.b_res ? gemm_dispatch<true, true>(g, grid, p, st) : gemm_dispatch<true, false>(g, grid, p, st);
