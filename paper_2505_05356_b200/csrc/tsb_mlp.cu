@@ -1867,6 +1867,226 @@ __global__ void __launch_bounds__(kMlpThreads + 32, 1) k_mlp_fwd_tm(MlpFwdArgs a
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined variant: layer l + 1's MMAs start on each 32-column K chunk of its input as soon
+// as the epilogue of layer l has written it (instead of after the whole epilogue).  Layers
+// alternate between two accumulators (TMEM: D0 0-127, D1 128-255, A hi 256-383, A lo
+// 384-511), so layer l + 1 accumulates while layer l's is still being read.  Roles: warps
+// 0-15 encode / epilogue / store the staging tile; warp 16 lane 0 streams the weights;
+// warp 17 lane 0 issues the MMAs.
+//   a_ready[c]  the 16 compute warps wrote A columns [32c, 32c + 32) of the next layer's
+//               input (one barrier per chunk index: each completes once per layer, so a
+//               parity wait cannot be lapped)
+//   mb_layer    a layer's MMAs are done (its accumulator may be read)
+// ---------------------------------------------------------------------------
+constexpr uint32_t kTpD1 = 128, kTpA = 256, kTpAlo = 384;
+constexpr int kMlpThreadsP = kMlpThreads + 64;
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                 "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(kMlpThreadsP, 1) k_mlp_fwd_tp(MlpFwdArgs a) {
+    extern __shared__ __align__(1024) char smem[];
+    __shared__ __align__(8) uint64_t mb_full[kMlpStagesT], mb_empty[kMlpStagesT], mb_layer, a_ready[4];
+    __shared__ uint32_t tmem_base_s;
+    char* ring = smem;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const MlpLayout& lay = a.lay;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_s))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < kMlpStagesT; ++i) {
+            mbar_init(&mb_full[i], 1);
+            mbar_init(&mb_empty[i], 1);
+        }
+        mbar_init(&mb_layer, 1);
+        for (int c = 0; c < 4; ++c) mbar_init(&a_ready[c], kMlpThreads / 32);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    const uint32_t tmem = tmem_base_s;
+    const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's lane quadrant
+    const int wg = warp >> 2;                                          // column group (0..3)
+    const int ntiles = (int)((a.n + 127) / 128);
+    const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const uint32_t total = (uint32_t)my_tiles * (uint32_t)lay.total_chunks;
+
+    if (warp == kMlpThreads / 32) {  // ---- weight producer ----
+        if (lane == 0)
+            for (uint32_t q = 0; q < total; ++q) {
+                const int st = (int)(q % kMlpStagesT);
+                if (q >= (uint32_t)kMlpStagesT) mbar_wait(&mb_empty[st], ((q / kMlpStagesT) - 1) & 1u);
+                const uint32_t local = q % (uint32_t)lay.total_chunks;
+                int l = 0;
+                uint32_t base = 0;
+                while (local >= base + (uint32_t)lay.chunks[l]) {
+                    base += lay.chunks[l];
+                    ++l;
+                }
+                const uint32_t bytes = (uint32_t)lay.nt[l] * kGemmKc * 8u;
+                bulk_g2s(ring + (size_t)st * kMlpStageBytes, a.wpack + lay.chunk_off[l] + (int64_t)(local - base) * bytes,
+                         bytes, &mb_full[st]);
+            }
+        __syncwarp();
+    } else if (warp == kMlpThreads / 32 + 1) {  // ---- MMA issuer ----
+        if (lane == 0) {
+            uint32_t q = 0, aph = 0;  // aph: bit c = parity of a_ready[c]'s next completion
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int l = 0; l < lay.layers; ++l) {
+                    const int nt = lay.nt[l];
+                    const uint32_t idesc = idesc_tf32(128, nt);
+                    const uint32_t d = tmem + ((l & 1) ? kTpD1 : 0u);
+                    for (int c = 0; c < lay.chunks[l]; ++c, ++q) {
+                        mbar_wait(&a_ready[c], (aph >> c) & 1u);
+                        aph ^= 1u << c;
+                        const int st = (int)(q % kMlpStagesT);
+                        mbar_wait(&mb_full[st], (q / kMlpStagesT) & 1u);
+                        tc_after_sync();
+                        const uint32_t bh = smem_u32(ring + (size_t)st * kMlpStageBytes);
+                        const uint32_t bl = bh + (uint32_t)nt * kGemmKc * 4;
+#pragma unroll
+                        for (int s = 0; s < kGemmKc / 8; ++s) {
+                            const uint32_t k0 = (uint32_t)(c * kGemmKc + 8 * s);
+                            const uint32_t boff = (uint32_t)(2 * s) * kCoreBytes;
+                            const uint64_t dbh = umma_desc(bh + boff, kCoreBytes, kGroupBytes);
+                            const uint64_t dbl = umma_desc(bl + boff, kCoreBytes, kGroupBytes);
+                            mma_tf32_at(d, tmem + kTpA + k0, dbh, idesc, (c > 0 || s > 0) ? 1u : 0u);
+                            mma_tf32_at(d, tmem + kTpA + k0, dbl, idesc, 1u);
+                            mma_tf32_at(d, tmem + kTpAlo + k0, dbh, idesc, 1u);
+                        }
+                        mma_commit(&mb_empty[st]);
+                    }
+                    mma_commit(&mb_layer);
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---- compute warps: encode, epilogues, staging stores ----
+        uint32_t lphase = 0;
+        const int ex = 1 + 2 * a.l_x;
+        const int kpad0 = lay.chunks[0] * kGemmKc;
+        float* S = reinterpret_cast<float*>(smem + (size_t)kMlpStagesT * kMlpStageBytes);  // [128][kStgLd]
+        const int r = (warp & 3) * 32 + lane;  // = the TMEM lane this thread may access
+        float* srow = S + r * kStgLd;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int64_t m0 = (int64_t)tile * 128;
+            const int64_t m = m0 + r;
+            const bool rv = m < a.n;
+            {  // positional encoding -> staging tile (warp group: x, y, z, time + zero padding)
+                const int kb = wg * ex;
+                if (wg < 3) {
+                    const double v = rv ? (double)a.pos[m * a.pos_stride + wg] * a.inv_scale : 0.0;
+                    srow[kb] = (float)v;
+                    double sn, co;
+                    sincospi(v, &sn, &co);
+                    for (int l = 0; l < a.l_x; ++l) {
+                        if (l) sincospi_double(sn, co);
+                        srow[kb + 1 + 2 * l] = (float)sn;
+                        srow[kb + 2 + 2 * l] = (float)co;
+                    }
+                } else {
+                    for (int k = kb; k < kpad0; ++k) srow[k] = k - kb < a.te.n ? a.te.v[k - kb] : 0.f;
+                }
+            }
+            bar_compute();
+            // A = split(staging) for layer 0, one 32-column chunk per a_ready phase
+            for (int c = 0; c < lay.chunks[0]; ++c) {
+                const int col = c * 32 + 8 * wg;
+                uint32_t hv[8], lv[8];
+#pragma unroll
+                for (int j = 0; j < 8; j += 4) {
+                    const float4 x = *reinterpret_cast<const float4*>(srow + col + j);
+                    float h, lo;
+                    split_exact(x.x, h, lo); hv[j] = __float_as_uint(h); lv[j] = __float_as_uint(lo);
+                    split_exact(x.y, h, lo); hv[j + 1] = __float_as_uint(h); lv[j + 1] = __float_as_uint(lo);
+                    split_exact(x.z, h, lo); hv[j + 2] = __float_as_uint(h); lv[j + 2] = __float_as_uint(lo);
+                    split_exact(x.w, h, lo); hv[j + 3] = __float_as_uint(h); lv[j + 3] = __float_as_uint(lo);
+                }
+                tmem_st8(tl + kTpA + (uint32_t)col, hv);
+                tmem_st8(tl + kTpAlo + (uint32_t)col, lv);
+                tmem_st_wait();
+                tc_before_sync();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&a_ready[c]);
+            }
+            for (int l = 0; l < lay.layers; ++l) {
+                // the staging tile holds layer l's input: store it for the backward while layer
+                // l's MMAs finish
+                if (l == 0 && a.X) store_staged(S, a.X, a.ldx, m0, a.n, a.din, nullptr, 0, kMlpThreads / 32);
+                if (l > 0 && a.H[l - 1])
+                    store_staged(S, a.H[l - 1], a.ldh, m0, a.n, lay.rows[l - 1], a.Hbits[l - 1], 0, kMlpThreads / 32);
+                mbar_wait(&mb_layer, lphase & 1u);
+                ++lphase;
+                bar_compute();  // the staging tile is free again
+                tc_after_sync();
+                const float* bias = a.params + lay.b_off[l];
+                const int rows = lay.rows[l], nt = lay.nt[l];
+                const uint32_t dl = (l & 1) ? kTpD1 : 0u;
+                if (l + 1 < lay.layers) {
+                    // epilogue in the next layer's K chunks: D -> bias, ReLU -> staging + A
+                    for (int c = 0; c < lay.chunks[l + 1]; ++c) {
+                        const int col = c * 32 + 8 * wg;
+                        uint32_t v[8], hv[8], lv[8];
+                        float x[8];
+                        if (col < nt) {
+                            tmem_ld8(tl + dl + (uint32_t)col, v);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j)
+                                x[j] = col + j < rows ? fmaxf(__uint_as_float(v[j]) + __ldg(bias + col + j), 0.f) : 0.f;
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) x[j] = 0.f;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            float h, lo;
+                            split_exact(x[j], h, lo);
+                            hv[j] = __float_as_uint(h);
+                            lv[j] = __float_as_uint(lo);
+                        }
+                        *reinterpret_cast<float4*>(srow + col) = make_float4(x[0], x[1], x[2], x[3]);
+                        *reinterpret_cast<float4*>(srow + col + 4) = make_float4(x[4], x[5], x[6], x[7]);
+                        tmem_st8(tl + kTpA + (uint32_t)col, hv);
+                        tmem_st8(tl + kTpAlo + (uint32_t)col, lv);
+                        tmem_st_wait();
+                        tc_before_sync();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&a_ready[c]);
+                    }
+                    bar_compute();  // the staging tile is complete before it is stored
+                } else if (warp < 4) {
+                    uint32_t v[16];
+                    tmem_ld16(tl + dl, v);
+                    if (rv)
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (j < rows) a.out[m * a.out_stride + j] = __uint_as_float(v[j]) + __ldg(bias + j);
+                }
+            }
+            tc_before_sync();
+            bar_compute();  // (the next tile's encoding overwrites the staging tile)
+        }
+    }
+    tc_before_sync();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
 size_t mlp_tm_smem_bytes() { return (size_t)kMlpStagesT * kMlpStageBytes + (size_t)128 * kStgLd * 4; }
 
 size_t mlp_fused_smem_bytes() { return 2 * (size_t)kMlpAHalf + (size_t)kMlpStages * kMlpStageBytes; }
@@ -1880,6 +2100,7 @@ void launch_mlp_fwd_fused(const MlpFwdArgs& a, cudaStream_t st) {
     if (!attr) {
         cudaFuncSetAttribute(k_mlp_fwd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mlp_fused_smem_bytes());
         cudaFuncSetAttribute(k_mlp_fwd_tm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mlp_tm_smem_bytes());
+        cudaFuncSetAttribute(k_mlp_fwd_tp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mlp_tm_smem_bytes());
         attr = true;
     }
     if (a.n <= 0) return;
@@ -1888,6 +2109,14 @@ void launch_mlp_fwd_fused(const MlpFwdArgs& a, cudaStream_t st) {
         const char* e = std::getenv("TSB_MLP_ATMEM");
         return !(e && e[0] == '0');
     }();
+    static const bool unpiped = [] {  // TSB_MLP_PIPE=0: layer-serial TMEM kernel (A/B timing)
+        const char* e = std::getenv("TSB_MLP_PIPE");
+        return e && e[0] == '0';
+    }();
+    if (tmem_a && !unpiped) {
+        k_mlp_fwd_tp<<<std::min(ntiles, 148), kMlpThreadsP, mlp_tm_smem_bytes(), st>>>(a);
+        return;
+    }
     if (tmem_a) {
         k_mlp_fwd_tm<<<std::min(ntiles, 148), kMlpThreads + 32, mlp_tm_smem_bytes(), st>>>(a);
         return;
