@@ -705,6 +705,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mbar)) : "memory");
 }
 
+constexpr int kEpiLd = 20;  // staging row stride (floats): 16 columns + 4 (conflict-free float4 rows)
+constexpr size_t kEpiStageBytes = (size_t)(kGemmThreads / 64) * 32 * kEpiLd * 4;  // 8 epilogue warps
+
 template <int NT>
 __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(GemmArgs g, int kRaw) {
     extern __shared__ __align__(1024) char smem[];
@@ -815,6 +818,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(GemmArgs g, int kRa
         // ---- epilogue: TMEM lane quadrant warp % 4, column half (warp - 8) / 4 ----
         const int ew = warp - kMain / 32;
         const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        // warp-private staging blocks after the raw ring (kEpiStageBytes, reserved by the launcher)
+        float* epi_stage = reinterpret_cast<float*>(raw0 + (size_t)kRaw * raw_stage);
+        const bool staged = !g.mask && (g.N & 3) == 0 && (g.ldc & 3) == 0 && (((uintptr_t)g.C) & 15) == 0;
         constexpr int kEpiGroups = NT >= 32 ? 2 : 1;
         constexpr int kColHalf = NT / kEpiGroups;
         const int col0 = ((ew >> 2) % kEpiGroups) * kColHalf;
@@ -864,6 +870,40 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(GemmArgs g, int kRa
                         const float val = (float)(acc * g.chain_inv_scale);
                         *o = g.chain_acc ? *o + val : val;
                     }
+                }
+            } else if (epi_warp && staged) {
+                // row-major stores through a warp-private staging block: the TMEM read-out
+                // gives a lane one row's 16 columns (a warp store would touch 32 rows / cache
+                // lines); after the transpose a warp store writes 8 rows x 64 contiguous bytes
+                float* stg = epi_stage + (size_t)(warp - kMain / 32) * 32 * kEpiLd;
+                const int rr = lane >> 2, qq = lane & 3;
+#pragma unroll
+                for (int cc = 0; cc < kColHalf; cc += 16) {
+                    const int n0 = col0 + cc;
+                    if (n0 >= g.N) continue;
+                    const uint32_t bits = ((n0 >> 5) > (col0 >> 5) ? mb1 : mb0) >> (n0 & 31);
+                    float x[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        x[j] = __uint_as_float(v[cc + j]);
+                        if (g.bias && n0 + j < g.N) x[j] += __ldg(g.bias + n0 + j);
+                        if (g.relu) x[j] = fmaxf(x[j], 0.f);
+                        if (!((bits >> j) & 1u)) x[j] = 0.f;
+                    }
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4)
+                        *reinterpret_cast<float4*>(stg + lane * kEpiLd + 4 * q4) =
+                            make_float4(x[4 * q4], x[4 * q4 + 1], x[4 * q4 + 2], x[4 * q4 + 3]);
+                    __syncwarp();
+                    const bool colv = n0 + 4 * qq + 4 <= g.N;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int row = 8 * j + rr;
+                        const int mm = m0 + (warp & 3) * 32 + row;
+                        const float4 o = *reinterpret_cast<const float4*>(stg + row * kEpiLd + 4 * qq);
+                        if (mm < g.M && colv) *reinterpret_cast<float4*>(C_row(g, mm) + n0 + 4 * qq) = o;
+                    }
+                    __syncwarp();
                 }
             } else if (epi_warp && row_ok) {
 #pragma unroll
@@ -1200,7 +1240,13 @@ int launch_gemm_tf32x3(const GemmArgs& g, int slices, cudaStream_t st) {
     const bool ws = !flush && p.b_res && nck > 0 && slices <= 1 && g.K <= g.k_per_slice && !ws_off;
     if (g.chain_x && (!ws || nt != 128 || g.N < 63)) return kGemmNoChain;
     if (ws) {
-        const size_t bytes = p.bytes;
+        GemmPlan pw = p;  // the epilogue's staging blocks come after the raw ring
+        while (pw.raw > 2 && pw.bytes + kEpiStageBytes > (size_t)kGemmMaxSmem) {
+            --pw.raw;
+            pw.bytes = gemm_bytes(nt, nck, true, g.a_m == 1, g.b_n == 1, pw.raw);
+        }
+        const size_t bytes = pw.bytes + kEpiStageBytes;
+        p = pw;
         if (nt == 16) k_gemm_ws<16><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
         else if (nt == 32) k_gemm_ws<32><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
         else if (nt == 64) k_gemm_ws<64><<<grid, kGemmThreads, bytes, st>>>(g, p.raw);
