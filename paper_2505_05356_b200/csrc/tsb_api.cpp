@@ -154,6 +154,9 @@ struct tsb_pass {
     tsb_ctx* ctx = nullptr;
     cudaStream_t stream = nullptr;   // each pass runs on its own stream (frames overlap)
     cudaEvent_t done_ev = nullptr;   // recorded after every enqueue (tsb_ctx_join)
+    // per scene this pass has read: an event after its last enqueue reading it (a parameter
+    // upload waits for the readers of its own scene only)
+    std::vector<std::pair<const tsb_scene*, cudaEvent_t>> scene_evs;
     cudaEvent_t fwd_ev = nullptr;    // end of the last forward (its abort word is final): settle waits here,
                                      // not for the frame's backward or downloads
     void* pinned = nullptr;          // per-pass pinned staging
@@ -379,6 +382,32 @@ int tsb_ctx_scan_counts(tsb_ctx* c, int64_t* ranks, int64_t* list_entries) {
 namespace {
 int settle(tsb_pass* p);
 int flush_prepare(tsb_pass* p);
+// done_ev, and the event of the pass's scene (the enqueued work may read it)
+cudaError_t record_done(tsb_pass* p, cudaStream_t st) {
+    cudaError_t e = cudaEventRecord(p->done_ev, st);
+    if (e != cudaSuccess || !p->scene) return e;
+    for (auto& se : p->scene_evs)
+        if (se.first == p->scene) return cudaEventRecord(se.second, st);
+    cudaEvent_t ev;
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+    p->scene_evs.push_back({p->scene, ev});
+    return cudaEventRecord(ev, st);
+}
+// The context stream waits for every enqueue that read scene s (passes prepared with s are
+// settled first: a redone frame must see the parameters it was prepared with).
+int scene_join(tsb_scene* s) {
+    tsb_ctx* c = s->ctx;
+    for (tsb_pass* p : c->passes) {
+        if (p->scene == s) {
+            int rc = flush_prepare(p);
+            if (!rc) rc = settle(p);
+            if (rc) return rc;
+        }
+        for (auto& se : p->scene_evs)
+            if (se.first == s) TSB_CUDA(cudaStreamWaitEvent(c->stream, se.second, 0));
+    }
+    return TSB_OK;
+}
 int settle_all(tsb_ctx* c) {
     for (tsb_pass* p : c->passes) {
         int rc = flush_prepare(p);  // a prepared frame reads the scene as it is now
@@ -510,7 +539,8 @@ int pack_one(tsb_scene* s, float4* dst, const float* src, int where, int comps, 
     launch_pack_params(dst, dsrc, n, comps, comp0, 4, st);
     s->ctx->launches++;
     TSB_CHECK_LAUNCH();
-    if (where == TSB_HOST) TSB_CUDA(cudaStreamSynchronize(st));  // staging reuse
+    // (the next component's copy into the staging buffer is ordered after this pack on the
+    // same stream; callers that return to the host sync once at the end)
     return TSB_OK;
 }
 
@@ -537,7 +567,7 @@ int tsb_scene_set_params(tsb_scene* s, int where, const float* position, const f
     TSB_CUDA(cudaSetDevice(s->ctx->device));
     const int n = s->d.n;
     int rc;
-    if ((rc = tsb_ctx_join(s->ctx))) return rc;  // passes may still be reading the parameters
+    if ((rc = scene_join(s))) return rc;  // passes may still be reading this scene's parameters
     if ((rc = pack_one(s, s->params, position, where, 3, 0))) return rc;
     if ((rc = pack_one(s, s->params, opacity_logit, where, 1, 3))) return rc;
     if ((rc = pack_one(s, s->params + n, log_scale, where, 3, 0))) return rc;
@@ -549,6 +579,8 @@ int tsb_scene_set_params(tsb_scene* s, int where, const float* position, const f
                 return rc;
     if ((rc = refresh_param_cache(s))) return rc;
     TSB_CUDA(cudaEventRecord(s->params_ev, s->ctx->stream));
+    // host sources are read by asynchronous copies: they are free again on return
+    if (where == TSB_HOST) TSB_CUDA(cudaStreamSynchronize(s->ctx->stream));
     return TSB_OK;
 }
 
@@ -1219,6 +1251,7 @@ void tsb_pass_destroy(tsb_pass* p) {
     dev_free(p->ext_dmacc); dev_free(p->ext_ftgt); dev_free(p->ext_fl_part); dev_free(p->ext_fl_res);
     if (p->pinned) cudaFreeHost(p->pinned);
     if (p->done_ev) cudaEventDestroy(p->done_ev);
+    for (auto& e : p->scene_evs) cudaEventDestroy(e.second);
     if (p->fwd_ev) cudaEventDestroy(p->fwd_ev);
     for (auto& fg : p->fwd)
         if (fg.exec) cudaGraphExecDestroy(fg.exec);
@@ -1540,7 +1573,7 @@ int flush_prepare(tsb_pass* p) {
     if (rc) return rc;
     p->ctx->launches += l;
     p->prep_deferred = false;
-    TSB_CUDA(cudaEventRecord(p->done_ev, p->stream));
+    TSB_CUDA(record_done(p, p->stream));
     return TSB_OK;
 }
 
@@ -1719,7 +1752,7 @@ int enqueue_forward(tsb_pass* p, const float* target, bool loss, const ChW& chw,
     p->pend_bwd = false;
     p->pend_dl.clear();
     TSB_CUDA(cudaEventRecord(p->fwd_ev, st));
-    TSB_CUDA(cudaEventRecord(p->done_ev, st));
+    TSB_CUDA(record_done(p, st));
     return TSB_OK;
 }
 
@@ -1818,7 +1851,7 @@ int settle(tsb_pass* p) {
             TSB_CUDA(cudaMemcpyAsync(d.host, dp, std::min(b, d.bytes), cudaMemcpyDeviceToHost, st));
             p->pend_dl.push_back(d);
         }
-        TSB_CUDA(cudaEventRecord(p->done_ev, st));
+        TSB_CUDA(record_done(p, st));
     }
     return TSB_OK;
 }
@@ -1973,7 +2006,7 @@ int tsb_pass_download_async(tsb_pass* p, int which, void* host, size_t bytes) {
     if (rc) return rc;
     if (bytes < b) return fail(TSB_ERR_INVALID, "tsb_pass_download_async: host buffer too small");
     TSB_CUDA(cudaMemcpyAsync(host, d, b, cudaMemcpyDeviceToHost, p->stream));
-    TSB_CUDA(cudaEventRecord(p->done_ev, p->stream));
+    TSB_CUDA(record_done(p, p->stream));
     if (p->pending) p->pend_dl.push_back({which, host, bytes});
     return TSB_OK;
 }
@@ -2083,7 +2116,7 @@ int enqueue_backward(tsb_pass* p, const UpK& up) {
     p->ctx->launches += 3;
     TSB_CHECK_LAUNCH();
     TSB_CUDA(cudaEventRecord(s->grads_ev, st));
-    TSB_CUDA(cudaEventRecord(p->done_ev, st));
+    TSB_CUDA(record_done(p, st));
     p->pend_bwd = true;
     p->pend_up = up;
     return TSB_OK;
