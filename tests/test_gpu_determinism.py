@@ -90,3 +90,38 @@ def test_deterministic_mode_with_recomposited_pixels(tsb, ctx):
     scene = gpu_scene(tsb, ctx, g, cfg.tof)
     rp = tsb.RenderPass(ctx).prepare(scene, cfg.camera, det, (0, 0.3)).forward()
     assert rp.debug_fixups() > 0
+
+
+def test_upload_to_one_scene_while_another_renders(tsb, ctx):
+    """tsb_scene_set_params waits only for the frames reading its own scene: uploading scene
+    B while frames of scene A are still queued leaves A's frames intact, and B's frames see
+    B's new parameters (each compared with a synchronous render of the same frame)."""
+    from paper_2505_05356_b200 import synthetic
+    cfg = synthetic.config("c1", n=30_000)
+    ga, gb = synthetic.gaussians(30_000, 3, n_keyframes=2), synthetic.gaussians(30_000, 4, n_keyframes=2)
+    sa, sb = gpu_scene(tsb, ctx, ga, cfg.tof), gpu_scene(tsb, ctx, ga, cfg.tof)
+    cam, opts = cfg.camera, tsb.RenderOptions()
+    H, W = cam.height, cam.width
+    frames = [(0, 0.1 * i) for i in range(6)]
+    rps = [tsb.RenderPass(ctx) for _ in range(4)]
+    bufs = [np.zeros(4 * H * W, np.float32) for _ in range(12)]
+    for i, fr in enumerate(frames):  # scene A, queued
+        rp = rps[i % 4]
+        rp.prepare(sa, cam, opts, fr).forward()
+        rp.download_async(tsb._abi.OUT_QUAD, bufs[i])
+        if i == 3:  # scene B's upload while A's frames are in flight
+            sb.set_params(gb.position, gb.log_scale, gb.rotation, gb.opacity_logit, gb.reflectivity_dc, gb.motion)
+    for i, fr in enumerate(frames):  # scene B
+        rp = rps[(i + 2) % 4]
+        rp.prepare(sb, cam, opts, fr).forward()
+        rp.download_async(tsb._abi.OUT_QUAD, bufs[6 + i])
+    for rp in rps:
+        rp.wait()
+    ref = tsb.RenderPass(ctx)
+    for k, (sc, base) in enumerate(((sa, 0), (sb, 6))):
+        for i, fr in enumerate(frames):
+            ref.prepare(sc, cam, opts, fr).forward()
+            want = ref.download(tsb._abi.OUT_QUAD)
+            assert np.array_equal(bufs[base + i], want), (k, i)
+    # and B really holds gb (not A's parameters)
+    assert np.array_equal(sb.get_params()["position"], gb.position.astype(np.float32))
