@@ -1166,13 +1166,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_wsf(GemmArgs g, int kR
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
 }
 
-// out[i] (+)= sum_s part[s * stride + i]
-__global__ void k_reduce_slices(const float* __restrict__ part, int slices, int64_t stride, int64_t n,
-                                float* __restrict__ out, int accumulate) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+// out[i] (+)= sum_s part[s * stride + i], in fp64 in a fixed order (deterministic).  A block
+// takes 32 consecutive outputs (coalesced 128-byte rows of each slice) x 8 slice groups; the
+// 8 group partials are added in group order.
+__global__ void __launch_bounds__(256) k_reduce_slices(const float* __restrict__ part, int slices, int64_t stride,
+                                                       int64_t n, float* __restrict__ out, int accumulate) {
+    __shared__ double red[8][33];
+    const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+    for (int64_t i0 = (int64_t)blockIdx.x * 32; i0 < n; i0 += (int64_t)gridDim.x * 32) {
+        const int64_t i = i0 + lane;
         double s = 0.0;
-        for (int k = 0; k < slices; ++k) s += part[k * stride + i];
-        out[i] = accumulate ? out[i] + (float)s : (float)s;
+        if (i < n)
+            for (int k = grp; k < slices; k += 8) s += part[k * stride + i];
+        red[grp][lane] = s;
+        __syncthreads();
+        if (grp == 0 && i < n) {
+            double t = 0.0;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) t += red[g][lane];
+            out[i] = accumulate ? out[i] + (float)t : (float)t;
+        }
+        __syncthreads();
     }
 }
 
@@ -1274,7 +1288,7 @@ int launch_gemm_tf32x3(const GemmArgs& g, int slices, cudaStream_t st) {
 void launch_reduce_slices(const float* part, int slices, int64_t stride, int64_t n, float* out, bool accumulate,
                           cudaStream_t st) {
     if (n <= 0) return;
-    const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    const int grid = (int)std::min<int64_t>((n + 31) / 32, 148 * 8);
     k_reduce_slices<<<grid, 256, 0, st>>>(part, slices, stride, n, out, accumulate ? 1 : 0);
 }
 
