@@ -143,11 +143,23 @@ __device__ __forceinline__ int lean_visible(const SceneK& S, const CamK& C, cons
     return (bx > 0.f && ax > 0.f && by > 0.f && ay > 0.f) ? 1 : 0;
 }
 
+// The exact fp64 decision for the rare undecided Gaussians, out of line: inlined, its
+// registers made the lean path spill (7 local-memory accesses per Gaussian at 40 registers).
+// (The kernel's parameter structs are __grid_constant__, so passing them by reference does
+// not copy them to the stack.)
+// Returns the depth of a visible Gaussian, -1 for a culled one (by value: no stack slot).
+__device__ __noinline__ double lean_exact(const SceneK& S, const CamK& C, const OptK& O, const FrameK& F, int gi) {
+    Prep64 s;
+    return prep64<false>(S, C, O, F, gi, s) ? s.depth : -1.0;
+}
+
 // LEAN (prefix-sorted frames): only the sort key, tiles touched and the visible
 // count / key range; the records of the Gaussians the frame reads -- its sorted
 // prefix -- are written after the sort by k_records.
 template <bool LEAN>
-__global__ void __launch_bounds__(256, LEAN ? TSB_PRE_CTAS : 5) k_preprocess(SceneK S, CamK C, OptK O, const FrameDev* __restrict__ fd,
+__global__ void __launch_bounds__(256, LEAN ? TSB_PRE_CTAS : 5) k_preprocess(const __grid_constant__ SceneK S,
+                                                    const __grid_constant__ CamK C,
+                                                    const __grid_constant__ OptK O, const FrameDev* __restrict__ fd,
                                                     uint32_t* __restrict__ depth_key,
                                                     double* __restrict__ depth64,
                                                     uint32_t* __restrict__ gidx,
@@ -164,9 +176,8 @@ __global__ void __launch_bounds__(256, LEAN ? TSB_PRE_CTAS : 5) k_preprocess(Sce
         double depth = 0.0;
         int v = lean_visible(S, C, O, F, gi, depth);
         if (v == 2) {
-            Prep64 s;
-            v = prep64<false>(S, C, O, F, gi, s) ? 1 : 0;
-            depth = s.depth;
+            depth = lean_exact(S, C, O, F, gi);
+            v = depth >= 0.0 ? 1 : 0;
         }
         vis = v == 1;
         if (vis) {
