@@ -473,6 +473,101 @@ __global__ void __launch_bounds__(kSortThreads) k_prefix_compact(const uint32_t*
     }
 }
 
+// A selection that fits one tile (the common prefix cap): all three 8-bit LSD passes in one
+// CTA, in shared memory -- the same stable in-tile ranking as k_onesweep, with the tile's own
+// digit scan as the offsets (no histograms, look-back or global round trips between passes;
+// one launch instead of k_sort_scan + 3 x k_onesweep).
+__global__ void __launch_bounds__(kSortThreads) k_sort_small(const uint32_t* __restrict__ keys_in,
+                                                           const uint32_t* __restrict__ vals_in,
+                                                           uint32_t* __restrict__ keys_out,
+                                                           uint32_t* __restrict__ vals_out,
+                                                           const uint32_t* __restrict__ range,
+                                                           const int32_t* __restrict__ n_dev) {
+    __shared__ uint32_t warp_cnt[kSortWarps][256];
+    __shared__ uint32_t block_start[256];
+    __shared__ uint32_t s_keys[kSortTile];
+    __shared__ uint32_t s_vals[kSortTile];
+    __shared__ uint32_t s_wsum[kSortWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = min(*n_dev, kSortTile);
+    uint32_t kmin, kshift;
+    key_xform(range, kmin, kshift);
+    uint32_t k[kSortIPT], v[kSortIPT], lr[kSortIPT];
+#pragma unroll
+    for (int i = 0; i < kSortIPT; ++i) {
+        const int idx = warp * 32 * kSortIPT + i * 32 + lane;
+        const bool valid = idx < n;
+        k[i] = valid ? key24(keys_in[idx], kmin, kshift) : 0u;
+        v[i] = valid ? vals_in[idx] : 0u;
+    }
+    const unsigned lt_mask = (1u << lane) - 1u;
+#pragma unroll 1
+    for (int shift = 0; shift < 24; shift += 8) {
+        for (int i = tid; i < kSortWarps * 256; i += kSortThreads) (&warp_cnt[0][0])[i] = 0u;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kSortIPT; ++i) {
+            const int idx = warp * 32 * kSortIPT + i * 32 + lane;
+            const bool valid = idx < n;
+            const uint32_t d = (k[i] >> shift) & 255u;
+            const unsigned peers = peers8(d, valid);
+            uint32_t cur = 0;
+            lr[i] = 0xffffffffu;
+            if (valid) {
+                cur = warp_cnt[warp][d];
+                lr[i] = cur + (uint32_t)__popc(peers & lt_mask);
+            }
+            __syncwarp();
+            if (valid && (peers & lt_mask) == 0u) warp_cnt[warp][d] = cur + (uint32_t)__popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        {  // per digit (thread d): exclusive offsets across warps, then the block scan
+            const int d = tid;
+            uint32_t total = 0;
+#pragma unroll
+            for (int w = 0; w < kSortWarps; ++w) {
+                const uint32_t c = warp_cnt[w][d];
+                warp_cnt[w][d] = total;
+                total += c;
+            }
+            uint32_t inc = total;
+            for (int s2 = 1; s2 < 32; s2 <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xffffffffu, inc, s2);
+                if (lane >= s2) inc += u;
+            }
+            if (lane == 31) s_wsum[warp] = inc;
+            __syncthreads();
+            uint32_t woff = 0;
+            for (int w = 0; w < warp; ++w) woff += s_wsum[w];
+            block_start[d] = woff + inc - total;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kSortIPT; ++i) {
+            if (lr[i] == 0xffffffffu) continue;
+            const uint32_t dd = (k[i] >> shift) & 255u;
+            const uint32_t pos = block_start[dd] + warp_cnt[warp][dd] + lr[i];
+            s_keys[pos] = k[i];
+            s_vals[pos] = v[i];
+        }
+        __syncthreads();
+        if (shift < 16) {  // the next pass reads the tile in its new order
+#pragma unroll
+            for (int i = 0; i < kSortIPT; ++i) {
+                const int idx = warp * 32 * kSortIPT + i * 32 + lane;
+                k[i] = idx < n ? s_keys[idx] : 0u;
+                v[i] = idx < n ? s_vals[idx] : 0u;
+            }
+            __syncthreads();  // (s_wsum / warp_cnt / the tile are rewritten by the next pass)
+        }
+    }
+    for (int j = tid; j < n; j += kSortThreads) {
+        keys_out[j] = s_keys[j];
+        vals_out[j] = s_vals[j];
+    }
+}
+
 size_t prefix_sort_scratch_words(int cap) {
     const int tiles = (cap + kSortTile - 1) / kSortTile;
     return (size_t)kPrefStatus + (size_t)3 * 256 * tiles;
@@ -489,6 +584,10 @@ int radix_sort24_prefix(const uint32_t* keys, uint32_t* keys_out, uint32_t* vals
     k_sort_hist<true><<<hgrid, kSortThreads, 0, st>>>(keys, n, hist, nullptr, 0, range);
     k_prefix_select<<<1, 32, 0, st>>>(hist, n, cap, n_visible, ps, n_bin, abort_word);
     k_prefix_compact<<<hgrid, kSortThreads, 0, st>>>(keys, n, range, ps, 3 * 256 * ctiles, tmp_keys, tmp_vals);
+    if (ctiles == 1) {  // the whole selection in one tile: one kernel, three passes in shared memory
+        k_sort_small<<<1, kSortThreads, 0, st>>>(tmp_keys, tmp_vals, keys_out, vals_out, range, n_bin);
+        return 4;
+    }
     uint32_t* hc = ps + kPrefHistC;
     uint32_t* tk = ps + kPrefTickets;
     uint32_t* status = ps + kPrefStatus;
